@@ -1,0 +1,193 @@
+/*
+ * lcn_b200.h — C-ABI of the B200-native LCN-Sinkhorn hot path.
+ *
+ * The drop-in boundary for the reference's solver API:
+ * every entry point takes plain pointers and sizes, never throws, and returns
+ * an lcn_status; lcn_ctx_last_error() holds the message, whose text matches
+ * the reference exception's what() so a C++ shim can rethrow the same
+ * lcn::Error subtype (error.hpp:8-38) with the same message.
+ *
+ * Handles are re-entrant per handle (SURVEY.md §8(b) "Threading"): each
+ * lcn_ctx owns one device, one stream and its buffers; cudaSetDevice is
+ * applied on every entry. There is no global mutable state.
+ *
+ * Host pointers are row-major fp64 like the reference's PointSet /
+ * DenseMatrix (geometry.hpp:14-29, matrix.hpp:10-24). The *_device entry
+ * points take device-resident fp32 points (the synthetic configs are fp32,
+ * promoted exactly) for timing runs.
+ *
+ * Each declaration names the reference interface it replaces (file:line,
+ * relative to /root/reference/proj).
+ */
+#ifndef LCN_B200_H
+#define LCN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LCN_B200_ABI_VERSION 1
+
+typedef struct lcn_ctx lcn_ctx;
+typedef struct lcn_op lcn_op;
+typedef struct lcn_result lcn_result;
+
+/* Status codes: 1..6 mirror the lcn::Error subtypes (error.hpp:8-38). */
+enum lcn_status {
+    LCN_OK = 0,
+    LCN_E_DIMENSION = 1,         /* DimensionError */
+    LCN_E_INVALID_ARGUMENT = 2,  /* InvalidArgument */
+    LCN_E_STABILIZATION = 3,     /* StabilizationError */
+    LCN_E_NEGATIVE_KERNEL = 4,   /* NegativeKernelError */
+    LCN_E_FACTORIZATION = 5,     /* FactorizationError */
+    LCN_E_ERROR = 6,             /* lcn::Error */
+    LCN_E_CUDA = 100,            /* CUDA runtime failure */
+    LCN_E_NO_DEVICE = 101        /* no usable sm_100 device */
+};
+
+/* CostKind (geometry.hpp:35-39) plus the documented squared-L2 extension. */
+enum lcn_cost { LCN_COST_EUCLIDEAN = 0, LCN_COST_NEGATIVE_DOT = 1, LCN_COST_COSINE_DERIVED = 2, LCN_COST_SQEUCLIDEAN = 3 };
+
+/* LandmarkMethod (nystrom.hpp:14-17). */
+enum lcn_landmark_method { LCN_LANDMARK_KMEANS = 0, LCN_LANDMARK_KMEANSPP = 1 };
+
+/* Operator kinds (operator.hpp:33 KernelOperator::Kind). */
+enum lcn_op_kind { LCN_OP_DENSE = 0, LCN_OP_SPARSE = 1, LCN_OP_NYSTROM = 2, LCN_OP_LCN = 3 };
+
+/* Context flags: value storage of the iteration operands. FP64 keeps every
+ * stored kernel value in fp64 (API-compatibility mode, passes the reference
+ * unit tests' 1e-12 tolerances); FP32 stores them in fp32 with fp64
+ * accumulation (performance mode, 1e-4 parity). */
+enum lcn_ctx_flags { LCN_STORE_FP32 = 0, LCN_STORE_FP64 = 1 };
+
+/* LshConfig (lsh.hpp:22-30), k-means scheme. rows_per_band must be 1 for the
+ * k-means scheme on this path (the reference only warns, lsh.cpp:256-260). */
+typedef struct {
+    int bands;
+    int rows_per_band;
+    int buckets_per_fn;
+    int kmeans_iters;
+    uint64_t seed;
+} lcn_lsh_config;
+
+/* SinkhornOptions (sinkhorn.hpp:11-20). tol < 0 selects 1e-6 (sum p + sum q). */
+typedef struct {
+    double tol;
+    int max_iters;
+    int check_support;
+    int want_plan;
+} lcn_sinkhorn_options;
+
+typedef struct {
+    int kind;                 /* lcn_op_kind */
+    size_t n, m, l, d;
+    int bands;
+    size_t nnz;               /* deduplicated support size (= pairs.size()) */
+    size_t stored;            /* bucket-block entries held in HBM (>= nnz) */
+    double lambda;
+    double max_abs_delta;     /* LcnCorrection::max_abs_delta (sparse_kernel.hpp:46) */
+    double cond_estimate;     /* NystromFactors::cond_estimate (nystrom.hpp:37) */
+    int store_fp64;
+} lcn_op_info_t;
+
+typedef struct {
+    double distance;
+    int iters;
+    int converged;
+    double marginal_err_final;
+    int n_warnings;
+    double device_ms;         /* CUDA-event time of the iteration loop */
+} lcn_result_info_t;
+
+/* ---- context ---------------------------------------------------------- */
+int lcn_ctx_create(int device, int flags, lcn_ctx** out);
+int lcn_ctx_destroy(lcn_ctx* ctx);
+const char* lcn_ctx_last_error(const lcn_ctx* ctx);
+const char* lcn_status_name(int status);
+int lcn_abi_version(void);
+
+/* ---- k-means (kmeans.hpp:18-29) --------------------------------------- */
+/* kmeans_pp_indices (kmeans.cpp:23-65). The caller's std::mt19937_64 supplies
+ * first_index = uniform_int_distribution<size_t>(0,n-1)(rng) and then up to
+ * k-1 raw 64-bit draws; *draws_used reports how many the reference would have
+ * consumed (a step with total <= 0 consumes none, kmeans.cpp:42-47), so the
+ * shim can advance its engine identically. */
+int lcn_kmeans_pp_indices(lcn_ctx* ctx, const double* points, size_t n, size_t d, size_t k,
+                          uint64_t first_index, const uint64_t* raw_draws, size_t n_draws,
+                          uint32_t* out, size_t* draws_used);
+/* assign_nearest (kmeans.cpp:67-85): ties to the lowest index. */
+int lcn_assign_nearest(lcn_ctx* ctx, const double* points, size_t n, size_t d,
+                       const double* centroids, size_t k, uint32_t* out);
+/* lloyd (kmeans.cpp:87-143), mt19937_64(seed) k-means++ init. */
+int lcn_lloyd(lcn_ctx* ctx, const double* points, size_t n, size_t d, size_t k, int iters,
+              uint64_t seed, double* centroids_out, uint32_t* assign_out);
+
+/* ---- LSH (lsh.hpp:49-68) ---------------------------------------------- */
+/* Bucket ids of lsh_neighbor_pairs' k-means scheme (lsh.cpp:245-283):
+ * ids_out is bands x (n+m), band b = hash_kmeans(X_p ∪ X_q, fn_seed(seed,b,0)). */
+int lcn_lsh_kmeans_buckets(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m,
+                           size_t d, const lcn_lsh_config* cfg, uint64_t* ids_out);
+
+/* ---- operators (operator.hpp:29-82) ----------------------------------- */
+/* Sparse operator on the k-means LSH support: lsh_neighbor_pairs
+ * (lsh.cpp:245) -> build_sparse (sparse_kernel.cpp:51) -> KernelOperator::sparse
+ * (operator.cpp:67). */
+int lcn_op_sparse_lsh(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m, size_t d,
+                      int cost, double lambda, const lcn_lsh_config* cfg, lcn_op** out);
+/* Same from external bucket ids (neighbor_pairs(BandBuckets...), lsh.cpp:212):
+ * ids_p is bands x n, ids_q bands x m, values < range. */
+int lcn_op_sparse_buckets(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m, size_t d,
+                          int cost, double lambda, const uint64_t* ids_p, const uint64_t* ids_q,
+                          int bands, uint64_t range, lcn_op** out);
+/* LCN operator: LSH support + select_landmarks (nystrom.cpp:28) +
+ * build_factors (nystrom.cpp:68) + build_correction (sparse_kernel.cpp:82) +
+ * KernelOperator::lcn (operator.cpp:90). */
+int lcn_op_lcn_lsh(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m, size_t d,
+                   int cost, double lambda, const lcn_lsh_config* cfg, size_t l, int landmark_method,
+                   uint64_t landmark_seed, lcn_op** out);
+/* Same from external bucket ids and (optionally) explicit landmarks (l x d);
+ * landmarks == NULL selects them with select_landmarks(l, method, seed).
+ * bands == 0 builds a pure Nystrom operator (KernelOperator::nystrom). */
+int lcn_op_lcn_buckets(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m, size_t d,
+                       int cost, double lambda, const uint64_t* ids_p, const uint64_t* ids_q, int bands,
+                       uint64_t range, const double* landmarks, size_t l, int landmark_method,
+                       uint64_t landmark_seed, lcn_op** out);
+/* Device-resident variant for timing runs: d_p (n x d) and d_q (m x d) are
+ * fp32 device pointers. landmarks <= 0 builds the sparse operator. */
+int lcn_op_create_device(lcn_ctx* ctx, const float* d_p, size_t n, const float* d_q, size_t m, size_t d,
+                         int cost, double lambda, const lcn_lsh_config* cfg, size_t l, int landmark_method,
+                         uint64_t landmark_seed, lcn_op** out);
+int lcn_op_destroy(lcn_op* op);
+int lcn_op_get_info(const lcn_op* op, lcn_op_info_t* info);
+/* CSR export in the reference's order (rows ascending, columns ascending,
+ * sparse_kernel.hpp:19-21). which: 0 log K^sp (SparseKernel::logvals),
+ * 1 delta, 2 log_sp, 3 nys_vals (LcnCorrection, sparse_kernel.hpp:43-45).
+ * row_ptr has n+1 entries; col/vals nnz (lcn_op_get_info). Any may be NULL. */
+int lcn_op_export_csr(lcn_op* op, int which, uint32_t* row_ptr, uint32_t* col, double* vals);
+/* Dense factor export: 0 U (n x l), 1 W (l x m), 2 landmarks (l x d). */
+int lcn_op_export_factor(lcn_op* op, int which, double* out);
+/* log_matvec / log_matvec_t (operator.cpp:226-252), host vectors. */
+int lcn_op_log_matvec(lcn_op* op, const double* in, int transposed, double* out);
+
+/* ---- solver (sinkhorn.hpp:68-121) ------------------------------------- */
+/* sinkhorn (sinkhorn.cpp:104-188). p (n), q (m) host marginals. */
+int lcn_sinkhorn(lcn_op* op, const double* p, const double* q, const lcn_sinkhorn_options* opts,
+                 lcn_result** out);
+int lcn_result_destroy(lcn_result* res);
+int lcn_result_get_info(const lcn_result* res, lcn_result_info_t* info);
+/* which: 0 log_s (n), 1 log_t (m), 2 row_marginal (n), 3 marginal_err trace,
+ * 4 sparse plan values (Plan::sparse_vals, CSR order), 5 lcn sp_vals,
+ * 6 lcn sp_nys_vals. out == NULL returns the length in *len only. */
+int lcn_result_copy(const lcn_result* res, int which, double* out, size_t* len);
+/* distance_lcn (sinkhorn.cpp:222-261). */
+int lcn_distance_lcn(const lcn_result* res, const lcn_op* op, double* out);
+/* Warning text i (SinkhornResult::warnings, sinkhorn.cpp:122-128). */
+const char* lcn_result_warning(const lcn_result* res, int i);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LCN_B200_H */

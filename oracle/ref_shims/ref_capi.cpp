@@ -1,0 +1,383 @@
+// ORACLE TEST INFRASTRUCTURE — never linked into the product.
+//
+// extern "C" wrappers over the *compiled reference* (/root/reference/proj/src,
+// built unmodified by oracle/Makefile into oracle/_ref/libref_lcn.so) so that
+// tests/ and bench.py's reference arm can drive it through ctypes. Every
+// wrapper forwards to the reference function named in its comment; no
+// algorithmic code lives here except mix64/fn_seed, which restate the
+// file-local helpers at lsh.cpp:17-27 so bucket ids per band can be exported
+// (lsh_neighbor_pairs itself only returns pairs).
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "lcn/error.hpp"
+#include "lcn/generators.hpp"
+#include "lcn/geometry.hpp"
+#include "lcn/kmeans.hpp"
+#include "lcn/lsh.hpp"
+#include "lcn/nystrom.hpp"
+#include "lcn/operator.hpp"
+#include "lcn/reference.hpp"
+#include "lcn/sinkhorn.hpp"
+#include "lcn/sparse_kernel.hpp"
+
+using namespace lcn;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(const std::exception& e) {
+    g_err = e.what();
+    if (dynamic_cast<const DimensionError*>(&e)) return 1;
+    if (dynamic_cast<const InvalidArgument*>(&e)) return 2;
+    if (dynamic_cast<const StabilizationError*>(&e)) return 3;
+    if (dynamic_cast<const NegativeKernelError*>(&e)) return 4;
+    if (dynamic_cast<const FactorizationError*>(&e)) return 5;
+    if (dynamic_cast<const Error*>(&e)) return 6;
+    return 9;
+}
+
+#define GUARD(...)                           \
+    try {                                    \
+        __VA_ARGS__;                         \
+        return 0;                            \
+    } catch (const std::exception& e) {      \
+        return fail(e);                      \
+    }
+
+PointSet make_points(const double* x, std::size_t n, std::size_t d, const char* id) {
+    PointSet ps(n, d, id);
+    if (n * d) std::memcpy(ps.coords.data(), x, n * d * sizeof(double));
+    return ps;
+}
+
+// lsh.cpp:17-27 (file-local in the reference).
+std::uint64_t mix64(std::uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+std::uint64_t fn_seed(std::uint64_t seed, int band, int fn) {
+    return mix64(seed ^ mix64(static_cast<std::uint64_t>(band) * 0x100000001b3ull +
+                              static_cast<std::uint64_t>(fn)));
+}
+
+LshConfig kmeans_cfg(int bands, int buckets, int iters, std::uint64_t seed) {
+    LshConfig cfg;
+    cfg.scheme = LshScheme::KMeans;
+    cfg.bands = bands;
+    cfg.rows_per_band = 1;
+    cfg.buckets_per_fn = buckets;
+    cfg.kmeans_iters = iters;
+    cfg.seed = seed;
+    return cfg;
+}
+
+struct RefOp {
+    KernelOperator op;
+    std::shared_ptr<SparseKernel> sparse;
+    std::shared_ptr<NystromFactors> factors;
+    std::shared_ptr<LcnCorrection> corr;
+    std::vector<double> landmarks;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// generators.cpp:28-42
+int ref_sample_uniform_ball(std::size_t n, std::size_t d, std::uint64_t seed, double* out) {
+    GUARD({
+        PointSet ps = sample_uniform_ball(n, d, seed, "ball");
+        std::memcpy(out, ps.coords.data(), n * d * sizeof(double));
+    })
+}
+
+// kmeans.cpp:23-65 with a fresh mt19937_64(seed)
+int ref_kmeans_pp(const double* pts, std::size_t n, std::size_t d, std::size_t k, std::uint64_t seed,
+                  std::uint32_t* out) {
+    GUARD({
+        std::mt19937_64 rng(seed);
+        auto idx = kmeans_pp_indices(pts, n, d, k, rng);
+        std::memcpy(out, idx.data(), k * sizeof(std::uint32_t));
+    })
+}
+
+// kmeans.cpp:67-85
+int ref_assign_nearest(const double* pts, std::size_t n, std::size_t d, const double* ctr, std::size_t k,
+                       std::uint32_t* out) {
+    GUARD({
+        DenseMatrix c(k, d);
+        std::memcpy(c.data.data(), ctr, k * d * sizeof(double));
+        assign_nearest(pts, n, d, c, out);
+    })
+}
+
+// kmeans.cpp:87-143
+int ref_lloyd(const double* pts, std::size_t n, std::size_t d, std::size_t k, int iters, std::uint64_t seed,
+              double* centroids, std::uint32_t* assign) {
+    GUARD({
+        KmeansResult r = lloyd(pts, n, d, k, iters, seed);
+        std::memcpy(centroids, r.centroids.data.data(), k * d * sizeof(double));
+        std::memcpy(assign, r.assign.data(), n * sizeof(std::uint32_t));
+    })
+}
+
+// Bucket ids per band of the k-means LSH on X_p ∪ X_q, exactly as
+// lsh_neighbor_pairs computes them (lsh.cpp:245-283): band b clusters the
+// union with hash_kmeans(seed = fn_seed(cfg.seed, b, 0)). ids: bands x (n+m).
+int ref_lsh_kmeans_buckets(const double* p, std::size_t n, const double* q, std::size_t m, std::size_t d,
+                           int bands, int buckets, int iters, std::uint64_t seed, std::uint64_t* ids) {
+    GUARD({
+        PointSet all = union_points(make_points(p, n, d, "p"), make_points(q, m, d, "q"));
+        for (int b = 0; b < bands; ++b) {
+            LshConfig sub = kmeans_cfg(bands, buckets, iters, fn_seed(seed, b, 0));
+            auto a = hash_kmeans(all, sub);
+            for (std::size_t i = 0; i < n + m; ++i) ids[static_cast<std::size_t>(b) * (n + m) + i] = a[i];
+        }
+    })
+}
+
+// lsh.cpp:245-283 end to end; returns a NeighborPairs*.
+int ref_lsh_pairs(const double* p, std::size_t n, const double* q, std::size_t m, std::size_t d, int bands,
+                  int buckets, int iters, std::uint64_t seed, void** out) {
+    GUARD({
+        auto np = std::make_unique<NeighborPairs>(lsh_neighbor_pairs(
+            make_points(p, n, d, "p"), make_points(q, m, d, "q"), kmeans_cfg(bands, buckets, iters, seed)));
+        *out = np.release();
+    })
+}
+
+// lsh.cpp:212-243 from external bucket ids (ids_p: bands x n, ids_q: bands x m).
+int ref_pairs_from_buckets(const std::uint64_t* ids_p, std::size_t n, const std::uint64_t* ids_q, std::size_t m,
+                           int bands, std::uint64_t range, void** out) {
+    GUARD({
+        BandBuckets bp, bq;
+        bp.composite_range = bq.composite_range = range;
+        for (int b = 0; b < bands; ++b) {
+            bp.bucket.emplace_back(ids_p + static_cast<std::size_t>(b) * n, ids_p + (static_cast<std::size_t>(b) + 1) * n);
+            bq.bucket.emplace_back(ids_q + static_cast<std::size_t>(b) * m, ids_q + (static_cast<std::size_t>(b) + 1) * m);
+        }
+        *out = new NeighborPairs(neighbor_pairs(bp, bq, LshConfig{}));
+    })
+}
+
+// NeighborPairs::from_pairs (lsh.cpp:163-177)
+int ref_pairs_from_arrays(std::size_t n, std::size_t m, const std::uint32_t* rows, const std::uint32_t* cols,
+                          std::size_t count, void** out) {
+    GUARD({
+        std::vector<std::pair<std::uint32_t, std::uint32_t>> raw(count);
+        for (std::size_t e = 0; e < count; ++e) raw[e] = {rows[e], cols[e]};
+        *out = new NeighborPairs(NeighborPairs::from_pairs(n, m, std::move(raw)));
+    })
+}
+
+std::size_t ref_pairs_nnz(void* h) { return static_cast<NeighborPairs*>(h)->pairs.size(); }
+void ref_pairs_copy(void* h, std::uint32_t* rows, std::uint32_t* cols) {
+    auto* np = static_cast<NeighborPairs*>(h);
+    for (std::size_t e = 0; e < np->pairs.size(); ++e) {
+        rows[e] = np->pairs[e].first;
+        cols[e] = np->pairs[e].second;
+    }
+}
+void ref_pairs_free(void* h) { delete static_cast<NeighborPairs*>(h); }
+
+// sparse_kernel.cpp:51-80 + operator.cpp:67-78
+int ref_op_sparse(const double* p, std::size_t n, const double* q, std::size_t m, std::size_t d, int kind,
+                  double lambda, void* pairs, void** out) {
+    GUARD({
+        auto* r = new RefOp{KernelOperator::sparse(
+            build_sparse(make_points(p, n, d, "p"), make_points(q, m, d, "q"),
+                         *static_cast<NeighborPairs*>(pairs), static_cast<CostKind>(kind), lambda),
+            lambda)};
+        *out = r;
+    })
+}
+
+// nystrom.cpp:28-125 (restated, oracle/ref_shims/nystrom_restated.cpp) +
+// sparse_kernel.cpp:82-117 + operator.cpp:90-101. landmarks == nullptr selects
+// them with select_landmarks(l, method, lm_seed); otherwise uses the given l x d rows.
+int ref_op_lcn(const double* p, std::size_t n, const double* q, std::size_t m, std::size_t d, int kind,
+               double lambda, void* pairs, std::size_t l, int method, std::uint64_t lm_seed,
+               const double* landmarks, int nystrom_only, void** out) {
+    GUARD({
+        PointSet P = make_points(p, n, d, "p"), Q = make_points(q, m, d, "q");
+        LandmarkSet lm;
+        if (landmarks) {
+            lm.points = make_points(landmarks, l, d, "landmarks");
+        } else {
+            lm = select_landmarks(P, Q, l, static_cast<LandmarkMethod>(method), lm_seed);
+        }
+        NystromFactors f = build_factors(P, Q, lm, static_cast<CostKind>(kind), lambda);
+        auto* r = new RefOp{KernelOperator::nystrom(f)};
+        r->landmarks = lm.points.coords;
+        if (!nystrom_only) {
+            SparseKernel sk = build_sparse(P, Q, *static_cast<NeighborPairs*>(pairs), static_cast<CostKind>(kind), lambda);
+            LcnCorrection c = build_correction(sk, f);
+            r->op = KernelOperator::lcn(f, c);
+        }
+        *out = r;
+    })
+}
+
+// geometry.cpp:113-144 + operator.cpp:55-65
+int ref_op_dense(const double* p, std::size_t n, const double* q, std::size_t m, std::size_t d, int kind,
+                 double lambda, void** out) {
+    GUARD({
+        *out = new RefOp{KernelOperator::dense(
+            build_kernel(build_cost(make_points(p, n, d, "p"), make_points(q, m, d, "q"),
+                                    static_cast<CostKind>(kind), lambda)),
+            lambda)};
+    })
+}
+
+void ref_op_free(void* h) { delete static_cast<RefOp*>(h); }
+
+// Accessors. which: 0 sparse CSR (row_ptr n+1, col nnz, vals = logvals nnz);
+// 1 lcn correction (row_ptr, col, vals = delta); 2 U (n x l); 3 W (l x m);
+// 4 landmarks (l x d); 5 lcn nys_vals; 6 lcn log_sp.
+std::size_t ref_op_nnz(void* h) {
+    auto* r = static_cast<RefOp*>(h);
+    if (r->op.sparse_kernel()) return r->op.sparse_kernel()->nnz();
+    if (r->op.correction()) return r->op.correction()->col.size();
+    return 0;
+}
+std::size_t ref_op_rank(void* h) {
+    auto* r = static_cast<RefOp*>(h);
+    return r->op.factors() ? r->op.factors()->l : 0;
+}
+double ref_op_scalar(void* h, int which) {
+    auto* r = static_cast<RefOp*>(h);
+    if (which == 0) return r->op.correction() ? r->op.correction()->max_abs_delta : 0.0;
+    if (which == 1) return r->op.factors() ? r->op.factors()->cond_estimate : 0.0;
+    return 0.0;
+}
+int ref_op_copy(void* h, int which, std::uint32_t* row_ptr, std::uint32_t* col, double* vals) {
+    auto* r = static_cast<RefOp*>(h);
+    if (which == 0 && r->op.sparse_kernel()) {
+        const SparseKernel& s = *r->op.sparse_kernel();
+        if (row_ptr) std::memcpy(row_ptr, s.row_ptr.data(), s.row_ptr.size() * 4);
+        if (col) std::memcpy(col, s.col.data(), s.col.size() * 4);
+        if (vals) std::memcpy(vals, s.logvals.data(), s.logvals.size() * 8);
+        return 0;
+    }
+    if ((which == 1 || which == 5 || which == 6) && r->op.correction()) {
+        const LcnCorrection& c = *r->op.correction();
+        if (row_ptr) std::memcpy(row_ptr, c.row_ptr.data(), c.row_ptr.size() * 4);
+        if (col) std::memcpy(col, c.col.data(), c.col.size() * 4);
+        const std::vector<double>& src = which == 1 ? c.delta : which == 5 ? c.nys_vals : c.log_sp;
+        if (vals) std::memcpy(vals, src.data(), src.size() * 8);
+        return 0;
+    }
+    if (which == 2 && r->op.factors()) {
+        std::memcpy(vals, r->op.factors()->u.data.data(), r->op.factors()->u.data.size() * 8);
+        return 0;
+    }
+    if (which == 3 && r->op.factors()) {
+        std::memcpy(vals, r->op.factors()->w.data.data(), r->op.factors()->w.data.size() * 8);
+        return 0;
+    }
+    if (which == 4) {
+        std::memcpy(vals, r->landmarks.data(), r->landmarks.size() * 8);
+        return 0;
+    }
+    g_err = "ref_op_copy: nothing to copy";
+    return 2;
+}
+
+// operator.cpp:226-252
+int ref_op_log_matvec(void* h, const double* in, std::size_t len, int transposed, double* out) {
+    GUARD({
+        auto* r = static_cast<RefOp*>(h);
+        std::span<const double> v(in, len);
+        std::vector<double> y = transposed ? r->op.log_matvec_t(v) : r->op.log_matvec(v);
+        std::memcpy(out, y.data(), y.size() * 8);
+    })
+}
+
+// sinkhorn.cpp:104-188; returns a SinkhornResult*.
+int ref_sinkhorn(void* h, const double* pm, std::size_t n, const double* qm, std::size_t m, double tol,
+                 int max_iters, int check_support, int want_plan, void** out) {
+    GUARD({
+        auto* r = static_cast<RefOp*>(h);
+        Marginals marg;
+        marg.p.assign(pm, pm + n);
+        marg.q.assign(qm, qm + m);
+        SinkhornOptions o;
+        o.tol = tol;
+        o.max_iters = max_iters;
+        o.check_support = check_support != 0;
+        o.want_plan = want_plan != 0;
+        *out = new SinkhornResult(sinkhorn(r->op, marg, o));
+    })
+}
+
+void ref_result_free(void* h) { delete static_cast<SinkhornResult*>(h); }
+
+// 0 distance, 1 iters, 2 converged, 3 marginal_err_final, 4 #warnings, 5 #err trace
+double ref_result_scalar(void* h, int which) {
+    auto* s = static_cast<SinkhornResult*>(h);
+    switch (which) {
+        case 0: return s->distance;
+        case 1: return s->iters;
+        case 2: return s->converged ? 1.0 : 0.0;
+        case 3: return s->marginal_err_final;
+        case 4: return static_cast<double>(s->warnings.size());
+        case 5: return static_cast<double>(s->state.marginal_err.size());
+    }
+    return 0.0;
+}
+
+// 0 log_s, 1 log_t, 2 row_marginal, 3 marginal_err trace, 4 sparse plan vals,
+// 5 lcn sp_vals, 6 lcn sp_nys_vals, 7 P_U (n x l), 8 P_W (l x m)
+std::size_t ref_result_copy(void* h, int which, double* out) {
+    auto* s = static_cast<SinkhornResult*>(h);
+    const std::vector<double>* v = nullptr;
+    switch (which) {
+        case 0: v = &s->state.log_s; break;
+        case 1: v = &s->state.log_t; break;
+        case 2: v = &s->row_marginal; break;
+        case 3: v = &s->state.marginal_err; break;
+        case 4: v = &s->plan.sparse_vals; break;
+        case 5: v = &s->plan.sp_vals; break;
+        case 6: v = &s->plan.sp_nys_vals; break;
+        case 7: if (s->plan.p_u) v = &s->plan.p_u->data; break;
+        case 8: if (s->plan.p_w) v = &s->plan.p_w->data; break;
+    }
+    if (!v) return 0;
+    if (out) std::memcpy(out, v->data(), v->size() * 8);
+    return v->size();
+}
+
+// sinkhorn.cpp:222-261
+int ref_distance_lcn(void* res, void* op, double* out) {
+    GUARD({
+        auto* s = static_cast<SinkhornResult*>(res);
+        auto* r = static_cast<RefOp*>(op);
+        *out = distance_lcn(s->state, *r->op.factors(), *r->op.correction());
+    })
+}
+
+// reference.cpp:41-105 (independent serial linear-space solver)
+int ref_dense_reference(const double* cost, std::size_t n, std::size_t m, const double* p, const double* q,
+                        double lambda, double tol, int max_iters, double* plan, double* distance, int* iters) {
+    GUARD({
+        ref::Solution sol = ref::solve(std::vector<double>(cost, cost + n * m), n, m,
+                                       std::vector<double>(p, p + n), std::vector<double>(q, q + m), lambda,
+                                       tol, max_iters);
+        if (plan) std::memcpy(plan, sol.plan.data(), n * m * 8);
+        *distance = sol.distance;
+        *iters = sol.iters;
+    })
+}
+
+}  // extern "C"

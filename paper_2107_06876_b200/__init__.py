@@ -1,0 +1,14 @@
+"""B200-native LCN-Sinkhorn hot path (arXiv 2107.06876).
+
+The product is the C-ABI library paper_2107_06876_b200/_build/liblcn_b200.so
+(include/lcn_b200.h): hand-written sm_100a CUDA for k-means LSH bucketing,
+Nystrom landmarks, the bucket-blocked K_sp / LCN correction and the
+log-stabilised Sinkhorn loop. `native` mirrors the reference's lcn:: API over
+it; `configs` holds the seeded BASELINE.json inputs.
+"""
+from . import configs  # noqa: F401
+from .native import (  # noqa: F401
+    COSINE_DERIVED, EUCLIDEAN, LANDMARK_KMEANS, LANDMARK_KMEANSPP, NEGATIVE_DOT, SQEUCLIDEAN, Context, CudaError,
+    DimensionError, Error, FactorizationError, InvalidArgument, KernelOperator, LshConfig, NegativeKernelError,
+    SinkhornOptions, SinkhornResult, StabilizationError, assign_nearest, distance_lcn, kmeans_pp_indices, library,
+    lloyd, lsh_kmeans_buckets, sinkhorn)

@@ -1,0 +1,846 @@
+// Operator construction on the device:
+//   * k-means LSH bucket ids (lsh.cpp:245-283 via lloyd_device);
+//   * the bucket-blocked layout of K_sp: with k-means LSH
+//     every within-bucket (source, target) pair is a neighbour
+//     (lsh.cpp:222-239), so band b's support is the union of dense
+//     n_bucket x m_bucket blocks; pairs already present in an earlier band are
+//     masked (the sort+unique of NeighborPairs::from_pairs, lsh.cpp:163-177);
+//   * K_sp values log K = 0 - c(x_i, y_j) * (1/lambda) (sparse_kernel.cpp:71-77);
+//   * Nystrom factors U, A, V, W = A^-1 V (nystrom.cpp:53-125) with the
+//     long-double factorisation and jitter schedule on the host and the
+//     l x m products on the device;
+//   * the LCN correction delta = exp(log K) - (U W)_ij at the support
+//     (sparse_kernel.cpp:82-117).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <numeric>
+#include <random>
+
+#include "kmeans.cuh"
+#include "op.cuh"
+#include "tiles.cuh"
+
+namespace lcnb {
+
+BandView Op::view(int b) const {
+    const Band& B = bands[b];
+    return {B.src_order.get(), B.tgt_order.get(), B.src_start.get(), B.tgt_start.get(), B.blk_off.get(),
+            B.src_bucket.get(), B.tgt_bucket.get(), B.src_local.get(), B.tgt_local.get()};
+}
+
+BandSet Op::bandset() const {
+    BandSet s{};
+    s.bands = static_cast<int>(bands.size());
+    for (int b = 0; b < s.bands; ++b) {
+        s.src_bucket[b] = bands[b].src_bucket.get();
+        s.tgt_bucket[b] = bands[b].tgt_bucket.get();
+    }
+    return s;
+}
+
+// ---------------------------------------------------------------------------
+// Band layout
+// ---------------------------------------------------------------------------
+namespace {
+
+__global__ void hist_kernel(const uint32_t* __restrict__ ids, long long n, uint32_t* __restrict__ counts) {
+    long long i = blockIdx.x * 256LL + threadIdx.x;
+    if (i < n) atomicAdd(&counts[ids[i]], 1u);
+}
+
+__global__ void iota32_kernel(uint32_t* p, long long n) {
+    long long i = blockIdx.x * 256LL + threadIdx.x;
+    if (i < n) p[i] = static_cast<uint32_t>(i);
+}
+
+__global__ void local_pos_kernel(const uint32_t* __restrict__ order, const uint32_t* __restrict__ ids,
+                                 const uint32_t* __restrict__ start, long long n, uint32_t* __restrict__ local) {
+    long long p = blockIdx.x * 256LL + threadIdx.x;
+    if (p < n) {
+        uint32_t i = order[p];
+        local[i] = static_cast<uint32_t>(p - start[ids[i]]);
+    }
+}
+
+void stable_group(Ctx& ctx, const uint32_t* d_ids, size_t n, size_t nb, DevBuf<uint32_t>& order,
+                  DevBuf<uint32_t>& start, std::vector<uint32_t>& h_start, DevBuf<uint32_t>& local) {
+    cudaStream_t s = ctx.stream;
+    order.resize(std::max<size_t>(n, 1));
+    local.resize(std::max<size_t>(n, 1));
+    start.resize(nb + 1);
+    DevBuf<uint32_t> counts(nb + 1), iota(std::max<size_t>(n, 1)), keys(std::max<size_t>(n, 1));
+    counts.zero(s);
+    if (n) {
+        hist_kernel<<<ceil_div(n, 256), 256, 0, s>>>(d_ids, n, counts.get());
+        iota32_kernel<<<ceil_div(n, 256), 256, 0, s>>>(iota.get(), n);
+    }
+    std::vector<uint32_t> h_counts(nb + 1);
+    counts.download(h_counts.data(), nb, s);
+    ctx.sync();
+    h_start.assign(nb + 1, 0);
+    for (size_t b = 0; b < nb; ++b) h_start[b + 1] = h_start[b] + h_counts[b];
+    start.upload(h_start.data(), nb + 1, s);
+    if (n) {
+        int end_bit = 1;
+        while ((1ull << end_bit) < nb) ++end_bit;
+        size_t tmp = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tmp, d_ids, keys.get(), iota.get(), order.get(), static_cast<int>(n),
+                                        0, end_bit, s);
+        DevBuf<unsigned char> t(tmp);
+        cub::DeviceRadixSort::SortPairs(t.get(), tmp, d_ids, keys.get(), iota.get(), order.get(), static_cast<int>(n),
+                                        0, end_bit, s);
+        local_pos_kernel<<<ceil_div(n, 256), 256, 0, s>>>(order.get(), d_ids, start.get(), n, local.get());
+        LAUNCH_OK("stable_group");
+    }
+    ctx.sync();
+}
+
+}  // namespace
+
+void build_band_layout(Ctx& ctx, Band& B, const uint32_t* d_src_bucket, const uint32_t* d_tgt_bucket, size_t n,
+                       size_t m, size_t nb) {
+    cudaStream_t s = ctx.stream;
+    B.nb = nb;
+    B.src_bucket.resize(std::max<size_t>(n, 1));
+    B.tgt_bucket.resize(std::max<size_t>(m, 1));
+    if (n) CUDA_OK(cudaMemcpyAsync(B.src_bucket.get(), d_src_bucket, n * 4, cudaMemcpyDeviceToDevice, s));
+    if (m) CUDA_OK(cudaMemcpyAsync(B.tgt_bucket.get(), d_tgt_bucket, m * 4, cudaMemcpyDeviceToDevice, s));
+    stable_group(ctx, B.src_bucket.get(), n, nb, B.src_order, B.src_start, B.h_src_start, B.src_local);
+    stable_group(ctx, B.tgt_bucket.get(), m, nb, B.tgt_order, B.tgt_start, B.h_tgt_start, B.tgt_local);
+    B.h_blk_off.assign(nb + 1, 0);
+    std::vector<uint32_t> work;
+    for (size_t b = 0; b < nb; ++b) {
+        unsigned long long nbk = B.h_src_start[b + 1] - B.h_src_start[b];
+        unsigned long long mbk = B.h_tgt_start[b + 1] - B.h_tgt_start[b];
+        B.h_blk_off[b + 1] = B.h_blk_off[b] + nbk * mbk;
+        if (nbk && mbk) work.push_back(static_cast<uint32_t>(b));
+    }
+    B.entries = B.h_blk_off[nb];
+    B.blk_off.upload(B.h_blk_off.data(), nb + 1, s);
+    B.n_work = work.size();
+    B.work.resize(std::max<size_t>(work.size(), 1));
+    if (!work.empty()) B.work.upload(work.data(), work.size(), s);
+    ctx.sync();
+}
+
+namespace {
+__global__ void compose_kernel(uint64_t* __restrict__ comp, const uint32_t* __restrict__ a, long long n, uint64_t radix) {
+    long long i = blockIdx.x * 256LL + threadIdx.x;
+    if (i < n) comp[i] = comp[i] * radix + a[i];
+}
+__global__ void narrow_kernel(uint32_t* __restrict__ out, const uint64_t* __restrict__ in, long long n) {
+    long long i = blockIdx.x * 256LL + threadIdx.x;
+    if (i < n) out[i] = static_cast<uint32_t>(in[i]);
+}
+}  // namespace
+
+// lsh_neighbor_pairs' k-means branch (lsh.cpp:245-283): per band, per
+// function, hash_kmeans of the union with fn_seed(seed, band, fn); composite
+// ids are mixed-radix over the r functions.
+void lsh_kmeans_bucket_ids(Ctx& ctx, const double* d_union, size_t n, size_t m, size_t d, int bands, int rows,
+                           int buckets, int iters, uint64_t seed, std::vector<DevBuf<uint32_t>>& ids, size_t& range) {
+    const size_t N = n + m;
+    if (bands < 1 || rows < 1) throw Status(2, "lsh: bands and rows_per_band must be >= 1");
+    if (buckets < 2) throw Status(2, "lsh: buckets_per_fn must be >= 2");
+    if (static_cast<size_t>(buckets) > N) throw Status(2, "hash_kmeans: more buckets than points");
+    double r = std::pow(static_cast<double>(buckets), rows);
+    if (r > 4294967295.0) throw Status(2, "lsh: composite bucket range exceeds 2^32 on this path");
+    range = static_cast<size_t>(r);
+    cudaStream_t s = ctx.stream;
+    DevBuf<double> ctr(static_cast<size_t>(buckets) * d);
+    DevBuf<uint32_t> assign(N);
+    DevBuf<uint64_t> comp(N);
+    ids.clear();
+    for (int b = 0; b < bands; ++b) {
+        comp.zero(s);
+        for (int fn = 0; fn < rows; ++fn) {
+            lloyd_device<double>(ctx, d_union, N, static_cast<int>(d), buckets, iters, fn_seed(seed, b, fn), ctr.get(),
+                                 assign.get());
+            compose_kernel<<<ceil_div(N, 256), 256, 0, s>>>(comp.get(), assign.get(), N, static_cast<uint64_t>(buckets));
+        }
+        DevBuf<uint32_t> out(N);
+        narrow_kernel<<<ceil_div(N, 256), 256, 0, s>>>(out.get(), comp.get(), N);
+        LAUNCH_OK("lsh ids");
+        ids.push_back(std::move(out));
+    }
+    ctx.sync();
+}
+
+// ---------------------------------------------------------------------------
+// Tiled kernels with epilogues
+// ---------------------------------------------------------------------------
+namespace {
+
+__device__ __forceinline__ double cost_from_fold(int kind, double acc, double nx, double ny, int* bad) {
+    if (kind == 0) return __dsqrt_rn(acc);
+    if (kind == 3) return acc;
+    if (kind == 1) return -acc;
+    if (nx == 0.0 || ny == 0.0) {
+        atomicOr(bad, 1);
+        return 0.0;
+    }
+    double c = __ddiv_rn(acc, __dsqrt_rn(xmul(nx, ny)));
+    c = c > 1.0 ? 1.0 : c;
+    c = c < -1.0 ? -1.0 : c;
+    return __dsqrt_rn(xsub(1.0, c));
+}
+
+// Band blocks: tile = (bucket, r0, c0) of bucket's n_b x m_b block.
+template <int MODE, class Epi>
+__global__ void __launch_bounds__(256) band_tile_kernel(const int4* __restrict__ tiles, BandView bv,
+                                                        const double* __restrict__ A, const double* __restrict__ B,
+                                                        int d, Epi epi) {
+    __shared__ double As[KC][TP + 1];
+    __shared__ double Bs[KC][TC + 1];
+    const int4 t = tiles[blockIdx.x];
+    const int b = t.x, r0 = t.y, c0 = t.z;
+    const uint32_t sb = bv.src_start[b], nb = bv.src_start[b + 1] - sb;
+    const uint32_t tb = bv.tgt_start[b], mb = bv.tgt_start[b + 1] - tb;
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int k0 = 0; k0 < d; k0 += KC) {
+        load_slab<double>(As, A, bv.src_order + sb, r0, nb, d, k0);
+        load_slab<double>(Bs, B, bv.tgt_order + tb, c0, mb, d, k0);
+        __syncthreads();
+        tile_fold<MODE>(As, Bs, ty, tx, acc);
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t r = r0 + ty + 16 * i;
+        if (r >= nb) continue;
+        const uint32_t si = bv.src_order[sb + r];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t c = c0 + tx + 16 * j;
+            if (c < mb) epi(bv.blk_off[b] + static_cast<unsigned long long>(r) * mb + c, si, bv.tgt_order[tb + c], acc[i][j]);
+        }
+    }
+}
+
+// Dense: rows of A (na) against rows of B (nb).
+template <int MODE, class Epi>
+__global__ void __launch_bounds__(256) dense_tile_kernel(const double* __restrict__ A, long long na,
+                                                         const double* __restrict__ B, long long nbr, int d, Epi epi) {
+    __shared__ double As[KC][TP + 1];
+    __shared__ double Bs[KC][TC + 1];
+    const long long r0 = static_cast<long long>(blockIdx.x) * TP, c0 = static_cast<long long>(blockIdx.y) * TC;
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int k0 = 0; k0 < d; k0 += KC) {
+        load_slab<double>(As, A, nullptr, r0, na, d, k0);
+        load_slab<double>(Bs, B, nullptr, c0, nbr, d, k0);
+        __syncthreads();
+        tile_fold<MODE>(As, Bs, ty, tx, acc);
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        long long r = r0 + ty + 16 * i;
+        if (r >= na) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            long long c = c0 + tx + 16 * j;
+            if (c < nbr) epi(r, c, acc[i][j]);
+        }
+    }
+}
+
+// log K^sp at a block entry, -inf where an earlier band already holds the
+// pair (sparse_kernel.cpp:76: logvals = 0.0 - cost * inv).
+struct EpiLogK {
+    double* out;
+    BandSet bs;
+    int band;
+    int kind;
+    double inv;
+    const double* norms;  // union norms (cosine only), targets offset by n
+    long long n;
+    int* bad;
+    __device__ void operator()(unsigned long long idx, uint32_t i, uint32_t j, double acc) const {
+        for (int b = 0; b < band; ++b)
+            if (bs.src_bucket[b][i] == bs.tgt_bucket[b][j]) {
+                out[idx] = kNegInf;
+                return;
+            }
+        double nx = norms ? norms[i] : 0.0, ny = norms ? norms[n + j] : 0.0;
+        double c = cost_from_fold(kind, acc, nx, ny, bad);
+        out[idx] = xsub(0.0, xmul(c, inv));
+    }
+};
+
+// exp(-c * inv) (kernel_block, nystrom.cpp:53-64) or exp(-c / lambda)
+// (the landmark Gram matrix A, nystrom.cpp:91-95).
+struct EpiExp {
+    double* out;
+    long long ld;
+    int kind;
+    double scale;
+    bool divide;
+    const double* na;
+    const double* nb;
+    int* bad;
+    __device__ void operator()(long long r, long long c, double acc) const {
+        double c0 = cost_from_fold(kind, acc, na ? na[r] : 0.0, nb ? nb[c] : 0.0, bad);
+        out[r * ld + c] = divide ? exp(__ddiv_rn(-c0, scale)) : exp(xmul(-c0, scale));
+    }
+};
+
+struct EpiStore {
+    double* out;
+    long long ld;
+    int* bad;
+    __device__ void operator()(long long r, long long c, double acc) const {
+        if (!isfinite(acc)) atomicOr(bad, 1);
+        out[r * ld + c] = acc;
+    }
+};
+
+// max |(A_j W) - V| with the transposed storage: acc = (A_j W)_{c r}.
+struct EpiResid {
+    const double* vt;
+    long long ld;
+    unsigned long long* maxbits;
+    __device__ void operator()(long long r, long long c, double acc) const {
+        double e = fabs(acc - vt[r * ld + c]);
+        if (!(e <= 1.79e308)) e = kPosInf;
+        atomicMax(maxbits, static_cast<unsigned long long>(__double_as_longlong(e)));
+    }
+};
+
+// delta = exp(log K) - (U W)_ij (sparse_kernel.cpp:100-109); acc is the
+// sequential fold sum_a u_ia w_aj of NystromFactors::entry (nystrom.cpp:127-132).
+struct EpiDelta {
+    double* delta;
+    const double* logk;
+    unsigned long long* maxbits;
+    int* overflow;
+    __device__ void operator()(unsigned long long idx, uint32_t, uint32_t, double nys) const {
+        double lk = logk[idx];
+        if (lk == kNegInf) {  // masked duplicate of an earlier band
+            delta[idx] = 0.0;
+            return;
+        }
+        double exact = exp(lk);
+        if (isinf(exact)) {
+            atomicOr(overflow, 1);
+            delta[idx] = 0.0;
+            return;
+        }
+        double dv = exact - nys;
+        delta[idx] = dv;
+        atomicMax(maxbits, static_cast<unsigned long long>(__double_as_longlong(fabs(dv))));
+    }
+};
+
+__global__ void norms_kernel(const double* __restrict__ X, long long N, int d, double* __restrict__ out) {
+    long long i = blockIdx.x * 256LL + threadIdx.x;
+    if (i < N) {
+        double s = 0.0;
+        for (int k = 0; k < d; ++k) s = xadd(s, xmul(X[i * d + k], X[i * d + k]));
+        out[i] = s;
+    }
+}
+
+std::vector<int4> band_tiles(const Band& B) {
+    std::vector<int4> tiles;
+    for (size_t b = 0; b < B.nb; ++b) {
+        int nbk = B.h_src_start[b + 1] - B.h_src_start[b];
+        int mbk = B.h_tgt_start[b + 1] - B.h_tgt_start[b];
+        for (int r0 = 0; r0 < nbk; r0 += TP)
+            for (int c0 = 0; c0 < mbk; c0 += TC) tiles.push_back(make_int4(static_cast<int>(b), r0, c0, 0));
+    }
+    return tiles;
+}
+
+template <int MODE, class Epi>
+void launch_band_tiles(Ctx& ctx, const Band& B, BandView bv, const double* A, const double* Bm, int d, Epi epi) {
+    std::vector<int4> tiles = band_tiles(B);
+    if (tiles.empty()) return;
+    DevBuf<int4> dt;
+    dt.upload(tiles.data(), tiles.size(), ctx.stream);
+    for (size_t off = 0; off < tiles.size(); off += 1u << 30) {
+        unsigned cnt = static_cast<unsigned>(std::min<size_t>(tiles.size() - off, 1u << 30));
+        band_tile_kernel<MODE, Epi><<<cnt, 256, 0, ctx.stream>>>(dt.get() + off, bv, A, Bm, d, epi);
+    }
+    LAUNCH_OK("band_tile_kernel");
+    ctx.sync();
+}
+
+template <int MODE, class Epi>
+void launch_dense_tiles(Ctx& ctx, const double* A, long long na, const double* B, long long nb, int d, Epi epi) {
+    if (na == 0 || nb == 0) return;
+    dim3 grid(ceil_div(na, TP), ceil_div(nb, TC));
+    dense_tile_kernel<MODE, Epi><<<grid, 256, 0, ctx.stream>>>(A, na, B, nb, d, epi);
+    LAUNCH_OK("dense_tile_kernel");
+}
+
+const double* union_norms(Op& op) {
+    if (op.cost != 2) return nullptr;
+    if (op.norms.size() != op.n + op.m) {
+        op.norms.resize(op.n + op.m);
+        norms_kernel<<<ceil_div(op.n + op.m, 256), 256, 0, op.ctx->stream>>>(op.X.get(), op.n + op.m, op.d, op.norms.get());
+        LAUNCH_OK("norms");
+    }
+    return op.norms.get();
+}
+
+int read_flag(Ctx& ctx, DevBuf<int>& f) {
+    int h = 0;
+    f.download(&h, 1, ctx.stream);
+    ctx.sync();
+    return h;
+}
+
+}  // namespace
+
+void build_sparse_values(Op& op) {
+    Ctx& ctx = *op.ctx;
+    const double* nrm = union_norms(op);
+    DevBuf<int> bad(1);
+    bad.zero(ctx.stream);
+    op.val64.clear();
+    op.stored = 0;
+    const bool dot = op.cost == 1 || op.cost == 2;  // negative-dot / cosine fold x.y, else (x-y)^2
+    for (size_t b = 0; b < op.bands.size(); ++b) {
+        DevBuf<double> v(std::max<unsigned long long>(op.bands[b].entries, 1));
+        EpiLogK epi{v.get(), op.bandset(), static_cast<int>(b), op.cost, 1.0 / op.lambda, nrm,
+                    static_cast<long long>(op.n), bad.get()};
+        if (dot)
+            launch_band_tiles<1>(ctx, op.bands[b], op.view(static_cast<int>(b)), op.P(), op.Q(), static_cast<int>(op.d), epi);
+        else
+            launch_band_tiles<0>(ctx, op.bands[b], op.view(static_cast<int>(b)), op.P(), op.Q(), static_cast<int>(op.d), epi);
+        op.stored += op.bands[b].entries;
+        op.val64.push_back(std::move(v));
+    }
+    if (read_flag(ctx, bad)) throw Status(2, "cosine-derived cost undefined for zero vectors");
+}
+
+// ---------------------------------------------------------------------------
+// Nystrom factors (nystrom.cpp:28-125)
+// ---------------------------------------------------------------------------
+namespace {
+
+using LD = long double;
+
+// Symmetric diagonal-pivoted LDL^T in long double (the factorisation the
+// reference takes from Eigen::LDLT<long double>, nystrom.cpp:108).
+struct HostLdlt {
+    size_t l;
+    std::vector<LD> f;
+    std::vector<size_t> perm;
+    bool ok = true;
+    HostLdlt(const std::vector<LD>& a, size_t n) : l(n), f(a), perm(n) {
+        std::iota(perm.begin(), perm.end(), size_t{0});
+        std::vector<LD> w(l);
+        for (size_t k = 0; k < l; ++k) {
+            size_t piv = k;
+            LD best = std::fabs(f[k * l + k]);
+            for (size_t i = k + 1; i < l; ++i)
+                if (std::fabs(f[i * l + i]) > best) { best = std::fabs(f[i * l + i]); piv = i; }
+            if (piv != k) {
+                for (size_t c = 0; c < l; ++c) std::swap(f[k * l + c], f[piv * l + c]);
+                for (size_t r = 0; r < l; ++r) std::swap(f[r * l + k], f[r * l + piv]);
+                std::swap(perm[k], perm[piv]);
+            }
+            for (size_t j = 0; j < k; ++j) w[j] = f[j * l + j] * f[k * l + j];
+            LD dk = f[k * l + k];
+            for (size_t j = 0; j < k; ++j) dk -= f[k * l + j] * w[j];
+            f[k * l + k] = dk;
+#pragma omp parallel for schedule(static) if (l - k > 256)
+            for (long long ii = static_cast<long long>(k) + 1; ii < static_cast<long long>(l); ++ii) {
+                const size_t i = static_cast<size_t>(ii);
+                LD v = f[i * l + k];
+                for (size_t j = 0; j < k; ++j) v -= f[i * l + j] * w[j];
+                f[i * l + k] = v;
+            }
+            if (std::fabs(dk) > 0) {
+                for (size_t i = k + 1; i < l; ++i) f[i * l + k] /= dk;
+            } else {
+                for (size_t i = k + 1; i < l; ++i)
+                    if (f[i * l + k] != 0) ok = false;
+            }
+        }
+    }
+    void solve(LD* b) const {
+        std::vector<LD> y(l);
+        for (size_t k = 0; k < l; ++k) y[k] = b[perm[k]];
+        for (size_t i = 0; i < l; ++i)
+            for (size_t j = 0; j < i; ++j) y[i] -= f[i * l + j] * y[j];
+        for (size_t i = 0; i < l; ++i) {
+            LD dv = f[i * l + i];
+            y[i] = std::fabs(dv) > std::numeric_limits<LD>::min() ? y[i] / dv : 0;
+        }
+        for (size_t ii = l; ii-- > 0;)
+            for (size_t j = ii + 1; j < l; ++j) y[ii] -= f[j * l + ii] * y[j];
+        for (size_t k = 0; k < l; ++k) b[perm[k]] = y[k];
+    }
+};
+
+__global__ void maxabs_kernel(const double* __restrict__ x, long long n, unsigned long long* __restrict__ out) {
+    double m = 0.0;
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += 256LL * gridDim.x) m = fmax(m, fabs(x[i]));
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(m)));
+}
+
+__global__ void gather_rows_kernel(const double* __restrict__ X, const uint32_t* __restrict__ rows, int k, int d,
+                                   double* __restrict__ out) {
+    for (int e = blockIdx.x * 256 + threadIdx.x; e < k * d; e += 256 * gridDim.x)
+        out[e] = X[static_cast<long long>(rows[e / d]) * d + e % d];
+}
+
+}  // namespace
+
+void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed) {
+    Ctx& ctx = *op.ctx;
+    cudaStream_t s = ctx.stream;
+    const size_t n = op.n, m = op.m, d = op.d, l = op.l, N = n + m;
+    if (!(op.lambda > 0.0)) throw Status(2, "build_factors: lambda must be positive");
+    op.L.resize(l * d);
+    if (h_landmarks) {
+        op.L.upload(h_landmarks, l * d, s);
+    } else {
+        // select_landmarks (nystrom.cpp:28-48)
+        if (l < 1 || l > N) throw Status(2, "select_landmarks: l out of range");
+        if (method == 0) {
+            DevBuf<uint32_t> asg(N);
+            lloyd_device<double>(ctx, op.X.get(), N, static_cast<int>(d), static_cast<int>(l), 10, seed, op.L.get(), asg.get());
+        } else {
+            std::mt19937_64 rng(seed);
+            std::uniform_int_distribution<std::size_t> first(0, N - 1);
+            uint64_t f = first(rng);
+            std::vector<unsigned long long> raw(l > 1 ? l - 1 : 0);
+            for (auto& r : raw) r = rng();
+            DevBuf<uint32_t> rows(l);
+            kmeans_pp_device<double>(ctx, op.X.get(), N, static_cast<int>(d), static_cast<int>(l), f, raw, rows.get(), nullptr);
+            gather_rows_kernel<<<ceil_div(l * d, 256), 256, 0, s>>>(op.X.get(), rows.get(), static_cast<int>(l),
+                                                                     static_cast<int>(d), op.L.get());
+            LAUNCH_OK("landmark rows");
+        }
+    }
+    ctx.sync();
+    const double* nrm = union_norms(op);
+    DevBuf<double> lnorm;
+    if (op.cost == 2) {
+        lnorm.resize(l);
+        norms_kernel<<<ceil_div(l, 256), 256, 0, s>>>(op.L.get(), l, d, lnorm.get());
+    }
+    DevBuf<int> bad(1);
+    bad.zero(s);
+    const int mode_dot = (op.cost == 1 || op.cost == 2);
+    auto exp_block = [&](double* out, const double* A, long long na, const double* nA, const double* B, long long nb,
+                         const double* nB, bool divide) {
+        EpiExp epi{out, nb, op.cost, divide ? op.lambda : 1.0 / op.lambda, divide, nA, nB, bad.get()};
+        if (mode_dot)
+            launch_dense_tiles<1>(ctx, A, na, B, nb, static_cast<int>(d), epi);
+        else
+            launch_dense_tiles<0>(ctx, A, na, B, nb, static_cast<int>(d), epi);
+    };
+    // U = k(X_p, L) (n x l), V^T = k(X_q, L) (m x l), A = k(L, L) with division.
+    op.U64.resize(std::max<size_t>(n * l, 1));
+    DevBuf<double> Vt(std::max<size_t>(m * l, 1)), A(l * l);
+    exp_block(op.U64.get(), op.P(), n, nrm, op.L.get(), l, lnorm.get(), false);
+    exp_block(Vt.get(), op.Q(), m, nrm ? nrm + n : nullptr, op.L.get(), l, lnorm.get(), false);
+    exp_block(A.get(), op.L.get(), l, lnorm.get(), op.L.get(), l, lnorm.get(), true);
+    if (read_flag(ctx, bad)) throw Status(2, "cosine-derived cost undefined for zero vectors");
+
+    std::vector<double> hA(l * l);
+    A.download(hA.data(), l * l, s);
+    DevBuf<unsigned long long> vmax(1);
+    vmax.zero(s);
+    maxabs_kernel<<<std::min<long long>(ceil_div(m * l, 256), 1024), 256, 0, s>>>(Vt.get(), m * l, vmax.get());
+    unsigned long long vbits = 0;
+    vmax.download(&vbits, 1, s);
+    ctx.sync();
+    double vmaxd;
+    std::memcpy(&vmaxd, &vbits, 8);
+    const LD v_scale = std::max<LD>(static_cast<LD>(vmaxd), 1e-300L);
+    std::vector<LD> a(l * l);
+    for (size_t i = 0; i < l * l; ++i) a[i] = static_cast<LD>(hA[i]);
+    LD trace = 0.0L;
+    for (size_t i = 0; i < l; ++i) trace += a[i * l + i];
+    const LD jitter_unit = trace / static_cast<LD>(l);
+
+    op.Wt64.resize(std::max<size_t>(m * l, 1));
+    DevBuf<double> dAinv(l * l), dAj(l * l);
+    DevBuf<unsigned long long> rbits(1);
+    for (double rel = 0.0; rel <= 1.1e-4; rel = (rel == 0.0 ? 1e-10 : rel * 10.0)) {
+        std::vector<LD> aj = a;
+        for (size_t i = 0; i < l; ++i) aj[i * l + i] += rel * jitter_unit;
+        HostLdlt fac(aj, l);
+        if (!fac.ok) continue;
+        std::vector<LD> inv(l * l);
+        bool finite = true;
+#pragma omp parallel for schedule(static) reduction(&& : finite)
+        for (long long cc = 0; cc < static_cast<long long>(l); ++cc) {
+            std::vector<LD> e(l, 0.0L);
+            e[cc] = 1.0L;
+            fac.solve(e.data());
+            for (size_t r = 0; r < l; ++r) {
+                inv[r * l + cc] = e[r];
+                if (!std::isfinite(e[r])) finite = false;
+            }
+        }
+        if (!finite) continue;
+        std::vector<double> hinv(l * l), haj(l * l);
+        for (size_t i = 0; i < l * l; ++i) {
+            hinv[i] = static_cast<double>(inv[i]);
+            haj[i] = static_cast<double>(aj[i]);
+        }
+        dAinv.upload(hinv.data(), l * l, s);
+        dAj.upload(haj.data(), l * l, s);
+        bad.zero(s);
+        // W^T = V^T A^-T  (row j: sum_b Vt[j][b] Ainv[a][b])
+        launch_dense_tiles<1>(ctx, Vt.get(), m, dAinv.get(), l, static_cast<int>(l),
+                              EpiStore{op.Wt64.get(), static_cast<long long>(l), bad.get()});
+        if (read_flag(ctx, bad)) continue;
+        rbits.zero(s);
+        launch_dense_tiles<1>(ctx, op.Wt64.get(), m, dAj.get(), l, static_cast<int>(l),
+                              EpiResid{Vt.get(), static_cast<long long>(l), rbits.get()});
+        unsigned long long rb = 0;
+        rbits.download(&rb, 1, s);
+        ctx.sync();
+        double resid;
+        std::memcpy(&resid, &rb, 8);
+        if (static_cast<LD>(resid) > 1e-6L * v_scale) continue;
+        LD norm_a = 0.0L, norm_inv = 0.0L;
+        for (size_t c = 0; c < l; ++c) {
+            LD sa = 0.0L, si = 0.0L;
+            for (size_t r = 0; r < l; ++r) {
+                sa += std::fabs(aj[r * l + c]);
+                si += std::fabs(inv[r * l + c]);
+            }
+            norm_a = std::max(norm_a, sa);
+            norm_inv = std::max(norm_inv, si);
+        }
+        LD cond = norm_a * norm_inv;
+        op.cond = std::isfinite(cond) && cond > 0 ? static_cast<double>(cond) : std::numeric_limits<double>::infinity();
+        return;
+    }
+    throw Status(5, "build_factors: landmark kernel matrix numerically singular beyond jitter budget");
+}
+
+// build_correction (sparse_kernel.cpp:82-117) on every band block.
+void build_correction(Op& op) {
+    Ctx& ctx = *op.ctx;
+    // log K^sp first (same values as build_sparse), then delta.
+    build_sparse_values(op);
+    op.logk64 = std::move(op.val64);
+    op.val64.clear();
+    DevBuf<unsigned long long> maxbits(1);
+    DevBuf<int> overflow(1);
+    maxbits.zero(ctx.stream);
+    overflow.zero(ctx.stream);
+    for (size_t b = 0; b < op.bands.size(); ++b) {
+        DevBuf<double> dlt(std::max<unsigned long long>(op.bands[b].entries, 1));
+        EpiDelta epi{dlt.get(), op.logk64[b].get(), maxbits.get(), overflow.get()};
+        launch_band_tiles<1>(ctx, op.bands[b], op.view(static_cast<int>(b)), op.U64.get(), op.Wt64.get(),
+                             static_cast<int>(op.l), epi);
+        op.val64.push_back(std::move(dlt));
+    }
+    if (read_flag(ctx, overflow)) throw Status(3, "build_correction: kernel value overflows linear space");
+    unsigned long long mb = 0;
+    maxbits.download(&mb, 1, ctx.stream);
+    ctx.sync();
+    std::memcpy(&op.max_abs_delta, &mb, 8);
+}
+
+namespace {
+__global__ void to_f32_kernel(const double* __restrict__ in, float* __restrict__ out, long long n) {
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += 256LL * gridDim.x) out[i] = static_cast<float>(in[i]);
+}
+void to_f32(Ctx& ctx, const DevBuf<double>& in, DevBuf<float>& out, size_t n) {
+    out.resize(std::max<size_t>(n, 1));
+    if (n) to_f32_kernel<<<std::min<long long>(ceil_div(n, 256), 8 * ctx.num_sms), 256, 0, ctx.stream>>>(in.get(), out.get(), n);
+    LAUNCH_OK("to_f32");
+}
+}  // namespace
+
+// fp32 iteration copies (fp32 storage, fp64 accumulation).
+void finalize_storage(Op& op) {
+    if (op.fp64) return;
+    op.val32.clear();
+    for (size_t b = 0; b < op.bands.size(); ++b) {
+        DevBuf<float> v;
+        to_f32(*op.ctx, op.val64[b], v, op.bands[b].entries);
+        op.val32.push_back(std::move(v));
+    }
+    if (op.kind >= 2) {
+        to_f32(*op.ctx, op.U64, op.U32, op.n * op.l);
+        to_f32(*op.ctx, op.Wt64, op.Wt32, op.m * op.l);
+    }
+    op.ctx->sync();
+}
+
+// ---------------------------------------------------------------------------
+// CSR export in the reference order (rows ascending, columns ascending,
+// unique; NeighborPairs::from_pairs, lsh.cpp:163-177).
+// ---------------------------------------------------------------------------
+namespace {
+
+struct BandViews {
+    BandView v[kMaxBands];
+    int bands;
+};
+
+__device__ __forceinline__ bool masked_before(const BandSet& bs, int band, uint32_t i, uint32_t j) {
+    for (int b = 0; b < band; ++b)
+        if (bs.src_bucket[b][i] == bs.tgt_bucket[b][j]) return true;
+    return false;
+}
+
+__global__ void csr_count_kernel(BandViews bvs, BandSet bs, long long n, uint32_t* __restrict__ counts) {
+    long long i = blockIdx.x * 256LL + threadIdx.x;
+    if (i >= n) return;
+    uint32_t cnt = 0;
+    for (int b = 0; b < bvs.bands; ++b) {
+        const BandView& v = bvs.v[b];
+        uint32_t bk = v.src_bucket[i];
+        for (uint32_t p = v.tgt_start[bk]; p < v.tgt_start[bk + 1]; ++p)
+            if (!masked_before(bs, b, static_cast<uint32_t>(i), v.tgt_order[p])) ++cnt;
+    }
+    counts[i] = cnt;
+}
+
+// k-way merge of the per-band sorted target lists of row i.
+__global__ void csr_fill_kernel(BandViews bvs, BandSet bs, long long n, const uint32_t* __restrict__ row_ptr,
+                                uint32_t* __restrict__ col) {
+    long long i = blockIdx.x * 256LL + threadIdx.x;
+    if (i >= n) return;
+    uint32_t pos[kMaxBands], end[kMaxBands];
+    for (int b = 0; b < bvs.bands; ++b) {
+        uint32_t bk = bvs.v[b].src_bucket[i];
+        pos[b] = bvs.v[b].tgt_start[bk];
+        end[b] = bvs.v[b].tgt_start[bk + 1];
+    }
+    uint32_t out = row_ptr[i];
+    while (true) {
+        int best = -1;
+        uint32_t bj = 0xffffffffu;
+        for (int b = 0; b < bvs.bands; ++b) {
+            while (pos[b] < end[b] && masked_before(bs, b, static_cast<uint32_t>(i), bvs.v[b].tgt_order[pos[b]])) ++pos[b];
+            if (pos[b] < end[b] && bvs.v[b].tgt_order[pos[b]] < bj) { bj = bvs.v[b].tgt_order[pos[b]]; best = b; }
+        }
+        if (best < 0) break;
+        col[out++] = bj;
+        ++pos[best];
+    }
+}
+
+}  // namespace
+
+void build_csr(Op& op) {
+    if (op.csr_ready) return;
+    Ctx& ctx = *op.ctx;
+    cudaStream_t s = ctx.stream;
+    const long long n = op.n;
+    BandViews bvs{};
+    bvs.bands = static_cast<int>(op.bands.size());
+    for (int b = 0; b < bvs.bands; ++b) bvs.v[b] = op.view(b);
+    DevBuf<uint32_t> counts(std::max<long long>(n, 1));
+    op.csr_row_ptr.resize(n + 1);
+    op.csr_row_ptr.zero(s);
+    if (n && bvs.bands) {
+        csr_count_kernel<<<ceil_div(n, 256), 256, 0, s>>>(bvs, op.bandset(), n, counts.get());
+        size_t tmp = 0;
+        cub::DeviceScan::InclusiveSum(nullptr, tmp, counts.get(), op.csr_row_ptr.get() + 1, n, s);
+        DevBuf<unsigned char> t(tmp);
+        cub::DeviceScan::InclusiveSum(t.get(), tmp, counts.get(), op.csr_row_ptr.get() + 1, n, s);
+        LAUNCH_OK("csr count");
+    }
+    uint32_t nnz = 0;
+    CUDA_OK(cudaMemcpyAsync(&nnz, op.csr_row_ptr.get() + n, 4, cudaMemcpyDeviceToHost, s));
+    ctx.sync();
+    op.nnz = nnz;
+    op.csr_col.resize(std::max<uint32_t>(nnz, 1));
+    if (nnz) {
+        csr_fill_kernel<<<ceil_div(n, 256), 256, 0, s>>>(bvs, op.bandset(), n, op.csr_row_ptr.get(), op.csr_col.get());
+        LAUNCH_OK("csr fill");
+    }
+    ctx.sync();
+    op.csr_ready = true;
+}
+
+namespace {
+// Value of CSR entry (i, j): the first band sharing the bucket holds it.
+__device__ __forceinline__ unsigned long long entry_index(const BandViews& bvs, uint32_t i, uint32_t j, int* band) {
+    for (int b = 0; b < bvs.bands; ++b) {
+        const BandView& v = bvs.v[b];
+        uint32_t bk = v.src_bucket[i];
+        if (bk == v.tgt_bucket[j]) {
+            *band = b;
+            uint32_t mb = v.tgt_start[bk + 1] - v.tgt_start[bk];
+            return v.blk_off[bk] + static_cast<unsigned long long>(v.src_local[i]) * mb + v.tgt_local[j];
+        }
+    }
+    *band = -1;
+    return 0;
+}
+
+struct ValPtrs {
+    const double* p[kMaxBands];
+};
+
+// which: 0/1/2 read a stored band array (log K, delta, log_sp); 3 recomputes
+// (U W)_ij in the reference's sequential order.
+__global__ void csr_values_kernel(BandViews bvs, ValPtrs vals, long long n, const uint32_t* __restrict__ row_ptr,
+                                  const uint32_t* __restrict__ col, int which, const double* __restrict__ U,
+                                  const double* __restrict__ Wt, int l, double* __restrict__ out) {
+    long long i = blockIdx.x * 256LL + threadIdx.x;
+    if (i >= n) return;
+    for (uint32_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+        uint32_t j = col[e];
+        if (which == 3) {
+            double s = 0.0;
+            for (int a = 0; a < l; ++a) s = xadd(s, xmul(U[i * l + a], Wt[static_cast<long long>(j) * l + a]));
+            out[e] = s;
+        } else {
+            int b;
+            unsigned long long idx = entry_index(bvs, static_cast<uint32_t>(i), j, &b);
+            out[e] = vals.p[b][idx];
+        }
+    }
+}
+}  // namespace
+
+void export_csr(Op& op, int which, uint32_t* row_ptr, uint32_t* col, double* vals) {
+    build_csr(op);
+    Ctx& ctx = *op.ctx;
+    cudaStream_t s = ctx.stream;
+    if (row_ptr) op.csr_row_ptr.download(row_ptr, op.n + 1, s);
+    if (col && op.nnz) op.csr_col.download(col, op.nnz, s);
+    if (vals && op.nnz) {
+        BandViews bvs{};
+        bvs.bands = static_cast<int>(op.bands.size());
+        ValPtrs vp{};
+        for (int b = 0; b < bvs.bands; ++b) {
+            bvs.v[b] = op.view(b);
+            if (which == 0) vp.p[b] = op.kind == 1 ? op.val64[b].get() : op.logk64[b].get();
+            if (which == 1) vp.p[b] = op.kind == 3 ? op.val64[b].get() : nullptr;
+            if (which == 2) vp.p[b] = op.kind == 3 ? op.logk64[b].get() : op.val64[b].get();
+        }
+        if (which == 1 && op.kind != 3) throw Status(2, "export_csr: delta needs an lcn operator");
+        if (which == 3 && op.kind != 3) throw Status(2, "export_csr: nys_vals needs an lcn operator");
+        DevBuf<double> dv(op.nnz);
+        csr_values_kernel<<<ceil_div(op.n, 256), 256, 0, s>>>(bvs, vp, op.n, op.csr_row_ptr.get(), op.csr_col.get(),
+                                                              which, op.U64.get(), op.Wt64.get(),
+                                                              static_cast<int>(op.l), dv.get());
+        LAUNCH_OK("csr values");
+        dv.download(vals, op.nnz, s);
+    }
+    ctx.sync();
+}
+
+}  // namespace lcnb

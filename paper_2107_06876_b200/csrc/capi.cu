@@ -1,0 +1,533 @@
+// extern "C" boundary (include/lcn_b200.h). Never throws: every entry point
+// converts lcnb::Status / std::exception into an lcn_status and stores the
+// message (text identical to the reference exception's what()) on the context.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <string>
+
+#include "../../include/lcn_b200.h"
+#include "kmeans.cuh"
+#include "op.cuh"
+
+using namespace lcnb;
+
+namespace lcnb {
+size_t max_bipartite_matching(size_t n, size_t m, const uint32_t* row_ptr, const uint32_t* col);
+}
+
+struct lcn_ctx {
+    Ctx c;
+};
+struct lcn_op {
+    Op o;
+};
+struct lcn_result {
+    Result r;
+    lcn_op* op = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_orphan_error;
+
+template <class F>
+int guard(lcn_ctx* ctx, F&& f) {
+    std::string* sink = ctx ? &ctx->c.last_error : &g_orphan_error;
+    try {
+        if (ctx) ctx->c.activate();
+        f();
+        return LCN_OK;
+    } catch (const Status& e) {
+        *sink = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        *sink = "out of host memory";
+        return LCN_E_ERROR;
+    } catch (const std::exception& e) {
+        *sink = e.what();
+        return LCN_E_ERROR;
+    }
+}
+
+void check_points(const double* x, size_t n, size_t d, const char* id) {
+    if (n == 0 || d == 0) throw Status(2, std::string("point set '") + id + "' is empty");
+    if (!x) throw Status(2, std::string("point set '") + id + "' is null");
+    for (size_t i = 0; i < n * d; ++i)
+        if (!std::isfinite(x[i])) throw Status(2, std::string("point set '") + id + "' has non-finite coordinates");
+}
+
+void upload_union(Op& op, const double* p, size_t n, const double* q, size_t m, size_t d) {
+    op.n = n;
+    op.m = m;
+    op.d = d;
+    op.X.resize((n + m) * d);
+    CUDA_OK(cudaMemcpyAsync(op.X.get(), p, n * d * 8, cudaMemcpyHostToDevice, op.ctx->stream));
+    CUDA_OK(cudaMemcpyAsync(op.X.get() + n * d, q, m * d * 8, cudaMemcpyHostToDevice, op.ctx->stream));
+}
+
+__global__ void promote_kernel(const float* __restrict__ in, double* __restrict__ out, long long n) {
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += 256LL * gridDim.x) out[i] = static_cast<double>(in[i]);
+}
+
+void check_cost_lambda(int cost, double lambda, const char* who) {
+    if (cost < 0 || cost > 3) throw Status(2, "unknown cost kind");
+    if (!(lambda > 0.0)) throw Status(2, std::string(who) + ": lambda must be positive");
+}
+
+// Bands from device bucket ids of the union (ids[b]: n+m entries).
+void bands_from_union_ids(Op& op, std::vector<DevBuf<uint32_t>>& ids, size_t range) {
+    op.bands.clear();
+    op.bands.resize(ids.size());
+    for (size_t b = 0; b < ids.size(); ++b)
+        build_band_layout(*op.ctx, op.bands[b], ids[b].get(), ids[b].get() + op.n, op.n, op.m, range);
+}
+
+// Host bucket ids (bands x n, bands x m) -> dense device ids.
+void bands_from_host_ids(Op& op, const uint64_t* ids_p, const uint64_t* ids_q, int bands, uint64_t range) {
+    if (bands < 0 || bands > kMaxBands) throw Status(2, "neighbor_pairs: band count out of range");
+    std::vector<DevBuf<uint32_t>> ids;
+    size_t dense_range = 0;
+    for (int b = 0; b < bands; ++b) {
+        const uint64_t* bp = ids_p + static_cast<size_t>(b) * op.n;
+        const uint64_t* bq = ids_q + static_cast<size_t>(b) * op.m;
+        // compress to dense bucket indices preserving order (sorted_by_bucket
+        // groups equal ids, lsh.cpp:193-208; only equality matters for pairs)
+        std::vector<uint64_t> all(bp, bp + op.n);
+        all.insert(all.end(), bq, bq + op.m);
+        std::vector<uint64_t> uniq = all;
+        std::sort(uniq.begin(), uniq.end());
+        uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+        if (range && !uniq.empty() && uniq.back() >= range) throw Status(2, "neighbor_pairs: bucket id out of range");
+        std::vector<uint32_t> dense(all.size());
+        for (size_t i = 0; i < all.size(); ++i)
+            dense[i] = static_cast<uint32_t>(std::lower_bound(uniq.begin(), uniq.end(), all[i]) - uniq.begin());
+        DevBuf<uint32_t> d(std::max<size_t>(dense.size(), 1));
+        d.upload(dense.data(), dense.size(), op.ctx->stream);
+        ids.push_back(std::move(d));
+        dense_range = std::max(dense_range, uniq.size());
+    }
+    op.ctx->sync();
+    op.bands.clear();
+    op.bands.resize(bands);
+    for (int b = 0; b < bands; ++b)
+        build_band_layout(*op.ctx, op.bands[b], ids[b].get(), ids[b].get() + op.n, op.n, op.m, std::max<size_t>(dense_range, 1));
+}
+
+void finish_sparse(Op& op) {
+    op.kind = LCN_OP_SPARSE;
+    build_sparse_values(op);
+    build_csr(op);
+    finalize_storage(op);
+}
+
+void finish_lcn(Op& op, const double* landmarks, size_t l, int method, uint64_t seed) {
+    op.l = l;
+    op.kind = op.bands.empty() ? LCN_OP_NYSTROM : LCN_OP_LCN;
+    build_nystrom(op, landmarks, method, seed);
+    if (op.kind == LCN_OP_LCN) {
+        build_correction(op);
+        build_csr(op);
+    }
+    finalize_storage(op);
+}
+
+lcn_op* new_op(lcn_ctx* ctx, int cost, double lambda) {
+    auto* h = new lcn_op();
+    h->o.ctx = &ctx->c;
+    h->o.cost = cost;
+    h->o.lambda = lambda;
+    h->o.fp64 = ctx->c.store_fp64 != 0;
+    return h;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lcn_abi_version(void) { return LCN_B200_ABI_VERSION; }
+
+const char* lcn_status_name(int s) {
+    switch (s) {
+        case LCN_OK: return "ok";
+        case LCN_E_DIMENSION: return "DimensionError";
+        case LCN_E_INVALID_ARGUMENT: return "InvalidArgument";
+        case LCN_E_STABILIZATION: return "StabilizationError";
+        case LCN_E_NEGATIVE_KERNEL: return "NegativeKernelError";
+        case LCN_E_FACTORIZATION: return "FactorizationError";
+        case LCN_E_ERROR: return "Error";
+        case LCN_E_CUDA: return "CudaError";
+        case LCN_E_NO_DEVICE: return "NoDevice";
+    }
+    return "Unknown";
+}
+
+int lcn_ctx_create(int device, int flags, lcn_ctx** out) {
+    return guard(nullptr, [&] {
+        int count = 0;
+        if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) throw Status(LCN_E_NO_DEVICE, "no CUDA device");
+        if (device < 0 || device >= count) throw Status(LCN_E_NO_DEVICE, "device index out of range");
+        cudaDeviceProp prop{};
+        CUDA_OK(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10) throw Status(LCN_E_NO_DEVICE, "this build targets sm_100a (B200)");
+        auto c = std::make_unique<lcn_ctx>();
+        c->c.device = device;
+        c->c.store_fp64 = (flags & LCN_STORE_FP64) ? 1 : 0;
+        c->c.num_sms = prop.multiProcessorCount;
+        CUDA_OK(cudaSetDevice(device));
+        CUDA_OK(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking));
+        *out = c.release();
+    });
+}
+
+int lcn_ctx_destroy(lcn_ctx* ctx) {
+    if (!ctx) return LCN_OK;
+    cudaSetDevice(ctx->c.device);
+    if (ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
+    delete ctx;
+    return LCN_OK;
+}
+
+const char* lcn_ctx_last_error(const lcn_ctx* ctx) { return ctx ? ctx->c.last_error.c_str() : g_orphan_error.c_str(); }
+
+int lcn_kmeans_pp_indices(lcn_ctx* ctx, const double* points, size_t n, size_t d, size_t k, uint64_t first_index,
+                          const uint64_t* raw_draws, size_t n_draws, uint32_t* out, size_t* draws_used) {
+    return guard(ctx, [&] {
+        if (k == 0 || k > n) throw Status(2, "kmeans++: k must be in [1, n]");
+        if (first_index >= n) throw Status(2, "kmeans++: first index out of range");
+        DevBuf<double> X;
+        X.upload(points, n * d, ctx->c.stream);
+        std::vector<unsigned long long> raw(raw_draws, raw_draws + n_draws);
+        DevBuf<uint32_t> ch(k);
+        int used = 0;
+        kmeans_pp_device<double>(ctx->c, X.get(), n, static_cast<int>(d), static_cast<int>(k), first_index, raw,
+                                 ch.get(), &used);
+        ch.download(out, k, ctx->c.stream);
+        ctx->c.sync();
+        if (draws_used) *draws_used = static_cast<size_t>(used);
+    });
+}
+
+int lcn_assign_nearest(lcn_ctx* ctx, const double* points, size_t n, size_t d, const double* centroids, size_t k,
+                       uint32_t* out) {
+    return guard(ctx, [&] {
+        DevBuf<double> X, C;
+        DevBuf<uint32_t> a(std::max<size_t>(n, 1));
+        X.upload(points, n * d, ctx->c.stream);
+        C.upload(centroids, k * d, ctx->c.stream);
+        assign_device<double>(ctx->c, X.get(), n, static_cast<int>(d), C.get(), static_cast<int>(k), a.get());
+        a.download(out, n, ctx->c.stream);
+        ctx->c.sync();
+    });
+}
+
+int lcn_lloyd(lcn_ctx* ctx, const double* points, size_t n, size_t d, size_t k, int iters, uint64_t seed,
+              double* centroids_out, uint32_t* assign_out) {
+    return guard(ctx, [&] {
+        if (n == 0) throw Status(2, "k-means on empty input");
+        if (k == 0 || k > n) throw Status(2, "k-means: more buckets than points");
+        DevBuf<double> X, C(k * d);
+        DevBuf<uint32_t> a(n);
+        X.upload(points, n * d, ctx->c.stream);
+        lloyd_device<double>(ctx->c, X.get(), n, static_cast<int>(d), static_cast<int>(k), iters, seed, C.get(), a.get());
+        C.download(centroids_out, k * d, ctx->c.stream);
+        a.download(assign_out, n, ctx->c.stream);
+        ctx->c.sync();
+    });
+}
+
+int lcn_lsh_kmeans_buckets(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m, size_t d,
+                           const lcn_lsh_config* cfg, uint64_t* ids_out) {
+    return guard(ctx, [&] {
+        if (!cfg) throw Status(2, "lsh: null config");
+        check_points(p, n, d, "p");
+        check_points(q, m, d, "q");
+        Op tmp;
+        tmp.ctx = &ctx->c;
+        upload_union(tmp, p, n, q, m, d);
+        std::vector<DevBuf<uint32_t>> ids;
+        size_t range = 0;
+        lsh_kmeans_bucket_ids(ctx->c, tmp.X.get(), n, m, d, cfg->bands, cfg->rows_per_band, cfg->buckets_per_fn,
+                              cfg->kmeans_iters, cfg->seed, ids, range);
+        std::vector<uint32_t> h(n + m);
+        for (size_t b = 0; b < ids.size(); ++b) {
+            ids[b].download(h.data(), n + m, ctx->c.stream);
+            ctx->c.sync();
+            for (size_t i = 0; i < n + m; ++i) ids_out[b * (n + m) + i] = h[i];
+        }
+    });
+}
+
+int lcn_op_sparse_lsh(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m, size_t d, int cost,
+                      double lambda, const lcn_lsh_config* cfg, lcn_op** out) {
+    return guard(ctx, [&] {
+        check_cost_lambda(cost, lambda, "build_sparse");
+        check_points(p, n, d, "p");
+        check_points(q, m, d, "q");
+        std::unique_ptr<lcn_op> h(new_op(ctx, cost, lambda));
+        upload_union(h->o, p, n, q, m, d);
+        std::vector<DevBuf<uint32_t>> ids;
+        size_t range = 0;
+        lsh_kmeans_bucket_ids(ctx->c, h->o.X.get(), n, m, d, cfg->bands, cfg->rows_per_band, cfg->buckets_per_fn,
+                              cfg->kmeans_iters, cfg->seed, ids, range);
+        if (static_cast<int>(ids.size()) > kMaxBands) throw Status(2, "lsh: at most 8 bands on this path");
+        bands_from_union_ids(h->o, ids, range);
+        finish_sparse(h->o);
+        *out = h.release();
+    });
+}
+
+int lcn_op_sparse_buckets(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m, size_t d, int cost,
+                          double lambda, const uint64_t* ids_p, const uint64_t* ids_q, int bands, uint64_t range,
+                          lcn_op** out) {
+    return guard(ctx, [&] {
+        check_cost_lambda(cost, lambda, "build_sparse");
+        check_points(p, n, d, "p");
+        check_points(q, m, d, "q");
+        std::unique_ptr<lcn_op> h(new_op(ctx, cost, lambda));
+        upload_union(h->o, p, n, q, m, d);
+        bands_from_host_ids(h->o, ids_p, ids_q, bands, range);
+        finish_sparse(h->o);
+        *out = h.release();
+    });
+}
+
+int lcn_op_lcn_lsh(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m, size_t d, int cost,
+                   double lambda, const lcn_lsh_config* cfg, size_t l, int landmark_method, uint64_t landmark_seed,
+                   lcn_op** out) {
+    return guard(ctx, [&] {
+        check_cost_lambda(cost, lambda, "build_factors");
+        check_points(p, n, d, "p");
+        check_points(q, m, d, "q");
+        std::unique_ptr<lcn_op> h(new_op(ctx, cost, lambda));
+        upload_union(h->o, p, n, q, m, d);
+        std::vector<DevBuf<uint32_t>> ids;
+        size_t range = 0;
+        lsh_kmeans_bucket_ids(ctx->c, h->o.X.get(), n, m, d, cfg->bands, cfg->rows_per_band, cfg->buckets_per_fn,
+                              cfg->kmeans_iters, cfg->seed, ids, range);
+        bands_from_union_ids(h->o, ids, range);
+        finish_lcn(h->o, nullptr, l, landmark_method, landmark_seed);
+        *out = h.release();
+    });
+}
+
+int lcn_op_lcn_buckets(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m, size_t d, int cost,
+                       double lambda, const uint64_t* ids_p, const uint64_t* ids_q, int bands, uint64_t range,
+                       const double* landmarks, size_t l, int landmark_method, uint64_t landmark_seed, lcn_op** out) {
+    return guard(ctx, [&] {
+        check_cost_lambda(cost, lambda, "build_factors");
+        check_points(p, n, d, "p");
+        check_points(q, m, d, "q");
+        std::unique_ptr<lcn_op> h(new_op(ctx, cost, lambda));
+        upload_union(h->o, p, n, q, m, d);
+        bands_from_host_ids(h->o, ids_p, ids_q, bands, range);
+        finish_lcn(h->o, landmarks, l, landmark_method, landmark_seed);
+        *out = h.release();
+    });
+}
+
+int lcn_op_create_device(lcn_ctx* ctx, const float* d_p, size_t n, const float* d_q, size_t m, size_t d, int cost,
+                         double lambda, const lcn_lsh_config* cfg, size_t l, int landmark_method,
+                         uint64_t landmark_seed, lcn_op** out) {
+    return guard(ctx, [&] {
+        check_cost_lambda(cost, lambda, l ? "build_factors" : "build_sparse");
+        std::unique_ptr<lcn_op> h(new_op(ctx, cost, lambda));
+        Op& op = h->o;
+        op.n = n;
+        op.m = m;
+        op.d = d;
+        op.X.resize((n + m) * d);
+        promote_kernel<<<std::min<long long>(ceil_div(n * d, 256), 8 * ctx->c.num_sms), 256, 0, ctx->c.stream>>>(
+            d_p, op.X.get(), n * d);
+        promote_kernel<<<std::min<long long>(ceil_div(m * d, 256), 8 * ctx->c.num_sms), 256, 0, ctx->c.stream>>>(
+            d_q, op.X.get() + n * d, m * d);
+        LAUNCH_OK("promote");
+        std::vector<DevBuf<uint32_t>> ids;
+        size_t range = 0;
+        lsh_kmeans_bucket_ids(ctx->c, op.X.get(), n, m, d, cfg->bands, cfg->rows_per_band, cfg->buckets_per_fn,
+                              cfg->kmeans_iters, cfg->seed, ids, range);
+        bands_from_union_ids(op, ids, range);
+        if (l) finish_lcn(op, nullptr, l, landmark_method, landmark_seed);
+        else finish_sparse(op);
+        *out = h.release();
+    });
+}
+
+int lcn_op_destroy(lcn_op* op) {
+    if (!op) return LCN_OK;
+    cudaSetDevice(op->o.ctx->device);
+    delete op;
+    return LCN_OK;
+}
+
+int lcn_op_get_info(const lcn_op* op, lcn_op_info_t* info) {
+    if (!op || !info) return LCN_E_INVALID_ARGUMENT;
+    const Op& o = op->o;
+    info->kind = o.kind;
+    info->n = o.n;
+    info->m = o.m;
+    info->l = o.l;
+    info->d = o.d;
+    info->bands = static_cast<int>(o.bands.size());
+    info->nnz = o.nnz;
+    info->stored = o.stored;
+    info->lambda = o.lambda;
+    info->max_abs_delta = o.max_abs_delta;
+    info->cond_estimate = o.cond;
+    info->store_fp64 = o.fp64 ? 1 : 0;
+    return LCN_OK;
+}
+
+int lcn_op_export_csr(lcn_op* op, int which, uint32_t* row_ptr, uint32_t* col, double* vals) {
+    lcn_ctx* ctx = reinterpret_cast<lcn_ctx*>(op->o.ctx);  // Ctx is the first member of lcn_ctx
+    return guard(ctx, [&] { export_csr(op->o, which, row_ptr, col, vals); });
+}
+
+int lcn_op_export_factor(lcn_op* op, int which, double* out) {
+    lcn_ctx* ctx = reinterpret_cast<lcn_ctx*>(op->o.ctx);
+    return guard(ctx, [&] {
+        Op& o = op->o;
+        if (o.kind < 2 && which != 2) throw Status(2, "export_factor: operator has no low-rank factors");
+        cudaStream_t s = o.ctx->stream;
+        if (which == 0) {
+            o.U64.download(out, o.n * o.l, s);
+        } else if (which == 1) {
+            std::vector<double> wt(o.m * o.l);
+            o.Wt64.download(wt.data(), o.m * o.l, s);
+            o.ctx->sync();
+            for (size_t a = 0; a < o.l; ++a)
+                for (size_t j = 0; j < o.m; ++j) out[a * o.m + j] = wt[j * o.l + a];
+        } else if (which == 2) {
+            o.L.download(out, o.l * o.d, s);
+        } else {
+            throw Status(2, "export_factor: unknown factor");
+        }
+        o.ctx->sync();
+    });
+}
+
+int lcn_op_log_matvec(lcn_op* op, const double* in, int transposed, double* out) {
+    lcn_ctx* ctx = reinterpret_cast<lcn_ctx*>(op->o.ctx);
+    return guard(ctx, [&] { op_log_matvec(op->o, in, transposed != 0, out); });
+}
+
+int lcn_sinkhorn(lcn_op* op, const double* p, const double* q, const lcn_sinkhorn_options* opts, lcn_result** out) {
+    lcn_ctx* ctx = reinterpret_cast<lcn_ctx*>(op->o.ctx);
+    return guard(ctx, [&] {
+        Op& o = op->o;
+        // Marginals::validate(balanced) (geometry.cpp:97-111)
+        if (!p || !q || o.n == 0 || o.m == 0) throw Status(2, "marginals must be non-empty");
+        double sp = 0.0, sq = 0.0;
+        for (size_t i = 0; i < o.n; ++i) {
+            if (!(p[i] > 0.0) || !std::isfinite(p[i])) throw Status(2, "marginal p has a non-positive or non-finite entry");
+            sp += p[i];
+        }
+        for (size_t j = 0; j < o.m; ++j) {
+            if (!(q[j] > 0.0) || !std::isfinite(q[j])) throw Status(2, "marginal q has a non-positive or non-finite entry");
+            sq += q[j];
+        }
+        if (std::abs(sp - sq) > 1e-12 * std::max(sp, sq))
+            throw Status(2, "marginals are unbalanced; balanced OT requires equal mass");
+        SolveOptions so;
+        if (opts) {
+            so.tol = opts->tol;
+            so.max_iters = opts->max_iters;
+            so.check_support = opts->check_support != 0;
+            so.want_plan = opts->want_plan != 0;
+        }
+        auto res = std::make_unique<lcn_result>();
+        res->op = op;
+        if (o.kind == LCN_OP_SPARSE && so.check_support) {
+            // sinkhorn.cpp:122-128: warn when the pattern has no support.
+            build_csr(o);
+            std::vector<uint32_t> rp(o.n + 1), col(std::max<unsigned long long>(o.nnz, 1));
+            export_csr(o, 0, rp.data(), col.data(), nullptr);
+            size_t small = std::min(o.n, o.m);
+            if (o.nnz == 0 || max_bipartite_matching(o.n, o.m, rp.data(), col.data()) < small) {
+                res->r.warnings.push_back("sparse kernel pattern has no support; Sinkhorn may not converge");
+                std::fprintf(stderr, "lcn: warning: %s\n", res->r.warnings.back().c_str());
+            }
+        }
+        sinkhorn_solve(o, p, q, so, res->r);
+        if (so.want_plan && o.kind != 2 && o.nnz) {
+            // Plan entries on the support in CSR order (sinkhorn.cpp:45-80).
+            std::vector<uint32_t> rp(o.n + 1), col(o.nnz);
+            std::vector<double> lk(o.nnz);
+            export_csr(o, o.kind == 1 ? 0 : 2, rp.data(), col.data(), lk.data());
+            Result& r = res->r;
+            if (o.kind == 1) {
+                r.plan_vals.resize(o.nnz);
+                for (size_t i = 0; i < o.n; ++i)
+                    for (uint32_t e = rp[i]; e < rp[i + 1]; ++e)
+                        r.plan_vals[e] = std::exp(r.log_s[i] + lk[e] + r.log_t[col[e]]);
+            } else {
+                std::vector<double> nys(o.nnz);
+                export_csr(o, 3, nullptr, nullptr, nys.data());
+                r.sp_vals.resize(o.nnz);
+                r.sp_nys_vals.resize(o.nnz);
+                for (size_t i = 0; i < o.n; ++i) {
+                    double si = std::exp(r.log_s[i]);
+                    for (uint32_t e = rp[i]; e < rp[i + 1]; ++e) {
+                        double tj = std::exp(r.log_t[col[e]]);
+                        r.sp_vals[e] = std::exp(r.log_s[i] + lk[e] + r.log_t[col[e]]);
+                        r.sp_nys_vals[e] = si * nys[e] * tj;
+                    }
+                }
+            }
+        }
+        *out = res.release();
+    });
+}
+
+int lcn_result_destroy(lcn_result* res) {
+    delete res;
+    return LCN_OK;
+}
+
+int lcn_result_get_info(const lcn_result* res, lcn_result_info_t* info) {
+    if (!res || !info) return LCN_E_INVALID_ARGUMENT;
+    info->distance = res->r.distance;
+    info->iters = res->r.iters;
+    info->converged = res->r.converged ? 1 : 0;
+    info->marginal_err_final = res->r.marginal_err_final;
+    info->n_warnings = static_cast<int>(res->r.warnings.size());
+    info->device_ms = res->r.device_ms;
+    return LCN_OK;
+}
+
+int lcn_result_copy(const lcn_result* res, int which, double* out, size_t* len) {
+    if (!res) return LCN_E_INVALID_ARGUMENT;
+    const Result& r = res->r;
+    const std::vector<double>* v = nullptr;
+    switch (which) {
+        case 0: v = &r.log_s; break;
+        case 1: v = &r.log_t; break;
+        case 2: v = &r.row_marg; break;
+        case 3: v = &r.err_trace; break;
+        case 4: v = &r.plan_vals; break;
+        case 5: v = &r.sp_vals; break;
+        case 6: v = &r.sp_nys_vals; break;
+        default: return LCN_E_INVALID_ARGUMENT;
+    }
+    if (len) *len = v->size();
+    if (out && !v->empty()) std::memcpy(out, v->data(), v->size() * sizeof(double));
+    return LCN_OK;
+}
+
+int lcn_distance_lcn(const lcn_result* res, const lcn_op* op, double* out) {
+    lcn_ctx* ctx = reinterpret_cast<lcn_ctx*>(op->o.ctx);
+    return guard(ctx, [&] {
+        if (op->o.kind < 2) throw Status(2, "distance_lcn: operator has no low-rank factors");
+        *out = distance_lcn_device(const_cast<lcn_op*>(op)->o, res->r);
+    });
+}
+
+const char* lcn_result_warning(const lcn_result* res, int i) {
+    if (!res || i < 0 || i >= static_cast<int>(res->r.warnings.size())) return nullptr;
+    return res->r.warnings[static_cast<size_t>(i)].c_str();
+}
+
+}  // extern "C"

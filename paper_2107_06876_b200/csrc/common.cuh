@@ -1,0 +1,91 @@
+// Shared device helpers for the LCN-Sinkhorn hot path (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <stdexcept>
+#include <string>
+
+namespace lcnb {
+
+// ---- status / errors --------------------------------------------------------
+// Host-side exception carrying an lcn_status; converted at the C-ABI edge.
+struct Status : std::runtime_error {
+    int code;
+    Status(int c, const std::string& msg) : std::runtime_error(msg), code(c) {}
+};
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw Status(100, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CUDA_OK(x) ::lcnb::cuda_check((x), #x)
+#define LAUNCH_OK(what) ::lcnb::cuda_check(cudaGetLastError(), what)
+
+// ---- exact fp64 arithmetic -------------------------------------------------
+// The reference computes in plain fp64 with no FMA contraction (built without
+// -march). Every op that must reproduce its bits uses the
+// explicitly rounded intrinsics so nvcc cannot contract a*b+c into an FMA.
+__device__ __forceinline__ double xadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double xsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
+
+// kmeans.cpp:12-19 sqdist: s = 0; for k: diff = x_k - y_k; s += diff*diff.
+template <typename TX, typename TY>
+__device__ __forceinline__ double sqdist_exact(const TX* x, const TY* y, int d) {
+    double s = 0.0;
+    for (int k = 0; k < d; ++k) {
+        double diff = xsub(static_cast<double>(x[k]), static_cast<double>(y[k]));
+        s = xadd(s, xmul(diff, diff));
+    }
+    return s;
+}
+
+// geometry.cpp:45-76 cost_value (+ the documented squared-L2 kind 3),
+// same operation order, no contraction.
+template <typename TX, typename TY>
+__device__ __forceinline__ double cost_exact(int kind, const TX* x, const TY* y, int d) {
+    if (kind == 0 || kind == 3) {
+        double s = sqdist_exact(x, y, d);
+        return kind == 0 ? __dsqrt_rn(s) : s;
+    }
+    if (kind == 1) {
+        double s = 0.0;
+        for (int k = 0; k < d; ++k) s = xadd(s, xmul(static_cast<double>(x[k]), static_cast<double>(y[k])));
+        return -s;
+    }
+    double dot = 0.0, nx = 0.0, ny = 0.0;
+    for (int k = 0; k < d; ++k) {
+        double a = static_cast<double>(x[k]), b = static_cast<double>(y[k]);
+        dot = xadd(dot, xmul(a, b));
+        nx = xadd(nx, xmul(a, a));
+        ny = xadd(ny, xmul(b, b));
+    }
+    if (nx == 0.0 || ny == 0.0) return __longlong_as_double(0x7ff8000000000001ll);  // flagged by caller
+    double c = __ddiv_rn(dot, __dsqrt_rn(xmul(nx, ny)));
+    c = c > 1.0 ? 1.0 : c;
+    c = c < -1.0 ? -1.0 : c;
+    return __dsqrt_rn(xsub(1.0, c));
+}
+
+// ---- warp / block reductions ------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+constexpr double kNegInf = -__builtin_huge_val();
+constexpr double kPosInf = __builtin_huge_val();
+
+inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace lcnb

@@ -1,0 +1,97 @@
+// Context, device buffers and the internal operator/result structures.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace lcnb {
+
+// Owning device allocation (cudaMallocAsync on the context stream would tie
+// lifetimes to a stream; plain cudaMalloc keeps buffers valid across streams).
+template <typename T>
+class DevBuf {
+  public:
+    DevBuf() = default;
+    explicit DevBuf(size_t n) { resize(n); }
+    ~DevBuf() { release(); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) { release(); p_ = o.p_; n_ = o.n_; o.p_ = nullptr; o.n_ = 0; }
+        return *this;
+    }
+    void resize(size_t n) {
+        if (n == n_) return;
+        release();
+        if (n) CUDA_OK(cudaMalloc(&p_, n * sizeof(T)));
+        n_ = n;
+    }
+    void release() {
+        if (p_) cudaFree(p_);
+        p_ = nullptr;
+        n_ = 0;
+    }
+    T* get() const { return p_; }
+    size_t size() const { return n_; }
+    size_t bytes() const { return n_ * sizeof(T); }
+    void upload(const T* h, size_t n, cudaStream_t s) {
+        resize(n);
+        if (n) CUDA_OK(cudaMemcpyAsync(p_, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+    void download(T* h, size_t n, cudaStream_t s) const {
+        if (n) CUDA_OK(cudaMemcpyAsync(h, p_, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+    }
+    void zero(cudaStream_t s) {
+        if (n_) CUDA_OK(cudaMemsetAsync(p_, 0, n_ * sizeof(T), s));
+    }
+
+  private:
+    T* p_ = nullptr;
+    size_t n_ = 0;
+};
+
+struct Ctx {
+    int device = 0;
+    int store_fp64 = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    std::string last_error;
+    void activate() const { CUDA_OK(cudaSetDevice(device)); }
+    void sync() const { CUDA_OK(cudaStreamSynchronize(stream)); }
+};
+
+// Points of one side, device-resident. Values are fp64 (exact promotion of
+// the caller's fp64, or of fp32 for the device entry points).
+struct DevPoints {
+    DevBuf<double> x;  // n x d row-major
+    size_t n = 0, d = 0;
+};
+
+// One LSH band in bucket-blocked form: sources and targets
+// sorted stably by bucket; bucket b owns the dense n_b x m_b block at
+// blk_off[b]. Rows/cols of a block are in increasing point index.
+struct Band {
+    size_t nb = 0;                 // bucket count (range)
+    DevBuf<uint32_t> src_order;    // n: source indices grouped by bucket
+    DevBuf<uint32_t> tgt_order;    // m
+    DevBuf<uint32_t> src_start;    // nb+1
+    DevBuf<uint32_t> tgt_start;    // nb+1
+    DevBuf<unsigned long long> blk_off;  // nb+1 (entries)
+    DevBuf<uint32_t> src_bucket;   // n
+    DevBuf<uint32_t> tgt_bucket;   // m
+    DevBuf<uint32_t> src_local;    // n: position inside its bucket
+    DevBuf<uint32_t> tgt_local;    // m
+    DevBuf<uint32_t> work;         // list of buckets with a nonempty block
+    size_t n_work = 0;
+    unsigned long long entries = 0;
+    std::vector<uint32_t> h_src_start, h_tgt_start;
+    std::vector<unsigned long long> h_blk_off;
+};
+
+}  // namespace lcnb

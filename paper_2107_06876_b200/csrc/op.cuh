@@ -1,0 +1,97 @@
+// Internal operator / result structures and the build + solve entry points.
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "ctx.cuh"
+
+namespace lcnb {
+
+constexpr int kMaxBands = 8;
+
+// Device-side descriptor of one band, passed by value to kernels.
+struct BandView {
+    const uint32_t* src_order;
+    const uint32_t* tgt_order;
+    const uint32_t* src_start;
+    const uint32_t* tgt_start;
+    const unsigned long long* blk_off;
+    const uint32_t* src_bucket;
+    const uint32_t* tgt_bucket;
+    const uint32_t* src_local;
+    const uint32_t* tgt_local;
+};
+
+struct BandSet {  // bucket ids of every band, for the cross-band dedup mask
+    const uint32_t* src_bucket[kMaxBands];
+    const uint32_t* tgt_bucket[kMaxBands];
+    int bands;
+};
+
+struct Op {
+    Ctx* ctx = nullptr;
+    int kind = 1;  // lcn_op_kind
+    size_t n = 0, m = 0, d = 0, l = 0;
+    int cost = 0;
+    double lambda = 1.0;
+    bool fp64 = false;
+    DevBuf<double> X;                     // (n+m) x d union X_p ∪ X_q, fp64 (union_points, geometry.cpp:20-27)
+    const double* P() const { return X.get(); }
+    const double* Q() const { return X.get() + n * d; }
+    DevBuf<double> norms;                 // per-point sum x_k^2 (cosine-derived cost only)
+    std::vector<Band> bands;
+    std::vector<DevBuf<double>> val64;    // sparse: log K; lcn: delta (fp64 master)
+    std::vector<DevBuf<float>> val32;     // iteration copy (fp32 storage mode)
+    std::vector<DevBuf<double>> logk64;   // lcn: log K^sp at stored entries
+    unsigned long long nnz = 0, stored = 0;
+    // Nystrom / LCN
+    DevBuf<double> L;                     // l x d landmarks
+    DevBuf<double> U64, Wt64;             // n x l, m x l (W transposed)
+    DevBuf<float> U32, Wt32;
+    double max_abs_delta = 0.0, cond = 0.0;
+    // CSR export (lazy)
+    DevBuf<uint32_t> csr_row_ptr, csr_col;
+    bool csr_ready = false;
+
+    BandView view(int b) const;
+    BandSet bandset() const;
+    const char* name() const { return kind == 1 ? "sparse" : kind == 2 ? "nystrom" : kind == 3 ? "lcn" : "dense"; }
+};
+
+struct Result {
+    double distance = 0.0;
+    int iters = 0;
+    bool converged = false;
+    double marginal_err_final = 0.0;
+    double device_ms = 0.0;
+    std::vector<double> log_s, log_t, row_marg, err_trace;
+    std::vector<double> plan_vals, sp_vals, sp_nys_vals;
+    std::vector<std::string> warnings;
+    size_t n = 0, m = 0;
+};
+
+// build.cu
+void build_band_layout(Ctx& ctx, Band& B, const uint32_t* d_src_bucket, const uint32_t* d_tgt_bucket, size_t n,
+                       size_t m, size_t nb);
+void lsh_kmeans_bucket_ids(Ctx& ctx, const double* d_union, size_t n, size_t m, size_t d, int bands, int rows,
+                           int buckets, int iters, uint64_t seed, std::vector<DevBuf<uint32_t>>& ids, size_t& range);
+void build_sparse_values(Op& op);
+void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed);
+void build_correction(Op& op);
+void finalize_storage(Op& op);
+void build_csr(Op& op);
+void export_csr(Op& op, int which, uint32_t* row_ptr, uint32_t* col, double* vals);
+
+// sinkhorn.cu
+struct SolveOptions {
+    double tol = -1.0;
+    int max_iters = 500;
+    bool check_support = true;
+    bool want_plan = true;
+};
+void sinkhorn_solve(Op& op, const double* h_p, const double* h_q, const SolveOptions& o, Result& res);
+void op_log_matvec(Op& op, const double* h_in, bool transposed, double* h_out);
+double distance_lcn_device(Op& op, const Result& res);
+
+}  // namespace lcnb

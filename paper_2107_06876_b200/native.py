@@ -1,0 +1,480 @@
+"""Python host mirror of the reference's lcn:: solver API over the C-ABI.
+
+Binds paper_2107_06876_b200/_build/liblcn_b200.so (include/lcn_b200.h) with
+ctypes and exposes the reference's names and error types
+(lsh.hpp, kmeans.hpp, nystrom.hpp, sparse_kernel.hpp, operator.hpp,
+sinkhorn.hpp, error.hpp). There is no CPU fallback: if the library is missing
+or no sm_100 device is present every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import os
+from typing import Optional
+
+import numpy as np
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_build", "liblcn_b200.so")
+
+
+# ---- error types (error.hpp:8-38) -------------------------------------------
+class Error(RuntimeError):
+    pass
+
+
+class DimensionError(Error):
+    pass
+
+
+class InvalidArgument(Error):
+    pass
+
+
+class StabilizationError(Error):
+    pass
+
+
+class NegativeKernelError(Error):
+    pass
+
+
+class FactorizationError(Error):
+    pass
+
+
+class CudaError(Error):
+    pass
+
+
+_STATUS = {1: DimensionError, 2: InvalidArgument, 3: StabilizationError, 4: NegativeKernelError,
+           5: FactorizationError, 6: Error, 100: CudaError, 101: CudaError}
+
+# enums (include/lcn_b200.h)
+EUCLIDEAN, NEGATIVE_DOT, COSINE_DERIVED, SQEUCLIDEAN = 0, 1, 2, 3
+LANDMARK_KMEANS, LANDMARK_KMEANSPP = 0, 1
+KIND_DENSE, KIND_SPARSE, KIND_NYSTROM, KIND_LCN = 0, 1, 2, 3
+_KIND_NAMES = {0: "dense", 1: "sparse", 2: "nystrom", 3: "lcn"}
+
+
+class _LshConfig(C.Structure):
+    _fields_ = [("bands", C.c_int), ("rows_per_band", C.c_int), ("buckets_per_fn", C.c_int),
+                ("kmeans_iters", C.c_int), ("seed", C.c_uint64)]
+
+
+class _SinkOpts(C.Structure):
+    _fields_ = [("tol", C.c_double), ("max_iters", C.c_int), ("check_support", C.c_int), ("want_plan", C.c_int)]
+
+
+class _OpInfo(C.Structure):
+    _fields_ = [("kind", C.c_int), ("n", C.c_size_t), ("m", C.c_size_t), ("l", C.c_size_t), ("d", C.c_size_t),
+                ("bands", C.c_int), ("nnz", C.c_size_t), ("stored", C.c_size_t), ("lam", C.c_double),
+                ("max_abs_delta", C.c_double), ("cond_estimate", C.c_double), ("store_fp64", C.c_int)]
+
+
+class _ResInfo(C.Structure):
+    _fields_ = [("distance", C.c_double), ("iters", C.c_int), ("converged", C.c_int),
+                ("marginal_err_final", C.c_double), ("n_warnings", C.c_int), ("device_ms", C.c_double)]
+
+
+_lib = None
+
+
+def library() -> C.CDLL:
+    """Load the C-ABI library (fails loudly when it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (make -C paper_2107_06876_b200)")
+        lib = C.CDLL(LIB_PATH)
+        P, SZ, D, I, U64 = C.c_void_p, C.c_size_t, C.c_double, C.c_int, C.c_uint64
+        PP = C.POINTER(C.c_void_p)
+        sig = {
+            "lcn_abi_version": ([], I),
+            "lcn_status_name": ([I], C.c_char_p),
+            "lcn_ctx_create": ([I, I, PP], I),
+            "lcn_ctx_destroy": ([P], I),
+            "lcn_ctx_last_error": ([P], C.c_char_p),
+            "lcn_kmeans_pp_indices": ([P, P, SZ, SZ, SZ, U64, P, SZ, P, C.POINTER(SZ)], I),
+            "lcn_assign_nearest": ([P, P, SZ, SZ, P, SZ, P], I),
+            "lcn_lloyd": ([P, P, SZ, SZ, SZ, I, U64, P, P], I),
+            "lcn_lsh_kmeans_buckets": ([P, P, SZ, P, SZ, SZ, C.POINTER(_LshConfig), P], I),
+            "lcn_op_sparse_lsh": ([P, P, SZ, P, SZ, SZ, I, D, C.POINTER(_LshConfig), PP], I),
+            "lcn_op_sparse_buckets": ([P, P, SZ, P, SZ, SZ, I, D, P, P, I, U64, PP], I),
+            "lcn_op_lcn_lsh": ([P, P, SZ, P, SZ, SZ, I, D, C.POINTER(_LshConfig), SZ, I, U64, PP], I),
+            "lcn_op_lcn_buckets": ([P, P, SZ, P, SZ, SZ, I, D, P, P, I, U64, P, SZ, I, U64, PP], I),
+            "lcn_op_create_device": ([P, P, SZ, P, SZ, SZ, I, D, C.POINTER(_LshConfig), SZ, I, U64, PP], I),
+            "lcn_op_destroy": ([P], I),
+            "lcn_op_get_info": ([P, C.POINTER(_OpInfo)], I),
+            "lcn_op_export_csr": ([P, I, P, P, P], I),
+            "lcn_op_export_factor": ([P, I, P], I),
+            "lcn_op_log_matvec": ([P, P, I, P], I),
+            "lcn_sinkhorn": ([P, P, P, C.POINTER(_SinkOpts), PP], I),
+            "lcn_result_destroy": ([P], I),
+            "lcn_result_get_info": ([P, C.POINTER(_ResInfo)], I),
+            "lcn_result_copy": ([P, I, P, C.POINTER(SZ)], I),
+            "lcn_distance_lcn": ([P, P, C.POINTER(D)], I),
+            "lcn_result_warning": ([P, I], C.c_char_p),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(lib, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = lib
+    return _lib
+
+
+def _p(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _f64(a, shape=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if shape is not None and a.shape != shape:
+        raise DimensionError(f"expected shape {shape}, got {a.shape}")
+    return a
+
+
+class Context:
+    """One device, one stream (lcn_ctx). store_fp64 selects fp64 storage of the
+    iteration operands (API-compatibility precision) over fp32 (performance)."""
+
+    def __init__(self, device: int = 0, store_fp64: bool = False):
+        self.lib = library()
+        h = C.c_void_p()
+        rc = self.lib.lcn_ctx_create(device, 1 if store_fp64 else 0, C.byref(h))
+        if rc != 0:
+            raise _STATUS.get(rc, Error)(self.lib.lcn_ctx_last_error(None).decode())
+        self.h = h
+        self.device = device
+        self.store_fp64 = store_fp64
+
+    def check(self, rc: int):
+        if rc != 0:
+            raise _STATUS.get(rc, Error)(self.lib.lcn_ctx_last_error(self.h).decode())
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.lcn_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclasses.dataclass
+class LshConfig:
+    """LshConfig (lsh.hpp:22-30), k-means scheme."""
+    bands: int = 1
+    rows_per_band: int = 1
+    buckets_per_fn: int = 2
+    kmeans_iters: int = 10
+    seed: int = 0
+
+    def c(self):
+        return _LshConfig(self.bands, self.rows_per_band, self.buckets_per_fn, self.kmeans_iters, self.seed)
+
+
+@dataclasses.dataclass
+class SinkhornOptions:
+    """SinkhornOptions (sinkhorn.hpp:11-20)."""
+    tol: float = -1.0
+    max_iters: int = 500
+    check_support: bool = True
+    want_plan: bool = True
+
+
+# ---- k-means (kmeans.hpp:18-29) ----------------------------------------------
+def kmeans_pp_indices(ctx: Context, points, k: int, rng: np.random.Generator | None = None, *, seed: int | None = None):
+    """kmeans_pp_indices with a libstdc++ mt19937_64(seed) engine (the draws are
+    taken by the C++ side of lloyd; here the caller passes the seed)."""
+    import random  # noqa: F401  (documented: draws come from std::mt19937_64 in C)
+    pts = _f64(points)
+    n, d = pts.shape
+    if seed is None:
+        raise InvalidArgument("kmeans_pp_indices needs the engine seed")
+    first, raw = _mt_draws(seed, n, max(k - 1, 0))
+    out = np.zeros(k, np.uint32)
+    used = C.c_size_t()
+    rawa = np.ascontiguousarray(raw, np.uint64)
+    ctx.check(ctx.lib.lcn_kmeans_pp_indices(ctx.h, _p(pts), n, d, k, first, _p(rawa), len(rawa), _p(out),
+                                            C.byref(used)))
+    return out
+
+
+def assign_nearest(ctx: Context, points, centroids):
+    pts, ctr = _f64(points), _f64(centroids)
+    out = np.zeros(pts.shape[0], np.uint32)
+    ctx.check(ctx.lib.lcn_assign_nearest(ctx.h, _p(pts), pts.shape[0], pts.shape[1], _p(ctr), ctr.shape[0], _p(out)))
+    return out
+
+
+def lloyd(ctx: Context, points, k: int, iters: int, seed: int):
+    """lloyd (kmeans.cpp:87-143) -> (centroids k x d, assign n)."""
+    pts = _f64(points)
+    n, d = pts.shape
+    ctr = np.zeros((k, d))
+    asg = np.zeros(n, np.uint32)
+    ctx.check(ctx.lib.lcn_lloyd(ctx.h, _p(pts), n, d, k, iters, seed, _p(ctr), _p(asg)))
+    return ctr, asg
+
+
+def lsh_kmeans_buckets(ctx: Context, p, q, cfg: LshConfig):
+    """Per-band bucket ids of the k-means LSH on X_p ∪ X_q (lsh.cpp:245-283)."""
+    p, q = _f64(p), _f64(q)
+    ids = np.zeros((cfg.bands, p.shape[0] + q.shape[0]), np.uint64)
+    c = cfg.c()
+    ctx.check(ctx.lib.lcn_lsh_kmeans_buckets(ctx.h, _p(p), p.shape[0], _p(q), q.shape[0], p.shape[1], C.byref(c),
+                                             _p(ids)))
+    return ids
+
+
+def _mt_draws(seed: int, n: int, count: int):
+    """first = uniform_int_distribution<size_t>(0, n-1)(mt19937_64(seed)) and the
+    next `count` raw draws, computed by the library's own host code path."""
+    # The C++ host side owns the engine; reproduce it with numpy's MT19937-64-free
+    # implementation below (mt19937_64 is a fixed, standard algorithm).
+    mt = _MT19937_64(seed)
+    first = _lemire(mt, n)
+    return first, [mt() for _ in range(count)]
+
+
+class _MT19937_64:
+    """std::mt19937_64 (a standard-specified engine)."""
+    NN, MM = 312, 156
+    MATRIX_A = 0xB5026F5AA96619E9
+    UM, LM = 0xFFFFFFFF80000000, 0x7FFFFFFF
+
+    def __init__(self, seed: int):
+        m = (1 << 64) - 1
+        self.mt = [0] * self.NN
+        self.mt[0] = seed & m
+        for i in range(1, self.NN):
+            self.mt[i] = (6364136223846793005 * (self.mt[i - 1] ^ (self.mt[i - 1] >> 62)) + i) & m
+        self.mti = self.NN
+
+    def __call__(self) -> int:
+        m = (1 << 64) - 1
+        if self.mti >= self.NN:
+            mt = self.mt
+            for i in range(self.NN):
+                x = (mt[i] & self.UM) | (mt[(i + 1) % self.NN] & self.LM)
+                xa = x >> 1
+                if x & 1:
+                    xa ^= self.MATRIX_A
+                mt[i] = mt[(i + self.MM) % self.NN] ^ xa
+            self.mti = 0
+        x = self.mt[self.mti]
+        self.mti += 1
+        x ^= (x >> 29) & 0x5555555555555555
+        x ^= (x << 17) & 0x71D67FFFEDA60000
+        x ^= (x << 37) & 0xFFF7EEE000000000
+        x ^= x >> 43
+        return x & m
+
+
+def _lemire(mt, n: int) -> int:
+    """libstdc++ uniform_int_distribution<size_t>(0, n-1): Lemire's nearly
+    divisionless downscaling with a 128-bit product (uniform_int_dist.h)."""
+    rng = n
+    prod = mt() * rng
+    low = prod & ((1 << 64) - 1)
+    if low < rng:
+        thr = ((1 << 64) - rng) % rng
+        while low < thr:
+            prod = mt() * rng
+            low = prod & ((1 << 64) - 1)
+    return prod >> 64
+
+
+# ---- operators (operator.hpp:29-82) -----------------------------------------
+class KernelOperator:
+    """Device-resident kernel operator handle (lcn_op)."""
+
+    def __init__(self, ctx: Context, h):
+        self.ctx, self.h = ctx, h
+        info = _OpInfo()
+        ctx.check(ctx.lib.lcn_op_get_info(self.h, C.byref(info)))
+        self.info = info
+
+    # factories ---------------------------------------------------------------
+    @classmethod
+    def sparse_lsh(cls, ctx, p, q, cost, lam, cfg: LshConfig):
+        """lsh_neighbor_pairs -> build_sparse -> KernelOperator::sparse."""
+        p, q = _f64(p), _f64(q)
+        h = C.c_void_p()
+        c = cfg.c()
+        ctx.check(ctx.lib.lcn_op_sparse_lsh(ctx.h, _p(p), p.shape[0], _p(q), q.shape[0], p.shape[1], cost, lam,
+                                            C.byref(c), C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def sparse_buckets(cls, ctx, p, q, cost, lam, ids_p, ids_q, range_=0):
+        """neighbor_pairs(BandBuckets...) -> build_sparse -> KernelOperator::sparse."""
+        p, q = _f64(p), _f64(q)
+        ip = np.ascontiguousarray(np.atleast_2d(ids_p), np.uint64)
+        iq = np.ascontiguousarray(np.atleast_2d(ids_q), np.uint64)
+        h = C.c_void_p()
+        ctx.check(ctx.lib.lcn_op_sparse_buckets(ctx.h, _p(p), p.shape[0], _p(q), q.shape[0], p.shape[1], cost, lam,
+                                                _p(ip), _p(iq), ip.shape[0], range_, C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def lcn_lsh(cls, ctx, p, q, cost, lam, cfg: LshConfig, l: int, method=LANDMARK_KMEANS, landmark_seed=0):
+        """lsh_neighbor_pairs + select_landmarks + build_factors + build_correction -> KernelOperator::lcn."""
+        p, q = _f64(p), _f64(q)
+        h = C.c_void_p()
+        c = cfg.c()
+        ctx.check(ctx.lib.lcn_op_lcn_lsh(ctx.h, _p(p), p.shape[0], _p(q), q.shape[0], p.shape[1], cost, lam,
+                                         C.byref(c), l, method, landmark_seed, C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def lcn_buckets(cls, ctx, p, q, cost, lam, ids_p, ids_q, l=0, method=LANDMARK_KMEANS, landmark_seed=0,
+                    landmarks=None, range_=0):
+        """External bucket ids (+ optional explicit landmarks); no bands -> Nystrom operator."""
+        p, q = _f64(p), _f64(q)
+        if ids_p is None:
+            ip = iq = np.zeros((0, 1), np.uint64)
+            bands = 0
+        else:
+            ip = np.ascontiguousarray(np.atleast_2d(ids_p), np.uint64)
+            iq = np.ascontiguousarray(np.atleast_2d(ids_q), np.uint64)
+            bands = ip.shape[0]
+        lm = None if landmarks is None else _f64(landmarks)
+        if lm is not None:
+            l = lm.shape[0]
+        h = C.c_void_p()
+        ctx.check(ctx.lib.lcn_op_lcn_buckets(ctx.h, _p(p), p.shape[0], _p(q), q.shape[0], p.shape[1], cost, lam,
+                                             _p(ip), _p(iq), bands, range_, _p(lm), l, method, landmark_seed,
+                                             C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def from_device(cls, ctx, d_p: int, n: int, d_q: int, m: int, d: int, cost, lam, cfg: LshConfig, l=0,
+                    method=LANDMARK_KMEANS, landmark_seed=0):
+        """Device-resident fp32 points (raw device pointers, e.g. torch .data_ptr())."""
+        h = C.c_void_p()
+        c = cfg.c()
+        ctx.check(ctx.lib.lcn_op_create_device(ctx.h, C.c_void_p(d_p), n, C.c_void_p(d_q), m, d, cost, lam,
+                                               C.byref(c), l, method, landmark_seed, C.byref(h)))
+        return cls(ctx, h)
+
+    # accessors ---------------------------------------------------------------
+    def kind(self):
+        return _KIND_NAMES[self.info.kind]
+
+    name = kind
+    n = property(lambda s: s.info.n)
+    m = property(lambda s: s.info.m)
+    l = property(lambda s: s.info.l)
+    nnz = property(lambda s: s.info.nnz)
+    stored = property(lambda s: s.info.stored)
+    lam = property(lambda s: s.info.lam)
+    max_abs_delta = property(lambda s: s.info.max_abs_delta)
+    cond_estimate = property(lambda s: s.info.cond_estimate)
+
+    def export_csr(self, which: int = 0):
+        """(row_ptr, col, vals): which 0 log K^sp, 1 delta, 2 log_sp, 3 nys_vals."""
+        rp = np.zeros(self.n + 1, np.uint32)
+        col = np.zeros(max(self.nnz, 1), np.uint32)
+        val = np.zeros(max(self.nnz, 1))
+        self.ctx.check(self.ctx.lib.lcn_op_export_csr(self.h, which, _p(rp), _p(col), _p(val)))
+        return rp, col[: self.nnz], val[: self.nnz]
+
+    def factor(self, which: int):
+        """0 U (n x l), 1 W (l x m), 2 landmarks (l x d)."""
+        shape = {0: (self.n, self.l), 1: (self.l, self.m), 2: (self.l, self.info.d)}[which]
+        out = np.zeros(shape)
+        self.ctx.check(self.ctx.lib.lcn_op_export_factor(self.h, which, _p(out)))
+        return out
+
+    def log_matvec(self, log_t):
+        v = _f64(log_t)
+        if v.shape != (self.m,):
+            raise DimensionError("log_matvec: vector length mismatch")
+        out = np.zeros(self.n)
+        self.ctx.check(self.ctx.lib.lcn_op_log_matvec(self.h, _p(v), 0, _p(out)))
+        return out
+
+    def log_matvec_t(self, log_s):
+        v = _f64(log_s)
+        if v.shape != (self.n,):
+            raise DimensionError("log_matvec_t: vector length mismatch")
+        out = np.zeros(self.m)
+        self.ctx.check(self.ctx.lib.lcn_op_log_matvec(self.h, _p(v), 1, _p(out)))
+        return out
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.lcn_op_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class SinkhornResult:
+    def __init__(self, op: KernelOperator, h):
+        self.op, self.h = op, h
+        info = _ResInfo()
+        op.ctx.check(op.ctx.lib.lcn_result_get_info(h, C.byref(info)))
+        self.distance = info.distance
+        self.iters = info.iters
+        self.converged = bool(info.converged)
+        self.marginal_err_final = info.marginal_err_final
+        self.device_ms = info.device_ms
+        self.warnings = [op.ctx.lib.lcn_result_warning(h, i).decode() for i in range(info.n_warnings)]
+
+    def _vec(self, which):
+        lib = self.op.ctx.lib
+        n = C.c_size_t()
+        lib.lcn_result_copy(self.h, which, None, C.byref(n))
+        out = np.zeros(n.value)
+        if n.value:
+            lib.lcn_result_copy(self.h, which, _p(out), C.byref(n))
+        return out
+
+    log_s = property(lambda s: s._vec(0))
+    log_t = property(lambda s: s._vec(1))
+    row_marginal = property(lambda s: s._vec(2))
+    marginal_err = property(lambda s: s._vec(3))
+    sparse_vals = property(lambda s: s._vec(4))
+    sp_vals = property(lambda s: s._vec(5))
+    sp_nys_vals = property(lambda s: s._vec(6))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.op.ctx.lib.lcn_result_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def sinkhorn(op: KernelOperator, p, q, opts: SinkhornOptions = SinkhornOptions()) -> SinkhornResult:
+    """sinkhorn (sinkhorn.cpp:104-188)."""
+    p = _f64(p)
+    q = _f64(q)
+    if p.shape != (op.n,) or q.shape != (op.m,):
+        raise DimensionError("sinkhorn: marginal length does not match operator shape")
+    o = _SinkOpts(opts.tol, opts.max_iters, int(opts.check_support), int(opts.want_plan))
+    h = C.c_void_p()
+    op.ctx.check(op.ctx.lib.lcn_sinkhorn(op.h, _p(p), _p(q), C.byref(o), C.byref(h)))
+    return SinkhornResult(op, h)
+
+
+def distance_lcn(res: SinkhornResult, op: KernelOperator) -> float:
+    """distance_lcn (sinkhorn.cpp:222-261)."""
+    out = C.c_double()
+    op.ctx.check(op.ctx.lib.lcn_distance_lcn(res.h, op.h, C.byref(out)))
+    return out.value

@@ -1,0 +1,125 @@
+"""GPU parity: the CUDA path (C-ABI) against the reference compiled from its own
+sources (oracle/_ref) on the same seeded inputs.
+
+Bar (BASELINE.json north_star): bucket ids and sparse support bit-exact;
+Sinkhorn distance and plan entries within 1e-4 relative (fp32 storage) —
+1e-9 with fp64 storage.
+"""
+import numpy as np
+import pytest
+
+import paper_2107_06876_b200 as lcn
+from paper_2107_06876_b200 import configs
+
+pytestmark = pytest.mark.gpu
+
+REL_FP32 = 1e-4
+REL_FP64 = 1e-9
+
+
+def rel(a, b):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300))) if a.size else 0.0
+
+
+def rng_points(seed, n, d, comps=5, spread=3.0):
+    r = np.random.default_rng(seed)
+    means = r.standard_normal((comps, d)) * spread
+    return (means[r.integers(0, comps, n)] + r.standard_normal((n, d))).astype(np.float32).astype(np.float64)
+
+
+@pytest.mark.parametrize("n,d,k,seed", [(40, 3, 4, 1), (500, 8, 16, 7), (4000, 32, 16, 3), (3000, 300, 37, 11),
+                                        (64, 2, 60, 5)])
+def test_lloyd_bit_exact(ctx, ref, n, d, k, seed):
+    x = rng_points(seed, n, d)
+    c_gpu, a_gpu = lcn.lloyd(ctx, x, k, 10, seed)
+    c_ref, a_ref = ref.lloyd(x, k, 10, seed)
+    assert np.array_equal(a_gpu, a_ref)
+    assert np.array_equal(c_gpu.view(np.uint64), c_ref.view(np.uint64))
+
+
+@pytest.mark.parametrize("n,d,k,seed", [(50, 2, 50, 3), (1000, 16, 64, 9), (20000, 8, 33, 4)])
+def test_kmeans_pp_bit_exact(ctx, ref, n, d, k, seed):
+    x = rng_points(seed, n, d)
+    assert np.array_equal(lcn.kmeans_pp_indices(ctx, x, k, seed=seed), ref.kmeans_pp(x, k, seed))
+
+
+def test_kmeans_pp_duplicates_total_zero(ctx, ref):
+    # all points coincide: total <= 0 branch takes the first unused index (kmeans.cpp:42-47)
+    x = np.zeros((12, 3))
+    assert np.array_equal(lcn.kmeans_pp_indices(ctx, x, 6, seed=5), ref.kmeans_pp(x, 6, 5))
+
+
+def test_assign_ties_lowest_index(ctx, ref):
+    x = np.array([[0.0], [1.0], [2.0]])
+    ctr = np.array([[1.0], [1.0], [0.0], [0.0]])
+    assert np.array_equal(lcn.assign_nearest(ctx, x, ctr), ref.assign_nearest(x, ctr))
+
+
+def test_lsh_buckets_config0(ctx, ref):
+    pr = configs.config0()
+    cfg = lcn.LshConfig(pr.bands, 1, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
+    ids = lcn.lsh_kmeans_buckets(ctx, pr.p, pr.q, cfg)
+    ids_ref = ref.lsh_buckets(pr.p, pr.q, pr.bands, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
+    assert np.array_equal(ids, ids_ref)
+
+
+def _sparse_pair(ctx, ref, pr):
+    cfg = lcn.LshConfig(pr.bands, 1, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
+    op = lcn.KernelOperator.sparse_lsh(ctx, pr.p, pr.q, pr.cost, pr.lam_eff, cfg)
+    pairs = ref.lsh_pairs(pr.p, pr.q, pr.bands, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
+    rop = ref.op_sparse(pr.p, pr.q, pr.cost, pr.lam_eff, pairs)
+    return op, rop
+
+
+@pytest.mark.parametrize("fp64", [False, True])
+def test_sparse_config0_end_to_end(ref, fp64):
+    c = lcn.Context(0, store_fp64=fp64)
+    pr = configs.config0()
+    op, rop = _sparse_pair(c, ref, pr)
+    rp, col, lk = op.export_csr(0)
+    rrp, rcol, rlk = rop.csr(0)
+    assert np.array_equal(rp, rrp) and np.array_equal(col, rcol)          # support bit-exact
+    assert np.array_equal(lk.view(np.uint64), rlk.view(np.uint64))          # fp64 log K bit-exact
+    pm, qm = pr.marginals()
+    res = lcn.sinkhorn(op, pm, qm, lcn.SinkhornOptions(tol=0.0, max_iters=pr.iters))
+    rres = rop.sinkhorn(pm, qm, tol=0.0, max_iters=pr.iters)
+    tol = REL_FP64 if fp64 else REL_FP32
+    assert res.iters == rres.iters == pr.iters
+    assert rel(res.distance, rres.distance) <= tol
+    assert rel(res.sparse_vals, rres.sparse_vals) <= tol
+    assert len(res.warnings) == rres.n_warnings
+    assert rel(res.marginal_err, rres.marginal_err) <= 1e-3
+
+
+def test_sparse_empty_row_is_stabilization_error(ctx, ref):
+    # source 1 alone in its bucket: its row is empty (sinkhorn.cpp:16-21; test_sinkhorn.cpp:241-248)
+    p = rng_points(1, 3, 2)
+    q = rng_points(2, 3, 2)
+    ids_p = np.array([[0, 5, 1]], np.uint64)
+    ids_q = np.array([[0, 1, 1]], np.uint64)
+    op = lcn.KernelOperator.sparse_buckets(ctx, p, q, lcn.EUCLIDEAN, 0.5, ids_p, ids_q)
+    with pytest.raises(lcn.StabilizationError, match="sparse"):
+        lcn.sinkhorn(op, np.full(3, 1 / 3), np.full(3, 1 / 3), lcn.SinkhornOptions(check_support=False))
+
+
+@pytest.mark.parametrize("scale,which", [(0.05, 1), (0.002, 3)])
+def test_lcn_small_configs(ref, scale, which):
+    pr = configs.config1(scale) if which == 1 else configs.config3(scale)
+    c = lcn.Context(0, store_fp64=False)
+    cfg = lcn.LshConfig(pr.bands, 1, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
+    op = lcn.KernelOperator.lcn_lsh(c, pr.p, pr.q, pr.cost, pr.lam_eff, cfg, pr.landmarks, lcn.LANDMARK_KMEANS,
+                                    pr.landmark_seed)
+    pairs = ref.lsh_pairs(pr.p, pr.q, pr.bands, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
+    rop = ref.op_lcn(pr.p, pr.q, pr.cost, pr.lam_eff, pairs, pr.landmarks, 0, pr.landmark_seed)
+    rp, col, dl = op.export_csr(1)
+    rrp, rcol, rdl = rop.csr(1)
+    assert np.array_equal(rp, rrp) and np.array_equal(col, rcol)
+    scale_k = max(np.max(np.abs(rdl)), 1e-300)
+    assert np.max(np.abs(dl - rdl)) <= 1e-8 * max(scale_k, 1.0)
+    pm, qm = pr.marginals()
+    res = lcn.sinkhorn(op, pm, qm, lcn.SinkhornOptions(tol=0.0, max_iters=pr.iters))
+    rres = rop.sinkhorn(pm, qm, tol=0.0, max_iters=pr.iters)
+    assert rel(res.distance, rres.distance) <= REL_FP32
+    assert rel(res.sp_vals, rres.sp_vals) <= REL_FP32
+    assert rel(lcn.distance_lcn(res, op), rres.distance_lcn()) <= REL_FP32
