@@ -14,6 +14,10 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <cmath>
 #include <limits>
 #include <numeric>
@@ -24,6 +28,20 @@
 #include "tiles.cuh"
 
 namespace lcnb {
+
+PhaseTimer::PhaseTimer(Ctx& c, const char* n) : ctx(c), name(n), t0(0), on(std::getenv("LCN_TIMING") != nullptr) {
+    if (on) {
+        ctx.sync();
+        t0 = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    }
+}
+PhaseTimer::~PhaseTimer() {
+    if (on) {
+        cudaStreamSynchronize(ctx.stream);
+        double t1 = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+        std::fprintf(stderr, "[lcn timing] %-36s %10.2f ms\n", name, t1 - t0);
+    }
+}
 
 BandView Op::view(int b) const {
     const Band& B = bands[b];
@@ -140,7 +158,8 @@ __global__ void narrow_kernel(uint32_t* __restrict__ out, const uint64_t* __rest
 // lsh_neighbor_pairs' k-means branch (lsh.cpp:245-283): per band, per
 // function, hash_kmeans of the union with fn_seed(seed, band, fn); composite
 // ids are mixed-radix over the r functions.
-void lsh_kmeans_bucket_ids(Ctx& ctx, const double* d_union, size_t n, size_t m, size_t d, int bands, int rows,
+void lsh_kmeans_bucket_ids(Ctx& ctx, const double* d_union, const float* d_union32, size_t n, size_t m, size_t d,
+                           int bands, int rows,
                            int buckets, int iters, uint64_t seed, std::vector<DevBuf<uint32_t>>& ids, size_t& range) {
     const size_t N = n + m;
     if (bands < 1 || rows < 1) throw Status(2, "lsh: bands and rows_per_band must be >= 1");
@@ -157,8 +176,13 @@ void lsh_kmeans_bucket_ids(Ctx& ctx, const double* d_union, size_t n, size_t m, 
     for (int b = 0; b < bands; ++b) {
         comp.zero(s);
         for (int fn = 0; fn < rows; ++fn) {
-            lloyd_device<double>(ctx, d_union, N, static_cast<int>(d), buckets, iters, fn_seed(seed, b, fn), ctr.get(),
-                                 assign.get());
+            PhaseTimer pt(ctx, "lsh k-means (one band function)");
+            if (d_union32)
+                lloyd_device<float>(ctx, d_union32, N, static_cast<int>(d), buckets, iters, fn_seed(seed, b, fn),
+                                    ctr.get(), assign.get());
+            else
+                lloyd_device<double>(ctx, d_union, N, static_cast<int>(d), buckets, iters, fn_seed(seed, b, fn),
+                                     ctr.get(), assign.get());
             compose_kernel<<<ceil_div(N, 256), 256, 0, s>>>(comp.get(), assign.get(), N, static_cast<uint64_t>(buckets));
         }
         DevBuf<uint32_t> out(N);
@@ -407,6 +431,7 @@ int read_flag(Ctx& ctx, DevBuf<int>& f) {
 
 void build_sparse_values(Op& op) {
     Ctx& ctx = *op.ctx;
+    PhaseTimer pt(ctx, "K_sp bucket blocks");
     const double* nrm = union_norms(op);
     DevBuf<int> bad(1);
     bad.zero(ctx.stream);
@@ -514,9 +539,13 @@ void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed)
     } else {
         // select_landmarks (nystrom.cpp:28-48)
         if (l < 1 || l > N) throw Status(2, "select_landmarks: l out of range");
+        PhaseTimer pt(ctx, "landmarks");
         if (method == 0) {
             DevBuf<uint32_t> asg(N);
-            lloyd_device<double>(ctx, op.X.get(), N, static_cast<int>(d), static_cast<int>(l), 10, seed, op.L.get(), asg.get());
+            if (op.X32.size())
+                lloyd_device<float>(ctx, op.X32.get(), N, static_cast<int>(d), static_cast<int>(l), 10, seed, op.L.get(), asg.get());
+            else
+                lloyd_device<double>(ctx, op.X.get(), N, static_cast<int>(d), static_cast<int>(l), 10, seed, op.L.get(), asg.get());
         } else {
             std::mt19937_64 rng(seed);
             std::uniform_int_distribution<std::size_t> first(0, N - 1);
@@ -531,6 +560,7 @@ void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed)
         }
     }
     ctx.sync();
+    PhaseTimer ptf(ctx, "nystrom factors U, V, A, W");
     const double* nrm = union_norms(op);
     DevBuf<double> lnorm;
     if (op.cost == 2) {
@@ -635,6 +665,7 @@ void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed)
 // build_correction (sparse_kernel.cpp:82-117) on every band block.
 void build_correction(Op& op) {
     Ctx& ctx = *op.ctx;
+    PhaseTimer pt(ctx, "LCN correction (incl. K_sp)");
     // log K^sp first (same values as build_sparse), then delta.
     build_sparse_values(op);
     op.logk64 = std::move(op.val64);
@@ -744,6 +775,7 @@ __global__ void csr_fill_kernel(BandViews bvs, BandSet bs, long long n, const ui
 void build_csr(Op& op) {
     if (op.csr_ready) return;
     Ctx& ctx = *op.ctx;
+    PhaseTimer pt(ctx, "CSR support export");
     cudaStream_t s = ctx.stream;
     const long long n = op.n;
     BandViews bvs{};

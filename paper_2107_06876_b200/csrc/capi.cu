@@ -67,6 +67,13 @@ void upload_union(Op& op, const double* p, size_t n, const double* q, size_t m, 
     op.X.resize((n + m) * d);
     CUDA_OK(cudaMemcpyAsync(op.X.get(), p, n * d * 8, cudaMemcpyHostToDevice, op.ctx->stream));
     CUDA_OK(cudaMemcpyAsync(op.X.get() + n * d, q, m * d * 8, cudaMemcpyHostToDevice, op.ctx->stream));
+    // fp32 copy for the k-means reads when the promotion is exact
+    std::vector<float> f((n + m) * d);
+    bool exact = true;
+    for (size_t i = 0; i < n * d && exact; ++i) exact = static_cast<double>(f[i] = static_cast<float>(p[i])) == p[i];
+    for (size_t i = 0; i < m * d && exact; ++i) exact = static_cast<double>(f[n * d + i] = static_cast<float>(q[i])) == q[i];
+    if (exact) op.X32.upload(f.data(), f.size(), op.ctx->stream);
+    op.ctx->sync();
 }
 
 __global__ void promote_kernel(const float* __restrict__ in, double* __restrict__ out, long long n) {
@@ -250,7 +257,7 @@ int lcn_lsh_kmeans_buckets(lcn_ctx* ctx, const double* p, size_t n, const double
         upload_union(tmp, p, n, q, m, d);
         std::vector<DevBuf<uint32_t>> ids;
         size_t range = 0;
-        lsh_kmeans_bucket_ids(ctx->c, tmp.X.get(), n, m, d, cfg->bands, cfg->rows_per_band, cfg->buckets_per_fn,
+        lsh_kmeans_bucket_ids(ctx->c, tmp.X.get(), tmp.X32.size() ? tmp.X32.get() : nullptr, n, m, d, cfg->bands, cfg->rows_per_band, cfg->buckets_per_fn,
                               cfg->kmeans_iters, cfg->seed, ids, range);
         std::vector<uint32_t> h(n + m);
         for (size_t b = 0; b < ids.size(); ++b) {
@@ -271,7 +278,7 @@ int lcn_op_sparse_lsh(lcn_ctx* ctx, const double* p, size_t n, const double* q, 
         upload_union(h->o, p, n, q, m, d);
         std::vector<DevBuf<uint32_t>> ids;
         size_t range = 0;
-        lsh_kmeans_bucket_ids(ctx->c, h->o.X.get(), n, m, d, cfg->bands, cfg->rows_per_band, cfg->buckets_per_fn,
+        lsh_kmeans_bucket_ids(ctx->c, h->o.X.get(), h->o.X32.size() ? h->o.X32.get() : nullptr, n, m, d, cfg->bands, cfg->rows_per_band, cfg->buckets_per_fn,
                               cfg->kmeans_iters, cfg->seed, ids, range);
         if (static_cast<int>(ids.size()) > kMaxBands) throw Status(2, "lsh: at most 8 bands on this path");
         bands_from_union_ids(h->o, ids, range);
@@ -306,7 +313,7 @@ int lcn_op_lcn_lsh(lcn_ctx* ctx, const double* p, size_t n, const double* q, siz
         upload_union(h->o, p, n, q, m, d);
         std::vector<DevBuf<uint32_t>> ids;
         size_t range = 0;
-        lsh_kmeans_bucket_ids(ctx->c, h->o.X.get(), n, m, d, cfg->bands, cfg->rows_per_band, cfg->buckets_per_fn,
+        lsh_kmeans_bucket_ids(ctx->c, h->o.X.get(), h->o.X32.size() ? h->o.X32.get() : nullptr, n, m, d, cfg->bands, cfg->rows_per_band, cfg->buckets_per_fn,
                               cfg->kmeans_iters, cfg->seed, ids, range);
         bands_from_union_ids(h->o, ids, range);
         finish_lcn(h->o, nullptr, l, landmark_method, landmark_seed);
@@ -340,6 +347,9 @@ int lcn_op_create_device(lcn_ctx* ctx, const float* d_p, size_t n, const float* 
         op.m = m;
         op.d = d;
         op.X.resize((n + m) * d);
+        op.X32.resize((n + m) * d);
+        CUDA_OK(cudaMemcpyAsync(op.X32.get(), d_p, n * d * 4, cudaMemcpyDeviceToDevice, ctx->c.stream));
+        CUDA_OK(cudaMemcpyAsync(op.X32.get() + n * d, d_q, m * d * 4, cudaMemcpyDeviceToDevice, ctx->c.stream));
         promote_kernel<<<std::min<long long>(ceil_div(n * d, 256), 8 * ctx->c.num_sms), 256, 0, ctx->c.stream>>>(
             d_p, op.X.get(), n * d);
         promote_kernel<<<std::min<long long>(ceil_div(m * d, 256), 8 * ctx->c.num_sms), 256, 0, ctx->c.stream>>>(
@@ -347,7 +357,7 @@ int lcn_op_create_device(lcn_ctx* ctx, const float* d_p, size_t n, const float* 
         LAUNCH_OK("promote");
         std::vector<DevBuf<uint32_t>> ids;
         size_t range = 0;
-        lsh_kmeans_bucket_ids(ctx->c, op.X.get(), n, m, d, cfg->bands, cfg->rows_per_band, cfg->buckets_per_fn,
+        lsh_kmeans_bucket_ids(ctx->c, op.X.get(), op.X32.size() ? op.X32.get() : nullptr, n, m, d, cfg->bands, cfg->rows_per_band, cfg->buckets_per_fn,
                               cfg->kmeans_iters, cfg->seed, ids, range);
         bands_from_union_ids(op, ids, range);
         if (l) finish_lcn(op, nullptr, l, landmark_method, landmark_seed);

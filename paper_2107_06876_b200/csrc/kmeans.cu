@@ -121,17 +121,19 @@ struct FoldResult {
     long long pick;
 };
 
-__device__ FoldResult warp_exact_fold(const double* __restrict__ x, long long n, bool search, double target) {
+constexpr double kMinNormal = 2.2250738585072014e-308;
+constexpr long long kTwo53 = 1LL << 53;
+
+__device__ FoldResult warp_exact_fold(const double* __restrict__ x, long long begin, long long end, double s,
+                                      bool search, double target) {
     const int lane = threadIdx.x & 31;
-    const long long two53 = 1LL << 53;
-    double s = 0.0;
     long long pick = -1;
-    for (long long base = 0; base < n; base += 32) {
-        const int cnt = static_cast<int>(min(32LL, n - base));
+    for (long long base = begin; base < end; base += 32) {
+        const int cnt = static_cast<int>(min(32LL, end - base));
         const double v = lane < cnt ? x[base + lane] : 0.0;
         int a = 0;
         while (a < cnt) {
-            if (!(s >= 2.2250738585072014e-308 && s < kPosInf)) {  // zero / subnormal / inf: real add
+            if (!(s >= kMinNormal && s < kPosInf)) {  // zero / subnormal / inf: real add
                 double va = __shfl_sync(0xffffffffu, v, a);
                 s = xadd(s, va);
                 if (search && pick < 0 && s >= target && va > 0.0) pick = base + a;
@@ -150,7 +152,7 @@ __device__ FoldResult warp_exact_fold(const double* __restrict__ x, long long n,
                 r = static_cast<long long>(K) + (f > 0.5 ? 1 : 0);
                 tie = (f == 0.5);
             } else if (big) {
-                r = two53;
+                r = kTwo53;
             }
             long long P = r;
 #pragma unroll
@@ -158,7 +160,7 @@ __device__ FoldResult warp_exact_fold(const double* __restrict__ x, long long n,
                 long long t = __shfl_up_sync(0xffffffffu, P, o);
                 if (lane >= o) P += t;
             }
-            const bool bad = mine && (big || tie || S + P >= two53);
+            const bool bad = mine && (big || tie || S + P >= kTwo53);
             const unsigned bm = __ballot_sync(0xffffffffu, bad);
             const int fb = bm ? __ffs(bm) - 1 : cnt;
             if (search && pick < 0) {
@@ -183,32 +185,160 @@ __device__ FoldResult warp_exact_fold(const double* __restrict__ x, long long n,
     return {s, pick};
 }
 
-// One k-means++ step after the distance update: total, target, pick
-// (kmeans.cpp:35-62). raw[] holds the caller's engine draws in order; a step
-// with total <= 0 consumes none (kmeans.cpp:42-47).
-__global__ void pp_pick_kernel(double* __restrict__ dist2, unsigned char* __restrict__ used, long long N,
-                               const unsigned long long* __restrict__ raw, int n_raw, int* __restrict__ draw_counter,
-                               uint32_t* __restrict__ chosen, int t) {
+// ---- chunk-parallel exact fold ----------------------------------------------
+// The fold over N values is cut into chunks of kFoldChunk. Most chunks lie
+// inside one binade of the running sum, where the fold's result depends only
+// on that binade: S_end = S_start + u_e * sum_j RN(x_j / u_e). So
+//   A) approximate chunk sums (any order)            -> predicted start A_c
+//   B) predicted binade e_c of each chunk (dirty if the interval
+//      [A_c (1-1e-9), A_{c+1} (1+1e-9)] straddles a power of two)
+//   C) integer rounding sums R_c(e_c) in parallel, dirty on ties / huge x
+//   D) one warp walks the chunks in order with the exact running sum: a clean
+//      chunk whose actual binade matches e_c advances by u * R_c exactly,
+//      any other chunk is folded element-wise by warp_exact_fold.
+// The prediction only decides which path a chunk takes; the walk re-checks
+// the actual binade, so the result is exact regardless.
+constexpr int kFoldChunk = 2048;
+
+__global__ void fold_chunk_sum_kernel(const double* __restrict__ x, long long N, double* __restrict__ csum) {
+    __shared__ double red[8];
+    const long long b = static_cast<long long>(blockIdx.x) * kFoldChunk;
+    const long long e = min(N, b + kFoldChunk);
+    double s = 0.0;
+    for (long long i = b + threadIdx.x; i < e; i += blockDim.x) s += x[i];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        csum[blockIdx.x] = t;
+    }
+}
+
+__global__ void fold_plan_kernel(const double* __restrict__ csum, int nch, int* __restrict__ ebin) {
+    // single block of 1024: blocked exclusive scan of the approximate sums
+    __shared__ double tot[1024];
+    const int per = (nch + 1023) / 1024;
+    const int c0 = threadIdx.x * per, c1 = min(nch, c0 + per);
+    double s = 0.0;
+    for (int c = c0; c < c1; ++c) s += csum[c];
+    tot[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+        double v = threadIdx.x >= o ? tot[threadIdx.x - o] : 0.0;
+        __syncthreads();
+        tot[threadIdx.x] += v;
+        __syncthreads();
+    }
+    double a = threadIdx.x ? tot[threadIdx.x - 1] : 0.0;
+    for (int c = c0; c < c1; ++c) {
+        double lo = a * (1.0 - 1e-9), hi = (a + csum[c]) * (1.0 + 1e-9);
+        a += csum[c];
+        int e = -100000;
+        if (lo >= kMinNormal && hi < kPosInf && ilogb(lo) == ilogb(hi)) e = ilogb(lo);
+        ebin[c] = e;
+    }
+}
+
+__global__ void fold_round_kernel(const double* __restrict__ x, long long N, const int* __restrict__ ebin,
+                                  long long* __restrict__ R) {
+    __shared__ long long red[8];
+    __shared__ int bad_any;
+    const int e = ebin[blockIdx.x];
+    if (e == -100000) {
+        if (threadIdx.x == 0) R[blockIdx.x] = -1;
+        return;
+    }
+    if (threadIdx.x == 0) bad_any = 0;
+    __syncthreads();
+    const long long b = static_cast<long long>(blockIdx.x) * kFoldChunk;
+    const long long en = min(N, b + kFoldChunk);
+    long long r = 0;
+    bool bad = false;
+    for (long long i = b + threadIdx.x; i < en; i += blockDim.x) {
+        double q = scalbn(x[i], 52 - e);
+        if (!(q < 9007199254740992.0)) { bad = true; continue; }
+        double K = floor(q), f = q - K;
+        if (f == 0.5) bad = true;
+        r += static_cast<long long>(K) + (f > 0.5 ? 1 : 0);
+    }
+    if (bad) bad_any = 1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = r;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        R[blockIdx.x] = bad_any ? -1 : t;
+    }
+}
+
+// D) walk + draw + pick for k-means++ step t (kmeans.cpp:35-62). raw[] holds
+// the caller's engine draws in order; a step with total <= 0 consumes none
+// (kmeans.cpp:42-47).
+__global__ void pp_walk_pick_kernel(double* __restrict__ dist2, unsigned char* __restrict__ used, long long N, int nch,
+                                    const int* __restrict__ ebin, const long long* __restrict__ R,
+                                    double* __restrict__ sstart, const unsigned long long* __restrict__ raw, int n_raw,
+                                    int* __restrict__ draw_counter, uint32_t* __restrict__ chosen, int t) {
     const int lane = threadIdx.x;
-    FoldResult tot = warp_exact_fold(dist2, N, false, 0.0);
+    double S = 0.0;
+    for (int cb = 0; cb < nch; cb += 32) {
+        const int c_l = cb + lane;
+        const int e_l = c_l < nch ? ebin[c_l] : 0;
+        const long long r_l = c_l < nch ? R[c_l] : -1;
+        const int cnt = min(32, nch - cb);
+        for (int k = 0; k < cnt; ++k) {
+            const int c = cb + k;
+            if (lane == 0) sstart[c] = S;
+            const int e = __shfl_sync(0xffffffffu, e_l, k);
+            const long long Rc = __shfl_sync(0xffffffffu, r_l, k);
+            bool fast = Rc >= 0 && S >= kMinNormal && S < kPosInf && ilogb(S) == e;
+            long long Si = 0;
+            if (fast) {
+                Si = static_cast<long long>(scalbn(S, 52 - e));
+                fast = Si + Rc < kTwo53;
+            }
+            if (fast) {
+                S = scalbn(static_cast<double>(Si + Rc), e - 52);
+            } else {
+                const long long b = static_cast<long long>(c) * kFoldChunk;
+                S = warp_exact_fold(dist2, b, min(N, b + kFoldChunk), S, false, 0.0).s;
+            }
+        }
+    }
+    if (lane == 0) sstart[nch] = S;
     long long pick;
-    if (tot.s <= 0.0) {
-        pick = N;  // first unused
+    if (S <= 0.0) {
+        pick = N;  // all remaining points coincide with a centroid: first unused
         for (long long base = 0; base < N; base += 32) {
             bool free_ = base + lane < N && used[base + lane] == 0;
             unsigned m = __ballot_sync(0xffffffffu, free_);
             if (m) { pick = base + __ffs(m) - 1; break; }
         }
     } else {
-        int di = *draw_counter;
-        unsigned long long u = di < n_raw ? raw[di] : 0ull;
+        const int di = *draw_counter;
+        const unsigned long long u = di < n_raw ? raw[di] : 0ull;
         // generate_canonical<double,53>(mt19937_64): double(u) / 2^64, clamped
         // below 1 (libstdc++ random.tcc); uniform_real(0,total) = c*total + 0.
         double c = __ull2double_rn(u) * 5.421010862427522e-20;  // exact: * 2^-64
         if (c >= 1.0) c = 0.99999999999999989;                 // nextafter(1, 0)
-        double target = xadd(xmul(c, xsub(tot.s, 0.0)), 0.0);
-        FoldResult sr = warp_exact_fold(dist2, N, true, target);
-        pick = sr.pick >= 0 ? sr.pick : N - 1;
+        const double target = xadd(xmul(c, xsub(S, 0.0)), 0.0);
+        // first chunk whose running sum reaches the target (the sum is monotone)
+        int cstar = nch;
+        for (int cb = 0; cb < nch; cb += 32) {
+            const int c_l = cb + lane;
+            const bool hit = c_l < nch && sstart[c_l + 1] >= target;
+            const unsigned m = __ballot_sync(0xffffffffu, hit);
+            if (m) { cstar = cb + __ffs(m) - 1; break; }
+        }
+        pick = -1;
+        if (cstar < nch) {
+            FoldResult sr = warp_exact_fold(dist2, static_cast<long long>(cstar) * kFoldChunk, N, sstart[cstar], true, target);
+            pick = sr.pick;
+        }
+        if (pick < 0) pick = N - 1;
         if (lane == 0) *draw_counter = di + 1;
     }
     __syncwarp();
@@ -230,7 +360,10 @@ template <typename T>
 void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t first,
                       const std::vector<unsigned long long>& raw, uint32_t* d_chosen, int* draws_used) {
     cudaStream_t s = ctx.stream;
-    DevBuf<double> dist2(N);
+    const int nch = ceil_div(N, kFoldChunk);
+    DevBuf<double> dist2(N), csum(nch), sstart(nch + 1);
+    DevBuf<int> ebin(nch);
+    DevBuf<long long> R(nch);
     DevBuf<unsigned char> used(N);
     DevBuf<unsigned long long> d_raw(raw.size() ? raw.size() : 1);
     DevBuf<int> counter(1);
@@ -244,14 +377,15 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     CUDA_OK(cudaMemcpyAsync(used.get() + first, &one, 1, cudaMemcpyHostToDevice, s));
     for (int t = 1; t < k; ++t) {
         pp_update_kernel<T><<<ceil_div(N, TP), TP, 0, s>>>(X, N, d, d_chosen, t - 1, dist2.get());
-        pp_pick_kernel<<<1, 32, 0, s>>>(dist2.get(), used.get(), N, d_raw.get(), static_cast<int>(raw.size()),
-                                        counter.get(), d_chosen, t);
+        fold_chunk_sum_kernel<<<nch, 256, 0, s>>>(dist2.get(), N, csum.get());
+        fold_plan_kernel<<<1, 1024, 0, s>>>(csum.get(), nch, ebin.get());
+        fold_round_kernel<<<nch, 256, 0, s>>>(dist2.get(), N, ebin.get(), R.get());
+        pp_walk_pick_kernel<<<1, 32, 0, s>>>(dist2.get(), used.get(), N, nch, ebin.get(), R.get(), sstart.get(),
+                                             d_raw.get(), static_cast<int>(raw.size()), counter.get(), d_chosen, t);
     }
     LAUNCH_OK("kmeans++");
-    if (draws_used) {
-        counter.download(draws_used, 1, s);
-        ctx.sync();
-    }
+    if (draws_used) counter.download(draws_used, 1, s);
+    ctx.sync();
 }
 
 // ---- Lloyd (kmeans.cpp:87-143) ---------------------------------------------
@@ -411,9 +545,13 @@ void lloyd_device(Ctx& ctx, const T* X, long long N, int d, int k, int iters, ui
     assign_device<T>(ctx, X, N, d, d_ctr, k, d_assign);
 }
 
-template void kmeans_pp_device<double>(Ctx&, const double*, long long, int, int, uint64_t,
-                                       const std::vector<unsigned long long>&, uint32_t*, int*);
-template void assign_device<double>(Ctx&, const double*, long long, int, const double*, int, uint32_t*);
-template void lloyd_device<double>(Ctx&, const double*, long long, int, int, int, uint64_t, double*, uint32_t*);
+#define LCNB_INST(T)                                                                                    \
+    template void kmeans_pp_device<T>(Ctx&, const T*, long long, int, int, uint64_t,                    \
+                                      const std::vector<unsigned long long>&, uint32_t*, int*);         \
+    template void assign_device<T>(Ctx&, const T*, long long, int, const double*, int, uint32_t*);      \
+    template void lloyd_device<T>(Ctx&, const T*, long long, int, int, int, uint64_t, double*, uint32_t*);
+LCNB_INST(double)
+LCNB_INST(float)
+#undef LCNB_INST
 
 }  // namespace lcnb

@@ -39,6 +39,7 @@ struct Op {
     DevBuf<double> X;                     // (n+m) x d union X_p ∪ X_q, fp64 (union_points, geometry.cpp:20-27)
     const double* P() const { return X.get(); }
     const double* Q() const { return X.get() + n * d; }
+    DevBuf<float> X32;                    // fp32 copy of X when every coordinate is fp32-exact (k-means reads)
     DevBuf<double> norms;                 // per-point sum x_k^2 (cosine-derived cost only)
     std::vector<Band> bands;
     std::vector<DevBuf<double>> val64;    // sparse: log K; lcn: delta (fp64 master)
@@ -74,7 +75,7 @@ struct Result {
 // build.cu
 void build_band_layout(Ctx& ctx, Band& B, const uint32_t* d_src_bucket, const uint32_t* d_tgt_bucket, size_t n,
                        size_t m, size_t nb);
-void lsh_kmeans_bucket_ids(Ctx& ctx, const double* d_union, size_t n, size_t m, size_t d, int bands, int rows,
+void lsh_kmeans_bucket_ids(Ctx& ctx, const double* d_union, const float* d_union32, size_t n, size_t m, size_t d, int bands, int rows,
                            int buckets, int iters, uint64_t seed, std::vector<DevBuf<uint32_t>>& ids, size_t& range);
 void build_sparse_values(Op& op);
 void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed);
@@ -82,6 +83,16 @@ void build_correction(Op& op);
 void finalize_storage(Op& op);
 void build_csr(Op& op);
 void export_csr(Op& op, int which, uint32_t* row_ptr, uint32_t* col, double* vals);
+
+// Phase timing to stderr when LCN_TIMING is set (host clock around synced phases).
+struct PhaseTimer {
+    Ctx& ctx;
+    const char* name;
+    double t0;
+    bool on;
+    PhaseTimer(Ctx& c, const char* n);
+    ~PhaseTimer();
+};
 
 // sinkhorn.cu
 struct SolveOptions {
