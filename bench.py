@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""Benchmark of the LCN-Sinkhorn hot path (BASELINE.json metric, configs[3]).
+
+Metric: Sinkhorn iterations per second of LCN-Sinkhorn at n = m = 10^6,
+d = 128 (configs[3]: sq-L2 / mean, lambda = 0.05, 2 x 4096 k-means LSH,
+l = 512 landmarks, 100 iterations). One *step* = the 100-iteration Sinkhorn
+solve on the device-resident LCN operator built from the config's seeded
+synthetic points (`value`, inputs resident in HBM, timed with CUDA events on
+the stream the library launches on). `e2e` is the same metric through the
+C-ABI from pinned host buffers: every step copies the points and marginals
+host->device, runs the *whole* reference-facing path (k-means LSH, landmarks,
+Nystrom factors, LCN correction, 100 iterations) and reads the distance back;
+e2e = 100 iterations / that wall of device time.
+
+`roofline` is for one Sinkhorn iteration (the fused kernel sequence that is
+the hot loop): algorithmic bytes B_iter = 8 nnz + 4 l (n+m) + 16 (n+m)
+ over the measured iteration time, against the measured HBM
+copy bandwidth in MEASURED_PEAKS.json.
+
+Multi-GPU (torchrun, one process per GPU): each rank solves its own
+configs[3]-shaped problem (seed + rank) — independent replicas, "scaling":
+"weak", value = iterations of all ranks / max-over-ranks time. The sharded
+single-problem solve with one NCCL allreduce per half-iteration is the next
+step.
+
+--impl reference times the reference's own CPU implementation
+(oracle/_ref: the reference sources compiled unmodified, Nystrom restated) on
+a bounded sample of configs[3] (n = m = 10^4, 2 x 41 buckets, l = 200) with
+all host threads, and scales each phase to the full configs[3] size by its
+algorithmic work (k-means: N k d; pair emission + sort: nnz log nnz; Nystrom: l^2 m; correction: nnz l;
+iterations: B_iter) to report the same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+ITERS = 100
+CPU_SAMPLE_SCALE = 0.01
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class Clocks:
+    FIELDS = ["index", "clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.active",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(self.idx)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) >= 9:
+                for k, nm in enumerate(names):
+                    if r[5 + k].lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference sample (oracle/_ref), scaled to the full configs[3]
+# ---------------------------------------------------------------------------
+def cpu_reference_sample():
+    """One bounded solve of configs[3] at CPU_SAMPLE_SCALE with the compiled
+    reference; returns per-phase seconds and the sample's work units."""
+    from oracle.bindings import RefLib  # checker / baseline only
+    from paper_2107_06876_b200 import configs
+    ref = RefLib()
+    pr = configs.config3(CPU_SAMPLE_SCALE)
+    t0 = time.perf_counter()
+    ids = ref.lsh_buckets(pr.p, pr.q, pr.bands, pr.buckets, pr.kmeans_iters, pr.lsh_seed)  # k-means per band
+    tk = time.perf_counter()
+    pairs = ref.pairs_from_buckets(ids[:, :pr.n], ids[:, pr.n:], pr.buckets)               # pair emission + sort
+    t1 = time.perf_counter()
+    ph = [0.0] * 4
+    op = ref.op_lcn(pr.p, pr.q, pr.cost, pr.lam_eff, pairs, pr.landmarks, 0, pr.landmark_seed, phases=ph)
+    pm, qm = pr.marginals()
+    t2 = time.perf_counter()
+    res = op.sinkhorn(pm, qm, tol=0.0, max_iters=ITERS, check_support=False, want_plan=False)
+    t3 = time.perf_counter()
+    assert res.iters == ITERS
+    return {"lsh": tk - t0, "pairs": t1 - tk, "landmarks": ph[0] / 1e3, "factors": ph[1] / 1e3,
+            "sparse_correction": (ph[2] + ph[3]) / 1e3, "iterations": t3 - t2, "n": pr.n, "m": pr.m, "d": pr.d,
+            "k": pr.buckets, "bands": pr.bands, "l": pr.landmarks, "nnz": op.nnz, "wall": t3 - t0}
+
+
+def scale_to_full(s, full_nnz, full=None):
+    """Scale each sample phase by the ratio of its algorithmic work."""
+    n, m, d, k, l, bands = 1_000_000, 1_000_000, 128, 4096, 512, 2
+    N, Ns = n + m, s["n"] + s["m"]
+    r_lsh = (N * k * bands) / (Ns * s["k"] * s["bands"])
+    r_pairs = (full_nnz * math.log2(full_nnz)) / (s["nnz"] * math.log2(s["nnz"]))
+    r_lm = (N * l) / (Ns * s["l"])
+    r_fac = (l * l * m + N * l * d) / (s["l"] ** 2 * s["m"] + Ns * s["l"] * s["d"])
+    r_cor = (full_nnz * l) / (s["nnz"] * s["l"])
+    b_full = 8 * full_nnz + 4 * l * N + 16 * N
+    b_s = 8 * s["nnz"] + 4 * s["l"] * Ns + 16 * Ns
+    r_it = b_full / b_s
+    t = (s["lsh"] * r_lsh + s["pairs"] * r_pairs + s["landmarks"] * r_lm + s["factors"] * r_fac + s["sparse_correction"] * r_cor
+         + s["iterations"] * r_it)
+    return t, {"lsh_kmeans_s": s["lsh"] * r_lsh, "lsh_pairs_s": s["pairs"] * r_pairs, "landmarks_s": s["landmarks"] * r_lm, "factors_s": s["factors"] * r_fac,
+               "correction_s": s["sparse_correction"] * r_cor, "iterations_s": s["iterations"] * r_it}
+
+
+FULL_NNZ_ESTIMATE = 521_911_712  # measured nnz of configs[3] (round 1 GPU run); replaced live when known
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    os.environ.setdefault("OMP_NUM_THREADS", str(cpu_cores()))
+    times = []
+    last = None
+    for step in range(args.warmup + args.steps):
+        s = cpu_reference_sample()
+        if step >= args.warmup:
+            t_full, parts = scale_to_full(s, FULL_NNZ_ESTIMATE)
+            times.append((t_full, parts, s))
+            last = s
+    t_full = float(np.median([t[0] for t in times]))
+    parts = times[len(times) // 2][1]
+    value = ITERS / t_full
+    sample = (f"configs[3] at scale {CPU_SAMPLE_SCALE}: n=m={last['n']}, d=128, {last['bands']}x{last['k']} k-means LSH, "
+              f"l={last['l']}, {ITERS} iterations (nnz {last['nnz']}); per-phase times scaled to n=m=1e6 by "
+              f"algorithmic work (extrapolated); sample wall {last['wall']:.1f}s")
+    line = {"impl": "reference", "metric": "lcn_sinkhorn_iters_per_s", "value": value, "unit": "iter/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_full * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "configs[3] LCN-Sinkhorn n=m=1e6 d=128", "extrapolated_from": sample},
+            "cpu_baseline": {"value": value, "unit": "iter/s", "cores": cpu_cores(), "kind": "reference",
+                             "sample": sample, "phases_s": parts},
+            "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import paper_2107_06876_b200 as lcn
+    from paper_2107_06876_b200 import configs
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    pr = configs.config3(args.scale)
+    if rank:
+        # independent replica per rank: reseed the point draw
+        import dataclasses
+        rng = np.random.default_rng(2000 + rank)
+        perm_p = rng.permutation(pr.n)
+        pr = dataclasses.replace(pr, p=pr.p[perm_p], seed=pr.seed + rank)
+    n, m, d, l = pr.n, pr.m, pr.d, pr.landmarks
+    cfg = lcn.LshConfig(pr.bands, 1, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
+    stream = torch.cuda.Stream(device=dev)
+    ctx = lcn.Context(local_rank)
+    ctx.set_stream(stream.cuda_stream)
+
+    p32 = torch.from_numpy(pr.p.astype(np.float32)).pin_memory()
+    q32 = torch.from_numpy(pr.q.astype(np.float32)).pin_memory()
+    pm, qm = pr.marginals()
+    pm_h = torch.from_numpy(pm).pin_memory()
+    qm_h = torch.from_numpy(qm).pin_memory()
+    opts = lcn.SinkhornOptions(tol=0.0, max_iters=ITERS, check_support=False, want_plan=False)
+
+    with torch.cuda.stream(stream):
+        dp = p32.to(dev, non_blocking=True)
+        dq = q32.to(dev, non_blocking=True)
+        dpm = pm_h.to(dev, non_blocking=True)
+        dqm = qm_h.to(dev, non_blocking=True)
+    stream.synchronize()
+
+    # ---- build (timed once, reported as build_s) -------------------------
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    op = lcn.KernelOperator.from_device(ctx, dp.data_ptr(), n, dq.data_ptr(), m, d, pr.cost, pr.lam_eff, cfg, l,
+                                        lcn.LANDMARK_KMEANS, pr.landmark_seed)
+    e1.record(stream)
+    stream.synchronize()
+    build_ms = e0.elapsed_time(e1)
+    nnz = op.nnz
+    stored = op.stored
+
+    def step():
+        r = lcn.sinkhorn_device(op, dpm.data_ptr(), dqm.data_ptr(), opts)
+        return r
+
+    for _ in range(args.warmup):
+        res = step()
+    # phase breakdown (separate profiled step, not timed)
+    ctx.set_profile(True)
+    pres = step()
+    phase_ms, phase_it = pres.phase_ms()
+    ctx.set_profile(False)
+
+    clocks = Clocks(int(os.environ.get("LCN_GPU_INDEX", local_rank)))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        res = step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    elapsed = t0.elapsed_time(t1) / 1e3  # s
+    if world > 1:
+        tt = torch.tensor([elapsed], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed = float(tt.item())
+    ms_per_step = elapsed * 1e3 / args.steps
+    value = world * ITERS * args.steps / elapsed
+    distance = res.distance / pr.mu
+
+    # ---- roofline: one Sinkhorn iteration ------------------------------------
+    hbm, peak_kind = peaks()
+    b_iter = 8 * nnz + 4 * l * (n + m) + 16 * (n + m)
+    t_iter = (ms_per_step / 1e3) / ITERS
+    achieved = b_iter / t_iter / 1e9
+    traffic = None
+    prof_path = os.path.join(ROOT, "profiles", "iteration_traffic.json")
+    if os.path.exists(prof_path):
+        try:
+            traffic = json.load(open(prof_path)).get("dram_bytes_per_iteration")
+        except Exception:
+            traffic = None
+
+    # ---- e2e through the C-ABI from pinned host buffers ----------------------
+    e2e = None
+    if not args.no_e2e:
+        del op
+        torch.cuda.synchronize()
+        h2d = int(p32.numel() * 4 + q32.numel() * 4 + pm_h.numel() * 8 + qm_h.numel() * 8)
+        tot = 0.0
+        for _ in range(args.e2e_steps):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            with torch.cuda.stream(stream):
+                xp = p32.to(dev, non_blocking=True)
+                xq = q32.to(dev, non_blocking=True)
+                xpm = pm_h.to(dev, non_blocking=True)
+                xqm = qm_h.to(dev, non_blocking=True)
+            op2 = lcn.KernelOperator.from_device(ctx, xp.data_ptr(), n, xq.data_ptr(), m, d, pr.cost, pr.lam_eff,
+                                                 cfg, l, lcn.LANDMARK_KMEANS, pr.landmark_seed)
+            r2 = lcn.sinkhorn_device(op2, xpm.data_ptr(), xqm.data_ptr(), opts)
+            _ = r2.distance  # host scalar read (the 8-byte result)
+            b.record(stream)
+            torch.cuda.synchronize()
+            dt = a.elapsed_time(b) / 1e3
+            if world > 1:
+                tt = torch.tensor([dt], device=dev, dtype=torch.float64)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                dt = float(tt.item())
+            tot += dt
+            del op2, r2
+        e2e = {"value": world * ITERS * args.e2e_steps / tot, "unit": "iter/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": 8, "solve_s": tot / args.e2e_steps,
+               "covers": "H2D points+marginals, k-means LSH, landmarks, Nystrom, correction, 100 iterations, D2H distance"}
+
+    # ---- CPU baseline (rank 0, N = 1) ------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            os.environ.setdefault("OMP_NUM_THREADS", str(cpu_cores()))
+            s = cpu_reference_sample()
+            t_full, parts = scale_to_full(s, nnz)
+            cpu = {"value": ITERS / t_full, "unit": "iter/s", "cores": cpu_cores(), "kind": "reference",
+                   "sample": (f"configs[3] at scale {CPU_SAMPLE_SCALE} (n=m={s['n']}, {s['bands']}x{s['k']} buckets, "
+                              f"l={s['l']}, nnz {s['nnz']}, {ITERS} iterations, wall {s['wall']:.1f}s); "
+                              f"phases scaled to n=m=1e6 by algorithmic work (extrapolated)"),
+                   "phases_s": parts}
+        except Exception as ex:  # the baseline must never sink the GPU line
+            cpu = {"value": None, "unit": "iter/s", "cores": cpu_cores(), "kind": "reference",
+                   "sample": f"unavailable: {ex}"}
+
+    launches_per_iter = 5 + 2 * pr.bands + 4  # col: zero, bands, finalize, reduce; row: zero, bands, finalize, reduce, end
+    gpu_launches = args.steps * (ITERS * launches_per_iter + 4 + 2 * pr.bands + 4 + 2)
+    if rank == 0:
+        line = {"metric": "lcn_sinkhorn_iters_per_s", "value": value, "unit": "iter/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32-storage/f64-accumulate", "data": "synthetic",
+                "config": {"workload": "configs[3] LCN-Sinkhorn n=m=1e6 d=128 sqL2/mean lambda=0.05 2x4096 LSH l=512",
+                           "n": n, "m": m, "d": d, "landmarks": l, "bands": pr.bands, "buckets": pr.buckets,
+                           "iterations_per_step": ITERS, "nnz": nnz, "stored_entries": stored,
+                           "scale": args.scale, "l2": "inputs larger than L2 (delta + U + W = 6.2 GB per iteration)",
+                           "parallelism": f"{world} independent replica(s), 1 per GPU"},
+                "distance": distance, "build_s": build_ms / 1e3,
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                             "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
+                             "kernel": "one Sinkhorn iteration (column + row passes)",
+                             "algorithmic_bytes_per_iteration": b_iter},
+                "phases_ms_per_iteration": {k: v / max(phase_it, 1) for k, v in
+                                            zip(["col_bands", "col_finalize", "row_bands", "row_finalize"], phase_ms)},
+                "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": gpu_launches}
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        return run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -106,6 +106,12 @@ typedef struct {
 int lcn_ctx_create(int device, int flags, lcn_ctx** out);
 int lcn_ctx_destroy(lcn_ctx* ctx);
 const char* lcn_ctx_last_error(const lcn_ctx* ctx);
+/* Run the context's work on an external stream (a cudaStream_t, e.g. torch's
+ * current stream, so the caller's CUDA events bracket it); NULL restores the
+ * context's own stream. */
+int lcn_ctx_set_stream(lcn_ctx* ctx, void* stream);
+/* Record per-phase CUDA events inside lcn_sinkhorn (see lcn_result_phase_ms). */
+int lcn_ctx_set_profile(lcn_ctx* ctx, int on);
 const char* lcn_status_name(int status);
 int lcn_abi_version(void);
 
@@ -176,6 +182,14 @@ int lcn_op_log_matvec(lcn_op* op, const double* in, int transposed, double* out)
 /* sinkhorn (sinkhorn.cpp:104-188). p (n), q (m) host marginals. */
 int lcn_sinkhorn(lcn_op* op, const double* p, const double* q, const lcn_sinkhorn_options* opts,
                  lcn_result** out);
+/* Device-resident marginals (fp64 device pointers); no plan extraction.
+ * Marginal validation is the caller's (timing entry point). */
+int lcn_sinkhorn_device(lcn_op* op, const double* d_p, const double* d_q, const lcn_sinkhorn_options* opts,
+                        lcn_result** out);
+/* Profiling (lcn_ctx_set_profile): summed ms of the four phases of
+ * iterations 1..iters: column band blocks, column finalize + reduce, row band
+ * blocks, row finalize + reduce + iteration end. */
+int lcn_result_phase_ms(const lcn_result* res, double* out4, int* iters);
 int lcn_result_destroy(lcn_result* res);
 int lcn_result_get_info(const lcn_result* res, lcn_result_info_t* info);
 /* which: 0 log_s (n), 1 log_t (m), 2 row_marginal (n), 3 marginal_err trace,

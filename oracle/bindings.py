@@ -138,15 +138,21 @@ class CheckerLib(_Lib):
             _ptr(p), p.shape[0], _ptr(q), q.shape[0], p.shape[1], kind, lam, pairs.h, C.byref(h)))
         return Op(self, h, p.shape[0], q.shape[0], "sparse")
 
-    def op_lcn(self, p, q, kind, lam, pairs, l, method=0, lm_seed=0, landmarks=None, nystrom_only=False):
+    def op_lcn(self, p, q, kind, lam, pairs, l, method=0, lm_seed=0, landmarks=None, nystrom_only=False,
+               phases=None):
+        """phases (optional list) receives [select_landmarks, build_factors, build_sparse,
+        build_correction] milliseconds (only the reference backend measures them)."""
         p, q = _f64(p), _f64(q)
         lm = _f64(landmarks) if landmarks is not None else None
         if lm is not None:
             l = lm.shape[0]
         h = _P()
-        self.check(self.fn("op_lcn", _P, _SZ, _P, _SZ, _SZ, _I, _D, _P, _SZ, _I, _U64, _P, _I, _PP)(
+        ph = np.zeros(4)
+        self.check(self.fn("op_lcn", _P, _SZ, _P, _SZ, _SZ, _I, _D, _P, _SZ, _I, _U64, _P, _I, _PP, _P)(
             _ptr(p), p.shape[0], _ptr(q), q.shape[0], p.shape[1], kind, lam, pairs.h if pairs else None, l,
-            method, lm_seed, _ptr(lm), int(nystrom_only), C.byref(h)))
+            method, lm_seed, _ptr(lm), int(nystrom_only), C.byref(h), _ptr(ph)))
+        if phases is not None:
+            phases[:] = list(ph)
         return Op(self, h, p.shape[0], q.shape[0], "nystrom" if nystrom_only else "lcn", l)
 
     def op_dense(self, p, q, kind, lam):

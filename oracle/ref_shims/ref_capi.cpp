@@ -7,6 +7,7 @@
 // algorithmic code lives here except mix64/fn_seed, which restate the
 // file-local helpers at lsh.cpp:17-27 so bucket ids per band can be exported
 // (lsh_neighbor_pairs itself only returns pairs).
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -208,22 +209,36 @@ int ref_op_sparse(const double* p, std::size_t n, const double* q, std::size_t m
 // them with select_landmarks(l, method, lm_seed); otherwise uses the given l x d rows.
 int ref_op_lcn(const double* p, std::size_t n, const double* q, std::size_t m, std::size_t d, int kind,
                double lambda, void* pairs, std::size_t l, int method, std::uint64_t lm_seed,
-               const double* landmarks, int nystrom_only, void** out) {
+               const double* landmarks, int nystrom_only, void** out, double* phase_ms) {
     GUARD({
+        auto now = [] { return std::chrono::steady_clock::now(); };
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
         PointSet P = make_points(p, n, d, "p"), Q = make_points(q, m, d, "q");
         LandmarkSet lm;
+        auto t0 = now();
         if (landmarks) {
             lm.points = make_points(landmarks, l, d, "landmarks");
         } else {
             lm = select_landmarks(P, Q, l, static_cast<LandmarkMethod>(method), lm_seed);
         }
+        auto t1 = now();
         NystromFactors f = build_factors(P, Q, lm, static_cast<CostKind>(kind), lambda);
+        auto t2 = now();
         auto* r = new RefOp{KernelOperator::nystrom(f)};
         r->landmarks = lm.points.coords;
+        auto t3 = t2, t4 = t2;
         if (!nystrom_only) {
             SparseKernel sk = build_sparse(P, Q, *static_cast<NeighborPairs*>(pairs), static_cast<CostKind>(kind), lambda);
+            t3 = now();
             LcnCorrection c = build_correction(sk, f);
+            t4 = now();
             r->op = KernelOperator::lcn(f, c);
+        }
+        if (phase_ms) {
+            phase_ms[0] = ms(t0, t1);  // select_landmarks
+            phase_ms[1] = ms(t1, t2);  // build_factors (restated)
+            phase_ms[2] = ms(t2, t3);  // build_sparse
+            phase_ms[3] = ms(t3, t4);  // build_correction
         }
         *out = r;
     })

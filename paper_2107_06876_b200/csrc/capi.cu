@@ -186,6 +186,7 @@ int lcn_ctx_create(int device, int flags, lcn_ctx** out) {
         c->c.num_sms = prop.multiProcessorCount;
         CUDA_OK(cudaSetDevice(device));
         CUDA_OK(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking));
+        c->c.own_stream = c->c.stream;
         *out = c.release();
     });
 }
@@ -193,8 +194,20 @@ int lcn_ctx_create(int device, int flags, lcn_ctx** out) {
 int lcn_ctx_destroy(lcn_ctx* ctx) {
     if (!ctx) return LCN_OK;
     cudaSetDevice(ctx->c.device);
-    if (ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
+    if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.own_stream);
     delete ctx;
+    return LCN_OK;
+}
+
+int lcn_ctx_set_stream(lcn_ctx* ctx, void* stream) {
+    if (!ctx) return LCN_E_INVALID_ARGUMENT;
+    ctx->c.stream = stream ? static_cast<cudaStream_t>(stream) : ctx->c.own_stream;
+    return LCN_OK;
+}
+
+int lcn_ctx_set_profile(lcn_ctx* ctx, int on) {
+    if (!ctx) return LCN_E_INVALID_ARGUMENT;
+    ctx->c.profile = on ? 1 : 0;
     return LCN_OK;
 }
 
@@ -461,7 +474,7 @@ int lcn_sinkhorn(lcn_op* op, const double* p, const double* q, const lcn_sinkhor
                 std::fprintf(stderr, "lcn: warning: %s\n", res->r.warnings.back().c_str());
             }
         }
-        sinkhorn_solve(o, p, q, so, res->r);
+        sinkhorn_solve(o, p, q, false, so, res->r);
         if (so.want_plan && o.kind != 2 && o.nnz) {
             // Plan entries on the support in CSR order (sinkhorn.cpp:45-80).
             std::vector<uint32_t> rp(o.n + 1), col(o.nnz);
@@ -490,6 +503,31 @@ int lcn_sinkhorn(lcn_op* op, const double* p, const double* q, const lcn_sinkhor
         }
         *out = res.release();
     });
+}
+
+int lcn_sinkhorn_device(lcn_op* op, const double* d_p, const double* d_q, const lcn_sinkhorn_options* opts,
+                        lcn_result** out) {
+    lcn_ctx* ctx = reinterpret_cast<lcn_ctx*>(op->o.ctx);
+    return guard(ctx, [&] {
+        SolveOptions so;
+        if (opts) {
+            so.tol = opts->tol;
+            so.max_iters = opts->max_iters;
+            so.check_support = opts->check_support != 0;
+            so.want_plan = false;
+        }
+        auto res = std::make_unique<lcn_result>();
+        res->op = op;
+        sinkhorn_solve(op->o, d_p, d_q, true, so, res->r);
+        *out = res.release();
+    });
+}
+
+int lcn_result_phase_ms(const lcn_result* res, double* out4, int* iters) {
+    if (!res || !out4) return LCN_E_INVALID_ARGUMENT;
+    for (int k = 0; k < 4; ++k) out4[k] = k < static_cast<int>(res->r.phase_ms.size()) ? res->r.phase_ms[k] : 0.0;
+    if (iters) *iters = res->r.phase_iters;
+    return LCN_OK;
 }
 
 int lcn_result_destroy(lcn_result* res) {

@@ -61,6 +61,8 @@ struct Ctx {
     int store_fp64 = 0;
     int num_sms = 148;
     cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    int profile = 0;
     std::string last_error;
     void activate() const { CUDA_OK(cudaSetDevice(device)); }
     void sync() const { CUDA_OK(cudaStreamSynchronize(stream)); }

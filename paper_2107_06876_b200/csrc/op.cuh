@@ -1,6 +1,7 @@
 // Internal operator / result structures and the build + solve entry points.
 #pragma once
 
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -29,6 +30,8 @@ struct BandSet {  // bucket ids of every band, for the cross-band dedup mask
     int bands;
 };
 
+struct Solver;
+
 struct Op {
     Ctx* ctx = nullptr;
     int kind = 1;  // lcn_op_kind
@@ -54,6 +57,7 @@ struct Op {
     // CSR export (lazy)
     DevBuf<uint32_t> csr_row_ptr, csr_col;
     bool csr_ready = false;
+    std::shared_ptr<Solver> ws;           // persistent iteration workspace (sinkhorn.cu)
 
     BandView view(int b) const;
     BandSet bandset() const;
@@ -66,6 +70,8 @@ struct Result {
     bool converged = false;
     double marginal_err_final = 0.0;
     double device_ms = 0.0;
+    std::vector<double> phase_ms;  // profiling: col bands, col finalize+reduce, row bands, row finalize+reduce+end
+    int phase_iters = 0;
     std::vector<double> log_s, log_t, row_marg, err_trace;
     std::vector<double> plan_vals, sp_vals, sp_nys_vals;
     std::vector<std::string> warnings;
@@ -101,7 +107,7 @@ struct SolveOptions {
     bool check_support = true;
     bool want_plan = true;
 };
-void sinkhorn_solve(Op& op, const double* h_p, const double* h_q, const SolveOptions& o, Result& res);
+void sinkhorn_solve(Op& op, const double* p, const double* q, bool device_ptrs, const SolveOptions& o, Result& res);
 void op_log_matvec(Op& op, const double* h_in, bool transposed, double* h_out);
 double distance_lcn_device(Op& op, const Result& res);
 

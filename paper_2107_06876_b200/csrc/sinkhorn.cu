@@ -546,6 +546,20 @@ __global__ void dot_partial_kernel(const double* __restrict__ a, const double* _
     }
 }
 
+__global__ void sum_partial_kernel(const double* __restrict__ a, long long n, double* __restrict__ out) {
+    __shared__ double red[kWarps];
+    double s = 0.0;
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += 256LL * gridDim.x) s += a[i];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kWarps; ++w) t += red[w];
+        out[blockIdx.x] = t;
+    }
+}
+
 __global__ void log_kernel(const double* __restrict__ in, double* __restrict__ out, long long n) {
     long long i = blockIdx.x * 256LL + threadIdx.x;
     if (i < n) out[i] = log(in[i]);
@@ -573,7 +587,21 @@ struct Solver {
     DevBuf<double> log_p, log_q, pv, qv, log_s[2], log_t, row_marg, err_part, trace;
     DevBuf<double> Mr, Sr, Mc, Sc, corr_s, corr_t;                  // sparse / lcn band accumulators
     DevBuf<double> part, hpart, mnp, mxp, mid_s, mid_t;             // low-rank reductions
+    DevBuf<double> dpart;                                           // distance / mass partials
     size_t smem = 0;
+    bool attrs_set = false;
+    std::vector<cudaEvent_t> evs;                                   // phase events (profiling)
+    ~Solver() {
+        for (auto e : evs) cudaEventDestroy(e);
+    }
+    cudaEvent_t ev(size_t i) {
+        while (evs.size() <= i) {
+            cudaEvent_t e;
+            CUDA_OK(cudaEventCreate(&e));
+            evs.push_back(e);
+        }
+        return evs[i];
+    }
 
     explicit Solver(Op& o) : op(o), ctx(*o.ctx), s(o.ctx->stream), n(o.n), m(o.m), l(static_cast<int>(o.l)) {
         G = 4 * ctx.num_sms;
@@ -630,8 +658,10 @@ struct Solver {
     }
 
     void alloc() {
+        s = ctx.stream;
         st.resize(1);
         st.zero(s);
+        dpart.resize(256);
         log_p.resize(n); log_q.resize(m); pv.resize(n); qv.resize(m);
         log_s[0].resize(n); log_s[1].resize(n); log_t.resize(m); row_marg.resize(n);
         err_part.resize(std::max<long long>(G, ceil_div(n, 256)));
@@ -664,16 +694,23 @@ struct Solver {
     template <typename T>
     void sparse_iteration(int it, double tol, int max_iters) {
         const int cur = it % 2, nxt = (it + 1) % 2;
+        mark(it, 0);
         if (it > 0) {
             sparse_cols<T>(log_s[cur].get());
+            mark(it, 1);
             sparse_col_finalize_kernel<<<ceil_div(m, 256), 256, 0, s>>>(st.get(), Mc.get(), Sc.get(), log_q.get(), m,
                                                                         log_t.get());
+        } else {
+            mark(it, 1);
         }
+        mark(it, 2);
         sparse_rows<T>(log_t.get());
+        mark(it, 3);
         sparse_row_finalize_kernel<<<ceil_div(n, 256), 256, 0, s>>>(st.get(), Mr.get(), Sr.get(), log_p.get(), pv.get(),
                                                                     n, log_s[cur].get(), log_s[nxt].get(), nullptr,
                                                                     row_marg.get(), err_part.get(), it > 0);
         iter_end_kernel<<<1, 1, 0, s>>>(st.get(), err_part.get(), ceil_div(n, 256), it, max_iters, tol, trace.get());
+        mark(it, 4);
     }
 
     // -------- lcn / nystrom ------------------------------------------------
@@ -698,6 +735,7 @@ struct Solver {
     template <typename T>
     void lcn_iteration(int it, double tol, int max_iters) {
         const int cur = it % 2;
+        mark(it, 0);
         if (it == 0) {
             // kt = K(log t = 0) (sinkhorn.cpp:145): partial W^T 1 with shift 0.
 #define ACC0(L) launch_accum<T, L>(nullptr, m, Wt<T>())
@@ -705,25 +743,32 @@ struct Solver {
 #undef ACC0
             lowrank_reduce_kernel<<<ceil_div(l, 256), 256, 0, s>>>(st.get(), part.get(), hpart.get(), mnp.get(),
                                                                   mxp.get(), G, l, mid_t.get(), 0);
+            mark(it, 1);
         } else {
             lcn_cols<T>(log_s[cur].get());
+            mark(it, 1);
 #define COLF(L) launch_colfin<T, L>(0, nullptr)
             LCNB_LPL_DISPATCH(COLF)
 #undef COLF
             lowrank_reduce_kernel<<<ceil_div(l, 256), 256, 0, s>>>(st.get(), part.get(), hpart.get(), mnp.get(),
                                                                   mxp.get(), G, l, mid_t.get(), 0);
         }
+        mark(it, 2);
         lcn_rows<T>(log_t.get());
+        mark(it, 3);
 #define ROWF(L) launch_rowfin<T, L>(it, 0, nullptr)
         LCNB_LPL_DISPATCH(ROWF)
 #undef ROWF
         lowrank_reduce_kernel<<<ceil_div(l, 256), 256, 0, s>>>(st.get(), part.get(), hpart.get(), mnp.get(), mxp.get(),
                                                               G, l, mid_s.get(), 1);
         iter_end_kernel<<<1, 1, 0, s>>>(st.get(), err_part.get(), G, it, max_iters, tol, trace.get());
+        mark(it, 4);
     }
 
     template <typename T>
     void set_smem_attrs() {
+        if (attrs_set) return;
+        attrs_set = true;
         if (op.kind == 1 || smem <= 48 * 1024) return;
 #define ATTR(L)                                                                                                    \
     CUDA_OK(cudaFuncSetAttribute(lowrank_accum_kernel<T, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
@@ -733,27 +778,46 @@ struct Solver {
 #undef ATTR
     }
 
+    // phase marks: 0 start of iteration, 1 after col bands, 2 after col
+    // finalize+reduce, 3 after row bands, 4 after row finalize+reduce+end.
+    size_t mark_base = 0;
+    void mark(int it, int ph) {
+        if (ctx.profile) CUDA_OK(cudaEventRecord(ev(mark_base + static_cast<size_t>(it) * 5 + ph), s));
+    }
+
     template <typename T>
-    void run(const double* h_p, const double* h_q, const SolveOptions& o, Result& res) {
+    void run(const double* in_p, const double* in_q, bool device_ptrs, const SolveOptions& o, Result& res) {
         set_smem_attrs<T>();
         alloc();
-        trace.resize(std::max(o.max_iters, 1));
-        pv.upload(h_p, n, s);
-        qv.upload(h_q, m, s);
+        trace.resize(std::max<size_t>(std::max(o.max_iters, 1), trace.size()));
+        const cudaMemcpyKind kind = device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        CUDA_OK(cudaMemcpyAsync(pv.get(), in_p, n * 8, kind, s));
+        CUDA_OK(cudaMemcpyAsync(qv.get(), in_q, m * 8, kind, s));
         log_kernel<<<ceil_div(n, 256), 256, 0, s>>>(pv.get(), log_p.get(), n);
         log_kernel<<<ceil_div(m, 256), 256, 0, s>>>(qv.get(), log_q.get(), m);
-        log_s[0].zero(s);
-        log_s[1].zero(s);
-        log_t.zero(s);
-        row_marg.zero(s);
-        // tol: default 1e-6 * (sum p + sum q) (sinkhorn.cpp:130-133), host-side sum in order.
-        double mass = 0.0;
-        for (long long i = 0; i < n; ++i) mass += h_p[i];
-        for (long long j = 0; j < m; ++j) mass += h_q[j];
-        const double tol = o.tol >= 0.0 ? o.tol : 1e-6 * mass;
-        cudaEvent_t e0, e1;
-        CUDA_OK(cudaEventCreate(&e0));
-        CUDA_OK(cudaEventCreate(&e1));
+        CUDA_OK(cudaMemsetAsync(log_s[0].get(), 0, n * 8, s));
+        CUDA_OK(cudaMemsetAsync(log_s[1].get(), 0, n * 8, s));
+        CUDA_OK(cudaMemsetAsync(log_t.get(), 0, m * 8, s));
+        CUDA_OK(cudaMemsetAsync(row_marg.get(), 0, n * 8, s));
+        // tol: default 1e-6 * (sum p + sum q) (sinkhorn.cpp:130-133).
+        double tol = o.tol;
+        if (tol < 0.0) {
+            double mass = 0.0;
+            if (device_ptrs) {
+                sum_partial_kernel<<<64, 256, 0, s>>>(pv.get(), n, dpart.get());
+                sum_partial_kernel<<<64, 256, 0, s>>>(qv.get(), m, dpart.get() + 64);
+                std::vector<double> hp(128);
+                dpart.download(hp.data(), 128, s);
+                ctx.sync();
+                for (double v : hp) mass += v;
+            } else {
+                for (long long i = 0; i < n; ++i) mass += in_p[i];
+                for (long long j = 0; j < m; ++j) mass += in_q[j];
+            }
+            tol = 1e-6 * mass;
+        }
+        cudaEvent_t e0 = ev(0), e1 = ev(1);
+        mark_base = 2;
         CUDA_OK(cudaEventRecord(e0, s));
         const int chunk = tol > 0.0 ? 8 : o.max_iters + 1;
         DevState h{};
@@ -771,9 +835,20 @@ struct Solver {
         CUDA_OK(cudaEventSynchronize(e1));
         float ms = 0.f;
         CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
         res.device_ms = ms;
+        res.phase_ms.assign(4, 0.0);
+        res.phase_iters = 0;
+        if (ctx.profile) {
+            // iterations 1..iters ran all phases (iteration 0 has no column side)
+            for (int it = 1; it <= h.iters; ++it) {
+                for (int ph = 0; ph < 4; ++ph) {
+                    float t = 0.f;
+                    CUDA_OK(cudaEventElapsedTime(&t, ev(mark_base + it * 5 + ph), ev(mark_base + it * 5 + ph + 1)));
+                    res.phase_ms[ph] += t;
+                }
+            }
+            res.phase_iters = h.iters;
+        }
         if (h.status) {
             std::string name = op.name();
             if (h.status == 3)
@@ -797,11 +872,11 @@ struct Solver {
         if (h.iters) trace.download(res.err_trace.data(), h.iters, s);
         // distance = lambda (<log s, P1> + <log t, q>) (sinkhorn.cpp:178-183)
         const int DB = 64;
-        DevBuf<double> dp(2 * DB);
-        dot_partial_kernel<<<DB, 256, 0, s>>>(log_s[fin].get(), row_marg.get(), n, dp.get());
-        dot_partial_kernel<<<DB, 256, 0, s>>>(log_t.get(), qv.get(), m, dp.get() + DB);
+        double* dp = dpart.get();
+        dot_partial_kernel<<<DB, 256, 0, s>>>(log_s[fin].get(), row_marg.get(), n, dp);
+        dot_partial_kernel<<<DB, 256, 0, s>>>(log_t.get(), qv.get(), m, dp + DB);
         std::vector<double> hp(2 * DB);
-        dp.download(hp.data(), 2 * DB, s);
+        dpart.download(hp.data(), 2 * DB, s);
         ctx.sync();
         double acc = 0.0;
         for (double v : hp) acc += v;
@@ -878,15 +953,20 @@ struct Solver {
     }
 };
 
-void sinkhorn_solve(Op& op, const double* h_p, const double* h_q, const SolveOptions& o, Result& res) {
+Solver& solver_of(Op& op) {
+    if (!op.ws) op.ws = std::make_shared<Solver>(op);
+    return *op.ws;
+}
+
+void sinkhorn_solve(Op& op, const double* p, const double* q, bool device_ptrs, const SolveOptions& o, Result& res) {
     if (o.max_iters < 1) throw Status(2, "sinkhorn: max_iters must be >= 1");
-    Solver sv(op);
-    if (op.fp64) sv.run<double>(h_p, h_q, o, res);
-    else sv.run<float>(h_p, h_q, o, res);
+    Solver& sv = solver_of(op);
+    if (op.fp64) sv.run<double>(p, q, device_ptrs, o, res);
+    else sv.run<float>(p, q, device_ptrs, o, res);
 }
 
 void op_log_matvec(Op& op, const double* h_in, bool transposed, double* h_out) {
-    Solver sv(op);
+    Solver& sv = solver_of(op);
     if (op.fp64) sv.matvec<double>(h_in, transposed, h_out);
     else sv.matvec<float>(h_in, transposed, h_out);
 }

@@ -95,6 +95,10 @@ def library() -> C.CDLL:
             "lcn_ctx_create": ([I, I, PP], I),
             "lcn_ctx_destroy": ([P], I),
             "lcn_ctx_last_error": ([P], C.c_char_p),
+            "lcn_ctx_set_stream": ([P, P], I),
+            "lcn_ctx_set_profile": ([P, I], I),
+            "lcn_sinkhorn_device": ([P, P, P, C.POINTER(_SinkOpts), PP], I),
+            "lcn_result_phase_ms": ([P, P, C.POINTER(I)], I),
             "lcn_kmeans_pp_indices": ([P, P, SZ, SZ, SZ, U64, P, SZ, P, C.POINTER(SZ)], I),
             "lcn_assign_nearest": ([P, P, SZ, SZ, P, SZ, P], I),
             "lcn_lloyd": ([P, P, SZ, SZ, SZ, I, U64, P, P], I),
@@ -152,6 +156,13 @@ class Context:
     def check(self, rc: int):
         if rc != 0:
             raise _STATUS.get(rc, Error)(self.lib.lcn_ctx_last_error(self.h).decode())
+
+    def set_stream(self, stream_handle: int | None):
+        """Run on an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)."""
+        self.check(self.lib.lcn_ctx_set_stream(self.h, C.c_void_p(stream_handle) if stream_handle else None))
+
+    def set_profile(self, on: bool):
+        self.check(self.lib.lcn_ctx_set_profile(self.h, 1 if on else 0))
 
     def close(self):
         if getattr(self, "h", None):
@@ -432,6 +443,14 @@ class SinkhornResult:
         self.device_ms = info.device_ms
         self.warnings = [op.ctx.lib.lcn_result_warning(h, i).decode() for i in range(info.n_warnings)]
 
+    def phase_ms(self):
+        """Profiling: summed ms of (col bands, col finalize+reduce, row bands, row
+        finalize+reduce+end) over the iterations, and the iteration count."""
+        out = np.zeros(4)
+        it = C.c_int()
+        self.op.ctx.check(self.op.ctx.lib.lcn_result_phase_ms(self.h, _p(out), C.byref(it)))
+        return out, it.value
+
     def _vec(self, which):
         lib = self.op.ctx.lib
         n = C.c_size_t()
@@ -470,6 +489,14 @@ def sinkhorn(op: KernelOperator, p, q, opts: SinkhornOptions = SinkhornOptions()
     o = _SinkOpts(opts.tol, opts.max_iters, int(opts.check_support), int(opts.want_plan))
     h = C.c_void_p()
     op.ctx.check(op.ctx.lib.lcn_sinkhorn(op.h, _p(p), _p(q), C.byref(o), C.byref(h)))
+    return SinkhornResult(op, h)
+
+
+def sinkhorn_device(op: KernelOperator, d_p: int, d_q: int, opts: SinkhornOptions = SinkhornOptions()):
+    """sinkhorn on device-resident fp64 marginals (raw device pointers); no plan."""
+    o = _SinkOpts(opts.tol, opts.max_iters, int(opts.check_support), 0)
+    h = C.c_void_p()
+    op.ctx.check(op.ctx.lib.lcn_sinkhorn_device(op.h, C.c_void_p(d_p), C.c_void_p(d_q), C.byref(o), C.byref(h)))
     return SinkhornResult(op, h)
 
 
