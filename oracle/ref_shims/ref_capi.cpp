@@ -285,11 +285,11 @@ int ref_op_copy(void* h, int which, std::uint32_t* row_ptr, std::uint32_t* col, 
         if (vals) std::memcpy(vals, s.logvals.data(), s.logvals.size() * 8);
         return 0;
     }
-    if ((which == 1 || which == 5 || which == 6) && r->op.correction()) {
-        const LcnCorrection& c = *r->op.correction();
+    if ((which == 0 || which == 1 || which == 5 || which == 6) && r->op.correction()) {
+        const LcnCorrection& c = *r->op.correction();  // which 0 on an lcn operator: log K^sp = log_sp
         if (row_ptr) std::memcpy(row_ptr, c.row_ptr.data(), c.row_ptr.size() * 4);
         if (col) std::memcpy(col, c.col.data(), c.col.size() * 4);
-        const std::vector<double>& src = which == 1 ? c.delta : which == 5 ? c.nys_vals : c.log_sp;
+        const std::vector<double>& src = which == 1 ? c.delta : which == 5 ? c.nys_vals : c.log_sp;  // 0, 6: log_sp
         if (vals) std::memcpy(vals, src.data(), src.size() * 8);
         return 0;
     }
