@@ -130,12 +130,26 @@ void build_band_layout(Ctx& ctx, Band& B, const uint32_t* d_src_bucket, const ui
     stable_group(ctx, B.tgt_bucket.get(), m, nb, B.tgt_order, B.tgt_start, B.h_tgt_start, B.tgt_local);
     B.h_blk_off.assign(nb + 1, 0);
     std::vector<uint32_t> work;
+    B.real_entries = 0;
     for (size_t b = 0; b < nb; ++b) {
         unsigned long long nbk = B.h_src_start[b + 1] - B.h_src_start[b];
         unsigned long long mbk = B.h_tgt_start[b + 1] - B.h_tgt_start[b];
-        B.h_blk_off[b + 1] = B.h_blk_off[b] + nbk * mbk;
+        // rows padded to a multiple of 4 entries: every block row starts 16-byte
+        // aligned so the iteration kernels stream it as float4 / double2x2.
+        // ... and every block starts on a 128-byte line (32 entries) so the
+        // bulk-copy chunks of the streaming kernels are line aligned.
+        B.h_blk_off[b + 1] = (B.h_blk_off[b] + nbk * row_stride(mbk) + 31ull) & ~31ull;
+        B.real_entries += nbk * mbk;
         if (nbk && mbk) work.push_back(static_cast<uint32_t>(b));
     }
+    // largest blocks first: better tail balance for the per-bucket kernels
+    std::stable_sort(work.begin(), work.end(), [&](uint32_t x, uint32_t y) {
+        auto sz = [&](uint32_t k) {
+            return static_cast<unsigned long long>(B.h_src_start[k + 1] - B.h_src_start[k]) *
+                   (B.h_tgt_start[k + 1] - B.h_tgt_start[k]);
+        };
+        return sz(x) > sz(y);
+    });
     B.entries = B.h_blk_off[nb];
     B.blk_off.upload(B.h_blk_off.data(), nb + 1, s);
     B.n_work = work.size();
@@ -244,7 +258,7 @@ __global__ void __launch_bounds__(256) band_tile_kernel(const int4* __restrict__
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const uint32_t c = c0 + tx + 16 * j;
-            if (c < mb) epi(bv.blk_off[b] + static_cast<unsigned long long>(r) * mb + c, si, bv.tgt_order[tb + c], acc[i][j]);
+            if (c < mb) epi(bv.blk_off[b] + static_cast<unsigned long long>(r) * row_stride(mb) + c, si, bv.tgt_order[tb + c], acc[i][j]);
         }
     }
 }
@@ -368,6 +382,13 @@ struct EpiDelta {
     }
 };
 
+__global__ void fill_value_kernel(double* __restrict__ p, unsigned long long n, double v) {
+    for (unsigned long long i = blockIdx.x * 256ull + threadIdx.x; i < n; i += 256ull * gridDim.x) p[i] = v;
+}
+void fill_value(Ctx& ctx, double* p, unsigned long long n, double v) {
+    if (n) fill_value_kernel<<<std::min<long long>(ceil_div(n, 256), 16 * ctx.num_sms), 256, 0, ctx.stream>>>(p, n, v);
+}
+
 __global__ void norms_kernel(const double* __restrict__ X, long long N, int d, double* __restrict__ out) {
     long long i = blockIdx.x * 256LL + threadIdx.x;
     if (i < N) {
@@ -440,13 +461,14 @@ void build_sparse_values(Op& op) {
     const bool dot = op.cost == 1 || op.cost == 2;  // negative-dot / cosine fold x.y, else (x-y)^2
     for (size_t b = 0; b < op.bands.size(); ++b) {
         DevBuf<double> v(std::max<unsigned long long>(op.bands[b].entries, 1));
+        fill_value(ctx, v.get(), op.bands[b].entries, kNegInf);  // row padding: log K = -inf
         EpiLogK epi{v.get(), op.bandset(), static_cast<int>(b), op.cost, 1.0 / op.lambda, nrm,
                     static_cast<long long>(op.n), bad.get()};
         if (dot)
             launch_band_tiles<1>(ctx, op.bands[b], op.view(static_cast<int>(b)), op.P(), op.Q(), static_cast<int>(op.d), epi);
         else
             launch_band_tiles<0>(ctx, op.bands[b], op.view(static_cast<int>(b)), op.P(), op.Q(), static_cast<int>(op.d), epi);
-        op.stored += op.bands[b].entries;
+        op.stored += op.bands[b].real_entries;
         op.val64.push_back(std::move(v));
     }
     if (read_flag(ctx, bad)) throw Status(2, "cosine-derived cost undefined for zero vectors");
@@ -676,6 +698,7 @@ void build_correction(Op& op) {
     overflow.zero(ctx.stream);
     for (size_t b = 0; b < op.bands.size(); ++b) {
         DevBuf<double> dlt(std::max<unsigned long long>(op.bands[b].entries, 1));
+        fill_value(ctx, dlt.get(), op.bands[b].entries, 0.0);  // row padding: delta = 0
         EpiDelta epi{dlt.get(), op.logk64[b].get(), maxbits.get(), overflow.get()};
         launch_band_tiles<1>(ctx, op.bands[b], op.view(static_cast<int>(b)), op.U64.get(), op.Wt64.get(),
                              static_cast<int>(op.l), epi);
@@ -697,22 +720,49 @@ void to_f32(Ctx& ctx, const DevBuf<double>& in, DevBuf<float>& out, size_t n) {
     if (n) to_f32_kernel<<<std::min<long long>(ceil_div(n, 256), 8 * ctx.num_sms), 256, 0, ctx.stream>>>(in.get(), out.get(), n);
     LAUNCH_OK("to_f32");
 }
+// rows x l -> rows x lp (zero padded), converted to T
+template <typename T>
+__global__ void pad_rows_kernel(const double* __restrict__ in, long long rows, int l, int lp, T* __restrict__ out) {
+    for (long long e = blockIdx.x * 256LL + threadIdx.x; e < rows * lp; e += 256LL * gridDim.x) {
+        long long r = e / lp;
+        int a = static_cast<int>(e % lp);
+        out[e] = a < l ? static_cast<T>(in[r * l + a]) : T(0);
+    }
+}
+template <typename T>
+void pad_rows(Ctx& ctx, const DevBuf<double>& in, size_t rows, size_t l, size_t lp, DevBuf<T>& out) {
+    out.resize(std::max<size_t>(rows * lp, 1));
+    if (rows)
+        pad_rows_kernel<T><<<std::min<long long>(ceil_div(rows * lp, 256), 16 * ctx.num_sms), 256, 0, ctx.stream>>>(
+            in.get(), rows, static_cast<int>(l), static_cast<int>(lp), out.get());
+    LAUNCH_OK("pad_rows");
+}
 }  // namespace
 
-// fp32 iteration copies (fp32 storage, fp64 accumulation).
+// Iteration copies (fp32 storage, fp64 accumulation;
+// fp64 storage in the exact mode). Low-rank factor rows are padded to
+// lp = round_up(l, 4) entries so each row starts 16-byte aligned.
 void finalize_storage(Op& op) {
-    if (op.fp64) return;
-    op.val32.clear();
-    for (size_t b = 0; b < op.bands.size(); ++b) {
-        DevBuf<float> v;
-        to_f32(*op.ctx, op.val64[b], v, op.bands[b].entries);
-        op.val32.push_back(std::move(v));
+    Ctx& ctx = *op.ctx;
+    op.lp = (op.l + 3) & ~size_t(3);
+    if (!op.fp64) {
+        op.val32.clear();
+        for (size_t b = 0; b < op.bands.size(); ++b) {
+            DevBuf<float> v;
+            to_f32(ctx, op.val64[b], v, op.bands[b].entries);
+            op.val32.push_back(std::move(v));
+        }
     }
     if (op.kind >= 2) {
-        to_f32(*op.ctx, op.U64, op.U32, op.n * op.l);
-        to_f32(*op.ctx, op.Wt64, op.Wt32, op.m * op.l);
+        if (op.fp64) {
+            pad_rows<double>(ctx, op.U64, op.n, op.l, op.lp, op.U64p);
+            pad_rows<double>(ctx, op.Wt64, op.m, op.l, op.lp, op.Wt64p);
+        } else {
+            pad_rows<float>(ctx, op.U64, op.n, op.l, op.lp, op.U32);
+            pad_rows<float>(ctx, op.Wt64, op.m, op.l, op.lp, op.Wt32);
+        }
     }
-    op.ctx->sync();
+    ctx.sync();
 }
 
 // ---------------------------------------------------------------------------
@@ -814,7 +864,7 @@ __device__ __forceinline__ unsigned long long entry_index(const BandViews& bvs, 
         if (bk == v.tgt_bucket[j]) {
             *band = b;
             uint32_t mb = v.tgt_start[bk + 1] - v.tgt_start[bk];
-            return v.blk_off[bk] + static_cast<unsigned long long>(v.src_local[i]) * mb + v.tgt_local[j];
+            return v.blk_off[bk] + static_cast<unsigned long long>(v.src_local[i]) * row_stride(mb) + v.tgt_local[j];
         }
     }
     *band = -1;

@@ -56,6 +56,9 @@ class DevBuf {
     size_t n_ = 0;
 };
 
+// Row stride of a bucket block: m_b padded to a multiple of 4 entries.
+__host__ __device__ __forceinline__ unsigned long long row_stride(unsigned long long mb) { return (mb + 3ull) & ~3ull; }
+
 struct Ctx {
     int device = 0;
     int store_fp64 = 0;
@@ -91,7 +94,8 @@ struct Band {
     DevBuf<uint32_t> tgt_local;    // m
     DevBuf<uint32_t> work;         // list of buckets with a nonempty block
     size_t n_work = 0;
-    unsigned long long entries = 0;
+    unsigned long long entries = 0;       // padded block entries held in HBM
+    unsigned long long real_entries = 0;  // sum n_b * m_b
     std::vector<uint32_t> h_src_start, h_tgt_start;
     std::vector<unsigned long long> h_blk_off;
 };

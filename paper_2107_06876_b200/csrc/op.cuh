@@ -52,7 +52,9 @@ struct Op {
     // Nystrom / LCN
     DevBuf<double> L;                     // l x d landmarks
     DevBuf<double> U64, Wt64;             // n x l, m x l (W transposed)
-    DevBuf<float> U32, Wt32;
+    DevBuf<float> U32, Wt32;              // iteration copies, rows padded to lp (fp32 mode)
+    DevBuf<double> U64p, Wt64p;           // iteration copies, rows padded to lp (fp64 mode)
+    size_t lp = 0;
     double max_abs_delta = 0.0, cond = 0.0;
     // CSR export (lazy)
     DevBuf<uint32_t> csr_row_ptr, csr_col;

@@ -5,17 +5,25 @@
 // application and marginal error (sinkhorn.cpp:149-168). On the device it is a
 // fixed sequence of kernels, all enqueued ahead and gated by a device-side
 // `done` flag, so the host never waits inside the loop:
-//   col side  : [band blocks: K_sp^T / Delta^T over each bucket] -> col finalize
-//               (low-rank W^T mid, positivity, log t = log q - K^T(log s),
-//               finiteness, and - LCN - the partial W tt of the next half)
-//               -> low-rank reduce (global shift H_t, mid_t = W tt)
-//   row side  : [band blocks] -> row finalize (U mid, kt, row marginal, err
-//               partial, next log s, partial U^T ss) -> iteration end
-//               (err, convergence, error precedence, next shift H_s).
+//   col side : band blocks (Delta^T ss per band / sparse column LSE)  ->
+//              low-rank pass over W^T rows (W^T_j . mid_s + corrections,
+//              positivity, log t = log q - K^T(log s), finiteness, and the
+//              partial W tt of the next half)  ->  reduce (H_t, mid_t)
+//   row side : band blocks  ->  low-rank pass over U rows (kt, row marginal,
+//              error partial, next log s, partial U^T ss)  ->  reduce + end
 // Low-rank shifts: the reference shifts by the global max of the input log
-// vector (operator.cpp:147-151); here each warp keeps a running max with
-// online rescaling and the reduce rescales block partials to the global max,
-// which is the same product in exact arithmetic and needs no extra pass.
+// vector (operator.cpp:147-151); each CTA keeps a running max with online
+// rescaling and the reduce rescales the CTA partials to the global max — the
+// same product in exact arithmetic, with no extra pass over the factors.
+//
+// Streaming design (HBM-bound passes). Loaded HBM latency on this part is a
+// few microseconds, so an SM needs ~200 KB of reads in flight to approach
+// peak (Little's law). Both the low-rank pass and the band passes are
+// warp-specialized: producer warps keep a shared-memory ring full with
+// cp.async.bulk copies (SASS UBLKCP) tracked by mbarriers, consumer warps
+// only wait on `full` barriers and compute from shared memory. Block rows are
+// padded to 16-byte multiples and blocks start on 128-byte lines (build.cu),
+// factor rows to lp = round_up(l, 4).
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -23,6 +31,7 @@
 #include <cstring>
 #include <type_traits>
 
+#include "async.cuh"
 #include "op.cuh"
 
 namespace lcnb {
@@ -50,16 +59,36 @@ struct DevState {
     int allpos_s, allpos_t;
 };
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 256;  // consumer threads per CTA
 constexpr int kWarps = kThreads / 32;
-constexpr int kTile = 4096;  // bucket-side vector tile staged in shared memory
+constexpr int kTile = 4096;    // bucket-side vector tile of the per-bucket kernels
 
-__device__ __forceinline__ double ld_val(const float* p, unsigned long long i) { return static_cast<double>(__ldg(p + i)); }
-__device__ __forceinline__ double ld_val(const double* p, unsigned long long i) { return __ldg(p + i); }
+template <typename T>
+struct Raw4 {
+    T v[4];
+};
+__device__ __forceinline__ Raw4<float> raw4(const float* p) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+    return {{v.x, v.y, v.z, v.w}};
+}
+__device__ __forceinline__ Raw4<double> raw4(const double* p) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    return {{a.x, a.y, b.x, b.y}};
+}
+__device__ __forceinline__ double ld1(const float* p) { return static_cast<double>(__ldg(p)); }
+__device__ __forceinline__ double ld1(const double* p) { return __ldg(p); }
+
+// consumer-only barrier (producer warps never join)
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory"); }
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 
 // ---------------------------------------------------------------------------
-// Sparse (log-domain) band kernels: per bucket block, per row / column online
-// log-sum-exp, merged across bands as (max, sum) pairs.
+// Sparse (log-domain) band kernels: per bucket block, per row / column
+// log-sum-exp (sparse_kernel.cpp:119-155), merged across bands as (max, sum).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void lse_merge(double& M, double& S, double m2, double s2) {
     if (m2 == kNegInf) return;
@@ -79,6 +108,7 @@ __global__ void __launch_bounds__(kThreads) sparse_row_band_kernel(const DevStat
     const uint32_t b = work[blockIdx.x];
     const uint32_t sb = bv.src_start[b], nb = bv.src_start[b + 1] - sb;
     const uint32_t tb = bv.tgt_start[b], mb = bv.tgt_start[b + 1] - tb;
+    const unsigned long long ms = row_stride(mb);
     const unsigned long long off = bv.blk_off[b];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (uint32_t c0 = 0; c0 < mb; c0 += kTile) {
@@ -87,13 +117,13 @@ __global__ void __launch_bounds__(kThreads) sparse_row_band_kernel(const DevStat
         for (uint32_t c = threadIdx.x; c < cn; c += kThreads) lt[c] = log_t[bv.tgt_order[tb + c0 + c]];
         __syncthreads();
         for (uint32_t r = warp; r < nb; r += kWarps) {
-            const unsigned long long row = off + static_cast<unsigned long long>(r) * mb + c0;
+            const T* row = vals + off + r * ms + c0;
             double hi = kNegInf;
-            for (uint32_t c = lane; c < cn; c += 32) hi = fmax(hi, ld_val(vals, row + c) + lt[c]);
+            for (uint32_t c = lane; c < cn; c += 32) hi = fmax(hi, ld1(row + c) + lt[c]);
             hi = warp_max(hi);
             double acc = 0.0;
             if (hi != kNegInf)
-                for (uint32_t c = lane; c < cn; c += 32) acc += exp(ld_val(vals, row + c) + lt[c] - hi);
+                for (uint32_t c = lane; c < cn; c += 32) acc += exp(ld1(row + c) + lt[c] - hi);
             acc = warp_sum(acc);
             if (lane == 0) {
                 const uint32_t i = bv.src_order[sb + r];
@@ -117,6 +147,7 @@ __global__ void __launch_bounds__(kThreads) sparse_col_band_kernel(const DevStat
     const uint32_t b = work[blockIdx.x];
     const uint32_t sb = bv.src_start[b], nb = bv.src_start[b + 1] - sb;
     const uint32_t tb = bv.tgt_start[b], mb = bv.tgt_start[b + 1] - tb;
+    const unsigned long long ms = row_stride(mb);
     const unsigned long long off = bv.blk_off[b];
     for (uint32_t r0 = 0; r0 < nb; r0 += kTile) {
         const uint32_t rn = min(nb - r0, static_cast<uint32_t>(kTile));
@@ -125,11 +156,10 @@ __global__ void __launch_bounds__(kThreads) sparse_col_band_kernel(const DevStat
         __syncthreads();
         for (uint32_t c = threadIdx.x; c < mb; c += kThreads) {
             double hi = kNegInf;
-            for (uint32_t r = 0; r < rn; ++r) hi = fmax(hi, ld_val(vals, off + static_cast<unsigned long long>(r0 + r) * mb + c) + ls[r]);
+            for (uint32_t r = 0; r < rn; ++r) hi = fmax(hi, ld1(vals + off + (r0 + r) * ms + c) + ls[r]);
             double acc = 0.0;
             if (hi != kNegInf)
-                for (uint32_t r = 0; r < rn; ++r)
-                    acc += exp(ld_val(vals, off + static_cast<unsigned long long>(r0 + r) * mb + c) + ls[r] - hi);
+                for (uint32_t r = 0; r < rn; ++r) acc += exp(ld1(vals + off + (r0 + r) * ms + c) + ls[r] - hi);
             const uint32_t j = bv.tgt_order[tb + c];
             double M = Mcol[j], S = Scol[j];
             lse_merge(M, S, hi, acc);
@@ -196,183 +226,705 @@ __global__ void sparse_row_finalize_kernel(DevState* __restrict__ st, const doub
 }
 
 // ---------------------------------------------------------------------------
-// LCN (linear-space) band kernels: correction products Delta tt / Delta^T ss.
+// LCN band kernels for oversized buckets (either side > kBandVec). Work items
+// are (bucket, chunk): the row kernel's chunk is a range of kItemRows rows,
+// the column kernel's a range of 256 columns, so a large bucket spreads over
+// several CTAs and every output is written by exactly one CTA (plain stores).
 // ---------------------------------------------------------------------------
+constexpr int kRowsPerWarp = 8;
+constexpr int kItemRows = 64;
+
 template <typename T>
-__global__ void __launch_bounds__(kThreads) lcn_row_band_kernel(const DevState* __restrict__ st, BandView bv,
-                                                                const uint32_t* __restrict__ work,
+__global__ void __launch_bounds__(kThreads, 3) lcn_row_band_kernel(const DevState* __restrict__ st, BandView bv,
+                                                                const uint2* __restrict__ items,
                                                                 const T* __restrict__ vals,
                                                                 const double* __restrict__ log_t,
                                                                 double* __restrict__ corr) {
     if (st->done) return;
-    __shared__ double tt[kTile];
+    __shared__ __align__(16) double tt[kTile];
     const double H = st->H_t;
-    const uint32_t b = work[blockIdx.x];
-    const uint32_t sb = bv.src_start[b], nb = bv.src_start[b + 1] - sb;
+    const uint32_t b = items[blockIdx.x].x;
+    const uint32_t rbeg = items[blockIdx.x].y * kItemRows;
+    const uint32_t nb_all = bv.src_start[b + 1] - bv.src_start[b];
+    const uint32_t sb = bv.src_start[b] + rbeg;
+    const uint32_t nb = min(nb_all - rbeg, static_cast<uint32_t>(kItemRows));
     const uint32_t tb = bv.tgt_start[b], mb = bv.tgt_start[b + 1] - tb;
-    const unsigned long long off = bv.blk_off[b];
+    const uint32_t ms = static_cast<uint32_t>(row_stride(mb));
+    const unsigned long long off = bv.blk_off[b] + static_cast<unsigned long long>(rbeg) * ms;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint32_t c0 = 0; c0 < mb; c0 += kTile) {
-        const uint32_t cn = min(mb - c0, static_cast<uint32_t>(kTile));
+    for (uint32_t c0 = 0; c0 < ms; c0 += kTile) {
+        const uint32_t cn = min(ms - c0, static_cast<uint32_t>(kTile));  // multiple of 4
         __syncthreads();
-        for (uint32_t c = threadIdx.x; c < cn; c += kThreads) tt[c] = exp(log_t[bv.tgt_order[tb + c0 + c]] - H);
+        for (uint32_t c = threadIdx.x; c < cn; c += kThreads)
+            tt[c] = c0 + c < mb ? exp(log_t[bv.tgt_order[tb + c0 + c]] - H) : 0.0;
         __syncthreads();
-        for (uint32_t r = warp; r < nb; r += kWarps) {
-            const unsigned long long row = off + static_cast<unsigned long long>(r) * mb + c0;
-            double acc = 0.0;
-            for (uint32_t c = lane; c < cn; c += 32) acc += ld_val(vals, row + c) * tt[c];
-            acc = warp_sum(acc);
-            if (lane == 0) corr[bv.src_order[sb + r]] += acc;
+        const uint32_t nq = cn / 4;
+        for (uint32_t r0 = warp * kRowsPerWarp; r0 < nb; r0 += kWarps * kRowsPerWarp) {
+            double acc[kRowsPerWarp];
+#pragma unroll
+            for (int j = 0; j < kRowsPerWarp; ++j) acc[j] = 0.0;
+            for (uint32_t q = lane; q < nq; q += 32) {
+                Raw4<T> v[kRowsPerWarp];
+#pragma unroll
+                for (int j = 0; j < kRowsPerWarp; ++j) {
+                    if (r0 + j < nb) v[j] = raw4(vals + off + static_cast<unsigned long long>(r0 + j) * ms + c0 + 4 * q);
+                    else v[j].v[0] = v[j].v[1] = v[j].v[2] = v[j].v[3] = T(0);
+                }
+                const double t0 = tt[4 * q], t1 = tt[4 * q + 1], t2 = tt[4 * q + 2], t3 = tt[4 * q + 3];
+#pragma unroll
+                for (int j = 0; j < kRowsPerWarp; ++j)
+                    acc[j] += static_cast<double>(v[j].v[0]) * t0 + static_cast<double>(v[j].v[1]) * t1 +
+                              static_cast<double>(v[j].v[2]) * t2 + static_cast<double>(v[j].v[3]) * t3;
+            }
+#pragma unroll
+            for (int j = 0; j < kRowsPerWarp; ++j) acc[j] = warp_sum(acc[j]);
+            if (lane < kRowsPerWarp && r0 + lane < nb) {
+                double a = acc[0];
+#pragma unroll
+                for (int j = 1; j < kRowsPerWarp; ++j)
+                    if (lane == j) a = acc[j];
+                const uint32_t i = bv.src_order[sb + r0 + lane];
+                corr[i] = c0 == 0 ? a : corr[i] + a;
+            }
         }
     }
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kThreads) lcn_col_band_kernel(const DevState* __restrict__ st, BandView bv,
-                                                                const uint32_t* __restrict__ work,
+__global__ void __launch_bounds__(kThreads, 3) lcn_col_band_kernel(const DevState* __restrict__ st, BandView bv,
+                                                                const uint2* __restrict__ items,
                                                                 const T* __restrict__ vals,
                                                                 const double* __restrict__ log_s,
                                                                 double* __restrict__ corr) {
     if (st->done) return;
+    constexpr int kGroups = 4, kGT = kThreads / kGroups;  // 64 quads (256 columns) per chunk
     __shared__ double ss[kTile];
+    __shared__ double red[kGroups][kGT * 4];
     const double H = st->H_s;
-    const uint32_t b = work[blockIdx.x];
+    const uint32_t b = items[blockIdx.x].x;
+    const uint32_t qbeg = items[blockIdx.x].y * kGT;
     const uint32_t sb = bv.src_start[b], nb = bv.src_start[b + 1] - sb;
     const uint32_t tb = bv.tgt_start[b], mb = bv.tgt_start[b + 1] - tb;
+    const uint32_t ms = static_cast<uint32_t>(row_stride(mb));
     const unsigned long long off = bv.blk_off[b];
+    const int g = threadIdx.x / kGT, t = threadIdx.x % kGT;
     for (uint32_t r0 = 0; r0 < nb; r0 += kTile) {
         const uint32_t rn = min(nb - r0, static_cast<uint32_t>(kTile));
         __syncthreads();
         for (uint32_t r = threadIdx.x; r < rn; r += kThreads) ss[r] = exp(log_s[bv.src_order[sb + r0 + r]] - H);
         __syncthreads();
-        for (uint32_t c = threadIdx.x; c < mb; c += kThreads) {
-            double acc = 0.0;
-            for (uint32_t r = 0; r < rn; ++r) acc += ld_val(vals, off + static_cast<unsigned long long>(r0 + r) * mb + c) * ss[r];
-            corr[bv.tgt_order[tb + c]] += acc;
+        const uint32_t q = qbeg + t;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        if (q < ms / 4) {
+            const T* col = vals + off + static_cast<unsigned long long>(r0) * ms + 4 * q;
+            uint32_t r = g;
+            for (; r + 3 * kGroups < rn; r += 4 * kGroups) {
+                const Raw4<T> v0 = raw4(col + static_cast<unsigned long long>(r) * ms);
+                const Raw4<T> v1 = raw4(col + static_cast<unsigned long long>(r + kGroups) * ms);
+                const Raw4<T> v2 = raw4(col + static_cast<unsigned long long>(r + 2 * kGroups) * ms);
+                const Raw4<T> v3 = raw4(col + static_cast<unsigned long long>(r + 3 * kGroups) * ms);
+                const double s0 = ss[r], s1 = ss[r + kGroups], s2 = ss[r + 2 * kGroups], s3 = ss[r + 3 * kGroups];
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    acc[k] += static_cast<double>(v0.v[k]) * s0 + static_cast<double>(v1.v[k]) * s1 +
+                              static_cast<double>(v2.v[k]) * s2 + static_cast<double>(v3.v[k]) * s3;
+            }
+            for (; r < rn; r += kGroups) {
+                const Raw4<T> v0 = raw4(col + static_cast<unsigned long long>(r) * ms);
+                const double s0 = ss[r];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) acc[k] += static_cast<double>(v0.v[k]) * s0;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) red[g][4 * t + k] = acc[k];
+        __syncthreads();
+        const uint32_t c = 4 * qbeg + threadIdx.x;  // 256 threads cover the chunk's 256 columns
+        if (c < mb) {
+            const double a = red[0][threadIdx.x] + red[1][threadIdx.x] + red[2][threadIdx.x] + red[3][threadIdx.x];
+            const uint32_t j = bv.tgt_order[tb + c];
+            corr[j] = r0 == 0 ? a : corr[j] + a;
         }
     }
 }
 
-__global__ void zero_kernel(const DevState* __restrict__ st, double* __restrict__ p, long long n) {
-    if (st->done) return;
-    long long i = blockIdx.x * 256LL + threadIdx.x;
-    if (i < n) p[i] = 0.0;
-}
+// ---------------------------------------------------------------------------
+// Streaming band kernels (warp-specialized), one persistent CTA per SM taking
+// buckets w = blockIdx.x, blockIdx.x + gridDim.x, ... of the size-sorted work
+// list. Warp kWarps streams the bucket's rows through a ring of kBandStages
+// shared stages with bulk copies; warp kWarps+1 gathers the bucket's scaling
+// values (tt_c = exp(log t - H_t) for the row pass, ss_r = exp(log s - H_s)
+// for the column pass) and output indices into one of two slots. The 8
+// consumer warps only wait on mbarriers and compute from shared memory.
+// ROWS = true: corr[src] = sum_c delta[r][c] tt[c]  (K side)
+// ROWS = false: corr[tgt] = sum_r delta[r][c] ss[r]  (K^T side)
+// Each band has its own corr vector (plain stores; rows of buckets without
+// a partner stay 0).
+// ---------------------------------------------------------------------------
+constexpr int kBandStages = 10;
+constexpr int kBandStageBytes = 16 * 1024;
+constexpr int kBandVec = 1024;  // max bucket side handled by the streaming kernels
+constexpr int kColGroups = 2;   // column pass: row groups of kThreads / kColGroups threads
 
-// ---------------------------------------------------------------------------
-// Low-rank passes. A warp owns a row of the tall factor F (U: n x l, or W^T:
-// m x l); lane a-slices are a = lane + 32 k. The finalize kernel computes
-// y = F_row . mid + corr, checks it, produces the new log vector, and folds
-// F_row * exp(v - h) into the warp's running partial of the next product,
-// rescaling when the running max h grows.
-// ---------------------------------------------------------------------------
-template <int LPL>
-struct Partial {
-    double h;
-    double acc[LPL];
-    __device__ void init() {
-        h = kNegInf;
-#pragma unroll
-        for (int k = 0; k < LPL; ++k) acc[k] = 0.0;
-    }
-    template <typename T>
-    __device__ void add(const T* __restrict__ row, int l, int lane, double v) {
-        if (!(v > kNegInf && v < kPosInf)) return;  // non-finite inputs are flagged elsewhere
-        if (v > h) {
-            double sc = h == kNegInf ? 0.0 : exp(h - v);
-#pragma unroll
-            for (int k = 0; k < LPL; ++k) acc[k] *= sc;
-            h = v;
-        }
-        const double w = exp(v - h);
-#pragma unroll
-        for (int k = 0; k < LPL; ++k) {
-            int a = lane + 32 * k;
-            if (a < l) acc[k] += static_cast<double>(row[a]) * w;
-        }
-    }
+struct BandSmem {
+    unsigned char ring[kBandStages][kBandStageBytes];
+    double vec[2][kBandVec];           // tt (row pass) / ss (column pass) per bucket slot
+    uint32_t out[2][kBandVec];         // output index per row (row pass) / column (column pass)
+    double red[kColGroups][kBandVec];  // column pass: per-row-group partial sums
+    uint64_t full[kBandStages], empty[kBandStages], vfull[2], vempty[2];
 };
 
-// Combine the warps' partials of a block into one (h_b, partial_b[l]).
-template <int LPL>
-__device__ void block_combine(Partial<LPL>& P, int l, double* __restrict__ part_out, double* __restrict__ h_out,
-                              double vmin, double vmax, double* __restrict__ min_out, double* __restrict__ max_out) {
-    extern __shared__ double sm[];  // [kWarps * l] + [kWarps] h + 2*kWarps
-    double* sp = sm;
-    double* sh = sm + kWarps * l;
-    double* smin = sh + kWarps;
-    double* smax = smin + kWarps;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    vmin = -warp_max(-vmin);
-    vmax = warp_max(vmax);
-#pragma unroll
-    for (int k = 0; k < LPL; ++k) {
-        int a = lane + 32 * k;
-        if (a < l) sp[warp * l + a] = P.acc[k];
-    }
-    if (lane == 0) {
-        sh[warp] = P.h;
-        smin[warp] = vmin;
-        smax[warp] = vmax;
+// rows per ring stage; a multiple of 8 keeps every chunk start 128-byte
+// aligned (row bytes are a multiple of 16, block starts of 128)
+template <typename T>
+__device__ __forceinline__ int band_rows_per_stage(uint32_t ms) {
+    int r = static_cast<int>(kBandStageBytes / (ms * sizeof(T)));
+    if (r >= 8) r &= ~7;
+    return r < 1 ? 1 : r;
+}
+
+template <typename T, bool ROWS>
+__global__ void __launch_bounds__(kThreads + 64, 1) band_stream_kernel(const DevState* __restrict__ st, BandView bv,
+                                                                      const uint32_t* __restrict__ work, int nwork,
+                                                                      const T* __restrict__ vals,
+                                                                      const double* __restrict__ logv,
+                                                                      double* __restrict__ corr) {
+    if (st->done) return;
+    extern __shared__ __align__(128) unsigned char dyn[];
+    BandSmem& sm = *reinterpret_cast<BandSmem*>(dyn);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const double H = ROWS ? st->H_t : st->H_s;
+    if (tid == 0) {
+        for (int k = 0; k < kBandStages; ++k) {
+            mbar_init(&sm.full[k], 1);
+            mbar_init(&sm.empty[k], kWarps);
+        }
+        for (int k = 0; k < 2; ++k) {
+            mbar_init(&sm.vfull[k], 1);
+            mbar_init(&sm.vempty[k], kWarps);
+        }
+        fence_mbar_init();
     }
     __syncthreads();
-    double H = kNegInf;
-    for (int w = 0; w < kWarps; ++w) H = fmax(H, sh[w]);
-    for (int a = threadIdx.x; a < l; a += kThreads) {
-        double s = 0.0;
-        if (H != kNegInf)
-            for (int w = 0; w < kWarps; ++w)
-                if (sh[w] != kNegInf) s += sp[w * l + a] * exp(sh[w] - H);
-        part_out[static_cast<long long>(blockIdx.x) * l + a] = s;
+    if (warp == kWarps) {
+        // ---------------- producer 1: bulk copies of the block rows ----------------
+        if (lane == 0) {
+            int chunk = 0;
+            for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+                const uint32_t b = work[w];
+                const uint32_t nb = bv.src_start[b + 1] - bv.src_start[b];
+                const uint32_t ms = static_cast<uint32_t>(row_stride(bv.tgt_start[b + 1] - bv.tgt_start[b]));
+                const int R = band_rows_per_stage<T>(ms);
+                const T* blk = vals + bv.blk_off[b];
+                for (uint32_t r0 = 0; r0 < nb; r0 += R, ++chunk) {
+                    const int stage = chunk % kBandStages;
+                    const uint32_t nr = nb - r0 < static_cast<uint32_t>(R) ? nb - r0 : static_cast<uint32_t>(R);
+                    if (chunk >= kBandStages) mbar_wait(&sm.empty[stage], ((chunk / kBandStages) - 1) & 1);
+                    const uint32_t bytes = nr * ms * static_cast<uint32_t>(sizeof(T));
+                    mbar_arrive_expect_tx(&sm.full[stage], bytes);
+                    bulk_g2s(sm.ring[stage], blk + static_cast<unsigned long long>(r0) * ms, bytes, &sm.full[stage]);
+                }
+            }
+        }
+        return;
     }
-    if (threadIdx.x == 0) {
-        h_out[blockIdx.x] = H;
-        double mn = kPosInf, mx = kNegInf;
-        for (int w = 0; w < kWarps; ++w) { mn = fmin(mn, smin[w]); mx = fmax(mx, smax[w]); }
-        min_out[blockIdx.x] = mn;
-        max_out[blockIdx.x] = mx;
+    if (warp == kWarps + 1) {
+        // ---------------- producer 2: gathered scaling values + output indices ----------------
+        int kb = 0;
+        for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++kb) {
+            const uint32_t b = work[w];
+            const uint32_t sb = bv.src_start[b], nb = bv.src_start[b + 1] - sb;
+            const uint32_t tb = bv.tgt_start[b], mb = bv.tgt_start[b + 1] - tb;
+            const uint32_t count = ROWS ? static_cast<uint32_t>(row_stride(mb)) : nb;
+            const uint32_t valid = ROWS ? mb : nb;
+            const uint32_t* order = ROWS ? bv.tgt_order + tb : bv.src_order + sb;
+            const int slot = kb & 1;
+            if (kb >= 2) mbar_wait(&sm.vempty[slot], ((kb >> 1) - 1) & 1);
+            constexpr int kB = 8;  // independent gathers in flight per lane
+            for (uint32_t base = 0; base < count; base += 32 * kB) {
+                uint32_t idx[kB];
+#pragma unroll
+                for (int k = 0; k < kB; ++k) {
+                    const uint32_t c = base + lane + 32 * k;
+                    idx[k] = c < valid ? __ldg(order + c) : 0u;
+                }
+                double lv[kB];
+#pragma unroll
+                for (int k = 0; k < kB; ++k) {
+                    const uint32_t c = base + lane + 32 * k;
+                    lv[k] = c < valid ? __ldg(logv + idx[k]) : kNegInf;
+                }
+#pragma unroll
+                for (int k = 0; k < kB; ++k) {
+                    const uint32_t c = base + lane + 32 * k;
+                    if (c < count) sm.vec[slot][c] = lv[k] == kNegInf ? 0.0 : exp(lv[k] - H);
+                }
+            }
+            // destinations of the results: sources (row pass) / targets (column pass)
+            const uint32_t* dst = ROWS ? bv.src_order + sb : bv.tgt_order + tb;
+            const uint32_t ndst = ROWS ? nb : mb;
+            for (uint32_t c = lane; c < ndst; c += 32) sm.out[slot][c] = __ldg(dst + c);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.vfull[slot]);
+        }
+        return;
+    }
+    // ---------------- consumers ----------------
+    constexpr int kGT = kThreads / kColGroups;
+    const int g = tid / kGT, t = tid % kGT;
+    int chunk = 0, kb = 0;
+    for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++kb) {
+        const uint32_t b = work[w];
+        const uint32_t nb = bv.src_start[b + 1] - bv.src_start[b];
+        const uint32_t mb = bv.tgt_start[b + 1] - bv.tgt_start[b];
+        const uint32_t ms = static_cast<uint32_t>(row_stride(mb));
+        const uint32_t nq = ms / 4;
+        const int slot = kb & 1;
+        const int R = band_rows_per_stage<T>(ms);
+        mbar_wait(&sm.vfull[slot], (kb >> 1) & 1);
+        const double* vec = sm.vec[slot];
+        // column pass: thread (g, t) owns quads t, t + kGT, ... over row group g;
+        // its partial sums live in sm.red[g] (exclusive ownership)
+        if (!ROWS)
+            for (uint32_t q = t; q < nq; q += kGT)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) sm.red[g][4 * q + k] = 0.0;
+        for (uint32_t r0 = 0; r0 < nb; r0 += R, ++chunk) {
+            const int stage = chunk % kBandStages;
+            const uint32_t nr = nb - r0 < static_cast<uint32_t>(R) ? nb - r0 : static_cast<uint32_t>(R);
+            mbar_wait(&sm.full[stage], (chunk / kBandStages) & 1);
+            const T* blk = reinterpret_cast<const T*>(sm.ring[stage]);
+            if (ROWS) {
+                // two rows per warp step: independent load/FMA/shuffle chains interleave
+                for (uint32_t r = warp; r < nr; r += 2 * kWarps) {
+                    const uint32_t r2 = r + kWarps;
+                    const bool two = r2 < nr;
+                    const T* row = blk + r * ms;
+                    const T* row2 = blk + (two ? r2 : r) * ms;
+                    double acc = 0.0, acc2 = 0.0;
+                    for (uint32_t q = lane; q < nq; q += 32) {
+                        const double2 t01 = *reinterpret_cast<const double2*>(vec + 4 * q);
+                        const double2 t23 = *reinterpret_cast<const double2*>(vec + 4 * q + 2);
+                        double v[4], u[4];
+                        if constexpr (sizeof(T) == 4) {
+                            const float4 x = *reinterpret_cast<const float4*>(row + 4 * q);
+                            const float4 y = *reinterpret_cast<const float4*>(row2 + 4 * q);
+                            v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+                            u[0] = y.x; u[1] = y.y; u[2] = y.z; u[3] = y.w;
+                        } else {
+                            const double2 x0 = *reinterpret_cast<const double2*>(row + 4 * q);
+                            const double2 x1 = *reinterpret_cast<const double2*>(row + 4 * q + 2);
+                            const double2 y0 = *reinterpret_cast<const double2*>(row2 + 4 * q);
+                            const double2 y1 = *reinterpret_cast<const double2*>(row2 + 4 * q + 2);
+                            v[0] = x0.x; v[1] = x0.y; v[2] = x1.x; v[3] = x1.y;
+                            u[0] = y0.x; u[1] = y0.y; u[2] = y1.x; u[3] = y1.y;
+                        }
+                        acc += v[0] * t01.x + v[1] * t01.y + v[2] * t23.x + v[3] * t23.y;
+                        acc2 += u[0] * t01.x + u[1] * t01.y + u[2] * t23.x + u[3] * t23.y;
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                        acc2 += __shfl_xor_sync(0xffffffffu, acc2, o);
+                    }
+                    if (lane == 0) corr[sm.out[slot][r0 + r]] = acc;
+                    if (lane == 1 && two) corr[sm.out[slot][r0 + r2]] = acc2;
+                }
+            } else {
+                for (uint32_t q = t; q < nq; q += kGT) {
+                    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+                    for (uint32_t r = g; r < nr; r += kColGroups) {
+                        const T* p = blk + r * ms + 4 * q;
+                        const double sr = vec[r0 + r];
+                        if constexpr (sizeof(T) == 4) {
+                            const float4 x = *reinterpret_cast<const float4*>(p);
+                            a0 += x.x * sr; a1 += x.y * sr; a2 += x.z * sr; a3 += x.w * sr;
+                        } else {
+                            const double2 x0 = *reinterpret_cast<const double2*>(p);
+                            const double2 x1 = *reinterpret_cast<const double2*>(p + 2);
+                            a0 += x0.x * sr; a1 += x0.y * sr; a2 += x1.x * sr; a3 += x1.y * sr;
+                        }
+                    }
+                    double* o = &sm.red[g][4 * q];
+                    o[0] += a0; o[1] += a1; o[2] += a2; o[3] += a3;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.empty[stage]);
+        }
+        if (!ROWS) {
+            // combine the row groups, one thread per column
+            consumers_sync();
+            for (uint32_t c = tid; c < mb; c += kThreads) {
+                double a = 0.0;
+#pragma unroll
+                for (int gg = 0; gg < kColGroups; ++gg) a += sm.red[gg][c];
+                corr[sm.out[slot][c]] = a;
+            }
+            consumers_sync();
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.vempty[slot]);
     }
 }
 
-// Partial F^T exp(v - h) for an arbitrary input vector (initial t = 0 and
-// the log_matvec API).
-template <typename T, int LPL>
-__global__ void __launch_bounds__(kThreads) lowrank_accum_kernel(const DevState* __restrict__ st, const double* __restrict__ v,
-                                                                 long long rows, const T* __restrict__ F, int l,
-                                                                 double* __restrict__ part, double* __restrict__ hpart,
-                                                                 double* __restrict__ mnp, double* __restrict__ mxp) {
-    if (st->done) return;
-    const int lane = threadIdx.x & 31;
-    Partial<LPL> P;
-    P.init();
-    double vmin = kPosInf, vmax = kNegInf;
-    const long long gw = (static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
-    const long long nw = static_cast<long long>(gridDim.x) * kWarps;
-    for (long long i = gw; i < rows; i += nw) {
-        double x = v ? v[i] : 0.0;
-        vmin = fmin(vmin, x);
-        vmax = fmax(vmax, x);
-        P.add(F + i * l, l, lane, x);
+// ---------------------------------------------------------------------------
+// Low-rank pass over the factor F (U: n x lp, or W^T: m x lp), streamed in
+// tiles of kRT rows through a shared-memory ring by a producer warp; the tile
+// carries the rows' scalar streams too (per-band corrections, log marginal,
+// current log s, marginal). Consumer thread t owns columns CPT t .. CPT t +
+// CPT - 1: row dots y_r = F_r . mid (warp transpose reduction + shared
+// combine), per-row finalize by kRT threads, then the running partial
+// sum_r F_r exp(v_r - h) of the next half's product.
+//   mode 0 (iteration): row side (SIDE 0) / column side (SIDE 1) update
+//   mode 1 (log_matvec): out[r] = H + log y_r, no partial
+//   mode 2 (accumulate): partial of F^T exp(in - h) only (in == null -> 0)
+// ---------------------------------------------------------------------------
+constexpr int kRT = 16;  // rows per low-rank tile (transpose_reduce16)
+
+struct PassArgs {
+    DevState* st;
+    long long rows;
+    int l, lp;
+    const double* mid;              // lp (row dots)
+    const double* corr[kMaxBands];  // per-band correction products (rows)
+    int ncorr;
+    const double* log_marg;         // log p (row side) / log q (col side)
+    const double* marg;             // p (row side, error) or null
+    const double* log_cur;          // log s of this iteration (row side, row marginal)
+    double* log_out;                // next log s (row side) / log t (col side)
+    double* row_marg;
+    double* err_part;
+    int with_err;
+    double* part;                   // [G x lp]
+    double* hpart;                  // [G]
+    double* mnp;                    // [G]
+    double* mxp;                    // [G]
+    int mode;
+    const double* in;               // mode 2 input vector
+    double* out;                    // mode 1 output
+};
+
+// Sum over the 32 lanes of each of 16 per-lane values with 16 shuffles instead
+// of 16 x 5: at every step a lane keeps half of its values and trades the
+// other half with its partner. On exit lane L holds the full sum of value
+// (L >> 1) & 15 (both lanes of a pair hold the same row).
+__device__ __forceinline__ double transpose_reduce16(double (&v)[16], int lane) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {  // xor 16
+        const bool hi = lane & 16;
+        const double send = hi ? v[k] : v[k + 8];
+        const double keep = hi ? v[k + 8] : v[k];
+        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
     }
-    block_combine<LPL>(P, l, part, hpart, vmin, vmax, mnp, mxp);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {  // xor 8
+        const bool hi = lane & 8;
+        const double send = hi ? v[k] : v[k + 4];
+        const double keep = hi ? v[k + 4] : v[k];
+        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {  // xor 4
+        const bool hi = lane & 4;
+        const double send = hi ? v[k] : v[k + 2];
+        const double keep = hi ? v[k + 2] : v[k];
+        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    {  // xor 2
+        const bool hi = lane & 2;
+        const double send = hi ? v[0] : v[1];
+        const double keep = hi ? v[1] : v[0];
+        v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+    return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
-// Global shift and mid = sum_b exp(h_b - H) part_b; which: 0 -> t side, 1 -> s side.
-__global__ void lowrank_reduce_kernel(DevState* __restrict__ st, const double* __restrict__ part,
-                                      const double* __restrict__ hpart, const double* __restrict__ mnp,
-                                      const double* __restrict__ mxp, int G, int l, double* __restrict__ mid, int which) {
+// Per-row transcendentals of the low-rank finalize. In fp32-storage mode the
+// operands carry fp32 rounding already, so log y and exp of non-positive
+// arguments run on the fp32 MUFU path (range-safe: the exponent of y is split
+// off in fp64 first); fp64 storage keeps them in fp64.
+template <typename T>
+__device__ __forceinline__ double fin_log(double y) {
+    if constexpr (sizeof(T) == 4) {
+        if (!(y > 0.0) || !(y < kPosInf)) return log(y);
+        int e;
+        const double mant = frexp(y, &e);  // [0.5, 1)
+        return static_cast<double>(__logf(static_cast<float>(mant))) + e * 0.6931471805599453;
+    } else {
+        return log(y);
+    }
+}
+template <typename T>
+__device__ __forceinline__ double fin_exp_neg(double x) {  // x <= 0
+    if constexpr (sizeof(T) == 4) return x < -87.0 ? 0.0 : static_cast<double>(__expf(static_cast<float>(x)));
+    else return exp(x);
+}
+
+template <typename T>
+struct PassStages {
+    static constexpr int kStages = 3;
+};
+
+template <typename T>
+__host__ __device__ constexpr size_t pass_stage_bytes(int lp) {
+    return static_cast<size_t>(kRT) * lp * sizeof(T) + (kMaxBands + 3) * kRT * sizeof(double);
+}
+
+template <int CPT, typename T>
+__device__ __forceinline__ void lds_cols(const T* p, double (&o)[CPT]) {
+    if constexpr (CPT == 2 && sizeof(T) == 4) {
+        const float2 v = *reinterpret_cast<const float2*>(p);
+        o[0] = v.x;
+        o[1] = v.y;
+    } else if constexpr (CPT == 4 && sizeof(T) == 4) {
+        const float4 v = *reinterpret_cast<const float4*>(p);
+        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+    } else {
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) o[k] = static_cast<double>(p[k]);
+    }
+}
+
+template <typename T, int CPT, int SIDE>
+__global__ void __launch_bounds__(kThreads + 32, 2) lowrank_pass_kernel(const T* __restrict__ F, PassArgs a) {
+    DevState* st = a.st;
     if (st->done) return;
+    constexpr int S = PassStages<T>::kStages;
+    extern __shared__ __align__(128) unsigned char dyn[];
+    __shared__ __align__(8) uint64_t full[S], empty[S];
+    __shared__ double red[kWarps][kRT];
+    __shared__ double w_s[kRT];
+    __shared__ double sc_s, h_sh;
+    __shared__ double err_s[kWarps], mn_s[kWarps], mx_s[kWarps];
+    __shared__ unsigned fl_s;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const size_t stage_bytes = pass_stage_bytes<T>(a.lp);
+    const uint32_t frow = static_cast<uint32_t>(a.lp * sizeof(T));
+    // streams: [corr_0 .. corr_{nc-1}] [log marg] [log cur] [marg]; mode 2: [in]
+    const int nc = a.mode == 2 ? 0 : a.ncorr;
+    const double* sv[kMaxBands + 3];
+    int nsv = 0;
+    if (a.mode == 2) {
+        sv[nsv++] = a.in;
+    } else {
+        for (int k = 0; k < nc; ++k) sv[nsv++] = a.corr[k];
+        sv[nsv++] = a.mode == 0 ? a.log_marg : nullptr;
+        sv[nsv++] = (a.mode == 0 && SIDE == 0 && a.with_err) ? a.log_cur : nullptr;
+        sv[nsv++] = (a.mode == 0 && SIDE == 0 && a.with_err) ? a.marg : nullptr;
+    }
+    const long long ntiles = (a.rows + kRT - 1) / kRT;
+    if (tid == 0) {
+        for (int k = 0; k < S; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], kWarps);
+        }
+        fence_mbar_init();
+        fl_s = 0u;
+        h_sh = kNegInf;  // CTA running shift
+    }
+    __syncthreads();
+    if (warp == kWarps) {
+        // ---------------- producer ----------------
+        if (lane == 0) {
+            int it = 0;
+            for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+                const int stage = it % S;
+                if (it >= S) mbar_wait(&empty[stage], ((it / S) - 1) & 1);
+                const long long r0 = tile * kRT;
+                const int nr = static_cast<int>(a.rows - r0 < kRT ? a.rows - r0 : kRT);
+                unsigned char* base = dyn + stage * stage_bytes;
+                const uint32_t sbytes = static_cast<uint32_t>((nr * 8 + 15) & ~15);  // vectors padded to kRT rows
+                uint32_t bytes = nr * frow;
+                for (int k = 0; k < nsv; ++k)
+                    if (sv[k]) bytes += sbytes;
+                mbar_arrive_expect_tx(&full[stage], bytes);
+                bulk_g2s(base, F + r0 * a.lp, nr * frow, &full[stage]);
+                double* sc = reinterpret_cast<double*>(base + static_cast<size_t>(kRT) * frow);
+                for (int k = 0; k < nsv; ++k)
+                    if (sv[k]) bulk_g2s(sc + k * kRT, sv[k] + r0, sbytes, &full[stage]);
+            }
+        }
+        return;
+    }
+    // ---------------- consumers ----------------
+    const int c0 = CPT * tid;
+    const bool own = c0 < a.lp;
+    const double H = SIDE == 0 ? st->H_t : st->H_s;
+    const int allpos = SIDE == 0 ? st->allpos_t : st->allpos_s;
+    double mid[CPT], acc[CPT];
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+        mid[k] = (a.mode != 2 && own) ? a.mid[c0 + k] : 0.0;
+        acc[k] = 0.0;
+    }
+    double vmin = kPosInf, vmax = kNegInf, err = 0.0;
+    int it = 0;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int stage = it % S;
+        const long long r0 = tile * kRT;
+        const int nr = static_cast<int>(a.rows - r0 < kRT ? a.rows - r0 : kRT);
+        mbar_wait(&full[stage], (it / S) & 1);
+        const T* fs = reinterpret_cast<const T*>(dyn + stage * stage_bytes);
+        const double* scal = reinterpret_cast<const double*>(dyn + stage * stage_bytes + static_cast<size_t>(kRT) * frow);
+        if (a.mode != 2) {
+            // row dots y_r = F_r . mid: per-thread partials, warp transpose
+            // reduction, then the kWarps warp sums meet in shared memory.
+            double dp[kRT];
+#pragma unroll
+            for (int r = 0; r < kRT; ++r) {
+                double d = 0.0;
+                if (own && r < nr) {
+                    double u[CPT];
+                    lds_cols<CPT>(fs + r * a.lp + c0, u);
+#pragma unroll
+                    for (int k = 0; k < CPT; ++k) d += u[k] * mid[k];
+                }
+                dp[r] = d;
+            }
+            const double wsum = transpose_reduce16(dp, lane);
+            if ((lane & 1) == 0) red[warp][(lane >> 1) & 15] = wsum;
+        }
+        consumers_sync();
+        if (tid < kRT) {
+            const long long i = r0 + tid;
+            double v = kNegInf;
+            bool live = tid < nr;
+            if (live) {
+                if (a.mode == 2) {
+                    v = sv[0] ? scal[tid] : 0.0;
+                } else {
+                    double nys = 0.0;
+#pragma unroll
+                    for (int w = 0; w < kWarps; ++w) nys += red[w][tid];
+                    double y = nys;
+                    for (int k = 0; k < nc; ++k) y += scal[k * kRT + tid];
+                    unsigned fl = 0;
+                    if (allpos && !(nys > 0.0)) fl |= SIDE == 0 ? F_NYS_ROW : F_NYS_COL;
+                    if (!(y > 0.0)) fl |= SIDE == 0 ? F_NEG_ROW : F_NEG_COL;
+                    const double k = H + fin_log<T>(y);
+                    if (a.mode == 1) {
+                        a.out[i] = k;
+                        live = false;
+                    } else {
+                        if (SIDE == 0 && a.with_err) {
+                            const double rm = exp(scal[(nc + 1) * kRT + tid] + k);
+                            a.row_marg[i] = rm;
+                            err += fabs(rm - scal[(nc + 2) * kRT + tid]);
+                        }
+                        v = scal[nc * kRT + tid] - k;
+                        a.log_out[i] = v;
+                        if (!isfinite(v)) fl |= SIDE == 0 ? F_LOGS : F_LOGT;
+                    }
+                    if (fl) atomicOr(&fl_s, fl);
+                }
+                if (live) {
+                    vmin = fmin(vmin, v);
+                    vmax = fmax(vmax, v);
+                }
+            }
+            // tile shift: running max over the finite values
+            const double h_old = h_sh;
+            const double tv = (live && v > kNegInf && v < kPosInf) ? v : kNegInf;
+            double tmax = tv;
+#pragma unroll
+            for (int o = kRT / 2; o > 0; o >>= 1) tmax = fmax(tmax, __shfl_xor_sync((1u << kRT) - 1u, tmax, o));
+            const double hn = fmax(h_old, tmax);
+            w_s[tid] = tv == kNegInf ? 0.0 : fin_exp_neg<T>(tv - hn);
+            __syncwarp((1u << kRT) - 1u);
+            if (tid == 0) {
+                sc_s = (h_old == kNegInf || hn == kNegInf) ? 0.0 : fin_exp_neg<T>(h_old - hn);
+                h_sh = hn;
+            }
+        }
+        consumers_sync();
+        if (a.mode != 1 && own) {
+            const double sc = sc_s;
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) acc[k] *= sc;
+#pragma unroll
+            for (int r = 0; r < kRT; ++r) {
+                if (r < nr) {
+                    double u[CPT];
+                    lds_cols<CPT>(fs + r * a.lp + c0, u);
+                    const double w = w_s[r];
+#pragma unroll
+                    for (int k = 0; k < CPT; ++k) acc[k] += u[k] * w;
+                }
+            }
+        }
+        // release the stage to the producer (one arrival per consumer warp)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+    }
+    if (a.mode == 1) {
+        consumers_sync();
+        if (tid == 0 && fl_s) atomicOr(&st->flags, fl_s);
+        return;
+    }
+    vmin = -warp_max(-vmin);
+    vmax = warp_max(vmax);
+    err = warp_sum(err);
+    if (lane == 0) {
+        mn_s[warp] = vmin;
+        mx_s[warp] = vmax;
+        err_s[warp] = err;
+    }
+    consumers_sync();
+    const double hb = h_sh;
+#pragma unroll
+    for (int k = 0; k < CPT; ++k)
+        if (own) a.part[static_cast<long long>(blockIdx.x) * a.lp + c0 + k] = hb == kNegInf ? 0.0 : acc[k];
+    if (tid == 0) {
+        double mn = kPosInf, mx = kNegInf, e = 0.0;
+        for (int w = 0; w < kWarps; ++w) {
+            mn = fmin(mn, mn_s[w]);
+            mx = fmax(mx, mx_s[w]);
+            e += err_s[w];
+        }
+        a.hpart[blockIdx.x] = hb;
+        a.mnp[blockIdx.x] = mn;
+        a.mxp[blockIdx.x] = mx;
+        if (SIDE == 0 && a.with_err) a.err_part[blockIdx.x] = e;
+        if (fl_s) atomicOr(&st->flags, fl_s);
+    }
+}
+
+// Global shift and mid = sum_b exp(h_b - H) part_b over the G CTA partials;
+// which: 0 -> t side, 1 -> s side. One CTA per 32 columns: lane = column,
+// warps split the partials, shared memory combines them.
+__global__ void __launch_bounds__(256) lowrank_reduce_kernel(DevState* __restrict__ st, const double* __restrict__ part,
+                                                             const double* __restrict__ hpart,
+                                                             const double* __restrict__ mnp, int G, int lp,
+                                                             double* __restrict__ mid, int which) {
+    if (st->done) return;
+    __shared__ double sh[8], sm[8], acc_s[8][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double H = kNegInf, mn = kPosInf;
-    for (int b = 0; b < G; ++b) {
+    for (int b = threadIdx.x; b < G; b += 256) {
         H = fmax(H, hpart[b]);
         mn = fmin(mn, mnp[b]);
     }
-    for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < l; a += gridDim.x * blockDim.x) {
-        double s = 0.0;
-        if (H != kNegInf)
-            for (int b = 0; b < G; ++b)
-                if (hpart[b] != kNegInf) s += part[static_cast<long long>(b) * l + a] * exp(hpart[b] - H);
-        mid[a] = s;
+    H = warp_max(H);
+    mn = -warp_max(-mn);
+    if (lane == 0) { sh[warp] = H; sm[warp] = mn; }
+    __syncthreads();
+    H = kNegInf;
+    mn = kPosInf;
+    for (int w = 0; w < 8; ++w) { H = fmax(H, sh[w]); mn = fmin(mn, sm[w]); }
+    const int a = blockIdx.x * 32 + lane;
+    double s = 0.0;
+    if (H != kNegInf && a < lp)
+        for (int b = warp; b < G; b += 8) {
+            const double hb = hpart[b];
+            if (hb != kNegInf) s += part[static_cast<long long>(b) * lp + a] * exp(hb - H);
+        }
+    acc_s[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && a < lp) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += acc_s[w][lane];
+        mid[a] = t;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         // positive_input of nys_matvec(_t) (nystrom.cpp:139-141): every exp(v - H) > 0.
@@ -382,123 +934,22 @@ __global__ void lowrank_reduce_kernel(DevState* __restrict__ st, const double* _
     }
 }
 
-// Column finalize (K^T side): y_j = W^T_j . mid_s + corr_t[j]; kts, log t,
-// and the partial of W tt for the row side.
-template <typename T, int LPL>
-__global__ void __launch_bounds__(kThreads) lcn_col_finalize_kernel(
-    DevState* __restrict__ st, const T* __restrict__ Wt, int l, long long m, const double* __restrict__ mid_s,
-    const double* __restrict__ corr, const double* __restrict__ log_q, double* __restrict__ log_t,
-    double* __restrict__ part, double* __restrict__ hpart, double* __restrict__ mnp, double* __restrict__ mxp, int mode,
-    double* __restrict__ out) {
-    if (st->done) return;
-    const int lane = threadIdx.x & 31;
-    const double H = st->H_s;
-    const int allpos = st->allpos_s;
-    double mids[LPL];
-#pragma unroll
-    for (int k = 0; k < LPL; ++k) mids[k] = lane + 32 * k < l ? mid_s[lane + 32 * k] : 0.0;
-    Partial<LPL> P;
-    P.init();
-    double vmin = kPosInf, vmax = kNegInf;
-    unsigned fl = 0;
-    const long long gw = (static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
-    const long long nw = static_cast<long long>(gridDim.x) * kWarps;
-    for (long long j = gw; j < m; j += nw) {
-        const T* row = Wt + j * l;
-        double nys = 0.0;
-#pragma unroll
-        for (int k = 0; k < LPL; ++k) {
-            int a = lane + 32 * k;
-            if (a < l) nys += static_cast<double>(row[a]) * mids[k];
-        }
-        nys = warp_sum(nys);
-        double y = nys + (corr ? corr[j] : 0.0);
-        if (allpos && !(nys > 0.0)) fl |= F_NYS_COL;
-        if (!(y > 0.0)) fl |= F_NEG_COL;
-        double kts = H + log(y);
-        if (mode == 1) {
-            if (lane == 0) out[j] = kts;
-            continue;
-        }
-        double v = log_q[j] - kts;
-        if (lane == 0) log_t[j] = v;
-        if (!isfinite(v)) fl |= F_LOGT;
-        vmin = fmin(vmin, v);
-        vmax = fmax(vmax, v);
-        P.add(row, l, lane, v);
-    }
-    if (fl && lane == 0) atomicOr(&st->flags, fl);
-    if (mode == 0) block_combine<LPL>(P, l, part, hpart, vmin, vmax, mnp, mxp);
-}
-
-// Row finalize (K side): y_i = U_i . mid_t + corr_s[i]; kt, row marginal,
-// error partial, next log s and the partial of U^T ss for the next K^T.
-template <typename T, int LPL>
-__global__ void __launch_bounds__(kThreads) lcn_row_finalize_kernel(
-    DevState* __restrict__ st, const T* __restrict__ U, int l, long long n, const double* __restrict__ mid_t,
-    const double* __restrict__ corr, const double* __restrict__ log_p, const double* __restrict__ p,
-    const double* __restrict__ log_s_cur, double* __restrict__ log_s_next, double* __restrict__ row_marg,
-    double* __restrict__ err_part, int with_err, double* __restrict__ part, double* __restrict__ hpart,
-    double* __restrict__ mnp, double* __restrict__ mxp, int mode, double* __restrict__ out) {
-    if (st->done) return;
-    __shared__ double red[kWarps];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const double H = st->H_t;
-    const int allpos = st->allpos_t;
-    double mids[LPL];
-#pragma unroll
-    for (int k = 0; k < LPL; ++k) mids[k] = lane + 32 * k < l ? mid_t[lane + 32 * k] : 0.0;
-    Partial<LPL> P;
-    P.init();
-    double vmin = kPosInf, vmax = kNegInf, e = 0.0;
-    unsigned fl = 0;
-    const long long gw = (static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
-    const long long nw = static_cast<long long>(gridDim.x) * kWarps;
-    for (long long i = gw; i < n; i += nw) {
-        const T* row = U + i * l;
-        double nys = 0.0;
-#pragma unroll
-        for (int k = 0; k < LPL; ++k) {
-            int a = lane + 32 * k;
-            if (a < l) nys += static_cast<double>(row[a]) * mids[k];
-        }
-        nys = warp_sum(nys);
-        double y = nys + (corr ? corr[i] : 0.0);
-        if (allpos && !(nys > 0.0)) fl |= F_NYS_ROW;
-        if (!(y > 0.0)) fl |= F_NEG_ROW;
-        double kt = H + log(y);
-        if (mode == 1) {
-            if (lane == 0) out[i] = kt;
-            continue;
-        }
-        if (with_err) {
-            double rm = exp(log_s_cur[i] + kt);
-            if (lane == 0) row_marg[i] = rm;
-            e += fabs(rm - p[i]);
-        }
-        double v = log_p[i] - kt;
-        if (lane == 0) log_s_next[i] = v;
-        if (!isfinite(v)) fl |= F_LOGS;
-        vmin = fmin(vmin, v);
-        vmax = fmax(vmax, v);
-        P.add(row, l, lane, v);
-    }
-    if (fl && lane == 0) atomicOr(&st->flags, fl);
-    if (mode == 1) return;
-    if (lane == 0) red[warp] = e;
-    block_combine<LPL>(P, l, part, hpart, vmin, vmax, mnp, mxp);
-    if (threadIdx.x == 0 && with_err) {
-        double s = 0.0;
-        for (int w = 0; w < kWarps; ++w) s += red[w];
-        err_part[blockIdx.x] = s;
-    }
-}
-
 // End of iteration `it` (0 = the initial K(log t = 0)): error precedence in
 // the reference's order, marginal error, trace, convergence.
-__global__ void iter_end_kernel(DevState* __restrict__ st, const double* __restrict__ err_part, int G, int it,
-                                int max_iters, double tol, double* __restrict__ trace) {
+__global__ void __launch_bounds__(256) iter_end_kernel(DevState* __restrict__ st, const double* __restrict__ err_part,
+                                                       int G, int it, int max_iters, double tol,
+                                                       double* __restrict__ trace) {
     if (st->done) return;
+    __shared__ double red[8];
+    double e = 0.0;
+    if (it > 0)
+        for (int b = threadIdx.x; b < G; b += 256) e += err_part[b];
+    e = warp_sum(e);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = e;
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    e = 0.0;
+    for (int w = 0; w < 8; ++w) e += red[w];
     const unsigned f = st->flags;
     auto fail = [&](int status, int which) {
         st->status = status;
@@ -511,8 +962,6 @@ __global__ void iter_end_kernel(DevState* __restrict__ st, const double* __restr
     }
     if (f & (F_NEG_ROW | F_NYS_ROW)) return fail(4, 2);
     if (it > 0) {
-        double e = 0.0;
-        for (int b = 0; b < G; ++b) e += err_part[b];
         st->err = e;
         trace[it - 1] = e;
         st->iters = it;
@@ -565,13 +1014,6 @@ __global__ void log_kernel(const double* __restrict__ in, double* __restrict__ o
     if (i < n) out[i] = log(in[i]);
 }
 
-int lpl_of(size_t l) {
-    int k = static_cast<int>((l + 31) / 32);
-    int p = 1;
-    while (p < k) p <<= 1;
-    return p;
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -582,18 +1024,96 @@ struct Solver {
     Ctx& ctx;
     cudaStream_t s;
     long long n, m;
-    int l, G, LPL;
+    int l, lp, G, CPT;
     DevBuf<DevState> st;
     DevBuf<double> log_p, log_q, pv, qv, log_s[2], log_t, row_marg, err_part, trace;
-    DevBuf<double> Mr, Sr, Mc, Sc, corr_s, corr_t;                  // sparse / lcn band accumulators
-    DevBuf<double> part, hpart, mnp, mxp, mid_s, mid_t;             // low-rank reductions
-    DevBuf<double> dpart;                                           // distance / mass partials
-    size_t smem = 0;
-    bool attrs_set = false;
-    std::vector<cudaEvent_t> evs;                                   // phase events (profiling)
+    DevBuf<double> Mr, Sr, Mc, Sc;                          // sparse band accumulators
+    std::vector<DevBuf<double>> corr_s, corr_t;             // lcn: one correction product per band
+    DevBuf<double> part, hpart, mnp, mxp, mid_s, mid_t;     // low-rank reductions
+    DevBuf<double> dpart;                                   // distance / mass partials
+    std::vector<cudaEvent_t> evs;                           // phase events (profiling)
+    size_t mark_base = 0;
+    size_t smem = 0;                                        // low-rank pass stage ring
+    // band work: streamable buckets (both sides <= kBandVec) and the
+    // (bucket, chunk) items of the oversized ones
+    std::vector<DevBuf<uint32_t>> work_stream;
+    std::vector<DevBuf<uint2>> items_rows, items_cols;
+    std::vector<int> n_stream, n_rows_items, n_cols_items;
+    int band_grid = 0;
+
+    explicit Solver(Op& o) : op(o), ctx(*o.ctx), s(o.ctx->stream), n(o.n), m(o.m), l(static_cast<int>(o.l)) {
+        lp = static_cast<int>(o.lp);
+        CPT = lp <= kThreads ? 1 : lp <= 2 * kThreads ? 2 : 4;
+        if (lp > 4 * kThreads) throw Status(2, "lcn: landmark count above 1024 is not supported on this path");
+        int occ = 1;
+        if (op.kind != 1) {
+            smem = op.fp64 ? PassStages<double>::kStages * pass_stage_bytes<double>(lp)
+                           : PassStages<float>::kStages * pass_stage_bytes<float>(lp);
+            if (op.fp64) set_attrs<double>();
+            else set_attrs<float>();
+            if (op.fp64)
+                CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lowrank_pass_kernel<double, 2, 0>, kThreads + 32, smem));
+            else
+                CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lowrank_pass_kernel<float, 2, 0>, kThreads + 32, smem));
+        }
+        G = std::max(1, occ) * ctx.num_sms;
+        if (op.kind == 3) init_band_stream();
+    }
     ~Solver() {
         for (auto e : evs) cudaEventDestroy(e);
     }
+
+    template <typename T>
+    void set_attrs() {
+        const int b = static_cast<int>(smem);
+        CUDA_OK(cudaFuncSetAttribute(lowrank_pass_kernel<T, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        CUDA_OK(cudaFuncSetAttribute(lowrank_pass_kernel<T, 2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        CUDA_OK(cudaFuncSetAttribute(lowrank_pass_kernel<T, 4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        CUDA_OK(cudaFuncSetAttribute(lowrank_pass_kernel<T, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        CUDA_OK(cudaFuncSetAttribute(lowrank_pass_kernel<T, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        CUDA_OK(cudaFuncSetAttribute(lowrank_pass_kernel<T, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    }
+
+    void init_band_stream() {
+        const int bytes = static_cast<int>(sizeof(BandSmem));
+        CUDA_OK(cudaFuncSetAttribute(band_stream_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        CUDA_OK(cudaFuncSetAttribute(band_stream_kernel<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        CUDA_OK(cudaFuncSetAttribute(band_stream_kernel<double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        CUDA_OK(cudaFuncSetAttribute(band_stream_kernel<double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        int occ = 1;
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, band_stream_kernel<float, true>, kThreads + 64,
+                                                              sizeof(BandSmem)));
+        band_grid = std::max(occ, 1) * ctx.num_sms;
+        for (const Band& B : op.bands) {
+            std::vector<uint32_t> w(B.n_work), ws;  // work is sorted by block size, largest first
+            std::vector<uint2> ir, ic;
+            if (B.n_work) B.work.download(w.data(), B.n_work, s);
+            ctx.sync();
+            for (uint32_t k : w) {
+                const size_t nb = B.h_src_start[k + 1] - B.h_src_start[k];
+                const size_t ms = row_stride(B.h_tgt_start[k + 1] - B.h_tgt_start[k]);
+                if (nb <= kBandVec && ms <= kBandVec && ms * 4 <= kBandStageBytes) {
+                    ws.push_back(k);
+                } else {
+                    for (size_t c = 0; c * kItemRows < nb; ++c) ir.push_back(make_uint2(k, static_cast<uint32_t>(c)));
+                    for (size_t c = 0; c * 256 < ms; ++c) ic.push_back(make_uint2(k, static_cast<uint32_t>(c)));
+                }
+            }
+            DevBuf<uint32_t> a(std::max<size_t>(ws.size(), 1));
+            DevBuf<uint2> r(std::max<size_t>(ir.size(), 1)), c(std::max<size_t>(ic.size(), 1));
+            if (!ws.empty()) a.upload(ws.data(), ws.size(), s);
+            if (!ir.empty()) r.upload(ir.data(), ir.size(), s);
+            if (!ic.empty()) c.upload(ic.data(), ic.size(), s);
+            n_stream.push_back(static_cast<int>(ws.size()));
+            n_rows_items.push_back(static_cast<int>(ir.size()));
+            n_cols_items.push_back(static_cast<int>(ic.size()));
+            work_stream.push_back(std::move(a));
+            items_rows.push_back(std::move(r));
+            items_cols.push_back(std::move(c));
+        }
+        ctx.sync();
+    }
+
     cudaEvent_t ev(size_t i) {
         while (evs.size() <= i) {
             cudaEvent_t e;
@@ -602,11 +1122,8 @@ struct Solver {
         }
         return evs[i];
     }
-
-    explicit Solver(Op& o) : op(o), ctx(*o.ctx), s(o.ctx->stream), n(o.n), m(o.m), l(static_cast<int>(o.l)) {
-        G = 4 * ctx.num_sms;
-        LPL = lpl_of(std::max(l, 1));
-        smem = (kWarps * static_cast<size_t>(std::max(l, 1)) + 3 * kWarps) * sizeof(double);
+    void mark(int it, int ph) {
+        if (ctx.profile) CUDA_OK(cudaEventRecord(ev(mark_base + static_cast<size_t>(it) * 5 + ph), s));
     }
 
     template <typename T>
@@ -617,44 +1134,12 @@ struct Solver {
     template <typename T>
     const T* U() const {
         if constexpr (std::is_same_v<T, float>) return op.U32.get();
-        else return op.U64.get();
+        else return op.U64p.get();
     }
     template <typename T>
     const T* Wt() const {
         if constexpr (std::is_same_v<T, float>) return op.Wt32.get();
-        else return op.Wt64.get();
-    }
-
-    template <typename T, int LPLc>
-    void launch_accum(const double* v, long long rows, const T* F) {
-        lowrank_accum_kernel<T, LPLc><<<G, kThreads, smem, s>>>(st.get(), v, rows, F, l, part.get(), hpart.get(),
-                                                               mnp.get(), mxp.get());
-    }
-    template <typename T, int LPLc>
-    void launch_colfin(int mode, double* out) {
-        lcn_col_finalize_kernel<T, LPLc><<<G, kThreads, smem, s>>>(st.get(), Wt<T>(), l, m, mid_s.get(),
-                                                                  op.kind == 3 ? corr_t.get() : nullptr, log_q.get(),
-                                                                  log_t.get(), part.get(), hpart.get(), mnp.get(),
-                                                                  mxp.get(), mode, out);
-    }
-    template <typename T, int LPLc>
-    void launch_rowfin(int it, int mode, double* out) {
-        const int cur = it % 2, nxt = (it + 1) % 2;
-        lcn_row_finalize_kernel<T, LPLc><<<G, kThreads, smem, s>>>(
-            st.get(), U<T>(), l, n, mid_t.get(), op.kind == 3 ? corr_s.get() : nullptr, log_p.get(), pv.get(),
-            log_s[cur].get(), log_s[nxt].get(), row_marg.get(), err_part.get(), it > 0, part.get(), hpart.get(),
-            mnp.get(), mxp.get(), mode, out);
-    }
-
-#define LCNB_LPL_DISPATCH(CALL)                        \
-    switch (LPL) {                                     \
-        case 1: CALL(1); break;                        \
-        case 2: CALL(2); break;                        \
-        case 4: CALL(4); break;                        \
-        case 8: CALL(8); break;                        \
-        case 16: CALL(16); break;                      \
-        case 32: CALL(32); break;                      \
-        default: throw Status(2, "lcn: landmark count above 1024 is not supported on this path"); \
+        else return op.Wt64p.get();
     }
 
     void alloc() {
@@ -662,16 +1147,55 @@ struct Solver {
         st.resize(1);
         st.zero(s);
         dpart.resize(256);
-        log_p.resize(n); log_q.resize(m); pv.resize(n); qv.resize(m);
-        log_s[0].resize(n); log_s[1].resize(n); log_t.resize(m); row_marg.resize(n);
+        // row vectors padded to a multiple of kRT (the bulk copies read whole tiles)
+        const long long np = (n + kRT - 1) / kRT * kRT, mpd = (m + kRT - 1) / kRT * kRT;
+        log_p.resize(np); log_q.resize(mpd); pv.resize(np); qv.resize(mpd);
+        log_s[0].resize(np); log_s[1].resize(np); log_t.resize(mpd); row_marg.resize(np);
         err_part.resize(std::max<long long>(G, ceil_div(n, 256)));
         if (op.kind == 1) {
             Mr.resize(n); Sr.resize(n); Mc.resize(m); Sc.resize(m);
         } else {
-            corr_s.resize(n); corr_t.resize(m);
-            part.resize(static_cast<size_t>(G) * l); hpart.resize(G); mnp.resize(G); mxp.resize(G);
-            mid_s.resize(l); mid_t.resize(l);
+            corr_s.resize(op.bands.size());
+            corr_t.resize(op.bands.size());
+            for (size_t b = 0; b < op.bands.size(); ++b) {
+                if (corr_s[b].size() != static_cast<size_t>(np)) {
+                    corr_s[b].resize(np);
+                    corr_s[b].zero(s);  // rows outside any work bucket stay 0
+                }
+                if (corr_t[b].size() != static_cast<size_t>(mpd)) {
+                    corr_t[b].resize(mpd);
+                    corr_t[b].zero(s);
+                }
+            }
+            part.resize(static_cast<size_t>(G) * lp); hpart.resize(G); mnp.resize(G); mxp.resize(G);
+            mid_s.resize(lp); mid_t.resize(lp);
         }
+    }
+
+    template <typename T, int SIDE>
+    void pass(const PassArgs& a) {
+        const T* F = SIDE == 0 ? U<T>() : Wt<T>();
+        switch (CPT) {
+            case 1: lowrank_pass_kernel<T, 1, SIDE><<<G, kThreads + 32, smem, s>>>(F, a); break;
+            case 2: lowrank_pass_kernel<T, 2, SIDE><<<G, kThreads + 32, smem, s>>>(F, a); break;
+            case 4: lowrank_pass_kernel<T, 4, SIDE><<<G, kThreads + 32, smem, s>>>(F, a); break;
+        }
+    }
+    PassArgs base_args() {
+        PassArgs a{};
+        a.st = st.get();
+        a.l = l;
+        a.lp = lp;
+        a.part = part.get();
+        a.hpart = hpart.get();
+        a.mnp = mnp.get();
+        a.mxp = mxp.get();
+        a.err_part = err_part.get();
+        return a;
+    }
+    void reduce(double* mid, int which) {
+        lowrank_reduce_kernel<<<ceil_div(lp, 32), 256, 0, s>>>(st.get(), part.get(), hpart.get(), mnp.get(), G, lp,
+                                                               mid, which);
     }
 
     // -------- sparse -------------------------------------------------------
@@ -709,85 +1233,83 @@ struct Solver {
         sparse_row_finalize_kernel<<<ceil_div(n, 256), 256, 0, s>>>(st.get(), Mr.get(), Sr.get(), log_p.get(), pv.get(),
                                                                     n, log_s[cur].get(), log_s[nxt].get(), nullptr,
                                                                     row_marg.get(), err_part.get(), it > 0);
-        iter_end_kernel<<<1, 1, 0, s>>>(st.get(), err_part.get(), ceil_div(n, 256), it, max_iters, tol, trace.get());
+        iter_end_kernel<<<1, 256, 0, s>>>(st.get(), err_part.get(), ceil_div(n, 256), it, max_iters, tol, trace.get());
         mark(it, 4);
     }
 
     // -------- lcn / nystrom ------------------------------------------------
-    template <typename T>
-    void lcn_rows(const double* lt) {
+    template <typename T, bool ROWS>
+    void bands(const double* logv, std::vector<DevBuf<double>>& corr) {
         if (op.kind != 3) return;
-        zero_kernel<<<ceil_div(n, 256), 256, 0, s>>>(st.get(), corr_s.get(), n);
-        for (size_t b = 0; b < op.bands.size(); ++b)
-            if (op.bands[b].n_work)
-                lcn_row_band_kernel<T><<<op.bands[b].n_work, kThreads, 0, s>>>(
-                    st.get(), op.view(b), op.bands[b].work.get(), band_vals<T>(b), lt, corr_s.get());
+        for (size_t b = 0; b < op.bands.size(); ++b) {
+            if (n_stream[b])
+                band_stream_kernel<T, ROWS><<<std::min(band_grid, n_stream[b]), kThreads + 64, sizeof(BandSmem), s>>>(
+                    st.get(), op.view(b), work_stream[b].get(), n_stream[b], band_vals<T>(b), logv, corr[b].get());
+            if (ROWS && n_rows_items[b])
+                lcn_row_band_kernel<T><<<n_rows_items[b], kThreads, 0, s>>>(st.get(), op.view(b), items_rows[b].get(),
+                                                                          band_vals<T>(b), logv, corr[b].get());
+            if (!ROWS && n_cols_items[b])
+                lcn_col_band_kernel<T><<<n_cols_items[b], kThreads, 0, s>>>(st.get(), op.view(b), items_cols[b].get(),
+                                                                          band_vals<T>(b), logv, corr[b].get());
+        }
     }
     template <typename T>
-    void lcn_cols(const double* ls) {
+    void lcn_rows(const double* lt) { bands<T, true>(lt, corr_s); }
+    template <typename T>
+    void lcn_cols(const double* ls) { bands<T, false>(ls, corr_t); }
+    void set_corr(PassArgs& a, int side) {
+        a.ncorr = 0;
         if (op.kind != 3) return;
-        zero_kernel<<<ceil_div(m, 256), 256, 0, s>>>(st.get(), corr_t.get(), m);
-        for (size_t b = 0; b < op.bands.size(); ++b)
-            if (op.bands[b].n_work)
-                lcn_col_band_kernel<T><<<op.bands[b].n_work, kThreads, 0, s>>>(
-                    st.get(), op.view(b), op.bands[b].work.get(), band_vals<T>(b), ls, corr_t.get());
+        for (size_t b = 0; b < op.bands.size(); ++b) a.corr[a.ncorr++] = side == 0 ? corr_s[b].get() : corr_t[b].get();
     }
+
     template <typename T>
     void lcn_iteration(int it, double tol, int max_iters) {
-        const int cur = it % 2;
+        const int cur = it % 2, nxt = (it + 1) % 2;
         mark(it, 0);
         if (it == 0) {
             // kt = K(log t = 0) (sinkhorn.cpp:145): partial W^T 1 with shift 0.
-#define ACC0(L) launch_accum<T, L>(nullptr, m, Wt<T>())
-            LCNB_LPL_DISPATCH(ACC0)
-#undef ACC0
-            lowrank_reduce_kernel<<<ceil_div(l, 256), 256, 0, s>>>(st.get(), part.get(), hpart.get(), mnp.get(),
-                                                                  mxp.get(), G, l, mid_t.get(), 0);
+            PassArgs a = base_args();
+            a.rows = m;
+            a.mode = 2;
+            a.in = nullptr;
+            pass<T, 1>(a);
             mark(it, 1);
         } else {
             lcn_cols<T>(log_s[cur].get());
             mark(it, 1);
-#define COLF(L) launch_colfin<T, L>(0, nullptr)
-            LCNB_LPL_DISPATCH(COLF)
-#undef COLF
-            lowrank_reduce_kernel<<<ceil_div(l, 256), 256, 0, s>>>(st.get(), part.get(), hpart.get(), mnp.get(),
-                                                                  mxp.get(), G, l, mid_t.get(), 0);
+            PassArgs a = base_args();
+            a.rows = m;
+            a.mode = 0;
+            a.mid = mid_s.get();
+            set_corr(a, 1);
+            a.log_marg = log_q.get();
+            a.log_out = log_t.get();
+            pass<T, 1>(a);
         }
+        reduce(mid_t.get(), 0);
         mark(it, 2);
         lcn_rows<T>(log_t.get());
         mark(it, 3);
-#define ROWF(L) launch_rowfin<T, L>(it, 0, nullptr)
-        LCNB_LPL_DISPATCH(ROWF)
-#undef ROWF
-        lowrank_reduce_kernel<<<ceil_div(l, 256), 256, 0, s>>>(st.get(), part.get(), hpart.get(), mnp.get(), mxp.get(),
-                                                              G, l, mid_s.get(), 1);
-        iter_end_kernel<<<1, 1, 0, s>>>(st.get(), err_part.get(), G, it, max_iters, tol, trace.get());
+        PassArgs a = base_args();
+        a.rows = n;
+        a.mode = 0;
+        a.mid = mid_t.get();
+        set_corr(a, 0);
+        a.log_marg = log_p.get();
+        a.marg = pv.get();
+        a.log_cur = log_s[cur].get();
+        a.log_out = log_s[nxt].get();
+        a.row_marg = row_marg.get();
+        a.with_err = it > 0;
+        pass<T, 0>(a);
+        reduce(mid_s.get(), 1);
+        iter_end_kernel<<<1, 256, 0, s>>>(st.get(), err_part.get(), G, it, max_iters, tol, trace.get());
         mark(it, 4);
     }
 
     template <typename T>
-    void set_smem_attrs() {
-        if (attrs_set) return;
-        attrs_set = true;
-        if (op.kind == 1 || smem <= 48 * 1024) return;
-#define ATTR(L)                                                                                                    \
-    CUDA_OK(cudaFuncSetAttribute(lowrank_accum_kernel<T, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    CUDA_OK(cudaFuncSetAttribute(lcn_col_finalize_kernel<T, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    CUDA_OK(cudaFuncSetAttribute(lcn_row_finalize_kernel<T, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))
-        LCNB_LPL_DISPATCH(ATTR)
-#undef ATTR
-    }
-
-    // phase marks: 0 start of iteration, 1 after col bands, 2 after col
-    // finalize+reduce, 3 after row bands, 4 after row finalize+reduce+end.
-    size_t mark_base = 0;
-    void mark(int it, int ph) {
-        if (ctx.profile) CUDA_OK(cudaEventRecord(ev(mark_base + static_cast<size_t>(it) * 5 + ph), s));
-    }
-
-    template <typename T>
     void run(const double* in_p, const double* in_q, bool device_ptrs, const SolveOptions& o, Result& res) {
-        set_smem_attrs<T>();
         alloc();
         trace.resize(std::max<size_t>(std::max(o.max_iters, 1), trace.size()));
         const cudaMemcpyKind kind = device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
@@ -886,10 +1408,9 @@ struct Solver {
     // log_matvec / log_matvec_t (operator.cpp:226-252) on a host vector.
     template <typename T>
     void matvec(const double* h_in, bool transposed, double* h_out) {
-        set_smem_attrs<T>();
         alloc();
         const long long len_in = transposed ? n : m, len_out = transposed ? m : n;
-        DevBuf<double> vin(len_in), vout(len_out);
+        DevBuf<double> vin((len_in + kRT - 1) / kRT * kRT), vout(len_out);
         vin.upload(h_in, len_in, s);
         if (op.kind == 1) {
             if (!transposed) {
@@ -899,34 +1420,37 @@ struct Solver {
                                                                             vout.get(), nullptr, nullptr, 0);
             } else {
                 sparse_cols<T>(vin.get());
-                // kts only: reuse the finalize with log_q = 0 and read M/S directly
                 DevBuf<double> zq(m);
                 zq.zero(s);
                 sparse_col_finalize_kernel<<<ceil_div(m, 256), 256, 0, s>>>(st.get(), Mc.get(), Sc.get(), zq.get(), m,
                                                                             vout.get());
-                // vout = 0 - kts -> negate on host below
+                // vout = 0 - kts -> negated on the host below
             }
         } else {
+            PassArgs acc = base_args();
+            acc.mode = 2;
+            acc.in = vin.get();
+            PassArgs mv = base_args();
+            mv.mode = 1;
+            mv.out = vout.get();
             if (!transposed) {
-#define ACC1(L) launch_accum<T, L>(vin.get(), m, Wt<T>())
-                LCNB_LPL_DISPATCH(ACC1)
-#undef ACC1
-                lowrank_reduce_kernel<<<ceil_div(l, 256), 256, 0, s>>>(st.get(), part.get(), hpart.get(), mnp.get(),
-                                                                      mxp.get(), G, l, mid_t.get(), 0);
+                acc.rows = m;
+                pass<T, 1>(acc);
+                reduce(mid_t.get(), 0);
                 lcn_rows<T>(vin.get());
-#define ROWM(L) launch_rowfin<T, L>(0, 1, vout.get())
-                LCNB_LPL_DISPATCH(ROWM)
-#undef ROWM
+                mv.rows = n;
+                mv.mid = mid_t.get();
+                set_corr(mv, 0);
+                pass<T, 0>(mv);
             } else {
-#define ACC2(L) launch_accum<T, L>(vin.get(), n, U<T>())
-                LCNB_LPL_DISPATCH(ACC2)
-#undef ACC2
-                lowrank_reduce_kernel<<<ceil_div(l, 256), 256, 0, s>>>(st.get(), part.get(), hpart.get(), mnp.get(),
-                                                                      mxp.get(), G, l, mid_s.get(), 1);
+                acc.rows = n;
+                pass<T, 0>(acc);
+                reduce(mid_s.get(), 1);
                 lcn_cols<T>(vin.get());
-#define COLM(L) launch_colfin<T, L>(1, vout.get())
-                LCNB_LPL_DISPATCH(COLM)
-#undef COLM
+                mv.rows = m;
+                mv.mid = mid_s.get();
+                set_corr(mv, 1);
+                pass<T, 1>(mv);
             }
         }
         LAUNCH_OK("log_matvec");
@@ -971,8 +1495,8 @@ void op_log_matvec(Op& op, const double* h_in, bool transposed, double* h_out) {
     else sv.matvec<float>(h_in, transposed, h_out);
 }
 
-// distance_lcn (sinkhorn.cpp:222-261), from the fp64 factors on the device
-// (host-side reduction order).
+// distance_lcn (sinkhorn.cpp:222-261), from the fp64 factors (host-side
+// reduction order as the reference).
 double distance_lcn_device(Op& op, const Result& res) {
     Ctx& ctx = *op.ctx;
     const size_t n = op.n, m = op.m, l = op.l;

@@ -9,6 +9,7 @@ from paper_2107_06876_b200 import configs
 
 which = sys.argv[1] if len(sys.argv) > 1 else "c3"
 scale = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 t = time.time()
 pr = {"c0": configs.config0, "c1": configs.config1, "c3": configs.config3}[which](scale)
 print(f"{pr.name} n={pr.n} d={pr.d} buckets={pr.buckets}x{pr.bands} l={pr.landmarks} gen {time.time()-t:.1f}s", flush=True)
@@ -22,7 +23,7 @@ op = lcn.KernelOperator.from_device(ctx, dp.data_ptr(), pr.n, dq.data_ptr(), pr.
                                     pr.landmarks, lcn.LANDMARK_KMEANS, pr.landmark_seed)
 print(f"build {time.time()-t:.2f}s nnz={op.nnz} stored={op.stored} max|delta|={op.max_abs_delta:.3e} cond={op.cond_estimate:.3e}", flush=True)
 pm, qm = pr.marginals()
-for rep in range(3):
+for rep in range(reps):
     res = lcn.sinkhorn(op, pm, qm, lcn.SinkhornOptions(tol=0.0, max_iters=pr.iters, want_plan=False, check_support=False))
     l = pr.landmarks
     B = 8 * op.nnz + 4 * l * (pr.n + pr.m) + 16 * (pr.n + pr.m)
