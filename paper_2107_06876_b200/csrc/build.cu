@@ -46,7 +46,8 @@ PhaseTimer::~PhaseTimer() {
 BandView Op::view(int b) const {
     const Band& B = bands[b];
     return {B.src_order.get(), B.tgt_order.get(), B.src_start.get(), B.tgt_start.get(), B.blk_off.get(),
-            B.src_bucket.get(), B.tgt_bucket.get(), B.src_local.get(), B.tgt_local.get()};
+            B.src_bucket.get(), B.tgt_bucket.get(), B.src_local.get(), B.tgt_local.get(), B.src_pos.get(),
+            B.tgt_pos.get()};
 }
 
 BandSet Op::bandset() const {
@@ -75,18 +76,26 @@ __global__ void iota32_kernel(uint32_t* p, long long n) {
 }
 
 __global__ void local_pos_kernel(const uint32_t* __restrict__ order, const uint32_t* __restrict__ ids,
-                                 const uint32_t* __restrict__ start, long long n, uint32_t* __restrict__ local) {
+                                 const uint32_t* __restrict__ start, long long n, uint32_t* __restrict__ local,
+                                 uint32_t* __restrict__ pos) {
     long long p = blockIdx.x * 256LL + threadIdx.x;
     if (p < n) {
         uint32_t i = order[p];
         local[i] = static_cast<uint32_t>(p - start[ids[i]]);
+        pos[i] = static_cast<uint32_t>(p);
     }
 }
 
+// order / pos arrays carry 16 spare entries: the iteration kernels bulk-copy
+// 16-byte-aligned supersets of their ranges.
 void stable_group(Ctx& ctx, const uint32_t* d_ids, size_t n, size_t nb, DevBuf<uint32_t>& order,
-                  DevBuf<uint32_t>& start, std::vector<uint32_t>& h_start, DevBuf<uint32_t>& local) {
+                  DevBuf<uint32_t>& start, std::vector<uint32_t>& h_start, DevBuf<uint32_t>& local,
+                  DevBuf<uint32_t>& pos) {
     cudaStream_t s = ctx.stream;
-    order.resize(std::max<size_t>(n, 1));
+    order.resize(n + 16);
+    order.zero(s);
+    pos.resize(n + 16);
+    pos.zero(s);
     local.resize(std::max<size_t>(n, 1));
     start.resize(nb + 1);
     DevBuf<uint32_t> counts(nb + 1), iota(std::max<size_t>(n, 1)), keys(std::max<size_t>(n, 1));
@@ -110,7 +119,7 @@ void stable_group(Ctx& ctx, const uint32_t* d_ids, size_t n, size_t nb, DevBuf<u
         DevBuf<unsigned char> t(tmp);
         cub::DeviceRadixSort::SortPairs(t.get(), tmp, d_ids, keys.get(), iota.get(), order.get(), static_cast<int>(n),
                                         0, end_bit, s);
-        local_pos_kernel<<<ceil_div(n, 256), 256, 0, s>>>(order.get(), d_ids, start.get(), n, local.get());
+        local_pos_kernel<<<ceil_div(n, 256), 256, 0, s>>>(order.get(), d_ids, start.get(), n, local.get(), pos.get());
         LAUNCH_OK("stable_group");
     }
     ctx.sync();
@@ -126,8 +135,8 @@ void build_band_layout(Ctx& ctx, Band& B, const uint32_t* d_src_bucket, const ui
     B.tgt_bucket.resize(std::max<size_t>(m, 1));
     if (n) CUDA_OK(cudaMemcpyAsync(B.src_bucket.get(), d_src_bucket, n * 4, cudaMemcpyDeviceToDevice, s));
     if (m) CUDA_OK(cudaMemcpyAsync(B.tgt_bucket.get(), d_tgt_bucket, m * 4, cudaMemcpyDeviceToDevice, s));
-    stable_group(ctx, B.src_bucket.get(), n, nb, B.src_order, B.src_start, B.h_src_start, B.src_local);
-    stable_group(ctx, B.tgt_bucket.get(), m, nb, B.tgt_order, B.tgt_start, B.h_tgt_start, B.tgt_local);
+    stable_group(ctx, B.src_bucket.get(), n, nb, B.src_order, B.src_start, B.h_src_start, B.src_local, B.src_pos);
+    stable_group(ctx, B.tgt_bucket.get(), m, nb, B.tgt_order, B.tgt_start, B.h_tgt_start, B.tgt_local, B.tgt_pos);
     B.h_blk_off.assign(nb + 1, 0);
     std::vector<uint32_t> work;
     B.real_entries = 0;

@@ -92,6 +92,8 @@ struct Band {
     DevBuf<uint32_t> tgt_bucket;   // m
     DevBuf<uint32_t> src_local;    // n: position inside its bucket
     DevBuf<uint32_t> tgt_local;    // m
+    DevBuf<uint32_t> src_pos;      // n (+16): position of each source in src_order
+    DevBuf<uint32_t> tgt_pos;      // m (+16)
     DevBuf<uint32_t> work;         // list of buckets with a nonempty block
     size_t n_work = 0;
     unsigned long long entries = 0;       // padded block entries held in HBM

@@ -22,6 +22,8 @@ struct BandView {
     const uint32_t* tgt_bucket;
     const uint32_t* src_local;
     const uint32_t* tgt_local;
+    const uint32_t* src_pos;
+    const uint32_t* tgt_pos;
 };
 
 struct BandSet {  // bucket ids of every band, for the cross-band dedup mask

@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 
@@ -369,9 +370,11 @@ constexpr int kColGroups = 2;   // column pass: row groups of kThreads / kColGro
 struct BandSmem {
     unsigned char ring[kBandStages][kBandStageBytes];
     double vec[2][kBandVec];           // tt (row pass) / ss (column pass) per bucket slot
-    uint32_t out[2][kBandVec];         // output index per row (row pass) / column (column pass)
+    double lvraw[2][kBandVec + 2];     // bulk-copied bucket-ordered log values (16-byte aligned superset)
+    uint32_t out[2][kBandVec + 4];     // bulk-copied output indices (aligned superset)
     double red[kColGroups][kBandVec];  // column pass: per-row-group partial sums
-    uint64_t full[kBandStages], empty[kBandStages], vfull[2], vempty[2];
+    uint32_t out_off[2];
+    uint64_t full[kBandStages], empty[kBandStages], vfull[2], vempty[2], lvfull[2];
 };
 
 // rows per ring stage; a multiple of 8 keeps every chunk start 128-byte
@@ -383,12 +386,14 @@ __device__ __forceinline__ int band_rows_per_stage(uint32_t ms) {
     return r < 1 ? 1 : r;
 }
 
+// logvp: the band's bucket-ordered copy of log t (row pass) / log s (column
+// pass), written by the low-rank pass that produced the log vector.
 template <typename T, bool ROWS>
 __global__ void __launch_bounds__(kThreads + 64, 1) band_stream_kernel(const DevState* __restrict__ st, BandView bv,
                                                                       const uint32_t* __restrict__ work, int nwork,
                                                                       const T* __restrict__ vals,
-                                                                      const double* __restrict__ logv,
-                                                                      double* __restrict__ corr) {
+                                                                      const double* __restrict__ logvp,
+                                                                      double* __restrict__ corr, int debug) {
     if (st->done) return;
     extern __shared__ __align__(128) unsigned char dyn[];
     BandSmem& sm = *reinterpret_cast<BandSmem*>(dyn);
@@ -402,6 +407,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) band_stream_kernel(const Dev
         for (int k = 0; k < 2; ++k) {
             mbar_init(&sm.vfull[k], 1);
             mbar_init(&sm.vempty[k], kWarps);
+            mbar_init(&sm.lvfull[k], 1);
         }
         fence_mbar_init();
     }
@@ -429,7 +435,9 @@ __global__ void __launch_bounds__(kThreads + 64, 1) band_stream_kernel(const Dev
         return;
     }
     if (warp == kWarps + 1) {
-        // ---------------- producer 2: gathered scaling values + output indices ----------------
+        // ---------------- producer 2: scaling values + output indices ----------------
+        // Both are contiguous ranges (bucket order): one pair of bulk copies per
+        // bucket, then exp(log v - H) into the bucket's slot.
         int kb = 0;
         for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++kb) {
             const uint32_t b = work[w];
@@ -437,33 +445,25 @@ __global__ void __launch_bounds__(kThreads + 64, 1) band_stream_kernel(const Dev
             const uint32_t tb = bv.tgt_start[b], mb = bv.tgt_start[b + 1] - tb;
             const uint32_t count = ROWS ? static_cast<uint32_t>(row_stride(mb)) : nb;
             const uint32_t valid = ROWS ? mb : nb;
-            const uint32_t* order = ROWS ? bv.tgt_order + tb : bv.src_order + sb;
+            const uint32_t lv0 = ROWS ? tb : sb;
+            const uint32_t o0 = ROWS ? sb : tb;
+            const uint32_t ndst = ROWS ? nb : mb;
+            const uint32_t* order = ROWS ? bv.src_order : bv.tgt_order;
             const int slot = kb & 1;
             if (kb >= 2) mbar_wait(&sm.vempty[slot], ((kb >> 1) - 1) & 1);
-            constexpr int kB = 8;  // independent gathers in flight per lane
-            for (uint32_t base = 0; base < count; base += 32 * kB) {
-                uint32_t idx[kB];
-#pragma unroll
-                for (int k = 0; k < kB; ++k) {
-                    const uint32_t c = base + lane + 32 * k;
-                    idx[k] = c < valid ? __ldg(order + c) : 0u;
-                }
-                double lv[kB];
-#pragma unroll
-                for (int k = 0; k < kB; ++k) {
-                    const uint32_t c = base + lane + 32 * k;
-                    lv[k] = c < valid ? __ldg(logv + idx[k]) : kNegInf;
-                }
-#pragma unroll
-                for (int k = 0; k < kB; ++k) {
-                    const uint32_t c = base + lane + 32 * k;
-                    if (c < count) sm.vec[slot][c] = lv[k] == kNegInf ? 0.0 : exp(lv[k] - H);
-                }
+            const uint32_t lva = lv0 & ~1u, lvo = lv0 - lva;
+            const uint32_t oa = o0 & ~3u, oo = o0 - oa;
+            if (lane == 0) {
+                const uint32_t blv = ((valid + lvo) * 8 + 15) & ~15u;
+                const uint32_t bo = ((ndst + oo) * 4 + 15) & ~15u;
+                mbar_arrive_expect_tx(&sm.lvfull[slot], blv + bo);
+                bulk_g2s(sm.lvraw[slot], logvp + lva, blv, &sm.lvfull[slot]);
+                bulk_g2s(sm.out[slot], order + oa, bo, &sm.lvfull[slot]);
+                sm.out_off[slot] = oo;
             }
-            // destinations of the results: sources (row pass) / targets (column pass)
-            const uint32_t* dst = ROWS ? bv.src_order + sb : bv.tgt_order + tb;
-            const uint32_t ndst = ROWS ? nb : mb;
-            for (uint32_t c = lane; c < ndst; c += 32) sm.out[slot][c] = __ldg(dst + c);
+            mbar_wait(&sm.lvfull[slot], (kb >> 1) & 1);
+            for (uint32_t c = lane; c < count; c += 32)
+                sm.vec[slot][c] = c < valid ? exp(sm.lvraw[slot][lvo + c] - H) : 0.0;
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.vfull[slot]);
         }
@@ -483,6 +483,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) band_stream_kernel(const Dev
         const int R = band_rows_per_stage<T>(ms);
         mbar_wait(&sm.vfull[slot], (kb >> 1) & 1);
         const double* vec = sm.vec[slot];
+        const uint32_t* outi = sm.out[slot] + sm.out_off[slot];
         // column pass: thread (g, t) owns quads t, t + kGT, ... over row group g;
         // its partial sums live in sm.red[g] (exclusive ownership)
         if (!ROWS)
@@ -494,7 +495,8 @@ __global__ void __launch_bounds__(kThreads + 64, 1) band_stream_kernel(const Dev
             const uint32_t nr = nb - r0 < static_cast<uint32_t>(R) ? nb - r0 : static_cast<uint32_t>(R);
             mbar_wait(&sm.full[stage], (chunk / kBandStages) & 1);
             const T* blk = reinterpret_cast<const T*>(sm.ring[stage]);
-            if (ROWS) {
+            if (debug) {
+            } else if (ROWS) {
                 // two rows per warp step: independent load/FMA/shuffle chains interleave
                 for (uint32_t r = warp; r < nr; r += 2 * kWarps) {
                     const uint32_t r2 = r + kWarps;
@@ -527,8 +529,8 @@ __global__ void __launch_bounds__(kThreads + 64, 1) band_stream_kernel(const Dev
                         acc += __shfl_xor_sync(0xffffffffu, acc, o);
                         acc2 += __shfl_xor_sync(0xffffffffu, acc2, o);
                     }
-                    if (lane == 0) corr[sm.out[slot][r0 + r]] = acc;
-                    if (lane == 1 && two) corr[sm.out[slot][r0 + r2]] = acc2;
+                    if (lane == 0) corr[outi[r0 + r]] = acc;
+                    if (lane == 1 && two) corr[outi[r0 + r2]] = acc2;
                 }
             } else {
                 for (uint32_t q = t; q < nq; q += kGT) {
@@ -559,7 +561,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) band_stream_kernel(const Dev
                 double a = 0.0;
 #pragma unroll
                 for (int gg = 0; gg < kColGroups; ++gg) a += sm.red[gg][c];
-                corr[sm.out[slot][c]] = a;
+                corr[outi[c]] = a;
             }
             consumers_sync();
         }
@@ -603,6 +605,10 @@ struct PassArgs {
     int mode;
     const double* in;               // mode 2 input vector
     double* out;                    // mode 1 output
+    // mode 0: also write v into each band's bucket-ordered copy, perm[b][pos[b][i]]
+    const uint32_t* pos[kMaxBands];
+    double* perm[kMaxBands];
+    int nperm;
 };
 
 // Sum over the 32 lanes of each of 16 per-lane values with 16 shuffles instead
@@ -668,7 +674,8 @@ struct PassStages {
 
 template <typename T>
 __host__ __device__ constexpr size_t pass_stage_bytes(int lp) {
-    return static_cast<size_t>(kRT) * lp * sizeof(T) + (kMaxBands + 3) * kRT * sizeof(double);
+    return static_cast<size_t>(kRT) * lp * sizeof(T) + (kMaxBands + 3) * kRT * sizeof(double) +
+           kMaxBands * kRT * sizeof(uint32_t);
 }
 
 template <int CPT, typename T>
@@ -713,6 +720,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) lowrank_pass_kernel(const T*
         sv[nsv++] = (a.mode == 0 && SIDE == 0 && a.with_err) ? a.log_cur : nullptr;
         sv[nsv++] = (a.mode == 0 && SIDE == 0 && a.with_err) ? a.marg : nullptr;
     }
+    const int np = a.mode == 0 ? a.nperm : 0;
     const long long ntiles = (a.rows + kRT - 1) / kRT;
     if (tid == 0) {
         for (int k = 0; k < S; ++k) {
@@ -738,11 +746,15 @@ __global__ void __launch_bounds__(kThreads + 32, 2) lowrank_pass_kernel(const T*
                 uint32_t bytes = nr * frow;
                 for (int k = 0; k < nsv; ++k)
                     if (sv[k]) bytes += sbytes;
+                bytes += np * static_cast<uint32_t>((nr * 4 + 15) & ~15);
                 mbar_arrive_expect_tx(&full[stage], bytes);
                 bulk_g2s(base, F + r0 * a.lp, nr * frow, &full[stage]);
                 double* sc = reinterpret_cast<double*>(base + static_cast<size_t>(kRT) * frow);
                 for (int k = 0; k < nsv; ++k)
                     if (sv[k]) bulk_g2s(sc + k * kRT, sv[k] + r0, sbytes, &full[stage]);
+                uint32_t* ps = reinterpret_cast<uint32_t*>(sc + (kMaxBands + 3) * kRT);
+                const uint32_t pbytes = static_cast<uint32_t>((nr * 4 + 15) & ~15);  // pos arrays padded by 16
+                for (int k = 0; k < np; ++k) bulk_g2s(ps + k * kRT, a.pos[k] + r0, pbytes, &full[stage]);
             }
         }
         return;
@@ -814,6 +826,8 @@ __global__ void __launch_bounds__(kThreads + 32, 2) lowrank_pass_kernel(const T*
                         }
                         v = scal[nc * kRT + tid] - k;
                         a.log_out[i] = v;
+                        const uint32_t* ps = reinterpret_cast<const uint32_t*>(scal + (kMaxBands + 3) * kRT);
+                        for (int pb = 0; pb < np; ++pb) a.perm[pb][ps[pb * kRT + tid]] = v;
                         if (!isfinite(v)) fl |= SIDE == 0 ? F_LOGS : F_LOGT;
                     }
                     if (fl) atomicOr(&fl_s, fl);
@@ -1009,6 +1023,12 @@ __global__ void sum_partial_kernel(const double* __restrict__ a, long long n, do
     }
 }
 
+__global__ void perm_scatter_kernel(const double* __restrict__ in, long long n, const uint32_t* __restrict__ pos,
+                                    double* __restrict__ out) {
+    long long i = blockIdx.x * 256LL + threadIdx.x;
+    if (i < n) out[pos[i]] = in[i];
+}
+
 __global__ void log_kernel(const double* __restrict__ in, double* __restrict__ out, long long n) {
     long long i = blockIdx.x * 256LL + threadIdx.x;
     if (i < n) out[i] = log(in[i]);
@@ -1029,6 +1049,7 @@ struct Solver {
     DevBuf<double> log_p, log_q, pv, qv, log_s[2], log_t, row_marg, err_part, trace;
     DevBuf<double> Mr, Sr, Mc, Sc;                          // sparse band accumulators
     std::vector<DevBuf<double>> corr_s, corr_t;             // lcn: one correction product per band
+    std::vector<DevBuf<double>> ltp, lsp[2];                // per-band bucket-ordered log t / log s copies
     DevBuf<double> part, hpart, mnp, mxp, mid_s, mid_t;     // low-rank reductions
     DevBuf<double> dpart;                                   // distance / mass partials
     std::vector<cudaEvent_t> evs;                           // phase events (profiling)
@@ -1040,6 +1061,7 @@ struct Solver {
     std::vector<DevBuf<uint2>> items_rows, items_cols;
     std::vector<int> n_stream, n_rows_items, n_cols_items;
     int band_grid = 0;
+    int band_debug = std::getenv("LCN_BAND_DEBUG") ? std::atoi(std::getenv("LCN_BAND_DEBUG")) : 0;
 
     explicit Solver(Op& o) : op(o), ctx(*o.ctx), s(o.ctx->stream), n(o.n), m(o.m), l(static_cast<int>(o.l)) {
         lp = static_cast<int>(o.lp);
@@ -1167,6 +1189,15 @@ struct Solver {
                     corr_t[b].zero(s);
                 }
             }
+            ltp.resize(op.bands.size());
+            lsp[0].resize(op.bands.size());
+            lsp[1].resize(op.bands.size());
+            for (size_t b = 0; b < op.bands.size(); ++b) {
+                ltp[b].resize(m + 16);
+                lsp[0][b].resize(n + 16);
+                lsp[1][b].resize(n + 16);
+                ltp[b].zero(s);  // log t = 0 before the first row side
+            }
             part.resize(static_cast<size_t>(G) * lp); hpart.resize(G); mnp.resize(G); mxp.resize(G);
             mid_s.resize(lp); mid_t.resize(lp);
         }
@@ -1238,13 +1269,16 @@ struct Solver {
     }
 
     // -------- lcn / nystrom ------------------------------------------------
+    // logv: natural-order log vector (oversized-bucket kernels gather from it);
+    // logvp[b]: band b's bucket-ordered copy (streaming kernels bulk-copy it).
     template <typename T, bool ROWS>
-    void bands(const double* logv, std::vector<DevBuf<double>>& corr) {
+    void bands(const double* logv, std::vector<DevBuf<double>>& logvp, std::vector<DevBuf<double>>& corr) {
         if (op.kind != 3) return;
         for (size_t b = 0; b < op.bands.size(); ++b) {
             if (n_stream[b])
                 band_stream_kernel<T, ROWS><<<std::min(band_grid, n_stream[b]), kThreads + 64, sizeof(BandSmem), s>>>(
-                    st.get(), op.view(b), work_stream[b].get(), n_stream[b], band_vals<T>(b), logv, corr[b].get());
+                    st.get(), op.view(b), work_stream[b].get(), n_stream[b], band_vals<T>(b), logvp[b].get(),
+                    corr[b].get(), band_debug);
             if (ROWS && n_rows_items[b])
                 lcn_row_band_kernel<T><<<n_rows_items[b], kThreads, 0, s>>>(st.get(), op.view(b), items_rows[b].get(),
                                                                           band_vals<T>(b), logv, corr[b].get());
@@ -1254,9 +1288,24 @@ struct Solver {
         }
     }
     template <typename T>
-    void lcn_rows(const double* lt) { bands<T, true>(lt, corr_s); }
+    void lcn_rows(const double* lt) { bands<T, true>(lt, ltp, corr_s); }
     template <typename T>
-    void lcn_cols(const double* ls) { bands<T, false>(ls, corr_t); }
+    void lcn_cols(const double* ls, int parity) { bands<T, false>(ls, lsp[parity], corr_t); }
+    void set_perm(PassArgs& a, int side, int parity) {
+        a.nperm = 0;
+        if (op.kind != 3) return;
+        for (size_t b = 0; b < op.bands.size(); ++b) {
+            a.pos[a.nperm] = side == 0 ? op.bands[b].src_pos.get() : op.bands[b].tgt_pos.get();
+            a.perm[a.nperm++] = side == 0 ? lsp[parity][b].get() : ltp[b].get();
+        }
+    }
+    void scatter_perm(const double* v, long long len, int side, int parity) {
+        if (op.kind != 3) return;
+        for (size_t b = 0; b < op.bands.size(); ++b)
+            perm_scatter_kernel<<<ceil_div(len, 256), 256, 0, s>>>(
+                v, len, side == 0 ? op.bands[b].src_pos.get() : op.bands[b].tgt_pos.get(),
+                side == 0 ? lsp[parity][b].get() : ltp[b].get());
+    }
     void set_corr(PassArgs& a, int side) {
         a.ncorr = 0;
         if (op.kind != 3) return;
@@ -1276,13 +1325,14 @@ struct Solver {
             pass<T, 1>(a);
             mark(it, 1);
         } else {
-            lcn_cols<T>(log_s[cur].get());
+            lcn_cols<T>(log_s[cur].get(), cur);
             mark(it, 1);
             PassArgs a = base_args();
             a.rows = m;
             a.mode = 0;
             a.mid = mid_s.get();
             set_corr(a, 1);
+            set_perm(a, 1, 0);
             a.log_marg = log_q.get();
             a.log_out = log_t.get();
             pass<T, 1>(a);
@@ -1302,6 +1352,7 @@ struct Solver {
         a.log_out = log_s[nxt].get();
         a.row_marg = row_marg.get();
         a.with_err = it > 0;
+        set_perm(a, 0, nxt);
         pass<T, 0>(a);
         reduce(mid_s.get(), 1);
         iter_end_kernel<<<1, 256, 0, s>>>(st.get(), err_part.get(), G, it, max_iters, tol, trace.get());
@@ -1437,6 +1488,7 @@ struct Solver {
                 acc.rows = m;
                 pass<T, 1>(acc);
                 reduce(mid_t.get(), 0);
+                scatter_perm(vin.get(), m, 1, 0);
                 lcn_rows<T>(vin.get());
                 mv.rows = n;
                 mv.mid = mid_t.get();
@@ -1446,7 +1498,8 @@ struct Solver {
                 acc.rows = n;
                 pass<T, 0>(acc);
                 reduce(mid_s.get(), 1);
-                lcn_cols<T>(vin.get());
+                scatter_perm(vin.get(), n, 0, 0);
+                lcn_cols<T>(vin.get(), 0);
                 mv.rows = m;
                 mv.mid = mid_s.get();
                 set_corr(mv, 1);
