@@ -30,6 +30,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <queue>
+#include <utility>
 #include <type_traits>
 
 #include "async.cuh"
@@ -271,11 +273,22 @@ __global__ void __launch_bounds__(kThreads, 3) lcn_row_band_kernel(const DevStat
                     if (r0 + j < nb) v[j] = raw4(vals + off + static_cast<unsigned long long>(r0 + j) * ms + c0 + 4 * q);
                     else v[j].v[0] = v[j].v[1] = v[j].v[2] = v[j].v[3] = T(0);
                 }
-                const double t0 = tt[4 * q], t1 = tt[4 * q + 1], t2 = tt[4 * q + 2], t3 = tt[4 * q + 3];
+                if constexpr (sizeof(T) == 4) {
+                    // fp32 quad products, widened once per quad (F2F.F64 runs at
+                    // a quarter of the DFMA rate)
+                    const float t0 = static_cast<float>(tt[4 * q]), t1 = static_cast<float>(tt[4 * q + 1]);
+                    const float t2 = static_cast<float>(tt[4 * q + 2]), t3 = static_cast<float>(tt[4 * q + 3]);
 #pragma unroll
-                for (int j = 0; j < kRowsPerWarp; ++j)
-                    acc[j] += static_cast<double>(v[j].v[0]) * t0 + static_cast<double>(v[j].v[1]) * t1 +
-                              static_cast<double>(v[j].v[2]) * t2 + static_cast<double>(v[j].v[3]) * t3;
+                    for (int j = 0; j < kRowsPerWarp; ++j)
+                        acc[j] += static_cast<double>(
+                            fmaf(v[j].v[3], t3, fmaf(v[j].v[2], t2, fmaf(v[j].v[1], t1, v[j].v[0] * t0))));
+                } else {
+                    const double t0 = tt[4 * q], t1 = tt[4 * q + 1], t2 = tt[4 * q + 2], t3 = tt[4 * q + 3];
+#pragma unroll
+                    for (int j = 0; j < kRowsPerWarp; ++j)
+                        acc[j] += static_cast<double>(v[j].v[0]) * t0 + static_cast<double>(v[j].v[1]) * t1 +
+                                  static_cast<double>(v[j].v[2]) * t2 + static_cast<double>(v[j].v[3]) * t3;
+                }
             }
 #pragma unroll
             for (int j = 0; j < kRowsPerWarp; ++j) acc[j] = warp_sum(acc[j]);
@@ -324,11 +337,20 @@ __global__ void __launch_bounds__(kThreads, 3) lcn_col_band_kernel(const DevStat
                 const Raw4<T> v1 = raw4(col + static_cast<unsigned long long>(r + kGroups) * ms);
                 const Raw4<T> v2 = raw4(col + static_cast<unsigned long long>(r + 2 * kGroups) * ms);
                 const Raw4<T> v3 = raw4(col + static_cast<unsigned long long>(r + 3 * kGroups) * ms);
-                const double s0 = ss[r], s1 = ss[r + kGroups], s2 = ss[r + 2 * kGroups], s3 = ss[r + 3 * kGroups];
+                if constexpr (sizeof(T) == 4) {
+                    const float s0 = static_cast<float>(ss[r]), s1 = static_cast<float>(ss[r + kGroups]);
+                    const float s2 = static_cast<float>(ss[r + 2 * kGroups]), s3 = static_cast<float>(ss[r + 3 * kGroups]);
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    acc[k] += static_cast<double>(v0.v[k]) * s0 + static_cast<double>(v1.v[k]) * s1 +
-                              static_cast<double>(v2.v[k]) * s2 + static_cast<double>(v3.v[k]) * s3;
+                    for (int k = 0; k < 4; ++k)
+                        acc[k] += static_cast<double>(
+                            fmaf(v3.v[k], s3, fmaf(v2.v[k], s2, fmaf(v1.v[k], s1, v0.v[k] * s0))));
+                } else {
+                    const double s0 = ss[r], s1 = ss[r + kGroups], s2 = ss[r + 2 * kGroups], s3 = ss[r + 3 * kGroups];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        acc[k] += static_cast<double>(v0.v[k]) * s0 + static_cast<double>(v1.v[k]) * s1 +
+                                  static_cast<double>(v2.v[k]) * s2 + static_cast<double>(v3.v[k]) * s3;
+                }
             }
             for (; r < rn; r += kGroups) {
                 const Raw4<T> v0 = raw4(col + static_cast<unsigned long long>(r) * ms);
@@ -350,31 +372,42 @@ __global__ void __launch_bounds__(kThreads, 3) lcn_col_band_kernel(const DevStat
 }
 
 // ---------------------------------------------------------------------------
-// Streaming band kernels (warp-specialized), one persistent CTA per SM taking
-// buckets w = blockIdx.x, blockIdx.x + gridDim.x, ... of the size-sorted work
-// list. Warp kWarps streams the bucket's rows through a ring of kBandStages
-// shared stages with bulk copies; warp kWarps+1 gathers the bucket's scaling
-// values (tt_c = exp(log t - H_t) for the row pass, ss_r = exp(log s - H_s)
-// for the column pass) and output indices into one of two slots. The 8
-// consumer warps only wait on mbarriers and compute from shared memory.
-// ROWS = true: corr[src] = sum_c delta[r][c] tt[c]  (K side)
-// ROWS = false: corr[tgt] = sum_r delta[r][c] ss[r]  (K^T side)
-// Each band has its own corr vector (plain stores; rows of buckets without
-// a partner stay 0).
+// Streaming band kernels (warp-specialized). The band's work is a list of
+// items (bucket b, rows r0 .. r0 + nr) -- big buckets are split into row
+// pieces -- assigned to CTAs on the host by longest-processing-time greedy,
+// so every CTA streams about the same number of bytes. Per CTA:
+//   warp kWarps     bulk-copies the item's block rows through a ring of
+//                   kBandStages shared stages (mbarrier transaction counts);
+//   warp kWarps + 1 loads the item's scaling vector (tt_c = exp(log t - H_t)
+//                   for the row pass, ss_r = exp(log s - H_s) for the column
+//                   pass) and output indices into one of two slots;
+//   8 consumer warps only wait on mbarriers and compute from shared memory.
+// ROWS = true:  corr[src] = sum_c delta[r][c] tt[c]   (K side, plain stores)
+// ROWS = false: corr[tgt] = sum_r delta[r][c] ss[r]   (K^T side). A bucket
+//   split into K pieces writes K partial column sums to scratch; the piece
+//   that finishes last (per-bucket arrival counter) adds them in piece order,
+//   so the result does not depend on CTA timing.
+// Two CTAs per SM (smem 112 KB each) keep 16 consumer warps resident.
 // ---------------------------------------------------------------------------
-constexpr int kBandStages = 10;
+constexpr int kBandStages = 5;
 constexpr int kBandStageBytes = 16 * 1024;
-constexpr int kBandVec = 1024;  // max bucket side handled by the streaming kernels
-constexpr int kColGroups = 2;   // column pass: row groups of kThreads / kColGroups threads
+constexpr int kBandVec = 1024;  // max bucket columns / piece rows of the streaming kernels
 
 struct BandSmem {
     unsigned char ring[kBandStages][kBandStageBytes];
-    double vec[2][kBandVec];           // tt (row pass) / ss (column pass) per bucket slot
-    double lvraw[2][kBandVec + 2];     // bulk-copied bucket-ordered log values (16-byte aligned superset)
-    uint32_t out[2][kBandVec + 4];     // bulk-copied output indices (aligned superset)
-    double red[kColGroups][kBandVec];  // column pass: per-row-group partial sums
-    uint32_t out_off[2];
-    uint64_t full[kBandStages], empty[kBandStages], vfull[2], vempty[2], lvfull[2];
+    double vec[2][kBandVec];    // tt (row pass) / ss (column pass) per item slot (fp32 storage: float view)
+    uint32_t out[2][kBandVec];  // output indices per item slot
+    double red[kBandVec];       // column pass: per-row-group partial sums (groups x row stride <= kBandVec)
+    uint64_t full[kBandStages], empty[kBandStages], vfull[2], vempty[2];
+    uint32_t last;              // column pass: this CTA combines the split bucket
+};
+
+struct BandWork {
+    const uint4* items;      // {bucket, r0, nr, split}: split = sid << 8 | piece, or ~0u
+    const uint32_t* cta_off;  // CTA c processes items cta_off[c] .. cta_off[c + 1] - 1
+    const uint2* splits;      // sid -> {scratch offset (doubles), pieces}
+    uint32_t* counters;       // sid -> arrivals (reset by the combining CTA)
+    double* scratch;
 };
 
 // rows per ring stage; a multiple of 8 keeps every chunk start 128-byte
@@ -386,18 +419,19 @@ __device__ __forceinline__ int band_rows_per_stage(uint32_t ms) {
     return r < 1 ? 1 : r;
 }
 
-// logvp: the band's bucket-ordered copy of log t (row pass) / log s (column
+// logv: the band's bucket-ordered copy of log t (row pass) / log s (column
 // pass), written by the low-rank pass that produced the log vector.
 template <typename T, bool ROWS>
-__global__ void __launch_bounds__(kThreads + 64, 1) band_stream_kernel(const DevState* __restrict__ st, BandView bv,
-                                                                      const uint32_t* __restrict__ work, int nwork,
-                                                                      const T* __restrict__ vals,
-                                                                      const double* __restrict__ logvp,
-                                                                      double* __restrict__ corr, int debug) {
+__global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const DevState* __restrict__ st, BandView bv,
+                                                                      BandWork wk, const T* __restrict__ vals,
+                                                                      const double* __restrict__ logv,
+                                                                      double* __restrict__ corr) {
     if (st->done) return;
     extern __shared__ __align__(128) unsigned char dyn[];
     BandSmem& sm = *reinterpret_cast<BandSmem*>(dyn);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t i_beg = wk.cta_off[blockIdx.x], i_end = wk.cta_off[blockIdx.x + 1];
+    if (i_beg == i_end) return;
     const double H = ROWS ? st->H_t : st->H_s;
     if (tid == 0) {
         for (int k = 0; k < kBandStages; ++k) {
@@ -405,30 +439,35 @@ __global__ void __launch_bounds__(kThreads + 64, 1) band_stream_kernel(const Dev
             mbar_init(&sm.empty[k], kWarps);
         }
         for (int k = 0; k < 2; ++k) {
-            mbar_init(&sm.vfull[k], 1);
+            mbar_init(&sm.vfull[k], 32);
             mbar_init(&sm.vempty[k], kWarps);
-            mbar_init(&sm.lvfull[k], 1);
         }
         fence_mbar_init();
     }
     __syncthreads();
     if (warp == kWarps) {
-        // ---------------- producer 1: bulk copies of the block rows ----------------
+        // ---------------- producer 1: bulk copies of the item's block rows ----------------
         if (lane == 0) {
-            int chunk = 0;
-            for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
-                const uint32_t b = work[w];
-                const uint32_t nb = bv.src_start[b + 1] - bv.src_start[b];
+            int stage = 0;
+            uint32_t phase = 0;
+            bool wrapped = false;
+            for (uint32_t it = i_beg; it < i_end; ++it) {
+                const uint4 item = wk.items[it];
+                const uint32_t b = item.x;
                 const uint32_t ms = static_cast<uint32_t>(row_stride(bv.tgt_start[b + 1] - bv.tgt_start[b]));
                 const int R = band_rows_per_stage<T>(ms);
-                const T* blk = vals + bv.blk_off[b];
-                for (uint32_t r0 = 0; r0 < nb; r0 += R, ++chunk) {
-                    const int stage = chunk % kBandStages;
-                    const uint32_t nr = nb - r0 < static_cast<uint32_t>(R) ? nb - r0 : static_cast<uint32_t>(R);
-                    if (chunk >= kBandStages) mbar_wait(&sm.empty[stage], ((chunk / kBandStages) - 1) & 1);
+                const T* blk = vals + bv.blk_off[b] + static_cast<unsigned long long>(item.y) * ms;
+                for (uint32_t r0 = 0; r0 < item.z; r0 += R) {
+                    const uint32_t nr = item.z - r0 < static_cast<uint32_t>(R) ? item.z - r0 : static_cast<uint32_t>(R);
+                    if (wrapped) mbar_wait(&sm.empty[stage], phase ^ 1u);
                     const uint32_t bytes = nr * ms * static_cast<uint32_t>(sizeof(T));
                     mbar_arrive_expect_tx(&sm.full[stage], bytes);
                     bulk_g2s(sm.ring[stage], blk + static_cast<unsigned long long>(r0) * ms, bytes, &sm.full[stage]);
+                    if (++stage == kBandStages) {
+                        stage = 0;
+                        phase ^= 1u;
+                        wrapped = true;
+                    }
                 }
             }
         }
@@ -436,132 +475,169 @@ __global__ void __launch_bounds__(kThreads + 64, 1) band_stream_kernel(const Dev
     }
     if (warp == kWarps + 1) {
         // ---------------- producer 2: scaling values + output indices ----------------
-        // Both are contiguous ranges (bucket order): one pair of bulk copies per
-        // bucket, then exp(log v - H) into the bucket's slot.
         int kb = 0;
-        for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++kb) {
-            const uint32_t b = work[w];
-            const uint32_t sb = bv.src_start[b], nb = bv.src_start[b + 1] - sb;
+        for (uint32_t it = i_beg; it < i_end; ++it, ++kb) {
+            const uint4 item = wk.items[it];
+            const uint32_t b = item.x;
+            const uint32_t sb = bv.src_start[b] + item.y;
             const uint32_t tb = bv.tgt_start[b], mb = bv.tgt_start[b + 1] - tb;
-            const uint32_t count = ROWS ? static_cast<uint32_t>(row_stride(mb)) : nb;
-            const uint32_t valid = ROWS ? mb : nb;
-            const uint32_t lv0 = ROWS ? tb : sb;
+            const uint32_t count = ROWS ? static_cast<uint32_t>(row_stride(mb)) : item.z;
+            const uint32_t valid = ROWS ? mb : item.z;
+            const uint32_t v0 = ROWS ? tb : sb;
             const uint32_t o0 = ROWS ? sb : tb;
-            const uint32_t ndst = ROWS ? nb : mb;
+            const uint32_t nout = ROWS ? item.z : mb;
             const uint32_t* order = ROWS ? bv.src_order : bv.tgt_order;
             const int slot = kb & 1;
             if (kb >= 2) mbar_wait(&sm.vempty[slot], ((kb >> 1) - 1) & 1);
-            const uint32_t lva = lv0 & ~1u, lvo = lv0 - lva;
-            const uint32_t oa = o0 & ~3u, oo = o0 - oa;
-            if (lane == 0) {
-                const uint32_t blv = ((valid + lvo) * 8 + 15) & ~15u;
-                const uint32_t bo = ((ndst + oo) * 4 + 15) & ~15u;
-                mbar_arrive_expect_tx(&sm.lvfull[slot], blv + bo);
-                bulk_g2s(sm.lvraw[slot], logvp + lva, blv, &sm.lvfull[slot]);
-                bulk_g2s(sm.out[slot], order + oa, bo, &sm.lvfull[slot]);
-                sm.out_off[slot] = oo;
+            if constexpr (sizeof(T) == 4) {
+                // fp32 storage: the scalings enter fp32 products (values in (0, 1])
+                float* vf = reinterpret_cast<float*>(sm.vec[slot]);
+                for (uint32_t c = lane; c < count; c += 32)
+                    vf[c] = c < valid ? static_cast<float>(exp(logv[v0 + c] - H)) : 0.0f;
+            } else {
+                for (uint32_t c = lane; c < count; c += 32)
+                    sm.vec[slot][c] = c < valid ? exp(logv[v0 + c] - H) : 0.0;
             }
-            mbar_wait(&sm.lvfull[slot], (kb >> 1) & 1);
-            for (uint32_t c = lane; c < count; c += 32)
-                sm.vec[slot][c] = c < valid ? exp(sm.lvraw[slot][lvo + c] - H) : 0.0;
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.vfull[slot]);
+            for (uint32_t c = lane; c < nout; c += 32) sm.out[slot][c] = order[o0 + c];
+            mbar_arrive(&sm.vfull[slot]);  // all 32 lanes (release: their smem writes)
         }
         return;
     }
     // ---------------- consumers ----------------
-    constexpr int kGT = kThreads / kColGroups;
-    const int g = tid / kGT, t = tid % kGT;
-    int chunk = 0, kb = 0;
-    for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++kb) {
-        const uint32_t b = work[w];
-        const uint32_t nb = bv.src_start[b + 1] - bv.src_start[b];
+    int stage = 0;
+    uint32_t phase = 0;
+    int kb = 0;
+    for (uint32_t it = i_beg; it < i_end; ++it, ++kb) {
+        const uint4 item = wk.items[it];
+        const uint32_t b = item.x;
         const uint32_t mb = bv.tgt_start[b + 1] - bv.tgt_start[b];
         const uint32_t ms = static_cast<uint32_t>(row_stride(mb));
         const uint32_t nq = ms / 4;
         const int slot = kb & 1;
         const int R = band_rows_per_stage<T>(ms);
+        // column pass mapping: groups of nq threads, thread (g, q) owns quad q
+        // of rows g, g + ng, ... of every chunk; sums stay in registers
+        const uint32_t ng = nq >= static_cast<uint32_t>(kThreads) ? 1u : kThreads / nq;
+        const uint32_t g = static_cast<uint32_t>(tid) / nq, q = static_cast<uint32_t>(tid) % nq;
+        const bool col_own = g < ng;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         mbar_wait(&sm.vfull[slot], (kb >> 1) & 1);
-        const double* vec = sm.vec[slot];
-        const uint32_t* outi = sm.out[slot] + sm.out_off[slot];
-        // column pass: thread (g, t) owns quads t, t + kGT, ... over row group g;
-        // its partial sums live in sm.red[g] (exclusive ownership)
-        if (!ROWS)
-            for (uint32_t q = t; q < nq; q += kGT)
-#pragma unroll
-                for (int k = 0; k < 4; ++k) sm.red[g][4 * q + k] = 0.0;
-        for (uint32_t r0 = 0; r0 < nb; r0 += R, ++chunk) {
-            const int stage = chunk % kBandStages;
-            const uint32_t nr = nb - r0 < static_cast<uint32_t>(R) ? nb - r0 : static_cast<uint32_t>(R);
-            mbar_wait(&sm.full[stage], (chunk / kBandStages) & 1);
+        const uint32_t* outi = sm.out[slot];
+        for (uint32_t r0 = 0; r0 < item.z; r0 += R) {
+            const uint32_t nr = item.z - r0 < static_cast<uint32_t>(R) ? item.z - r0 : static_cast<uint32_t>(R);
+            mbar_wait(&sm.full[stage], phase);
             const T* blk = reinterpret_cast<const T*>(sm.ring[stage]);
-            if (debug) {
-            } else if (ROWS) {
+            if constexpr (ROWS) {
                 // two rows per warp step: independent load/FMA/shuffle chains interleave
                 for (uint32_t r = warp; r < nr; r += 2 * kWarps) {
                     const uint32_t r2 = r + kWarps;
                     const bool two = r2 < nr;
                     const T* row = blk + r * ms;
                     const T* row2 = blk + (two ? r2 : r) * ms;
-                    double acc = 0.0, acc2 = 0.0;
-                    for (uint32_t q = lane; q < nq; q += 32) {
-                        const double2 t01 = *reinterpret_cast<const double2*>(vec + 4 * q);
-                        const double2 t23 = *reinterpret_cast<const double2*>(vec + 4 * q + 2);
-                        double v[4], u[4];
-                        if constexpr (sizeof(T) == 4) {
-                            const float4 x = *reinterpret_cast<const float4*>(row + 4 * q);
-                            const float4 y = *reinterpret_cast<const float4*>(row2 + 4 * q);
-                            v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
-                            u[0] = y.x; u[1] = y.y; u[2] = y.z; u[3] = y.w;
-                        } else {
-                            const double2 x0 = *reinterpret_cast<const double2*>(row + 4 * q);
-                            const double2 x1 = *reinterpret_cast<const double2*>(row + 4 * q + 2);
-                            const double2 y0 = *reinterpret_cast<const double2*>(row2 + 4 * q);
-                            const double2 y1 = *reinterpret_cast<const double2*>(row2 + 4 * q + 2);
-                            v[0] = x0.x; v[1] = x0.y; v[2] = x1.x; v[3] = x1.y;
-                            u[0] = y0.x; u[1] = y0.y; u[2] = y1.x; u[3] = y1.y;
+                    double acc, acc2;
+                    if constexpr (sizeof(T) == 4) {
+                        // fp32 products and row partials (<= kBandVec terms), widened once
+                        const float* vf = reinterpret_cast<const float*>(sm.vec[slot]);
+                        float f = 0.0f, f2 = 0.0f;
+                        for (uint32_t qq = lane; qq < nq; qq += 32) {
+                            const float4 tq = *reinterpret_cast<const float4*>(vf + 4 * qq);
+                            const float4 x = *reinterpret_cast<const float4*>(row + 4 * qq);
+                            const float4 y = *reinterpret_cast<const float4*>(row2 + 4 * qq);
+                            f = fmaf(x.x, tq.x, f); f = fmaf(x.y, tq.y, f);
+                            f = fmaf(x.z, tq.z, f); f = fmaf(x.w, tq.w, f);
+                            f2 = fmaf(y.x, tq.x, f2); f2 = fmaf(y.y, tq.y, f2);
+                            f2 = fmaf(y.z, tq.z, f2); f2 = fmaf(y.w, tq.w, f2);
                         }
-                        acc += v[0] * t01.x + v[1] * t01.y + v[2] * t23.x + v[3] * t23.y;
-                        acc2 += u[0] * t01.x + u[1] * t01.y + u[2] * t23.x + u[3] * t23.y;
-                    }
 #pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) {
-                        acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                        acc2 += __shfl_xor_sync(0xffffffffu, acc2, o);
+                        for (int o = 16; o > 0; o >>= 1) {
+                            f += __shfl_xor_sync(0xffffffffu, f, o);
+                            f2 += __shfl_xor_sync(0xffffffffu, f2, o);
+                        }
+                        acc = f;
+                        acc2 = f2;
+                    } else {
+                        const double* vec = sm.vec[slot];
+                        acc = 0.0;
+                        acc2 = 0.0;
+                        for (uint32_t qq = lane; qq < nq; qq += 32) {
+                            const double2 t01 = *reinterpret_cast<const double2*>(vec + 4 * qq);
+                            const double2 t23 = *reinterpret_cast<const double2*>(vec + 4 * qq + 2);
+                            const double2 x0 = *reinterpret_cast<const double2*>(row + 4 * qq);
+                            const double2 x1 = *reinterpret_cast<const double2*>(row + 4 * qq + 2);
+                            const double2 y0 = *reinterpret_cast<const double2*>(row2 + 4 * qq);
+                            const double2 y1 = *reinterpret_cast<const double2*>(row2 + 4 * qq + 2);
+                            acc += x0.x * t01.x + x0.y * t01.y + x1.x * t23.x + x1.y * t23.y;
+                            acc2 += y0.x * t01.x + y0.y * t01.y + y1.x * t23.x + y1.y * t23.y;
+                        }
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) {
+                            acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                            acc2 += __shfl_xor_sync(0xffffffffu, acc2, o);
+                        }
                     }
                     if (lane == 0) corr[outi[r0 + r]] = acc;
                     if (lane == 1 && two) corr[outi[r0 + r2]] = acc2;
                 }
-            } else {
-                for (uint32_t q = t; q < nq; q += kGT) {
-                    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-                    for (uint32_t r = g; r < nr; r += kColGroups) {
-                        const T* p = blk + r * ms + 4 * q;
-                        const double sr = vec[r0 + r];
-                        if constexpr (sizeof(T) == 4) {
-                            const float4 x = *reinterpret_cast<const float4*>(p);
-                            a0 += x.x * sr; a1 += x.y * sr; a2 += x.z * sr; a3 += x.w * sr;
-                        } else {
-                            const double2 x0 = *reinterpret_cast<const double2*>(p);
-                            const double2 x1 = *reinterpret_cast<const double2*>(p + 2);
-                            a0 += x0.x * sr; a1 += x0.y * sr; a2 += x1.x * sr; a3 += x1.y * sr;
-                        }
+            } else if (col_own) {
+                const T* p = blk + 4 * q;
+                if constexpr (sizeof(T) == 4) {
+                    const float* vf = reinterpret_cast<const float*>(sm.vec[slot]) + r0;
+                    float f0 = 0.0f, f1 = 0.0f, f2 = 0.0f, f3 = 0.0f;
+                    for (uint32_t r = g; r < nr; r += ng) {
+                        const float4 x = *reinterpret_cast<const float4*>(p + r * ms);
+                        const float sr = vf[r];
+                        f0 = fmaf(x.x, sr, f0); f1 = fmaf(x.y, sr, f1);
+                        f2 = fmaf(x.z, sr, f2); f3 = fmaf(x.w, sr, f3);
                     }
-                    double* o = &sm.red[g][4 * q];
-                    o[0] += a0; o[1] += a1; o[2] += a2; o[3] += a3;
+                    a0 += f0; a1 += f1; a2 += f2; a3 += f3;
+                } else {
+                    const double* vec = sm.vec[slot] + r0;
+                    for (uint32_t r = g; r < nr; r += ng) {
+                        const double2 x0 = *reinterpret_cast<const double2*>(p + r * ms);
+                        const double2 x1 = *reinterpret_cast<const double2*>(p + r * ms + 2);
+                        const double sr = vec[r];
+                        a0 += x0.x * sr; a1 += x0.y * sr; a2 += x1.x * sr; a3 += x1.y * sr;
+                    }
                 }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.empty[stage]);
+            if (++stage == kBandStages) {
+                stage = 0;
+                phase ^= 1u;
+            }
         }
-        if (!ROWS) {
-            // combine the row groups, one thread per column
+        if constexpr (!ROWS) {
+            // combine the row groups: red[g * ms + c], one thread per column
+            if (col_own) {
+                double* o = sm.red + g * ms + 4 * q;
+                o[0] = a0; o[1] = a1; o[2] = a2; o[3] = a3;
+            }
             consumers_sync();
+            const bool split = item.w != 0xffffffffu;
+            const uint2 sp = split ? wk.splits[item.w >> 8] : make_uint2(0u, 0u);
+            double* part = split ? wk.scratch + sp.x + static_cast<size_t>(item.w & 0xffu) * ms : nullptr;
             for (uint32_t c = tid; c < mb; c += kThreads) {
-                double a = 0.0;
-#pragma unroll
-                for (int gg = 0; gg < kColGroups; ++gg) a += sm.red[gg][c];
-                corr[outi[c]] = a;
+                double v = 0.0;
+                for (uint32_t gg = 0; gg < ng; ++gg) v += sm.red[gg * ms + c];
+                if (split) part[c] = v;
+                else corr[outi[c]] = v;
+            }
+            if (split) {
+                __threadfence();
+                consumers_sync();
+                if (tid == 0) sm.last = atomicAdd(&wk.counters[item.w >> 8], 1u) == sp.y - 1;
+                consumers_sync();
+                if (sm.last) {
+                    __threadfence();
+                    const double* base = wk.scratch + sp.x;
+                    for (uint32_t c = tid; c < mb; c += kThreads) {
+                        double v = 0.0;
+                        for (uint32_t k = 0; k < sp.y; ++k) v += __ldcg(base + static_cast<size_t>(k) * ms + c);
+                        corr[outi[c]] = v;
+                    }
+                    if (tid == 0) wk.counters[item.w >> 8] = 0u;
+                }
             }
             consumers_sync();
         }
@@ -702,6 +778,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) lowrank_pass_kernel(const T*
     __shared__ __align__(8) uint64_t full[S], empty[S];
     __shared__ double red[kWarps][kRT];
     __shared__ double w_s[kRT];
+    __shared__ float w_f[kRT];
     __shared__ double sc_s, h_sh;
     __shared__ double err_s[kWarps], mn_s[kWarps], mx_s[kWarps];
     __shared__ unsigned fl_s;
@@ -765,9 +842,12 @@ __global__ void __launch_bounds__(kThreads + 32, 2) lowrank_pass_kernel(const T*
     const double H = SIDE == 0 ? st->H_t : st->H_s;
     const int allpos = SIDE == 0 ? st->allpos_t : st->allpos_s;
     double mid[CPT], acc[CPT];
+    float mid_hi[CPT], mid_lo[CPT];
 #pragma unroll
     for (int k = 0; k < CPT; ++k) {
         mid[k] = (a.mode != 2 && own) ? a.mid[c0 + k] : 0.0;
+        mid_hi[k] = static_cast<float>(mid[k]);
+        mid_lo[k] = static_cast<float>(mid[k] - static_cast<double>(mid_hi[k]));
         acc[k] = 0.0;
     }
     double vmin = kPosInf, vmax = kNegInf, err = 0.0;
@@ -787,10 +867,23 @@ __global__ void __launch_bounds__(kThreads + 32, 2) lowrank_pass_kernel(const T*
             for (int r = 0; r < kRT; ++r) {
                 double d = 0.0;
                 if (own && r < nr) {
-                    double u[CPT];
-                    lds_cols<CPT>(fs + r * a.lp + c0, u);
+                    if constexpr (sizeof(T) == 4) {
+                        // fp32 products of the fp32 factor row with mid (split
+                        // hi + lo so mid keeps ~48 bits), widened once per row
+                        float dh = 0.0f, dl = 0.0f;
 #pragma unroll
-                    for (int k = 0; k < CPT; ++k) d += u[k] * mid[k];
+                        for (int k = 0; k < CPT; ++k) {
+                            const float u = fs[r * a.lp + c0 + k];
+                            dh = fmaf(u, mid_hi[k], dh);
+                            dl = fmaf(u, mid_lo[k], dl);
+                        }
+                        d = static_cast<double>(dh) + static_cast<double>(dl);
+                    } else {
+                        double u[CPT];
+                        lds_cols<CPT>(fs + r * a.lp + c0, u);
+#pragma unroll
+                        for (int k = 0; k < CPT; ++k) d += u[k] * mid[k];
+                    }
                 }
                 dp[r] = d;
             }
@@ -845,6 +938,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) lowrank_pass_kernel(const T*
             for (int o = kRT / 2; o > 0; o >>= 1) tmax = fmax(tmax, __shfl_xor_sync((1u << kRT) - 1u, tmax, o));
             const double hn = fmax(h_old, tmax);
             w_s[tid] = tv == kNegInf ? 0.0 : fin_exp_neg<T>(tv - hn);
+            w_f[tid] = static_cast<float>(w_s[tid]);
             __syncwarp((1u << kRT) - 1u);
             if (tid == 0) {
                 sc_s = (h_old == kNegInf || hn == kNegInf) ? 0.0 : fin_exp_neg<T>(h_old - hn);
@@ -856,14 +950,31 @@ __global__ void __launch_bounds__(kThreads + 32, 2) lowrank_pass_kernel(const T*
             const double sc = sc_s;
 #pragma unroll
             for (int k = 0; k < CPT; ++k) acc[k] *= sc;
+            if constexpr (sizeof(T) == 4) {
+                // per-tile fp32 partial (kRT terms), widened once per tile
+                float pa[CPT];
 #pragma unroll
-            for (int r = 0; r < kRT; ++r) {
-                if (r < nr) {
-                    double u[CPT];
-                    lds_cols<CPT>(fs + r * a.lp + c0, u);
-                    const double w = w_s[r];
+                for (int k = 0; k < CPT; ++k) pa[k] = 0.0f;
 #pragma unroll
-                    for (int k = 0; k < CPT; ++k) acc[k] += u[k] * w;
+                for (int r = 0; r < kRT; ++r) {
+                    if (r < nr) {
+                        const float w = w_f[r];
+#pragma unroll
+                        for (int k = 0; k < CPT; ++k) pa[k] = fmaf(fs[r * a.lp + c0 + k], w, pa[k]);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < CPT; ++k) acc[k] += static_cast<double>(pa[k]);
+            } else {
+#pragma unroll
+                for (int r = 0; r < kRT; ++r) {
+                    if (r < nr) {
+                        double u[CPT];
+                        lds_cols<CPT>(fs + r * a.lp + c0, u);
+                        const double w = w_s[r];
+#pragma unroll
+                        for (int k = 0; k < CPT; ++k) acc[k] += u[k] * w;
+                    }
                 }
             }
         }
@@ -1055,13 +1166,20 @@ struct Solver {
     std::vector<cudaEvent_t> evs;                           // phase events (profiling)
     size_t mark_base = 0;
     size_t smem = 0;                                        // low-rank pass stage ring
-    // band work: streamable buckets (both sides <= kBandVec) and the
-    // (bucket, chunk) items of the oversized ones
-    std::vector<DevBuf<uint32_t>> work_stream;
+    // band work: streaming items (buckets with m_b <= kBandVec, split into
+    // row pieces, LPT-assigned to CTAs) and the (bucket, chunk) items of the
+    // oversized buckets
+    struct BandPlan {
+        DevBuf<uint4> items;
+        DevBuf<uint32_t> cta_off, counters;
+        DevBuf<uint2> splits;
+        DevBuf<double> scratch;
+        int nitems = 0;
+    };
+    std::vector<BandPlan> plans;
     std::vector<DevBuf<uint2>> items_rows, items_cols;
-    std::vector<int> n_stream, n_rows_items, n_cols_items;
+    std::vector<int> n_rows_items, n_cols_items;
     int band_grid = 0;
-    int band_debug = std::getenv("LCN_BAND_DEBUG") ? std::atoi(std::getenv("LCN_BAND_DEBUG")) : 0;
 
     explicit Solver(Op& o) : op(o), ctx(*o.ctx), s(o.ctx->stream), n(o.n), m(o.m), l(static_cast<int>(o.l)) {
         lp = static_cast<int>(o.lp);
@@ -1103,33 +1221,98 @@ struct Solver {
         CUDA_OK(cudaFuncSetAttribute(band_stream_kernel<double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
         CUDA_OK(cudaFuncSetAttribute(band_stream_kernel<double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
         int occ = 1;
-        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, band_stream_kernel<float, true>, kThreads + 64,
-                                                              sizeof(BandSmem)));
+        if (op.fp64)
+            CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, band_stream_kernel<double, true>, kThreads + 64,
+                                                                  sizeof(BandSmem)));
+        else
+            CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, band_stream_kernel<float, true>, kThreads + 64,
+                                                                  sizeof(BandSmem)));
         band_grid = std::max(occ, 1) * ctx.num_sms;
+        const size_t esz = op.fp64 ? 8 : 4;
         for (const Band& B : op.bands) {
-            std::vector<uint32_t> w(B.n_work), ws;  // work is sorted by block size, largest first
+            std::vector<uint32_t> w(B.n_work);
             std::vector<uint2> ir, ic;
             if (B.n_work) B.work.download(w.data(), B.n_work, s);
             ctx.sync();
+            // cost model (bytes): block bytes + per-row and per-item overheads
+            struct Piece { uint32_t b, r0, nr, split; double cost; };
+            auto cost_of = [&](size_t nr, size_t ms) { return double(nr * ms * esz) + 256.0 * nr + 4096.0; };
+            double total = 0.0;
             for (uint32_t k : w) {
                 const size_t nb = B.h_src_start[k + 1] - B.h_src_start[k];
-                const size_t ms = row_stride(B.h_tgt_start[k + 1] - B.h_tgt_start[k]);
-                if (nb <= kBandVec && ms <= kBandVec && ms * 4 <= kBandStageBytes) {
-                    ws.push_back(k);
-                } else {
+                const size_t mb = B.h_tgt_start[k + 1] - B.h_tgt_start[k];
+                if (mb <= static_cast<size_t>(kBandVec)) total += cost_of(nb, row_stride(mb));
+            }
+            const double cap = std::max(total / band_grid / 2.0, 65536.0);
+            std::vector<Piece> pieces;
+            std::vector<uint2> splits;
+            size_t scratch = 0;
+            for (uint32_t k : w) {
+                const size_t nb = B.h_src_start[k + 1] - B.h_src_start[k];
+                const size_t mb = B.h_tgt_start[k + 1] - B.h_tgt_start[k];
+                const size_t ms = row_stride(mb);
+                if (nb == 0 || mb == 0) continue;
+                if (mb > static_cast<size_t>(kBandVec)) {
                     for (size_t c = 0; c * kItemRows < nb; ++c) ir.push_back(make_uint2(k, static_cast<uint32_t>(c)));
                     for (size_t c = 0; c * 256 < ms; ++c) ic.push_back(make_uint2(k, static_cast<uint32_t>(c)));
+                    continue;
+                }
+                size_t K = static_cast<size_t>(std::ceil(cost_of(nb, ms) / cap));
+                K = std::max<size_t>(K, ceil_div(nb, kBandVec));
+                // piece rows: multiple of 8 (128-byte aligned chunk starts), <= kBandVec
+                size_t pr = (ceil_div(nb, std::max<size_t>(K, 1)) + 7) & ~size_t(7);
+                pr = std::min<size_t>(std::max<size_t>(pr, 8), kBandVec);
+                K = ceil_div(nb, pr);
+                if (K > 255) throw Status(2, "lcn: bucket split into more than 255 pieces");
+                uint32_t sid = 0xffffffffu;
+                if (K > 1) {
+                    sid = static_cast<uint32_t>(splits.size());
+                    splits.push_back(make_uint2(static_cast<uint32_t>(scratch), static_cast<uint32_t>(K)));
+                    scratch += K * ms;
+                }
+                for (size_t j = 0; j < K; ++j) {
+                    const size_t r0 = j * pr, nr = std::min(pr, nb - r0);
+                    pieces.push_back({k, static_cast<uint32_t>(r0), static_cast<uint32_t>(nr),
+                                      K > 1 ? (sid << 8) | static_cast<uint32_t>(j) : 0xffffffffu, cost_of(nr, ms)});
                 }
             }
-            DevBuf<uint32_t> a(std::max<size_t>(ws.size(), 1));
+            // longest-processing-time greedy: largest piece to the least loaded CTA
+            std::stable_sort(pieces.begin(), pieces.end(), [](const Piece& x, const Piece& y) { return x.cost > y.cost; });
+            using Load = std::pair<double, int>;
+            std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
+            for (int c = 0; c < band_grid; ++c) heap.push({0.0, c});
+            std::vector<std::vector<uint4>> per(band_grid);
+            for (const Piece& pc : pieces) {
+                Load ld = heap.top();
+                heap.pop();
+                per[ld.second].push_back(make_uint4(pc.b, pc.r0, pc.nr, pc.split));
+                ld.first += pc.cost;
+                heap.push(ld);
+            }
+            std::vector<uint4> items;
+            std::vector<uint32_t> off(band_grid + 1, 0);
+            for (int c = 0; c < band_grid; ++c) {
+                off[c] = static_cast<uint32_t>(items.size());
+                items.insert(items.end(), per[c].begin(), per[c].end());
+            }
+            off[band_grid] = static_cast<uint32_t>(items.size());
+            BandPlan P;
+            P.nitems = static_cast<int>(items.size());
+            P.items.resize(std::max<size_t>(items.size(), 1));
+            P.cta_off.resize(off.size());
+            P.splits.resize(std::max<size_t>(splits.size(), 1));
+            P.counters.resize(std::max<size_t>(splits.size(), 1));
+            P.scratch.resize(std::max<size_t>(scratch, 1));
+            if (!items.empty()) P.items.upload(items.data(), items.size(), s);
+            P.cta_off.upload(off.data(), off.size(), s);
+            if (!splits.empty()) P.splits.upload(splits.data(), splits.size(), s);
+            P.counters.zero(s);
+            plans.push_back(std::move(P));
             DevBuf<uint2> r(std::max<size_t>(ir.size(), 1)), c(std::max<size_t>(ic.size(), 1));
-            if (!ws.empty()) a.upload(ws.data(), ws.size(), s);
             if (!ir.empty()) r.upload(ir.data(), ir.size(), s);
             if (!ic.empty()) c.upload(ic.data(), ic.size(), s);
-            n_stream.push_back(static_cast<int>(ws.size()));
             n_rows_items.push_back(static_cast<int>(ir.size()));
             n_cols_items.push_back(static_cast<int>(ic.size()));
-            work_stream.push_back(std::move(a));
             items_rows.push_back(std::move(r));
             items_cols.push_back(std::move(c));
         }
@@ -1275,10 +1458,12 @@ struct Solver {
     void bands(const double* logv, std::vector<DevBuf<double>>& logvp, std::vector<DevBuf<double>>& corr) {
         if (op.kind != 3) return;
         for (size_t b = 0; b < op.bands.size(); ++b) {
-            if (n_stream[b])
-                band_stream_kernel<T, ROWS><<<std::min(band_grid, n_stream[b]), kThreads + 64, sizeof(BandSmem), s>>>(
-                    st.get(), op.view(b), work_stream[b].get(), n_stream[b], band_vals<T>(b), logvp[b].get(),
-                    corr[b].get(), band_debug);
+            if (plans[b].nitems) {
+                BandPlan& P = plans[b];
+                const BandWork wk{P.items.get(), P.cta_off.get(), P.splits.get(), P.counters.get(), P.scratch.get()};
+                band_stream_kernel<T, ROWS><<<band_grid, kThreads + 64, sizeof(BandSmem), s>>>(
+                    st.get(), op.view(b), wk, band_vals<T>(b), logvp[b].get(), corr[b].get());
+            }
             if (ROWS && n_rows_items[b])
                 lcn_row_band_kernel<T><<<n_rows_items[b], kThreads, 0, s>>>(st.get(), op.view(b), items_rows[b].get(),
                                                                           band_vals<T>(b), logv, corr[b].get());

@@ -30,3 +30,9 @@ for rep in range(reps):
     it_ms = res.device_ms / pr.iters
     print(f"sinkhorn {pr.iters} it: {res.device_ms:.2f} ms ({it_ms:.3f} ms/it, {B/it_ms/1e6:.0f} GB/s algorithmic) "
           f"dist={res.distance/pr.mu:.8f} err={res.marginal_err_final:.3e}", flush=True)
+ctx.set_profile(True)
+res = lcn.sinkhorn(op, pm, qm, lcn.SinkhornOptions(tol=0.0, max_iters=pr.iters, want_plan=False, check_support=False))
+ph, it = res.phase_ms()
+ctx.set_profile(False)
+print("phases ms/it: " + " ".join(f"{k}={v / max(it, 1):.3f}" for k, v in
+                                    zip(["col_bands", "col_finalize", "row_bands", "row_finalize"], ph)), flush=True)
