@@ -652,7 +652,8 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
 // carries the rows' scalar streams too (per-band corrections, log marginal,
 // current log s, marginal). Consumer thread t owns columns CPT t .. CPT t +
 // CPT - 1: row dots y_r = F_r . mid (warp transpose reduction + shared
-// combine), per-row finalize by kRT threads, then the running partial
+// combine), per-row finalize in a dedicated warp (tile k's finalize overlaps
+// the consumers' dots of tile k + 1), then the running partial
 // sum_r F_r exp(v_r - h) of the next half's product.
 //   mode 0 (iteration): row side (SIDE 0) / column side (SIDE 1) update
 //   mode 1 (log_matvec): out[r] = H + log y_r, no partial
@@ -770,48 +771,52 @@ __device__ __forceinline__ void lds_cols(const T* p, double (&o)[CPT]) {
 }
 
 template <typename T, int CPT, int SIDE>
-__global__ void __launch_bounds__(kThreads + 32, 2) lowrank_pass_kernel(const T* __restrict__ F, PassArgs a) {
+__global__ void __launch_bounds__(kThreads + 64, 2) lowrank_pass_kernel(const T* __restrict__ F, PassArgs a) {
     DevState* st = a.st;
     if (st->done) return;
     constexpr int S = PassStages<T>::kStages;
     extern __shared__ __align__(128) unsigned char dyn[];
-    __shared__ __align__(8) uint64_t full[S], empty[S];
-    __shared__ double red[kWarps][kRT];
-    __shared__ double w_s[kRT];
-    __shared__ float w_f[kRT];
-    __shared__ double sc_s, h_sh;
-    __shared__ double err_s[kWarps], mn_s[kWarps], mx_s[kWarps];
-    __shared__ unsigned fl_s;
+    // full: producer -> consumers + finalize; empty: consumers (kWarps) +
+    // finalize (1) -> producer; ydone: consumers' row dots -> finalize;
+    // wready: finalize's weights -> consumers (double-buffered by tile parity)
+    __shared__ __align__(8) uint64_t full[S], empty[S], ydone[2], wready[2];
+    __shared__ double red[2][kWarps][kRT];
+    __shared__ double w_s[2][kRT];
+    __shared__ float w_f[2][kRT];
+    __shared__ double sc_s[2], h_fin;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const size_t stage_bytes = pass_stage_bytes<T>(a.lp);
     const uint32_t frow = static_cast<uint32_t>(a.lp * sizeof(T));
     // streams: [corr_0 .. corr_{nc-1}] [log marg] [log cur] [marg]; mode 2: [in]
     const int nc = a.mode == 2 ? 0 : a.ncorr;
-    const double* sv[kMaxBands + 3];
-    int nsv = 0;
-    if (a.mode == 2) {
-        sv[nsv++] = a.in;
-    } else {
-        for (int k = 0; k < nc; ++k) sv[nsv++] = a.corr[k];
-        sv[nsv++] = a.mode == 0 ? a.log_marg : nullptr;
-        sv[nsv++] = (a.mode == 0 && SIDE == 0 && a.with_err) ? a.log_cur : nullptr;
-        sv[nsv++] = (a.mode == 0 && SIDE == 0 && a.with_err) ? a.marg : nullptr;
-    }
     const int np = a.mode == 0 ? a.nperm : 0;
     const long long ntiles = (a.rows + kRT - 1) / kRT;
     if (tid == 0) {
         for (int k = 0; k < S; ++k) {
             mbar_init(&full[k], 1);
-            mbar_init(&empty[k], kWarps);
+            mbar_init(&empty[k], kWarps + 1);
+        }
+        for (int k = 0; k < 2; ++k) {
+            mbar_init(&ydone[k], kWarps);
+            mbar_init(&wready[k], 32);
         }
         fence_mbar_init();
-        fl_s = 0u;
-        h_sh = kNegInf;  // CTA running shift
+        h_fin = kNegInf;
     }
     __syncthreads();
     if (warp == kWarps) {
         // ---------------- producer ----------------
         if (lane == 0) {
+            const double* sv[kMaxBands + 3];
+            int nsv = 0;
+            if (a.mode == 2) {
+                sv[nsv++] = a.in;
+            } else {
+                for (int k = 0; k < nc; ++k) sv[nsv++] = a.corr[k];
+                sv[nsv++] = a.mode == 0 ? a.log_marg : nullptr;
+                sv[nsv++] = (a.mode == 0 && SIDE == 0 && a.with_err) ? a.log_cur : nullptr;
+                sv[nsv++] = (a.mode == 0 && SIDE == 0 && a.with_err) ? a.marg : nullptr;
+            }
             int it = 0;
             for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
                 const int stage = it % S;
@@ -836,11 +841,98 @@ __global__ void __launch_bounds__(kThreads + 32, 2) lowrank_pass_kernel(const T*
         }
         return;
     }
+    if (warp == kWarps + 1) {
+        // ---------------- finalize warp: lane r < kRT owns row r of the tile ----------------
+        const double H = SIDE == 0 ? st->H_t : st->H_s;
+        const int allpos = SIDE == 0 ? st->allpos_t : st->allpos_s;
+        const bool has_in = a.mode == 2 && a.in != nullptr;
+        double vmin = kPosInf, vmax = kNegInf, err = 0.0, h_run = kNegInf;
+        unsigned fl = 0;
+        int it = 0;
+        for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            const int stage = it % S, buf = it & 1;
+            const long long r0 = tile * kRT;
+            const int nr = static_cast<int>(a.rows - r0 < kRT ? a.rows - r0 : kRT);
+            mbar_wait(&full[stage], (it / S) & 1);
+            if (a.mode != 2) mbar_wait(&ydone[buf], (it >> 1) & 1);
+            const double* scal =
+                reinterpret_cast<const double*>(dyn + stage * stage_bytes + static_cast<size_t>(kRT) * frow);
+            double v = kNegInf;
+            bool live = lane < nr;
+            if (live) {
+                const long long i = r0 + lane;
+                if (a.mode == 2) {
+                    v = has_in ? scal[lane] : 0.0;
+                } else {
+                    double nys = 0.0;
+#pragma unroll
+                    for (int w = 0; w < kWarps; ++w) nys += red[buf][w][lane];
+                    double y = nys;
+                    for (int k = 0; k < nc; ++k) y += scal[k * kRT + lane];
+                    if (allpos && !(nys > 0.0)) fl |= SIDE == 0 ? F_NYS_ROW : F_NYS_COL;
+                    if (!(y > 0.0)) fl |= SIDE == 0 ? F_NEG_ROW : F_NEG_COL;
+                    const double k = H + fin_log<T>(y);
+                    if (a.mode == 1) {
+                        a.out[i] = k;
+                        live = false;
+                    } else {
+                        if (SIDE == 0 && a.with_err) {
+                            const double rm = exp(scal[(nc + 1) * kRT + lane] + k);
+                            a.row_marg[i] = rm;
+                            err += fabs(rm - scal[(nc + 2) * kRT + lane]);
+                        }
+                        v = scal[nc * kRT + lane] - k;
+                        a.log_out[i] = v;
+                        const uint32_t* ps = reinterpret_cast<const uint32_t*>(scal + (kMaxBands + 3) * kRT);
+                        for (int pb = 0; pb < np; ++pb) a.perm[pb][ps[pb * kRT + lane]] = v;
+                        if (!isfinite(v)) fl |= SIDE == 0 ? F_LOGS : F_LOGT;
+                    }
+                }
+                if (live) {
+                    vmin = fmin(vmin, v);
+                    vmax = fmax(vmax, v);
+                }
+            }
+            if (a.mode != 1) {
+                // tile shift: running max over the finite values
+                const double tv = (live && v > kNegInf && v < kPosInf) ? v : kNegInf;
+                double tmax = tv;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) tmax = fmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+                const double hn = fmax(h_run, tmax);
+                if (lane < kRT) {
+                    const double w = tv == kNegInf ? 0.0 : fin_exp_neg<T>(tv - hn);
+                    w_s[buf][lane] = w;
+                    w_f[buf][lane] = static_cast<float>(w);
+                }
+                if (lane == 0) {
+                    sc_s[buf] = (h_run == kNegInf || hn == kNegInf) ? 0.0 : fin_exp_neg<T>(h_run - hn);
+                    h_fin = hn;
+                }
+                h_run = hn;
+            }
+            mbar_arrive(&wready[buf]);  // all 32 lanes (release: their shared writes)
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+        }
+        fl = __reduce_or_sync(0xffffffffu, fl);
+        if (a.mode != 1) {
+            vmin = -warp_max(-vmin);
+            vmax = warp_max(vmax);
+            err = warp_sum(err);
+            if (lane == 0) {
+                a.hpart[blockIdx.x] = h_run;
+                a.mnp[blockIdx.x] = vmin;
+                a.mxp[blockIdx.x] = vmax;
+                if (SIDE == 0 && a.with_err) a.err_part[blockIdx.x] = err;
+            }
+        }
+        if (lane == 0 && fl) atomicOr(&st->flags, fl);
+        return;
+    }
     // ---------------- consumers ----------------
     const int c0 = CPT * tid;
     const bool own = c0 < a.lp;
-    const double H = SIDE == 0 ? st->H_t : st->H_s;
-    const int allpos = SIDE == 0 ? st->allpos_t : st->allpos_s;
     double mid[CPT], acc[CPT];
     float mid_hi[CPT], mid_lo[CPT];
 #pragma unroll
@@ -850,18 +942,59 @@ __global__ void __launch_bounds__(kThreads + 32, 2) lowrank_pass_kernel(const T*
         mid_lo[k] = static_cast<float>(mid[k] - static_cast<double>(mid_hi[k]));
         acc[k] = 0.0;
     }
-    double vmin = kPosInf, vmax = kNegInf, err = 0.0;
-    int it = 0;
+    // running partial of tile j (weights from the finalize warp)
+    auto accumulate = [&](int j, int jnr) {
+        const int jstage = j % S, jbuf = j & 1;
+        mbar_wait(&wready[jbuf], (j >> 1) & 1);
+        const T* fs = reinterpret_cast<const T*>(dyn + jstage * stage_bytes);
+        if (own) {
+            const double sc = sc_s[jbuf];
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) acc[k] *= sc;
+            if constexpr (sizeof(T) == 4) {
+                // per-tile fp32 partial (kRT terms), widened once per tile
+                float pa[CPT];
+#pragma unroll
+                for (int k = 0; k < CPT; ++k) pa[k] = 0.0f;
+#pragma unroll
+                for (int r = 0; r < kRT; ++r) {
+                    if (r < jnr) {
+                        const float w = w_f[jbuf][r];
+#pragma unroll
+                        for (int k = 0; k < CPT; ++k) pa[k] = fmaf(fs[r * a.lp + c0 + k], w, pa[k]);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < CPT; ++k) acc[k] += static_cast<double>(pa[k]);
+            } else {
+#pragma unroll
+                for (int r = 0; r < kRT; ++r) {
+                    if (r < jnr) {
+                        double u[CPT];
+                        lds_cols<CPT>(fs + r * a.lp + c0, u);
+                        const double w = w_s[jbuf][r];
+#pragma unroll
+                        for (int k = 0; k < CPT; ++k) acc[k] += u[k] * w;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[jstage]);
+    };
+    int it = 0, prev_nr = 0;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const int stage = it % S;
+        const int stage = it % S, buf = it & 1;
         const long long r0 = tile * kRT;
         const int nr = static_cast<int>(a.rows - r0 < kRT ? a.rows - r0 : kRT);
         mbar_wait(&full[stage], (it / S) & 1);
-        const T* fs = reinterpret_cast<const T*>(dyn + stage * stage_bytes);
-        const double* scal = reinterpret_cast<const double*>(dyn + stage * stage_bytes + static_cast<size_t>(kRT) * frow);
         if (a.mode != 2) {
+            // red[buf] is free once the finalize warp is done with tile it - 2
+            // (implied by the accumulate wait below except in mode 1)
+            if (a.mode == 1 && it >= 2) mbar_wait(&wready[buf], ((it - 2) >> 1) & 1);
+            const T* fs = reinterpret_cast<const T*>(dyn + stage * stage_bytes);
             // row dots y_r = F_r . mid: per-thread partials, warp transpose
-            // reduction, then the kWarps warp sums meet in shared memory.
+            // reduction, the kWarps warp sums meet in the finalize warp
             double dp[kRT];
 #pragma unroll
             for (int r = 0; r < kRT; ++r) {
@@ -888,133 +1021,27 @@ __global__ void __launch_bounds__(kThreads + 32, 2) lowrank_pass_kernel(const T*
                 dp[r] = d;
             }
             const double wsum = transpose_reduce16(dp, lane);
-            if ((lane & 1) == 0) red[warp][(lane >> 1) & 15] = wsum;
+            if ((lane & 1) == 0) red[buf][warp][(lane >> 1) & 15] = wsum;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ydone[buf]);
         }
-        consumers_sync();
-        if (tid < kRT) {
-            const long long i = r0 + tid;
-            double v = kNegInf;
-            bool live = tid < nr;
-            if (live) {
-                if (a.mode == 2) {
-                    v = sv[0] ? scal[tid] : 0.0;
-                } else {
-                    double nys = 0.0;
-#pragma unroll
-                    for (int w = 0; w < kWarps; ++w) nys += red[w][tid];
-                    double y = nys;
-                    for (int k = 0; k < nc; ++k) y += scal[k * kRT + tid];
-                    unsigned fl = 0;
-                    if (allpos && !(nys > 0.0)) fl |= SIDE == 0 ? F_NYS_ROW : F_NYS_COL;
-                    if (!(y > 0.0)) fl |= SIDE == 0 ? F_NEG_ROW : F_NEG_COL;
-                    const double k = H + fin_log<T>(y);
-                    if (a.mode == 1) {
-                        a.out[i] = k;
-                        live = false;
-                    } else {
-                        if (SIDE == 0 && a.with_err) {
-                            const double rm = exp(scal[(nc + 1) * kRT + tid] + k);
-                            a.row_marg[i] = rm;
-                            err += fabs(rm - scal[(nc + 2) * kRT + tid]);
-                        }
-                        v = scal[nc * kRT + tid] - k;
-                        a.log_out[i] = v;
-                        const uint32_t* ps = reinterpret_cast<const uint32_t*>(scal + (kMaxBands + 3) * kRT);
-                        for (int pb = 0; pb < np; ++pb) a.perm[pb][ps[pb * kRT + tid]] = v;
-                        if (!isfinite(v)) fl |= SIDE == 0 ? F_LOGS : F_LOGT;
-                    }
-                    if (fl) atomicOr(&fl_s, fl);
-                }
-                if (live) {
-                    vmin = fmin(vmin, v);
-                    vmax = fmax(vmax, v);
-                }
-            }
-            // tile shift: running max over the finite values
-            const double h_old = h_sh;
-            const double tv = (live && v > kNegInf && v < kPosInf) ? v : kNegInf;
-            double tmax = tv;
-#pragma unroll
-            for (int o = kRT / 2; o > 0; o >>= 1) tmax = fmax(tmax, __shfl_xor_sync((1u << kRT) - 1u, tmax, o));
-            const double hn = fmax(h_old, tmax);
-            w_s[tid] = tv == kNegInf ? 0.0 : fin_exp_neg<T>(tv - hn);
-            w_f[tid] = static_cast<float>(w_s[tid]);
-            __syncwarp((1u << kRT) - 1u);
-            if (tid == 0) {
-                sc_s = (h_old == kNegInf || hn == kNegInf) ? 0.0 : fin_exp_neg<T>(h_old - hn);
-                h_sh = hn;
-            }
+        if (a.mode == 1) {
+            if (lane == 0) mbar_arrive(&empty[stage]);
+        } else if (it > 0) {
+            accumulate(it - 1, prev_nr);  // overlaps the finalize of tile `it`
         }
-        consumers_sync();
-        if (a.mode != 1 && own) {
-            const double sc = sc_s;
-#pragma unroll
-            for (int k = 0; k < CPT; ++k) acc[k] *= sc;
-            if constexpr (sizeof(T) == 4) {
-                // per-tile fp32 partial (kRT terms), widened once per tile
-                float pa[CPT];
-#pragma unroll
-                for (int k = 0; k < CPT; ++k) pa[k] = 0.0f;
-#pragma unroll
-                for (int r = 0; r < kRT; ++r) {
-                    if (r < nr) {
-                        const float w = w_f[r];
-#pragma unroll
-                        for (int k = 0; k < CPT; ++k) pa[k] = fmaf(fs[r * a.lp + c0 + k], w, pa[k]);
-                    }
-                }
-#pragma unroll
-                for (int k = 0; k < CPT; ++k) acc[k] += static_cast<double>(pa[k]);
-            } else {
-#pragma unroll
-                for (int r = 0; r < kRT; ++r) {
-                    if (r < nr) {
-                        double u[CPT];
-                        lds_cols<CPT>(fs + r * a.lp + c0, u);
-                        const double w = w_s[r];
-#pragma unroll
-                        for (int k = 0; k < CPT; ++k) acc[k] += u[k] * w;
-                    }
-                }
-            }
-        }
-        // release the stage to the producer (one arrival per consumer warp)
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);
+        prev_nr = nr;
     }
-    if (a.mode == 1) {
-        consumers_sync();
-        if (tid == 0 && fl_s) atomicOr(&st->flags, fl_s);
-        return;
-    }
-    vmin = -warp_max(-vmin);
-    vmax = warp_max(vmax);
-    err = warp_sum(err);
-    if (lane == 0) {
-        mn_s[warp] = vmin;
-        mx_s[warp] = vmax;
-        err_s[warp] = err;
-    }
+    if (a.mode == 1) return;
+    if (it > 0) accumulate(it - 1, prev_nr);
     consumers_sync();
-    const double hb = h_sh;
+    const double hb = h_fin;  // final CTA shift (written before the last wready)
 #pragma unroll
     for (int k = 0; k < CPT; ++k)
         if (own) a.part[static_cast<long long>(blockIdx.x) * a.lp + c0 + k] = hb == kNegInf ? 0.0 : acc[k];
-    if (tid == 0) {
-        double mn = kPosInf, mx = kNegInf, e = 0.0;
-        for (int w = 0; w < kWarps; ++w) {
-            mn = fmin(mn, mn_s[w]);
-            mx = fmax(mx, mx_s[w]);
-            e += err_s[w];
-        }
-        a.hpart[blockIdx.x] = hb;
-        a.mnp[blockIdx.x] = mn;
-        a.mxp[blockIdx.x] = mx;
-        if (SIDE == 0 && a.with_err) a.err_part[blockIdx.x] = e;
-        if (fl_s) atomicOr(&st->flags, fl_s);
-    }
 }
 
+// ---------------------------------------------------------------------------
 // Global shift and mid = sum_b exp(h_b - H) part_b over the G CTA partials;
 // which: 0 -> t side, 1 -> s side. One CTA per 32 columns: lane = column,
 // warps split the partials, shared memory combines them.
@@ -1192,9 +1219,9 @@ struct Solver {
             if (op.fp64) set_attrs<double>();
             else set_attrs<float>();
             if (op.fp64)
-                CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lowrank_pass_kernel<double, 2, 0>, kThreads + 32, smem));
+                CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lowrank_pass_kernel<double, 2, 0>, kThreads + 64, smem));
             else
-                CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lowrank_pass_kernel<float, 2, 0>, kThreads + 32, smem));
+                CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lowrank_pass_kernel<float, 2, 0>, kThreads + 64, smem));
         }
         G = std::max(1, occ) * ctx.num_sms;
         if (op.kind == 3) init_band_stream();
@@ -1390,9 +1417,9 @@ struct Solver {
     void pass(const PassArgs& a) {
         const T* F = SIDE == 0 ? U<T>() : Wt<T>();
         switch (CPT) {
-            case 1: lowrank_pass_kernel<T, 1, SIDE><<<G, kThreads + 32, smem, s>>>(F, a); break;
-            case 2: lowrank_pass_kernel<T, 2, SIDE><<<G, kThreads + 32, smem, s>>>(F, a); break;
-            case 4: lowrank_pass_kernel<T, 4, SIDE><<<G, kThreads + 32, smem, s>>>(F, a); break;
+            case 1: lowrank_pass_kernel<T, 1, SIDE><<<G, kThreads + 64, smem, s>>>(F, a); break;
+            case 2: lowrank_pass_kernel<T, 2, SIDE><<<G, kThreads + 64, smem, s>>>(F, a); break;
+            case 4: lowrank_pass_kernel<T, 4, SIDE><<<G, kThreads + 64, smem, s>>>(F, a); break;
         }
     }
     PassArgs base_args() {
