@@ -692,32 +692,33 @@ struct PassArgs {
 // of 16 x 5: at every step a lane keeps half of its values and trades the
 // other half with its partner. On exit lane L holds the full sum of value
 // (L >> 1) & 15 (both lanes of a pair hold the same row).
-__device__ __forceinline__ double transpose_reduce16(double (&v)[16], int lane) {
+template <typename V>
+__device__ __forceinline__ V transpose_reduce16(V (&v)[16], int lane) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) {  // xor 16
         const bool hi = lane & 16;
-        const double send = hi ? v[k] : v[k + 8];
-        const double keep = hi ? v[k + 8] : v[k];
+        const V send = hi ? v[k] : v[k + 8];
+        const V keep = hi ? v[k + 8] : v[k];
         v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {  // xor 8
         const bool hi = lane & 8;
-        const double send = hi ? v[k] : v[k + 4];
-        const double keep = hi ? v[k + 4] : v[k];
+        const V send = hi ? v[k] : v[k + 4];
+        const V keep = hi ? v[k + 4] : v[k];
         v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
     }
 #pragma unroll
     for (int k = 0; k < 2; ++k) {  // xor 4
         const bool hi = lane & 4;
-        const double send = hi ? v[k] : v[k + 2];
-        const double keep = hi ? v[k + 2] : v[k];
+        const V send = hi ? v[k] : v[k + 2];
+        const V keep = hi ? v[k + 2] : v[k];
         v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
     }
     {  // xor 2
         const bool hi = lane & 2;
-        const double send = hi ? v[0] : v[1];
-        const double keep = hi ? v[1] : v[0];
+        const V send = hi ? v[0] : v[1];
+        const V keep = hi ? v[1] : v[0];
         v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
     }
     return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
@@ -934,12 +935,11 @@ __global__ void __launch_bounds__(kThreads + 64, 2) lowrank_pass_kernel(const T*
     const int c0 = CPT * tid;
     const bool own = c0 < a.lp;
     double mid[CPT], acc[CPT];
-    float mid_hi[CPT], mid_lo[CPT];
+    float mid_hi[CPT];
 #pragma unroll
     for (int k = 0; k < CPT; ++k) {
         mid[k] = (a.mode != 2 && own) ? a.mid[c0 + k] : 0.0;
         mid_hi[k] = static_cast<float>(mid[k]);
-        mid_lo[k] = static_cast<float>(mid[k] - static_cast<double>(mid_hi[k]));
         acc[k] = 0.0;
     }
     // running partial of tile j (weights from the finalize warp)
@@ -995,33 +995,46 @@ __global__ void __launch_bounds__(kThreads + 64, 2) lowrank_pass_kernel(const T*
             const T* fs = reinterpret_cast<const T*>(dyn + stage * stage_bytes);
             // row dots y_r = F_r . mid: per-thread partials, warp transpose
             // reduction, the kWarps warp sums meet in the finalize warp
-            double dp[kRT];
+            if constexpr (sizeof(T) == 4) {
+                // fp32 storage: fp32 products and warp sums (the factor rows
+                // carry fp32 rounding already), widened per warp sum. Rows past
+                // nr hold stale data; their sums are never read.
+                float dp[kRT];
 #pragma unroll
-            for (int r = 0; r < kRT; ++r) {
-                double d = 0.0;
-                if (own && r < nr) {
-                    if constexpr (sizeof(T) == 4) {
-                        // fp32 products of the fp32 factor row with mid (split
-                        // hi + lo so mid keeps ~48 bits), widened once per row
-                        float dh = 0.0f, dl = 0.0f;
-#pragma unroll
-                        for (int k = 0; k < CPT; ++k) {
-                            const float u = fs[r * a.lp + c0 + k];
-                            dh = fmaf(u, mid_hi[k], dh);
-                            dl = fmaf(u, mid_lo[k], dl);
+                for (int r = 0; r < kRT; ++r) {
+                    float d = 0.0f;
+                    if (own) {
+                        const float* u = reinterpret_cast<const float*>(fs) + r * a.lp + c0;
+                        if constexpr (CPT == 4) {
+                            const float4 x = *reinterpret_cast<const float4*>(u);
+                            d = fmaf(x.w, mid_hi[3], fmaf(x.z, mid_hi[2], fmaf(x.y, mid_hi[1], x.x * mid_hi[0])));
+                        } else if constexpr (CPT == 2) {
+                            const float2 x = *reinterpret_cast<const float2*>(u);
+                            d = fmaf(x.y, mid_hi[1], x.x * mid_hi[0]);
+                        } else {
+                            d = u[0] * mid_hi[0];
                         }
-                        d = static_cast<double>(dh) + static_cast<double>(dl);
-                    } else {
+                    }
+                    dp[r] = d;
+                }
+                const float wsum = transpose_reduce16(dp, lane);
+                if ((lane & 1) == 0) red[buf][warp][(lane >> 1) & 15] = static_cast<double>(wsum);
+            } else {
+                double dp[kRT];
+#pragma unroll
+                for (int r = 0; r < kRT; ++r) {
+                    double d = 0.0;
+                    if (own && r < nr) {
                         double u[CPT];
                         lds_cols<CPT>(fs + r * a.lp + c0, u);
 #pragma unroll
                         for (int k = 0; k < CPT; ++k) d += u[k] * mid[k];
                     }
+                    dp[r] = d;
                 }
-                dp[r] = d;
+                const double wsum = transpose_reduce16(dp, lane);
+                if ((lane & 1) == 0) red[buf][warp][(lane >> 1) & 15] = wsum;
             }
-            const double wsum = transpose_reduce16(dp, lane);
-            if ((lane & 1) == 0) red[buf][warp][(lane >> 1) & 15] = wsum;
             __syncwarp();
             if (lane == 0) mbar_arrive(&ydone[buf]);
         }
