@@ -229,169 +229,29 @@ __global__ void sparse_row_finalize_kernel(DevState* __restrict__ st, const doub
 }
 
 // ---------------------------------------------------------------------------
-// LCN band kernels for oversized buckets (either side > kBandVec). Work items
-// are (bucket, chunk): the row kernel's chunk is a range of kItemRows rows,
-// the column kernel's a range of 256 columns, so a large bucket spreads over
-// several CTAs and every output is written by exactly one CTA (plain stores).
-// ---------------------------------------------------------------------------
-constexpr int kRowsPerWarp = 8;
-constexpr int kItemRows = 64;
-
-template <typename T>
-__global__ void __launch_bounds__(kThreads, 3) lcn_row_band_kernel(const DevState* __restrict__ st, BandView bv,
-                                                                const uint2* __restrict__ items,
-                                                                const T* __restrict__ vals,
-                                                                const double* __restrict__ log_t,
-                                                                double* __restrict__ corr) {
-    if (st->done) return;
-    __shared__ __align__(16) double tt[kTile];
-    const double H = st->H_t;
-    const uint32_t b = items[blockIdx.x].x;
-    const uint32_t rbeg = items[blockIdx.x].y * kItemRows;
-    const uint32_t nb_all = bv.src_start[b + 1] - bv.src_start[b];
-    const uint32_t sb = bv.src_start[b] + rbeg;
-    const uint32_t nb = min(nb_all - rbeg, static_cast<uint32_t>(kItemRows));
-    const uint32_t tb = bv.tgt_start[b], mb = bv.tgt_start[b + 1] - tb;
-    const uint32_t ms = static_cast<uint32_t>(row_stride(mb));
-    const unsigned long long off = bv.blk_off[b] + static_cast<unsigned long long>(rbeg) * ms;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint32_t c0 = 0; c0 < ms; c0 += kTile) {
-        const uint32_t cn = min(ms - c0, static_cast<uint32_t>(kTile));  // multiple of 4
-        __syncthreads();
-        for (uint32_t c = threadIdx.x; c < cn; c += kThreads)
-            tt[c] = c0 + c < mb ? exp(log_t[bv.tgt_order[tb + c0 + c]] - H) : 0.0;
-        __syncthreads();
-        const uint32_t nq = cn / 4;
-        for (uint32_t r0 = warp * kRowsPerWarp; r0 < nb; r0 += kWarps * kRowsPerWarp) {
-            double acc[kRowsPerWarp];
-#pragma unroll
-            for (int j = 0; j < kRowsPerWarp; ++j) acc[j] = 0.0;
-            for (uint32_t q = lane; q < nq; q += 32) {
-                Raw4<T> v[kRowsPerWarp];
-#pragma unroll
-                for (int j = 0; j < kRowsPerWarp; ++j) {
-                    if (r0 + j < nb) v[j] = raw4(vals + off + static_cast<unsigned long long>(r0 + j) * ms + c0 + 4 * q);
-                    else v[j].v[0] = v[j].v[1] = v[j].v[2] = v[j].v[3] = T(0);
-                }
-                if constexpr (sizeof(T) == 4) {
-                    // fp32 quad products, widened once per quad (F2F.F64 runs at
-                    // a quarter of the DFMA rate)
-                    const float t0 = static_cast<float>(tt[4 * q]), t1 = static_cast<float>(tt[4 * q + 1]);
-                    const float t2 = static_cast<float>(tt[4 * q + 2]), t3 = static_cast<float>(tt[4 * q + 3]);
-#pragma unroll
-                    for (int j = 0; j < kRowsPerWarp; ++j)
-                        acc[j] += static_cast<double>(
-                            fmaf(v[j].v[3], t3, fmaf(v[j].v[2], t2, fmaf(v[j].v[1], t1, v[j].v[0] * t0))));
-                } else {
-                    const double t0 = tt[4 * q], t1 = tt[4 * q + 1], t2 = tt[4 * q + 2], t3 = tt[4 * q + 3];
-#pragma unroll
-                    for (int j = 0; j < kRowsPerWarp; ++j)
-                        acc[j] += static_cast<double>(v[j].v[0]) * t0 + static_cast<double>(v[j].v[1]) * t1 +
-                                  static_cast<double>(v[j].v[2]) * t2 + static_cast<double>(v[j].v[3]) * t3;
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < kRowsPerWarp; ++j) acc[j] = warp_sum(acc[j]);
-            if (lane < kRowsPerWarp && r0 + lane < nb) {
-                double a = acc[0];
-#pragma unroll
-                for (int j = 1; j < kRowsPerWarp; ++j)
-                    if (lane == j) a = acc[j];
-                const uint32_t i = bv.src_order[sb + r0 + lane];
-                corr[i] = c0 == 0 ? a : corr[i] + a;
-            }
-        }
-    }
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kThreads, 3) lcn_col_band_kernel(const DevState* __restrict__ st, BandView bv,
-                                                                const uint2* __restrict__ items,
-                                                                const T* __restrict__ vals,
-                                                                const double* __restrict__ log_s,
-                                                                double* __restrict__ corr) {
-    if (st->done) return;
-    constexpr int kGroups = 4, kGT = kThreads / kGroups;  // 64 quads (256 columns) per chunk
-    __shared__ double ss[kTile];
-    __shared__ double red[kGroups][kGT * 4];
-    const double H = st->H_s;
-    const uint32_t b = items[blockIdx.x].x;
-    const uint32_t qbeg = items[blockIdx.x].y * kGT;
-    const uint32_t sb = bv.src_start[b], nb = bv.src_start[b + 1] - sb;
-    const uint32_t tb = bv.tgt_start[b], mb = bv.tgt_start[b + 1] - tb;
-    const uint32_t ms = static_cast<uint32_t>(row_stride(mb));
-    const unsigned long long off = bv.blk_off[b];
-    const int g = threadIdx.x / kGT, t = threadIdx.x % kGT;
-    for (uint32_t r0 = 0; r0 < nb; r0 += kTile) {
-        const uint32_t rn = min(nb - r0, static_cast<uint32_t>(kTile));
-        __syncthreads();
-        for (uint32_t r = threadIdx.x; r < rn; r += kThreads) ss[r] = exp(log_s[bv.src_order[sb + r0 + r]] - H);
-        __syncthreads();
-        const uint32_t q = qbeg + t;
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        if (q < ms / 4) {
-            const T* col = vals + off + static_cast<unsigned long long>(r0) * ms + 4 * q;
-            uint32_t r = g;
-            for (; r + 3 * kGroups < rn; r += 4 * kGroups) {
-                const Raw4<T> v0 = raw4(col + static_cast<unsigned long long>(r) * ms);
-                const Raw4<T> v1 = raw4(col + static_cast<unsigned long long>(r + kGroups) * ms);
-                const Raw4<T> v2 = raw4(col + static_cast<unsigned long long>(r + 2 * kGroups) * ms);
-                const Raw4<T> v3 = raw4(col + static_cast<unsigned long long>(r + 3 * kGroups) * ms);
-                if constexpr (sizeof(T) == 4) {
-                    const float s0 = static_cast<float>(ss[r]), s1 = static_cast<float>(ss[r + kGroups]);
-                    const float s2 = static_cast<float>(ss[r + 2 * kGroups]), s3 = static_cast<float>(ss[r + 3 * kGroups]);
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        acc[k] += static_cast<double>(
-                            fmaf(v3.v[k], s3, fmaf(v2.v[k], s2, fmaf(v1.v[k], s1, v0.v[k] * s0))));
-                } else {
-                    const double s0 = ss[r], s1 = ss[r + kGroups], s2 = ss[r + 2 * kGroups], s3 = ss[r + 3 * kGroups];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        acc[k] += static_cast<double>(v0.v[k]) * s0 + static_cast<double>(v1.v[k]) * s1 +
-                                  static_cast<double>(v2.v[k]) * s2 + static_cast<double>(v3.v[k]) * s3;
-                }
-            }
-            for (; r < rn; r += kGroups) {
-                const Raw4<T> v0 = raw4(col + static_cast<unsigned long long>(r) * ms);
-                const double s0 = ss[r];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) acc[k] += static_cast<double>(v0.v[k]) * s0;
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) red[g][4 * t + k] = acc[k];
-        __syncthreads();
-        const uint32_t c = 4 * qbeg + threadIdx.x;  // 256 threads cover the chunk's 256 columns
-        if (c < mb) {
-            const double a = red[0][threadIdx.x] + red[1][threadIdx.x] + red[2][threadIdx.x] + red[3][threadIdx.x];
-            const uint32_t j = bv.tgt_order[tb + c];
-            corr[j] = r0 == 0 ? a : corr[j] + a;
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
 // Streaming band kernels (warp-specialized). The band's work is a list of
-// items (bucket b, rows r0 .. r0 + nr) -- big buckets are split into row
-// pieces -- assigned to CTAs on the host by longest-processing-time greedy,
-// so every CTA streams about the same number of bytes. Per CTA:
-//   warp kWarps     bulk-copies the item's block rows through a ring of
-//                   kBandStages shared stages (mbarrier transaction counts);
+// items (bucket b, rows r0 .. r0 + nr, columns c0 .. c0 + cw): buckets with
+// more than kBandVec columns are cut into column tiles, big buckets into row
+// pieces; the items are assigned to CTAs on the host by longest-processing-
+// time greedy so every CTA streams about the same number of bytes. Per CTA:
+//   warp kWarps     bulk-copies the item's block rows (one copy per chunk of
+//                   whole rows, one per row for a column tile) through a ring
+//                   of kBandStages shared stages (mbarrier transaction counts);
 //   warp kWarps + 1 loads the item's scaling vector (tt_c = exp(log t - H_t)
 //                   for the row pass, ss_r = exp(log s - H_s) for the column
 //                   pass) and output indices into one of two slots;
 //   8 consumer warps only wait on mbarriers and compute from shared memory.
-// ROWS = true:  corr[src] = sum_c delta[r][c] tt[c]   (K side, plain stores)
-// ROWS = false: corr[tgt] = sum_r delta[r][c] ss[r]   (K^T side). A bucket
-//   split into K pieces writes K partial column sums to scratch; the piece
-//   that finishes last (per-bucket arrival counter) adds them in piece order,
-//   so the result does not depend on CTA timing.
-// Two CTAs per SM (smem 112 KB each) keep 16 consumer warps resident.
+// ROWS = true:  corr[src] = sum_c delta[r][c] tt[c]   (K side)
+// ROWS = false: corr[tgt] = sum_r delta[r][c] ss[r]   (K^T side)
+// An output split over K items (row sums of a bucket's column tiles, column
+// sums of its row pieces) goes through scratch: every piece writes its
+// partials, the piece that finishes last (arrival counter) adds them in piece
+// order, so results do not depend on CTA timing. Unsplit outputs are plain
+// stores. Two CTAs per SM (112 KB smem each) keep 16 consumer warps resident.
 // ---------------------------------------------------------------------------
 constexpr int kBandStages = 5;
 constexpr int kBandStageBytes = 16 * 1024;
-constexpr int kBandVec = 1024;  // max bucket columns / piece rows of the streaming kernels
+constexpr int kBandVec = 1024;  // max item columns / item rows
 
 struct BandSmem {
     unsigned char ring[kBandStages][kBandStageBytes];
@@ -399,24 +259,52 @@ struct BandSmem {
     uint32_t out[2][kBandVec];  // output indices per item slot
     double red[kBandVec];       // column pass: per-row-group partial sums (groups x row stride <= kBandVec)
     uint64_t full[kBandStages], empty[kBandStages], vfull[2], vempty[2];
-    uint32_t last;              // column pass: this CTA combines the split bucket
+    uint32_t last;              // this CTA combines a split output
+};
+
+struct BandItem {
+    uint32_t b, r0, nr, c0, cw;
+    uint32_t split[2];  // [0] row pass, [1] column pass: sid << 8 | piece, or ~0u
+    uint32_t pad;
 };
 
 struct BandWork {
-    const uint4* items;      // {bucket, r0, nr, split}: split = sid << 8 | piece, or ~0u
+    const BandItem* items;
     const uint32_t* cta_off;  // CTA c processes items cta_off[c] .. cta_off[c + 1] - 1
-    const uint2* splits;      // sid -> {scratch offset (doubles), pieces}
-    uint32_t* counters;       // sid -> arrivals (reset by the combining CTA)
+    const uint2* splits;      // this pass: sid -> {scratch offset (doubles), pieces}
+    uint32_t* counters;       // this pass: sid -> arrivals (reset by the combining CTA)
     double* scratch;
 };
 
 // rows per ring stage; a multiple of 8 keeps every chunk start 128-byte
 // aligned (row bytes are a multiple of 16, block starts of 128)
 template <typename T>
-__device__ __forceinline__ int band_rows_per_stage(uint32_t ms) {
-    int r = static_cast<int>(kBandStageBytes / (ms * sizeof(T)));
+__device__ __forceinline__ int band_rows_per_stage(uint32_t ws) {
+    int r = static_cast<int>(kBandStageBytes / (ws * sizeof(T)));
     if (r >= 8) r &= ~7;
     return r < 1 ? 1 : r;
+}
+
+// Split-output epilogue: partials of `count` outputs are in scratch at
+// base + piece * count; the last piece to arrive sums them in order into
+// corr[outi[c]]. Called by all consumer threads after they wrote their partials.
+__device__ __forceinline__ void band_combine(BandSmem& sm, const BandWork& wk, uint32_t split, uint32_t count,
+                                             const uint32_t* outi, double* __restrict__ corr, int tid) {
+    const uint2 sp = wk.splits[split >> 8];
+    __threadfence();
+    consumers_sync();
+    if (tid == 0) sm.last = atomicAdd(&wk.counters[split >> 8], 1u) == sp.y - 1;
+    consumers_sync();
+    if (sm.last) {
+        __threadfence();
+        const double* base = wk.scratch + sp.x;
+        for (uint32_t c = tid; c < count; c += kThreads) {
+            double v = 0.0;
+            for (uint32_t k = 0; k < sp.y; ++k) v += __ldcg(base + static_cast<size_t>(k) * count + c);
+            corr[outi[c]] = v;
+        }
+        if (tid == 0) wk.counters[split >> 8] = 0u;
+    }
 }
 
 // logv: the band's bucket-ordered copy of log t (row pass) / log s (column
@@ -452,17 +340,24 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
             uint32_t phase = 0;
             bool wrapped = false;
             for (uint32_t it = i_beg; it < i_end; ++it) {
-                const uint4 item = wk.items[it];
-                const uint32_t b = item.x;
-                const uint32_t ms = static_cast<uint32_t>(row_stride(bv.tgt_start[b + 1] - bv.tgt_start[b]));
-                const int R = band_rows_per_stage<T>(ms);
-                const T* blk = vals + bv.blk_off[b] + static_cast<unsigned long long>(item.y) * ms;
-                for (uint32_t r0 = 0; r0 < item.z; r0 += R) {
-                    const uint32_t nr = item.z - r0 < static_cast<uint32_t>(R) ? item.z - r0 : static_cast<uint32_t>(R);
+                const BandItem item = wk.items[it];
+                const uint32_t ms = static_cast<uint32_t>(row_stride(bv.tgt_start[item.b + 1] - bv.tgt_start[item.b]));
+                const uint32_t ws = static_cast<uint32_t>(row_stride(item.cw));  // item row width in the ring
+                const int R = band_rows_per_stage<T>(ws);
+                const T* blk = vals + bv.blk_off[item.b] + static_cast<unsigned long long>(item.r0) * ms + item.c0;
+                for (uint32_t r0 = 0; r0 < item.nr; r0 += R) {
+                    const uint32_t nr = item.nr - r0 < static_cast<uint32_t>(R) ? item.nr - r0 : static_cast<uint32_t>(R);
                     if (wrapped) mbar_wait(&sm.empty[stage], phase ^ 1u);
-                    const uint32_t bytes = nr * ms * static_cast<uint32_t>(sizeof(T));
-                    mbar_arrive_expect_tx(&sm.full[stage], bytes);
-                    bulk_g2s(sm.ring[stage], blk + static_cast<unsigned long long>(r0) * ms, bytes, &sm.full[stage]);
+                    const uint32_t rb = ws * static_cast<uint32_t>(sizeof(T));
+                    mbar_arrive_expect_tx(&sm.full[stage], nr * rb);
+                    const T* src = blk + static_cast<unsigned long long>(r0) * ms;
+                    if (ws == ms) {
+                        bulk_g2s(sm.ring[stage], src, nr * rb, &sm.full[stage]);
+                    } else {
+                        for (uint32_t r = 0; r < nr; ++r)
+                            bulk_g2s(sm.ring[stage] + r * rb, src + static_cast<unsigned long long>(r) * ms, rb,
+                                     &sm.full[stage]);
+                    }
                     if (++stage == kBandStages) {
                         stage = 0;
                         phase ^= 1u;
@@ -477,15 +372,14 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
         // ---------------- producer 2: scaling values + output indices ----------------
         int kb = 0;
         for (uint32_t it = i_beg; it < i_end; ++it, ++kb) {
-            const uint4 item = wk.items[it];
-            const uint32_t b = item.x;
-            const uint32_t sb = bv.src_start[b] + item.y;
-            const uint32_t tb = bv.tgt_start[b], mb = bv.tgt_start[b + 1] - tb;
-            const uint32_t count = ROWS ? static_cast<uint32_t>(row_stride(mb)) : item.z;
-            const uint32_t valid = ROWS ? mb : item.z;
+            const BandItem item = wk.items[it];
+            const uint32_t sb = bv.src_start[item.b] + item.r0;
+            const uint32_t tb = bv.tgt_start[item.b] + item.c0;
+            const uint32_t count = ROWS ? static_cast<uint32_t>(row_stride(item.cw)) : item.nr;
+            const uint32_t valid = ROWS ? item.cw : item.nr;
             const uint32_t v0 = ROWS ? tb : sb;
             const uint32_t o0 = ROWS ? sb : tb;
-            const uint32_t nout = ROWS ? item.z : mb;
+            const uint32_t nout = ROWS ? item.nr : item.cw;
             const uint32_t* order = ROWS ? bv.src_order : bv.tgt_order;
             const int slot = kb & 1;
             if (kb >= 2) mbar_wait(&sm.vempty[slot], ((kb >> 1) - 1) & 1);
@@ -508,13 +402,16 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
     uint32_t phase = 0;
     int kb = 0;
     for (uint32_t it = i_beg; it < i_end; ++it, ++kb) {
-        const uint4 item = wk.items[it];
-        const uint32_t b = item.x;
-        const uint32_t mb = bv.tgt_start[b + 1] - bv.tgt_start[b];
-        const uint32_t ms = static_cast<uint32_t>(row_stride(mb));
-        const uint32_t nq = ms / 4;
+        const BandItem item = wk.items[it];
+        const uint32_t ws = static_cast<uint32_t>(row_stride(item.cw));
+        const uint32_t nq = ws / 4;
         const int slot = kb & 1;
-        const int R = band_rows_per_stage<T>(ms);
+        const int R = band_rows_per_stage<T>(ws);
+        const uint32_t split = item.split[ROWS ? 0 : 1];
+        // row pass, split: partial row sums go to scratch
+        double* rpart = nullptr;
+        if (ROWS && split != 0xffffffffu)
+            rpart = wk.scratch + wk.splits[split >> 8].x + static_cast<size_t>(split & 0xffu) * item.nr;
         // column pass mapping: groups of nq threads, thread (g, q) owns quad q
         // of rows g, g + ng, ... of every chunk; sums stay in registers
         const uint32_t ng = nq >= static_cast<uint32_t>(kThreads) ? 1u : kThreads / nq;
@@ -523,18 +420,19 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         mbar_wait(&sm.vfull[slot], (kb >> 1) & 1);
         const uint32_t* outi = sm.out[slot];
-        for (uint32_t r0 = 0; r0 < item.z; r0 += R) {
-            const uint32_t nr = item.z - r0 < static_cast<uint32_t>(R) ? item.z - r0 : static_cast<uint32_t>(R);
+        for (uint32_t r0 = 0; r0 < item.nr; r0 += R) {
+            const uint32_t nr = item.nr - r0 < static_cast<uint32_t>(R) ? item.nr - r0 : static_cast<uint32_t>(R);
             mbar_wait(&sm.full[stage], phase);
             const T* blk = reinterpret_cast<const T*>(sm.ring[stage]);
             if constexpr (ROWS) {
-                // two rows per warp step: independent load/FMA/shuffle chains interleave
+                // two rows per warp step: independent load/FMA chains interleave
                 for (uint32_t r = warp; r < nr; r += 2 * kWarps) {
                     const uint32_t r2 = r + kWarps;
                     const bool two = r2 < nr;
-                    const T* row = blk + r * ms;
-                    const T* row2 = blk + (two ? r2 : r) * ms;
+                    const T* row = blk + r * ws;
+                    const T* row2 = blk + (two ? r2 : r) * ws;
                     double acc, acc2;
+                    int l1, l2;  // lanes holding the two sums
                     if constexpr (sizeof(T) == 4) {
                         // fp32 products and row partials (<= kBandVec terms), widened once
                         const float* vf = reinterpret_cast<const float*>(sm.vec[slot]);
@@ -548,13 +446,16 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
                             f2 = fmaf(y.x, tq.x, f2); f2 = fmaf(y.y, tq.y, f2);
                             f2 = fmaf(y.z, tq.z, f2); f2 = fmaf(y.w, tq.w, f2);
                         }
+                        // two-row transpose reduction: lanes < 16 end with row r's
+                        // sum, lanes >= 16 with row r2's (5 shuffles, not 10)
+                        const bool hi = lane & 16;
+                        float x = (hi ? f2 : f) + __shfl_xor_sync(0xffffffffu, hi ? f : f2, 16);
 #pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) {
-                            f += __shfl_xor_sync(0xffffffffu, f, o);
-                            f2 += __shfl_xor_sync(0xffffffffu, f2, o);
-                        }
-                        acc = f;
-                        acc2 = f2;
+                        for (int o = 8; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+                        acc = x;
+                        acc2 = x;
+                        l1 = 0;
+                        l2 = 16;
                     } else {
                         const double* vec = sm.vec[slot];
                         acc = 0.0;
@@ -574,9 +475,17 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
                             acc += __shfl_xor_sync(0xffffffffu, acc, o);
                             acc2 += __shfl_xor_sync(0xffffffffu, acc2, o);
                         }
+                        l1 = 0;
+                        l2 = 1;
                     }
-                    if (lane == 0) corr[outi[r0 + r]] = acc;
-                    if (lane == 1 && two) corr[outi[r0 + r2]] = acc2;
+                    if (lane == l1) {
+                        if (rpart) rpart[r0 + r] = acc;
+                        else corr[outi[r0 + r]] = acc;
+                    }
+                    if (lane == l2 && two) {
+                        if (rpart) rpart[r0 + r2] = acc2;
+                        else corr[outi[r0 + r2]] = acc2;
+                    }
                 }
             } else if (col_own) {
                 const T* p = blk + 4 * q;
@@ -584,7 +493,7 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
                     const float* vf = reinterpret_cast<const float*>(sm.vec[slot]) + r0;
                     float f0 = 0.0f, f1 = 0.0f, f2 = 0.0f, f3 = 0.0f;
                     for (uint32_t r = g; r < nr; r += ng) {
-                        const float4 x = *reinterpret_cast<const float4*>(p + r * ms);
+                        const float4 x = *reinterpret_cast<const float4*>(p + r * ws);
                         const float sr = vf[r];
                         f0 = fmaf(x.x, sr, f0); f1 = fmaf(x.y, sr, f1);
                         f2 = fmaf(x.z, sr, f2); f3 = fmaf(x.w, sr, f3);
@@ -593,8 +502,8 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
                 } else {
                     const double* vec = sm.vec[slot] + r0;
                     for (uint32_t r = g; r < nr; r += ng) {
-                        const double2 x0 = *reinterpret_cast<const double2*>(p + r * ms);
-                        const double2 x1 = *reinterpret_cast<const double2*>(p + r * ms + 2);
+                        const double2 x0 = *reinterpret_cast<const double2*>(p + r * ws);
+                        const double2 x1 = *reinterpret_cast<const double2*>(p + r * ws + 2);
                         const double sr = vec[r];
                         a0 += x0.x * sr; a1 += x0.y * sr; a2 += x1.x * sr; a3 += x1.y * sr;
                     }
@@ -607,39 +516,26 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
                 phase ^= 1u;
             }
         }
-        if constexpr (!ROWS) {
-            // combine the row groups: red[g * ms + c], one thread per column
+        if constexpr (ROWS) {
+            if (split != 0xffffffffu) band_combine(sm, wk, split, item.nr, outi, corr, tid);
+        } else {
+            // combine the row groups: red[g * ws + c], one thread per column
             if (col_own) {
-                double* o = sm.red + g * ms + 4 * q;
+                double* o = sm.red + g * ws + 4 * q;
                 o[0] = a0; o[1] = a1; o[2] = a2; o[3] = a3;
             }
             consumers_sync();
-            const bool split = item.w != 0xffffffffu;
-            const uint2 sp = split ? wk.splits[item.w >> 8] : make_uint2(0u, 0u);
-            double* part = split ? wk.scratch + sp.x + static_cast<size_t>(item.w & 0xffu) * ms : nullptr;
-            for (uint32_t c = tid; c < mb; c += kThreads) {
+            double* cpart = split != 0xffffffffu
+                                ? wk.scratch + wk.splits[split >> 8].x + static_cast<size_t>(split & 0xffu) * item.cw
+                                : nullptr;
+            for (uint32_t c = tid; c < item.cw; c += kThreads) {
                 double v = 0.0;
-                for (uint32_t gg = 0; gg < ng; ++gg) v += sm.red[gg * ms + c];
-                if (split) part[c] = v;
+                for (uint32_t gg = 0; gg < ng; ++gg) v += sm.red[gg * ws + c];
+                if (cpart) cpart[c] = v;
                 else corr[outi[c]] = v;
             }
-            if (split) {
-                __threadfence();
-                consumers_sync();
-                if (tid == 0) sm.last = atomicAdd(&wk.counters[item.w >> 8], 1u) == sp.y - 1;
-                consumers_sync();
-                if (sm.last) {
-                    __threadfence();
-                    const double* base = wk.scratch + sp.x;
-                    for (uint32_t c = tid; c < mb; c += kThreads) {
-                        double v = 0.0;
-                        for (uint32_t k = 0; k < sp.y; ++k) v += __ldcg(base + static_cast<size_t>(k) * ms + c);
-                        corr[outi[c]] = v;
-                    }
-                    if (tid == 0) wk.counters[item.w >> 8] = 0u;
-                }
-            }
-            consumers_sync();
+            if (cpart) band_combine(sm, wk, split, item.cw, outi, corr, tid);
+            consumers_sync();  // red is rewritten by the next item
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.vempty[slot]);
@@ -1058,15 +954,16 @@ __global__ void __launch_bounds__(kThreads + 64, 2) lowrank_pass_kernel(const T*
 // Global shift and mid = sum_b exp(h_b - H) part_b over the G CTA partials;
 // which: 0 -> t side, 1 -> s side. One CTA per 32 columns: lane = column,
 // warps split the partials, shared memory combines them.
-__global__ void __launch_bounds__(256) lowrank_reduce_kernel(DevState* __restrict__ st, const double* __restrict__ part,
-                                                             const double* __restrict__ hpart,
-                                                             const double* __restrict__ mnp, int G, int lp,
-                                                             double* __restrict__ mid, int which) {
+__global__ void __launch_bounds__(1024) lowrank_reduce_kernel(DevState* __restrict__ st, const double* __restrict__ part,
+                                                              const double* __restrict__ hpart,
+                                                              const double* __restrict__ mnp, int G, int lp,
+                                                              double* __restrict__ mid, int which) {
     if (st->done) return;
-    __shared__ double sh[8], sm[8], acc_s[8][32];
+    constexpr int W = 32;  // warps
+    __shared__ double sh[W], sm[W], acc_s[W][33];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double H = kNegInf, mn = kPosInf;
-    for (int b = threadIdx.x; b < G; b += 256) {
+    for (int b = threadIdx.x; b < G; b += 1024) {
         H = fmax(H, hpart[b]);
         mn = fmin(mn, mnp[b]);
     }
@@ -1076,19 +973,23 @@ __global__ void __launch_bounds__(256) lowrank_reduce_kernel(DevState* __restric
     __syncthreads();
     H = kNegInf;
     mn = kPosInf;
-    for (int w = 0; w < 8; ++w) { H = fmax(H, sh[w]); mn = fmin(mn, sm[w]); }
+#pragma unroll
+    for (int w = 0; w < W; ++w) { H = fmax(H, sh[w]); mn = fmin(mn, sm[w]); }
     const int a = blockIdx.x * 32 + lane;
     double s = 0.0;
-    if (H != kNegInf && a < lp)
-        for (int b = warp; b < G; b += 8) {
+    if (H != kNegInf && a < lp) {
+#pragma unroll 4
+        for (int b = warp; b < G; b += W) {
             const double hb = hpart[b];
             if (hb != kNegInf) s += part[static_cast<long long>(b) * lp + a] * exp(hb - H);
         }
+    }
     acc_s[warp][lane] = s;
     __syncthreads();
     if (warp == 0 && a < lp) {
         double t = 0.0;
-        for (int w = 0; w < 8; ++w) t += acc_s[w][lane];
+#pragma unroll
+        for (int w = 0; w < W; ++w) t += acc_s[w][lane];
         mid[a] = t;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1206,19 +1107,24 @@ struct Solver {
     std::vector<cudaEvent_t> evs;                           // phase events (profiling)
     size_t mark_base = 0;
     size_t smem = 0;                                        // low-rank pass stage ring
-    // band work: streaming items (buckets with m_b <= kBandVec, split into
-    // row pieces, LPT-assigned to CTAs) and the (bucket, chunk) items of the
-    // oversized buckets
-    struct BandPlan {
-        DevBuf<uint4> items;
-        DevBuf<uint32_t> cta_off, counters;
+    // band work: streaming items (row pieces x column tiles of the buckets),
+    // LPT-assigned to CTAs, with the split tables of both passes
+    struct SplitSet {
         DevBuf<uint2> splits;
+        DevBuf<uint32_t> counters;
         DevBuf<double> scratch;
+    };
+    struct BandPlan {
+        DevBuf<BandItem> items;
+        DevBuf<uint32_t> cta_off;
+        SplitSet pass[2];  // 0 row pass, 1 column pass
         int nitems = 0;
+        BandWork work(int p) {
+            return BandWork{items.get(), cta_off.get(), pass[p].splits.get(), pass[p].counters.get(),
+                            pass[p].scratch.get()};
+        }
     };
     std::vector<BandPlan> plans;
-    std::vector<DevBuf<uint2>> items_rows, items_cols;
-    std::vector<int> n_rows_items, n_cols_items;
     int band_grid = 0;
 
     explicit Solver(Op& o) : op(o), ctx(*o.ctx), s(o.ctx->stream), n(o.n), m(o.m), l(static_cast<int>(o.l)) {
@@ -1269,67 +1175,86 @@ struct Solver {
                                                                   sizeof(BandSmem)));
         band_grid = std::max(occ, 1) * ctx.num_sms;
         const size_t esz = op.fp64 ? 8 : 4;
+        // cost model (bytes): streamed bytes + per-row and per-item overheads
+        auto cost_of = [&](size_t nr, size_t ws) { return double(nr * ws * esz) + 256.0 * nr + 4096.0; };
         for (const Band& B : op.bands) {
             std::vector<uint32_t> w(B.n_work);
-            std::vector<uint2> ir, ic;
             if (B.n_work) B.work.download(w.data(), B.n_work, s);
             ctx.sync();
-            // cost model (bytes): block bytes + per-row and per-item overheads
-            struct Piece { uint32_t b, r0, nr, split; double cost; };
-            auto cost_of = [&](size_t nr, size_t ms) { return double(nr * ms * esz) + 256.0 * nr + 4096.0; };
             double total = 0.0;
             for (uint32_t k : w) {
                 const size_t nb = B.h_src_start[k + 1] - B.h_src_start[k];
                 const size_t mb = B.h_tgt_start[k + 1] - B.h_tgt_start[k];
-                if (mb <= static_cast<size_t>(kBandVec)) total += cost_of(nb, row_stride(mb));
+                if (nb && mb) total += cost_of(nb, row_stride(mb));
             }
             const double cap = std::max(total / band_grid / 2.0, 65536.0);
+            struct Piece { BandItem it; double cost; };
             std::vector<Piece> pieces;
-            std::vector<uint2> splits;
-            size_t scratch = 0;
+            std::vector<uint2> splits[2];
+            size_t scratch[2] = {0, 0};
             for (uint32_t k : w) {
                 const size_t nb = B.h_src_start[k + 1] - B.h_src_start[k];
                 const size_t mb = B.h_tgt_start[k + 1] - B.h_tgt_start[k];
-                const size_t ms = row_stride(mb);
                 if (nb == 0 || mb == 0) continue;
-                if (mb > static_cast<size_t>(kBandVec)) {
-                    for (size_t c = 0; c * kItemRows < nb; ++c) ir.push_back(make_uint2(k, static_cast<uint32_t>(c)));
-                    for (size_t c = 0; c * 256 < ms; ++c) ic.push_back(make_uint2(k, static_cast<uint32_t>(c)));
-                    continue;
-                }
-                size_t K = static_cast<size_t>(std::ceil(cost_of(nb, ms) / cap));
+                const size_t ms = row_stride(mb);
+                const size_t nct = ceil_div(mb, kBandVec);  // column tiles
+                const size_t wmax = std::min<size_t>(ms, kBandVec);
+                // row pieces: multiple of 8 rows (128-byte aligned chunk starts), <= kBandVec
+                size_t K = static_cast<size_t>(std::ceil(cost_of(nb, wmax) / cap));
                 K = std::max<size_t>(K, ceil_div(nb, kBandVec));
-                // piece rows: multiple of 8 (128-byte aligned chunk starts), <= kBandVec
                 size_t pr = (ceil_div(nb, std::max<size_t>(K, 1)) + 7) & ~size_t(7);
                 pr = std::min<size_t>(std::max<size_t>(pr, 8), kBandVec);
                 K = ceil_div(nb, pr);
-                if (K > 255) throw Status(2, "lcn: bucket split into more than 255 pieces");
-                uint32_t sid = 0xffffffffu;
-                if (K > 1) {
-                    sid = static_cast<uint32_t>(splits.size());
-                    splits.push_back(make_uint2(static_cast<uint32_t>(scratch), static_cast<uint32_t>(K)));
-                    scratch += K * ms;
-                }
-                for (size_t j = 0; j < K; ++j) {
-                    const size_t r0 = j * pr, nr = std::min(pr, nb - r0);
-                    pieces.push_back({k, static_cast<uint32_t>(r0), static_cast<uint32_t>(nr),
-                                      K > 1 ? (sid << 8) | static_cast<uint32_t>(j) : 0xffffffffu, cost_of(nr, ms)});
+                if (K > 255 || nct > 255) throw Status(2, "lcn: bucket split into more than 255 pieces");
+                // row-pass splits: one per row piece when there are several column tiles
+                std::vector<uint32_t> rsid(K, 0xffffffffu), csid(nct, 0xffffffffu);
+                if (nct > 1)
+                    for (size_t j = 0; j < K; ++j) {
+                        const size_t nr = std::min(pr, nb - j * pr);
+                        rsid[j] = static_cast<uint32_t>(splits[0].size());
+                        splits[0].push_back(make_uint2(static_cast<uint32_t>(scratch[0]), static_cast<uint32_t>(nct)));
+                        scratch[0] += nct * nr;
+                    }
+                // column-pass splits: one per column tile when there are several row pieces
+                if (K > 1)
+                    for (size_t ct = 0; ct < nct; ++ct) {
+                        const size_t cw = std::min<size_t>(kBandVec, mb - ct * kBandVec);
+                        csid[ct] = static_cast<uint32_t>(splits[1].size());
+                        splits[1].push_back(make_uint2(static_cast<uint32_t>(scratch[1]), static_cast<uint32_t>(K)));
+                        scratch[1] += K * cw;
+                    }
+                for (size_t ct = 0; ct < nct; ++ct) {
+                    const size_t c0 = ct * kBandVec, cw = std::min<size_t>(kBandVec, mb - c0);
+                    for (size_t j = 0; j < K; ++j) {
+                        const size_t r0 = j * pr, nr = std::min(pr, nb - r0);
+                        BandItem it{};
+                        it.b = k;
+                        it.r0 = static_cast<uint32_t>(r0);
+                        it.nr = static_cast<uint32_t>(nr);
+                        it.c0 = static_cast<uint32_t>(c0);
+                        it.cw = static_cast<uint32_t>(cw);
+                        it.split[0] = nct > 1 ? (rsid[j] << 8) | static_cast<uint32_t>(ct) : 0xffffffffu;
+                        it.split[1] = K > 1 ? (csid[ct] << 8) | static_cast<uint32_t>(j) : 0xffffffffu;
+                        pieces.push_back({it, cost_of(nr, row_stride(cw))});
+                    }
                 }
             }
+            if (scratch[0] > 0xffffffffull || scratch[1] > 0xffffffffull)
+                throw Status(2, "lcn: band split scratch above 2^32 entries");
             // longest-processing-time greedy: largest piece to the least loaded CTA
             std::stable_sort(pieces.begin(), pieces.end(), [](const Piece& x, const Piece& y) { return x.cost > y.cost; });
             using Load = std::pair<double, int>;
             std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
             for (int c = 0; c < band_grid; ++c) heap.push({0.0, c});
-            std::vector<std::vector<uint4>> per(band_grid);
+            std::vector<std::vector<BandItem>> per(band_grid);
             for (const Piece& pc : pieces) {
                 Load ld = heap.top();
                 heap.pop();
-                per[ld.second].push_back(make_uint4(pc.b, pc.r0, pc.nr, pc.split));
+                per[ld.second].push_back(pc.it);
                 ld.first += pc.cost;
                 heap.push(ld);
             }
-            std::vector<uint4> items;
+            std::vector<BandItem> items;
             std::vector<uint32_t> off(band_grid + 1, 0);
             for (int c = 0; c < band_grid; ++c) {
                 off[c] = static_cast<uint32_t>(items.size());
@@ -1340,21 +1265,16 @@ struct Solver {
             P.nitems = static_cast<int>(items.size());
             P.items.resize(std::max<size_t>(items.size(), 1));
             P.cta_off.resize(off.size());
-            P.splits.resize(std::max<size_t>(splits.size(), 1));
-            P.counters.resize(std::max<size_t>(splits.size(), 1));
-            P.scratch.resize(std::max<size_t>(scratch, 1));
             if (!items.empty()) P.items.upload(items.data(), items.size(), s);
             P.cta_off.upload(off.data(), off.size(), s);
-            if (!splits.empty()) P.splits.upload(splits.data(), splits.size(), s);
-            P.counters.zero(s);
+            for (int p = 0; p < 2; ++p) {
+                P.pass[p].splits.resize(std::max<size_t>(splits[p].size(), 1));
+                P.pass[p].counters.resize(std::max<size_t>(splits[p].size(), 1));
+                P.pass[p].scratch.resize(std::max<size_t>(scratch[p], 1));
+                if (!splits[p].empty()) P.pass[p].splits.upload(splits[p].data(), splits[p].size(), s);
+                P.pass[p].counters.zero(s);
+            }
             plans.push_back(std::move(P));
-            DevBuf<uint2> r(std::max<size_t>(ir.size(), 1)), c(std::max<size_t>(ic.size(), 1));
-            if (!ir.empty()) r.upload(ir.data(), ir.size(), s);
-            if (!ic.empty()) c.upload(ic.data(), ic.size(), s);
-            n_rows_items.push_back(static_cast<int>(ir.size()));
-            n_cols_items.push_back(static_cast<int>(ic.size()));
-            items_rows.push_back(std::move(r));
-            items_cols.push_back(std::move(c));
         }
         ctx.sync();
     }
@@ -1448,7 +1368,7 @@ struct Solver {
         return a;
     }
     void reduce(double* mid, int which) {
-        lowrank_reduce_kernel<<<ceil_div(lp, 32), 256, 0, s>>>(st.get(), part.get(), hpart.get(), mnp.get(), G, lp,
+        lowrank_reduce_kernel<<<ceil_div(lp, 32), 1024, 0, s>>>(st.get(), part.get(), hpart.get(), mnp.get(), G, lp,
                                                                mid, which);
     }
 
@@ -1492,30 +1412,21 @@ struct Solver {
     }
 
     // -------- lcn / nystrom ------------------------------------------------
-    // logv: natural-order log vector (oversized-bucket kernels gather from it);
-    // logvp[b]: band b's bucket-ordered copy (streaming kernels bulk-copy it).
+    // logvp[b]: band b's bucket-ordered copy of the log vector (written by the
+    // low-rank pass that produced it, or by scatter_perm).
     template <typename T, bool ROWS>
-    void bands(const double* logv, std::vector<DevBuf<double>>& logvp, std::vector<DevBuf<double>>& corr) {
+    void bands(std::vector<DevBuf<double>>& logvp, std::vector<DevBuf<double>>& corr) {
         if (op.kind != 3) return;
-        for (size_t b = 0; b < op.bands.size(); ++b) {
-            if (plans[b].nitems) {
-                BandPlan& P = plans[b];
-                const BandWork wk{P.items.get(), P.cta_off.get(), P.splits.get(), P.counters.get(), P.scratch.get()};
+        for (size_t b = 0; b < op.bands.size(); ++b)
+            if (plans[b].nitems)
                 band_stream_kernel<T, ROWS><<<band_grid, kThreads + 64, sizeof(BandSmem), s>>>(
-                    st.get(), op.view(b), wk, band_vals<T>(b), logvp[b].get(), corr[b].get());
-            }
-            if (ROWS && n_rows_items[b])
-                lcn_row_band_kernel<T><<<n_rows_items[b], kThreads, 0, s>>>(st.get(), op.view(b), items_rows[b].get(),
-                                                                          band_vals<T>(b), logv, corr[b].get());
-            if (!ROWS && n_cols_items[b])
-                lcn_col_band_kernel<T><<<n_cols_items[b], kThreads, 0, s>>>(st.get(), op.view(b), items_cols[b].get(),
-                                                                          band_vals<T>(b), logv, corr[b].get());
-        }
+                    st.get(), op.view(b), plans[b].work(ROWS ? 0 : 1), band_vals<T>(b), logvp[b].get(),
+                    corr[b].get());
     }
     template <typename T>
-    void lcn_rows(const double* lt) { bands<T, true>(lt, ltp, corr_s); }
+    void lcn_rows() { bands<T, true>(ltp, corr_s); }
     template <typename T>
-    void lcn_cols(const double* ls, int parity) { bands<T, false>(ls, lsp[parity], corr_t); }
+    void lcn_cols(int parity) { bands<T, false>(lsp[parity], corr_t); }
     void set_perm(PassArgs& a, int side, int parity) {
         a.nperm = 0;
         if (op.kind != 3) return;
@@ -1550,7 +1461,7 @@ struct Solver {
             pass<T, 1>(a);
             mark(it, 1);
         } else {
-            lcn_cols<T>(log_s[cur].get(), cur);
+            lcn_cols<T>(cur);
             mark(it, 1);
             PassArgs a = base_args();
             a.rows = m;
@@ -1564,7 +1475,7 @@ struct Solver {
         }
         reduce(mid_t.get(), 0);
         mark(it, 2);
-        lcn_rows<T>(log_t.get());
+        lcn_rows<T>();
         mark(it, 3);
         PassArgs a = base_args();
         a.rows = n;
@@ -1714,7 +1625,7 @@ struct Solver {
                 pass<T, 1>(acc);
                 reduce(mid_t.get(), 0);
                 scatter_perm(vin.get(), m, 1, 0);
-                lcn_rows<T>(vin.get());
+                lcn_rows<T>();
                 mv.rows = n;
                 mv.mid = mid_t.get();
                 set_corr(mv, 0);
@@ -1724,7 +1635,7 @@ struct Solver {
                 pass<T, 0>(acc);
                 reduce(mid_s.get(), 1);
                 scatter_perm(vin.get(), n, 0, 0);
-                lcn_cols<T>(vin.get(), 0);
+                lcn_cols<T>(0);
                 mv.rows = m;
                 mv.mid = mid_s.get();
                 set_corr(mv, 1);

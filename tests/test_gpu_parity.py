@@ -123,3 +123,31 @@ def test_lcn_small_configs(ref, scale, which):
     assert rel(res.distance, rres.distance) <= REL_FP32
     assert rel(res.sp_vals, rres.sp_vals) <= REL_FP32
     assert rel(lcn.distance_lcn(res, op), rres.distance_lcn()) <= REL_FP32
+
+
+@pytest.mark.parametrize("fp64", [False, True])
+def test_lcn_wide_and_split_buckets(ref, fp64):
+    """Two buckets of ~2000 x 2000: the band kernels cut them into <= 1024
+    column tiles and several row pieces, so both split-output combines (row
+    sums over column tiles, column sums over row pieces) run."""
+    import dataclasses
+    pr = dataclasses.replace(configs.config3(0.004), bands=1, buckets=2, landmarks=32, iters=30)
+    c = lcn.Context(0, store_fp64=fp64)
+    cfg = lcn.LshConfig(pr.bands, 1, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
+    op = lcn.KernelOperator.lcn_lsh(c, pr.p, pr.q, pr.cost, pr.lam_eff, cfg, pr.landmarks, lcn.LANDMARK_KMEANS,
+                                    pr.landmark_seed)
+    ids = lcn.lsh_kmeans_buckets(c, pr.p, pr.q, cfg)
+    sizes = np.bincount(ids[0, pr.n:].astype(np.int64))
+    assert sizes.max() > 1024
+    pairs = ref.lsh_pairs(pr.p, pr.q, pr.bands, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
+    rop = ref.op_lcn(pr.p, pr.q, pr.cost, pr.lam_eff, pairs, pr.landmarks, 0, pr.landmark_seed)
+    pm, qm = pr.marginals()
+    res = lcn.sinkhorn(op, pm, qm, lcn.SinkhornOptions(tol=0.0, max_iters=pr.iters))
+    rres = rop.sinkhorn(pm, qm, tol=0.0, max_iters=pr.iters)
+    tol = REL_FP64 if fp64 else REL_FP32
+    assert rel(res.distance, rres.distance) <= tol
+    assert rel(res.sp_vals, rres.sp_vals) <= tol
+    # repeat: split combines are order-fixed, results bit-identical run to run
+    res2 = lcn.sinkhorn(op, pm, qm, lcn.SinkhornOptions(tol=0.0, max_iters=pr.iters))
+    assert res2.distance == res.distance
+    assert np.array_equal(res2.sp_vals, res.sp_vals)
