@@ -39,7 +39,12 @@ PhaseTimer::~PhaseTimer() {
     if (on) {
         cudaStreamSynchronize(ctx.stream);
         double t1 = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
-        std::fprintf(stderr, "[lcn timing] %-36s %10.2f ms\n", name, t1 - t0);
+        std::fprintf(stderr, "[lcn timing] %-36s %10.2f ms", name, t1 - t0);
+        if (ctx.filter_points)
+            std::fprintf(stderr, "   (assign filter: %lld of %lld points to the exact scan)", ctx.filter_ambiguous,
+                         ctx.filter_points);
+        std::fprintf(stderr, "\n");
+        ctx.filter_points = ctx.filter_ambiguous = 0;
     }
 }
 

@@ -231,13 +231,31 @@ int lcn_kmeans_pp_indices(lcn_ctx* ctx, const double* points, size_t n, size_t d
     });
 }
 
+// fp32 copy of host points when every coordinate is fp32-representable (the
+// k-means kernels then read 4-byte points; distances are the same fp64 folds)
+static bool fp32_copy(const double* p, size_t count, std::vector<float>& f) {
+    f.resize(count);
+    for (size_t i = 0; i < count; ++i)
+        if (static_cast<double>(f[i] = static_cast<float>(p[i])) != p[i]) return false;
+    return true;
+}
+
 int lcn_assign_nearest(lcn_ctx* ctx, const double* points, size_t n, size_t d, const double* centroids, size_t k,
                        uint32_t* out) {
     return guard(ctx, [&] {
         DevBuf<double> X, C;
         DevBuf<uint32_t> a(std::max<size_t>(n, 1));
-        X.upload(points, n * d, ctx->c.stream);
         C.upload(centroids, k * d, ctx->c.stream);
+        std::vector<float> f;
+        if (fp32_copy(points, n * d, f)) {
+            DevBuf<float> X32;
+            X32.upload(f.data(), f.size(), ctx->c.stream);
+            assign_device<float>(ctx->c, X32.get(), n, static_cast<int>(d), C.get(), static_cast<int>(k), a.get());
+            a.download(out, n, ctx->c.stream);
+            ctx->c.sync();
+            return;
+        }
+        X.upload(points, n * d, ctx->c.stream);
         assign_device<double>(ctx->c, X.get(), n, static_cast<int>(d), C.get(), static_cast<int>(k), a.get());
         a.download(out, n, ctx->c.stream);
         ctx->c.sync();
@@ -250,9 +268,18 @@ int lcn_lloyd(lcn_ctx* ctx, const double* points, size_t n, size_t d, size_t k, 
         if (n == 0) throw Status(2, "k-means on empty input");
         if (k == 0 || k > n) throw Status(2, "k-means: more buckets than points");
         DevBuf<double> X, C(k * d);
+        DevBuf<float> X32;
         DevBuf<uint32_t> a(n);
-        X.upload(points, n * d, ctx->c.stream);
-        lloyd_device<double>(ctx->c, X.get(), n, static_cast<int>(d), static_cast<int>(k), iters, seed, C.get(), a.get());
+        std::vector<float> f;
+        if (fp32_copy(points, n * d, f)) {
+            X32.upload(f.data(), f.size(), ctx->c.stream);
+            lloyd_device<float>(ctx->c, X32.get(), n, static_cast<int>(d), static_cast<int>(k), iters, seed, C.get(),
+                                a.get());
+        } else {
+            X.upload(points, n * d, ctx->c.stream);
+            lloyd_device<double>(ctx->c, X.get(), n, static_cast<int>(d), static_cast<int>(k), iters, seed, C.get(),
+                                 a.get());
+        }
         C.download(centroids_out, k * d, ctx->c.stream);
         a.download(assign_out, n, ctx->c.stream);
         ctx->c.sync();

@@ -67,6 +67,8 @@ struct Ctx {
     cudaStream_t own_stream = nullptr;
     int profile = 0;
     std::string last_error;
+    // k-means assignment filter statistics (points filtered / sent to the exact scan)
+    long long filter_points = 0, filter_ambiguous = 0;
     void activate() const { CUDA_OK(cudaSetDevice(device)); }
     void sync() const { CUDA_OK(cudaStreamSynchronize(stream)); }
 };

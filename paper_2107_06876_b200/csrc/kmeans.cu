@@ -15,9 +15,11 @@
 #include <cub/cub.cuh>
 
 #include <random>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
+#include "async.cuh"
 #include "ctx.cuh"
 #include "kmeans.cuh"
 #include "tiles.cuh"
@@ -25,10 +27,13 @@
 namespace lcnb {
 
 // ---- assign_nearest (kmeans.cpp:67-85) -------------------------------------
+// rows != null: evaluate only the points rows[0 .. N) (the filter's
+// ambiguous list) and write out[rows[i]].
 template <typename T>
 __global__ void __launch_bounds__(256) assign_exact_kernel(const T* __restrict__ X, long long N, int d,
                                                            const double* __restrict__ Cm, int k,
-                                                           uint32_t* __restrict__ out, double* __restrict__ best_out) {
+                                                           uint32_t* __restrict__ out, double* __restrict__ best_out,
+                                                           const uint32_t* __restrict__ rows) {
     __shared__ double As[KC][TP + 1];
     __shared__ double Bs[KC][TC + 1];
     const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
@@ -44,7 +49,7 @@ __global__ void __launch_bounds__(256) assign_exact_kernel(const T* __restrict__
 #pragma unroll
             for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
         for (int k0 = 0; k0 < d; k0 += KC) {
-            load_slab<T>(As, X, nullptr, p0, N, d, k0);
+            load_slab<T>(As, X, rows, p0, N, d, k0);
             load_slab<double>(Bs, Cm, nullptr, c0, k, d, k0);
             __syncthreads();
             tile_fold<0>(As, Bs, ty, tx, acc);
@@ -72,8 +77,9 @@ __global__ void __launch_bounds__(256) assign_exact_kernel(const T* __restrict__
         }
         long long p = p0 + ty + 16 * i;
         if (tx == 0 && p < N) {
-            out[p] = static_cast<uint32_t>(a);
-            if (best_out) best_out[p] = b;
+            const long long q = rows ? rows[p] : p;
+            out[q] = static_cast<uint32_t>(a);
+            if (best_out) best_out[q] = b;
         }
     }
 }
@@ -123,14 +129,67 @@ struct FoldResult {
 
 constexpr double kMinNormal = 2.2250738585072014e-308;
 constexpr long long kTwo53 = 1LL << 53;
+constexpr long long kTwo52 = 1LL << 52;
 
-__device__ FoldResult warp_exact_fold(const double* __restrict__ x, long long begin, long long end, double s,
-                                      bool search, double target) {
+// IEEE-754 bit access for positive normal doubles (exact, no libm calls):
+// binade exponent, 53-bit integer significand, and the inverse.
+__device__ __forceinline__ int dbl_exp(double s) {
+    return static_cast<int>((__double_as_longlong(s) >> 52) & 0x7ff) - 1023;
+}
+__device__ __forceinline__ long long dbl_sig(double s) {
+    return (__double_as_longlong(s) & (kTwo52 - 1)) | kTwo52;
+}
+__device__ __forceinline__ double dbl_make(long long sig, int e) {  // sig in [2^52, 2^53)
+    return __longlong_as_double((static_cast<long long>(e + 1023) << 52) | (sig - kTwo52));
+}
+// x * 2^(52 - e), correctly rounded like scalbn (a product with an exact
+// power of two); scalbn itself when the power is not representable
+__device__ __forceinline__ double scale_to_grid(double x, int e) {
+    const int k = 52 - e;
+    if (k <= 1023 && k >= -1022) return x * __longlong_as_double(static_cast<long long>(k + 1023) << 52);
+    return scalbn(x, k);
+}
+
+// Effect of a run of additions on the integer significand S (grid u of one
+// binade): an element x = u (K + f) adds K, or K + 1 when f > 1/2; an exact
+// tie f = 1/2 rounds to even, adding K + ((S + K) & 1). So a run maps S to
+// S + inc[S & 1]; runs compose associatively:
+//   (f then g).inc[p] = f.inc[p] + g.inc[(p + f.inc[p]) & 1].
+struct ParInc {
+    long long i0, i1;
+};
+__device__ __forceinline__ ParInc par_compose(ParInc f, ParInc g) {
+    return {f.i0 + ((f.i0 & 1) ? g.i1 : g.i0), f.i1 + (((1 + f.i1) & 1) ? g.i1 : g.i0)};
+}
+// element x scaled to the grid (q = x / u, 0 <= q < 2^53)
+__device__ __forceinline__ ParInc par_element(double q) {
+    const double K = floor(q), f = q - K;
+    const long long k = static_cast<long long>(K);
+    if (f == 0.5) return {k + (k & 1), k + ((k + 1) & 1)};
+    const long long r = k + (f > 0.5 ? 1 : 0);
+    return {r, r};
+}
+__device__ __forceinline__ ParInc par_shfl_up(ParInc v, int o) {
+    return {__shfl_up_sync(0xffffffffu, v.i0, o), __shfl_up_sync(0xffffffffu, v.i1, o)};
+}
+// inclusive warp scan of ParInc in lane order (identity {0, 0})
+__device__ __forceinline__ ParInc par_scan(ParInc v, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const ParInc t = par_shfl_up(v, o);
+        if (lane >= o) v = par_compose(t, v);
+    }
+    return v;
+}
+
+// x[begin .. end) may be a shared-memory copy: xs points at element `begin`.
+__device__ FoldResult warp_exact_fold(const double* xs, long long begin, long long end, double s, bool search,
+                                      double target) {
     const int lane = threadIdx.x & 31;
     long long pick = -1;
     for (long long base = begin; base < end; base += 32) {
         const int cnt = static_cast<int>(min(32LL, end - base));
-        const double v = lane < cnt ? x[base + lane] : 0.0;
+        const double v = lane < cnt ? xs[base - begin + lane] : 0.0;
         int a = 0;
         while (a < cnt) {
             if (!(s >= kMinNormal && s < kPosInf)) {  // zero / subnormal / inf: real add
@@ -140,37 +199,25 @@ __device__ FoldResult warp_exact_fold(const double* __restrict__ x, long long be
                 ++a;
                 continue;
             }
-            const int e = ilogb(s);
-            const long long S = static_cast<long long>(scalbn(s, 52 - e));
+            const int e = dbl_exp(s);
+            const long long S = dbl_sig(s);
             const bool mine = lane >= a && lane < cnt;
-            double q = mine ? scalbn(v, 52 - e) : 0.0;
-            const bool big = !(q < 9007199254740992.0);
-            long long r = 0;
-            bool tie = false;
-            if (mine && !big) {
-                double K = floor(q), f = q - K;
-                r = static_cast<long long>(K) + (f > 0.5 ? 1 : 0);
-                tie = (f == 0.5);
-            } else if (big) {
-                r = kTwo53;
-            }
-            long long P = r;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                long long t = __shfl_up_sync(0xffffffffu, P, o);
-                if (lane >= o) P += t;
-            }
-            const bool bad = mine && (big || tie || S + P >= kTwo53);
+            const double q = mine ? scale_to_grid(v, e) : 0.0;
+            const bool big = mine && !(q < 9007199254740992.0);
+            const ParInc pf = par_scan((mine && !big) ? par_element(q) : ParInc{0, 0}, lane);
+            const long long P = (S & 1) ? pf.i1 : pf.i0;
+            // leave the fast path at a huge element or where the sum reaches 2^(e+1)
+            const bool bad = mine && (big || S + P >= kTwo53);
             const unsigned bm = __ballot_sync(0xffffffffu, bad);
             const int fb = bm ? __ffs(bm) - 1 : cnt;
             if (search && pick < 0) {
                 bool hit = false;
-                if (lane >= a && lane < fb) hit = scalbn(static_cast<double>(S + P), e - 52) >= target && v > 0.0;
+                if (lane >= a && lane < fb) hit = dbl_make(S + P, e) >= target && v > 0.0;
                 const unsigned hm = __ballot_sync(0xffffffffu, hit);
                 if (hm) pick = base + __ffs(hm) - 1;
             }
             const long long Pacc = fb > a ? __shfl_sync(0xffffffffu, P, fb - 1) : 0;
-            s = scalbn(static_cast<double>(S + Pacc), e - 52);
+            s = dbl_make(S + Pacc, e);
             if (fb < cnt) {
                 double vb = __shfl_sync(0xffffffffu, v, fb);
                 s = xadd(s, vb);
@@ -192,10 +239,12 @@ __device__ FoldResult warp_exact_fold(const double* __restrict__ x, long long be
 //   A) approximate chunk sums (any order)            -> predicted start A_c
 //   B) predicted binade e_c of each chunk (dirty if the interval
 //      [A_c (1-1e-9), A_{c+1} (1+1e-9)] straddles a power of two)
-//   C) integer rounding sums R_c(e_c) in parallel, dirty on ties / huge x
-//   D) one warp walks the chunks in order with the exact running sum: a clean
-//      chunk whose actual binade matches e_c advances by u * R_c exactly,
-//      any other chunk is folded element-wise by warp_exact_fold.
+//   C) the chunk's parity function R_c(e_c) = {inc[0], inc[1]} in parallel
+//      (ties included), dirty only on huge x
+//   D) one warp walks the chunks in order with the exact running sum: runs
+//      of clean chunks whose actual binade matches e_c advance by a
+//      parity-scan of their R_c, any other chunk is folded element-wise by
+//      warp_exact_fold.
 // The prediction only decides which path a chunk takes; the walk re-checks
 // the actual binade, so the result is exact regardless.
 constexpr int kFoldChunk = 2048;
@@ -241,70 +290,104 @@ __global__ void fold_plan_kernel(const double* __restrict__ csum, int nch, int* 
     }
 }
 
-__global__ void fold_round_kernel(const double* __restrict__ x, long long N, const int* __restrict__ ebin,
-                                  long long* __restrict__ R) {
-    __shared__ long long red[8];
+__global__ void __launch_bounds__(256) fold_round_kernel(const double* __restrict__ x, long long N,
+                                                         const int* __restrict__ ebin, longlong2* __restrict__ R) {
+    constexpr int kPer = kFoldChunk / 256;  // contiguous elements per thread, in order
+    __shared__ ParInc wred[8];
     __shared__ int bad_any;
     const int e = ebin[blockIdx.x];
     if (e == -100000) {
-        if (threadIdx.x == 0) R[blockIdx.x] = -1;
+        if (threadIdx.x == 0) R[blockIdx.x] = make_longlong2(-1, -1);
         return;
     }
     if (threadIdx.x == 0) bad_any = 0;
     __syncthreads();
-    const long long b = static_cast<long long>(blockIdx.x) * kFoldChunk;
-    const long long en = min(N, b + kFoldChunk);
-    long long r = 0;
+    const long long b = static_cast<long long>(blockIdx.x) * kFoldChunk + threadIdx.x * kPer;
+    ParInc acc{0, 0};
     bool bad = false;
-    for (long long i = b + threadIdx.x; i < en; i += blockDim.x) {
-        double q = scalbn(x[i], 52 - e);
-        if (!(q < 9007199254740992.0)) { bad = true; continue; }
-        double K = floor(q), f = q - K;
-        if (f == 0.5) bad = true;
-        r += static_cast<long long>(K) + (f > 0.5 ? 1 : 0);
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        const long long i = b + j;
+        if (i < N) {
+            const double q = scale_to_grid(x[i], e);
+            if (!(q < 9007199254740992.0)) bad = true;
+            else acc = par_compose(acc, par_element(q));
+        }
     }
     if (bad) bad_any = 1;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = r;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    acc = par_scan(acc, lane);
+    if (lane == 31) wred[warp] = acc;
     __syncthreads();
     if (threadIdx.x == 0) {
-        long long t = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-        R[blockIdx.x] = bad_any ? -1 : t;
+        ParInc t{0, 0};
+        for (int w = 0; w < 8; ++w) t = par_compose(t, wred[w]);
+        R[blockIdx.x] = bad_any ? make_longlong2(-1, -1) : make_longlong2(t.i0, t.i1);
     }
+}
+
+// Exact fold of chunk c by one warp from a shared-memory copy: all of the
+// chunk's loads are issued at once (one memory latency per chunk instead of
+// one per 32 elements).
+__device__ __forceinline__ FoldResult fold_chunk_staged(const double* __restrict__ x, long long N, int c, double s,
+                                                        bool search, double target, double* buf) {
+    const int lane = threadIdx.x & 31;
+    const long long b = static_cast<long long>(c) * kFoldChunk;
+    const long long e = min(N, b + kFoldChunk);
+    __syncwarp();
+#pragma unroll 16
+    for (int j = lane; j < kFoldChunk; j += 32) buf[j] = b + j < e ? x[b + j] : 0.0;
+    __syncwarp();
+    return warp_exact_fold(buf, b, e, s, search, target);
 }
 
 // D) walk + draw + pick for k-means++ step t (kmeans.cpp:35-62). raw[] holds
 // the caller's engine draws in order; a step with total <= 0 consumes none
 // (kmeans.cpp:42-47).
 __global__ void pp_walk_pick_kernel(double* __restrict__ dist2, unsigned char* __restrict__ used, long long N, int nch,
-                                    const int* __restrict__ ebin, const long long* __restrict__ R,
+                                    const int* __restrict__ ebin, const longlong2* __restrict__ R,
                                     double* __restrict__ sstart, const unsigned long long* __restrict__ raw, int n_raw,
                                     int* __restrict__ draw_counter, uint32_t* __restrict__ chosen, int t) {
+    __shared__ double buf[kFoldChunk];
     const int lane = threadIdx.x;
     double S = 0.0;
+    // 32 chunks per step: a run of clean chunks in the running sum's binade
+    // advances by an exact int64 prefix sum of their R_c; the walk goes
+    // element-wise only where the run breaks (binade change, dirty chunk).
     for (int cb = 0; cb < nch; cb += 32) {
         const int c_l = cb + lane;
         const int e_l = c_l < nch ? ebin[c_l] : 0;
-        const long long r_l = c_l < nch ? R[c_l] : -1;
+        const longlong2 r2 = c_l < nch ? R[c_l] : make_longlong2(-1, -1);
+        const ParInc r_l{r2.x, r2.y};
         const int cnt = min(32, nch - cb);
-        for (int k = 0; k < cnt; ++k) {
-            const int c = cb + k;
-            if (lane == 0) sstart[c] = S;
-            const int e = __shfl_sync(0xffffffffu, e_l, k);
-            const long long Rc = __shfl_sync(0xffffffffu, r_l, k);
-            bool fast = Rc >= 0 && S >= kMinNormal && S < kPosInf && ilogb(S) == e;
-            long long Si = 0;
-            if (fast) {
-                Si = static_cast<long long>(scalbn(S, 52 - e));
-                fast = Si + Rc < kTwo53;
-            }
-            if (fast) {
-                S = scalbn(static_cast<double>(Si + Rc), e - 52);
-            } else {
+        int k = 0;
+        while (k < cnt) {
+            const bool normal = S >= kMinNormal && S < kPosInf;
+            const int eS = normal ? dbl_exp(S) : -100001;
+            const long long Si = normal ? dbl_sig(S) : 0;
+            const bool in = lane >= k && lane < cnt;
+            const bool ok = in && normal && e_l == eS && r_l.i0 >= 0;
+            const unsigned notok = __ballot_sync(0xffffffffu, in && !ok);
+            int fb = notok ? __ffs(notok) - 1 : cnt;
+            const bool run = lane >= k && lane < fb;
+            const ParInc pf = par_scan(run ? r_l : ParInc{0, 0}, lane);
+            const long long P = (Si & 1) ? pf.i1 : pf.i0;
+            // a chunk whose end leaves the binade is folded element-wise
+            const unsigned cross = __ballot_sync(0xffffffffu, run && Si + P >= kTwo53);
+            if (cross) fb = min(fb, __ffs(cross) - 1);
+            // exclusive prefix = inclusive prefix of the previous lane
+            const long long Pprev = __shfl_up_sync(0xffffffffu, P, 1);
+            const long long Pex = lane > k ? Pprev : 0;
+            if (lane >= k && lane < fb) sstart[c_l] = dbl_make(Si + Pex, eS);
+            if (fb > k) S = dbl_make(Si + __shfl_sync(0xffffffffu, P, fb - 1), eS);
+            if (fb < cnt) {
+                const int c = cb + fb;
+                if (lane == 0) sstart[c] = S;
                 const long long b = static_cast<long long>(c) * kFoldChunk;
-                S = warp_exact_fold(dist2, b, min(N, b + kFoldChunk), S, false, 0.0).s;
+                S = fold_chunk_staged(dist2, N, c, S, false, 0.0, buf).s;
+                k = fb + 1;
+            } else {
+                k = cnt;
             }
         }
     }
@@ -335,8 +418,14 @@ __global__ void pp_walk_pick_kernel(double* __restrict__ dist2, unsigned char* _
         }
         pick = -1;
         if (cstar < nch) {
-            FoldResult sr = warp_exact_fold(dist2, static_cast<long long>(cstar) * kFoldChunk, N, sstart[cstar], true, target);
-            pick = sr.pick;
+            // the running sum reaches the target inside chunk cstar (an element
+            // that raises it is > 0); later chunks only as a guard
+            double sc = sstart[cstar];
+            for (int c = cstar; c < nch && pick < 0; ++c) {
+                const FoldResult sr = fold_chunk_staged(dist2, N, c, sc, true, target, buf);
+                pick = sr.pick;
+                sc = sr.s;
+            }
         }
         if (pick < 0) pick = N - 1;
         if (lane == 0) *draw_counter = di + 1;
@@ -363,7 +452,7 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     const int nch = ceil_div(N, kFoldChunk);
     DevBuf<double> dist2(N), csum(nch), sstart(nch + 1);
     DevBuf<int> ebin(nch);
-    DevBuf<long long> R(nch);
+    DevBuf<longlong2> R(nch);
     DevBuf<unsigned char> used(N);
     DevBuf<unsigned long long> d_raw(raw.size() ? raw.size() : 1);
     DevBuf<int> counter(1);
@@ -476,10 +565,213 @@ __global__ void reseed_apply_kernel(const T* __restrict__ X, int d, const double
     for (int kk = threadIdx.x; kk < d; kk += blockDim.x) ctr[static_cast<long long>(c) * d + kk] = static_cast<double>(X[arg * d + kk]);
 }
 
+
+// ---- fast assignment: fp32 filter + exact fallback -------------------------
+// For fp32 points with d <= kFD the argmin is first located with fp32 FMA
+// tiles: v(c) = |c_f|^2 - 2 x.c_f (c_f = fp32(c)), so that the exact fold
+// D(c) = |x|^2 + v(c) + err(c) with |err(c)| <= E(x) for every centroid
+// (rigorous bound below). If the best and second-best v differ by more than
+// 2 E(x), the best centroid is the exact argmin (no other centroid can tie or
+// win); otherwise the point goes to the ambiguous list and gets the full
+// exact fp64 scan with lowest-index ties. Results are identical to the exact
+// kernel; the filter only skips work that cannot change them.
+constexpr int kFB = 128;  // points per CTA = centroids per tile
+constexpr int kFD = 128;  // max dimension of the filter path
+
+struct FilterSmem {
+    float A[kFD][kFB];     // point tile, feature-major
+    float B[2][kFD][kFB];  // centroid tiles (double-buffered), feature-major
+    float nc[2][kFB];      // |c_f|^2 rounded to fp32 (+inf for padding)
+    double xn[kFB];        // |x|^2 (fp64)
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int NG>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(NG) : "memory"); }
+
+// CfT[kk][c] = fp32(C[c][kk]) for c < k, 0 for padding; ncf[c] = fp32(sum c_f^2)
+// (+inf for padding); cmax = max_c max(|c|^2, |c_f|^2) as fp64 bits.
+__global__ void __launch_bounds__(128) filter_prep_kernel(const double* __restrict__ C, int k, int d, int Kp,
+                                                          float* __restrict__ CfT, float* __restrict__ ncf,
+                                                          unsigned long long* __restrict__ cmax) {
+    __shared__ double r1[4], r2[4];
+    const int c = blockIdx.x;
+    double s1 = 0.0, s2 = 0.0;
+    for (int kk = threadIdx.x; kk < d; kk += 128) {
+        const double v = c < k ? C[static_cast<long long>(c) * d + kk] : 0.0;
+        const float f = static_cast<float>(v);
+        CfT[static_cast<long long>(kk) * Kp + c] = f;
+        s1 += static_cast<double>(f) * static_cast<double>(f);
+        s2 += v * v;
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if ((threadIdx.x & 31) == 0) { r1[threadIdx.x >> 5] = s1; r2[threadIdx.x >> 5] = s2; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        s1 = r1[0] + r1[1] + r1[2] + r1[3];
+        s2 = r2[0] + r2[1] + r2[2] + r2[3];
+        ncf[c] = c < k ? static_cast<float>(s1) : kPosInf;
+        if (c < k) atomicMax(cmax, static_cast<unsigned long long>(__double_as_longlong(fmax(s1, s2))));
+    }
+}
+
+__global__ void __launch_bounds__(256, 1) assign_filter_kernel(const float* __restrict__ X, long long N, int d,
+                                                               const float* __restrict__ CfT, const float* __restrict__ ncf,
+                                                               int Kp, const unsigned long long* __restrict__ cmax,
+                                                               uint32_t* __restrict__ out, uint32_t* __restrict__ amb,
+                                                               unsigned* __restrict__ namb) {
+    extern __shared__ __align__(16) unsigned char dyn[];
+    FilterSmem& sm = *reinterpret_cast<FilterSmem*>(dyn);
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const long long p0 = static_cast<long long>(blockIdx.x) * kFB;
+    const int ntile = Kp / kFB;
+    auto load_b = [&](int buf, int c0) {
+        for (int e = tid; e < d * (kFB / 4); e += 256) {
+            const int kk = e / (kFB / 4), ch = e % (kFB / 4);
+            cp_async16(&sm.B[buf][kk][ch * 4], CfT + static_cast<long long>(kk) * Kp + c0 + ch * 4);
+        }
+        if (tid < kFB / 4) cp_async16(&sm.nc[buf][tid * 4], ncf + c0 + tid * 4);
+        cp_async_commit();
+    };
+    load_b(0, 0);
+    // point tile, transposed to feature-major (a one-time load per CTA)
+    for (int e = tid; e < kFB * d; e += 256) {
+        const int pp = e % kFB, kk = e / kFB;
+        const long long p = p0 + pp;
+        sm.A[kk][pp] = p < N ? X[p * d + kk] : 0.0f;
+    }
+    __syncthreads();
+    if (tid < kFB) {
+        double sx = 0.0;
+        for (int kk = 0; kk < d; ++kk) sx += static_cast<double>(sm.A[kk][tid]) * static_cast<double>(sm.A[kk][tid]);
+        sm.xn[tid] = sx;
+    }
+    float v1[8], v2[8];
+    int i1[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { v1[i] = kPosInf; v2[i] = kPosInf; i1[i] = 0; }
+    for (int t = 0; t < ntile; ++t) {
+        const int buf = t & 1;
+        if (t + 1 < ntile) {
+            load_b(buf ^ 1, (t + 1) * kFB);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        float acc[8][8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+        const float* Bb = &sm.B[buf][0][0];
+#pragma unroll 4
+        for (int kk = 0; kk < d; ++kk) {
+            const float4 a0 = *reinterpret_cast<const float4*>(&sm.A[kk][ty * 4]);
+            const float4 a1 = *reinterpret_cast<const float4*>(&sm.A[kk][64 + ty * 4]);
+            const float4 b0 = *reinterpret_cast<const float4*>(Bb + kk * kFB + tx * 4);
+            const float4 b1 = *reinterpret_cast<const float4*>(Bb + kk * kFB + 64 + tx * 4);
+            const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int cl = j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4);
+            const float nc = sm.nc[buf][cl];
+            const int c = t * kFB + cl;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float v = fmaf(-2.0f, acc[i][j], nc);  // one rounding of |c_f|^2 - 2 x.c_f
+                if (v < v1[i]) { v2[i] = v1[i]; v1[i] = v; i1[i] = c; }
+                else if (v < v2[i]) v2[i] = v;
+            }
+        }
+        __syncthreads();  // buffer `buf` is refilled by the next iteration's load
+    }
+    // merge the 16 column threads of each point (half-warp): best, index, second
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+            const float ov1 = __shfl_xor_sync(0xffffffffu, v1[i], o);
+            const float ov2 = __shfl_xor_sync(0xffffffffu, v2[i], o);
+            const int oi = __shfl_xor_sync(0xffffffffu, i1[i], o);
+            if (ov1 < v1[i] || (ov1 == v1[i] && oi < i1[i])) {
+                v2[i] = fminf(v1[i], ov2);
+                v1[i] = ov1;
+                i1[i] = oi;
+            } else {
+                v2[i] = fminf(ov1, v2[i]);
+            }
+        }
+    }
+    if (tx == 0) {
+        const double u = 5.9604644775390625e-08;  // 2^-24
+        const double g = d * u / (1.0 - d * u);    // gamma_d of the fp32 FMA dot
+        const double C = sqrt(__longlong_as_double(*cmax)) * (1.0 + 1e-12);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int pp = i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4);
+            const long long p = p0 + pp;
+            if (p >= N) continue;
+            const double x = sqrt(sm.xn[pp]) * (1.0 + 1e-12);
+            // c -> c_f (2u(x+C)C + u^2 C^2), |c_f|^2 -> fp32 (u C^2), dot (2 g x C),
+            // final rounding (u (C^2 + 2 x C)), fp64 fold of D (<= 1e-13 (x+C)^2)
+            const double E = 1.05 * ((2.0 * g + 4.0 * u) * x * C + 4.0 * u * C * C + u * u * C * C) +
+                             1e-12 * (x + C) * (x + C);
+            const double gap = static_cast<double>(v2[i]) - static_cast<double>(v1[i]);
+            if (gap > 2.0 * E) out[p] = static_cast<uint32_t>(i1[i]);
+            else amb[atomicAdd(namb, 1u)] = static_cast<uint32_t>(p);
+        }
+    }
+}
+
 template <typename T>
 void assign_device(Ctx& ctx, const T* X, long long N, int d, const double* C, int k, uint32_t* out) {
     if (N == 0) return;
-    assign_exact_kernel<T><<<ceil_div(N, TP), 256, 0, ctx.stream>>>(X, N, d, C, k, out, nullptr);
+    cudaStream_t s = ctx.stream;
+    // fp32 filter for big problems (fp32 points, d <= kFD)
+    if (std::is_same<T, float>::value && d <= kFD && N * static_cast<long long>(k) >= (1LL << 22)) {
+        const int Kp = static_cast<int>(ceil_div(k, kFB)) * kFB;
+        DevBuf<float> CfT(static_cast<size_t>(d) * Kp), ncf(Kp);
+        DevBuf<unsigned long long> cmax(1);
+        DevBuf<uint32_t> amb(N);
+        DevBuf<unsigned> namb(1);
+        cmax.zero(s);
+        namb.zero(s);
+        filter_prep_kernel<<<Kp, 128, 0, s>>>(C, k, d, Kp, CfT.get(), ncf.get(), cmax.get());
+        static bool attr[64] = {};
+        if (ctx.device >= 64 || !attr[ctx.device]) {
+            CUDA_OK(cudaFuncSetAttribute(assign_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sizeof(FilterSmem))));
+            if (ctx.device < 64) attr[ctx.device] = true;
+        }
+        assign_filter_kernel<<<ceil_div(N, kFB), 256, sizeof(FilterSmem), s>>>(
+            reinterpret_cast<const float*>(X), N, d, CfT.get(), ncf.get(), Kp, cmax.get(), out, amb.get(), namb.get());
+        LAUNCH_OK("assign_filter_kernel");
+        unsigned h_amb = 0;
+        namb.download(&h_amb, 1, s);
+        ctx.sync();
+        ctx.filter_ambiguous += h_amb;
+        ctx.filter_points += N;
+        if (h_amb)
+            assign_exact_kernel<T><<<ceil_div(static_cast<long long>(h_amb), TP), 256, 0, s>>>(X, h_amb, d, C, k, out,
+                                                                                                nullptr, amb.get());
+        LAUNCH_OK("assign_exact_kernel (ambiguous)");
+        return;
+    }
+    assign_exact_kernel<T><<<ceil_div(N, TP), 256, 0, s>>>(X, N, d, C, k, out, nullptr, nullptr);
     LAUNCH_OK("assign_exact_kernel");
 }
 

@@ -23,3 +23,11 @@ for r in rows[start + 1:]:
 for k in sorted(agg):
     t, b = agg[k]
     print(f"{k:3d} {names[k]:60s} {t:9.1f} us {b:9.1f} MB {b / t * 1e3 if t else 0:7.0f} GB/s")
+if len(sys.argv) > 2 and sys.argv[2] == "--by-name":
+    tot = defaultdict(lambda: [0, 0.0])
+    for k in agg:
+        tot[names[k]][0] += 1
+        tot[names[k]][1] += agg[k][0]
+    print("---- by kernel name ----")
+    for n, (c, t) in sorted(tot.items(), key=lambda x: -x[1][1]):
+        print(f"{n:60s} {c:6d} launches {t / 1e3:9.2f} ms  {t / c:8.1f} us avg")

@@ -56,6 +56,27 @@ def test_assign_ties_lowest_index(ctx, ref):
     assert np.array_equal(lcn.assign_nearest(ctx, x, ctr), ref.assign_nearest(x, ctr))
 
 
+@pytest.mark.parametrize("n,d,k,seed,dup", [(40000, 128, 128, 21, False), (50000, 37, 96, 22, False),
+                                            (40000, 64, 128, 23, True)])
+def test_assign_filter_bit_exact(ctx, ref, n, d, k, seed, dup):
+    # N k >= 2^22 with fp32 points: the fp32 filter + exact fallback path.
+    # dup: centroids 64.. repeat 0.. -> exact ties, lowest index wins
+    x = rng_points(seed, n, d)
+    r = np.random.default_rng(seed)
+    ctr = x[r.choice(n, k, replace=False)] + r.standard_normal((k, d)) * 0.3  # fp64, not fp32-exact
+    if dup:
+        ctr[k // 2:] = ctr[:k // 2]
+    assert np.array_equal(lcn.assign_nearest(ctx, x, ctr), ref.assign_nearest(x, ctr))
+
+
+def test_lloyd_filter_bit_exact(ctx, ref):
+    x = rng_points(31, 30000, 64, comps=40)
+    c_gpu, a_gpu = lcn.lloyd(ctx, x, 160, 10, 31)
+    c_ref, a_ref = ref.lloyd(x, 160, 10, 31)
+    assert np.array_equal(a_gpu, a_ref)
+    assert np.array_equal(c_gpu.view(np.uint64), c_ref.view(np.uint64))
+
+
 def test_lsh_buckets_config0(ctx, ref):
     pr = configs.config0()
     cfg = lcn.LshConfig(pr.bands, 1, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
