@@ -113,15 +113,15 @@ __global__ void __launch_bounds__(256) pp_update_kernel(const T* __restrict__ X,
     if (p < N && acc < dist2[p]) dist2[p] = acc;
 }
 
-// Exact emulation of the sequential fp64 fold s_{i+1} = fl(s_i + x_i) by one
-// warp, 32 elements at a time. While s is a normal number in the binade
+// Exact emulation of the sequential fp64 fold s_{i+1} = fl(s_i + x_i)
+// (kmeans.cpp:36-40, 51-58). While s is a normal number in the binade
 // [2^e, 2^(e+1)) its grid is u = 2^(e-52) and fl(s + x) = s + u * RN(x/u)
-// (x >= 0); the per-lane integers RN(x/u) are prefix-summed exactly in int64.
-// A lane leaves the fast path when its rounding is a tie (parity-dependent),
-// when x/u is huge, or when the running sum would reach 2^(e+1); that element
-// is added with a real fp64 add and the binade is recomputed.
-// With search, also returns the first index whose running sum is >= target
-// and whose element is > 0 (kmeans.cpp:51-58).
+// (x >= 0), RN ties to even on the running significand (ParInc below); runs
+// of elements are composed exactly in int64. An element leaves the fast path
+// when x/u is huge or the running sum would reach 2^(e+1); it is added with a
+// real fp64 add and the binade is recomputed. With search, the fold also
+// returns the first index whose running sum is >= target and whose element is
+// > 0 (kmeans.cpp:51-58).
 struct FoldResult {
     double s;
     long long pick;
@@ -158,8 +158,13 @@ __device__ __forceinline__ double scale_to_grid(double x, int e) {
 struct ParInc {
     long long i0, i1;
 };
+// Increments saturate at 2^61: a run that large has left its binade anyway
+// (only runs below 2^53 are used), and int64 cannot overflow.
+constexpr long long kIncSat = 1LL << 61;
 __device__ __forceinline__ ParInc par_compose(ParInc f, ParInc g) {
-    return {f.i0 + ((f.i0 & 1) ? g.i1 : g.i0), f.i1 + (((1 + f.i1) & 1) ? g.i1 : g.i0)};
+    const long long a = f.i0 + ((f.i0 & 1) ? g.i1 : g.i0);
+    const long long b = f.i1 + (((1 + f.i1) & 1) ? g.i1 : g.i0);
+    return {a < kIncSat ? a : kIncSat, b < kIncSat ? b : kIncSat};
 }
 // element x scaled to the grid (q = x / u, 0 <= q < 2^53)
 __device__ __forceinline__ ParInc par_element(double q) {
@@ -182,56 +187,6 @@ __device__ __forceinline__ ParInc par_scan(ParInc v, int lane) {
     return v;
 }
 
-// x[begin .. end) may be a shared-memory copy: xs points at element `begin`.
-__device__ FoldResult warp_exact_fold(const double* xs, long long begin, long long end, double s, bool search,
-                                      double target) {
-    const int lane = threadIdx.x & 31;
-    long long pick = -1;
-    for (long long base = begin; base < end; base += 32) {
-        const int cnt = static_cast<int>(min(32LL, end - base));
-        const double v = lane < cnt ? xs[base - begin + lane] : 0.0;
-        int a = 0;
-        while (a < cnt) {
-            if (!(s >= kMinNormal && s < kPosInf)) {  // zero / subnormal / inf: real add
-                double va = __shfl_sync(0xffffffffu, v, a);
-                s = xadd(s, va);
-                if (search && pick < 0 && s >= target && va > 0.0) pick = base + a;
-                ++a;
-                continue;
-            }
-            const int e = dbl_exp(s);
-            const long long S = dbl_sig(s);
-            const bool mine = lane >= a && lane < cnt;
-            const double q = mine ? scale_to_grid(v, e) : 0.0;
-            const bool big = mine && !(q < 9007199254740992.0);
-            const ParInc pf = par_scan((mine && !big) ? par_element(q) : ParInc{0, 0}, lane);
-            const long long P = (S & 1) ? pf.i1 : pf.i0;
-            // leave the fast path at a huge element or where the sum reaches 2^(e+1)
-            const bool bad = mine && (big || S + P >= kTwo53);
-            const unsigned bm = __ballot_sync(0xffffffffu, bad);
-            const int fb = bm ? __ffs(bm) - 1 : cnt;
-            if (search && pick < 0) {
-                bool hit = false;
-                if (lane >= a && lane < fb) hit = dbl_make(S + P, e) >= target && v > 0.0;
-                const unsigned hm = __ballot_sync(0xffffffffu, hit);
-                if (hm) pick = base + __ffs(hm) - 1;
-            }
-            const long long Pacc = fb > a ? __shfl_sync(0xffffffffu, P, fb - 1) : 0;
-            s = dbl_make(S + Pacc, e);
-            if (fb < cnt) {
-                double vb = __shfl_sync(0xffffffffu, v, fb);
-                s = xadd(s, vb);
-                if (search && pick < 0 && s >= target && vb > 0.0) pick = base + fb;
-                a = fb + 1;
-            } else {
-                a = cnt;
-            }
-        }
-        if (search && pick >= 0) break;
-    }
-    return {s, pick};
-}
-
 // ---- chunk-parallel exact fold ----------------------------------------------
 // The fold over N values is cut into chunks of kFoldChunk. Most chunks lie
 // inside one binade of the running sum, where the fold's result depends only
@@ -244,7 +199,7 @@ __device__ FoldResult warp_exact_fold(const double* xs, long long begin, long lo
 //   D) one warp walks the chunks in order with the exact running sum: runs
 //      of clean chunks whose actual binade matches e_c advance by a
 //      parity-scan of their R_c, any other chunk is folded element-wise by
-//      warp_exact_fold.
+//      block_exact_fold.
 // The prediction only decides which path a chunk takes; the walk re-checks
 // the actual binade, so the result is exact regardless.
 constexpr int kFoldChunk = 2048;
@@ -326,34 +281,136 @@ __global__ void __launch_bounds__(256) fold_round_kernel(const double* __restric
     }
 }
 
-// Exact fold of chunk c by one warp from a shared-memory copy: all of the
-// chunk's loads are issued at once (one memory latency per chunk instead of
-// one per 32 elements).
-__device__ __forceinline__ FoldResult fold_chunk_staged(const double* __restrict__ x, long long N, int c, double s,
-                                                        bool search, double target, double* buf) {
-    const int lane = threadIdx.x & 31;
+// ---- block-wide exact fold of one staged chunk (kWalkThreads threads) -----
+// Thread t owns elements [kSeg t, kSeg t + kSeg) of the chunk. While the running
+// sum is normal in binade e, every thread composes its segment's parity
+// function (ParInc) and a block scan gives each segment's start and end sums.
+// The first segment that holds a huge element, leaves the binade, or (search)
+// reaches the target is walked element by element by its owner, which
+// publishes the exact stop; a stop element gets a real fp64 add and the fold
+// restarts behind it. A chunk typically restarts once per binade change.
+constexpr int kWalkThreads = 256;
+constexpr int kSeg = kFoldChunk / kWalkThreads;
+
+struct WalkShared {
+    double buf[kFoldChunk];
+    ParInc wsum[kWalkThreads / 32];
+    int flag_min;
+    int ev;           // 0: segment walked, no event; 1: real add at `stop`; 2: pick
+    int stop;
+    long long s_sig;  // significand before `stop` (ev 1) / after the segment (ev 0, 2)
+    long long pick;
+};
+
+__device__ FoldResult block_exact_fold(WalkShared& sh, int cnt, long long base, double s, bool search,
+                                       double target) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const double* xs = sh.buf;
+    int a = 0;
+    long long pick = -1;
+    while (a < cnt) {
+        if (!(s >= kMinNormal && s < kPosInf)) {  // zero / subnormal / inf: one real add
+            const double va = xs[a];
+            s = xadd(s, va);
+            if (search && s >= target && va > 0.0) { pick = base + a; break; }
+            ++a;
+            continue;
+        }
+        const int e = dbl_exp(s);
+        const long long S = dbl_sig(s);
+        const int lo = max(a, kSeg * tid), hi = min(cnt, kSeg * tid + kSeg);
+        ParInc f{0, 0};
+        bool big = false;
+        for (int i = lo; i < hi; ++i) {
+            const double q = scale_to_grid(xs[i], e);
+            if (!(q < 9007199254740992.0)) { big = true; break; }
+            f = par_compose(f, par_element(q));
+        }
+        const ParInc inc = par_scan(f, lane);  // inclusive, within the warp
+        if (lane == 31) sh.wsum[warp] = inc;
+        if (tid == 0) sh.flag_min = kWalkThreads;
+        __syncthreads();
+        ParInc pre{0, 0};
+        for (int w = 0; w < warp; ++w) pre = par_compose(pre, sh.wsum[w]);
+        const ParInc up = par_shfl_up(inc, 1);
+        const ParInc ex = par_compose(pre, lane ? up : ParInc{0, 0});  // before this segment
+        const ParInc fe = par_compose(ex, f);                              // through this segment
+        const long long s0 = S + ((S & 1) ? ex.i1 : ex.i0);
+        const long long s1 = S + ((S & 1) ? fe.i1 : fe.i0);
+        bool flag = lo < hi && (big || s1 >= kTwo53);
+        if (search && lo < hi && s1 < kTwo53 && dbl_make(s1, e) >= target) flag = true;
+        if (flag) atomicMin(&sh.flag_min, tid);
+        __syncthreads();
+        const int tf = sh.flag_min;
+        if (tf == kWalkThreads) {  // no event: the rest of the chunk is one run
+            if (tid == kWalkThreads - 1) sh.s_sig = s1;
+            __syncthreads();
+            s = dbl_make(sh.s_sig, e);
+            break;
+        }
+        if (tid == tf) {
+            long long cur = s0;
+            int ev = 0, stop = hi;
+            long long pk = -1;
+            for (int i = lo; i < hi; ++i) {
+                const double q = scale_to_grid(xs[i], e);
+                if (!(q < 9007199254740992.0)) { ev = 1; stop = i; break; }
+                const ParInc pe = par_element(q);
+                const long long nx = cur + ((cur & 1) ? pe.i1 : pe.i0);
+                if (nx >= kTwo53) { ev = 1; stop = i; break; }
+                cur = nx;
+                if (search && dbl_make(cur, e) >= target && xs[i] > 0.0) { ev = 2; pk = base + i; break; }
+            }
+            sh.ev = ev;
+            sh.stop = stop;
+            sh.s_sig = cur;
+            sh.pick = pk;
+        }
+        __syncthreads();
+        const int ev = sh.ev, stop = sh.stop;
+        s = dbl_make(sh.s_sig, e);
+        const long long pk = sh.pick;
+        __syncthreads();  // shared state is rewritten by the next round
+        if (ev == 2) { pick = pk; break; }
+        if (ev == 0) { a = stop; continue; }
+        const double vb = xs[stop];
+        s = xadd(s, vb);
+        if (search && s >= target && vb > 0.0) { pick = base + stop; break; }
+        a = stop + 1;
+    }
+    return {s, pick};
+}
+
+// Stage chunk c of x into shared memory (all threads) and fold it.
+__device__ __forceinline__ FoldResult fold_chunk_block(WalkShared& sh, const double* __restrict__ x, long long N,
+                                                       int c, double s, bool search, double target) {
     const long long b = static_cast<long long>(c) * kFoldChunk;
-    const long long e = min(N, b + kFoldChunk);
-    __syncwarp();
-#pragma unroll 16
-    for (int j = lane; j < kFoldChunk; j += 32) buf[j] = b + j < e ? x[b + j] : 0.0;
-    __syncwarp();
-    return warp_exact_fold(buf, b, e, s, search, target);
+    const int cnt = static_cast<int>(min(N - b, static_cast<long long>(kFoldChunk)));
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kSeg; ++j) {
+        const int i = threadIdx.x + j * kWalkThreads;
+        sh.buf[i] = i < cnt ? x[b + i] : 0.0;
+    }
+    __syncthreads();
+    return block_exact_fold(sh, cnt, b, s, search, target);
 }
 
 // D) walk + draw + pick for k-means++ step t (kmeans.cpp:35-62). raw[] holds
 // the caller's engine draws in order; a step with total <= 0 consumes none
-// (kmeans.cpp:42-47).
-__global__ void pp_walk_pick_kernel(double* __restrict__ dist2, unsigned char* __restrict__ used, long long N, int nch,
-                                    const int* __restrict__ ebin, const longlong2* __restrict__ R,
-                                    double* __restrict__ sstart, const unsigned long long* __restrict__ raw, int n_raw,
-                                    int* __restrict__ draw_counter, uint32_t* __restrict__ chosen, int t) {
-    __shared__ double buf[kFoldChunk];
-    const int lane = threadIdx.x;
+// (kmeans.cpp:42-47). Every warp runs the chunk walk redundantly (identical
+// values, uniform control flow); chunks that need an element-wise fold use
+// the whole block.
+__global__ void __launch_bounds__(kWalkThreads) pp_walk_pick_kernel(
+    double* __restrict__ dist2, unsigned char* __restrict__ used, long long N, int nch, const int* __restrict__ ebin,
+    const longlong2* __restrict__ R, double* __restrict__ sstart, const unsigned long long* __restrict__ raw,
+    int n_raw, int* __restrict__ draw_counter, uint32_t* __restrict__ chosen, int t) {
+    __shared__ WalkShared sh;
+    const int lane = threadIdx.x & 31;
+    const bool w0 = threadIdx.x < 32;
     double S = 0.0;
     // 32 chunks per step: a run of clean chunks in the running sum's binade
-    // advances by an exact int64 prefix sum of their R_c; the walk goes
-    // element-wise only where the run breaks (binade change, dirty chunk).
+    // advances by an exact parity scan of their R_c
     for (int cb = 0; cb < nch; cb += 32) {
         const int c_l = cb + lane;
         const int e_l = c_l < nch ? ebin[c_l] : 0;
@@ -375,23 +432,22 @@ __global__ void pp_walk_pick_kernel(double* __restrict__ dist2, unsigned char* _
             // a chunk whose end leaves the binade is folded element-wise
             const unsigned cross = __ballot_sync(0xffffffffu, run && Si + P >= kTwo53);
             if (cross) fb = min(fb, __ffs(cross) - 1);
-            // exclusive prefix = inclusive prefix of the previous lane
             const long long Pprev = __shfl_up_sync(0xffffffffu, P, 1);
             const long long Pex = lane > k ? Pprev : 0;
-            if (lane >= k && lane < fb) sstart[c_l] = dbl_make(Si + Pex, eS);
+            if (w0 && lane >= k && lane < fb) sstart[c_l] = dbl_make(Si + Pex, eS);
             if (fb > k) S = dbl_make(Si + __shfl_sync(0xffffffffu, P, fb - 1), eS);
             if (fb < cnt) {
                 const int c = cb + fb;
-                if (lane == 0) sstart[c] = S;
-                const long long b = static_cast<long long>(c) * kFoldChunk;
-                S = fold_chunk_staged(dist2, N, c, S, false, 0.0, buf).s;
+                if (threadIdx.x == 0) sstart[c] = S;
+                S = fold_chunk_block(sh, dist2, N, c, S, false, 0.0).s;
                 k = fb + 1;
             } else {
                 k = cnt;
             }
         }
     }
-    if (lane == 0) sstart[nch] = S;
+    if (threadIdx.x == 0) sstart[nch] = S;
+    __syncthreads();
     long long pick;
     if (S <= 0.0) {
         pick = N;  // all remaining points coincide with a centroid: first unused
@@ -417,21 +473,19 @@ __global__ void pp_walk_pick_kernel(double* __restrict__ dist2, unsigned char* _
             if (m) { cstar = cb + __ffs(m) - 1; break; }
         }
         pick = -1;
-        if (cstar < nch) {
-            // the running sum reaches the target inside chunk cstar (an element
-            // that raises it is > 0); later chunks only as a guard
-            double sc = sstart[cstar];
-            for (int c = cstar; c < nch && pick < 0; ++c) {
-                const FoldResult sr = fold_chunk_staged(dist2, N, c, sc, true, target, buf);
-                pick = sr.pick;
-                sc = sr.s;
-            }
+        // the running sum reaches the target inside chunk cstar (an element
+        // that raises it is > 0); later chunks only as a guard
+        double sc = cstar < nch ? sstart[cstar] : 0.0;
+        for (int cc = cstar; cc < nch && pick < 0; ++cc) {
+            const FoldResult sr = fold_chunk_block(sh, dist2, N, cc, sc, true, target);
+            pick = sr.pick;
+            sc = sr.s;
         }
         if (pick < 0) pick = N - 1;
-        if (lane == 0) *draw_counter = di + 1;
+        __syncthreads();
+        if (threadIdx.x == 0) *draw_counter = di + 1;
     }
-    __syncwarp();
-    if (lane == 0) {
+    if (threadIdx.x == 0) {
         chosen[t] = static_cast<uint32_t>(pick);
         if (pick < N) {
             dist2[pick] = 0.0;
@@ -469,7 +523,7 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
         fold_chunk_sum_kernel<<<nch, 256, 0, s>>>(dist2.get(), N, csum.get());
         fold_plan_kernel<<<1, 1024, 0, s>>>(csum.get(), nch, ebin.get());
         fold_round_kernel<<<nch, 256, 0, s>>>(dist2.get(), N, ebin.get(), R.get());
-        pp_walk_pick_kernel<<<1, 32, 0, s>>>(dist2.get(), used.get(), N, nch, ebin.get(), R.get(), sstart.get(),
+        pp_walk_pick_kernel<<<1, kWalkThreads, 0, s>>>(dist2.get(), used.get(), N, nch, ebin.get(), R.get(), sstart.get(),
                                              d_raw.get(), static_cast<int>(raw.size()), counter.get(), d_chosen, t);
     }
     LAUNCH_OK("kmeans++");
