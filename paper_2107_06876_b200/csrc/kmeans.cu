@@ -86,31 +86,78 @@ __global__ void __launch_bounds__(256) assign_exact_kernel(const T* __restrict__
 
 // ---- k-means++ (kmeans.cpp:23-65) ------------------------------------------
 // dist2[i] = min(dist2[i], sqdist(x_i, x_last)), strict < as kmeans.cpp:38.
+// Pruning (exactness-preserving): near[i] is the seed whose fold gave
+// dist2[i]; with dc[j] = |x_{seed j} - x_last| (fp64, |rel err| < 1e-13), the
+// triangle inequality |x_i - x_last| >= dc[near] - |x_i - x_near| shows that
+// dc[near] >= 2 sqrt(dist2[i]) (with margins) makes the new fold >= dist2[i],
+// so the point cannot update and is skipped. The remaining points of a block
+// are compacted and folded exactly (one thread per point, slabs staged).
 template <typename T>
-__global__ void __launch_bounds__(256) pp_update_kernel(const T* __restrict__ X, long long N, int d,
-                                                        const uint32_t* __restrict__ chosen, int t,
-                                                        double* __restrict__ dist2) {
+__global__ void __launch_bounds__(64) pp_update_kernel(const T* __restrict__ X, long long N, int d,
+                                                       const uint32_t* __restrict__ chosen, int t,
+                                                       double* __restrict__ dist2, uint32_t* __restrict__ near,
+                                                       const double* __restrict__ dc) {
     __shared__ double As[KC][TP + 1];
     __shared__ double Cs[KC];
+    __shared__ uint32_t rows[TP];
+    __shared__ int cnt;
     const long long p0 = static_cast<long long>(blockIdx.x) * TP;
     const long long last = chosen[t];
-    // 4 threads per point would break the sequential fold; one thread folds
-    // one point, slabs staged for coalescing.
+    const int r = threadIdx.x;  // blockDim = TP
+    const long long p = p0 + r;
+    bool need = p < N;
+    double D = kPosInf;
+    if (need) {
+        D = dist2[p];
+        if (D < kPosInf && t > 0) {
+            const double lb = dc[near[p]] * (1.0 - 1e-12);
+            if (lb >= 2.0 * sqrt(D) * (1.0 + 1e-9)) need = false;
+        }
+    }
+    if (r == 0) cnt = 0;
+    __syncthreads();
+    if (need) rows[atomicAdd(&cnt, 1)] = static_cast<uint32_t>(p);
+    __syncthreads();
+    const int n_need = cnt;
+    if (n_need == 0) return;
     double acc = 0.0;
-    const int r = threadIdx.x;  // blockDim = 64
     for (int k0 = 0; k0 < d; k0 += KC) {
-        load_slab<T>(As, X, nullptr, p0, N, d, k0);
+        load_slab<T>(As, X, rows, 0, n_need, d, k0);
         if (threadIdx.x < KC) Cs[threadIdx.x] = k0 + threadIdx.x < d ? static_cast<double>(X[last * d + k0 + threadIdx.x]) : 0.0;
         __syncthreads();
+        if (r < n_need) {
 #pragma unroll
-        for (int kk = 0; kk < KC; ++kk) {
-            double df = xsub(As[kk][r], Cs[kk]);
-            acc = xadd(acc, xmul(df, df));
+            for (int kk = 0; kk < KC; ++kk) {
+                double df = xsub(As[kk][r], Cs[kk]);
+                acc = xadd(acc, xmul(df, df));
+            }
         }
         __syncthreads();
     }
-    long long p = p0 + r;
-    if (p < N && acc < dist2[p]) dist2[p] = acc;
+    if (r < n_need) {
+        const uint32_t q = rows[r];
+        if (acc < dist2[q]) {
+            dist2[q] = acc;
+            near[q] = static_cast<uint32_t>(t);
+        }
+    }
+}
+
+// dc[j] = |x_{chosen[j]} - x_{chosen[t]}| for j < t (fp64, one warp per j)
+template <typename T>
+__global__ void __launch_bounds__(256) seed_dist_kernel(const T* __restrict__ X, int d,
+                                                        const uint32_t* __restrict__ chosen, int t,
+                                                        double* __restrict__ dc) {
+    const int j = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (j >= t) return;
+    const long long a = chosen[j], b = chosen[t];
+    double s2 = 0.0;
+    for (int k = lane; k < d; k += 32) {
+        const double df = static_cast<double>(X[a * d + k]) - static_cast<double>(X[b * d + k]);
+        s2 += df * df;
+    }
+    s2 = warp_sum(s2);
+    if (lane == 0) dc[j] = sqrt(s2);
 }
 
 // Exact emulation of the sequential fp64 fold s_{i+1} = fl(s_i + x_i)
@@ -508,9 +555,12 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     DevBuf<int> ebin(nch);
     DevBuf<longlong2> R(nch);
     DevBuf<unsigned char> used(N);
+    DevBuf<uint32_t> near(N);
+    DevBuf<double> dc(std::max(k, 1));
     DevBuf<unsigned long long> d_raw(raw.size() ? raw.size() : 1);
     DevBuf<int> counter(1);
     used.zero(s);
+    near.zero(s);
     counter.zero(s);
     if (!raw.empty()) d_raw.upload(raw.data(), raw.size(), s);
     fill_kernel<<<ceil_div(N, 256), 256, 0, s>>>(dist2.get(), N, kPosInf);
@@ -519,7 +569,8 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     CUDA_OK(cudaMemcpyAsync(d_chosen, &f32, 4, cudaMemcpyHostToDevice, s));
     CUDA_OK(cudaMemcpyAsync(used.get() + first, &one, 1, cudaMemcpyHostToDevice, s));
     for (int t = 1; t < k; ++t) {
-        pp_update_kernel<T><<<ceil_div(N, TP), TP, 0, s>>>(X, N, d, d_chosen, t - 1, dist2.get());
+        if (t > 1) seed_dist_kernel<T><<<ceil_div(t - 1, 8), 256, 0, s>>>(X, d, d_chosen, t - 1, dc.get());
+        pp_update_kernel<T><<<ceil_div(N, TP), TP, 0, s>>>(X, N, d, d_chosen, t - 1, dist2.get(), near.get(), dc.get());
         fold_chunk_sum_kernel<<<nch, 256, 0, s>>>(dist2.get(), N, csum.get());
         fold_plan_kernel<<<1, 1024, 0, s>>>(csum.get(), nch, ebin.get());
         fold_round_kernel<<<nch, 256, 0, s>>>(dist2.get(), N, ebin.get(), R.get());
