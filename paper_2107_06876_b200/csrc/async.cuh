@@ -24,14 +24,17 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                  : "memory");
 }
 
-// wait until the barrier's phase with the given parity has completed
+// wait until the barrier's phase with the given parity has completed; the
+// suspend-time hint (ns) lets the waiting warp sleep until the phase flips
+// instead of re-polling (retry spins otherwise take issue slots from the
+// compute warps sharing the SM sub-partition)
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "r"(1000000u)
         : "memory");
 }
 

@@ -253,11 +253,19 @@ constexpr int kBandStages = 5;
 constexpr int kBandStageBytes = 16 * 1024;
 constexpr int kBandVec = 1024;  // max item columns / item rows
 
+// per item slot, resolved by producer 2 so consumers never touch global
+// metadata (dependent L2 round trips at every item start otherwise)
+struct ItemMeta {
+    uint32_t nr, cw, split, pieces;
+    double* part;  // this piece's scratch partials (split outputs), else null
+};
+
 struct BandSmem {
     unsigned char ring[kBandStages][kBandStageBytes];
     double vec[2][kBandVec];    // tt (row pass) / ss (column pass) per item slot (fp32 storage: float view)
     uint32_t out[2][kBandVec];  // output indices per item slot
     double red[kBandVec];       // column pass: per-row-group partial sums (groups x row stride <= kBandVec)
+    ItemMeta meta[2];
     uint64_t full[kBandStages], empty[kBandStages], vfull[2], vempty[2];
     uint32_t last;              // this CTA combines a split output
 };
@@ -288,22 +296,21 @@ __device__ __forceinline__ int band_rows_per_stage(uint32_t ws) {
 // Split-output epilogue: partials of `count` outputs are in scratch at
 // base + piece * count; the last piece to arrive sums them in order into
 // corr[outi[c]]. Called by all consumer threads after they wrote their partials.
-__device__ __forceinline__ void band_combine(BandSmem& sm, const BandWork& wk, uint32_t split, uint32_t count,
+__device__ __forceinline__ void band_combine(BandSmem& sm, const BandWork& wk, const ItemMeta& mt, uint32_t count,
                                              const uint32_t* outi, double* __restrict__ corr, int tid) {
-    const uint2 sp = wk.splits[split >> 8];
     __threadfence();
     consumers_sync();
-    if (tid == 0) sm.last = atomicAdd(&wk.counters[split >> 8], 1u) == sp.y - 1;
+    if (tid == 0) sm.last = atomicAdd(&wk.counters[mt.split >> 8], 1u) == mt.pieces - 1;
     consumers_sync();
     if (sm.last) {
         __threadfence();
-        const double* base = wk.scratch + sp.x;
+        const double* base = mt.part - static_cast<size_t>(mt.split & 0xffu) * count;  // piece 0
         for (uint32_t c = tid; c < count; c += kThreads) {
             double v = 0.0;
-            for (uint32_t k = 0; k < sp.y; ++k) v += __ldcg(base + static_cast<size_t>(k) * count + c);
+            for (uint32_t k = 0; k < mt.pieces; ++k) v += __ldcg(base + static_cast<size_t>(k) * count + c);
             corr[outi[c]] = v;
         }
-        if (tid == 0) wk.counters[split >> 8] = 0u;
+        if (tid == 0) wk.counters[mt.split >> 8] = 0u;
     }
 }
 
@@ -393,6 +400,21 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
                     sm.vec[slot][c] = c < valid ? exp(logv[v0 + c] - H) : 0.0;
             }
             for (uint32_t c = lane; c < nout; c += 32) sm.out[slot][c] = order[o0 + c];
+            if (lane == 0) {
+                ItemMeta mt;
+                mt.nr = item.nr;
+                mt.cw = item.cw;
+                mt.split = item.split[ROWS ? 0 : 1];
+                mt.pieces = 0;
+                mt.part = nullptr;
+                if (mt.split != 0xffffffffu) {
+                    const uint2 sp = wk.splits[mt.split >> 8];
+                    const uint32_t count = ROWS ? item.nr : item.cw;  // partials per piece
+                    mt.pieces = sp.y;
+                    mt.part = wk.scratch + sp.x + static_cast<size_t>(mt.split & 0xffu) * count;
+                }
+                sm.meta[slot] = mt;
+            }
             mbar_arrive(&sm.vfull[slot]);  // all 32 lanes (release: their smem writes)
         }
         return;
@@ -402,26 +424,23 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
     uint32_t phase = 0;
     int kb = 0;
     for (uint32_t it = i_beg; it < i_end; ++it, ++kb) {
-        const BandItem item = wk.items[it];
-        const uint32_t ws = static_cast<uint32_t>(row_stride(item.cw));
-        const uint32_t nq = ws / 4;
         const int slot = kb & 1;
+        mbar_wait(&sm.vfull[slot], (kb >> 1) & 1);
+        const ItemMeta mt = sm.meta[slot];
+        const uint32_t ws = static_cast<uint32_t>(row_stride(mt.cw));
+        const uint32_t nq = ws / 4;
         const int R = band_rows_per_stage<T>(ws);
-        const uint32_t split = item.split[ROWS ? 0 : 1];
         // row pass, split: partial row sums go to scratch
-        double* rpart = nullptr;
-        if (ROWS && split != 0xffffffffu)
-            rpart = wk.scratch + wk.splits[split >> 8].x + static_cast<size_t>(split & 0xffu) * item.nr;
+        double* rpart = ROWS ? mt.part : nullptr;
         // column pass mapping: groups of nq threads, thread (g, q) owns quad q
         // of rows g, g + ng, ... of every chunk; sums stay in registers
         const uint32_t ng = nq >= static_cast<uint32_t>(kThreads) ? 1u : kThreads / nq;
         const uint32_t g = static_cast<uint32_t>(tid) / nq, q = static_cast<uint32_t>(tid) % nq;
         const bool col_own = g < ng;
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        mbar_wait(&sm.vfull[slot], (kb >> 1) & 1);
         const uint32_t* outi = sm.out[slot];
-        for (uint32_t r0 = 0; r0 < item.nr; r0 += R) {
-            const uint32_t nr = item.nr - r0 < static_cast<uint32_t>(R) ? item.nr - r0 : static_cast<uint32_t>(R);
+        for (uint32_t r0 = 0; r0 < mt.nr; r0 += R) {
+            const uint32_t nr = mt.nr - r0 < static_cast<uint32_t>(R) ? mt.nr - r0 : static_cast<uint32_t>(R);
             mbar_wait(&sm.full[stage], phase);
             const T* blk = reinterpret_cast<const T*>(sm.ring[stage]);
             if constexpr (ROWS) {
@@ -517,7 +536,7 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
             }
         }
         if constexpr (ROWS) {
-            if (split != 0xffffffffu) band_combine(sm, wk, split, item.nr, outi, corr, tid);
+            if (rpart) band_combine(sm, wk, mt, mt.nr, outi, corr, tid);
         } else {
             // combine the row groups: red[g * ws + c], one thread per column
             if (col_own) {
@@ -525,16 +544,14 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
                 o[0] = a0; o[1] = a1; o[2] = a2; o[3] = a3;
             }
             consumers_sync();
-            double* cpart = split != 0xffffffffu
-                                ? wk.scratch + wk.splits[split >> 8].x + static_cast<size_t>(split & 0xffu) * item.cw
-                                : nullptr;
-            for (uint32_t c = tid; c < item.cw; c += kThreads) {
+            double* cpart = mt.part;
+            for (uint32_t c = tid; c < mt.cw; c += kThreads) {
                 double v = 0.0;
                 for (uint32_t gg = 0; gg < ng; ++gg) v += sm.red[gg * ws + c];
                 if (cpart) cpart[c] = v;
                 else corr[outi[c]] = v;
             }
-            if (cpart) band_combine(sm, wk, split, item.cw, outi, corr, tid);
+            if (cpart) band_combine(sm, wk, mt, mt.cw, outi, corr, tid);
             consumers_sync();  // red is rewritten by the next item
         }
         __syncwarp();
