@@ -51,7 +51,7 @@ PhaseTimer::~PhaseTimer() {
 BandView Op::view(int b) const {
     const Band& B = bands[b];
     return {B.src_order.get(), B.tgt_order.get(), B.src_start.get(), B.tgt_start.get(), B.blk_off.get(),
-            B.src_bucket.get(), B.tgt_bucket.get(), B.src_local.get(), B.tgt_local.get(), B.src_pos.get(),
+            B.blkT_off.get(), B.src_bucket.get(), B.tgt_bucket.get(), B.src_local.get(), B.tgt_local.get(), B.src_pos.get(),
             B.tgt_pos.get()};
 }
 
@@ -143,6 +143,7 @@ void build_band_layout(Ctx& ctx, Band& B, const uint32_t* d_src_bucket, const ui
     stable_group(ctx, B.src_bucket.get(), n, nb, B.src_order, B.src_start, B.h_src_start, B.src_local, B.src_pos);
     stable_group(ctx, B.tgt_bucket.get(), m, nb, B.tgt_order, B.tgt_start, B.h_tgt_start, B.tgt_local, B.tgt_pos);
     B.h_blk_off.assign(nb + 1, 0);
+    B.h_blkT_off.assign(nb + 1, 0);
     std::vector<uint32_t> work;
     B.real_entries = 0;
     for (size_t b = 0; b < nb; ++b) {
@@ -153,6 +154,7 @@ void build_band_layout(Ctx& ctx, Band& B, const uint32_t* d_src_bucket, const ui
         // ... and every block starts on a 128-byte line (32 entries) so the
         // bulk-copy chunks of the streaming kernels are line aligned.
         B.h_blk_off[b + 1] = (B.h_blk_off[b] + nbk * row_stride(mbk) + 31ull) & ~31ull;
+        B.h_blkT_off[b + 1] = (B.h_blkT_off[b] + mbk * row_stride(nbk) + 31ull) & ~31ull;
         B.real_entries += nbk * mbk;
         if (nbk && mbk) work.push_back(static_cast<uint32_t>(b));
     }
@@ -165,7 +167,9 @@ void build_band_layout(Ctx& ctx, Band& B, const uint32_t* d_src_bucket, const ui
         return sz(x) > sz(y);
     });
     B.entries = B.h_blk_off[nb];
+    B.entriesT = B.h_blkT_off[nb];
     B.blk_off.upload(B.h_blk_off.data(), nb + 1, s);
+    B.blkT_off.upload(B.h_blkT_off.data(), nb + 1, s);
     B.n_work = work.size();
     B.work.resize(std::max<size_t>(work.size(), 1));
     if (!work.empty()) B.work.upload(work.data(), work.size(), s);
@@ -753,6 +757,41 @@ void pad_rows(Ctx& ctx, const DevBuf<double>& in, size_t rows, size_t l, size_t 
 }
 }  // namespace
 
+namespace {
+// Transposed copy of every bucket block: out block b is m_b rows x
+// row_stride(n_b) (padding columns stay 0 from the memset). 32 x 32 tiles
+// through shared memory; one CTA per bucket walks its tiles.
+template <typename T>
+__global__ void __launch_bounds__(256) transpose_blocks_kernel(const double* __restrict__ in,
+                                                               const unsigned long long* __restrict__ blk_off,
+                                                               const unsigned long long* __restrict__ blkT_off,
+                                                               const uint32_t* __restrict__ src_start,
+                                                               const uint32_t* __restrict__ tgt_start,
+                                                               T* __restrict__ out) {
+    __shared__ double tile[32][33];
+    const uint32_t b = blockIdx.x;
+    const uint32_t nb = src_start[b + 1] - src_start[b], mb = tgt_start[b + 1] - tgt_start[b];
+    if (nb == 0 || mb == 0) return;
+    const unsigned long long ms = row_stride(mb), ns = row_stride(nb);
+    const double* A = in + blk_off[b];
+    T* O = out + blkT_off[b];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    for (uint32_t i0 = 0; i0 < nb; i0 += 32)
+        for (uint32_t j0 = 0; j0 < mb; j0 += 32) {
+            __syncthreads();
+            for (int r = ty; r < 32; r += 8) {
+                const uint32_t i = i0 + r, j = j0 + tx;
+                tile[r][tx] = (i < nb && j < mb) ? A[i * ms + j] : 0.0;
+            }
+            __syncthreads();
+            for (int r = ty; r < 32; r += 8) {
+                const uint32_t j = j0 + r, i = i0 + tx;
+                if (j < mb && i < nb) O[j * ns + i] = static_cast<T>(tile[tx][r]);
+            }
+        }
+}
+}  // namespace
+
 // Iteration copies (fp32 storage, fp64 accumulation;
 // fp64 storage in the exact mode). Low-rank factor rows are padded to
 // lp = round_up(l, 4) entries so each row starts 16-byte aligned.
@@ -765,6 +804,34 @@ void finalize_storage(Op& op) {
             DevBuf<float> v;
             to_f32(ctx, op.val64[b], v, op.bands[b].entries);
             op.val32.push_back(std::move(v));
+        }
+    }
+    if (op.kind == 3) {
+        // LCN: delta also stored transposed (targets x sources) so the row
+        // pass streams its blocks in the same output-stationary order as the
+        // column pass (2 x the delta bytes in HBM, same bytes per iteration)
+        op.val32T.clear();
+        op.val64T.clear();
+        for (size_t b = 0; b < op.bands.size(); ++b) {
+            const Band& B = op.bands[b];
+            if (op.fp64) {
+                DevBuf<double> t(std::max<unsigned long long>(B.entriesT, 1));
+                t.zero(ctx.stream);
+                if (B.nb)
+                    transpose_blocks_kernel<double><<<static_cast<unsigned>(B.nb), 256, 0, ctx.stream>>>(
+                        op.val64[b].get(), B.blk_off.get(), B.blkT_off.get(), B.src_start.get(), B.tgt_start.get(),
+                        t.get());
+                op.val64T.push_back(std::move(t));
+            } else {
+                DevBuf<float> t(std::max<unsigned long long>(B.entriesT, 1));
+                t.zero(ctx.stream);
+                if (B.nb)
+                    transpose_blocks_kernel<float><<<static_cast<unsigned>(B.nb), 256, 0, ctx.stream>>>(
+                        op.val64[b].get(), B.blk_off.get(), B.blkT_off.get(), B.src_start.get(), B.tgt_start.get(),
+                        t.get());
+                op.val32T.push_back(std::move(t));
+            }
+            LAUNCH_OK("transpose_blocks");
         }
     }
     if (op.kind >= 2) {

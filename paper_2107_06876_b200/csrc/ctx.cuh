@@ -89,7 +89,8 @@ struct Band {
     DevBuf<uint32_t> tgt_order;    // m
     DevBuf<uint32_t> src_start;    // nb+1
     DevBuf<uint32_t> tgt_start;    // nb+1
-    DevBuf<unsigned long long> blk_off;  // nb+1 (entries)
+    DevBuf<unsigned long long> blk_off;  // nb+1 (entries): block b, n_b rows x row_stride(m_b)
+    DevBuf<unsigned long long> blkT_off; // nb+1: transposed block b, m_b rows x row_stride(n_b) (lcn)
     DevBuf<uint32_t> src_bucket;   // n
     DevBuf<uint32_t> tgt_bucket;   // m
     DevBuf<uint32_t> src_local;    // n: position inside its bucket
@@ -99,9 +100,10 @@ struct Band {
     DevBuf<uint32_t> work;         // list of buckets with a nonempty block
     size_t n_work = 0;
     unsigned long long entries = 0;       // padded block entries held in HBM
+    unsigned long long entriesT = 0;      // padded transposed-block entries
     unsigned long long real_entries = 0;  // sum n_b * m_b
     std::vector<uint32_t> h_src_start, h_tgt_start;
-    std::vector<unsigned long long> h_blk_off;
+    std::vector<unsigned long long> h_blk_off, h_blkT_off;
 };
 
 }  // namespace lcnb

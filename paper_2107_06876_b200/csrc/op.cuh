@@ -18,6 +18,7 @@ struct BandView {
     const uint32_t* src_start;
     const uint32_t* tgt_start;
     const unsigned long long* blk_off;
+    const unsigned long long* blkT_off;
     const uint32_t* src_bucket;
     const uint32_t* tgt_bucket;
     const uint32_t* src_local;
@@ -49,6 +50,9 @@ struct Op {
     std::vector<Band> bands;
     std::vector<DevBuf<double>> val64;    // sparse: log K; lcn: delta (fp64 master)
     std::vector<DevBuf<float>> val32;     // iteration copy (fp32 storage mode)
+    // lcn: delta blocks transposed (targets x sources), the row pass's layout
+    std::vector<DevBuf<float>> val32T;
+    std::vector<DevBuf<double>> val64T;
     std::vector<DevBuf<double>> logk64;   // lcn: log K^sp at stored entries
     unsigned long long nnz = 0, stored = 0;
     // Nystrom / LCN

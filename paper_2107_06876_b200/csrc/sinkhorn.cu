@@ -229,58 +229,62 @@ __global__ void sparse_row_finalize_kernel(DevState* __restrict__ st, const doub
 }
 
 // ---------------------------------------------------------------------------
-// Streaming band kernels (warp-specialized). The band's work is a list of
-// items (bucket b, rows r0 .. r0 + nr, columns c0 .. c0 + cw): buckets with
-// more than kBandVec columns are cut into column tiles, big buckets into row
-// pieces; the items are assigned to CTAs on the host by longest-processing-
-// time greedy so every CTA streams about the same number of bytes. Per CTA:
-//   warp kWarps     bulk-copies the item's block rows (one copy per chunk of
-//                   whole rows, one per row for a column tile) through a ring
-//                   of kBandStages shared stages (mbarrier transaction counts);
-//   warp kWarps + 1 loads the item's scaling vector (tt_c = exp(log t - H_t)
-//                   for the row pass, ss_r = exp(log s - H_s) for the column
-//                   pass) and output indices into one of two slots;
-//   8 consumer warps only wait on mbarriers and compute from shared memory.
-// ROWS = true:  corr[src] = sum_c delta[r][c] tt[c]   (K side)
-// ROWS = false: corr[tgt] = sum_r delta[r][c] ss[r]   (K^T side)
-// An output split over K items (row sums of a bucket's column tiles, column
-// sums of its row pieces) goes through scratch: every piece writes its
-// partials, the piece that finishes last (arrival counter) adds them in piece
-// order, so results do not depend on CTA timing. Unsplit outputs are plain
-// stores. Two CTAs per SM (112 KB smem each) keep 16 consumer warps resident.
+// Streaming band kernels (warp-specialized). Both half-iterations stream
+// bucket blocks along their reduction dimension and keep the outputs in
+// registers ("output-stationary"):
+//   column pass (K^T s): blocks n_b x row_stride(m_b), stream = sources,
+//                        outputs = targets; corr_t[tgt] = sum_r delta ss_r
+//   row pass (K t):      transposed blocks m_b x row_stride(n_b), stream =
+//                        targets, outputs = sources; corr_s[src] = sum_c delta tt_c
+// The band's work is a list of items (bucket b, stream rows s0 .. s0 + ns,
+// output columns o0 .. o0 + ow): wide buckets are cut into <= kBandVec output
+// tiles, long ones into stream pieces; items are assigned to CTAs on the host
+// by longest-processing-time greedy so every CTA streams about the same bytes.
+// Per CTA:
+//   warp kWarps     bulk-copies the item's rows (one copy per chunk of whole
+//                   rows, one per row for an output tile) through a ring of
+//                   kBandStages shared stages (mbarrier transaction counts);
+//   warp kWarps + 1 loads the item's stream scalings (exp(log v - H)), output
+//                   indices and metadata into one of two slots;
+//   8 consumer warps: thread (g, q) owns output quad q of stream rows g, g+ng,
+//                   ... of every chunk, sums in registers; one shared-memory
+//                   combine of the ng groups per item.
+// An output split over K stream pieces goes through scratch: every piece writes
+// its partials, the piece that finishes last (arrival counter) adds them in
+// piece order, so results do not depend on CTA timing. Unsplit outputs are
+// plain stores. Two CTAs per SM (112 KB smem each) keep 16 consumer warps.
 // ---------------------------------------------------------------------------
 constexpr int kBandStages = 5;
 constexpr int kBandStageBytes = 16 * 1024;
-constexpr int kBandVec = 1024;  // max item columns / item rows
+constexpr int kBandVec = 1024;  // max item output width / item stream rows
 
 // per item slot, resolved by producer 2 so consumers never touch global
 // metadata (dependent L2 round trips at every item start otherwise)
 struct ItemMeta {
-    uint32_t nr, cw, split, pieces;
+    uint32_t ns, ow, split, pieces;
     double* part;  // this piece's scratch partials (split outputs), else null
 };
 
 struct BandSmem {
     unsigned char ring[kBandStages][kBandStageBytes];
-    double vec[2][kBandVec];    // tt (row pass) / ss (column pass) per item slot (fp32 storage: float view)
+    double vec[2][kBandVec];    // stream scalings per item slot (fp32 storage: float view)
     uint32_t out[2][kBandVec];  // output indices per item slot
-    double red[kBandVec];       // column pass: per-row-group partial sums (groups x row stride <= kBandVec)
+    double red[kBandVec];       // per-group partial sums (groups x row width <= kBandVec)
     ItemMeta meta[2];
     uint64_t full[kBandStages], empty[kBandStages], vfull[2], vempty[2];
     uint32_t last;              // this CTA combines a split output
 };
 
 struct BandItem {
-    uint32_t b, r0, nr, c0, cw;
-    uint32_t split[2];  // [0] row pass, [1] column pass: sid << 8 | piece, or ~0u
-    uint32_t pad;
+    uint32_t b, s0, ns, o0, ow, split;  // split = sid << 8 | piece, or ~0u
+    uint32_t pad[2];
 };
 
 struct BandWork {
     const BandItem* items;
     const uint32_t* cta_off;  // CTA c processes items cta_off[c] .. cta_off[c + 1] - 1
-    const uint2* splits;      // this pass: sid -> {scratch offset (doubles), pieces}
-    uint32_t* counters;       // this pass: sid -> arrivals (reset by the combining CTA)
+    const uint2* splits;      // sid -> {scratch offset (doubles), pieces}
+    uint32_t* counters;       // sid -> arrivals (reset by the combining CTA)
     double* scratch;
 };
 
@@ -314,8 +318,9 @@ __device__ __forceinline__ void band_combine(BandSmem& sm, const BandWork& wk, c
     }
 }
 
-// logv: the band's bucket-ordered copy of log t (row pass) / log s (column
-// pass), written by the low-rank pass that produced the log vector.
+// ROWS selects the row pass (transposed blocks). logv: the band's
+// bucket-ordered copy of the stream side's log vector (log t for the row pass,
+// log s for the column pass), written by the low-rank pass that produced it.
 template <typename T, bool ROWS>
 __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const DevState* __restrict__ st, BandView bv,
                                                                       BandWork wk, const T* __restrict__ vals,
@@ -328,6 +333,11 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
     const uint32_t i_beg = wk.cta_off[blockIdx.x], i_end = wk.cta_off[blockIdx.x + 1];
     if (i_beg == i_end) return;
     const double H = ROWS ? st->H_t : st->H_s;
+    // stream side / output side of this pass
+    const uint32_t* s_start = ROWS ? bv.tgt_start : bv.src_start;
+    const uint32_t* o_start = ROWS ? bv.src_start : bv.tgt_start;
+    const uint32_t* o_order = ROWS ? bv.src_order : bv.tgt_order;
+    const unsigned long long* boff = ROWS ? bv.blkT_off : bv.blk_off;
     if (tid == 0) {
         for (int k = 0; k < kBandStages; ++k) {
             mbar_init(&sm.full[k], 1);
@@ -341,28 +351,28 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
     }
     __syncthreads();
     if (warp == kWarps) {
-        // ---------------- producer 1: bulk copies of the item's block rows ----------------
+        // ---------------- producer 1: bulk copies of the item's rows ----------------
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
             bool wrapped = false;
             for (uint32_t it = i_beg; it < i_end; ++it) {
                 const BandItem item = wk.items[it];
-                const uint32_t ms = static_cast<uint32_t>(row_stride(bv.tgt_start[item.b + 1] - bv.tgt_start[item.b]));
-                const uint32_t ws = static_cast<uint32_t>(row_stride(item.cw));  // item row width in the ring
+                const uint32_t rs = static_cast<uint32_t>(row_stride(o_start[item.b + 1] - o_start[item.b]));
+                const uint32_t ws = static_cast<uint32_t>(row_stride(item.ow));  // item row width in the ring
                 const int R = band_rows_per_stage<T>(ws);
-                const T* blk = vals + bv.blk_off[item.b] + static_cast<unsigned long long>(item.r0) * ms + item.c0;
-                for (uint32_t r0 = 0; r0 < item.nr; r0 += R) {
-                    const uint32_t nr = item.nr - r0 < static_cast<uint32_t>(R) ? item.nr - r0 : static_cast<uint32_t>(R);
+                const T* blk = vals + boff[item.b] + static_cast<unsigned long long>(item.s0) * rs + item.o0;
+                for (uint32_t r0 = 0; r0 < item.ns; r0 += R) {
+                    const uint32_t nr = item.ns - r0 < static_cast<uint32_t>(R) ? item.ns - r0 : static_cast<uint32_t>(R);
                     if (wrapped) mbar_wait(&sm.empty[stage], phase ^ 1u);
                     const uint32_t rb = ws * static_cast<uint32_t>(sizeof(T));
                     mbar_arrive_expect_tx(&sm.full[stage], nr * rb);
-                    const T* src = blk + static_cast<unsigned long long>(r0) * ms;
-                    if (ws == ms) {
+                    const T* src = blk + static_cast<unsigned long long>(r0) * rs;
+                    if (ws == rs) {
                         bulk_g2s(sm.ring[stage], src, nr * rb, &sm.full[stage]);
                     } else {
                         for (uint32_t r = 0; r < nr; ++r)
-                            bulk_g2s(sm.ring[stage] + r * rb, src + static_cast<unsigned long long>(r) * ms, rb,
+                            bulk_g2s(sm.ring[stage] + r * rb, src + static_cast<unsigned long long>(r) * rs, rb,
                                      &sm.full[stage]);
                     }
                     if (++stage == kBandStages) {
@@ -376,42 +386,33 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
         return;
     }
     if (warp == kWarps + 1) {
-        // ---------------- producer 2: scaling values + output indices ----------------
+        // ---------------- producer 2: stream scalings, output indices, metadata ----------------
         int kb = 0;
         for (uint32_t it = i_beg; it < i_end; ++it, ++kb) {
             const BandItem item = wk.items[it];
-            const uint32_t sb = bv.src_start[item.b] + item.r0;
-            const uint32_t tb = bv.tgt_start[item.b] + item.c0;
-            const uint32_t count = ROWS ? static_cast<uint32_t>(row_stride(item.cw)) : item.nr;
-            const uint32_t valid = ROWS ? item.cw : item.nr;
-            const uint32_t v0 = ROWS ? tb : sb;
-            const uint32_t o0 = ROWS ? sb : tb;
-            const uint32_t nout = ROWS ? item.nr : item.cw;
-            const uint32_t* order = ROWS ? bv.src_order : bv.tgt_order;
+            const uint32_t v0 = s_start[item.b] + item.s0;
+            const uint32_t o0 = o_start[item.b] + item.o0;
             const int slot = kb & 1;
             if (kb >= 2) mbar_wait(&sm.vempty[slot], ((kb >> 1) - 1) & 1);
             if constexpr (sizeof(T) == 4) {
                 // fp32 storage: the scalings enter fp32 products (values in (0, 1])
                 float* vf = reinterpret_cast<float*>(sm.vec[slot]);
-                for (uint32_t c = lane; c < count; c += 32)
-                    vf[c] = c < valid ? static_cast<float>(exp(logv[v0 + c] - H)) : 0.0f;
+                for (uint32_t c = lane; c < item.ns; c += 32) vf[c] = static_cast<float>(exp(logv[v0 + c] - H));
             } else {
-                for (uint32_t c = lane; c < count; c += 32)
-                    sm.vec[slot][c] = c < valid ? exp(logv[v0 + c] - H) : 0.0;
+                for (uint32_t c = lane; c < item.ns; c += 32) sm.vec[slot][c] = exp(logv[v0 + c] - H);
             }
-            for (uint32_t c = lane; c < nout; c += 32) sm.out[slot][c] = order[o0 + c];
+            for (uint32_t c = lane; c < item.ow; c += 32) sm.out[slot][c] = o_order[o0 + c];
             if (lane == 0) {
                 ItemMeta mt;
-                mt.nr = item.nr;
-                mt.cw = item.cw;
-                mt.split = item.split[ROWS ? 0 : 1];
+                mt.ns = item.ns;
+                mt.ow = item.ow;
+                mt.split = item.split;
                 mt.pieces = 0;
                 mt.part = nullptr;
-                if (mt.split != 0xffffffffu) {
-                    const uint2 sp = wk.splits[mt.split >> 8];
-                    const uint32_t count = ROWS ? item.nr : item.cw;  // partials per piece
+                if (item.split != 0xffffffffu) {
+                    const uint2 sp = wk.splits[item.split >> 8];
                     mt.pieces = sp.y;
-                    mt.part = wk.scratch + sp.x + static_cast<size_t>(mt.split & 0xffu) * count;
+                    mt.part = wk.scratch + sp.x + static_cast<size_t>(item.split & 0xffu) * item.ow;
                 }
                 sm.meta[slot] = mt;
             }
@@ -427,88 +428,24 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
         const int slot = kb & 1;
         mbar_wait(&sm.vfull[slot], (kb >> 1) & 1);
         const ItemMeta mt = sm.meta[slot];
-        const uint32_t ws = static_cast<uint32_t>(row_stride(mt.cw));
+        const uint32_t ws = static_cast<uint32_t>(row_stride(mt.ow));
         const uint32_t nq = ws / 4;
         const int R = band_rows_per_stage<T>(ws);
-        // row pass, split: partial row sums go to scratch
-        double* rpart = ROWS ? mt.part : nullptr;
-        // column pass mapping: groups of nq threads, thread (g, q) owns quad q
-        // of rows g, g + ng, ... of every chunk; sums stay in registers
+        // groups of nq threads: thread (g, q) owns output quad q of stream rows
+        // g, g + ng, ... of every chunk
         const uint32_t ng = nq >= static_cast<uint32_t>(kThreads) ? 1u : kThreads / nq;
         const uint32_t g = static_cast<uint32_t>(tid) / nq, q = static_cast<uint32_t>(tid) % nq;
-        const bool col_own = g < ng;
+        const bool own = g < ng;
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         const uint32_t* outi = sm.out[slot];
-        for (uint32_t r0 = 0; r0 < mt.nr; r0 += R) {
-            const uint32_t nr = mt.nr - r0 < static_cast<uint32_t>(R) ? mt.nr - r0 : static_cast<uint32_t>(R);
+        for (uint32_t r0 = 0; r0 < mt.ns; r0 += R) {
+            const uint32_t nr = mt.ns - r0 < static_cast<uint32_t>(R) ? mt.ns - r0 : static_cast<uint32_t>(R);
             mbar_wait(&sm.full[stage], phase);
             const T* blk = reinterpret_cast<const T*>(sm.ring[stage]);
-            if constexpr (ROWS) {
-                // two rows per warp step: independent load/FMA chains interleave
-                for (uint32_t r = warp; r < nr; r += 2 * kWarps) {
-                    const uint32_t r2 = r + kWarps;
-                    const bool two = r2 < nr;
-                    const T* row = blk + r * ws;
-                    const T* row2 = blk + (two ? r2 : r) * ws;
-                    double acc, acc2;
-                    int l1, l2;  // lanes holding the two sums
-                    if constexpr (sizeof(T) == 4) {
-                        // fp32 products and row partials (<= kBandVec terms), widened once
-                        const float* vf = reinterpret_cast<const float*>(sm.vec[slot]);
-                        float f = 0.0f, f2 = 0.0f;
-                        for (uint32_t qq = lane; qq < nq; qq += 32) {
-                            const float4 tq = *reinterpret_cast<const float4*>(vf + 4 * qq);
-                            const float4 x = *reinterpret_cast<const float4*>(row + 4 * qq);
-                            const float4 y = *reinterpret_cast<const float4*>(row2 + 4 * qq);
-                            f = fmaf(x.x, tq.x, f); f = fmaf(x.y, tq.y, f);
-                            f = fmaf(x.z, tq.z, f); f = fmaf(x.w, tq.w, f);
-                            f2 = fmaf(y.x, tq.x, f2); f2 = fmaf(y.y, tq.y, f2);
-                            f2 = fmaf(y.z, tq.z, f2); f2 = fmaf(y.w, tq.w, f2);
-                        }
-                        // two-row transpose reduction: lanes < 16 end with row r's
-                        // sum, lanes >= 16 with row r2's (5 shuffles, not 10)
-                        const bool hi = lane & 16;
-                        float x = (hi ? f2 : f) + __shfl_xor_sync(0xffffffffu, hi ? f : f2, 16);
-#pragma unroll
-                        for (int o = 8; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-                        acc = x;
-                        acc2 = x;
-                        l1 = 0;
-                        l2 = 16;
-                    } else {
-                        const double* vec = sm.vec[slot];
-                        acc = 0.0;
-                        acc2 = 0.0;
-                        for (uint32_t qq = lane; qq < nq; qq += 32) {
-                            const double2 t01 = *reinterpret_cast<const double2*>(vec + 4 * qq);
-                            const double2 t23 = *reinterpret_cast<const double2*>(vec + 4 * qq + 2);
-                            const double2 x0 = *reinterpret_cast<const double2*>(row + 4 * qq);
-                            const double2 x1 = *reinterpret_cast<const double2*>(row + 4 * qq + 2);
-                            const double2 y0 = *reinterpret_cast<const double2*>(row2 + 4 * qq);
-                            const double2 y1 = *reinterpret_cast<const double2*>(row2 + 4 * qq + 2);
-                            acc += x0.x * t01.x + x0.y * t01.y + x1.x * t23.x + x1.y * t23.y;
-                            acc2 += y0.x * t01.x + y0.y * t01.y + y1.x * t23.x + y1.y * t23.y;
-                        }
-#pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) {
-                            acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                            acc2 += __shfl_xor_sync(0xffffffffu, acc2, o);
-                        }
-                        l1 = 0;
-                        l2 = 1;
-                    }
-                    if (lane == l1) {
-                        if (rpart) rpart[r0 + r] = acc;
-                        else corr[outi[r0 + r]] = acc;
-                    }
-                    if (lane == l2 && two) {
-                        if (rpart) rpart[r0 + r2] = acc2;
-                        else corr[outi[r0 + r2]] = acc2;
-                    }
-                }
-            } else if (col_own) {
+            if (own) {
                 const T* p = blk + 4 * q;
                 if constexpr (sizeof(T) == 4) {
+                    // fp32 products and per-chunk partials, widened once per chunk
                     const float* vf = reinterpret_cast<const float*>(sm.vec[slot]) + r0;
                     float f0 = 0.0f, f1 = 0.0f, f2 = 0.0f, f3 = 0.0f;
                     for (uint32_t r = g; r < nr; r += ng) {
@@ -535,25 +472,21 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
                 phase ^= 1u;
             }
         }
-        if constexpr (ROWS) {
-            if (rpart) band_combine(sm, wk, mt, mt.nr, outi, corr, tid);
-        } else {
-            // combine the row groups: red[g * ws + c], one thread per column
-            if (col_own) {
-                double* o = sm.red + g * ws + 4 * q;
-                o[0] = a0; o[1] = a1; o[2] = a2; o[3] = a3;
-            }
-            consumers_sync();
-            double* cpart = mt.part;
-            for (uint32_t c = tid; c < mt.cw; c += kThreads) {
-                double v = 0.0;
-                for (uint32_t gg = 0; gg < ng; ++gg) v += sm.red[gg * ws + c];
-                if (cpart) cpart[c] = v;
-                else corr[outi[c]] = v;
-            }
-            if (cpart) band_combine(sm, wk, mt, mt.cw, outi, corr, tid);
-            consumers_sync();  // red is rewritten by the next item
+        // combine the groups: red[g * ws + c], one thread per output
+        if (own) {
+            double* o = sm.red + g * ws + 4 * q;
+            o[0] = a0; o[1] = a1; o[2] = a2; o[3] = a3;
         }
+        consumers_sync();
+        double* part = mt.part;
+        for (uint32_t c = tid; c < mt.ow; c += kThreads) {
+            double v = 0.0;
+            for (uint32_t gg = 0; gg < ng; ++gg) v += sm.red[gg * ws + c];
+            if (part) part[c] = v;
+            else corr[outi[c]] = v;
+        }
+        if (part) band_combine(sm, wk, mt, mt.ow, outi, corr, tid);
+        consumers_sync();  // red is rewritten by the next item
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.vempty[slot]);
     }
@@ -1124,24 +1057,20 @@ struct Solver {
     std::vector<cudaEvent_t> evs;                           // phase events (profiling)
     size_t mark_base = 0;
     size_t smem = 0;                                        // low-rank pass stage ring
-    // band work: streaming items (row pieces x column tiles of the buckets),
-    // LPT-assigned to CTAs, with the split tables of both passes
-    struct SplitSet {
-        DevBuf<uint2> splits;
-        DevBuf<uint32_t> counters;
-        DevBuf<double> scratch;
-    };
-    struct BandPlan {
+    // band work per pass ([0] row pass on the transposed blocks, [1] column
+    // pass): items (stream pieces x output tiles of the buckets) LPT-assigned
+    // to CTAs, with the pass's split table
+    struct PassPlan {
         DevBuf<BandItem> items;
-        DevBuf<uint32_t> cta_off;
-        SplitSet pass[2];  // 0 row pass, 1 column pass
+        DevBuf<uint32_t> cta_off, counters;
+        DevBuf<uint2> splits;
+        DevBuf<double> scratch;
         int nitems = 0;
-        BandWork work(int p) {
-            return BandWork{items.get(), cta_off.get(), pass[p].splits.get(), pass[p].counters.get(),
-                            pass[p].scratch.get()};
+        BandWork work() {
+            return BandWork{items.get(), cta_off.get(), splits.get(), counters.get(), scratch.get()};
         }
     };
-    std::vector<BandPlan> plans;
+    std::vector<PassPlan> plans[2];
     int band_grid = 0;
 
     explicit Solver(Op& o) : op(o), ctx(*o.ctx), s(o.ctx->stream), n(o.n), m(o.m), l(static_cast<int>(o.l)) {
@@ -1191,109 +1120,106 @@ struct Solver {
             CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, band_stream_kernel<float, true>, kThreads + 64,
                                                                   sizeof(BandSmem)));
         band_grid = std::max(occ, 1) * ctx.num_sms;
-        const size_t esz = op.fp64 ? 8 : 4;
-        // cost model (bytes): streamed bytes + per-row and per-item overheads
-        auto cost_of = [&](size_t nr, size_t ws) { return double(nr * ws * esz) + 256.0 * nr + 4096.0; };
         for (const Band& B : op.bands) {
             std::vector<uint32_t> w(B.n_work);
             if (B.n_work) B.work.download(w.data(), B.n_work, s);
             ctx.sync();
-            double total = 0.0;
-            for (uint32_t k : w) {
-                const size_t nb = B.h_src_start[k + 1] - B.h_src_start[k];
-                const size_t mb = B.h_tgt_start[k + 1] - B.h_tgt_start[k];
-                if (nb && mb) total += cost_of(nb, row_stride(mb));
-            }
-            const double cap = std::max(total / band_grid / 2.0, 65536.0);
-            struct Piece { BandItem it; double cost; };
-            std::vector<Piece> pieces;
-            std::vector<uint2> splits[2];
-            size_t scratch[2] = {0, 0};
-            for (uint32_t k : w) {
-                const size_t nb = B.h_src_start[k + 1] - B.h_src_start[k];
-                const size_t mb = B.h_tgt_start[k + 1] - B.h_tgt_start[k];
-                if (nb == 0 || mb == 0) continue;
-                const size_t ms = row_stride(mb);
-                const size_t nct = ceil_div(mb, kBandVec);  // column tiles
-                const size_t wmax = std::min<size_t>(ms, kBandVec);
-                // row pieces: multiple of 8 rows (128-byte aligned chunk starts), <= kBandVec
-                size_t K = static_cast<size_t>(std::ceil(cost_of(nb, wmax) / cap));
-                K = std::max<size_t>(K, ceil_div(nb, kBandVec));
-                size_t pr = (ceil_div(nb, std::max<size_t>(K, 1)) + 7) & ~size_t(7);
-                pr = std::min<size_t>(std::max<size_t>(pr, 8), kBandVec);
-                K = ceil_div(nb, pr);
-                if (K > 255 || nct > 255) throw Status(2, "lcn: bucket split into more than 255 pieces");
-                // row-pass splits: one per row piece when there are several column tiles
-                std::vector<uint32_t> rsid(K, 0xffffffffu), csid(nct, 0xffffffffu);
-                if (nct > 1)
-                    for (size_t j = 0; j < K; ++j) {
-                        const size_t nr = std::min(pr, nb - j * pr);
-                        rsid[j] = static_cast<uint32_t>(splits[0].size());
-                        splits[0].push_back(make_uint2(static_cast<uint32_t>(scratch[0]), static_cast<uint32_t>(nct)));
-                        scratch[0] += nct * nr;
-                    }
-                // column-pass splits: one per column tile when there are several row pieces
-                if (K > 1)
-                    for (size_t ct = 0; ct < nct; ++ct) {
-                        const size_t cw = std::min<size_t>(kBandVec, mb - ct * kBandVec);
-                        csid[ct] = static_cast<uint32_t>(splits[1].size());
-                        splits[1].push_back(make_uint2(static_cast<uint32_t>(scratch[1]), static_cast<uint32_t>(K)));
-                        scratch[1] += K * cw;
-                    }
-                for (size_t ct = 0; ct < nct; ++ct) {
-                    const size_t c0 = ct * kBandVec, cw = std::min<size_t>(kBandVec, mb - c0);
-                    for (size_t j = 0; j < K; ++j) {
-                        const size_t r0 = j * pr, nr = std::min(pr, nb - r0);
-                        BandItem it{};
-                        it.b = k;
-                        it.r0 = static_cast<uint32_t>(r0);
-                        it.nr = static_cast<uint32_t>(nr);
-                        it.c0 = static_cast<uint32_t>(c0);
-                        it.cw = static_cast<uint32_t>(cw);
-                        it.split[0] = nct > 1 ? (rsid[j] << 8) | static_cast<uint32_t>(ct) : 0xffffffffu;
-                        it.split[1] = K > 1 ? (csid[ct] << 8) | static_cast<uint32_t>(j) : 0xffffffffu;
-                        pieces.push_back({it, cost_of(nr, row_stride(cw))});
-                    }
-                }
-            }
-            if (scratch[0] > 0xffffffffull || scratch[1] > 0xffffffffull)
-                throw Status(2, "lcn: band split scratch above 2^32 entries");
-            // longest-processing-time greedy: largest piece to the least loaded CTA
-            std::stable_sort(pieces.begin(), pieces.end(), [](const Piece& x, const Piece& y) { return x.cost > y.cost; });
-            using Load = std::pair<double, int>;
-            std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
-            for (int c = 0; c < band_grid; ++c) heap.push({0.0, c});
-            std::vector<std::vector<BandItem>> per(band_grid);
-            for (const Piece& pc : pieces) {
-                Load ld = heap.top();
-                heap.pop();
-                per[ld.second].push_back(pc.it);
-                ld.first += pc.cost;
-                heap.push(ld);
-            }
-            std::vector<BandItem> items;
-            std::vector<uint32_t> off(band_grid + 1, 0);
-            for (int c = 0; c < band_grid; ++c) {
-                off[c] = static_cast<uint32_t>(items.size());
-                items.insert(items.end(), per[c].begin(), per[c].end());
-            }
-            off[band_grid] = static_cast<uint32_t>(items.size());
-            BandPlan P;
-            P.nitems = static_cast<int>(items.size());
-            P.items.resize(std::max<size_t>(items.size(), 1));
-            P.cta_off.resize(off.size());
-            if (!items.empty()) P.items.upload(items.data(), items.size(), s);
-            P.cta_off.upload(off.data(), off.size(), s);
-            for (int p = 0; p < 2; ++p) {
-                P.pass[p].splits.resize(std::max<size_t>(splits[p].size(), 1));
-                P.pass[p].counters.resize(std::max<size_t>(splits[p].size(), 1));
-                P.pass[p].scratch.resize(std::max<size_t>(scratch[p], 1));
-                if (!splits[p].empty()) P.pass[p].splits.upload(splits[p].data(), splits[p].size(), s);
-                P.pass[p].counters.zero(s);
-            }
-            plans.push_back(std::move(P));
+            plans[0].push_back(plan_pass(B, w, true));
+            plans[1].push_back(plan_pass(B, w, false));
         }
         ctx.sync();
+    }
+
+    // Items of one pass: per bucket, output tiles of <= kBandVec columns and
+    // stream pieces (multiples of 8 rows, <= kBandVec, sized so no piece
+    // exceeds half a CTA's share), then longest-processing-time greedy.
+    PassPlan plan_pass(const Band& B, const std::vector<uint32_t>& w, bool rows) {
+        const size_t esz = op.fp64 ? 8 : 4;
+        // cost model (bytes): streamed bytes + per-row and per-item overheads
+        auto cost_of = [&](size_t nr, size_t ws) { return double(nr * ws * esz) + 64.0 * nr + 4096.0; };
+        auto lens = [&](uint32_t k, size_t& sl, size_t& ol) {
+            const size_t nb = B.h_src_start[k + 1] - B.h_src_start[k];
+            const size_t mb = B.h_tgt_start[k + 1] - B.h_tgt_start[k];
+            sl = rows ? mb : nb;
+            ol = rows ? nb : mb;
+        };
+        double total = 0.0;
+        for (uint32_t k : w) {
+            size_t sl, ol;
+            lens(k, sl, ol);
+            if (sl && ol) total += cost_of(sl, row_stride(ol));
+        }
+        const double cap = std::max(total / band_grid / 2.0, 65536.0);
+        struct Piece { BandItem it; double cost; };
+        std::vector<Piece> pieces;
+        std::vector<uint2> splits;
+        size_t scratch = 0;
+        for (uint32_t k : w) {
+            size_t sl, ol;
+            lens(k, sl, ol);
+            if (sl == 0 || ol == 0) continue;
+            const size_t rs = row_stride(ol);
+            const size_t nct = ceil_div(ol, kBandVec);  // output tiles
+            const size_t wmax = std::min<size_t>(rs, kBandVec);
+            size_t K = static_cast<size_t>(std::ceil(cost_of(sl, wmax) / cap));
+            K = std::max<size_t>(K, ceil_div(sl, kBandVec));
+            size_t pr = (ceil_div(sl, std::max<size_t>(K, 1)) + 7) & ~size_t(7);
+            pr = std::min<size_t>(std::max<size_t>(pr, 8), kBandVec);
+            K = ceil_div(sl, pr);
+            if (K > 255) throw Status(2, "lcn: bucket split into more than 255 pieces");
+            for (size_t ct = 0; ct < nct; ++ct) {
+                const size_t o0 = ct * kBandVec, ow = std::min<size_t>(kBandVec, ol - o0);
+                uint32_t sid = 0xffffffffu;
+                if (K > 1) {
+                    sid = static_cast<uint32_t>(splits.size());
+                    splits.push_back(make_uint2(static_cast<uint32_t>(scratch), static_cast<uint32_t>(K)));
+                    scratch += K * ow;
+                }
+                for (size_t j = 0; j < K; ++j) {
+                    const size_t s0 = j * pr, ns = std::min(pr, sl - s0);
+                    BandItem it{};
+                    it.b = k;
+                    it.s0 = static_cast<uint32_t>(s0);
+                    it.ns = static_cast<uint32_t>(ns);
+                    it.o0 = static_cast<uint32_t>(o0);
+                    it.ow = static_cast<uint32_t>(ow);
+                    it.split = K > 1 ? (sid << 8) | static_cast<uint32_t>(j) : 0xffffffffu;
+                    pieces.push_back({it, cost_of(ns, row_stride(ow))});
+                }
+            }
+        }
+        if (scratch > 0xffffffffull) throw Status(2, "lcn: band split scratch above 2^32 entries");
+        std::stable_sort(pieces.begin(), pieces.end(), [](const Piece& x, const Piece& y) { return x.cost > y.cost; });
+        using Load = std::pair<double, int>;
+        std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
+        for (int c = 0; c < band_grid; ++c) heap.push({0.0, c});
+        std::vector<std::vector<BandItem>> per(band_grid);
+        for (const Piece& pc : pieces) {
+            Load ld = heap.top();
+            heap.pop();
+            per[ld.second].push_back(pc.it);
+            ld.first += pc.cost;
+            heap.push(ld);
+        }
+        std::vector<BandItem> items;
+        std::vector<uint32_t> off(band_grid + 1, 0);
+        for (int c = 0; c < band_grid; ++c) {
+            off[c] = static_cast<uint32_t>(items.size());
+            items.insert(items.end(), per[c].begin(), per[c].end());
+        }
+        off[band_grid] = static_cast<uint32_t>(items.size());
+        PassPlan P;
+        P.nitems = static_cast<int>(items.size());
+        P.items.resize(std::max<size_t>(items.size(), 1));
+        P.cta_off.resize(off.size());
+        if (!items.empty()) P.items.upload(items.data(), items.size(), s);
+        P.cta_off.upload(off.data(), off.size(), s);
+        P.splits.resize(std::max<size_t>(splits.size(), 1));
+        P.counters.resize(std::max<size_t>(splits.size(), 1));
+        P.scratch.resize(std::max<size_t>(scratch, 1));
+        if (!splits.empty()) P.splits.upload(splits.data(), splits.size(), s);
+        P.counters.zero(s);
+        return P;
     }
 
     cudaEvent_t ev(size_t i) {
@@ -1312,6 +1238,11 @@ struct Solver {
     const T* band_vals(int b) const {
         if constexpr (std::is_same_v<T, float>) return op.val32[b].get();
         else return op.val64[b].get();
+    }
+    template <typename T>
+    const T* band_valsT(int b) const {
+        if constexpr (std::is_same_v<T, float>) return op.val32T[b].get();
+        else return op.val64T[b].get();
     }
     template <typename T>
     const T* U() const {
@@ -1434,11 +1365,13 @@ struct Solver {
     template <typename T, bool ROWS>
     void bands(std::vector<DevBuf<double>>& logvp, std::vector<DevBuf<double>>& corr) {
         if (op.kind != 3) return;
-        for (size_t b = 0; b < op.bands.size(); ++b)
-            if (plans[b].nitems)
+        for (size_t b = 0; b < op.bands.size(); ++b) {
+            PassPlan& P = plans[ROWS ? 0 : 1][b];
+            if (P.nitems)
                 band_stream_kernel<T, ROWS><<<band_grid, kThreads + 64, sizeof(BandSmem), s>>>(
-                    st.get(), op.view(b), plans[b].work(ROWS ? 0 : 1), band_vals<T>(b), logvp[b].get(),
+                    st.get(), op.view(b), P.work(), ROWS ? band_valsT<T>(b) : band_vals<T>(b), logvp[b].get(),
                     corr[b].get());
+        }
     }
     template <typename T>
     void lcn_rows() { bands<T, true>(ltp, corr_s); }
