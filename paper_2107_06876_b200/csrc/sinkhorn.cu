@@ -586,6 +586,12 @@ __device__ __forceinline__ double fin_log(double y) {
     }
 }
 template <typename T>
+__device__ __forceinline__ double fin_exp(double x) {  // row marginal exp(log s + log Kt)
+    if constexpr (sizeof(T) == 4)
+        if (x > -80.0 && x < 80.0) return static_cast<double>(__expf(static_cast<float>(x)));
+    return exp(x);
+}
+template <typename T>
 __device__ __forceinline__ double fin_exp_neg(double x) {  // x <= 0
     if constexpr (sizeof(T) == 4) return x < -87.0 ? 0.0 : static_cast<double>(__expf(static_cast<float>(x)));
     else return exp(x);
@@ -652,39 +658,45 @@ __global__ void __launch_bounds__(kThreads + 64, 2) lowrank_pass_kernel(const T*
     }
     __syncthreads();
     if (warp == kWarps) {
-        // ---------------- producer ----------------
-        if (lane == 0) {
-            const double* sv[kMaxBands + 3];
-            int nsv = 0;
-            if (a.mode == 2) {
-                sv[nsv++] = a.in;
-            } else {
-                for (int k = 0; k < nc; ++k) sv[nsv++] = a.corr[k];
-                sv[nsv++] = a.mode == 0 ? a.log_marg : nullptr;
-                sv[nsv++] = (a.mode == 0 && SIDE == 0 && a.with_err) ? a.log_cur : nullptr;
-                sv[nsv++] = (a.mode == 0 && SIDE == 0 && a.with_err) ? a.marg : nullptr;
-            }
-            int it = 0;
-            for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-                const int stage = it % S;
+        // ---------------- producer: one lane per stream ----------------
+        // lanes 0 .. kMaxBands + 2: scalar streams [corr_0 .. corr_{nc-1}]
+        // [log marg] [log cur] [marg] (mode 2: [in]) into slot `lane`; lanes
+        // 16 .. 16 + np - 1: the band position streams; lane 0 also copies the
+        // factor tile. Pointers come straight from the kernel parameters (no
+        // local-memory array), copies are issued by all lanes at once.
+        const double* sp = nullptr;
+        if (a.mode == 2) {
+            if (lane == 0) sp = a.in;
+        } else if (lane < nc) {
+            sp = a.corr[lane];
+        } else if (lane == nc) {
+            sp = a.mode == 0 ? a.log_marg : nullptr;
+        } else if (lane == nc + 1) {
+            sp = (a.mode == 0 && SIDE == 0 && a.with_err) ? a.log_cur : nullptr;
+        } else if (lane == nc + 2) {
+            sp = (a.mode == 0 && SIDE == 0 && a.with_err) ? a.marg : nullptr;
+        }
+        const uint32_t* pp = (lane >= 16 && lane - 16 < np) ? a.pos[lane - 16] : nullptr;
+        int it = 0;
+        for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            const int stage = it % S;
+            const long long r0 = tile * kRT;
+            const int nr = static_cast<int>(a.rows - r0 < kRT ? a.rows - r0 : kRT);
+            const uint32_t sbytes = static_cast<uint32_t>((nr * 8 + 15) & ~15);  // vectors padded to kRT rows
+            const uint32_t pbytes = static_cast<uint32_t>((nr * 4 + 15) & ~15);  // pos arrays padded by 16
+            const uint32_t mine = (sp ? sbytes : 0u) + (pp ? pbytes : 0u) + (lane == 0 ? nr * frow : 0u);
+            const uint32_t bytes = __reduce_add_sync(0xffffffffu, mine);
+            if (lane == 0) {
                 if (it >= S) mbar_wait(&empty[stage], ((it / S) - 1) & 1);
-                const long long r0 = tile * kRT;
-                const int nr = static_cast<int>(a.rows - r0 < kRT ? a.rows - r0 : kRT);
-                unsigned char* base = dyn + stage * stage_bytes;
-                const uint32_t sbytes = static_cast<uint32_t>((nr * 8 + 15) & ~15);  // vectors padded to kRT rows
-                uint32_t bytes = nr * frow;
-                for (int k = 0; k < nsv; ++k)
-                    if (sv[k]) bytes += sbytes;
-                bytes += np * static_cast<uint32_t>((nr * 4 + 15) & ~15);
                 mbar_arrive_expect_tx(&full[stage], bytes);
-                bulk_g2s(base, F + r0 * a.lp, nr * frow, &full[stage]);
-                double* sc = reinterpret_cast<double*>(base + static_cast<size_t>(kRT) * frow);
-                for (int k = 0; k < nsv; ++k)
-                    if (sv[k]) bulk_g2s(sc + k * kRT, sv[k] + r0, sbytes, &full[stage]);
-                uint32_t* ps = reinterpret_cast<uint32_t*>(sc + (kMaxBands + 3) * kRT);
-                const uint32_t pbytes = static_cast<uint32_t>((nr * 4 + 15) & ~15);  // pos arrays padded by 16
-                for (int k = 0; k < np; ++k) bulk_g2s(ps + k * kRT, a.pos[k] + r0, pbytes, &full[stage]);
             }
+            __syncwarp();
+            unsigned char* base = dyn + stage * stage_bytes;
+            double* sc = reinterpret_cast<double*>(base + static_cast<size_t>(kRT) * frow);
+            uint32_t* ps = reinterpret_cast<uint32_t*>(sc + (kMaxBands + 3) * kRT);
+            if (lane == 0) bulk_g2s(base, F + r0 * a.lp, nr * frow, &full[stage]);
+            if (sp) bulk_g2s(sc + lane * kRT, sp + r0, sbytes, &full[stage]);
+            if (pp) bulk_g2s(ps + (lane - 16) * kRT, pp + r0, pbytes, &full[stage]);
         }
         return;
     }
@@ -724,7 +736,7 @@ __global__ void __launch_bounds__(kThreads + 64, 2) lowrank_pass_kernel(const T*
                         live = false;
                     } else {
                         if (SIDE == 0 && a.with_err) {
-                            const double rm = exp(scal[(nc + 1) * kRT + lane] + k);
+                            const double rm = fin_exp<T>(scal[(nc + 1) * kRT + lane] + k);
                             a.row_marg[i] = rm;
                             err += fabs(rm - scal[(nc + 2) * kRT + lane]);
                         }
@@ -829,11 +841,86 @@ __global__ void __launch_bounds__(kThreads + 64, 2) lowrank_pass_kernel(const T*
         if (lane == 0) mbar_arrive(&empty[jstage]);
     };
     int it = 0, prev_nr = 0;
+    // fp32 storage with <= 2 columns per thread: the tile's factor values stay
+    // in registers from the dot to the lagged accumulate, so the stage goes
+    // back to the producer right after the dot (two of three stages prefetch)
+    constexpr bool kReg = sizeof(T) == 4 && CPT <= 2;
+    float uc[kReg ? kRT : 1][CPT], up[kReg ? kRT : 1][CPT];
+    if constexpr (kReg) {
+#pragma unroll
+        for (int r = 0; r < kRT; ++r)
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) up[r][k] = 0.0f;
+    }
+    auto accumulate_reg = [&](int j, int jnr) {
+        const int jbuf = j & 1;
+        mbar_wait(&wready[jbuf], (j >> 1) & 1);
+        if (own) {
+            const double sc = sc_s[jbuf];
+            float pa[CPT];
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) {
+                acc[k] *= sc;
+                pa[k] = 0.0f;
+            }
+#pragma unroll
+            for (int r = 0; r < kRT; ++r) {
+                const float w = w_f[jbuf][r];  // 0 for rows past jnr
+#pragma unroll
+                for (int k = 0; k < CPT; ++k) pa[k] = fmaf(up[r][k], w, pa[k]);
+            }
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) acc[k] += static_cast<double>(pa[k]);
+        }
+        (void)jnr;
+    };
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int stage = it % S, buf = it & 1;
         const long long r0 = tile * kRT;
         const int nr = static_cast<int>(a.rows - r0 < kRT ? a.rows - r0 : kRT);
         mbar_wait(&full[stage], (it / S) & 1);
+        if constexpr (kReg) {
+            const float* fsf = reinterpret_cast<const float*>(dyn + stage * stage_bytes);
+#pragma unroll
+            for (int r = 0; r < kRT; ++r) {
+                if (own && r < nr) {
+                    if constexpr (CPT == 2) {
+                        const float2 x = *reinterpret_cast<const float2*>(fsf + r * a.lp + c0);
+                        uc[r][0] = x.x;
+                        uc[r][CPT - 1] = x.y;
+                    } else {
+                        uc[r][0] = fsf[r * a.lp + c0];
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < CPT; ++k) uc[r][k] = 0.0f;  // never stale smem (could be NaN)
+                }
+            }
+            if (a.mode != 2) {
+                if (a.mode == 1 && it >= 2) mbar_wait(&wready[buf], ((it - 2) >> 1) & 1);
+                float dp[kRT];
+#pragma unroll
+                for (int r = 0; r < kRT; ++r) {
+                    float d = uc[r][0] * mid_hi[0];
+#pragma unroll
+                    for (int k = 1; k < CPT; ++k) d = fmaf(uc[r][k], mid_hi[k], d);
+                    dp[r] = d;
+                }
+                const float wsum = transpose_reduce16(dp, lane);
+                if ((lane & 1) == 0) red[buf][warp][(lane >> 1) & 15] = static_cast<double>(wsum);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&ydone[buf]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);  // the tile lives in registers now
+            if (a.mode != 1 && it > 0) accumulate_reg(it - 1, prev_nr);  // overlaps the finalize of tile `it`
+#pragma unroll
+            for (int r = 0; r < kRT; ++r)
+#pragma unroll
+                for (int k = 0; k < CPT; ++k) up[r][k] = uc[r][k];
+            prev_nr = nr;
+            continue;
+        }
         if (a.mode != 2) {
             // red[buf] is free once the finalize warp is done with tile it - 2
             // (implied by the accumulate wait below except in mode 1)
@@ -851,15 +938,9 @@ __global__ void __launch_bounds__(kThreads + 64, 2) lowrank_pass_kernel(const T*
                     float d = 0.0f;
                     if (own) {
                         const float* u = reinterpret_cast<const float*>(fs) + r * a.lp + c0;
-                        if constexpr (CPT == 4) {
-                            const float4 x = *reinterpret_cast<const float4*>(u);
-                            d = fmaf(x.w, mid_hi[3], fmaf(x.z, mid_hi[2], fmaf(x.y, mid_hi[1], x.x * mid_hi[0])));
-                        } else if constexpr (CPT == 2) {
-                            const float2 x = *reinterpret_cast<const float2*>(u);
-                            d = fmaf(x.y, mid_hi[1], x.x * mid_hi[0]);
-                        } else {
-                            d = u[0] * mid_hi[0];
-                        }
+                        const float4 x = *reinterpret_cast<const float4*>(u);
+                        d = fmaf(x.w, mid_hi[CPT - 1], fmaf(x.z, mid_hi[CPT > 2 ? 2 : 0],
+                                 fmaf(x.y, mid_hi[CPT > 1 ? 1 : 0], x.x * mid_hi[0])));
                     }
                     dp[r] = d;
                 }
@@ -892,7 +973,10 @@ __global__ void __launch_bounds__(kThreads + 64, 2) lowrank_pass_kernel(const T*
         prev_nr = nr;
     }
     if (a.mode == 1) return;
-    if (it > 0) accumulate(it - 1, prev_nr);
+    if (it > 0) {
+        if constexpr (kReg) accumulate_reg(it - 1, prev_nr);
+        else accumulate(it - 1, prev_nr);
+    }
     consumers_sync();
     const double hb = h_fin;  // final CTA shift (written before the last wready)
 #pragma unroll
