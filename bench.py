@@ -196,6 +196,18 @@ def run_reference(args, rank, world):
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
+def count_launches(step):
+    """Kernels of ours (lcnb::) launched by one step, counted from a CUPTI
+    trace of one extra, untimed step (torch.profiler)."""
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            step()
+        names = [e.name for e in prof.events() if e.device_type.name == "CUDA"]
+        return sum(1 for nm in names if "lcnb" in nm)
+    except Exception:
+        return None
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -248,11 +260,7 @@ def run_ours(args, rank, world, local_rank):
 
     for _ in range(args.warmup):
         res = step()
-    # phase breakdown (separate profiled step, not timed)
-    ctx.set_profile(True)
-    pres = step()
-    phase_ms, phase_it = pres.phase_ms()
-    ctx.set_profile(False)
+    launches_per_step = count_launches(step)
 
     clocks = Clocks(int(os.environ.get("LCN_GPU_INDEX", local_rank)))
     if world > 1:
@@ -264,6 +272,19 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(args.steps):
         res = step()
     t1.record(stream)
+    torch.cuda.synchronize()
+    # kernel durations: a second timed region of the same K steps with phase
+    # events recorded by the library on its own stream between its launches
+    # (kept out of the region `value` is measured on: ~4% event overhead)
+    ctx.set_profile(True)
+    phase_ms, phase_it = [0.0] * 4, 0
+    for _ in range(args.steps):
+        r_ = step()
+        pm_, it_ = r_.phase_ms()
+        phase_ms = [a_ + b_ for a_, b_ in zip(phase_ms, pm_)]
+        phase_it += it_
+        del r_
+    ctx.set_profile(False)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -277,18 +298,33 @@ def run_ours(args, rank, world, local_rank):
     value = world * ITERS * args.steps / elapsed
     distance = res.distance / pr.mu
 
-    # ---- roofline: one Sinkhorn iteration ------------------------------------
+    # ---- roofline ------------------------------------------------------------
+    # Dominant kernel: band_stream_kernel (2 bands x {row, column} pass launches
+    # per iteration). Algorithmic bytes per iteration:
+    #   delta over the support, fp32, read once per pass: 8 nnz
+    #   per band and pass one fp64 scaling vector in + one fp64 correction out:
+    #   16 (n + m) per band
+    # divided by the band launches' time, from the live phase events.
     hbm, peak_kind = peaks()
-    b_iter = 8 * nnz + 4 * l * (n + m) + 16 * (n + m)
-    t_iter = (ms_per_step / 1e3) / ITERS
-    achieved = b_iter / t_iter / 1e9
+    per_it = {k: v / max(phase_it, 1) for k, v in
+              zip(["col_bands", "col_finalize", "row_bands", "row_finalize"], phase_ms)}
+    band_launches = 2 * pr.bands
+    a_band = 8 * nnz + 16 * pr.bands * (n + m)
+    t_band = (per_it["row_bands"] + per_it["col_bands"]) / 1e3  # s per iteration
+    achieved = (a_band / band_launches) / (t_band / band_launches) / 1e9
     traffic = None
-    prof_path = os.path.join(ROOT, "profiles", "iteration_traffic.json")
+    prof_path = os.path.join(ROOT, "profiles", "band_traffic.json")
     if os.path.exists(prof_path):
         try:
-            traffic = json.load(open(prof_path)).get("dram_bytes_per_iteration")
+            tj = json.load(open(prof_path))
+            if tj.get("nnz") == nnz:
+                traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    # whole iteration (SURVEY.md 8(d) B_iter)
+    b_iter = 8 * nnz + 4 * l * (n + m) + 16 * (n + m)
+    t_iter = (ms_per_step / 1e3) / ITERS
+    it_achieved = b_iter / t_iter / 1e9
 
     # ---- e2e through the C-ABI from pinned host buffers ----------------------
     e2e = None
@@ -341,8 +377,7 @@ def run_ours(args, rank, world, local_rank):
             cpu = {"value": None, "unit": "iter/s", "cores": cpu_cores(), "kind": "reference",
                    "sample": f"unavailable: {ex}"}
 
-    launches_per_iter = 5 + 2 * pr.bands + 4  # col: zero, bands, finalize, reduce; row: zero, bands, finalize, reduce, end
-    gpu_launches = args.steps * (ITERS * launches_per_iter + 4 + 2 * pr.bands + 4 + 2)
+    gpu_launches = args.steps * launches_per_step if launches_per_step else None
     if rank == 0:
         line = {"metric": "lcn_sinkhorn_iters_per_s", "value": value, "unit": "iter/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -355,10 +390,15 @@ def run_ours(args, rank, world, local_rank):
                 "distance": distance, "build_s": build_ms / 1e3,
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                              "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
-                             "kernel": "one Sinkhorn iteration (column + row passes)",
-                             "algorithmic_bytes_per_iteration": b_iter},
-                "phases_ms_per_iteration": {k: v / max(phase_it, 1) for k, v in
-                                            zip(["col_bands", "col_finalize", "row_bands", "row_finalize"], phase_ms)},
+                             "kernel": "band_stream_kernel (row + column band passes)",
+                             "algorithmic_bytes_per_launch": a_band / band_launches,
+                             "launches_per_iteration": band_launches,
+                             "avg_launch_ms": t_band * 1e3 / band_launches,
+                             "share_of_iteration": t_band / t_iter},
+                "iteration_roofline": {"bound": "hbm", "achieved": it_achieved, "peak": hbm, "unit": "GB/s",
+                                       "frac": it_achieved / hbm, "algorithmic_bytes_per_iteration": b_iter,
+                                       "ms_per_iteration": t_iter * 1e3},
+                "phases_ms_per_iteration": per_it,
                 "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": gpu_launches}
         print(json.dumps(line), flush=True)
     return 0
