@@ -92,54 +92,81 @@ __global__ void __launch_bounds__(256) assign_exact_kernel(const T* __restrict__
 // dc[near] >= 2 sqrt(dist2[i]) (with margins) makes the new fold >= dist2[i],
 // so the point cannot update and is skipped. The remaining points of a block
 // are compacted and folded exactly (one thread per point, slabs staged).
-template <typename T>
-__global__ void __launch_bounds__(64) pp_update_kernel(const T* __restrict__ X, long long N, int d,
-                                                       const uint32_t* __restrict__ chosen, int t,
-                                                       double* __restrict__ dist2, uint32_t* __restrict__ near,
-                                                       const double* __restrict__ dc) {
-    __shared__ double As[KC][TP + 1];
-    __shared__ double Cs[KC];
-    __shared__ uint32_t rows[TP];
-    __shared__ int cnt;
-    const long long p0 = static_cast<long long>(blockIdx.x) * TP;
-    const long long last = chosen[t];
-    const int r = threadIdx.x;  // blockDim = TP
-    const long long p = p0 + r;
+// Pruning pass: one thread per point; the points that can still update are
+// appended to `list` (warp-aggregated; the order is irrelevant: every point
+// is updated independently).
+__global__ void __launch_bounds__(256) pp_prune_kernel(long long N, int t, const double* __restrict__ dist2,
+                                                       const uint32_t* __restrict__ near,
+                                                       const double* __restrict__ dc, uint32_t* __restrict__ list,
+                                                       unsigned* __restrict__ count) {
+    const long long p = blockIdx.x * 256LL + threadIdx.x;
     bool need = p < N;
-    double D = kPosInf;
-    if (need) {
-        D = dist2[p];
-        if (D < kPosInf && t > 0) {
+    if (need && t > 0) {
+        const double D = dist2[p];
+        if (D < kPosInf) {
             const double lb = dc[near[p]] * (1.0 - 1e-12);
             if (lb >= 2.0 * sqrt(D) * (1.0 + 1e-9)) need = false;
         }
     }
-    if (r == 0) cnt = 0;
+    // block-aggregated append: one global atomic per block (a single counter
+    // hit by every warp serialises at L2)
+    __shared__ unsigned wcnt[8], wbase[8], bbase;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned m = __ballot_sync(0xffffffffu, need);
+    if (lane == 0) wcnt[warp] = __popc(m);
     __syncthreads();
-    if (need) rows[atomicAdd(&cnt, 1)] = static_cast<uint32_t>(p);
+    if (threadIdx.x == 0) {
+        unsigned tot = 0;
+        for (int w = 0; w < 8; ++w) {
+            wbase[w] = tot;
+            tot += wcnt[w];
+        }
+        bbase = tot ? atomicAdd(count, tot) : 0u;
+    }
     __syncthreads();
-    const int n_need = cnt;
-    if (n_need == 0) return;
-    double acc = 0.0;
-    for (int k0 = 0; k0 < d; k0 += KC) {
-        load_slab<T>(As, X, rows, 0, n_need, d, k0);
-        if (threadIdx.x < KC) Cs[threadIdx.x] = k0 + threadIdx.x < d ? static_cast<double>(X[last * d + k0 + threadIdx.x]) : 0.0;
-        __syncthreads();
-        if (r < n_need) {
-#pragma unroll
-            for (int kk = 0; kk < KC; ++kk) {
-                double df = xsub(As[kk][r], Cs[kk]);
+    if (need) list[bbase + wbase[warp] + __popc(m & ((1u << lane) - 1u))] = static_cast<uint32_t>(p);
+}
+
+// Exact pass over the listed points: each warp stages 32 listed rows in
+// shared memory with coalesced loads (row stride d + 1: conflict-free), then
+// lane j folds row j sequentially in fp64 (kmeans.cpp:12-19) and applies the
+// strict-< update (kmeans.cpp:38).
+template <typename T>
+__global__ void __launch_bounds__(128) pp_exact_kernel(const T* __restrict__ X, int d,
+                                                       const uint32_t* __restrict__ chosen, int t,
+                                                       double* __restrict__ dist2, uint32_t* __restrict__ near,
+                                                       const uint32_t* __restrict__ list,
+                                                       const unsigned* __restrict__ count) {
+    extern __shared__ __align__(16) unsigned char dyn[];
+    double* cs = reinterpret_cast<double*>(dyn);  // the new seed, fp64
+    T* rows = reinterpret_cast<T*>(cs + d);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    T* buf = rows + static_cast<size_t>(warp) * 32 * (d + 1);
+    const long long last = chosen[t];
+    for (int k = threadIdx.x; k < d; k += blockDim.x) cs[k] = static_cast<double>(X[last * d + k]);
+    __syncthreads();
+    const unsigned cnt = *count;
+    for (unsigned b0 = (blockIdx.x * nw + warp) * 32u; b0 < cnt; b0 += gridDim.x * nw * 32u) {
+        const unsigned nb = cnt - b0 < 32u ? cnt - b0 : 32u;
+        const uint32_t mine = lane < static_cast<int>(nb) ? list[b0 + lane] : 0u;
+        for (unsigned j = 0; j < nb; ++j) {
+            const long long row = __shfl_sync(0xffffffffu, mine, j);
+            for (int k = lane; k < d; k += 32) buf[j * (d + 1) + k] = X[row * d + k];
+        }
+        __syncwarp();
+        if (lane < static_cast<int>(nb)) {
+            const T* r = buf + lane * (d + 1);
+            double acc = 0.0;
+            for (int k = 0; k < d; ++k) {
+                const double df = xsub(static_cast<double>(r[k]), cs[k]);
                 acc = xadd(acc, xmul(df, df));
             }
+            if (acc < dist2[mine]) {
+                dist2[mine] = acc;
+                near[mine] = static_cast<uint32_t>(t);
+            }
         }
-        __syncthreads();
-    }
-    if (r < n_need) {
-        const uint32_t q = rows[r];
-        if (acc < dist2[q]) {
-            dist2[q] = acc;
-            near[q] = static_cast<uint32_t>(t);
-        }
+        __syncwarp();
     }
 }
 
@@ -555,8 +582,19 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     DevBuf<int> ebin(nch);
     DevBuf<longlong2> R(nch);
     DevBuf<unsigned char> used(N);
-    DevBuf<uint32_t> near(N);
+    DevBuf<uint32_t> near(N), list(N);
+    DevBuf<unsigned> cnt(1);
     DevBuf<double> dc(std::max(k, 1));
+    // exact-pass geometry: warps per CTA so one CTA's row buffers stay <= 96 KB
+    int ex_warps = 4;
+    while (ex_warps > 1 && static_cast<size_t>(ex_warps) * 32 * (d + 1) * sizeof(T) > 96 * 1024) ex_warps >>= 1;
+    const size_t ex_smem = static_cast<size_t>(d) * 8 + static_cast<size_t>(ex_warps) * 32 * (d + 1) * sizeof(T);
+    if (ex_smem > 200 * 1024) throw Status(2, "k-means++: dimension too large for the exact seeding pass");
+    CUDA_OK(cudaFuncSetAttribute(pp_exact_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(ex_smem)));
+    int ex_occ = 1;
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ex_occ, pp_exact_kernel<T>, ex_warps * 32, ex_smem));
+    const int ex_grid = std::max(1, ex_occ) * ctx.num_sms;
     DevBuf<unsigned long long> d_raw(raw.size() ? raw.size() : 1);
     DevBuf<int> counter(1);
     used.zero(s);
@@ -570,7 +608,11 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     CUDA_OK(cudaMemcpyAsync(used.get() + first, &one, 1, cudaMemcpyHostToDevice, s));
     for (int t = 1; t < k; ++t) {
         if (t > 1) seed_dist_kernel<T><<<ceil_div(t - 1, 8), 256, 0, s>>>(X, d, d_chosen, t - 1, dc.get());
-        pp_update_kernel<T><<<ceil_div(N, TP), TP, 0, s>>>(X, N, d, d_chosen, t - 1, dist2.get(), near.get(), dc.get());
+        cnt.zero(s);
+        pp_prune_kernel<<<ceil_div(N, 256), 256, 0, s>>>(N, t - 1, dist2.get(), near.get(), dc.get(), list.get(),
+                                                         cnt.get());
+        pp_exact_kernel<T><<<ex_grid, ex_warps * 32, ex_smem, s>>>(X, d, d_chosen, t - 1, dist2.get(), near.get(),
+                                                                   list.get(), cnt.get());
         fold_chunk_sum_kernel<<<nch, 256, 0, s>>>(dist2.get(), N, csum.get());
         fold_plan_kernel<<<1, 1024, 0, s>>>(csum.get(), nch, ebin.get());
         fold_round_kernel<<<nch, 256, 0, s>>>(dist2.get(), N, ebin.get(), R.get());
