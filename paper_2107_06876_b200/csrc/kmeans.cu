@@ -478,10 +478,26 @@ __device__ __forceinline__ FoldResult fold_chunk_block(WalkShared& sh, const dou
 __global__ void __launch_bounds__(kWalkThreads) pp_walk_pick_kernel(
     double* __restrict__ dist2, unsigned char* __restrict__ used, long long N, int nch, const int* __restrict__ ebin,
     const longlong2* __restrict__ R, double* __restrict__ sstart, const unsigned long long* __restrict__ raw,
-    int n_raw, int* __restrict__ draw_counter, uint32_t* __restrict__ chosen, int t) {
+    int n_raw, int* __restrict__ draw_counter, uint32_t* __restrict__ chosen, int t, int staged) {
     __shared__ WalkShared sh;
+    extern __shared__ __align__(16) unsigned char wdyn[];
     const int lane = threadIdx.x & 31;
     const bool w0 = threadIdx.x < 32;
+    // chunk plans and the running-sum table in shared memory when they fit:
+    // one memory latency for all plans instead of one per 32-chunk group
+    if (staged) {
+        longlong2* Rs = reinterpret_cast<longlong2*>(wdyn);
+        double* ss = reinterpret_cast<double*>(Rs + nch);
+        int* es = reinterpret_cast<int*>(ss + nch + 1);
+        for (int c = threadIdx.x; c < nch; c += kWalkThreads) {
+            Rs[c] = R[c];
+            es[c] = ebin[c];
+        }
+        __syncthreads();
+        R = Rs;
+        ebin = es;
+        sstart = ss;
+    }
     double S = 0.0;
     // 32 chunks per step: a run of clean chunks in the running sum's binade
     // advances by an exact parity scan of their R_c
@@ -538,14 +554,18 @@ __global__ void __launch_bounds__(kWalkThreads) pp_walk_pick_kernel(
         double c = __ull2double_rn(u) * 5.421010862427522e-20;  // exact: * 2^-64
         if (c >= 1.0) c = 0.99999999999999989;                 // nextafter(1, 0)
         const double target = xadd(xmul(c, xsub(S, 0.0)), 0.0);
-        // first chunk whose running sum reaches the target (the sum is monotone)
-        int cstar = nch;
-        for (int cb = 0; cb < nch; cb += 32) {
-            const int c_l = cb + lane;
-            const bool hit = c_l < nch && sstart[c_l + 1] >= target;
-            const unsigned m = __ballot_sync(0xffffffffu, hit);
-            if (m) { cstar = cb + __ffs(m) - 1; break; }
-        }
+        // first chunk whose running sum reaches the target (the sum is
+        // monotone): every thread tests its chunks, block-wide minimum
+        __syncthreads();
+        if (threadIdx.x == 0) sh.flag_min = nch;
+        __syncthreads();
+        for (int c = threadIdx.x; c < nch; c += kWalkThreads)
+            if (sstart[c + 1] >= target) {
+                atomicMin(&sh.flag_min, c);
+                break;
+            }
+        __syncthreads();
+        const int cstar = sh.flag_min;
         pick = -1;
         // the running sum reaches the target inside chunk cstar (an element
         // that raises it is > 0); later chunks only as a guard
@@ -582,6 +602,14 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     DevBuf<int> ebin(nch);
     DevBuf<longlong2> R(nch);
     DevBuf<unsigned char> used(N);
+    // walk: chunk plans + running-sum table staged in shared memory if they fit
+    size_t walk_smem = static_cast<size_t>(nch) * (sizeof(longlong2) + sizeof(double) + sizeof(int)) + sizeof(double);
+    int walk_staged = walk_smem + sizeof(WalkShared) <= 200 * 1024;
+    if (walk_staged)
+        CUDA_OK(cudaFuncSetAttribute(pp_walk_pick_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(walk_smem)));
+    else
+        walk_smem = 0;
     DevBuf<uint32_t> near(N), list(N);
     DevBuf<unsigned> cnt(1);
     DevBuf<double> dc(std::max(k, 1));
@@ -616,8 +644,9 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
         fold_chunk_sum_kernel<<<nch, 256, 0, s>>>(dist2.get(), N, csum.get());
         fold_plan_kernel<<<1, 1024, 0, s>>>(csum.get(), nch, ebin.get());
         fold_round_kernel<<<nch, 256, 0, s>>>(dist2.get(), N, ebin.get(), R.get());
-        pp_walk_pick_kernel<<<1, kWalkThreads, 0, s>>>(dist2.get(), used.get(), N, nch, ebin.get(), R.get(), sstart.get(),
-                                             d_raw.get(), static_cast<int>(raw.size()), counter.get(), d_chosen, t);
+        pp_walk_pick_kernel<<<1, kWalkThreads, walk_smem, s>>>(dist2.get(), used.get(), N, nch, ebin.get(), R.get(),
+                                                               sstart.get(), d_raw.get(), static_cast<int>(raw.size()),
+                                                               counter.get(), d_chosen, t, walk_staged);
     }
     LAUNCH_OK("kmeans++");
     if (draws_used) counter.download(draws_used, 1, s);
