@@ -21,6 +21,7 @@
 #include <cmath>
 #include <limits>
 #include <numeric>
+#include <optional>
 #include <random>
 
 #include "kmeans.cuh"
@@ -268,6 +269,7 @@ __global__ void __launch_bounds__(256) band_tile_kernel(const int4* __restrict__
         tile_fold<MODE>(As, Bs, ty, tx, acc);
         __syncthreads();
     }
+    double tmax = 0.0;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const uint32_t r = r0 + ty + 16 * i;
@@ -276,8 +278,17 @@ __global__ void __launch_bounds__(256) band_tile_kernel(const int4* __restrict__
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const uint32_t c = c0 + tx + 16 * j;
-            if (c < mb) epi(bv.blk_off[b] + static_cast<unsigned long long>(r) * row_stride(mb) + c, si, bv.tgt_order[tb + c], acc[i][j]);
+            if (c < mb) {
+                const double v = epi(bv.blk_off[b] + static_cast<unsigned long long>(r) * row_stride(mb) + c, si,
+                                     bv.tgt_order[tb + c], acc[i][j]);
+                if constexpr (Epi::kReduce) tmax = fmax(tmax, v);
+            }
         }
+    }
+    // one atomic per warp (a per-element atomic on one address serialises)
+    if constexpr (Epi::kReduce) {
+        tmax = warp_max(tmax);
+        if ((threadIdx.x & 31) == 0) atomicMax(epi.maxbits, static_cast<unsigned long long>(__double_as_longlong(tmax)));
     }
 }
 
@@ -301,6 +312,7 @@ __global__ void __launch_bounds__(256) dense_tile_kernel(const double* __restric
         tile_fold<MODE>(As, Bs, ty, tx, acc);
         __syncthreads();
     }
+    double tmax = 0.0;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         long long r = r0 + ty + 16 * i;
@@ -308,14 +320,22 @@ __global__ void __launch_bounds__(256) dense_tile_kernel(const double* __restric
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             long long c = c0 + tx + 16 * j;
-            if (c < nbr) epi(r, c, acc[i][j]);
+            if (c < nbr) {
+                const double v = epi(r, c, acc[i][j]);
+                if constexpr (Epi::kReduce) tmax = fmax(tmax, v);
+            }
         }
+    }
+    if constexpr (Epi::kReduce) {
+        tmax = warp_max(tmax);
+        if ((threadIdx.x & 31) == 0) atomicMax(epi.maxbits, static_cast<unsigned long long>(__double_as_longlong(tmax)));
     }
 }
 
 // log K^sp at a block entry, -inf where an earlier band already holds the
 // pair (sparse_kernel.cpp:76: logvals = 0.0 - cost * inv).
 struct EpiLogK {
+    static constexpr bool kReduce = false;
     double* out;
     BandSet bs;
     int band;
@@ -324,21 +344,23 @@ struct EpiLogK {
     const double* norms;  // union norms (cosine only), targets offset by n
     long long n;
     int* bad;
-    __device__ void operator()(unsigned long long idx, uint32_t i, uint32_t j, double acc) const {
+    __device__ double operator()(unsigned long long idx, uint32_t i, uint32_t j, double acc) const {
         for (int b = 0; b < band; ++b)
             if (bs.src_bucket[b][i] == bs.tgt_bucket[b][j]) {
                 out[idx] = kNegInf;
-                return;
+                return 0.0;
             }
         double nx = norms ? norms[i] : 0.0, ny = norms ? norms[n + j] : 0.0;
         double c = cost_from_fold(kind, acc, nx, ny, bad);
         out[idx] = xsub(0.0, xmul(c, inv));
+        return 0.0;
     }
 };
 
 // exp(-c * inv) (kernel_block, nystrom.cpp:53-64) or exp(-c / lambda)
 // (the landmark Gram matrix A, nystrom.cpp:91-95).
 struct EpiExp {
+    static constexpr bool kReduce = false;
     double* out;
     long long ld;
     int kind;
@@ -347,56 +369,61 @@ struct EpiExp {
     const double* na;
     const double* nb;
     int* bad;
-    __device__ void operator()(long long r, long long c, double acc) const {
+    __device__ double operator()(long long r, long long c, double acc) const {
         double c0 = cost_from_fold(kind, acc, na ? na[r] : 0.0, nb ? nb[c] : 0.0, bad);
         out[r * ld + c] = divide ? exp(__ddiv_rn(-c0, scale)) : exp(xmul(-c0, scale));
+        return 0.0;
     }
 };
 
 struct EpiStore {
+    static constexpr bool kReduce = false;
     double* out;
     long long ld;
     int* bad;
-    __device__ void operator()(long long r, long long c, double acc) const {
+    __device__ double operator()(long long r, long long c, double acc) const {
         if (!isfinite(acc)) atomicOr(bad, 1);
         out[r * ld + c] = acc;
+        return 0.0;
     }
 };
 
 // max |(A_j W) - V| with the transposed storage: acc = (A_j W)_{c r}.
 struct EpiResid {
+    static constexpr bool kReduce = true;  // max |.| reduced per warp by the tile kernel
     const double* vt;
     long long ld;
     unsigned long long* maxbits;
-    __device__ void operator()(long long r, long long c, double acc) const {
+    __device__ double operator()(long long r, long long c, double acc) const {
         double e = fabs(acc - vt[r * ld + c]);
         if (!(e <= 1.79e308)) e = kPosInf;
-        atomicMax(maxbits, static_cast<unsigned long long>(__double_as_longlong(e)));
+        return e;
     }
 };
 
 // delta = exp(log K) - (U W)_ij (sparse_kernel.cpp:100-109); acc is the
 // sequential fold sum_a u_ia w_aj of NystromFactors::entry (nystrom.cpp:127-132).
 struct EpiDelta {
+    static constexpr bool kReduce = true;
     double* delta;
     const double* logk;
     unsigned long long* maxbits;
     int* overflow;
-    __device__ void operator()(unsigned long long idx, uint32_t, uint32_t, double nys) const {
+    __device__ double operator()(unsigned long long idx, uint32_t, uint32_t, double nys) const {
         double lk = logk[idx];
         if (lk == kNegInf) {  // masked duplicate of an earlier band
             delta[idx] = 0.0;
-            return;
+            return 0.0;
         }
         double exact = exp(lk);
         if (isinf(exact)) {
             atomicOr(overflow, 1);
             delta[idx] = 0.0;
-            return;
+            return 0.0;
         }
         double dv = exact - nys;
         delta[idx] = dv;
-        atomicMax(maxbits, static_cast<unsigned long long>(__double_as_longlong(fabs(dv))));
+        return fabs(dv);
     }
 };
 
@@ -649,6 +676,8 @@ void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed)
     for (double rel = 0.0; rel <= 1.1e-4; rel = (rel == 0.0 ? 1e-10 : rel * 10.0)) {
         std::vector<LD> aj = a;
         for (size_t i = 0; i < l; ++i) aj[i * l + i] += rel * jitter_unit;
+        std::optional<PhaseTimer> pt_sub;
+        pt_sub.emplace(ctx, "  host LDLT + inverse (long double)");
         HostLdlt fac(aj, l);
         if (!fac.ok) continue;
         std::vector<LD> inv(l * l);
@@ -663,6 +692,8 @@ void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed)
                 if (!std::isfinite(e[r])) finite = false;
             }
         }
+        pt_sub.reset();
+        pt_sub.emplace(ctx, "  W = V A^-T, residual (device GEMMs)");
         if (!finite) continue;
         std::vector<double> hinv(l * l), haj(l * l);
         for (size_t i = 0; i < l * l; ++i) {

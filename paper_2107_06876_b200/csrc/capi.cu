@@ -28,6 +28,7 @@ struct lcn_op {
 struct lcn_result {
     Result r;
     lcn_op* op = nullptr;
+    int device = 0;  // the operator may be destroyed first
 };
 
 namespace {
@@ -37,6 +38,12 @@ thread_local std::string g_orphan_error;
 template <class F>
 int guard(lcn_ctx* ctx, F&& f) {
     std::string* sink = ctx ? &ctx->c.last_error : &g_orphan_error;
+    // device temporaries of this call are allocated / freed on its stream
+    struct StreamScope {
+        cudaStream_t saved;
+        explicit StreamScope(cudaStream_t s) : saved(alloc_stream()) { alloc_stream() = s; }
+        ~StreamScope() { alloc_stream() = saved; }
+    } scope(ctx ? ctx->c.stream : nullptr);
     try {
         if (ctx) ctx->c.activate();
         f();
@@ -185,6 +192,11 @@ int lcn_ctx_create(int device, int flags, lcn_ctx** out) {
         c->c.store_fp64 = (flags & LCN_STORE_FP64) ? 1 : 0;
         c->c.num_sms = prop.multiProcessorCount;
         CUDA_OK(cudaSetDevice(device));
+        // keep freed pool memory resident (stream-ordered DevBuf temporaries)
+        cudaMemPool_t pool;
+        CUDA_OK(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t keep = ~0ull;
+        CUDA_OK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
         CUDA_OK(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking));
         c->c.own_stream = c->c.stream;
         *out = c.release();
@@ -194,6 +206,7 @@ int lcn_ctx_create(int device, int flags, lcn_ctx** out) {
 int lcn_ctx_destroy(lcn_ctx* ctx) {
     if (!ctx) return LCN_OK;
     cudaSetDevice(ctx->c.device);
+    cudaDeviceSynchronize();
     if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.own_stream);
     delete ctx;
     return LCN_OK;
@@ -409,6 +422,7 @@ int lcn_op_create_device(lcn_ctx* ctx, const float* d_p, size_t n, const float* 
 int lcn_op_destroy(lcn_op* op) {
     if (!op) return LCN_OK;
     cudaSetDevice(op->o.ctx->device);
+    cudaDeviceSynchronize();  // any stream may still read the operator
     delete op;
     return LCN_OK;
 }
@@ -490,6 +504,7 @@ int lcn_sinkhorn(lcn_op* op, const double* p, const double* q, const lcn_sinkhor
         }
         auto res = std::make_unique<lcn_result>();
         res->op = op;
+        res->device = op->o.ctx->device;
         if (o.kind == LCN_OP_SPARSE && so.check_support) {
             // sinkhorn.cpp:122-128: warn when the pattern has no support.
             build_csr(o);
@@ -545,6 +560,7 @@ int lcn_sinkhorn_device(lcn_op* op, const double* d_p, const double* d_q, const 
         }
         auto res = std::make_unique<lcn_result>();
         res->op = op;
+        res->device = op->o.ctx->device;
         sinkhorn_solve(op->o, d_p, d_q, true, so, res->r);
         *out = res.release();
     });
@@ -558,6 +574,9 @@ int lcn_result_phase_ms(const lcn_result* res, double* out4, int* iters) {
 }
 
 int lcn_result_destroy(lcn_result* res) {
+    if (!res) return LCN_OK;
+    cudaSetDevice(res->device);
+    cudaDeviceSynchronize();
     delete res;
     return LCN_OK;
 }

@@ -11,8 +11,19 @@
 
 namespace lcnb {
 
-// Owning device allocation (cudaMallocAsync on the context stream would tie
-// lifetimes to a stream; plain cudaMalloc keeps buffers valid across streams).
+// Stream of the API call in progress on this thread (set by the C-ABI guard;
+// 0 = legacy default stream outside any call).
+inline cudaStream_t& alloc_stream() {
+    thread_local cudaStream_t s = nullptr;
+    return s;
+}
+
+// Owning device allocation, stream-ordered: cudaMallocAsync / cudaFreeAsync
+// on the calling API's stream from the device's default pool (kept resident,
+// see lcn_ctx_create). A synchronous cudaFree stalls the device at every
+// temporary; the pool hands memory back without synchronising. Destroy entry
+// points synchronise the device before freeing (objects may be released from
+// any thread / stream).
 template <typename T>
 class DevBuf {
   public:
@@ -29,11 +40,11 @@ class DevBuf {
     void resize(size_t n) {
         if (n == n_) return;
         release();
-        if (n) CUDA_OK(cudaMalloc(&p_, n * sizeof(T)));
+        if (n) CUDA_OK(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), alloc_stream()));
         n_ = n;
     }
     void release() {
-        if (p_) cudaFree(p_);
+        if (p_) cudaFreeAsync(p_, alloc_stream());
         p_ = nullptr;
         n_ = 0;
     }

@@ -22,9 +22,25 @@
 #include "async.cuh"
 #include "ctx.cuh"
 #include "kmeans.cuh"
+#include "op.cuh"
 #include "tiles.cuh"
 
 namespace lcnb {
+
+// ---- cp.async (LDGSTS) helpers: global -> shared without a register round
+// trip, so a warp can put many loads in flight before it waits once.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+template <typename T>
+__device__ __forceinline__ void cp_async_elem(T* dst, const T* src) {
+    static_assert(sizeof(T) == 4 || sizeof(T) == 8, "4- or 8-byte elements");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(dst)), "l"(src), "n"(sizeof(T))
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int NG>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(NG) : "memory"); }
 
 // ---- assign_nearest (kmeans.cpp:67-85) -------------------------------------
 // rows != null: evaluate only the points rows[0 .. N) (the filter's
@@ -151,8 +167,10 @@ __global__ void __launch_bounds__(128) pp_exact_kernel(const T* __restrict__ X, 
         const uint32_t mine = lane < static_cast<int>(nb) ? list[b0 + lane] : 0u;
         for (unsigned j = 0; j < nb; ++j) {
             const long long row = __shfl_sync(0xffffffffu, mine, j);
-            for (int k = lane; k < d; k += 32) buf[j * (d + 1) + k] = X[row * d + k];
+            for (int k = lane; k < d; k += 32) cp_async_elem(&buf[j * (d + 1) + k], X + row * d + k);
         }
+        cp_async_commit();
+        cp_async_wait<0>();  // one memory latency per 32 rows
         __syncwarp();
         if (lane < static_cast<int>(nb)) {
             const T* r = buf + lane * (d + 1);
@@ -677,7 +695,16 @@ __global__ void centroid_kernel(const T* __restrict__ X, int d, const uint32_t* 
     const double inv = __ddiv_rn(1.0, static_cast<double>(cnt));
     for (int kk = threadIdx.x; kk < d; kk += blockDim.x) {
         double s = 0.0;
-        for (int p = 0; p < cnt; ++p) s = xadd(s, static_cast<double>(X[static_cast<long long>(order[b + p]) * d + kk]));
+        int p = 0;
+        // 16 member rows loaded ahead of the (sequential) fold
+        for (; p + 16 <= cnt; p += 16) {
+            T v[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) v[u] = X[static_cast<long long>(order[b + p + u]) * d + kk];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) s = xadd(s, static_cast<double>(v[u]));
+        }
+        for (; p < cnt; ++p) s = xadd(s, static_cast<double>(X[static_cast<long long>(order[b + p]) * d + kk]));
         ctr[static_cast<long long>(c) * d + kk] = xmul(s, inv);
     }
 }
@@ -761,15 +788,6 @@ struct FilterSmem {
     double xn[kFB];        // |x|^2 (fp64)
 };
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int NG>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(NG) : "memory"); }
 
 // CfT[kk][c] = fp32(C[c][kk]) for c < k, 0 for padding; ncf[c] = fp32(sum c_f^2)
 // (+inf for padding); cmax = max_c max(|c|^2, |c_f|^2) as fp64 bits.
@@ -964,7 +982,11 @@ void lloyd_device(Ctx& ctx, const T* X, long long N, int d, int k, int iters, ui
     std::vector<unsigned long long> raw(k > 1 ? k - 1 : 0);
     for (auto& r : raw) r = rng();
     DevBuf<uint32_t> init(k);
-    kmeans_pp_device<T>(ctx, X, N, d, k, f, raw, init.get(), nullptr);
+    {
+        PhaseTimer pt(ctx, "  k-means++ seeding");
+        kmeans_pp_device<T>(ctx, X, N, d, k, f, raw, init.get(), nullptr);
+    }
+    PhaseTimer pt_lloyd(ctx, "  lloyd iterations + final assign");
     // centroids = rows of the seeds (kmeans.cpp:99-100)
     {
         DevBuf<int> dummy_counts(k), dummy_start(k);
