@@ -217,7 +217,8 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     pr = configs.config3(args.scale)
-    if rank:
+    sharded = (world > 1 and not args.replicas) or args.sharded
+    if rank and not sharded:
         # independent replica per rank: reseed the point draw
         import dataclasses
         rng = np.random.default_rng(2000 + rank)
@@ -228,6 +229,12 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.Stream(device=dev)
     ctx = lcn.Context(local_rank)
     ctx.set_stream(stream.cuda_stream)
+    if sharded:
+        # one problem over all ranks (lcn_ctx_set_comm): rank 0's NCCL id
+        obj = [lcn.nccl_unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0)
+        ctx.set_comm(world, rank, obj[0])
 
     p32 = torch.from_numpy(pr.p.astype(np.float32)).pin_memory()
     q32 = torch.from_numpy(pr.q.astype(np.float32)).pin_memory()
@@ -295,7 +302,8 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         elapsed = float(tt.item())
     ms_per_step = elapsed * 1e3 / args.steps
-    value = world * ITERS * args.steps / elapsed
+    # replicas: every rank solves its own problem; sharded: the ranks solve one
+    value = (1 if sharded else world) * ITERS * args.steps / elapsed
     distance = res.distance / pr.mu
 
     # ---- roofline ------------------------------------------------------------
@@ -310,6 +318,8 @@ def run_ours(args, rank, world, local_rank):
               zip(["col_bands", "col_finalize", "row_bands", "row_finalize"], phase_ms)}
     band_launches = 2 * pr.bands
     a_band = 8 * nnz + 16 * pr.bands * (n + m)
+    if sharded:  # this rank streams about 1/world of the band blocks
+        a_band /= world
     t_band = (per_it["row_bands"] + per_it["col_bands"]) / 1e3  # s per iteration
     achieved = (a_band / band_launches) / (t_band / band_launches) / 1e9
     traffic = None
@@ -357,7 +367,8 @@ def run_ours(args, rank, world, local_rank):
                 dt = float(tt.item())
             tot += dt
             del op2, r2
-        e2e = {"value": world * ITERS * args.e2e_steps / tot, "unit": "iter/s", "h2d_bytes_per_step": h2d,
+        e2e = {"value": (1 if sharded else world) * ITERS * args.e2e_steps / tot, "unit": "iter/s",
+               "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": 8, "solve_s": tot / args.e2e_steps,
                "covers": "H2D points+marginals, k-means LSH, landmarks, Nystrom, correction, 100 iterations, D2H distance"}
 
@@ -381,12 +392,16 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0:
         line = {"metric": "lcn_sinkhorn_iters_per_s", "value": value, "unit": "iter/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32-storage/f64-accumulate", "data": "synthetic",
+                "scaling": "strong" if sharded else "weak", "vs_baseline": None,
+                "dtype": "f32-storage/f64-accumulate", "data": "synthetic",
                 "config": {"workload": "configs[3] LCN-Sinkhorn n=m=1e6 d=128 sqL2/mean lambda=0.05 2x4096 LSH l=512",
                            "n": n, "m": m, "d": d, "landmarks": l, "bands": pr.bands, "buckets": pr.buckets,
                            "iterations_per_step": ITERS, "nnz": nnz, "stored_entries": stored,
                            "scale": args.scale, "l2": "inputs larger than L2 (delta + U + W = 6.2 GB per iteration)",
-                           "parallelism": f"{world} independent replica(s), 1 per GPU"},
+                           "parallelism": (f"one problem sharded over {world} GPUs: band buckets split by rank, "
+                                           f"low-rank rows in slices; per half-iteration NCCL reduce-scatter of the "
+                                           f"corrections, all-gather of the log vector, all-reduce of the low-rank "
+                                           f"partials" if sharded else f"{world} independent replica(s), 1 per GPU")},
                 "distance": distance, "build_s": build_ms / 1e3,
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                              "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
@@ -414,6 +429,10 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the sharded solve even on one GPU (1-rank communicator)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent problems per GPU instead of one sharded problem")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -112,6 +112,19 @@ const char* lcn_ctx_last_error(const lcn_ctx* ctx);
 int lcn_ctx_set_stream(lcn_ctx* ctx, void* stream);
 /* Record per-phase CUDA events inside lcn_sinkhorn (see lcn_result_phase_ms). */
 int lcn_ctx_set_profile(lcn_ctx* ctx, int on);
+
+/* ---- sharded solve over several GPUs ------------------ */
+/* A fresh NCCL unique id (128 bytes) on the calling rank (rank 0 makes it,
+ * the caller broadcasts it). */
+int lcn_nccl_unique_id(uint8_t* out128);
+/* Join `world` ranks (one process or thread per GPU) into one communicator;
+ * collective over the ranks. Afterwards lcn_sinkhorn* on operators of this
+ * context solve ONE problem together: every rank holds the operator (built
+ * from the same inputs), the band blocks are split by bucket across ranks and
+ * the low-rank rows into contiguous slices; per half-iteration the ranks
+ * exchange the band corrections (reduce-scatter), the new log vector
+ * (all-gather) and the low-rank partials (all-reduce). world = 1 is valid. */
+int lcn_ctx_set_comm(lcn_ctx* ctx, int world, int rank, const uint8_t* id128);
 const char* lcn_status_name(int status);
 int lcn_abi_version(void);
 

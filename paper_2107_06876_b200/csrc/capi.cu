@@ -9,6 +9,8 @@
 #include <random>
 #include <string>
 
+#include <nccl.h>
+
 #include "../../include/lcn_b200.h"
 #include "kmeans.cuh"
 #include "op.cuh"
@@ -207,6 +209,7 @@ int lcn_ctx_destroy(lcn_ctx* ctx) {
     if (!ctx) return LCN_OK;
     cudaSetDevice(ctx->c.device);
     cudaDeviceSynchronize();
+    if (ctx->c.nccl) ncclCommDestroy(static_cast<ncclComm_t>(ctx->c.nccl));
     if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.own_stream);
     delete ctx;
     return LCN_OK;
@@ -216,6 +219,35 @@ int lcn_ctx_set_stream(lcn_ctx* ctx, void* stream) {
     if (!ctx) return LCN_E_INVALID_ARGUMENT;
     ctx->c.stream = stream ? static_cast<cudaStream_t>(stream) : ctx->c.own_stream;
     return LCN_OK;
+}
+
+int lcn_nccl_unique_id(uint8_t* out128) {
+    return guard(nullptr, [&] {
+        if (!out128) throw Status(2, "null id buffer");
+        ncclUniqueId id;
+        if (ncclGetUniqueId(&id) != ncclSuccess) throw Status(LCN_E_CUDA, "ncclGetUniqueId failed");
+        static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+        std::memcpy(out128, &id, 128);
+    });
+}
+
+int lcn_ctx_set_comm(lcn_ctx* ctx, int world, int rank, const uint8_t* id128) {
+    return guard(ctx, [&] {
+        if (!ctx || !id128) throw Status(2, "null context or id");
+        if (world < 1 || rank < 0 || rank >= world) throw Status(2, "rank / world out of range");
+        if (ctx->c.nccl) {
+            ncclCommDestroy(static_cast<ncclComm_t>(ctx->c.nccl));
+            ctx->c.nccl = nullptr;
+        }
+        ncclUniqueId id;
+        std::memcpy(&id, id128, 128);
+        ncclComm_t comm;
+        const ncclResult_t r = ncclCommInitRank(&comm, world, id, rank);
+        if (r != ncclSuccess) throw Status(LCN_E_CUDA, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+        ctx->c.nccl = comm;
+        ctx->c.rank = rank;
+        ctx->c.world = world;
+    });
 }
 
 int lcn_ctx_set_profile(lcn_ctx* ctx, int on) {

@@ -80,6 +80,10 @@ struct Ctx {
     std::string last_error;
     // k-means assignment filter statistics (points filtered / sent to the exact scan)
     long long filter_points = 0, filter_ambiguous = 0;
+    // sharded solve: NCCL communicator over the ranks that
+    // share one problem (opaque ncclComm_t; null = single-GPU solve)
+    void* nccl = nullptr;
+    int rank = 0, world = 1;
     void activate() const { CUDA_OK(cudaSetDevice(device)); }
     void sync() const { CUDA_OK(cudaStreamSynchronize(stream)); }
 };

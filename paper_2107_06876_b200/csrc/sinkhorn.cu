@@ -34,6 +34,8 @@
 #include <utility>
 #include <type_traits>
 
+#include <nccl.h>
+
 #include "async.cuh"
 #include "op.cuh"
 
@@ -991,7 +993,8 @@ __global__ void __launch_bounds__(kThreads + 64, 2) lowrank_pass_kernel(const T*
 __global__ void __launch_bounds__(1024) lowrank_reduce_kernel(DevState* __restrict__ st, const double* __restrict__ part,
                                                               const double* __restrict__ hpart,
                                                               const double* __restrict__ mnp, int G, int lp,
-                                                              double* __restrict__ mid, int which) {
+                                                              double* __restrict__ mid, int which,
+                                                              double* __restrict__ hloc) {
     if (st->done) return;
     constexpr int W = 32;  // warps
     __shared__ double sh[W], sm[W], acc_s[W][33];
@@ -1031,15 +1034,34 @@ __global__ void __launch_bounds__(1024) lowrank_reduce_kernel(DevState* __restri
         int allpos = H != kNegInf && exp(mn - H) > 0.0;
         if (which == 0) { st->H_t = H; st->allpos_t = allpos; }
         else { st->H_s = H; st->allpos_s = allpos; }
+        if (hloc) {  // sharded: this rank's shift and minimum, combined across ranks next
+            hloc[0] = H;
+            hloc[1] = mn;
+        }
     }
 }
 
-// End of iteration `it` (0 = the initial K(log t = 0)): error precedence in
-// the reference's order, marginal error, trace, convergence.
-__global__ void __launch_bounds__(256) iter_end_kernel(DevState* __restrict__ st, const double* __restrict__ err_part,
-                                                       int G, int it, int max_iters, double tol,
-                                                       double* __restrict__ trace) {
+// Sharded solve: after the MAX / MIN all-reduce of (H, mn) into hloc[2..3],
+// rescale this rank's partial to the global shift (the SUM all-reduce of mid
+// follows) and publish the global shift / positivity flag.
+__global__ void shift_to_global_kernel(DevState* __restrict__ st, double* __restrict__ mid, int lp,
+                                       const double* __restrict__ hloc, int which) {
     if (st->done) return;
+    const double Hl = hloc[0], Hg = hloc[2], mng = hloc[3];
+    const double f = (Hl == kNegInf || Hg == kNegInf) ? 0.0 : exp(Hl - Hg);
+    for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < lp; a += gridDim.x * blockDim.x) mid[a] *= f;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const int allpos = Hg != kNegInf && exp(mng - Hg) > 0.0;
+        if (which == 0) { st->H_t = Hg; st->allpos_t = allpos; }
+        else { st->H_s = Hg; st->allpos_s = allpos; }
+    }
+}
+
+// Sharded solve: this rank's marginal-error partial and error flags, summed
+// across ranks by an all-reduce before iter_end (flags as per-bit counts).
+__global__ void __launch_bounds__(256) stage_err_kernel(const DevState* __restrict__ st,
+                                                        const double* __restrict__ err_part, int G, int it,
+                                                        double* __restrict__ gstage) {
     __shared__ double red[8];
     double e = 0.0;
     if (it > 0)
@@ -1047,10 +1069,39 @@ __global__ void __launch_bounds__(256) iter_end_kernel(DevState* __restrict__ st
     e = warp_sum(e);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = e;
     __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[w];
+        gstage[0] = t;
+        const unsigned f = st->flags;
+        for (int k = 0; k < 8; ++k) gstage[1 + k] = (f >> k) & 1u ? 1.0 : 0.0;
+    }
+}
+
+// End of iteration `it` (0 = the initial K(log t = 0)): error precedence in
+// the reference's order, marginal error, trace, convergence.
+__global__ void __launch_bounds__(256) iter_end_kernel(DevState* __restrict__ st, const double* __restrict__ err_part,
+                                                       int G, int it, int max_iters, double tol,
+                                                       double* __restrict__ trace,
+                                                       const double* __restrict__ gstage) {
+    if (st->done) return;
+    __shared__ double red[8];
+    double e = 0.0;
+    if (it > 0 && !gstage)
+        for (int b = threadIdx.x; b < G; b += 256) e += err_part[b];
+    e = warp_sum(e);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = e;
+    __syncthreads();
     if (threadIdx.x != 0) return;
     e = 0.0;
     for (int w = 0; w < 8; ++w) e += red[w];
-    const unsigned f = st->flags;
+    unsigned f = st->flags;
+    if (gstage) {  // sharded: error and flags summed over the ranks
+        e = it > 0 ? gstage[0] : 0.0;
+        f = 0u;
+        for (int k = 0; k < 8; ++k)
+            if (gstage[1 + k] > 0.5) f |= 1u << k;
+    }
     auto fail = [&](int status, int which) {
         st->status = status;
         st->which = which;
@@ -1156,8 +1207,28 @@ struct Solver {
     };
     std::vector<PassPlan> plans[2];
     int band_grid = 0;
+    // ---- sharded solve (ctx.nccl set): rank `rank` of `world` owns the band
+    // buckets assigned to it (per band and pass) and the low-rank row slices
+    // [lo_s, hi_s) / [lo_t, hi_t) of equal padded length cs / ct.
+    ncclComm_t comm = nullptr;
+    int rank = 0, world = 1;
+    long long cs = 0, ct = 0, lo_s = 0, hi_s = 0, lo_t = 0, hi_t = 0;
+    std::vector<DevBuf<double>> cslice_s, cslice_t;  // reduce-scattered corrections (own slice)
+    DevBuf<double> hloc, gstage;                      // shift exchange [Hl, mnl, Hg, mng]; err + flag counts
 
     explicit Solver(Op& o) : op(o), ctx(*o.ctx), s(o.ctx->stream), n(o.n), m(o.m), l(static_cast<int>(o.l)) {
+        comm = static_cast<ncclComm_t>(ctx.nccl);
+        rank = ctx.rank;
+        world = ctx.world;
+        if (comm) {
+            if (op.kind != 3) throw Status(2, "sharded solve: only the LCN operator is sharded on this path");
+            cs = (ceil_div(n, world) + kRT - 1) / kRT * kRT;
+            ct = (ceil_div(m, world) + kRT - 1) / kRT * kRT;
+            lo_s = std::min<long long>(n, rank * cs);
+            hi_s = std::min<long long>(n, lo_s + cs);
+            lo_t = std::min<long long>(m, rank * ct);
+            hi_t = std::min<long long>(m, lo_t + ct);
+        }
         lp = static_cast<int>(o.lp);
         CPT = lp <= kThreads ? 1 : lp <= 2 * kThreads ? 2 : 4;
         if (lp > 4 * kThreads) throw Status(2, "lcn: landmark count above 1024 is not supported on this path");
@@ -1208,10 +1279,38 @@ struct Solver {
             std::vector<uint32_t> w(B.n_work);
             if (B.n_work) B.work.download(w.data(), B.n_work, s);
             ctx.sync();
-            plans[0].push_back(plan_pass(B, w, true));
-            plans[1].push_back(plan_pass(B, w, false));
+            plans[0].push_back(plan_pass(B, owned_buckets(B, w, true), true));
+            plans[1].push_back(plan_pass(B, owned_buckets(B, w, false), false));
         }
         ctx.sync();
+    }
+
+    // Sharded solve: the buckets of one band and pass this rank processes.
+    // Whole buckets (all pieces of a split bucket stay on one rank), assigned
+    // by longest-processing-time greedy on the streamed bytes; every rank
+    // computes the same assignment.
+    std::vector<uint32_t> owned_buckets(const Band& B, const std::vector<uint32_t>& w, bool rows) const {
+        if (!comm || world == 1) return w;
+        std::vector<std::pair<double, uint32_t>> cost;
+        for (uint32_t k : w) {
+            const double nb = B.h_src_start[k + 1] - B.h_src_start[k];
+            const double mb = B.h_tgt_start[k + 1] - B.h_tgt_start[k];
+            const double sl = rows ? mb : nb, ol = rows ? nb : mb;
+            cost.push_back({sl * static_cast<double>(row_stride(static_cast<unsigned long long>(ol))) + 64.0 * sl, k});
+        }
+        std::stable_sort(cost.begin(), cost.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+        using Load = std::pair<double, int>;
+        std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
+        for (int r = 0; r < world; ++r) heap.push({0.0, r});
+        std::vector<uint32_t> mine;
+        for (const auto& c : cost) {
+            Load ld = heap.top();
+            heap.pop();
+            if (ld.second == rank) mine.push_back(c.second);
+            ld.first += c.first;
+            heap.push(ld);
+        }
+        return mine;
     }
 
     // Items of one pass: per bucket, output tiles of <= kBandVec columns and
@@ -1345,7 +1444,11 @@ struct Solver {
         st.zero(s);
         dpart.resize(256);
         // row vectors padded to a multiple of kRT (the bulk copies read whole tiles)
-        const long long np = (n + kRT - 1) / kRT * kRT, mpd = (m + kRT - 1) / kRT * kRT;
+        long long np = (n + kRT - 1) / kRT * kRT, mpd = (m + kRT - 1) / kRT * kRT;
+        if (comm) {  // all-gathered vectors span world equal slices
+            np = std::max(np, cs * world);
+            mpd = std::max(mpd, ct * world);
+        }
         log_p.resize(np); log_q.resize(mpd); pv.resize(np); qv.resize(mpd);
         log_s[0].resize(np); log_s[1].resize(np); log_t.resize(mpd); row_marg.resize(np);
         err_part.resize(std::max<long long>(G, ceil_div(n, 256)));
@@ -1375,12 +1478,22 @@ struct Solver {
             }
             part.resize(static_cast<size_t>(G) * lp); hpart.resize(G); mnp.resize(G); mxp.resize(G);
             mid_s.resize(lp); mid_t.resize(lp);
+            if (comm) {
+                cslice_s.resize(op.bands.size());
+                cslice_t.resize(op.bands.size());
+                for (size_t b = 0; b < op.bands.size(); ++b) {
+                    cslice_s[b].resize(cs);
+                    cslice_t[b].resize(ct);
+                }
+                hloc.resize(4);
+                gstage.resize(9);
+            }
         }
     }
 
     template <typename T, int SIDE>
-    void pass(const PassArgs& a) {
-        const T* F = SIDE == 0 ? U<T>() : Wt<T>();
+    void pass(const PassArgs& a, long long row0 = 0) {
+        const T* F = (SIDE == 0 ? U<T>() : Wt<T>()) + row0 * lp;
         switch (CPT) {
             case 1: lowrank_pass_kernel<T, 1, SIDE><<<G, kThreads + 64, smem, s>>>(F, a); break;
             case 2: lowrank_pass_kernel<T, 2, SIDE><<<G, kThreads + 64, smem, s>>>(F, a); break;
@@ -1401,7 +1514,7 @@ struct Solver {
     }
     void reduce(double* mid, int which) {
         lowrank_reduce_kernel<<<ceil_div(lp, 32), 1024, 0, s>>>(st.get(), part.get(), hpart.get(), mnp.get(), G, lp,
-                                                               mid, which);
+                                                                mid, which, nullptr);
     }
 
     // -------- sparse -------------------------------------------------------
@@ -1439,7 +1552,8 @@ struct Solver {
         sparse_row_finalize_kernel<<<ceil_div(n, 256), 256, 0, s>>>(st.get(), Mr.get(), Sr.get(), log_p.get(), pv.get(),
                                                                     n, log_s[cur].get(), log_s[nxt].get(), nullptr,
                                                                     row_marg.get(), err_part.get(), it > 0);
-        iter_end_kernel<<<1, 256, 0, s>>>(st.get(), err_part.get(), ceil_div(n, 256), it, max_iters, tol, trace.get());
+        iter_end_kernel<<<1, 256, 0, s>>>(st.get(), err_part.get(), ceil_div(n, 256), it, max_iters, tol, trace.get(),
+                                          nullptr);
         mark(it, 4);
     }
 
@@ -1525,7 +1639,92 @@ struct Solver {
         set_perm(a, 0, nxt);
         pass<T, 0>(a);
         reduce(mid_s.get(), 1);
-        iter_end_kernel<<<1, 256, 0, s>>>(st.get(), err_part.get(), G, it, max_iters, tol, trace.get());
+        iter_end_kernel<<<1, 256, 0, s>>>(st.get(), err_part.get(), G, it, max_iters, tol, trace.get(), nullptr);
+        mark(it, 4);
+    }
+
+    // ---- sharded solve ---------------------------------------------------
+    static void nccl_ok(ncclResult_t r, const char* what) {
+        if (r != ncclSuccess) throw Status(100, std::string(what) + ": " + ncclGetErrorString(r));
+    }
+    // low-rank reduce over this rank's CTAs, then the cross-rank combine:
+    // global shift H = max_r H_r (all-reduce MAX), mid = sum_r exp(H_r - H)
+    // mid_r (rescale + all-reduce SUM), positivity test on the global minimum
+    void reduce_global(double* mid, int which) {
+        lowrank_reduce_kernel<<<ceil_div(lp, 32), 1024, 0, s>>>(st.get(), part.get(), hpart.get(), mnp.get(), G, lp,
+                                                                mid, which, hloc.get());
+        nccl_ok(ncclAllReduce(hloc.get() + 0, hloc.get() + 2, 1, ncclDouble, ncclMax, comm, s), "allreduce shift");
+        nccl_ok(ncclAllReduce(hloc.get() + 1, hloc.get() + 3, 1, ncclDouble, ncclMin, comm, s), "allreduce min");
+        shift_to_global_kernel<<<ceil_div(lp, 256), 256, 0, s>>>(st.get(), mid, lp, hloc.get(), which);
+        nccl_ok(ncclAllReduce(mid, mid, lp, ncclDouble, ncclSum, comm, s), "allreduce mid");
+    }
+
+    // One iteration of the sharded solve; every rank holds
+    // the full vectors, band work is split by bucket, low-rank rows by slice.
+    // Per half-iteration: own band blocks -> reduce-scatter of the per-band
+    // corrections onto the row slices -> low-rank pass over the own slice ->
+    // all-gather of the new log vector (+ local re-scatter into the
+    // bucket-ordered copies) -> cross-rank low-rank combine; the marginal
+    // error and the error flags are summed across ranks before iter_end.
+    template <typename T>
+    void lcn_iteration_sharded(int it, double tol, int max_iters) {
+        const int cur = it % 2, nxt = (it + 1) % 2;
+        const int nb = static_cast<int>(op.bands.size());
+        mark(it, 0);
+        if (it == 0) {
+            PassArgs a = base_args();
+            a.rows = hi_t - lo_t;
+            a.mode = 2;
+            a.in = nullptr;
+            pass<T, 1>(a, lo_t);
+            mark(it, 1);
+        } else {
+            lcn_cols<T>(cur);
+            mark(it, 1);
+            for (int b = 0; b < nb; ++b)
+                nccl_ok(ncclReduceScatter(corr_t[b].get(), cslice_t[b].get(), ct, ncclDouble, ncclSum, comm, s),
+                        "reduce-scatter corr_t");
+            PassArgs a = base_args();
+            a.rows = hi_t - lo_t;
+            a.mode = 0;
+            a.mid = mid_s.get();
+            a.ncorr = nb;
+            for (int b = 0; b < nb; ++b) a.corr[b] = cslice_t[b].get();
+            a.nperm = 0;
+            a.log_marg = log_q.get() + lo_t;
+            a.log_out = log_t.get() + lo_t;
+            pass<T, 1>(a, lo_t);
+            nccl_ok(ncclAllGather(log_t.get() + rank * ct, log_t.get(), ct, ncclDouble, comm, s), "allgather log t");
+            scatter_perm(log_t.get(), m, 1, 0);
+        }
+        reduce_global(mid_t.get(), 0);
+        mark(it, 2);
+        lcn_rows<T>();
+        mark(it, 3);
+        for (int b = 0; b < nb; ++b)
+            nccl_ok(ncclReduceScatter(corr_s[b].get(), cslice_s[b].get(), cs, ncclDouble, ncclSum, comm, s),
+                    "reduce-scatter corr_s");
+        PassArgs a = base_args();
+        a.rows = hi_s - lo_s;
+        a.mode = 0;
+        a.mid = mid_t.get();
+        a.ncorr = nb;
+        for (int b = 0; b < nb; ++b) a.corr[b] = cslice_s[b].get();
+        a.nperm = 0;
+        a.log_marg = log_p.get() + lo_s;
+        a.marg = pv.get() + lo_s;
+        a.log_cur = log_s[cur].get() + lo_s;
+        a.log_out = log_s[nxt].get() + lo_s;
+        a.row_marg = row_marg.get() + lo_s;
+        a.with_err = it > 0;
+        pass<T, 0>(a, lo_s);
+        nccl_ok(ncclAllGather(log_s[nxt].get() + rank * cs, log_s[nxt].get(), cs, ncclDouble, comm, s),
+                "allgather log s");
+        scatter_perm(log_s[nxt].get(), n, 0, nxt);
+        reduce_global(mid_s.get(), 1);
+        stage_err_kernel<<<1, 256, 0, s>>>(st.get(), err_part.get(), G, it, gstage.get());
+        nccl_ok(ncclAllReduce(gstage.get(), gstage.get(), 9, ncclDouble, ncclSum, comm, s), "allreduce error");
+        iter_end_kernel<<<1, 256, 0, s>>>(st.get(), err_part.get(), G, it, max_iters, tol, trace.get(), gstage.get());
         mark(it, 4);
     }
 
@@ -1567,6 +1766,7 @@ struct Solver {
         for (int it0 = 0; it0 <= o.max_iters; it0 += chunk) {
             for (int it = it0; it < std::min(it0 + chunk, o.max_iters + 1); ++it) {
                 if (op.kind == 1) sparse_iteration<T>(it, tol, o.max_iters);
+                else if (comm) lcn_iteration_sharded<T>(it, tol, o.max_iters);
                 else lcn_iteration<T>(it, tol, o.max_iters);
             }
             LAUNCH_OK("sinkhorn iteration");
@@ -1599,6 +1799,9 @@ struct Solver {
                                     ") under the " + name + " operator");
             throw Status(4, name + (h.which == 3 ? " transposed matvec" : " matvec") + " produced a nonpositive entry");
         }
+        if (comm)  // row marginals of every slice (the distance needs all of P1)
+            nccl_ok(ncclAllGather(row_marg.get() + rank * cs, row_marg.get(), cs, ncclDouble, comm, s),
+                    "allgather row marginal");
         res.iters = h.iters;
         res.converged = h.converged != 0;
         res.marginal_err_final = h.err;
@@ -1629,6 +1832,7 @@ struct Solver {
     // log_matvec / log_matvec_t (operator.cpp:226-252) on a host vector.
     template <typename T>
     void matvec(const double* h_in, bool transposed, double* h_out) {
+        if (comm) throw Status(2, "log_matvec: not available on a sharded context (use a context without a communicator)");
         alloc();
         const long long len_in = transposed ? n : m, len_out = transposed ? m : n;
         DevBuf<double> vin((len_in + kRT - 1) / kRT * kRT), vout(len_out);
@@ -1701,7 +1905,11 @@ struct Solver {
 };
 
 Solver& solver_of(Op& op) {
-    if (!op.ws) op.ws = std::make_shared<Solver>(op);
+    // rebuild the workspace when the context's communicator changed (the band
+    // plans and row slices depend on rank / world)
+    if (!op.ws || op.ws->comm != static_cast<ncclComm_t>(op.ctx->nccl) || op.ws->rank != op.ctx->rank ||
+        op.ws->world != op.ctx->world)
+        op.ws = std::make_shared<Solver>(op);
     return *op.ws;
 }
 

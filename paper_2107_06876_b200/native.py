@@ -119,6 +119,8 @@ def library() -> C.CDLL:
             "lcn_result_copy": ([P, I, P, C.POINTER(SZ)], I),
             "lcn_distance_lcn": ([P, P, C.POINTER(D)], I),
             "lcn_result_warning": ([P, I], C.c_char_p),
+            "lcn_nccl_unique_id": ([P], I),
+            "lcn_ctx_set_comm": ([P, I, I, P], I),
         }
         for name, (args, res) in sig.items():
             f = getattr(lib, name)
@@ -163,6 +165,14 @@ class Context:
 
     def set_profile(self, on: bool):
         self.check(self.lib.lcn_ctx_set_profile(self.h, 1 if on else 0))
+
+    def set_comm(self, world: int, rank: int, uid: bytes):
+        """Join a sharded solve (lcn_ctx_set_comm): `uid` is rank 0's
+        nccl_unique_id(), broadcast to every rank; collective over the ranks."""
+        if len(uid) != 128:
+            raise InvalidArgument("NCCL unique id must be 128 bytes")
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        self.check(self.lib.lcn_ctx_set_comm(self.h, int(world), int(rank), C.addressof(buf)))
 
     def close(self):
         if getattr(self, "h", None):
@@ -214,6 +224,16 @@ def kmeans_pp_indices(ctx: Context, points, k: int, rng: np.random.Generator | N
     ctx.check(ctx.lib.lcn_kmeans_pp_indices(ctx.h, _p(pts), n, d, k, first, _p(rawa), len(rawa), _p(out),
                                             C.byref(used)))
     return out
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (lcn_nccl_unique_id), to broadcast from rank 0."""
+    lib = library()
+    buf = (C.c_uint8 * 128)()
+    st = lib.lcn_nccl_unique_id(C.addressof(buf))
+    if st != 0:
+        raise CudaError("lcn_nccl_unique_id failed")
+    return bytes(buf)
 
 
 def assign_nearest(ctx: Context, points, centroids):

@@ -1,14 +1,20 @@
-"""Host logic of the multi-GPU path.
+"""Host logic of the multi-GPU path, mirrored from the
+sharded solve in csrc/sinkhorn.cu (Solver::owned_buckets, the row slices and
+lcn_iteration_sharded) so it can be tested with gloo on CPU.
 
-Points are sharded across GPUs by round-1 LSH bucket so that every band-0
-K_sp / K_Delta block stays on one GPU; whole buckets are assigned greedily to
-balance  sum_b n_b m_b + (n_b + m_b) l  (block entries + low-rank rows).
-The only exchange per half-iteration is the low-rank partial: each rank holds
-(h_r, part_r = sum_{own rows} F_row exp(v_row - h_r)), and
-    H = max_r h_r,   mid = sum_r exp(h_r - H) part_r,
-which is exactly the cross-block combine of lowrank_reduce_kernel
-(csrc/sinkhorn.cu) lifted to ranks: one all-reduce(MAX) of h and one
-all-reduce(SUM) of l values (+ the marginal-error scalar) per half-iteration.
+One problem over `world` ranks; every rank holds the operator and the full
+scaling vectors.
+  * Band work: per band and pass, whole buckets go to ranks by
+    longest-processing-time greedy on their streamed bytes (`bucket_owners`).
+    A rank writes the corrections of its buckets' outputs, zeros elsewhere.
+  * Low-rank rows: equal slices of cs = round_up(ceil(n / world), 16) rows
+    (`row_slices`).
+  * Per half-iteration: reduce-scatter of the per-band corrections onto the
+    slices, low-rank pass over the own slice, all-gather of the new log
+    vector, and the cross-rank low-rank combine
+        H = max_r h_r,   mid = sum_r exp(h_r - H) part_r
+    (all-reduce MAX + rescale + all-reduce SUM, `allreduce_lowrank`), plus an
+    all-reduce SUM of the marginal-error partial and the error-flag counts.
 """
 from __future__ import annotations
 
@@ -77,3 +83,27 @@ def max_over_ranks(x: float, group=None) -> float:
     t = torch.tensor([x], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+def bucket_owners(costs, world: int) -> np.ndarray:
+    """Rank per bucket, as Solver::owned_buckets: buckets by decreasing cost
+    (stable), each to the least-loaded rank (ties to the lowest rank)."""
+    costs = np.asarray(costs, dtype=np.float64)
+    order = sorted(range(len(costs)), key=lambda b: -costs[b])  # stable
+    heap = [(0.0, r) for r in range(world)]
+    owner = np.zeros(len(costs), dtype=np.int32)
+    for b in order:
+        load, r = heapq.heappop(heap)
+        owner[b] = r
+        heapq.heappush(heap, (load + float(costs[b]), r))
+    return owner
+
+
+def row_slices(n: int, world: int, align: int = 16):
+    """Equal padded slices of the low-rank rows: (cs, [(lo_r, hi_r)])."""
+    cs = (-(-n // world) + align - 1) // align * align
+    out = []
+    for r in range(world):
+        lo = min(n, r * cs)
+        out.append((lo, min(n, lo + cs)))
+    return cs, out

@@ -172,3 +172,30 @@ def test_lcn_wide_and_split_buckets(ref, fp64):
     res2 = lcn.sinkhorn(op, pm, qm, lcn.SinkhornOptions(tol=0.0, max_iters=pr.iters))
     assert res2.distance == res.distance
     assert np.array_equal(res2.sp_vals, res.sp_vals)
+
+
+@pytest.mark.parametrize("fp64", [False, True])
+def test_sharded_solve_single_rank(ref, fp64):
+    """The sharded solve (§8(e)) through a 1-rank NCCL communicator: every
+    collective call site of the sharded loop runs (reduce-scatter, all-gather,
+    MAX/MIN/SUM all-reduces) and the result matches the unsharded solve and
+    the reference."""
+    pr = configs.config3(0.002)
+    pm, qm = pr.marginals()
+    cfg = lcn.LshConfig(pr.bands, 1, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
+    c = lcn.Context(0, store_fp64=fp64)
+    op = lcn.KernelOperator.lcn_lsh(c, pr.p, pr.q, pr.cost, pr.lam_eff, cfg, pr.landmarks, lcn.LANDMARK_KMEANS,
+                                    pr.landmark_seed)
+    opts = lcn.SinkhornOptions(tol=0.0, max_iters=pr.iters)
+    base = lcn.sinkhorn(op, pm, qm, opts)
+    c.set_comm(1, 0, lcn.nccl_unique_id())
+    res = lcn.sinkhorn(op, pm, qm, opts)
+    tol = 1e-12 if fp64 else 1e-9
+    assert rel(res.distance, base.distance) <= tol
+    assert rel(res.sp_vals, base.sp_vals) <= tol
+    pairs = ref.lsh_pairs(pr.p, pr.q, pr.bands, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
+    rop = ref.op_lcn(pr.p, pr.q, pr.cost, pr.lam_eff, pairs, pr.landmarks, 0, pr.landmark_seed)
+    rres = rop.sinkhorn(pm, qm, tol=0.0, max_iters=pr.iters)
+    assert rel(res.distance, rres.distance) <= (REL_FP64 if fp64 else REL_FP32)
+    with pytest.raises(lcn.InvalidArgument, match="sharded"):
+        op.log_matvec(np.zeros(pr.m))
