@@ -189,7 +189,7 @@ def run_reference(args, rank, world):
             "cpu_baseline": {"value": value, "unit": "iter/s", "cores": cpu_cores(), "kind": "reference",
                              "sample": sample, "phases_s": parts},
             "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -415,11 +415,27 @@ def run_ours(args, rank, world, local_rank):
                                        "ms_per_iteration": t_iter * 1e3},
                 "phases_ms_per_iteration": per_it,
                 "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": gpu_launches}
-        print(json.dumps(line), flush=True)
+        emit(line)
     return 0
 
 
+_OUT_FD = None
+
+
+def emit(line):
+    """Write the one JSON line to the original stdout (everything else, e.g.
+    NCCL's version banner, goes to stderr)."""
+    data = (json.dumps(line) + "\n").encode()
+    os.write(_OUT_FD if _OUT_FD is not None else 1, data)
+
+
 def main():
+    global _OUT_FD
+    # libraries (NCCL banners, ...) print to fd 1: send fd 1 to stderr and keep
+    # the original stdout for the JSON line
+    sys.stdout.flush()
+    _OUT_FD = os.dup(1)
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
