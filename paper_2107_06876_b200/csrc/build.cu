@@ -22,6 +22,9 @@
 #include <limits>
 #include <numeric>
 #include <optional>
+#include <functional>
+#include <thread>
+#include <exception>
 #include <random>
 
 #include "kmeans.cuh"
@@ -191,9 +194,50 @@ __global__ void narrow_kernel(uint32_t* __restrict__ out, const uint64_t* __rest
 // lsh_neighbor_pairs' k-means branch (lsh.cpp:245-283): per band, per
 // function, hash_kmeans of the union with fn_seed(seed, band, fn); composite
 // ids are mixed-radix over the r functions.
+// Independent build stages (the k-means of each LSH band, the landmark
+// k-means) run concurrently: one host thread and one non-blocking stream per
+// job, each on its own copy of the context. Their seeding walks are
+// latency-bound single-CTA kernels, so the jobs overlap well. Results do not
+// depend on the overlap (every job is deterministic on its own).
+void run_jobs(Ctx& ctx, std::vector<std::function<void(Ctx&)>>& jobs) {
+    if (jobs.size() == 1) {
+        jobs[0](ctx);
+        return;
+    }
+    ctx.sync();  // inputs are ready on the caller's stream
+    std::vector<Ctx> ctxs(jobs.size(), ctx);
+    std::vector<std::exception_ptr> errs(jobs.size());
+    for (auto& c : ctxs) {
+        c.own_stream = nullptr;
+        c.nccl = nullptr;
+        CUDA_OK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    }
+    std::vector<std::thread> th;
+    for (size_t i = 0; i < jobs.size(); ++i)
+        th.emplace_back([&, i] {
+            try {
+                CUDA_OK(cudaSetDevice(ctx.device));
+                alloc_stream() = ctxs[i].stream;
+                jobs[i](ctxs[i]);
+                CUDA_OK(cudaStreamSynchronize(ctxs[i].stream));
+            } catch (...) {
+                errs[i] = std::current_exception();
+            }
+        });
+    for (auto& t : th) t.join();
+    for (auto& c : ctxs) cudaStreamDestroy(c.stream);
+    for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
+}
+
+// lsh_neighbor_pairs' k-means branch (lsh.cpp:245-283): per band, per
+// function, hash_kmeans of the union with fn_seed(seed, band, fn); composite
+// ids are mixed-radix over the r functions. Bands run as concurrent jobs,
+// together with `extra` (the landmark k-means) when given.
 void lsh_kmeans_bucket_ids(Ctx& ctx, const double* d_union, const float* d_union32, size_t n, size_t m, size_t d,
-                           int bands, int rows,
-                           int buckets, int iters, uint64_t seed, std::vector<DevBuf<uint32_t>>& ids, size_t& range) {
+                           int bands, int rows, int buckets, int iters, uint64_t seed,
+                           std::vector<DevBuf<uint32_t>>& ids, size_t& range,
+                           const std::function<void(Ctx&)>& extra) {
     const size_t N = n + m;
     if (bands < 1 || rows < 1) throw Status(2, "lsh: bands and rows_per_band must be >= 1");
     if (buckets < 2) throw Status(2, "lsh: buckets_per_fn must be >= 2");
@@ -201,28 +245,35 @@ void lsh_kmeans_bucket_ids(Ctx& ctx, const double* d_union, const float* d_union
     double r = std::pow(static_cast<double>(buckets), rows);
     if (r > 4294967295.0) throw Status(2, "lsh: composite bucket range exceeds 2^32 on this path");
     range = static_cast<size_t>(r);
-    cudaStream_t s = ctx.stream;
-    DevBuf<double> ctr(static_cast<size_t>(buckets) * d);
-    DevBuf<uint32_t> assign(N);
-    DevBuf<uint64_t> comp(N);
     ids.clear();
-    for (int b = 0; b < bands; ++b) {
-        comp.zero(s);
-        for (int fn = 0; fn < rows; ++fn) {
-            PhaseTimer pt(ctx, "lsh k-means (one band function)");
-            if (d_union32)
-                lloyd_device<float>(ctx, d_union32, N, static_cast<int>(d), buckets, iters, fn_seed(seed, b, fn),
-                                    ctr.get(), assign.get());
-            else
-                lloyd_device<double>(ctx, d_union, N, static_cast<int>(d), buckets, iters, fn_seed(seed, b, fn),
-                                     ctr.get(), assign.get());
-            compose_kernel<<<ceil_div(N, 256), 256, 0, s>>>(comp.get(), assign.get(), N, static_cast<uint64_t>(buckets));
-        }
-        DevBuf<uint32_t> out(N);
-        narrow_kernel<<<ceil_div(N, 256), 256, 0, s>>>(out.get(), comp.get(), N);
-        LAUNCH_OK("lsh ids");
-        ids.push_back(std::move(out));
-    }
+    ids.resize(bands);
+    std::vector<std::function<void(Ctx&)>> jobs;
+    for (int b = 0; b < bands; ++b)
+        jobs.push_back([&, b](Ctx& jc) {
+            cudaStream_t s = jc.stream;
+            DevBuf<double> ctr(static_cast<size_t>(buckets) * d);
+            DevBuf<uint32_t> assign(N);
+            DevBuf<uint64_t> comp(N);
+            comp.zero(s);
+            for (int fn = 0; fn < rows; ++fn) {
+                PhaseTimer pt(jc, "lsh k-means (one band function)");
+                if (d_union32)
+                    lloyd_device<float>(jc, d_union32, N, static_cast<int>(d), buckets, iters, fn_seed(seed, b, fn),
+                                        ctr.get(), assign.get());
+                else
+                    lloyd_device<double>(jc, d_union, N, static_cast<int>(d), buckets, iters, fn_seed(seed, b, fn),
+                                         ctr.get(), assign.get());
+                compose_kernel<<<ceil_div(N, 256), 256, 0, s>>>(comp.get(), assign.get(), N,
+                                                                static_cast<uint64_t>(buckets));
+            }
+            DevBuf<uint32_t> out(N);
+            narrow_kernel<<<ceil_div(N, 256), 256, 0, s>>>(out.get(), comp.get(), N);
+            LAUNCH_OK("lsh ids");
+            jc.sync();
+            ids[b] = std::move(out);
+        });
+    if (extra) jobs.push_back(extra);
+    run_jobs(ctx, jobs);
     ctx.sync();
 }
 
@@ -595,37 +646,50 @@ __global__ void gather_rows_kernel(const double* __restrict__ X, const uint32_t*
 
 }  // namespace
 
+// select_landmarks (nystrom.cpp:28-48) into op.L, on the given context (the
+// build runs it as a job concurrent with the LSH k-means).
+void select_landmarks_device(Op& op, Ctx& ctx, int method, uint64_t seed) {
+    cudaStream_t s = ctx.stream;
+    const size_t d = op.d, l = op.l, N = op.n + op.m;
+    if (l < 1 || l > N) throw Status(2, "select_landmarks: l out of range");
+    PhaseTimer pt(ctx, "landmarks");
+    op.L.resize(l * d);
+    if (method == 0) {
+        DevBuf<uint32_t> asg(N);
+        if (op.X32.size())
+            lloyd_device<float>(ctx, op.X32.get(), N, static_cast<int>(d), static_cast<int>(l), 10, seed, op.L.get(),
+                                asg.get());
+        else
+            lloyd_device<double>(ctx, op.X.get(), N, static_cast<int>(d), static_cast<int>(l), 10, seed, op.L.get(),
+                                 asg.get());
+    } else {
+        std::mt19937_64 rng(seed);
+        std::uniform_int_distribution<std::size_t> first(0, N - 1);
+        uint64_t f = first(rng);
+        std::vector<unsigned long long> raw(l > 1 ? l - 1 : 0);
+        for (auto& r : raw) r = rng();
+        DevBuf<uint32_t> rows(l);
+        kmeans_pp_device<double>(ctx, op.X.get(), N, static_cast<int>(d), static_cast<int>(l), f, raw, rows.get(),
+                                 nullptr);
+        gather_rows_kernel<<<ceil_div(l * d, 256), 256, 0, s>>>(op.X.get(), rows.get(), static_cast<int>(l),
+                                                                 static_cast<int>(d), op.L.get());
+        LAUNCH_OK("landmark rows");
+    }
+    ctx.sync();
+}
+
 void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed) {
     Ctx& ctx = *op.ctx;
     cudaStream_t s = ctx.stream;
     const size_t n = op.n, m = op.m, d = op.d, l = op.l, N = n + m;
     if (!(op.lambda > 0.0)) throw Status(2, "build_factors: lambda must be positive");
-    op.L.resize(l * d);
     if (h_landmarks) {
+        op.L.resize(l * d);
         op.L.upload(h_landmarks, l * d, s);
-    } else {
-        // select_landmarks (nystrom.cpp:28-48)
-        if (l < 1 || l > N) throw Status(2, "select_landmarks: l out of range");
-        PhaseTimer pt(ctx, "landmarks");
-        if (method == 0) {
-            DevBuf<uint32_t> asg(N);
-            if (op.X32.size())
-                lloyd_device<float>(ctx, op.X32.get(), N, static_cast<int>(d), static_cast<int>(l), 10, seed, op.L.get(), asg.get());
-            else
-                lloyd_device<double>(ctx, op.X.get(), N, static_cast<int>(d), static_cast<int>(l), 10, seed, op.L.get(), asg.get());
-        } else {
-            std::mt19937_64 rng(seed);
-            std::uniform_int_distribution<std::size_t> first(0, N - 1);
-            uint64_t f = first(rng);
-            std::vector<unsigned long long> raw(l > 1 ? l - 1 : 0);
-            for (auto& r : raw) r = rng();
-            DevBuf<uint32_t> rows(l);
-            kmeans_pp_device<double>(ctx, op.X.get(), N, static_cast<int>(d), static_cast<int>(l), f, raw, rows.get(), nullptr);
-            gather_rows_kernel<<<ceil_div(l * d, 256), 256, 0, s>>>(op.X.get(), rows.get(), static_cast<int>(l),
-                                                                     static_cast<int>(d), op.L.get());
-            LAUNCH_OK("landmark rows");
-        }
+    } else if (!op.landmarks_ready) {
+        select_landmarks_device(op, ctx, method, seed);
     }
+    op.landmarks_ready = false;
     ctx.sync();
     PhaseTimer ptf(ctx, "nystrom factors U, V, A, W");
     const double* nrm = union_norms(op);

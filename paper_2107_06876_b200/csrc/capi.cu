@@ -398,10 +398,17 @@ int lcn_op_lcn_lsh(lcn_ctx* ctx, const double* p, size_t n, const double* q, siz
         upload_union(h->o, p, n, q, m, d);
         std::vector<DevBuf<uint32_t>> ids;
         size_t range = 0;
-        lsh_kmeans_bucket_ids(ctx->c, h->o.X.get(), h->o.X32.size() ? h->o.X32.get() : nullptr, n, m, d, cfg->bands, cfg->rows_per_band, cfg->buckets_per_fn,
-                              cfg->kmeans_iters, cfg->seed, ids, range);
-        bands_from_union_ids(h->o, ids, range);
-        finish_lcn(h->o, nullptr, l, landmark_method, landmark_seed);
+        Op& o = h->o;
+        o.l = l;
+        auto landmarks_job = [&](Ctx& jc) {
+            select_landmarks_device(o, jc, landmark_method, landmark_seed);
+            o.landmarks_ready = true;
+        };
+        lsh_kmeans_bucket_ids(ctx->c, o.X.get(), o.X32.size() ? o.X32.get() : nullptr, n, m, d, cfg->bands,
+                              cfg->rows_per_band, cfg->buckets_per_fn, cfg->kmeans_iters, cfg->seed, ids, range,
+                              landmarks_job);
+        bands_from_union_ids(o, ids, range);
+        finish_lcn(o, nullptr, l, landmark_method, landmark_seed);
         *out = h.release();
     });
 }
@@ -442,8 +449,16 @@ int lcn_op_create_device(lcn_ctx* ctx, const float* d_p, size_t n, const float* 
         LAUNCH_OK("promote");
         std::vector<DevBuf<uint32_t>> ids;
         size_t range = 0;
-        lsh_kmeans_bucket_ids(ctx->c, op.X.get(), op.X32.size() ? op.X32.get() : nullptr, n, m, d, cfg->bands, cfg->rows_per_band, cfg->buckets_per_fn,
-                              cfg->kmeans_iters, cfg->seed, ids, range);
+        op.l = l;
+        std::function<void(Ctx&)> landmarks_job;
+        if (l)
+            landmarks_job = [&](Ctx& jc) {
+                select_landmarks_device(op, jc, landmark_method, landmark_seed);
+                op.landmarks_ready = true;
+            };
+        lsh_kmeans_bucket_ids(ctx->c, op.X.get(), op.X32.size() ? op.X32.get() : nullptr, n, m, d, cfg->bands,
+                              cfg->rows_per_band, cfg->buckets_per_fn, cfg->kmeans_iters, cfg->seed, ids, range,
+                              landmarks_job);
         bands_from_union_ids(op, ids, range);
         if (l) finish_lcn(op, nullptr, l, landmark_method, landmark_seed);
         else finish_sparse(op);

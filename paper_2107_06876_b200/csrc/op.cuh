@@ -1,5 +1,6 @@
 // Internal operator / result structures and the build + solve entry points.
 #pragma once
+#include <functional>
 
 #include <memory>
 #include <string>
@@ -47,6 +48,7 @@ struct Op {
     const double* Q() const { return X.get() + n * d; }
     DevBuf<float> X32;                    // fp32 copy of X when every coordinate is fp32-exact (k-means reads)
     DevBuf<double> norms;                 // per-point sum x_k^2 (cosine-derived cost only)
+    bool landmarks_ready = false;         // L already selected (concurrently with the LSH k-means)
     std::vector<Band> bands;
     std::vector<DevBuf<double>> val64;    // sparse: log K; lcn: delta (fp64 master)
     std::vector<DevBuf<float>> val32;     // iteration copy (fp32 storage mode)
@@ -90,7 +92,9 @@ struct Result {
 void build_band_layout(Ctx& ctx, Band& B, const uint32_t* d_src_bucket, const uint32_t* d_tgt_bucket, size_t n,
                        size_t m, size_t nb);
 void lsh_kmeans_bucket_ids(Ctx& ctx, const double* d_union, const float* d_union32, size_t n, size_t m, size_t d, int bands, int rows,
-                           int buckets, int iters, uint64_t seed, std::vector<DevBuf<uint32_t>>& ids, size_t& range);
+                           int buckets, int iters, uint64_t seed, std::vector<DevBuf<uint32_t>>& ids, size_t& range,
+                           const std::function<void(Ctx&)>& extra = {});
+void select_landmarks_device(Op& op, Ctx& ctx, int method, uint64_t seed);
 void build_sparse_values(Op& op);
 void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed);
 void build_correction(Op& op);
