@@ -24,6 +24,11 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                  : "memory");
 }
 
+// plain arrive (count 1, release semantics)
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // wait until the barrier's phase with the given parity has completed; the
 // suspend-time hint (ns) lets the waiting warp sleep until the phase flips
 // instead of re-polling (retry spins otherwise take issue slots from the

@@ -13,6 +13,7 @@
 
 #include "../../include/lcn_b200.h"
 #include "kmeans.cuh"
+#include "kmeans_tc.cuh"
 #include "op.cuh"
 
 using namespace lcnb;
@@ -303,6 +304,29 @@ int lcn_assign_nearest(lcn_ctx* ctx, const double* points, size_t n, size_t d, c
         X.upload(points, n * d, ctx->c.stream);
         assign_device<double>(ctx->c, X.get(), n, static_cast<int>(d), C.get(), static_cast<int>(k), a.get());
         a.download(out, n, ctx->c.stream);
+        ctx->c.sync();
+    });
+}
+
+// Test hook (not part of the solver API): raw tensor-core accumulators of the
+// first centroid tile (64 centroids) for the first 128 points of an fp32
+// point set; hh_only = 1 issues only the x_hi . c_hi products.
+extern "C" int lcn_debug_tc_scores(lcn_ctx* ctx, const float* points, size_t n, size_t d, const double* centroids,
+                                   size_t k, int hh_only, float* acc_out) {
+    return guard(ctx, [&] {
+        DevBuf<float> X;
+        DevBuf<double> C;
+        X.upload(points, n * d, ctx->c.stream);
+        C.upload(centroids, k * d, ctx->c.stream);
+        DevBuf<uint32_t> out(std::max<size_t>(n, 1)), amb(std::max<size_t>(n, 1));
+        DevBuf<unsigned> namb(1);
+        DevBuf<float> dbg(128 * 64);
+        namb.zero(ctx->c.stream);
+        dbg.zero(ctx->c.stream);
+        if (!assign_filter_tc(ctx->c, X.get(), n, static_cast<int>(d), C.get(), static_cast<int>(k), out.get(),
+                              amb.get(), namb.get(), dbg.get(), hh_only))
+            throw Status(2, "shape not handled by the tensor-core filter");
+        dbg.download(acc_out, 128 * 64, ctx->c.stream);
         ctx->c.sync();
     });
 }

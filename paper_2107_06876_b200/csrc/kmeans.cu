@@ -14,7 +14,9 @@
 //     farthest point among clusters of size > 1 (kmeans.cpp:122-139).
 #include <cub/cub.cuh>
 
+#include <cstdlib>
 #include <random>
+#include <string>
 #include <type_traits>
 #include <vector>
 
@@ -22,6 +24,7 @@
 #include "async.cuh"
 #include "ctx.cuh"
 #include "kmeans.cuh"
+#include "kmeans_tc.cuh"
 #include "op.cuh"
 #include "tiles.cuh"
 
@@ -944,16 +947,24 @@ void assign_device(Ctx& ctx, const T* X, long long N, int d, const double* C, in
         DevBuf<unsigned> namb(1);
         cmax.zero(s);
         namb.zero(s);
-        filter_prep_kernel<<<Kp, 128, 0, s>>>(C, k, d, Kp, CfT.get(), ncf.get(), cmax.get());
-        static bool attr[64] = {};
-        if (ctx.device >= 64 || !attr[ctx.device]) {
-            CUDA_OK(cudaFuncSetAttribute(assign_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(sizeof(FilterSmem))));
-            if (ctx.device < 64) attr[ctx.device] = true;
+        // tensor-core (tcgen05, 3xTF32) filter; the fp32 FMA filter when the
+        // shape is not handled or LCN_FILTER=fma
+        const char* fsel = std::getenv("LCN_FILTER");
+        const bool fma_only = fsel && std::string(fsel) == "fma";
+        if (fma_only || !assign_filter_tc(ctx, reinterpret_cast<const float*>(X), N, d, C, k, out, amb.get(),
+                                          namb.get())) {
+            filter_prep_kernel<<<Kp, 128, 0, s>>>(C, k, d, Kp, CfT.get(), ncf.get(), cmax.get());
+            static bool attr[64] = {};
+            if (ctx.device >= 64 || !attr[ctx.device]) {
+                CUDA_OK(cudaFuncSetAttribute(assign_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(sizeof(FilterSmem))));
+                if (ctx.device < 64) attr[ctx.device] = true;
+            }
+            assign_filter_kernel<<<ceil_div(N, kFB), 256, sizeof(FilterSmem), s>>>(
+                reinterpret_cast<const float*>(X), N, d, CfT.get(), ncf.get(), Kp, cmax.get(), out, amb.get(),
+                namb.get());
+            LAUNCH_OK("assign_filter_kernel");
         }
-        assign_filter_kernel<<<ceil_div(N, kFB), 256, sizeof(FilterSmem), s>>>(
-            reinterpret_cast<const float*>(X), N, d, CfT.get(), ncf.get(), Kp, cmax.get(), out, amb.get(), namb.get());
-        LAUNCH_OK("assign_filter_kernel");
         unsigned h_amb = 0;
         namb.download(&h_amb, 1, s);
         ctx.sync();

@@ -1,0 +1,310 @@
+// Tensor-core (tcgen05) assignment filter for the k-means of the LSH / landmark
+// build: the fp32 filter of kmeans.cu on the 5th-generation tensor cores.
+//
+// Scores v(c) = |c_f|^2 - 2 x.c_f for 128 points (one CTA) against every
+// centroid, 64 centroids per tile, with the dot products in 3xTF32:
+//   x.c ~ x_hi.c_hi + x_hi.c_lo + x_lo.c_hi   (hi = fp32 with the low 13
+//   mantissa bits cleared, lo = fp32 remainder)
+// accumulated in fp32 in tensor memory. Per point the best and second-best
+// score are kept; a point whose gap exceeds twice the rigorous error bound
+// (tf32 truncation of the lo parts, the dropped lo.lo term, fp32 accumulation,
+// fp32 rounding of c and |c_f|^2, and the fp64 fold of the reference) gets the
+// best centroid; every other point goes to the exact fp64 scan, so the result
+// is bit-identical to kmeans.cpp:67-85.
+//
+// CTA (192 threads, 1 per SM):
+//   warp 0  producer: 1-D bulk copies (TMA) of pre-swizzled centroid tiles
+//           (hi + lo, 64 KB) into a 2-stage shared ring (mbarrier tx counts)
+//   warp 1  owns the TMEM allocation; one elected thread issues
+//           tcgen05.mma.kind::tf32 (A = points from TMEM, B = centroids from
+//           shared memory via UMMA descriptors, D = fp32 accumulators in
+//           TMEM, double-buffered) and tcgen05.commit to the barriers
+//   warps 2-5 epilogue: thread = TMEM lane = point; tcgen05.ld of the 64
+//           accumulators of a tile, running top-2 of the scores
+// TMEM columns: [0,128) x_hi, [128,256) x_lo, [256,320) / [320,384) D.
+#include <cstdint>
+
+#include "async.cuh"
+#include "common.cuh"
+#include "ctx.cuh"
+#include "kmeans_tc.cuh"
+
+namespace lcnb {
+namespace {
+
+constexpr int kTM = 128;        // points per CTA (UMMA_M, TMEM lanes)
+constexpr int kTN = 64;         // centroids per tile (UMMA_N)
+constexpr int kTD = 128;        // padded feature count (tf32 columns)
+constexpr int kTHalf = kTN * kTD * 4;   // bytes of one tile half (hi or lo): 32 KB
+constexpr int kTStage = 2 * kTHalf;     // hi + lo
+constexpr int kTStages = 2;
+constexpr int kTThreads = 192;
+
+// element (r, k) of a swizzled tile half: K-major, 128-byte swizzle atoms of
+// 8 rows x 32 tf32; K blocks of 32 features stacked (kTN rows each)
+__host__ __device__ __forceinline__ uint32_t tile_offset(int r, int k) {
+    const int kb = k >> 5, j = k & 31, chunk = j >> 2, w = j & 3;
+    return static_cast<uint32_t>(kb * (kTN * 128) + r * 128 + ((chunk ^ (r & 7)) << 4) + w * 4);
+}
+
+__device__ __forceinline__ float tf32_hi(float x) {
+    return __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+}
+
+// Centroid tiles: hi and lo halves in the swizzled layout, |c_f|^2 (fp32,
+// +inf for padding), and max_c max(|c|^2, |c_f|^2).
+__global__ void __launch_bounds__(128) tc_prep_kernel(const double* __restrict__ C, int k, int d, int ntile,
+                                                       unsigned char* __restrict__ tiles, float* __restrict__ ncf,
+                                                       unsigned long long* __restrict__ cmax) {
+    __shared__ double r1[4], r2[4];
+    const int c = blockIdx.x;  // centroid (padded to ntile * kTN)
+    const int t = c / kTN, r = c % kTN;
+    unsigned char* hi = tiles + static_cast<size_t>(t) * kTStage;
+    unsigned char* lo = hi + kTHalf;
+    double s1 = 0.0, s2 = 0.0;
+    for (int kk = threadIdx.x; kk < kTD; kk += 128) {
+        const double v = (c < k && kk < d) ? C[static_cast<long long>(c) * d + kk] : 0.0;
+        const float f = static_cast<float>(v);
+        const float h = tf32_hi(f);
+        *reinterpret_cast<float*>(hi + tile_offset(r, kk)) = h;
+        *reinterpret_cast<float*>(lo + tile_offset(r, kk)) = f - h;  // exact
+        s1 += static_cast<double>(f) * static_cast<double>(f);
+        s2 += v * v;
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if ((threadIdx.x & 31) == 0) { r1[threadIdx.x >> 5] = s1; r2[threadIdx.x >> 5] = s2; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        s1 = r1[0] + r1[1] + r1[2] + r1[3];
+        s2 = r2[0] + r2[1] + r2[2] + r2[3];
+        ncf[c] = c < k ? static_cast<float>(s1) : kPosInf;
+        if (c < k) atomicMax(cmax, static_cast<unsigned long long>(__double_as_longlong(fmax(s1, s2))));
+    }
+}
+
+// ---- tcgen05 / TMEM primitives (inline PTX, sm_100a) -----------------------
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row groups 1024 B
+// apart (SBO), version 1 (sm_100), base offset 0 (atoms 1024-byte aligned)
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+    uint64_t desc = 0;
+    desc |= static_cast<uint64_t>((saddr >> 4) & 0x3fffu);          // start address
+    desc |= static_cast<uint64_t>(1u) << 16;                         // LBO (unused for K-major swizzle)
+    desc |= static_cast<uint64_t>(1024u >> 4) << 32;                 // SBO
+    desc |= static_cast<uint64_t>(1u) << 46;                         // descriptor version (sm_100)
+    desc |= static_cast<uint64_t>(2u) << 61;                         // SWIZZLE_128B
+    return desc;
+}
+
+// instruction descriptor: D f32, A/B tf32, both K-major, N = kTN, M = kTM
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(kTN >> 3) << 17) |
+                            (static_cast<uint32_t>(kTM >> 4) << 24);
+
+__device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(kIdesc), "r"(acc)
+        : "memory");
+}
+
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tc_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31]) : "memory");
+}
+
+__device__ __forceinline__ void tc_ld64(uint32_t taddr, uint32_t (&r)[64]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32, %33, %34, %35, %36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, %48, %49, %50, %51, %52, %53, %54, %55, %56, %57, %58, %59, %60, %61, %62, %63}, [%64];" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63]) : "r"(taddr) : "memory");
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kTThreads, 1) assign_filter_tc_kernel(
+    const float* __restrict__ X, long long N, int d, const unsigned char* __restrict__ tiles,
+    const float* __restrict__ ncf, int ntile, const unsigned long long* __restrict__ cmax,
+    uint32_t* __restrict__ out, uint32_t* __restrict__ amb, unsigned* __restrict__ namb,
+    float* __restrict__ dbg, int hh_only) {
+    // all shared memory is dynamic (no static __shared__): the stage ring must
+    // sit on 1024-byte swizzle-atom boundaries of the shared window
+    extern __shared__ __align__(1024) unsigned char dyn_raw[];
+    const uint32_t raw = smem_u32(dyn_raw);
+    unsigned char* ring = dyn_raw + ((1024u - (raw & 1023u)) & 1023u);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kTStages * kTStage);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kTStages;
+    uint64_t* tfull = bars + 2 * kTStages;
+    uint64_t* tempty = bars + 2 * kTStages + 2;
+    uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 2 * kTStages + 4);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long p0 = static_cast<long long>(blockIdx.x) * kTM;
+
+    if (warp == 1) {  // TMEM: all 512 columns (one CTA per SM)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        for (int s = 0; s < kTStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 128);
+        }
+        fence_mbar_init();
+    }
+    // epilogue threads: own point row -> TMEM lane (hi, lo), |x|^2
+    double xn = 0.0;
+    const int eq = warp - 2;               // epilogue warp 0..3
+    const int lane_base = 32 * (warp & 3);  // TMEM lanes this warp may access
+    const int row = lane_base + lane;      // point within the CTA tile
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+    if (eq >= 0) {
+        const long long p = p0 + row;
+        const float* xr = X + p * d;
+        for (int c0 = 0; c0 < kTD; c0 += 32) {
+            uint32_t vh[32], vl[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const int kk = c0 + j;
+                const float x = (p < N && kk < d) ? xr[kk] : 0.0f;
+                const float h = tf32_hi(x);
+                vh[j] = __float_as_uint(h);
+                vl[j] = __float_as_uint(x - h);
+                xn += static_cast<double>(x) * static_cast<double>(x);
+            }
+            tc_st32(tmem + (static_cast<uint32_t>(lane_base) << 16) + c0, vh);
+            tc_st32(tmem + (static_cast<uint32_t>(lane_base) << 16) + kTD + c0, vl);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    if (warp == 0) {
+        // ---------------- producer ----------------
+        if (lane == 0) {
+            for (int t = 0; t < ntile; ++t) {
+                const int s = t % kTStages;
+                if (t >= kTStages) mbar_wait(&empty[s], ((t / kTStages) - 1) & 1);
+                mbar_arrive_expect_tx(&full[s], kTStage);
+                bulk_g2s(ring + s * kTStage, tiles + static_cast<size_t>(t) * kTStage, kTHalf, &full[s]);
+                bulk_g2s(ring + s * kTStage + kTHalf, tiles + static_cast<size_t>(t) * kTStage + kTHalf, kTHalf,
+                         &full[s]);
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
+            for (int t = 0; t < ntile; ++t) {
+                const int s = t % kTStages, b = t & 1;
+                mbar_wait(&full[s], (t / kTStages) & 1);
+                if (t >= 2) mbar_wait(&tempty[b], ((t >> 1) - 1) & 1);
+                tc_fence_after();
+                const uint32_t dt = tmem + 256 + b * kTN;
+                const uint32_t bh = smem_u32(ring + s * kTStage), bl = bh + kTHalf;
+#pragma unroll
+                for (int ks = 0; ks < kTD / 8; ++ks) {
+                    const uint32_t off = (ks >> 2) * (kTN * 128) + (ks & 3) * 32;
+                    const uint64_t dh = umma_desc_sw128(bh + off), dl = umma_desc_sw128(bl + off);
+                    tc_mma_tf32(dt, tmem + ks * 8, dh, ks > 0 ? 1u : 0u);   // x_hi . c_hi
+                    if (!hh_only) {
+                        tc_mma_tf32(dt, tmem + ks * 8, dl, 1u);             // x_hi . c_lo
+                        tc_mma_tf32(dt, tmem + kTD + ks * 8, dh, 1u);       // x_lo . c_hi
+                    }
+                }
+                tc_commit(&empty[s]);  // stage consumed once these MMAs complete
+                tc_commit(&tfull[b]);  // accumulator ready
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---------------- epilogue: thread = point ----------------
+        float v1 = kPosInf, v2 = kPosInf;
+        int i1 = 0;
+        for (int t = 0; t < ntile; ++t) {
+            const int b = t & 1;
+            mbar_wait(&tfull[b], (t >> 1) & 1);
+            tc_fence_after();
+            uint32_t r[64];
+            tc_ld64(tmem + (static_cast<uint32_t>(lane_base) << 16) + 256 + b * kTN, r);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            tc_fence_before();
+            mbar_arrive(&tempty[b]);
+            if (dbg && blockIdx.x == 0 && t == 0)  // test hook: raw accumulators of tile 0
+                for (int j = 0; j < kTN; ++j) dbg[row * kTN + j] = __uint_as_float(r[j]);
+            const float4* nc4 = reinterpret_cast<const float4*>(ncf + t * kTN);
+#pragma unroll
+            for (int j4 = 0; j4 < kTN / 4; ++j4) {
+                const float4 nc = __ldg(nc4 + j4);
+                const float ncj[4] = {nc.x, nc.y, nc.z, nc.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int j = 4 * j4 + u;
+                    const float v = fmaf(-2.0f, __uint_as_float(r[j]), ncj[u]);
+                    if (v < v1) { v2 = v1; v1 = v; i1 = t * kTN + j; }
+                    else if (v < v2) v2 = v;
+                }
+            }
+        }
+        const long long p = p0 + row;
+        if (p < N) {
+            const double u = 5.9604644775390625e-08;  // 2^-24
+            const double C = sqrt(__longlong_as_double(*cmax)) * (1.0 + 1e-12);
+            const double x = sqrt(xn) * (1.0 + 1e-12);
+            // 2 x.c term: 3xTF32 (lo truncation 2 x 2^-20, dropped lo.lo 2^-20) and
+            // fp32 tensor-core accumulation (<= 56 roundings of 2^-23), doubled
+            const double dot_rel = 2.0 * (3.0 * 9.5367431640625e-07 + 56.0 * 1.1920928955078125e-07);
+            const double E = 1.05 * ((dot_rel + 4.0 * u) * x * C + 4.0 * u * C * C + u * u * C * C) +
+                             1e-12 * (x + C) * (x + C);
+            const double gap = static_cast<double>(v2) - static_cast<double>(v1);
+            if (gap > 2.0 * E) out[p] = static_cast<uint32_t>(i1);
+            else amb[atomicAdd(namb, 1u)] = static_cast<uint32_t>(p);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+}
+
+// Host side: prepare the centroid tiles and launch. Returns false when the
+// shape is not handled (d > kTD).
+bool assign_filter_tc(Ctx& ctx, const float* X, long long N, int d, const double* C, int k, uint32_t* out,
+                      uint32_t* amb, unsigned* namb, float* dbg_acc, int hh_only) {
+    if (d > kTD || d < 1) return false;
+    cudaStream_t s = ctx.stream;
+    const int ntile = static_cast<int>(ceil_div(k, kTN));
+    DevBuf<unsigned char> tiles(static_cast<size_t>(ntile) * kTStage);
+    DevBuf<float> ncf(static_cast<size_t>(ntile) * kTN);
+    DevBuf<unsigned long long> cmax(1);
+    cmax.zero(s);
+    tc_prep_kernel<<<ntile * kTN, 128, 0, s>>>(C, k, d, ntile, tiles.get(), ncf.get(), cmax.get());
+    const int smem = kTStages * kTStage + 1024 + 128;
+    static bool attr[64] = {};
+    if (ctx.device >= 64 || !attr[ctx.device]) {
+        CUDA_OK(cudaFuncSetAttribute(assign_filter_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        if (ctx.device < 64) attr[ctx.device] = true;
+    }
+    assign_filter_tc_kernel<<<ceil_div(N, kTM), kTThreads, smem, s>>>(X, N, d, tiles.get(), ncf.get(), ntile,
+                                                                      cmax.get(), out, amb, namb, dbg_acc, hh_only);
+    LAUNCH_OK("assign_filter_tc_kernel");
+    return true;
+}
+
+}  // namespace lcnb

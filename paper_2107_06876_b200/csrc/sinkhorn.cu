@@ -87,9 +87,6 @@ __device__ __forceinline__ double ld1(const double* p) { return __ldg(p); }
 // consumer-only barrier (producer warps never join)
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory"); }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 
 // ---------------------------------------------------------------------------
 // Sparse (log-domain) band kernels: per bucket block, per row / column
