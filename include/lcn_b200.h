@@ -179,6 +179,17 @@ int lcn_op_lcn_buckets(lcn_ctx* ctx, const double* p, size_t n, const double* q,
 int lcn_op_create_device(lcn_ctx* ctx, const float* d_p, size_t n, const float* d_q, size_t m, size_t d,
                          int cost, double lambda, const lcn_lsh_config* cfg, size_t l, int landmark_method,
                          uint64_t landmark_seed, lcn_op** out);
+/* Dense operator (configs[2] anchor): build_cost + build_kernel +
+ * KernelOperator::dense (geometry.cpp:113-144, operator.cpp:55-64); log K of
+ * every pair from the sequential fp64 fold (bit-exact). The plan of a dense
+ * solve is the full n x m matrix (lcn_result_copy which 4, row-major). */
+int lcn_op_dense(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m, size_t d, int cost,
+                 double lambda, lcn_op** out);
+/* Same from device-resident fp32 points (timing runs). */
+int lcn_op_dense_device(lcn_ctx* ctx, const float* d_p, size_t n, const float* d_q, size_t m, size_t d, int cost,
+                        double lambda, lcn_op** out);
+/* DenseKernel::logk (n x m, row-major). */
+int lcn_op_export_dense(lcn_op* op, double* out);
 int lcn_op_destroy(lcn_op* op);
 int lcn_op_get_info(const lcn_op* op, lcn_op_info_t* info);
 /* CSR export in the reference's order (rows ascending, columns ascending,

@@ -213,6 +213,11 @@ class Op:
         self.lib.check(self.lib.fn("op_copy", _P, _I, _P, _P, _P)(self.h, which, _ptr(rp), _ptr(col), _ptr(val)))
         return rp, col, val
 
+    def dense_logk(self):
+        out = np.zeros((self.n, self.m))
+        self.lib.check(self.lib.fn("op_copy", _P, _I, _P, _P, _P)(self.h, 7, None, None, _ptr(out)))
+        return out
+
     def dense_factor(self, which):
         shape = {2: (self.n, self.l), 3: (self.l, self.m)}[which]
         out = np.zeros(shape)
@@ -268,6 +273,7 @@ class Result:
     sparse_vals = property(lambda s: s._v(4))
     sp_vals = property(lambda s: s._v(5))
     sp_nys_vals = property(lambda s: s._v(6))
+    dense_plan = property(lambda s: s._v(9))
 
     def distance_lcn(self):
         out = C.c_double()

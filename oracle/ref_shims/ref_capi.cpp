@@ -305,6 +305,10 @@ int ref_op_copy(void* h, int which, std::uint32_t* row_ptr, std::uint32_t* col, 
         std::memcpy(vals, r->landmarks.data(), r->landmarks.size() * 8);
         return 0;
     }
+    if (which == 7 && r->op.dense_kernel()) {  // DenseKernel::logk, n x m row-major
+        std::memcpy(vals, r->op.dense_kernel()->logk.data.data(), r->op.dense_kernel()->logk.data.size() * 8);
+        return 0;
+    }
     g_err = "ref_op_copy: nothing to copy";
     return 2;
 }
@@ -353,7 +357,7 @@ double ref_result_scalar(void* h, int which) {
 }
 
 // 0 log_s, 1 log_t, 2 row_marginal, 3 marginal_err trace, 4 sparse plan vals,
-// 5 lcn sp_vals, 6 lcn sp_nys_vals, 7 P_U (n x l), 8 P_W (l x m)
+// 5 lcn sp_vals, 6 lcn sp_nys_vals, 7 P_U (n x l), 8 P_W (l x m), 9 dense plan (n x m)
 std::size_t ref_result_copy(void* h, int which, double* out) {
     auto* s = static_cast<SinkhornResult*>(h);
     const std::vector<double>* v = nullptr;
@@ -367,6 +371,7 @@ std::size_t ref_result_copy(void* h, int which, double* out) {
         case 6: v = &s->plan.sp_nys_vals; break;
         case 7: if (s->plan.p_u) v = &s->plan.p_u->data; break;
         case 8: if (s->plan.p_w) v = &s->plan.p_w->data; break;
+        case 9: if (s->plan.dense) v = &s->plan.dense->data; break;
     }
     if (!v) return 0;
     if (out) std::memcpy(out, v->data(), v->size() * 8);

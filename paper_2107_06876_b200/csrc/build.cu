@@ -427,6 +427,24 @@ struct EpiExp {
     }
 };
 
+// dense log K (build_cost + build_kernel, geometry.cpp:113-144):
+// logk = 0.0 - c * inv with c the sequential-fold cost of the pair
+struct EpiDenseLogK {
+    static constexpr bool kReduce = false;
+    double* out;
+    long long ld;
+    int kind;
+    double inv;
+    const double* na;
+    const double* nb;
+    int* bad;
+    __device__ double operator()(long long r, long long c, double acc) const {
+        const double cst = cost_from_fold(kind, acc, na ? na[r] : 0.0, nb ? nb[c] : 0.0, bad);
+        out[r * ld + c] = xsub(0.0, xmul(cst, inv));
+        return 0.0;
+    }
+};
+
 struct EpiStore {
     static constexpr bool kReduce = false;
     double* out;
@@ -645,6 +663,60 @@ __global__ void gather_rows_kernel(const double* __restrict__ X, const uint32_t*
 }
 
 }  // namespace
+
+namespace {
+template <typename T>
+__global__ void __launch_bounds__(256) dense_transpose_kernel(const double* __restrict__ in, long long rows,
+                                                              long long cols, T* __restrict__ out, T* __restrict__ copy) {
+    __shared__ double tile[32][33];
+    const long long r0 = static_cast<long long>(blockIdx.y) * 32, c0 = static_cast<long long>(blockIdx.x) * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int r = ty; r < 32; r += 8) {
+        const long long i = r0 + r, j = c0 + tx;
+        const double v = (i < rows && j < cols) ? in[i * cols + j] : 0.0;
+        tile[r][tx] = v;
+        if (copy && i < rows && j < cols) copy[i * cols + j] = static_cast<T>(v);
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+        const long long j = c0 + r, i = r0 + tx;
+        if (j < cols && i < rows) out[j * rows + i] = static_cast<T>(tile[tx][r]);
+    }
+}
+}  // namespace
+
+// Dense operator (KernelOperator::dense, operator.cpp:55-64): exact fp64 log K
+// of every pair by the tiled sequential-fold kernel, then the iteration copies
+// (fp32 or fp64) in both orientations so both half-iterations stream rows.
+void build_dense(Op& op) {
+    Ctx& ctx = *op.ctx;
+    PhaseTimer pt(ctx, "dense log K");
+    const size_t n = op.n, m = op.m, d = op.d;
+    if (!(op.lambda > 0.0)) throw Status(2, "build_kernel: lambda must be positive");
+    const double* nrm = union_norms(op);
+    DevBuf<int> bad(1);
+    bad.zero(ctx.stream);
+    op.dk64.resize(std::max<size_t>(n * m, 1));
+    EpiDenseLogK epi{op.dk64.get(), static_cast<long long>(m), op.cost, 1.0 / op.lambda, nrm, nrm ? nrm + n : nullptr,
+                     bad.get()};
+    if (op.cost == 1 || op.cost == 2)
+        launch_dense_tiles<1>(ctx, op.P(), n, op.Q(), m, static_cast<int>(d), epi);
+    else
+        launch_dense_tiles<0>(ctx, op.P(), n, op.Q(), m, static_cast<int>(d), epi);
+    if (read_flag(ctx, bad)) throw Status(2, "cosine-derived cost undefined for zero vectors");
+    const dim3 grid(static_cast<unsigned>(ceil_div(m, 32)), static_cast<unsigned>(ceil_div(n, 32)));
+    if (op.fp64) {
+        op.dk64T.resize(std::max<size_t>(n * m, 1));
+        dense_transpose_kernel<double><<<grid, 256, 0, ctx.stream>>>(op.dk64.get(), n, m, op.dk64T.get(), nullptr);
+    } else {
+        op.dk32.resize(std::max<size_t>(n * m, 1));
+        op.dk32T.resize(std::max<size_t>(n * m, 1));
+        dense_transpose_kernel<float><<<grid, 256, 0, ctx.stream>>>(op.dk64.get(), n, m, op.dk32T.get(), op.dk32.get());
+    }
+    LAUNCH_OK("dense log K");
+    op.nnz = n * m;
+    ctx.sync();
+}
 
 // select_landmarks (nystrom.cpp:28-48) into op.L, on the given context (the
 // build runs it as a job concurrent with the LSH k-means).

@@ -452,6 +452,52 @@ int lcn_op_lcn_buckets(lcn_ctx* ctx, const double* p, size_t n, const double* q,
     });
 }
 
+int lcn_op_dense(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m, size_t d, int cost,
+                 double lambda, lcn_op** out) {
+    return guard(ctx, [&] {
+        check_cost_lambda(cost, lambda, "build_cost");
+        check_points(p, n, d, "p");
+        check_points(q, m, d, "q");
+        std::unique_ptr<lcn_op> h(new_op(ctx, cost, lambda));
+        upload_union(h->o, p, n, q, m, d);
+        h->o.kind = LCN_OP_DENSE;
+        build_dense(h->o);
+        *out = h.release();
+    });
+}
+
+int lcn_op_dense_device(lcn_ctx* ctx, const float* d_p, size_t n, const float* d_q, size_t m, size_t d, int cost,
+                        double lambda, lcn_op** out) {
+    return guard(ctx, [&] {
+        check_cost_lambda(cost, lambda, "build_cost");
+        if (n == 0 || m == 0 || d == 0) throw Status(2, "point set is empty");
+        std::unique_ptr<lcn_op> h(new_op(ctx, cost, lambda));
+        Op& op = h->o;
+        op.n = n;
+        op.m = m;
+        op.d = d;
+        op.X.resize((n + m) * d);
+        promote_kernel<<<std::min<long long>(ceil_div(n * d, 256), 8 * ctx->c.num_sms), 256, 0, ctx->c.stream>>>(
+            d_p, op.X.get(), n * d);
+        promote_kernel<<<std::min<long long>(ceil_div(m * d, 256), 8 * ctx->c.num_sms), 256, 0, ctx->c.stream>>>(
+            d_q, op.X.get() + n * d, m * d);
+        LAUNCH_OK("promote");
+        op.kind = LCN_OP_DENSE;
+        build_dense(op);
+        *out = h.release();
+    });
+}
+
+int lcn_op_export_dense(lcn_op* op, double* out) {
+    lcn_ctx* ctx = op ? reinterpret_cast<lcn_ctx*>(op->o.ctx) : nullptr;
+    return guard(ctx, [&] {
+        if (!op || !out) throw Status(2, "null operator or buffer");
+        if (op->o.kind != LCN_OP_DENSE) throw Status(2, "export_dense: not a dense operator");
+        op->o.dk64.download(out, op->o.n * op->o.m, op->o.ctx->stream);
+        op->o.ctx->sync();
+    });
+}
+
 int lcn_op_create_device(lcn_ctx* ctx, const float* d_p, size_t n, const float* d_q, size_t m, size_t d, int cost,
                          double lambda, const lcn_lsh_config* cfg, size_t l, int landmark_method,
                          uint64_t landmark_seed, lcn_op** out) {
@@ -588,7 +634,17 @@ int lcn_sinkhorn(lcn_op* op, const double* p, const double* q, const lcn_sinkhor
             }
         }
         sinkhorn_solve(o, p, q, false, so, res->r);
-        if (so.want_plan && o.kind != 2 && o.nnz) {
+        if (so.want_plan && o.kind == LCN_OP_DENSE) {
+            // dense plan (sinkhorn.cpp:23-44): exp(log s_i + log K_ij + log t_j), row-major n x m
+            std::vector<double> lk(o.n * o.m);
+            o.dk64.download(lk.data(), lk.size(), o.ctx->stream);
+            o.ctx->sync();
+            Result& r = res->r;
+            r.plan_vals.resize(o.n * o.m);
+            for (size_t i = 0; i < o.n; ++i)
+                for (size_t j = 0; j < o.m; ++j)
+                    r.plan_vals[i * o.m + j] = std::exp(r.log_s[i] + lk[i * o.m + j] + r.log_t[j]);
+        } else if (so.want_plan && o.kind != 2 && o.nnz) {
             // Plan entries on the support in CSR order (sinkhorn.cpp:45-80).
             std::vector<uint32_t> rp(o.n + 1), col(o.nnz);
             std::vector<double> lk(o.nnz);

@@ -56,6 +56,10 @@ struct Op {
     std::vector<DevBuf<float>> val32T;
     std::vector<DevBuf<double>> val64T;
     std::vector<DevBuf<double>> logk64;   // lcn: log K^sp at stored entries
+    // dense operator (kind 0, the configs[2] anchor): log K = 0 - c * (1/lambda)
+    // n x m row-major (fp64 master) and the iteration copies, plus transposes
+    DevBuf<double> dk64, dk64T;
+    DevBuf<float> dk32, dk32T;
     unsigned long long nnz = 0, stored = 0;
     // Nystrom / LCN
     DevBuf<double> L;                     // l x d landmarks
@@ -97,6 +101,7 @@ void lsh_kmeans_bucket_ids(Ctx& ctx, const double* d_union, const float* d_union
 void select_landmarks_device(Op& op, Ctx& ctx, int method, uint64_t seed);
 void build_sparse_values(Op& op);
 void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed);
+void build_dense(Op& op);
 void build_correction(Op& op);
 void finalize_storage(Op& op);
 void build_csr(Op& op);

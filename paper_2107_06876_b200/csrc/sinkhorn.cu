@@ -177,6 +177,130 @@ __global__ void lse_init_kernel(const DevState* __restrict__ st, double* __restr
     if (i < n) { M[i] = kNegInf; S[i] = 0.0; }
 }
 
+// Dense log-domain matvec (operator.cpp:125-140 / 178-192), as (max, sum)
+// pairs for the finalize kernels: for each of 8 rows per CTA, threads stream
+// the row (coalesced) against the shared vector with an online max-shifted
+// sum, then a warp / shared-memory merge. 8 rows per CTA share every read of
+// the vector. fp32 storage: exp of the shifted value on the fp32 MUFU path.
+constexpr int kDenseRows = 8;
+
+template <typename T>
+__device__ __forceinline__ double lse_exp(double x) {  // x <= 0
+    if constexpr (sizeof(T) == 4) return x < -87.0 ? 0.0 : static_cast<double>(__expf(static_cast<float>(x)));
+    else return exp(x);
+}
+
+template <typename T>
+__device__ __forceinline__ void lse_push(double& m, double& s, double v) {
+    if (v == kNegInf) return;
+    if (v > m) {
+        s = (m == kNegInf ? 0.0 : s * lse_exp<T>(m - v)) + 1.0;
+        m = v;
+    } else {
+        s += lse_exp<T>(v - m);
+    }
+}
+
+__device__ __forceinline__ void lse_pair_merge(double& m, double& s, double om, double os) {
+    const double mm = fmax(m, om);
+    if (mm == kNegInf) return;
+    s = (m == kNegInf ? 0.0 : s * exp(m - mm)) + (om == kNegInf ? 0.0 : os * exp(om - mm));
+    m = mm;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) dense_lse_kernel(const DevState* __restrict__ st, const T* __restrict__ logk,
+                                                        long long rows, long long cols,
+                                                        const double* __restrict__ logv, double* __restrict__ M,
+                                                        double* __restrict__ S) {
+    if (st->done) return;
+    __shared__ double wm[kWarps][kDenseRows], ws[kWarps][kDenseRows];
+    const long long i0 = static_cast<long long>(blockIdx.x) * kDenseRows;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double m[kDenseRows], sm[kDenseRows];
+#pragma unroll
+    for (int r = 0; r < kDenseRows; ++r) { m[r] = kNegInf; sm[r] = 0.0; }
+    const int nr = static_cast<int>(rows - i0 < kDenseRows ? rows - i0 : kDenseRows);
+    if constexpr (sizeof(T) == 4) {
+        // fp32 storage: the online max-shifted sum runs in fp32 (v = log K + log v
+        // has ~1e-6 relative error on the exponent already); widened per thread
+        float mf[kDenseRows], sf[kDenseRows];
+#pragma unroll
+        for (int r = 0; r < kDenseRows; ++r) { mf[r] = -INFINITY; sf[r] = 0.0f; }
+        // batches of 4 strided columns: one max, at most one rescale, then
+        // unconditional exps (no per-element divergence)
+        constexpr int kB = 4;
+        long long j0 = threadIdx.x;
+        for (; j0 + (kB - 1) * 256 < cols; j0 += kB * 256) {
+            float lv[kB];
+#pragma unroll
+            for (int u = 0; u < kB; ++u) lv[u] = static_cast<float>(logv[j0 + u * 256]);
+#pragma unroll
+            for (int r = 0; r < kDenseRows; ++r) {
+                if (r < nr) {
+                    const float* row = logk + (i0 + r) * cols + j0;
+                    float v[kB];
+#pragma unroll
+                    for (int u = 0; u < kB; ++u) v[u] = row[u * 256] + lv[u];
+                    const float bm = fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
+                    if (bm > mf[r]) {
+                        sf[r] *= __expf(mf[r] - bm);  // exp(-inf) = 0 for the first batch
+                        mf[r] = bm;
+                    }
+                    if (mf[r] != -INFINITY) {
+#pragma unroll
+                        for (int u = 0; u < kB; ++u) sf[r] += __expf(v[u] - mf[r]);
+                    }
+                }
+            }
+        }
+        for (long long j = j0; j < cols; j += 256) {  // tail
+            const float lv = static_cast<float>(logv[j]);
+#pragma unroll
+            for (int r = 0; r < kDenseRows; ++r) {
+                if (r < nr) {
+                    const float v = logk[(i0 + r) * cols + j] + lv;
+                    if (v > mf[r]) {
+                        sf[r] = sf[r] * __expf(mf[r] - v) + 1.0f;
+                        mf[r] = v;
+                    } else if (v != -INFINITY) {
+                        sf[r] += __expf(v - mf[r]);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < kDenseRows; ++r) {
+            m[r] = mf[r] == -INFINITY ? kNegInf : static_cast<double>(mf[r]);
+            sm[r] = static_cast<double>(sf[r]);
+        }
+    } else {
+        for (long long j = threadIdx.x; j < cols; j += 256) {
+            const double lv = logv[j];
+#pragma unroll
+            for (int r = 0; r < kDenseRows; ++r)
+                if (r < nr) lse_push<T>(m[r], sm[r], static_cast<double>(logk[(i0 + r) * cols + j]) + lv);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < kDenseRows; ++r) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double om = __shfl_xor_sync(0xffffffffu, m[r], o), os = __shfl_xor_sync(0xffffffffu, sm[r], o);
+            lse_pair_merge(m[r], sm[r], om, os);
+        }
+        if (lane == 0) { wm[warp][r] = m[r]; ws[warp][r] = sm[r]; }
+    }
+    __syncthreads();
+    if (threadIdx.x < nr) {
+        const int r = threadIdx.x;
+        double mm = kNegInf, ss = 0.0;
+        for (int w = 0; w < kWarps; ++w) lse_pair_merge(mm, ss, wm[w][r], ws[w][r]);
+        M[i0 + r] = mm;
+        S[i0 + r] = ss;
+    }
+}
+
 // kts = M + log S (empty -> -inf, sparse_kernel.cpp:129); log t = log q - kts.
 __global__ void sparse_col_finalize_kernel(DevState* __restrict__ st, const double* __restrict__ M,
                                            const double* __restrict__ S, const double* __restrict__ log_q, long long m,
@@ -1230,7 +1354,7 @@ struct Solver {
         CPT = lp <= kThreads ? 1 : lp <= 2 * kThreads ? 2 : 4;
         if (lp > 4 * kThreads) throw Status(2, "lcn: landmark count above 1024 is not supported on this path");
         int occ = 1;
-        if (op.kind != 1) {
+        if (op.kind >= 2) {
             smem = op.fp64 ? PassStages<double>::kStages * pass_stage_bytes<double>(lp)
                            : PassStages<float>::kStages * pass_stage_bytes<float>(lp);
             if (op.fp64) set_attrs<double>();
@@ -1449,7 +1573,7 @@ struct Solver {
         log_p.resize(np); log_q.resize(mpd); pv.resize(np); qv.resize(mpd);
         log_s[0].resize(np); log_s[1].resize(np); log_t.resize(mpd); row_marg.resize(np);
         err_part.resize(std::max<long long>(G, ceil_div(n, 256)));
-        if (op.kind == 1) {
+        if (op.kind <= 1) {
             Mr.resize(n); Sr.resize(n); Mc.resize(m); Sc.resize(m);
         } else {
             corr_s.resize(op.bands.size());
@@ -1516,7 +1640,17 @@ struct Solver {
 
     // -------- sparse -------------------------------------------------------
     template <typename T>
+    const T* dense_logk(bool transposed) const {
+        if constexpr (std::is_same_v<T, float>) return transposed ? op.dk32T.get() : op.dk32.get();
+        else return transposed ? op.dk64T.get() : op.dk64.get();
+    }
+    template <typename T>
     void sparse_rows(const double* lt) {
+        if (op.kind == 0) {  // dense: the whole row in one (max, sum) pair
+            dense_lse_kernel<T><<<ceil_div(n, kDenseRows), 256, 0, s>>>(st.get(), dense_logk<T>(false), n, m, lt,
+                                                                        Mr.get(), Sr.get());
+            return;
+        }
         lse_init_kernel<<<ceil_div(n, 256), 256, 0, s>>>(st.get(), Mr.get(), Sr.get(), n);
         for (size_t b = 0; b < op.bands.size(); ++b)
             if (op.bands[b].n_work)
@@ -1525,6 +1659,11 @@ struct Solver {
     }
     template <typename T>
     void sparse_cols(const double* ls) {
+        if (op.kind == 0) {  // dense: rows of the transposed copy
+            dense_lse_kernel<T><<<ceil_div(m, kDenseRows), 256, 0, s>>>(st.get(), dense_logk<T>(true), m, n, ls,
+                                                                        Mc.get(), Sc.get());
+            return;
+        }
         lse_init_kernel<<<ceil_div(m, 256), 256, 0, s>>>(st.get(), Mc.get(), Sc.get(), m);
         for (size_t b = 0; b < op.bands.size(); ++b)
             if (op.bands[b].n_work)
@@ -1762,7 +1901,7 @@ struct Solver {
         DevState h{};
         for (int it0 = 0; it0 <= o.max_iters; it0 += chunk) {
             for (int it = it0; it < std::min(it0 + chunk, o.max_iters + 1); ++it) {
-                if (op.kind == 1) sparse_iteration<T>(it, tol, o.max_iters);
+                if (op.kind <= 1) sparse_iteration<T>(it, tol, o.max_iters);
                 else if (comm) lcn_iteration_sharded<T>(it, tol, o.max_iters);
                 else lcn_iteration<T>(it, tol, o.max_iters);
             }
@@ -1834,7 +1973,7 @@ struct Solver {
         const long long len_in = transposed ? n : m, len_out = transposed ? m : n;
         DevBuf<double> vin((len_in + kRT - 1) / kRT * kRT), vout(len_out);
         vin.upload(h_in, len_in, s);
-        if (op.kind == 1) {
+        if (op.kind <= 1) {
             if (!transposed) {
                 sparse_rows<T>(vin.get());
                 sparse_row_finalize_kernel<<<ceil_div(n, 256), 256, 0, s>>>(st.get(), Mr.get(), Sr.get(), log_p.get(),
@@ -1882,9 +2021,9 @@ struct Solver {
         st.download(&h, 1, s);
         vout.download(h_out, len_out, s);
         ctx.sync();
-        if (op.kind == 1 && transposed)
+        if (op.kind <= 1 && transposed)
             for (long long j = 0; j < len_out; ++j) h_out[j] = -h_out[j];
-        if (op.kind != 1) {
+        if (op.kind >= 2) {
             // all -inf input -> all -inf output (operator.cpp:148-149)
             double hi = kNegInf;
             for (long long i = 0; i < len_in; ++i) hi = std::max(hi, h_in[i]);

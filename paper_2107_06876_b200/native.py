@@ -120,6 +120,9 @@ def library() -> C.CDLL:
             "lcn_distance_lcn": ([P, P, C.POINTER(D)], I),
             "lcn_result_warning": ([P, I], C.c_char_p),
             "lcn_nccl_unique_id": ([P], I),
+            "lcn_op_dense": ([P, P, SZ, P, SZ, SZ, I, D, PP], I),
+            "lcn_op_dense_device": ([P, P, SZ, P, SZ, SZ, I, D, PP], I),
+            "lcn_op_export_dense": ([P, P], I),
             "lcn_ctx_set_comm": ([P, I, I, P], I),
         }
         for name, (args, res) in sig.items():
@@ -332,6 +335,28 @@ class KernelOperator:
         self.info = info
 
     # factories ---------------------------------------------------------------
+    @classmethod
+    def dense(cls, ctx, p, q, cost, lam):
+        """build_cost -> build_kernel -> KernelOperator::dense (the configs[2] anchor)."""
+        p, q = _f64(p), _f64(q)
+        h = C.c_void_p()
+        ctx.check(ctx.lib.lcn_op_dense(ctx.h, _p(p), p.shape[0], _p(q), q.shape[0], p.shape[1], cost, lam,
+                                       C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def dense_device(cls, ctx, d_p: int, n: int, d_q: int, m: int, d: int, cost, lam):
+        h = C.c_void_p()
+        ctx.check(ctx.lib.lcn_op_dense_device(ctx.h, C.c_void_p(d_p), n, C.c_void_p(d_q), m, d, cost, lam,
+                                              C.byref(h)))
+        return cls(ctx, h)
+
+    def export_dense(self):
+        """DenseKernel::logk (n x m)."""
+        out = np.zeros((self.n, self.m))
+        self.ctx.check(self.ctx.lib.lcn_op_export_dense(self.h, _p(out)))
+        return out
+
     @classmethod
     def sparse_lsh(cls, ctx, p, q, cost, lam, cfg: LshConfig):
         """lsh_neighbor_pairs -> build_sparse -> KernelOperator::sparse."""

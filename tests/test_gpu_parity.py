@@ -199,3 +199,30 @@ def test_sharded_solve_single_rank(ref, fp64):
     assert rel(res.distance, rres.distance) <= (REL_FP64 if fp64 else REL_FP32)
     with pytest.raises(lcn.InvalidArgument, match="sharded"):
         op.log_matvec(np.zeros(pr.m))
+
+
+@pytest.mark.parametrize("fp64,cost,lam", [(False, lcn.EUCLIDEAN, 0.05), (True, lcn.EUCLIDEAN, 0.05),
+                                           (False, lcn.COSINE_DERIVED, 0.1), (False, lcn.NEGATIVE_DOT, 0.2)])
+def test_dense_anchor(ref, fp64, cost, lam):
+    """configs[2]-shaped dense operator (H19): log K bit-exact, distance and the
+    dense plan against the reference's dense solve."""
+    r = np.random.default_rng(5)
+    p = r.standard_normal((310, 12)).astype(np.float32).astype(np.float64)
+    q = (r.standard_normal((260, 12)) * 0.8 + 0.1).astype(np.float32).astype(np.float64)
+    p /= np.linalg.norm(p, axis=1, keepdims=True)
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    c = lcn.Context(0, store_fp64=fp64)
+    op = lcn.KernelOperator.dense(c, p, q, cost, lam)
+    rop = ref.op_dense(p, q, cost, lam)
+    lk, rlk = op.export_dense(), rop.dense_logk()
+    assert np.array_equal(lk.view(np.uint64), rlk.view(np.uint64))   # bit-exact log K
+    pm, qm = np.full(310, 1 / 310), np.full(260, 1 / 260)
+    res = lcn.sinkhorn(op, pm, qm, lcn.SinkhornOptions(tol=0.0, max_iters=50))
+    rres = rop.sinkhorn(pm, qm, tol=0.0, max_iters=50)
+    tol = REL_FP64 if fp64 else REL_FP32
+    assert res.iters == rres.iters == 50
+    assert rel(res.distance, rres.distance) <= tol
+    assert rel(res.sparse_vals, rres.dense_plan) <= (1e-8 if fp64 else 1e-3)
+    # the trace converges to the storage-precision floor: fp32 storage forms the
+    # exponents and row sums in fp32 (~1e-6 relative), fp64 storage in fp64
+    assert np.allclose(res.marginal_err, rres.marginal_err, rtol=1e-3, atol=1e-12 if fp64 else 2e-6)
