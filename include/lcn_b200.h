@@ -190,6 +190,15 @@ int lcn_op_dense_device(lcn_ctx* ctx, const float* d_p, size_t n, const float* d
                         double lambda, lcn_op** out);
 /* DenseKernel::logk (n x m, row-major). */
 int lcn_op_export_dense(lcn_op* op, double* out);
+/* multihead_lambdas + multihead (sinkhorn.cpp:322-353): lambda_k =
+ * 2^(k - heads/2) lambda for k = 1..heads, independent dense solves over one
+ * cost matrix (computed once on the device). Per head: lambda, distance,
+ * iterations, converged flag and status (0, or the lcn_status of the head's
+ * error; lcn_ctx_last_error holds the last head error message). */
+int lcn_multihead(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m, size_t d, int cost,
+                  double lambda, int heads, const double* pmarg, const double* qmarg,
+                  const lcn_sinkhorn_options* opts, double* lambdas_out, double* dist_out, int* iters_out,
+                  int* converged_out, int* status_out);
 int lcn_op_destroy(lcn_op* op);
 int lcn_op_get_info(const lcn_op* op, lcn_op_info_t* info);
 /* CSR export in the reference's order (rows ascending, columns ascending,

@@ -162,6 +162,15 @@ class CheckerLib(_Lib):
             _ptr(p), p.shape[0], _ptr(q), q.shape[0], p.shape[1], kind, lam, C.byref(h)))
         return Op(self, h, p.shape[0], q.shape[0], "dense")
 
+    def multihead(self, p, q, kind, lam, heads, pm, qm, tol=-1.0, max_iters=500):
+        p, q, pm, qm = _f64(p), _f64(q), _f64(pm), _f64(qm)
+        lam_o, dist_o = np.zeros(heads), np.zeros(heads)
+        it_o, cv_o, er_o = np.zeros(heads, np.int32), np.zeros(heads, np.int32), np.zeros(heads, np.int32)
+        self.check(self.fn("multihead", _P, _SZ, _P, _SZ, _SZ, _I, _D, _I, _P, _P, _D, _I, _P, _P, _P, _P, _P)(
+            _ptr(p), p.shape[0], _ptr(q), q.shape[0], p.shape[1], kind, lam, heads, _ptr(pm), _ptr(qm), tol,
+            max_iters, _ptr(lam_o), _ptr(dist_o), _ptr(it_o), _ptr(cv_o), _ptr(er_o)))
+        return lam_o, dist_o, it_o, cv_o, er_o
+
     def dense_reference(self, cost, pm, qm, lam, tol, max_iters):
         cost, pm, qm = _f64(cost), _f64(pm), _f64(qm)
         n, m = cost.shape

@@ -257,6 +257,35 @@ int ref_op_dense(const double* p, std::size_t n, const double* q, std::size_t m,
 
 void ref_op_free(void* h) { delete static_cast<RefOp*>(h); }
 
+// multihead (sinkhorn.cpp:333-353) over build_cost; per head: lambda,
+// distance, iterations, converged, error flag (1 = the head threw)
+int ref_multihead(const double* p, std::size_t n, const double* q, std::size_t m, std::size_t d, int kind,
+                  double lambda, int heads, const double* pm, const double* qm, double tol, int max_iters,
+                  double* lam_out, double* dist_out, int* iters_out, int* conv_out, int* err_out) {
+    GUARD({
+        DenseCost cost = build_cost(make_points(p, n, d, "p"), make_points(q, m, d, "q"),
+                                    static_cast<CostKind>(kind), lambda);
+        Marginals marg;
+        marg.p.assign(pm, pm + n);
+        marg.q.assign(qm, qm + m);
+        SinkhornOptions o;
+        o.tol = tol;
+        o.max_iters = max_iters;
+        o.want_plan = false;
+        MultiHeadConfig cfg;
+        cfg.heads = heads;
+        cfg.lambda = lambda;
+        std::vector<HeadOutcome> out = multihead(cost, marg, cfg, o);
+        for (std::size_t k = 0; k < out.size(); ++k) {
+            lam_out[k] = out[k].lambda;
+            dist_out[k] = out[k].distance;
+            iters_out[k] = out[k].iters;
+            conv_out[k] = out[k].converged ? 1 : 0;
+            err_out[k] = out[k].error.empty() ? 0 : 1;
+        }
+    })
+}
+
 // Accessors. which: 0 sparse CSR (row_ptr n+1, col nnz, vals = logvals nnz);
 // 1 lcn correction (row_ptr, col, vals = delta); 2 U (n x l); 3 W (l x m);
 // 4 landmarks (l x d); 5 lcn nys_vals; 6 lcn log_sp.

@@ -11,4 +11,4 @@ from .native import (  # noqa: F401
     COSINE_DERIVED, EUCLIDEAN, LANDMARK_KMEANS, LANDMARK_KMEANSPP, NEGATIVE_DOT, SQEUCLIDEAN, Context, CudaError,
     DimensionError, Error, FactorizationError, InvalidArgument, KernelOperator, LshConfig, NegativeKernelError,
     SinkhornOptions, SinkhornResult, StabilizationError, assign_nearest, distance_lcn, kmeans_pp_indices, library,
-    lloyd, lsh_kmeans_buckets, nccl_unique_id, sinkhorn, sinkhorn_device)
+    lloyd, lsh_kmeans_buckets, multihead, nccl_unique_id, sinkhorn, sinkhorn_device)

@@ -427,6 +427,21 @@ struct EpiExp {
     }
 };
 
+// dense cost (build_cost, geometry.cpp:113-130): c of every pair
+struct EpiDenseCost {
+    static constexpr bool kReduce = false;
+    double* out;
+    long long ld;
+    int kind;
+    const double* na;
+    const double* nb;
+    int* bad;
+    __device__ double operator()(long long r, long long c, double acc) const {
+        out[r * ld + c] = cost_from_fold(kind, acc, na ? na[r] : 0.0, nb ? nb[c] : 0.0, bad);
+        return 0.0;
+    }
+};
+
 // dense log K (build_cost + build_kernel, geometry.cpp:113-144):
 // logk = 0.0 - c * inv with c the sequential-fold cost of the pair
 struct EpiDenseLogK {
@@ -684,6 +699,56 @@ __global__ void __launch_bounds__(256) dense_transpose_kernel(const double* __re
     }
 }
 }  // namespace
+
+namespace {
+// build_kernel (geometry.cpp:132-144): logk = inf ? -inf : 0.0 - c * inv
+__global__ void logk_from_cost_kernel(const double* __restrict__ c, unsigned long long n, double inv,
+                                      double* __restrict__ out) {
+    for (unsigned long long i = blockIdx.x * 256ull + threadIdx.x; i < n; i += 256ull * gridDim.x) {
+        const double v = c[i];
+        out[i] = isinf(v) ? kNegInf : xsub(0.0, xmul(v, inv));
+    }
+}
+}  // namespace
+
+// Dense cost matrix (build_cost) into op.dc64, then log K for lambda via
+// dense_logk_from_cost (multi-head solves share one cost matrix).
+void build_dense_cost(Op& op) {
+    Ctx& ctx = *op.ctx;
+    const size_t n = op.n, m = op.m, d = op.d;
+    const double* nrm = union_norms(op);
+    DevBuf<int> bad(1);
+    bad.zero(ctx.stream);
+    op.dc64.resize(std::max<size_t>(n * m, 1));
+    EpiDenseCost epi{op.dc64.get(), static_cast<long long>(m), op.cost, nrm, nrm ? nrm + n : nullptr, bad.get()};
+    if (op.cost == 1 || op.cost == 2)
+        launch_dense_tiles<1>(ctx, op.P(), n, op.Q(), m, static_cast<int>(d), epi);
+    else
+        launch_dense_tiles<0>(ctx, op.P(), n, op.Q(), m, static_cast<int>(d), epi);
+    if (read_flag(ctx, bad)) throw Status(2, "cosine-derived cost undefined for zero vectors");
+}
+
+void dense_logk_from_cost(Op& op, double lambda) {
+    Ctx& ctx = *op.ctx;
+    if (!(lambda > 0.0)) throw Status(2, "build_kernel: lambda must be positive");
+    op.lambda = lambda;
+    const size_t n = op.n, m = op.m;
+    op.dk64.resize(std::max<size_t>(n * m, 1));
+    logk_from_cost_kernel<<<std::min<long long>(ceil_div(n * m, 256), 16 * ctx.num_sms), 256, 0, ctx.stream>>>(
+        op.dc64.get(), static_cast<unsigned long long>(n * m), 1.0 / lambda, op.dk64.get());
+    const dim3 grid(static_cast<unsigned>(ceil_div(m, 32)), static_cast<unsigned>(ceil_div(n, 32)));
+    if (op.fp64) {
+        op.dk64T.resize(std::max<size_t>(n * m, 1));
+        dense_transpose_kernel<double><<<grid, 256, 0, ctx.stream>>>(op.dk64.get(), n, m, op.dk64T.get(), nullptr);
+    } else {
+        op.dk32.resize(std::max<size_t>(n * m, 1));
+        op.dk32T.resize(std::max<size_t>(n * m, 1));
+        dense_transpose_kernel<float><<<grid, 256, 0, ctx.stream>>>(op.dk64.get(), n, m, op.dk32T.get(), op.dk32.get());
+    }
+    LAUNCH_OK("dense log K from cost");
+    op.nnz = n * m;
+    ctx.sync();
+}
 
 // Dense operator (KernelOperator::dense, operator.cpp:55-64): exact fp64 log K
 // of every pair by the tiled sequential-fold kernel, then the iteration copies

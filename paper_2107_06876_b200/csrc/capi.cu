@@ -488,6 +488,55 @@ int lcn_op_dense_device(lcn_ctx* ctx, const float* d_p, size_t n, const float* d
     });
 }
 
+int lcn_multihead(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m, size_t d, int cost,
+                  double lambda, int heads, const double* pmarg, const double* qmarg,
+                  const lcn_sinkhorn_options* opts, double* lambdas_out, double* dist_out, int* iters_out,
+                  int* converged_out, int* status_out) {
+    return guard(ctx, [&] {
+        // multihead_lambdas (sinkhorn.cpp:322-331)
+        if (heads < 1) throw Status(2, "multihead: heads must be >= 1");
+        if (!(lambda > 0.0)) throw Status(2, "multihead: lambda must be positive");
+        check_cost_lambda(cost, lambda, "build_cost");
+        check_points(p, n, d, "p");
+        check_points(q, m, d, "q");
+        std::unique_ptr<lcn_op> h(new_op(ctx, cost, lambda));
+        Op& op = h->o;
+        upload_union(op, p, n, q, m, d);
+        op.kind = LCN_OP_DENSE;
+        build_dense_cost(op);
+        SolveOptions so;
+        if (opts) {
+            so.tol = opts->tol;
+            so.max_iters = opts->max_iters;
+            so.check_support = false;
+            so.want_plan = false;
+        }
+        std::string last_err;
+        // multihead (sinkhorn.cpp:333-353): independent solves, per-head errors
+        for (int k = 1; k <= heads; ++k) {
+            const double lam_k = std::exp2(static_cast<double>(k) - static_cast<double>(heads) / 2.0) * lambda;
+            const int i = k - 1;
+            lambdas_out[i] = lam_k;
+            dist_out[i] = 0.0;
+            iters_out[i] = 0;
+            converged_out[i] = 0;
+            status_out[i] = LCN_OK;
+            try {
+                dense_logk_from_cost(op, lam_k);
+                Result r;
+                sinkhorn_solve(op, pmarg, qmarg, false, so, r);
+                dist_out[i] = r.distance;
+                iters_out[i] = r.iters;
+                converged_out[i] = r.converged ? 1 : 0;
+            } catch (const Status& e) {
+                status_out[i] = e.code;
+                last_err = e.what();
+            }
+        }
+        if (!last_err.empty()) ctx->c.last_error = last_err;
+    });
+}
+
 int lcn_op_export_dense(lcn_op* op, double* out) {
     lcn_ctx* ctx = op ? reinterpret_cast<lcn_ctx*>(op->o.ctx) : nullptr;
     return guard(ctx, [&] {

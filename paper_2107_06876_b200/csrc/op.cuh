@@ -60,6 +60,7 @@ struct Op {
     // n x m row-major (fp64 master) and the iteration copies, plus transposes
     DevBuf<double> dk64, dk64T;
     DevBuf<float> dk32, dk32T;
+    DevBuf<double> dc64;  // dense cost c (multi-head: log K per lambda from it)
     unsigned long long nnz = 0, stored = 0;
     // Nystrom / LCN
     DevBuf<double> L;                     // l x d landmarks
@@ -102,6 +103,8 @@ void select_landmarks_device(Op& op, Ctx& ctx, int method, uint64_t seed);
 void build_sparse_values(Op& op);
 void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed);
 void build_dense(Op& op);
+void build_dense_cost(Op& op);
+void dense_logk_from_cost(Op& op, double lambda);
 void build_correction(Op& op);
 void finalize_storage(Op& op);
 void build_csr(Op& op);

@@ -123,6 +123,7 @@ def library() -> C.CDLL:
             "lcn_op_dense": ([P, P, SZ, P, SZ, SZ, I, D, PP], I),
             "lcn_op_dense_device": ([P, P, SZ, P, SZ, SZ, I, D, PP], I),
             "lcn_op_export_dense": ([P, P], I),
+            "lcn_multihead": ([P, P, SZ, P, SZ, SZ, I, D, I, P, P, C.POINTER(_SinkOpts), P, P, P, P, P], I),
             "lcn_ctx_set_comm": ([P, I, I, P], I),
         }
         for name, (args, res) in sig.items():
@@ -209,6 +210,9 @@ class SinkhornOptions:
     max_iters: int = 500
     check_support: bool = True
     want_plan: bool = True
+
+    def c(self):
+        return _SinkOpts(self.tol, self.max_iters, int(self.check_support), int(self.want_plan))
 
 
 # ---- k-means (kmeans.hpp:18-29) ----------------------------------------------
@@ -543,6 +547,24 @@ def sinkhorn_device(op: KernelOperator, d_p: int, d_q: int, opts: SinkhornOption
     h = C.c_void_p()
     op.ctx.check(op.ctx.lib.lcn_sinkhorn_device(op.h, C.c_void_p(d_p), C.c_void_p(d_q), C.byref(o), C.byref(h)))
     return SinkhornResult(op, h)
+
+
+def multihead(ctx: Context, p, q, cost, lam: float, heads: int, pm, qm,
+              opts: SinkhornOptions = SinkhornOptions()):
+    """multihead_lambdas + multihead (sinkhorn.cpp:322-353): one dense solve per
+    lambda_k = 2^(k - heads/2) lambda; a failing head is reported, not raised.
+    Returns a list of dicts {lambda, distance, iters, converged, status, error}."""
+    p, q, pm, qm = _f64(p), _f64(q), _f64(pm), _f64(qm)
+    lam_o, dist_o = np.zeros(heads), np.zeros(heads)
+    it_o, cv_o, st_o = np.zeros(heads, np.int32), np.zeros(heads, np.int32), np.zeros(heads, np.int32)
+    so = opts.c()
+    ctx.check(ctx.lib.lcn_multihead(ctx.h, _p(p), p.shape[0], _p(q), q.shape[0], p.shape[1], cost, lam, heads,
+                                    _p(pm), _p(qm), C.byref(so), _p(lam_o), _p(dist_o), _p(it_o), _p(cv_o),
+                                    _p(st_o)))
+    err = ctx.lib.lcn_ctx_last_error(ctx.h)
+    return [{"lambda": float(lam_o[k]), "distance": float(dist_o[k]), "iters": int(it_o[k]),
+             "converged": bool(cv_o[k]), "status": int(st_o[k]),
+             "error": (err.decode() if err else "") if st_o[k] else ""} for k in range(heads)]
 
 
 def distance_lcn(res: SinkhornResult, op: KernelOperator) -> float:

@@ -226,3 +226,27 @@ def test_dense_anchor(ref, fp64, cost, lam):
     # the trace converges to the storage-precision floor: fp32 storage forms the
     # exponents and row sums in fp32 (~1e-6 relative), fp64 storage in fp64
     assert np.allclose(res.marginal_err, rres.marginal_err, rtol=1e-3, atol=1e-12 if fp64 else 2e-6)
+
+
+@pytest.mark.parametrize("fp64", [False, True])
+def test_multihead(ref, fp64):
+    """multihead_lambdas + multihead (H20): lambda schedule, per-head distance,
+    iterations and convergence against the reference."""
+    r = np.random.default_rng(9)
+    p = r.standard_normal((150, 6)).astype(np.float32).astype(np.float64)
+    q = (r.standard_normal((140, 6)) + 0.3).astype(np.float32).astype(np.float64)
+    pm, qm = np.full(150, 1 / 150), np.full(140, 1 / 140)
+    heads = 6
+    c = lcn.Context(0, store_fp64=fp64)
+    # tol well above the fp32-storage error floor: the stopping iteration is then
+    # not decided by round-off
+    out = lcn.multihead(c, p, q, lcn.EUCLIDEAN, 0.5, heads, pm, qm, lcn.SinkhornOptions(tol=1e-5, max_iters=300))
+    lam, dist, iters, conv, err = ref.multihead(p, q, lcn.EUCLIDEAN, 0.5, heads, pm, qm, tol=1e-5, max_iters=300)
+    assert [o["lambda"] for o in out] == list(lam)                       # same schedule bits
+    for k in range(heads):
+        assert out[k]["status"] == 0 and err[k] == 0
+        assert rel(out[k]["distance"], dist[k]) <= (REL_FP64 if fp64 else REL_FP32)
+        assert out[k]["converged"] == bool(conv[k])
+        assert abs(out[k]["iters"] - iters[k]) <= (0 if fp64 else 2)
+    with pytest.raises(lcn.InvalidArgument, match="heads"):
+        lcn.multihead(c, p, q, lcn.EUCLIDEAN, 0.5, 0, pm, qm)
