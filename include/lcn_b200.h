@@ -229,6 +229,12 @@ int lcn_result_get_info(const lcn_result* res, lcn_result_info_t* info);
  * 4 sparse plan values (Plan::sparse_vals, CSR order), 5 lcn sp_vals,
  * 6 lcn sp_nys_vals. out == NULL returns the length in *len only. */
 int lcn_result_copy(const lcn_result* res, int which, double* out, size_t* len);
+/* grad_cost (sinkhorn.cpp:263-320). which: 0 dense / sparse d d / d C (the plan:
+ * n x m row-major, or CSR order), 1 lcn / nystrom d d / d U (n x l),
+ * 2 d d / d W (l x m), 3 lcn d d / d log K^sp = -lambda P^sp, 4 lcn
+ * d d / d log K^sp_Nys = +lambda P^sp_Nys. out == NULL returns the length in
+ * *len; *stale = 1 when the result did not converge (a warning is printed). */
+int lcn_grad_cost(const lcn_result* res, const lcn_op* op, int which, double* out, size_t* len, int* stale);
 /* distance_lcn (sinkhorn.cpp:222-261). */
 int lcn_distance_lcn(const lcn_result* res, const lcn_op* op, double* out);
 /* Warning text i (SinkhornResult::warnings, sinkhorn.cpp:122-128). */

@@ -284,6 +284,15 @@ class Result:
     sp_nys_vals = property(lambda s: s._v(6))
     dense_plan = property(lambda s: s._v(9))
 
+    def grad_cost(self, which):
+        f = self.lib.fn("grad_cost", _P, _P, _I, _P, _P, restype=_SZ)
+        stale = C.c_int()
+        n = f(self.op.h, self.h, which, None, C.byref(stale))
+        out = np.zeros(n)
+        if n:
+            f(self.op.h, self.h, which, _ptr(out), C.byref(stale))
+        return out, bool(stale.value)
+
     def distance_lcn(self):
         out = C.c_double()
         self.lib.check(self.lib.fn("distance_lcn", _P, _P, C.POINTER(C.c_double))(self.h, self.op.h, C.byref(out)))

@@ -407,6 +407,32 @@ std::size_t ref_result_copy(void* h, int which, double* out) {
     return v->size();
 }
 
+// grad_cost (sinkhorn.cpp:263-320). which: 0 dense cost grad (n x m) or
+// sparse cost grad, 1 du (n x l), 2 dw (l x m), 3 log_sparse, 4 log_sparse_nys.
+// Returns the length (0 when absent); *stale as Gradients::stale.
+std::size_t ref_grad_cost(void* op, void* res, int which, double* out, int* stale) {
+    try {
+        auto* r = static_cast<RefOp*>(op);
+        auto* s = static_cast<SinkhornResult*>(res);
+        Gradients g = grad_cost(*s, r->op);
+        if (stale) *stale = g.stale ? 1 : 0;
+        const std::vector<double>* v = nullptr;
+        switch (which) {
+            case 0: v = g.cost ? &g.cost->data : &g.cost_sparse; break;
+            case 1: if (g.u) v = &g.u->data; break;
+            case 2: if (g.w) v = &g.w->data; break;
+            case 3: v = &g.log_sparse; break;
+            case 4: v = &g.log_sparse_nys; break;
+        }
+        if (!v) return 0;
+        if (out) std::memcpy(out, v->data(), v->size() * 8);
+        return v->size();
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 0;
+    }
+}
+
 // sinkhorn.cpp:222-261
 int ref_distance_lcn(void* res, void* op, double* out) {
     GUARD({

@@ -10,5 +10,5 @@ from . import configs  # noqa: F401
 from .native import (  # noqa: F401
     COSINE_DERIVED, EUCLIDEAN, LANDMARK_KMEANS, LANDMARK_KMEANSPP, NEGATIVE_DOT, SQEUCLIDEAN, Context, CudaError,
     DimensionError, Error, FactorizationError, InvalidArgument, KernelOperator, LshConfig, NegativeKernelError,
-    SinkhornOptions, SinkhornResult, StabilizationError, assign_nearest, distance_lcn, kmeans_pp_indices, library,
+    SinkhornOptions, SinkhornResult, StabilizationError, assign_nearest, distance_lcn, grad_cost, kmeans_pp_indices, library,
     lloyd, lsh_kmeans_buckets, multihead, nccl_unique_id, sinkhorn, sinkhorn_device)

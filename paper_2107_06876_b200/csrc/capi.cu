@@ -795,6 +795,93 @@ int lcn_distance_lcn(const lcn_result* res, const lcn_op* op, double* out) {
     });
 }
 
+// ---- grad_cost (sinkhorn.cpp:263-320) -----------------------------------
+namespace {
+// v[a] = sum_r F[r][a] x_r (F rows x l, fp64), one thread per column a, rows
+// split over blocks and combined by atomics into v (zeroed)
+__global__ void colsum_kernel(const double* __restrict__ F, long long rows, int l, const double* __restrict__ x,
+                              double* __restrict__ v) {
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= l) return;
+    const long long per = (rows + gridDim.y - 1) / gridDim.y;
+    const long long r0 = static_cast<long long>(blockIdx.y) * per, r1 = r0 + per < rows ? r0 + per : rows;
+    double acc = 0.0;
+    for (long long r = r0; r < r1; ++r) acc += F[r * l + a] * x[r];
+    atomicAdd(v + a, acc);
+}
+// out[r][a] = scale * x_r * y_a (rows x l)
+__global__ void outer_kernel(const double* __restrict__ x, long long rows, const double* __restrict__ y, int l,
+                             double scale, double* __restrict__ out) {
+    for (long long e = blockIdx.x * 256LL + threadIdx.x; e < rows * l; e += 256LL * gridDim.x)
+        out[e] = scale * x[e / l] * y[e % l];
+}
+}  // namespace
+
+int lcn_grad_cost(const lcn_result* res, const lcn_op* op, int which, double* out, size_t* len, int* stale) {
+    lcn_ctx* ctx = op ? reinterpret_cast<lcn_ctx*>(op->o.ctx) : nullptr;
+    return guard(ctx, [&] {
+        if (!res || !op || !len) throw Status(2, "null argument");
+        const Result& r = res->r;
+        const Op& o = op->o;
+        if (stale) *stale = r.converged ? 0 : 1;
+        if (!r.converged) std::fprintf(stderr, "lcn: warning: gradient requested before convergence (stale)\n");
+        const double lam = o.lambda;
+        auto put = [&](const std::vector<double>& v, double scale) {
+            if (out)
+                for (size_t i = 0; i < v.size(); ++i) out[i] = scale * v[i];
+            *len = v.size();
+        };
+        if (which == 0) {  // dense / sparse: d d / d C = plan
+            if (o.kind >= 2) throw Status(2, "grad_cost: d/dC is defined for the dense and sparse operators");
+            if (r.plan_vals.empty()) throw Status(2, "grad_cost: the solve kept no plan (want_plan = false)");
+            put(r.plan_vals, 1.0);
+            return;
+        }
+        if (which == 3 || which == 4) {  // lcn: -lambda P^sp, +lambda P^sp_Nys
+            if (o.kind != 3) throw Status(2, "grad_cost: log-sparse gradients are defined for the LCN operator");
+            if (r.sp_vals.empty()) throw Status(2, "grad_cost: the solve kept no plan (want_plan = false)");
+            put(which == 3 ? r.sp_vals : r.sp_nys_vals, which == 3 ? -lam : lam);
+            return;
+        }
+        if (which != 1 && which != 2) throw Status(2, "grad_cost: which out of range");
+        if (o.kind < 2) throw Status(2, "grad_cost: operator has no low-rank factors");
+        const size_t n = o.n, m = o.m, l = o.l;
+        const size_t count = which == 1 ? n * l : l * m;
+        *len = count;
+        if (!out) return;
+        cudaStream_t s = o.ctx->stream;
+        // s_i = exp(log s_i), t_j = exp(log t_j); wt = W t, su = U^T s
+        std::vector<double> sl(n), tl(m);
+        for (size_t i = 0; i < n; ++i) sl[i] = std::exp(r.log_s[i]);
+        for (size_t j = 0; j < m; ++j) tl[j] = std::exp(r.log_t[j]);
+        DevBuf<double> ds, dt, wt(l), su(l), g(count);
+        ds.upload(sl.data(), n, s);
+        dt.upload(tl.data(), m, s);
+        wt.zero(s);
+        su.zero(s);
+        const dim3 gs(static_cast<unsigned>(ceil_div(l, 128)), 64);
+        colsum_kernel<<<gs, 128, 0, s>>>(o.Wt64.get(), m, static_cast<int>(l), dt.get(), wt.get());
+        colsum_kernel<<<gs, 128, 0, s>>>(o.U64.get(), n, static_cast<int>(l), ds.get(), su.get());
+        const int grid = static_cast<int>(std::min<long long>(ceil_div(count, 256), 16 * o.ctx->num_sms));
+        if (which == 1) {
+            // du(i, a) = -lambda s_i wt_a (n x l)
+            outer_kernel<<<grid, 256, 0, s>>>(ds.get(), n, wt.get(), static_cast<int>(l), -lam, g.get());
+            LAUNCH_OK("grad_cost du");
+            g.download(out, count, s);
+        } else {
+            // dw(a, j) = -lambda su_a t_j (l x m): rows of the transpose, then transposed on the host
+            outer_kernel<<<grid, 256, 0, s>>>(dt.get(), m, su.get(), static_cast<int>(l), -lam, g.get());
+            LAUNCH_OK("grad_cost dw");
+            std::vector<double> tmp(count);
+            g.download(tmp.data(), count, s);
+            o.ctx->sync();
+            for (size_t j = 0; j < m; ++j)
+                for (size_t a = 0; a < l; ++a) out[a * m + j] = tmp[j * l + a];
+        }
+        o.ctx->sync();
+    });
+}
+
 const char* lcn_result_warning(const lcn_result* res, int i) {
     if (!res || i < 0 || i >= static_cast<int>(res->r.warnings.size())) return nullptr;
     return res->r.warnings[static_cast<size_t>(i)].c_str();

@@ -123,6 +123,7 @@ def library() -> C.CDLL:
             "lcn_op_dense": ([P, P, SZ, P, SZ, SZ, I, D, PP], I),
             "lcn_op_dense_device": ([P, P, SZ, P, SZ, SZ, I, D, PP], I),
             "lcn_op_export_dense": ([P, P], I),
+            "lcn_grad_cost": ([P, P, I, P, C.POINTER(SZ), C.POINTER(I)], I),
             "lcn_multihead": ([P, P, SZ, P, SZ, SZ, I, D, I, P, P, C.POINTER(_SinkOpts), P, P, P, P, P], I),
             "lcn_ctx_set_comm": ([P, I, I, P], I),
         }
@@ -565,6 +566,19 @@ def multihead(ctx: Context, p, q, cost, lam: float, heads: int, pm, qm,
     return [{"lambda": float(lam_o[k]), "distance": float(dist_o[k]), "iters": int(it_o[k]),
              "converged": bool(cv_o[k]), "status": int(st_o[k]),
              "error": (err.decode() if err else "") if st_o[k] else ""} for k in range(heads)]
+
+
+def grad_cost(res: SinkhornResult, op: KernelOperator, which: int):
+    """grad_cost (sinkhorn.cpp:263-320): which 0 d/dC (dense n x m / sparse CSR
+    order), 1 d/dU (n x l), 2 d/dW (l x m), 3 d/dlog K^sp, 4 d/dlog K^sp_Nys.
+    Returns (array, stale)."""
+    lib = op.ctx.lib
+    n = C.c_size_t()
+    st = C.c_int()
+    op.ctx.check(lib.lcn_grad_cost(res.h, op.h, which, None, C.byref(n), C.byref(st)))
+    out = np.zeros(n.value)
+    op.ctx.check(lib.lcn_grad_cost(res.h, op.h, which, _p(out), C.byref(n), C.byref(st)))
+    return out, bool(st.value)
 
 
 def distance_lcn(res: SinkhornResult, op: KernelOperator) -> float:

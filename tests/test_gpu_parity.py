@@ -250,3 +250,38 @@ def test_multihead(ref, fp64):
         assert abs(out[k]["iters"] - iters[k]) <= (0 if fp64 else 2)
     with pytest.raises(lcn.InvalidArgument, match="heads"):
         lcn.multihead(c, p, q, lcn.EUCLIDEAN, 0.5, 0, pm, qm)
+
+
+def test_grad_cost(ref):
+    """grad_cost (§8(f) 1): LCN d/dU, d/dW, d/dlog K^sp(_Nys); sparse and dense
+    d/dC; against the reference's Gradients."""
+    pr = configs.config3(0.002)
+    pm, qm = pr.marginals()
+    cfg = lcn.LshConfig(pr.bands, 1, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
+    c = lcn.Context(0, store_fp64=True)
+    op = lcn.KernelOperator.lcn_lsh(c, pr.p, pr.q, pr.cost, pr.lam_eff, cfg, pr.landmarks, lcn.LANDMARK_KMEANS,
+                                    pr.landmark_seed)
+    pairs = ref.lsh_pairs(pr.p, pr.q, pr.bands, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
+    rop = ref.op_lcn(pr.p, pr.q, pr.cost, pr.lam_eff, pairs, pr.landmarks, 0, pr.landmark_seed)
+    res = lcn.sinkhorn(op, pm, qm, lcn.SinkhornOptions(tol=0.0, max_iters=30))
+    rres = rop.sinkhorn(pm, qm, tol=0.0, max_iters=30)
+    for which in (1, 2, 3, 4):
+        g, stale = lcn.grad_cost(res, op, which)
+        rg, rstale = rres.grad_cost(which)
+        assert stale == rstale == True  # tol = 0: never converged
+        assert g.shape == rg.shape
+        assert np.max(np.abs(g - rg)) <= 1e-7 * max(np.max(np.abs(rg)), 1e-300)
+    # dense: d/dC is the plan
+    r = np.random.default_rng(3)
+    p = r.standard_normal((90, 5))
+    q = r.standard_normal((80, 5))
+    dop = lcn.KernelOperator.dense(c, p, q, lcn.EUCLIDEAN, 0.5)
+    drop = ref.op_dense(p, q, lcn.EUCLIDEAN, 0.5)
+    dres = lcn.sinkhorn(dop, np.full(90, 1 / 90), np.full(80, 1 / 80), lcn.SinkhornOptions(tol=1e-9, max_iters=500))
+    drres = drop.sinkhorn(np.full(90, 1 / 90), np.full(80, 1 / 80), tol=1e-9, max_iters=500)
+    g, stale = lcn.grad_cost(dres, dop, 0)
+    rg, rstale = drres.grad_cost(0)
+    assert not stale and not rstale
+    assert rel(g, rg) <= 1e-8
+    with pytest.raises(lcn.InvalidArgument):
+        lcn.grad_cost(dres, dop, 1)
