@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define LCN_B200_ABI_VERSION 1
+#define LCN_B200_ABI_VERSION 2
 
 typedef struct lcn_ctx lcn_ctx;
 typedef struct lcn_op lcn_op;
@@ -63,14 +63,20 @@ enum lcn_op_kind { LCN_OP_DENSE = 0, LCN_OP_SPARSE = 1, LCN_OP_NYSTROM = 2, LCN_
  * accumulation (performance mode, 1e-4 parity). */
 enum lcn_ctx_flags { LCN_STORE_FP32 = 0, LCN_STORE_FP64 = 1 };
 
-/* LshConfig (lsh.hpp:22-30), k-means scheme. rows_per_band must be 1 for the
- * k-means scheme on this path (the reference only warns, lsh.cpp:256-260). */
+/* LshScheme (lsh.hpp:13-17), same values. */
+enum lcn_lsh_scheme { LCN_LSH_CROSS_POLYTOPE = 0, LCN_LSH_KMEANS = 1, LCN_LSH_HIERARCHICAL_KMEANS = 2 };
+
+/* LshConfig (lsh.hpp:22-30). ABI 2 appended `scheme` and `branching`; a
+ * zero-initialised tail means scheme 0 (cross-polytope), so set scheme
+ * explicitly (LCN_LSH_KMEANS is the reference default). */
 typedef struct {
     int bands;
     int rows_per_band;
-    int buckets_per_fn;
+    int buckets_per_fn;  /* even for cross-polytope */
     int kmeans_iters;
     uint64_t seed;
+    int scheme;          /* enum lcn_lsh_scheme */
+    int branching;       /* hierarchical k-means only (reference default 2) */
 } lcn_lsh_config;
 
 /* SinkhornOptions (sinkhorn.hpp:11-20). tol < 0 selects 1e-6 (sum p + sum q). */
@@ -145,10 +151,20 @@ int lcn_lloyd(lcn_ctx* ctx, const double* points, size_t n, size_t d, size_t k, 
               uint64_t seed, double* centroids_out, uint32_t* assign_out);
 
 /* ---- LSH (lsh.hpp:49-68) ---------------------------------------------- */
-/* Bucket ids of lsh_neighbor_pairs' k-means scheme (lsh.cpp:245-283):
- * ids_out is bands x (n+m), band b = hash_kmeans(X_p ∪ X_q, fn_seed(seed,b,0)). */
+/* Bucket ids of lsh_neighbor_pairs (lsh.cpp:245-283) for cfg->scheme:
+ * ids_out is bands x (n+m) (p's points first), the composite mixed-radix id
+ * over the rows_per_band functions; cross-polytope = hash_cross_polytope
+ * (lsh.cpp:73-103) of p and q, k-means / hierarchical = hash_kmeans
+ * (lsh.cpp:145-158) of X_p ∪ X_q with fn_seed(seed, band, fn). */
+int lcn_lsh_buckets(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m,
+                    size_t d, const lcn_lsh_config* cfg, uint64_t* ids_out);
+/* ABI-1 name of lcn_lsh_buckets (same behaviour). */
 int lcn_lsh_kmeans_buckets(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m,
                            size_t d, const lcn_lsh_config* cfg, uint64_t* ids_out);
+/* cross_polytope_bucket (lsh.cpp:55-71) of n points against an explicit
+ * projection proj (d x half, row-major): argmax of [x^T R || -x^T R]. */
+int lcn_cross_polytope_buckets(lcn_ctx* ctx, const double* points, size_t n, size_t d,
+                               const double* proj, size_t half, uint32_t* out);
 
 /* ---- operators (operator.hpp:29-82) ----------------------------------- */
 /* Sparse operator on the k-means LSH support: lsh_neighbor_pairs

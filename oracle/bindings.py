@@ -99,6 +99,28 @@ class CheckerLib(_Lib):
             _ptr(p), p.shape[0], _ptr(q), q.shape[0], p.shape[1], bands, buckets, iters, seed, _ptr(ids)))
         return ids
 
+    def lsh_buckets_cfg(self, p, q, scheme, bands=1, rows=1, buckets=2, iters=10, branching=2, seed=0):
+        """Per-band composite ids (lsh.cpp:245-283) for any LshScheme value, p first."""
+        p, q = _f64(p), _f64(q)
+        ids = np.zeros((bands, p.shape[0] + q.shape[0]), np.uint64)
+        self.check(self.fn("lsh_buckets", _P, _SZ, _P, _SZ, _SZ, _I, _I, _I, _I, _I, _I, _U64, _P)(
+            _ptr(p), p.shape[0], _ptr(q), q.shape[0], p.shape[1], scheme, bands, rows, buckets, iters, branching,
+            seed, _ptr(ids)))
+        return ids
+
+    def cross_polytope_bucket(self, x, proj):
+        x = _f64(x)
+        proj = _f64(proj)
+        out = np.zeros(x.shape[0], np.uint32)
+        self.check(self.fn("cross_polytope_bucket", _P, _SZ, _SZ, _P, _SZ, _P)(
+            _ptr(x), x.shape[0], x.shape[1], _ptr(proj), proj.shape[1], _ptr(out)))
+        return out
+
+    def normal_draws(self, seed, count):
+        out = np.zeros(count)
+        self.check(self.fn("normal_draws", _U64, _SZ, _P)(seed, count, _ptr(out)))
+        return out
+
     def _pairs_out(self, h):
         nnz = self.fn("pairs_nnz", _P, restype=_SZ)(h)
         rows = np.zeros(nnz, np.uint32)
@@ -304,6 +326,15 @@ class RefLib(CheckerLib):
 
     def __init__(self, path=REF_SO):
         super().__init__(path)
+
+    def lsh_pairs_cfg(self, p, q, scheme, bands=1, rows=1, buckets=2, iters=10, branching=2, seed=0):
+        """lsh_neighbor_pairs (lsh.cpp:245-283) end to end for any scheme."""
+        p, q = _f64(p), _f64(q)
+        h = _P()
+        self.check(self.fn("lsh_pairs_cfg", _P, _SZ, _P, _SZ, _SZ, _I, _I, _I, _I, _I, _I, _U64, _PP)(
+            _ptr(p), p.shape[0], _ptr(q), q.shape[0], p.shape[1], scheme, bands, rows, buckets, iters, branching,
+            seed, C.byref(h)))
+        return Pairs(self, h, p.shape[0], q.shape[0])
 
     def sample_uniform_ball(self, n, d, seed):
         out = np.zeros((n, d))

@@ -369,6 +369,189 @@ int orc_lsh_kmeans_buckets(const double* p, size_t n, const double* q, size_t m,
     return rc;
 }
 
+/* normal_distribution<double>(0, 1) over mt19937_64 (bits/random.tcc,
+ * Marsaglia polar method): draws come in pairs from two canonical uniforms
+ * x, y in [-1, 1) with 0 < r2 = x^2 + y^2 <= 1; the call returns y * mult and
+ * caches x * mult for the next call. */
+typedef struct {
+    mt64 g;
+    int saved_ok;
+    double saved;
+} gauss_t;
+
+static double canonical(mt64* g) {
+    double c = (double)mt64_next(g) / 18446744073709551616.0;
+    return c >= 1.0 ? nextafter(1.0, 0.0) : c;
+}
+
+static double gauss_next(gauss_t* s) {
+    if (s->saved_ok) {
+        s->saved_ok = 0;
+        return s->saved * 1.0 + 0.0;
+    }
+    double x, y, r2;
+    do {
+        x = 2.0 * canonical(&s->g) - 1.0;
+        y = 2.0 * canonical(&s->g) - 1.0;
+        r2 = x * x + y * y;
+    } while (r2 > 1.0 || r2 == 0.0);
+    double mult = sqrt(-2 * log(r2) / r2);
+    s->saved = x * mult;
+    s->saved_ok = 1;
+    return y * mult * 1.0 + 0.0;
+}
+
+int orc_normal_draws(uint64_t seed, size_t count, double* out) {
+    gauss_t s;
+    mt64_seed(&s.g, seed);
+    s.saved_ok = 0;
+    for (size_t i = 0; i < count; ++i) out[i] = gauss_next(&s);
+    return 0;
+}
+
+/* cross_polytope_bucket (lsh.cpp:55-71): argmax over c of [x^T R || -x^T R],
+ * sequential dot, strict > (first maximum). proj is d x half, row-major. */
+static uint32_t cp_bucket(const double* x, size_t d, const double* proj, size_t half) {
+    double best = -INFINITY;
+    uint32_t arg = 0;
+    for (size_t c = 0; c < 2 * half; ++c) {
+        size_t col = c < half ? c : c - half;
+        double v = 0.0;
+        for (size_t k = 0; k < d; ++k) v += x[k] * proj[k * half + col];
+        if (c >= half) v = -v;
+        if (v > best) {
+            best = v;
+            arg = (uint32_t)c;
+        }
+    }
+    return arg;
+}
+
+int orc_cross_polytope_bucket(const double* x, size_t n, size_t d, const double* proj, size_t half, uint32_t* out) {
+    for (size_t i = 0; i < n; ++i) out[i] = cp_bucket(x + i * d, d, proj, half);
+    return 0;
+}
+
+/* hierarchical_assign (lsh.cpp:107-143): FIFO queue of clusters; a cluster
+ * is a leaf once queue + leaves + 1 >= target or it has < 2 points, else
+ * lloyd(k = min(branching, size), iters, mix64(seed ^ ++splits)) splits it and
+ * the non-empty children are queued in child order. */
+typedef struct {
+    uint32_t* idx;
+    size_t len;
+} cluster_t;
+
+static int hierarchical_assign(const double* pts, size_t n, size_t d, size_t target, int branching, int iters,
+                               uint64_t seed, uint32_t* assign) {
+    /* the queue never holds more than n clusters; a ring of n + 1 slots */
+    size_t cap = n + 1, head = 0, tail = 0, qn = 0, nleaves = 0;
+    cluster_t* q = xmalloc(cap * sizeof(cluster_t));
+    cluster_t* leaves = xmalloc(cap * sizeof(cluster_t));
+    q[tail].idx = xmalloc((n ? n : 1) * sizeof(uint32_t));
+    q[tail].len = n;
+    for (size_t i = 0; i < n; ++i) q[tail].idx[i] = (uint32_t)i;
+    tail = (tail + 1) % cap;
+    qn = 1;
+    uint64_t splits = 0;
+    double* sub = xmalloc((n ? n : 1) * d * sizeof(double));
+    double* ctr = xmalloc((size_t)branching * d * sizeof(double));
+    uint32_t* a = xmalloc((n ? n : 1) * sizeof(uint32_t));
+    size_t* cnt = xmalloc((size_t)branching * sizeof(size_t));
+    int rc = 0;
+    while (qn && !rc) {
+        cluster_t cl = q[head];
+        head = (head + 1) % cap;
+        --qn;
+        size_t live = qn + nleaves + 1;
+        if (live >= target || cl.len < 2) {
+            leaves[nleaves++] = cl;
+            continue;
+        }
+        size_t k = (size_t)branching < cl.len ? (size_t)branching : cl.len;
+        for (size_t i = 0; i < cl.len; ++i) memcpy(sub + i * d, pts + (size_t)cl.idx[i] * d, d * sizeof(double));
+        rc = lloyd(sub, cl.len, d, k, iters, mix64(seed ^ ++splits), ctr, a);
+        if (rc) {
+            free(cl.idx);
+            break;
+        }
+        memset(cnt, 0, k * sizeof(size_t));
+        for (size_t i = 0; i < cl.len; ++i) ++cnt[a[i]];
+        for (size_t c = 0; c < k; ++c) {
+            if (!cnt[c]) continue;
+            cluster_t ch = {xmalloc(cnt[c] * sizeof(uint32_t)), 0};
+            for (size_t i = 0; i < cl.len; ++i)
+                if (a[i] == c) ch.idx[ch.len++] = cl.idx[i];
+            q[tail] = ch;
+            tail = (tail + 1) % cap;
+            ++qn;
+        }
+        free(cl.idx);
+    }
+    for (size_t l = 0; l < nleaves; ++l) {
+        for (size_t i = 0; i < leaves[l].len; ++i) assign[leaves[l].idx[i]] = (uint32_t)l;
+        free(leaves[l].idx);
+    }
+    while (qn) {
+        free(q[head].idx);
+        head = (head + 1) % cap;
+        --qn;
+    }
+    free(q);
+    free(leaves);
+    free(sub);
+    free(ctr);
+    free(a);
+    free(cnt);
+    return rc;
+}
+
+/* lsh_neighbor_pairs (lsh.cpp:245-283) up to the per-band composite ids of
+ * X_p ∪ X_q (p first): scheme 0 = hash_cross_polytope (lsh.cpp:73-103) with
+ * proj drawn row-major from normal_distribution over mt19937_64(fn_seed);
+ * 1 = hash_kmeans = lloyd; 2 = hierarchical_assign; ids = ids * b + bucket
+ * over the rows_per_band functions. */
+int orc_lsh_buckets(const double* p, size_t n, const double* q, size_t m, size_t d, int scheme, int bands, int rows,
+                    int buckets, int iters, int branching, uint64_t seed, uint64_t* ids) {
+    if (bands < 1 || rows < 1) return fail(E_ARG, "lsh: bands and rows_per_band must be >= 1");
+    if (buckets < 2) return fail(E_ARG, "lsh: buckets_per_fn must be >= 2");
+    size_t N = n + m;
+    if (scheme == 0) {
+        if (buckets % 2) return fail(E_ARG, "cross-polytope needs an even bucket count");
+    } else if ((size_t)buckets > N) {
+        return fail(E_ARG, "hash_kmeans: more buckets than points");
+    }
+    double* all = xmalloc((N ? N : 1) * d * sizeof(double));
+    memcpy(all, p, n * d * sizeof(double));
+    memcpy(all + n * d, q, m * d * sizeof(double));
+    uint32_t* a = xmalloc((N ? N : 1) * sizeof(uint32_t));
+    double* ctr = xmalloc((size_t)buckets * (d ? d : 1) * sizeof(double));
+    size_t half = (size_t)buckets / 2;
+    double* proj = xmalloc((d ? d : 1) * half * sizeof(double));
+    memset(ids, 0, (size_t)bands * N * sizeof(uint64_t));
+    int rc = 0;
+    for (int b = 0; b < bands && !rc; ++b)
+        for (int fn = 0; fn < rows && !rc; ++fn) {
+            uint64_t s = fn_seed(seed, b, fn);
+            if (scheme == 0) {
+                gauss_t g;
+                mt64_seed(&g.g, s);
+                g.saved_ok = 0;
+                for (size_t e = 0; e < d * half; ++e) proj[e] = gauss_next(&g);
+                for (size_t i = 0; i < N; ++i) a[i] = cp_bucket(all + i * d, d, proj, half);
+            } else if (scheme == 2) {
+                rc = hierarchical_assign(all, N, d, (size_t)buckets, branching, iters, s, a);
+            } else {
+                rc = lloyd(all, N, d, (size_t)buckets, iters, s, ctr, a);
+            }
+            for (size_t i = 0; i < N && !rc; ++i) ids[(size_t)b * N + i] = ids[(size_t)b * N + i] * buckets + a[i];
+        }
+    free(all);
+    free(a);
+    free(ctr);
+    free(proj);
+    return rc;
+}
+
 int orc_lsh_pairs(const double* p, size_t n, const double* q, size_t m, size_t d, int bands, int buckets, int iters,
                   uint64_t seed, void** out) {
     size_t N = n + m;

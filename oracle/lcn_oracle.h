@@ -29,6 +29,10 @@ int orc_lloyd(const double* pts, size_t n, size_t d, size_t k, int iters, uint64
               uint32_t* assign);
 int orc_lsh_kmeans_buckets(const double* p, size_t n, const double* q, size_t m, size_t d, int bands, int buckets,
                            int iters, uint64_t seed, uint64_t* ids);
+int orc_lsh_buckets(const double* p, size_t n, const double* q, size_t m, size_t d, int scheme, int bands, int rows,
+                    int buckets, int iters, int branching, uint64_t seed, uint64_t* ids);
+int orc_cross_polytope_bucket(const double* x, size_t n, size_t d, const double* proj, size_t half, uint32_t* out);
+int orc_normal_draws(uint64_t seed, size_t count, double* out);
 int orc_lsh_pairs(const double* p, size_t n, const double* q, size_t m, size_t d, int bands, int buckets, int iters,
                   uint64_t seed, void** out);
 int orc_pairs_from_buckets(const uint64_t* ids_p, size_t n, const uint64_t* ids_q, size_t m, int bands,

@@ -7,6 +7,7 @@
 // algorithmic code lives here except mix64/fn_seed, which restate the
 // file-local helpers at lsh.cpp:17-27 so bucket ids per band can be exported
 // (lsh_neighbor_pairs itself only returns pairs).
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -81,6 +82,18 @@ LshConfig kmeans_cfg(int bands, int buckets, int iters, std::uint64_t seed) {
     return cfg;
 }
 
+LshConfig full_cfg(int scheme, int bands, int rows, int buckets, int iters, int branching, std::uint64_t seed) {
+    LshConfig cfg;
+    cfg.scheme = static_cast<LshScheme>(scheme);
+    cfg.bands = bands;
+    cfg.rows_per_band = rows;
+    cfg.buckets_per_fn = buckets;
+    cfg.kmeans_iters = iters;
+    cfg.branching = branching;
+    cfg.seed = seed;
+    return cfg;
+}
+
 struct RefOp {
     KernelOperator op;
     std::shared_ptr<SparseKernel> sparse;
@@ -145,6 +158,69 @@ int ref_lsh_kmeans_buckets(const double* p, std::size_t n, const double* q, std:
             auto a = hash_kmeans(all, sub);
             for (std::size_t i = 0; i < n + m; ++i) ids[static_cast<std::size_t>(b) * (n + m) + i] = a[i];
         }
+    })
+}
+
+// Composite bucket ids per band for any scheme, as lsh_neighbor_pairs
+// computes them before neighbor_pairs (lsh.cpp:245-283): cross-polytope =
+// hash_cross_polytope of p and of q; k-means schemes = the union loop over
+// hash_kmeans with fn_seed(seed, band, fn). ids: bands x (n+m), p first.
+int ref_lsh_buckets(const double* p, std::size_t n, const double* q, std::size_t m, std::size_t d, int scheme,
+                    int bands, int rows, int buckets, int iters, int branching, std::uint64_t seed, std::uint64_t* ids) {
+    GUARD({
+        LshConfig cfg = full_cfg(scheme, bands, rows, buckets, iters, branching, seed);
+        const std::size_t N = n + m;
+        if (cfg.scheme == LshScheme::CrossPolytope) {
+            BandBuckets bp = hash_cross_polytope(make_points(p, n, d, "p"), cfg);
+            BandBuckets bq = hash_cross_polytope(make_points(q, m, d, "q"), cfg);
+            for (int b = 0; b < bands; ++b) {
+                std::copy(bp.bucket[b].begin(), bp.bucket[b].end(), ids + static_cast<std::size_t>(b) * N);
+                std::copy(bq.bucket[b].begin(), bq.bucket[b].end(), ids + static_cast<std::size_t>(b) * N + n);
+            }
+        } else {
+            PointSet all = union_points(make_points(p, n, d, "p"), make_points(q, m, d, "q"));
+            for (int b = 0; b < bands; ++b) {
+                std::uint64_t* row = ids + static_cast<std::size_t>(b) * N;
+                std::fill(row, row + N, 0);
+                for (int fn = 0; fn < rows; ++fn) {
+                    LshConfig sub = cfg;
+                    sub.seed = fn_seed(seed, b, fn);
+                    auto a = hash_kmeans(all, sub);
+                    for (std::size_t i = 0; i < N; ++i) row[i] = row[i] * static_cast<std::uint64_t>(buckets) + a[i];
+                }
+            }
+        }
+    })
+}
+
+// cross_polytope_bucket (lsh.cpp:55-71) per point; proj is d x half row-major.
+int ref_cross_polytope_bucket(const double* x, std::size_t n, std::size_t d, const double* proj, std::size_t half,
+                              std::uint32_t* out) {
+    GUARD({
+        DenseMatrix R(d, half);
+        std::memcpy(R.data.data(), proj, d * half * sizeof(double));
+        for (std::size_t i = 0; i < n; ++i) out[i] = cross_polytope_bucket(x + i * d, d, R);
+    })
+}
+
+// std::normal_distribution<double>(0, 1) over mt19937_64(seed), as
+// hash_cross_polytope draws its projections (lsh.cpp:85-89).
+int ref_normal_draws(std::uint64_t seed, std::size_t count, double* out) {
+    GUARD({
+        std::mt19937_64 rng(seed);
+        std::normal_distribution<double> gauss(0.0, 1.0);
+        for (std::size_t i = 0; i < count; ++i) out[i] = gauss(rng);
+    })
+}
+
+// lsh_neighbor_pairs (lsh.cpp:245-283) for any scheme; returns a NeighborPairs*.
+int ref_lsh_pairs_cfg(const double* p, std::size_t n, const double* q, std::size_t m, std::size_t d, int scheme,
+                      int bands, int rows, int buckets, int iters, int branching, std::uint64_t seed, void** out) {
+    GUARD({
+        auto np = std::make_unique<NeighborPairs>(
+            lsh_neighbor_pairs(make_points(p, n, d, "p"), make_points(q, m, d, "q"),
+                               full_cfg(scheme, bands, rows, buckets, iters, branching, seed)));
+        *out = np.release();
     })
 }
 

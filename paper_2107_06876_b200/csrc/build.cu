@@ -12,6 +12,7 @@
 //   * the LCN correction delta = exp(log K) - (U W)_ij at the support
 //     (sparse_kernel.cpp:82-117).
 #include <cub/cub.cuh>
+#include <math_constants.h>
 
 #include <algorithm>
 #include <chrono>
@@ -25,6 +26,7 @@
 #include <functional>
 #include <thread>
 #include <exception>
+#include <deque>
 #include <random>
 
 #include "kmeans.cuh"
@@ -191,9 +193,6 @@ __global__ void narrow_kernel(uint32_t* __restrict__ out, const uint64_t* __rest
 }
 }  // namespace
 
-// lsh_neighbor_pairs' k-means branch (lsh.cpp:245-283): per band, per
-// function, hash_kmeans of the union with fn_seed(seed, band, fn); composite
-// ids are mixed-radix over the r functions.
 // Independent build stages (the k-means of each LSH band, the landmark
 // k-means) run concurrently: one host thread and one non-blocking stream per
 // job, each on its own copy of the context. Their seeding walks are
@@ -230,42 +229,288 @@ void run_jobs(Ctx& ctx, std::vector<std::function<void(Ctx&)>>& jobs) {
         if (e) std::rethrow_exception(e);
 }
 
-// lsh_neighbor_pairs' k-means branch (lsh.cpp:245-283): per band, per
-// function, hash_kmeans of the union with fn_seed(seed, band, fn); composite
-// ids are mixed-radix over the r functions. Bands run as concurrent jobs,
-// together with `extra` (the landmark k-means) when given.
-void lsh_kmeans_bucket_ids(Ctx& ctx, const double* d_union, const float* d_union32, size_t n, size_t m, size_t d,
-                           int bands, int rows, int buckets, int iters, uint64_t seed,
-                           std::vector<DevBuf<uint32_t>>& ids, size_t& range,
-                           const std::function<void(Ctx&)>& extra) {
+namespace {
+
+// cross_polytope_bucket (lsh.cpp:55-71) for a 64-point tile per CTA: every
+// v = x . proj(:, c) is folded over the features in increasing order with
+// separate multiply and add (bit-identical to the reference loop), and the
+// argmax over [v || -v] keeps the first maximum, i.e. the lexicographic
+// (value desc, index asc) winner. Rt is half x d, Rt[c*d + k] = proj(k, c).
+template <typename T>
+__global__ void __launch_bounds__(256) cp_hash_kernel(const T* __restrict__ X, long long N, int d,
+                                                      const double* __restrict__ Rt, int half, uint64_t radix,
+                                                      uint64_t* __restrict__ comp) {
+    __shared__ double As[KC][TP + 1];
+    __shared__ double Bs[KC][TC + 1];
+    const long long r0 = blockIdx.x * static_cast<long long>(TP);
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    double best[4];
+    uint32_t arg[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) best[i] = -CUDART_INF, arg[i] = 0xffffffffu;
+    auto better = [](double v, uint32_t a, double bv, uint32_t ba) { return v > bv || (v == bv && a < ba); };
+    for (int c0 = 0; c0 < half; c0 += TC) {
+        double acc[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+        for (int k0 = 0; k0 < d; k0 += KC) {
+            load_slab<T>(As, X, nullptr, r0, N, d, k0);
+            load_slab<double>(Bs, Rt, nullptr, c0, half, d, k0);
+            __syncthreads();
+            tile_fold<1>(As, Bs, ty, tx, acc);
+            __syncthreads();
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            double bv = -CUDART_INF;
+            uint32_t ba = 0xffffffffu;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int c = c0 + tx + 16 * j;
+                if (c >= half) continue;
+                if (better(acc[i][j], c, bv, ba)) bv = acc[i][j], ba = c;
+                if (better(-acc[i][j], c + half, bv, ba)) bv = -acc[i][j], ba = c + half;
+            }
+#pragma unroll
+            for (int o = 8; o; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const uint32_t oa = __shfl_xor_sync(0xffffffffu, ba, o);
+                if (better(ov, oa, bv, ba)) bv = ov, ba = oa;
+            }
+            if (better(bv, ba, best[i], arg[i])) best[i] = bv, arg[i] = ba;
+        }
+    }
+    if (tx == 0)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const long long r = r0 + ty + 16 * i;
+            if (r < N) comp[r] = comp[r] * radix + (arg[i] == 0xffffffffu ? 0u : arg[i]);
+        }
+}
+
+__global__ void seq_kernel(uint32_t* __restrict__ p, long long n) {
+    const long long i = blockIdx.x * 256LL + threadIdx.x;
+    if (i < n) p[i] = static_cast<uint32_t>(i);
+}
+
+template <typename T>
+__global__ void gather_rows_kernel(T* __restrict__ out, const T* __restrict__ X, const uint32_t* __restrict__ idx,
+                                   long long cnt, int d) {
+    const long long e = blockIdx.x * 256LL + threadIdx.x;
+    if (e < cnt * d) {
+        const long long r = e / d;
+        out[e] = X[static_cast<long long>(idx[r]) * d + (e - r * d)];
+    }
+}
+
+__global__ void child_count_kernel(const uint32_t* __restrict__ a, long long n, int k, int* __restrict__ counts) {
+    __shared__ int loc[64];
+    for (int c = threadIdx.x; c < k; c += blockDim.x) loc[c] = 0;
+    __syncthreads();
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += 256LL * gridDim.x) atomicAdd(&loc[a[i]], 1);
+    __syncthreads();
+    for (int c = threadIdx.x; c < k; c += blockDim.x)
+        if (loc[c]) atomicAdd(&counts[c], loc[c]);
+}
+
+// One CTA per leaf: every point of leaf segment blockIdx.x gets the leaf id.
+__global__ void leaf_fill_kernel(uint32_t* __restrict__ assign, const uint32_t* __restrict__ idx,
+                                 const long long* __restrict__ seg) {
+    const long long off = seg[2 * blockIdx.x], len = seg[2 * blockIdx.x + 1];
+    for (long long e = threadIdx.x; e < len; e += blockDim.x) assign[idx[off + e]] = blockIdx.x;
+}
+
+// hierarchical_assign (lsh.cpp:107-143): FIFO queue of clusters, a cluster
+// becomes a leaf once queue + leaves + 1 >= target (or it has < 2 points),
+// otherwise lloyd(k = min(branching, size), iters, mix64(seed ^ ++splits))
+// on its points splits it and the non-empty children are queued in child
+// order. Clusters are contiguous segments of a device permutation; a split
+// gathers its points, runs lloyd_device, and stable-sorts the segment by
+// child (the push_back order of lsh.cpp:134-135), so only the k child sizes
+// come back to the host for the queue.
+// Returns the leaf count: with branching > 2 the last split can overshoot the
+// target, and leaf ids >= target then flow into the composite ids exactly as
+// in the reference.
+template <typename T>
+long long hier_assign_device(Ctx& ctx, const T* X, long long N, int d, int target, int branching, int iters,
+                             uint64_t seed, uint32_t* assign) {
+    if (branching < 2) throw Status(2, "lsh: branching must be >= 2");
+    if (branching > 64) throw Status(2, "lsh: branching > 64 is not supported on this path");
+    cudaStream_t s = ctx.stream;
+    DevBuf<uint32_t> idx(N), idx2(N), keys(N), keys2(N);
+    DevBuf<T> sub(static_cast<size_t>(N) * d);
+    DevBuf<double> ctr(static_cast<size_t>(branching) * d);
+    DevBuf<int> counts(branching);
+    seq_kernel<<<ceil_div(N, 256), 256, 0, s>>>(idx.get(), N);
+    int end_bit = 1;
+    while ((1LL << end_bit) < branching) ++end_bit;
+    size_t tmp_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.get(), keys2.get(), idx.get(), idx2.get(),
+                                    static_cast<int>(N), 0, end_bit, s);
+    DevBuf<unsigned char> tmp(tmp_bytes);
+    std::deque<std::pair<long long, long long>> queue{{0, N}};
+    std::vector<long long> leaves;  // (off, len) pairs
+    uint64_t splits = 0;
+    std::vector<int> h_counts(branching);
+    while (!queue.empty()) {
+        const auto [off, len] = queue.front();
+        queue.pop_front();
+        const size_t live = queue.size() + leaves.size() / 2 + 1;
+        if (live >= static_cast<size_t>(target) || len < 2) {
+            leaves.push_back(off);
+            leaves.push_back(len);
+            continue;
+        }
+        const int k = static_cast<int>(std::min<long long>(branching, len));
+        gather_rows_kernel<T><<<ceil_div(len * d, 256), 256, 0, s>>>(sub.get(), X, idx.get() + off, len, d);
+        LAUNCH_OK("hierarchical gather");
+        lloyd_device<T>(ctx, sub.get(), len, d, k, iters, mix64(seed ^ ++splits), ctr.get(), keys.get());
+        size_t need = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, need, keys.get(), keys2.get(), idx.get() + off, idx2.get(),
+                                        static_cast<int>(len), 0, end_bit, s);
+        if (need > tmp_bytes) throw Status(6, "hierarchical k-means: sort scratch too small");
+        cub::DeviceRadixSort::SortPairs(tmp.get(), tmp_bytes, keys.get(), keys2.get(), idx.get() + off, idx2.get(),
+                                        static_cast<int>(len), 0, end_bit, s);
+        CUDA_OK(cudaMemcpyAsync(idx.get() + off, idx2.get(), len * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        CUDA_OK(cudaMemsetAsync(counts.get(), 0, k * sizeof(int), s));
+        child_count_kernel<<<static_cast<unsigned>(std::min<long long>(ceil_div(len, 256), 4LL * ctx.num_sms)), 256,
+                             0, s>>>(keys.get(), len, k, counts.get());
+        LAUNCH_OK("hierarchical child counts");
+        counts.download(h_counts.data(), k, s);
+        ctx.sync();
+        long long at = off;
+        for (int c = 0; c < k; ++c) {
+            if (h_counts[c] > 0) queue.emplace_back(at, h_counts[c]);
+            at += h_counts[c];
+        }
+    }
+    const long long nleaves = static_cast<long long>(leaves.size() / 2);
+    DevBuf<long long> seg(leaves.size());
+    seg.upload(leaves.data(), leaves.size(), s);
+    leaf_fill_kernel<<<static_cast<unsigned>(nleaves), 256, 0, s>>>(assign, idx.get(), seg.get());
+    LAUNCH_OK("hierarchical leaf ids");
+    ctx.sync();
+    return nleaves;
+}
+
+// hash_cross_polytope's projection (lsh.cpp:85-89): proj is d x half filled
+// row-major from normal_distribution<double>(0, 1) over mt19937_64(seed);
+// returned transposed (half x d) for the tile loads.
+std::vector<double> cp_projection(uint64_t seed, size_t d, size_t half) {
+    std::vector<double> proj(d * half), t(d * half);
+    std::mt19937_64 rng(seed);
+    std::normal_distribution<double> gauss(0.0, 1.0);
+    for (double& v : proj) v = gauss(rng);
+    for (size_t k = 0; k < d; ++k)
+        for (size_t c = 0; c < half; ++c) t[c * d + k] = proj[k * half + c];
+    return t;
+}
+
+}  // namespace
+
+// cross_polytope_bucket (lsh.cpp:55-71) for n device points against an
+// explicit host projection (d x half, row-major as DenseMatrix).
+void cross_polytope_buckets_device(Ctx& ctx, const double* X, long long N, int d, const double* h_proj, int half,
+                                   uint32_t* out) {
+    cudaStream_t s = ctx.stream;
+    std::vector<double> t(static_cast<size_t>(d) * half);
+    for (int k = 0; k < d; ++k)
+        for (int c = 0; c < half; ++c) t[static_cast<size_t>(c) * d + k] = h_proj[static_cast<size_t>(k) * half + c];
+    DevBuf<double> Rt(t.size());
+    Rt.upload(t.data(), t.size(), s);
+    DevBuf<uint64_t> comp(N);
+    comp.zero(s);
+    cp_hash_kernel<double><<<static_cast<unsigned>(ceil_div(N, TP)), 256, 0, s>>>(X, N, d, Rt.get(), half, 1,
+                                                                                  comp.get());
+    narrow_kernel<<<ceil_div(N, 256), 256, 0, s>>>(out, comp.get(), N);
+    LAUNCH_OK("cross-polytope buckets");
+    ctx.sync();
+}
+
+// lsh_neighbor_pairs (lsh.cpp:245-283) up to the bucket ids, per band, of the
+// union [p; q]:
+//   * cross-polytope: hash_cross_polytope of p and of q with the same
+//     projections (lsh.cpp:73-103) — the per-point hash does not depend on
+//     which set the point is in, so the union is hashed in one pass;
+//   * k-means / hierarchical k-means: hash_kmeans of the union
+//     (lsh.cpp:145-158) with fn_seed(seed, band, fn).
+// Composite ids are mixed-radix over the r functions. Bands run as concurrent
+// jobs, together with `extra` (the landmark k-means) when given.
+void lsh_bucket_ids(Ctx& ctx, const double* d_union, const float* d_union32, size_t n, size_t m, size_t d,
+                    const LshParams& cfg, std::vector<DevBuf<uint32_t>>& ids, size_t& range,
+                    const std::function<void(Ctx&)>& extra) {
     const size_t N = n + m;
+    const int bands = cfg.bands, rows = cfg.rows, buckets = cfg.buckets;
     if (bands < 1 || rows < 1) throw Status(2, "lsh: bands and rows_per_band must be >= 1");
     if (buckets < 2) throw Status(2, "lsh: buckets_per_fn must be >= 2");
-    if (static_cast<size_t>(buckets) > N) throw Status(2, "hash_kmeans: more buckets than points");
+    if (cfg.scheme < 0 || cfg.scheme > 2) throw Status(2, "unknown LSH scheme");
+    if (cfg.scheme == 0) {
+        if (buckets % 2 != 0) throw Status(2, "cross-polytope needs an even bucket count");
+    } else {
+        if (static_cast<size_t>(buckets) > N) throw Status(2, "hash_kmeans: more buckets than points");
+    }
     double r = std::pow(static_cast<double>(buckets), rows);
     if (r > 4294967295.0) throw Status(2, "lsh: composite bucket range exceeds 2^32 on this path");
     range = static_cast<size_t>(r);
     ids.clear();
     ids.resize(bands);
+    // per band: an upper bound on its composite ids (hierarchical leaves can
+    // exceed buckets - 1, see hier_assign_device)
+    std::vector<double> band_bound(bands, 0.0);
     std::vector<std::function<void(Ctx&)>> jobs;
     for (int b = 0; b < bands; ++b)
         jobs.push_back([&, b](Ctx& jc) {
             cudaStream_t s = jc.stream;
-            DevBuf<double> ctr(static_cast<size_t>(buckets) * d);
-            DevBuf<uint32_t> assign(N);
+            double bound = 0.0;
             DevBuf<uint64_t> comp(N);
             comp.zero(s);
-            for (int fn = 0; fn < rows; ++fn) {
-                PhaseTimer pt(jc, "lsh k-means (one band function)");
-                if (d_union32)
-                    lloyd_device<float>(jc, d_union32, N, static_cast<int>(d), buckets, iters, fn_seed(seed, b, fn),
-                                        ctr.get(), assign.get());
-                else
-                    lloyd_device<double>(jc, d_union, N, static_cast<int>(d), buckets, iters, fn_seed(seed, b, fn),
-                                         ctr.get(), assign.get());
-                compose_kernel<<<ceil_div(N, 256), 256, 0, s>>>(comp.get(), assign.get(), N,
-                                                                static_cast<uint64_t>(buckets));
+            const uint64_t radix = static_cast<uint64_t>(buckets);
+            if (cfg.scheme == 0) {
+                const int half = buckets / 2;
+                DevBuf<double> Rt(static_cast<size_t>(half) * d);
+                for (int fn = 0; fn < rows; ++fn) {
+                    PhaseTimer pt(jc, "lsh cross-polytope (one band function)");
+                    const std::vector<double> h = cp_projection(fn_seed(cfg.seed, b, fn), d, half);
+                    Rt.upload(h.data(), h.size(), s);
+                    const unsigned grid = static_cast<unsigned>(ceil_div(N, TP));
+                    if (d_union32)
+                        cp_hash_kernel<float><<<grid, 256, 0, s>>>(d_union32, N, static_cast<int>(d), Rt.get(), half,
+                                                                  radix, comp.get());
+                    else
+                        cp_hash_kernel<double><<<grid, 256, 0, s>>>(d_union, N, static_cast<int>(d), Rt.get(), half,
+                                                                   radix, comp.get());
+                    LAUNCH_OK("cross-polytope hash");
+                    jc.sync();  // h is reused by the next function's upload
+                }
+            } else {
+                DevBuf<double> ctr(static_cast<size_t>(buckets) * d);
+                DevBuf<uint32_t> assign(N);
+                for (int fn = 0; fn < rows; ++fn) {
+                    PhaseTimer pt(jc, "lsh k-means (one band function)");
+                    const uint64_t sd = fn_seed(cfg.seed, b, fn);
+                    const long long NN = static_cast<long long>(N);
+                    long long leaves = buckets;
+                    if (cfg.scheme == 2) {
+                        if (d_union32)
+                            leaves = hier_assign_device<float>(jc, d_union32, NN, static_cast<int>(d), buckets,
+                                                               cfg.branching, cfg.iters, sd, assign.get());
+                        else
+                            leaves = hier_assign_device<double>(jc, d_union, NN, static_cast<int>(d), buckets,
+                                                                cfg.branching, cfg.iters, sd, assign.get());
+                    } else if (d_union32) {
+                        lloyd_device<float>(jc, d_union32, NN, static_cast<int>(d), buckets, cfg.iters, sd, ctr.get(),
+                                            assign.get());
+                    } else {
+                        lloyd_device<double>(jc, d_union, NN, static_cast<int>(d), buckets, cfg.iters, sd, ctr.get(),
+                                             assign.get());
+                    }
+                    compose_kernel<<<ceil_div(N, 256), 256, 0, s>>>(comp.get(), assign.get(), N, radix);
+                    bound = bound * static_cast<double>(radix) + static_cast<double>(leaves - 1);
+                }
             }
+            band_bound[b] = bound;
             DevBuf<uint32_t> out(N);
             narrow_kernel<<<ceil_div(N, 256), 256, 0, s>>>(out.get(), comp.get(), N);
             LAUNCH_OK("lsh ids");
@@ -275,6 +520,10 @@ void lsh_kmeans_bucket_ids(Ctx& ctx, const double* d_union, const float* d_union
     if (extra) jobs.push_back(extra);
     run_jobs(ctx, jobs);
     ctx.sync();
+    for (double bb : band_bound) {
+        if (bb + 1.0 > 4294967295.0) throw Status(2, "lsh: composite bucket range exceeds 2^32 on this path");
+        range = std::max(range, static_cast<size_t>(bb) + 1);
+    }
 }
 
 // ---------------------------------------------------------------------------

@@ -38,6 +38,19 @@ namespace {
 
 thread_local std::string g_orphan_error;
 
+LshParams lsh_params(const lcn_lsh_config* cfg) {
+    if (!cfg) throw Status(2, "lsh: null config");
+    LshParams p;
+    p.scheme = cfg->scheme;
+    p.bands = cfg->bands;
+    p.rows = cfg->rows_per_band;
+    p.buckets = cfg->buckets_per_fn;
+    p.iters = cfg->kmeans_iters;
+    p.branching = cfg->branching;
+    p.seed = cfg->seed;
+    return p;
+}
+
 template <class F>
 int guard(lcn_ctx* ctx, F&& f) {
     std::string* sink = ctx ? &ctx->c.last_error : &g_orphan_error;
@@ -355,8 +368,29 @@ int lcn_lloyd(lcn_ctx* ctx, const double* points, size_t n, size_t d, size_t k, 
     });
 }
 
+int lcn_cross_polytope_buckets(lcn_ctx* ctx, const double* points, size_t n, size_t d, const double* proj,
+                               size_t half, uint32_t* out) {
+    return guard(ctx, [&] {
+        if (!proj || half == 0) throw Status(2, "cross_polytope_bucket: empty projection");
+        check_points(points, n, d, "points");
+        if (n == 0) return;
+        DevBuf<double> X(n * d);
+        X.upload(points, n * d, ctx->c.stream);
+        DevBuf<uint32_t> o(n);
+        cross_polytope_buckets_device(ctx->c, X.get(), static_cast<long long>(n), static_cast<int>(d), proj,
+                                      static_cast<int>(half), o.get());
+        o.download(out, n, ctx->c.stream);
+        ctx->c.sync();
+    });
+}
+
 int lcn_lsh_kmeans_buckets(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m, size_t d,
                            const lcn_lsh_config* cfg, uint64_t* ids_out) {
+    return lcn_lsh_buckets(ctx, p, n, q, m, d, cfg, ids_out);
+}
+
+int lcn_lsh_buckets(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m, size_t d,
+                    const lcn_lsh_config* cfg, uint64_t* ids_out) {
     return guard(ctx, [&] {
         if (!cfg) throw Status(2, "lsh: null config");
         check_points(p, n, d, "p");
@@ -366,8 +400,7 @@ int lcn_lsh_kmeans_buckets(lcn_ctx* ctx, const double* p, size_t n, const double
         upload_union(tmp, p, n, q, m, d);
         std::vector<DevBuf<uint32_t>> ids;
         size_t range = 0;
-        lsh_kmeans_bucket_ids(ctx->c, tmp.X.get(), tmp.X32.size() ? tmp.X32.get() : nullptr, n, m, d, cfg->bands, cfg->rows_per_band, cfg->buckets_per_fn,
-                              cfg->kmeans_iters, cfg->seed, ids, range);
+        lsh_bucket_ids(ctx->c, tmp.X.get(), tmp.X32.size() ? tmp.X32.get() : nullptr, n, m, d, lsh_params(cfg), ids, range);
         std::vector<uint32_t> h(n + m);
         for (size_t b = 0; b < ids.size(); ++b) {
             ids[b].download(h.data(), n + m, ctx->c.stream);
@@ -387,8 +420,7 @@ int lcn_op_sparse_lsh(lcn_ctx* ctx, const double* p, size_t n, const double* q, 
         upload_union(h->o, p, n, q, m, d);
         std::vector<DevBuf<uint32_t>> ids;
         size_t range = 0;
-        lsh_kmeans_bucket_ids(ctx->c, h->o.X.get(), h->o.X32.size() ? h->o.X32.get() : nullptr, n, m, d, cfg->bands, cfg->rows_per_band, cfg->buckets_per_fn,
-                              cfg->kmeans_iters, cfg->seed, ids, range);
+        lsh_bucket_ids(ctx->c, h->o.X.get(), h->o.X32.size() ? h->o.X32.get() : nullptr, n, m, d, lsh_params(cfg), ids, range);
         if (static_cast<int>(ids.size()) > kMaxBands) throw Status(2, "lsh: at most 8 bands on this path");
         bands_from_union_ids(h->o, ids, range);
         finish_sparse(h->o);
@@ -428,8 +460,7 @@ int lcn_op_lcn_lsh(lcn_ctx* ctx, const double* p, size_t n, const double* q, siz
             select_landmarks_device(o, jc, landmark_method, landmark_seed);
             o.landmarks_ready = true;
         };
-        lsh_kmeans_bucket_ids(ctx->c, o.X.get(), o.X32.size() ? o.X32.get() : nullptr, n, m, d, cfg->bands,
-                              cfg->rows_per_band, cfg->buckets_per_fn, cfg->kmeans_iters, cfg->seed, ids, range,
+        lsh_bucket_ids(ctx->c, o.X.get(), o.X32.size() ? o.X32.get() : nullptr, n, m, d, lsh_params(cfg), ids, range,
                               landmarks_job);
         bands_from_union_ids(o, ids, range);
         finish_lcn(o, nullptr, l, landmark_method, landmark_seed);
@@ -575,8 +606,7 @@ int lcn_op_create_device(lcn_ctx* ctx, const float* d_p, size_t n, const float* 
                 select_landmarks_device(op, jc, landmark_method, landmark_seed);
                 op.landmarks_ready = true;
             };
-        lsh_kmeans_bucket_ids(ctx->c, op.X.get(), op.X32.size() ? op.X32.get() : nullptr, n, m, d, cfg->bands,
-                              cfg->rows_per_band, cfg->buckets_per_fn, cfg->kmeans_iters, cfg->seed, ids, range,
+        lsh_bucket_ids(ctx->c, op.X.get(), op.X32.size() ? op.X32.get() : nullptr, n, m, d, lsh_params(cfg), ids, range,
                               landmarks_job);
         bands_from_union_ids(op, ids, range);
         if (l) finish_lcn(op, nullptr, l, landmark_method, landmark_seed);

@@ -96,9 +96,17 @@ struct Result {
 // build.cu
 void build_band_layout(Ctx& ctx, Band& B, const uint32_t* d_src_bucket, const uint32_t* d_tgt_bucket, size_t n,
                        size_t m, size_t nb);
-void lsh_kmeans_bucket_ids(Ctx& ctx, const double* d_union, const float* d_union32, size_t n, size_t m, size_t d, int bands, int rows,
-                           int buckets, int iters, uint64_t seed, std::vector<DevBuf<uint32_t>>& ids, size_t& range,
-                           const std::function<void(Ctx&)>& extra = {});
+// LshConfig (lsh.hpp:22-30); scheme uses the LshScheme values (lsh.hpp:13-17).
+struct LshParams {
+    int scheme = 1;  // 0 cross-polytope, 1 k-means, 2 hierarchical k-means
+    int bands = 1, rows = 1, buckets = 2, iters = 10, branching = 2;
+    uint64_t seed = 0;
+};
+void lsh_bucket_ids(Ctx& ctx, const double* d_union, const float* d_union32, size_t n, size_t m, size_t d,
+                    const LshParams& cfg, std::vector<DevBuf<uint32_t>>& ids, size_t& range,
+                    const std::function<void(Ctx&)>& extra = {});
+void cross_polytope_buckets_device(Ctx& ctx, const double* X, long long N, int d, const double* h_proj, int half,
+                                   uint32_t* out);
 void select_landmarks_device(Op& op, Ctx& ctx, int method, uint64_t seed);
 void build_sparse_values(Op& op);
 void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed);

@@ -53,13 +53,14 @@ _STATUS = {1: DimensionError, 2: InvalidArgument, 3: StabilizationError, 4: Nega
 # enums (include/lcn_b200.h)
 EUCLIDEAN, NEGATIVE_DOT, COSINE_DERIVED, SQEUCLIDEAN = 0, 1, 2, 3
 LANDMARK_KMEANS, LANDMARK_KMEANSPP = 0, 1
+LSH_CROSS_POLYTOPE, LSH_KMEANS, LSH_HIERARCHICAL_KMEANS = 0, 1, 2  # LshScheme (lsh.hpp:13-17)
 KIND_DENSE, KIND_SPARSE, KIND_NYSTROM, KIND_LCN = 0, 1, 2, 3
 _KIND_NAMES = {0: "dense", 1: "sparse", 2: "nystrom", 3: "lcn"}
 
 
 class _LshConfig(C.Structure):
     _fields_ = [("bands", C.c_int), ("rows_per_band", C.c_int), ("buckets_per_fn", C.c_int),
-                ("kmeans_iters", C.c_int), ("seed", C.c_uint64)]
+                ("kmeans_iters", C.c_int), ("seed", C.c_uint64), ("scheme", C.c_int), ("branching", C.c_int)]
 
 
 class _SinkOpts(C.Structure):
@@ -103,6 +104,8 @@ def library() -> C.CDLL:
             "lcn_assign_nearest": ([P, P, SZ, SZ, P, SZ, P], I),
             "lcn_lloyd": ([P, P, SZ, SZ, SZ, I, U64, P, P], I),
             "lcn_lsh_kmeans_buckets": ([P, P, SZ, P, SZ, SZ, C.POINTER(_LshConfig), P], I),
+            "lcn_lsh_buckets": ([P, P, SZ, P, SZ, SZ, C.POINTER(_LshConfig), P], I),
+            "lcn_cross_polytope_buckets": ([P, P, SZ, SZ, P, SZ, P], I),
             "lcn_op_sparse_lsh": ([P, P, SZ, P, SZ, SZ, I, D, C.POINTER(_LshConfig), PP], I),
             "lcn_op_sparse_buckets": ([P, P, SZ, P, SZ, SZ, I, D, P, P, I, U64, PP], I),
             "lcn_op_lcn_lsh": ([P, P, SZ, P, SZ, SZ, I, D, C.POINTER(_LshConfig), SZ, I, U64, PP], I),
@@ -193,15 +196,18 @@ class Context:
 
 @dataclasses.dataclass
 class LshConfig:
-    """LshConfig (lsh.hpp:22-30), k-means scheme."""
+    """LshConfig (lsh.hpp:22-30); scheme defaults to k-means like the reference."""
     bands: int = 1
     rows_per_band: int = 1
     buckets_per_fn: int = 2
     kmeans_iters: int = 10
     seed: int = 0
+    scheme: int = LSH_KMEANS
+    branching: int = 2
 
     def c(self):
-        return _LshConfig(self.bands, self.rows_per_band, self.buckets_per_fn, self.kmeans_iters, self.seed)
+        return _LshConfig(self.bands, self.rows_per_band, self.buckets_per_fn, self.kmeans_iters, self.seed,
+                          self.scheme, self.branching)
 
 
 @dataclasses.dataclass
@@ -261,8 +267,23 @@ def lloyd(ctx: Context, points, k: int, iters: int, seed: int):
     return ctr, asg
 
 
+def cross_polytope_buckets(ctx: Context, points, proj):
+    """cross_polytope_bucket (lsh.cpp:55-71) per point; proj is d x half."""
+    points = _f64(points)
+    proj = np.ascontiguousarray(proj, np.float64)
+    out = np.zeros(points.shape[0], np.uint32)
+    ctx.check(ctx.lib.lcn_cross_polytope_buckets(ctx.h, _p(points), points.shape[0], points.shape[1], _p(proj),
+                                                 proj.shape[1], _p(out)))
+    return out
+
+
+def lsh_buckets(ctx: Context, p, q, cfg: LshConfig):
+    """Per-band composite bucket ids of lsh_neighbor_pairs (lsh.cpp:245-283) for cfg.scheme, p's points first."""
+    return lsh_kmeans_buckets(ctx, p, q, cfg)
+
+
 def lsh_kmeans_buckets(ctx: Context, p, q, cfg: LshConfig):
-    """Per-band bucket ids of the k-means LSH on X_p ∪ X_q (lsh.cpp:245-283)."""
+    """Per-band bucket ids on X_p ∪ X_q (lsh.cpp:245-283); honours cfg.scheme."""
     p, q = _f64(p), _f64(q)
     ids = np.zeros((cfg.bands, p.shape[0] + q.shape[0]), np.uint64)
     c = cfg.c()

@@ -23,6 +23,9 @@ from oracle.bindings import RefLib  # noqa: E402
 from paper_2107_06876_b200 import configs  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
+# (scheme, bands, rows, buckets, branching, seed); scheme = LshScheme value
+LSH_CASES = [(0, 2, 1, 4, 2, 42), (0, 3, 2, 4, 2, 17), (0, 1, 1, 16, 2, 5), (1, 1, 1, 4, 2, 42),
+             (2, 1, 1, 4, 2, 42), (2, 1, 1, 12, 3, 9), (2, 2, 2, 4, 2, 3)]
 
 
 def sha(*arrays):
@@ -78,6 +81,24 @@ def main():
                          (12, 2, 1001), (20, 3, 900), (20, 3, 901), (3, 2, 1100), (3, 2, 1101), (10, 4, 41),
                          (10, 4, 42)]:
         arrays[f"ball_{n}_{d}_{seed}"] = ref.sample_uniform_ball(n, d, seed)
+    # --- the other LSH schemes (lsh.cpp:55-143) on the generator's balls ----------
+    # (p, q as in test_lsh.cpp "identical seeds give identical pair sets")
+    p = ref.sample_uniform_ball(60, 4, 21)
+    q = ref.sample_uniform_ball(50, 4, 22)
+    arrays["lsh_p"], arrays["lsh_q"] = p, q
+    for (scheme, bands, rows, buckets, branching, seed) in LSH_CASES:
+        ids = ref.lsh_buckets_cfg(p, q, scheme, bands, rows, buckets, 10, branching, seed)
+        key = "lsh_%d_%d_%d_%d_%d_%d" % (scheme, bands, rows, buckets, branching, seed)
+        arrays[key + "_ids"] = ids.astype(np.uint32)
+        fixtures[key] = {"max_id": int(ids.max())}
+        # hierarchical leaves can overshoot buckets_per_fn (branching > 2); the
+        # reference's counting sort then indexes past its range
+        # (lsh.cpp:197-200), so pairs are pinned only for in-range ids
+        if ids.max() < buckets ** rows:
+            pr = ref.lsh_pairs_cfg(p, q, scheme, bands, rows, buckets, 10, branching, seed).arrays()
+            fixtures[key].update({"pairs_sha256": sha(*pr), "nnz": int(len(pr[0]))})
+    for seed in (0, 7, 2024):
+        arrays[f"normal_{seed}"] = ref.normal_draws(seed, 33)
     np.savez_compressed(os.path.join(OUT, "golden.npz"), **arrays)
     with open(os.path.join(OUT, "golden.json"), "w") as f:
         json.dump(fixtures, f, indent=1, sort_keys=True)

@@ -277,6 +277,81 @@ def test_kmeans_k_equals_n_and_too_many_buckets(orc):
 
 
 # ---------------------------------------------------------------------------
+# the other LSH schemes: cross-polytope and hierarchical k-means (lsh.cpp:55-143)
+# ---------------------------------------------------------------------------
+def test_cross_polytope_hand_oracle(orc):
+    # test_lsh.cpp:16-27: identity columns, d=2, b=4 -> (x0, x1, -x0, -x1)
+    proj = np.zeros((2, 2))
+    proj[0, 0] = proj[1, 1] = 1.0
+    x = np.array([[1.0, 0.0], [-1.0, 0.0], [0.6, 0.8]])
+    assert orc.cross_polytope_bucket(x, proj).tolist() == [0, 2, 1]
+
+
+def test_cross_polytope_first_maximum_wins(orc):
+    # ties: v == -v at 0 and equal columns -> the lowest concatenated index
+    proj = np.array([[1.0, 1.0, 0.0]])
+    x = np.array([[0.0], [2.0], [-2.0]])
+    assert orc.cross_polytope_bucket(x, proj).tolist() == [0, 0, 3]
+
+
+@pytest.mark.parametrize("seed", [0, 7, 2024])
+def test_normal_draws_golden(orc, seed):
+    # std::normal_distribution<double> over mt19937_64 (libstdc++ polar method)
+    assert np.array_equal(orc.normal_draws(seed, 33).view(np.uint64), ARR[f"normal_{seed}"].view(np.uint64))
+
+
+@pytest.mark.parametrize("key", [k for k in GOLD if k.startswith("lsh_")])
+def test_golden_lsh_schemes(orc, key):
+    scheme, bands, rows, buckets, branching, seed = map(int, key.split("_")[1:])
+    p, q = ARR["lsh_p"], ARR["lsh_q"]
+    ids = orc.lsh_buckets_cfg(p, q, scheme, bands, rows, buckets, 10, branching, seed)
+    assert np.array_equal(ids, ARR[key + "_ids"].astype(np.uint64))
+    assert int(ids.max()) == GOLD[key]["max_id"]
+    if "pairs_sha256" in GOLD[key]:  # in-range ids only (see make_golden.py)
+        n = p.shape[0]
+        pairs = orc.pairs_from_buckets(ids[:, :n], ids[:, n:], 0)
+        assert sha(*pairs.arrays()) == GOLD[key]["pairs_sha256"]
+        assert GOLD[key]["nnz"] > 0
+
+
+def test_cross_polytope_odd_buckets_rejected(orc):
+    # test_lsh.cpp:29-35
+    p = ball(10, 4, 41)
+    with pytest.raises(LcnError) as e:
+        orc.lsh_buckets_cfg(p, p, 0, 1, 1, 3, 10, 2, 0)
+    assert e.value.kind == "InvalidArgument"
+
+
+def test_hierarchical_recovers_four_clusters(orc):
+    # test_lsh.cpp:71-96: four tight clusters, branching 2, buckets 4
+    r = np.random.default_rng(5)
+    centers = np.array([[0, 0], [50, 0], [0, 50], [50, 50]], float)
+    truth = np.arange(12) % 4
+    x = centers[truth] + r.uniform(-0.2, 0.2, (12, 2))
+    ids = orc.lsh_buckets_cfg(x[:6], x[6:], 2, 1, 1, 4, 10, 2, 9)[0]
+    assert len(set(ids.tolist())) == 4
+    assert np.array_equal(ids[:, None] == ids[None, :], truth[:, None] == truth[None, :])
+
+
+@pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("scheme,bands,rows,buckets,branching", [(0, 2, 2, 8, 2), (0, 1, 1, 64, 2), (2, 1, 1, 24, 2),
+                                                                 (2, 1, 1, 20, 5), (2, 1, 1, 19, 3), (1, 2, 2, 6, 2)])
+def test_oracle_lsh_schemes_vs_reference(orc, scheme, bands, rows, buckets, branching):
+    r = np.random.default_rng(buckets)
+    p, q = r.standard_normal((300, 7)), r.standard_normal((250, 7)) + 0.5
+    ref = RefLib()
+    a = orc.lsh_buckets_cfg(p, q, scheme, bands, rows, buckets, 10, branching, 11)
+    b = ref.lsh_buckets_cfg(p, q, scheme, bands, rows, buckets, 10, branching, 11)
+    assert np.array_equal(a, b)
+    if a.max() >= buckets ** rows:
+        return  # leaves overshot buckets_per_fn: the reference's pair grouping is out of range
+    n = p.shape[0]
+    ra, ca = orc.pairs_from_buckets(a[:, :n], a[:, n:], 0).arrays()
+    rb, cb = ref.lsh_pairs_cfg(p, q, scheme, bands, rows, buckets, 10, branching, 11).arrays()
+    assert np.array_equal(ra, rb) and np.array_equal(ca, cb)
+
+
+# ---------------------------------------------------------------------------
 # boundary: the C-ABI library loads and exports every declared symbol
 # ---------------------------------------------------------------------------
 def test_capi_library_exports_header_symbols():
@@ -287,7 +362,7 @@ def test_capi_library_exports_header_symbols():
     assert len(names) >= 25
     missing = [nm for nm in names if not hasattr(lib, nm)]
     assert not missing, missing
-    assert lib.lcn_abi_version() == 1
+    assert lib.lcn_abi_version() == 2
 
 
 def test_capi_without_gpu_fails_loudly():
