@@ -217,11 +217,6 @@ __global__ void __launch_bounds__(256) seed_dist_kernel(const T* __restrict__ X,
 // real fp64 add and the binade is recomputed. With search, the fold also
 // returns the first index whose running sum is >= target and whose element is
 // > 0 (kmeans.cpp:51-58).
-struct FoldResult {
-    double s;
-    long long pick;
-};
-
 constexpr double kMinNormal = 2.2250738585072014e-308;
 constexpr long long kTwo53 = 1LL << 53;
 constexpr long long kTwo52 = 1LL << 52;
@@ -282,6 +277,39 @@ __device__ __forceinline__ ParInc par_scan(ParInc v, int lane) {
     return v;
 }
 
+// Conversion-free par_element: for 0 <= q < 2^52, q + 2^52 rounds q to the
+// nearest integer with ties to even (the grid of [2^52, 2^53) is 1), and the
+// bits of that sum minus the bits of 2^52 are the integer itself. A tie
+// (|q - RNE(q)| == 1/2, exact by Sterbenz) gives the other neighbour for the
+// odd parity. q in [2^52, 2^53) is already an integer. Same values as
+// par_element.
+constexpr double kTwo52d = 4503599627370496.0;
+__device__ __forceinline__ ParInc par_element_fast(double q) {
+    const bool hiq = q >= kTwo52d;
+    const double t = hiq ? q : q + kTwo52d;
+    const long long r = __double_as_longlong(t) - 0x4330000000000000LL + (hiq ? kTwo52 : 0);
+    const double diff = hiq ? 0.0 : q - (t - kTwo52d);
+    const long long r1 = fabs(diff) == 0.5 ? r + (diff > 0.0 ? 1 : -1) : r;
+    return {r, r1};
+}
+// Composition without saturation, for operands whose components are at most
+// 2^53 each and at most 2^10 of them (no int64 overflow); stored plans are
+// clamped to 2^53 (a clamped run leaves its binade anyway).
+__device__ __forceinline__ ParInc par_compose_ns(ParInc f, ParInc g) {
+    return {f.i0 + ((f.i0 & 1) ? g.i1 : g.i0), f.i1 + ((f.i1 & 1) ? g.i0 : g.i1)};
+}
+__device__ __forceinline__ ParInc par_scan_ns(ParInc v, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const ParInc t = par_shfl_up(v, o);
+        if (lane >= o) v = par_compose_ns(t, v);
+    }
+    return v;
+}
+__device__ __forceinline__ longlong2 par_clamp(ParInc v) {
+    return make_longlong2(min(v.i0, kTwo53), min(v.i1, kTwo53));
+}
+
 // ---- chunk-parallel exact fold ----------------------------------------------
 // The fold over N values is cut into chunks of kFoldChunk. Most chunks lie
 // inside one binade of the running sum, where the fold's result depends only
@@ -315,7 +343,8 @@ __global__ void fold_chunk_sum_kernel(const double* __restrict__ x, long long N,
     }
 }
 
-__global__ void fold_plan_kernel(const double* __restrict__ csum, int nch, int* __restrict__ ebin) {
+__global__ void fold_plan_kernel(const double* __restrict__ csum, int nch, int* __restrict__ ebin,
+                                 double* __restrict__ astart) {
     // single block of 1024: blocked exclusive scan of the approximate sums
     __shared__ double tot[1024];
     const int per = (nch + 1023) / 1024;
@@ -333,6 +362,7 @@ __global__ void fold_plan_kernel(const double* __restrict__ csum, int nch, int* 
     double a = threadIdx.x ? tot[threadIdx.x - 1] : 0.0;
     for (int c = c0; c < c1; ++c) {
         double lo = a * (1.0 - 1e-9), hi = (a + csum[c]) * (1.0 + 1e-9);
+        astart[c] = a;
         a += csum[c];
         int e = -100000;
         if (lo >= kMinNormal && hi < kPosInf && ilogb(lo) == ilogb(hi)) e = ilogb(lo);
@@ -340,225 +370,470 @@ __global__ void fold_plan_kernel(const double* __restrict__ csum, int nch, int* 
     }
 }
 
-__global__ void __launch_bounds__(256) fold_round_kernel(const double* __restrict__ x, long long N,
-                                                         const int* __restrict__ ebin, longlong2* __restrict__ R) {
-    constexpr int kPer = kFoldChunk / 256;  // contiguous elements per thread, in order
-    __shared__ ParInc wred[8];
-    __shared__ int bad_any;
-    const int e = ebin[blockIdx.x];
-    if (e == -100000) {
-        if (threadIdx.x == 0) R[blockIdx.x] = make_longlong2(-1, -1);
-        return;
-    }
-    if (threadIdx.x == 0) bad_any = 0;
-    __syncthreads();
-    const long long b = static_cast<long long>(blockIdx.x) * kFoldChunk + threadIdx.x * kPer;
-    ParInc acc{0, 0};
-    bool bad = false;
+// C) per chunk: its parity function for the predicted binade (clean chunks)
+// and, per segment of kSegLen elements, a predicted base binade eb_s (from
+// the approximate running sum at the segment's start and end) with the
+// segment's parity functions for binades eb_s and eb_s + 1. The walk skips
+// whole segments with them and folds literally only the segments in which
+// the running sum changes binade; the first such segment (predicted) is
+// recorded so the walk can prefetch it. Segments get their own base binade
+// so that even the first chunk, where the sum climbs many binades from zero,
+// is mostly skipped.
+constexpr int kSegLen = 64;
+constexpr int kSegs = kFoldChunk / kSegLen;
+static_assert(kSegs == 32, "one segment table entry per lane and binade");
+constexpr int kRoundPer = kFoldChunk / 256;          // contiguous elements per thread
+constexpr int kLanesPerSeg = kSegLen / kRoundPer;    // lanes per segment
+static_assert(kLanesPerSeg == 8, "segmented scans below are width 8");
+constexpr int kNoBinade = -100000;
+
+__device__ __forceinline__ ParInc par_scan8(ParInc v, int lane) {  // inclusive, within 8-lane groups
 #pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-        const long long i = b + j;
-        if (i < N) {
-            const double q = scale_to_grid(x[i], e);
-            if (!(q < 9007199254740992.0)) bad = true;
-            else acc = par_compose(acc, par_element(q));
+    for (int o = 1; o < kLanesPerSeg; o <<= 1) {
+        const ParInc t = par_shfl_up(v, o);
+        if ((lane & (kLanesPerSeg - 1)) >= o) v = par_compose(t, v);
+    }
+    return v;
+}
+
+// predicted binade of a fold interval [lo, hi] (approximate sums widened by
+// 1e-9): its binade when it has one, the lower one when it straddles one
+// power of two, none otherwise
+__device__ __forceinline__ void predict_binade(double a, double b, int& e_one, int& e_base) {
+    const double lo = a * (1.0 - 1e-9), hi = b * (1.0 + 1e-9);
+    e_one = e_base = kNoBinade;
+    if (lo >= kMinNormal && hi < kPosInf) {
+        const int el = ilogb(lo), eh = ilogb(hi);
+        if (el == eh) e_one = el;
+        if (eh - el <= 1) e_base = el;
+    }
+}
+
+__global__ void __launch_bounds__(256) fold_round_kernel(const double* __restrict__ x, long long N,
+                                                         const int* __restrict__ ebin, const double* __restrict__ astart,
+                                                         longlong2* __restrict__ R, longlong2* __restrict__ Rseg,
+                                                         int* __restrict__ Eseg, int* __restrict__ spred,
+                                                         unsigned* __restrict__ smask) {
+    __shared__ ParInc stot[kSegs];
+    __shared__ double ssum[kSegs];
+    __shared__ int sbase[kSegs];
+    __shared__ int all_one;
+    const int e = ebin[blockIdx.x];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane / kLanesPerSeg;
+    const int si = warp * (32 / kLanesPerSeg) + g;
+    const long long b = static_cast<long long>(blockIdx.x) * kFoldChunk + threadIdx.x * kRoundPer;
+    double xv[kRoundPer];
+    double xsum = 0.0;
+#pragma unroll
+    for (int j = 0; j < kRoundPer; ++j) {
+        xv[j] = b + j < N ? x[b + j] : 0.0;
+        xsum += xv[j];
+    }
+#pragma unroll
+    for (int o = 1; o < kLanesPerSeg; o <<= 1) xsum += __shfl_xor_sync(0xffffffffu, xsum, o);
+    if ((lane & (kLanesPerSeg - 1)) == 0) ssum[si] = xsum;
+    __syncthreads();
+    if (warp == 0) {  // approximate segment starts -> per-segment binades
+        double v = ssum[lane];
+        double incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const double a0 = astart[blockIdx.x];
+        int e_one, e_base;
+        predict_binade(a0 + (incl - v), a0 + incl, e_one, e_base);
+        sbase[lane] = e_base;
+        Eseg[static_cast<long long>(blockIdx.x) * kSegs + lane] = e_base;
+        const unsigned straddle = __ballot_sync(0xffffffffu, e_one == kNoBinade);
+        const unsigned one = __ballot_sync(0xffffffffu, e_one == e && e != kNoBinade);
+        if (lane == 0) {
+            all_one = one == 0xffffffffu;
+            spred[blockIdx.x] = straddle ? __ffs(straddle) - 1 : 0;
+            smask[blockIdx.x] = straddle;
         }
     }
-    if (bad) bad_any = 1;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    acc = par_scan(acc, lane);
-    if (lane == 31) wred[warp] = acc;
+    __syncthreads();
+    const int eb = sbase[si];
+    ParInc acc0{0, 0}, acc1{0, 0};
+    bool bad0 = eb == kNoBinade, bad1 = eb == kNoBinade;
+    if (eb != kNoBinade) {
+#pragma unroll
+        for (int j = 0; j < kRoundPer; ++j) {
+            if (b + j < N) {
+                const double q0 = scale_to_grid(xv[j], eb);
+                if (!(q0 < 9007199254740992.0)) bad0 = true;
+                else acc0 = par_compose(acc0, par_element_fast(q0));
+                const double q1 = scale_to_grid(xv[j], eb + 1);
+                if (!(q1 < 9007199254740992.0)) bad1 = true;
+                else acc1 = par_compose(acc1, par_element_fast(q1));
+            }
+        }
+    }
+    const unsigned gmask = 0xffu << (g * kLanesPerSeg);
+    const bool sbad0 = (__ballot_sync(0xffffffffu, bad0) & gmask) != 0;
+    const bool sbad1 = (__ballot_sync(0xffffffffu, bad1) & gmask) != 0;
+    acc0 = par_scan8(acc0, lane);
+    acc1 = par_scan8(acc1, lane);
+    longlong2* seg = Rseg + static_cast<long long>(blockIdx.x) * (2 * kSegs);
+    if ((lane & (kLanesPerSeg - 1)) == kLanesPerSeg - 1) {
+        seg[si] = sbad0 ? make_longlong2(-1, -1) : par_clamp(acc0);
+        seg[kSegs + si] = sbad1 ? make_longlong2(-1, -1) : par_clamp(acc1);
+        stot[si] = sbad0 ? ParInc{-1, -1} : acc0;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
+        // clean chunk: every segment predicted inside binade e
+        bool ok = all_one;
         ParInc t{0, 0};
-        for (int w = 0; w < 8; ++w) t = par_compose(t, wred[w]);
-        R[blockIdx.x] = bad_any ? make_longlong2(-1, -1) : make_longlong2(t.i0, t.i1);
+        for (int w = 0; w < kSegs && ok; ++w) {
+            if (stot[w].i0 < 0) ok = false;
+            else t = par_compose(t, stot[w]);
+        }
+        R[blockIdx.x] = ok ? par_clamp(t) : make_longlong2(-1, -1);
     }
 }
 
-// ---- block-wide exact fold of one staged chunk (kWalkThreads threads) -----
-// Thread t owns elements [kSeg t, kSeg t + kSeg) of the chunk. While the running
-// sum is normal in binade e, every thread composes its segment's parity
-// function (ParInc) and a block scan gives each segment's start and end sums.
-// The first segment that holds a huge element, leaves the binade, or (search)
-// reaches the target is walked element by element by its owner, which
-// publishes the exact stop; a stop element gets a real fp64 add and the fold
-// restarts behind it. A chunk typically restarts once per binade change.
+// ---- literal fold of one segment -------------------------------------------
+// A segment in which the running sum changes binade, meets a huge element or
+// (search) reaches the target is folded literally: s = fl(s + x_i) in index
+// order, the reference's own loop. The warp stages the segment in shared
+// memory and every lane runs the same add chain on broadcast loads, so no
+// result needs broadcasting back. The walk is one warp: its cost is latency
+// chains, and a dependent fp64 add (8 cycles) over one short segment beats
+// any further parity round; the parity tables skip the segments without
+// events.
+constexpr int kPerLane = kSegLen / 32;
+constexpr int kGrp = 8;  // search granularity
 constexpr int kWalkThreads = 256;
-constexpr int kSeg = kFoldChunk / kWalkThreads;
+constexpr int kMaxPre = 48;  // dirty chunks whose tables and segment are prefetched
 
-struct WalkShared {
-    double buf[kFoldChunk];
-    ParInc wsum[kWalkThreads / 32];
-    int flag_min;
-    int ev;           // 0: segment walked, no event; 1: real add at `stop`; 2: pick
-    int stop;
-    long long s_sig;  // significand before `stop` (ev 1) / after the segment (ev 0, 2)
-    long long pick;
+struct SegFold {
+    double s;
+    long long pick;  // >= 0: search hit (global index)
 };
 
-__device__ FoldResult block_exact_fold(WalkShared& sh, int cnt, long long base, double s, bool search,
-                                       double target) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const double* xs = sh.buf;
-    int a = 0;
-    long long pick = -1;
-    while (a < cnt) {
-        if (!(s >= kMinNormal && s < kPosInf)) {  // zero / subnormal / inf: one real add
-            const double va = xs[a];
-            s = xadd(s, va);
-            if (search && s >= target && va > 0.0) { pick = base + a; break; }
-            ++a;
-            continue;
-        }
-        const int e = dbl_exp(s);
-        const long long S = dbl_sig(s);
-        const int lo = max(a, kSeg * tid), hi = min(cnt, kSeg * tid + kSeg);
-        ParInc f{0, 0};
-        bool big = false;
-        for (int i = lo; i < hi; ++i) {
-            const double q = scale_to_grid(xs[i], e);
-            if (!(q < 9007199254740992.0)) { big = true; break; }
-            f = par_compose(f, par_element(q));
-        }
-        const ParInc inc = par_scan(f, lane);  // inclusive, within the warp
-        if (lane == 31) sh.wsum[warp] = inc;
-        if (tid == 0) sh.flag_min = kWalkThreads;
-        __syncthreads();
-        ParInc pre{0, 0};
-        for (int w = 0; w < warp; ++w) pre = par_compose(pre, sh.wsum[w]);
-        const ParInc up = par_shfl_up(inc, 1);
-        const ParInc ex = par_compose(pre, lane ? up : ParInc{0, 0});  // before this segment
-        const ParInc fe = par_compose(ex, f);                              // through this segment
-        const long long s0 = S + ((S & 1) ? ex.i1 : ex.i0);
-        const long long s1 = S + ((S & 1) ? fe.i1 : fe.i0);
-        bool flag = lo < hi && (big || s1 >= kTwo53);
-        if (search && lo < hi && s1 < kTwo53 && dbl_make(s1, e) >= target) flag = true;
-        if (flag) atomicMin(&sh.flag_min, tid);
-        __syncthreads();
-        const int tf = sh.flag_min;
-        if (tf == kWalkThreads) {  // no event: the rest of the chunk is one run
-            if (tid == kWalkThreads - 1) sh.s_sig = s1;
-            __syncthreads();
-            s = dbl_make(sh.s_sig, e);
-            break;
-        }
-        if (tid == tf) {
-            long long cur = s0;
-            int ev = 0, stop = hi;
-            long long pk = -1;
-            for (int i = lo; i < hi; ++i) {
-                const double q = scale_to_grid(xs[i], e);
-                if (!(q < 9007199254740992.0)) { ev = 1; stop = i; break; }
-                const ParInc pe = par_element(q);
-                const long long nx = cur + ((cur & 1) ? pe.i1 : pe.i0);
-                if (nx >= kTwo53) { ev = 1; stop = i; break; }
-                cur = nx;
-                if (search && dbl_make(cur, e) >= target && xs[i] > 0.0) { ev = 2; pk = base + i; break; }
-            }
-            sh.ev = ev;
-            sh.stop = stop;
-            sh.s_sig = cur;
-            sh.pick = pk;
-        }
-        __syncthreads();
-        const int ev = sh.ev, stop = sh.stop;
-        s = dbl_make(sh.s_sig, e);
-        const long long pk = sh.pick;
-        __syncthreads();  // shared state is rewritten by the next round
-        if (ev == 2) { pick = pk; break; }
-        if (ev == 0) { a = stop; continue; }
-        const double vb = xs[stop];
-        s = xadd(s, vb);
-        if (search && s >= target && vb > 0.0) { pick = base + stop; break; }
-        a = stop + 1;
+// Development timing of the walk (build with EXTRA=-DLCN_WALK_PROFILE; the
+// host prints cycles per launch when LCN_WALK_STATS is set).
+#ifdef LCN_WALK_PROFILE
+__device__ unsigned long long g_wt[16];
+__host__ void* g_wt_ptr() {
+    void* p = nullptr;
+    cudaGetSymbolAddress(&p, g_wt);
+    return p;
+}
+#define WALK_T(v) const long long v = clock64()
+#define WALK_ADD(i, val) if ((threadIdx.x & 31) == 0) atomicAdd(&g_wt[i], static_cast<unsigned long long>(val))
+#else
+#define WALK_T(v)
+#define WALK_ADD(i, val)
+#endif
+
+// zero-padded: adding +0 leaves a positive sum unchanged
+__device__ __noinline__ double warp_add_segment(const double* __restrict__ buf, double S) {
+    const double2* b2 = reinterpret_cast<const double2*>(buf);
+#pragma unroll
+    for (int i = 0; i < kSegLen / 2; ++i) {
+        const double2 w = b2[i];
+        S = xadd(S, w.x);
+        S = xadd(S, w.y);
     }
-    return {s, pick};
+    return S;
+}
+// The sum is monotone: the target is reached inside a group iff the group's
+// end reaches it.
+__device__ __noinline__ SegFold warp_search_segment(const double* __restrict__ buf, long long g0, double S,
+                                                    double target) {
+#pragma unroll
+    for (int g = 0; g < kSegLen / kGrp; ++g) {
+        double s2 = S;
+#pragma unroll
+        for (int j = 0; j < kGrp; ++j) s2 = xadd(s2, buf[g * kGrp + j]);
+        if (s2 >= target) {
+#pragma unroll 1
+            for (int j = 0; j < kGrp; ++j) {
+                const double wj = buf[g * kGrp + j];
+                S = xadd(S, wj);
+                if (S >= target && wj > 0.0) return {S, g0 + g * kGrp + j};
+            }
+        }
+        S = s2;
+    }
+    return {S, -1};
 }
 
-// Stage chunk c of x into shared memory (all threads) and fold it.
-__device__ __forceinline__ FoldResult fold_chunk_block(WalkShared& sh, const double* __restrict__ x, long long N,
-                                                       int c, double s, bool search, double target) {
-    const long long b = static_cast<long long>(c) * kFoldChunk;
-    const int cnt = static_cast<int>(min(N - b, static_cast<long long>(kFoldChunk)));
-    __syncthreads();
+// Exact fold of chunk c from the running sum S (one warp). Runs of segments
+// whose parity tables match S's binade advance by one scan; the segment in
+// which the sum leaves the binade (or reaches the target) is folded
+// literally. tabs: the chunk's 2 x kSegs tables (shared memory when
+// prefetched); pre: segment sp's values when prefetched; smask: segments
+// predicted to change binade (loaded while the previous one is folded).
+__device__ __noinline__ SegFold warp_fold_chunk(const double* __restrict__ x, double* __restrict__ buf, long long N,
+                                                int c, int sp, unsigned smask, const longlong2* __restrict__ tabs,
+                                                const int* __restrict__ ebs, const double* __restrict__ pre, double S,
+                                                bool search, double target) {
+    const int lane = threadIdx.x & 31;
+    const long long base = static_cast<long long>(c) * kFoldChunk;
+    const int cnt = static_cast<int>(min(N - base, static_cast<long long>(kFoldChunk)));
+    const int nseg = (cnt + kSegLen - 1) / kSegLen;
+    auto load = [&](int sg, double (&v)[kPerLane]) {
+        const int i0 = sg * kSegLen + lane * kPerLane;
 #pragma unroll
-    for (int j = 0; j < kSeg; ++j) {
-        const int i = threadIdx.x + j * kWalkThreads;
-        sh.buf[i] = i < cnt ? x[b + i] : 0.0;
+        for (int j = 0; j < kPerLane; ++j) v[j] = i0 + j < cnt ? x[base + i0 + j] : 0.0;
+    };
+    // lane l: segment l's tables and base binade
+    const longlong2 tab0 = tabs[lane], tab1 = tabs[kSegs + lane];
+    const int eb_l = ebs[lane];
+    double cur[kPerLane];
+    int cur_sg = min(sp, nseg - 1);
+    if (pre) {
+#pragma unroll
+        for (int j = 0; j < kPerLane; ++j) cur[j] = pre[lane * kPerLane + j];
+    } else {
+        load(cur_sg, cur);
     }
-    __syncthreads();
-    return block_exact_fold(sh, cnt, b, s, search, target);
+    int sg = 0;
+#pragma unroll 1
+    while (sg < nseg) {
+        if (S >= kMinNormal && S < kPosInf) {
+            const int eS = dbl_exp(S);
+            const long long Si = dbl_sig(S);
+            // this lane's segment map for the binade eS, if its tables have it
+            const int jl = eS - eb_l;
+            const longlong2 own = (eb_l == kNoBinade || (jl != 0 && jl != 1)) ? make_longlong2(-1, -1)
+                                  : (jl ? tab1 : tab0);
+            const int src = min(sg + lane, kSegs - 1);
+            const long long t0 = __shfl_sync(0xffffffffu, own.x, src);
+            const long long t1 = __shfl_sync(0xffffffffu, own.y, src);
+            const bool in = sg + lane < nseg;
+            const ParInc r{in ? t0 : 0, in ? t1 : 0};
+            const unsigned inval = __ballot_sync(0xffffffffu, in && t0 < 0);
+            int fb = inval ? __ffs(inval) - 1 : nseg - sg;
+            if (fb > 0) {
+                const ParInc pf = par_scan_ns(lane < fb ? r : ParInc{0, 0}, lane);
+                const long long P = (Si & 1) ? pf.i1 : pf.i0;
+                bool ev = lane < fb && Si + P >= kTwo53;
+                if (search && lane < fb && !ev && dbl_make(Si + P, eS) >= target) ev = true;
+                const unsigned evm = __ballot_sync(0xffffffffu, ev);
+                if (evm) fb = min(fb, __ffs(evm) - 1);
+                if (fb > 0) {
+                    S = dbl_make(Si + __shfl_sync(0xffffffffu, P, fb - 1), eS);
+                    sg += fb;
+                    if (sg >= nseg) break;
+                }
+            }
+        }
+        if (cur_sg != sg) {
+            load(sg, cur);
+            cur_sg = sg;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < kPerLane; ++j) buf[lane * kPerLane + j] = cur[j];
+        __syncwarp();
+        if (sg + 1 < nseg && ((smask >> (sg + 1)) & 1)) {  // predicted fold: load it during this one
+            load(sg + 1, cur);
+            cur_sg = sg + 1;
+        }
+        WALK_T(ts0);
+        if (search) {
+            const SegFold r = warp_search_segment(buf, base + static_cast<long long>(sg) * kSegLen, S, target);
+            if (r.pick >= 0) return r;
+            S = r.s;
+        } else {
+            S = warp_add_segment(buf, S);
+        }
+        WALK_T(ts1);
+        WALK_ADD(6, ts1 - ts0);
+        WALK_ADD(7, 1);
+        ++sg;
+    }
+    return {S, -1};
 }
 
 // D) walk + draw + pick for k-means++ step t (kmeans.cpp:35-62). raw[] holds
 // the caller's engine draws in order; a step with total <= 0 consumes none
-// (kmeans.cpp:42-47). Every warp runs the chunk walk redundantly (identical
-// values, uniform control flow); chunks that need an element-wise fold use
-// the whole block.
+// (kmeans.cpp:42-47). Warp 0 walks the chunks in order; the other warps help
+// stage the chunk plans and find the target chunk.
 __global__ void __launch_bounds__(kWalkThreads) pp_walk_pick_kernel(
     double* __restrict__ dist2, unsigned char* __restrict__ used, long long N, int nch, const int* __restrict__ ebin,
-    const longlong2* __restrict__ R, double* __restrict__ sstart, const unsigned long long* __restrict__ raw,
-    int n_raw, int* __restrict__ draw_counter, uint32_t* __restrict__ chosen, int t, int staged) {
-    __shared__ WalkShared sh;
+    const int* __restrict__ spred, const longlong2* __restrict__ R, const longlong2* __restrict__ Rseg,
+    const int* __restrict__ Eseg, const unsigned* __restrict__ smask, double* __restrict__ sstart, const unsigned long long* __restrict__ raw, int n_raw, int* __restrict__ draw_counter,
+    uint32_t* __restrict__ chosen, int t, int staged) {
+    __shared__ int flag_min;
+    __shared__ double total;
+    __shared__ __align__(16) double segbuf[kSegLen];
+    __shared__ int wcount[kWalkThreads / 32];
+    __shared__ int pre_list[kMaxPre];
     extern __shared__ __align__(16) unsigned char wdyn[];
-    const int lane = threadIdx.x & 31;
-    const bool w0 = threadIdx.x < 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    WALK_T(T0);
     // chunk plans and the running-sum table in shared memory when they fit:
-    // one memory latency for all plans instead of one per 32-chunk group
+    // one memory latency for all plans instead of one per 32-chunk group;
+    // then the segment tables and the predicted crossing segment of every
+    // chunk the walk will fold (R < 0), so those folds start without a
+    // memory round trip
+    int* slot = nullptr;
+    longlong2* pre_tab = nullptr;
+    double* pre_seg = nullptr;
+    int* pre_eb = nullptr;
     if (staged) {
-        longlong2* Rs = reinterpret_cast<longlong2*>(wdyn);
+        pre_tab = reinterpret_cast<longlong2*>(wdyn);
+        pre_seg = reinterpret_cast<double*>(pre_tab + kMaxPre * 2 * kSegs);
+        pre_eb = reinterpret_cast<int*>(pre_seg + kMaxPre * kSegLen);
+        longlong2* Rs = reinterpret_cast<longlong2*>(pre_eb + kMaxPre * kSegs);
         double* ss = reinterpret_cast<double*>(Rs + nch);
         int* es = reinterpret_cast<int*>(ss + nch + 1);
-        for (int c = threadIdx.x; c < nch; c += kWalkThreads) {
-            Rs[c] = R[c];
+        int* ps = es + nch;
+        slot = ps + nch;
+        unsigned* ms = reinterpret_cast<unsigned*>(slot + nch);
+        // contiguous chunk ranges per thread, so slots follow chunk order
+        const int per = (nch + kWalkThreads - 1) / kWalkThreads;
+        const int c0 = min(nch, static_cast<int>(threadIdx.x) * per), c1 = min(nch, c0 + per);
+        int nd = 0;
+        for (int c = c0; c < c1; ++c) {
+            const longlong2 r = R[c];
+            Rs[c] = r;
             es[c] = ebin[c];
+            ps[c] = spred[c];
+            ms[c] = smask[c];
+            nd += r.x < 0;
+        }
+        int incl = nd;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (lane == 31) wcount[warp] = incl;
+        __syncthreads();
+        int off = incl - nd;
+        for (int w = 0; w < warp; ++w) off += wcount[w];
+        for (int c = c0; c < c1; ++c) {
+            int sl = -1;
+            if (Rs[c].x < 0) {
+                if (off < kMaxPre) {
+                    sl = off;
+                    pre_list[off] = c;
+                }
+                ++off;
+            }
+            slot[c] = sl;
+        }
+        __syncthreads();
+        int ndirty = 0;
+        for (int w = 0; w < kWalkThreads / 32; ++w) ndirty += wcount[w];
+        ndirty = min(ndirty, kMaxPre);
+        for (int e = threadIdx.x; e < ndirty * 2 * kSegs; e += kWalkThreads) {
+            const int sl = e / (2 * kSegs), k = e % (2 * kSegs);
+            pre_tab[e] = Rseg[static_cast<long long>(pre_list[sl]) * (2 * kSegs) + k];
+        }
+        for (int e = threadIdx.x; e < ndirty * kSegs; e += kWalkThreads) {
+            const int sl = e / kSegs, k = e % kSegs;
+            pre_eb[e] = Eseg[static_cast<long long>(pre_list[sl]) * kSegs + k];
+        }
+        for (int e = threadIdx.x; e < ndirty * kSegLen; e += kWalkThreads) {
+            const int sl = e / kSegLen, k = e % kSegLen;
+            const int c = pre_list[sl];
+            const long long i = static_cast<long long>(c) * kFoldChunk + static_cast<long long>(ps[c]) * kSegLen + k;
+            pre_seg[e] = i < N ? dist2[i] : 0.0;
         }
         __syncthreads();
         R = Rs;
         ebin = es;
+        spred = ps;
+        smask = ms;
         sstart = ss;
     }
-    double S = 0.0;
-    // 32 chunks per step: a run of clean chunks in the running sum's binade
-    // advances by an exact parity scan of their R_c
-    for (int cb = 0; cb < nch; cb += 32) {
-        const int c_l = cb + lane;
-        const int e_l = c_l < nch ? ebin[c_l] : 0;
-        const longlong2 r2 = c_l < nch ? R[c_l] : make_longlong2(-1, -1);
-        const ParInc r_l{r2.x, r2.y};
-        const int cnt = min(32, nch - cb);
-        int k = 0;
-        while (k < cnt) {
-            const bool normal = S >= kMinNormal && S < kPosInf;
-            const int eS = normal ? dbl_exp(S) : -100001;
-            const long long Si = normal ? dbl_sig(S) : 0;
-            const bool in = lane >= k && lane < cnt;
-            const bool ok = in && normal && e_l == eS && r_l.i0 >= 0;
-            const unsigned notok = __ballot_sync(0xffffffffu, in && !ok);
-            int fb = notok ? __ffs(notok) - 1 : cnt;
-            const bool run = lane >= k && lane < fb;
-            const ParInc pf = par_scan(run ? r_l : ParInc{0, 0}, lane);
-            const long long P = (Si & 1) ? pf.i1 : pf.i0;
-            // a chunk whose end leaves the binade is folded element-wise
-            const unsigned cross = __ballot_sync(0xffffffffu, run && Si + P >= kTwo53);
-            if (cross) fb = min(fb, __ffs(cross) - 1);
-            const long long Pprev = __shfl_up_sync(0xffffffffu, P, 1);
-            const long long Pex = lane > k ? Pprev : 0;
-            if (w0 && lane >= k && lane < fb) sstart[c_l] = dbl_make(Si + Pex, eS);
-            if (fb > k) S = dbl_make(Si + __shfl_sync(0xffffffffu, P, fb - 1), eS);
-            if (fb < cnt) {
-                const int c = cb + fb;
-                if (threadIdx.x == 0) sstart[c] = S;
-                S = fold_chunk_block(sh, dist2, N, c, S, false, 0.0).s;
-                k = fb + 1;
-            } else {
-                k = cnt;
+    WALK_T(T1);
+    if (threadIdx.x < 32) {
+        double S = 0.0;
+        // kCPL x 32 chunks per step: a run of clean chunks in the running
+        // sum's binade advances by one exact parity scan of their R_c; each
+        // lane composes its kCPL chunks, then steps through them for their
+        // exact starts (sstart) and the first chunk whose end leaves the
+        // binade
+        constexpr int kCPL = 4;
+        for (int cb = 0; cb < nch; cb += 32 * kCPL) {
+            ParInc rj[kCPL];
+            int ej[kCPL];
+#pragma unroll
+            for (int j = 0; j < kCPL; ++j) {
+                const int c = cb + kCPL * lane + j;
+                const longlong2 r2 = c < nch ? R[c] : make_longlong2(-1, -1);
+                rj[j] = ParInc{r2.x, r2.y};
+                ej[j] = c < nch ? ebin[c] : 0;
+            }
+            const int cnt = min(32 * kCPL, nch - cb);
+            int k = 0;
+#pragma unroll 1
+            while (k < cnt) {
+                const bool normal = S >= kMinNormal && S < kPosInf;
+                const int eS = normal ? dbl_exp(S) : -100001;
+                const long long Si = normal ? dbl_sig(S) : 0;
+                int lbad = 1 << 30;
+#pragma unroll
+                for (int j = 0; j < kCPL; ++j) {
+                    const int idx = kCPL * lane + j;
+                    const bool in = idx >= k && idx < cnt;
+                    const bool ok = normal && ej[j] == eS && rj[j].i0 >= 0;
+                    if (in && !ok && lbad == (1 << 30)) lbad = idx;
+                }
+                int fb = min(static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(lbad))), cnt);
+                if (fb > k) {
+                    ParInc f{0, 0};
+#pragma unroll
+                    for (int j = 0; j < kCPL; ++j) {
+                        const int idx = kCPL * lane + j;
+                        if (idx >= k && idx < fb) f = par_compose_ns(f, rj[j]);
+                    }
+                    const ParInc inc = par_scan_ns(f, lane);
+                    const ParInc up = par_shfl_up(inc, 1);
+                    long long cur = Si + (lane ? ((Si & 1) ? up.i1 : up.i0) : 0);
+                    int lcross = 1 << 30;
+#pragma unroll
+                    for (int j = 0; j < kCPL; ++j) {
+                        const int idx = kCPL * lane + j;
+                        if (idx >= k && idx < fb && lcross == (1 << 30)) {
+                            sstart[cb + idx] = dbl_make(cur, eS);
+                            const long long nx = cur + ((cur & 1) ? rj[j].i1 : rj[j].i0);
+                            if (nx >= kTwo53) lcross = idx;  // this chunk leaves the binade
+                            else cur = nx;
+                        }
+                    }
+                    // a chunk whose end leaves the binade is folded segment-wise
+                    fb = min(fb, static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(lcross))));
+                    if (fb > k) S = dbl_make(__shfl_sync(0xffffffffu, cur, (fb - 1) / kCPL), eS);
+                }
+                if (fb < cnt) {
+                    const int c = cb + fb;
+                    if (lane == 0) sstart[c] = S;
+                    WALK_T(ta);
+                    const int sl = slot ? slot[c] : -1;
+                    S = sl >= 0 ? warp_fold_chunk(dist2, segbuf, N, c, spred[c], smask[c], pre_tab + sl * 2 * kSegs,
+                                                  pre_eb + sl * kSegs, pre_seg + sl * kSegLen, S, false, 0.0).s
+                                : warp_fold_chunk(dist2, segbuf, N, c, spred[c], smask[c],
+                                                  Rseg + static_cast<long long>(c) * 2 * kSegs,
+                                                  Eseg + static_cast<long long>(c) * kSegs, nullptr, S, false, 0.0).s;
+                    WALK_T(tb);
+                    WALK_ADD(c == 0 ? 8 : 2, tb - ta);
+                    WALK_ADD(3, 1);
+                    k = fb + 1;
+                } else {
+                    k = cnt;
+                }
             }
         }
+        if (lane == 0) {
+            sstart[nch] = S;
+            total = S;
+        }
     }
-    if (threadIdx.x == 0) sstart[nch] = S;
+    WALK_T(T2);
     __syncthreads();
+    const double S = total;
     long long pick;
     if (S <= 0.0) {
         pick = N;  // all remaining points coincide with a centroid: first unused
@@ -577,30 +852,36 @@ __global__ void __launch_bounds__(kWalkThreads) pp_walk_pick_kernel(
         const double target = xadd(xmul(c, xsub(S, 0.0)), 0.0);
         // first chunk whose running sum reaches the target (the sum is
         // monotone): every thread tests its chunks, block-wide minimum
+        if (threadIdx.x == 0) flag_min = nch;
         __syncthreads();
-        if (threadIdx.x == 0) sh.flag_min = nch;
-        __syncthreads();
-        for (int c = threadIdx.x; c < nch; c += kWalkThreads)
-            if (sstart[c + 1] >= target) {
-                atomicMin(&sh.flag_min, c);
+        for (int cc = threadIdx.x; cc < nch; cc += kWalkThreads)
+            if (sstart[cc + 1] >= target) {
+                atomicMin(&flag_min, cc);
                 break;
             }
         __syncthreads();
-        const int cstar = sh.flag_min;
+        const int cstar = flag_min;
         pick = -1;
-        // the running sum reaches the target inside chunk cstar (an element
-        // that raises it is > 0); later chunks only as a guard
-        double sc = cstar < nch ? sstart[cstar] : 0.0;
-        for (int cc = cstar; cc < nch && pick < 0; ++cc) {
-            const FoldResult sr = fold_chunk_block(sh, dist2, N, cc, sc, true, target);
-            pick = sr.pick;
-            sc = sr.s;
+        if (threadIdx.x < 32) {
+            // the running sum reaches the target inside chunk cstar (an element
+            // that raises it is > 0); later chunks only as a guard
+            double sc = cstar < nch ? sstart[cstar] : 0.0;
+            for (int cc = cstar; cc < nch && pick < 0; ++cc) {
+                const SegFold sr = warp_fold_chunk(dist2, segbuf, N, cc, 0, 0u, Rseg + static_cast<long long>(cc) * 2 * kSegs,
+                                                   Eseg + static_cast<long long>(cc) * kSegs, nullptr, sc, true, target);
+                pick = sr.pick;
+                sc = sr.s;
+            }
+            if (pick < 0) pick = N - 1;
         }
-        if (pick < 0) pick = N - 1;
-        __syncthreads();
         if (threadIdx.x == 0) *draw_counter = di + 1;
     }
     if (threadIdx.x == 0) {
+        WALK_T(T3);
+        WALK_ADD(0, T1 - T0);
+        WALK_ADD(1, T2 - T1);
+        WALK_ADD(4, T3 - T2);
+        WALK_ADD(5, 1);
         chosen[t] = static_cast<uint32_t>(pick);
         if (pick < N) {
             dist2[pick] = 0.0;
@@ -620,12 +901,16 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     cudaStream_t s = ctx.stream;
     const int nch = ceil_div(N, kFoldChunk);
     DevBuf<double> dist2(N), csum(nch), sstart(nch + 1);
-    DevBuf<int> ebin(nch);
-    DevBuf<longlong2> R(nch);
+    DevBuf<int> ebin(nch), spred(nch), Eseg(static_cast<size_t>(nch) * kSegs);
+    DevBuf<unsigned> smask(nch);
+    DevBuf<double> astart(nch);
+    DevBuf<longlong2> R(nch), Rseg(static_cast<size_t>(nch) * 2 * kSegs);
     DevBuf<unsigned char> used(N);
     // walk: chunk plans + running-sum table staged in shared memory if they fit
-    size_t walk_smem = static_cast<size_t>(nch) * (sizeof(longlong2) + sizeof(double) + sizeof(int)) + sizeof(double);
-    int walk_staged = walk_smem + sizeof(WalkShared) <= 200 * 1024;
+    size_t walk_smem = static_cast<size_t>(nch) * (sizeof(longlong2) + sizeof(double) + 4 * sizeof(int)) + sizeof(double) +
+                       static_cast<size_t>(kMaxPre) * (2 * kSegs * sizeof(longlong2) + kSegLen * sizeof(double) +
+                                                       kSegs * sizeof(int));
+    int walk_staged = walk_smem <= 200 * 1024;
     if (walk_staged)
         CUDA_OK(cudaFuncSetAttribute(pp_walk_pick_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(walk_smem)));
@@ -663,15 +948,30 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
         pp_exact_kernel<T><<<ex_grid, ex_warps * 32, ex_smem, s>>>(X, d, d_chosen, t - 1, dist2.get(), near.get(),
                                                                    list.get(), cnt.get());
         fold_chunk_sum_kernel<<<nch, 256, 0, s>>>(dist2.get(), N, csum.get());
-        fold_plan_kernel<<<1, 1024, 0, s>>>(csum.get(), nch, ebin.get());
-        fold_round_kernel<<<nch, 256, 0, s>>>(dist2.get(), N, ebin.get(), R.get());
-        pp_walk_pick_kernel<<<1, kWalkThreads, walk_smem, s>>>(dist2.get(), used.get(), N, nch, ebin.get(), R.get(),
-                                                               sstart.get(), d_raw.get(), static_cast<int>(raw.size()),
-                                                               counter.get(), d_chosen, t, walk_staged);
+        fold_plan_kernel<<<1, 1024, 0, s>>>(csum.get(), nch, ebin.get(), astart.get());
+        fold_round_kernel<<<nch, 256, 0, s>>>(dist2.get(), N, ebin.get(), astart.get(), R.get(), Rseg.get(),
+                                              Eseg.get(), spred.get(), smask.get());
+        pp_walk_pick_kernel<<<1, kWalkThreads, walk_smem, s>>>(
+            dist2.get(), used.get(), N, nch, ebin.get(), spred.get(), R.get(), Rseg.get(), Eseg.get(), smask.get(),
+            sstart.get(),
+            d_raw.get(),
+            static_cast<int>(raw.size()), counter.get(), d_chosen, t, walk_staged);
     }
     LAUNCH_OK("kmeans++");
     if (draws_used) counter.download(draws_used, 1, s);
     ctx.sync();
+#ifdef LCN_WALK_PROFILE
+    if (std::getenv("LCN_WALK_STATS")) {
+        unsigned long long h[16];
+        CUDA_OK(cudaMemcpyFromSymbol(h, g_wt, sizeof(h)));
+        const double n = h[5] ? static_cast<double>(h[5]) : 1.0;
+        std::fprintf(stderr,
+                     "[walk] cycles per launch: stage %.0f level1 %.0f (chunk0 %.0f, other chunks %.0f in %.1f calls; "
+                     "segment folds %.0f in %.1f) search+pick %.0f\n",
+                     h[0] / n, h[1] / n, h[8] / n, h[2] / n, h[3] / n, h[6] / n, h[7] / n, h[4] / n);
+        CUDA_OK(cudaMemset(g_wt_ptr(), 0, sizeof(h)));
+    }
+#endif
 }
 
 // ---- Lloyd (kmeans.cpp:87-143) ---------------------------------------------

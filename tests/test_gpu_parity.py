@@ -44,6 +44,20 @@ def test_kmeans_pp_bit_exact(ctx, ref, n, d, k, seed):
     assert np.array_equal(lcn.kmeans_pp_indices(ctx, x, k, seed=seed), ref.kmeans_pp(x, k, seed))
 
 
+@pytest.mark.parametrize("kind", ["mixture", "outliers", "duplicates"])
+def test_kmeans_pp_large_walk(ctx, ref, kind):
+    # ~700 fold chunks: clean runs, binade-crossing segments, huge elements
+    # (outliers far away) and runs of zeros (duplicated points)
+    n, d, k = 1_400_000, 3, 24
+    x = rng_points(77, n, d, comps=12)
+    if kind == "outliers":
+        r = np.random.default_rng(78)
+        x[r.choice(n, 50, replace=False)] *= 1e5
+    elif kind == "duplicates":
+        x[: n // 2] = x[0]
+    assert np.array_equal(lcn.kmeans_pp_indices(ctx, x, k, seed=9), ref.kmeans_pp(x, k, 9))
+
+
 def test_kmeans_pp_duplicates_total_zero(ctx, ref):
     # all points coincide: total <= 0 branch takes the first unused index (kmeans.cpp:42-47)
     x = np.zeros((12, 3))
