@@ -272,24 +272,6 @@ int lcn_ctx_set_profile(lcn_ctx* ctx, int on) {
 
 const char* lcn_ctx_last_error(const lcn_ctx* ctx) { return ctx ? ctx->c.last_error.c_str() : g_orphan_error.c_str(); }
 
-int lcn_kmeans_pp_indices(lcn_ctx* ctx, const double* points, size_t n, size_t d, size_t k, uint64_t first_index,
-                          const uint64_t* raw_draws, size_t n_draws, uint32_t* out, size_t* draws_used) {
-    return guard(ctx, [&] {
-        if (k == 0 || k > n) throw Status(2, "kmeans++: k must be in [1, n]");
-        if (first_index >= n) throw Status(2, "kmeans++: first index out of range");
-        DevBuf<double> X;
-        X.upload(points, n * d, ctx->c.stream);
-        std::vector<unsigned long long> raw(raw_draws, raw_draws + n_draws);
-        DevBuf<uint32_t> ch(k);
-        int used = 0;
-        kmeans_pp_device<double>(ctx->c, X.get(), n, static_cast<int>(d), static_cast<int>(k), first_index, raw,
-                                 ch.get(), &used);
-        ch.download(out, k, ctx->c.stream);
-        ctx->c.sync();
-        if (draws_used) *draws_used = static_cast<size_t>(used);
-    });
-}
-
 // fp32 copy of host points when every coordinate is fp32-representable (the
 // k-means kernels then read 4-byte points; distances are the same fp64 folds)
 static bool fp32_copy(const double* p, size_t count, std::vector<float>& f) {
@@ -297,6 +279,32 @@ static bool fp32_copy(const double* p, size_t count, std::vector<float>& f) {
     for (size_t i = 0; i < count; ++i)
         if (static_cast<double>(f[i] = static_cast<float>(p[i])) != p[i]) return false;
     return true;
+}
+
+int lcn_kmeans_pp_indices(lcn_ctx* ctx, const double* points, size_t n, size_t d, size_t k, uint64_t first_index,
+                          const uint64_t* raw_draws, size_t n_draws, uint32_t* out, size_t* draws_used) {
+    return guard(ctx, [&] {
+        if (k == 0 || k > n) throw Status(2, "kmeans++: k must be in [1, n]");
+        if (first_index >= n) throw Status(2, "kmeans++: first index out of range");
+        std::vector<unsigned long long> raw(raw_draws, raw_draws + n_draws);
+        DevBuf<uint32_t> ch(k);
+        int used = 0;
+        std::vector<float> f;
+        if (fp32_copy(points, n * d, f)) {
+            DevBuf<float> X32;
+            X32.upload(f.data(), f.size(), ctx->c.stream);
+            kmeans_pp_device<float>(ctx->c, X32.get(), n, static_cast<int>(d), static_cast<int>(k), first_index, raw,
+                                    ch.get(), &used);
+        } else {
+            DevBuf<double> X;
+            X.upload(points, n * d, ctx->c.stream);
+            kmeans_pp_device<double>(ctx->c, X.get(), n, static_cast<int>(d), static_cast<int>(k), first_index, raw,
+                                     ch.get(), &used);
+        }
+        ch.download(out, k, ctx->c.stream);
+        ctx->c.sync();
+        if (draws_used) *draws_used = static_cast<size_t>(used);
+    });
 }
 
 int lcn_assign_nearest(lcn_ctx* ctx, const double* points, size_t n, size_t d, const double* centroids, size_t k,

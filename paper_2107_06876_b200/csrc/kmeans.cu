@@ -13,6 +13,7 @@
 //   * empty clusters are re-seeded in increasing cluster order to the first
 //     farthest point among clusters of size > 1 (kmeans.cpp:122-139).
 #include <cub/cub.cuh>
+#include <cuda_fp16.h>
 
 #include <cstdlib>
 #include <random>
@@ -188,6 +189,193 @@ __global__ void __launch_bounds__(128) pp_exact_kernel(const T* __restrict__ X, 
             }
         }
         __syncwarp();
+    }
+}
+
+// ---- fp16 pre-filter of the exact pass --------------------------------------
+// Most listed points cannot update (the triangle bound is weak in high
+// dimensions), yet proving it exactly costs a 4d-byte row read and a d-step
+// fp64 fold. An fp16 copy x^ = s h (s a power of two per row, |h| <= 1) with
+// a rigorous eps_x >= ||x - x^||_2 decides most of them from 2d bytes:
+//   ||x - c|| >= ||x^ - c32|| - eps_x - eps_c        (norm triangle inequality)
+// with c32 the fp32 center (eps_c >= ||c - c32||) and ||x^ - c32||^2 from an
+// fp32 sum whose relative error is below (dp + 4) 2^-23. When the square of
+// that lower bound, less 1e-12 relative (the fp64 fold's own error is below
+// (d + 2) 2^-53), is >= dist2[i], the exact fold cannot be < dist2[i]
+// (kmeans.cpp:38 updates on strict <), so the point is skipped; every other
+// point gets the exact fold.
+constexpr int kFiltMaxQ = 4;  // 8-byte chunks per lane: rows of up to 512 halves
+#ifdef LCN_WALK_PROFILE
+__device__ unsigned long long g_filt_surv;
+#endif
+
+template <typename T>
+__global__ void __launch_bounds__(256) pp_half_prep_kernel(const T* __restrict__ X, long long N, int d, int dp,
+                                                           __half* __restrict__ Xh, float2* __restrict__ se) {
+    const long long row = blockIdx.x * 8LL + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= N) return;
+    const T* x = X + row * d;
+    double m = 0.0;
+    for (int k = lane; k < d; k += 32) m = fmax(m, fabs(static_cast<double>(x[k])));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    int e = 0;
+    frexp(m, &e);  // m < 2^e
+    const bool ok = m == 0.0 || (m < 1e30 && m > 1e-30);
+    const double sc = ldexp(1.0, e), inv = ldexp(1.0, -e);
+    double err2 = 0.0;
+    for (int k = lane; k < dp; k += 32) {
+        const double v = k < d ? static_cast<double>(x[k]) : 0.0;
+        const __half h = __float2half_rn(static_cast<float>(v * inv));
+        Xh[row * dp + k] = h;
+        const double df = v - static_cast<double>(__half2float(h)) * sc;
+        err2 += df * df;
+    }
+    err2 = warp_sum(err2);
+    if (lane == 0)
+        se[row] = make_float2(static_cast<float>(sc), ok ? __double2float_ru(sqrt(err2) * (1.0 + 1e-12) + 1e-300)
+                                                         : kPosInf);
+}
+
+// 32 values per lane -> lane l gets the warp sum of value l (31 shuffles)
+__device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
+#pragma unroll
+    for (int w = 16; w >= 1; w >>= 1) {
+        const bool hi = lane & w;
+#pragma unroll
+        for (int i = 0; i < w; ++i) {
+            const float send = hi ? v[i] : v[i + w];
+            const float keep = hi ? v[i + w] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+        }
+    }
+    return v[0];
+}
+
+// Filtered exact pass: per warp, 32 listed points. Their fp16 rows are
+// staged in shared memory with 16-byte cp.async (one memory latency per 32
+// rows), the bound is computed lane-parallel with one transpose reduction,
+// and the survivors' rows are staged into the same buffer and folded exactly
+// as in pp_exact_kernel. dp is a multiple of 8 (16-byte row chunks).
+template <typename T, int NQ>
+__global__ void __launch_bounds__(128) pp_filter_exact_kernel(const T* __restrict__ X, const __half* __restrict__ Xh,
+                                                              const float2* __restrict__ se, int d, int dp,
+                                                              const uint32_t* __restrict__ chosen, int t,
+                                                              double* __restrict__ dist2, uint32_t* __restrict__ near,
+                                                              const uint32_t* __restrict__ list,
+                                                              const unsigned* __restrict__ count, int wbuf_bytes) {
+    extern __shared__ __align__(16) unsigned char dyn[];
+    __shared__ double eps_c;
+    double* cs = reinterpret_cast<double*>(dyn);  // the new seed, fp64
+    float* c32 = reinterpret_cast<float*>(cs + d);  // max(dp, NQ 128) entries
+    unsigned char* wb = dyn + (static_cast<size_t>(d) * 8 + (max(dp, NQ * 128) + 4) * 4 + 15) / 16 * 16;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    unsigned char* mybuf = wb + static_cast<size_t>(warp) * wbuf_bytes;
+    __half* hbuf = reinterpret_cast<__half*>(mybuf);  // 32 x dp halves
+    T* buf = reinterpret_cast<T*>(mybuf);             // 32 x (d + 1) survivors' rows
+    const long long last = chosen[t];
+    for (int k = threadIdx.x; k < NQ * 128; k += blockDim.x) {
+        const double v = k < d ? static_cast<double>(X[last * d + k]) : 0.0;
+        if (k < d) cs[k] = v;
+        c32[k] = static_cast<float>(v);
+    }
+    __syncthreads();
+    if (warp == 0) {
+        double e2 = 0.0;
+        for (int k = lane; k < d; k += 32) {
+            const double df = cs[k] - static_cast<double>(c32[k]);
+            e2 += df * df;
+        }
+        e2 = warp_sum(e2);
+        if (lane == 0) eps_c = sqrt(e2) * (1.0 + 1e-12) + 1e-300;
+    }
+    __syncthreads();
+    const double ec = eps_c;
+    const double gam = 1.0 - (dp + 4) * 1.1920928955078125e-07;  // (dp + 4) 2^-23
+    const int nch16 = dp / 8;                                     // 16-byte chunks per fp16 row
+    // lane's 4-value chunks of the center (zero beyond dp: hbuf there is never
+    // staged, its products are multiplied out below)
+    float4 cq[NQ];
+    bool qin[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const int ch = lane + 32 * q;
+        qin[q] = ch * 4 < dp;
+        cq[q] = qin[q] ? make_float4(c32[4 * ch], c32[4 * ch + 1], c32[4 * ch + 2], c32[4 * ch + 3])
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const unsigned cnt = *count;
+    for (unsigned b0 = (blockIdx.x * nw + warp) * 32u; b0 < cnt; b0 += gridDim.x * nw * 32u) {
+        const unsigned nb = cnt - b0 < 32u ? cnt - b0 : 32u;
+        // rows past the batch read row 0 (harmless; their lanes are ignored)
+        const uint32_t mine = lane < static_cast<int>(nb) ? list[b0 + lane] : 0u;
+        __syncwarp();
+        for (int e = lane; e < 32 * nch16; e += 32) {  // one (row, chunk) per lane and step
+            const int j = e / nch16, c = e - j * nch16;
+            const long long row = __shfl_sync(0xffffffffu, mine, j);
+            cp_async16(hbuf + j * dp + c * 8, Xh + row * dp + c * 8);
+        }
+        cp_async_commit();
+        const float2 my_se = se[mine];
+        const double my_d2 = dist2[mine];
+        cp_async_wait<0>();
+        __syncwarp();
+        float part[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const float sj = __shfl_sync(0xffffffffu, my_se.x, j);
+            float acc = 0.f;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                if (!qin[q]) continue;
+                const uint2 raw = *reinterpret_cast<const uint2*>(hbuf + j * dp + 4 * (lane + 32 * q));
+                const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
+                const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
+                const float d0 = fmaf(a.x, sj, -cq[q].x), d1 = fmaf(a.y, sj, -cq[q].y);
+                const float d2 = fmaf(b.x, sj, -cq[q].z), d3 = fmaf(b.y, sj, -cq[q].w);
+                acc = fmaf(d0, d0, acc);
+                acc = fmaf(d1, d1, acc);
+                acc = fmaf(d2, d2, acc);
+                acc = fmaf(d3, d3, acc);
+            }
+            part[j] = acc;
+        }
+        const float A = transpose_reduce32(part, lane);
+        bool need = false;
+        if (lane < static_cast<int>(nb)) {
+            const double lo = sqrt(static_cast<double>(A) * gam) - static_cast<double>(my_se.y) - ec;
+            need = !(lo > 0.0 && lo * lo * (1.0 - 1e-12) >= my_d2);
+        }
+        const unsigned sv = __ballot_sync(0xffffffffu, need);
+        const int ns = __popc(sv);
+#ifdef LCN_WALK_PROFILE
+        if (lane == 0) atomicAdd(&g_filt_surv, static_cast<unsigned long long>(ns));
+#endif
+        if (!ns) continue;
+        // lane r takes the r-th survivor
+        const int jr = lane < ns ? static_cast<int>(__fns(sv, 0, lane + 1)) : 0;
+        const uint32_t srow = __shfl_sync(0xffffffffu, mine, jr);
+        __syncwarp();
+        for (int r = 0; r < ns; ++r) {
+            const long long row = __shfl_sync(0xffffffffu, srow, r);
+            for (int k = lane; k < d; k += 32) cp_async_elem(&buf[r * (d + 1) + k], X + row * d + k);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncwarp();
+        if (lane < ns) {
+            const T* r = buf + lane * (d + 1);
+            double acc = 0.0;
+            for (int k = 0; k < d; ++k) {
+                const double df = xsub(static_cast<double>(r[k]), cs[k]);
+                acc = xadd(acc, xmul(df, df));
+            }
+            if (acc < dist2[srow]) {
+                dist2[srow] = acc;
+                near[srow] = static_cast<uint32_t>(t);
+            }
+        }
     }
 }
 
@@ -929,6 +1117,36 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     int ex_occ = 1;
     CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ex_occ, pp_exact_kernel<T>, ex_warps * 32, ex_smem));
     const int ex_grid = std::max(1, ex_occ) * ctx.num_sms;
+    // fp16 filter copy (rows up to 512 halves)
+    const int dp = (d + 7) / 8 * 8;
+    const bool filt = dp <= kFiltMaxQ * 128 && std::getenv("LCN_PP_NOFILTER") == nullptr;
+    DevBuf<__half> Xh(filt ? static_cast<size_t>(N) * dp : 1);
+    DevBuf<float2> se(filt ? static_cast<size_t>(N) : 1);
+    const int wbuf_bytes = static_cast<int>(
+        (std::max(static_cast<size_t>(32) * dp * 2, static_cast<size_t>(32) * (d + 1) * sizeof(T)) + 15) / 16 * 16);
+    const int nq = (dp / 4 + 31) / 32;
+    // c32 is read for NQ * 128 entries; the per-warp buffers start 16-aligned
+    const size_t fx_smem = (static_cast<size_t>(d) * 8 + (std::max(dp, nq * 128) + 4) * 4 + 15) / 16 * 16 +
+                           static_cast<size_t>(ex_warps) * wbuf_bytes;
+    auto fx_kernel = [&]() -> void (*)(const T*, const __half*, const float2*, int, int, const uint32_t*, int,
+                                       double*, uint32_t*, const uint32_t*, const unsigned*, int) {
+        switch (nq) {
+            case 1: return pp_filter_exact_kernel<T, 1>;
+            case 2: return pp_filter_exact_kernel<T, 2>;
+            case 3: return pp_filter_exact_kernel<T, 3>;
+            default: return pp_filter_exact_kernel<T, 4>;
+        }
+    }();
+    int fx_grid = ex_grid;
+    if (filt) {
+        pp_half_prep_kernel<T><<<ceil_div(N, 8), 256, 0, s>>>(X, N, d, dp, Xh.get(), se.get());
+        LAUNCH_OK("kmeans++ fp16 filter copy");
+        CUDA_OK(cudaFuncSetAttribute(fx_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(fx_smem)));
+        int occ = 1;
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fx_kernel, ex_warps * 32, fx_smem));
+        fx_grid = std::max(1, occ) * ctx.num_sms;
+    }
     DevBuf<unsigned long long> d_raw(raw.size() ? raw.size() : 1);
     DevBuf<int> counter(1);
     used.zero(s);
@@ -945,8 +1163,26 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
         cnt.zero(s);
         pp_prune_kernel<<<ceil_div(N, 256), 256, 0, s>>>(N, t - 1, dist2.get(), near.get(), dc.get(), list.get(),
                                                          cnt.get());
-        pp_exact_kernel<T><<<ex_grid, ex_warps * 32, ex_smem, s>>>(X, d, d_chosen, t - 1, dist2.get(), near.get(),
-                                                                   list.get(), cnt.get());
+        if (filt)
+            fx_kernel<<<fx_grid, ex_warps * 32, fx_smem, s>>>(X, Xh.get(), se.get(), d, dp, d_chosen, t - 1,
+                                                              dist2.get(), near.get(), list.get(), cnt.get(),
+                                                              wbuf_bytes);
+        else
+            pp_exact_kernel<T><<<ex_grid, ex_warps * 32, ex_smem, s>>>(X, d, d_chosen, t - 1, dist2.get(), near.get(),
+                                                                       list.get(), cnt.get());
+#ifdef LCN_WALK_PROFILE
+        if (std::getenv("LCN_WALK_STATS") && (t % 256 == 0 || t == k - 1)) {
+            unsigned hc = 0;
+            cnt.download(&hc, 1, s);
+            ctx.sync();
+            unsigned long long hs = 0;
+            CUDA_OK(cudaMemcpyFromSymbol(&hs, g_filt_surv, sizeof(hs)));
+            const unsigned long long z = 0;
+            CUDA_OK(cudaMemcpyToSymbol(g_filt_surv, &z, sizeof(z)));
+            std::fprintf(stderr, "[seed] N=%lld t=%d candidates %u (%.2f%%), exact folds since last %llu\n", N, t, hc,
+                         100.0 * hc / N, hs);
+        }
+#endif
         fold_chunk_sum_kernel<<<nch, 256, 0, s>>>(dist2.get(), N, csum.get());
         fold_plan_kernel<<<1, 1024, 0, s>>>(csum.get(), nch, ebin.get(), astart.get());
         fold_round_kernel<<<nch, 256, 0, s>>>(dist2.get(), N, ebin.get(), astart.get(), R.get(), Rseg.get(),
