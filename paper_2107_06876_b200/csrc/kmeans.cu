@@ -105,6 +105,7 @@ __global__ void __launch_bounds__(256) assign_exact_kernel(const T* __restrict__
 }
 
 // ---- k-means++ (kmeans.cpp:23-65) ------------------------------------------
+constexpr int kFoldChunk = 2048;  // fold chunk (see the chunk-parallel exact fold below)
 // dist2[i] = min(dist2[i], sqdist(x_i, x_last)), strict < as kmeans.cpp:38.
 // Pruning (exactness-preserving): near[i] is the seed whose fold gave
 // dist2[i]; with dc[j] = |x_{seed j} - x_last| (fp64, |rel err| < 1e-13), the
@@ -118,33 +119,64 @@ __global__ void __launch_bounds__(256) assign_exact_kernel(const T* __restrict__
 __global__ void __launch_bounds__(256) pp_prune_kernel(long long N, int t, const double* __restrict__ dist2,
                                                        const uint32_t* __restrict__ near,
                                                        const double* __restrict__ dc, uint32_t* __restrict__ list,
-                                                       unsigned* __restrict__ count) {
-    const long long p = blockIdx.x * 256LL + threadIdx.x;
-    bool need = p < N;
-    if (need && t > 0) {
-        const double D = dist2[p];
-        if (D < kPosInf) {
-            const double lb = dc[near[p]] * (1.0 - 1e-12);
-            if (lb >= 2.0 * sqrt(D) * (1.0 + 1e-9)) need = false;
-        }
-    }
-    // block-aggregated append: one global atomic per block (a single counter
-    // hit by every warp serialises at L2)
+                                                       unsigned* __restrict__ count, double* __restrict__ csum) {
+    // one block per fold chunk (kFoldChunk points, kPP per thread, strided
+    // for coalescing): one list-append atomic per chunk, and the chunk's
+    // dist2 sum (approximate chunk sums steer the fold's binade predictions
+    // only; the exact pass subtracts its updates)
+    constexpr int kPP = kFoldChunk / 256;
     __shared__ unsigned wcnt[8], wbase[8], bbase;
+    __shared__ double wsum[8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const unsigned m = __ballot_sync(0xffffffffu, need);
-    if (lane == 0) wcnt[warp] = __popc(m);
+    const long long base = static_cast<long long>(blockIdx.x) * kFoldChunk + threadIdx.x;
+    unsigned m[kPP];
+    double bs = 0.0;
+    unsigned wc = 0;
+    // all loads first (memory-level parallelism), then the gathers, then the tests
+    double D[kPP], C[kPP];
+    uint32_t nr[kPP];
+#pragma unroll
+    for (int j = 0; j < kPP; ++j) {
+        const long long p = base + j * 256;
+        D[j] = p < N ? dist2[p] : 0.0;
+        nr[j] = p < N && t > 0 ? near[p] : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < kPP; ++j) C[j] = t > 0 ? dc[nr[j]] : 0.0;
+#pragma unroll
+    for (int j = 0; j < kPP; ++j) {
+        const long long p = base + j * 256;
+        bool need = p < N;
+        bs += D[j];
+        if (need && t > 0 && D[j] < kPosInf && C[j] * (1.0 - 1e-12) >= 2.0 * sqrt(D[j]) * (1.0 + 1e-9)) need = false;
+        m[j] = __ballot_sync(0xffffffffu, need);
+        wc += __popc(m[j]);
+    }
+    bs = warp_sum(bs);
+    if (lane == 0) {
+        wcnt[warp] = wc;
+        wsum[warp] = bs;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned tot = 0;
+        double cs = 0.0;
         for (int w = 0; w < 8; ++w) {
             wbase[w] = tot;
             tot += wcnt[w];
+            cs += wsum[w];
         }
         bbase = tot ? atomicAdd(count, tot) : 0u;
+        csum[blockIdx.x] = cs;
     }
     __syncthreads();
-    if (need) list[bbase + wbase[warp] + __popc(m & ((1u << lane) - 1u))] = static_cast<uint32_t>(p);
+    unsigned off = bbase + wbase[warp];
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int j = 0; j < kPP; ++j) {
+        if ((m[j] >> lane) & 1) list[off + __popc(m[j] & lt)] = static_cast<uint32_t>(base + j * 256);
+        off += __popc(m[j]);
+    }
 }
 
 // Exact pass over the listed points: each warp stages 32 listed rows in
@@ -156,7 +188,8 @@ __global__ void __launch_bounds__(128) pp_exact_kernel(const T* __restrict__ X, 
                                                        const uint32_t* __restrict__ chosen, int t,
                                                        double* __restrict__ dist2, uint32_t* __restrict__ near,
                                                        const uint32_t* __restrict__ list,
-                                                       const unsigned* __restrict__ count) {
+                                                       const unsigned* __restrict__ count,
+                                                       double* __restrict__ csum) {
     extern __shared__ __align__(16) unsigned char dyn[];
     double* cs = reinterpret_cast<double*>(dyn);  // the new seed, fp64
     T* rows = reinterpret_cast<T*>(cs + d);
@@ -183,9 +216,11 @@ __global__ void __launch_bounds__(128) pp_exact_kernel(const T* __restrict__ X, 
                 const double df = xsub(static_cast<double>(r[k]), cs[k]);
                 acc = xadd(acc, xmul(df, df));
             }
-            if (acc < dist2[mine]) {
+            const double old = dist2[mine];
+            if (acc < old) {
                 dist2[mine] = acc;
                 near[mine] = static_cast<uint32_t>(t);
+                if (old < kPosInf) atomicAdd(&csum[mine / kFoldChunk], acc - old);
             }
         }
         __syncwarp();
@@ -264,7 +299,8 @@ __global__ void __launch_bounds__(128) pp_filter_exact_kernel(const T* __restric
                                                               const uint32_t* __restrict__ chosen, int t,
                                                               double* __restrict__ dist2, uint32_t* __restrict__ near,
                                                               const uint32_t* __restrict__ list,
-                                                              const unsigned* __restrict__ count, int wbuf_bytes) {
+                                                              const unsigned* __restrict__ count, int wbuf_bytes,
+                                                              double* __restrict__ csum) {
     extern __shared__ __align__(16) unsigned char dyn[];
     __shared__ double eps_c;
     double* cs = reinterpret_cast<double*>(dyn);  // the new seed, fp64
@@ -371,9 +407,11 @@ __global__ void __launch_bounds__(128) pp_filter_exact_kernel(const T* __restric
                 const double df = xsub(static_cast<double>(r[k]), cs[k]);
                 acc = xadd(acc, xmul(df, df));
             }
-            if (acc < dist2[srow]) {
+            const double old = dist2[srow];
+            if (acc < old) {
                 dist2[srow] = acc;
                 near[srow] = static_cast<uint32_t>(t);
+                if (old < kPosInf) atomicAdd(&csum[srow / kFoldChunk], acc - old);
             }
         }
     }
@@ -502,18 +540,18 @@ __device__ __forceinline__ longlong2 par_clamp(ParInc v) {
 // The fold over N values is cut into chunks of kFoldChunk. Most chunks lie
 // inside one binade of the running sum, where the fold's result depends only
 // on that binade: S_end = S_start + u_e * sum_j RN(x_j / u_e). So
-//   A) approximate chunk sums (any order)            -> predicted start A_c
+//   A) approximate chunk sums (any order; accumulated by the prune pass,
+//      corrected by the exact pass)                  -> predicted start A_c
 //   B) predicted binade e_c of each chunk (dirty if the interval
 //      [A_c (1-1e-9), A_{c+1} (1+1e-9)] straddles a power of two)
 //   C) the chunk's parity function R_c(e_c) = {inc[0], inc[1]} in parallel
-//      (ties included), dirty only on huge x
+//      (ties included), dirty only on huge x; B and C in fold_round
 //   D) one warp walks the chunks in order with the exact running sum: runs
 //      of clean chunks whose actual binade matches e_c advance by a
-//      parity-scan of their R_c, any other chunk is folded element-wise by
-//      block_exact_fold.
+//      parity-scan of their R_c, any other chunk by warp_fold_chunk
+//      (segment tables, literal folds where the binade changes).
 // The prediction only decides which path a chunk takes; the walk re-checks
 // the actual binade, so the result is exact regardless.
-constexpr int kFoldChunk = 2048;
 
 __global__ void fold_chunk_sum_kernel(const double* __restrict__ x, long long N, double* __restrict__ csum) {
     __shared__ double red[8];
@@ -528,33 +566,6 @@ __global__ void fold_chunk_sum_kernel(const double* __restrict__ x, long long N,
         double t = 0.0;
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
         csum[blockIdx.x] = t;
-    }
-}
-
-__global__ void fold_plan_kernel(const double* __restrict__ csum, int nch, int* __restrict__ ebin,
-                                 double* __restrict__ astart) {
-    // single block of 1024: blocked exclusive scan of the approximate sums
-    __shared__ double tot[1024];
-    const int per = (nch + 1023) / 1024;
-    const int c0 = threadIdx.x * per, c1 = min(nch, c0 + per);
-    double s = 0.0;
-    for (int c = c0; c < c1; ++c) s += csum[c];
-    tot[threadIdx.x] = s;
-    __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {
-        double v = threadIdx.x >= o ? tot[threadIdx.x - o] : 0.0;
-        __syncthreads();
-        tot[threadIdx.x] += v;
-        __syncthreads();
-    }
-    double a = threadIdx.x ? tot[threadIdx.x - 1] : 0.0;
-    for (int c = c0; c < c1; ++c) {
-        double lo = a * (1.0 - 1e-9), hi = (a + csum[c]) * (1.0 + 1e-9);
-        astart[c] = a;
-        a += csum[c];
-        int e = -100000;
-        if (lo >= kMinNormal && hi < kPosInf && ilogb(lo) == ilogb(hi)) e = ilogb(lo);
-        ebin[c] = e;
     }
 }
 
@@ -598,15 +609,16 @@ __device__ __forceinline__ void predict_binade(double a, double b, int& e_one, i
 }
 
 __global__ void __launch_bounds__(256) fold_round_kernel(const double* __restrict__ x, long long N,
-                                                         const int* __restrict__ ebin, const double* __restrict__ astart,
+                                                         const double* __restrict__ csum, int* __restrict__ ebin,
                                                          longlong2* __restrict__ R, longlong2* __restrict__ Rseg,
                                                          int* __restrict__ Eseg, int* __restrict__ spred,
-                                                         unsigned* __restrict__ smask) {
+                                                         unsigned* __restrict__ smask, double* __restrict__ s0end) {
     __shared__ ParInc stot[kSegs];
     __shared__ double ssum[kSegs];
+    __shared__ double red[8];
     __shared__ int sbase[kSegs];
-    __shared__ int all_one;
-    const int e = ebin[blockIdx.x];
+    __shared__ int all_one, e_chunk;
+    __shared__ __align__(16) double c0buf[kFoldChunk];  // chunk 0, folded literally by block 0
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane / kLanesPerSeg;
     const int si = warp * (32 / kLanesPerSeg) + g;
@@ -618,27 +630,40 @@ __global__ void __launch_bounds__(256) fold_round_kernel(const double* __restric
         xv[j] = b + j < N ? x[b + j] : 0.0;
         xsum += xv[j];
     }
+    // approximate start of this chunk: the earlier chunks' approximate sums
+    double a = 0.0;
+    for (int c = threadIdx.x; c < static_cast<int>(blockIdx.x); c += 256) a += csum[c];
+    a = warp_sum(a);
+    if (lane == 0) red[warp] = a;
 #pragma unroll
     for (int o = 1; o < kLanesPerSeg; o <<= 1) xsum += __shfl_xor_sync(0xffffffffu, xsum, o);
     if ((lane & (kLanesPerSeg - 1)) == 0) ssum[si] = xsum;
+    if (blockIdx.x == 0)
+#pragma unroll
+        for (int j = 0; j < kRoundPer; ++j) c0buf[threadIdx.x * kRoundPer + j] = xv[j];
     __syncthreads();
     if (warp == 0) {  // approximate segment starts -> per-segment binades
-        double v = ssum[lane];
+        double a0 = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) a0 += red[w];
+        const double v = ssum[lane];
         double incl = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const double t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
+            const double tt = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += tt;
         }
-        const double a0 = astart[blockIdx.x];
-        int e_one, e_base;
+        int e_one, e_base, ec_one, ec_base;
         predict_binade(a0 + (incl - v), a0 + incl, e_one, e_base);
+        predict_binade(a0, a0 + __shfl_sync(0xffffffffu, incl, 31), ec_one, ec_base);
         sbase[lane] = e_base;
         Eseg[static_cast<long long>(blockIdx.x) * kSegs + lane] = e_base;
         const unsigned straddle = __ballot_sync(0xffffffffu, e_one == kNoBinade);
-        const unsigned one = __ballot_sync(0xffffffffu, e_one == e && e != kNoBinade);
+        const unsigned one = __ballot_sync(0xffffffffu, e_one == ec_one && ec_one != kNoBinade);
         if (lane == 0) {
             all_one = one == 0xffffffffu;
+            e_chunk = ec_one;
+            ebin[blockIdx.x] = ec_one;
             spred[blockIdx.x] = straddle ? __ffs(straddle) - 1 : 0;
             smask[blockIdx.x] = straddle;
         }
@@ -672,16 +697,29 @@ __global__ void __launch_bounds__(256) fold_round_kernel(const double* __restric
         stot[si] = sbad0 ? ParInc{-1, -1} : acc0;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        // clean chunk: every segment predicted inside binade e
-        bool ok = all_one;
-        ParInc t{0, 0};
-        for (int w = 0; w < kSegs && ok; ++w) {
-            if (stot[w].i0 < 0) ok = false;
-            else t = par_compose(t, stot[w]);
+    if (warp == 0) {
+        // clean chunk: every segment predicted inside the chunk's binade; its
+        // map is the composition of the segment maps (lane = segment)
+        const bool ok = all_one && __ballot_sync(0xffffffffu, stot[lane].i0 < 0) == 0;
+        const ParInc tot = par_scan(stot[lane], lane);
+        if (lane == 31) R[blockIdx.x] = ok ? par_clamp(tot) : make_longlong2(-1, -1);
+        if (blockIdx.x == 0) {
+            // chunk 0 starts the fold at 0, where the sum climbs binade after
+            // binade: fold it literally here, in parallel with the other chunks
+            const double2* c2 = reinterpret_cast<const double2*>(c0buf);
+            const int cnt0 = static_cast<int>(min(N, static_cast<long long>(kFoldChunk)));
+            double S = 0.0;
+#pragma unroll 8
+            for (int i = 0; i < cnt0 / 2; ++i) {
+                const double2 w = c2[i];
+                S = xadd(S, w.x);
+                S = xadd(S, w.y);
+            }
+            if (cnt0 & 1) S = xadd(S, c0buf[cnt0 - 1]);
+            if (lane == 0) *s0end = S;
         }
-        R[blockIdx.x] = ok ? par_clamp(t) : make_longlong2(-1, -1);
     }
+    (void)e_chunk;
 }
 
 // ---- literal fold of one segment -------------------------------------------
@@ -848,7 +886,8 @@ __device__ __noinline__ SegFold warp_fold_chunk(const double* __restrict__ x, do
 __global__ void __launch_bounds__(kWalkThreads) pp_walk_pick_kernel(
     double* __restrict__ dist2, unsigned char* __restrict__ used, long long N, int nch, const int* __restrict__ ebin,
     const int* __restrict__ spred, const longlong2* __restrict__ R, const longlong2* __restrict__ Rseg,
-    const int* __restrict__ Eseg, const unsigned* __restrict__ smask, double* __restrict__ sstart, const unsigned long long* __restrict__ raw, int n_raw, int* __restrict__ draw_counter,
+    const int* __restrict__ Eseg, const unsigned* __restrict__ smask, const double* __restrict__ s0end,
+    double* __restrict__ csum, unsigned* __restrict__ cand_count, double* __restrict__ sstart, const unsigned long long* __restrict__ raw, int n_raw, int* __restrict__ draw_counter,
     uint32_t* __restrict__ chosen, int t, int staged) {
     __shared__ int flag_min;
     __shared__ double total;
@@ -858,6 +897,8 @@ __global__ void __launch_bounds__(kWalkThreads) pp_walk_pick_kernel(
     extern __shared__ __align__(16) unsigned char wdyn[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     WALK_T(T0);
+    // the next step's prune appends to the candidate list from zero
+    if (threadIdx.x == 0) *cand_count = 0u;
     // chunk plans and the running-sum table in shared memory when they fit:
     // one memory latency for all plans instead of one per 32-chunk group;
     // then the segment tables and the predicted crossing segment of every
@@ -887,7 +928,7 @@ __global__ void __launch_bounds__(kWalkThreads) pp_walk_pick_kernel(
             es[c] = ebin[c];
             ps[c] = spred[c];
             ms[c] = smask[c];
-            nd += r.x < 0;
+            nd += r.x < 0 && c > 0;
         }
         int incl = nd;
 #pragma unroll
@@ -901,7 +942,7 @@ __global__ void __launch_bounds__(kWalkThreads) pp_walk_pick_kernel(
         for (int w = 0; w < warp; ++w) off += wcount[w];
         for (int c = c0; c < c1; ++c) {
             int sl = -1;
-            if (Rs[c].x < 0) {
+            if (Rs[c].x < 0 && c > 0) {
                 if (off < kMaxPre) {
                     sl = off;
                     pre_list[off] = c;
@@ -937,14 +978,16 @@ __global__ void __launch_bounds__(kWalkThreads) pp_walk_pick_kernel(
     }
     WALK_T(T1);
     if (threadIdx.x < 32) {
-        double S = 0.0;
+        // chunk 0 was folded literally by fold_round
+        double S = *s0end;
+        if (lane == 0) sstart[0] = 0.0;
         // kCPL x 32 chunks per step: a run of clean chunks in the running
         // sum's binade advances by one exact parity scan of their R_c; each
         // lane composes its kCPL chunks, then steps through them for their
         // exact starts (sstart) and the first chunk whose end leaves the
         // binade
         constexpr int kCPL = 4;
-        for (int cb = 0; cb < nch; cb += 32 * kCPL) {
+        for (int cb = 1; cb < nch; cb += 32 * kCPL) {
             ParInc rj[kCPL];
             int ej[kCPL];
 #pragma unroll
@@ -1091,7 +1134,7 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     DevBuf<double> dist2(N), csum(nch), sstart(nch + 1);
     DevBuf<int> ebin(nch), spred(nch), Eseg(static_cast<size_t>(nch) * kSegs);
     DevBuf<unsigned> smask(nch);
-    DevBuf<double> astart(nch);
+    DevBuf<double> s0end(1);
     DevBuf<longlong2> R(nch), Rseg(static_cast<size_t>(nch) * 2 * kSegs);
     DevBuf<unsigned char> used(N);
     // walk: chunk plans + running-sum table staged in shared memory if they fit
@@ -1129,7 +1172,7 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     const size_t fx_smem = (static_cast<size_t>(d) * 8 + (std::max(dp, nq * 128) + 4) * 4 + 15) / 16 * 16 +
                            static_cast<size_t>(ex_warps) * wbuf_bytes;
     auto fx_kernel = [&]() -> void (*)(const T*, const __half*, const float2*, int, int, const uint32_t*, int,
-                                       double*, uint32_t*, const uint32_t*, const unsigned*, int) {
+                                       double*, uint32_t*, const uint32_t*, const unsigned*, int, double*) {
         switch (nq) {
             case 1: return pp_filter_exact_kernel<T, 1>;
             case 2: return pp_filter_exact_kernel<T, 2>;
@@ -1152,6 +1195,8 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     used.zero(s);
     near.zero(s);
     counter.zero(s);
+    csum.zero(s);
+    cnt.zero(s);
     if (!raw.empty()) d_raw.upload(raw.data(), raw.size(), s);
     fill_kernel<<<ceil_div(N, 256), 256, 0, s>>>(dist2.get(), N, kPosInf);
     uint32_t f32 = static_cast<uint32_t>(first);
@@ -1160,16 +1205,15 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     CUDA_OK(cudaMemcpyAsync(used.get() + first, &one, 1, cudaMemcpyHostToDevice, s));
     for (int t = 1; t < k; ++t) {
         if (t > 1) seed_dist_kernel<T><<<ceil_div(t - 1, 8), 256, 0, s>>>(X, d, d_chosen, t - 1, dc.get());
-        cnt.zero(s);
-        pp_prune_kernel<<<ceil_div(N, 256), 256, 0, s>>>(N, t - 1, dist2.get(), near.get(), dc.get(), list.get(),
-                                                         cnt.get());
+        pp_prune_kernel<<<nch, 256, 0, s>>>(N, t - 1, dist2.get(), near.get(), dc.get(), list.get(), cnt.get(),
+                                            csum.get());
         if (filt)
             fx_kernel<<<fx_grid, ex_warps * 32, fx_smem, s>>>(X, Xh.get(), se.get(), d, dp, d_chosen, t - 1,
                                                               dist2.get(), near.get(), list.get(), cnt.get(),
-                                                              wbuf_bytes);
+                                                              wbuf_bytes, csum.get());
         else
             pp_exact_kernel<T><<<ex_grid, ex_warps * 32, ex_smem, s>>>(X, d, d_chosen, t - 1, dist2.get(), near.get(),
-                                                                       list.get(), cnt.get());
+                                                                       list.get(), cnt.get(), csum.get());
 #ifdef LCN_WALK_PROFILE
         if (std::getenv("LCN_WALK_STATS") && (t % 256 == 0 || t == k - 1)) {
             unsigned hc = 0;
@@ -1183,13 +1227,14 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
                          100.0 * hc / N, hs);
         }
 #endif
-        fold_chunk_sum_kernel<<<nch, 256, 0, s>>>(dist2.get(), N, csum.get());
-        fold_plan_kernel<<<1, 1024, 0, s>>>(csum.get(), nch, ebin.get(), astart.get());
-        fold_round_kernel<<<nch, 256, 0, s>>>(dist2.get(), N, ebin.get(), astart.get(), R.get(), Rseg.get(),
-                                              Eseg.get(), spred.get(), smask.get());
+        // the first pass moves every point off +inf: its chunk sums are taken
+        // afresh (later steps: prune sums minus the exact pass's updates)
+        if (t == 1) fold_chunk_sum_kernel<<<nch, 256, 0, s>>>(dist2.get(), N, csum.get());
+        fold_round_kernel<<<nch, 256, 0, s>>>(dist2.get(), N, csum.get(), ebin.get(), R.get(), Rseg.get(),
+                                              Eseg.get(), spred.get(), smask.get(), s0end.get());
         pp_walk_pick_kernel<<<1, kWalkThreads, walk_smem, s>>>(
             dist2.get(), used.get(), N, nch, ebin.get(), spred.get(), R.get(), Rseg.get(), Eseg.get(), smask.get(),
-            sstart.get(),
+            s0end.get(), csum.get(), cnt.get(), sstart.get(),
             d_raw.get(),
             static_cast<int>(raw.size()), counter.get(), d_chosen, t, walk_staged);
     }
