@@ -590,7 +590,7 @@ __device__ __forceinline__ ParInc par_scan8(ParInc v, int lane) {  // inclusive,
 #pragma unroll
     for (int o = 1; o < kLanesPerSeg; o <<= 1) {
         const ParInc t = par_shfl_up(v, o);
-        if ((lane & (kLanesPerSeg - 1)) >= o) v = par_compose(t, v);
+        if ((lane & (kLanesPerSeg - 1)) >= o) v = par_compose_ns(t, v);
     }
     return v;
 }
@@ -608,8 +608,8 @@ __device__ __forceinline__ void predict_binade(double a, double b, int& e_one, i
     }
 }
 
-__global__ void __launch_bounds__(256) fold_round_kernel(const double* __restrict__ x, long long N,
-                                                         const double* __restrict__ csum, int* __restrict__ ebin,
+__global__ void __launch_bounds__(256, 4) fold_round_kernel(const double* __restrict__ x, long long N,
+                                                            const double* __restrict__ csum, int* __restrict__ ebin,
                                                          longlong2* __restrict__ R, longlong2* __restrict__ Rseg,
                                                          int* __restrict__ Eseg, int* __restrict__ spred,
                                                          unsigned* __restrict__ smask, double* __restrict__ s0end) {
@@ -673,18 +673,31 @@ __global__ void __launch_bounds__(256) fold_round_kernel(const double* __restric
     ParInc acc0{0, 0}, acc1{0, 0};
     bool bad0 = eb == kNoBinade, bad1 = eb == kNoBinade;
     if (eb != kNoBinade) {
+        // grid scalings 2^(52-eb), 2^(51-eb) as exact power-of-two products
+        // when representable (scale_to_grid's fast path), else scalbn per
+        // element. Each map is at most 2^53 (q < 2^53), so 8 of them compose
+        // without saturation.
+        const int k0 = 52 - eb;
+        const bool fast = k0 <= 1023 && k0 - 1 >= -1022;
+        const double f0 = fast ? __longlong_as_double(static_cast<long long>(k0 + 1023) << 52) : 0.0;
+        const double f1 = fast ? __longlong_as_double(static_cast<long long>(k0 + 1022) << 52) : 0.0;
+        // one binade at a time (register pressure: 4 blocks per SM)
+        auto maps = [&](double f, int e, bool& bad) {
+            ParInc p[kRoundPer];
 #pragma unroll
-        for (int j = 0; j < kRoundPer; ++j) {
-            if (b + j < N) {
-                const double q0 = scale_to_grid(xv[j], eb);
-                if (!(q0 < 9007199254740992.0)) bad0 = true;
-                else acc0 = par_compose(acc0, par_element_fast(q0));
-                const double q1 = scale_to_grid(xv[j], eb + 1);
-                if (!(q1 < 9007199254740992.0)) bad1 = true;
-                else acc1 = par_compose(acc1, par_element_fast(q1));
+            for (int j = 0; j < kRoundPer; ++j) {
+                const double q = fast ? xv[j] * f : scale_to_grid(xv[j], e);
+                const bool in = b + j < N;
+                bad |= in && !(q < 9007199254740992.0);
+                p[j] = in && q < 9007199254740992.0 ? par_element_fast(q) : ParInc{0, 0};
             }
-        }
+            return par_compose_ns(par_compose_ns(par_compose_ns(p[0], p[1]), par_compose_ns(p[2], p[3])),
+                                  par_compose_ns(par_compose_ns(p[4], p[5]), par_compose_ns(p[6], p[7])));
+        };
+        acc0 = maps(f0, eb, bad0);
+        acc1 = maps(f1, eb + 1, bad1);
     }
+    static_assert(kRoundPer == 8, "tree composition above");
     const unsigned gmask = 0xffu << (g * kLanesPerSeg);
     const bool sbad0 = (__ballot_sync(0xffffffffu, bad0) & gmask) != 0;
     const bool sbad1 = (__ballot_sync(0xffffffffu, bad1) & gmask) != 0;
@@ -694,14 +707,16 @@ __global__ void __launch_bounds__(256) fold_round_kernel(const double* __restric
     if ((lane & (kLanesPerSeg - 1)) == kLanesPerSeg - 1) {
         seg[si] = sbad0 ? make_longlong2(-1, -1) : par_clamp(acc0);
         seg[kSegs + si] = sbad1 ? make_longlong2(-1, -1) : par_clamp(acc1);
-        stot[si] = sbad0 ? ParInc{-1, -1} : acc0;
+        const longlong2 cl = par_clamp(acc0);
+        stot[si] = sbad0 ? ParInc{-1, -1} : ParInc{cl.x, cl.y};
     }
     __syncthreads();
     if (warp == 0) {
         // clean chunk: every segment predicted inside the chunk's binade; its
         // map is the composition of the segment maps (lane = segment)
         const bool ok = all_one && __ballot_sync(0xffffffffu, stot[lane].i0 < 0) == 0;
-        const ParInc tot = par_scan(stot[lane], lane);
+        const ParInc sl = stot[lane];
+        const ParInc tot = par_scan_ns(sl.i0 < 0 ? ParInc{0, 0} : sl, lane);
         if (lane == 31) R[blockIdx.x] = ok ? par_clamp(tot) : make_longlong2(-1, -1);
         if (blockIdx.x == 0) {
             // chunk 0 starts the fold at 0, where the sum climbs binade after
