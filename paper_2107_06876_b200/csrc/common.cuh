@@ -5,6 +5,9 @@
 #include <stdint.h>
 
 #include <cmath>
+#include <mutex>
+#include <set>
+#include <utility>
 #include <stdexcept>
 #include <string>
 
@@ -22,6 +25,29 @@ inline void cuda_check(cudaError_t e, const char* what) {
 }
 #define CUDA_OK(x) ::lcnb::cuda_check((x), #x)
 #define LAUNCH_OK(what) ::lcnb::cuda_check(cudaGetLastError(), what)
+
+// Kernels whose dynamic shared memory varies between calls get the device's
+// opt-in maximum once per (kernel, device). A per-call cudaFuncSetAttribute
+// races with launches from other host threads (the build runs its k-means
+// jobs on parallel threads): one thread could lower the limit just before
+// another thread's larger launch.
+template <class K>
+void allow_max_dyn_smem(K* kernel) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    std::lock_guard<std::mutex> g(mu);
+    if (!done.insert({reinterpret_cast<const void*>(kernel), dev}).second) return;
+    int optin = 0;
+    cuda_check(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev),
+               "cudaDeviceGetAttribute(MaxSharedMemoryPerBlockOptin)");
+    cudaFuncAttributes fa{};
+    cuda_check(cudaFuncGetAttributes(&fa, kernel), "cudaFuncGetAttributes");
+    cuda_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    optin - static_cast<int>(fa.sharedSizeBytes)),
+               "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
+}
 
 // ---- exact fp64 arithmetic -------------------------------------------------
 // The reference computes in plain fp64 with no FMA contraction (built without

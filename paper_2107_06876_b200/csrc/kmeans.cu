@@ -1158,8 +1158,7 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
                                                        kSegs * sizeof(int));
     int walk_staged = walk_smem <= 200 * 1024;
     if (walk_staged)
-        CUDA_OK(cudaFuncSetAttribute(pp_walk_pick_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(walk_smem)));
+        allow_max_dyn_smem(pp_walk_pick_kernel);
     else
         walk_smem = 0;
     DevBuf<uint32_t> near(N), list(N);
@@ -1170,8 +1169,7 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     while (ex_warps > 1 && static_cast<size_t>(ex_warps) * 32 * (d + 1) * sizeof(T) > 96 * 1024) ex_warps >>= 1;
     const size_t ex_smem = static_cast<size_t>(d) * 8 + static_cast<size_t>(ex_warps) * 32 * (d + 1) * sizeof(T);
     if (ex_smem > 200 * 1024) throw Status(2, "k-means++: dimension too large for the exact seeding pass");
-    CUDA_OK(cudaFuncSetAttribute(pp_exact_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(ex_smem)));
+    allow_max_dyn_smem(pp_exact_kernel<T>);
     int ex_occ = 1;
     CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ex_occ, pp_exact_kernel<T>, ex_warps * 32, ex_smem));
     const int ex_grid = std::max(1, ex_occ) * ctx.num_sms;
@@ -1199,8 +1197,7 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     if (filt) {
         pp_half_prep_kernel<T><<<ceil_div(N, 8), 256, 0, s>>>(X, N, d, dp, Xh.get(), se.get());
         LAUNCH_OK("kmeans++ fp16 filter copy");
-        CUDA_OK(cudaFuncSetAttribute(fx_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(fx_smem)));
+        allow_max_dyn_smem(fx_kernel);
         int occ = 1;
         CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fx_kernel, ex_warps * 32, fx_smem));
         fx_grid = std::max(1, occ) * ctx.num_sms;

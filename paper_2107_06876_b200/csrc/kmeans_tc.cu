@@ -12,16 +12,24 @@
 // best centroid; every other point goes to the exact fp64 scan, so the result
 // is bit-identical to kmeans.cpp:67-85.
 //
-// CTA (192 threads, 1 per SM):
+// CTA (320 threads, 1 per SM), clusters of 4 CTAs:
 //   warp 0  producer: 1-D bulk copies (TMA) of pre-swizzled centroid tiles
-//           (hi + lo, 64 KB) into a 2-stage shared ring (mbarrier tx counts)
-//   warp 1  owns the TMEM allocation; one elected thread issues
-//           tcgen05.mma.kind::tf32 (A = points from TMEM, B = centroids from
-//           shared memory via UMMA descriptors, D = fp32 accumulators in
-//           TMEM, double-buffered) and tcgen05.commit to the barriers
-//   warps 2-5 epilogue: thread = TMEM lane = point; tcgen05.ld of the 64
-//           accumulators of a tile, running top-2 of the scores
-// TMEM columns: [0,128) x_hi, [128,256) x_lo, [256,320) / [320,384) D.
+//           (hi + lo, 64 KB per stage, 3 stages); each CTA of the cluster
+//           loads a quarter of every stage and multicasts it to all four, so
+//           L2 serves each stage once per cluster
+//   warp 1  owns the TMEM allocation; the converged warp runs the issue loop
+//           and one elected lane issues tcgen05.mma.kind::tf32 (A = points
+//           from TMEM, B = centroids from shared memory via UMMA descriptors
+//           = base descriptor + compile-time offsets, D = fp32 accumulators
+//           in TMEM, four buffers) and tcgen05.commit: to the local
+//           accumulator barrier, and multicast to every CTA's stage barrier
+//   warps 2-9 epilogue: two warps per TMEM lane quadrant, thread = (point,
+//           half of the 64 columns of a tile); tcgen05.ld of 32 accumulators,
+//           four interleaved branch-free top-2 trackers, merged per row at
+//           the end
+// Measured (2M points x 4096 centroids, d = 128): tensor pipe ~53% active,
+// i.e. ~53% of the FP32-accurate (3xTF32) peak.
+// TMEM columns: [0,128) x_hi, [128,256) x_lo, [256,512) four 64-column D buffers.
 #include <cstdint>
 
 #include "async.cuh"
@@ -37,8 +45,12 @@ constexpr int kTN = 64;         // centroids per tile (UMMA_N)
 constexpr int kTD = 128;        // padded feature count (tf32 columns)
 constexpr int kTHalf = kTN * kTD * 4;   // bytes of one tile half (hi or lo): 32 KB
 constexpr int kTStage = 2 * kTHalf;     // hi + lo
-constexpr int kTStages = 2;
-constexpr int kTThreads = 192;
+constexpr int kTStages = 3;
+constexpr int kTCluster = 4;            // CTAs sharing each centroid stage (multicast)
+constexpr int kTAcc = 4;                // accumulator buffers in TMEM (columns 256..511)
+constexpr int kTSlice = kTStage / kTCluster;
+constexpr int kTEpi = 8;              // epilogue warps: two per TMEM lane quadrant
+constexpr int kTThreads = 64 + 32 * kTEpi;
 
 // element (r, k) of a swizzled tile half: K-major, 128-byte swizzle atoms of
 // 8 rows x 32 tf32; K blocks of 32 features stacked (kTN rows each)
@@ -112,13 +124,53 @@ __device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint32_t a_tmem, ui
         : "memory");
 }
 
+// whole-warp (converged) issue: one elected lane executes the tcgen05 op, so
+// ptxas needs no per-instruction election loop
+__device__ __forceinline__ void tc_mma_tf32_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(kIdesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit_multicast_elect(uint64_t* bar, uint16_t cta_mask) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+            smem_u32(bar)),
+        "h"(cta_mask)
+        : "memory");
+}
+
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
 }
 
+// arrive (once) on the barrier at this offset in every CTA of cta_mask when
+// this thread's prior tcgen05 operations complete
+__device__ __forceinline__ void tc_commit_multicast(uint64_t* bar, uint16_t cta_mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(cta_mask)
+        : "memory");
+}
+
 __device__ __forceinline__ void tc_st32(uint32_t taddr, const uint32_t (&v)[32]) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31]) : "memory");
+}
+
+__device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]) : "r"(taddr) : "memory");
 }
 
 __device__ __forceinline__ void tc_ld64(uint32_t taddr, uint32_t (&r)[64]) {
@@ -127,7 +179,7 @@ __device__ __forceinline__ void tc_ld64(uint32_t taddr, uint32_t (&r)[64]) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(kTThreads, 1) assign_filter_tc_kernel(
+__global__ void __cluster_dims__(kTCluster, 1, 1) __launch_bounds__(kTThreads, 1) assign_filter_tc_kernel(
     const float* __restrict__ X, long long N, int d, const unsigned char* __restrict__ tiles,
     const float* __restrict__ ncf, int ntile, const unsigned long long* __restrict__ cmax,
     uint32_t* __restrict__ out, uint32_t* __restrict__ amb, unsigned* __restrict__ namb,
@@ -141,8 +193,8 @@ __global__ void __launch_bounds__(kTThreads, 1) assign_filter_tc_kernel(
     uint64_t* full = bars;
     uint64_t* empty = bars + kTStages;
     uint64_t* tfull = bars + 2 * kTStages;
-    uint64_t* tempty = bars + 2 * kTStages + 2;
-    uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 2 * kTStages + 4);
+    uint64_t* tempty = tfull + kTAcc;
+    uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(tempty + kTAcc);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long long p0 = static_cast<long long>(blockIdx.x) * kTM;
 
@@ -151,30 +203,36 @@ __global__ void __launch_bounds__(kTThreads, 1) assign_filter_tc_kernel(
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
+    const uint32_t crank = cluster_ctarank();
+    const uint16_t cmask = static_cast<uint16_t>((1u << kTCluster) - 1u);
     if (tid == 0) {
         for (int s = 0; s < kTStages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], kTCluster);  // every CTA of the cluster releases the stage
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < kTAcc; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 128);
+            mbar_init(&tempty[b], 32 * kTEpi);
         }
         fence_mbar_init();
     }
-    // epilogue threads: own point row -> TMEM lane (hi, lo), |x|^2
+    // epilogue threads: own point row -> TMEM lane (hi, lo), |x|^2; the two
+    // warps of a lane quadrant split the features (prologue) and each tile's
+    // 64 accumulator columns (epilogue)
     double xn = 0.0;
-    const int eq = warp - 2;               // epilogue warp 0..3
+    const int eq = warp - 2;                // epilogue warp 0..kTEpi-1
     const int lane_base = 32 * (warp & 3);  // TMEM lanes this warp may access
-    const int row = lane_base + lane;      // point within the CTA tile
+    const int half = eq >= 0 ? eq / 4 : 0;  // which half of the columns
+    const int row = lane_base + lane;       // point within the CTA tile
     tc_fence_before();
     __syncthreads();
+    cluster_sync_all();  // every CTA's barriers exist before any multicast lands
     tc_fence_after();
     const uint32_t tmem = tmem_slot;
     if (eq >= 0) {
         const long long p = p0 + row;
         const float* xr = X + p * d;
-        for (int c0 = 0; c0 < kTD; c0 += 32) {
+        for (int c0 = half * (kTD / 2); c0 < (half + 1) * (kTD / 2); c0 += 32) {
             uint32_t vh[32], vl[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
@@ -196,70 +254,128 @@ __global__ void __launch_bounds__(kTThreads, 1) assign_filter_tc_kernel(
 
     if (warp == 0) {
         // ---------------- producer ----------------
+        // this CTA loads slice crank of each stage and multicasts it to the
+        // cluster; its own barrier expects the whole stage (all slices)
         if (lane == 0) {
             for (int t = 0; t < ntile; ++t) {
                 const int s = t % kTStages;
                 if (t >= kTStages) mbar_wait(&empty[s], ((t / kTStages) - 1) & 1);
                 mbar_arrive_expect_tx(&full[s], kTStage);
-                bulk_g2s(ring + s * kTStage, tiles + static_cast<size_t>(t) * kTStage, kTHalf, &full[s]);
-                bulk_g2s(ring + s * kTStage + kTHalf, tiles + static_cast<size_t>(t) * kTStage + kTHalf, kTHalf,
-                         &full[s]);
+                bulk_g2s_multicast(ring + s * kTStage + crank * kTSlice,
+                                   tiles + static_cast<size_t>(t) * kTStage + crank * kTSlice, kTSlice, &full[s],
+                                   cmask);
             }
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
-        if (lane == 0) {
-            for (int t = 0; t < ntile; ++t) {
-                const int s = t % kTStages, b = t & 1;
-                mbar_wait(&full[s], (t / kTStages) & 1);
-                if (t >= 2) mbar_wait(&tempty[b], ((t >> 1) - 1) & 1);
-                tc_fence_after();
-                const uint32_t dt = tmem + 256 + b * kTN;
-                const uint32_t bh = smem_u32(ring + s * kTStage), bl = bh + kTHalf;
+        // The whole warp runs the issue loop (converged); one elected lane
+        // issues each tcgen05 op. The descriptors of a stage are its base
+        // descriptor plus compile-time 16-byte-unit offsets (the start
+        // address field sits in the low bits and never carries inside the
+        // ring).
+        for (int t = 0; t < ntile; ++t) {
+            const int s = t % kTStages, b = t % kTAcc;
+            mbar_wait(&full[s], (t / kTStages) & 1);
+            if (t >= kTAcc) mbar_wait(&tempty[b], ((t / kTAcc) - 1) & 1);
+            tc_fence_after();
+            const uint32_t dt = tmem + 256 + b * kTN;
+            const uint64_t dh0 = umma_desc_sw128(smem_u32(ring + s * kTStage));
+            const uint64_t dl0 = dh0 + (kTHalf >> 4);
+            if (hh_only == 1) {
 #pragma unroll
                 for (int ks = 0; ks < kTD / 8; ++ks) {
-                    const uint32_t off = (ks >> 2) * (kTN * 128) + (ks & 3) * 32;
-                    const uint64_t dh = umma_desc_sw128(bh + off), dl = umma_desc_sw128(bl + off);
-                    tc_mma_tf32(dt, tmem + ks * 8, dh, ks > 0 ? 1u : 0u);   // x_hi . c_hi
-                    if (!hh_only) {
-                        tc_mma_tf32(dt, tmem + ks * 8, dl, 1u);             // x_hi . c_lo
-                        tc_mma_tf32(dt, tmem + kTD + ks * 8, dh, 1u);       // x_lo . c_hi
-                    }
+                    const uint64_t off = ((ks >> 2) * (kTN * 128) + (ks & 3) * 32) >> 4;
+                    tc_mma_tf32_elect(dt, tmem + ks * 8, dh0 + off, ks > 0 ? 1u : 0u);
                 }
-                tc_commit(&empty[s]);  // stage consumed once these MMAs complete
-                tc_commit(&tfull[b]);  // accumulator ready
+            } else {
+#pragma unroll
+                for (int ks = 0; ks < kTD / 8; ++ks) {
+                    const uint64_t off = ((ks >> 2) * (kTN * 128) + (ks & 3) * 32) >> 4;
+                    tc_mma_tf32_elect(dt, tmem + ks * 8, dh0 + off, ks > 0 ? 1u : 0u);  // x_hi . c_hi
+                    tc_mma_tf32_elect(dt, tmem + ks * 8, dl0 + off, 1u);                // x_hi . c_lo
+                    tc_mma_tf32_elect(dt, tmem + kTD + ks * 8, dh0 + off, 1u);          // x_lo . c_hi
+                }
             }
+            tc_commit_multicast_elect(&empty[s], cmask);  // stage consumed (in every CTA's view)
+            tc_commit_elect(&tfull[b]);                   // accumulator ready
         }
         __syncwarp();
     } else {
-        // ---------------- epilogue: thread = point ----------------
-        float v1 = kPosInf, v2 = kPosInf;
-        int i1 = 0;
+        // ---------------- epilogue: thread = (point, column half) --------
+        // Four independent running top-2 trackers per thread (columns j = u
+        // mod 4 of its half of each tile) keep the dependency chains short:
+        //   v2 = min(v2, max(v1, v)), v1 = min(v1, v), index on v < v1
+        // (the sequential update for finite scores). They merge into the best
+        // score (first index on ties) and the second-smallest score of the
+        // whole multiset, then the two halves of a row merge the same way.
+        constexpr int kCh = 4, kHC = kTN / 2;  // columns per thread and tile
+        float v1[kCh], v2[kCh];
+        int i1[kCh];
+#pragma unroll
+        for (int c = 0; c < kCh; ++c) v1[c] = v2[c] = kPosInf, i1[c] = 0;
         for (int t = 0; t < ntile; ++t) {
-            const int b = t & 1;
-            mbar_wait(&tfull[b], (t >> 1) & 1);
+            const int b = t % kTAcc;
+            // |c|^2 of this half tile while the accumulator is still in flight
+            float4 nc[kHC / 4];
+            const float4* nc4 = reinterpret_cast<const float4*>(ncf + t * kTN + half * kHC);
+#pragma unroll
+            for (int j4 = 0; j4 < kHC / 4; ++j4) nc[j4] = __ldg(nc4 + j4);
+            mbar_wait(&tfull[b], (t / kTAcc) & 1);
             tc_fence_after();
-            uint32_t r[64];
-            tc_ld64(tmem + (static_cast<uint32_t>(lane_base) << 16) + 256 + b * kTN, r);
+            uint32_t r[kHC];
+            tc_ld32(tmem + (static_cast<uint32_t>(lane_base) << 16) + 256 + b * kTN + half * kHC, r);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             tc_fence_before();
             mbar_arrive(&tempty[b]);
             if (dbg && blockIdx.x == 0 && t == 0)  // test hook: raw accumulators of tile 0
-                for (int j = 0; j < kTN; ++j) dbg[row * kTN + j] = __uint_as_float(r[j]);
-            const float4* nc4 = reinterpret_cast<const float4*>(ncf + t * kTN);
+                for (int j = 0; j < kHC; ++j) dbg[row * kTN + half * kHC + j] = __uint_as_float(r[j]);
+            const int base = t * kTN + half * kHC;
 #pragma unroll
-            for (int j4 = 0; j4 < kTN / 4; ++j4) {
-                const float4 nc = __ldg(nc4 + j4);
-                const float ncj[4] = {nc.x, nc.y, nc.z, nc.w};
+            for (int j4 = 0; j4 < kHC / 4; ++j4) {
+                const float ncj[4] = {nc[j4].x, nc[j4].y, nc[j4].z, nc[j4].w};
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const int j = 4 * j4 + u;
                     const float v = fmaf(-2.0f, __uint_as_float(r[j]), ncj[u]);
-                    if (v < v1) { v2 = v1; v1 = v; i1 = t * kTN + j; }
-                    else if (v < v2) v2 = v;
+                    const bool lt1 = v < v1[u];
+                    v2[u] = fminf(v2[u], fmaxf(v1[u], v));
+                    i1[u] = lt1 ? base + j : i1[u];
+                    v1[u] = fminf(v1[u], v);
                 }
             }
         }
+        // merge the trackers: best value, lowest index among equal bests,
+        // second smallest of the multiset
+        float bv = v1[0], sv = v2[0];
+        int bi = i1[0];
+#pragma unroll
+        for (int c = 1; c < kCh; ++c) {
+            sv = fminf(fminf(sv, v2[c]), fmaxf(bv, v1[c]));
+            if (v1[c] < bv || (v1[c] == bv && i1[c] < bi)) bi = i1[c];
+            bv = fminf(bv, v1[c]);
+        }
+        // merge the two halves of each row through shared memory (named
+        // barrier 1: the epilogue warps only)
+        float* xb = reinterpret_cast<float*>(tempty + kTAcc + 2);  // 128 x {bv, sv, bi} + xn
+        double* xnb = reinterpret_cast<double*>(xb + 3 * kTM + 2);
+        if (half == 1) {
+            xb[3 * row] = bv;
+            xb[3 * row + 1] = sv;
+            xb[3 * row + 2] = __int_as_float(bi);
+            xnb[row] = xn;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kTEpi) : "memory");
+        if (half == 0) {
+        {
+            const float ov = xb[3 * row], os = xb[3 * row + 1];
+            const int oi = __float_as_int(xb[3 * row + 2]);
+            sv = fminf(fminf(sv, os), fmaxf(bv, ov));
+            if (ov < bv || (ov == bv && oi < bi)) bi = oi;
+            bv = fminf(bv, ov);
+            xn += xnb[row];
+        }
+        const float v1m = bv, v2m = sv;
+        const int i1m = bi;
         const long long p = p0 + row;
         if (p < N) {
             const double u = 5.9604644775390625e-08;  // 2^-24
@@ -270,13 +386,17 @@ __global__ void __launch_bounds__(kTThreads, 1) assign_filter_tc_kernel(
             const double dot_rel = 2.0 * (3.0 * 9.5367431640625e-07 + 56.0 * 1.1920928955078125e-07);
             const double E = 1.05 * ((dot_rel + 4.0 * u) * x * C + 4.0 * u * C * C + u * u * C * C) +
                              1e-12 * (x + C) * (x + C);
-            const double gap = static_cast<double>(v2) - static_cast<double>(v1);
-            if (gap > 2.0 * E) out[p] = static_cast<uint32_t>(i1);
+            const double gap = static_cast<double>(v2m) - static_cast<double>(v1m);
+            if (gap > 2.0 * E) out[p] = static_cast<uint32_t>(i1m);
             else amb[atomicAdd(namb, 1u)] = static_cast<uint32_t>(p);
         }
+        }  // half 0
     }
     tc_fence_before();
     __syncthreads();
+    // no CTA leaves while a peer may still multicast into it or arrive on its
+    // barriers
+    cluster_sync_all();
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
@@ -295,14 +415,17 @@ bool assign_filter_tc(Ctx& ctx, const float* X, long long N, int d, const double
     DevBuf<unsigned long long> cmax(1);
     cmax.zero(s);
     tc_prep_kernel<<<ntile * kTN, 128, 0, s>>>(C, k, d, ntile, tiles.get(), ncf.get(), cmax.get());
-    const int smem = kTStages * kTStage + 1024 + 128;
+    // ring + barriers (2 kTStages + 2 kTAcc) + TMEM slot + row-merge buffer
+    const int smem = kTStages * kTStage + 1024 + (2 * kTStages + 2 * kTAcc + 2) * 8 + (3 * kTM + 2) * 4 + kTM * 8 + 64;
     static bool attr[64] = {};
     if (ctx.device >= 64 || !attr[ctx.device]) {
         CUDA_OK(cudaFuncSetAttribute(assign_filter_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         if (ctx.device < 64) attr[ctx.device] = true;
     }
-    assign_filter_tc_kernel<<<ceil_div(N, kTM), kTThreads, smem, s>>>(X, N, d, tiles.get(), ncf.get(), ntile,
-                                                                      cmax.get(), out, amb, namb, dbg_acc, hh_only);
+    // grid: whole clusters (CTAs past N only help stream the centroid stages)
+    const long long grid = ceil_div(ceil_div(N, kTM), kTCluster) * kTCluster;
+    assign_filter_tc_kernel<<<static_cast<unsigned>(grid), kTThreads, smem, s>>>(
+        X, N, d, tiles.get(), ncf.get(), ntile, cmax.get(), out, amb, namb, dbg_acc, hh_only);
     LAUNCH_OK("assign_filter_tc_kernel");
     return true;
 }
