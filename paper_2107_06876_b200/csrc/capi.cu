@@ -710,12 +710,34 @@ int lcn_sinkhorn(lcn_op* op, const double* p, const double* q, const lcn_sinkhor
         res->op = op;
         res->device = op->o.ctx->device;
         if (o.kind == LCN_OP_SPARSE && so.check_support) {
-            // sinkhorn.cpp:122-128: warn when the pattern has no support.
-            build_csr(o);
-            std::vector<uint32_t> rp(o.n + 1), col(std::max<unsigned long long>(o.nnz, 1));
-            export_csr(o, 0, rp.data(), col.data(), nullptr);
-            size_t small = std::min(o.n, o.m);
-            if (o.nnz == 0 || max_bipartite_matching(o.n, o.m, rp.data(), col.data()) < small) {
+            // sinkhorn.cpp:122-128: warn when the pattern has no support
+            // (maximum bipartite matching < min(n, m), sparse_kernel.cpp:189-196).
+            // Band 1's pattern is a disjoint union of complete bipartite
+            // blocks, whose maximum matching is sum_b min(n_b, m_b): exact for
+            // one band, a lower bound of the union otherwise. Only a union
+            // whose band-1 bound falls short needs the general matching.
+            const size_t small = std::min(o.n, o.m);
+            bool support = o.nnz > 0;
+            if (support && !o.bands.empty()) {
+                const Band& B0 = o.bands[0];
+                unsigned long long mb = 0;
+                for (size_t b = 0; b + 1 < B0.h_src_start.size(); ++b)
+                    mb += std::min(B0.h_src_start[b + 1] - B0.h_src_start[b], B0.h_tgt_start[b + 1] - B0.h_tgt_start[b]);
+                if (mb >= small) support = true;
+                else if (o.bands.size() == 1) support = false;
+                else support = [&] {
+                    build_csr(o);
+                    std::vector<uint32_t> rp(o.n + 1), col(std::max<unsigned long long>(o.nnz, 1));
+                    export_csr(o, 0, rp.data(), col.data(), nullptr);
+                    return max_bipartite_matching(o.n, o.m, rp.data(), col.data()) >= small;
+                }();
+            } else if (support) {
+                build_csr(o);
+                std::vector<uint32_t> rp(o.n + 1), col(std::max<unsigned long long>(o.nnz, 1));
+                export_csr(o, 0, rp.data(), col.data(), nullptr);
+                support = max_bipartite_matching(o.n, o.m, rp.data(), col.data()) >= small;
+            }
+            if (!support) {
                 res->r.warnings.push_back("sparse kernel pattern has no support; Sinkhorn may not converge");
                 std::fprintf(stderr, "lcn: warning: %s\n", res->r.warnings.back().c_str());
             }

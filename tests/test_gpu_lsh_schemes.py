@@ -111,3 +111,39 @@ def test_sparse_operator_on_scheme(ctx, ref, scheme, bands, rows, buckets, branc
     res = lcn.sinkhorn(op, pm, qm, lcn.SinkhornOptions(tol=0.0, max_iters=40, check_support=False))
     rres = rop.sinkhorn(pm, qm, tol=0.0, max_iters=40, check_support=False)
     assert rel(res.distance, rres.distance) <= 1e-4
+
+
+@pytest.mark.parametrize("case", ["one_band_full", "one_band_short", "two_band_union_full", "two_band_short"])
+def test_support_check_block_matching(ctx, ref, case):
+    """sinkhorn.cpp:122-128 support warning: band-1 block matching sum_b
+    min(n_b, m_b) decides one band exactly; a short multi-band bound falls
+    back to the general matching. Warnings must equal the reference's."""
+    n = m = 6
+    r = np.random.default_rng(3)
+    p, q = r.standard_normal((n, 2)), r.standard_normal((m, 2))
+    if case == "one_band_full":
+        ids_p, ids_q = np.array([[0, 0, 1, 1, 2, 2]]), np.array([[2, 1, 0, 0, 1, 2]])
+    elif case == "one_band_short":
+        ids_p, ids_q = np.array([[0, 0, 0, 1, 1, 2]]), np.array([[0, 1, 1, 1, 2, 2]])
+    elif case == "two_band_union_full":
+        ids_p = np.array([[0, 0, 0, 1, 1, 2], [5, 6, 7, 8, 9, 10]])
+        ids_q = np.array([[0, 1, 1, 1, 2, 2], [11, 12, 7, 13, 14, 15]])
+        ids_q[1] = [5, 12, 7, 8, 9, 10]
+    else:
+        ids_p = np.array([[0, 0, 0, 1, 1, 2], [3, 3, 3, 4, 4, 4]])
+        ids_q = np.array([[0, 1, 1, 1, 2, 2], [5, 5, 5, 4, 4, 4]])
+    ids_p, ids_q = ids_p.astype(np.uint64), ids_q.astype(np.uint64)
+    op = lcn.KernelOperator.sparse_buckets(ctx, p, q, lcn.EUCLIDEAN, 1.0, ids_p, ids_q)
+    pairs = ref.pairs_from_buckets(ids_p, ids_q, 16)
+    rop = ref.op_sparse(p, q, lcn.EUCLIDEAN, 1.0, pairs)
+    pm = qm = np.full(n, 1.0 / n)
+    try:
+        res = lcn.sinkhorn(op, pm, qm, lcn.SinkhornOptions(tol=0.0, max_iters=5))
+        nw = len(res.warnings)
+    except lcn.StabilizationError:
+        nw = None
+    try:
+        nw_ref = rop.sinkhorn(pm, qm, tol=0.0, max_iters=5).n_warnings
+    except Exception:
+        nw_ref = None
+    assert nw == nw_ref
