@@ -215,6 +215,22 @@ int lcn_multihead(lcn_ctx* ctx, const double* p, size_t n, const double* q, size
                   double lambda, int heads, const double* pmarg, const double* qmarg,
                   const lcn_sinkhorn_options* opts, double* lambdas_out, double* dist_out, int* iters_out,
                   int* converged_out, int* status_out);
+/* configs[4]: nprob independent small LCN problems in ragged launches (one
+ * CTA per problem). X holds the problems back to back, problem k as n[k]
+ * source rows then m[k] target rows (d columns, row-major). Per problem, as
+ * the reference pipeline: lsh_neighbor_pairs with k-means LSH (1 band,
+ * `buckets`, kmeans_iters, lsh_seeds[k]) -> build_sparse -> select_landmarks
+ * (KMeans, l, landmark_seeds[k]) -> build_factors -> build_correction ->
+ * KernelOperator::lcn -> sinkhorn with uniform marginals, tol 0, `iters`
+ * iterations. Outputs per problem: the distance, the status (0, or the
+ * lcn_status of the reference's first error for that problem; its distance
+ * is NaN) and the iterations run. Limits on this path: d <= 32,
+ * n + m <= 1024, buckets and l in [2 or 1, 16], cost euclidean or squared
+ * euclidean. */
+int lcn_batched_lcn(lcn_ctx* ctx, const double* X, size_t rows, size_t d, int nprob, const int* n, const int* m,
+                    int cost, double lambda, int buckets, int kmeans_iters, const uint64_t* lsh_seeds, size_t l,
+                    const uint64_t* landmark_seeds, int iters, double* distance_out, int* status_out,
+                    int* iters_out);
 int lcn_op_destroy(lcn_op* op);
 int lcn_op_get_info(const lcn_op* op, lcn_op_info_t* info);
 /* CSR export in the reference's order (rows ascending, columns ascending,

@@ -99,6 +99,15 @@ class CheckerLib(_Lib):
             _ptr(p), p.shape[0], _ptr(q), q.shape[0], p.shape[1], bands, buckets, iters, seed, _ptr(ids)))
         return ids
 
+    def lcn_problem(self, p, q, kind, lam, buckets, kmeans_iters, lsh_seed, l, lm_seed, iters):
+        """configs[4] unit: one small LCN solve end to end; returns the distance."""
+        p, q = _f64(p), _f64(q)
+        out = C.c_double()
+        self.check(self.fn("lcn_problem", _P, _SZ, _P, _SZ, _SZ, _I, _D, _I, _I, _U64, _SZ, _U64, _I,
+                           C.POINTER(C.c_double))(_ptr(p), p.shape[0], _ptr(q), q.shape[0], p.shape[1], kind, lam,
+                                                  buckets, kmeans_iters, lsh_seed, l, lm_seed, iters, C.byref(out)))
+        return out.value
+
     def lsh_buckets_cfg(self, p, q, scheme, bands=1, rows=1, buckets=2, iters=10, branching=2, seed=0):
         """Per-band composite ids (lsh.cpp:245-283) for any LshScheme value, p first."""
         p, q = _f64(p), _f64(q)

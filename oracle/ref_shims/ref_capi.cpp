@@ -445,6 +445,33 @@ int ref_sinkhorn(void* h, const double* pm, std::size_t n, const double* qm, std
     })
 }
 
+// One small LCN problem end to end (the configs[4] unit):
+// lsh_neighbor_pairs (k-means, 1 band) -> build_sparse -> select_landmarks
+// (KMeans) -> build_factors -> build_correction -> KernelOperator::lcn ->
+// sinkhorn(tol 0, iters). Returns the distance; errors as status codes.
+int ref_lcn_problem(const double* p, std::size_t n, const double* q, std::size_t m, std::size_t d, int kind,
+                    double lambda, int buckets, int kmeans_iters, std::uint64_t lsh_seed, std::size_t l,
+                    std::uint64_t lm_seed, int iters, double* distance) {
+    GUARD({
+        PointSet P = make_points(p, n, d, "p"), Q = make_points(q, m, d, "q");
+        NeighborPairs pairs = lsh_neighbor_pairs(P, Q, kmeans_cfg(1, buckets, kmeans_iters, lsh_seed));
+        SparseKernel sk = build_sparse(P, Q, pairs, static_cast<CostKind>(kind), lambda);
+        LandmarkSet lm = select_landmarks(P, Q, l, LandmarkMethod::KMeans, lm_seed);
+        NystromFactors f = build_factors(P, Q, lm, static_cast<CostKind>(kind), lambda);
+        LcnCorrection c = build_correction(sk, f);
+        KernelOperator op = KernelOperator::lcn(f, c);
+        Marginals marg;
+        marg.p.assign(n, 1.0 / static_cast<double>(n));
+        marg.q.assign(m, 1.0 / static_cast<double>(m));
+        SinkhornOptions o;
+        o.tol = 0.0;
+        o.max_iters = iters;
+        o.check_support = false;
+        o.want_plan = false;
+        *distance = sinkhorn(op, marg, o).distance;
+    })
+}
+
 void ref_result_free(void* h) { delete static_cast<SinkhornResult*>(h); }
 
 // 0 distance, 1 iters, 2 converged, 3 marginal_err_final, 4 #warnings, 5 #err trace

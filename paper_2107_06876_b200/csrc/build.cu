@@ -913,6 +913,39 @@ struct HostLdlt {
     }
 };
 
+}  // namespace
+
+// One jitter level of build_factors' factorisation (nystrom.cpp:96-108) for a
+// small l x l landmark matrix A (fp64, row-major): A_j = A + rel * trace(A)/l
+// on the diagonal in long double, its diagonal-pivoted LDL^T and inverse.
+// false when the factorisation fails or the inverse is not finite (the
+// reference moves to the next level then); the caller tests the residual.
+bool nystrom_inverse_host(const double* A, int l, double rel, double* ainv, double* aj_out) {
+    const size_t L = static_cast<size_t>(l);
+    std::vector<LD> a(L * L);
+    LD trace = 0.0L;
+    for (size_t i = 0; i < L * L; ++i) a[i] = static_cast<LD>(A[i]);
+    for (size_t i = 0; i < L; ++i) trace += a[i * L + i];
+    const LD jitter_unit = trace / static_cast<LD>(L);
+    for (size_t i = 0; i < L; ++i) a[i * L + i] += rel * jitter_unit;
+    HostLdlt fac(a, L);
+    if (!fac.ok) return false;
+    std::vector<LD> e(L);
+    for (size_t c = 0; c < L; ++c) {
+        std::fill(e.begin(), e.end(), 0.0L);
+        e[c] = 1.0L;
+        fac.solve(e.data());
+        for (size_t r = 0; r < L; ++r) {
+            if (!std::isfinite(e[r])) return false;
+            ainv[r * L + c] = static_cast<double>(e[r]);
+        }
+    }
+    for (size_t i = 0; i < L * L; ++i) aj_out[i] = static_cast<double>(a[i]);
+    return true;
+}
+
+namespace {
+
 __global__ void maxabs_kernel(const double* __restrict__ x, long long n, unsigned long long* __restrict__ out) {
     double m = 0.0;
     for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += 256LL * gridDim.x) m = fmax(m, fabs(x[i]));

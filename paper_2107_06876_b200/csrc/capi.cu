@@ -623,6 +623,22 @@ int lcn_op_create_device(lcn_ctx* ctx, const float* d_p, size_t n, const float* 
     });
 }
 
+int lcn_batched_lcn(lcn_ctx* ctx, const double* X, size_t rows, size_t d, int nprob, const int* n, const int* m,
+                    int cost, double lambda, int buckets, int kmeans_iters, const uint64_t* lsh_seeds, size_t l,
+                    const uint64_t* landmark_seeds, int iters, double* distance_out, int* status_out,
+                    int* iters_out) {
+    return guard(ctx, [&] {
+        if (nprob < 0 || (nprob > 0 && (!X || !n || !m || !lsh_seeds || !landmark_seeds || !distance_out || !status_out)))
+            throw Status(2, "batched LCN: null argument");
+        if (iters < 1) throw Status(2, "sinkhorn: max_iters must be >= 1");
+        if (nprob == 0) return;
+        for (size_t i = 0; i < rows * d; ++i)
+            if (!std::isfinite(X[i])) throw Status(2, "point set has a non-finite coordinate");
+        batched_lcn(ctx->c, X, rows, static_cast<int>(d), nprob, n, m, cost, lambda, buckets, kmeans_iters, lsh_seeds,
+                    static_cast<int>(l), landmark_seeds, iters, distance_out, status_out, iters_out);
+    });
+}
+
 int lcn_op_destroy(lcn_op* op) {
     if (!op) return LCN_OK;
     cudaSetDevice(op->o.ctx->device);

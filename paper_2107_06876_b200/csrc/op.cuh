@@ -107,6 +107,11 @@ void lsh_bucket_ids(Ctx& ctx, const double* d_union, const float* d_union32, siz
                     const std::function<void(Ctx&)>& extra = {});
 void cross_polytope_buckets_device(Ctx& ctx, const double* X, long long N, int d, const double* h_proj, int half,
                                    uint32_t* out);
+bool nystrom_inverse_host(const double* A, int l, double rel, double* ainv, double* aj_out);
+// batched.cu: configs[4], many small LCN problems in ragged launches
+void batched_lcn(Ctx& ctx, const double* h_X, size_t rows, int d, int nprob, const int* h_n, const int* h_m,
+                 int kind, double lambda, int buckets, int kmeans_iters, const uint64_t* lsh_seeds, int l,
+                 const uint64_t* lm_seeds, int iters, double* dist_out, int* status_out, int* iters_out);
 void select_landmarks_device(Op& op, Ctx& ctx, int method, uint64_t seed);
 void build_sparse_values(Op& op);
 void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed);

@@ -106,6 +106,7 @@ def library() -> C.CDLL:
             "lcn_lsh_kmeans_buckets": ([P, P, SZ, P, SZ, SZ, C.POINTER(_LshConfig), P], I),
             "lcn_lsh_buckets": ([P, P, SZ, P, SZ, SZ, C.POINTER(_LshConfig), P], I),
             "lcn_cross_polytope_buckets": ([P, P, SZ, SZ, P, SZ, P], I),
+            "lcn_batched_lcn": ([P, P, SZ, SZ, I, P, P, I, D, I, I, P, SZ, P, I, P, P, P], I),
             "lcn_op_sparse_lsh": ([P, P, SZ, P, SZ, SZ, I, D, C.POINTER(_LshConfig), PP], I),
             "lcn_op_sparse_buckets": ([P, P, SZ, P, SZ, SZ, I, D, P, P, I, U64, PP], I),
             "lcn_op_lcn_lsh": ([P, P, SZ, P, SZ, SZ, I, D, C.POINTER(_LshConfig), SZ, I, U64, PP], I),
@@ -265,6 +266,25 @@ def lloyd(ctx: Context, points, k: int, iters: int, seed: int):
     asg = np.zeros(n, np.uint32)
     ctx.check(ctx.lib.lcn_lloyd(ctx.h, _p(pts), n, d, k, iters, seed, _p(ctr), _p(asg)))
     return ctr, asg
+
+
+def batched_lcn(ctx: Context, batch):
+    """configs[4]: every problem of a configs.Batch in ragged launches (one
+    CTA per problem). Returns (distances, statuses, iterations); a problem
+    with a non-zero status (the reference's first error for it) has distance NaN."""
+    X = _f64(batch.X)
+    k = batch.count
+    n = np.ascontiguousarray(batch.n, np.int32)
+    m = np.ascontiguousarray(batch.m, np.int32)
+    lsh = np.array([batch.lsh_seed(i) for i in range(k)], np.uint64)
+    lms = np.array([batch.landmark_seed(i) for i in range(k)], np.uint64)
+    dist = np.zeros(k)
+    st = np.zeros(k, np.int32)
+    it = np.zeros(k, np.int32)
+    ctx.check(ctx.lib.lcn_batched_lcn(ctx.h, _p(X), X.shape[0], X.shape[1], k, _p(n), _p(m), batch.cost, batch.lam,
+                                      batch.buckets, batch.kmeans_iters, _p(lsh), batch.landmarks, _p(lms),
+                                      batch.iters, _p(dist), _p(st), _p(it)))
+    return dist, st, it
 
 
 def cross_polytope_buckets(ctx: Context, points, proj):
