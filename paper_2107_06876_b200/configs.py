@@ -37,6 +37,15 @@ def mix_seed(seed: int, salt: int) -> int:
     return x ^ (x >> 31)
 
 
+def mix_seed_array(seeds: np.ndarray, salt: int) -> np.ndarray:
+    """mix_seed over a uint64 array (wrapping arithmetic)."""
+    with np.errstate(over="ignore"):
+        x = np.asarray(seeds, np.uint64) ^ np.uint64((salt * 0x9E3779B97F4A7C15) & ((1 << 64) - 1))
+        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return x ^ (x >> np.uint64(31))
+
+
 @dataclasses.dataclass
 class Problem:
     name: str
@@ -181,6 +190,12 @@ class Batch:
 
     def landmark_seed(self, k):
         return mix_seed(int(self.seeds[k]), 4)
+
+    def lsh_seeds(self):
+        return mix_seed_array(self.seeds, 3)
+
+    def landmark_seeds(self):
+        return mix_seed_array(self.seeds, 4)
 
     def problem(self, k):
         o, n, m = int(self.row_off[k]), int(self.n[k]), int(self.m[k])

@@ -29,6 +29,7 @@
 #include <limits>
 #include <vector>
 
+#include <optional>
 #include <random>
 
 #include "common.cuh"
@@ -39,7 +40,8 @@
 namespace lcnb {
 namespace {
 
-constexpr int kBT = 256;        // threads per problem CTA
+constexpr int kBT = 256;        // threads per problem CTA (solve)
+constexpr int kKT = 128;        // threads per problem CTA (k-means: several CTAs per SM hide the serial folds)
 constexpr int kBMaxK = 16;      // clusters / landmarks per problem
 constexpr int kBMaxD = 32;      // features
 constexpr int kBMaxN = 1024;    // points per problem (n + m)
@@ -56,10 +58,30 @@ struct BatProb {
 // sqdist with the reference's separate roundings (kmeans.cpp:12-19)
 __device__ __forceinline__ double bat_sqdist(const double* __restrict__ x, const double* __restrict__ y, int d) {
     double s = 0.0;
+#pragma unroll 8
     for (int k = 0; k < d; ++k) {
         const double df = xsub(x[k], y[k]);
         s = xadd(s, xmul(df, df));
     }
+    return s;
+}
+
+// the same fold with the point held in registers (DP >= d, predicated): the
+// hot loops of the k-means compare one point against many centres
+template <int DP>
+__device__ __forceinline__ void bat_load(const double* __restrict__ x, int d, double (&v)[DP]) {
+#pragma unroll
+    for (int k = 0; k < DP; ++k) v[k] = k < d ? x[k] : 0.0;
+}
+template <int DP>
+__device__ __forceinline__ double bat_sqdist_reg(const double (&v)[DP], const double* __restrict__ y, int d) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < DP; ++k)
+        if (k < d) {
+            const double df = xsub(v[k], y[k]);
+            s = xadd(s, xmul(df, df));
+        }
     return s;
 }
 
@@ -83,45 +105,63 @@ struct BatKm {  // one lloyd call, shared memory
 
 // kmeans_pp_indices (kmeans.cpp:23-65): first = the engine's first index,
 // raw = its later 64-bit draws (one per step with total > 0).
+template <int DP>
 __device__ void cta_kmeanspp(const double* __restrict__ X, int N, int d, int k, uint32_t first,
                              const unsigned long long* __restrict__ raw, BatKm& s) {
+    __shared__ double target_s;
+    __shared__ int pick_s, mode_s;
     const int tid = threadIdx.x;
-    for (int i = tid; i < N; i += kBT) s.dist2[i] = kPosInf;
+    for (int i = tid; i < N; i += kKT) s.dist2[i] = kPosInf;
     if (tid == 0) s.chosen[0] = first;
     __syncthreads();
     int draw = 0;
     for (int t = 1; t < k; ++t) {
         const double* last = X + static_cast<long long>(s.chosen[t - 1]) * d;
-        for (int i = tid; i < N; i += kBT) {
-            const double d2 = bat_sqdist(X + static_cast<long long>(i) * d, last, d);
+        double lv[DP];
+        bat_load<DP>(last, d, lv);
+        for (int i = tid; i < N; i += kKT) {
+            const double d2 = bat_sqdist_reg<DP>(lv, X + static_cast<long long>(i) * d, d);  // same fold (x - y)^2
             if (d2 < s.dist2[i]) s.dist2[i] = d2;
         }
         __syncthreads();
         if (tid == 0) {
             double total = 0.0;  // left fold in index order (kmeans.cpp:39)
             for (int i = 0; i < N; ++i) s.prefix[i] = total = xadd(total, s.dist2[i]);
-            int pick;
-            if (total <= 0.0) {  // first unused (kmeans.cpp:42-47), no draw
-                pick = 0;
-                for (;;) {
-                    bool used = false;
-                    for (int c = 0; c < t; ++c) used |= s.chosen[c] == static_cast<uint32_t>(pick);
-                    if (!used || pick >= N) break;
-                    ++pick;
-                }
+            if (total <= 0.0) {
+                mode_s = 0;
             } else {
                 // uniform_real_distribution(0, total): generate_canonical = u 2^-64,
                 // clamped below 1; (b - a) c + a (kmeans.cpp:49-50)
                 double c = __ull2double_rn(raw[draw++]) * 5.421010862427522e-20;
                 if (c >= 1.0) c = 0.99999999999999989;
-                const double target = xadd(xmul(c, xsub(total, 0.0)), 0.0);
-                pick = N - 1;
-                for (int i = 0; i < N; ++i)
-                    if (s.prefix[i] >= target && s.dist2[i] > 0.0) {
-                        pick = i;
-                        break;
-                    }
+                target_s = xadd(xmul(c, xsub(total, 0.0)), 0.0);
+                mode_s = 1;
             }
+            pick_s = N;
+        }
+        __syncthreads();
+        if (mode_s == 1) {
+            // first i with running sum >= target and dist2 > 0 (kmeans.cpp:51-58)
+            const double target = target_s;
+            for (int i = tid; i < N; i += kKT)
+                if (s.prefix[i] >= target && s.dist2[i] > 0.0) {
+                    atomicMin(&pick_s, i);
+                    break;
+                }
+        } else {
+            // first unused index (kmeans.cpp:42-47), no draw
+            for (int i = tid; i < N; i += kKT) {
+                bool used = false;
+                for (int c = 0; c < t; ++c) used |= s.chosen[c] == static_cast<uint32_t>(i);
+                if (!used) {
+                    atomicMin(&pick_s, i);
+                    break;
+                }
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            const int pick = pick_s < N ? pick_s : N - 1;
             s.chosen[t] = static_cast<uint32_t>(pick);
             s.dist2[pick] = 0.0;
         }
@@ -130,13 +170,15 @@ __device__ void cta_kmeanspp(const double* __restrict__ X, int N, int d, int k, 
 }
 
 // assign_nearest (kmeans.cpp:67-85): strict < over c = 0..k-1
+template <int DP>
 __device__ void cta_assign(const double* __restrict__ X, int N, int d, int k, BatKm& s) {
-    for (int i = threadIdx.x; i < N; i += kBT) {
-        const double* x = X + static_cast<long long>(i) * d;
+    for (int i = threadIdx.x; i < N; i += kKT) {
+        double xv[DP];
+        bat_load<DP>(X + static_cast<long long>(i) * d, d, xv);
         double best = kPosInf;
         uint32_t arg = 0;
         for (int c = 0; c < k; ++c) {
-            const double d2 = bat_sqdist(x, s.ctr + c * d, d);
+            const double d2 = bat_sqdist_reg<DP>(xv, s.ctr + c * d, d);
             if (d2 < best) {
                 best = d2;
                 arg = static_cast<uint32_t>(c);
@@ -148,38 +190,59 @@ __device__ void cta_assign(const double* __restrict__ X, int N, int d, int k, Ba
 }
 
 // lloyd (kmeans.cpp:87-143)
+template <int DP>
 __device__ void cta_lloyd(const double* __restrict__ X, int N, int d, int k, int iters, uint32_t first,
                           const unsigned long long* __restrict__ raw, BatKm& s) {
     const int tid = threadIdx.x;
-    cta_kmeanspp(X, N, d, k, first, raw, s);
-    for (int e = tid; e < k * d; e += kBT) s.ctr[e] = X[static_cast<long long>(s.chosen[e / d]) * d + e % d];
+    cta_kmeanspp<DP>(X, N, d, k, first, raw, s);
+    for (int e = tid; e < k * d; e += kKT) s.ctr[e] = X[static_cast<long long>(s.chosen[e / d]) * d + e % d];
     __syncthreads();
     for (int it = 0; it < iters; ++it) {
-        cta_assign(X, N, d, k, s);
-        if (tid == 0) {  // members of each cluster in point order (a stable counting sort)
-            for (int c = 0; c <= k; ++c) s.start[c] = 0;
-            for (int i = 0; i < N; ++i) ++s.start[s.assign[i] + 1];
-            for (int c = 0; c < k; ++c) {
-                s.counts[c] = s.start[c + 1];
-                s.start[c + 1] += s.start[c];
+        cta_assign<DP>(X, N, d, k, s);
+        for (int c = tid; c < k; c += kKT) s.counts[c] = 0;
+        __syncthreads();
+        for (int i = tid; i < N; i += kKT) atomicAdd(&s.counts[s.assign[i]], 1);
+        __syncthreads();
+        if (tid < 32) {
+            // members of each cluster in point order: a stable partition,
+            // 32 points at a time (lanes of a cluster ranked by lane)
+            if (tid == 0) {
+                int acc = 0;
+                for (int c = 0; c < k; ++c) {
+                    s.start[c] = acc;
+                    acc += s.counts[c];
+                }
+                s.start[k] = acc;
             }
-            for (int c = 0; c < k; ++c) s.prefix[c] = s.start[c];  // cursor (reuse)
-            for (int i = 0; i < N; ++i) {
-                const uint32_t c = s.assign[i];
-                s.order[static_cast<int>(s.prefix[c])] = static_cast<uint32_t>(i);
-                s.prefix[c] += 1.0;
+            __syncwarp();
+            int cur = tid < k ? s.start[tid] : 0;  // lane c: next slot of cluster c
+            for (int b0 = 0; b0 < N; b0 += 32) {
+                const int i = b0 + tid;
+                const uint32_t c = i < N ? s.assign[i] : 0xffffffffu;
+                const unsigned grp = __match_any_sync(0xffffffffu, c);
+                const int base = __shfl_sync(0xffffffffu, cur, static_cast<int>(c < 32 ? c : 0));
+                if (i < N) s.order[base + __popc(grp & ((1u << tid) - 1u))] = static_cast<uint32_t>(i);
+                // advance each cluster's cursor by its members in this chunk
+                for (int cc = 0; cc < k; ++cc) {
+                    const unsigned mc = __ballot_sync(0xffffffffu, c == static_cast<uint32_t>(cc));
+                    if (tid == cc) cur += __popc(mc);
+                }
             }
         }
         __syncthreads();
-        // sums in point order per (cluster, feature), then s * (1 / count) (kmeans.cpp:106-121)
-        for (int e = tid; e < k * d; e += kBT) {
+        // sums in point order per (cluster, feature), then s * (1 / count)
+        // (kmeans.cpp:106-121)
+        for (int e = tid; e < k * d; e += kKT) {
             const int c = e / d, kk = e % d;
             if (s.counts[c] == 0) continue;
             double acc = 0.0;
             for (int r = s.start[c]; r < s.start[c + 1]; ++r)
                 acc = xadd(acc, X[static_cast<long long>(s.order[r]) * d + kk]);
-            s.ctr[e] = xmul(acc, __ddiv_rn(1.0, static_cast<double>(s.counts[c])));
+            s.sums[e] = xmul(acc, __ddiv_rn(1.0, static_cast<double>(s.counts[c])));
         }
+        __syncthreads();
+        for (int e = tid; e < k * d; e += kKT)
+            if (s.counts[e / d] != 0) s.ctr[e] = s.sums[e];
         __syncthreads();
         if (tid == 0) {  // empty clusters: the farthest point, first max (kmeans.cpp:122-139)
             for (int c = 0; c < k; ++c) {
@@ -202,12 +265,13 @@ __device__ void cta_lloyd(const double* __restrict__ X, int N, int d, int k, int
         }
         __syncthreads();
     }
-    cta_assign(X, N, d, k, s);
+    cta_assign<DP>(X, N, d, k, s);
 }
 
 // Per problem: LSH bucket ids (k-means of the union, fn_seed(seed, 0, 0)),
 // landmarks (k-means of the union, 10 iterations) and A = exp(-c(L, L) / lambda).
-__global__ void __launch_bounds__(kBT) bat_kmeans_kernel(const double* __restrict__ X, int d,
+template <int DP>
+__global__ void __launch_bounds__(kKT, 8) bat_kmeans_kernel(const double* __restrict__ X, int d,
                                                          const BatProb* __restrict__ probs,
                                                          const unsigned long long* __restrict__ raw, int buckets,
                                                          int kmeans_iters, int l, int kind, double lambda,
@@ -232,11 +296,11 @@ __global__ void __launch_bounds__(kBT) bat_kmeans_kernel(const double* __restric
     const int tid = threadIdx.x;
 
     // LSH: one band, one function (lsh.cpp:264-276)
-    cta_lloyd(Xp, N, d, buckets, kmeans_iters, pr.lsh_first, raw + pr.lsh_raw, s);
-    for (int i = tid; i < N; i += kBT) bucket_out[pr.row0 + i] = s.assign[i];
+    cta_lloyd<DP>(Xp, N, d, buckets, kmeans_iters, pr.lsh_first, raw + pr.lsh_raw, s);
+    for (int i = tid; i < N; i += kKT) bucket_out[pr.row0 + i] = s.assign[i];
     if (tid < kBMaxK) bcnt[0][tid] = bcnt[1][tid] = 0;
     __syncthreads();
-    for (int i = tid; i < N; i += kBT) atomicAdd(&bcnt[i < pr.n ? 0 : 1][s.assign[i]], 1);
+    for (int i = tid; i < N; i += kKT) atomicAdd(&bcnt[i < pr.n ? 0 : 1][s.assign[i]], 1);
     __syncthreads();
     if (tid == 0) {
         unsigned long long nnz = 0;
@@ -246,12 +310,12 @@ __global__ void __launch_bounds__(kBT) bat_kmeans_kernel(const double* __restric
     __syncthreads();
 
     // landmarks: lloyd(union, l, 10, seed) centroids (nystrom.cpp:35-37)
-    cta_lloyd(Xp, N, d, l, 10, pr.lm_first, raw + pr.lm_raw, s);
+    cta_lloyd<DP>(Xp, N, d, l, 10, pr.lm_first, raw + pr.lm_raw, s);
     double* L = lm_out + static_cast<long long>(blockIdx.x) * l * d;
-    for (int e = tid; e < l * d; e += kBT) L[e] = s.ctr[e];
+    for (int e = tid; e < l * d; e += kKT) L[e] = s.ctr[e];
     // A_ab = exp(-c(L_a, L_b) / lambda) (nystrom.cpp:88-93: division)
     double* A = a_out + static_cast<long long>(blockIdx.x) * l * l;
-    for (int e = tid; e < l * l; e += kBT)
+    for (int e = tid; e < l * l; e += kKT)
         A[e] = exp(-bat_cost(kind, s.ctr + (e / l) * d, s.ctr + (e % l) * d, d) / lambda);
 }
 
@@ -297,7 +361,7 @@ __device__ __forceinline__ void block_sums(double* v, int l, double* red, double
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(kBT) bat_solve_kernel(
+__global__ void __launch_bounds__(kBT, 4) bat_solve_kernel(
     const double* __restrict__ X, int d, const BatProb* __restrict__ probs, const int* __restrict__ todo,
     const uint32_t* __restrict__ bucket, const double* __restrict__ lm, const double* __restrict__ ainv,
     const double* __restrict__ aj, int buckets, int l, int kind, double lambda, int iters,
@@ -574,6 +638,8 @@ void batched_lcn(Ctx& ctx, const double* h_X, size_t rows, int d, int nprob, con
         row += N;
     }
     if (static_cast<size_t>(row) != rows) throw Status(1, "batched LCN: row count does not match n + m totals");
+    std::optional<PhaseTimer> pt;
+    pt.emplace(ctx, "batched: upload");
     DevBuf<double> X(rows * d);
     X.upload(h_X, rows * d, s);
     DevBuf<unsigned long long> draws(std::max<size_t>(raw.size(), 1));
@@ -583,11 +649,16 @@ void batched_lcn(Ctx& ctx, const double* h_X, size_t rows, int d, int nprob, con
     DevBuf<uint32_t> bucket(rows);
     DevBuf<double> lm(static_cast<size_t>(nprob) * l * d), A(static_cast<size_t>(nprob) * l * l);
     DevBuf<unsigned long long> nnz(nprob);
-    const size_t km_smem = static_cast<size_t>(kBMaxN) * (8 + 8 + 4 + 4) + 2 * kBMaxK * kBMaxD * 8 +
+    int maxN = 1;
+    for (int k = 0; k < nprob; ++k) maxN = std::max(maxN, h_n[k] + h_m[k]);
+    // shared memory sized by the batch's largest problem (more CTAs per SM)
+    const size_t km_smem = static_cast<size_t>(maxN) * (8 + 8 + 4 + 4) + 2 * kBMaxK * static_cast<size_t>(d) * 8 +
                            (3 * kBMaxK + 2) * 4 + 64;
-    allow_max_dyn_smem(bat_kmeans_kernel);
-    bat_kmeans_kernel<<<nprob, kBT, km_smem, s>>>(X.get(), d, dprob.get(), draws.get(), buckets, kmeans_iters, l,
-                                                  kind, lambda, bucket.get(), lm.get(), A.get(), nnz.get());
+    auto kmk = d <= 16 ? bat_kmeans_kernel<16> : bat_kmeans_kernel<32>;
+    allow_max_dyn_smem(kmk);
+    pt.emplace(ctx, "batched: k-means LSH + landmarks (device)");
+    kmk<<<nprob, kKT, km_smem, s>>>(X.get(), d, dprob.get(), draws.get(), buckets, kmeans_iters, l, kind, lambda,
+                                    bucket.get(), lm.get(), A.get(), nnz.get());
     LAUNCH_OK("bat_kmeans_kernel");
     std::vector<double> hA(static_cast<size_t>(nprob) * l * l);
     std::vector<unsigned long long> hnnz(nprob);
@@ -606,7 +677,8 @@ void batched_lcn(Ctx& ctx, const double* h_X, size_t rows, int d, int nprob, con
     std::vector<double> hAinv(hA.size()), hAj(hA.size());
     std::vector<int> level(nprob, 0), todo(nprob), hstat(nprob, kNeedJitter);
     for (int k = 0; k < nprob; ++k) todo[k] = k;
-    const size_t sv_smem = static_cast<size_t>(kBMaxN) * 8 * 5 + (kBMaxK + 1) * 8 + kBMaxN * 8 + (kBMaxK + 1) * 8 + 64;
+    const size_t sv_smem = static_cast<size_t>(maxN) * 8 * 5 + (kBMaxK + 1) * 8 + static_cast<size_t>(maxN) * 8 +
+                           (kBMaxK + 1) * 8 + 64;
     allow_max_dyn_smem(bat_solve_kernel);
     // jitter schedule rel = 0, 1e-10, then rel * 10 while <= 1.1e-4 (nystrom.cpp:99)
     std::vector<double> rels;
@@ -614,6 +686,7 @@ void batched_lcn(Ctx& ctx, const double* h_X, size_t rows, int d, int nprob, con
     const int kLevels = static_cast<int>(rels.size());
     auto rel_of = [&](int lv) { return rels[lv]; };
     while (!todo.empty()) {
+        pt.emplace(ctx, "batched: LDL^T + inverse (host, long double)");
         // host: LDL^T of A + rel * trace / l in long double, inverse (shared with the big path)
         std::vector<int> launch;
 #pragma omp parallel for schedule(dynamic, 64)
@@ -631,6 +704,7 @@ void batched_lcn(Ctx& ctx, const double* h_X, size_t rows, int d, int nprob, con
             else launch.push_back(k);
         }
         if (launch.empty()) break;
+        pt.emplace(ctx, "batched: factors, correction, Sinkhorn (device)");
         dAinv.upload(hAinv.data(), hAinv.size(), s);
         dAj.upload(hAj.data(), hAj.size(), s);
         dtodo.upload(launch.data(), launch.size(), s);
@@ -650,6 +724,7 @@ void batched_lcn(Ctx& ctx, const double* h_X, size_t rows, int d, int nprob, con
             }
         }
     }
+    pt.reset();
     ddist.download(dist_out, nprob, s);
     std::vector<int> it(nprob);
     diters.download(it.data(), nprob, s);

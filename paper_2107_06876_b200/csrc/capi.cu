@@ -632,8 +632,10 @@ int lcn_batched_lcn(lcn_ctx* ctx, const double* X, size_t rows, size_t d, int np
             throw Status(2, "batched LCN: null argument");
         if (iters < 1) throw Status(2, "sinkhorn: max_iters must be >= 1");
         if (nprob == 0) return;
-        for (size_t i = 0; i < rows * d; ++i)
-            if (!std::isfinite(X[i])) throw Status(2, "point set has a non-finite coordinate");
+        bool finite = true;
+#pragma omp parallel for schedule(static) reduction(&& : finite)
+        for (long long i = 0; i < static_cast<long long>(rows * d); ++i) finite = finite && std::isfinite(X[i]);
+        if (!finite) throw Status(2, "point set has a non-finite coordinate");
         batched_lcn(ctx->c, X, rows, static_cast<int>(d), nprob, n, m, cost, lambda, buckets, kmeans_iters, lsh_seeds,
                     static_cast<int>(l), landmark_seeds, iters, distance_out, status_out, iters_out);
     });

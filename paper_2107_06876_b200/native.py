@@ -276,8 +276,8 @@ def batched_lcn(ctx: Context, batch):
     k = batch.count
     n = np.ascontiguousarray(batch.n, np.int32)
     m = np.ascontiguousarray(batch.m, np.int32)
-    lsh = np.array([batch.lsh_seed(i) for i in range(k)], np.uint64)
-    lms = np.array([batch.landmark_seed(i) for i in range(k)], np.uint64)
+    lsh = np.ascontiguousarray(batch.lsh_seeds(), np.uint64)
+    lms = np.ascontiguousarray(batch.landmark_seeds(), np.uint64)
     dist = np.zeros(k)
     st = np.zeros(k, np.int32)
     it = np.zeros(k, np.int32)
