@@ -48,12 +48,15 @@ constexpr int kBMaxN = 1024;    // points per problem (n + m)
 constexpr int kNeedJitter = 50; // status: residual test failed at this jitter level
 
 struct BatProb {
+    long long nnz;         // support size (sum over buckets of n_b m_b)
     long long row0;        // first row of the problem in X (n sources, then m targets)
     int n, m;
     uint32_t lsh_first, lm_first;  // k-means++ first indices (host engine)
     long long lsh_raw, lm_raw;     // offsets of the engine's raw draws
     long long scr;                 // scratch offset (doubles): U n x l, V l x m, W l x m, delta nnz
 };
+
+__device__ __forceinline__ long long s_nnz_of(const BatProb& p) { return p.nnz; }
 
 // sqdist with the reference's separate roundings (kmeans.cpp:12-19)
 __device__ __forceinline__ double bat_sqdist(const double* __restrict__ x, const double* __restrict__ y, int d) {
@@ -321,7 +324,7 @@ __global__ void __launch_bounds__(kKT, 8) bat_kmeans_kernel(const double* __rest
 
 // ---- solve ------------------------------------------------------------------
 struct BatSolveSmem {
-    double *log_s, *log_t, *kt, *tt, *rowm;  // vectors (N max)
+    double *log_s, *log_t, *kt, *kt2, *tt, *rowm;  // vectors
     int *p_ord, *q_ord, *p_rank, *q_rank;    // sources / targets grouped by bucket, rank inside
     int *p_start, *q_start;                  // bucket offsets (buckets + 1)
     unsigned long long* blk;                 // delta block offsets (buckets + 1)
@@ -384,11 +387,13 @@ __global__ void __launch_bounds__(kBT, 4) bat_solve_kernel(
     double* V = U + static_cast<long long>(n) * l;  // l x m
     double* W = V + static_cast<long long>(l) * m;  // l x m
     double* D = W + static_cast<long long>(l) * m;  // delta, bucket blocks row-major
+    double* DT = D + s_nnz_of(pr);                  // delta, bucket blocks transposed (column pass)
     BatSolveSmem s;
     s.log_s = reinterpret_cast<double*>(bdyn);
     s.log_t = s.log_s + n;
     s.kt = s.log_t + m;
-    s.tt = s.kt + std::max(n, m);
+    s.kt2 = s.kt + n;
+    s.tt = s.kt2 + m;
     s.rowm = s.tt + std::max(n, m);
     s.blk = reinterpret_cast<unsigned long long*>(s.rowm + n);
     s.p_ord = reinterpret_cast<int*>(s.blk + buckets + 1);
@@ -475,6 +480,7 @@ __global__ void __launch_bounds__(kBT, 4) bat_solve_kernel(
             double nys = 0.0;
             for (int a = 0; a < l; ++a) nys += U[i * l + a] * W[a * m + j];
             D[s.blk[b] + e] = ex - nys;
+            DT[s.blk[b] + static_cast<long long>(e % mb) * nb + e / mb] = ex - nys;
         }
     }
     if (block_any(over, &flag)) {
@@ -483,119 +489,118 @@ __global__ void __launch_bounds__(kBT, 4) bat_solve_kernel(
     }
 
     // ---- Sinkhorn (sinkhorn.cpp:104-188), uniform marginals, tol 0 ----------
+    // Every check the reference makes (non-finite log scalings, zero linear
+    // scalings, non-positive Nystrom / LCN row sums, an exact fixed point)
+    // goes into per-pass flags that are read at the barriers the data flow
+    // needs anyway: five barriers per half-iteration.
     const double lp = log(1.0 / n), lq = log(1.0 / m);
-    double part[kBMaxK];
-    // out[i] = hi + log(U_i W tt + delta_i. tt) with tt = exp(log_t - hi) (operator.cpp:148-176)
-    auto row_pass = [&]() -> int {
+    __shared__ int f_nf, f_zero, f_nys, f_neg, f_ne;
+    // one LCN log matvec (operator.cpp:148-176): in[len_in] are log scalings,
+    // out[len_out] = hi + log(Fo mid + delta tt), mid = Fi^T tt, tt = exp(in - hi).
+    // src: when given, in[k] = base - src[k] is formed on the fly (the
+    // s-update / t-update of sinkhorn.cpp:151-156) and checked for finiteness.
+    auto pass = [&](double* in, const double* src, double base, int len_in, int len_out, const double* Fi,
+                    int fi_rs, int fi_cs, const double* Fo, int fo_rs, int fo_cs, const double* Dm, bool rows,
+                    double* out) -> int {
+        if (tid == 0) f_nf = f_zero = f_nys = f_neg = 0;
         double hi = -kPosInf;
-        for (int j = tid; j < m; j += kBT) hi = fmax(hi, s.log_t[j]);
-        hi = block_max(hi, red);
-        bool pos = true;
-        for (int j = tid; j < m; j += kBT) {
-            s.tt[j] = exp(s.log_t[j] - hi);
-            pos &= s.tt[j] > 0.0;
+        bool nf = false;
+        for (int k2 = tid; k2 < len_in; k2 += kBT) {
+            double v = in[k2];
+            if (src) {
+                v = base - src[k2];
+                in[k2] = v;
+                nf |= !isfinite(v);
+            }
+            hi = fmax(hi, v);
         }
-        const bool all_pos = !block_any(!pos, &flag);
-        for (int a = 0; a < l; ++a) part[a] = 0.0;
-        for (int j = tid; j < m; j += kBT)
-            for (int a = 0; a < l; ++a) part[a] += W[a * m + j] * s.tt[j];
-        block_sums(part, l, red, mid);
-        bool neg = false;
-        for (int i = tid; i < n; i += kBT) {
+        if (nf) f_nf = 1;
+        hi = block_max(hi, red);  // 2 barriers
+        if (f_nf) return 3;       // StabilizationError: non-finite scaling
+        bool zero = false;
+        for (int k2 = tid; k2 < len_in; k2 += kBT) {
+            const double t = exp(in[k2] - hi);
+            s.tt[k2] = t;
+            zero |= !(t > 0.0);
+        }
+        if (zero) f_zero = 1;
+        __syncthreads();  // 1 barrier: tt complete
+        // mid_a = sum_k Fi(k, a) tt_k: warp w owns landmarks a = w, w + 8, ...
+        for (int a = tid >> 5; a < l; a += kBT / 32) {
+            double acc = 0.0;
+            for (int k2 = tid & 31; k2 < len_in; k2 += 32)
+                acc += Fi[static_cast<long long>(k2) * fi_rs + a * fi_cs] * s.tt[k2];
+            acc = warp_sum(acc);
+            if ((tid & 31) == 0) mid[a] = acc;
+        }
+        __syncthreads();  // 1 barrier: mid complete
+        bool nys = false, neg = false;
+        for (int o = tid; o < len_out; o += kBT) {
             double y = 0.0;
-            for (int a = 0; a < l; ++a) y += U[i * l + a] * mid[a];
-            if (all_pos && !(y > 0.0)) neg = true;  // nys_matvec (nystrom.cpp:157-160)
-            const int b = bk[i], mb = s.q_start[b + 1] - s.q_start[b];
-            const double* Dr = D + s.blk[b] + static_cast<long long>(s.p_rank[i]) * mb;
+            for (int a = 0; a < l; ++a) y += Fo[static_cast<long long>(o) * fo_rs + a * fo_cs] * mid[a];
+            nys |= !(y > 0.0);  // nys_matvec (nystrom.cpp:157-160) when every tt > 0
+            const int b = rows ? bk[o] : bk[n + o];
+            const int ob = rows ? s.q_start[b] : s.p_start[b];
+            const int nbk = (rows ? s.q_start[b + 1] : s.p_start[b + 1]) - ob;
+            const int* ord = rows ? s.q_ord : s.p_ord;
+            const double* Dr = Dm + s.blk[b] + static_cast<long long>(rows ? s.p_rank[o] : s.q_rank[o]) * nbk;
             double c = 0.0;
-            for (int r = 0; r < mb; ++r) c += Dr[r] * s.tt[s.q_ord[s.q_start[b] + r]];
+            for (int r = 0; r < nbk; ++r) c += Dr[r] * s.tt[ord[ob + r]];
             y += c;
-            if (!(y > 0.0)) neg = true;
-            s.kt[i] = hi + log(y);
+            neg |= !(y > 0.0);
+            out[o] = hi + log(y);
         }
-        return block_any(neg, &flag) ? 4 : 0;
-    };
-    auto col_pass = [&]() -> int {
-        double hi = -kPosInf;
-        for (int i = tid; i < n; i += kBT) hi = fmax(hi, s.log_s[i]);
-        hi = block_max(hi, red);
-        bool pos = true;
-        for (int i = tid; i < n; i += kBT) {
-            s.tt[i] = exp(s.log_s[i] - hi);
-            pos &= s.tt[i] > 0.0;
-        }
-        const bool all_pos = !block_any(!pos, &flag);
-        for (int a = 0; a < l; ++a) part[a] = 0.0;
-        for (int i = tid; i < n; i += kBT)
-            for (int a = 0; a < l; ++a) part[a] += U[i * l + a] * s.tt[i];
-        block_sums(part, l, red, mid);
-        bool neg = false;
-        for (int j = tid; j < m; j += kBT) {
-            double y = 0.0;
-            for (int a = 0; a < l; ++a) y += W[a * m + j] * mid[a];
-            if (all_pos && !(y > 0.0)) neg = true;
-            const int b = bk[n + j], mb = s.q_start[b + 1] - s.q_start[b], nb = s.p_start[b + 1] - s.p_start[b];
-            const double* Dc = D + s.blk[b] + s.q_rank[j];
-            double c = 0.0;
-            for (int r = 0; r < nb; ++r) c += Dc[static_cast<long long>(r) * mb] * s.tt[s.p_ord[s.p_start[b] + r]];
-            y += c;
-            if (!(y > 0.0)) neg = true;
-            s.kt[j] = hi + log(y);  // kts
-        }
-        return block_any(neg, &flag) ? 4 : 0;
+        if (nys) f_nys = 1;
+        if (neg) f_neg = 1;
+        __syncthreads();  // 1 barrier: out complete, flags final
+        if (f_neg || (f_nys && !f_zero)) return 4;  // NegativeKernelError
+        return 0;
     };
     for (int j = tid; j < m; j += kBT) s.log_t[j] = 0.0;
     __syncthreads();
-    int st = row_pass();
+    // kt = log_matvec(log t = 0)
+    int st = pass(s.log_t, nullptr, 0.0, m, n, W, 1, m, U, l, 1, D, true, s.kt);
     if (st) {
         fail(st);
         return;
     }
-    __syncthreads();
     int it = 0;
     while (it < iters) {
         ++it;
-        bool nf = false;
-        for (int i = tid; i < n; i += kBT) {
-            s.log_s[i] = lp - s.kt[i];
-            nf |= !isfinite(s.log_s[i]);
-        }
-        if (block_any(nf, &flag)) {
-            fail(3);
-            return;
-        }
-        if ((st = col_pass())) {
+        // log s = log p - kt, then kts = log_matvec_t(log s)
+        if ((st = pass(s.log_s, s.kt, lp, n, m, U, l, 1, W, 1, m, DT, false, s.kt2))) {
             fail(st);
             return;
         }
-        __syncthreads();
-        for (int j = tid; j < m; j += kBT) {
-            s.log_t[j] = lq - s.kt[j];
-            nf |= !isfinite(s.log_t[j]);
-        }
-        if (block_any(nf, &flag)) {
-            fail(3);
-            return;
-        }
-        if ((st = row_pass())) {
+        // log t = log q - kts, then kt = log_matvec(log t)
+        if ((st = pass(s.log_t, s.kt2, lq, m, n, W, 1, m, U, l, 1, D, true, s.kt))) {
             fail(st);
             return;
         }
+        // err = sum |exp(log s + kt) - p| <= tol = 0 only at an exact fixed point
+        if (tid == 0) f_ne = 0;
         __syncthreads();
-        for (int i = tid; i < n; i += kBT) s.rowm[i] = exp(s.log_s[i] + s.kt[i]);
-        // tol = 0: err <= 0 only for an exact fixed point
-        double e = 0.0;
-        for (int i = tid; i < n; i += kBT) e += fabs(s.rowm[i] - 1.0 / n);
-        part[0] = e;
-        block_sums(part, 1, red, mid);
-        if (mid[0] <= 0.0) break;
+        bool ne = false;
+        for (int i = tid; i < n; i += kBT) ne |= exp(s.log_s[i] + s.kt[i]) != 1.0 / n;
+        if (ne) f_ne = 1;
+        __syncthreads();
+        if (!f_ne) break;
     }
+    for (int i = tid; i < n; i += kBT) s.rowm[i] = exp(s.log_s[i] + s.kt[i]);
+    __syncthreads();
     // distance = lambda (<log s, P1> + <log t, q>) (sinkhorn.cpp:178-183)
     double acc = 0.0;
     for (int i = tid; i < n; i += kBT) acc += s.log_s[i] * s.rowm[i];
     for (int j = tid; j < m; j += kBT) acc += s.log_t[j] * (1.0 / m);
-    part[0] = acc;
-    block_sums(part, 1, red, mid);
+    acc = warp_sum(acc);
+    if ((tid & 31) == 0) red[tid >> 5] = acc;
+    __syncthreads();
+    if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kBT / 32; ++w) t += red[w];
+        mid[0] = t;
+    }
+    __syncthreads();
     if (tid == 0) {
         status_out[pi] = 0;
         dist_out[pi] = lambda * mid[0];
@@ -616,7 +621,10 @@ void batched_lcn(Ctx& ctx, const double* h_X, size_t rows, int d, int nprob, con
     if (!(lambda > 0.0)) throw Status(2, "build_factors: lambda must be positive");
     cudaStream_t s = ctx.stream;
     std::vector<BatProb> pr(nprob);
-    std::vector<unsigned long long> raw;
+    // the caller engines' draws per problem (fixed slots: buckets - 1 for the
+    // LSH k-means++, then l - 1 for the landmark one), independent problems
+    const long long slot = static_cast<long long>(buckets - 1) + (l - 1);
+    std::vector<unsigned long long> raw(std::max<long long>(static_cast<long long>(nprob) * slot, 1));
     long long row = 0;
     for (int k = 0; k < nprob; ++k) {
         const int N = h_n[k] + h_m[k];
@@ -626,16 +634,21 @@ void batched_lcn(Ctx& ctx, const double* h_X, size_t rows, int d, int nprob, con
         pr[k].row0 = row;
         pr[k].n = h_n[k];
         pr[k].m = h_m[k];
-        auto draws = [&](uint64_t seed, int kk, uint32_t& first, long long& off) {
+        row += N;
+    }
+#pragma omp parallel for schedule(static)
+    for (int k = 0; k < nprob; ++k) {
+        const int N = h_n[k] + h_m[k];
+        auto draws = [&](uint64_t seed, int kk, uint32_t& first, long long off) {
             std::mt19937_64 rng(seed);
             std::uniform_int_distribution<std::size_t> fst(0, static_cast<std::size_t>(N - 1));
             first = static_cast<uint32_t>(fst(rng));
-            off = static_cast<long long>(raw.size());
-            for (int t = 0; t < kk - 1; ++t) raw.push_back(rng());
+            for (int t = 0; t < kk - 1; ++t) raw[off + t] = rng();
         };
+        pr[k].lsh_raw = static_cast<long long>(k) * slot;
+        pr[k].lm_raw = pr[k].lsh_raw + (buckets - 1);
         draws(fn_seed(lsh_seeds[k], 0, 0), buckets, pr[k].lsh_first, pr[k].lsh_raw);
         draws(lm_seeds[k], l, pr[k].lm_first, pr[k].lm_raw);
-        row += N;
     }
     if (static_cast<size_t>(row) != rows) throw Status(1, "batched LCN: row count does not match n + m totals");
     std::optional<PhaseTimer> pt;
@@ -668,7 +681,8 @@ void batched_lcn(Ctx& ctx, const double* h_X, size_t rows, int d, int nprob, con
     long long scr = 0;
     for (int k = 0; k < nprob; ++k) {
         pr[k].scr = scr;
-        scr += static_cast<long long>(pr[k].n) * l + 2LL * l * pr[k].m + static_cast<long long>(hnnz[k]);
+        pr[k].nnz = static_cast<long long>(hnnz[k]);
+        scr += static_cast<long long>(pr[k].n) * l + 2LL * l * pr[k].m + 2LL * static_cast<long long>(hnnz[k]);
     }
     dprob.upload(pr.data(), nprob, s);
     DevBuf<double> scratch(std::max<long long>(scr, 1));
@@ -677,7 +691,7 @@ void batched_lcn(Ctx& ctx, const double* h_X, size_t rows, int d, int nprob, con
     std::vector<double> hAinv(hA.size()), hAj(hA.size());
     std::vector<int> level(nprob, 0), todo(nprob), hstat(nprob, kNeedJitter);
     for (int k = 0; k < nprob; ++k) todo[k] = k;
-    const size_t sv_smem = static_cast<size_t>(maxN) * 8 * 5 + (kBMaxK + 1) * 8 + static_cast<size_t>(maxN) * 8 +
+    const size_t sv_smem = static_cast<size_t>(maxN) * 8 * 6 + (kBMaxK + 1) * 8 + static_cast<size_t>(maxN) * 8 +
                            (kBMaxK + 1) * 8 + 64;
     allow_max_dyn_smem(bat_solve_kernel);
     // jitter schedule rel = 0, 1e-10, then rel * 10 while <= 1.1e-4 (nystrom.cpp:99)
