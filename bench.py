@@ -261,6 +261,48 @@ def distance_roofline(iv, n, m, d, bands, buckets, landmarks, iters):
                     "landmarks; MMA flops 2 N_pad K_pad 128 x 3"}
 
 
+def batched_c4(lcn, ctx, with_cpu):
+    """configs[4]: all 32768 (pair, head) problems through lcn_batched_lcn
+    (host buffers in, distances out: upload, both ragged launches, the host
+    factorisation and the download are inside the wall time; one untimed
+    warm-up call), and the reference pipeline per problem (oracle/_ref) on a
+    bounded sample of the same problems, single-threaded like the
+    reference's serial loop over heads (sinkhorn.cpp:341-351)."""
+    import time
+    from paper_2107_06876_b200 import configs
+    b = configs.config4(1.0)
+    lcn.batched_lcn(ctx, b)  # warm-up
+    t0 = time.perf_counter()
+    dist, st, it = lcn.batched_lcn(ctx, b)
+    wall = time.perf_counter() - t0
+    out = {"problems": int(b.count), "problems_per_s": b.count / wall, "wall_s": wall,
+           "statuses_ok": int((st == 0).sum()), "mean_distance": float(np.nanmean(dist)),
+           "config": "configs[4]: 4096 pairs x 8 heads, n, m ~ U[20, 200], d = 16 after projection, L2, "
+                     "lambda = 0.1, l = 10 k-means landmarks, 1 x 8 k-means LSH, 50 iterations",
+           "input_bytes": int(b.X.nbytes), "launches": "2 ragged kernels (+ one per jitter retry)"}
+    if with_cpu:
+        try:
+            from oracle.bindings import RefLib, ref_available
+            if ref_available():
+                ref = RefLib()
+                os.environ["OMP_NUM_THREADS"] = "1"
+                k_s, t0 = 0, time.perf_counter()
+                while k_s < b.count and (time.perf_counter() - t0 < 3.0 or k_s < 64):
+                    p_, q_ = b.problem(k_s)
+                    try:
+                        ref.lcn_problem(p_, q_, b.cost, b.lam, b.buckets, b.kmeans_iters, b.lsh_seed(k_s),
+                                        b.landmarks, b.landmark_seed(k_s), b.iters)
+                    except Exception:
+                        pass
+                    k_s += 1
+                tw = time.perf_counter() - t0
+                out["cpu_baseline"] = {"value": k_s / tw, "unit": "problems/s", "cores": 1, "kind": "reference",
+                                       "sample": f"the first {k_s} problems of the batch, {tw:.2f} s"}
+        except Exception as ex:
+            out["cpu_baseline"] = {"value": None, "sample": f"unavailable: {ex}"}
+    return out
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -458,6 +500,13 @@ def run_ours(args, rank, world, local_rank):
             cpu = {"value": None, "unit": "iter/s", "cores": cpu_cores(), "kind": "reference",
                    "sample": f"unavailable: {ex}"}
 
+    c4 = None
+    if rank == 0 and world == 1 and not args.no_c4:
+        try:
+            c4 = batched_c4(lcn, ctx, not args.no_cpu)
+        except Exception as ex:
+            c4 = {"unavailable": str(ex)}
+
     gpu_launches = args.steps * launches_per_step if launches_per_step else None
     if rank == 0:
         line = {"metric": "lcn_sinkhorn_iters_per_s", "value": value, "unit": "iter/s", "n_gpus": world,
@@ -484,6 +533,7 @@ def run_ours(args, rank, world, local_rank):
                                        "frac": it_achieved / hbm, "algorithmic_bytes_per_iteration": b_iter,
                                        "ms_per_iteration": t_iter * 1e3},
                 "distance_roofline": dist_roof,
+                "batched_c4": c4,
                 "phases_ms_per_iteration": per_it,
                 "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": gpu_launches}
         emit(line)
@@ -515,6 +565,7 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-warmup", type=int, default=1)
+    ap.add_argument("--no-c4", action="store_true", help="skip the configs[4] batched-problems line")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sharded", action="store_true",
