@@ -355,6 +355,7 @@ def run_ours(args, rank, world, local_rank):
     build_ms = e0.elapsed_time(e1)
     nnz = op.nnz
     stored = op.stored
+    streamed = op.streamed
 
     def step():
         r = lcn.sinkhorn_device(op, dpm.data_ptr(), dqm.data_ptr(), opts)
@@ -515,7 +516,7 @@ def run_ours(args, rank, world, local_rank):
                 "dtype": "f32-storage/f64-accumulate", "data": "synthetic",
                 "config": {"workload": "configs[3] LCN-Sinkhorn n=m=1e6 d=128 sqL2/mean lambda=0.05 2x4096 LSH l=512",
                            "n": n, "m": m, "d": d, "landmarks": l, "bands": pr.bands, "buckets": pr.buckets,
-                           "iterations_per_step": ITERS, "nnz": nnz, "stored_entries": stored,
+                           "iterations_per_step": ITERS, "nnz": nnz, "stored_entries": stored, "streamed_entries": streamed,
                            "scale": args.scale, "l2": "inputs larger than L2 (delta + U + W = 6.2 GB per iteration)",
                            "parallelism": (f"one problem sharded over {world} GPUs: band buckets split by rank, "
                                            f"low-rank rows in slices; per half-iteration NCCL reduce-scatter of the "

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define LCN_B200_ABI_VERSION 2
+#define LCN_B200_ABI_VERSION 3  /* 3: lcn_op_info_t.streamed */
 
 typedef struct lcn_ctx lcn_ctx;
 typedef struct lcn_op lcn_op;
@@ -97,6 +97,7 @@ typedef struct {
     double max_abs_delta;     /* LcnCorrection::max_abs_delta (sparse_kernel.hpp:46) */
     double cond_estimate;     /* NystromFactors::cond_estimate (nystrom.hpp:37) */
     int store_fp64;
+    size_t streamed;          /* band entries one column pass streams (LCN iteration layout, >= nnz) */
 } lcn_op_info_t;
 
 typedef struct {

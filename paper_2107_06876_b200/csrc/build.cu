@@ -1304,19 +1304,239 @@ __global__ void __launch_bounds__(256) transpose_blocks_kernel(const double* __r
             }
         }
 }
+
+// ---- iteration layout (BandPanel, op.cuh) ----
+__global__ void iter_key_kernel(const uint32_t* __restrict__ b, const uint32_t* __restrict__ b0, long long n,
+                                unsigned long long r0, unsigned long long* __restrict__ key) {
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += 256LL * gridDim.x)
+        key[i] = static_cast<unsigned long long>(b[i]) * r0 + b0[i];
+}
+__global__ void inv_perm_kernel(const uint32_t* __restrict__ order, long long n, uint32_t* __restrict__ pos) {
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += 256LL * gridDim.x)
+        pos[order[i]] = static_cast<uint32_t>(i);
+}
+
+// One CTA per panel: stored entry (r, c) <- the fp64 block master at the pair
+// (stream point of row r, output point c); ROWS: stream = targets.
+template <bool ROWS>
+__global__ void __launch_bounds__(256) panel_gather_kernel(const double* __restrict__ master,
+                                                           const BandPanel* __restrict__ panels,
+                                                           const uint32_t* __restrict__ s_order,
+                                                           const uint32_t* __restrict__ o_order,
+                                                           const uint32_t* __restrict__ src_local,
+                                                           const uint32_t* __restrict__ tgt_local,
+                                                           const unsigned long long* __restrict__ blk_off,
+                                                           const uint32_t* __restrict__ tgt_start,
+                                                           float* __restrict__ out) {
+    const BandPanel P = panels[blockIdx.x];
+    const unsigned long long ms = row_stride(tgt_start[P.bucket + 1] - tgt_start[P.bucket]);
+    const double* A = master + blk_off[P.bucket];
+    const unsigned long long rs = row_stride(P.ow);
+    float* O = out + P.val_off;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t c0 = 0; c0 < P.ow; c0 += 32) {
+        const uint32_t c = c0 + lane;
+        const bool okc = c < P.ow;
+        const uint32_t po = okc ? o_order[P.o_base + c] : 0u;
+        const uint32_t lo = okc ? (ROWS ? src_local[po] : tgt_local[po]) : 0u;
+        for (uint32_t r = warp; r < P.ns; r += 8) {
+            const uint32_t sp = r < P.gap0 ? r : r + P.gapn;
+            const uint32_t ps = s_order[P.s_base + sp];
+            const uint32_t ls = ROWS ? tgt_local[ps] : src_local[ps];
+            if (okc) {
+                const double v = ROWS ? A[static_cast<unsigned long long>(lo) * ms + ls]
+                                      : A[static_cast<unsigned long long>(ls) * ms + lo];
+                O[r * rs + c] = static_cast<float>(v);
+            }
+        }
+    }
+}
+
+struct Group {
+    uint32_t b0, start, count;  // band-0 bucket, first local position, size
+};
+
+// runs of equal key in keys[lo, hi) (sorted), local positions relative to lo
+void key_groups(const std::vector<unsigned long long>& keys, size_t lo, size_t hi, unsigned long long r0,
+                std::vector<Group>& g) {
+    g.clear();
+    for (size_t i = lo; i < hi;) {
+        size_t j = i + 1;
+        while (j < hi && keys[j] == keys[i]) ++j;
+        g.push_back({static_cast<uint32_t>(keys[i] % r0), static_cast<uint32_t>(i - lo), static_cast<uint32_t>(j - i)});
+        i = j;
+    }
+}
+
+// Panels of one pass over one bucket: outputs `og`, stream groups `sg` (both in
+// band-0 order). An output group whose band-0 twin in the stream is big enough
+// gets its own panel without those rows; the rest share plain panels.
+void bucket_panels(uint32_t bucket, uint32_t s_base, uint32_t ns, uint32_t o_base, const std::vector<Group>& og,
+                   const std::vector<Group>& sg, uint32_t min_w, uint32_t min_area, std::vector<BandPanel>& out) {
+    size_t j = 0;
+    uint32_t run0 = 0, runw = 0;
+    auto flush = [&]() {
+        if (runw) out.push_back({0ull, bucket, s_base, ns, ns, 0u, o_base + run0, runw, 0u});
+        runw = 0;
+    };
+    for (const Group& g : og) {
+        while (j < sg.size() && sg[j].b0 < g.b0) ++j;
+        const bool twin = j < sg.size() && sg[j].b0 == g.b0;
+        const uint32_t same = twin ? sg[j].count : 0u;
+        if (twin && g.count >= min_w && static_cast<unsigned long long>(same) * g.count >= min_area) {
+            flush();
+            if (ns > same) out.push_back({0ull, bucket, s_base, ns - same, sg[j].start, same, o_base + g.start, g.count, 0u});
+            // ns == same: every pair of the group is in band 0; its outputs stay 0
+        } else {
+            if (!runw) run0 = g.start;
+            runw += g.count;
+        }
+    }
+    flush();
+}
+
+unsigned env_uint(const char* name, unsigned dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? static_cast<unsigned>(std::strtoul(v, nullptr, 10)) : dflt;
+}
+
+void iter_order(Ctx& ctx, const uint32_t* d_b, const uint32_t* d_b0, size_t n, unsigned long long r0,
+                unsigned long long range, DevBuf<uint32_t>& order, DevBuf<uint32_t>& pos,
+                std::vector<unsigned long long>& h_keys) {
+    cudaStream_t s = ctx.stream;
+    order.resize(n + 16);
+    order.zero(s);
+    pos.resize(n + 16);
+    pos.zero(s);
+    h_keys.assign(n, 0ull);
+    if (!n) return;
+    DevBuf<unsigned long long> key(n), skey(n);
+    DevBuf<uint32_t> iota(n);
+    const int g = static_cast<int>(std::min<long long>(ceil_div(n, 256), 8 * ctx.num_sms));
+    iter_key_kernel<<<g, 256, 0, s>>>(d_b, d_b0, n, r0, key.get());
+    iota32_kernel<<<ceil_div(n, 256), 256, 0, s>>>(iota.get(), n);
+    int end_bit = 1;
+    while (end_bit < 64 && (1ull << end_bit) < range) ++end_bit;
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, key.get(), skey.get(), iota.get(), order.get(), static_cast<int>(n), 0,
+                                    end_bit, s);
+    DevBuf<unsigned char> t(tmp);
+    cub::DeviceRadixSort::SortPairs(t.get(), tmp, key.get(), skey.get(), iota.get(), order.get(), static_cast<int>(n), 0,
+                                    end_bit, s);
+    inv_perm_kernel<<<g, 256, 0, s>>>(order.get(), n, pos.get());
+    skey.download(h_keys.data(), n, s);
+    LAUNCH_OK("iter_order");
+    ctx.sync();
+}
 }  // namespace
+
+// Iteration layout of every band (BandPanel, op.cuh). Compact bands (fp32
+// storage, bands after the first, LCN_PANELS != 0) get their own orders and
+// panel value arrays gathered from the fp64 master; everything else keeps the
+// bucket blocks with one plain panel per bucket.
+void build_iter_layout(Op& op) {
+    Ctx& ctx = *op.ctx;
+    PhaseTimer pt(ctx, "band iteration layout (panels)");
+    cudaStream_t s = ctx.stream;
+    const bool panels_on = env_uint("LCN_PANELS", 1) != 0;
+    const uint32_t min_w = env_uint("LCN_PANEL_W", 64), min_area = env_uint("LCN_PANEL_A", 4096);
+    op.iter.clear();
+    op.iter.resize(op.bands.size());
+    for (size_t b = 0; b < op.bands.size(); ++b) {
+        const Band& B = op.bands[b];
+        BandIter& I = op.iter[b];
+        I.compact = panels_on && !op.fp64 && b > 0 && B.n_work > 0;
+        if (!I.compact) {
+            I.so = B.src_order.get();
+            I.to = B.tgt_order.get();
+            I.sp = B.src_pos.get();
+            I.tp = B.tgt_pos.get();
+            for (int pass = 0; pass < 2; ++pass) {
+                const bool rows = pass == 0;
+                std::vector<BandPanel>& P = I.h_panels[pass];
+                P.clear();
+                for (size_t k = 0; k < B.nb; ++k) {
+                    const uint32_t nbk = B.h_src_start[k + 1] - B.h_src_start[k];
+                    const uint32_t mbk = B.h_tgt_start[k + 1] - B.h_tgt_start[k];
+                    if (!nbk || !mbk) continue;
+                    const uint32_t sl = rows ? mbk : nbk, ol = rows ? nbk : mbk;
+                    P.push_back({rows ? B.h_blkT_off[k] : B.h_blk_off[k], static_cast<uint32_t>(k),
+                                 rows ? B.h_tgt_start[k] : B.h_src_start[k], sl, sl, 0u,
+                                 rows ? B.h_src_start[k] : B.h_tgt_start[k], ol, 0u});
+                    I.real[pass] += static_cast<unsigned long long>(sl) * ol;
+                }
+                I.entries[pass] = rows ? B.entriesT : B.entries;
+                I.panels[pass].upload(P.data(), std::max<size_t>(P.size(), 1), s);
+            }
+            continue;
+        }
+        const Band& B0 = op.bands[0];
+        const unsigned long long r0 = std::max<size_t>(B0.nb, 1);
+        std::vector<unsigned long long> ks, kt;
+        iter_order(ctx, B.src_bucket.get(), B0.src_bucket.get(), op.n, r0, B.nb * r0, I.src_order, I.src_pos, ks);
+        iter_order(ctx, B.tgt_bucket.get(), B0.tgt_bucket.get(), op.m, r0, B.nb * r0, I.tgt_order, I.tgt_pos, kt);
+        I.so = I.src_order.get();
+        I.to = I.tgt_order.get();
+        I.sp = I.src_pos.get();
+        I.tp = I.tgt_pos.get();
+        std::vector<Group> sg, tg;
+        I.h_panels[0].clear();
+        I.h_panels[1].clear();
+        for (size_t k = 0; k < B.nb; ++k) {
+            const uint32_t s0 = B.h_src_start[k], s1 = B.h_src_start[k + 1];
+            const uint32_t t0 = B.h_tgt_start[k], t1 = B.h_tgt_start[k + 1];
+            if (s0 == s1 || t0 == t1) continue;
+            key_groups(ks, s0, s1, r0, sg);
+            key_groups(kt, t0, t1, r0, tg);
+            bucket_panels(static_cast<uint32_t>(k), t0, t1 - t0, s0, sg, tg, min_w, min_area, I.h_panels[0]);
+            bucket_panels(static_cast<uint32_t>(k), s0, s1 - s0, t0, tg, sg, min_w, min_area, I.h_panels[1]);
+        }
+        for (int pass = 0; pass < 2; ++pass) {
+            unsigned long long off = 0;
+            for (BandPanel& p : I.h_panels[pass]) {
+                p.val_off = off;
+                off = (off + static_cast<unsigned long long>(p.ns) * row_stride(p.ow) + 31ull) & ~31ull;
+                I.real[pass] += static_cast<unsigned long long>(p.ns) * p.ow;
+            }
+            I.entries[pass] = off;
+            const std::vector<BandPanel>& P = I.h_panels[pass];
+            I.panels[pass].upload(P.data(), std::max<size_t>(P.size(), 1), s);
+            DevBuf<float> v(std::max<unsigned long long>(off, 1));
+            v.zero(s);
+            if (!P.empty()) {
+                if (pass == 0)
+                    panel_gather_kernel<true><<<static_cast<unsigned>(P.size()), 256, 0, s>>>(
+                        op.val64[b].get(), I.panels[0].get(), I.to, I.so, B.src_local.get(), B.tgt_local.get(),
+                        B.blk_off.get(), B.tgt_start.get(), v.get());
+                else
+                    panel_gather_kernel<false><<<static_cast<unsigned>(P.size()), 256, 0, s>>>(
+                        op.val64[b].get(), I.panels[1].get(), I.so, I.to, B.src_local.get(), B.tgt_local.get(),
+                        B.blk_off.get(), B.tgt_start.get(), v.get());
+                LAUNCH_OK("panel_gather");
+            }
+            if (pass == 0) op.val32T[b] = std::move(v);
+            else op.val32[b] = std::move(v);
+        }
+    }
+    ctx.sync();
+}
 
 // Iteration copies (fp32 storage, fp64 accumulation;
 // fp64 storage in the exact mode). Low-rank factor rows are padded to
 // lp = round_up(l, 4) entries so each row starts 16-byte aligned.
 void finalize_storage(Op& op) {
     Ctx& ctx = *op.ctx;
+    PhaseTimer pt(ctx, "iteration storage (fp32 copies, transposes)");
     op.lp = (op.l + 3) & ~size_t(3);
+    // compact bands (build_iter_layout) get panel arrays instead of block copies
+    auto compact = [&](size_t b) {
+        return op.kind == 3 && !op.fp64 && b > 0 && op.bands[b].n_work > 0 && env_uint("LCN_PANELS", 1) != 0;
+    };
     if (!op.fp64) {
         op.val32.clear();
         for (size_t b = 0; b < op.bands.size(); ++b) {
             DevBuf<float> v;
-            to_f32(ctx, op.val64[b], v, op.bands[b].entries);
+            if (!compact(b)) to_f32(ctx, op.val64[b], v, op.bands[b].entries);
             op.val32.push_back(std::move(v));
         }
     }
@@ -1336,6 +1556,9 @@ void finalize_storage(Op& op) {
                         op.val64[b].get(), B.blk_off.get(), B.blkT_off.get(), B.src_start.get(), B.tgt_start.get(),
                         t.get());
                 op.val64T.push_back(std::move(t));
+            } else if (compact(b)) {
+                op.val32T.emplace_back();
+                continue;
             } else {
                 DevBuf<float> t(std::max<unsigned long long>(B.entriesT, 1));
                 t.zero(ctx.stream);
@@ -1347,6 +1570,7 @@ void finalize_storage(Op& op) {
             }
             LAUNCH_OK("transpose_blocks");
         }
+        build_iter_layout(op);
     }
     if (op.kind >= 2) {
         if (op.fp64) {

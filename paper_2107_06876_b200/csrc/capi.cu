@@ -664,6 +664,11 @@ int lcn_op_get_info(const lcn_op* op, lcn_op_info_t* info) {
     info->max_abs_delta = o.max_abs_delta;
     info->cond_estimate = o.cond;
     info->store_fp64 = o.fp64 ? 1 : 0;
+    info->streamed = o.stored;
+    if (o.kind == 3 && o.iter.size() == o.bands.size()) {
+        info->streamed = 0;
+        for (const auto& I : o.iter) info->streamed += I.real[1];
+    }
     return LCN_OK;
 }
 

@@ -34,6 +34,31 @@ struct BandSet {  // bucket ids of every band, for the cross-band dedup mask
     int bands;
 };
 
+// Iteration layout of the band streams (LCN). A panel is one output group of a
+// bucket block, stored as ns rows (stream side) x row_stride(ow) entries
+// starting at val_off. Stream row r is the bucket's stream position
+// r < gap0 ? r : r + gapn (from s_base); output c is o_order[o_base + c].
+// Bands after the first skip the pairs an earlier band already holds (the
+// support is the union of the bands, lsh.cpp:163-177): inside a bucket both
+// sides are ordered by their band-0 bucket, so the pairs of a target group
+// that band 0 owns are one contiguous run of sources, left out of the stored
+// rows (the gap). Small groups share plain panels that keep those entries as
+// zeros. The first band has one plain panel per bucket on the block layout.
+struct BandPanel {
+    unsigned long long val_off;
+    uint32_t bucket, s_base, ns, gap0, gapn, o_base, ow, pad;
+};
+
+struct BandIter {
+    DevBuf<BandPanel> panels[2];         // [0] row pass (streams targets), [1] column pass (streams sources)
+    std::vector<BandPanel> h_panels[2];
+    DevBuf<uint32_t> src_order, tgt_order, src_pos, tgt_pos;  // compact bands: (bucket, band-0 bucket, index) order
+    const uint32_t *so = nullptr, *to = nullptr, *sp = nullptr, *tp = nullptr;  // orders the kernels use
+    bool compact = false;
+    unsigned long long entries[2] = {0, 0};  // stored entries per pass (padded)
+    unsigned long long real[2] = {0, 0};     // sum ns * ow per pass
+};
+
 struct Solver;
 
 struct Op {
@@ -56,6 +81,9 @@ struct Op {
     std::vector<DevBuf<float>> val32T;
     std::vector<DevBuf<double>> val64T;
     std::vector<DevBuf<double>> logk64;   // lcn: log K^sp at stored entries
+    // lcn: iteration layout per band; in fp32 storage the compact bands' val32
+    // (column pass) and val32T (row pass) hold their panels instead of blocks
+    std::vector<BandIter> iter;
     // dense operator (kind 0, the configs[2] anchor): log K = 0 - c * (1/lambda)
     // n x m row-major (fp64 master) and the iteration copies, plus transposes
     DevBuf<double> dk64, dk64T;

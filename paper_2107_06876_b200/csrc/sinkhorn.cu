@@ -398,9 +398,16 @@ struct BandSmem {
     uint32_t last;              // this CTA combines a split output
 };
 
+// One work item: stream rows [s0, s0 + ns) x outputs [o0, o0 + ow) of a panel,
+// resolved on the host so the producers need no panel lookups.
 struct BandItem {
-    uint32_t b, s0, ns, o0, ow, split;  // split = sid << 8 | piece, or ~0u
-    uint32_t pad[2];
+    unsigned long long off;  // first stored entry (panel val_off + s0 * rs + o0)
+    uint32_t rs;             // panel row stride (entries)
+    uint32_t ns, ow, split;  // stream rows, outputs; split = sid << 8 | piece, or ~0u
+    uint32_t va;             // bucket-ordered stream position of stored row s0
+    uint32_t g0;             // stored rows of the item before the gap
+    uint32_t gapn;           // stream rows in the gap
+    uint32_t oa;             // o_order index of output o0
 };
 
 struct BandWork {
@@ -445,8 +452,8 @@ __device__ __forceinline__ void band_combine(BandSmem& sm, const BandWork& wk, c
 // bucket-ordered copy of the stream side's log vector (log t for the row pass,
 // log s for the column pass), written by the low-rank pass that produced it.
 template <typename T, bool ROWS>
-__global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const DevState* __restrict__ st, BandView bv,
-                                                                      BandWork wk, const T* __restrict__ vals,
+__global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const DevState* __restrict__ st,
+                                                                      const uint32_t* __restrict__ o_order, BandWork wk, const T* __restrict__ vals,
                                                                       const double* __restrict__ logv,
                                                                       double* __restrict__ corr) {
     if (st->done) return;
@@ -456,11 +463,6 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
     const uint32_t i_beg = wk.cta_off[blockIdx.x], i_end = wk.cta_off[blockIdx.x + 1];
     if (i_beg == i_end) return;
     const double H = ROWS ? st->H_t : st->H_s;
-    // stream side / output side of this pass
-    const uint32_t* s_start = ROWS ? bv.tgt_start : bv.src_start;
-    const uint32_t* o_start = ROWS ? bv.src_start : bv.tgt_start;
-    const uint32_t* o_order = ROWS ? bv.src_order : bv.tgt_order;
-    const unsigned long long* boff = ROWS ? bv.blkT_off : bv.blk_off;
     if (tid == 0) {
         for (int k = 0; k < kBandStages; ++k) {
             mbar_init(&sm.full[k], 1);
@@ -481,10 +483,10 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
             bool wrapped = false;
             for (uint32_t it = i_beg; it < i_end; ++it) {
                 const BandItem item = wk.items[it];
-                const uint32_t rs = static_cast<uint32_t>(row_stride(o_start[item.b + 1] - o_start[item.b]));
+                const uint32_t rs = item.rs;
                 const uint32_t ws = static_cast<uint32_t>(row_stride(item.ow));  // item row width in the ring
                 const int R = band_rows_per_stage<T>(ws);
-                const T* blk = vals + boff[item.b] + static_cast<unsigned long long>(item.s0) * rs + item.o0;
+                const T* blk = vals + item.off;
                 for (uint32_t r0 = 0; r0 < item.ns; r0 += R) {
                     const uint32_t nr = item.ns - r0 < static_cast<uint32_t>(R) ? item.ns - r0 : static_cast<uint32_t>(R);
                     if (wrapped) mbar_wait(&sm.empty[stage], phase ^ 1u);
@@ -513,18 +515,32 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
         int kb = 0;
         for (uint32_t it = i_beg; it < i_end; ++it, ++kb) {
             const BandItem item = wk.items[it];
-            const uint32_t v0 = s_start[item.b] + item.s0;
-            const uint32_t o0 = o_start[item.b] + item.o0;
+            // stored row c of the item is stream position c (c < g0) or c + gapn
+            const double* va = logv + item.va;
+            const double* vb = va + item.gapn;
             const int slot = kb & 1;
             if (kb >= 2) mbar_wait(&sm.vempty[slot], ((kb >> 1) - 1) & 1);
-            if constexpr (sizeof(T) == 4) {
-                // fp32 storage: the scalings enter fp32 products (values in (0, 1])
-                float* vf = reinterpret_cast<float*>(sm.vec[slot]);
-                for (uint32_t c = lane; c < item.ns; c += 32) vf[c] = static_cast<float>(exp(logv[v0 + c] - H));
-            } else {
-                for (uint32_t c = lane; c < item.ns; c += 32) sm.vec[slot][c] = exp(logv[v0 + c] - H);
+            // 4 independent loads in flight per lane before the exps (one warp
+            // resolves every stream row of the item; L2 latency bound otherwise)
+            for (uint32_t c0 = lane; c0 < item.ns; c0 += 128) {
+                double x[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t c = c0 + 32u * k;
+                    x[k] = c < item.ns ? (c < item.g0 ? va[c] : vb[c]) : 0.0;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t c = c0 + 32u * k;
+                    if (c < item.ns) {
+                        if constexpr (sizeof(T) == 4)  // fp32 storage: the scalings enter fp32 products
+                            reinterpret_cast<float*>(sm.vec[slot])[c] = static_cast<float>(exp(x[k] - H));
+                        else
+                            sm.vec[slot][c] = exp(x[k] - H);
+                    }
+                }
             }
-            for (uint32_t c = lane; c < item.ow; c += 32) sm.out[slot][c] = o_order[o0 + c];
+            for (uint32_t c = lane; c < item.ow; c += 32) sm.out[slot][c] = o_order[item.oa + c];
             if (lane == 0) {
                 ItemMeta mt;
                 mt.ns = item.ns;
@@ -1400,8 +1416,9 @@ struct Solver {
             std::vector<uint32_t> w(B.n_work);
             if (B.n_work) B.work.download(w.data(), B.n_work, s);
             ctx.sync();
-            plans[0].push_back(plan_pass(B, owned_buckets(B, w, true), true));
-            plans[1].push_back(plan_pass(B, owned_buckets(B, w, false), false));
+            const BandIter& I = op.iter[&B - op.bands.data()];
+            plans[0].push_back(plan_pass(B, I, owned_buckets(B, w, true), true));
+            plans[1].push_back(plan_pass(B, I, owned_buckets(B, w, false), false));
         }
         ctx.sync();
     }
@@ -1434,18 +1451,23 @@ struct Solver {
         return mine;
     }
 
-    // Items of one pass: per bucket, output tiles of <= kBandVec columns and
-    // stream pieces (multiples of 8 rows, <= kBandVec, sized so no piece
-    // exceeds half a CTA's share), then longest-processing-time greedy.
-    PassPlan plan_pass(const Band& B, const std::vector<uint32_t>& w, bool rows) {
+    // Items of one pass: per panel of an owned bucket (BandPanel, op.cuh),
+    // output tiles of <= kBandVec columns and stream pieces (multiples of 8
+    // rows, <= kBandVec, sized so no piece exceeds half a CTA's share), then
+    // longest-processing-time greedy.
+    PassPlan plan_pass(const Band& B, const BandIter& I, const std::vector<uint32_t>& owned, bool rows) {
         const size_t esz = op.fp64 ? 8 : 4;
         // cost model (bytes): streamed bytes + per-row and per-item overheads
         auto cost_of = [&](size_t nr, size_t ws) { return double(nr * ws * esz) + 64.0 * nr + 4096.0; };
+        std::vector<char> mine(B.nb, 0);
+        for (uint32_t k : owned) mine[k] = 1;
+        const std::vector<BandPanel>& panels = I.h_panels[rows ? 0 : 1];
+        std::vector<uint32_t> w;  // panels of the owned buckets
+        for (size_t p = 0; p < panels.size(); ++p)
+            if (mine[panels[p].bucket]) w.push_back(static_cast<uint32_t>(p));
         auto lens = [&](uint32_t k, size_t& sl, size_t& ol) {
-            const size_t nb = B.h_src_start[k + 1] - B.h_src_start[k];
-            const size_t mb = B.h_tgt_start[k + 1] - B.h_tgt_start[k];
-            sl = rows ? mb : nb;
-            ol = rows ? nb : mb;
+            sl = panels[k].ns;
+            ol = panels[k].ow;
         };
         double total = 0.0;
         for (uint32_t k : w) {
@@ -1463,7 +1485,7 @@ struct Solver {
             lens(k, sl, ol);
             if (sl == 0 || ol == 0) continue;
             const size_t rs = row_stride(ol);
-            const size_t nct = ceil_div(ol, kBandVec);  // output tiles
+            const size_t nct = ceil_div(ol, kBandVec);  // output tiles (a bucket wider than kBandVec)
             const size_t wmax = std::min<size_t>(rs, kBandVec);
             size_t K = static_cast<size_t>(std::ceil(cost_of(sl, wmax) / cap));
             K = std::max<size_t>(K, ceil_div(sl, kBandVec));
@@ -1481,12 +1503,16 @@ struct Solver {
                 }
                 for (size_t j = 0; j < K; ++j) {
                     const size_t s0 = j * pr, ns = std::min(pr, sl - s0);
+                    const BandPanel& pn = panels[k];
                     BandItem it{};
-                    it.b = k;
-                    it.s0 = static_cast<uint32_t>(s0);
+                    it.off = pn.val_off + s0 * rs + o0;
+                    it.rs = static_cast<uint32_t>(rs);
                     it.ns = static_cast<uint32_t>(ns);
-                    it.o0 = static_cast<uint32_t>(o0);
                     it.ow = static_cast<uint32_t>(ow);
+                    it.va = pn.s_base + static_cast<uint32_t>(s0);  // rows from g0 on read va[c + gapn]
+                    it.g0 = s0 >= pn.gap0 ? 0u : static_cast<uint32_t>(std::min<size_t>(pn.gap0 - s0, ns));
+                    it.gapn = pn.gapn;
+                    it.oa = pn.o_base + static_cast<uint32_t>(o0);
                     it.split = K > 1 ? (sid << 8) | static_cast<uint32_t>(j) : 0xffffffffu;
                     pieces.push_back({it, cost_of(ns, row_stride(ow))});
                 }
@@ -1703,8 +1729,8 @@ struct Solver {
             PassPlan& P = plans[ROWS ? 0 : 1][b];
             if (P.nitems)
                 band_stream_kernel<T, ROWS><<<band_grid, kThreads + 64, sizeof(BandSmem), s>>>(
-                    st.get(), op.view(b), P.work(), ROWS ? band_valsT<T>(b) : band_vals<T>(b), logvp[b].get(),
-                    corr[b].get());
+                    st.get(), ROWS ? op.iter[b].so : op.iter[b].to, P.work(),
+                    ROWS ? band_valsT<T>(b) : band_vals<T>(b), logvp[b].get(), corr[b].get());
         }
     }
     template <typename T>
@@ -1715,7 +1741,7 @@ struct Solver {
         a.nperm = 0;
         if (op.kind != 3) return;
         for (size_t b = 0; b < op.bands.size(); ++b) {
-            a.pos[a.nperm] = side == 0 ? op.bands[b].src_pos.get() : op.bands[b].tgt_pos.get();
+            a.pos[a.nperm] = side == 0 ? op.iter[b].sp : op.iter[b].tp;
             a.perm[a.nperm++] = side == 0 ? lsp[parity][b].get() : ltp[b].get();
         }
     }
@@ -1723,7 +1749,7 @@ struct Solver {
         if (op.kind != 3) return;
         for (size_t b = 0; b < op.bands.size(); ++b)
             perm_scatter_kernel<<<ceil_div(len, 256), 256, 0, s>>>(
-                v, len, side == 0 ? op.bands[b].src_pos.get() : op.bands[b].tgt_pos.get(),
+                v, len, side == 0 ? op.iter[b].sp : op.iter[b].tp,
                 side == 0 ? lsp[parity][b].get() : ltp[b].get());
     }
     void set_corr(PassArgs& a, int side) {

@@ -54,6 +54,7 @@ _STATUS = {1: DimensionError, 2: InvalidArgument, 3: StabilizationError, 4: Nega
 EUCLIDEAN, NEGATIVE_DOT, COSINE_DERIVED, SQEUCLIDEAN = 0, 1, 2, 3
 LANDMARK_KMEANS, LANDMARK_KMEANSPP = 0, 1
 LSH_CROSS_POLYTOPE, LSH_KMEANS, LSH_HIERARCHICAL_KMEANS = 0, 1, 2  # LshScheme (lsh.hpp:13-17)
+ABI_VERSION = 3  # include/lcn_b200.h LCN_B200_ABI_VERSION
 KIND_DENSE, KIND_SPARSE, KIND_NYSTROM, KIND_LCN = 0, 1, 2, 3
 _KIND_NAMES = {0: "dense", 1: "sparse", 2: "nystrom", 3: "lcn"}
 
@@ -70,7 +71,8 @@ class _SinkOpts(C.Structure):
 class _OpInfo(C.Structure):
     _fields_ = [("kind", C.c_int), ("n", C.c_size_t), ("m", C.c_size_t), ("l", C.c_size_t), ("d", C.c_size_t),
                 ("bands", C.c_int), ("nnz", C.c_size_t), ("stored", C.c_size_t), ("lam", C.c_double),
-                ("max_abs_delta", C.c_double), ("cond_estimate", C.c_double), ("store_fp64", C.c_int)]
+                ("max_abs_delta", C.c_double), ("cond_estimate", C.c_double), ("store_fp64", C.c_int),
+                ("streamed", C.c_size_t)]
 
 
 class _ResInfo(C.Structure):
@@ -135,6 +137,8 @@ def library() -> C.CDLL:
             f = getattr(lib, name)
             f.argtypes = args
             f.restype = res
+        if lib.lcn_abi_version() != ABI_VERSION:
+            raise ImportError(f"{LIB_PATH}: ABI {lib.lcn_abi_version()}, this mirror is ABI {ABI_VERSION} (rebuild)")
         _lib = lib
     return _lib
 
@@ -475,6 +479,7 @@ class KernelOperator:
     l = property(lambda s: s.info.l)
     nnz = property(lambda s: s.info.nnz)
     stored = property(lambda s: s.info.stored)
+    streamed = property(lambda s: s.info.streamed)
     lam = property(lambda s: s.info.lam)
     max_abs_delta = property(lambda s: s.info.max_abs_delta)
     cond_estimate = property(lambda s: s.info.cond_estimate)

@@ -18,6 +18,13 @@ dp = torch.from_numpy(pr.p.astype(np.float32)).cuda()
 dq = torch.from_numpy(pr.q.astype(np.float32)).cuda()
 torch.cuda.synchronize()
 cfg = lcn.LshConfig(pr.bands, 1, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
+for _b in range(int(os.environ.get("PROBE_BUILDS", "1")) - 1):  # warm-up builds (pool, first touch)
+    if os.environ.get("LCN_TIMING"):
+        print(f"---- warm-up build {_b}", file=sys.stderr, flush=True)
+    lcn.KernelOperator.from_device(ctx, dp.data_ptr(), pr.n, dq.data_ptr(), pr.m, pr.d, pr.cost, pr.lam_eff, cfg,
+                                   pr.landmarks, lcn.LANDMARK_KMEANS, pr.landmark_seed)
+if os.environ.get("LCN_TIMING"):
+    print("---- timed build", file=sys.stderr, flush=True)
 t = time.time()
 op = lcn.KernelOperator.from_device(ctx, dp.data_ptr(), pr.n, dq.data_ptr(), pr.m, pr.d, pr.cost, pr.lam_eff, cfg,
                                     pr.landmarks, lcn.LANDMARK_KMEANS, pr.landmark_seed)

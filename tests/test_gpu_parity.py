@@ -299,3 +299,43 @@ def test_grad_cost(ref):
     assert rel(g, rg) <= 1e-8
     with pytest.raises(lcn.InvalidArgument):
         lcn.grad_cost(dres, dop, 1)
+
+
+@pytest.mark.parametrize("layout", [{"LCN_PANEL_W": "1", "LCN_PANEL_A": "0"}, {},
+                                    {"LCN_PANEL_W": "1000000"}, {"LCN_PANELS": "0"}])
+@pytest.mark.parametrize("shape", ["c3", "three_bands", "wide"])
+def test_lcn_panel_layouts(ref, monkeypatch, layout, shape):
+    """The band streams of later bands skip the pairs band 0 already holds
+    (gapped panels, BandPanel in op.cuh). Every panel policy — each band-0
+    group its own panel, the default thresholds, all plain panels, the block
+    layout — must give the reference's distance and support plan; `wide`
+    forces gapped panels taller than one stream piece (split combines)."""
+    import dataclasses
+    for k, v in layout.items():
+        monkeypatch.setenv(k, v)
+    if shape == "c3":
+        pr = configs.config3(0.02)
+    elif shape == "three_bands":
+        pr = dataclasses.replace(configs.config3(0.01), bands=3)
+    else:
+        pr = dataclasses.replace(configs.config3(0.004), bands=2, buckets=3, landmarks=32, iters=30)
+    c = lcn.Context(0, store_fp64=False)
+    cfg = lcn.LshConfig(pr.bands, 1, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
+    op = lcn.KernelOperator.lcn_lsh(c, pr.p, pr.q, pr.cost, pr.lam_eff, cfg, pr.landmarks, lcn.LANDMARK_KMEANS,
+                                    pr.landmark_seed)
+    pairs = ref.lsh_pairs(pr.p, pr.q, pr.bands, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
+    rop = ref.op_lcn(pr.p, pr.q, pr.cost, pr.lam_eff, pairs, pr.landmarks, 0, pr.landmark_seed)
+    if layout.get("LCN_PANELS") == "0" or layout.get("LCN_PANEL_W") == "1000000":
+        assert op.streamed == op.stored
+    else:
+        assert op.nnz <= op.streamed < op.stored
+    pm, qm = pr.marginals()
+    res = lcn.sinkhorn(op, pm, qm, lcn.SinkhornOptions(tol=0.0, max_iters=pr.iters))
+    rres = rop.sinkhorn(pm, qm, tol=0.0, max_iters=pr.iters)
+    assert rel(res.distance, rres.distance) <= REL_FP32
+    assert rel(res.sp_vals, rres.sp_vals) <= REL_FP32
+    # log_matvec goes through the same band streams (both orientations)
+    # (log domain: absolute 1e-4 = relative 1e-4 of K t; entries near log 1 = 0)
+    for mine, theirs in [(op.log_matvec(rres.log_t), rop.log_matvec(rres.log_t)),
+                         (op.log_matvec_t(rres.log_s), rop.log_matvec(rres.log_s, transposed=True))]:
+        assert np.max(np.abs(mine - theirs) / np.maximum(np.abs(theirs), 1.0)) <= REL_FP32
