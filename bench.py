@@ -237,7 +237,35 @@ def union_us(iv):
     return tot
 
 
-def distance_roofline(iv, n, m, d, bands, buckets, landmarks, iters):
+def measure_tf32_peak(dev):
+    """Dense TF32 tensor-core rate on this GPU: cuBLAS fp32 GEMM 8192^3 with
+    TF32 allowed (torch.matmul), best of 10 after warm-up, CUDA events.
+    MEASURED_PEAKS.json has no TF32 entry (measure it)."""
+    import torch
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        g = torch.Generator(device=dev).manual_seed(0)
+        a = torch.randn(8192, 8192, device=dev, generator=g)
+        b = torch.randn(8192, 8192, device=dev, generator=g)
+        c = torch.empty(8192, 8192, device=dev)
+        for _ in range(3):
+            torch.matmul(a, b, out=c)
+        best = float("inf")
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b, out=c)
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        del a, b, c
+        return 2.0 * 8192 ** 3 / (best * 1e-3) / 1e12
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
+def distance_roofline(iv, n, m, d, bands, buckets, landmarks, iters, tf32_peak=None):
     """Tensor-core roofline of the distance blocks (the tcgen05 3xTF32
     assignment filter of the k-means in the LSH and landmark build): MMA work
     of one build = per assign launch 2 N_pad K_pad 128 x 3 (hi.hi, hi.lo,
@@ -251,10 +279,14 @@ def distance_roofline(iv, n, m, d, bands, buckets, landmarks, iters):
     mma = sum(2.0 * npad * (-(-k // 64) * 64) * 128 * 3 for k in launches)
     fp32 = sum(2.0 * N * k * d for k in launches)
     t = union_us(iv) * 1e-6
-    peak = 1100.0  # TF32 dense, B200_PROFILING.md (no measured TF32 peak in MEASURED_PEAKS.json)
+    nominal = 1100.0  # TF32 dense, B200_PROFILING.md
+    peak = tf32_peak if tf32_peak else nominal
+    kind = ("measured: cuBLAS TF32 GEMM 8192^3 (torch.matmul, allow_tf32), best of 10, this run"
+            if tf32_peak else "guide (tf32 dense)")
     ach = mma / t / 1e12
     return {"bound": "tensor", "kernel": "assign_filter_tc_kernel (tcgen05.mma kind::tf32, 3xTF32)",
-            "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "peak_kind": "guide (tf32 dense)",
+            "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "peak_kind": kind,
+            "nominal_peak": nominal, "frac_vs_nominal": ach / nominal,
             "fp32_accurate_achieved": fp32 / t / 1e12, "fp32_accurate_peak": peak / 3,
             "launches": len(iv), "device_ms": t * 1e3,
             "work": "per build: bands x (iters + 1) assigns of n+m points to the buckets + 11 to the "
@@ -300,6 +332,50 @@ def batched_c4(lcn, ctx, with_cpu):
                                        "sample": f"the first {k_s} problems of the batch, {tw:.2f} s"}
         except Exception as ex:
             out["cpu_baseline"] = {"value": None, "sample": f"unavailable: {ex}"}
+    return out
+
+
+def dense_anchor(lcn, ctx, peak_gbs):
+    """configs[2]: the dense operator on configs[1]'s points (n = m = 20000,
+    d = 300, L2, lambda = 0.05): exact fp64 log K built on the device, 50
+    log-domain iterations streaming the fp32 copy (dense_lse_tma_kernel, both
+    orientations), device-timed; and the approximation error of the LCN and
+    sparse operators of configs[1] against its distance."""
+    import torch
+    from paper_2107_06876_b200 import configs
+    pr = configs.config1(1.0)
+    dp = torch.from_numpy(pr.p.astype(np.float32)).cuda()
+    dq = torch.from_numpy(pr.q.astype(np.float32)).cuda()
+    pm, qm = pr.marginals()
+    op = lcn.KernelOperator.dense_device(ctx, dp.data_ptr(), pr.n, dq.data_ptr(), pr.m, pr.d, pr.cost, pr.lam_eff)
+    opts = lcn.SinkhornOptions(tol=0.0, max_iters=pr.iters, want_plan=False, check_support=False)
+    lcn.sinkhorn(op, pm, qm, opts)  # warm-up
+    runs = [lcn.sinkhorn(op, pm, qm, opts) for _ in range(3)]
+    ms_it = float(np.median([r.device_ms for r in runs])) / pr.iters
+    dense_d = runs[0].distance
+    b_it = 2 * 4 * pr.n * pr.m  # fp32 log K read once per half-iteration
+    out = {"config": "configs[2]: dense, configs[1] points (n = m = 20000, d = 300), L2, lambda = 0.05, 50 iterations",
+           "ms_per_iteration": ms_it, "iters_per_s": 1e3 / ms_it,
+           "roofline": {"bound": "hbm", "achieved": b_it / (ms_it * 1e-3) / 1e9, "peak": peak_gbs, "unit": "GB/s",
+                        "frac": b_it / (ms_it * 1e-3) / 1e9 / peak_gbs,
+                        "algorithmic_bytes_per_iteration": b_it, "kernel": "dense_lse_tma_kernel"},
+           "distance_dense": dense_d}
+    del op
+    cfg = lcn.LshConfig(pr.bands, 1, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
+    lop = lcn.KernelOperator.lcn_lsh(ctx, pr.p, pr.q, pr.cost, pr.lam_eff, cfg, pr.landmarks, lcn.LANDMARK_KMEANS,
+                                     pr.landmark_seed)
+    ld = lcn.sinkhorn(lop, pm, qm, opts).distance
+    out["distance_lcn"] = ld
+    out["rel_error_lcn"] = abs(ld - dense_d) / abs(dense_d)
+    del lop
+    try:
+        sop = lcn.KernelOperator.sparse_lsh(ctx, pr.p, pr.q, pr.cost, pr.lam_eff, cfg)
+        sd = lcn.sinkhorn(sop, pm, qm, opts).distance
+        out["distance_sparse"] = sd
+        out["rel_error_sparse"] = abs(sd - dense_d) / abs(dense_d)
+    except lcn.Error as ex:  # rows without LSH neighbours (SURVEY.md App. B item 3), as in the reference
+        out["distance_sparse"] = None
+        out["sparse_error"] = f"{type(ex).__name__}: {ex}"
     return out
 
 
@@ -435,6 +511,7 @@ def run_ours(args, rank, world, local_rank):
     # ---- e2e through the C-ABI from pinned host buffers ----------------------
     e2e = None
     dist_roof = None
+    dist_iv = None
     if not args.no_e2e:
         del op
         torch.cuda.synchronize()
@@ -461,7 +538,7 @@ def run_ours(args, rank, world, local_rank):
                 holder = []
                 try:
                     iv = kernel_intervals(lambda: holder.append(build2()), "assign_filter_tc_kernel")
-                    dist_roof = distance_roofline(iv, n, m, d, pr.bands, pr.buckets, l, pr.kmeans_iters)
+                    dist_iv = iv  # roofline computed after the timed regions (TF32 peak GEMM)
                 except Exception as ex:  # profiler unavailable: report none
                     print("distance roofline unavailable:", ex, file=sys.stderr)
                 op2 = holder[0] if holder else build2()
@@ -507,6 +584,19 @@ def run_ours(args, rank, world, local_rank):
             c4 = batched_c4(lcn, ctx, not args.no_cpu)
         except Exception as ex:
             c4 = {"unavailable": str(ex)}
+    if dist_iv is not None:
+        tf32 = None
+        try:
+            tf32 = measure_tf32_peak(dev)
+        except Exception as ex:
+            print("tf32 peak measurement failed:", ex, file=sys.stderr)
+        dist_roof = distance_roofline(dist_iv, n, m, d, pr.bands, pr.buckets, l, pr.kmeans_iters, tf32)
+    anchor = None
+    if rank == 0 and not args.no_dense:
+        try:
+            anchor = dense_anchor(lcn, ctx, hbm)
+        except Exception as ex:
+            anchor = {"unavailable": str(ex)}
 
     gpu_launches = args.steps * launches_per_step if launches_per_step else None
     if rank == 0:
@@ -535,6 +625,7 @@ def run_ours(args, rank, world, local_rank):
                                        "ms_per_iteration": t_iter * 1e3},
                 "distance_roofline": dist_roof,
                 "batched_c4": c4,
+                "dense_anchor": anchor,
                 "phases_ms_per_iteration": per_it,
                 "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": gpu_launches}
         emit(line)
@@ -565,8 +656,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--e2e-warmup", type=int, default=1)
+    ap.add_argument("--e2e-warmup", type=int, default=2)
     ap.add_argument("--no-c4", action="store_true", help="skip the configs[4] batched-problems line")
+    ap.add_argument("--no-dense", action="store_true", help="skip the configs[2] dense-anchor object")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sharded", action="store_true",

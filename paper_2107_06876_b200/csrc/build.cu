@@ -1466,7 +1466,8 @@ void build_iter_layout(Op& op) {
                     I.real[pass] += static_cast<unsigned long long>(sl) * ol;
                 }
                 I.entries[pass] = rows ? B.entriesT : B.entries;
-                I.panels[pass].upload(P.data(), std::max<size_t>(P.size(), 1), s);
+                if (P.empty()) I.panels[pass].resize(1);  // a band without any two-sided bucket
+                else I.panels[pass].upload(P.data(), P.size(), s);
             }
             continue;
         }
@@ -1500,7 +1501,8 @@ void build_iter_layout(Op& op) {
             }
             I.entries[pass] = off;
             const std::vector<BandPanel>& P = I.h_panels[pass];
-            I.panels[pass].upload(P.data(), std::max<size_t>(P.size(), 1), s);
+            if (P.empty()) I.panels[pass].resize(1);
+            else I.panels[pass].upload(P.data(), P.size(), s);
             DevBuf<float> v(std::max<unsigned long long>(off, 1));
             v.zero(s);
             if (!P.empty()) {

@@ -645,7 +645,13 @@ int lcn_op_destroy(lcn_op* op) {
     if (!op) return LCN_OK;
     cudaSetDevice(op->o.ctx->device);
     cudaDeviceSynchronize();  // any stream may still read the operator
+    // free on the context's stream: the pool hands the blocks straight back to
+    // the next build on that stream (frees on another stream are only reused
+    // opportunistically, and the pool grows instead)
+    cudaStream_t saved = alloc_stream();
+    alloc_stream() = op->o.ctx->stream;
     delete op;
+    alloc_stream() = saved;
     return LCN_OK;
 }
 

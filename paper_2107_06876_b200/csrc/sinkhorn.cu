@@ -301,6 +301,142 @@ __global__ void __launch_bounds__(256) dense_lse_kernel(const DevState* __restri
     }
 }
 
+__device__ __forceinline__ float ex2_ftz(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// fp32 storage, cols % 4 == 0: the same (max, sum) pairs, streamed through
+// shared memory by the bulk-copy engine. Persistent CTAs walk (row group of 8,
+// column chunk of 512) units in order; warp 8 bulk-copies each unit's 8 row
+// chunks and the matching log v chunk into a ring of kLseStages stages
+// (mbarrier transaction counts), so ~80 KB per CTA are in flight without
+// registers. Consumer thread t owns column quad t & 127 of rows
+// 4 (t >> 7) .. 4 (t >> 7) + 3 and keeps an online (max, sum) per row in fp32;
+// at the end of a row group the 128 threads of each row set merge them.
+constexpr int kLseChunk = 512;   // columns per unit
+constexpr int kLseStages = 4;
+struct LseSmem {
+    float rows[kLseStages][kDenseRows][kLseChunk];
+    double lv[kLseStages][kLseChunk];
+    double wm[kWarps][4], ws[kWarps][4];
+    uint64_t full[kLseStages], empty[kLseStages];
+};
+
+__global__ void __launch_bounds__(kThreads + 32, 2) dense_lse_tma_kernel(const DevState* __restrict__ st,
+                                                                         const float* __restrict__ logk,
+                                                                         long long rows, long long cols,
+                                                                         const double* __restrict__ logv,
+                                                                         double* __restrict__ M, double* __restrict__ S) {
+    if (st->done) return;
+    extern __shared__ __align__(128) unsigned char dyn[];
+    LseSmem& sm = *reinterpret_cast<LseSmem*>(dyn);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long groups = (rows + kDenseRows - 1) / kDenseRows;
+    const int nch = static_cast<int>((cols + kLseChunk - 1) / kLseChunk);
+    if (tid == 0) {
+        for (int k = 0; k < kLseStages; ++k) {
+            mbar_init(&sm.full[k], 1);
+            mbar_init(&sm.empty[k], kWarps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == kWarps) {  // producer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            bool wrapped = false;
+            for (long long g = blockIdx.x; g < groups; g += gridDim.x) {
+                const long long i0 = g * kDenseRows;
+                const int nr = static_cast<int>(rows - i0 < kDenseRows ? rows - i0 : kDenseRows);
+                for (int c = 0; c < nch; ++c) {
+                    const long long j0 = static_cast<long long>(c) * kLseChunk;
+                    const uint32_t w = static_cast<uint32_t>(cols - j0 < kLseChunk ? cols - j0 : kLseChunk);
+                    if (wrapped) mbar_wait(&sm.empty[stage], phase ^ 1u);
+                    mbar_arrive_expect_tx(&sm.full[stage], w * (4u * nr + 8u));
+                    for (int r = 0; r < nr; ++r) bulk_g2s(sm.rows[stage][r], logk + (i0 + r) * cols + j0, w * 4u, &sm.full[stage]);
+                    bulk_g2s(sm.lv[stage], logv + j0, w * 8u, &sm.full[stage]);
+                    if (++stage == kLseStages) {
+                        stage = 0;
+                        phase ^= 1u;
+                        wrapped = true;
+                    }
+                }
+            }
+        }
+        return;
+    }
+    constexpr float kL2E = 1.4426950408889634f;
+    const int qi = tid & 127, h = tid >> 7;  // column quad, row set
+    int stage = 0;
+    uint32_t phase = 0;
+    for (long long g = blockIdx.x; g < groups; g += gridDim.x) {
+        const long long i0 = g * kDenseRows;
+        const int nr = static_cast<int>(rows - i0 < kDenseRows ? rows - i0 : kDenseRows);
+        float mf[4], sf[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) { mf[r] = -INFINITY; sf[r] = 0.0f; }
+        for (int c = 0; c < nch; ++c) {
+            const long long j0 = static_cast<long long>(c) * kLseChunk;
+            const int w = static_cast<int>(cols - j0 < kLseChunk ? cols - j0 : kLseChunk);
+            mbar_wait(&sm.full[stage], phase);
+            if (4 * qi < w) {
+                const double2 a0 = *reinterpret_cast<const double2*>(&sm.lv[stage][4 * qi]);
+                const double2 a1 = *reinterpret_cast<const double2*>(&sm.lv[stage][4 * qi + 2]);
+                const float l0 = static_cast<float>(a0.x), l1 = static_cast<float>(a0.y);
+                const float l2 = static_cast<float>(a1.x), l3 = static_cast<float>(a1.y);
+                // rows past nr (last group) reduce stale stage data; their pairs are dropped
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    {
+                        const float4 x = *reinterpret_cast<const float4*>(&sm.rows[stage][4 * h + r][4 * qi]);
+                        const float v0 = x.x + l0, v1 = x.y + l1, v2 = x.z + l2, v3 = x.w + l3;
+                        const float bm = fmaxf(fmaxf(v0, v1), fmaxf(v2, v3));
+                        if (bm > mf[r]) {
+                            sf[r] *= ex2_ftz((mf[r] - bm) * kL2E);  // 2^-inf = 0 for the first batch
+                            mf[r] = bm;
+                        }
+                        if (mf[r] != -INFINITY) {
+                            const float ms = mf[r] * kL2E;
+                            sf[r] += (ex2_ftz(fmaf(v0, kL2E, -ms)) + ex2_ftz(fmaf(v1, kL2E, -ms))) +
+                                     (ex2_ftz(fmaf(v2, kL2E, -ms)) + ex2_ftz(fmaf(v3, kL2E, -ms)));
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.empty[stage]);
+            if (++stage == kLseStages) {
+                stage = 0;
+                phase ^= 1u;
+            }
+        }
+        // merge the 128 threads of each row set: warps, then 4 warps via smem
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            double m = mf[r] == -INFINITY ? kNegInf : static_cast<double>(mf[r]);
+            double sv = static_cast<double>(sf[r]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double om = __shfl_xor_sync(0xffffffffu, m, o), os = __shfl_xor_sync(0xffffffffu, sv, o);
+                lse_pair_merge(m, sv, om, os);
+            }
+            if (lane == 0) { sm.wm[warp][r] = m; sm.ws[warp][r] = sv; }
+        }
+        consumers_sync();
+        if (tid < nr) {
+            const int hh = tid >> 2, r = tid & 3;
+            double mm = kNegInf, ss = 0.0;
+            for (int w = 4 * hh; w < 4 * hh + 4; ++w) lse_pair_merge(mm, ss, sm.wm[w][r], sm.ws[w][r]);
+            M[i0 + tid] = mm;
+            S[i0 + tid] = ss;
+        }
+        consumers_sync();  // wm / ws are rewritten by the next group
+    }
+}
+
 // kts = M + log S (empty -> -inf, sparse_kernel.cpp:129); log t = log q - kts.
 __global__ void sparse_col_finalize_kernel(DevState* __restrict__ st, const double* __restrict__ M,
                                            const double* __restrict__ S, const double* __restrict__ log_q, long long m,
@@ -359,10 +495,10 @@ __global__ void sparse_row_finalize_kernel(DevState* __restrict__ st, const doub
 //                        outputs = targets; corr_t[tgt] = sum_r delta ss_r
 //   row pass (K t):      transposed blocks m_b x row_stride(n_b), stream =
 //                        targets, outputs = sources; corr_s[src] = sum_c delta tt_c
-// The band's work is a list of items (bucket b, stream rows s0 .. s0 + ns,
-// output columns o0 .. o0 + ow): wide buckets are cut into <= kBandVec output
-// tiles, long ones into stream pieces; items are assigned to CTAs on the host
-// by longest-processing-time greedy so every CTA streams about the same bytes.
+// The band's work is a list of items (panel p of op.iter, stream rows s0 .. s0
+// + ns, output columns o0 .. o0 + ow): wide panels are cut into <= kBandVec
+// output tiles, long ones into stream pieces; the CTAs claim items largest
+// first from a global counter (LCN_BAND_STATIC: host LPT ranges per CTA).
 // Per CTA:
 //   warp kWarps     bulk-copies the item's rows (one copy per chunk of whole
 //                   rows, one per row for an output tile) through a ring of
@@ -388,8 +524,12 @@ struct ItemMeta {
     double* part;  // this piece's scratch partials (split outputs), else null
 };
 
+constexpr int kBandQ = 8;  // item queue depth (producer 1 -> producer 2)
+
 struct BandSmem {
     unsigned char ring[kBandStages][kBandStageBytes];
+    uint32_t q[kBandQ];         // item indices in the order producer 1 claimed them
+    uint64_t qfull[kBandQ], qempty[kBandQ];
     double vec[2][kBandVec];    // stream scalings per item slot (fp32 storage: float view)
     uint32_t out[2][kBandVec];  // output indices per item slot
     double red[kBandVec];       // per-group partial sums (groups x row width <= kBandVec)
@@ -410,9 +550,13 @@ struct BandItem {
     uint32_t oa;             // o_order index of output o0
 };
 
+// Items are claimed dynamically (largest first): producer 1 of each CTA takes
+// the next index from ctr[0]; the CTA that finishes last resets both counters.
 struct BandWork {
     const BandItem* items;
-    const uint32_t* cta_off;  // CTA c processes items cta_off[c] .. cta_off[c + 1] - 1
+    uint32_t nitems;
+    uint32_t* ctr;            // [0] next item, [1] finished CTAs
+    const uint32_t* cta_off;  // static mode (LCN_BAND_STATIC): CTA c takes items cta_off[c] .. cta_off[c + 1] - 1
     const uint2* splits;      // sid -> {scratch offset (doubles), pieces}
     uint32_t* counters;       // sid -> arrivals (reset by the combining CTA)
     double* scratch;
@@ -460,9 +604,8 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
     extern __shared__ __align__(128) unsigned char dyn[];
     BandSmem& sm = *reinterpret_cast<BandSmem*>(dyn);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t i_beg = wk.cta_off[blockIdx.x], i_end = wk.cta_off[blockIdx.x + 1];
-    if (i_beg == i_end) return;
     const double H = ROWS ? st->H_t : st->H_s;
+    constexpr uint32_t kEnd = 0xffffffffu;
     if (tid == 0) {
         for (int k = 0; k < kBandStages; ++k) {
             mbar_init(&sm.full[k], 1);
@@ -471,6 +614,10 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
         for (int k = 0; k < 2; ++k) {
             mbar_init(&sm.vfull[k], 32);
             mbar_init(&sm.vempty[k], kWarps);
+        }
+        for (int k = 0; k < kBandQ; ++k) {
+            mbar_init(&sm.qfull[k], 1);
+            mbar_init(&sm.qempty[k], 1);
         }
         fence_mbar_init();
     }
@@ -481,7 +628,16 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
             int stage = 0;
             uint32_t phase = 0;
             bool wrapped = false;
-            for (uint32_t it = i_beg; it < i_end; ++it) {
+            const uint32_t s_beg = wk.cta_off ? wk.cta_off[blockIdx.x] : 0u;
+            const uint32_t s_end = wk.cta_off ? wk.cta_off[blockIdx.x + 1] : 0u;
+            for (uint32_t k = 0;; ++k) {
+                const uint32_t claim = wk.cta_off ? s_beg + k : atomicAdd(&wk.ctr[0], 1u);
+                const uint32_t it = claim < (wk.cta_off ? s_end : wk.nitems) ? claim : kEnd;
+                const int qs = static_cast<int>(k % kBandQ);
+                if (k >= static_cast<uint32_t>(kBandQ)) mbar_wait(&sm.qempty[qs], ((k / kBandQ) - 1) & 1);
+                sm.q[qs] = it;
+                mbar_arrive(&sm.qfull[qs]);  // release: the queue entry
+                if (it == kEnd) break;
                 const BandItem item = wk.items[it];
                 const uint32_t rs = item.rs;
                 const uint32_t ws = static_cast<uint32_t>(row_stride(item.ow));  // item row width in the ring
@@ -512,14 +668,23 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
     }
     if (warp == kWarps + 1) {
         // ---------------- producer 2: stream scalings, output indices, metadata ----------------
-        int kb = 0;
-        for (uint32_t it = i_beg; it < i_end; ++it, ++kb) {
+        for (uint32_t kb = 0;; ++kb) {
+            const int qs = static_cast<int>(kb % kBandQ);
+            mbar_wait(&sm.qfull[qs], (kb / kBandQ) & 1);
+            const uint32_t it = sm.q[qs];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.qempty[qs]);
+            const int slot = kb & 1;
+            if (kb >= 2) mbar_wait(&sm.vempty[slot], ((kb >> 1) - 1) & 1);
+            if (it == kEnd) {
+                if (lane == 0) sm.meta[slot].ns = kEnd;
+                mbar_arrive(&sm.vfull[slot]);
+                break;
+            }
             const BandItem item = wk.items[it];
             // stored row c of the item is stream position c (c < g0) or c + gapn
             const double* va = logv + item.va;
             const double* vb = va + item.gapn;
-            const int slot = kb & 1;
-            if (kb >= 2) mbar_wait(&sm.vempty[slot], ((kb >> 1) - 1) & 1);
             // 4 independent loads in flight per lane before the exps (one warp
             // resolves every stream row of the item; L2 latency bound otherwise)
             for (uint32_t c0 = lane; c0 < item.ns; c0 += 128) {
@@ -562,11 +727,11 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
     // ---------------- consumers ----------------
     int stage = 0;
     uint32_t phase = 0;
-    int kb = 0;
-    for (uint32_t it = i_beg; it < i_end; ++it, ++kb) {
+    for (uint32_t kb = 0;; ++kb) {
         const int slot = kb & 1;
         mbar_wait(&sm.vfull[slot], (kb >> 1) & 1);
         const ItemMeta mt = sm.meta[slot];
+        if (mt.ns == kEnd) break;
         const uint32_t ws = static_cast<uint32_t>(row_stride(mt.ow));
         const uint32_t nq = ws / 4;
         const int R = band_rows_per_stage<T>(ws);
@@ -628,6 +793,12 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
         consumers_sync();  // red is rewritten by the next item
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.vempty[slot]);
+    }
+    // every producer of this launch has claimed past the end before its CTA
+    // gets here, so the last CTA may reset the claim counter for the next launch
+    if (tid == 0 && atomicAdd(&wk.ctr[1], 1u) == gridDim.x - 1) {
+        wk.ctr[0] = 0u;
+        wk.ctr[1] = 0u;
     }
 }
 
@@ -1330,20 +1501,23 @@ struct Solver {
     size_t mark_base = 0;
     size_t smem = 0;                                        // low-rank pass stage ring
     // band work per pass ([0] row pass on the transposed blocks, [1] column
-    // pass): items (stream pieces x output tiles of the buckets) LPT-assigned
-    // to CTAs, with the pass's split table
+    // pass): items (stream pieces x output tiles of the panels), largest
+    // first, claimed dynamically by the CTAs; the pass's split table
     struct PassPlan {
         DevBuf<BandItem> items;
-        DevBuf<uint32_t> cta_off, counters;
+        DevBuf<uint32_t> ctr, counters, cta_off;
+        bool stat = false;
         DevBuf<uint2> splits;
         DevBuf<double> scratch;
         int nitems = 0;
         BandWork work() {
-            return BandWork{items.get(), cta_off.get(), splits.get(), counters.get(), scratch.get()};
+            return BandWork{items.get(), static_cast<uint32_t>(nitems), ctr.get(), stat ? cta_off.get() : nullptr,
+                            splits.get(), counters.get(), scratch.get()};
         }
     };
     std::vector<PassPlan> plans[2];
     int band_grid = 0;
+    int lse_grid = 0;  // dense_lse_tma_kernel: persistent CTAs
     // ---- sharded solve (ctx.nccl set): rank `rank` of `world` owns the band
     // buckets assigned to it (per band and pass) and the low-rank row slices
     // [lo_s, hi_s) / [lo_t, hi_t) of equal padded length cs / ct.
@@ -1382,6 +1556,13 @@ struct Solver {
         }
         G = std::max(1, occ) * ctx.num_sms;
         if (op.kind == 3) init_band_stream();
+        if (op.kind == 0) {
+            const int bytes = static_cast<int>(sizeof(LseSmem));
+            CUDA_OK(cudaFuncSetAttribute(dense_lse_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+            int o = 1;
+            CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, dense_lse_tma_kernel, kThreads + 32, bytes));
+            lse_grid = std::max(1, o) * ctx.num_sms;
+        }
     }
     ~Solver() {
         for (auto e : evs) cudaEventDestroy(e);
@@ -1519,31 +1700,40 @@ struct Solver {
             }
         }
         if (scratch > 0xffffffffull) throw Status(2, "lcn: band split scratch above 2^32 entries");
+        // largest first: the CTAs' dynamic claims then approximate LPT list
+        // scheduling without a cost model of the per-item overheads
         std::stable_sort(pieces.begin(), pieces.end(), [](const Piece& x, const Piece& y) { return x.cost > y.cost; });
-        using Load = std::pair<double, int>;
-        std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
-        for (int c = 0; c < band_grid; ++c) heap.push({0.0, c});
-        std::vector<std::vector<BandItem>> per(band_grid);
-        for (const Piece& pc : pieces) {
-            Load ld = heap.top();
-            heap.pop();
-            per[ld.second].push_back(pc.it);
-            ld.first += pc.cost;
-            heap.push(ld);
-        }
         std::vector<BandItem> items;
-        std::vector<uint32_t> off(band_grid + 1, 0);
-        for (int c = 0; c < band_grid; ++c) {
-            off[c] = static_cast<uint32_t>(items.size());
-            items.insert(items.end(), per[c].begin(), per[c].end());
-        }
-        off[band_grid] = static_cast<uint32_t>(items.size());
+        items.reserve(pieces.size());
         PassPlan P;
+        P.stat = std::getenv("LCN_BAND_STATIC") != nullptr;
+        if (P.stat) {  // LPT-assigned static ranges per CTA
+            using Load = std::pair<double, int>;
+            std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
+            for (int c = 0; c < band_grid; ++c) heap.push({0.0, c});
+            std::vector<std::vector<BandItem>> per(band_grid);
+            for (const Piece& pc : pieces) {
+                Load ld = heap.top();
+                heap.pop();
+                per[ld.second].push_back(pc.it);
+                ld.first += pc.cost;
+                heap.push(ld);
+            }
+            std::vector<uint32_t> off(band_grid + 1, 0);
+            for (int c = 0; c < band_grid; ++c) {
+                off[c] = static_cast<uint32_t>(items.size());
+                items.insert(items.end(), per[c].begin(), per[c].end());
+            }
+            off[band_grid] = static_cast<uint32_t>(items.size());
+            P.cta_off.upload(off.data(), off.size(), s);
+        } else {
+            for (const Piece& pc : pieces) items.push_back(pc.it);
+        }
         P.nitems = static_cast<int>(items.size());
         P.items.resize(std::max<size_t>(items.size(), 1));
-        P.cta_off.resize(off.size());
         if (!items.empty()) P.items.upload(items.data(), items.size(), s);
-        P.cta_off.upload(off.data(), off.size(), s);
+        P.ctr.resize(2);
+        P.ctr.zero(s);
         P.splits.resize(std::max<size_t>(splits.size(), 1));
         P.counters.resize(std::max<size_t>(splits.size(), 1));
         P.scratch.resize(std::max<size_t>(scratch, 1));
@@ -1673,6 +1863,12 @@ struct Solver {
     template <typename T>
     void sparse_rows(const double* lt) {
         if (op.kind == 0) {  // dense: the whole row in one (max, sum) pair
+            if constexpr (sizeof(T) == 4)
+                if (m % 4 == 0) {
+                    dense_lse_tma_kernel<<<lse_grid, kThreads + 32, sizeof(LseSmem), s>>>(
+                        st.get(), dense_logk<T>(false), n, m, lt, Mr.get(), Sr.get());
+                    return;
+                }
             dense_lse_kernel<T><<<ceil_div(n, kDenseRows), 256, 0, s>>>(st.get(), dense_logk<T>(false), n, m, lt,
                                                                         Mr.get(), Sr.get());
             return;
@@ -1686,6 +1882,12 @@ struct Solver {
     template <typename T>
     void sparse_cols(const double* ls) {
         if (op.kind == 0) {  // dense: rows of the transposed copy
+            if constexpr (sizeof(T) == 4)
+                if (n % 4 == 0) {
+                    dense_lse_tma_kernel<<<lse_grid, kThreads + 32, sizeof(LseSmem), s>>>(
+                        st.get(), dense_logk<T>(true), m, n, ls, Mc.get(), Sc.get());
+                    return;
+                }
             dense_lse_kernel<T><<<ceil_div(m, kDenseRows), 256, 0, s>>>(st.get(), dense_logk<T>(true), m, n, ls,
                                                                         Mc.get(), Sc.get());
             return;

@@ -215,14 +215,18 @@ def test_sharded_solve_single_rank(ref, fp64):
         op.log_matvec(np.zeros(pr.m))
 
 
-@pytest.mark.parametrize("fp64,cost,lam", [(False, lcn.EUCLIDEAN, 0.05), (True, lcn.EUCLIDEAN, 0.05),
-                                           (False, lcn.COSINE_DERIVED, 0.1), (False, lcn.NEGATIVE_DOT, 0.2)])
-def test_dense_anchor(ref, fp64, cost, lam):
+@pytest.mark.parametrize("fp64,cost,lam,n,m", [(False, lcn.EUCLIDEAN, 0.05, 310, 260),
+                                               (True, lcn.EUCLIDEAN, 0.05, 310, 260),
+                                               (False, lcn.COSINE_DERIVED, 0.1, 310, 260),
+                                               (False, lcn.NEGATIVE_DOT, 0.2, 310, 260),
+                                               (False, lcn.EUCLIDEAN, 0.05, 1200, 2052)])
+def test_dense_anchor(ref, fp64, cost, lam, n, m):
     """configs[2]-shaped dense operator (H19): log K bit-exact, distance and the
-    dense plan against the reference's dense solve."""
+    dense plan against the reference's dense solve. Row lengths divisible by 4
+    take the 16-byte streaming kernel (dense_lse4_kernel), others the scalar one."""
     r = np.random.default_rng(5)
-    p = r.standard_normal((310, 12)).astype(np.float32).astype(np.float64)
-    q = (r.standard_normal((260, 12)) * 0.8 + 0.1).astype(np.float32).astype(np.float64)
+    p = r.standard_normal((n, 12)).astype(np.float32).astype(np.float64)
+    q = (r.standard_normal((m, 12)) * 0.8 + 0.1).astype(np.float32).astype(np.float64)
     p /= np.linalg.norm(p, axis=1, keepdims=True)
     q /= np.linalg.norm(q, axis=1, keepdims=True)
     c = lcn.Context(0, store_fp64=fp64)
@@ -230,7 +234,7 @@ def test_dense_anchor(ref, fp64, cost, lam):
     rop = ref.op_dense(p, q, cost, lam)
     lk, rlk = op.export_dense(), rop.dense_logk()
     assert np.array_equal(lk.view(np.uint64), rlk.view(np.uint64))   # bit-exact log K
-    pm, qm = np.full(310, 1 / 310), np.full(260, 1 / 260)
+    pm, qm = np.full(n, 1 / n), np.full(m, 1 / m)
     res = lcn.sinkhorn(op, pm, qm, lcn.SinkhornOptions(tol=0.0, max_iters=50))
     rres = rop.sinkhorn(pm, qm, tol=0.0, max_iters=50)
     tol = REL_FP64 if fp64 else REL_FP32
@@ -339,3 +343,22 @@ def test_lcn_panel_layouts(ref, monkeypatch, layout, shape):
     for mine, theirs in [(op.log_matvec(rres.log_t), rop.log_matvec(rres.log_t)),
                          (op.log_matvec_t(rres.log_s), rop.log_matvec(rres.log_s, transposed=True))]:
         assert np.max(np.abs(mine - theirs) / np.maximum(np.abs(theirs), 1.0)) <= REL_FP32
+
+
+def test_lcn_bands_without_two_sided_buckets(ref):
+    """Sources and targets in separate far clusters: every LSH bucket of both
+    bands is one-sided, so no band has work (empty support) and the LCN
+    operator reduces to its Nystrom part — as in the reference."""
+    r = np.random.default_rng(21)
+    p = (r.standard_normal((300, 6)) * 0.3 + 4.0).astype(np.float32).astype(np.float64)
+    q = (r.standard_normal((280, 6)) * 0.3 - 4.0).astype(np.float32).astype(np.float64)
+    c = lcn.Context(0, store_fp64=False)
+    cfg = lcn.LshConfig(2, 1, 2, 10, 7)
+    op = lcn.KernelOperator.lcn_lsh(c, p, q, lcn.EUCLIDEAN, 2.0, cfg, 12, lcn.LANDMARK_KMEANS, 3)
+    pairs = ref.lsh_pairs(p, q, 2, 2, 10, 7)
+    rop = ref.op_lcn(p, q, lcn.EUCLIDEAN, 2.0, pairs, 12, 0, 3)
+    assert op.nnz == 0
+    pm, qm = np.full(300, 1 / 300), np.full(280, 1 / 280)
+    res = lcn.sinkhorn(op, pm, qm, lcn.SinkhornOptions(tol=0.0, max_iters=30))
+    rres = rop.sinkhorn(pm, qm, tol=0.0, max_iters=30)
+    assert rel(res.distance, rres.distance) <= REL_FP32
