@@ -273,6 +273,25 @@ int lcn_distance_lcn(const lcn_result* res, const lcn_op* op, double* out);
 /* Warning text i (SinkhornResult::warnings, sinkhorn.cpp:122-128). */
 const char* lcn_result_warning(const lcn_result* res, int i);
 
+/* ---- Data formats and generators either side of the path (host only, no
+ * device needed). Errors: LCN_E_INVALID_ARGUMENT with
+ * the reference's InvalidArgument text in lcn_io_last_error(). ---- */
+/* read_points_file (io.cpp:105-116): LCNPTS1 binary (magic, u64-LE n, u64-LE
+ * d, n*d f64-LE; io.cpp:77-95) or text (`n d` then rows, '#' comments;
+ * io.cpp:33-63), PointSet::validate (geometry.cpp:10-18). out == NULL returns
+ * the shape in *n, *d; otherwise *n, *d must hold that shape. */
+int lcn_points_read(const char* path, double* out, size_t* n, size_t* d);
+/* write_points_file (io.cpp:118-126): binary != 0 LCNPTS1, else text with 17
+ * significant digits (io.cpp:65-75). */
+int lcn_points_write(const char* path, const double* pts, size_t n, size_t d, int binary);
+/* sample_uniform_ball (generators.cpp:26-40): n x d, the reference's draws. */
+int lcn_sample_uniform_ball(size_t n, size_t d, uint64_t seed, double* out);
+/* sample_clustered (generators.cpp:42-106): p and q n x d each, centers c x d
+ * (centers_out may be NULL). */
+int lcn_sample_clustered(size_t n, size_t d, size_t c, double D, double r, uint64_t seed, double* p_out,
+                         double* q_out, double* centers_out);
+const char* lcn_io_last_error(void);
+
 #ifdef __cplusplus
 }
 #endif

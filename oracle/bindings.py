@@ -336,6 +336,39 @@ class RefLib(CheckerLib):
     def __init__(self, path=REF_SO):
         super().__init__(path)
 
+    def points_read(self, path):
+        """read_points_file (io.cpp:105-116)."""
+        n, d = _SZ(0), _SZ(0)
+        f = self.fn("points_read", C.c_char_p, _P, C.POINTER(_SZ), C.POINTER(_SZ))
+        self.check(f(os.fsencode(path), None, C.byref(n), C.byref(d)))
+        out = np.empty((n.value, d.value))
+        self.check(f(os.fsencode(path), _ptr(out), C.byref(n), C.byref(d)))
+        return out
+
+    def points_write(self, path, pts, binary=True):
+        """write_points_file (io.cpp:118-126)."""
+        pts = _f64(pts)
+        self.check(self.fn("points_write", C.c_char_p, _P, _SZ, _SZ, _I)(os.fsencode(path), _ptr(pts), pts.shape[0],
+                                                                         pts.shape[1], int(bool(binary))))
+
+    def sample_clustered(self, n, d, c, D, r, seed):
+        """sample_clustered (generators.cpp:42-106): (p, q, centers)."""
+        p, q, ctr = np.empty((n, d)), np.empty((n, d)), np.empty((c, d))
+        self.check(self.fn("sample_clustered", _SZ, _SZ, _SZ, C.c_double, C.c_double, _U64, _P, _P, _P)(
+            n, d, c, D, r, seed, _ptr(p), _ptr(q), _ptr(ctr)))
+        return p, q, ctr
+
+    def run_all_json(self, config: dict):
+        """run_all (runner.cpp:344-418) on a config_from_json dict -> records."""
+        import json
+        out = C.c_void_p()
+        self.check(self.fn("run_all_json", C.c_char_p, C.POINTER(C.c_void_p))(json.dumps(config).encode(),
+                                                                              C.byref(out)))
+        try:
+            return json.loads(C.string_at(out.value).decode())["records"]
+        finally:
+            self.fn("free_string", C.c_void_p, restype=None)(out)
+
     def lsh_pairs_cfg(self, p, q, scheme, bands=1, rows=1, buckets=2, iters=10, branching=2, seed=0):
         """lsh_neighbor_pairs (lsh.cpp:245-283) end to end for any scheme."""
         p, q = _f64(p), _f64(q)

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -20,6 +21,8 @@
 #include "lcn/error.hpp"
 #include "lcn/generators.hpp"
 #include "lcn/geometry.hpp"
+#include "lcn/io.hpp"
+#include "lcn/runner.hpp"
 #include "lcn/kmeans.hpp"
 #include "lcn/lsh.hpp"
 #include "lcn/nystrom.hpp"
@@ -557,5 +560,48 @@ int ref_dense_reference(const double* cost, std::size_t n, std::size_t m, const 
         *iters = sol.iters;
     })
 }
+
+// sample_clustered (generators.cpp:42-106)
+int ref_sample_clustered(std::size_t n, std::size_t d, std::size_t c, double D, double r, std::uint64_t seed,
+                         double* p_out, double* q_out, double* centers_out) {
+    GUARD({
+        ClusteredProblem cp = sample_clustered(n, d, c, D, r, seed);
+        std::memcpy(p_out, cp.p.coords.data(), n * d * sizeof(double));
+        std::memcpy(q_out, cp.q.coords.data(), n * d * sizeof(double));
+        if (centers_out) std::memcpy(centers_out, cp.centers.data.data(), c * d * sizeof(double));
+    })
+}
+
+// read_points_file (io.cpp:105-116); out == nullptr: shape only
+int ref_points_read(const char* path, double* out, std::size_t* n, std::size_t* d) {
+    GUARD({
+        PointSet ps = read_points_file(path);
+        if (out) std::memcpy(out, ps.coords.data(), ps.coords.size() * sizeof(double));
+        *n = ps.n;
+        *d = ps.dim;
+    })
+}
+
+// write_points_file (io.cpp:118-126)
+int ref_points_write(const char* path, const double* pts, std::size_t n, std::size_t d, int binary) {
+    GUARD(write_points_file(path, make_points(pts, n, d, "p"), binary != 0))
+}
+
+// run_all (runner.cpp:344-418) on a JSON config (config_from_json,
+// runner.cpp:92-141); *out = {"records": [record_to_json ...]} (free with
+// ref_free_string). Timing fields are dropped by strict-deterministic configs.
+int ref_run_all_json(const char* config_json, char** out) {
+    GUARD({
+        RunConfig cfg = config_from_json(nlohmann::json::parse(config_json));
+        nlohmann::json j;
+        j["records"] = nlohmann::json::array();
+        for (const RunRecord& r : run_all(cfg)) j["records"].push_back(record_to_json(r));
+        const std::string s = j.dump();
+        *out = static_cast<char*>(std::malloc(s.size() + 1));
+        std::memcpy(*out, s.c_str(), s.size() + 1);
+    })
+}
+
+void ref_free_string(char* p) { std::free(p); }
 
 }  // extern "C"

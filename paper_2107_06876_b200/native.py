@@ -83,12 +83,29 @@ class _ResInfo(C.Structure):
 _lib = None
 
 
+def _preload_nccl():
+    """The library links libnccl.so.2. When PyTorch's bundled NCCL (newer than
+    the system copy) is installed, load it first so both resolve to the same
+    libnccl.so.2 whatever the import order (torch needs its own version's
+    symbols; the NCCL calls here work on either)."""
+    import sys
+    for base in sys.path:
+        cand = os.path.join(base, "nvidia", "nccl", "lib", "libnccl.so.2")
+        if os.path.exists(cand):
+            try:
+                C.CDLL(cand, mode=C.RTLD_GLOBAL)
+            except OSError:
+                pass
+            return
+
+
 def library() -> C.CDLL:
     """Load the C-ABI library (fails loudly when it was not built)."""
     global _lib
     if _lib is None:
         if not os.path.exists(LIB_PATH):
             raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (make -C paper_2107_06876_b200)")
+        _preload_nccl()
         lib = C.CDLL(LIB_PATH)
         P, SZ, D, I, U64 = C.c_void_p, C.c_size_t, C.c_double, C.c_int, C.c_uint64
         PP = C.POINTER(C.c_void_p)
@@ -632,3 +649,64 @@ def distance_lcn(res: SinkhornResult, op: KernelOperator) -> float:
     out = C.c_double()
     op.ctx.check(op.ctx.lib.lcn_distance_lcn(res.h, op.h, C.byref(out)))
     return out.value
+
+
+# ---- data formats and generators either side of the path (host only) -------
+def _io_check(lib, rc: int):
+    if rc != 0:
+        raise _STATUS.get(rc, Error)(lib.lcn_io_last_error().decode())
+
+
+def _io_lib():
+    lib = library()
+    if not getattr(lib, "_io_sigs", False):
+        P, SZ, U64, I = C.c_void_p, C.c_size_t, C.c_uint64, C.c_int
+        for name, args in {"lcn_points_read": [C.c_char_p, P, C.POINTER(SZ), C.POINTER(SZ)],
+                           "lcn_points_write": [C.c_char_p, P, SZ, SZ, I],
+                           "lcn_sample_uniform_ball": [SZ, SZ, U64, P],
+                           "lcn_sample_clustered": [SZ, SZ, SZ, C.c_double, C.c_double, U64, P, P, P]}.items():
+            f = getattr(lib, name)
+            f.argtypes = args
+            f.restype = I
+        lib.lcn_io_last_error.argtypes = []
+        lib.lcn_io_last_error.restype = C.c_char_p
+        lib._io_sigs = True
+    return lib
+
+
+def read_points_file(path: str) -> np.ndarray:
+    """read_points_file (io.cpp:105-116): LCNPTS1 binary or text, validated."""
+    lib = _io_lib()
+    n, d = C.c_size_t(0), C.c_size_t(0)
+    _io_check(lib, lib.lcn_points_read(os.fsencode(path), None, C.byref(n), C.byref(d)))
+    out = np.empty((n.value, d.value))
+    _io_check(lib, lib.lcn_points_read(os.fsencode(path), _p(out), C.byref(n), C.byref(d)))
+    return out
+
+
+def write_points_file(path: str, points, binary: bool = True) -> None:
+    """write_points_file (io.cpp:118-126)."""
+    x = _f64(points)
+    if x.ndim != 2:
+        raise DimensionError("write_points_file: points must be n x d")
+    lib = _io_lib()
+    _io_check(lib, lib.lcn_points_write(os.fsencode(path), _p(x), x.shape[0], x.shape[1], int(bool(binary))))
+
+
+def sample_uniform_ball(n: int, d: int, seed: int) -> np.ndarray:
+    """sample_uniform_ball (generators.cpp:26-40), the reference's draws."""
+    lib = _io_lib()
+    out = np.empty((n, d)) if n and d else np.empty((0, 0))
+    _io_check(lib, lib.lcn_sample_uniform_ball(n, d, seed, _p(out) if out.size else None))
+    return out
+
+
+def sample_clustered(n: int, d: int, c: int, D: float, r: float, seed: int):
+    """sample_clustered (generators.cpp:42-106): (p, q, centers)."""
+    lib = _io_lib()
+    ok = n and d and c
+    p, q = (np.empty((n, d)), np.empty((n, d))) if ok else (np.empty((0, 0)), np.empty((0, 0)))
+    ctr = np.empty((c, d)) if ok else np.empty((0, 0))
+    _io_check(lib, lib.lcn_sample_clustered(n, d, c, D, r, seed, _p(p) if ok else None, _p(q) if ok else None,
+                                            _p(ctr) if ok else None))
+    return p, q, ctr
