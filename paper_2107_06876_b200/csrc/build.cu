@@ -1718,13 +1718,12 @@ __global__ void csr_values_kernel(BandViews bvs, ValPtrs vals, long long n, cons
 }
 }  // namespace
 
-void export_csr(Op& op, int which, uint32_t* row_ptr, uint32_t* col, double* vals) {
+// CSR-ordered values of the support into device memory (d_vals: nnz).
+void csr_values_device(Op& op, int which, double* d_vals) {
     build_csr(op);
     Ctx& ctx = *op.ctx;
     cudaStream_t s = ctx.stream;
-    if (row_ptr) op.csr_row_ptr.download(row_ptr, op.n + 1, s);
-    if (col && op.nnz) op.csr_col.download(col, op.nnz, s);
-    if (vals && op.nnz) {
+    if (op.nnz) {
         BandViews bvs{};
         bvs.bands = static_cast<int>(op.bands.size());
         ValPtrs vp{};
@@ -1736,11 +1735,22 @@ void export_csr(Op& op, int which, uint32_t* row_ptr, uint32_t* col, double* val
         }
         if (which == 1 && op.kind != 3) throw Status(2, "export_csr: delta needs an lcn operator");
         if (which == 3 && op.kind != 3) throw Status(2, "export_csr: nys_vals needs an lcn operator");
-        DevBuf<double> dv(op.nnz);
         csr_values_kernel<<<ceil_div(op.n, 256), 256, 0, s>>>(bvs, vp, op.n, op.csr_row_ptr.get(), op.csr_col.get(),
                                                               which, op.U64.get(), op.Wt64.get(),
-                                                              static_cast<int>(op.l), dv.get());
+                                                              static_cast<int>(op.l), d_vals);
         LAUNCH_OK("csr values");
+    }
+}
+
+void export_csr(Op& op, int which, uint32_t* row_ptr, uint32_t* col, double* vals) {
+    build_csr(op);
+    Ctx& ctx = *op.ctx;
+    cudaStream_t s = ctx.stream;
+    if (row_ptr) op.csr_row_ptr.download(row_ptr, op.n + 1, s);
+    if (col && op.nnz) op.csr_col.download(col, op.nnz, s);
+    if (vals && op.nnz) {
+        DevBuf<double> dv(op.nnz);
+        csr_values_device(op, which, dv.get());
         dv.download(vals, op.nnz, s);
     }
     ctx.sync();

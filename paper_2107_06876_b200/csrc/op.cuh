@@ -150,6 +150,7 @@ void build_correction(Op& op);
 void finalize_storage(Op& op);
 void build_csr(Op& op);
 void export_csr(Op& op, int which, uint32_t* row_ptr, uint32_t* col, double* vals);
+void csr_values_device(Op& op, int which, double* d_vals);
 
 // Phase timing to stderr when LCN_TIMING is set (host clock around synced phases).
 struct PhaseTimer {

@@ -2290,43 +2290,115 @@ void op_log_matvec(Op& op, const double* h_in, bool transposed, double* h_out) {
     else sv.matvec<float>(h_in, transposed, h_out);
 }
 
-// distance_lcn (sinkhorn.cpp:222-261), from the fp64 factors (host-side
-// reduction order as the reference).
+namespace {
+// distance_lcn pieces (sinkhorn.cpp:222-261), fp64, deterministic: fixed
+// per-block row ranges, block partials combined in block order.
+constexpr int kDlBlocks = 256;
+
+__global__ void exp_kernel(const double* __restrict__ in, double* __restrict__ out, long long n) {
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += 256LL * gridDim.x) out[i] = exp(in[i]);
+}
+
+// part[blk * l + a] = sum over the block's rows r of F[r, a] * v[r]
+__global__ void __launch_bounds__(256) colsum_partial_kernel(const double* __restrict__ F, long long rows, int l,
+                                                             const double* __restrict__ v, double* __restrict__ part) {
+    const long long per = (rows + gridDim.x - 1) / gridDim.x;
+    const long long r0 = blockIdx.x * per, r1 = r0 + per < rows ? r0 + per : rows;
+    for (int a = threadIdx.x; a < l; a += 256) {
+        double acc = 0.0;
+        for (long long r = r0; r < r1; ++r) acc += F[r * l + a] * v[r];
+        part[static_cast<long long>(blockIdx.x) * l + a] = acc;
+    }
+}
+
+__global__ void colsum_reduce_kernel(const double* __restrict__ part, int blocks, int l, double* __restrict__ out) {
+    const int a = blockIdx.x * 256 + threadIdx.x;
+    if (a >= l) return;
+    double acc = 0.0;
+    for (int b = 0; b < blocks; ++b) acc += part[static_cast<long long>(b) * l + a];
+    out[a] = acc;
+}
+
+// block partial of sum_r logv[r] * lin[r] * (F_r . w): one warp per row
+__global__ void __launch_bounds__(256) rowdot_term_kernel(const double* __restrict__ F, long long rows, int l,
+                                                          const double* __restrict__ w, const double* __restrict__ logv,
+                                                          const double* __restrict__ lin, double* __restrict__ part) {
+    __shared__ double red[8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double acc = 0.0;
+    for (long long r = blockIdx.x * 8LL + warp; r < rows; r += 8LL * gridDim.x) {
+        double row = 0.0;
+        for (int a = lane; a < l; a += 32) row += F[r * l + a] * w[a];
+        row = warp_sum(row);
+        acc += logv[r] * (lin[r] * row);
+    }
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int k = 0; k < 8; ++k) t += red[k];
+        part[blockIdx.x] = t;
+    }
+}
+
+// block partial of sum over the support of s_i delta_e t_j (log s_i + log t_j)
+__global__ void __launch_bounds__(256) support_term_kernel(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ col,
+                                                           const double* __restrict__ dl, long long n,
+                                                           const double* __restrict__ sl, const double* __restrict__ tl,
+                                                           const double* __restrict__ ls, const double* __restrict__ lt,
+                                                           double* __restrict__ part) {
+    __shared__ double red[8];
+    double acc = 0.0;
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += 256LL * gridDim.x)
+        for (uint32_t e = rp[i]; e < rp[i + 1]; ++e) {
+            const uint32_t j = col[e];
+            acc += (sl[i] * dl[e] * tl[j]) * (ls[i] + lt[j]);
+        }
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int k = 0; k < 8; ++k) t += red[k];
+        part[blockIdx.x] = t;
+    }
+}
+}  // namespace
+
+// distance_lcn (sinkhorn.cpp:222-261) on the device from the fp64 factors:
+// P_Nys 1 = diag(s) U (W t), 1^T P_Nys = (s^T U) W diag(t), plus the
+// correction's mass on the support.
 double distance_lcn_device(Op& op, const Result& res) {
     Ctx& ctx = *op.ctx;
-    const size_t n = op.n, m = op.m, l = op.l;
-    std::vector<double> U(n * l), Wt(m * l);
-    op.U64.download(U.data(), n * l, ctx.stream);
-    op.Wt64.download(Wt.data(), m * l, ctx.stream);
-    ctx.sync();
-    std::vector<double> s_lin(n), t_lin(m), wt(l, 0.0), su(l, 0.0);
-    for (size_t i = 0; i < n; ++i) s_lin[i] = std::exp(res.log_s[i]);
-    for (size_t j = 0; j < m; ++j) t_lin[j] = std::exp(res.log_t[j]);
-    for (size_t j = 0; j < m; ++j)
-        for (size_t a = 0; a < l; ++a) wt[a] += Wt[j * l + a] * t_lin[j];
-    for (size_t i = 0; i < n; ++i)
-        for (size_t a = 0; a < l; ++a) su[a] += U[i * l + a] * s_lin[i];
-    double term = 0.0;
-    for (size_t i = 0; i < n; ++i) {
-        double row = 0.0;
-        for (size_t a = 0; a < l; ++a) row += U[i * l + a] * wt[a];
-        term += res.log_s[i] * (s_lin[i] * row);
-    }
-    for (size_t j = 0; j < m; ++j) {
-        double col = 0.0;
-        for (size_t a = 0; a < l; ++a) col += su[a] * Wt[j * l + a];
-        term += res.log_t[j] * (col * t_lin[j]);
-    }
+    cudaStream_t s = ctx.stream;
+    const long long n = static_cast<long long>(op.n), m = static_cast<long long>(op.m);
+    const int l = static_cast<int>(op.l);
+    DevBuf<double> ls(n), lt(m), sl(n), tl(m), part(static_cast<size_t>(kDlBlocks) * l), wt(l), su(l), terms(3 * kDlBlocks);
+    ls.upload(res.log_s.data(), n, s);
+    lt.upload(res.log_t.data(), m, s);
+    terms.zero(s);
+    exp_kernel<<<kDlBlocks, 256, 0, s>>>(ls.get(), sl.get(), n);
+    exp_kernel<<<kDlBlocks, 256, 0, s>>>(lt.get(), tl.get(), m);
+    // wt = W t (Wt64 is m x l), su = U^T s (U64 is n x l)
+    colsum_partial_kernel<<<kDlBlocks, 256, 0, s>>>(op.Wt64.get(), m, l, tl.get(), part.get());
+    colsum_reduce_kernel<<<ceil_div(l, 256), 256, 0, s>>>(part.get(), kDlBlocks, l, wt.get());
+    colsum_partial_kernel<<<kDlBlocks, 256, 0, s>>>(op.U64.get(), n, l, sl.get(), part.get());
+    colsum_reduce_kernel<<<ceil_div(l, 256), 256, 0, s>>>(part.get(), kDlBlocks, l, su.get());
+    rowdot_term_kernel<<<kDlBlocks, 256, 0, s>>>(op.U64.get(), n, l, wt.get(), ls.get(), sl.get(), terms.get());
+    rowdot_term_kernel<<<kDlBlocks, 256, 0, s>>>(op.Wt64.get(), m, l, su.get(), lt.get(), tl.get(),
+                                                 terms.get() + kDlBlocks);
     if (op.kind == 3 && op.nnz) {
-        std::vector<uint32_t> rp(n + 1), col(op.nnz);
-        std::vector<double> dl(op.nnz);
-        export_csr(op, 1, rp.data(), col.data(), dl.data());
-        for (size_t i = 0; i < n; ++i)
-            for (uint32_t e = rp[i]; e < rp[i + 1]; ++e) {
-                double mass = s_lin[i] * dl[e] * t_lin[col[e]];
-                term += mass * (res.log_s[i] + res.log_t[col[e]]);
-            }
+        DevBuf<double> dl(op.nnz);
+        csr_values_device(op, 1, dl.get());
+        support_term_kernel<<<kDlBlocks, 256, 0, s>>>(op.csr_row_ptr.get(), op.csr_col.get(), dl.get(), n, sl.get(),
+                                                      tl.get(), ls.get(), lt.get(), terms.get() + 2 * kDlBlocks);
     }
+    LAUNCH_OK("distance_lcn");
+    std::vector<double> h(3 * kDlBlocks);
+    terms.download(h.data(), h.size(), s);
+    ctx.sync();
+    double term = 0.0;
+    for (double v : h) term += v;
     return op.lambda * term;
 }
 
