@@ -772,42 +772,7 @@ int lcn_sinkhorn(lcn_op* op, const double* p, const double* q, const lcn_sinkhor
             }
         }
         sinkhorn_solve(o, p, q, false, so, res->r);
-        if (so.want_plan && o.kind == LCN_OP_DENSE) {
-            // dense plan (sinkhorn.cpp:23-44): exp(log s_i + log K_ij + log t_j), row-major n x m
-            std::vector<double> lk(o.n * o.m);
-            o.dk64.download(lk.data(), lk.size(), o.ctx->stream);
-            o.ctx->sync();
-            Result& r = res->r;
-            r.plan_vals.resize(o.n * o.m);
-            for (size_t i = 0; i < o.n; ++i)
-                for (size_t j = 0; j < o.m; ++j)
-                    r.plan_vals[i * o.m + j] = std::exp(r.log_s[i] + lk[i * o.m + j] + r.log_t[j]);
-        } else if (so.want_plan && o.kind != 2 && o.nnz) {
-            // Plan entries on the support in CSR order (sinkhorn.cpp:45-80).
-            std::vector<uint32_t> rp(o.n + 1), col(o.nnz);
-            std::vector<double> lk(o.nnz);
-            export_csr(o, o.kind == 1 ? 0 : 2, rp.data(), col.data(), lk.data());
-            Result& r = res->r;
-            if (o.kind == 1) {
-                r.plan_vals.resize(o.nnz);
-                for (size_t i = 0; i < o.n; ++i)
-                    for (uint32_t e = rp[i]; e < rp[i + 1]; ++e)
-                        r.plan_vals[e] = std::exp(r.log_s[i] + lk[e] + r.log_t[col[e]]);
-            } else {
-                std::vector<double> nys(o.nnz);
-                export_csr(o, 3, nullptr, nullptr, nys.data());
-                r.sp_vals.resize(o.nnz);
-                r.sp_nys_vals.resize(o.nnz);
-                for (size_t i = 0; i < o.n; ++i) {
-                    double si = std::exp(r.log_s[i]);
-                    for (uint32_t e = rp[i]; e < rp[i + 1]; ++e) {
-                        double tj = std::exp(r.log_t[col[e]]);
-                        r.sp_vals[e] = std::exp(r.log_s[i] + lk[e] + r.log_t[col[e]]);
-                        r.sp_nys_vals[e] = si * nys[e] * tj;
-                    }
-                }
-            }
-        }
+        if (so.want_plan) extract_plan_device(o, res->r);  // sinkhorn.cpp:23-100
         *out = res.release();
     });
 }

@@ -172,5 +172,6 @@ struct SolveOptions {
 void sinkhorn_solve(Op& op, const double* p, const double* q, bool device_ptrs, const SolveOptions& o, Result& res);
 void op_log_matvec(Op& op, const double* h_in, bool transposed, double* h_out);
 double distance_lcn_device(Op& op, const Result& res);
+void extract_plan_device(Op& op, Result& res);
 
 }  // namespace lcnb

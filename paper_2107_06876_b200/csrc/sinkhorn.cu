@@ -2365,6 +2365,73 @@ __global__ void __launch_bounds__(256) support_term_kernel(const uint32_t* __res
 }
 }  // namespace
 
+namespace {
+__global__ void dense_plan_kernel(const double* __restrict__ lk, const double* __restrict__ ls,
+                                  const double* __restrict__ lt, long long n, long long m, double* __restrict__ out) {
+    const long long tot = n * m;
+    for (long long e = blockIdx.x * 256LL + threadIdx.x; e < tot; e += 256LL * gridDim.x) {
+        const long long i = e / m, j = e - i * m;
+        out[e] = exp(ls[i] + lk[e] + lt[j]);
+    }
+}
+// one thread per row: plan entries of the row's support (CSR order)
+__global__ void support_plan_kernel(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ col,
+                                    const double* __restrict__ lk, const double* __restrict__ nys, long long n,
+                                    const double* __restrict__ ls, const double* __restrict__ lt,
+                                    double* __restrict__ vals, double* __restrict__ nys_out) {
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += 256LL * gridDim.x) {
+        const double si = exp(ls[i]);
+        for (uint32_t e = rp[i]; e < rp[i + 1]; ++e) {
+            const uint32_t j = col[e];
+            vals[e] = exp(ls[i] + lk[e] + lt[j]);
+            if (nys_out) nys_out[e] = si * nys[e] * exp(lt[j]);
+        }
+    }
+}
+}  // namespace
+
+// extract_plan_impl (sinkhorn.cpp:23-100) on the device: the dense plan
+// exp(log s_i + log K_ij + log t_j) (row-major), the sparse plan on the
+// support (CSR order) and the LCN sp_vals / sp_nys_vals.
+void extract_plan_device(Op& op, Result& r) {
+    Ctx& ctx = *op.ctx;
+    cudaStream_t s = ctx.stream;
+    const long long n = static_cast<long long>(op.n), m = static_cast<long long>(op.m);
+    if (op.kind == 2 || (op.kind != 0 && op.nnz == 0)) return;
+    DevBuf<double> ls(n), lt(m);
+    ls.upload(r.log_s.data(), n, s);
+    lt.upload(r.log_t.data(), m, s);
+    const int grid = 8 * ctx.num_sms;
+    if (op.kind == 0) {
+        DevBuf<double> out(static_cast<size_t>(n * m));
+        dense_plan_kernel<<<grid, 256, 0, s>>>(op.dk64.get(), ls.get(), lt.get(), n, m, out.get());
+        LAUNCH_OK("dense plan");
+        r.plan_vals.resize(static_cast<size_t>(n * m));
+        out.download(r.plan_vals.data(), r.plan_vals.size(), s);
+        ctx.sync();
+        return;
+    }
+    const size_t nnz = op.nnz;
+    DevBuf<double> lk(nnz), vals(nnz), nys, nys_out;
+    csr_values_device(op, op.kind == 1 ? 0 : 2, lk.get());
+    if (op.kind == 3) {
+        nys.resize(nnz);
+        nys_out.resize(nnz);
+        csr_values_device(op, 3, nys.get());
+    }
+    support_plan_kernel<<<ceil_div(n, 256), 256, 0, s>>>(op.csr_row_ptr.get(), op.csr_col.get(), lk.get(), nys.get(), n,
+                                                         ls.get(), lt.get(), vals.get(), nys_out.get());
+    LAUNCH_OK("support plan");
+    std::vector<double>& dst = op.kind == 1 ? r.plan_vals : r.sp_vals;
+    dst.resize(nnz);
+    vals.download(dst.data(), nnz, s);
+    if (op.kind == 3) {
+        r.sp_nys_vals.resize(nnz);
+        nys_out.download(r.sp_nys_vals.data(), nnz, s);
+    }
+    ctx.sync();
+}
+
 // distance_lcn (sinkhorn.cpp:222-261) on the device from the fp64 factors:
 // P_Nys 1 = diag(s) U (W t), 1^T P_Nys = (s^T U) W diag(t), plus the
 // correction's mass on the support.
