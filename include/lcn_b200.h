@@ -232,6 +232,12 @@ int lcn_batched_lcn(lcn_ctx* ctx, const double* X, size_t rows, size_t d, int np
                     int cost, double lambda, int buckets, int kmeans_iters, const uint64_t* lsh_seeds, size_t l,
                     const uint64_t* landmark_seeds, int iters, double* distance_out, int* status_out,
                     int* iters_out);
+/* KernelOperator::with_bp (operator.cpp:103-115), in place: deletion kernels
+ * c_{p,eps} (n) and c_{eps,q} (m), finite and >= 0 (BpExtension::from_costs
+ * gives exp(-c / lambda), operator.cpp:33-43). Solves then use the extended
+ * problem of sinkhorn.cpp:115-120 with unbalanced marginals allowed. NULL,
+ * NULL removes the extension. Not on sharded contexts. */
+int lcn_op_set_bp(lcn_op* op, const double* del_p, const double* del_q);
 int lcn_op_destroy(lcn_op* op);
 int lcn_op_get_info(const lcn_op* op, lcn_op_info_t* info);
 /* CSR export in the reference's order (rows ascending, columns ascending,
@@ -260,7 +266,9 @@ int lcn_result_destroy(lcn_result* res);
 int lcn_result_get_info(const lcn_result* res, lcn_result_info_t* info);
 /* which: 0 log_s (n), 1 log_t (m), 2 row_marginal (n), 3 marginal_err trace,
  * 4 sparse plan values (Plan::sparse_vals, CSR order), 5 lcn sp_vals,
- * 6 lcn sp_nys_vals. out == NULL returns the length in *len only. */
+ * 6 lcn sp_nys_vals; under BP (lcn_op_set_bp): 7 del_p_mass (n), 8 del_q_mass
+ * (m), 9 eps_mass (1) (Plan, sinkhorn.hpp:47-51), and 0-3 are the extended
+ * (n + m) vectors. out == NULL returns the length in *len only. */
 int lcn_result_copy(const lcn_result* res, int which, double* out, size_t* len);
 /* grad_cost (sinkhorn.cpp:263-320). which: 0 dense / sparse d d / d C (the plan:
  * n x m row-major, or CSR order), 1 lcn / nystrom d d / d U (n x l),

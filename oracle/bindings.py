@@ -264,6 +264,13 @@ class Op:
         self.lib.check(self.lib.fn("op_copy", _P, _I, _P, _P, _P)(self.h, which, None, None, _ptr(out)))
         return out
 
+    def with_bp(self, cost_p, cost_q, lam):
+        """KernelOperator::with_bp(BpExtension::from_costs(...)) in place."""
+        cp, cq = _f64(cost_p), _f64(cost_q)
+        self.lib.check(self.lib.fn("op_with_bp", _P, _P, _SZ, _P, _SZ, C.c_double)(self.h, _ptr(cp), len(cp), _ptr(cq),
+                                                                                    len(cq), lam))
+        return self
+
     def log_matvec(self, v, transposed=False):
         v = _f64(v)
         out = np.zeros(self.m if transposed else self.n)
@@ -314,6 +321,9 @@ class Result:
     sp_vals = property(lambda s: s._v(5))
     sp_nys_vals = property(lambda s: s._v(6))
     dense_plan = property(lambda s: s._v(9))
+    del_p_mass = property(lambda s: s._v(10))
+    del_q_mass = property(lambda s: s._v(11))
+    eps_mass = property(lambda s: s._s(6))
 
     def grad_cost(self, which):
         f = self.lib.fn("grad_cost", _P, _P, _I, _P, _P, restype=_SZ)

@@ -15,6 +15,7 @@
 #include <exception>
 #include <memory>
 #include <random>
+#include <span>
 #include <string>
 #include <vector>
 
@@ -487,6 +488,7 @@ double ref_result_scalar(void* h, int which) {
         case 3: return s->marginal_err_final;
         case 4: return static_cast<double>(s->warnings.size());
         case 5: return static_cast<double>(s->state.marginal_err.size());
+        case 6: return s->plan.eps_mass;
     }
     return 0.0;
 }
@@ -507,6 +509,8 @@ std::size_t ref_result_copy(void* h, int which, double* out) {
         case 7: if (s->plan.p_u) v = &s->plan.p_u->data; break;
         case 8: if (s->plan.p_w) v = &s->plan.p_w->data; break;
         case 9: if (s->plan.dense) v = &s->plan.dense->data; break;
+        case 10: v = &s->plan.del_p_mass; break;
+        case 11: v = &s->plan.del_q_mass; break;
     }
     if (!v) return 0;
     if (out) std::memcpy(out, v->data(), v->size() * 8);
@@ -603,5 +607,15 @@ int ref_run_all_json(const char* config_json, char** out) {
 }
 
 void ref_free_string(char* p) { std::free(p); }
+
+// KernelOperator::with_bp (operator.cpp:103-115) with
+// BpExtension::from_costs (operator.cpp:33-43), replacing the handle's operator
+int ref_op_with_bp(void* h, const double* cost_p, std::size_t n, const double* cost_q, std::size_t m, double lambda) {
+    GUARD({
+        auto* r = static_cast<RefOp*>(h);
+        r->op = r->op.with_bp(BpExtension::from_costs(std::span<const double>(cost_p, n),
+                                                      std::span<const double>(cost_q, m), lambda));
+    })
+}
 
 }  // extern "C"

@@ -655,6 +655,35 @@ int lcn_op_destroy(lcn_op* op) {
     return LCN_OK;
 }
 
+int lcn_op_set_bp(lcn_op* op, const double* del_p, const double* del_q) {
+    lcn_ctx* ctx = op ? reinterpret_cast<lcn_ctx*>(op->o.ctx) : nullptr;
+    return guard(ctx, [&] {
+        if (!op) throw Status(2, "null operator");
+        Op& o = op->o;
+        if (!del_p && !del_q) {
+            o.bp = false;
+            return;
+        }
+        if (!del_p || !del_q) throw Status(1, "with_bp: deletion vector length mismatch");
+        if (o.ctx->nccl) throw Status(2, "with_bp: the BP extension is not available on a sharded context");
+        std::vector<double> lp(o.n), lq(o.m);
+        for (size_t i = 0; i < o.n; ++i) {
+            if (!(del_p[i] >= 0.0) || !std::isfinite(del_p[i]))
+                throw Status(2, "with_bp: deletion kernels must be finite and nonnegative");
+            lp[i] = std::log(del_p[i]);
+        }
+        for (size_t j = 0; j < o.m; ++j) {
+            if (!(del_q[j] >= 0.0) || !std::isfinite(del_q[j]))
+                throw Status(2, "with_bp: deletion kernels must be finite and nonnegative");
+            lq[j] = std::log(del_q[j]);
+        }
+        o.bp_ldp.upload(lp.data(), o.n, o.ctx->stream);
+        o.bp_ldq.upload(lq.data(), o.m, o.ctx->stream);
+        o.ctx->sync();
+        o.bp = true;
+    });
+}
+
 int lcn_op_get_info(const lcn_op* op, lcn_op_info_t* info) {
     if (!op || !info) return LCN_E_INVALID_ARGUMENT;
     const Op& o = op->o;
@@ -726,7 +755,7 @@ int lcn_sinkhorn(lcn_op* op, const double* p, const double* q, const lcn_sinkhor
             if (!(q[j] > 0.0) || !std::isfinite(q[j])) throw Status(2, "marginal q has a non-positive or non-finite entry");
             sq += q[j];
         }
-        if (std::abs(sp - sq) > 1e-12 * std::max(sp, sq))
+        if (!o.bp && std::abs(sp - sq) > 1e-12 * std::max(sp, sq))  // validate(balanced = !has_bp)
             throw Status(2, "marginals are unbalanced; balanced OT requires equal mass");
         SolveOptions so;
         if (opts) {
@@ -771,8 +800,9 @@ int lcn_sinkhorn(lcn_op* op, const double* p, const double* q, const lcn_sinkhor
                 std::fprintf(stderr, "lcn: warning: %s\n", res->r.warnings.back().c_str());
             }
         }
-        sinkhorn_solve(o, p, q, false, so, res->r);
-        if (so.want_plan) extract_plan_device(o, res->r);  // sinkhorn.cpp:23-100
+        if (o.bp) sinkhorn_solve_bp(o, p, q, so, res->r);
+        else sinkhorn_solve(o, p, q, false, so, res->r);
+        if (so.want_plan) extract_plan_device(o, res->r);  // sinkhorn.cpp:23-100 (base block under BP)
         *out = res.release();
     });
 }
@@ -834,6 +864,12 @@ int lcn_result_copy(const lcn_result* res, int which, double* out, size_t* len) 
         case 4: v = &r.plan_vals; break;
         case 5: v = &r.sp_vals; break;
         case 6: v = &r.sp_nys_vals; break;
+        case 7: v = &r.del_p_mass; break;
+        case 8: v = &r.del_q_mass; break;
+        case 9:
+            if (len) *len = 1;
+            if (out) *out = r.eps_mass;
+            return LCN_OK;
         default: return LCN_E_INVALID_ARGUMENT;
     }
     if (len) *len = v->size();

@@ -101,14 +101,21 @@ struct Op {
     DevBuf<uint32_t> csr_row_ptr, csr_col;
     bool csr_ready = false;
     std::shared_ptr<Solver> ws;           // persistent iteration workspace (sinkhorn.cu)
+    // BP extension (KernelOperator::with_bp, operator.cpp:103-115): log of the
+    // deletion kernels c_{p,eps} (n) and c_{eps,q} (m); set in place
+    bool bp = false;
+    DevBuf<double> bp_ldp, bp_ldq;
 
     BandView view(int b) const;
     BandSet bandset() const;
     const char* name() const { return kind == 1 ? "sparse" : kind == 2 ? "nystrom" : kind == 3 ? "lcn" : "dense"; }
+    std::string full_name() const { return std::string(name()) + (bp ? "+bp" : ""); }  // KernelOperator::name
 };
 
 struct Result {
     double distance = 0.0;
+    std::vector<double> del_p_mass, del_q_mass;  // BP plan quadrants (Plan, sinkhorn.hpp:47-51)
+    double eps_mass = 0.0;
     int iters = 0;
     bool converged = false;
     double marginal_err_final = 0.0;
@@ -173,5 +180,6 @@ void sinkhorn_solve(Op& op, const double* p, const double* q, bool device_ptrs, 
 void op_log_matvec(Op& op, const double* h_in, bool transposed, double* h_out);
 double distance_lcn_device(Op& op, const Result& res);
 void extract_plan_device(Op& op, Result& res);
+void sinkhorn_solve_bp(Op& op, const double* p, const double* q, const SolveOptions& o, Result& res);
 
 }  // namespace lcnb

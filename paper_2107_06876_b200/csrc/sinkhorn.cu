@@ -1484,6 +1484,118 @@ __global__ void log_kernel(const double* __restrict__ in, double* __restrict__ o
 // ---------------------------------------------------------------------------
 // Host driver
 // ---------------------------------------------------------------------------
+// ---- BP extension (operator.cpp:226-266, sinkhorn.cpp:115-120) -------------
+__device__ __forceinline__ double lse2_dev(double a, double b) {  // operator.cpp:14-19
+    if (a == kNegInf) return b;
+    if (b == kNegInf) return a;
+    const double hi = fmax(a, b);
+    return hi + log(exp(a - hi) + exp(b - hi));
+}
+
+// log sum exp of x (n), one CTA: max, then the shifted sum (operator.cpp:22-29)
+__global__ void __launch_bounds__(1024) lse_one_kernel(const double* __restrict__ x, long long n, double* __restrict__ out) {
+    __shared__ double red[32];
+    double hi = kNegInf;
+    for (long long i = threadIdx.x; i < n; i += 1024) hi = fmax(hi, x[i]);
+    for (int o = 16; o > 0; o >>= 1) hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = hi;
+    __syncthreads();
+    hi = kNegInf;
+    for (int k = 0; k < 32; ++k) hi = fmax(hi, red[k]);
+    __syncthreads();
+    double acc = 0.0;
+    if (hi != kNegInf)
+        for (long long i = threadIdx.x; i < n; i += 1024) acc += exp(x[i] - hi);
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int k = 0; k < 32; ++k) t += red[k];
+        *out = hi == kNegInf ? kNegInf : hi + log(t);
+    }
+}
+
+// K_BP v = [base + c_a (.) lower ; c_b (.) upper + (1^T lower) 1] in logs:
+// y[k < na] = lse2(base[k], lda[k] + lower[k]); y[na + k] = lse2(ldb[k] + upper[k], total).
+// out = log_marg - y (the scaling update) or y itself (log_marg == null);
+// non-finite outputs raise *bad.
+__global__ void bp_combine_kernel(const double* __restrict__ base, const double* __restrict__ lda,
+                                  const double* __restrict__ lower, const double* __restrict__ ldb,
+                                  const double* __restrict__ upper, const double* __restrict__ total, long long na,
+                                  long long nb, const double* __restrict__ log_marg, double* __restrict__ out,
+                                  unsigned* __restrict__ bad) {
+    const long long k = blockIdx.x * 256LL + threadIdx.x;
+    if (k >= na + nb) return;
+    const double y = k < na ? lse2_dev(base[k], lda[k] + lower[k]) : lse2_dev(ldb[k - na] + upper[k - na], *total);
+    const double v = log_marg ? log_marg[k] - y : y;
+    out[k] = v;
+    if (log_marg && !isfinite(v)) atomicOr(bad, 1u);
+}
+
+// row marginal exp(log s + K_BP t) and the partial of sum |rm - p|
+__global__ void bp_err_kernel(const double* __restrict__ ls, const double* __restrict__ kt, const double* __restrict__ p,
+                              long long rows, double* __restrict__ rm, double* __restrict__ part) {
+    __shared__ double red[8];
+    double e = 0.0;
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < rows; i += 256LL * gridDim.x) {
+        const double v = exp(ls[i] + kt[i]);
+        rm[i] = v;
+        e += fabs(v - p[i]);
+    }
+    e = warp_sum(e);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = e;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int k = 0; k < 8; ++k) t += red[k];
+        part[blockIdx.x] = t;
+    }
+}
+
+__global__ void sub_kernel(const double* __restrict__ a, const double* __restrict__ b, long long n,
+                           double* __restrict__ out, unsigned* __restrict__ bad) {
+    const long long i = blockIdx.x * 256LL + threadIdx.x;
+    if (i >= n) return;
+    const double v = a[i] - b[i];
+    out[i] = v;
+    if (!isfinite(v)) atomicOr(bad, 1u);
+}
+
+// BP plan quadrants (sinkhorn.cpp:82-98): deletion masses
+// del_p[i] exp(log s_i + log t_{m+i}), del_q[j] exp(log s_{n+j} + log t_j)
+__global__ void bp_mass_kernel(const double* __restrict__ ldp, const double* __restrict__ ldq,
+                               const double* __restrict__ ls, const double* __restrict__ lt, long long n, long long m,
+                               double* __restrict__ dpm, double* __restrict__ dqm) {
+    const long long k = blockIdx.x * 256LL + threadIdx.x;
+    if (k < n) dpm[k] = exp(ldp[k]) * exp(ls[k] + lt[m + k]);
+    else if (k < n + m) dqm[k - n] = exp(ldq[k - n]) * exp(ls[n + (k - n)] + lt[k - n]);
+}
+
+__global__ void exp_sum_partial_kernel(const double* __restrict__ x, long long n, double* __restrict__ part) {
+    __shared__ double red[8];
+    double acc = 0.0;
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += 256LL * gridDim.x) acc += exp(x[i]);
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int k = 0; k < 8; ++k) t += red[k];
+        part[blockIdx.x] = t;
+    }
+}
+
+__global__ void negate_kernel(double* __restrict__ x, long long n) {
+    const long long i = blockIdx.x * 256LL + threadIdx.x;
+    if (i < n) x[i] = -x[i];
+}
+
+__global__ void log_dev_kernel(const double* __restrict__ in, long long n, double* __restrict__ out) {
+    const long long i = blockIdx.x * 256LL + threadIdx.x;
+    if (i < n) out[i] = log(in[i]);
+}
+
 struct Solver {
     Op& op;
     Ctx& ctx;
@@ -2193,6 +2305,180 @@ struct Solver {
         res.distance = op.lambda * acc;
     }
 
+    // base_log_matvec(_t) (operator.cpp:123-224) between device vectors (d_in
+    // readable kRT entries past its length). LCN / Nystrom positivity failures
+    // are left in st->flags for the caller.
+    template <typename T>
+    void base_mv(const double* d_in, bool transposed, double* d_out) {
+        if (op.kind <= 1) {
+            if (!transposed) {
+                sparse_rows<T>(d_in);
+                sparse_row_finalize_kernel<<<ceil_div(n, 256), 256, 0, s>>>(st.get(), Mr.get(), Sr.get(), log_p.get(),
+                                                                            pv.get(), n, nullptr, log_s[1].get(), d_out,
+                                                                            nullptr, nullptr, 0);
+            } else {
+                sparse_cols<T>(d_in);
+                CUDA_OK(cudaMemsetAsync(log_t.get(), 0, m * 8, s));  // zero "log q": out = -kts
+                sparse_col_finalize_kernel<<<ceil_div(m, 256), 256, 0, s>>>(st.get(), Mc.get(), Sc.get(), log_t.get(), m,
+                                                                            d_out);
+                negate_kernel<<<ceil_div(m, 256), 256, 0, s>>>(d_out, m);
+            }
+            return;
+        }
+        PassArgs acc = base_args();
+        acc.mode = 2;
+        acc.in = d_in;
+        PassArgs mv = base_args();
+        mv.mode = 1;
+        mv.out = d_out;
+        if (!transposed) {
+            acc.rows = m;
+            pass<T, 1>(acc);
+            reduce(mid_t.get(), 0);
+            scatter_perm(d_in, m, 1, 0);
+            lcn_rows<T>();
+            mv.rows = n;
+            mv.mid = mid_t.get();
+            set_corr(mv, 0);
+            pass<T, 0>(mv);
+        } else {
+            acc.rows = n;
+            pass<T, 0>(acc);
+            reduce(mid_s.get(), 1);
+            scatter_perm(d_in, n, 0, 0);
+            lcn_cols<T>(0);
+            mv.rows = m;
+            mv.mid = mid_s.get();
+            set_corr(mv, 1);
+            pass<T, 1>(mv);
+        }
+    }
+
+    // sinkhorn (sinkhorn.cpp:104-188) with the BP extension: extended
+    // marginals [p; q] / [q; p], K_BP products from the base products plus the
+    // deletion diagonals and the eps-eps block (operator.cpp:226-266), on the
+    // device; one host check per product keeps the reference's error order.
+    template <typename T>
+    void run_bp(const double* in_p, const double* in_q, const SolveOptions& o, Result& res) {
+        if (comm) throw Status(2, "sinkhorn: the BP extension is not available on a sharded context");
+        alloc();
+        const long long R = n + m;  // rows of the extended problem (= columns)
+        const size_t pad = static_cast<size_t>(R) + 2 * kRT;
+        DevBuf<double> pe(pad), qe(pad), lpe(pad), lqe(pad), ls(pad), lt(pad), kt(pad), kts(pad), rm(pad), base(pad);
+        DevBuf<double> tot(1), part(256);
+        DevBuf<unsigned> bad(1);
+        for (DevBuf<double>* b : {&ls, &lt, &kt, &kts, &base}) b->zero(s);
+        CUDA_OK(cudaMemcpyAsync(pe.get(), in_p, n * 8, cudaMemcpyHostToDevice, s));
+        CUDA_OK(cudaMemcpyAsync(pe.get() + n, in_q, m * 8, cudaMemcpyHostToDevice, s));
+        CUDA_OK(cudaMemcpyAsync(qe.get(), in_q, m * 8, cudaMemcpyHostToDevice, s));
+        CUDA_OK(cudaMemcpyAsync(qe.get() + m, in_p, n * 8, cudaMemcpyHostToDevice, s));
+        log_dev_kernel<<<ceil_div(R, 256), 256, 0, s>>>(pe.get(), R, lpe.get());
+        log_dev_kernel<<<ceil_div(R, 256), 256, 0, s>>>(qe.get(), R, lqe.get());
+        double mass = 0.0;
+        for (long long i = 0; i < n; ++i) mass += in_p[i];
+        for (long long j = 0; j < m; ++j) mass += in_q[j];
+        mass *= 2.0;  // sum of [p; q] and [q; p]
+        const double tol = o.tol >= 0.0 ? o.tol : 1e-6 * mass;
+        const std::string name = op.full_name();
+        auto check_neg = [&](bool transposed) {
+            DevState h{};
+            st.download(&h, 1, s);
+            ctx.sync();
+            const unsigned f = h.flags;
+            if (op.kind >= 2) {
+                if (!transposed && (f & (F_NEG_ROW | F_NYS_ROW)))
+                    throw Status(4, std::string(op.name()) + " matvec produced a nonpositive entry");
+                if (transposed && (f & (F_NEG_COL | F_NYS_COL)))
+                    throw Status(4, std::string(op.name()) + " transposed matvec produced a nonpositive entry");
+            }
+        };
+        auto check_bad = [&](const char* which) {
+            unsigned hb = 0;
+            bad.download(&hb, 1, s);
+            ctx.sync();
+            if (hb) throw Status(3, std::string("sinkhorn: non-finite scaling (") + which + ") under the " + name +
+                                        " operator");
+        };
+        const int gR = static_cast<int>(ceil_div(R, 256));
+        // kt = K_BP(log t); y written to `out` (log_marg null) or the update log_marg - y
+        auto kbp = [&](const double* ltv, const double* log_marg, double* out) {
+            base_mv<T>(ltv, false, base.get());  // K t^ (upper m entries of t)
+            lse_one_kernel<<<1, 1024, 0, s>>>(ltv + m, n, tot.get());
+            bp_combine_kernel<<<gR, 256, 0, s>>>(base.get(), op.bp_ldp.get(), ltv + m, op.bp_ldq.get(), ltv, tot.get(),
+                                                 n, m, log_marg, out, bad.get());
+            check_neg(false);
+        };
+        auto kbpt = [&](const double* lsv, const double* log_marg, double* out) {
+            base_mv<T>(lsv, true, base.get());  // K^T s^ (upper n entries of s)
+            lse_one_kernel<<<1, 1024, 0, s>>>(lsv + n, m, tot.get());
+            bp_combine_kernel<<<gR, 256, 0, s>>>(base.get(), op.bp_ldq.get(), lsv + n, op.bp_ldp.get(), lsv, tot.get(),
+                                                 m, n, log_marg, out, bad.get());
+            check_neg(true);
+        };
+        bad.zero(s);
+        kbp(lt.get(), nullptr, kt.get());
+        res.err_trace.clear();
+        bool converged = false;
+        double err = std::numeric_limits<double>::infinity();
+        int iter = 0;
+        std::vector<double> hp(256);
+        while (iter < o.max_iters) {
+            ++iter;
+            // log s = log p - kt (the BP product of the previous log t)
+            sub_kernel<<<gR, 256, 0, s>>>(lpe.get(), kt.get(), R, ls.get(), bad.get());
+            check_bad("log s");
+            kbpt(ls.get(), lqe.get(), lt.get());
+            check_bad("log t");
+            kbp(lt.get(), nullptr, kt.get());
+            bp_err_kernel<<<256, 256, 0, s>>>(ls.get(), kt.get(), pe.get(), R, rm.get(), part.get());
+            part.download(hp.data(), 256, s);
+            ctx.sync();
+            err = 0.0;
+            for (double v : hp) err += v;
+            res.err_trace.push_back(err);
+            if (err <= tol) {
+                converged = true;
+                break;
+            }
+        }
+        res.iters = iter;
+        res.converged = converged;
+        res.marginal_err_final = err;
+        res.n = n;
+        res.m = m;
+        res.log_s.resize(R);
+        res.log_t.resize(R);
+        res.row_marg.resize(R);
+        ls.download(res.log_s.data(), R, s);
+        lt.download(res.log_t.data(), R, s);
+        rm.download(res.row_marg.data(), R, s);
+        // distance = lambda (<log s, P1> + <log t, q_ext>) (sinkhorn.cpp:178-183)
+        dot_partial_kernel<<<64, 256, 0, s>>>(ls.get(), rm.get(), R, part.get());
+        dot_partial_kernel<<<64, 256, 0, s>>>(lt.get(), qe.get(), R, part.get() + 64);
+        part.download(hp.data(), 128, s);
+        ctx.sync();
+        double acc = 0.0;
+        for (int k = 0; k < 128; ++k) acc += hp[k];
+        res.distance = op.lambda * acc;
+        if (o.want_plan) {
+            DevBuf<double> dpm(n), dqm(m);
+            bp_mass_kernel<<<gR, 256, 0, s>>>(op.bp_ldp.get(), op.bp_ldq.get(), ls.get(), lt.get(), n, m, dpm.get(),
+                                              dqm.get());
+            exp_sum_partial_kernel<<<64, 256, 0, s>>>(ls.get() + n, m, part.get());
+            exp_sum_partial_kernel<<<64, 256, 0, s>>>(lt.get() + m, n, part.get() + 64);
+            res.del_p_mass.resize(n);
+            res.del_q_mass.resize(m);
+            dpm.download(res.del_p_mass.data(), n, s);
+            dqm.download(res.del_q_mass.data(), m, s);
+            part.download(hp.data(), 128, s);
+            ctx.sync();
+            double ss = 0.0, tt = 0.0;
+            for (int k = 0; k < 64; ++k) ss += hp[k];
+            for (int k = 64; k < 128; ++k) tt += hp[k];
+            res.eps_mass = ss * tt;
+        }
+    }
+
     // log_matvec / log_matvec_t (operator.cpp:226-252) on a host vector.
     template <typename T>
     void matvec(const double* h_in, bool transposed, double* h_out) {
@@ -2282,6 +2568,13 @@ void sinkhorn_solve(Op& op, const double* p, const double* q, bool device_ptrs, 
     Solver& sv = solver_of(op);
     if (op.fp64) sv.run<double>(p, q, device_ptrs, o, res);
     else sv.run<float>(p, q, device_ptrs, o, res);
+}
+
+void sinkhorn_solve_bp(Op& op, const double* p, const double* q, const SolveOptions& o, Result& res) {
+    if (o.max_iters < 1) throw Status(2, "sinkhorn: max_iters must be >= 1");
+    Solver& sv = solver_of(op);
+    if (op.fp64) sv.run_bp<double>(p, q, o, res);
+    else sv.run_bp<float>(p, q, o, res);
 }
 
 void op_log_matvec(Op& op, const double* h_in, bool transposed, double* h_out) {

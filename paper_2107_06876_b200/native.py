@@ -149,6 +149,7 @@ def library() -> C.CDLL:
             "lcn_grad_cost": ([P, P, I, P, C.POINTER(SZ), C.POINTER(I)], I),
             "lcn_multihead": ([P, P, SZ, P, SZ, SZ, I, D, I, P, P, C.POINTER(_SinkOpts), P, P, P, P, P], I),
             "lcn_ctx_set_comm": ([P, I, I, P], I),
+            "lcn_op_set_bp": ([P, P, P], I),
         }
         for name, (args, res) in sig.items():
             f = getattr(lib, name)
@@ -205,9 +206,23 @@ class Context:
         self.check(self.lib.lcn_ctx_set_comm(self.h, int(world), int(rank), C.addressof(buf)))
 
     def close(self):
+        # live operators keep a pointer to the context: its destruction waits
+        # for the last one (finalizers run in any order in cyclic collection,
+        # after weak references are cleared)
         if getattr(self, "h", None):
+            if getattr(self, "_live", 0) > 0:
+                self._close_pending = True
+                return
             self.lib.lcn_ctx_destroy(self.h)
             self.h = None
+
+    def _adopt(self, child):
+        self._live = getattr(self, "_live", 0) + 1
+
+    def _release(self):
+        self._live -= 1
+        if self._live == 0 and getattr(self, "_close_pending", False):
+            self.close()
 
     def __del__(self):
         try:
@@ -397,6 +412,7 @@ class KernelOperator:
 
     def __init__(self, ctx: Context, h):
         self.ctx, self.h = ctx, h
+        ctx._adopt(self)
         info = _OpInfo()
         ctx.check(ctx.lib.lcn_op_get_info(self.h, C.byref(info)))
         self.info = info
@@ -516,6 +532,16 @@ class KernelOperator:
         self.ctx.check(self.ctx.lib.lcn_op_export_factor(self.h, which, _p(out)))
         return out
 
+    def with_bp(self, cost_p, cost_q):
+        """KernelOperator::with_bp(BpExtension::from_costs(cost_p, cost_q, lambda))
+        (operator.cpp:33-43, 103-115), applied to this operator in place."""
+        cp, cq = _f64(cost_p, (self.n,)), _f64(cost_q, (self.m,))
+        if not (self.lam > 0.0):
+            raise InvalidArgument("BpExtension: lambda must be positive")
+        dp, dq = np.exp(-cp / self.lam), np.exp(-cq / self.lam)
+        self.ctx.check(self.ctx.lib.lcn_op_set_bp(self.h, _p(dp), _p(dq)))
+        return self
+
     def log_matvec(self, log_t):
         v = _f64(log_t)
         if v.shape != (self.m,):
@@ -536,6 +562,7 @@ class KernelOperator:
         if getattr(self, "h", None):
             self.ctx.lib.lcn_op_destroy(self.h)
             self.h = None
+            self.ctx._release()
 
     def __del__(self):
         try:
@@ -580,6 +607,9 @@ class SinkhornResult:
     sparse_vals = property(lambda s: s._vec(4))
     sp_vals = property(lambda s: s._vec(5))
     sp_nys_vals = property(lambda s: s._vec(6))
+    del_p_mass = property(lambda s: s._vec(7))
+    del_q_mass = property(lambda s: s._vec(8))
+    eps_mass = property(lambda s: float(s._vec(9)[0]))
 
     def close(self):
         if getattr(self, "h", None):

@@ -11,9 +11,8 @@ reference when n m <= 10^6 for rel-err-d, PCC and top-0.1% IoU
 (write_outputs, :420-445). Every operator and solve runs through the C-ABI on
 the GPU; plans are densified and compared on the device. Records run in
 order on one context (the reference's worker pool shares its CPU cores; here
-the variants share one GPU). The BP extension is not on this path: a `bp`
-config yields a per-record error, as a failing variant does in the
-reference.
+the variants share one GPU). `bp` configs run the BP-extended solve
+(KernelOperator::with_bp) with the scalar deletion cost on both sides.
 """
 from __future__ import annotations
 
@@ -252,8 +251,8 @@ def run_one(ctx: N.Context, c: RunConfig, variant: str, seed: int, sc: _SeedCont
                                               _LANDMARKS[c.landmark_method], mix_seed(seed, 4))
         else:
             raise N.InvalidArgument(f"unknown variant '{variant}'")
-        if c.bp:
-            raise N.InvalidArgument("the BP extension (operator.cpp:226-266) is not available on the GPU path")
+        if c.bp:  # runner.cpp:282-286: scalar deletion cost on both sides
+            op.with_bp(np.full(n, c.deletion_cost), np.full(m, c.deletion_cost))
         ms_kernel = (time.perf_counter() - t0) * 1e3
         t1 = time.perf_counter()
         if c.heads > 1 and variant == "full":

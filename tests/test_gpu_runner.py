@@ -72,10 +72,9 @@ def test_runner_files_and_outputs(ref, tmp_path):
     assert code == (2 if any("error" in r for r in recs) else 0)
 
 
-def test_runner_bp_is_a_record_error(tmp_path):
-    cfg = {"problem": {"generator": "uniform-ball", "n": 50, "d": 2}, "variants": ["full"], "bp": {"enabled": True},
-           "seeds": [1], "output": str(tmp_path / "o.csv")}
-    c = runner.config_from_json(cfg)
-    recs = runner.run_all(c, lcn.Context(0))
-    assert "BP extension" in recs[0]["error"] and recs[0]["error"].endswith("[variant=full seed=1]")
-    assert runner.write_outputs(c, recs) == 2
+def test_runner_bp_matches_reference(ref):
+    cfg = {"problem": {"generator": "clustered", "n": 120, "d": 3, "c": 3, "D": 6.0, "r": 1.0},
+           "variants": ["full", "sparse", "lcn", "nystrom"], "lambda": 0.4, "bp": {"enabled": True, "deletion-cost": 2.5},
+           "budget": {"neighbors": 20, "landmarks": 10}, "max-iters": 150, "seeds": [4], "strict-deterministic": True}
+    ours = runner.run_all(runner.config_from_json(cfg), lcn.Context(0, store_fp64=True))
+    compare(ours, ref.run_all_json(cfg))
