@@ -907,6 +907,13 @@ __global__ void outer_kernel(const double* __restrict__ x, long long rows, const
 }
 }  // namespace
 
+namespace {
+__global__ void exp_inplace_kernel(double* __restrict__ x, long long n) {
+    const long long i = blockIdx.x * 256LL + threadIdx.x;
+    if (i < n) x[i] = exp(x[i]);
+}
+}  // namespace
+
 int lcn_grad_cost(const lcn_result* res, const lcn_op* op, int which, double* out, size_t* len, int* stale) {
     lcn_ctx* ctx = op ? reinterpret_cast<lcn_ctx*>(op->o.ctx) : nullptr;
     return guard(ctx, [&] {
@@ -940,13 +947,12 @@ int lcn_grad_cost(const lcn_result* res, const lcn_op* op, int which, double* ou
         *len = count;
         if (!out) return;
         cudaStream_t s = o.ctx->stream;
-        // s_i = exp(log s_i), t_j = exp(log t_j); wt = W t, su = U^T s
-        std::vector<double> sl(n), tl(m);
-        for (size_t i = 0; i < n; ++i) sl[i] = std::exp(r.log_s[i]);
-        for (size_t j = 0; j < m; ++j) tl[j] = std::exp(r.log_t[j]);
+        // s_i = exp(log s_i), t_j = exp(log t_j) on the device; wt = W t, su = U^T s
         DevBuf<double> ds, dt, wt(l), su(l), g(count);
-        ds.upload(sl.data(), n, s);
-        dt.upload(tl.data(), m, s);
+        ds.upload(r.log_s.data(), n, s);
+        dt.upload(r.log_t.data(), m, s);
+        exp_inplace_kernel<<<ceil_div(n, 256), 256, 0, s>>>(ds.get(), static_cast<long long>(n));
+        exp_inplace_kernel<<<ceil_div(m, 256), 256, 0, s>>>(dt.get(), static_cast<long long>(m));
         wt.zero(s);
         su.zero(s);
         const dim3 gs(static_cast<unsigned>(ceil_div(l, 128)), 64);
