@@ -306,7 +306,7 @@ def test_grad_cost(ref):
 
 
 @pytest.mark.parametrize("layout", [{"LCN_PANEL_W": "1", "LCN_PANEL_A": "0"}, {},
-                                    {"LCN_PANEL_W": "1000000"}, {"LCN_PANELS": "0"}])
+                                    {"LCN_PANEL_W": "1000000"}, {"LCN_PANELS": "0"}, {"LCN_BAND_STATIC": "1"}])
 @pytest.mark.parametrize("shape", ["c3", "three_bands", "wide"])
 def test_lcn_panel_layouts(ref, monkeypatch, layout, shape):
     """The band streams of later bands skip the pairs band 0 already holds
@@ -362,3 +362,24 @@ def test_lcn_bands_without_two_sided_buckets(ref):
     res = lcn.sinkhorn(op, pm, qm, lcn.SinkhornOptions(tol=0.0, max_iters=30))
     rres = rop.sinkhorn(pm, qm, tol=0.0, max_iters=30)
     assert rel(res.distance, rres.distance) <= REL_FP32
+
+
+def test_band_claim_order_does_not_change_results(monkeypatch):
+    """Dynamic item claims (default) and static per-CTA ranges give bit-identical
+    iterations: unsplit outputs are plain stores and split outputs are
+    combined in piece order, whatever CTA processed them."""
+    import dataclasses
+    pr = dataclasses.replace(configs.config3(0.004), bands=2, buckets=3, landmarks=32, iters=30)
+    out = []
+    for static in (False, True):
+        if static:
+            monkeypatch.setenv("LCN_BAND_STATIC", "1")
+        c = lcn.Context(0, store_fp64=False)
+        cfg = lcn.LshConfig(pr.bands, 1, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
+        op = lcn.KernelOperator.lcn_lsh(c, pr.p, pr.q, pr.cost, pr.lam_eff, cfg, pr.landmarks, lcn.LANDMARK_KMEANS,
+                                        pr.landmark_seed)
+        pm, qm = pr.marginals()
+        res = lcn.sinkhorn(op, pm, qm, lcn.SinkhornOptions(tol=0.0, max_iters=pr.iters))
+        out.append((res.distance, res.log_s.copy()))
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1].view(np.uint64), out[1][1].view(np.uint64))
