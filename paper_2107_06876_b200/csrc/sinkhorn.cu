@@ -1768,7 +1768,11 @@ struct Solver {
             lens(k, sl, ol);
             if (sl && ol) total += cost_of(sl, row_stride(ol));
         }
-        const double cap = std::max(total / band_grid / 2.0, 65536.0);
+        static const double cap_div = [] {  // pieces per CTA share (LCN_BAND_CAP_DIV; 4 measured ~2 % faster than 2)
+            const char* e = std::getenv("LCN_BAND_CAP_DIV");
+            return e && *e ? std::max(1.0, std::atof(e)) : 4.0;
+        }();
+        const double cap = std::max(total / band_grid / cap_div, 65536.0);
         struct Piece { BandItem it; double cost; };
         std::vector<Piece> pieces;
         std::vector<uint2> splits;
