@@ -49,6 +49,10 @@ import numpy as np  # noqa: E402
 
 ITERS = 100
 CPU_SAMPLE_SCALE = 0.01
+# what the headline arithmetic is (bench's `dtype`): delta, U and W stored in
+# fp32; products and per-chunk partial sums in fp32; rows / tiles / chunks
+# combined in fp64; log vectors, shifts and global reductions in fp64
+DTYPE_LABEL = "f32 storage, f32 products + per-chunk partials, f64 cross-chunk accumulation and log vectors"
 
 
 def peaks():
@@ -316,20 +320,43 @@ def batched_c4(lcn, ctx, with_cpu):
         try:
             from oracle.bindings import RefLib, ref_available
             if ref_available():
+                import ctypes
+                import threading
                 ref = RefLib()
-                os.environ["OMP_NUM_THREADS"] = "1"
-                k_s, t0 = 0, time.perf_counter()
-                while k_s < b.count and (time.perf_counter() - t0 < 3.0 or k_s < 64):
-                    p_, q_ = b.problem(k_s)
-                    try:
-                        ref.lcn_problem(p_, q_, b.cost, b.lam, b.buckets, b.kmeans_iters, b.lsh_seed(k_s),
-                                        b.landmarks, b.landmark_seed(k_s), b.iters)
-                    except Exception:
-                        pass
-                    k_s += 1
+                gomp = ctypes.CDLL("libgomp.so.1")
+                cores = cpu_cores()
+                nxt, lock, done = [0], threading.Lock(), [0]
+                t0 = time.perf_counter()
+
+                def worker():
+                    # one problem per host thread: each solve single-threaded (the
+                    # reference's loop over heads is serial, sinkhorn.cpp:341-351);
+                    # omp_set_num_threads sets this thread's OpenMP team size
+                    gomp.omp_set_num_threads(1)
+                    while True:
+                        with lock:
+                            k = nxt[0]
+                            if k >= b.count or (time.perf_counter() - t0 > 5.0 and k >= 64 * cores):
+                                return
+                            nxt[0] += 1
+                        p_, q_ = b.problem(k)
+                        try:
+                            ref.lcn_problem(p_, q_, b.cost, b.lam, b.buckets, b.kmeans_iters, b.lsh_seed(k),
+                                            b.landmarks, b.landmark_seed(k), b.iters)
+                        except Exception:
+                            pass
+                        with lock:
+                            done[0] += 1
+
+                th = [threading.Thread(target=worker) for _ in range(cores)]
+                for t_ in th:
+                    t_.start()
+                for t_ in th:
+                    t_.join()
                 tw = time.perf_counter() - t0
-                out["cpu_baseline"] = {"value": k_s / tw, "unit": "problems/s", "cores": 1, "kind": "reference",
-                                       "sample": f"the first {k_s} problems of the batch, {tw:.2f} s"}
+                out["cpu_baseline"] = {"value": done[0] / tw, "unit": "problems/s", "cores": cores, "kind": "reference",
+                                       "sample": f"the first {done[0]} problems of the batch on {cores} host threads "
+                                                 f"(one problem per thread), {tw:.2f} s"}
         except Exception as ex:
             out["cpu_baseline"] = {"value": None, "sample": f"unavailable: {ex}"}
     return out
@@ -508,31 +535,77 @@ def run_ours(args, rank, world, local_rank):
     t_iter = (ms_per_step / 1e3) / ITERS
     it_achieved = b_iter / t_iter / 1e9
 
-    # ---- e2e through the C-ABI from pinned host buffers ----------------------
+    # ---- fp64 storage (LCN_STORE_FP64: the reference's precision) -------------
+    fp64_line = None
+    if not args.no_fp64:
+        del op
+        torch.cuda.synchronize()
+        ctx64 = lcn.Context(local_rank, store_fp64=True)
+        ctx64.set_stream(stream.cuda_stream)
+        if sharded:  # a fresh NCCL id per communicator
+            obj64 = [lcn.nccl_unique_id() if rank == 0 else None]
+            if world > 1:
+                dist.broadcast_object_list(obj64, src=0)
+            ctx64.set_comm(world, rank, obj64[0])
+        op64 = lcn.KernelOperator.from_device(ctx64, dp.data_ptr(), n, dq.data_ptr(), m, d, pr.cost, pr.lam_eff, cfg, l,
+                                              lcn.LANDMARK_KMEANS, pr.landmark_seed)
+        k64 = max(3, min(args.steps, 5))
+        r64 = lcn.sinkhorn_device(op64, dpm.data_ptr(), dqm.data_ptr(), opts)  # warm-up
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a64, b64 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a64.record(stream)
+        for _ in range(k64):
+            r64 = lcn.sinkhorn_device(op64, dpm.data_ptr(), dqm.data_ptr(), opts)
+        b64.record(stream)
+        torch.cuda.synchronize()
+        el64 = a64.elapsed_time(b64) / 1e3
+        if world > 1:
+            tt = torch.tensor([el64], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            el64 = float(tt.item())
+        t_it64 = el64 / (k64 * ITERS)
+        b_iter64 = 16 * nnz + 8 * l * (n + m) + 16 * (n + m)
+        fp64_line = {"value": (1 if sharded else world) * ITERS * k64 / el64, "unit": "iter/s", "steps": k64,
+                     "ms_per_iteration": t_it64 * 1e3, "distance": r64.distance / pr.mu,
+                     "dtype": "f64 storage and arithmetic (LCN_STORE_FP64)",
+                     "iteration_roofline": {"bound": "hbm", "achieved": b_iter64 / t_it64 / 1e9, "peak": hbm,
+                                            "unit": "GB/s", "frac": b_iter64 / t_it64 / 1e9 / hbm,
+                                            "algorithmic_bytes_per_iteration": b_iter64}}
+        del r64, op64
+        ctx64.close()
+        torch.cuda.synchronize()
+
+    # ---- e2e through the reference-facing C-ABI from pinned host buffers -------
+    # lcn_op_lcn_lsh (fp64 host points, as the reference's PointSet) + lcn_sinkhorn
+    # (host marginals, Marginals::validate on the host, no plan): the call a
+    # caller of lsh_neighbor_pairs / select_landmarks / build_factors /
+    # build_correction / sinkhorn makes
     e2e = None
     dist_roof = None
     dist_iv = None
     if not args.no_e2e:
-        del op
+        if fp64_line is None:
+            del op
         torch.cuda.synchronize()
-        h2d = int(p32.numel() * 4 + q32.numel() * 4 + pm_h.numel() * 8 + qm_h.numel() * 8)
+        p64 = torch.from_numpy(pr.p).pin_memory().numpy()
+        q64 = torch.from_numpy(pr.q).pin_memory().numpy()
+        pm64 = torch.from_numpy(pm).pin_memory().numpy()
+        qm64 = torch.from_numpy(qm).pin_memory().numpy()
+        h2d = int(p64.nbytes + q64.nbytes + pm64.nbytes + qm64.nbytes)
         tot = 0.0
-        # one untimed warm-up solve (first-use costs: pool growth, pinned
-        # staging), then e2e_steps timed ones
+        # untimed warm-up solves (first-use costs: pool growth), then e2e_steps timed ones
         for it in range(args.e2e_warmup + args.e2e_steps):
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            with torch.cuda.stream(stream):
-                xp = p32.to(dev, non_blocking=True)
-                xq = q32.to(dev, non_blocking=True)
-                xpm = pm_h.to(dev, non_blocking=True)
-                xqm = qm_h.to(dev, non_blocking=True)
+
             def build2():
-                return lcn.KernelOperator.from_device(ctx, xp.data_ptr(), n, xq.data_ptr(), m, d, pr.cost,
-                                                      pr.lam_eff, cfg, l, lcn.LANDMARK_KMEANS, pr.landmark_seed)
+                return lcn.KernelOperator.lcn_lsh(ctx, p64, q64, pr.cost, pr.lam_eff, cfg, l, lcn.LANDMARK_KMEANS,
+                                                  pr.landmark_seed)
             if it == 0 and args.e2e_warmup > 0:
                 # the untimed warm-up build doubles as the tensor-core trace
                 holder = []
@@ -544,8 +617,8 @@ def run_ours(args, rank, world, local_rank):
                 op2 = holder[0] if holder else build2()
             else:
                 op2 = build2()
-            r2 = lcn.sinkhorn_device(op2, xpm.data_ptr(), xqm.data_ptr(), opts)
-            _ = r2.distance  # host scalar read (the 8-byte result)
+            r2 = lcn.sinkhorn(op2, pm64, qm64, opts)  # distance read back to the host (8 B)
+            _ = r2.distance
             b.record(stream)
             torch.cuda.synchronize()
             dt = a.elapsed_time(b) / 1e3
@@ -559,8 +632,9 @@ def run_ours(args, rank, world, local_rank):
         e2e = {"value": (1 if sharded else world) * ITERS * args.e2e_steps / tot, "unit": "iter/s",
                "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": 8, "solve_s": tot / args.e2e_steps, "steps": args.e2e_steps,
-               "warmup": args.e2e_warmup,
-               "covers": "H2D points+marginals, k-means LSH, landmarks, Nystrom, correction, 100 iterations, D2H distance"}
+               "warmup": args.e2e_warmup, "entry": "lcn_op_lcn_lsh + lcn_sinkhorn (host fp64 buffers, pinned)",
+               "covers": "H2D fp64 points + marginals, k-means LSH, landmarks, Nystrom, correction, 100 iterations, "
+                         "D2H distance"}
 
     # ---- CPU baseline (rank 0, N = 1) ------------------------------------------
     cpu = None
@@ -603,7 +677,7 @@ def run_ours(args, rank, world, local_rank):
         line = {"metric": "lcn_sinkhorn_iters_per_s", "value": value, "unit": "iter/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "strong" if sharded else "weak", "vs_baseline": None,
-                "dtype": "f32-storage/f64-accumulate", "data": "synthetic",
+                "dtype": DTYPE_LABEL, "data": "synthetic",
                 "config": {"workload": "configs[3] LCN-Sinkhorn n=m=1e6 d=128 sqL2/mean lambda=0.05 2x4096 LSH l=512",
                            "n": n, "m": m, "d": d, "landmarks": l, "bands": pr.bands, "buckets": pr.buckets,
                            "iterations_per_step": ITERS, "nnz": nnz, "stored_entries": stored, "streamed_entries": streamed,
@@ -627,12 +701,31 @@ def run_ours(args, rank, world, local_rank):
                 "batched_c4": c4,
                 "dense_anchor": anchor,
                 "phases_ms_per_iteration": per_it,
+                "fp64_storage": fp64_line,
                 "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": gpu_launches}
         emit(line)
     return 0
 
 
 _OUT_FD = None
+
+
+def spawn_ranks(n):
+    """`python bench.py --gpus N` outside torchrun: re-launch this command as
+    N ranks (one process per GPU) through torch.distributed.run on 127.0.0.1,
+    the way the driver launches it, with NCCL's init lines on stderr."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    print("bench: spawning", " ".join(cmd), file=sys.stderr, flush=True)
+    # rank 0 writes the JSON line to its stdout; pass the original stdout through
+    return subprocess.call(cmd, env=env, stdout=_OUT_FD if _OUT_FD is not None else None)
 
 
 def emit(line):
@@ -661,17 +754,27 @@ def main():
     ap.add_argument("--no-dense", action="store_true", help="skip the configs[2] dense-anchor object")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-fp64", action="store_true", help="skip the LCN_STORE_FP64 iteration line")
+    ap.add_argument("--dry-run", action="store_true", help="print the rank layout and exit (launch check)")
     ap.add_argument("--sharded", action="store_true",
                     help="use the sharded solve even on one GPU (1-rank communicator)")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent problems per GPU instead of one sharded problem")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dry_run:  # launch check only: which rank am I, out of how many
+        if rank == 0 or world == 1:
+            emit({"dry_run": True, "n_gpus": world, "rank": rank, "local_rank": local_rank})
+        return 0
     if args.impl == "reference":
         return run_reference(args, rank, world)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # NCCL's init lines (rings, NVLS) go to stderr
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)

@@ -393,6 +393,60 @@ class RefLib(CheckerLib):
         self.check(self.fn("sample_uniform_ball", _SZ, _SZ, _U64, _P)(n, d, seed, _ptr(out)))
         return out
 
+    # ---- full-size parity (oracle/parity_c3.py) ---------------------------
+    def hash_kmeans_band(self, all_pts, buckets, iters, seed, band):
+        """One band of the k-means LSH on the union (lsh.cpp:267-281)."""
+        all_pts = _f64(all_pts)
+        ids = np.zeros(all_pts.shape[0], np.uint64)
+        self.check(self.fn("hash_kmeans_band", _P, _SZ, _SZ, _I, _I, _U64, _I, _P)(
+            _ptr(all_pts), all_pts.shape[0], all_pts.shape[1], buckets, iters, seed, band, _ptr(ids)))
+        return ids
+
+    def select_landmarks(self, p, q, l, method, seed):
+        """select_landmarks (nystrom.cpp:28-48) -> l x d."""
+        p, q = _f64(p), _f64(q)
+        out = np.zeros((l, p.shape[1]))
+        self.check(self.fn("select_landmarks", _P, _SZ, _P, _SZ, _SZ, _SZ, _I, _U64, _P)(
+            _ptr(p), p.shape[0], _ptr(q), q.shape[0], p.shape[1], l, method, seed, _ptr(out)))
+        return out
+
+    def lcn_pipeline(self, p, q, kind, lam, ids_p, ids_q, range_, landmarks):
+        """neighbor_pairs(BandBuckets) -> build_sparse -> build_factors ->
+        build_correction -> KernelOperator::lcn; returns (Op, phase seconds)."""
+        p, q, lm = _f64(p), _f64(q), _f64(landmarks)
+        ids_p = np.ascontiguousarray(ids_p, np.uint64)
+        ids_q = np.ascontiguousarray(ids_q, np.uint64)
+        h = _P()
+        ph = np.zeros(4)
+        self.check(self.fn("lcn_pipeline", _P, _SZ, _P, _SZ, _SZ, _I, _D, _P, _P, _I, _U64, _P, _SZ, _P, _PP)(
+            _ptr(p), p.shape[0], _ptr(q), q.shape[0], p.shape[1], kind, lam, _ptr(ids_p), _ptr(ids_q),
+            ids_p.shape[0], range_, _ptr(lm), lm.shape[0], _ptr(ph), C.byref(h)))
+        phases = dict(zip(["neighbor_pairs", "build_sparse", "build_factors", "build_correction"], ph / 1e3))
+        return Op(self, h, p.shape[0], q.shape[0], "lcn", lm.shape[0]), phases
+
+    def row_digest(self, op):
+        """Per-row (count, sum mix64(col), xor mix64(col)) of the support."""
+        cnt = np.zeros(op.n, np.uint32)
+        hs = np.zeros(op.n, np.uint64)
+        hx = np.zeros(op.n, np.uint64)
+        self.check(self.fn("op_row_digest", _P, _P, _P, _P)(op.h, _ptr(cnt), _ptr(hs), _ptr(hx)))
+        return cnt, hs, hx
+
+    def plan_rows(self, op, res, rows, counts):
+        """extract_plan entries of the listed rows: dict of cols, log_sp,
+        delta, sp_vals, sp_nys_vals (flat, row after row)."""
+        rows = np.ascontiguousarray(rows, np.uint32)
+        tot = int(np.asarray(counts, np.int64)[rows].sum())
+        cnt = np.zeros(len(rows), np.uint32)
+        out = {"cols": np.zeros(tot, np.uint32)}
+        for k in ("log_sp", "delta", "sp_vals", "sp_nys_vals"):
+            out[k] = np.zeros(tot)
+        self.check(self.fn("plan_rows", _P, _P, _P, _SZ, _P, _P, _P, _P, _P, _P)(
+            op.h, res.h, _ptr(rows), len(rows), _ptr(cnt), _ptr(out["cols"]), _ptr(out["log_sp"]),
+            _ptr(out["delta"]), _ptr(out["sp_vals"]), _ptr(out["sp_nys_vals"])))
+        out["cnt"] = cnt
+        return out
+
 
 class OracleLib(CheckerLib):
     prefix = "orc_"

@@ -608,6 +608,146 @@ int ref_run_all_json(const char* config_json, char** out) {
 
 void ref_free_string(char* p) { std::free(p); }
 
+// ---- full-size parity (configs[3] at n = m = 1e6, tests/ and oracle/parity_c3.py) ----
+
+// One band of the k-means LSH on the union (lsh.cpp:267-281): hash_kmeans
+// with fn_seed(seed, band, 0). Separate entry so the bands can run on
+// separate host threads (the reference loops them; ids do not depend on it).
+int ref_hash_kmeans_band(const double* all, std::size_t N, std::size_t d, int buckets, int iters, std::uint64_t seed,
+                         int band, std::uint64_t* ids) {
+    GUARD({
+        PointSet ps = make_points(all, N, d, "union");
+        LshConfig sub = kmeans_cfg(1, buckets, iters, fn_seed(seed, band, 0));
+        auto a = hash_kmeans(ps, sub);
+        for (std::size_t i = 0; i < N; ++i) ids[i] = a[i];
+    })
+}
+
+// select_landmarks (nystrom.cpp:28-48); out: l x d.
+int ref_select_landmarks(const double* p, std::size_t n, const double* q, std::size_t m, std::size_t d,
+                         std::size_t l, int method, std::uint64_t seed, double* out) {
+    GUARD({
+        LandmarkSet lm = select_landmarks(make_points(p, n, d, "p"), make_points(q, m, d, "q"), l,
+                                          static_cast<LandmarkMethod>(method), seed);
+        std::memcpy(out, lm.points.coords.data(), l * d * sizeof(double));
+    })
+}
+
+// The reference's staged LCN build from external bucket ids and explicit
+// landmarks, as run_one does it (runner.cpp:258-271) but with
+// neighbor_pairs(BandBuckets...) (lsh.cpp:212-243) in place of the LSH:
+// neighbor_pairs -> build_sparse -> build_factors -> build_correction ->
+// KernelOperator::lcn. Intermediates are released as soon as the next stage
+// has consumed them (the configs[3] operator is ~27 GB of host memory).
+// phase_ms: pairs, build_sparse, build_factors, build_correction.
+int ref_lcn_pipeline(const double* p, std::size_t n, const double* q, std::size_t m, std::size_t d, int kind,
+                     double lambda, const std::uint64_t* ids_p, const std::uint64_t* ids_q, int bands,
+                     std::uint64_t range, const double* landmarks, std::size_t l, double* phase_ms, void** out) {
+    GUARD({
+        auto now = [] { return std::chrono::steady_clock::now(); };
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        PointSet P = make_points(p, n, d, "p"), Q = make_points(q, m, d, "q");
+        auto t0 = now();
+        auto np = std::make_unique<NeighborPairs>();
+        {
+            BandBuckets bp, bq;
+            bp.composite_range = bq.composite_range = range;
+            for (int b = 0; b < bands; ++b) {
+                bp.bucket.emplace_back(ids_p + static_cast<std::size_t>(b) * n,
+                                       ids_p + (static_cast<std::size_t>(b) + 1) * n);
+                bq.bucket.emplace_back(ids_q + static_cast<std::size_t>(b) * m,
+                                       ids_q + (static_cast<std::size_t>(b) + 1) * m);
+            }
+            *np = neighbor_pairs(bp, bq, LshConfig{});
+        }
+        auto t1 = now();
+        auto sk = std::make_unique<SparseKernel>(build_sparse(P, Q, *np, static_cast<CostKind>(kind), lambda));
+        np.reset();
+        auto t2 = now();
+        LandmarkSet lm;
+        lm.points = make_points(landmarks, l, d, "landmarks");
+        NystromFactors f = build_factors(P, Q, lm, static_cast<CostKind>(kind), lambda);
+        auto t3 = now();
+        LcnCorrection c = build_correction(*sk, f);
+        sk.reset();
+        auto t4 = now();
+        auto* r = new RefOp{KernelOperator::lcn(std::move(f), std::move(c))};
+        r->landmarks = lm.points.coords;
+        if (phase_ms) {
+            phase_ms[0] = ms(t0, t1);
+            phase_ms[1] = ms(t1, t2);
+            phase_ms[2] = ms(t2, t3);
+            phase_ms[3] = ms(t3, t4);
+        }
+        *out = r;
+    })
+}
+
+// Per-row digest of the operator's support (CSR of the LCN correction or the
+// sparse kernel): count and two 64-bit folds of mix64(col) (wrapping sum and
+// xor). Columns are sorted within a row (sparse_kernel.hpp:19-21), so equal
+// digests mean equal rows with overwhelming probability.
+int ref_op_row_digest(void* h, std::uint32_t* cnt, std::uint64_t* hsum, std::uint64_t* hxor) {
+    try {
+        auto* r = static_cast<RefOp*>(h);
+        const std::vector<std::uint32_t>* rp = nullptr;
+        const std::vector<std::uint32_t>* col = nullptr;
+        if (r->op.correction()) {
+            rp = &r->op.correction()->row_ptr;
+            col = &r->op.correction()->col;
+        } else if (r->op.sparse_kernel()) {
+            rp = &r->op.sparse_kernel()->row_ptr;
+            col = &r->op.sparse_kernel()->col;
+        } else {
+            throw InvalidArgument("ref_op_row_digest: operator has no support");
+        }
+        const std::size_t rows = rp->size() - 1;
+#pragma omp parallel for schedule(static)
+        for (std::ptrdiff_t ii = 0; ii < static_cast<std::ptrdiff_t>(rows); ++ii) {
+            const std::size_t i = static_cast<std::size_t>(ii);
+            std::uint64_t s = 0, x = 0;
+            for (std::uint32_t e = (*rp)[i]; e < (*rp)[i + 1]; ++e) {
+                std::uint64_t hcol = mix64((*col)[e]);
+                s += hcol;
+                x ^= hcol;
+            }
+            cnt[i] = (*rp)[i + 1] - (*rp)[i];
+            hsum[i] = s;
+            hxor[i] = x;
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// extract_plan (sinkhorn.cpp:365-369) of a solved LCN operator, copied out
+// only for the listed rows (ascending): per entry the column, log K^sp,
+// delta, sp_vals and sp_nys_vals (Plan, sinkhorn.hpp:34-52). cnt[k] = row
+// length; the flat outputs hold sum(cnt) entries (size them with
+// ref_op_row_digest's counts).
+int ref_plan_rows(void* op, void* res, const std::uint32_t* rows, std::size_t nrows, std::uint32_t* cnt,
+                  std::uint32_t* cols, double* log_sp, double* delta, double* sp_vals, double* sp_nys_vals) {
+    GUARD({
+        auto* r = static_cast<RefOp*>(op);
+        auto* s = static_cast<SinkhornResult*>(res);
+        const LcnCorrection& c = *r->op.correction();
+        Plan plan = extract_plan(r->op, s->state);
+        std::size_t o = 0;
+        for (std::size_t k = 0; k < nrows; ++k) {
+            const std::uint32_t i = rows[k];
+            cnt[k] = c.row_ptr[i + 1] - c.row_ptr[i];
+            for (std::uint32_t e = c.row_ptr[i]; e < c.row_ptr[i + 1]; ++e, ++o) {
+                cols[o] = c.col[e];
+                log_sp[o] = c.log_sp[e];
+                delta[o] = c.delta[e];
+                sp_vals[o] = plan.sp_vals[e];
+                sp_nys_vals[o] = plan.sp_nys_vals[e];
+            }
+        }
+    })
+}
+
 // KernelOperator::with_bp (operator.cpp:103-115) with
 // BpExtension::from_costs (operator.cpp:33-43), replacing the handle's operator
 int ref_op_with_bp(void* h, const double* cost_p, std::size_t n, const double* cost_q, std::size_t m, double lambda) {

@@ -83,6 +83,18 @@ void check_points(const double* x, size_t n, size_t d, const char* id) {
         if (!std::isfinite(x[i])) throw Status(2, std::string("point set '") + id + "' has non-finite coordinates");
 }
 
+__global__ void demote_check_kernel(const double* __restrict__ in, float* __restrict__ out, long long n,
+                                    unsigned* __restrict__ inexact) {
+    bool bad = false;
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += 256LL * gridDim.x) {
+        const double v = in[i];
+        const float f = static_cast<float>(v);
+        out[i] = f;
+        bad |= static_cast<double>(f) != v;
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(inexact, 1u);
+}
+
 void upload_union(Op& op, const double* p, size_t n, const double* q, size_t m, size_t d) {
     op.n = n;
     op.m = m;
@@ -90,13 +102,19 @@ void upload_union(Op& op, const double* p, size_t n, const double* q, size_t m, 
     op.X.resize((n + m) * d);
     CUDA_OK(cudaMemcpyAsync(op.X.get(), p, n * d * 8, cudaMemcpyHostToDevice, op.ctx->stream));
     CUDA_OK(cudaMemcpyAsync(op.X.get() + n * d, q, m * d * 8, cudaMemcpyHostToDevice, op.ctx->stream));
-    // fp32 copy for the k-means reads when the promotion is exact
-    std::vector<float> f((n + m) * d);
-    bool exact = true;
-    for (size_t i = 0; i < n * d && exact; ++i) exact = static_cast<double>(f[i] = static_cast<float>(p[i])) == p[i];
-    for (size_t i = 0; i < m * d && exact; ++i) exact = static_cast<double>(f[n * d + i] = static_cast<float>(q[i])) == q[i];
-    if (exact) op.X32.upload(f.data(), f.size(), op.ctx->stream);
+    // fp32 copy for the k-means reads when the promotion is exact, made and
+    // checked on the device (no host pass over the points)
+    const long long cnt = static_cast<long long>((n + m) * d);
+    op.X32.resize(cnt);
+    DevBuf<unsigned> inexact(1);
+    inexact.zero(op.ctx->stream);
+    demote_check_kernel<<<static_cast<int>(std::min<long long>(ceil_div(cnt, 256), 8LL * op.ctx->num_sms)), 256, 0,
+                          op.ctx->stream>>>(op.X.get(), op.X32.get(), cnt, inexact.get());
+    LAUNCH_OK("demote_check");
+    unsigned h = 0;
+    inexact.download(&h, 1, op.ctx->stream);
     op.ctx->sync();
+    if (h) op.X32 = DevBuf<float>();
 }
 
 __global__ void promote_kernel(const float* __restrict__ in, double* __restrict__ out, long long n) {
@@ -767,7 +785,7 @@ int lcn_sinkhorn(lcn_op* op, const double* p, const double* q, const lcn_sinkhor
         auto res = std::make_unique<lcn_result>();
         res->op = op;
         res->device = op->o.ctx->device;
-        if (o.kind == LCN_OP_SPARSE && so.check_support) {
+        if (o.kind == LCN_OP_SPARSE && so.check_support && !o.bp) {  // sinkhorn.cpp:122 (!op.has_bp())
             // sinkhorn.cpp:122-128: warn when the pattern has no support
             // (maximum bipartite matching < min(n, m), sparse_kernel.cpp:189-196).
             // Band 1's pattern is a disjoint union of complete bipartite
@@ -818,6 +836,8 @@ int lcn_sinkhorn_device(lcn_op* op, const double* d_p, const double* d_q, const 
             so.check_support = opts->check_support != 0;
             so.want_plan = false;
         }
+        if (op->o.bp)  // the device entry solves the balanced base problem only
+            throw Status(2, "lcn_sinkhorn_device: BP-extended operators need lcn_sinkhorn (host marginals)");
         auto res = std::make_unique<lcn_result>();
         res->op = op;
         res->device = op->o.ctx->device;
@@ -888,16 +908,25 @@ int lcn_distance_lcn(const lcn_result* res, const lcn_op* op, double* out) {
 // ---- grad_cost (sinkhorn.cpp:263-320) -----------------------------------
 namespace {
 // v[a] = sum_r F[r][a] x_r (F rows x l, fp64), one thread per column a, rows
-// split over blocks and combined by atomics into v (zeroed)
+// split over gridDim.y blocks; each block writes its partial to
+// part[blockIdx.y * l + a] and colsum_combine_kernel adds them in block
+// order, so the gradients are bit-identical run to run (as distance_lcn)
 __global__ void colsum_kernel(const double* __restrict__ F, long long rows, int l, const double* __restrict__ x,
-                              double* __restrict__ v) {
+                              double* __restrict__ part) {
     const int a = blockIdx.x * blockDim.x + threadIdx.x;
     if (a >= l) return;
     const long long per = (rows + gridDim.y - 1) / gridDim.y;
     const long long r0 = static_cast<long long>(blockIdx.y) * per, r1 = r0 + per < rows ? r0 + per : rows;
     double acc = 0.0;
     for (long long r = r0; r < r1; ++r) acc += F[r * l + a] * x[r];
-    atomicAdd(v + a, acc);
+    part[static_cast<long long>(blockIdx.y) * l + a] = acc;
+}
+__global__ void colsum_combine_kernel(const double* __restrict__ part, int blocks, int l, double* __restrict__ v) {
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= l) return;
+    double acc = 0.0;
+    for (int b = 0; b < blocks; ++b) acc += part[static_cast<long long>(b) * l + a];
+    v[a] = acc;
 }
 // out[r][a] = scale * x_r * y_a (rows x l)
 __global__ void outer_kernel(const double* __restrict__ x, long long rows, const double* __restrict__ y, int l,
@@ -922,6 +951,7 @@ int lcn_grad_cost(const lcn_result* res, const lcn_op* op, int which, double* ou
         const Op& o = op->o;
         if (stale) *stale = r.converged ? 0 : 1;
         if (!r.converged) std::fprintf(stderr, "lcn: warning: gradient requested before convergence (stale)\n");
+        if (o.bp) throw Status(2, "grad_cost: gradients are defined for the unextended operators");  // sinkhorn.cpp:269-270
         const double lam = o.lambda;
         auto put = [&](const std::vector<double>& v, double scale) {
             if (out)
@@ -948,16 +978,18 @@ int lcn_grad_cost(const lcn_result* res, const lcn_op* op, int which, double* ou
         if (!out) return;
         cudaStream_t s = o.ctx->stream;
         // s_i = exp(log s_i), t_j = exp(log t_j) on the device; wt = W t, su = U^T s
-        DevBuf<double> ds, dt, wt(l), su(l), g(count);
+        constexpr int kParts = 64;
+        DevBuf<double> ds, dt, wt(l), su(l), g(count), part(kParts * l);
         ds.upload(r.log_s.data(), n, s);
         dt.upload(r.log_t.data(), m, s);
         exp_inplace_kernel<<<ceil_div(n, 256), 256, 0, s>>>(ds.get(), static_cast<long long>(n));
         exp_inplace_kernel<<<ceil_div(m, 256), 256, 0, s>>>(dt.get(), static_cast<long long>(m));
-        wt.zero(s);
-        su.zero(s);
-        const dim3 gs(static_cast<unsigned>(ceil_div(l, 128)), 64);
-        colsum_kernel<<<gs, 128, 0, s>>>(o.Wt64.get(), m, static_cast<int>(l), dt.get(), wt.get());
-        colsum_kernel<<<gs, 128, 0, s>>>(o.U64.get(), n, static_cast<int>(l), ds.get(), su.get());
+        const dim3 gs(static_cast<unsigned>(ceil_div(l, 128)), kParts);
+        const unsigned gc = static_cast<unsigned>(ceil_div(l, 128));
+        colsum_kernel<<<gs, 128, 0, s>>>(o.Wt64.get(), m, static_cast<int>(l), dt.get(), part.get());
+        colsum_combine_kernel<<<gc, 128, 0, s>>>(part.get(), kParts, static_cast<int>(l), wt.get());
+        colsum_kernel<<<gs, 128, 0, s>>>(o.U64.get(), n, static_cast<int>(l), ds.get(), part.get());
+        colsum_combine_kernel<<<gc, 128, 0, s>>>(part.get(), kParts, static_cast<int>(l), su.get());
         const int grid = static_cast<int>(std::min<long long>(ceil_div(count, 256), 16 * o.ctx->num_sms));
         if (which == 1) {
             // du(i, a) = -lambda s_i wt_a (n x l)

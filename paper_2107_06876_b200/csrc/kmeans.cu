@@ -1547,7 +1547,7 @@ void assign_device(Ctx& ctx, const T* X, long long N, int d, const double* C, in
         if (fma_only || !assign_filter_tc(ctx, reinterpret_cast<const float*>(X), N, d, C, k, out, amb.get(),
                                           namb.get())) {
             filter_prep_kernel<<<Kp, 128, 0, s>>>(C, k, d, Kp, CfT.get(), ncf.get(), cmax.get());
-            static bool attr[64] = {};
+            static std::atomic<bool> attr[64];  // set once per device; concurrent build jobs may race here (benign, idempotent)
             if (ctx.device >= 64 || !attr[ctx.device]) {
                 CUDA_OK(cudaFuncSetAttribute(assign_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(sizeof(FilterSmem))));

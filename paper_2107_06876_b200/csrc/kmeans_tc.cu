@@ -417,7 +417,7 @@ bool assign_filter_tc(Ctx& ctx, const float* X, long long N, int d, const double
     tc_prep_kernel<<<ntile * kTN, 128, 0, s>>>(C, k, d, ntile, tiles.get(), ncf.get(), cmax.get());
     // ring + barriers (2 kTStages + 2 kTAcc) + TMEM slot + row-merge buffer
     const int smem = kTStages * kTStage + 1024 + (2 * kTStages + 2 * kTAcc + 2) * 8 + (3 * kTM + 2) * 4 + kTM * 8 + 64;
-    static bool attr[64] = {};
+    static std::atomic<bool> attr[64];  // set once per device; concurrent build jobs may race here (benign, idempotent)
     if (ctx.device >= 64 || !attr[ctx.device]) {
         CUDA_OK(cudaFuncSetAttribute(assign_filter_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         if (ctx.device < 64) attr[ctx.device] = true;

@@ -1768,10 +1768,10 @@ struct Solver {
             lens(k, sl, ol);
             if (sl && ol) total += cost_of(sl, row_stride(ol));
         }
-        static const double cap_div = [] {  // pieces per CTA share (LCN_BAND_CAP_DIV; 4 measured ~2 % faster than 2)
-            const char* e = std::getenv("LCN_BAND_CAP_DIV");
-            return e && *e ? std::max(1.0, std::atof(e)) : 4.0;
-        }();
+        // pieces per CTA share (LCN_BAND_CAP_DIV, read per plan like
+        // LCN_BAND_STATIC; 4 measured ~2 % faster than 2)
+        const char* cap_env = std::getenv("LCN_BAND_CAP_DIV");
+        const double cap_div = cap_env && *cap_env ? std::max(1.0, std::atof(cap_env)) : 4.0;
         const double cap = std::max(total / band_grid / cap_div, 65536.0);
         struct Piece { BandItem it; double cost; };
         std::vector<Piece> pieces;
@@ -1788,8 +1788,11 @@ struct Solver {
             K = std::max<size_t>(K, ceil_div(sl, kBandVec));
             size_t pr = (ceil_div(sl, std::max<size_t>(K, 1)) + 7) & ~size_t(7);
             pr = std::min<size_t>(std::max<size_t>(pr, 8), kBandVec);
+            // the piece index is 8 bits: a long bucket gets longer pieces
+            // rather than more of them (one dominant bucket, small problems)
+            pr = std::max<size_t>(pr, (ceil_div(sl, 255) + 7) & ~size_t(7));
+            if (pr > kBandVec) throw Status(2, "lcn: bucket longer than 255 band pieces");
             K = ceil_div(sl, pr);
-            if (K > 255) throw Status(2, "lcn: bucket split into more than 255 pieces");
             for (size_t ct = 0; ct < nct; ++ct) {
                 const size_t o0 = ct * kBandVec, ow = std::min<size_t>(kBandVec, ol - o0);
                 uint32_t sid = 0xffffffffu;

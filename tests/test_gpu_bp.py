@@ -66,3 +66,44 @@ def test_bp_converges_and_rejects_bad_kernels(ref):
     assert res.converged == rres.converged and res.iters == rres.iters
     with pytest.raises(lcn.InvalidArgument, match="deletion kernels must be finite and nonnegative"):
         op.with_bp(np.full(90, np.nan), np.full(70, 1.0))
+
+
+@pytest.mark.parametrize("kind", ["dense", "lcn"])
+def test_bp_grad_cost_rejected(ref, kind):
+    # grad_cost on a BP-extended operator throws InvalidArgument after the
+    # stale warning (sinkhorn.cpp:265-270), like the reference
+    p, q, pm, qm = problem(7, 60, 50)
+    ctx = lcn.Context(0, store_fp64=True)
+    op, rop = build(ctx, ref, kind, p, q, 0.5)
+    op.with_bp(np.full(60, 1.2), np.full(50, 1.2))
+    res = lcn.sinkhorn(op, pm, qm, lcn.SinkhornOptions(tol=0.0, max_iters=5))
+    for which in ((0,) if kind == "dense" else (1, 2, 3)):
+        with pytest.raises(lcn.InvalidArgument, match="gradients are defined for the unextended operators"):
+            lcn.grad_cost(res, op, which)
+
+
+def test_bp_device_solve_rejected(ref):
+    # the device-marginal entry solves only the balanced base problem: a BP
+    # operator must go through lcn_sinkhorn, not be solved unextended silently
+    import torch
+    p, q, pm, qm = problem(8, 40, 30)
+    ctx = lcn.Context(0, store_fp64=True)
+    op, _ = build(ctx, ref, "sparse", p, q, 0.5)
+    op.with_bp(np.full(40, 1.0), np.full(30, 1.0))
+    dp = torch.from_numpy(pm).cuda()
+    dq = torch.from_numpy(qm).cuda()
+    with pytest.raises(lcn.InvalidArgument, match="BP-extended"):
+        lcn.sinkhorn_device(op, dp.data_ptr(), dq.data_ptr(), lcn.SinkhornOptions(tol=0.0, max_iters=5))
+
+
+def test_bp_sparse_skips_support_check(ref):
+    # sinkhorn.cpp:122: the support check runs only without BP, so a BP solve
+    # of a pattern without support emits no warning
+    p, q, pm, qm = problem(9, 70, 40)
+    ctx = lcn.Context(0, store_fp64=True)
+    op, rop = build(ctx, ref, "sparse", p, q, 0.5)
+    op.with_bp(np.full(70, 1.0), np.full(40, 1.0))
+    rop.with_bp(np.full(70, 1.0), np.full(40, 1.0), 0.5)
+    res = lcn.sinkhorn(op, pm, qm, lcn.SinkhornOptions(tol=0.0, max_iters=5, check_support=True))
+    rres = rop.sinkhorn(pm, qm, tol=0.0, max_iters=5, check_support=True)
+    assert len(res.warnings) == rres.n_warnings == 0

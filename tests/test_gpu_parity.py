@@ -188,6 +188,26 @@ def test_lcn_wide_and_split_buckets(ref, fp64):
     assert np.array_equal(res2.sp_vals, res.sp_vals)
 
 
+@pytest.mark.parametrize("n,m", [(5000, 3000), (8000, 2000), (6000, 1500)])
+def test_lcn_one_dominant_bucket(ref, n, m):
+    """One bucket holding every point (buckets = 1): the band planner must
+    lengthen the stream pieces instead of exceeding the 8-bit piece index
+    (these shapes threw 'more than 255 pieces')."""
+    r = np.random.default_rng(n + m)
+    p = r.standard_normal((n, 6)).astype(np.float32).astype(np.float64)
+    q = (r.standard_normal((m, 6)) * 0.9).astype(np.float32).astype(np.float64)
+    c = lcn.Context(0)
+    cfg = lcn.LshConfig(1, 1, 1, 10, 5)
+    op = lcn.KernelOperator.lcn_lsh(c, p, q, lcn.SQEUCLIDEAN, 2.0, cfg, 16, lcn.LANDMARK_KMEANS, 3)
+    assert op.nnz == n * m
+    pairs = ref.lsh_pairs(p, q, 1, 1, 10, 5)
+    rop = ref.op_lcn(p, q, lcn.SQEUCLIDEAN, 2.0, pairs, 16, 0, 3)
+    pm, qm = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
+    res = lcn.sinkhorn(op, pm, qm, lcn.SinkhornOptions(tol=0.0, max_iters=20, want_plan=False))
+    rres = rop.sinkhorn(pm, qm, tol=0.0, max_iters=20, want_plan=False)
+    assert rel(res.distance, rres.distance) <= REL_FP32
+
+
 @pytest.mark.parametrize("fp64", [False, True])
 def test_sharded_solve_single_rank(ref, fp64):
     """The sharded solve (§8(e)) through a 1-rank NCCL communicator: every
