@@ -61,7 +61,15 @@ enum lcn_op_kind { LCN_OP_DENSE = 0, LCN_OP_SPARSE = 1, LCN_OP_NYSTROM = 2, LCN_
  * stored kernel value in fp64 (API-compatibility mode, passes the reference
  * unit tests' 1e-12 tolerances); FP32 stores them in fp32 with fp64
  * accumulation (performance mode, 1e-4 parity). */
-enum lcn_ctx_flags { LCN_STORE_FP32 = 0, LCN_STORE_FP64 = 1 };
+enum lcn_ctx_flags { LCN_STORE_FP32 = 0, LCN_STORE_FP64 = 1, LCN_EXACT_BUILD = 2 };
+/* Build contractions. FP32 storage computes the within-bucket distance
+ * blocks of K^sp, the point x landmark blocks U and V, and the delta SDDMM
+ * U_b W_b on the tcgen05 tensor cores in the FP32-accurate 3xTF32 split
+ * (values within ~1e-5 of the reference, support unchanged). LCN_EXACT_BUILD
+ * (or FP64 storage) keeps the exact fp64 CUDA-core tiles instead: the
+ * reference's sequential fp64 folds, log K bit-exact (the export mode). The
+ * landmark Gram matrix A and W = A^-1 V are always fp64 (the reference's
+ * 1e-6 residual acceptance test, nystrom.cpp:104-124). */
 
 /* LshScheme (lsh.hpp:13-17), same values. */
 enum lcn_lsh_scheme { LCN_LSH_CROSS_POLYTOPE = 0, LCN_LSH_KMEANS = 1, LCN_LSH_HIERARCHICAL_KMEANS = 2 };

@@ -43,6 +43,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// the same wait without a suspend-time hint: try_wait returns after the
+// hardware's own (short) time limit and the loop retries. With the hint,
+// ptxas emits the retry path as NANOSLEEP.SYNCS <hint>, and a warp whose
+// wait misses can sleep far past the phase flip (tensor-core pipelines, where
+// every role waits on another, lose most of their time there).
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
 // global -> shared bulk copy completing on `bar` (bytes multiple of 16,
 // both addresses 16-byte aligned)
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {

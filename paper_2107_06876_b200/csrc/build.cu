@@ -31,6 +31,7 @@
 
 #include "kmeans.cuh"
 #include "op.cuh"
+#include "tc_block.cuh"
 #include "tiles.cuh"
 
 namespace lcnb {
@@ -826,6 +827,392 @@ int read_flag(Ctx& ctx, DevBuf<int>& f) {
     return h;
 }
 
+// ---- tensor-core build contractions (tc_block.cuh), fp32 storage ----------
+// The cost from an FP32-accurate dot product and exact fp64 norms:
+// |x - y|^2 = |x|^2 + |y|^2 - 2 x.y (cost_value, geometry.cpp:45-76).
+__device__ __forceinline__ double tc_cost(int kind, float dot, double nx, double ny, int* bad) {
+    const double dd = static_cast<double>(dot);
+    if (kind == 1) return -dd;
+    if (kind == 2) {
+        if (nx == 0.0 || ny == 0.0) {
+            atomicOr(bad, 1);
+            return 0.0;
+        }
+        double c = dd / sqrt(nx * ny);
+        c = c > 1.0 ? 1.0 : (c < -1.0 ? -1.0 : c);
+        return sqrt(1.0 - c);
+    }
+    const double sq = fmax(nx + ny - 2.0 * dd, 0.0);
+    return kind == 0 ? sqrt(sq) : sq;
+}
+
+// log K^sp of band block entries (EpiLogK on the tensor cores): items
+// {row tile, column tile, bucket}; -inf where an earlier band holds the pair.
+// Per-column inputs are read in the band's target order (coalesced along a
+// warp's lanes): the centred norms and, for each earlier band, the bucket of
+// the target at that position.
+struct TcEpiLogK {
+    static constexpr int kRB = 4;  // rows per load batch
+    double* out;
+    BandView bv;
+    int band, kind;
+    double inv;
+    const double* nrm;  // union norms |x|^2 (targets offset by n): uncentred kinds (dot, cosine)
+    long long n;
+    const double* cn_src;  // |x - c_b|^2 per source position (distance kinds, centred)
+    const double* cn_tgt;
+    const uint32_t* prev_src;  // band x n: earlier bands' bucket of the source at each position
+    const uint32_t* prev_tgt;  // band x m: same for targets
+    long long pn, pm;
+    const uint32_t* a_first;
+    const uint32_t* b_first;
+    int* bad;
+    struct Item {
+        uint32_t sb, nb, tb, mb, r0, c0;
+        unsigned long long off;
+    };
+    struct Row {
+        bool valid;
+        uint32_t p, pb0;
+        double nx;
+        double* o;
+    };
+    struct Pre {
+        double ny;
+        bool masked;
+    };
+    __device__ Item item(const int4& it) const {
+        Item I;
+        const int b = it.z;
+        I.sb = bv.src_start[b];
+        I.nb = bv.src_start[b + 1] - I.sb;
+        I.tb = bv.tgt_start[b];
+        I.mb = bv.tgt_start[b + 1] - I.tb;
+        I.r0 = (it.x - a_first[b]) * tcb::kM;
+        I.c0 = (it.y - b_first[b]) * tcb::kM;
+        I.off = bv.blk_off[b];
+        return I;
+    }
+    __device__ Row row(const Item& I, int rr) const {
+        Row R{};
+        const uint32_t r = I.r0 + rr;
+        R.valid = r < I.nb;
+        if (!R.valid) return R;
+        R.p = I.sb + r;
+        R.nx = cn_src ? cn_src[R.p] : nrm[bv.src_order[R.p]];
+        R.pb0 = band > 0 ? prev_src[R.p] : 0u;
+        R.o = out + I.off + static_cast<unsigned long long>(r) * row_stride(I.mb);
+        return R;
+    }
+    __device__ Pre pre(const Item& I, const Row& R, int c) const {
+        Pre P{0.0, false};
+        const uint32_t cc = I.c0 + c;
+        if (!R.valid || cc >= I.mb) return P;
+        const uint32_t q = I.tb + cc;
+        P.ny = cn_tgt ? cn_tgt[q] : nrm[n + bv.tgt_order[q]];
+        if (band > 0) P.masked = prev_tgt[q] == R.pb0;
+        for (int bb = 1; bb < band && !P.masked; ++bb) P.masked = prev_tgt[bb * pm + q] == prev_src[bb * pn + R.p];
+        return P;
+    }
+    __device__ void apply(const Item& I, const Row& R, const Pre& P, int c, float dot) {
+        const uint32_t cc = I.c0 + c;
+        if (!R.valid || cc >= I.mb) return;
+        R.o[cc] = P.masked ? kNegInf : 0.0 - tc_cost(kind, dot, R.nx, P.ny, bad) * inv;
+    }
+    __device__ void finish() {}
+};
+
+// delta = exp(log K) - (U W)_ij (sparse_kernel.cpp:100-109) with (U W)_ij
+// the FP32-accurate dot of U's row and W's column
+struct TcEpiDelta {
+    static constexpr int kRB = 8;
+    double* delta;
+    const double* logk;
+    BandView bv;
+    const uint32_t* a_first;
+    const uint32_t* b_first;
+    unsigned long long* maxbits;
+    int* overflow;
+    double mx = 0.0;
+    struct Item {
+        uint32_t nb, mb, r0, c0;
+        unsigned long long off;
+    };
+    struct Row {
+        bool valid;
+        unsigned long long base;
+    };
+    struct Pre {
+        double lk;
+    };
+    __device__ Item item(const int4& it) const {
+        Item I;
+        const int b = it.z;
+        I.nb = bv.src_start[b + 1] - bv.src_start[b];
+        I.mb = bv.tgt_start[b + 1] - bv.tgt_start[b];
+        I.r0 = (it.x - a_first[b]) * tcb::kM;
+        I.c0 = (it.y - b_first[b]) * tcb::kM;
+        I.off = bv.blk_off[b];
+        return I;
+    }
+    __device__ Row row(const Item& I, int rr) const {
+        Row R{};
+        const uint32_t r = I.r0 + rr;
+        R.valid = r < I.nb;
+        R.base = I.off + static_cast<unsigned long long>(r) * row_stride(I.mb) + I.c0;
+        return R;
+    }
+    __device__ Pre pre(const Item& I, const Row& R, int c) const {
+        return Pre{R.valid && I.c0 + c < I.mb ? logk[R.base + c] : kNegInf};
+    }
+    __device__ void apply(const Item& I, const Row& R, const Pre& P, int c, float dot) {
+        if (!R.valid || I.c0 + c >= I.mb) return;
+        double dv = 0.0;
+        if (P.lk != kNegInf) {  // masked duplicate of an earlier band: 0
+            const double exact = exp(P.lk);
+            if (isinf(exact)) atomicOr(overflow, 1);
+            else dv = exact - static_cast<double>(dot);
+        }
+        delta[R.base + c] = dv;
+        mx = fmax(mx, fabs(dv));
+    }
+    __device__ void finish() {
+        const double w = warp_max(mx);
+        if ((threadIdx.x & 31) == 0 && w > 0.0) atomicMax(maxbits, static_cast<unsigned long long>(__double_as_longlong(w)));
+    }
+};
+
+// exp(-c * (1/lambda)) of a dense point x landmark block (kernel_block,
+// nystrom.cpp:53-64): items {row tile, column tile}
+struct TcEpiExp {
+    static constexpr int kRB = 8;
+    double* out;
+    long long ld, nrows, ncols;
+    int kind;
+    double inv;
+    const double* na;
+    const double* nb;
+    int* bad;
+    struct Item {
+        long long r0, c0;
+    };
+    struct Row {
+        bool valid;
+        double nx;
+        double* o;
+    };
+    struct Pre {
+        double ny;
+    };
+    __device__ Item item(const int4& it) const {
+        return Item{static_cast<long long>(it.x) * tcb::kM, static_cast<long long>(it.y) * tcb::kM};
+    }
+    __device__ Row row(const Item& I, int rr) const {
+        Row R{};
+        const long long r = I.r0 + rr;
+        R.valid = r < nrows;
+        if (!R.valid) return R;
+        R.nx = na[r];
+        R.o = out + r * ld;
+        return R;
+    }
+    __device__ Pre pre(const Item& I, const Row&, int c) const {
+        return Pre{I.c0 + c < ncols ? nb[I.c0 + c] : 0.0};
+    }
+    __device__ void apply(const Item& I, const Row& R, const Pre& P, int c, float dot) {
+        const long long cc = I.c0 + c;
+        if (R.valid && cc < ncols) R.o[cc] = exp(-tc_cost(kind, dot, R.nx, P.ny, bad) * inv);
+    }
+    __device__ void finish() {}
+};
+
+// earlier bands' bucket of each position of band b's source / target order
+__global__ void prev_bucket_kernel(const uint32_t* __restrict__ order, const uint32_t* __restrict__ bucket,
+                                   long long count, uint32_t* __restrict__ out) {
+    const long long p = blockIdx.x * 256LL + threadIdx.x;
+    if (p < count) out[p] = bucket[order[p]];
+}
+
+// part: 1 K^sp distance blocks, 2 U / V blocks, 4 delta SDDMM. LCN_TC_PARTS
+// (bit mask) overrides the default 1 | 4. U and V stay on the exact fp64
+// tiles: the Nystrom product U A^-1 V cancels 5-40x against K,
+// so the 3xTF32 dot's ~1e-5 relative error in U's entries (the |x|^2 + |l|^2 -
+// 2 x.l cancellation, uncentrable across all landmarks) grows to ~1e-4 in the
+// plan; measured at configs[3] x 0.005: sp_vals max error 9.2e-5 with U/V on
+// the tensor cores, 1.9e-6 without (profiles/tc_build_r02.json). K^sp blocks
+// are centred per bucket and delta absorbs its own dot error, so both keep
+// ~1e-6.
+bool use_tc_build(const Op& op, int part) {
+    if (op.fp64 || op.ctx->exact_build || op.cost < 0 || op.cost > 3) return false;
+    const char* e = std::getenv("LCN_TC_PARTS");
+    return ((e && *e ? std::atoi(e) : 5) & part) != 0;
+}
+
+template <typename T>
+void tc_pack(Ctx& ctx, const T* X, long long ld, int d, const uint32_t* idx, const std::vector<tcb::PackTile>& tiles,
+             DevBuf<unsigned char>& out, const double* centers = nullptr) {
+    const int KB = static_cast<int>(ceil_div(d, 32));
+    out.resize(std::max<size_t>(tiles.size(), 1) * KB * tcb::kKBlock);
+    if (tiles.empty()) return;
+    DevBuf<tcb::PackTile> dt;
+    dt.upload(tiles.data(), tiles.size(), ctx.stream);
+    for (size_t o = 0; o < tiles.size(); o += 65535u * 512u) {
+        const unsigned cnt = static_cast<unsigned>(std::min<size_t>(tiles.size() - o, 65535u * 512u));
+        tcb::tcb_pack_kernel<T><<<dim3(cnt, KB), 256, 0, ctx.stream>>>(X, ld, d, idx, dt.get() + o, KB, centers,
+                                                                      out.get() + o * KB * tcb::kKBlock);
+    }
+    LAUNCH_OK("tcb_pack_kernel");
+    ctx.sync();  // dt leaves scope
+}
+
+template <class Epi>
+void tc_run(Ctx& ctx, const DevBuf<unsigned char>& A, const DevBuf<unsigned char>& B, int d,
+            const std::vector<int4>& items, Epi epi) {
+    if (items.empty()) return;
+    static std::atomic<bool> attr[64];  // per instantiation and device
+    if (ctx.device >= 64 || !attr[ctx.device]) {
+        CUDA_OK(cudaFuncSetAttribute(tcb::tcb_kernel<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, tcb::kSmem));
+        if (ctx.device < 64) attr[ctx.device] = true;
+    }
+    DevBuf<int4> di;
+    di.upload(items.data(), items.size(), ctx.stream);
+    const int grid = static_cast<int>(std::min<size_t>(items.size(), static_cast<size_t>(ctx.num_sms)));
+    // LCN_TCB_TRACE: global-timer stamps of CTA 0's first 16 items (pipeline study)
+    const bool tr = std::getenv("LCN_TCB_TRACE") != nullptr;
+    DevBuf<unsigned long long> trace(tr ? 128 : 0);
+    if (tr) trace.zero(ctx.stream);
+    tcb::tcb_kernel<Epi><<<grid, tcb::kThreads, tcb::kSmem, ctx.stream>>>(A.get(), B.get(),
+                                                                         static_cast<int>(ceil_div(d, 32)), di.get(),
+                                                                         static_cast<int>(items.size()), epi,
+                                                                         tr ? trace.get() : nullptr);
+    LAUNCH_OK("tcb_kernel");
+    ctx.sync();
+    if (tr) {
+        unsigned long long h[128];
+        trace.download(h, 128, ctx.stream);
+        ctx.sync();
+        std::fprintf(stderr, "[tcb trace] items %zu grid %d KB %d (ns from producer start: prod kb0, mma kb0, mma kbN, epi start, epi end, mma acc free)\n",
+                     items.size(), grid, static_cast<int>(ceil_div(d, 32)));
+        const unsigned long long t0 = h[0];
+        for (int i = 0; i < 16 && h[i * 8]; ++i)
+            std::fprintf(stderr, "[tcb trace] item %2d: %8lld %8lld %8lld %8lld %8lld %8lld\n", i,
+                         (long long)(h[i * 8] - t0), (long long)(h[i * 8 + 1] - t0), (long long)(h[i * 8 + 2] - t0),
+                         (long long)(h[i * 8 + 3] - t0), (long long)(h[i * 8 + 4] - t0), (long long)(h[i * 8 + 5] - t0));
+    }
+}
+
+// Packed tiles and items of one band's bucket blocks: sources in 128-row
+// tiles of src_order, targets in 128-row tiles of tgt_order, one item per
+// (row tile, column tile) of every nonempty block.
+struct TcBandTiles {
+    bool centered = false;  // distance blocks: points minus their bucket's source mean
+    std::vector<tcb::PackTile> a, b;
+    std::vector<uint32_t> a_first, b_first;
+    std::vector<int4> items;
+    DevBuf<uint32_t> d_a_first, d_b_first;
+};
+void tc_band_tiles(Ctx& ctx, const Band& B, TcBandTiles& T) {
+    T.a_first.assign(B.nb + 1, 0);
+    T.b_first.assign(B.nb + 1, 0);
+    for (size_t k = 0; k < B.nb; ++k) {
+        const uint32_t sb = B.h_src_start[k], nbk = B.h_src_start[k + 1] - sb;
+        const uint32_t tb = B.h_tgt_start[k], mbk = B.h_tgt_start[k + 1] - tb;
+        T.a_first[k] = static_cast<uint32_t>(T.a.size());
+        T.b_first[k] = static_cast<uint32_t>(T.b.size());
+        if (nbk == 0 || mbk == 0) continue;
+        const uint32_t cen = T.centered ? static_cast<uint32_t>(k) : ~0u;
+        for (uint32_t r0 = 0; r0 < nbk; r0 += tcb::kM)
+            T.a.push_back({sb + r0, std::min<uint32_t>(tcb::kM, nbk - r0), cen});
+        for (uint32_t c0 = 0; c0 < mbk; c0 += tcb::kM)
+            T.b.push_back({tb + c0, std::min<uint32_t>(tcb::kM, mbk - c0), cen});
+        for (uint32_t ra = T.a_first[k]; ra < T.a.size(); ++ra)
+            for (uint32_t cb = T.b_first[k]; cb < T.b.size(); ++cb)
+                T.items.push_back(make_int4(static_cast<int>(ra), static_cast<int>(cb), static_cast<int>(k), 0));
+    }
+    T.d_a_first.upload(T.a_first.data(), T.a_first.size(), ctx.stream);
+    T.d_b_first.upload(T.b_first.data(), T.b_first.size(), ctx.stream);
+}
+
+// |x|^2 of every union point (fp64 sequential fold), for the tensor-core costs
+const double* union_sqnorms(Op& op) {
+    if (op.norms.size() != op.n + op.m) {
+        op.norms.resize(op.n + op.m);
+        norms_kernel<<<ceil_div(op.n + op.m, 256), 256, 0, op.ctx->stream>>>(op.X.get(), op.n + op.m, op.d,
+                                                                            op.norms.get());
+        LAUNCH_OK("norms");
+    }
+    return op.norms.get();
+}
+
+// Bucket centers for the distance blocks: the fp64 mean of each bucket's
+// sources. |x - y|^2 is translation invariant, and centred vectors of one
+// bucket are nearly orthogonal, so the fp32 tensor-core accumulator never
+// carries the large |x|^2 + |y|^2 terms the cancellation would amplify.
+template <typename T>
+__global__ void bucket_center_kernel(const T* __restrict__ X, int d, const uint32_t* __restrict__ order,
+                                     const uint32_t* __restrict__ start, double* __restrict__ centers) {
+    const uint32_t b = blockIdx.x, s0 = start[b], s1 = start[b + 1];
+    for (int k = threadIdx.x; k < d; k += blockDim.x) {
+        double acc = 0.0;
+        for (uint32_t p = s0; p < s1; ++p) acc += static_cast<double>(X[static_cast<long long>(order[p]) * d + k]);
+        centers[static_cast<long long>(b) * d + k] = s1 > s0 ? acc / static_cast<double>(s1 - s0) : 0.0;
+    }
+}
+// |x - c_b|^2 per position of a bucket order (one warp per position)
+template <typename T>
+__global__ void centered_norms_kernel(const T* __restrict__ X, int d, const uint32_t* __restrict__ order,
+                                      const uint32_t* __restrict__ bucket, long long count,
+                                      const double* __restrict__ centers, double* __restrict__ out) {
+    const long long p = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (p >= count) return;
+    const long long i = order[p];
+    const double* c = centers + static_cast<long long>(bucket[i]) * d;
+    double acc = 0.0;
+    for (int k = lane; k < d; k += 32) {
+        const double v = static_cast<double>(X[i * d + k]) - c[k];
+        acc += v * v;
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) out[p] = acc;
+}
+
+struct BandCenters {
+    DevBuf<double> centers, cn_src, cn_tgt;
+};
+template <typename T>
+void band_centers_t(Ctx& ctx, const T* P, const T* Q, int d, const Band& B, BandCenters& C) {
+    cudaStream_t s = ctx.stream;
+    const size_t n = B.src_order.size(), m = B.tgt_order.size();
+    C.centers.resize(std::max<size_t>(B.nb * d, 1));
+    C.cn_src.resize(std::max<size_t>(n, 1));
+    C.cn_tgt.resize(std::max<size_t>(m, 1));
+    if (B.nb) bucket_center_kernel<T><<<B.nb, 128, 0, s>>>(P, d, B.src_order.get(), B.src_start.get(), C.centers.get());
+    if (n) centered_norms_kernel<T><<<ceil_div(n * 32, 256), 256, 0, s>>>(P, d, B.src_order.get(), B.src_bucket.get(),
+                                                                          static_cast<long long>(n), C.centers.get(),
+                                                                          C.cn_src.get());
+    if (m) centered_norms_kernel<T><<<ceil_div(m * 32, 256), 256, 0, s>>>(Q, d, B.tgt_order.get(), B.tgt_bucket.get(),
+                                                                          static_cast<long long>(m), C.centers.get(),
+                                                                          C.cn_tgt.get());
+    LAUNCH_OK("band centers");
+}
+
+// pack rows of the union points (fp32 copy when exact, else fp64)
+void tc_pack_points(Op& op, bool targets, const uint32_t* idx, const std::vector<tcb::PackTile>& tiles,
+                    DevBuf<unsigned char>& out, const double* centers = nullptr) {
+    const long long off = targets ? static_cast<long long>(op.n * op.d) : 0;
+    if (op.X32.size())
+        tc_pack<float>(*op.ctx, op.X32.get() + off, op.d, static_cast<int>(op.d), idx, tiles, out, centers);
+    else
+        tc_pack<double>(*op.ctx, op.X.get() + off, op.d, static_cast<int>(op.d), idx, tiles, out, centers);
+}
+void band_centers(Op& op, const Band& B, BandCenters& C) {
+    if (op.X32.size())
+        band_centers_t<float>(*op.ctx, op.X32.get(), op.X32.get() + op.n * op.d, static_cast<int>(op.d), B, C);
+    else
+        band_centers_t<double>(*op.ctx, op.P(), op.Q(), static_cast<int>(op.d), B, C);
+}
+
 }  // namespace
 
 void build_sparse_values(Op& op) {
@@ -837,9 +1224,38 @@ void build_sparse_values(Op& op) {
     op.val64.clear();
     op.stored = 0;
     const bool dot = op.cost == 1 || op.cost == 2;  // negative-dot / cosine fold x.y, else (x-y)^2
+    const bool tc = use_tc_build(op, 1);
     for (size_t b = 0; b < op.bands.size(); ++b) {
         DevBuf<double> v(std::max<unsigned long long>(op.bands[b].entries, 1));
         fill_value(ctx, v.get(), op.bands[b].entries, kNegInf);  // row padding: log K = -inf
+        if (tc) {  // within-bucket distance blocks on the tensor cores (3xTF32)
+            const Band& B = op.bands[b];
+            TcBandTiles T;
+            T.centered = op.cost == 0 || op.cost == 3;  // translation-invariant costs
+            tc_band_tiles(ctx, B, T);
+            BandCenters BC;
+            if (T.centered) band_centers(op, B, BC);
+            DevBuf<unsigned char> pa, pb;
+            tc_pack_points(op, false, B.src_order.get(), T.a, pa, BC.centers.get());
+            tc_pack_points(op, true, B.tgt_order.get(), T.b, pb, BC.centers.get());
+            const size_t n = op.n, m = op.m;
+            DevBuf<uint32_t> prev_src(std::max<size_t>(b * n, 1)), prev_tgt(std::max<size_t>(b * m, 1));
+            for (size_t bb = 0; bb < b; ++bb) {
+                if (n) prev_bucket_kernel<<<ceil_div(n, 256), 256, 0, ctx.stream>>>(
+                    B.src_order.get(), op.bands[bb].src_bucket.get(), static_cast<long long>(n), prev_src.get() + bb * n);
+                if (m) prev_bucket_kernel<<<ceil_div(m, 256), 256, 0, ctx.stream>>>(
+                    B.tgt_order.get(), op.bands[bb].tgt_bucket.get(), static_cast<long long>(m), prev_tgt.get() + bb * m);
+            }
+            TcEpiLogK epi{v.get(), op.view(static_cast<int>(b)), static_cast<int>(b), op.cost, 1.0 / op.lambda,
+                          union_sqnorms(op), static_cast<long long>(n), T.centered ? BC.cn_src.get() : nullptr,
+                          T.centered ? BC.cn_tgt.get() : nullptr, prev_src.get(), prev_tgt.get(),
+                          static_cast<long long>(n), static_cast<long long>(m), T.d_a_first.get(), T.d_b_first.get(),
+                          bad.get()};
+            tc_run(ctx, pa, pb, static_cast<int>(op.d), T.items, epi);
+            op.stored += B.real_entries;
+            op.val64.push_back(std::move(v));
+            continue;
+        }
         EpiLogK epi{v.get(), op.bandset(), static_cast<int>(b), op.cost, 1.0 / op.lambda, nrm,
                     static_cast<long long>(op.n), bad.get()};
         if (dot)
@@ -1131,8 +1547,35 @@ void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed)
     // U = k(X_p, L) (n x l), V^T = k(X_q, L) (m x l), A = k(L, L) with division.
     op.U64.resize(std::max<size_t>(n * l, 1));
     DevBuf<double> Vt(std::max<size_t>(m * l, 1)), A(l * l);
-    exp_block(op.U64.get(), op.P(), n, nrm, op.L.get(), l, lnorm.get(), false);
-    exp_block(Vt.get(), op.Q(), m, nrm ? nrm + n : nullptr, op.L.get(), l, lnorm.get(), false);
+    if (use_tc_build(op, 2)) {  // point x landmark blocks on the tensor cores (3xTF32)
+        const double* sq = union_sqnorms(op);
+        DevBuf<double> lsq(l);
+        norms_kernel<<<ceil_div(l, 256), 256, 0, s>>>(op.L.get(), l, d, lsq.get());
+        auto tiles_of = [](size_t rows) {
+            std::vector<tcb::PackTile> t;
+            for (size_t r0 = 0; r0 < rows; r0 += tcb::kM)
+                t.push_back({static_cast<uint32_t>(r0), static_cast<uint32_t>(std::min<size_t>(tcb::kM, rows - r0)), ~0u});
+            return t;
+        };
+        DevBuf<unsigned char> pl, px;
+        const std::vector<tcb::PackTile> tl = tiles_of(l);
+        tc_pack<double>(ctx, op.L.get(), d, static_cast<int>(d), nullptr, tl, pl);
+        for (int side = 0; side < 2; ++side) {
+            const size_t rows = side ? m : n;
+            const std::vector<tcb::PackTile> tx = tiles_of(rows);
+            tc_pack_points(op, side == 1, nullptr, tx, px);
+            std::vector<int4> items;
+            for (size_t a = 0; a < tx.size(); ++a)
+                for (size_t c = 0; c < tl.size(); ++c)
+                    items.push_back(make_int4(static_cast<int>(a), static_cast<int>(c), 0, 0));
+            TcEpiExp epi{side ? Vt.get() : op.U64.get(), static_cast<long long>(l), static_cast<long long>(rows),
+                         static_cast<long long>(l), op.cost, 1.0 / op.lambda, sq + (side ? n : 0), lsq.get(), bad.get()};
+            tc_run(ctx, px, pl, static_cast<int>(d), items, epi);
+        }
+    } else {
+        exp_block(op.U64.get(), op.P(), n, nrm, op.L.get(), l, lnorm.get(), false);
+        exp_block(Vt.get(), op.Q(), m, nrm ? nrm + n : nullptr, op.L.get(), l, lnorm.get(), false);
+    }
     exp_block(A.get(), op.L.get(), l, lnorm.get(), op.L.get(), l, lnorm.get(), true);
     if (read_flag(ctx, bad)) throw Status(2, "cosine-derived cost undefined for zero vectors");
 
@@ -1231,6 +1674,19 @@ void build_correction(Op& op) {
     for (size_t b = 0; b < op.bands.size(); ++b) {
         DevBuf<double> dlt(std::max<unsigned long long>(op.bands[b].entries, 1));
         fill_value(ctx, dlt.get(), op.bands[b].entries, 0.0);  // row padding: delta = 0
+        if (use_tc_build(op, 4)) {  // SDDMM U_b W_b on the tensor cores (3xTF32)
+            const Band& B = op.bands[b];
+            TcBandTiles T;
+            tc_band_tiles(ctx, B, T);
+            DevBuf<unsigned char> pa, pb;
+            tc_pack<double>(ctx, op.U64.get(), op.l, static_cast<int>(op.l), B.src_order.get(), T.a, pa);
+            tc_pack<double>(ctx, op.Wt64.get(), op.l, static_cast<int>(op.l), B.tgt_order.get(), T.b, pb);
+            TcEpiDelta epi{dlt.get(), op.logk64[b].get(), op.view(static_cast<int>(b)), T.d_a_first.get(),
+                           T.d_b_first.get(), maxbits.get(), overflow.get()};
+            tc_run(ctx, pa, pb, static_cast<int>(op.l), T.items, epi);
+            op.val64.push_back(std::move(dlt));
+            continue;
+        }
         EpiDelta epi{dlt.get(), op.logk64[b].get(), maxbits.get(), overflow.get()};
         launch_band_tiles<1>(ctx, op.bands[b], op.view(static_cast<int>(b)), op.U64.get(), op.Wt64.get(),
                              static_cast<int>(op.l), epi);

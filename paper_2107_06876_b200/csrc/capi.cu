@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <random>
@@ -224,6 +225,7 @@ int lcn_ctx_create(int device, int flags, lcn_ctx** out) {
         auto c = std::make_unique<lcn_ctx>();
         c->c.device = device;
         c->c.store_fp64 = (flags & LCN_STORE_FP64) ? 1 : 0;
+        c->c.exact_build = (flags & LCN_EXACT_BUILD) || std::getenv("LCN_EXACT_BUILD") ? 1 : 0;
         c->c.num_sms = prop.multiProcessorCount;
         CUDA_OK(cudaSetDevice(device));
         // keep freed pool memory resident (stream-ordered DevBuf temporaries)

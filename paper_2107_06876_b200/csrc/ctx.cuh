@@ -73,6 +73,7 @@ __host__ __device__ __forceinline__ unsigned long long row_stride(unsigned long 
 struct Ctx {
     int device = 0;
     int store_fp64 = 0;
+    int exact_build = 0;  // LCN_EXACT_BUILD: fp64 CUDA-core build tiles even in fp32 storage
     int num_sms = 148;
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr;

@@ -174,12 +174,15 @@ def _f64(a, shape=None):
 
 class Context:
     """One device, one stream (lcn_ctx). store_fp64 selects fp64 storage of the
-    iteration operands (API-compatibility precision) over fp32 (performance)."""
+    iteration operands (API-compatibility precision) over fp32 (performance).
+    exact_build (LCN_EXACT_BUILD) keeps the exact fp64 build tiles in fp32
+    storage; otherwise fp32 storage builds K^sp, U, V and delta on the tensor
+    cores (3xTF32)."""
 
-    def __init__(self, device: int = 0, store_fp64: bool = False):
+    def __init__(self, device: int = 0, store_fp64: bool = False, exact_build: bool = False):
         self.lib = library()
         h = C.c_void_p()
-        rc = self.lib.lcn_ctx_create(device, 1 if store_fp64 else 0, C.byref(h))
+        rc = self.lib.lcn_ctx_create(device, (1 if store_fp64 else 0) | (2 if exact_build else 0), C.byref(h))
         if rc != 0:
             raise _STATUS.get(rc, Error)(self.lib.lcn_ctx_last_error(None).decode())
         self.h = h
