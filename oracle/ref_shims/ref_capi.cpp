@@ -32,6 +32,14 @@
 #include "lcn/sinkhorn.hpp"
 #include "lcn/sparse_kernel.hpp"
 
+namespace lcn {
+// ref_shims/correction_blocked.cpp: build_correction with the reference's
+// per-entry arithmetic, visited bucket block by bucket block
+LcnCorrection build_correction_blocked(const SparseKernel& sparse, const NystromFactors& factors,
+                                       const std::uint64_t* ids_p, const std::uint64_t* ids_q, int bands,
+                                       std::uint64_t range);
+}  // namespace lcn
+
 using namespace lcn;
 
 namespace {
@@ -668,7 +676,11 @@ int ref_lcn_pipeline(const double* p, std::size_t n, const double* q, std::size_
         lm.points = make_points(landmarks, l, d, "landmarks");
         NystromFactors f = build_factors(P, Q, lm, static_cast<CostKind>(kind), lambda);
         auto t3 = now();
-        LcnCorrection c = build_correction(*sk, f);
+        // LCN_REF_BLOCKED_CORRECTION=1: same values, bucket-blocked traversal
+        // (the row walk of sparse_kernel.cpp:96-109 is days at configs[3])
+        const char* blk = std::getenv("LCN_REF_BLOCKED_CORRECTION");
+        LcnCorrection c = (blk && *blk == '1') ? build_correction_blocked(*sk, f, ids_p, ids_q, bands, range)
+                                               : build_correction(*sk, f);
         sk.reset();
         auto t4 = now();
         auto* r = new RefOp{KernelOperator::lcn(std::move(f), std::move(c))};

@@ -376,3 +376,29 @@ def test_capi_without_gpu_fails_loudly():
         pytest.skip("GPU present")
     with pytest.raises(lcn.CudaError):
         lcn.Context(0)
+
+
+@pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built")
+def test_blocked_correction_bit_exact(monkeypatch):
+    """oracle/ref_shims/correction_blocked.cpp (the full-size parity run's
+    build_correction) gives the reference's build_correction bits
+    (sparse_kernel.cpp:82-117): delta, nys_vals, the support and max |delta|,
+    on a two-band k-means LSH pattern with buckets of uneven size."""
+    from oracle.bindings import RefLib
+    ref = RefLib()
+    pr = configs.config3(0.002)
+    ids = ref.lsh_buckets(pr.p, pr.q, pr.bands, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
+    lm = ref.select_landmarks(pr.p, pr.q, 40, configs.LANDMARK_KMEANS, pr.landmark_seed)
+    ids_p, ids_q = np.ascontiguousarray(ids[:, :pr.n]), np.ascontiguousarray(ids[:, pr.n:])
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("LCN_REF_BLOCKED_CORRECTION", flag)
+        op, _ = ref.lcn_pipeline(pr.p, pr.q, pr.cost, pr.lam_eff, ids_p, ids_q, pr.buckets, lm)
+        out[flag] = [op.csr(1), op.csr(5), op.scalar(0)]
+    (rp0, c0, d0), (_, _, n0), s0 = out["0"]
+    (rp1, c1, d1), (_, _, n1), s1 = out["1"]
+    assert len(c0) > 1000
+    assert np.array_equal(rp0, rp1) and np.array_equal(c0, c1)
+    assert np.array_equal(d0.view(np.uint64), d1.view(np.uint64))
+    assert np.array_equal(n0.view(np.uint64), n1.view(np.uint64))
+    assert s0 == s1
