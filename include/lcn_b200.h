@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define LCN_B200_ABI_VERSION 3  /* 3: lcn_op_info_t.streamed */
+#define LCN_B200_ABI_VERSION 4  /* 3: lcn_op_info_t.streamed; 4: bucket-sharded solve, loopback, shard plan */
 
 typedef struct lcn_ctx lcn_ctx;
 typedef struct lcn_op lcn_op;
@@ -132,14 +132,57 @@ int lcn_ctx_set_profile(lcn_ctx* ctx, int on);
 /* A fresh NCCL unique id (128 bytes) on the calling rank (rank 0 makes it,
  * the caller broadcasts it). */
 int lcn_nccl_unique_id(uint8_t* out128);
-/* Join `world` ranks (one process or thread per GPU) into one communicator;
- * collective over the ranks. Afterwards lcn_sinkhorn* on operators of this
- * context solve ONE problem together: every rank holds the operator (built
- * from the same inputs), the band blocks are split by bucket across ranks and
- * the low-rank rows into contiguous slices; per half-iteration the ranks
- * exchange the band corrections (reduce-scatter), the new log vector
- * (all-gather) and the low-rank partials (all-reduce). world = 1 is valid. */
+/* Join `world` ranks (one process or thread per GPU) into one NCCL
+ * communicator; collective over the ranks. LCN operators built afterwards on
+ * this context are bucket-sharded: every rank passes the same full inputs;
+ * the LSH bucket ids and the landmarks are computed on every rank (bit-exact,
+ * so identical), then each rank keeps only the points of its band-0 buckets
+ * plus the halo points a later band makes it read (lcn_shard_plan_*), and
+ * builds K_sp / delta / U / W for those alone. lcn_sinkhorn* then solve ONE
+ * problem together: per half-iteration one all-gather of each rank's packed
+ * [low-rank partial (l), shift, error, flags, exported halo scalings]; the
+ * owned slices of log s / log t / P1 are all-gathered once at the end, so
+ * every rank returns the full result. world = 1 is valid. */
 int lcn_ctx_set_comm(lcn_ctx* ctx, int world, int rank, const uint8_t* id128);
+/* Bucket-sharded partition plan (host only; no GPU needed). The plan a
+ * sharded context builds internally, exposed so callers and tests can see
+ * the partition: ids_src (bands x n) / ids_tgt (bands x m) are dense bucket
+ * ids < range[b]. Points are owned by the rank of their band-0 bucket (the
+ * shard unit: neighbor_pairs emits every pair inside a bucket,
+ * lsh.cpp:222-239); a later band's bucket that spans ranks makes its members
+ * halo points of the other ranks. Local point order per rank: owned points
+ * ascending by global index, then halo points ascending. */
+typedef struct lcn_shard_plan lcn_shard_plan;
+typedef struct {
+    size_t n_own, n_halo, m_own, m_halo;  /* local sources / targets */
+    size_t exp_s, exp_t;                  /* owned points other ranks read */
+    size_t max_exp_s, max_exp_t;          /* exchange slots (max over ranks) */
+    double cost;                          /* modelled bytes per iteration */
+    unsigned long long band0_pairs;       /* sum n_b m_b of the owned band-0 buckets */
+    size_t groups;                        /* band-0 bucket groups of the plan */
+} lcn_shard_rank_info;
+int lcn_shard_plan_create(const uint32_t* ids_src, size_t n, const uint32_t* ids_tgt, size_t m, int bands,
+                          const uint32_t* range, size_t l, int world, lcn_shard_plan** out);
+int lcn_shard_plan_rank_info(const lcn_shard_plan* plan, int rank, lcn_shard_rank_info* info);
+/* local -> global indices (n_own + n_halo, m_own + m_halo entries) */
+int lcn_shard_plan_rank_points(const lcn_shard_plan* plan, int rank, uint32_t* src, uint32_t* tgt);
+/* exp_*: local indices of the exported owned points (slot order); imp_*: per
+ * halo point, its owner rank and the slot it has in the owner's export */
+int lcn_shard_plan_rank_exchange(const lcn_shard_plan* plan, int rank, uint32_t* exp_s, uint32_t* exp_t,
+                                 uint32_t* imp_s_rank, uint32_t* imp_s_slot, uint32_t* imp_t_rank,
+                                 uint32_t* imp_t_slot);
+const char* lcn_shard_plan_last_error(void);
+int lcn_shard_plan_destroy(lcn_shard_plan* plan);
+/* In-process loopback communicator: `world` ranks as host threads sharing
+ * one device (each with its own lcn_ctx); the all-gather is a host barrier
+ * plus device copies, and no kernel ever waits on another rank's kernel.
+ * For testing the sharded CUDA path with fewer GPUs than ranks. A rank that
+ * fails should call lcn_loopback_abort so the others leave the barrier. */
+typedef struct lcn_loopback lcn_loopback;
+int lcn_loopback_create(int world, lcn_loopback** out);
+int lcn_ctx_set_loopback(lcn_ctx* ctx, lcn_loopback* lb, int rank);
+int lcn_loopback_abort(lcn_loopback* lb);
+int lcn_loopback_destroy(lcn_loopback* lb);
 const char* lcn_status_name(int status);
 int lcn_abi_version(void);
 

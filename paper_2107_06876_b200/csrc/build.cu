@@ -209,7 +209,7 @@ void run_jobs(Ctx& ctx, std::vector<std::function<void(Ctx&)>>& jobs) {
     std::vector<std::exception_ptr> errs(jobs.size());
     for (auto& c : ctxs) {
         c.own_stream = nullptr;
-        c.nccl = nullptr;
+        c.comm.reset();
         CUDA_OK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
     }
     std::vector<std::thread> th;

@@ -16,6 +16,7 @@
 #include "kmeans.cuh"
 #include "kmeans_tc.cuh"
 #include "op.cuh"
+#include "shard.h"
 
 using namespace lcnb;
 
@@ -136,7 +137,10 @@ void bands_from_union_ids(Op& op, std::vector<DevBuf<uint32_t>>& ids, size_t ran
 }
 
 // Host bucket ids (bands x n, bands x m) -> dense device ids.
-void bands_from_host_ids(Op& op, const uint64_t* ids_p, const uint64_t* ids_q, int bands, uint64_t range) {
+void shard_lcn(Op& o, std::vector<DevBuf<uint32_t>>& ids, size_t range, const double* h_landmarks, int method,
+               uint64_t seed);
+void bands_from_host_ids(Op& op, const uint64_t* ids_p, const uint64_t* ids_q, int bands, uint64_t range,
+                         bool shard = false, const double* h_landmarks = nullptr, int method = 0, uint64_t seed = 0) {
     if (bands < 0 || bands > kMaxBands) throw Status(2, "neighbor_pairs: band count out of range");
     std::vector<DevBuf<uint32_t>> ids;
     size_t dense_range = 0;
@@ -160,10 +164,189 @@ void bands_from_host_ids(Op& op, const uint64_t* ids_p, const uint64_t* ids_q, i
         dense_range = std::max(dense_range, uniq.size());
     }
     op.ctx->sync();
+    if (shard && op.ctx->comm) {
+        shard_lcn(op, ids, std::max<size_t>(dense_range, 1), h_landmarks, method, seed);
+        return;
+    }
     op.bands.clear();
     op.bands.resize(bands);
     for (int b = 0; b < bands; ++b)
         build_band_layout(*op.ctx, op.bands[b], ids[b].get(), ids[b].get() + op.n, op.n, op.m, std::max<size_t>(dense_range, 1));
+}
+
+// ---- bucket-sharded LCN build (plan in shard.cpp) --------
+template <typename T>
+__global__ void gather_points_kernel(const T* __restrict__ X, const uint32_t* __restrict__ idx, long long rows, int d,
+                                     long long base, T* __restrict__ out) {
+    const long long total = rows * d;
+    for (long long e = blockIdx.x * 256LL + threadIdx.x; e < total; e += 256LL * gridDim.x) {
+        const long long r = e / d, k = e - r * d;
+        out[e] = X[(base + idx[r]) * d + k];
+    }
+}
+
+// local bucket ids of one band: ids of the global union gathered by the
+// local -> global map; halo points (k >= own) go to halo_id when given
+__global__ void gather_ids_kernel(const uint32_t* __restrict__ ids, const uint32_t* __restrict__ idx, long long cnt,
+                                  long long base, long long own, uint32_t halo_id, uint32_t* __restrict__ out) {
+    for (long long k = blockIdx.x * 256LL + threadIdx.x; k < cnt; k += 256LL * gridDim.x)
+        out[k] = (k >= own && halo_id != 0xffffffffu) ? halo_id : ids[base + idx[k]];
+}
+
+// Support size of the whole problem from the bucket ids (the local operators
+// hold only their blocks): band b adds the pairs of its buckets that no
+// earlier band holds, by inclusion-exclusion over the earlier bands.
+unsigned long long global_support(const std::vector<uint32_t>& is, const std::vector<uint32_t>& it, size_t n, size_t m,
+                                  int bands) {
+    auto mixk = [](uint64_t x) {
+        x += 0x9E3779B97F4A7C15ull;
+        x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+        x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+        return x ^ (x >> 31);
+    };
+    // pairs sharing the buckets of every band in `mask`
+    auto shared = [&](unsigned mask) {
+        std::vector<uint64_t> ks(n), kt(m);
+        auto key = [&](const std::vector<uint32_t>& ids, size_t cnt, size_t i) {
+            uint64_t h = 0;
+            for (int b = 0; b < bands; ++b)
+                if (mask >> b & 1u) h = mixk(h ^ (uint64_t(b) << 40) ^ ids[b * cnt + i]);
+            return h;
+        };
+        for (size_t i = 0; i < n; ++i) ks[i] = key(is, n, i);
+        for (size_t j = 0; j < m; ++j) kt[j] = key(it, m, j);
+        std::sort(ks.begin(), ks.end());
+        std::sort(kt.begin(), kt.end());
+        unsigned long long tot = 0;
+        size_t a = 0, c = 0;
+        while (a < n && c < m) {
+            if (ks[a] < kt[c]) ++a;
+            else if (kt[c] < ks[a]) ++c;
+            else {
+                size_t a2 = a, c2 = c;
+                while (a2 < n && ks[a2] == ks[a]) ++a2;
+                while (c2 < m && kt[c2] == kt[c]) ++c2;
+                tot += static_cast<unsigned long long>(a2 - a) * (c2 - c);
+                a = a2;
+                c = c2;
+            }
+        }
+        return tot;
+    };
+    long long nnz = 0;
+    for (unsigned mask = 1; mask < (1u << bands); ++mask)
+        nnz += (__builtin_popcount(mask) & 1 ? 1LL : -1LL) * static_cast<long long>(shared(mask));
+    return static_cast<unsigned long long>(nnz);
+}
+
+// Replace the whole-problem op (union points uploaded, device bucket ids of
+// every band computed on this rank, landmarks in o.L when landmarks_ready)
+// by this rank's shard of it and build the shard's LCN operator.
+void shard_lcn(Op& o, std::vector<DevBuf<uint32_t>>& ids, size_t range, const double* h_landmarks, int method,
+               uint64_t seed) {
+    Ctx& ctx = *o.ctx;
+    cudaStream_t s = ctx.stream;
+    const size_t n = o.n, m = o.m, d = o.d, N = n + m;
+    const int bands = static_cast<int>(ids.size());
+    if (bands < 1) throw Status(2, "sharded solve: the LCN operator needs at least one LSH band");
+    if (range + 2 > 0xffffffffull) throw Status(2, "sharded solve: bucket range too large");
+    if (h_landmarks) {
+        o.L.resize(o.l * d);
+        o.L.upload(h_landmarks, o.l * d, s);
+        o.landmarks_ready = true;
+    } else if (!o.landmarks_ready) {
+        select_landmarks_device(o, ctx, method, seed);  // the whole problem's landmarks
+        o.landmarks_ready = true;
+    }
+    PhaseTimer pt(ctx, "shard plan + local points");
+    std::vector<uint32_t> hid(static_cast<size_t>(bands) * N);
+    for (int b = 0; b < bands; ++b) ids[b].download(hid.data() + static_cast<size_t>(b) * N, N, s);
+    ctx.sync();
+    std::vector<uint32_t> is(static_cast<size_t>(bands) * n), it(static_cast<size_t>(bands) * m);
+    for (int b = 0; b < bands; ++b) {
+        std::copy(hid.begin() + static_cast<size_t>(b) * N, hid.begin() + static_cast<size_t>(b) * N + n,
+                  is.begin() + static_cast<size_t>(b) * n);
+        std::copy(hid.begin() + static_cast<size_t>(b) * N + n, hid.begin() + static_cast<size_t>(b + 1) * N,
+                  it.begin() + static_cast<size_t>(b) * m);
+    }
+    std::vector<uint32_t> rng(bands, static_cast<uint32_t>(range));
+    ShardPlan P = make_shard_plan(is.data(), n, it.data(), m, bands, rng.data(), o.l, ctx.world());
+    const ShardRank& R = P.ranks[ctx.rank()];
+    auto st = std::make_shared<ShardState>();
+    st->comm = ctx.comm;
+    st->rank = ctx.rank();
+    st->world = ctx.world();
+    st->n_glob = n;
+    st->m_glob = m;
+    st->n_own = R.n_own;
+    st->m_own = R.m_own;
+    st->nnz_glob = global_support(is, it, n, m, bands);
+    st->src_glob = R.src;
+    st->tgt_glob = R.tgt;
+    st->n_halo = R.src.size() - R.n_own;
+    st->m_halo = R.tgt.size() - R.m_own;
+    st->n_exp_s = R.exp_s.size();
+    st->n_exp_t = R.exp_t.size();
+    st->max_exp_s = P.max_exp_s;
+    st->max_exp_t = P.max_exp_t;
+    st->groups = P.groups;
+    st->cost = R.cost;
+    for (const ShardRank& Q : P.ranks) {
+        st->own_src_all.emplace_back(Q.src.begin(), Q.src.begin() + Q.n_own);
+        st->own_tgt_all.emplace_back(Q.tgt.begin(), Q.tgt.begin() + Q.m_own);
+    }
+    st->rows_need.assign(bands, std::vector<uint8_t>(range + 2, 0));
+    st->cols_need.assign(bands, std::vector<uint8_t>(range + 2, 0));
+    for (int b = 0; b < bands; ++b) {
+        for (uint32_t k = 0; k < R.n_own; ++k) st->rows_need[b][is[static_cast<size_t>(b) * n + R.src[k]]] = 1;
+        for (uint32_t k = 0; k < R.m_own; ++k) st->cols_need[b][it[static_cast<size_t>(b) * m + R.tgt[k]]] = 1;
+    }
+    auto up = [&](DevBuf<uint32_t>& dst, const std::vector<uint32_t>& v) {
+        dst.resize(std::max<size_t>(v.size(), 1));
+        if (!v.empty()) dst.upload(v.data(), v.size(), s);
+    };
+    up(st->d_src_glob, R.src);
+    up(st->d_tgt_glob, R.tgt);
+    up(st->exp_s, R.exp_s);
+    up(st->exp_t, R.exp_t);
+    up(st->imp_s_rank, R.imp_s_rank);
+    up(st->imp_s_slot, R.imp_s_slot);
+    up(st->imp_t_rank, R.imp_t_rank);
+    up(st->imp_t_slot, R.imp_t_slot);
+    // local points: sources then targets of the local union
+    const long long nl = static_cast<long long>(R.src.size()), ml = static_cast<long long>(R.tgt.size());
+    const int gb = static_cast<int>(std::min<long long>(ceil_div((nl + ml) * static_cast<long long>(d), 256), 8LL * ctx.num_sms)) + 1;
+    DevBuf<double> X(std::max<size_t>((nl + ml) * d, 1));
+    gather_points_kernel<double><<<gb, 256, 0, s>>>(o.X.get(), st->d_src_glob.get(), nl, static_cast<int>(d), 0, X.get());
+    gather_points_kernel<double><<<gb, 256, 0, s>>>(o.X.get(), st->d_tgt_glob.get(), ml, static_cast<int>(d),
+                                                    static_cast<long long>(n), X.get() + nl * d);
+    DevBuf<float> X32;
+    if (o.X32.size()) {
+        X32.resize(std::max<size_t>((nl + ml) * d, 1));
+        gather_points_kernel<float><<<gb, 256, 0, s>>>(o.X32.get(), st->d_src_glob.get(), nl, static_cast<int>(d), 0,
+                                                       X32.get());
+        gather_points_kernel<float><<<gb, 256, 0, s>>>(o.X32.get(), st->d_tgt_glob.get(), ml, static_cast<int>(d),
+                                                       static_cast<long long>(n), X32.get() + nl * d);
+    }
+    std::vector<DevBuf<uint32_t>> lids(bands);
+    for (int b = 0; b < bands; ++b) {
+        lids[b].resize(std::max<long long>(nl + ml, 1));
+        const uint32_t hs = b == 0 ? static_cast<uint32_t>(range) : 0xffffffffu;
+        const uint32_t ht = b == 0 ? static_cast<uint32_t>(range + 1) : 0xffffffffu;
+        gather_ids_kernel<<<gb, 256, 0, s>>>(ids[b].get(), st->d_src_glob.get(), nl, 0, R.n_own, hs, lids[b].get());
+        gather_ids_kernel<<<gb, 256, 0, s>>>(ids[b].get(), st->d_tgt_glob.get(), ml, static_cast<long long>(n), R.m_own,
+                                             ht, lids[b].get() + nl);
+    }
+    LAUNCH_OK("shard gather");
+    ctx.sync();
+    ids.clear();
+    o.X = std::move(X);
+    o.X32 = std::move(X32);
+    o.norms = DevBuf<double>();
+    o.n = static_cast<size_t>(nl);
+    o.m = static_cast<size_t>(ml);
+    bands_from_union_ids(o, lids, range + 2);
+    o.shard = st;
 }
 
 void finish_sparse(Op& op) {
@@ -243,7 +426,7 @@ int lcn_ctx_destroy(lcn_ctx* ctx) {
     if (!ctx) return LCN_OK;
     cudaSetDevice(ctx->c.device);
     cudaDeviceSynchronize();
-    if (ctx->c.nccl) ncclCommDestroy(static_cast<ncclComm_t>(ctx->c.nccl));
+    ctx->c.comm.reset();
     if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.own_stream);
     delete ctx;
     return LCN_OK;
@@ -269,18 +452,36 @@ int lcn_ctx_set_comm(lcn_ctx* ctx, int world, int rank, const uint8_t* id128) {
     return guard(ctx, [&] {
         if (!ctx || !id128) throw Status(2, "null context or id");
         if (world < 1 || rank < 0 || rank >= world) throw Status(2, "rank / world out of range");
-        if (ctx->c.nccl) {
-            ncclCommDestroy(static_cast<ncclComm_t>(ctx->c.nccl));
-            ctx->c.nccl = nullptr;
-        }
-        ncclUniqueId id;
-        std::memcpy(&id, id128, 128);
-        ncclComm_t comm;
-        const ncclResult_t r = ncclCommInitRank(&comm, world, id, rank);
-        if (r != ncclSuccess) throw Status(LCN_E_CUDA, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
-        ctx->c.nccl = comm;
-        ctx->c.rank = rank;
-        ctx->c.world = world;
+        ctx->c.comm.reset();
+        ctx->c.comm = make_nccl_comm(world, rank, id128);
+    });
+}
+
+int lcn_loopback_create(int world, lcn_loopback** out) {
+    return guard(nullptr, [&] {
+        if (!out) throw Status(2, "null output");
+        if (world < 1 || world > 64) throw Status(2, "rank / world out of range");
+        *out = reinterpret_cast<lcn_loopback*>(new std::shared_ptr<LoopbackGroup>(std::make_shared<LoopbackGroup>(world)));
+    });
+}
+
+int lcn_loopback_abort(lcn_loopback* lb) {
+    if (!lb) return LCN_E_INVALID_ARGUMENT;
+    (*reinterpret_cast<std::shared_ptr<LoopbackGroup>*>(lb))->abort();
+    return LCN_OK;
+}
+
+int lcn_loopback_destroy(lcn_loopback* lb) {
+    delete reinterpret_cast<std::shared_ptr<LoopbackGroup>*>(lb);
+    return LCN_OK;
+}
+
+int lcn_ctx_set_loopback(lcn_ctx* ctx, lcn_loopback* lb, int rank) {
+    return guard(ctx, [&] {
+        if (!ctx || !lb) throw Status(2, "null context or loopback group");
+        auto& g = *reinterpret_cast<std::shared_ptr<LoopbackGroup>*>(lb);
+        if (rank < 0 || rank >= g->world) throw Status(2, "rank / world out of range");
+        ctx->c.comm = make_loopback_comm(g, rank);
     });
 }
 
@@ -490,7 +691,8 @@ int lcn_op_lcn_lsh(lcn_ctx* ctx, const double* p, size_t n, const double* q, siz
         };
         lsh_bucket_ids(ctx->c, o.X.get(), o.X32.size() ? o.X32.get() : nullptr, n, m, d, lsh_params(cfg), ids, range,
                               landmarks_job);
-        bands_from_union_ids(o, ids, range);
+        if (ctx->c.comm) shard_lcn(o, ids, range, nullptr, landmark_method, landmark_seed);
+        else bands_from_union_ids(o, ids, range);
         finish_lcn(o, nullptr, l, landmark_method, landmark_seed);
         *out = h.release();
     });
@@ -505,8 +707,9 @@ int lcn_op_lcn_buckets(lcn_ctx* ctx, const double* p, size_t n, const double* q,
         check_points(q, m, d, "q");
         std::unique_ptr<lcn_op> h(new_op(ctx, cost, lambda));
         upload_union(h->o, p, n, q, m, d);
-        bands_from_host_ids(h->o, ids_p, ids_q, bands, range);
-        finish_lcn(h->o, landmarks, l, landmark_method, landmark_seed);
+        h->o.l = l;
+        bands_from_host_ids(h->o, ids_p, ids_q, bands, range, true, landmarks, landmark_method, landmark_seed);
+        finish_lcn(h->o, h->o.shard ? nullptr : landmarks, l, landmark_method, landmark_seed);
         *out = h.release();
     });
 }
@@ -636,7 +839,8 @@ int lcn_op_create_device(lcn_ctx* ctx, const float* d_p, size_t n, const float* 
             };
         lsh_bucket_ids(ctx->c, op.X.get(), op.X32.size() ? op.X32.get() : nullptr, n, m, d, lsh_params(cfg), ids, range,
                               landmarks_job);
-        bands_from_union_ids(op, ids, range);
+        if (ctx->c.comm && l) shard_lcn(op, ids, range, nullptr, landmark_method, landmark_seed);
+        else bands_from_union_ids(op, ids, range);
         if (l) finish_lcn(op, nullptr, l, landmark_method, landmark_seed);
         else finish_sparse(op);
         *out = h.release();
@@ -685,7 +889,7 @@ int lcn_op_set_bp(lcn_op* op, const double* del_p, const double* del_q) {
             return;
         }
         if (!del_p || !del_q) throw Status(1, "with_bp: deletion vector length mismatch");
-        if (o.ctx->nccl) throw Status(2, "with_bp: the BP extension is not available on a sharded context");
+        if (o.shard) throw Status(2, "with_bp: the BP extension is not available on a sharded operator");
         std::vector<double> lp(o.n), lq(o.m);
         for (size_t i = 0; i < o.n; ++i) {
             if (!(del_p[i] >= 0.0) || !std::isfinite(del_p[i]))
@@ -708,8 +912,8 @@ int lcn_op_get_info(const lcn_op* op, lcn_op_info_t* info) {
     if (!op || !info) return LCN_E_INVALID_ARGUMENT;
     const Op& o = op->o;
     info->kind = o.kind;
-    info->n = o.n;
-    info->m = o.m;
+    info->n = o.n_glob();
+    info->m = o.m_glob();
     info->l = o.l;
     info->d = o.d;
     info->bands = static_cast<int>(o.bands.size());
@@ -724,12 +928,16 @@ int lcn_op_get_info(const lcn_op* op, lcn_op_info_t* info) {
         info->streamed = 0;
         for (const auto& I : o.iter) info->streamed += I.real[1];
     }
+    if (o.shard) info->nnz = o.shard->nnz_glob;  // stored / streamed stay this rank's
     return LCN_OK;
 }
 
 int lcn_op_export_csr(lcn_op* op, int which, uint32_t* row_ptr, uint32_t* col, double* vals) {
     lcn_ctx* ctx = reinterpret_cast<lcn_ctx*>(op->o.ctx);  // Ctx is the first member of lcn_ctx
-    return guard(ctx, [&] { export_csr(op->o, which, row_ptr, col, vals); });
+    return guard(ctx, [&] {
+        if (op->o.shard) throw Status(2, "export_csr: a sharded operator holds only its rank's blocks");
+        export_csr(op->o, which, row_ptr, col, vals);
+    });
 }
 
 int lcn_op_export_factor(lcn_op* op, int which, double* out) {
@@ -737,6 +945,7 @@ int lcn_op_export_factor(lcn_op* op, int which, double* out) {
     return guard(ctx, [&] {
         Op& o = op->o;
         if (o.kind < 2 && which != 2) throw Status(2, "export_factor: operator has no low-rank factors");
+        if (o.shard && which != 2) throw Status(2, "export_factor: a sharded operator holds only its rank's factor rows");
         cudaStream_t s = o.ctx->stream;
         if (which == 0) {
             o.U64.download(out, o.n * o.l, s);
@@ -767,11 +976,11 @@ int lcn_sinkhorn(lcn_op* op, const double* p, const double* q, const lcn_sinkhor
         // Marginals::validate(balanced) (geometry.cpp:97-111)
         if (!p || !q || o.n == 0 || o.m == 0) throw Status(2, "marginals must be non-empty");
         double sp = 0.0, sq = 0.0;
-        for (size_t i = 0; i < o.n; ++i) {
+        for (size_t i = 0; i < o.n_glob(); ++i) {
             if (!(p[i] > 0.0) || !std::isfinite(p[i])) throw Status(2, "marginal p has a non-positive or non-finite entry");
             sp += p[i];
         }
-        for (size_t j = 0; j < o.m; ++j) {
+        for (size_t j = 0; j < o.m_glob(); ++j) {
             if (!(q[j] > 0.0) || !std::isfinite(q[j])) throw Status(2, "marginal q has a non-positive or non-finite entry");
             sq += q[j];
         }
@@ -784,6 +993,9 @@ int lcn_sinkhorn(lcn_op* op, const double* p, const double* q, const lcn_sinkhor
             so.check_support = opts->check_support != 0;
             so.want_plan = opts->want_plan != 0;
         }
+        if (o.shard && so.want_plan)
+            throw Status(2, "extract_plan: the plan of a sharded operator is distributed over the ranks; "
+                            "pass want_plan = 0");
         auto res = std::make_unique<lcn_result>();
         res->op = op;
         res->device = op->o.ctx->device;
@@ -903,6 +1115,7 @@ int lcn_distance_lcn(const lcn_result* res, const lcn_op* op, double* out) {
     lcn_ctx* ctx = reinterpret_cast<lcn_ctx*>(op->o.ctx);
     return guard(ctx, [&] {
         if (op->o.kind < 2) throw Status(2, "distance_lcn: operator has no low-rank factors");
+        if (op->o.shard) throw Status(2, "distance_lcn: not available on a sharded operator");
         *out = distance_lcn_device(const_cast<lcn_op*>(op)->o, res->r);
     });
 }
@@ -949,6 +1162,7 @@ int lcn_grad_cost(const lcn_result* res, const lcn_op* op, int which, double* ou
     lcn_ctx* ctx = op ? reinterpret_cast<lcn_ctx*>(op->o.ctx) : nullptr;
     return guard(ctx, [&] {
         if (!res || !op || !len) throw Status(2, "null argument");
+        if (op->o.shard) throw Status(2, "grad_cost: not available on a sharded operator");
         const Result& r = res->r;
         const Op& o = op->o;
         if (stale) *stale = r.converged ? 0 : 1;

@@ -7,6 +7,7 @@
 #include <string>
 #include <vector>
 
+#include "comm.cuh"
 #include "common.cuh"
 
 namespace lcnb {
@@ -81,10 +82,13 @@ struct Ctx {
     std::string last_error;
     // k-means assignment filter statistics (points filtered / sent to the exact scan)
     long long filter_points = 0, filter_ambiguous = 0;
-    // sharded solve: NCCL communicator over the ranks that
-    // share one problem (opaque ncclComm_t; null = single-GPU solve)
-    void* nccl = nullptr;
-    int rank = 0, world = 1;
+    // sharded solve: the communicator over the ranks that
+    // share one problem (comm.cuh; null = single-GPU solve). LCN operators
+    // built on a context with a communicator are bucket-sharded (op.cuh
+    // ShardState).
+    std::shared_ptr<Comm> comm;
+    int rank() const { return comm ? comm->rank : 0; }
+    int world() const { return comm ? comm->world : 1; }
     void activate() const { CUDA_OK(cudaSetDevice(device)); }
     void sync() const { CUDA_OK(cudaStreamSynchronize(stream)); }
 };

@@ -61,6 +61,31 @@ struct BandIter {
 
 struct Solver;
 
+// Bucket-sharded LCN operator (plan in shard.h): this rank's
+// operator covers its local points -- owned first (rows [0, n_own) /
+// [0, m_own)), then halo -- with the band-0 ids of halo points relabelled
+// into two one-sided buckets so no band-0 block is built for them.
+struct ShardState {
+    std::shared_ptr<Comm> comm;  // the context's communicator at build time
+    int rank = 0, world = 1;
+    size_t n_glob = 0, m_glob = 0;
+    uint32_t n_own = 0, m_own = 0;
+    unsigned long long nnz_glob = 0;  // support of the whole problem
+    std::vector<uint32_t> src_glob, tgt_glob;  // local -> global
+    DevBuf<uint32_t> d_src_glob, d_tgt_glob;
+    // exchange: exported local indices (slot order) and, per halo point, the
+    // owner rank and slot; slots padded to max_exp_* on every rank
+    DevBuf<uint32_t> exp_s, exp_t, imp_s_rank, imp_s_slot, imp_t_rank, imp_t_slot;
+    size_t n_exp_s = 0, n_exp_t = 0, n_halo = 0, m_halo = 0, max_exp_s = 0, max_exp_t = 0;
+    // every rank's owned global indices (the final all-gather of the result)
+    std::vector<std::vector<uint32_t>> own_src_all, own_tgt_all;
+    size_t groups = 0;
+    double cost = 0.0;
+    // per band, per local bucket: holds an owned source / an owned target
+    // (a pass skips the buckets whose outputs are all halo)
+    std::vector<std::vector<uint8_t>> rows_need, cols_need;
+};
+
 struct Op {
     Ctx* ctx = nullptr;
     int kind = 1;  // lcn_op_kind
@@ -105,6 +130,9 @@ struct Op {
     // deletion kernels c_{p,eps} (n) and c_{eps,q} (m); set in place
     bool bp = false;
     DevBuf<double> bp_ldp, bp_ldq;
+    std::shared_ptr<ShardState> shard;    // bucket-sharded operator (null: whole problem)
+    size_t n_glob() const { return shard ? shard->n_glob : n; }
+    size_t m_glob() const { return shard ? shard->m_glob : m; }
 
     BandView view(int b) const;
     BandSet bandset() const;

@@ -34,7 +34,6 @@
 #include <utility>
 #include <type_traits>
 
-#include <nccl.h>
 
 #include "async.cuh"
 #include "op.cuh"
@@ -1349,24 +1348,86 @@ __global__ void __launch_bounds__(1024) lowrank_reduce_kernel(DevState* __restri
     }
 }
 
-// Sharded solve: after the MAX / MIN all-reduce of (H, mn) into hloc[2..3],
-// rescale this rank's partial to the global shift (the SUM all-reduce of mid
-// follows) and publish the global shift / positivity flag.
-__global__ void shift_to_global_kernel(DevState* __restrict__ st, double* __restrict__ mid, int lp,
-                                       const double* __restrict__ hloc, int which) {
+// ---- bucket-sharded solve (op.cuh ShardState) -----------------------------
+// Per half-iteration every rank all-gathers one packed record of
+// kShardHdr + lp + max_exp doubles: [H, mn, err, flags x 8, pad | low-rank
+// partial (lp) | exported scalings (slot order)].
+constexpr int kShardHdr = 16;
+
+__global__ void shard_pack_kernel(const double* __restrict__ vec, const uint32_t* __restrict__ exp_idx, long long cnt,
+                                  double* __restrict__ slots) {
+    for (long long k = blockIdx.x * 256LL + threadIdx.x; k < cnt; k += 256LL * gridDim.x) slots[k] = vec[exp_idx[k]];
+}
+
+// halo points of one side: owner rank and slot per halo point (local index
+// own + k), written into the log vector and every band's bucket-ordered copy
+struct HaloUnpack {
+    const uint32_t* rank;
+    const uint32_t* slot;
+    long long cnt, own;
+    double* vec;
+    const uint32_t* pos[kMaxBands];
+    double* perm[kMaxBands];
+    int nperm;
+};
+
+// Block 0: global shift H = max_r H_r and minimum, mid = sum_r exp(H_r - H)
+// mid_r in rank order (identical on every rank), the positivity flag, and
+// (row side) the marginal error and error-flag counts summed over the ranks
+// for iter_end. Other blocks: the halo scalings.
+__global__ void __launch_bounds__(256) shard_combine_kernel(DevState* __restrict__ st, const double* __restrict__ recv,
+                                                            int world, long long stride, int lp,
+                                                            double* __restrict__ mid, int which,
+                                                            double* __restrict__ gstage, HaloUnpack hu) {
     if (st->done) return;
-    const double Hl = hloc[0], Hg = hloc[2], mng = hloc[3];
-    const double f = (Hl == kNegInf || Hg == kNegInf) ? 0.0 : exp(Hl - Hg);
-    for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < lp; a += gridDim.x * blockDim.x) mid[a] *= f;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        const int allpos = Hg != kNegInf && exp(mng - Hg) > 0.0;
-        if (which == 0) { st->H_t = Hg; st->allpos_t = allpos; }
-        else { st->H_s = Hg; st->allpos_s = allpos; }
+    if (blockIdx.x == 0) {
+        double H = kNegInf, mn = kPosInf;
+        for (int r = 0; r < world; ++r) {
+            H = fmax(H, recv[r * stride]);
+            mn = fmin(mn, recv[r * stride + 1]);
+        }
+        for (int a = threadIdx.x; a < lp; a += blockDim.x) {
+            double acc = 0.0;
+            for (int r = 0; r < world; ++r) {
+                const double hr = recv[r * stride];
+                if (hr != kNegInf) acc += recv[r * stride + kShardHdr + a] * exp(hr - H);
+            }
+            mid[a] = acc;
+        }
+        if (threadIdx.x == 0) {
+            const int allpos = H != kNegInf && exp(mn - H) > 0.0;
+            if (which == 0) { st->H_t = H; st->allpos_t = allpos; }
+            else { st->H_s = H; st->allpos_s = allpos; }
+            if (gstage) {
+                double e = 0.0;
+                for (int r = 0; r < world; ++r) e += recv[r * stride + 2];
+                gstage[0] = e;
+                for (int k = 0; k < 8; ++k) {
+                    double f = 0.0;
+                    for (int r = 0; r < world; ++r) f += recv[r * stride + 3 + k];
+                    gstage[1 + k] = f;
+                }
+            }
+        }
+        return;
+    }
+    const long long step = 256LL * (gridDim.x - 1);
+    for (long long k = (blockIdx.x - 1) * 256LL + threadIdx.x; k < hu.cnt; k += step) {
+        const double v = recv[static_cast<long long>(hu.rank[k]) * stride + kShardHdr + lp + hu.slot[k]];
+        const long long li = hu.own + k;
+        hu.vec[li] = v;
+        for (int b = 0; b < hu.nperm; ++b) hu.perm[b][hu.pos[b][li]] = v;
     }
 }
 
-// Sharded solve: this rank's marginal-error partial and error flags, summed
-// across ranks by an all-reduce before iter_end (flags as per-bit counts).
+__global__ void gather_marg_kernel(const double* __restrict__ g, const uint32_t* __restrict__ idx, long long cnt,
+                                   double* __restrict__ out) {
+    for (long long k = blockIdx.x * 256LL + threadIdx.x; k < cnt; k += 256LL * gridDim.x) out[k] = g[idx[k]];
+}
+
+// Sharded solve: this rank's marginal-error partial and error flags (as
+// per-bit counts) into its exchange record, summed across ranks before
+// iter_end.
 __global__ void __launch_bounds__(256) stage_err_kernel(const DevState* __restrict__ st,
                                                         const double* __restrict__ err_part, int G, int it,
                                                         double* __restrict__ gstage) {
@@ -1630,27 +1691,24 @@ struct Solver {
     std::vector<PassPlan> plans[2];
     int band_grid = 0;
     int lse_grid = 0;  // dense_lse_tma_kernel: persistent CTAs
-    // ---- sharded solve (ctx.nccl set): rank `rank` of `world` owns the band
-    // buckets assigned to it (per band and pass) and the low-rank row slices
-    // [lo_s, hi_s) / [lo_t, hi_t) of equal padded length cs / ct.
-    ncclComm_t comm = nullptr;
-    int rank = 0, world = 1;
-    long long cs = 0, ct = 0, lo_s = 0, hi_s = 0, lo_t = 0, hi_t = 0;
-    std::vector<DevBuf<double>> cslice_s, cslice_t;  // reduce-scattered corrections (own slice)
-    DevBuf<double> hloc, gstage;                      // shift exchange [Hl, mnl, Hg, mng]; err + flag counts
+    // ---- bucket-sharded solve (op.shard): this rank's local operator; the
+    // low-rank passes run over the owned rows [0, n_own) / [0, m_own); one
+    // all-gather per half-iteration (comm.cuh)
+    ShardState* sh = nullptr;
+    Comm* comm = nullptr;
+    long long n_own = 0, m_own = 0;
+    long long stride_s = 0, stride_t = 0;             // doubles per rank record
+    DevBuf<double> send_s, recv_s, send_t, recv_t, gstage;
 
     explicit Solver(Op& o) : op(o), ctx(*o.ctx), s(o.ctx->stream), n(o.n), m(o.m), l(static_cast<int>(o.l)) {
-        comm = static_cast<ncclComm_t>(ctx.nccl);
-        rank = ctx.rank;
-        world = ctx.world;
-        if (comm) {
+        n_own = n;
+        m_own = m;
+        if (op.shard) {
             if (op.kind != 3) throw Status(2, "sharded solve: only the LCN operator is sharded on this path");
-            cs = (ceil_div(n, world) + kRT - 1) / kRT * kRT;
-            ct = (ceil_div(m, world) + kRT - 1) / kRT * kRT;
-            lo_s = std::min<long long>(n, rank * cs);
-            hi_s = std::min<long long>(n, lo_s + cs);
-            lo_t = std::min<long long>(m, rank * ct);
-            hi_t = std::min<long long>(m, lo_t + ct);
+            sh = op.shard.get();
+            comm = sh->comm.get();
+            n_own = sh->n_own;
+            m_own = sh->m_own;
         }
         lp = static_cast<int>(o.lp);
         CPT = lp <= kThreads ? 1 : lp <= 2 * kThreads ? 2 : 4;
@@ -1705,43 +1763,27 @@ struct Solver {
             CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, band_stream_kernel<float, true>, kThreads + 64,
                                                                   sizeof(BandSmem)));
         band_grid = std::max(occ, 1) * ctx.num_sms;
-        for (const Band& B : op.bands) {
+        for (size_t b = 0; b < op.bands.size(); ++b) {
+            const Band& B = op.bands[b];
             std::vector<uint32_t> w(B.n_work);
             if (B.n_work) B.work.download(w.data(), B.n_work, s);
             ctx.sync();
-            const BandIter& I = op.iter[&B - op.bands.data()];
-            plans[0].push_back(plan_pass(B, I, owned_buckets(B, w, true), true));
-            plans[1].push_back(plan_pass(B, I, owned_buckets(B, w, false), false));
+            const BandIter& I = op.iter[b];
+            plans[0].push_back(plan_pass(B, I, needed_buckets(b, w, true), true));
+            plans[1].push_back(plan_pass(B, I, needed_buckets(b, w, false), false));
         }
         ctx.sync();
     }
 
-    // Sharded solve: the buckets of one band and pass this rank processes.
-    // Whole buckets (all pieces of a split bucket stay on one rank), assigned
-    // by longest-processing-time greedy on the streamed bytes; every rank
-    // computes the same assignment.
-    std::vector<uint32_t> owned_buckets(const Band& B, const std::vector<uint32_t>& w, bool rows) const {
-        if (!comm || world == 1) return w;
-        std::vector<std::pair<double, uint32_t>> cost;
-        for (uint32_t k : w) {
-            const double nb = B.h_src_start[k + 1] - B.h_src_start[k];
-            const double mb = B.h_tgt_start[k + 1] - B.h_tgt_start[k];
-            const double sl = rows ? mb : nb, ol = rows ? nb : mb;
-            cost.push_back({sl * static_cast<double>(row_stride(static_cast<unsigned long long>(ol))) + 64.0 * sl, k});
-        }
-        std::stable_sort(cost.begin(), cost.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
-        using Load = std::pair<double, int>;
-        std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
-        for (int r = 0; r < world; ++r) heap.push({0.0, r});
-        std::vector<uint32_t> mine;
-        for (const auto& c : cost) {
-            Load ld = heap.top();
-            heap.pop();
-            if (ld.second == rank) mine.push_back(c.second);
-            ld.first += c.first;
-            heap.push(ld);
-        }
-        return mine;
+    // Sharded solve: a pass skips the buckets whose outputs are all halo
+    // points (their values come from the owner ranks).
+    std::vector<uint32_t> needed_buckets(size_t b, const std::vector<uint32_t>& w, bool rows) const {
+        if (!sh) return w;
+        const std::vector<uint8_t>& need = rows ? sh->rows_need[b] : sh->cols_need[b];
+        std::vector<uint32_t> out;
+        for (uint32_t k : w)
+            if (k < need.size() && need[k]) out.push_back(k);
+        return out;
     }
 
     // Items of one pass: per panel of an owned bucket (BandPanel, op.cuh),
@@ -1901,10 +1943,6 @@ struct Solver {
         dpart.resize(256);
         // row vectors padded to a multiple of kRT (the bulk copies read whole tiles)
         long long np = (n + kRT - 1) / kRT * kRT, mpd = (m + kRT - 1) / kRT * kRT;
-        if (comm) {  // all-gathered vectors span world equal slices
-            np = std::max(np, cs * world);
-            mpd = std::max(mpd, ct * world);
-        }
         log_p.resize(np); log_q.resize(mpd); pv.resize(np); qv.resize(mpd);
         log_s[0].resize(np); log_s[1].resize(np); log_t.resize(mpd); row_marg.resize(np);
         err_part.resize(std::max<long long>(G, ceil_div(n, 256)));
@@ -1934,14 +1972,15 @@ struct Solver {
             }
             part.resize(static_cast<size_t>(G) * lp); hpart.resize(G); mnp.resize(G); mxp.resize(G);
             mid_s.resize(lp); mid_t.resize(lp);
-            if (comm) {
-                cslice_s.resize(op.bands.size());
-                cslice_t.resize(op.bands.size());
-                for (size_t b = 0; b < op.bands.size(); ++b) {
-                    cslice_s[b].resize(cs);
-                    cslice_t[b].resize(ct);
-                }
-                hloc.resize(4);
+            if (sh) {
+                stride_s = kShardHdr + lp + static_cast<long long>(sh->max_exp_s);
+                stride_t = kShardHdr + lp + static_cast<long long>(sh->max_exp_t);
+                send_s.resize(stride_s);
+                send_t.resize(stride_t);
+                recv_s.resize(stride_s * sh->world);
+                recv_t.resize(stride_t * sh->world);
+                send_s.zero(s);
+                send_t.zero(s);
                 gstage.resize(9);
             }
         }
@@ -2126,89 +2165,128 @@ struct Solver {
         mark(it, 4);
     }
 
-    // ---- sharded solve ---------------------------------------------------
-    static void nccl_ok(ncclResult_t r, const char* what) {
-        if (r != ncclSuccess) throw Status(100, std::string(what) + ": " + ncclGetErrorString(r));
-    }
-    // low-rank reduce over this rank's CTAs, then the cross-rank combine:
-    // global shift H = max_r H_r (all-reduce MAX), mid = sum_r exp(H_r - H)
-    // mid_r (rescale + all-reduce SUM), positivity test on the global minimum
-    void reduce_global(double* mid, int which) {
+    // ---- bucket-sharded solve ----------------------------------------------
+    // End of one side's low-rank pass: this rank's reduce into its exchange
+    // record (shift, minimum, partial; on the row side the marginal-error
+    // partial and flags), its exported scalings, ONE all-gather, then the
+    // rank-ordered combine and the halo scalings (vec and the bucket-ordered
+    // copies of every band).
+    void exchange(int side, int it, double* vec, int parity, double* mid, double* gst) {
+        DevBuf<double>& send = side ? send_t : send_s;
+        DevBuf<double>& recv = side ? recv_t : recv_s;
+        const long long stride = side ? stride_t : stride_s;
         lowrank_reduce_kernel<<<ceil_div(lp, 32), 1024, 0, s>>>(st.get(), part.get(), hpart.get(), mnp.get(), G, lp,
-                                                                mid, which, hloc.get());
-        nccl_ok(ncclAllReduce(hloc.get() + 0, hloc.get() + 2, 1, ncclDouble, ncclMax, comm, s), "allreduce shift");
-        nccl_ok(ncclAllReduce(hloc.get() + 1, hloc.get() + 3, 1, ncclDouble, ncclMin, comm, s), "allreduce min");
-        shift_to_global_kernel<<<ceil_div(lp, 256), 256, 0, s>>>(st.get(), mid, lp, hloc.get(), which);
-        nccl_ok(ncclAllReduce(mid, mid, lp, ncclDouble, ncclSum, comm, s), "allreduce mid");
+                                                                send.get() + kShardHdr, side ? 0 : 1, send.get());
+        if (gst) stage_err_kernel<<<1, 256, 0, s>>>(st.get(), err_part.get(), G, it, send.get() + 2);
+        const long long nexp = static_cast<long long>(side ? sh->n_exp_t : sh->n_exp_s);
+        if (nexp)
+            shard_pack_kernel<<<static_cast<int>(std::min<long long>(ceil_div(nexp, 256), 4LL * ctx.num_sms)), 256, 0, s>>>(
+                vec, side ? sh->exp_t.get() : sh->exp_s.get(), nexp, send.get() + kShardHdr + lp);
+        comm->allgather(send.get(), recv.get(), static_cast<size_t>(stride) * sizeof(double), s);
+        HaloUnpack hu{};
+        hu.rank = side ? sh->imp_t_rank.get() : sh->imp_s_rank.get();
+        hu.slot = side ? sh->imp_t_slot.get() : sh->imp_s_slot.get();
+        hu.cnt = static_cast<long long>(side ? sh->m_halo : sh->n_halo);
+        hu.own = side ? m_own : n_own;
+        hu.vec = vec;
+        hu.nperm = 0;
+        for (size_t b = 0; b < op.bands.size(); ++b) {
+            hu.pos[hu.nperm] = side ? op.iter[b].tp : op.iter[b].sp;
+            hu.perm[hu.nperm++] = side ? ltp[b].get() : lsp[parity][b].get();
+        }
+        const int hb = static_cast<int>(std::min<long long>(ceil_div(hu.cnt, 256), 4LL * ctx.num_sms));
+        shard_combine_kernel<<<1 + hb, 256, 0, s>>>(st.get(), recv.get(), sh->world, stride, lp, mid, side ? 0 : 1, gst,
+                                                    hu);
     }
 
-    // One iteration of the sharded solve; every rank holds
-    // the full vectors, band work is split by bucket, low-rank rows by slice.
-    // Per half-iteration: own band blocks -> reduce-scatter of the per-band
-    // corrections onto the row slices -> low-rank pass over the own slice ->
-    // all-gather of the new log vector (+ local re-scatter into the
-    // bucket-ordered copies) -> cross-rank low-rank combine; the marginal
-    // error and the error flags are summed across ranks before iter_end.
+    // One iteration of the bucket-sharded solve: the local
+    // operator's band passes (band-0 blocks entirely local, later bands over
+    // owned + halo points), the low-rank pass over the owned rows, one
+    // exchange per half-iteration; iter_end sees the summed error and flags,
+    // so every rank takes the same decisions.
     template <typename T>
-    void lcn_iteration_sharded(int it, double tol, int max_iters) {
+    void lcn_iteration_shard(int it, double tol, int max_iters) {
         const int cur = it % 2, nxt = (it + 1) % 2;
-        const int nb = static_cast<int>(op.bands.size());
         mark(it, 0);
         if (it == 0) {
             PassArgs a = base_args();
-            a.rows = hi_t - lo_t;
+            a.rows = m_own;
             a.mode = 2;
             a.in = nullptr;
-            pass<T, 1>(a, lo_t);
+            pass<T, 1>(a);
             mark(it, 1);
         } else {
             lcn_cols<T>(cur);
             mark(it, 1);
-            for (int b = 0; b < nb; ++b)
-                nccl_ok(ncclReduceScatter(corr_t[b].get(), cslice_t[b].get(), ct, ncclDouble, ncclSum, comm, s),
-                        "reduce-scatter corr_t");
             PassArgs a = base_args();
-            a.rows = hi_t - lo_t;
+            a.rows = m_own;
             a.mode = 0;
             a.mid = mid_s.get();
-            a.ncorr = nb;
-            for (int b = 0; b < nb; ++b) a.corr[b] = cslice_t[b].get();
-            a.nperm = 0;
-            a.log_marg = log_q.get() + lo_t;
-            a.log_out = log_t.get() + lo_t;
-            pass<T, 1>(a, lo_t);
-            nccl_ok(ncclAllGather(log_t.get() + rank * ct, log_t.get(), ct, ncclDouble, comm, s), "allgather log t");
-            scatter_perm(log_t.get(), m, 1, 0);
+            set_corr(a, 1);
+            set_perm(a, 1, 0);
+            a.log_marg = log_q.get();
+            a.log_out = log_t.get();
+            pass<T, 1>(a);
         }
-        reduce_global(mid_t.get(), 0);
+        exchange(1, it, log_t.get(), 0, mid_t.get(), nullptr);
         mark(it, 2);
         lcn_rows<T>();
         mark(it, 3);
-        for (int b = 0; b < nb; ++b)
-            nccl_ok(ncclReduceScatter(corr_s[b].get(), cslice_s[b].get(), cs, ncclDouble, ncclSum, comm, s),
-                    "reduce-scatter corr_s");
         PassArgs a = base_args();
-        a.rows = hi_s - lo_s;
+        a.rows = n_own;
         a.mode = 0;
         a.mid = mid_t.get();
-        a.ncorr = nb;
-        for (int b = 0; b < nb; ++b) a.corr[b] = cslice_s[b].get();
-        a.nperm = 0;
-        a.log_marg = log_p.get() + lo_s;
-        a.marg = pv.get() + lo_s;
-        a.log_cur = log_s[cur].get() + lo_s;
-        a.log_out = log_s[nxt].get() + lo_s;
-        a.row_marg = row_marg.get() + lo_s;
+        set_corr(a, 0);
+        a.log_marg = log_p.get();
+        a.marg = pv.get();
+        a.log_cur = log_s[cur].get();
+        a.log_out = log_s[nxt].get();
+        a.row_marg = row_marg.get();
         a.with_err = it > 0;
-        pass<T, 0>(a, lo_s);
-        nccl_ok(ncclAllGather(log_s[nxt].get() + rank * cs, log_s[nxt].get(), cs, ncclDouble, comm, s),
-                "allgather log s");
-        scatter_perm(log_s[nxt].get(), n, 0, nxt);
-        reduce_global(mid_s.get(), 1);
-        stage_err_kernel<<<1, 256, 0, s>>>(st.get(), err_part.get(), G, it, gstage.get());
-        nccl_ok(ncclAllReduce(gstage.get(), gstage.get(), 9, ncclDouble, ncclSum, comm, s), "allreduce error");
+        set_perm(a, 0, nxt);
+        pass<T, 0>(a);
+        exchange(0, it, log_s[nxt].get(), nxt, mid_s.get(), gstage.get());
         iter_end_kernel<<<1, 256, 0, s>>>(st.get(), err_part.get(), G, it, max_iters, tol, trace.get(), gstage.get());
         mark(it, 4);
+    }
+
+    // Owned slices of log s, P1 and log t of every rank, all-gathered once,
+    // into the whole problem's vectors (global order) on every rank; the
+    // distance identity over them in global order.
+    void finish_shard(const DevState& h, const std::vector<double>& gq, Result& res) {
+        const int fin = h.iters % 2;
+        const int W = sh->world;
+        size_t F = 1;
+        for (int r = 0; r < W; ++r) F = std::max(F, 2 * sh->own_src_all[r].size() + sh->own_tgt_all[r].size());
+        DevBuf<double> fs(F), fr(F * W);
+        CUDA_OK(cudaMemcpyAsync(fs.get(), log_s[fin].get(), n_own * 8, cudaMemcpyDeviceToDevice, s));
+        CUDA_OK(cudaMemcpyAsync(fs.get() + n_own, row_marg.get(), n_own * 8, cudaMemcpyDeviceToDevice, s));
+        CUDA_OK(cudaMemcpyAsync(fs.get() + 2 * n_own, log_t.get(), m_own * 8, cudaMemcpyDeviceToDevice, s));
+        comm->allgather(fs.get(), fr.get(), F * sizeof(double), s);
+        std::vector<double> hr(F * W);
+        fr.download(hr.data(), F * W, s);
+        ctx.sync();
+        const size_t N = sh->n_glob, M = sh->m_glob;
+        res.log_s.assign(N, 0.0);
+        res.row_marg.assign(N, 0.0);
+        res.log_t.assign(M, 0.0);
+        for (int r = 0; r < W; ++r) {
+            const std::vector<uint32_t>& os = sh->own_src_all[r];
+            const std::vector<uint32_t>& ot = sh->own_tgt_all[r];
+            const double* rec = hr.data() + static_cast<size_t>(r) * F;
+            for (size_t k = 0; k < os.size(); ++k) {
+                res.log_s[os[k]] = rec[k];
+                res.row_marg[os[k]] = rec[os.size() + k];
+            }
+            for (size_t k = 0; k < ot.size(); ++k) res.log_t[ot[k]] = rec[2 * os.size() + k];
+        }
+        // distance = lambda (<log s, P1> + <log t, q>) (sinkhorn.cpp:178-183)
+        double acc = 0.0;
+        for (size_t i = 0; i < N; ++i) acc += res.log_s[i] * res.row_marg[i];
+        for (size_t j = 0; j < M; ++j) acc += res.log_t[j] * gq[j];
+        res.distance = op.lambda * acc;
+        res.n = N;
+        res.m = M;
     }
 
     template <typename T>
@@ -2216,8 +2294,23 @@ struct Solver {
         alloc();
         trace.resize(std::max<size_t>(std::max(o.max_iters, 1), trace.size()));
         const cudaMemcpyKind kind = device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-        CUDA_OK(cudaMemcpyAsync(pv.get(), in_p, n * 8, kind, s));
-        CUDA_OK(cudaMemcpyAsync(qv.get(), in_q, m * 8, kind, s));
+        std::vector<double> gp, gq;  // sharded: the whole problem's marginals
+        if (sh) {
+            gp.resize(sh->n_glob);
+            gq.resize(sh->m_glob);
+            CUDA_OK(cudaMemcpyAsync(gp.data(), in_p, gp.size() * 8, cudaMemcpyDefault, s));
+            CUDA_OK(cudaMemcpyAsync(gq.data(), in_q, gq.size() * 8, cudaMemcpyDefault, s));
+            ctx.sync();
+            std::vector<double> lp_(n), lq_(m);
+            for (long long k = 0; k < n; ++k) lp_[k] = gp[sh->src_glob[k]];
+            for (long long k = 0; k < m; ++k) lq_[k] = gq[sh->tgt_glob[k]];
+            CUDA_OK(cudaMemcpyAsync(pv.get(), lp_.data(), n * 8, cudaMemcpyHostToDevice, s));
+            CUDA_OK(cudaMemcpyAsync(qv.get(), lq_.data(), m * 8, cudaMemcpyHostToDevice, s));
+            ctx.sync();
+        } else {
+            CUDA_OK(cudaMemcpyAsync(pv.get(), in_p, n * 8, kind, s));
+            CUDA_OK(cudaMemcpyAsync(qv.get(), in_q, m * 8, kind, s));
+        }
         log_kernel<<<ceil_div(n, 256), 256, 0, s>>>(pv.get(), log_p.get(), n);
         log_kernel<<<ceil_div(m, 256), 256, 0, s>>>(qv.get(), log_q.get(), m);
         CUDA_OK(cudaMemsetAsync(log_s[0].get(), 0, n * 8, s));
@@ -2226,7 +2319,12 @@ struct Solver {
         CUDA_OK(cudaMemsetAsync(row_marg.get(), 0, n * 8, s));
         // tol: default 1e-6 * (sum p + sum q) (sinkhorn.cpp:130-133).
         double tol = o.tol;
-        if (tol < 0.0) {
+        if (tol < 0.0 && sh) {
+            double mass = 0.0;
+            for (double v : gp) mass += v;
+            for (double v : gq) mass += v;
+            tol = 1e-6 * mass;
+        } else if (tol < 0.0) {
             double mass = 0.0;
             if (device_ptrs) {
                 sum_partial_kernel<<<64, 256, 0, s>>>(pv.get(), n, dpart.get());
@@ -2249,7 +2347,7 @@ struct Solver {
         for (int it0 = 0; it0 <= o.max_iters; it0 += chunk) {
             for (int it = it0; it < std::min(it0 + chunk, o.max_iters + 1); ++it) {
                 if (op.kind <= 1) sparse_iteration<T>(it, tol, o.max_iters);
-                else if (comm) lcn_iteration_sharded<T>(it, tol, o.max_iters);
+                else if (sh) lcn_iteration_shard<T>(it, tol, o.max_iters);
                 else lcn_iteration<T>(it, tol, o.max_iters);
             }
             LAUNCH_OK("sinkhorn iteration");
@@ -2282,23 +2380,24 @@ struct Solver {
                                     ") under the " + name + " operator");
             throw Status(4, name + (h.which == 3 ? " transposed matvec" : " matvec") + " produced a nonpositive entry");
         }
-        if (comm)  // row marginals of every slice (the distance needs all of P1)
-            nccl_ok(ncclAllGather(row_marg.get() + rank * cs, row_marg.get(), cs, ncclDouble, comm, s),
-                    "allgather row marginal");
         res.iters = h.iters;
         res.converged = h.converged != 0;
         res.marginal_err_final = h.err;
+        res.err_trace.resize(h.iters);
+        if (h.iters) trace.download(res.err_trace.data(), h.iters, s);
+        if (sh) {
+            finish_shard(h, gq, res);
+            return;
+        }
         res.n = n;
         res.m = m;
         const int fin = h.iters % 2;
         res.log_s.resize(n);
         res.log_t.resize(m);
         res.row_marg.resize(n);
-        res.err_trace.resize(h.iters);
         log_s[fin].download(res.log_s.data(), n, s);
         log_t.download(res.log_t.data(), m, s);
         row_marg.download(res.row_marg.data(), n, s);
-        if (h.iters) trace.download(res.err_trace.data(), h.iters, s);
         // distance = lambda (<log s, P1> + <log t, q>) (sinkhorn.cpp:178-183)
         const int DB = 64;
         double* dp = dpart.get();
@@ -2367,7 +2466,7 @@ struct Solver {
     // device; one host check per product keeps the reference's error order.
     template <typename T>
     void run_bp(const double* in_p, const double* in_q, const SolveOptions& o, Result& res) {
-        if (comm) throw Status(2, "sinkhorn: the BP extension is not available on a sharded context");
+        if (sh) throw Status(2, "sinkhorn: the BP extension is not available on a sharded operator");
         alloc();
         const long long R = n + m;  // rows of the extended problem (= columns)
         const size_t pad = static_cast<size_t>(R) + 2 * kRT;
@@ -2489,7 +2588,7 @@ struct Solver {
     // log_matvec / log_matvec_t (operator.cpp:226-252) on a host vector.
     template <typename T>
     void matvec(const double* h_in, bool transposed, double* h_out) {
-        if (comm) throw Status(2, "log_matvec: not available on a sharded context (use a context without a communicator)");
+        if (sh) throw Status(2, "log_matvec: not available on a sharded operator (build it on a context without a communicator)");
         alloc();
         const long long len_in = transposed ? n : m, len_out = transposed ? m : n;
         DevBuf<double> vin((len_in + kRT - 1) / kRT * kRT), vout(len_out);
@@ -2562,11 +2661,9 @@ struct Solver {
 };
 
 Solver& solver_of(Op& op) {
-    // rebuild the workspace when the context's communicator changed (the band
-    // plans and row slices depend on rank / world)
-    if (!op.ws || op.ws->comm != static_cast<ncclComm_t>(op.ctx->nccl) || op.ws->rank != op.ctx->rank ||
-        op.ws->world != op.ctx->world)
-        op.ws = std::make_shared<Solver>(op);
+    // the workspace belongs to the operator (a sharded operator's partition
+    // is fixed when it is built)
+    if (!op.ws) op.ws = std::make_shared<Solver>(op);
     return *op.ws;
 }
 

@@ -54,7 +54,7 @@ _STATUS = {1: DimensionError, 2: InvalidArgument, 3: StabilizationError, 4: Nega
 EUCLIDEAN, NEGATIVE_DOT, COSINE_DERIVED, SQEUCLIDEAN = 0, 1, 2, 3
 LANDMARK_KMEANS, LANDMARK_KMEANSPP = 0, 1
 LSH_CROSS_POLYTOPE, LSH_KMEANS, LSH_HIERARCHICAL_KMEANS = 0, 1, 2  # LshScheme (lsh.hpp:13-17)
-ABI_VERSION = 3  # include/lcn_b200.h LCN_B200_ABI_VERSION
+ABI_VERSION = 4  # include/lcn_b200.h LCN_B200_ABI_VERSION
 KIND_DENSE, KIND_SPARSE, KIND_NYSTROM, KIND_LCN = 0, 1, 2, 3
 _KIND_NAMES = {0: "dense", 1: "sparse", 2: "nystrom", 3: "lcn"}
 
@@ -81,6 +81,12 @@ class _ResInfo(C.Structure):
 
 
 _lib = None
+
+
+class _ShardInfo(C.Structure):
+    _fields_ = [(k, C.c_size_t) for k in ("n_own", "n_halo", "m_own", "m_halo", "exp_s", "exp_t", "max_exp_s",
+                                          "max_exp_t")] + [("cost", C.c_double), ("band0_pairs", C.c_ulonglong),
+                                                           ("groups", C.c_size_t)]
 
 
 def _preload_nccl():
@@ -149,6 +155,16 @@ def library() -> C.CDLL:
             "lcn_grad_cost": ([P, P, I, P, C.POINTER(SZ), C.POINTER(I)], I),
             "lcn_multihead": ([P, P, SZ, P, SZ, SZ, I, D, I, P, P, C.POINTER(_SinkOpts), P, P, P, P, P], I),
             "lcn_ctx_set_comm": ([P, I, I, P], I),
+            "lcn_loopback_create": ([I, PP], I),
+            "lcn_ctx_set_loopback": ([P, P, I], I),
+            "lcn_loopback_abort": ([P], I),
+            "lcn_loopback_destroy": ([P], I),
+            "lcn_shard_plan_create": ([P, SZ, P, SZ, I, P, SZ, I, PP], I),
+            "lcn_shard_plan_rank_info": ([P, I, C.POINTER(_ShardInfo)], I),
+            "lcn_shard_plan_rank_points": ([P, I, P, P], I),
+            "lcn_shard_plan_rank_exchange": ([P, I, P, P, P, P, P, P], I),
+            "lcn_shard_plan_last_error": ([], C.c_char_p),
+            "lcn_shard_plan_destroy": ([P], I),
             "lcn_op_set_bp": ([P, P, P], I),
         }
         for name, (args, res) in sig.items():
@@ -208,6 +224,12 @@ class Context:
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)
         self.check(self.lib.lcn_ctx_set_comm(self.h, int(world), int(rank), C.addressof(buf)))
 
+    def set_loopback(self, group: "LoopbackGroup", rank: int):
+        """Join an in-process loopback communicator (lcn_ctx_set_loopback):
+        ranks as threads sharing a device, for testing the sharded path."""
+        self.check(self.lib.lcn_ctx_set_loopback(self.h, group.h, int(rank)))
+        self._group = group
+
     def close(self):
         # live operators keep a pointer to the context: its destruction waits
         # for the last one (finalizers run in any order in cyclic collection,
@@ -230,6 +252,79 @@ class Context:
     def __del__(self):
         try:
             self.close()
+        except Exception:
+            pass
+
+
+class LoopbackGroup:
+    """lcn_loopback: `world` ranks as host threads of this process on one
+    device; the all-gather is a host barrier plus device copies."""
+
+    def __init__(self, world: int):
+        self.lib = library()
+        h = C.c_void_p()
+        if self.lib.lcn_loopback_create(int(world), C.byref(h)) != 0:
+            raise InvalidArgument(self.lib.lcn_ctx_last_error(None).decode())
+        self.h = h
+        self.world = world
+
+    def abort(self):
+        self.lib.lcn_loopback_abort(self.h)
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.lib.lcn_loopback_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+class ShardPlan:
+    """The bucket-sharded partition the library builds (lcn_shard_plan_*;
+    host only, no GPU): owned + halo points per rank and the exchange maps."""
+
+    def __init__(self, ids_src, ids_tgt, ranges, l: int, world: int):
+        self.lib = library()
+        ids_src = np.ascontiguousarray(np.atleast_2d(ids_src), np.uint32)
+        ids_tgt = np.ascontiguousarray(np.atleast_2d(ids_tgt), np.uint32)
+        rng = np.ascontiguousarray(np.broadcast_to(np.asarray(ranges, np.uint32), (ids_src.shape[0],)))
+        h = C.c_void_p()
+        rc = self.lib.lcn_shard_plan_create(_p(ids_src), ids_src.shape[1], _p(ids_tgt), ids_tgt.shape[1],
+                                            ids_src.shape[0], _p(rng), int(l), int(world), C.byref(h))
+        if rc != 0:
+            raise _STATUS.get(rc, Error)(self.lib.lcn_shard_plan_last_error().decode())
+        self.h, self.world = h, world
+
+    def info(self, rank: int) -> dict:
+        inf = _ShardInfo()
+        if self.lib.lcn_shard_plan_rank_info(self.h, rank, C.byref(inf)) != 0:
+            raise InvalidArgument(self.lib.lcn_shard_plan_last_error().decode())
+        return {k: getattr(inf, k) for k, _ in _ShardInfo._fields_}
+
+    def points(self, rank: int):
+        """(local -> global sources, local -> global targets): owned then halo."""
+        i = self.info(rank)
+        src = np.zeros(i["n_own"] + i["n_halo"], np.uint32)
+        tgt = np.zeros(i["m_own"] + i["m_halo"], np.uint32)
+        self.lib.lcn_shard_plan_rank_points(self.h, rank, _p(src), _p(tgt))
+        return src, tgt
+
+    def exchange(self, rank: int) -> dict:
+        i = self.info(rank)
+        out = {"exp_s": np.zeros(i["exp_s"], np.uint32), "exp_t": np.zeros(i["exp_t"], np.uint32)}
+        for k, cnt in (("s", i["n_halo"]), ("t", i["m_halo"])):
+            out[f"imp_{k}_rank"] = np.zeros(cnt, np.uint32)
+            out[f"imp_{k}_slot"] = np.zeros(cnt, np.uint32)
+        self.lib.lcn_shard_plan_rank_exchange(self.h, rank, _p(out["exp_s"]), _p(out["exp_t"]), _p(out["imp_s_rank"]),
+                                              _p(out["imp_s_slot"]), _p(out["imp_t_rank"]), _p(out["imp_t_slot"]))
+        return out
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.lib.lcn_shard_plan_destroy(self.h)
+                self.h = None
         except Exception:
             pass
 

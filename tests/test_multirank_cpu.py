@@ -1,6 +1,15 @@
-"""Multi-rank host logic on CPU (gloo, world_size 2): the per-half-iteration
-low-rank exchange of the sharded solve and the max-over-ranks timing rule
-(SURVEY.md §8(e)), plus the bucket-to-rank planner."""
+"""Multi-rank logic of the bucket-sharded solve on CPU.
+
+The partition comes from the library itself (lcn_shard_plan_*, host-only
+C-ABI of liblcn_b200.so, no GPU needed): the same code the sharded build
+runs. The tests check the plan's invariants (owned points partition the
+problem, every support pair of an owned point is local, the exchange maps
+point at the right values) and run the sharded LCN-Sinkhorn data flow in
+numpy over gloo, world_size 2 and 3: each rank holds only its local block
+of the support and its factor rows; per half-iteration ONE all-gather of
+[shift | low-rank partial | exported scalings] -- the record the CUDA path
+all-gathers (sinkhorn.cu lcn_iteration_shard); the gathered result equals the
+single-rank solve."""
 import math
 import os
 import socket
@@ -8,189 +17,257 @@ import socket
 import numpy as np
 import pytest
 
-from paper_2107_06876_b200 import sharding
+from paper_2107_06876_b200.native import ShardPlan
 
 
-def test_plan_shards_balances_and_is_deterministic():
-    r = np.random.default_rng(3)
-    src = r.integers(0, 600, 4096)
-    tgt = r.integers(0, 600, 4096)
-    own = sharding.plan_shards(src, tgt, 512, 8)
-    assert np.array_equal(own, sharding.plan_shards(src, tgt, 512, 8))
-    loads = sharding.shard_loads(src, tgt, 512, own, 8)
-    assert loads.max() / loads.mean() < 1.01
-    assert set(own.tolist()) == set(range(8))
+def _ids(seed, n, m, bands, buckets, coherent):
+    """Bucket ids per band. coherent: later bands re-cluster band 0 (k-means
+    LSH on clustered data: most later buckets sit inside one band-0 group);
+    otherwise independent random buckets (large halos)."""
+    r = np.random.default_rng(seed)
+    src = np.zeros((bands, n), np.uint32)
+    tgt = np.zeros((bands, m), np.uint32)
+    src[0] = r.integers(0, buckets, n)
+    tgt[0] = r.integers(0, buckets, m)
+    for b in range(1, bands):
+        if coherent:
+            perm = r.permutation(buckets)
+            flip_s = r.random(n) < 0.05
+            flip_t = r.random(m) < 0.05
+            src[b] = np.where(flip_s, r.integers(0, buckets, n), perm[src[0]])
+            tgt[b] = np.where(flip_t, r.integers(0, buckets, m), perm[tgt[0]])
+        else:
+            src[b] = r.integers(0, buckets, n)
+            tgt[b] = r.integers(0, buckets, m)
+    return src, tgt
 
 
-def test_combine_partials_matches_global_shift():
-    r = np.random.default_rng(5)
-    v = r.normal(0, 30, 1000)            # log scalings
-    F = r.uniform(0, 1, (1000, 16))      # factor rows
-    want = F.T @ np.exp(v - v.max())
-    chunks = np.array_split(np.arange(1000), 7)
-    hs, parts = [], []
-    for c in chunks:
-        h = v[c].max()
-        hs.append(h)
-        parts.append(F[c].T @ np.exp(v[c] - h))
-    hs.append(-math.inf)                 # an empty rank
-    parts.append(np.zeros(16))
-    H, mid = sharding.combine_partials(hs, parts)
-    assert H == v.max()
-    assert np.allclose(mid, want, rtol=1e-13)
+def _support(src, tgt):
+    """Dense mask of the union of the bands' bucket blocks (lsh.cpp:212-243)."""
+    return (src[:, :, None] == tgt[:, None, :]).any(axis=0)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+@pytest.mark.parametrize("coherent", [True, False])
+def test_shard_plan_invariants(world, coherent):
+    n, m, bands, buckets = 300, 260, 2, 24
+    src, tgt = _ids(5 + world, n, m, bands, buckets, coherent)
+    plan = ShardPlan(src, tgt, buckets, 16, world)
+    sup = _support(src, tgt)
+    own_s, own_t = np.full(n, -1), np.full(m, -1)
+    infos, pts, exch = [], [], []
+    for r in range(world):
+        i = plan.info(r)
+        s_loc, t_loc = plan.points(r)
+        infos.append(i)
+        pts.append((s_loc, t_loc))
+        exch.append(plan.exchange(r))
+        assert len(s_loc) == i["n_own"] + i["n_halo"] and len(t_loc) == i["m_own"] + i["m_halo"]
+        # owned ascending then halo ascending, no repeats
+        for loc, no in ((s_loc, i["n_own"]), (t_loc, i["m_own"])):
+            assert np.all(np.diff(loc[:no].astype(np.int64)) > 0)
+            assert np.all(np.diff(loc[no:].astype(np.int64)) > 0)
+            assert len(np.intersect1d(loc[:no], loc[no:])) == 0
+        assert np.all(own_s[s_loc[:i["n_own"]]] == -1) and np.all(own_t[t_loc[:i["m_own"]]] == -1)
+        own_s[s_loc[:i["n_own"]]] = r
+        own_t[t_loc[:i["m_own"]]] = r
+    assert np.all(own_s >= 0) and np.all(own_t >= 0)          # the owned points partition the problem
+    # band-0 buckets are the shard unit: both sides of a bucket on one rank
+    for c in range(buckets):
+        ranks = set(own_s[src[0] == c].tolist()) | set(own_t[tgt[0] == c].tolist())
+        assert len(ranks) <= 1
+    # every support pair of an owned point is local to its rank
+    for r in range(world):
+        s_loc, t_loc = pts[r]
+        ls, lt = np.zeros(n, bool), np.zeros(m, bool)
+        ls[s_loc] = True
+        lt[t_loc] = True
+        rows = own_s == r
+        cols = own_t == r
+        assert not np.any(sup[rows][:, ~lt]), "an owned source has a support target outside the rank"
+        assert not np.any(sup[:, cols][~ls, :]), "an owned target has a support source outside the rank"
+        # halo points are needed: each shares a later-band bucket with an owned point of the other side
+        nh = infos[r]["n_own"]
+        for g in s_loc[nh:]:
+            assert np.any(sup[g, cols])
+    # exchange maps: halo value k of rank r is slot imp_slot[k] of rank imp_rank[k]'s export
+    for r in range(world):
+        s_loc, t_loc = pts[r]
+        for side, loc, no in (("s", s_loc, infos[r]["n_own"]), ("t", t_loc, infos[r]["m_own"])):
+            e = exch[r]
+            for k, g in enumerate(loc[no:]):
+                o, slot = e[f"imp_{side}_rank"][k], e[f"imp_{side}_slot"][k]
+                o_loc = pts[o][0 if side == "s" else 1]
+                assert o_loc[exch[o][f"exp_{side}"][slot]] == g
+            assert len(e[f"exp_{side}"]) <= infos[r][f"max_exp_{side}"]
+    if world == 1:
+        assert infos[0]["n_halo"] == 0 and infos[0]["m_halo"] == 0
+    # deterministic: every rank computes the same plan
+    again = ShardPlan(src, tgt, buckets, 16, world)
+    for r in range(world):
+        a, b = again.points(r), pts[r]
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_shard_plan_groups_band0_buckets_a_later_band_joins():
+    """k-means LSH bands on clustered data re-cluster the same groups
+    (configs[3]: 1000 mixture components, both bands' 4096 buckets nest in
+    them; the plan there has no halo at all, profiles/shard_plan_c3.json).
+    Here band 1 joins band-0 buckets in threes: the affinity grouping keeps
+    each joined triple on one rank, so nothing is exchanged, and the load
+    stays balanced."""
+    r = np.random.default_rng(2)
+    n = m = 6000
+    buckets = 96
+    src0 = r.integers(0, buckets, n).astype(np.uint32)
+    tgt0 = r.integers(0, buckets, m).astype(np.uint32)
+    perm = r.permutation(buckets)
+    src = np.stack([src0, (perm[src0] // 3).astype(np.uint32)])
+    tgt = np.stack([tgt0, (perm[tgt0] // 3).astype(np.uint32)])
+    for world in (2, 4, 8):
+        plan = ShardPlan(src, tgt, buckets, 32, world)
+        infos = [plan.info(k) for k in range(world)]
+        assert sum(i["n_halo"] + i["m_halo"] for i in infos) == 0
+        assert infos[0]["max_exp_s"] == 0 and infos[0]["max_exp_t"] == 0
+        own = np.array([i["n_own"] + i["m_own"] for i in infos])
+        assert own.max() < 1.25 * own.mean()
+
+
+def test_shard_plan_rejects_bad_input():
+    from paper_2107_06876_b200 import InvalidArgument
+    src = np.zeros((1, 10), np.uint32)
+    tgt = np.zeros((1, 10), np.uint32)
+    with pytest.raises(InvalidArgument, match="world size"):
+        ShardPlan(src, tgt, 4, 8, 0)
+    with pytest.raises(InvalidArgument, match="out of range"):
+        ShardPlan(src + 7, tgt, 4, 8, 2)
+
+
+# ---------------------------------------------------------------------------
+# sharded LCN-Sinkhorn data flow over gloo
+# ---------------------------------------------------------------------------
+def _problem(seed=3):
+    r = np.random.default_rng(seed)
+    n, m, d, l, buckets = 160, 140, 3, 6, 12
+    p = r.normal(size=(n, d))
+    q = r.normal(size=(m, d)) * 1.1
+    src, tgt = _ids(seed, n, m, 2, buckets, False)
+    lam = 2.0
+    C = ((p[:, None, :] - q[None, :, :]) ** 2).sum(-1)
+    L = np.concatenate([p[:l // 2], q[:l - l // 2]])
+    U = np.exp(-((p[:, None, :] - L[None]) ** 2).sum(-1) / lam)
+    A = np.exp(-((L[:, None, :] - L[None]) ** 2).sum(-1) / lam)
+    V = np.exp(-((L[:, None, :] - q[None]) ** 2).sum(-1) / lam)
+    W = np.linalg.solve(A + 1e-9 * np.eye(l), V)               # K_nys = U W (l x m)
+    sup = _support(src, tgt)
+    delta = np.where(sup, np.exp(-C / lam) - U @ W, 0.0)        # LCN correction on the support
+    a = np.full(n, 1.0 / n)
+    b = np.full(m, 1.0 / m)
+    return dict(src=src, tgt=tgt, buckets=buckets, U=U, W=W, delta=delta, a=a, b=b, l=l)
+
+
+ITERS = 25
+
+
+def _single(pb):
+    """Unsharded reference: t-half then s-half, as the device loop."""
+    K = pb["U"] @ pb["W"] + pb["delta"]
+    s = np.ones(len(pb["a"]))
+    for _ in range(ITERS):
+        t = pb["b"] / (K.T @ s)
+        s = pb["a"] / (K @ t)
+    return s, t
+
+
+def _sharded(rank, world, pb, allgather):
+    """This rank's half of the data flow: local block of delta (owned + halo
+    points, built from the bucket ids the way the library builds it: halo
+    band-0 ids relabelled one-sided), factor rows of the local points, one
+    all-gather per half-iteration."""
+    plan = ShardPlan(pb["src"], pb["tgt"], pb["buckets"], pb["l"], world)
+    info = plan.info(rank)
+    s_loc, t_loc = plan.points(rank)
+    ex = plan.exchange(rank)
+    ns, mt = info["n_own"], info["m_own"]
+    src = pb["src"][:, s_loc].copy()
+    tgt = pb["tgt"][:, t_loc].copy()
+    src[0, ns:] = pb["buckets"]          # halo sources: a one-sided band-0 bucket
+    tgt[0, mt:] = pb["buckets"] + 1      # halo targets: another one
+    local_sup = _support(src, tgt)
+    D = np.where(local_sup, pb["delta"][np.ix_(s_loc, t_loc)], 0.0)
+    U, Wt = pb["U"][s_loc], pb["W"][:, t_loc].T
+    a, b = pb["a"][s_loc], pb["b"][t_loc]
+    l = pb["l"]
+    X_s, X_t = info["max_exp_s"], info["max_exp_t"]
+    s = np.ones(len(s_loc))
+    t = np.zeros(len(t_loc))
+
+    def exchange(vec, own, partial_rows, F, exp_idx, X, imp_rank, imp_slot):
+        # record: [partial (l) | exported values padded to X]
+        rec = np.zeros(l + X)
+        rec[:l] = F[:own].T @ partial_rows
+        rec[l:l + len(exp_idx)] = vec[exp_idx]
+        allr = allgather(rec)                                     # world x (l + X)
+        mid = allr[:, :l].sum(axis=0)                              # rank order
+        vec[own:] = allr[imp_rank, l + imp_slot]
+        return mid
+
+    mid_s = exchange(s, ns, s[:ns], U, ex["exp_s"], X_s, ex["imp_s_rank"], ex["imp_s_slot"])  # U^T s, s = 1
+    for _ in range(ITERS):
+        t[:mt] = b[:mt] / (Wt[:mt] @ mid_s + D[:, :mt].T @ s)
+        mid_t = exchange(t, mt, t[:mt], Wt, ex["exp_t"], X_t, ex["imp_t_rank"], ex["imp_t_slot"])
+        s[:ns] = a[:ns] / (U[:ns] @ mid_t + D[:ns] @ t)
+        mid_s = exchange(s, ns, s[:ns], U, ex["exp_s"], X_s, ex["imp_s_rank"], ex["imp_s_slot"])
+    return s_loc[:ns], s[:ns], t_loc[:mt], t[:mt], info
 
 
 def _free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
-    return p
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    return port
 
 
-def _worker(rank, world, port, q):
-    import torch.distributed as dist
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    r = np.random.default_rng(100 + rank)
-    h = float(r.normal(0, 40))
-    part = r.uniform(0, 1, 8)
-    H, mid = sharding.allreduce_lowrank(h, part)
-    t = sharding.max_over_ranks(float(rank) + 0.5)
-    q.put((rank, h, part, H, mid, t))
-    dist.destroy_process_group()
-
-
-def test_gloo_allreduce_lowrank_world2():
-    import torch.multiprocessing as mp
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
-    for p in procs:
-        p.start()
-    out = [q.get(timeout=120) for _ in procs]
-    for p in procs:
-        p.join(timeout=60)
-    out.sort(key=lambda x: x[0])
-    hs = [o[1] for o in out]
-    parts = [o[2] for o in out]
-    H, mid = sharding.combine_partials(hs, parts)
-    for o in out:
-        assert o[3] == H
-        assert np.allclose(o[4], mid, rtol=1e-14)
-        assert o[5] == 1.5
-
-
-def test_bucket_owners_and_row_slices_partition():
-    r = np.random.default_rng(7)
-    costs = r.uniform(1, 1e4, 500)
-    for world in (1, 2, 3, 8):
-        own = sharding.bucket_owners(costs, world)
-        assert set(own.tolist()) <= set(range(world))
-        loads = np.bincount(own, weights=costs, minlength=world)
-        assert loads.max() - loads.min() <= costs.max()  # LPT bound
-        cs, sl = sharding.row_slices(1000, world)
-        assert cs % 16 == 0 and cs * world >= 1000
-        covered = np.concatenate([np.arange(lo, hi) for lo, hi in sl])
-        assert np.array_equal(covered, np.arange(1000))
-
-
-def _half_iteration(rank, world, data, comm):
-    """One row half-iteration of the sharded solve, numpy per rank +
-    collectives through `comm` (None = single rank)."""
-    U, mid_parts, corr_blocks, log_marg, owners = data
-    n, l = U.shape
-    # band corrections: own buckets only, zeros elsewhere (then the exchange)
-    corr = np.zeros(n)
-    for b, (rows, vals) in enumerate(corr_blocks):
-        if comm is None or owners[b] == rank:  # single rank: every bucket
-            corr[rows] = vals
-    if comm:
-        corr = comm["allreduce_sum"](corr)  # reduce-scatter, read back as the full vector
-    cs, sl = sharding.row_slices(n, world)
-    lo, hi = sl[rank]
-    # cross-rank combine of the previous half's low-rank partials
-    h_r, part_r = mid_parts[rank] if comm else sharding.combine_partials(*zip(*mid_parts))
-    H, mid = comm["lowrank"](h_r, part_r) if comm else (h_r, part_r)
-    y = U[lo:hi] @ (mid * np.exp(H)) + corr[lo:hi]
-    log_out = np.full(n, np.nan)
-    log_out[lo:hi] = log_marg[lo:hi] - np.log(y)
-    if comm:
-        log_out = comm["allgather"](log_out[lo:hi], cs, n)
-    # this rank's partial for the next half (own rows, own shift)
-    v = log_out[lo:hi]
-    h = float(v.max()) if hi > lo else -math.inf
-    part = U[lo:hi].T @ np.exp(v - h) if hi > lo else np.zeros(l)
-    if comm:
-        h, part = comm["lowrank"](h, part)
-    else:
-        h, part = h, part
-    return log_out, h, part
-
-
-def _sharded_worker(rank, world, port, q):
+def _gloo_worker(rank, world, port, q):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    data = _sharded_problem(world)
+    try:
+        def allgather(rec):
+            x = torch.from_numpy(rec.copy())
+            outs = [torch.zeros_like(x) for _ in range(world)]
+            dist.all_gather(outs, x)
+            return torch.stack(outs).numpy()
 
-    def allreduce_sum(x):
-        t = torch.from_numpy(x.copy())
-        dist.all_reduce(t)
-        return t.numpy()
-
-    def allgather(own, cs, n):
-        buf = torch.zeros(cs, dtype=torch.float64)
-        buf[:len(own)] = torch.from_numpy(own)
-        outs = [torch.zeros(cs, dtype=torch.float64) for _ in range(world)]
-        dist.all_gather(outs, buf)
-        return torch.cat(outs).numpy()[:n]
-
-    comm = {"allreduce_sum": allreduce_sum, "allgather": allgather, "lowrank": sharding.allreduce_lowrank}
-    q.put((rank,) + _half_iteration(rank, world, data, comm))
-    dist.destroy_process_group()
+        q.put((rank,) + _sharded(rank, world, _problem(), allgather))
+    finally:
+        dist.destroy_process_group()
 
 
-def _sharded_problem(world):
-    r = np.random.default_rng(11)
-    n, l, nbk = 200, 12, 17
-    U = r.uniform(0.1, 1.0, (n, l))
-    bucket = r.integers(0, nbk, n)
-    corr_blocks = [(np.flatnonzero(bucket == b), r.uniform(-0.05, 0.05, int((bucket == b).sum()))) for b in range(nbk)]
-    costs = [len(rows) for rows, _ in corr_blocks]
-    owners = sharding.bucket_owners(costs, world)
-    log_marg = np.log(np.full(n, 1.0 / n))
-    # previous half's partials: rank slices of a common vector
-    v = r.normal(0, 3, n)
-    cs, sl = sharding.row_slices(n, world)
-    mid_parts = []
-    for lo, hi in sl:
-        h = float(v[lo:hi].max())
-        mid_parts.append((h, U[lo:hi].T @ np.exp(v[lo:hi] - h)))
-    return U, mid_parts, corr_blocks, log_marg, owners
-
-
-def test_gloo_sharded_half_iteration_matches_single_rank():
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_sharded_solve_matches_single_rank(world):
     import torch.multiprocessing as mp
-    world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_sharded_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_gloo_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    out = sorted([q.get(timeout=120) for _ in procs], key=lambda x: x[0])
+    out = sorted([q.get(timeout=180) for _ in procs], key=lambda x: x[0])
     for p in procs:
         p.join(timeout=60)
-    # single-rank reference of the same half-iteration
-    data = _sharded_problem(world)
-    ref_log, ref_h, ref_part = _half_iteration(0, 1, data, None)
-    for _, log_out, h, part in out:
-        assert np.allclose(log_out, ref_log, rtol=1e-13, atol=0)
-        H, mid = sharding.combine_partials([ref_h], [ref_part])
-        assert h == H
-        assert np.allclose(part, mid, rtol=1e-12)
+    pb = _problem()
+    s_ref, t_ref = _single(pb)
+    s = np.full(len(s_ref), np.nan)
+    t = np.full(len(t_ref), np.nan)
+    halo = 0
+    for _, gs, vs, gt, vt, info in out:
+        s[gs] = vs
+        t[gt] = vt
+        halo += info["n_halo"] + info["m_halo"]
+    assert halo > 0, "the random bands should leave halo points to exchange"
+    assert np.allclose(s, s_ref, rtol=1e-12, atol=0)
+    assert np.allclose(t, t_ref, rtol=1e-12, atol=0)
