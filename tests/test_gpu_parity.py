@@ -220,29 +220,34 @@ def test_lcn_one_dominant_bucket(ref, n, m):
 
 @pytest.mark.parametrize("fp64", [False, True])
 def test_sharded_solve_single_rank(ref, fp64):
-    """The sharded solve (§8(e)) through a 1-rank NCCL communicator: every
-    collective call site of the sharded loop runs (reduce-scatter, all-gather,
-    MAX/MIN/SUM all-reduces) and the result matches the unsharded solve and
-    the reference."""
+    """The bucket-sharded solve (§8(e)) through a real 1-rank NCCL
+    communicator: the shard build and every exchange of the sharded loop run
+    (ncclAllGather of the per-half-iteration record and of the result
+    slices); the result matches the unsharded solve and the reference."""
     pr = configs.config3(0.002)
     pm, qm = pr.marginals()
     cfg = lcn.LshConfig(pr.bands, 1, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
     c = lcn.Context(0, store_fp64=fp64)
     op = lcn.KernelOperator.lcn_lsh(c, pr.p, pr.q, pr.cost, pr.lam_eff, cfg, pr.landmarks, lcn.LANDMARK_KMEANS,
                                     pr.landmark_seed)
-    opts = lcn.SinkhornOptions(tol=0.0, max_iters=pr.iters)
+    opts = lcn.SinkhornOptions(tol=0.0, max_iters=pr.iters, want_plan=False)
     base = lcn.sinkhorn(op, pm, qm, opts)
-    c.set_comm(1, 0, lcn.nccl_unique_id())
-    res = lcn.sinkhorn(op, pm, qm, opts)
+    cs = lcn.Context(0, store_fp64=fp64)
+    cs.set_comm(1, 0, lcn.nccl_unique_id())
+    sop = lcn.KernelOperator.lcn_lsh(cs, pr.p, pr.q, pr.cost, pr.lam_eff, cfg, pr.landmarks, lcn.LANDMARK_KMEANS,
+                                     pr.landmark_seed)
+    res = lcn.sinkhorn(sop, pm, qm, opts)
     tol = 1e-12 if fp64 else 1e-9
+    assert sop.nnz == op.nnz
     assert rel(res.distance, base.distance) <= tol
-    assert rel(res.sp_vals, base.sp_vals) <= tol
+    assert np.max(np.abs(res.log_s - base.log_s)) <= 1e-9
+    assert np.max(np.abs(res.log_t - base.log_t)) <= 1e-9
     pairs = ref.lsh_pairs(pr.p, pr.q, pr.bands, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
     rop = ref.op_lcn(pr.p, pr.q, pr.cost, pr.lam_eff, pairs, pr.landmarks, 0, pr.landmark_seed)
     rres = rop.sinkhorn(pm, qm, tol=0.0, max_iters=pr.iters)
     assert rel(res.distance, rres.distance) <= (REL_FP64 if fp64 else REL_FP32)
     with pytest.raises(lcn.InvalidArgument, match="sharded"):
-        op.log_matvec(np.zeros(pr.m))
+        sop.log_matvec(np.zeros(pr.m))
 
 
 @pytest.mark.parametrize("fp64,cost,lam,n,m", [(False, lcn.EUCLIDEAN, 0.05, 310, 260),

@@ -109,8 +109,7 @@ def test_sharded_solve_with_halo_exchange(world):
     c0 = lcn.Context(0, store_fp64=True)
     op = build(c0)
     single = lcn.sinkhorn(op, pm, qm, opts)
-    plan_ids = np.stack([ids_p.astype(np.uint32), ids_q.astype(np.uint32)], axis=0)
-    plan = lcn.native.ShardPlan(plan_ids[0], plan_ids[1], buckets, l, world)
+    plan = lcn.ShardPlan(ids_p.astype(np.uint32), ids_q.astype(np.uint32), buckets, l, world)
     assert sum(plan.info(k)["n_halo"] for k in range(world)) > 0
     shards = _run_ranks(world, build, True, pm, qm, opts)
     _compare(single, shards, 1e-12, 1e-9)
