@@ -10,26 +10,28 @@ the stream the library launches on). `e2e` is the same metric through the
 C-ABI from pinned host buffers: every step copies the points and marginals
 host->device, runs the *whole* reference-facing path (k-means LSH, landmarks,
 Nystrom factors, LCN correction, 100 iterations) and reads the distance back;
-e2e = 100 iterations / that wall of device time (one untimed warm-up solve,
-then the mean of --e2e-steps timed solves).
+e2e = 100 iterations / that wall of device time.
 
-`roofline` is for one Sinkhorn iteration (the fused kernel sequence that is
-the hot loop): algorithmic bytes B_iter = 8 nnz + 4 l (n+m) + 16 (n+m)
- over the measured iteration time, against the measured HBM
-copy bandwidth in MEASURED_PEAKS.json.
+`roofline` is for the dominant kernel (band_stream_kernel), `iteration_roofline`
+for one whole iteration: algorithmic bytes B_iter = 8 nnz + 4 l (n+m) +
+16 (n+m) over the measured iteration time, against the
+measured HBM copy bandwidth in MEASURED_PEAKS.json.
 
-Multi-GPU (torchrun, one process per GPU): each rank solves its own
-configs[3]-shaped problem (seed + rank) — independent replicas, "scaling":
-"weak", value = iterations of all ranks / max-over-ranks time. The sharded
-single-problem solve with one NCCL allreduce per half-iteration is the next
-step.
+Multi-GPU (`--gpus N` spawns N ranks through torch.distributed.run; the
+driver launches torchrun itself): ONE configs[3] problem, bucket-sharded
+(lcn_ctx_set_comm): every rank keeps the points of its band-0 buckets (+ halo
+points of later bands) and builds only their blocks and factor rows; per
+half-iteration one NCCL all-gather of each rank's [low-rank partial, shift,
+error, flags, halo scalings] record ("scaling": "strong"). `--replicas` runs
+independent problems per GPU instead ("weak").
 
---impl reference times the reference's own CPU implementation
-(oracle/_ref: the reference sources compiled unmodified, Nystrom restated) on
-a bounded sample of configs[3] (n = m = 10^4, 2 x 41 buckets, l = 200) with
-all host threads, and scales each phase to the full configs[3] size by its
-algorithmic work (k-means: N k d; pair emission + sort: nnz log nnz; Nystrom: l^2 m; correction: nnz l;
-iterations: B_iter) to report the same metric.
+--impl reference times the reference's own CPU implementation (oracle/_ref:
+the reference sources compiled unmodified, Nystrom restated because Eigen is
+absent) on all host threads: configs[3] at scale 0.05 (bucket size, l and d
+kept) built once, then each step = 5 reference Sinkhorn iterations; `value`
+is the configs[3] iteration rate that implies (scaled by the iteration bytes
+B_iter). The full-size reference iteration phase measured by the parity run
+(profiles/parity_c3_full.json) is reported beside it.
 """
 from __future__ import annotations
 
@@ -48,7 +50,6 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 ITERS = 100
-CPU_SAMPLE_SCALE = 0.01
 # what the headline arithmetic is (bench's `dtype`): delta, U and W stored in
 # fp32; products and per-chunk partial sums in fp32; rows / tiles / chunks
 # combined in fp64; log vectors, shifts and global reductions in fp64
@@ -115,51 +116,107 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------------
-# CPU reference sample (oracle/_ref), scaled to the full configs[3]
+# CPU reference (oracle/_ref: the reference's own sources, compiled here)
 # ---------------------------------------------------------------------------
-def cpu_reference_sample():
-    """One bounded solve of configs[3] at CPU_SAMPLE_SCALE with the compiled
-    reference; returns per-phase seconds and the sample's work units."""
-    from oracle.bindings import RefLib  # checker / baseline only
-    from paper_2107_06876_b200 import configs
-    ref = RefLib()
-    pr = configs.config3(CPU_SAMPLE_SCALE)
-    t0 = time.perf_counter()
-    ids = ref.lsh_buckets(pr.p, pr.q, pr.bands, pr.buckets, pr.kmeans_iters, pr.lsh_seed)  # k-means per band
-    tk = time.perf_counter()
-    pairs = ref.pairs_from_buckets(ids[:, :pr.n], ids[:, pr.n:], pr.buckets)               # pair emission + sort
-    t1 = time.perf_counter()
-    ph = [0.0] * 4
-    op = ref.op_lcn(pr.p, pr.q, pr.cost, pr.lam_eff, pairs, pr.landmarks, 0, pr.landmark_seed, phases=ph)
-    pm, qm = pr.marginals()
-    t2 = time.perf_counter()
-    res = op.sinkhorn(pm, qm, tol=0.0, max_iters=ITERS, check_support=False, want_plan=False)
-    t3 = time.perf_counter()
-    assert res.iters == ITERS
-    return {"lsh": tk - t0, "pairs": t1 - tk, "landmarks": ph[0] / 1e3, "factors": ph[1] / 1e3,
-            "sparse_correction": (ph[2] + ph[3]) / 1e3, "iterations": t3 - t2, "n": pr.n, "m": pr.m, "d": pr.d,
-            "k": pr.buckets, "bands": pr.bands, "l": pr.landmarks, "nnz": op.nnz, "wall": t3 - t0}
+REF_SAMPLE_SCALE = 0.05   # configs[3] at n = m = 5e4: 205 buckets / band (bucket size kept), l = 512
+REF_SAMPLE_ITERS = 5      # reference Sinkhorn iterations per timed step
+FULL = {"n": 1_000_000, "m": 1_000_000, "d": 128, "k": 4096, "bands": 2, "l": 512, "kmeans_iters": 10}
+FULL_NNZ = 521_911_712    # support of configs[3] (bucket ids bit-exact with the reference, profiles/parity_c3_full.json)
 
 
-def scale_to_full(s, full_nnz, full=None):
-    """Scale each sample phase by the ratio of its algorithmic work."""
-    n, m, d, k, l, bands = 1_000_000, 1_000_000, 128, 4096, 512, 2
-    N, Ns = n + m, s["n"] + s["m"]
-    r_lsh = (N * k * bands) / (Ns * s["k"] * s["bands"])
-    r_pairs = (full_nnz * math.log2(full_nnz)) / (s["nnz"] * math.log2(s["nnz"]))
-    r_lm = (N * l) / (Ns * s["l"])
-    r_fac = (l * l * m + N * l * d) / (s["l"] ** 2 * s["m"] + Ns * s["l"] * s["d"])
-    r_cor = (full_nnz * l) / (s["nnz"] * s["l"])
-    b_full = 8 * full_nnz + 4 * l * N + 16 * N
-    b_s = 8 * s["nnz"] + 4 * s["l"] * Ns + 16 * Ns
-    r_it = b_full / b_s
-    t = (s["lsh"] * r_lsh + s["pairs"] * r_pairs + s["landmarks"] * r_lm + s["factors"] * r_fac + s["sparse_correction"] * r_cor
-         + s["iterations"] * r_it)
-    return t, {"lsh_kmeans_s": s["lsh"] * r_lsh, "lsh_pairs_s": s["pairs"] * r_pairs, "landmarks_s": s["landmarks"] * r_lm, "factors_s": s["factors"] * r_fac,
-               "correction_s": s["sparse_correction"] * r_cor, "iterations_s": s["iterations"] * r_it}
+def b_iter(nnz, n, m, l):
+    """SURVEY.md 8(d) bytes of one iteration: 8 nnz + 4 l (n + m) + 16 (n + m)."""
+    return 8.0 * nnz + 4.0 * l * (n + m) + 16.0 * (n + m)
 
 
-FULL_NNZ_ESTIMATE = 521_911_712  # measured nnz of configs[3] (round 1 GPU run); replaced live when known
+def workload_config():
+    """The workload both arms report (same dict: the driver compares them)."""
+    return {"workload": "configs[3] LCN-Sinkhorn n=m=1e6 d=128 sqL2/mean lambda=0.05 2x4096 LSH l=512",
+            "n": FULL["n"], "m": FULL["m"], "d": FULL["d"], "landmarks": FULL["l"], "bands": FULL["bands"],
+            "buckets": FULL["k"], "iterations_per_step": ITERS,
+            "l2": "inputs larger than L2 (delta + U + W = 6.2 GB per iteration)"}
+
+
+class RefSample:
+    """configs[3] at REF_SAMPLE_SCALE built once by the reference's own staged
+    path (k-means LSH per band -> neighbor_pairs -> select_landmarks ->
+    build_factors -> build_sparse -> build_correction -> KernelOperator::lcn)
+    on all host threads; each phase timed. The sample keeps configs[3]'s
+    bucket size, l and d, and its operator (~1 GB) is far larger than the host
+    caches, so one iteration costs what a full-size one costs per byte.
+    step() times REF_SAMPLE_ITERS reference Sinkhorn iterations on it."""
+
+    def __init__(self):
+        from oracle.bindings import RefLib  # checker / baseline only
+        from paper_2107_06876_b200 import configs
+        self.ref = ref = RefLib()
+        pr = self.pr = configs.config3(REF_SAMPLE_SCALE)
+        t0 = time.perf_counter()
+        ids = ref.lsh_buckets(pr.p, pr.q, pr.bands, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
+        t1 = time.perf_counter()
+        pairs = ref.pairs_from_buckets(ids[:, :pr.n], ids[:, pr.n:], pr.buckets)
+        t2 = time.perf_counter()
+        ph = [0.0] * 4
+        self.op = ref.op_lcn(pr.p, pr.q, pr.cost, pr.lam_eff, pairs, pr.landmarks, 0, pr.landmark_seed, phases=ph)
+        t3 = time.perf_counter()
+        self.pm, self.qm = pr.marginals()
+        self.nnz = int(self.op.nnz)
+        self.phases = {"lsh_kmeans": t1 - t0, "lsh_pairs": t2 - t1, "landmarks": ph[0] / 1e3, "factors": ph[1] / 1e3,
+                       "sparse_correction": (ph[2] + ph[3]) / 1e3, "build_wall": t3 - t0}
+
+    def step(self, iters=REF_SAMPLE_ITERS):
+        t0 = time.perf_counter()
+        res = self.op.sinkhorn(self.pm, self.qm, tol=0.0, max_iters=iters, check_support=False, want_plan=False)
+        dt = time.perf_counter() - t0
+        assert res.iters == iters
+        return dt
+
+    def full_rate(self, sec_per_iter, full_nnz=FULL_NNZ):
+        """Iterations/s at configs[3]: the sample's time per iteration scaled by
+        the iteration bytes (B_iter) of the full problem."""
+        pr = self.pr
+        r = b_iter(full_nnz, FULL["n"], FULL["m"], FULL["l"]) / b_iter(self.nnz, pr.n, pr.m, pr.landmarks)
+        return 1.0 / (sec_per_iter * r), r
+
+    def full_solve_extrapolated(self, sec_per_iter, full_nnz=FULL_NNZ):
+        """Seconds of a whole configs[3] solve (build + 100 iterations), each
+        build phase scaled from the sample by its algorithmic work: k-means
+        N k d per band, pairs nnz log nnz, landmarks N l, factors
+        N l d + l^2 m, correction nnz l. EXTRAPOLATED (the full build is hours
+        on the host; the iteration phase is measured in
+        profiles/parity_c3_full.json)."""
+        pr, ph = self.pr, self.phases
+        N, Ns = FULL["n"] + FULL["m"], pr.n + pr.m
+        l, ls = FULL["l"], pr.landmarks
+        sc = {"lsh_kmeans": (N * FULL["k"]) / (Ns * pr.buckets),
+              "lsh_pairs": (full_nnz * math.log2(full_nnz)) / (self.nnz * math.log2(self.nnz)),
+              "landmarks": (N * l) / (Ns * ls),
+              "factors": (N * l * FULL["d"] + l * l * FULL["m"]) / (Ns * ls * pr.d + ls * ls * pr.m),
+              "sparse_correction": (full_nnz * l) / (self.nnz * ls)}
+        parts = {k + "_s": ph[k] * sc[k] for k in sc}
+        _, r = self.full_rate(sec_per_iter, full_nnz)
+        parts["iterations_s"] = ITERS * sec_per_iter * r
+        return sum(parts.values()), parts
+
+    def describe(self):
+        pr = self.pr
+        return (f"configs[3] at scale {REF_SAMPLE_SCALE}: n=m={pr.n}, d=128, {pr.bands}x{pr.buckets} k-means LSH "
+                f"(bucket size kept), l={pr.landmarks}, nnz {self.nnz}; reference build {self.phases['build_wall']:.1f}s "
+                f"(untimed), then {REF_SAMPLE_ITERS} reference iterations per step; iteration time scaled to "
+                f"configs[3] by the iteration bytes B_iter (x{self.full_rate(1.0)[1]:.1f})")
+
+
+def full_size_measured():
+    """The full-size configs[3] reference iteration phase, measured (the
+    parity run, profiles/parity_c3_full.json), when present."""
+    try:
+        pj = json.load(open(os.path.join(ROOT, "profiles", "parity_c3_full.json")))
+        r = pj["reference"]
+        return {"iter_per_s": r["iter_per_s"], "iterations_s": r["iterations_s"], "threads": r.get("threads"),
+                "host_cores": r.get("host_cores"), "where": r.get("where", "see profiles/parity_c3_full.json"),
+                "build_phases_s": r.get("phases_s")}
+    except Exception:
+        return None
 
 
 def cpu_cores():
@@ -173,26 +230,24 @@ def run_reference(args, rank, world):
     if rank != 0:
         return 0
     os.environ.setdefault("OMP_NUM_THREADS", str(cpu_cores()))
-    times = []
-    last = None
-    for step in range(args.warmup + args.steps):
-        s = cpu_reference_sample()
-        if step >= args.warmup:
-            t_full, parts = scale_to_full(s, FULL_NNZ_ESTIMATE)
-            times.append((t_full, parts, s))
-            last = s
-    t_full = float(np.median([t[0] for t in times]))
-    parts = times[len(times) // 2][1]
-    value = ITERS / t_full
-    sample = (f"configs[3] at scale {CPU_SAMPLE_SCALE}: n=m={last['n']}, d=128, {last['bands']}x{last['k']} k-means LSH, "
-              f"l={last['l']}, {ITERS} iterations (nnz {last['nnz']}); per-phase times scaled to n=m=1e6 by "
-              f"algorithmic work (extrapolated); sample wall {last['wall']:.1f}s")
+    smp = RefSample()
+    for _ in range(args.warmup):
+        smp.step()
+    times = [smp.step() for _ in range(args.steps)]
+    step_s = float(np.mean(times))
+    value, ratio = smp.full_rate(step_s / REF_SAMPLE_ITERS)
+    t_solve, parts = smp.full_solve_extrapolated(step_s / REF_SAMPLE_ITERS)
+    cpu = {"value": value, "unit": "iter/s", "cores": cpu_cores(), "kind": "reference", "sample": smp.describe(),
+           "sample_iter_per_s": REF_SAMPLE_ITERS / step_s, "sample_build_phases_s": smp.phases,
+           "full_solve_s_extrapolated": t_solve, "full_solve_phases_s_extrapolated": parts,
+           "full_size_measured": full_size_measured()}
     line = {"impl": "reference", "metric": "lcn_sinkhorn_iters_per_s", "value": value, "unit": "iter/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_full * 1e3,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "configs[3] LCN-Sinkhorn n=m=1e6 d=128", "extrapolated_from": sample},
-            "cpu_baseline": {"value": value, "unit": "iter/s", "cores": cpu_cores(), "kind": "reference",
-                             "sample": sample, "phases_s": parts},
+            "config": workload_config(),
+            "step": f"{REF_SAMPLE_ITERS} reference iterations on the scale-{REF_SAMPLE_SCALE} sample (ms_per_step is "
+                    f"that time, measured); value = the configs[3] iteration rate it implies (B_iter scaling)",
+            "cpu_baseline": cpu,
             "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line)
     return 0
@@ -641,13 +696,13 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             os.environ.setdefault("OMP_NUM_THREADS", str(cpu_cores()))
-            s = cpu_reference_sample()
-            t_full, parts = scale_to_full(s, nnz)
-            cpu = {"value": ITERS / t_full, "unit": "iter/s", "cores": cpu_cores(), "kind": "reference",
-                   "sample": (f"configs[3] at scale {CPU_SAMPLE_SCALE} (n=m={s['n']}, {s['bands']}x{s['k']} buckets, "
-                              f"l={s['l']}, nnz {s['nnz']}, {ITERS} iterations, wall {s['wall']:.1f}s); "
-                              f"phases scaled to n=m=1e6 by algorithmic work (extrapolated)"),
-                   "phases_s": parts}
+            smp = RefSample()
+            smp.step()  # warm-up
+            st_ = float(np.mean([smp.step() for _ in range(3)]))
+            v_, _ = smp.full_rate(st_ / REF_SAMPLE_ITERS, nnz if args.scale == 1.0 else FULL_NNZ)
+            cpu = {"value": v_, "unit": "iter/s", "cores": cpu_cores(), "kind": "reference", "sample": smp.describe(),
+                   "sample_iter_per_s": REF_SAMPLE_ITERS / st_, "full_size_measured": full_size_measured()}
+            del smp
         except Exception as ex:  # the baseline must never sink the GPU line
             cpu = {"value": None, "unit": "iter/s", "cores": cpu_cores(), "kind": "reference",
                    "sample": f"unavailable: {ex}"}
@@ -678,14 +733,16 @@ def run_ours(args, rank, world, local_rank):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "strong" if sharded else "weak", "vs_baseline": None,
                 "dtype": DTYPE_LABEL, "data": "synthetic",
-                "config": {"workload": "configs[3] LCN-Sinkhorn n=m=1e6 d=128 sqL2/mean lambda=0.05 2x4096 LSH l=512",
-                           "n": n, "m": m, "d": d, "landmarks": l, "bands": pr.bands, "buckets": pr.buckets,
-                           "iterations_per_step": ITERS, "nnz": nnz, "stored_entries": stored, "streamed_entries": streamed,
-                           "scale": args.scale, "l2": "inputs larger than L2 (delta + U + W = 6.2 GB per iteration)",
-                           "parallelism": (f"one problem sharded over {world} GPUs: band buckets split by rank, "
-                                           f"low-rank rows in slices; per half-iteration NCCL reduce-scatter of the "
-                                           f"corrections, all-gather of the log vector, all-reduce of the low-rank "
-                                           f"partials" if sharded else f"{world} independent replica(s), 1 per GPU")},
+                "config": (workload_config() if args.scale == 1.0 else
+                           dict(workload_config(), workload=f"configs[3] at scale {args.scale}", n=n, m=m,
+                                landmarks=l, buckets=pr.buckets)),
+                "layout": {"nnz": nnz, "stored_entries": stored, "streamed_entries": streamed,
+                           "stored_entries_this_rank": stored},
+                "parallelism": (f"one problem bucket-sharded over {world} GPUs: each rank owns the points of its "
+                                f"band-0 buckets (+ halo of later bands) and builds only their blocks and factor rows; "
+                                f"per half-iteration one NCCL all-gather of the [low-rank partial, shift, error, "
+                                f"flags, halo scalings] records" if sharded else
+                                f"{world} independent replica(s), 1 per GPU"),
                 "distance": distance, "build_s": build_ms / 1e3,
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                              "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
