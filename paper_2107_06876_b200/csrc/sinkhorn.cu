@@ -523,7 +523,8 @@ struct ItemMeta {
     double* part;  // this piece's scratch partials (split outputs), else null
 };
 
-constexpr int kBandQ = 8;  // item queue depth (producer 1 -> producer 2)
+constexpr int kBandQ = 8;     // item queue depth (producer 1 -> producer 2)
+constexpr int kBandLook = 2;  // items claimed ahead of the one whose rows producer 1 copies
 
 struct BandSmem {
     unsigned char ring[kBandStages][kBandStageBytes];
@@ -623,21 +624,44 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
     __syncthreads();
     if (warp == kWarps) {
         // ---------------- producer 1: bulk copies of the item's rows ----------------
+        // Items are claimed kBandLook ahead of the one being copied and
+        // published to producer 2 at claim time, so the claim's atomic and
+        // producer 2's scalings / output indices for the next item overlap
+        // this item's stream instead of stalling the item boundary.
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
             bool wrapped = false;
             const uint32_t s_beg = wk.cta_off ? wk.cta_off[blockIdx.x] : 0u;
             const uint32_t s_end = wk.cta_off ? wk.cta_off[blockIdx.x + 1] : 0u;
-            for (uint32_t k = 0;; ++k) {
-                const uint32_t claim = wk.cta_off ? s_beg + k : atomicAdd(&wk.ctr[0], 1u);
-                const uint32_t it = claim < (wk.cta_off ? s_end : wk.nitems) ? claim : kEnd;
+            uint32_t ids[kBandQ];
+            uint32_t claimed = 0;
+            bool ended = false;
+            auto publish = [&]() {
+                const uint32_t k = claimed++;
+                uint32_t it = kEnd;
+                if (!ended) {
+                    const uint32_t c = wk.cta_off ? s_beg + k : atomicAdd(&wk.ctr[0], 1u);
+                    it = c < (wk.cta_off ? s_end : wk.nitems) ? c : kEnd;
+                }
                 const int qs = static_cast<int>(k % kBandQ);
                 if (k >= static_cast<uint32_t>(kBandQ)) mbar_wait(&sm.qempty[qs], ((k / kBandQ) - 1) & 1);
                 sm.q[qs] = it;
+                ids[qs] = it;
                 mbar_arrive(&sm.qfull[qs]);  // release: the queue entry
+                if (it == kEnd) ended = true;
+            };
+            for (int j = 0; j < kBandLook; ++j)
+                if (!ended) publish();
+            BandItem next{};
+            if (ids[0] != kEnd) next = wk.items[ids[0]];
+            for (uint32_t k = 0;; ++k) {
+                const uint32_t it = ids[k % kBandQ];
                 if (it == kEnd) break;
-                const BandItem item = wk.items[it];
+                if (!ended) publish();  // item k + kBandLook
+                const BandItem item = next;
+                const uint32_t it_next = ids[(k + 1) % kBandQ];
+                if (it_next != kEnd) next = wk.items[it_next];  // in flight while this item is issued
                 const uint32_t rs = item.rs;
                 const uint32_t ws = static_cast<uint32_t>(row_stride(item.ow));  // item row width in the ring
                 const int R = band_rows_per_stage<T>(ws);
@@ -684,17 +708,17 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
             // stored row c of the item is stream position c (c < g0) or c + gapn
             const double* va = logv + item.va;
             const double* vb = va + item.gapn;
-            // 4 independent loads in flight per lane before the exps (one warp
+            // 8 independent loads in flight per lane before the exps (one warp
             // resolves every stream row of the item; L2 latency bound otherwise)
-            for (uint32_t c0 = lane; c0 < item.ns; c0 += 128) {
-                double x[4];
+            for (uint32_t c0 = lane; c0 < item.ns; c0 += 256) {
+                double x[8];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
+                for (int k = 0; k < 8; ++k) {
                     const uint32_t c = c0 + 32u * k;
                     x[k] = c < item.ns ? (c < item.g0 ? va[c] : vb[c]) : 0.0;
                 }
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
+                for (int k = 0; k < 8; ++k) {
                     const uint32_t c = c0 + 32u * k;
                     if (c < item.ns) {
                         if constexpr (sizeof(T) == 4)  // fp32 storage: the scalings enter fp32 products
@@ -751,6 +775,7 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
                     // fp32 products and per-chunk partials, widened once per chunk
                     const float* vf = reinterpret_cast<const float*>(sm.vec[slot]) + r0;
                     float f0 = 0.0f, f1 = 0.0f, f2 = 0.0f, f3 = 0.0f;
+#pragma unroll 4
                     for (uint32_t r = g; r < nr; r += ng) {
                         const float4 x = *reinterpret_cast<const float4*>(p + r * ws);
                         const float sr = vf[r];
