@@ -168,6 +168,47 @@ def test_lcn_small_configs(ref, scale, which, exact):
     assert rel(lcn.distance_lcn(res, op), rres.distance_lcn()) <= REL_FP32
 
 
+_LARGE_REF = {}
+
+
+@pytest.mark.parametrize("fp64", [False, True])
+@pytest.mark.parametrize("scale,which", [(1.0, 1), (0.1, 3)])
+def test_lcn_large_configs(ref, scale, which, fp64):
+    """Full configs[1] (n = m = 2e4, d = 300, 2 x 128 buckets, l = 200) and
+    configs[3] at scale 0.1 (n = m = 1e5, 2 x 410 buckets, l = 512) against the
+    compiled reference end to end (its own k-means LSH, landmarks, factors,
+    correction, solve): support bit-exact, distance / distance_lcn and the plan
+    entries on the support within the storage mode's bar. Full configs[3]:
+    profiles/parity_c3_full.json."""
+    pr = configs.config1(scale) if which == 1 else configs.config3(scale)
+    c = lcn.Context(0, store_fp64=fp64)
+    cfg = lcn.LshConfig(pr.bands, 1, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
+    op = lcn.KernelOperator.lcn_lsh(c, pr.p, pr.q, pr.cost, pr.lam_eff, cfg, pr.landmarks, lcn.LANDMARK_KMEANS,
+                                    pr.landmark_seed)
+    pm, qm = pr.marginals()
+    key = (scale, which)
+    if key not in _LARGE_REF:  # the reference side once per config (minutes of host time)
+        pairs = ref.lsh_pairs(pr.p, pr.q, pr.bands, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
+        rop = ref.op_lcn(pr.p, pr.q, pr.cost, pr.lam_eff, pairs, pr.landmarks, 0, pr.landmark_seed)
+        del pairs
+        rres = rop.sinkhorn(pm, qm, tol=0.0, max_iters=pr.iters, check_support=False)
+        _LARGE_REF[key] = dict(csr=rop.csr(1), iters=rres.iters, distance=rres.distance, sp_vals=rres.sp_vals,
+                               distance_lcn=rres.distance_lcn())
+        del rres, rop
+    R = _LARGE_REF[key]
+    rp, col, dl = op.export_csr(1)
+    rrp, rcol, rdl = R["csr"]
+    assert np.array_equal(rp, rrp) and np.array_equal(col, rcol)
+    assert np.max(np.abs(dl - rdl)) <= (1e-8 if fp64 else 1e-4)
+    del rp, col, dl
+    res = lcn.sinkhorn(op, pm, qm, lcn.SinkhornOptions(tol=0.0, max_iters=pr.iters, check_support=False))
+    tol = REL_FP64 if fp64 else REL_FP32
+    assert res.iters == R["iters"] == pr.iters
+    assert rel(res.distance, R["distance"]) <= tol
+    assert rel(res.sp_vals, R["sp_vals"]) <= tol
+    assert rel(lcn.distance_lcn(res, op), R["distance_lcn"]) <= tol
+
+
 @pytest.mark.parametrize("fp64", [False, True])
 def test_lcn_wide_and_split_buckets(ref, fp64):
     """Two buckets of ~2000 x 2000: the band kernels cut them into <= 1024
@@ -254,7 +295,9 @@ def test_sharded_solve_single_rank(ref, fp64):
                                                (True, lcn.EUCLIDEAN, 0.05, 310, 260),
                                                (False, lcn.COSINE_DERIVED, 0.1, 310, 260),
                                                (False, lcn.NEGATIVE_DOT, 0.2, 310, 260),
-                                               (False, lcn.EUCLIDEAN, 0.05, 1200, 2052)])
+                                               (False, lcn.EUCLIDEAN, 0.05, 1200, 2052),
+                                               (False, lcn.EUCLIDEAN, 0.05, 5000, 5000),
+                                               (True, lcn.EUCLIDEAN, 0.05, 5000, 5000)])
 def test_dense_anchor(ref, fp64, cost, lam, n, m):
     """configs[2]-shaped dense operator (H19): log K bit-exact, distance and the
     dense plan against the reference's dense solve. Row lengths divisible by 4
