@@ -199,7 +199,11 @@ def test_lcn_large_configs(ref, scale, which, fp64):
     rp, col, dl = op.export_csr(1)
     rrp, rcol, rdl = R["csr"]
     assert np.array_equal(rp, rrp) and np.array_equal(col, rcol)
-    assert np.max(np.abs(dl - rdl)) <= (1e-8 if fp64 else 1e-4)
+    # configs[1]'s target is a rotated copy: the union's k-means never puts a
+    # source and a target in one bucket, so its support is empty on both sides
+    # and the LCN operator is its Nystrom part
+    if len(dl):
+        assert np.max(np.abs(dl - rdl)) <= (1e-8 if fp64 else 1e-4)
     del rp, col, dl
     res = lcn.sinkhorn(op, pm, qm, lcn.SinkhornOptions(tol=0.0, max_iters=pr.iters, check_support=False))
     tol = REL_FP64 if fp64 else REL_FP32
