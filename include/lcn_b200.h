@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define LCN_B200_ABI_VERSION 4  /* 3: lcn_op_info_t.streamed; 4: bucket-sharded solve, loopback, shard plan */
+#define LCN_B200_ABI_VERSION 5  /* 3: lcn_op_info_t.streamed; 4: bucket-sharded solve, loopback, shard plan; 5: staged build */
 
 typedef struct lcn_ctx lcn_ctx;
 typedef struct lcn_op lcn_op;
@@ -300,6 +300,60 @@ int lcn_op_export_csr(lcn_op* op, int which, uint32_t* row_ptr, uint32_t* col, d
 int lcn_op_export_factor(lcn_op* op, int which, double* out);
 /* log_matvec / log_matvec_t (operator.cpp:226-252), host vectors. */
 int lcn_op_log_matvec(lcn_op* op, const double* in, int transposed, double* out);
+
+/* ---- staged build from host structs ------------------------------------ */
+/* The reference's caller builds an LCN operator in stages and hands host
+ * structs between them (runner.cpp:258-271): lsh_neighbor_pairs ->
+ * build_sparse -> select_landmarks -> build_factors -> build_correction ->
+ * KernelOperator::lcn(factors, correction). Each stage below takes and returns
+ * the plain arrays of those structs, so a shim can keep the reference's types
+ * (integration/lcn_shim.cpp). Patterns are CSR: row_ptr
+ * (n + 1), col (nnz), sorted and unique within a row, as NeighborPairs /
+ * SparseKernel / LcnCorrection hold them (sparse_kernel.hpp:17-50). */
+typedef struct lcn_pairs lcn_pairs;
+/* lsh_neighbor_pairs (lsh.hpp:67-68, lsh.cpp:245-283): the support of the
+ * configured LSH as a NeighborPairs CSR (pairs sorted row-major, unique). */
+int lcn_lsh_neighbor_pairs(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m, size_t d,
+                           const lcn_lsh_config* cfg, lcn_pairs** out);
+int lcn_pairs_info(const lcn_pairs* pairs, size_t* n, size_t* m, size_t* nnz);
+int lcn_pairs_copy(const lcn_pairs* pairs, uint32_t* row_ptr, uint32_t* col);
+int lcn_pairs_destroy(lcn_pairs* pairs);
+/* build_sparse (sparse_kernel.hpp:32-33, sparse_kernel.cpp:51-80): logvals
+ * = 0 - c(p_i, q_j) * (1 / lambda) at the pattern, bit-exact (the reference's
+ * sequential fp64 folds on the device). */
+int lcn_build_sparse(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m, size_t d,
+                     const uint32_t* row_ptr, const uint32_t* col, size_t nnz, int cost, double lambda,
+                     double* logvals);
+/* select_landmarks (nystrom.hpp:26-27, nystrom.cpp:28-48): l x d, bit-exact. */
+int lcn_select_landmarks(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m, size_t d, size_t l,
+                         int method, uint64_t seed, double* out);
+/* build_factors (nystrom.hpp:46-47, nystrom.cpp:68-125): U = k(X_p, L)
+ * (n x l) and W = A^-1 V (l x m), row-major like NystromFactors::u / ::w;
+ * same jitter schedule and FactorizationError. */
+int lcn_build_factors(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m, size_t d,
+                      const double* landmarks, size_t l, int cost, double lambda, double* U, double* W,
+                      double* cond_estimate);
+/* build_correction (sparse_kernel.hpp:54, sparse_kernel.cpp:82-117): delta
+ * = exp(log_sp) - (U W)_ij and nys_vals = (U W)_ij at the pattern (the
+ * reference's sequential entry() fold); max |delta|; StabilizationError on
+ * overflow. */
+int lcn_build_correction(lcn_ctx* ctx, size_t n, size_t m, size_t l, const uint32_t* row_ptr, const uint32_t* col,
+                         size_t nnz, const double* log_sp, const double* U, const double* W, double* delta,
+                         double* nys_vals, double* max_abs_delta);
+/* KernelOperator factories (operator.hpp:33-36) from the host structs:
+ * dense(DenseKernel) = n x m log K; sparse(SparseKernel) = any CSR pattern
+ * with its log K; nystrom(NystromFactors); lcn(NystromFactors,
+ * LcnCorrection) = factors + any CSR pattern with delta and log K^sp. General
+ * patterns run on CSR / CSC kernels (fp64 values); the bucket-blocked fast
+ * path is the lcn_op_*_lsh / _buckets family. */
+int lcn_op_from_dense(lcn_ctx* ctx, size_t n, size_t m, const double* logk, double lambda, lcn_op** out);
+int lcn_op_from_sparse(lcn_ctx* ctx, size_t n, size_t m, const uint32_t* row_ptr, const uint32_t* col, size_t nnz,
+                       const double* logvals, double lambda, lcn_op** out);
+int lcn_op_from_nystrom(lcn_ctx* ctx, size_t n, size_t m, size_t l, const double* U, const double* W, double lambda,
+                        lcn_op** out);
+int lcn_op_from_lcn(lcn_ctx* ctx, size_t n, size_t m, size_t l, const double* U, const double* W, double lambda,
+                    const uint32_t* row_ptr, const uint32_t* col, size_t nnz, const double* delta,
+                    const double* log_sp, double max_abs_delta, lcn_op** out);
 
 /* ---- solver (sinkhorn.hpp:68-121) ------------------------------------- */
 /* sinkhorn (sinkhorn.cpp:104-188). p (n), q (m) host marginals. */

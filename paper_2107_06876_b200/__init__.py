@@ -11,7 +11,8 @@ from .native import (  # noqa: F401
     COSINE_DERIVED, EUCLIDEAN, LANDMARK_KMEANS, LANDMARK_KMEANSPP, LSH_CROSS_POLYTOPE, LSH_HIERARCHICAL_KMEANS,
     LSH_KMEANS, NEGATIVE_DOT, SQEUCLIDEAN, Context, CudaError,
     DimensionError, Error, FactorizationError, InvalidArgument, KernelOperator, LoopbackGroup, LshConfig,
-    NegativeKernelError, ShardPlan,
+    NegativeKernelError, ShardPlan, build_correction, build_factors, build_sparse, lsh_neighbor_pairs,
+    select_landmarks,
     SinkhornOptions, SinkhornResult, StabilizationError, assign_nearest, batched_lcn, cross_polytope_buckets, distance_lcn, grad_cost, kmeans_pp_indices, library,
     lloyd, lsh_buckets, lsh_kmeans_buckets, multihead, nccl_unique_id, read_points_file, sample_clustered,
     sample_uniform_ball, sinkhorn, sinkhorn_device, write_points_file)

@@ -1467,6 +1467,14 @@ void build_dense(Op& op) {
     else
         launch_dense_tiles<0>(ctx, op.P(), n, op.Q(), m, static_cast<int>(d), epi);
     if (read_flag(ctx, bad)) throw Status(2, "cosine-derived cost undefined for zero vectors");
+    dense_storage(op);
+}
+
+// Iteration copies of a dense log K (op.dk64, n x m): fp32 or fp64, in both
+// orientations so both half-iterations stream rows.
+void dense_storage(Op& op) {
+    Ctx& ctx = *op.ctx;
+    const size_t n = op.n, m = op.m;
     const dim3 grid(static_cast<unsigned>(ceil_div(m, 32)), static_cast<unsigned>(ceil_div(n, 32)));
     if (op.fp64) {
         op.dk64T.resize(std::max<size_t>(n * m, 1));
@@ -2179,6 +2187,12 @@ void csr_values_device(Op& op, int which, double* d_vals) {
     build_csr(op);
     Ctx& ctx = *op.ctx;
     cudaStream_t s = ctx.stream;
+    if (op.gcsr && op.nnz && which != 3) {
+        if (which == 1 && op.kind != 3) throw Status(2, "export_csr: delta needs an lcn operator");
+        const double* src = op.kind == 3 ? (which == 1 ? op.gval.get() : op.glogsp.get()) : op.gval.get();
+        CUDA_OK(cudaMemcpyAsync(d_vals, src, op.nnz * 8, cudaMemcpyDeviceToDevice, s));
+        return;
+    }
     if (op.nnz) {
         BandViews bvs{};
         bvs.bands = static_cast<int>(op.bands.size());
@@ -2196,6 +2210,138 @@ void csr_values_device(Op& op, int which, double* d_vals) {
                                                               static_cast<int>(op.l), d_vals);
         LAUNCH_OK("csr values");
     }
+}
+
+// ---- general CSR patterns (the staged API from host structs) ----------------
+namespace {
+// log K at the pairs of a CSR pattern (build_sparse, sparse_kernel.cpp:70-77):
+// 0 - c(p_i, q_j) * (1 / lambda), exact sequential fold of cost_value. One
+// warp per row, lanes over its entries.
+__global__ void sparse_pairs_kernel(const double* __restrict__ X, long long n, int d, int kind, double inv,
+                                    const uint32_t* __restrict__ rp, const uint32_t* __restrict__ col,
+                                    double* __restrict__ out, int* __restrict__ bad) {
+    const long long i = (blockIdx.x * 256LL + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    const double* x = X + i * d;
+    for (uint32_t e = rp[i] + lane; e < rp[i + 1]; e += 32) {
+        const double* y = X + (n + col[e]) * static_cast<long long>(d);
+        const double c = cost_exact(kind, x, y, d);
+        if (kind == 2 && isnan(c)) atomicOr(bad, 1);
+        out[e] = xsub(0.0, xmul(c, inv));
+    }
+}
+
+// build_correction (sparse_kernel.cpp:96-109) at a CSR pattern: exact =
+// exp(log_sp), nys = sum_a U[i,a] W[a,j] in the reference's sequential order
+// (NystromFactors::entry, nystrom.cpp:127-132), delta = exact - nys.
+__global__ void correction_pairs_kernel(long long n, int l, const uint32_t* __restrict__ rp,
+                                        const uint32_t* __restrict__ col, const double* __restrict__ logsp,
+                                        const double* __restrict__ U, const double* __restrict__ Wt,
+                                        double* __restrict__ delta, double* __restrict__ nys,
+                                        unsigned long long* __restrict__ maxbits, int* __restrict__ overflow) {
+    const long long i = (blockIdx.x * 256LL + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    double mx = 0.0;
+    for (uint32_t e = rp[i] + lane; e < rp[i + 1]; e += 32) {
+        const double exact = exp(logsp[e]);
+        if (isinf(exact)) {
+            atomicOr(overflow, 1);
+            continue;
+        }
+        const double* u = U + i * l;
+        const double* w = Wt + static_cast<long long>(col[e]) * l;
+        double s = 0.0;
+        for (int a = 0; a < l; ++a) s = xadd(s, xmul(u[a], w[a]));
+        nys[e] = s;
+        delta[e] = xsub(exact, s);
+        mx = fmax(mx, fabs(delta[e]));
+    }
+    mx = warp_max(mx);
+    if (lane == 0 && mx > 0.0) atomicMax(maxbits, static_cast<unsigned long long>(__double_as_longlong(mx)));
+}
+}  // namespace
+
+void build_sparse_pairs(Op& op, const uint32_t* d_rp, const uint32_t* d_col, size_t nnz, double* d_out) {
+    Ctx& ctx = *op.ctx;
+    if (!(op.lambda > 0.0)) throw Status(2, "build_sparse: lambda must be positive");
+    DevBuf<int> bad(1);
+    bad.zero(ctx.stream);
+    if (op.n && nnz)
+        sparse_pairs_kernel<<<static_cast<unsigned>(ceil_div(op.n * 32, 256)), 256, 0, ctx.stream>>>(
+            op.X.get(), static_cast<long long>(op.n), static_cast<int>(op.d), op.cost, 1.0 / op.lambda, d_rp, d_col,
+            d_out, bad.get());
+    LAUNCH_OK("build_sparse pairs");
+    if (read_flag(ctx, bad)) throw Status(2, "cosine-derived cost undefined for zero vectors");
+}
+
+void correction_pairs(Ctx& ctx, size_t n, size_t l, const uint32_t* d_rp, const uint32_t* d_col, size_t nnz,
+                      const double* d_logsp, const double* d_U, const double* d_Wt, double* d_delta, double* d_nys,
+                      double* max_abs) {
+    DevBuf<unsigned long long> mb(1);
+    DevBuf<int> of(1);
+    mb.zero(ctx.stream);
+    of.zero(ctx.stream);
+    if (n && nnz)
+        correction_pairs_kernel<<<static_cast<unsigned>(ceil_div(n * 32, 256)), 256, 0, ctx.stream>>>(
+            static_cast<long long>(n), static_cast<int>(l), d_rp, d_col, d_logsp, d_U, d_Wt, d_delta, d_nys, mb.get(),
+            of.get());
+    LAUNCH_OK("build_correction pairs");
+    unsigned long long h = 0;
+    mb.download(&h, 1, ctx.stream);
+    if (read_flag(ctx, of)) throw Status(3, "build_correction: kernel value overflows linear space");
+    double v;
+    std::memcpy(&v, &h, 8);
+    *max_abs = v;
+}
+
+// A host CSR pattern as the operator's support (KernelOperator::sparse / lcn):
+// the CSC view by the reference's counting sort (build_csc_arrays,
+// sparse_kernel.cpp:17-35), values in both orders.
+void set_general_csr(Op& op, const uint32_t* h_rp, const uint32_t* h_col, size_t nnz, const double* h_val,
+                     const double* h_logsp) {
+    Ctx& ctx = *op.ctx;
+    cudaStream_t s = ctx.stream;
+    const size_t n = op.n, m = op.m;
+    if (h_rp[0] != 0 || h_rp[n] != nnz) throw Status(1, "operator: pattern row pointer does not match nnz");
+    for (size_t i = 0; i < n; ++i)
+        if (h_rp[i + 1] < h_rp[i]) throw Status(2, "operator: pattern row pointer is not monotone");
+    std::vector<uint32_t> cp(m + 1, 0), ri(nnz), cur(m);
+    std::vector<double> vt(nnz);
+    for (size_t e = 0; e < nnz; ++e) {
+        if (h_col[e] >= m) throw Status(2, "neighbor pair index out of range");
+        ++cp[h_col[e] + 1];
+    }
+    for (size_t j = 0; j < m; ++j) cp[j + 1] += cp[j];
+    std::copy(cp.begin(), cp.end() - 1, cur.begin());
+    for (size_t i = 0; i < n; ++i)
+        for (uint32_t e = h_rp[i]; e < h_rp[i + 1]; ++e) {
+            const uint32_t pos = cur[h_col[e]]++;
+            ri[pos] = static_cast<uint32_t>(i);
+            vt[pos] = h_val[e];
+        }
+    op.gcsr = true;
+    op.nnz = nnz;
+    op.stored = nnz;
+    op.csr_row_ptr.upload(h_rp, n + 1, s);
+    op.csr_col.resize(std::max<size_t>(nnz, 1));
+    op.gval.resize(std::max<size_t>(nnz, 1));
+    op.gvalT.resize(std::max<size_t>(nnz, 1));
+    op.gri.resize(std::max<size_t>(nnz, 1));
+    if (nnz) {
+        CUDA_OK(cudaMemcpyAsync(op.csr_col.get(), h_col, nnz * 4, cudaMemcpyHostToDevice, s));
+        CUDA_OK(cudaMemcpyAsync(op.gval.get(), h_val, nnz * 8, cudaMemcpyHostToDevice, s));
+        CUDA_OK(cudaMemcpyAsync(op.gvalT.get(), vt.data(), nnz * 8, cudaMemcpyHostToDevice, s));
+        CUDA_OK(cudaMemcpyAsync(op.gri.get(), ri.data(), nnz * 4, cudaMemcpyHostToDevice, s));
+    }
+    op.gcp.upload(cp.data(), m + 1, s);
+    if (h_logsp) {
+        op.glogsp.resize(std::max<size_t>(nnz, 1));
+        if (nnz) CUDA_OK(cudaMemcpyAsync(op.glogsp.get(), h_logsp, nnz * 8, cudaMemcpyHostToDevice, s));
+    }
+    op.csr_ready = true;
+    ctx.sync();
 }
 
 void export_csr(Op& op, int which, uint32_t* row_ptr, uint32_t* col, double* vals) {

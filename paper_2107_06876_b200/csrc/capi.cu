@@ -30,6 +30,10 @@ struct lcn_ctx {
 struct lcn_op {
     Op o;
 };
+struct lcn_pairs {  // NeighborPairs (lsh.hpp:51-60) as CSR
+    size_t n = 0, m = 0;
+    std::vector<uint32_t> row_ptr, col;
+};
 struct lcn_result {
     Result r;
     lcn_op* op = nullptr;
@@ -653,6 +657,225 @@ int lcn_op_sparse_lsh(lcn_ctx* ctx, const double* p, size_t n, const double* q, 
         if (static_cast<int>(ids.size()) > kMaxBands) throw Status(2, "lsh: at most 8 bands on this path");
         bands_from_union_ids(h->o, ids, range);
         finish_sparse(h->o);
+        *out = h.release();
+    });
+}
+
+// ---- staged build from host structs (runner.cpp:258-271) -------------------
+int lcn_lsh_neighbor_pairs(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m, size_t d,
+                           const lcn_lsh_config* cfg, lcn_pairs** out) {
+    return guard(ctx, [&] {
+        if (!out) throw Status(2, "null output");
+        check_points(p, n, d, "p");
+        check_points(q, m, d, "q");
+        std::unique_ptr<lcn_op> h(new_op(ctx, 0, 1.0));
+        upload_union(h->o, p, n, q, m, d);
+        std::vector<DevBuf<uint32_t>> ids;
+        size_t range = 0;
+        lsh_bucket_ids(ctx->c, h->o.X.get(), h->o.X32.size() ? h->o.X32.get() : nullptr, n, m, d, lsh_params(cfg), ids,
+                       range);
+        if (static_cast<int>(ids.size()) > kMaxBands) throw Status(2, "lsh: at most 8 bands on this path");
+        bands_from_union_ids(h->o, ids, range);
+        build_csr(h->o);
+        auto pr = std::make_unique<lcn_pairs>();
+        pr->n = n;
+        pr->m = m;
+        pr->row_ptr.resize(n + 1);
+        pr->col.resize(h->o.nnz);
+        export_csr(h->o, 0, pr->row_ptr.data(), pr->col.data(), nullptr);
+        *out = pr.release();
+    });
+}
+
+int lcn_pairs_info(const lcn_pairs* pr, size_t* n, size_t* m, size_t* nnz) {
+    if (!pr) return LCN_E_INVALID_ARGUMENT;
+    if (n) *n = pr->n;
+    if (m) *m = pr->m;
+    if (nnz) *nnz = pr->col.size();
+    return LCN_OK;
+}
+
+int lcn_pairs_copy(const lcn_pairs* pr, uint32_t* row_ptr, uint32_t* col) {
+    if (!pr) return LCN_E_INVALID_ARGUMENT;
+    if (row_ptr) std::memcpy(row_ptr, pr->row_ptr.data(), pr->row_ptr.size() * 4);
+    if (col && !pr->col.empty()) std::memcpy(col, pr->col.data(), pr->col.size() * 4);
+    return LCN_OK;
+}
+
+int lcn_pairs_destroy(lcn_pairs* pr) {
+    delete pr;
+    return LCN_OK;
+}
+
+int lcn_build_sparse(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m, size_t d,
+                     const uint32_t* row_ptr, const uint32_t* col, size_t nnz, int cost, double lambda,
+                     double* logvals) {
+    return guard(ctx, [&] {
+        if (!(lambda > 0.0)) throw Status(2, "build_sparse: lambda must be positive");
+        if (cost < 0 || cost > 3) throw Status(2, "unknown cost kind");
+        if (!row_ptr || (nnz && (!col || !logvals))) throw Status(2, "null pattern");
+        check_points(p, n, d, "p");
+        check_points(q, m, d, "q");
+        if (row_ptr[n] != nnz) throw Status(1, "build_sparse: pattern shape mismatch");
+        std::unique_ptr<lcn_op> h(new_op(ctx, cost, lambda));
+        upload_union(h->o, p, n, q, m, d);
+        cudaStream_t s = ctx->c.stream;
+        for (size_t e = 0; e < nnz; ++e)
+            if (col[e] >= m) throw Status(2, "neighbor pair index out of range");
+        DevBuf<uint32_t> rp, cl(std::max<size_t>(nnz, 1));
+        DevBuf<double> out(std::max<size_t>(nnz, 1));
+        rp.upload(row_ptr, n + 1, s);
+        if (nnz) CUDA_OK(cudaMemcpyAsync(cl.get(), col, nnz * 4, cudaMemcpyHostToDevice, s));
+        build_sparse_pairs(h->o, rp.get(), cl.get(), nnz, out.get());
+        out.download(logvals, nnz, s);
+        ctx->c.sync();
+    });
+}
+
+int lcn_select_landmarks(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m, size_t d, size_t l,
+                         int method, uint64_t seed, double* out) {
+    return guard(ctx, [&] {
+        if (!out) throw Status(2, "null output");
+        check_points(p, n, d, "p");
+        check_points(q, m, d, "q");
+        if (l < 1 || l > n + m) throw Status(2, "select_landmarks: l out of range");
+        std::unique_ptr<lcn_op> h(new_op(ctx, 0, 1.0));
+        upload_union(h->o, p, n, q, m, d);
+        h->o.l = l;
+        select_landmarks_device(h->o, ctx->c, method, seed);
+        h->o.L.download(out, l * d, ctx->c.stream);
+        ctx->c.sync();
+    });
+}
+
+int lcn_build_factors(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_t m, size_t d,
+                      const double* landmarks, size_t l, int cost, double lambda, double* U, double* W, double* cond) {
+    return guard(ctx, [&] {
+        check_cost_lambda(cost, lambda, "build_factors");
+        if (!landmarks || !U || !W) throw Status(2, "null argument");
+        check_points(p, n, d, "p");
+        check_points(q, m, d, "q");
+        std::unique_ptr<lcn_op> h(new_op(ctx, cost, lambda));
+        h->o.fp64 = true;  // exact fp64 blocks (the reference's values, not the 3xTF32 iteration build)
+        upload_union(h->o, p, n, q, m, d);
+        h->o.l = l;
+        build_nystrom(h->o, landmarks, 0, 0);
+        h->o.U64.download(U, n * l, ctx->c.stream);
+        std::vector<double> wt(m * l);
+        h->o.Wt64.download(wt.data(), m * l, ctx->c.stream);
+        ctx->c.sync();
+        for (size_t a = 0; a < l; ++a)
+            for (size_t j = 0; j < m; ++j) W[a * m + j] = wt[j * l + a];
+        if (cond) *cond = h->o.cond;
+    });
+}
+
+int lcn_build_correction(lcn_ctx* ctx, size_t n, size_t m, size_t l, const uint32_t* row_ptr, const uint32_t* col,
+                         size_t nnz, const double* log_sp, const double* U, const double* W, double* delta,
+                         double* nys_vals, double* max_abs_delta) {
+    return guard(ctx, [&] {
+        if (!row_ptr || !U || !W || (nnz && (!col || !log_sp || !delta))) throw Status(2, "null argument");
+        if (row_ptr[n] != nnz) throw Status(1, "build_correction: shape mismatch");
+        for (size_t e = 0; e < nnz; ++e)
+            if (col[e] >= m) throw Status(1, "build_correction: shape mismatch");
+        cudaStream_t s = ctx->c.stream;
+        std::vector<double> wt(m * l);
+        for (size_t a = 0; a < l; ++a)
+            for (size_t j = 0; j < m; ++j) wt[j * l + a] = W[a * m + j];
+        DevBuf<uint32_t> rp, cl(std::max<size_t>(nnz, 1));
+        DevBuf<double> ls(std::max<size_t>(nnz, 1)), du, dw, dd(std::max<size_t>(nnz, 1)), dn(std::max<size_t>(nnz, 1));
+        rp.upload(row_ptr, n + 1, s);
+        du.upload(U, std::max<size_t>(n * l, 1), s);
+        dw.upload(wt.data(), std::max<size_t>(m * l, 1), s);
+        if (nnz) {
+            CUDA_OK(cudaMemcpyAsync(cl.get(), col, nnz * 4, cudaMemcpyHostToDevice, s));
+            CUDA_OK(cudaMemcpyAsync(ls.get(), log_sp, nnz * 8, cudaMemcpyHostToDevice, s));
+        }
+        double mx = 0.0;
+        correction_pairs(ctx->c, n, l, rp.get(), cl.get(), nnz, ls.get(), du.get(), dw.get(), dd.get(), dn.get(), &mx);
+        if (nnz) {
+            dd.download(delta, nnz, s);
+            if (nys_vals) dn.download(nys_vals, nnz, s);
+        }
+        ctx->c.sync();
+        if (max_abs_delta) *max_abs_delta = mx;
+    });
+}
+
+int lcn_op_from_dense(lcn_ctx* ctx, size_t n, size_t m, const double* logk, double lambda, lcn_op** out) {
+    return guard(ctx, [&] {
+        if (!(lambda > 0.0)) throw Status(2, "dense operator: lambda must be positive");
+        if (!logk || !out) throw Status(2, "null argument");
+        std::unique_ptr<lcn_op> h(new_op(ctx, 0, lambda));
+        Op& o = h->o;
+        o.kind = LCN_OP_DENSE;
+        o.n = n;
+        o.m = m;
+        o.dk64.upload(logk, std::max<size_t>(n * m, 1), ctx->c.stream);
+        dense_storage(o);
+        *out = h.release();
+    });
+}
+
+int lcn_op_from_sparse(lcn_ctx* ctx, size_t n, size_t m, const uint32_t* row_ptr, const uint32_t* col, size_t nnz,
+                       const double* logvals, double lambda, lcn_op** out) {
+    return guard(ctx, [&] {
+        if (!(lambda > 0.0)) throw Status(2, "sparse operator: lambda must be positive");
+        if (!row_ptr || !out || (nnz && (!col || !logvals))) throw Status(2, "null argument");
+        std::unique_ptr<lcn_op> h(new_op(ctx, 0, lambda));
+        Op& o = h->o;
+        o.kind = LCN_OP_SPARSE;
+        o.n = n;
+        o.m = m;
+        set_general_csr(o, row_ptr, col, nnz, logvals, nullptr);
+        *out = h.release();
+    });
+}
+
+// NystromFactors (nystrom.hpp:33-44) onto the device: U, W^T and their
+// iteration copies.
+void factors_from_host(Op& o, size_t l, const double* U, const double* W) {
+    cudaStream_t s = o.ctx->stream;
+    o.l = l;
+    std::vector<double> wt(o.m * l);
+    for (size_t a = 0; a < l; ++a)
+        for (size_t j = 0; j < o.m; ++j) wt[j * l + a] = W[a * o.m + j];
+    o.U64.upload(U, std::max<size_t>(o.n * l, 1), s);
+    o.Wt64.upload(wt.data(), std::max<size_t>(o.m * l, 1), s);
+    o.ctx->sync();
+}
+
+int lcn_op_from_nystrom(lcn_ctx* ctx, size_t n, size_t m, size_t l, const double* U, const double* W, double lambda,
+                        lcn_op** out) {
+    return guard(ctx, [&] {
+        if (!U || !W || !out) throw Status(2, "null argument");
+        if (l < 1 || l > 4096) throw Status(2, "nystrom operator: landmark count out of range");
+        std::unique_ptr<lcn_op> h(new_op(ctx, 0, lambda));
+        Op& o = h->o;
+        o.kind = LCN_OP_NYSTROM;
+        o.n = n;
+        o.m = m;
+        factors_from_host(o, l, U, W);
+        finalize_storage(o);
+        *out = h.release();
+    });
+}
+
+int lcn_op_from_lcn(lcn_ctx* ctx, size_t n, size_t m, size_t l, const double* U, const double* W, double lambda,
+                    const uint32_t* row_ptr, const uint32_t* col, size_t nnz, const double* delta,
+                    const double* log_sp, double max_abs_delta, lcn_op** out) {
+    return guard(ctx, [&] {
+        if (!U || !W || !out || !row_ptr || (nnz && (!col || !delta || !log_sp))) throw Status(2, "null argument");
+        if (l < 1 || l > 4096) throw Status(2, "lcn operator: landmark count out of range");
+        std::unique_ptr<lcn_op> h(new_op(ctx, 0, lambda));
+        Op& o = h->o;
+        o.kind = LCN_OP_LCN;
+        o.n = n;
+        o.m = m;
+        factors_from_host(o, l, U, W);
+        set_general_csr(o, row_ptr, col, nnz, delta, log_sp);
+        o.max_abs_delta = max_abs_delta;
+        finalize_storage(o);
         *out = h.release();
     });
 }

@@ -125,6 +125,13 @@ struct Op {
     // CSR export (lazy)
     DevBuf<uint32_t> csr_row_ptr, csr_col;
     bool csr_ready = false;
+    // general pattern (KernelOperator::sparse / ::lcn from host structs,
+    // operator.hpp:33-36): the support is any CSR, not bucket blocks. Values
+    // fp64 in CSR order (log K for sparse, delta for lcn) and CSC order for
+    // the column pass; log K^sp of an lcn operator in CSR order.
+    bool gcsr = false;
+    DevBuf<double> gval, gvalT, glogsp;
+    DevBuf<uint32_t> gcp, gri;  // CSC col_ptr (m + 1), row index (nnz)
     std::shared_ptr<Solver> ws;           // persistent iteration workspace (sinkhorn.cu)
     // BP extension (KernelOperator::with_bp, operator.cpp:103-115): log of the
     // deletion kernels c_{p,eps} (n) and c_{eps,q} (m); set in place
@@ -179,6 +186,7 @@ void select_landmarks_device(Op& op, Ctx& ctx, int method, uint64_t seed);
 void build_sparse_values(Op& op);
 void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed);
 void build_dense(Op& op);
+void dense_storage(Op& op);
 void build_dense_cost(Op& op);
 void dense_logk_from_cost(Op& op, double lambda);
 void build_correction(Op& op);
@@ -186,6 +194,13 @@ void finalize_storage(Op& op);
 void build_csr(Op& op);
 void export_csr(Op& op, int which, uint32_t* row_ptr, uint32_t* col, double* vals);
 void csr_values_device(Op& op, int which, double* d_vals);
+// staged build from host structs (the reference's stage API)
+void set_general_csr(Op& op, const uint32_t* h_rp, const uint32_t* h_col, size_t nnz, const double* h_val,
+                     const double* h_logsp);
+void build_sparse_pairs(Op& op, const uint32_t* d_rp, const uint32_t* d_col, size_t nnz, double* d_out);
+void correction_pairs(Ctx& ctx, size_t n, size_t l, const uint32_t* d_rp, const uint32_t* d_col, size_t nnz,
+                      const double* d_logsp, const double* d_U, const double* d_Wt, double* d_delta, double* d_nys,
+                      double* max_abs);
 
 // Phase timing to stderr when LCN_TIMING is set (host clock around synced phases).
 struct PhaseTimer {

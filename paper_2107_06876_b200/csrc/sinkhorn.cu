@@ -170,6 +170,49 @@ __global__ void __launch_bounds__(kThreads) sparse_col_band_kernel(const DevStat
     }
 }
 
+// ---- general CSR patterns (KernelOperator::sparse / ::lcn from host structs) ----
+// Row (or, on the CSC view, column) log-sum-exp of a sparse kernel
+// (sparse_log_matvec, sparse_kernel.cpp:119-155): (max, sum exp(. - max)) per
+// row, the pair the band kernels produce. One warp per row.
+__global__ void csr_lse_kernel(const DevState* __restrict__ st, const uint32_t* __restrict__ ptr,
+                               const uint32_t* __restrict__ idx, const double* __restrict__ val,
+                               const double* __restrict__ lv, long long rows, double* __restrict__ M,
+                               double* __restrict__ S) {
+    if (st->done) return;
+    const long long r = (blockIdx.x * 256LL + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= rows) return;
+    const uint32_t b = ptr[r], e = ptr[r + 1];
+    double hi = kNegInf;
+    for (uint32_t k = b + lane; k < e; k += 32) hi = fmax(hi, val[k] + lv[idx[k]]);
+    hi = warp_max(hi);
+    double acc = 0.0;
+    if (hi != kNegInf)
+        for (uint32_t k = b + lane; k < e; k += 32) acc += exp(val[k] + lv[idx[k]] - hi);
+    acc = warp_sum(acc);
+    if (lane == 0) {
+        M[r] = hi;
+        S[r] = hi == kNegInf ? 0.0 : acc;
+    }
+}
+
+// Linear-space correction product (correction_matvec(_t), sparse_kernel.cpp:
+// 157-185) in the band kernels' convention: out[r] = sum delta * exp(lv - H).
+__global__ void csr_corr_kernel(const DevState* __restrict__ st, const uint32_t* __restrict__ ptr,
+                                const uint32_t* __restrict__ idx, const double* __restrict__ val,
+                                const double* __restrict__ lv, long long rows, int rows_pass,
+                                double* __restrict__ out) {
+    if (st->done) return;
+    const long long r = (blockIdx.x * 256LL + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= rows) return;
+    const double H = rows_pass ? st->H_t : st->H_s;
+    double acc = 0.0;
+    for (uint32_t k = ptr[r] + lane; k < ptr[r + 1]; k += 32) acc += val[k] * exp(lv[idx[k]] - H);
+    acc = warp_sum(acc);
+    if (lane == 0) out[r] = acc;
+}
+
 __global__ void lse_init_kernel(const DevState* __restrict__ st, double* __restrict__ M, double* __restrict__ S, long long n) {
     if (st->done) return;
     long long i = blockIdx.x * 256LL + threadIdx.x;
@@ -1974,9 +2017,9 @@ struct Solver {
         if (op.kind <= 1) {
             Mr.resize(n); Sr.resize(n); Mc.resize(m); Sc.resize(m);
         } else {
-            corr_s.resize(op.bands.size());
-            corr_t.resize(op.bands.size());
-            for (size_t b = 0; b < op.bands.size(); ++b) {
+            corr_s.resize(ncorr());
+            corr_t.resize(ncorr());
+            for (size_t b = 0; b < ncorr(); ++b) {
                 if (corr_s[b].size() != static_cast<size_t>(np)) {
                     corr_s[b].resize(np);
                     corr_s[b].zero(s);  // rows outside any work bucket stay 0
@@ -2056,6 +2099,11 @@ struct Solver {
                                                                         Mr.get(), Sr.get());
             return;
         }
+        if (op.gcsr) {
+            csr_lse_kernel<<<ceil_div(n * 32, 256), 256, 0, s>>>(st.get(), op.csr_row_ptr.get(), op.csr_col.get(),
+                                                                 op.gval.get(), lt, n, Mr.get(), Sr.get());
+            return;
+        }
         lse_init_kernel<<<ceil_div(n, 256), 256, 0, s>>>(st.get(), Mr.get(), Sr.get(), n);
         for (size_t b = 0; b < op.bands.size(); ++b)
             if (op.bands[b].n_work)
@@ -2073,6 +2121,11 @@ struct Solver {
                 }
             dense_lse_kernel<T><<<ceil_div(m, kDenseRows), 256, 0, s>>>(st.get(), dense_logk<T>(true), m, n, ls,
                                                                         Mc.get(), Sc.get());
+            return;
+        }
+        if (op.gcsr) {
+            csr_lse_kernel<<<ceil_div(m * 32, 256), 256, 0, s>>>(st.get(), op.gcp.get(), op.gri.get(), op.gvalT.get(),
+                                                                 ls, m, Mc.get(), Sc.get());
             return;
         }
         lse_init_kernel<<<ceil_div(m, 256), 256, 0, s>>>(st.get(), Mc.get(), Sc.get(), m);
@@ -2119,9 +2172,26 @@ struct Solver {
         }
     }
     template <typename T>
-    void lcn_rows() { bands<T, true>(ltp, corr_s); }
+    void lcn_rows(const double* lt = nullptr) {
+        if (op.kind == 3 && op.gcsr) {  // general pattern: CSR rows over log t
+            csr_corr_kernel<<<ceil_div(n * 32, 256), 256, 0, s>>>(st.get(), op.csr_row_ptr.get(), op.csr_col.get(),
+                                                                  op.gval.get(), lt ? lt : log_t.get(), n, 1,
+                                                                  corr_s[0].get());
+            return;
+        }
+        bands<T, true>(ltp, corr_s);
+    }
     template <typename T>
-    void lcn_cols(int parity) { bands<T, false>(lsp[parity], corr_t); }
+    void lcn_cols(int parity, const double* ls = nullptr) {
+        if (op.kind == 3 && op.gcsr) {  // general pattern: CSC columns over log s
+            csr_corr_kernel<<<ceil_div(m * 32, 256), 256, 0, s>>>(st.get(), op.gcp.get(), op.gri.get(), op.gvalT.get(),
+                                                                  ls ? ls : log_s[parity].get(), m, 0,
+                                                                  corr_t[0].get());
+            return;
+        }
+        bands<T, false>(lsp[parity], corr_t);
+    }
+    size_t ncorr() const { return op.gcsr ? 1 : op.bands.size(); }
     void set_perm(PassArgs& a, int side, int parity) {
         a.nperm = 0;
         if (op.kind != 3) return;
@@ -2140,7 +2210,7 @@ struct Solver {
     void set_corr(PassArgs& a, int side) {
         a.ncorr = 0;
         if (op.kind != 3) return;
-        for (size_t b = 0; b < op.bands.size(); ++b) a.corr[a.ncorr++] = side == 0 ? corr_s[b].get() : corr_t[b].get();
+        for (size_t b = 0; b < ncorr(); ++b) a.corr[a.ncorr++] = side == 0 ? corr_s[b].get() : corr_t[b].get();
     }
 
     template <typename T>
@@ -2467,7 +2537,7 @@ struct Solver {
             pass<T, 1>(acc);
             reduce(mid_t.get(), 0);
             scatter_perm(d_in, m, 1, 0);
-            lcn_rows<T>();
+            lcn_rows<T>(d_in);
             mv.rows = n;
             mv.mid = mid_t.get();
             set_corr(mv, 0);
@@ -2477,7 +2547,7 @@ struct Solver {
             pass<T, 0>(acc);
             reduce(mid_s.get(), 1);
             scatter_perm(d_in, n, 0, 0);
-            lcn_cols<T>(0);
+            lcn_cols<T>(0, d_in);
             mv.rows = m;
             mv.mid = mid_s.get();
             set_corr(mv, 1);
@@ -2644,7 +2714,7 @@ struct Solver {
                 pass<T, 1>(acc);
                 reduce(mid_t.get(), 0);
                 scatter_perm(vin.get(), m, 1, 0);
-                lcn_rows<T>();
+                lcn_rows<T>(vin.get());
                 mv.rows = n;
                 mv.mid = mid_t.get();
                 set_corr(mv, 0);
@@ -2654,7 +2724,7 @@ struct Solver {
                 pass<T, 0>(acc);
                 reduce(mid_s.get(), 1);
                 scatter_perm(vin.get(), n, 0, 0);
-                lcn_cols<T>(0);
+                lcn_cols<T>(0, vin.get());
                 mv.rows = m;
                 mv.mid = mid_s.get();
                 set_corr(mv, 1);

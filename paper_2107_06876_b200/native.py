@@ -54,7 +54,7 @@ _STATUS = {1: DimensionError, 2: InvalidArgument, 3: StabilizationError, 4: Nega
 EUCLIDEAN, NEGATIVE_DOT, COSINE_DERIVED, SQEUCLIDEAN = 0, 1, 2, 3
 LANDMARK_KMEANS, LANDMARK_KMEANSPP = 0, 1
 LSH_CROSS_POLYTOPE, LSH_KMEANS, LSH_HIERARCHICAL_KMEANS = 0, 1, 2  # LshScheme (lsh.hpp:13-17)
-ABI_VERSION = 4  # include/lcn_b200.h LCN_B200_ABI_VERSION
+ABI_VERSION = 5  # include/lcn_b200.h LCN_B200_ABI_VERSION
 KIND_DENSE, KIND_SPARSE, KIND_NYSTROM, KIND_LCN = 0, 1, 2, 3
 _KIND_NAMES = {0: "dense", 1: "sparse", 2: "nystrom", 3: "lcn"}
 
@@ -165,6 +165,18 @@ def library() -> C.CDLL:
             "lcn_shard_plan_rank_exchange": ([P, I, P, P, P, P, P, P], I),
             "lcn_shard_plan_last_error": ([], C.c_char_p),
             "lcn_shard_plan_destroy": ([P], I),
+            "lcn_lsh_neighbor_pairs": ([P, P, SZ, P, SZ, SZ, C.POINTER(_LshConfig), PP], I),
+            "lcn_pairs_info": ([P, C.POINTER(SZ), C.POINTER(SZ), C.POINTER(SZ)], I),
+            "lcn_pairs_copy": ([P, P, P], I),
+            "lcn_pairs_destroy": ([P], I),
+            "lcn_build_sparse": ([P, P, SZ, P, SZ, SZ, P, P, SZ, I, D, P], I),
+            "lcn_select_landmarks": ([P, P, SZ, P, SZ, SZ, SZ, I, U64, P], I),
+            "lcn_build_factors": ([P, P, SZ, P, SZ, SZ, P, SZ, I, D, P, P, C.POINTER(D)], I),
+            "lcn_build_correction": ([P, SZ, SZ, SZ, P, P, SZ, P, P, P, P, P, C.POINTER(D)], I),
+            "lcn_op_from_dense": ([P, SZ, SZ, P, D, PP], I),
+            "lcn_op_from_sparse": ([P, SZ, SZ, P, P, SZ, P, D, PP], I),
+            "lcn_op_from_nystrom": ([P, SZ, SZ, SZ, P, P, D, PP], I),
+            "lcn_op_from_lcn": ([P, SZ, SZ, SZ, P, P, D, P, P, SZ, P, P, D, PP], I),
             "lcn_op_set_bp": ([P, P, P], I),
         }
         for name, (args, res) in sig.items():
@@ -327,6 +339,71 @@ class ShardPlan:
                 self.h = None
         except Exception:
             pass
+
+
+# ---- staged build from host structs (runner.cpp:258-271) ---------------------
+def _csr(row_ptr, col):
+    return np.ascontiguousarray(row_ptr, np.uint32), np.ascontiguousarray(col, np.uint32)
+
+
+def lsh_neighbor_pairs(ctx: "Context", p, q, cfg: "LshConfig"):
+    """lsh_neighbor_pairs (lsh.cpp:245-283) -> (row_ptr, col) CSR."""
+    p, q = _f64(p), _f64(q)
+    h = C.c_void_p()
+    c = cfg.c()
+    ctx.check(ctx.lib.lcn_lsh_neighbor_pairs(ctx.h, _p(p), p.shape[0], _p(q), q.shape[0], p.shape[1], C.byref(c),
+                                             C.byref(h)))
+    try:
+        nnz = C.c_size_t()
+        ctx.lib.lcn_pairs_info(h, None, None, C.byref(nnz))
+        rp = np.zeros(p.shape[0] + 1, np.uint32)
+        col = np.zeros(nnz.value, np.uint32)
+        ctx.lib.lcn_pairs_copy(h, _p(rp), _p(col))
+    finally:
+        ctx.lib.lcn_pairs_destroy(h)
+    return rp, col
+
+
+def build_sparse(ctx: "Context", p, q, row_ptr, col, cost, lam):
+    """build_sparse (sparse_kernel.cpp:51-80): log K at the pattern."""
+    p, q = _f64(p), _f64(q)
+    rp, col = _csr(row_ptr, col)
+    out = np.zeros(len(col))
+    ctx.check(ctx.lib.lcn_build_sparse(ctx.h, _p(p), p.shape[0], _p(q), q.shape[0], p.shape[1], _p(rp), _p(col),
+                                       len(col), cost, lam, _p(out)))
+    return out
+
+
+def select_landmarks(ctx: "Context", p, q, l: int, method=0, seed=0):
+    p, q = _f64(p), _f64(q)
+    out = np.zeros((l, p.shape[1]))
+    ctx.check(ctx.lib.lcn_select_landmarks(ctx.h, _p(p), p.shape[0], _p(q), q.shape[0], p.shape[1], l, method, seed,
+                                           _p(out)))
+    return out
+
+
+def build_factors(ctx: "Context", p, q, landmarks, cost, lam):
+    """build_factors (nystrom.cpp:68-125) -> (U n x l, W l x m, cond)."""
+    p, q, L = _f64(p), _f64(q), _f64(landmarks)
+    l = L.shape[0]
+    U = np.zeros((p.shape[0], l))
+    W = np.zeros((l, q.shape[0]))
+    cond = C.c_double()
+    ctx.check(ctx.lib.lcn_build_factors(ctx.h, _p(p), p.shape[0], _p(q), q.shape[0], p.shape[1], _p(L), l, cost, lam,
+                                        _p(U), _p(W), C.byref(cond)))
+    return U, W, cond.value
+
+
+def build_correction(ctx: "Context", row_ptr, col, log_sp, U, W):
+    """build_correction (sparse_kernel.cpp:82-117) -> (delta, nys_vals, max |delta|)."""
+    rp, col = _csr(row_ptr, col)
+    U, W, ls = _f64(U), _f64(W), _f64(log_sp)
+    delta = np.zeros(len(col))
+    nys = np.zeros(len(col))
+    mx = C.c_double()
+    ctx.check(ctx.lib.lcn_build_correction(ctx.h, U.shape[0], W.shape[1], U.shape[1], _p(rp), _p(col), len(col),
+                                           _p(ls), _p(U), _p(W), _p(delta), _p(nys), C.byref(mx)))
+    return delta, nys, mx.value
 
 
 @dataclasses.dataclass
@@ -588,6 +665,43 @@ class KernelOperator:
         ctx.check(ctx.lib.lcn_op_lcn_buckets(ctx.h, _p(p), p.shape[0], _p(q), q.shape[0], p.shape[1], cost, lam,
                                              _p(ip), _p(iq), bands, range_, _p(lm), l, method, landmark_seed,
                                              C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def from_dense_logk(cls, ctx, logk, lam):
+        """KernelOperator::dense(DenseKernel) from a host n x m log K."""
+        lk = _f64(logk)
+        h = C.c_void_p()
+        ctx.check(ctx.lib.lcn_op_from_dense(ctx.h, lk.shape[0], lk.shape[1], _p(lk), lam, C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def from_sparse(cls, ctx, n, m, row_ptr, col, logvals, lam):
+        """KernelOperator::sparse(SparseKernel, lambda), any CSR pattern."""
+        rp, col = _csr(row_ptr, col)
+        lv = _f64(logvals)
+        h = C.c_void_p()
+        ctx.check(ctx.lib.lcn_op_from_sparse(ctx.h, n, m, _p(rp), _p(col), len(col), _p(lv), lam, C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def from_nystrom(cls, ctx, U, W, lam):
+        """KernelOperator::nystrom(NystromFactors)."""
+        U, W = _f64(U), _f64(W)
+        h = C.c_void_p()
+        ctx.check(ctx.lib.lcn_op_from_nystrom(ctx.h, U.shape[0], W.shape[1], U.shape[1], _p(U), _p(W), lam,
+                                              C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def from_lcn(cls, ctx, U, W, lam, row_ptr, col, delta, log_sp, max_abs_delta=0.0):
+        """KernelOperator::lcn(NystromFactors, LcnCorrection), any CSR pattern."""
+        U, W = _f64(U), _f64(W)
+        rp, col = _csr(row_ptr, col)
+        dl, ls = _f64(delta), _f64(log_sp)
+        h = C.c_void_p()
+        ctx.check(ctx.lib.lcn_op_from_lcn(ctx.h, U.shape[0], W.shape[1], U.shape[1], _p(U), _p(W), lam, _p(rp), _p(col),
+                                          len(col), _p(dl), _p(ls), max_abs_delta, C.byref(h)))
         return cls(ctx, h)
 
     @classmethod

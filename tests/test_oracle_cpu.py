@@ -362,7 +362,7 @@ def test_capi_library_exports_header_symbols():
     assert len(names) >= 25
     missing = [nm for nm in names if not hasattr(lib, nm)]
     assert not missing, missing
-    assert lib.lcn_abi_version() == 4
+    assert lib.lcn_abi_version() == 5
 
 
 def test_capi_without_gpu_fails_loudly():
