@@ -1,7 +1,7 @@
 // Drop-in shim: the reference's lcn:: hot-path functions implemented over the
 // B200 C-ABI (include/lcn_b200.h). Compiled against the reference's own
 // headers; linked in place of the reference's definitions of the same
-// functions (integration/Makefile renames those at compile time), every
+// functions (integration/Makefile weakens those definitions), every
 // caller of the reference's API -- runner.cpp's run_one, the reference's unit
 // tests -- runs its staged build and its Sinkhorn solves on the GPU with no
 // source change:
