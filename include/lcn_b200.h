@@ -61,7 +61,12 @@ enum lcn_op_kind { LCN_OP_DENSE = 0, LCN_OP_SPARSE = 1, LCN_OP_NYSTROM = 2, LCN_
  * stored kernel value in fp64 (API-compatibility mode, passes the reference
  * unit tests' 1e-12 tolerances); FP32 stores them in fp32 with fp64
  * accumulation (performance mode, 1e-4 parity). */
-enum lcn_ctx_flags { LCN_STORE_FP32 = 0, LCN_STORE_FP64 = 1, LCN_EXACT_BUILD = 2 };
+enum lcn_ctx_flags { LCN_STORE_FP32 = 0, LCN_STORE_FP64 = 1, LCN_EXACT_BUILD = 2, LCN_DENSE_RECOMPUTE = 4 };
+/* LCN_DENSE_RECOMPUTE (fp32 storage, configs[2]'s wording): lcn_op_dense /
+ * lcn_op_dense_device keep no n x m log K; every half-iteration recomputes
+ * the kernel as a tcgen05 3xTF32 GEMM of the points (x.y, fp64 norms) fused
+ * with the row / column log-sum-exp (dense_tc.cu). The plan and
+ * export_dense rebuild the exact log K on demand. Not for the cosine cost. */
 /* Build contractions. FP32 storage computes the within-bucket distance
  * blocks of K^sp, the point x landmark blocks U and V, and the delta SDDMM
  * U_b W_b on the tcgen05 tensor cores in the FP32-accurate 3xTF32 split

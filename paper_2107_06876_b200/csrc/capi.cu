@@ -413,6 +413,7 @@ int lcn_ctx_create(int device, int flags, lcn_ctx** out) {
         c->c.device = device;
         c->c.store_fp64 = (flags & LCN_STORE_FP64) ? 1 : 0;
         c->c.exact_build = (flags & LCN_EXACT_BUILD) || std::getenv("LCN_EXACT_BUILD") ? 1 : 0;
+        c->c.dense_recompute = (flags & LCN_DENSE_RECOMPUTE) ? 1 : 0;
         c->c.num_sms = prop.multiProcessorCount;
         CUDA_OK(cudaSetDevice(device));
         // keep freed pool memory resident (stream-ordered DevBuf temporaries)
@@ -946,7 +947,8 @@ int lcn_op_dense(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_
         std::unique_ptr<lcn_op> h(new_op(ctx, cost, lambda));
         upload_union(h->o, p, n, q, m, d);
         h->o.kind = LCN_OP_DENSE;
-        build_dense(h->o);
+        if (ctx->c.dense_recompute && !h->o.fp64) dense_tc_prepare(h->o);
+        else build_dense(h->o);
         *out = h.release();
     });
 }
@@ -968,7 +970,8 @@ int lcn_op_dense_device(lcn_ctx* ctx, const float* d_p, size_t n, const float* d
             d_q, op.X.get() + n * d, m * d);
         LAUNCH_OK("promote");
         op.kind = LCN_OP_DENSE;
-        build_dense(op);
+        if (ctx->c.dense_recompute && !op.fp64) dense_tc_prepare(op);
+        else build_dense(op);
         *out = h.release();
     });
 }
@@ -1027,6 +1030,16 @@ int lcn_op_export_dense(lcn_op* op, double* out) {
     return guard(ctx, [&] {
         if (!op || !out) throw Status(2, "null operator or buffer");
         if (op->o.kind != LCN_OP_DENSE) throw Status(2, "export_dense: not a dense operator");
+        if (op->o.dense_tc) {  // recomputed operator: the exact log K on demand
+            build_dense(op->o);
+            op->o.dk64.download(out, op->o.n * op->o.m, op->o.ctx->stream);
+            op->o.ctx->sync();
+            op->o.dk64 = DevBuf<double>();
+            op->o.dk32 = DevBuf<float>();
+            op->o.dk32T = DevBuf<float>();
+            op->o.dk64T = DevBuf<double>();
+            return;
+        }
         op->o.dk64.download(out, op->o.n * op->o.m, op->o.ctx->stream);
         op->o.ctx->sync();
     });

@@ -75,6 +75,7 @@ struct Ctx {
     int device = 0;
     int store_fp64 = 0;
     int exact_build = 0;  // LCN_EXACT_BUILD: fp64 CUDA-core build tiles even in fp32 storage
+    int dense_recompute = 0;  // LCN_DENSE_RECOMPUTE: dense operators recompute exp(-C/lambda) per iteration
     int num_sms = 148;
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr;

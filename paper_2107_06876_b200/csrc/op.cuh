@@ -114,6 +114,13 @@ struct Op {
     DevBuf<double> dk64, dk64T;
     DevBuf<float> dk32, dk32T;
     DevBuf<double> dc64;  // dense cost c (multi-head: log K per lambda from it)
+    // dense kernel recomputed every half-iteration (LCN_DENSE_RECOMPUTE,
+    // dense_tc.cu): packed tf32 hi/lo tiles of the union, |x|^2, per
+    // (row, column tile) partials; no n x m storage
+    bool dense_tc = false;
+    int dtc_nta = 0, dtc_ntb = 0;
+    DevBuf<unsigned char> dtc_tiles;
+    DevBuf<double> dtc_norm, dtc_pm, dtc_ps;
     unsigned long long nnz = 0, stored = 0;
     // Nystrom / LCN
     DevBuf<double> L;                     // l x d landmarks
@@ -187,6 +194,9 @@ void build_sparse_values(Op& op);
 void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed);
 void build_dense(Op& op);
 void dense_storage(Op& op);
+// dense_tc.cu: the dense kernel recomputed per half-iteration on tcgen05
+void dense_tc_prepare(Op& op);
+void dense_tc_lse(Op& op, bool transposed, const double* lv, const int* done, double* M, double* S);
 void build_dense_cost(Op& op);
 void dense_logk_from_cost(Op& op, double lambda);
 void build_correction(Op& op);

@@ -2080,6 +2080,10 @@ struct Solver {
                                                                 mid, which, nullptr);
     }
 
+    const int* done_ptr() const {
+        return reinterpret_cast<const int*>(reinterpret_cast<const char*>(st.get()) + offsetof(DevState, done));
+    }
+
     // -------- sparse -------------------------------------------------------
     template <typename T>
     const T* dense_logk(bool transposed) const {
@@ -2088,6 +2092,10 @@ struct Solver {
     }
     template <typename T>
     void sparse_rows(const double* lt) {
+        if (op.kind == 0 && op.dense_tc) {  // dense, recomputed on the tensor cores
+            dense_tc_lse(op, false, lt, done_ptr(), Mr.get(), Sr.get());
+            return;
+        }
         if (op.kind == 0) {  // dense: the whole row in one (max, sum) pair
             if constexpr (sizeof(T) == 4)
                 if (m % 4 == 0) {
@@ -2112,6 +2120,10 @@ struct Solver {
     }
     template <typename T>
     void sparse_cols(const double* ls) {
+        if (op.kind == 0 && op.dense_tc) {  // dense, recomputed on the tensor cores
+            dense_tc_lse(op, true, ls, done_ptr(), Mc.get(), Sc.get());
+            return;
+        }
         if (op.kind == 0) {  // dense: rows of the transposed copy
             if constexpr (sizeof(T) == 4)
                 if (n % 4 == 0) {
@@ -2895,8 +2907,17 @@ void extract_plan_device(Op& op, Result& r) {
     lt.upload(r.log_t.data(), m, s);
     const int grid = 8 * ctx.num_sms;
     if (op.kind == 0) {
+        const bool tmp = op.dense_tc;  // recomputed operator: the exact log K for the plan only
+        if (tmp) build_dense(op);
         DevBuf<double> out(static_cast<size_t>(n * m));
         dense_plan_kernel<<<grid, 256, 0, s>>>(op.dk64.get(), ls.get(), lt.get(), n, m, out.get());
+        if (tmp) {
+            ctx.sync();
+            op.dk64 = DevBuf<double>();
+            op.dk32 = DevBuf<float>();
+            op.dk32T = DevBuf<float>();
+            op.dk64T = DevBuf<double>();
+        }
         LAUNCH_OK("dense plan");
         r.plan_vals.resize(static_cast<size_t>(n * m));
         out.download(r.plan_vals.data(), r.plan_vals.size(), s);

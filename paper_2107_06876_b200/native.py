@@ -207,10 +207,12 @@ class Context:
     storage; otherwise fp32 storage builds K^sp, U, V and delta on the tensor
     cores (3xTF32)."""
 
-    def __init__(self, device: int = 0, store_fp64: bool = False, exact_build: bool = False):
+    def __init__(self, device: int = 0, store_fp64: bool = False, exact_build: bool = False,
+                 dense_recompute: bool = False):
         self.lib = library()
         h = C.c_void_p()
-        rc = self.lib.lcn_ctx_create(device, (1 if store_fp64 else 0) | (2 if exact_build else 0), C.byref(h))
+        flags = (1 if store_fp64 else 0) | (2 if exact_build else 0) | (4 if dense_recompute else 0)
+        rc = self.lib.lcn_ctx_create(device, flags, C.byref(h))
         if rc != 0:
             raise _STATUS.get(rc, Error)(self.lib.lcn_ctx_last_error(None).decode())
         self.h = h

@@ -328,6 +328,51 @@ def test_dense_anchor(ref, fp64, cost, lam, n, m):
     assert np.allclose(res.marginal_err, rres.marginal_err, rtol=1e-3, atol=1e-12 if fp64 else 2e-6)
 
 
+@pytest.mark.parametrize("cost,lam,n,m,d", [(lcn.EUCLIDEAN, 0.05, 310, 260, 12),
+                                             (lcn.EUCLIDEAN, 0.2, 1000, 777, 40),
+                                             (lcn.NEGATIVE_DOT, 0.2, 300, 500, 300),
+                                             (lcn.EUCLIDEAN, 0.05, 5000, 5000, 300)])
+def test_dense_recompute(ref, cost, lam, n, m, d):
+    """configs[2]'s dense operator with exp(-C/lambda) recomputed every
+    half-iteration as a tcgen05 3xTF32 GEMM fused with the log-sum-exp
+    (LCN_DENSE_RECOMPUTE, dense_tc.cu; no n x m storage) against the
+    reference's dense solve: distance and the dense plan."""
+    r = np.random.default_rng(7)
+    p = r.standard_normal((n, d)).astype(np.float32).astype(np.float64)
+    q = (r.standard_normal((m, d)) * 0.8 + 0.1).astype(np.float32).astype(np.float64)
+    p /= np.linalg.norm(p, axis=1, keepdims=True)
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    c = lcn.Context(0, dense_recompute=True)
+    op = lcn.KernelOperator.dense(c, p, q, cost, lam)
+    rop = ref.op_dense(p, q, cost, lam)
+    pm, qm = np.full(n, 1 / n), np.full(m, 1 / m)
+    res = lcn.sinkhorn(op, pm, qm, lcn.SinkhornOptions(tol=0.0, max_iters=50))
+    rres = rop.sinkhorn(pm, qm, tol=0.0, max_iters=50)
+    assert res.iters == rres.iters == 50
+    assert rel(res.distance, rres.distance) <= REL_FP32
+    if n * m <= 1e6:
+        assert rel(res.sparse_vals, rres.dense_plan) <= 1e-3
+        assert np.array_equal(op.export_dense().view(np.uint64), rop.dense_logk().view(np.uint64))
+
+
+def test_dense_config2_full(ref):
+    """configs[2] at full size (configs[1]'s points: n = m = 20000, d = 300,
+    L2, lambda = 0.05, 50 iterations): the stored fp32 operator and the
+    tcgen05 recompute against the reference's dense solve."""
+    pr = configs.config1(1.0)
+    pm, qm = pr.marginals()
+    opts = lcn.SinkhornOptions(tol=0.0, max_iters=pr.iters, want_plan=False, check_support=False)
+    rop = ref.op_dense(pr.p, pr.q, pr.cost, pr.lam_eff)
+    want = rop.sinkhorn(pm, qm, tol=0.0, max_iters=pr.iters, check_support=False, want_plan=False).distance
+    del rop
+    for recompute in (False, True):
+        c = lcn.Context(0, dense_recompute=recompute)
+        op = lcn.KernelOperator.dense(c, pr.p, pr.q, pr.cost, pr.lam_eff)
+        got = lcn.sinkhorn(op, pm, qm, opts).distance
+        assert rel(got, want) <= REL_FP32, (recompute, got, want)
+        del op
+
+
 @pytest.mark.parametrize("fp64", [False, True])
 def test_multihead(ref, fp64):
     """multihead_lambdas + multihead (H20): lambda schedule, per-head distance,
