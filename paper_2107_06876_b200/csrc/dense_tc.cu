@@ -23,16 +23,19 @@ namespace {
 
 using namespace tcb;
 
-__device__ __forceinline__ double dense_cost(int kind, float dot, double nx, double ny) {
-    const double dd = static_cast<double>(dot);
-    if (kind == 1) return -dd;
+// The cost from the FP32-accurate dot and the fp64 norms (cost_value,
+// geometry.cpp:45-76), in fp32: the dot already carries ~1e-7 relative error,
+// and fp32 keeps the epilogue off the fp64 pipe (sqrt in fp64 is a
+// multi-instruction sequence per entry).
+__device__ __forceinline__ float dense_cost(int kind, float dot, float nx, float ny) {
+    if (kind == 1) return -dot;
     if (kind == 2) {
-        double c = dd / sqrt(nx * ny);
-        c = c > 1.0 ? 1.0 : (c < -1.0 ? -1.0 : c);
-        return sqrt(1.0 - c);
+        float c = dot * rsqrtf(nx * ny);
+        c = fminf(fmaxf(c, -1.0f), 1.0f);
+        return sqrtf(1.0f - c);
     }
-    const double sq = fmax(nx + ny - 2.0 * dd, 0.0);
-    return kind == 0 ? sqrt(sq) : sq;
+    const float sq = fmaxf(nx + ny - 2.0f * dot, 0.0f);
+    return kind == 0 ? sqrtf(sq) : sq;
 }
 
 // items: it -> (row tile it / ntb, column tile it % ntb)
@@ -131,13 +134,15 @@ __global__ void __launch_bounds__(kThreads, 1) dense_lse_tc_kernel(const unsigne
             const uint32_t buf = j % kAcc;
             const int at = it / ntb, ct = it % ntb;
             // this lane's columns of the tile: lane + 32 k
-            double cl[4], cn[4];
+            double cl[4];
+            float cn[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const long long c = static_cast<long long>(ct) * kM + lane + 32 * k;
                 cl[k] = c < cols ? lv[c] : kNegInf;
-                cn[k] = c < cols ? nb[c] : 0.0;
+                cn[k] = c < cols ? static_cast<float>(nb[c]) : 0.0f;
             }
+            const float finv = static_cast<float>(inv);
             mbar_wait_spin(&tfull[buf], (j / kAcc) & 1);
             fence_after();
             uint32_t v[kEpiCols];
@@ -157,12 +162,12 @@ __global__ void __launch_bounds__(kThreads, 1) dense_lse_tc_kernel(const unsigne
                 const int r = ew * kRows + i;
                 const long long gr = static_cast<long long>(at) * kM + r;
                 if (gr >= rows) break;  // uniform across the warp
-                const double nx = na[gr];
+                const float nx = static_cast<float>(na[gr]);
                 double x[4], mx = kNegInf;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    x[k] = cl[k] == kNegInf ? kNegInf
-                                            : cl[k] - dense_cost(kind, stage[r * kStageLd + lane + 32 * k], nx, cn[k]) * inv;
+                    const float c = dense_cost(kind, stage[r * kStageLd + lane + 32 * k], nx, cn[k]);
+                    x[k] = cl[k] == kNegInf ? kNegInf : cl[k] - static_cast<double>(c * finv);
                     mx = fmax(mx, x[k]);
                 }
                 mx = warp_max(mx);
