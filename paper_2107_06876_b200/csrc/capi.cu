@@ -82,23 +82,33 @@ int guard(lcn_ctx* ctx, F&& f) {
     }
 }
 
-void check_points(const double* x, size_t n, size_t d, const char* id) {
+// PointSet::validate (geometry.cpp): shape on the host; the finiteness scan of
+// the coordinates runs on the device for sets that upload_union takes
+// (check_points_shape + upload_union), on the host otherwise.
+void check_points_shape(const double* x, size_t n, size_t d, const char* id) {
     if (n == 0 || d == 0) throw Status(2, std::string("point set '") + id + "' is empty");
     if (!x) throw Status(2, std::string("point set '") + id + "' is null");
+}
+void check_points(const double* x, size_t n, size_t d, const char* id) {
+    check_points_shape(x, n, d, id);
     for (size_t i = 0; i < n * d; ++i)
         if (!std::isfinite(x[i])) throw Status(2, std::string("point set '") + id + "' has non-finite coordinates");
 }
 
+// fp32 copy of the union, whether the demotion is exact (flag bit 0), and the
+// finiteness of each side's coordinates (bit 1: p, bit 2: q; split = n d)
 __global__ void demote_check_kernel(const double* __restrict__ in, float* __restrict__ out, long long n,
-                                    unsigned* __restrict__ inexact) {
-    bool bad = false;
+                                    long long split, unsigned* __restrict__ inexact) {
+    unsigned bad = 0;
     for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += 256LL * gridDim.x) {
         const double v = in[i];
         const float f = static_cast<float>(v);
         out[i] = f;
-        bad |= static_cast<double>(f) != v;
+        if (static_cast<double>(f) != v) bad |= 1u;
+        if (!isfinite(v)) bad |= i < split ? 2u : 4u;
     }
-    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(inexact, 1u);
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if (bad && (threadIdx.x & 31) == 0) atomicOr(inexact, bad);
 }
 
 void upload_union(Op& op, const double* p, size_t n, const double* q, size_t m, size_t d) {
@@ -115,12 +125,15 @@ void upload_union(Op& op, const double* p, size_t n, const double* q, size_t m, 
     DevBuf<unsigned> inexact(1);
     inexact.zero(op.ctx->stream);
     demote_check_kernel<<<static_cast<int>(std::min<long long>(ceil_div(cnt, 256), 8LL * op.ctx->num_sms)), 256, 0,
-                          op.ctx->stream>>>(op.X.get(), op.X32.get(), cnt, inexact.get());
+                          op.ctx->stream>>>(op.X.get(), op.X32.get(), cnt, static_cast<long long>(n * d),
+                                            inexact.get());
     LAUNCH_OK("demote_check");
     unsigned h = 0;
     inexact.download(&h, 1, op.ctx->stream);
     op.ctx->sync();
-    if (h) op.X32 = DevBuf<float>();
+    if (h & 2u) throw Status(2, "point set 'p' has non-finite coordinates");
+    if (h & 4u) throw Status(2, "point set 'q' has non-finite coordinates");
+    if (h & 1u) op.X32 = DevBuf<float>();
 }
 
 __global__ void promote_kernel(const float* __restrict__ in, double* __restrict__ out, long long n) {
@@ -627,8 +640,8 @@ int lcn_lsh_buckets(lcn_ctx* ctx, const double* p, size_t n, const double* q, si
                     const lcn_lsh_config* cfg, uint64_t* ids_out) {
     return guard(ctx, [&] {
         if (!cfg) throw Status(2, "lsh: null config");
-        check_points(p, n, d, "p");
-        check_points(q, m, d, "q");
+        check_points_shape(p, n, d, "p");
+        check_points_shape(q, m, d, "q");
         Op tmp;
         tmp.ctx = &ctx->c;
         upload_union(tmp, p, n, q, m, d);
@@ -648,8 +661,8 @@ int lcn_op_sparse_lsh(lcn_ctx* ctx, const double* p, size_t n, const double* q, 
                       double lambda, const lcn_lsh_config* cfg, lcn_op** out) {
     return guard(ctx, [&] {
         check_cost_lambda(cost, lambda, "build_sparse");
-        check_points(p, n, d, "p");
-        check_points(q, m, d, "q");
+        check_points_shape(p, n, d, "p");
+        check_points_shape(q, m, d, "q");
         std::unique_ptr<lcn_op> h(new_op(ctx, cost, lambda));
         upload_union(h->o, p, n, q, m, d);
         std::vector<DevBuf<uint32_t>> ids;
@@ -667,8 +680,8 @@ int lcn_lsh_neighbor_pairs(lcn_ctx* ctx, const double* p, size_t n, const double
                            const lcn_lsh_config* cfg, lcn_pairs** out) {
     return guard(ctx, [&] {
         if (!out) throw Status(2, "null output");
-        check_points(p, n, d, "p");
-        check_points(q, m, d, "q");
+        check_points_shape(p, n, d, "p");
+        check_points_shape(q, m, d, "q");
         std::unique_ptr<lcn_op> h(new_op(ctx, 0, 1.0));
         upload_union(h->o, p, n, q, m, d);
         std::vector<DevBuf<uint32_t>> ids;
@@ -715,8 +728,8 @@ int lcn_build_sparse(lcn_ctx* ctx, const double* p, size_t n, const double* q, s
         if (!(lambda > 0.0)) throw Status(2, "build_sparse: lambda must be positive");
         if (cost < 0 || cost > 3) throw Status(2, "unknown cost kind");
         if (!row_ptr || (nnz && (!col || !logvals))) throw Status(2, "null pattern");
-        check_points(p, n, d, "p");
-        check_points(q, m, d, "q");
+        check_points_shape(p, n, d, "p");
+        check_points_shape(q, m, d, "q");
         if (row_ptr[n] != nnz) throw Status(1, "build_sparse: pattern shape mismatch");
         std::unique_ptr<lcn_op> h(new_op(ctx, cost, lambda));
         upload_union(h->o, p, n, q, m, d);
@@ -737,8 +750,8 @@ int lcn_select_landmarks(lcn_ctx* ctx, const double* p, size_t n, const double* 
                          int method, uint64_t seed, double* out) {
     return guard(ctx, [&] {
         if (!out) throw Status(2, "null output");
-        check_points(p, n, d, "p");
-        check_points(q, m, d, "q");
+        check_points_shape(p, n, d, "p");
+        check_points_shape(q, m, d, "q");
         if (l < 1 || l > n + m) throw Status(2, "select_landmarks: l out of range");
         std::unique_ptr<lcn_op> h(new_op(ctx, 0, 1.0));
         upload_union(h->o, p, n, q, m, d);
@@ -754,8 +767,8 @@ int lcn_build_factors(lcn_ctx* ctx, const double* p, size_t n, const double* q, 
     return guard(ctx, [&] {
         check_cost_lambda(cost, lambda, "build_factors");
         if (!landmarks || !U || !W) throw Status(2, "null argument");
-        check_points(p, n, d, "p");
-        check_points(q, m, d, "q");
+        check_points_shape(p, n, d, "p");
+        check_points_shape(q, m, d, "q");
         std::unique_ptr<lcn_op> h(new_op(ctx, cost, lambda));
         h->o.fp64 = true;  // exact fp64 blocks (the reference's values, not the 3xTF32 iteration build)
         upload_union(h->o, p, n, q, m, d);
@@ -886,8 +899,8 @@ int lcn_op_sparse_buckets(lcn_ctx* ctx, const double* p, size_t n, const double*
                           lcn_op** out) {
     return guard(ctx, [&] {
         check_cost_lambda(cost, lambda, "build_sparse");
-        check_points(p, n, d, "p");
-        check_points(q, m, d, "q");
+        check_points_shape(p, n, d, "p");
+        check_points_shape(q, m, d, "q");
         std::unique_ptr<lcn_op> h(new_op(ctx, cost, lambda));
         upload_union(h->o, p, n, q, m, d);
         bands_from_host_ids(h->o, ids_p, ids_q, bands, range);
@@ -901,8 +914,8 @@ int lcn_op_lcn_lsh(lcn_ctx* ctx, const double* p, size_t n, const double* q, siz
                    lcn_op** out) {
     return guard(ctx, [&] {
         check_cost_lambda(cost, lambda, "build_factors");
-        check_points(p, n, d, "p");
-        check_points(q, m, d, "q");
+        check_points_shape(p, n, d, "p");
+        check_points_shape(q, m, d, "q");
         std::unique_ptr<lcn_op> h(new_op(ctx, cost, lambda));
         upload_union(h->o, p, n, q, m, d);
         std::vector<DevBuf<uint32_t>> ids;
@@ -927,8 +940,8 @@ int lcn_op_lcn_buckets(lcn_ctx* ctx, const double* p, size_t n, const double* q,
                        const double* landmarks, size_t l, int landmark_method, uint64_t landmark_seed, lcn_op** out) {
     return guard(ctx, [&] {
         check_cost_lambda(cost, lambda, "build_factors");
-        check_points(p, n, d, "p");
-        check_points(q, m, d, "q");
+        check_points_shape(p, n, d, "p");
+        check_points_shape(q, m, d, "q");
         std::unique_ptr<lcn_op> h(new_op(ctx, cost, lambda));
         upload_union(h->o, p, n, q, m, d);
         h->o.l = l;
@@ -942,8 +955,8 @@ int lcn_op_dense(lcn_ctx* ctx, const double* p, size_t n, const double* q, size_
                  double lambda, lcn_op** out) {
     return guard(ctx, [&] {
         check_cost_lambda(cost, lambda, "build_cost");
-        check_points(p, n, d, "p");
-        check_points(q, m, d, "q");
+        check_points_shape(p, n, d, "p");
+        check_points_shape(q, m, d, "q");
         std::unique_ptr<lcn_op> h(new_op(ctx, cost, lambda));
         upload_union(h->o, p, n, q, m, d);
         h->o.kind = LCN_OP_DENSE;
@@ -985,8 +998,8 @@ int lcn_multihead(lcn_ctx* ctx, const double* p, size_t n, const double* q, size
         if (heads < 1) throw Status(2, "multihead: heads must be >= 1");
         if (!(lambda > 0.0)) throw Status(2, "multihead: lambda must be positive");
         check_cost_lambda(cost, lambda, "build_cost");
-        check_points(p, n, d, "p");
-        check_points(q, m, d, "q");
+        check_points_shape(p, n, d, "p");
+        check_points_shape(q, m, d, "q");
         std::unique_ptr<lcn_op> h(new_op(ctx, cost, lambda));
         Op& op = h->o;
         upload_union(op, p, n, q, m, d);
