@@ -27,7 +27,7 @@ independent problems per GPU instead ("weak").
 
 --impl reference times the reference's own CPU implementation (oracle/_ref:
 the reference sources compiled unmodified, Nystrom restated because Eigen is
-absent) on all host threads: configs[3] at scale 0.05 (bucket size, l and d
+absent) on all host threads: configs[3] at scale 0.1 (bucket size, l and d
 kept) built once, then each step = 5 reference Sinkhorn iterations; `value`
 is the configs[3] iteration rate that implies (scaled by the iteration bytes
 B_iter). The full-size reference iteration phase measured by the parity run
@@ -118,7 +118,7 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # CPU reference (oracle/_ref: the reference's own sources, compiled here)
 # ---------------------------------------------------------------------------
-REF_SAMPLE_SCALE = 0.05   # configs[3] at n = m = 5e4: 205 buckets / band (bucket size kept), l = 512
+REF_SAMPLE_SCALE = 0.1    # configs[3] at n = m = 1e5: 410 buckets / band (bucket size kept), l = 512; operator ~2 GB, beyond the host caches
 REF_SAMPLE_ITERS = 5      # reference Sinkhorn iterations per timed step
 FULL = {"n": 1_000_000, "m": 1_000_000, "d": 128, "k": 4096, "bands": 2, "l": 512, "kmeans_iters": 10}
 FULL_NNZ = 521_911_712    # support of configs[3] (bucket ids bit-exact with the reference, profiles/parity_c3_full.json)

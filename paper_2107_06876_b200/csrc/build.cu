@@ -19,6 +19,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+
+#include <cublas_v2.h>
 #include <cmath>
 #include <limits>
 #include <numeric>
@@ -210,6 +212,7 @@ void run_jobs(Ctx& ctx, std::vector<std::function<void(Ctx&)>>& jobs) {
     for (auto& c : ctxs) {
         c.own_stream = nullptr;
         c.comm.reset();
+        c.cublas = nullptr;  // a job that needs one creates its own (released below)
         CUDA_OK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
     }
     std::vector<std::thread> th;
@@ -225,7 +228,10 @@ void run_jobs(Ctx& ctx, std::vector<std::function<void(Ctx&)>>& jobs) {
             }
         });
     for (auto& t : th) t.join();
-    for (auto& c : ctxs) cudaStreamDestroy(c.stream);
+    for (auto& c : ctxs) {
+        if (c.cublas) cublasDestroy(static_cast<cublasHandle_t>(c.cublas));
+        cudaStreamDestroy(c.stream);
+    }
     for (auto& e : errs)
         if (e) std::rethrow_exception(e);
 }
@@ -1521,6 +1527,9 @@ void select_landmarks_device(Op& op, Ctx& ctx, int method, uint64_t seed) {
     ctx.sync();
 }
 
+void wgemm_resid(Ctx& ctx, const double* Vt, const double* Ainv, const double* Aj, size_t m, size_t l, double* Wt,
+                 int* bad, unsigned long long* maxbits);
+
 void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed) {
     Ctx& ctx = *op.ctx;
     cudaStream_t s = ctx.stream;
@@ -1637,13 +1646,11 @@ void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed)
         dAinv.upload(hinv.data(), l * l, s);
         dAj.upload(haj.data(), l * l, s);
         bad.zero(s);
-        // W^T = V^T A^-T  (row j: sum_b Vt[j][b] Ainv[a][b])
-        launch_dense_tiles<1>(ctx, Vt.get(), m, dAinv.get(), l, static_cast<int>(l),
-                              EpiStore{op.Wt64.get(), static_cast<long long>(l), bad.get()});
-        if (read_flag(ctx, bad)) continue;
+        // W^T = V^T A^-T  (row j: sum_b Vt[j][b] Ainv[a][b]) and the residual
+        // max |A_j W - V| (nystrom.cpp:104-124): plain fp64 GEMMs, cuBLAS
         rbits.zero(s);
-        launch_dense_tiles<1>(ctx, op.Wt64.get(), m, dAj.get(), l, static_cast<int>(l),
-                              EpiResid{Vt.get(), static_cast<long long>(l), rbits.get()});
+        wgemm_resid(ctx, Vt.get(), dAinv.get(), dAj.get(), m, l, op.Wt64.get(), bad.get(), rbits.get());
+        if (read_flag(ctx, bad)) continue;
         unsigned long long rb = 0;
         rbits.download(&rb, 1, s);
         ctx.sync();
@@ -1665,6 +1672,63 @@ void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed)
         return;
     }
     throw Status(5, "build_factors: landmark kernel matrix numerically singular beyond jitter budget");
+}
+
+// ---- W = V A^-T and the residual test on cuBLAS (fp64 GEMMs) ---------------
+namespace {
+__global__ void resid_max_kernel(const double* __restrict__ R, const double* __restrict__ Vt, long long cnt,
+                                 unsigned long long* __restrict__ maxbits, int* __restrict__ bad,
+                                 const double* __restrict__ W) {
+    double mx = 0.0;
+    int nf = 0;
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < cnt; i += 256LL * gridDim.x) {
+        double e = fabs(R[i] - Vt[i]);
+        if (!(e <= 1.79e308)) e = kPosInf;
+        mx = fmax(mx, e);
+        nf |= !isfinite(W[i]);
+    }
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) {
+        if (mx > 0.0) atomicMax(maxbits, static_cast<unsigned long long>(__double_as_longlong(mx)));
+        if (__any_sync(0xffffffffu, nf) || nf) atomicOr(bad, 1);
+    }
+}
+}  // namespace
+
+cublasHandle_t cublas_of(Ctx& ctx) {
+    if (!ctx.cublas) {
+        cublasHandle_t h = nullptr;
+        if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) throw Status(100, "cublasCreate failed");
+        ctx.cublas = h;
+    }
+    cublasHandle_t h = static_cast<cublasHandle_t>(ctx.cublas);
+    cublasSetStream(h, ctx.stream);
+    return h;
+}
+
+// Wt (m x l, row-major) = Vt Ainv^T; residual max |Wt Aj^T - Vt| into maxbits
+// (as bits of a non-negative double), non-finite W flagged in bad. Row-major
+// X (r x c) is column-major X^T, so each product is one DGEMM; the residual
+// runs in row chunks (a bounded temporary).
+void wgemm_resid(Ctx& ctx, const double* Vt, const double* Ainv, const double* Aj, size_t m, size_t l, double* Wt,
+                 int* bad, unsigned long long* maxbits) {
+    cublasHandle_t h = cublas_of(ctx);
+    const double one = 1.0, zero = 0.0;
+    const int L = static_cast<int>(l);
+    const size_t chunk = std::max<size_t>(1, (size_t(64) << 20) / std::max<size_t>(l, 1));  // rows per 512 MB
+    DevBuf<double> R(std::min(m, chunk) * l);
+    for (size_t r0 = 0; r0 < m; r0 += chunk) {
+        const int rows = static_cast<int>(std::min(chunk, m - r0));
+        if (cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, L, rows, L, &one, Ainv, L, Vt + r0 * l, L, &zero, Wt + r0 * l,
+                        L) != CUBLAS_STATUS_SUCCESS ||
+            cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, L, rows, L, &one, Aj, L, Wt + r0 * l, L, &zero, R.get(), L) !=
+                CUBLAS_STATUS_SUCCESS)
+            throw Status(100, "cublasDgemm failed");
+        const long long cnt = static_cast<long long>(rows) * L;
+        resid_max_kernel<<<static_cast<int>(std::min<long long>(ceil_div(cnt, 256), 8LL * ctx.num_sms)), 256, 0,
+                           ctx.stream>>>(R.get(), Vt + r0 * l, cnt, maxbits, bad, Wt + r0 * l);
+    }
+    LAUNCH_OK("W = V A^-T (cuBLAS)");
 }
 
 // build_correction (sparse_kernel.cpp:82-117) on every band block.

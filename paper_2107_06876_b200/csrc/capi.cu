@@ -10,6 +10,7 @@
 #include <random>
 #include <string>
 
+#include <cublas_v2.h>
 #include <nccl.h>
 
 #include "../../include/lcn_b200.h"
@@ -445,6 +446,7 @@ int lcn_ctx_destroy(lcn_ctx* ctx) {
     cudaSetDevice(ctx->c.device);
     cudaDeviceSynchronize();
     ctx->c.comm.reset();
+    if (ctx->c.cublas) cublasDestroy(static_cast<cublasHandle_t>(ctx->c.cublas));
     if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.own_stream);
     delete ctx;
     return LCN_OK;

@@ -88,6 +88,8 @@ struct Ctx {
     // built on a context with a communicator are bucket-sharded (op.cuh
     // ShardState).
     std::shared_ptr<Comm> comm;
+    // cuBLAS handle (lazy; plain library GEMMs: W = V A^-T and its residual)
+    void* cublas = nullptr;
     int rank() const { return comm ? comm->rank : 0; }
     int world() const { return comm ? comm->world : 1; }
     void activate() const { CUDA_OK(cudaSetDevice(device)); }

@@ -6,14 +6,14 @@
 //   out_i = LSE_j( -c(x_i, y_j) / lambda + log v_j )
 // with x.y from tcgen05 3xTF32 MMAs (tc_block.cuh operands and pipeline),
 // c(x, y) from the dot and exact fp64 norms, and the log-sum-exp fused into
-// the epilogue: per (row, 128-column tile) a partial (max, sum), merged per
-// row in tile order by a second kernel (deterministic).
+// the epilogue: per (row, 64-column half tile) a partial (max, sum), merged
+// per row in order by a second kernel (deterministic).
 //
 // CTA (persistent, one per SM): warp 0 bulk-copies the row tile's and the
-// column tile's k-blocks into a 2-stage ring, warp 1 issues
+// column tile's k-blocks into a 3-stage ring, warp 1 issues
 // tcgen05.mma.kind::tf32 (hi.hi + hi.lo + lo.hi) into one of two TMEM
-// accumulators, 8 epilogue warps tcgen05.ld the 128 x 128 dots to a shared
-// staging tile and reduce each row with its lanes along the columns.
+// accumulators, 8 epilogue warps tcgen05.ld their row's 64 dots and reduce
+// them in registers.
 #include "op.cuh"
 #include "tc_block.cuh"
 
@@ -38,7 +38,17 @@ __device__ __forceinline__ float dense_cost(int kind, float dot, float nx, float
     return kind == 0 ? sqrtf(sq) : sq;
 }
 
-// items: it -> (row tile it / ntb, column tile it % ntb)
+// Ring depth of the recompute kernel: the epilogue reads the accumulators
+// straight from TMEM (no staging tile), so 3 stages of 64 KB fit -- the
+// operand feed is latency-bound at 2 (profiles/dense_tc_r02.json).
+constexpr int kDS = 3;
+constexpr int kDSmem = kDS * kStage + 2 * (kM * 8 + kM * 4) + 1024 + 128;
+
+// items: it -> (row tile it / ntb, column tile it % ntb). Epilogue thread =
+// (accumulator row = TMEM lane, half h of the 128 columns): its 64 dots come
+// from two tcgen05.ld's, the per-column log v and |y|^2 of the item from a
+// shared table; the row's (max, sum) over its 64 columns is written as
+// partial 2 ct + h.
 __global__ void __launch_bounds__(kThreads, 1) dense_lse_tc_kernel(const unsigned char* __restrict__ A,
                                                                    const unsigned char* __restrict__ B, int KB,
                                                                    int nta, int ntb, long long rows, long long cols,
@@ -51,13 +61,14 @@ __global__ void __launch_bounds__(kThreads, 1) dense_lse_tc_kernel(const unsigne
     extern __shared__ __align__(1024) unsigned char dyn_raw[];
     const uint32_t raw = smem_u32(dyn_raw);
     unsigned char* ring = dyn_raw + ((1024u - (raw & 1023u)) & 1023u);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kStages * kStage);
+    double* col_lv = reinterpret_cast<double*>(ring + kDS * kStage);  // [2][kM]
+    float* col_nb = reinterpret_cast<float*>(col_lv + 2 * kM);        // [2][kM]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(col_nb + 2 * kM);
     uint64_t* full = bars;
-    uint64_t* empty = bars + kStages;
-    uint64_t* tfull = bars + 2 * kStages;
+    uint64_t* empty = bars + kDS;
+    uint64_t* tfull = bars + 2 * kDS;
     uint64_t* tempty = tfull + kAcc;
     uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(tempty + kAcc);
-    float* stage = reinterpret_cast<float*>(ring + kStages * kStage + 128);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nitems = nta * ntb;
     if (warp == 1) {
@@ -67,7 +78,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_lse_tc_kernel(const unsigne
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < kDS; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
@@ -90,8 +101,8 @@ __global__ void __launch_bounds__(kThreads, 1) dense_lse_tc_kernel(const unsigne
                 const unsigned char* a = A + static_cast<size_t>(it / ntb) * tile_bytes;
                 const unsigned char* b = B + static_cast<size_t>(it % ntb) * tile_bytes;
                 for (int kb = 0; kb < KB; ++kb, ++g) {
-                    const uint32_t s = g % kStages;
-                    if (g >= kStages) mbar_wait_spin(&empty[s], ((g / kStages) - 1) & 1);
+                    const uint32_t s = g % kDS;
+                    if (g >= kDS) mbar_wait_spin(&empty[s], ((g / kDS) - 1) & 1);
                     mbar_arrive_expect_tx(&full[s], kStage);
                     bulk_g2s(ring + s * kStage, a + static_cast<size_t>(kb) * kKBlock, kKBlock, &full[s]);
                     bulk_g2s(ring + s * kStage + kKBlock, b + static_cast<size_t>(kb) * kKBlock, kKBlock, &full[s]);
@@ -106,8 +117,8 @@ __global__ void __launch_bounds__(kThreads, 1) dense_lse_tc_kernel(const unsigne
             fence_after();
             const uint32_t dt = tmem + buf * kM;
             for (int kb = 0; kb < KB; ++kb, ++g) {
-                const uint32_t s = g % kStages;
-                mbar_wait_spin(&full[s], (g / kStages) & 1);
+                const uint32_t s = g % kDS;
+                mbar_wait_spin(&full[s], (g / kDS) & 1);
                 fence_after();
                 const uint32_t base = smem_u32(ring + s * kStage);
                 const uint64_t ah = desc_sw128(base), al = desc_sw128(base + kHalf);
@@ -127,60 +138,57 @@ __global__ void __launch_bounds__(kThreads, 1) dense_lse_tc_kernel(const unsigne
     } else {
         const int q = warp & 3;
         const int row = 32 * q + lane;
-        const int c0 = ((warp - 2) >> 2) * kEpiCols;
-        const int ew = warp - 2;
+        const int h = (warp - 2) >> 2;  // column half
+        const int c0 = h * kEpiCols;
+        const int et = tid - 64;        // 0..255
+        const float finv = static_cast<float>(inv);
         uint32_t j = 0;
         for (int it = blockIdx.x; it < nitems; it += gridDim.x, ++j) {
             const uint32_t buf = j % kAcc;
             const int at = it / ntb, ct = it % ntb;
-            // this lane's columns of the tile: lane + 32 k
-            double cl[4];
-            float cn[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const long long c = static_cast<long long>(ct) * kM + lane + 32 * k;
-                cl[k] = c < cols ? lv[c] : kNegInf;
-                cn[k] = c < cols ? static_cast<float>(nb[c]) : 0.0f;
+            const int cb = j & 1;  // column-table buffer (the previous item may still be reading the other)
+            if (et < kM) {
+                const long long c = static_cast<long long>(ct) * kM + et;
+                col_lv[cb * kM + et] = c < cols ? lv[c] : kNegInf;
+                col_nb[cb * kM + et] = c < cols ? static_cast<float>(nb[c]) : 0.0f;
             }
-            const float finv = static_cast<float>(inv);
+            const long long gr = static_cast<long long>(at) * kM + row;
+            const float nx = gr < rows ? static_cast<float>(na[gr]) : 0.0f;
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");  // column table visible
             mbar_wait_spin(&tfull[buf], (j / kAcc) & 1);
             fence_after();
-            uint32_t v[kEpiCols];
             const uint32_t ta = tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * kM + c0;
-            ld32(ta, v);
-            ld32(ta + 32, v + 32);
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            fence_before();
-            mbar_arrive(&tempty[buf]);
-            asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+            const double* tl = col_lv + cb * kM + c0;
+            const float* tn = col_nb + cb * kM + c0;
+            // online (max, sum): one pass, nothing stored per column
+            double mx = kNegInf;
+            float sum = 0.0f;
 #pragma unroll
-            for (int c = 0; c < kEpiCols; ++c) stage[row * kStageLd + c0 + c] = __uint_as_float(v[c]);
-            asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
-            constexpr int kRows = kM / kEpiWarps;  // 16 rows per warp
-#pragma unroll 2
-            for (int i = 0; i < kRows; ++i) {
-                const int r = ew * kRows + i;
-                const long long gr = static_cast<long long>(at) * kM + r;
-                if (gr >= rows) break;  // uniform across the warp
-                const float nx = static_cast<float>(na[gr]);
-                double x[4], mx = kNegInf;
+            for (int half = 0; half < 2; ++half) {
+                uint32_t v[32];
+                ld32(ta + 32 * half, v);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (half == 1) {
+                    fence_before();
+                    mbar_arrive(&tempty[buf]);  // accumulator free for the item after next
+                }
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const float c = dense_cost(kind, stage[r * kStageLd + lane + 32 * k], nx, cn[k]);
-                    x[k] = cl[k] == kNegInf ? kNegInf : cl[k] - static_cast<double>(c * finv);
-                    mx = fmax(mx, x[k]);
+                for (int c = 0; c < 32; ++c) {
+                    const double l = tl[32 * half + c];
+                    if (l == kNegInf) continue;
+                    const double x = l - static_cast<double>(dense_cost(kind, __uint_as_float(v[c]), nx,
+                                                                        tn[32 * half + c]) * finv);
+                    if (x > mx) {
+                        sum = sum * __expf(static_cast<float>(mx - x)) + 1.0f;
+                        mx = x;
+                    } else {
+                        sum += __expf(static_cast<float>(x - mx));
+                    }
                 }
-                mx = warp_max(mx);
-                float s = 0.0f;
-                if (mx != kNegInf) {
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) s += __expf(static_cast<float>(x[k] - mx));
-                }
-                s = warp_sum(s);
-                if (lane == 0) {
-                    PM[gr * ntb + ct] = mx;
-                    PS[gr * ntb + ct] = static_cast<double>(s);
-                }
+            }
+            if (gr < rows) {
+                PM[(gr * ntb + ct) * 2 + h] = mx;
+                PS[(gr * ntb + ct) * 2 + h] = static_cast<double>(sum);
             }
         }
     }
@@ -243,7 +251,7 @@ void dense_tc_prepare(Op& op) {
         op.X.get(), d, d, nullptr, dt.get(), KB, nullptr, op.dtc_tiles.get());
     op.dtc_norm.resize(static_cast<size_t>(n + m));
     sqnorm_kernel<<<ceil_div(n + m, 256), 256, 0, s>>>(op.X.get(), n + m, d, op.dtc_norm.get());
-    op.dtc_pm.resize(static_cast<size_t>(std::max(n * op.dtc_ntb, m * op.dtc_nta)));
+    op.dtc_pm.resize(static_cast<size_t>(2 * std::max(n * op.dtc_ntb, m * op.dtc_nta)));
     op.dtc_ps.resize(op.dtc_pm.size());
     LAUNCH_OK("dense recompute operands");
     ctx.sync();
@@ -258,7 +266,7 @@ void dense_tc_lse(Op& op, bool transposed, const double* lv, const int* done, do
     Ctx& ctx = *op.ctx;
     static std::atomic<bool> attr[64];
     if (ctx.device >= 64 || !attr[ctx.device]) {
-        CUDA_OK(cudaFuncSetAttribute(dense_lse_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+        CUDA_OK(cudaFuncSetAttribute(dense_lse_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDSmem));
         if (ctx.device < 64) attr[ctx.device] = true;
     }
     const int KB = static_cast<int>(ceil_div(op.d, 32));
@@ -271,11 +279,11 @@ void dense_tc_lse(Op& op, bool transposed, const double* lv, const int* done, do
     const double* na = op.dtc_norm.get() + (transposed ? n : 0);
     const double* nb = op.dtc_norm.get() + (transposed ? 0 : n);
     const int grid = std::min(nta * ntb, ctx.num_sms);
-    dense_lse_tc_kernel<<<grid, kThreads, kSmem, ctx.stream>>>(transposed ? Q : P, transposed ? P : Q, KB, nta, ntb,
+    dense_lse_tc_kernel<<<grid, kThreads, kDSmem, ctx.stream>>>(transposed ? Q : P, transposed ? P : Q, KB, nta, ntb,
                                                                rows, cols, na, nb, op.cost, 1.0 / op.lambda, lv, done,
                                                                op.dtc_pm.get(), op.dtc_ps.get());
-    lse_merge_kernel<<<ceil_div(rows, 256), 256, 0, ctx.stream>>>(op.dtc_pm.get(), op.dtc_ps.get(), rows, ntb, done, M,
-                                                                  S);
+    lse_merge_kernel<<<ceil_div(rows, 256), 256, 0, ctx.stream>>>(op.dtc_pm.get(), op.dtc_ps.get(), rows, 2 * ntb,
+                                                                  done, M, S);
 }
 
 }  // namespace lcnb

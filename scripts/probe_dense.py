@@ -8,7 +8,7 @@ from paper_2107_06876_b200 import configs
 
 scale = float(sys.argv[1]) if len(sys.argv) > 1 else 1.0
 pr = configs.config1(scale)
-ctx = lcn.Context(0)
+ctx = lcn.Context(0, dense_recompute=os.environ.get("LCN_DENSE_RECOMPUTE") == "1")
 dp = torch.from_numpy(pr.p.astype(np.float32)).cuda()
 dq = torch.from_numpy(pr.q.astype(np.float32)).cuda()
 torch.cuda.synchronize()
@@ -17,7 +17,7 @@ op = lcn.KernelOperator.dense_device(ctx, dp.data_ptr(), pr.n, dq.data_ptr(), pr
 torch.cuda.synchronize()
 print(f"dense n={pr.n} m={pr.m} d={pr.d}: build {time.time() - t:.3f}s", flush=True)
 pm, qm = pr.marginals()
-for rep in range(3):
+for rep in range(int(os.environ.get("PROBE_REPS", "3"))):
     res = lcn.sinkhorn(op, pm, qm, lcn.SinkhornOptions(tol=0.0, max_iters=50, want_plan=False, check_support=False))
     it_ms = res.device_ms / 50
     B = 2 * 4 * pr.n * pr.m
