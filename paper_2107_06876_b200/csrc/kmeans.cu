@@ -273,6 +273,40 @@ __global__ void __launch_bounds__(256) pp_half_prep_kernel(const T* __restrict__
                                                          : kPosInf);
 }
 
+// int8 filter copy: per row a power-of-two scale s with max |x| / s <= 127,
+// q_k = rint(x_k / s) (q s exact in fp32), and eps = |x - q s| in fp64,
+// rounded up: half the bytes of the fp16 copy per listed point for the
+// filter pass, whose rigorous bound absorbs the coarser grid.
+template <typename T>
+__global__ void __launch_bounds__(256) pp_i8_prep_kernel(const T* __restrict__ X, long long N, int d, int dp,
+                                                         int8_t* __restrict__ Xq, float2* __restrict__ se) {
+    const long long row = blockIdx.x * 8LL + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= N) return;
+    const T* x = X + row * d;
+    double m = 0.0;
+    for (int k = lane; k < d; k += 32) m = fmax(m, fabs(static_cast<double>(x[k])));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const bool ok = m == 0.0 || (m < 1e30 && m > 1e-30);
+    int e = 0;
+    frexp(m / 127.0, &e);  // m / 127 < 2^e
+    const double sc = ok && m > 0.0 ? ldexp(1.0, e) : 1.0, inv = 1.0 / sc;
+    double err2 = 0.0;
+    for (int k = lane; k < dp; k += 32) {
+        const double v = k < d ? static_cast<double>(x[k]) : 0.0;
+        double qv = ok ? rint(v * inv) : 0.0;
+        qv = fmin(fmax(qv, -127.0), 127.0);
+        Xq[row * dp + k] = static_cast<int8_t>(qv);
+        const double df = v - qv * sc;
+        err2 += df * df;
+    }
+    err2 = warp_sum(err2);
+    if (lane == 0)
+        se[row] = make_float2(static_cast<float>(sc), ok ? __double2float_ru(sqrt(err2) * (1.0 + 1e-12) + 1e-300)
+                                                         : kPosInf);
+}
+
 // 32 values per lane -> lane l gets the warp sum of value l (31 shuffles)
 __device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
 #pragma unroll
@@ -293,8 +327,8 @@ __device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
 // rows), the bound is computed lane-parallel with one transpose reduction,
 // and the survivors' rows are staged into the same buffer and folded exactly
 // as in pp_exact_kernel. dp is a multiple of 8 (16-byte row chunks).
-template <typename T, int NQ>
-__global__ void __launch_bounds__(128) pp_filter_exact_kernel(const T* __restrict__ X, const __half* __restrict__ Xh,
+template <typename T, typename QT, int NQ>
+__global__ void __launch_bounds__(128) pp_filter_exact_kernel(const T* __restrict__ X, const QT* __restrict__ Xh,
                                                               const float2* __restrict__ se, int d, int dp,
                                                               const uint32_t* __restrict__ chosen, int t,
                                                               double* __restrict__ dist2, uint32_t* __restrict__ near,
@@ -308,7 +342,7 @@ __global__ void __launch_bounds__(128) pp_filter_exact_kernel(const T* __restric
     unsigned char* wb = dyn + (static_cast<size_t>(d) * 8 + (max(dp, NQ * 128) + 4) * 4 + 15) / 16 * 16;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     unsigned char* mybuf = wb + static_cast<size_t>(warp) * wbuf_bytes;
-    __half* hbuf = reinterpret_cast<__half*>(mybuf);  // 32 x dp halves
+    QT* hbuf = reinterpret_cast<QT*>(mybuf);          // 32 x dp filter values (fp16 or int8)
     T* buf = reinterpret_cast<T*>(mybuf);             // 32 x (d + 1) survivors' rows
     const long long last = chosen[t];
     for (int k = threadIdx.x; k < NQ * 128; k += blockDim.x) {
@@ -329,7 +363,8 @@ __global__ void __launch_bounds__(128) pp_filter_exact_kernel(const T* __restric
     __syncthreads();
     const double ec = eps_c;
     const double gam = 1.0 - (dp + 4) * 1.1920928955078125e-07;  // (dp + 4) 2^-23
-    const int nch16 = dp / 8;                                     // 16-byte chunks per fp16 row
+    constexpr int kPer16 = 16 / static_cast<int>(sizeof(QT));    // values per 16-byte chunk
+    const int nch16 = dp / kPer16;                                // 16-byte chunks per filter row
     // lane's 4-value chunks of the center (zero beyond dp: hbuf there is never
     // staged, its products are multiplied out below)
     float4 cq[NQ];
@@ -350,7 +385,7 @@ __global__ void __launch_bounds__(128) pp_filter_exact_kernel(const T* __restric
         for (int e = lane; e < 32 * nch16; e += 32) {  // one (row, chunk) per lane and step
             const int j = e / nch16, c = e - j * nch16;
             const long long row = __shfl_sync(0xffffffffu, mine, j);
-            cp_async16(hbuf + j * dp + c * 8, Xh + row * dp + c * 8);
+            cp_async16(hbuf + j * dp + c * kPer16, Xh + row * dp + c * kPer16);
         }
         cp_async_commit();
         const float2 my_se = se[mine];
@@ -365,9 +400,16 @@ __global__ void __launch_bounds__(128) pp_filter_exact_kernel(const T* __restric
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
                 if (!qin[q]) continue;
-                const uint2 raw = *reinterpret_cast<const uint2*>(hbuf + j * dp + 4 * (lane + 32 * q));
-                const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
-                const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
+                float2 a, b;
+                if constexpr (sizeof(QT) == 2) {
+                    const uint2 raw = *reinterpret_cast<const uint2*>(hbuf + j * dp + 4 * (lane + 32 * q));
+                    a = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
+                    b = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
+                } else {
+                    const char4 c4 = *reinterpret_cast<const char4*>(hbuf + j * dp + 4 * (lane + 32 * q));
+                    a = make_float2(static_cast<float>(c4.x), static_cast<float>(c4.y));
+                    b = make_float2(static_cast<float>(c4.z), static_cast<float>(c4.w));
+                }
                 const float d0 = fmaf(a.x, sj, -cq[q].x), d1 = fmaf(a.y, sj, -cq[q].y);
                 const float d2 = fmaf(b.x, sj, -cq[q].z), d3 = fmaf(b.y, sj, -cq[q].w);
                 acc = fmaf(d0, d0, acc);
@@ -1173,33 +1215,52 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     int ex_occ = 1;
     CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ex_occ, pp_exact_kernel<T>, ex_warps * 32, ex_smem));
     const int ex_grid = std::max(1, ex_occ) * ctx.num_sms;
-    // fp16 filter copy (rows up to 512 halves)
-    const int dp = (d + 7) / 8 * 8;
+    // filter copy of the points: fp16 rows with a power-of-two scale per row
+    // (default) or int8 rows (LCN_PP_FILTER=i8: half the bytes, measured no
+    // faster at configs[3] -- the filter pass is latency-, not byte-bound);
+    // rows up to 512 values
+    const char* fenv = std::getenv("LCN_PP_FILTER");
+    const bool i8 = fenv && std::string(fenv) == "i8";
+    const int qsz = i8 ? 1 : 2;
+    const int dp = i8 ? (d + 15) / 16 * 16 : (d + 7) / 8 * 8;
     const bool filt = dp <= kFiltMaxQ * 128 && std::getenv("LCN_PP_NOFILTER") == nullptr;
-    DevBuf<__half> Xh(filt ? static_cast<size_t>(N) * dp : 1);
+    DevBuf<unsigned char> Xq(filt ? static_cast<size_t>(N) * dp * qsz : 1);
     DevBuf<float2> se(filt ? static_cast<size_t>(N) : 1);
     const int wbuf_bytes = static_cast<int>(
-        (std::max(static_cast<size_t>(32) * dp * 2, static_cast<size_t>(32) * (d + 1) * sizeof(T)) + 15) / 16 * 16);
+        (std::max(static_cast<size_t>(32) * dp * qsz, static_cast<size_t>(32) * (d + 1) * sizeof(T)) + 15) / 16 * 16);
     const int nq = (dp / 4 + 31) / 32;
     // c32 is read for NQ * 128 entries; the per-warp buffers start 16-aligned
     const size_t fx_smem = (static_cast<size_t>(d) * 8 + (std::max(dp, nq * 128) + 4) * 4 + 15) / 16 * 16 +
                            static_cast<size_t>(ex_warps) * wbuf_bytes;
-    auto fx_kernel = [&]() -> void (*)(const T*, const __half*, const float2*, int, int, const uint32_t*, int,
-                                       double*, uint32_t*, const uint32_t*, const unsigned*, int, double*) {
-        switch (nq) {
-            case 1: return pp_filter_exact_kernel<T, 1>;
-            case 2: return pp_filter_exact_kernel<T, 2>;
-            case 3: return pp_filter_exact_kernel<T, 3>;
-            default: return pp_filter_exact_kernel<T, 4>;
-        }
-    }();
+    using FxH = void (*)(const T*, const __half*, const float2*, int, int, const uint32_t*, int, double*, uint32_t*,
+                         const uint32_t*, const unsigned*, int, double*);
+    using FxQ = void (*)(const T*, const int8_t*, const float2*, int, int, const uint32_t*, int, double*, uint32_t*,
+                         const uint32_t*, const unsigned*, int, double*);
+    const FxH fx_h = nq == 1 ? pp_filter_exact_kernel<T, __half, 1>
+                   : nq == 2 ? pp_filter_exact_kernel<T, __half, 2>
+                   : nq == 3 ? pp_filter_exact_kernel<T, __half, 3>
+                             : pp_filter_exact_kernel<T, __half, 4>;
+    const FxQ fx_q = nq == 1 ? pp_filter_exact_kernel<T, int8_t, 1>
+                   : nq == 2 ? pp_filter_exact_kernel<T, int8_t, 2>
+                   : nq == 3 ? pp_filter_exact_kernel<T, int8_t, 3>
+                             : pp_filter_exact_kernel<T, int8_t, 4>;
     int fx_grid = ex_grid;
     if (filt) {
-        pp_half_prep_kernel<T><<<ceil_div(N, 8), 256, 0, s>>>(X, N, d, dp, Xh.get(), se.get());
-        LAUNCH_OK("kmeans++ fp16 filter copy");
-        allow_max_dyn_smem(fx_kernel);
+        if (i8)
+            pp_i8_prep_kernel<T><<<ceil_div(N, 8), 256, 0, s>>>(X, N, d, dp, reinterpret_cast<int8_t*>(Xq.get()),
+                                                               se.get());
+        else
+            pp_half_prep_kernel<T><<<ceil_div(N, 8), 256, 0, s>>>(X, N, d, dp, reinterpret_cast<__half*>(Xq.get()),
+                                                                 se.get());
+        LAUNCH_OK("kmeans++ filter copy");
         int occ = 1;
-        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fx_kernel, ex_warps * 32, fx_smem));
+        if (i8) {
+            allow_max_dyn_smem(fx_q);
+            CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fx_q, ex_warps * 32, fx_smem));
+        } else {
+            allow_max_dyn_smem(fx_h);
+            CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fx_h, ex_warps * 32, fx_smem));
+        }
         fx_grid = std::max(1, occ) * ctx.num_sms;
     }
     DevBuf<unsigned long long> d_raw(raw.size() ? raw.size() : 1);
@@ -1219,10 +1280,14 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
         if (t > 1) seed_dist_kernel<T><<<ceil_div(t - 1, 8), 256, 0, s>>>(X, d, d_chosen, t - 1, dc.get());
         pp_prune_kernel<<<nch, 256, 0, s>>>(N, t - 1, dist2.get(), near.get(), dc.get(), list.get(), cnt.get(),
                                             csum.get());
-        if (filt)
-            fx_kernel<<<fx_grid, ex_warps * 32, fx_smem, s>>>(X, Xh.get(), se.get(), d, dp, d_chosen, t - 1,
-                                                              dist2.get(), near.get(), list.get(), cnt.get(),
-                                                              wbuf_bytes, csum.get());
+        if (filt && i8)
+            fx_q<<<fx_grid, ex_warps * 32, fx_smem, s>>>(X, reinterpret_cast<const int8_t*>(Xq.get()), se.get(), d, dp,
+                                                         d_chosen, t - 1, dist2.get(), near.get(), list.get(),
+                                                         cnt.get(), wbuf_bytes, csum.get());
+        else if (filt)
+            fx_h<<<fx_grid, ex_warps * 32, fx_smem, s>>>(X, reinterpret_cast<const __half*>(Xq.get()), se.get(), d, dp,
+                                                         d_chosen, t - 1, dist2.get(), near.get(), list.get(),
+                                                         cnt.get(), wbuf_bytes, csum.get());
         else
             pp_exact_kernel<T><<<ex_grid, ex_warps * 32, ex_smem, s>>>(X, d, d_chosen, t - 1, dist2.get(), near.get(),
                                                                        list.get(), cnt.get(), csum.get());
