@@ -2070,10 +2070,11 @@ void finalize_storage(Op& op) {
             op.val32.push_back(std::move(v));
         }
     }
-    if (op.kind == 3) {
+    if (op.kind == 3 || op.kind == 1) {
         // LCN: delta also stored transposed (targets x sources) so the row
         // pass streams its blocks in the same output-stationary order as the
-        // column pass (2 x the delta bytes in HBM, same bytes per iteration)
+        // column pass (2 x the delta bytes in HBM, same bytes per iteration).
+        // Sparse: log K transposed, so the column log-sum-exp reads rows too.
         op.val32T.clear();
         op.val64T.clear();
         for (size_t b = 0; b < op.bands.size(); ++b) {
@@ -2100,7 +2101,7 @@ void finalize_storage(Op& op) {
             }
             LAUNCH_OK("transpose_blocks");
         }
-        build_iter_layout(op);
+        if (op.kind == 3) build_iter_layout(op);
     }
     if (op.kind >= 2) {
         if (op.fp64) {

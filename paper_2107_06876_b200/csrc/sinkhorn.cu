@@ -25,6 +25,7 @@
 // padded to 16-byte multiples and blocks start on 128-byte lines (build.cu),
 // factor rows to lp = round_up(l, 4).
 #include <cub/cub.cuh>
+#include <math_constants.h>
 
 #include <algorithm>
 #include <cmath>
@@ -117,15 +118,59 @@ __global__ void __launch_bounds__(kThreads) sparse_row_band_kernel(const DevStat
         __syncthreads();
         for (uint32_t c = threadIdx.x; c < cn; c += kThreads) lt[c] = log_t[bv.tgt_order[tb + c0 + c]];
         __syncthreads();
+        if constexpr (sizeof(T) == 4) {
+            // fp32 storage: 4 rows per warp at a time (4 x the loads in
+            // flight), exponents in fp32 (MUFU), each row's sum widened once;
+            // the second read of the rows hits L1
+            constexpr int kRW = 4;
+            for (uint32_t r0w = warp * kRW; r0w < nb; r0w += kWarps * kRW) {
+                float hf[kRW], af[kRW];
+#pragma unroll
+                for (int k = 0; k < kRW; ++k) {
+                    hf[k] = -CUDART_INF_F;
+                    af[k] = 0.0f;
+                }
+                for (uint32_t c = lane; c < cn; c += 32) {
+                    const float l = static_cast<float>(lt[c]);
+#pragma unroll
+                    for (int k = 0; k < kRW; ++k)
+                        if (r0w + k < nb) hf[k] = fmaxf(hf[k], vals[off + (r0w + k) * ms + c0 + c] + l);
+                }
+#pragma unroll
+                for (int k = 0; k < kRW; ++k) hf[k] = warp_max(hf[k]);
+                for (uint32_t c = lane; c < cn; c += 32) {
+                    const float l = static_cast<float>(lt[c]);
+#pragma unroll
+                    for (int k = 0; k < kRW; ++k)
+                        if (r0w + k < nb && hf[k] != -CUDART_INF_F)
+                            af[k] += __expf(vals[off + (r0w + k) * ms + c0 + c] + l - hf[k]);
+                }
+#pragma unroll
+                for (int k = 0; k < kRW; ++k) af[k] = warp_sum(af[k]);
+                if (lane < kRW && r0w + lane < nb) {
+                    float h = hf[0], a = af[0];
+#pragma unroll
+                    for (int k = 1; k < kRW; ++k)
+                        if (lane == k) { h = hf[k]; a = af[k]; }
+                    const uint32_t i = bv.src_order[sb + r0w + lane];
+                    double M = Mrow[i], S = Srow[i];
+                    lse_merge(M, S, h == -CUDART_INF_F ? kNegInf : static_cast<double>(h), static_cast<double>(a));
+                    Mrow[i] = M;
+                    Srow[i] = S;
+                }
+            }
+            continue;
+        }
         for (uint32_t r = warp; r < nb; r += kWarps) {
             const T* row = vals + off + r * ms + c0;
-            double hi = kNegInf;
-            for (uint32_t c = lane; c < cn; c += 32) hi = fmax(hi, ld1(row + c) + lt[c]);
-            hi = warp_max(hi);
-            double acc = 0.0;
-            if (hi != kNegInf)
-                for (uint32_t c = lane; c < cn; c += 32) acc += exp(ld1(row + c) + lt[c] - hi);
-            acc = warp_sum(acc);
+            double hi = kNegInf, acc = 0.0;
+            {
+                for (uint32_t c = lane; c < cn; c += 32) hi = fmax(hi, ld1(row + c) + lt[c]);
+                hi = warp_max(hi);
+                if (hi != kNegInf)
+                    for (uint32_t c = lane; c < cn; c += 32) acc += exp(ld1(row + c) + lt[c] - hi);
+                acc = warp_sum(acc);
+            }
             if (lane == 0) {
                 const uint32_t i = bv.src_order[sb + r];
                 double M = Mrow[i], S = Srow[i];
@@ -156,11 +201,33 @@ __global__ void __launch_bounds__(kThreads) sparse_col_band_kernel(const DevStat
         for (uint32_t r = threadIdx.x; r < rn; r += kThreads) ls[r] = log_s[bv.src_order[sb + r0 + r]];
         __syncthreads();
         for (uint32_t c = threadIdx.x; c < mb; c += kThreads) {
-            double hi = kNegInf;
-            for (uint32_t r = 0; r < rn; ++r) hi = fmax(hi, ld1(vals + off + (r0 + r) * ms + c) + ls[r]);
-            double acc = 0.0;
-            if (hi != kNegInf)
-                for (uint32_t r = 0; r < rn; ++r) acc += exp(ld1(vals + off + (r0 + r) * ms + c) + ls[r] - hi);
+            double hi = kNegInf, acc = 0.0;
+            if constexpr (sizeof(T) == 4) {  // fp32 storage: fp32 exponents (MUFU); the second pass hits L2
+                const T* col = vals + off + static_cast<unsigned long long>(r0) * ms + c;
+                float h4[4] = {-CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F};
+                uint32_t r = 0;
+                for (; r + 4 <= rn; r += 4)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        h4[k] = fmaxf(h4[k], col[static_cast<unsigned long long>(r + k) * ms] + static_cast<float>(ls[r + k]));
+                for (; r < rn; ++r) h4[0] = fmaxf(h4[0], col[static_cast<unsigned long long>(r) * ms] + static_cast<float>(ls[r]));
+                const float hf = fmaxf(fmaxf(h4[0], h4[1]), fmaxf(h4[2], h4[3]));
+                float a4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+                if (hf != -CUDART_INF_F) {
+                    r = 0;
+                    for (; r + 4 <= rn; r += 4)
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            a4[k] += __expf(col[static_cast<unsigned long long>(r + k) * ms] + static_cast<float>(ls[r + k]) - hf);
+                    for (; r < rn; ++r) a4[0] += __expf(col[static_cast<unsigned long long>(r) * ms] + static_cast<float>(ls[r]) - hf);
+                }
+                hi = hf == -CUDART_INF_F ? kNegInf : static_cast<double>(hf);
+                acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+            } else {
+                for (uint32_t r = 0; r < rn; ++r) hi = fmax(hi, ld1(vals + off + (r0 + r) * ms + c) + ls[r]);
+                if (hi != kNegInf)
+                    for (uint32_t r = 0; r < rn; ++r) acc += exp(ld1(vals + off + (r0 + r) * ms + c) + ls[r] - hi);
+            }
             const uint32_t j = bv.tgt_order[tb + c];
             double M = Mcol[j], S = Scol[j];
             lse_merge(M, S, hi, acc);
@@ -1989,6 +2056,11 @@ struct Solver {
         else return op.val64[b].get();
     }
     template <typename T>
+    bool has_valsT(size_t b) const {
+        if constexpr (std::is_same_v<T, float>) return b < op.val32T.size() && op.val32T[b].size() > 0;
+        else return b < op.val64T.size() && op.val64T[b].size() > 0;
+    }
+    template <typename T>
     const T* band_valsT(int b) const {
         if constexpr (std::is_same_v<T, float>) return op.val32T[b].get();
         else return op.val64T[b].get();
@@ -2142,9 +2214,20 @@ struct Solver {
         }
         lse_init_kernel<<<ceil_div(m, 256), 256, 0, s>>>(st.get(), Mc.get(), Sc.get(), m);
         for (size_t b = 0; b < op.bands.size(); ++b)
-            if (op.bands[b].n_work)
-                sparse_col_band_kernel<T><<<op.bands[b].n_work, kThreads, 0, s>>>(
-                    st.get(), op.view(b), op.bands[b].work.get(), band_vals<T>(b), ls, Mc.get(), Sc.get());
+            if (op.bands[b].n_work) {
+                if (has_valsT<T>(b)) {
+                    // the transposed blocks (targets x sources): the row kernel with the roles swapped
+                    BandView tv = op.view(b);
+                    std::swap(tv.src_order, tv.tgt_order);
+                    std::swap(tv.src_start, tv.tgt_start);
+                    tv.blk_off = tv.blkT_off;
+                    sparse_row_band_kernel<T><<<op.bands[b].n_work, kThreads, 0, s>>>(
+                        st.get(), tv, op.bands[b].work.get(), band_valsT<T>(b), ls, Mc.get(), Sc.get());
+                } else {
+                    sparse_col_band_kernel<T><<<op.bands[b].n_work, kThreads, 0, s>>>(
+                        st.get(), op.view(b), op.bands[b].work.get(), band_vals<T>(b), ls, Mc.get(), Sc.get());
+                }
+            }
     }
     template <typename T>
     void sparse_iteration(int it, double tol, int max_iters) {

@@ -18,6 +18,9 @@ dp = torch.from_numpy(pr.p.astype(np.float32)).cuda()
 dq = torch.from_numpy(pr.q.astype(np.float32)).cuda()
 torch.cuda.synchronize()
 cfg = lcn.LshConfig(pr.bands, 1, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
+if os.environ.get("PROBE_SPARSE") == "1":  # the sparse-only operator (KernelOperator::sparse) on the same LSH
+    import dataclasses
+    pr = dataclasses.replace(pr, landmarks=0)
 for _b in range(int(os.environ.get("PROBE_BUILDS", "1")) - 1):  # warm-up builds (pool, first touch)
     if os.environ.get("LCN_TIMING"):
         print(f"---- warm-up build {_b}", file=sys.stderr, flush=True)

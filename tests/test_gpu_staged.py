@@ -121,3 +121,25 @@ def test_reference_hand_built_cases(ref, ctx64):
         lcn.KernelOperator.from_sparse(ctx64, 3, 3, rp, col, lv, 0.0)
     with pytest.raises(lcn.DimensionError):
         lcn.build_correction(ctx64, rp, col[:-1], lv[:-1], np.ones((3, 1)), np.ones((1, 3)))
+
+
+def test_factorization_error_beyond_jitter_budget(ctx64):
+    """build_factors (nystrom.cpp:104-124): a landmark kernel matrix that no
+    jitter level makes factorizable (non-finite landmark coordinates) raises
+    FactorizationError with the reference's message, through the staged API
+    and through a configs[3]-sized operator build with external landmarks."""
+    r = np.random.default_rng(3)
+    p = r.normal(size=(50, 4))
+    q = r.normal(size=(40, 4))
+    L = r.normal(size=(6, 4))
+    L[2, 1] = np.nan
+    with pytest.raises(lcn.FactorizationError, match="jitter budget"):
+        lcn.build_factors(ctx64, p, q, L, lcn.SQEUCLIDEAN, 1.0)
+    pr = configs.config3(0.01)
+    ids = lcn.lsh_kmeans_buckets(ctx64, pr.p, pr.q, lcn.LshConfig(pr.bands, 1, pr.buckets, pr.kmeans_iters,
+                                                                     pr.lsh_seed))
+    Lbig = np.ascontiguousarray(pr.p[:pr.landmarks].copy())
+    Lbig[5, 7] = np.inf
+    with pytest.raises(lcn.FactorizationError):
+        lcn.KernelOperator.lcn_buckets(ctx64, pr.p, pr.q, pr.cost, pr.lam_eff, ids[:, :pr.n], ids[:, pr.n:],
+                                       landmarks=Lbig, range_=pr.buckets)
