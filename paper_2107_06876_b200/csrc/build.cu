@@ -1529,6 +1529,8 @@ void select_landmarks_device(Op& op, Ctx& ctx, int method, uint64_t seed) {
 
 void wgemm_resid(Ctx& ctx, const double* Vt, const double* Ainv, const double* Aj, size_t m, size_t l, double* Wt,
                  int* bad, unsigned long long* maxbits);
+void uv_gemm_exp(Ctx& ctx, const double* X, size_t rows, const double* L, size_t l, size_t d, const double* xsq,
+                 const double* lsq, int kind, double inv, double* out, int* bad);
 
 void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed) {
     Ctx& ctx = *op.ctx;
@@ -1589,6 +1591,17 @@ void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed)
                          static_cast<long long>(l), op.cost, 1.0 / op.lambda, sq + (side ? n : 0), lsq.get(), bad.get()};
             tc_run(ctx, px, pl, static_cast<int>(d), items, epi);
         }
+    } else if (!op.fp64 && !ctx.exact_build && op.cost >= 0 && op.cost <= 3 && std::getenv("LCN_UV_TILES") == nullptr) {
+        // fp32 storage: the point x landmark dots as fp64 GEMMs on cuBLAS
+        // (FP64 tensor cores), the cost and exp in an elementwise pass. fp64
+        // dots keep U / V ~1e-15 from the reference's sequential folds (the
+        // 3xTF32 split loses ~1e-4 of the plan to the 2 x.l cancellation,
+        // see use_tc_build); LCN_UV_TILES forces the exact fold tiles.
+        const double* sq = union_sqnorms(op);
+        DevBuf<double> lsq(l);
+        norms_kernel<<<ceil_div(l, 256), 256, 0, s>>>(op.L.get(), l, d, lsq.get());
+        uv_gemm_exp(ctx, op.P(), n, op.L.get(), l, d, sq, lsq.get(), op.cost, 1.0 / op.lambda, op.U64.get(), bad.get());
+        uv_gemm_exp(ctx, op.Q(), m, op.L.get(), l, d, sq + n, lsq.get(), op.cost, 1.0 / op.lambda, Vt.get(), bad.get());
     } else {
         exp_block(op.U64.get(), op.P(), n, nrm, op.L.get(), l, lnorm.get(), false);
         exp_block(Vt.get(), op.Q(), m, nrm ? nrm + n : nullptr, op.L.get(), l, lnorm.get(), false);
@@ -1694,6 +1707,55 @@ __global__ void resid_max_kernel(const double* __restrict__ R, const double* __r
     }
 }
 }  // namespace
+
+cublasHandle_t cublas_of(Ctx& ctx);
+
+namespace {
+// k(x, l) = exp(-c(x, l) * (1 / lambda)) from the fp64 dot (in place) and the
+// points' / landmarks' |.|^2 (kernel_block, nystrom.cpp:53-64)
+__global__ void uv_exp_kernel(double* __restrict__ D, long long rows, int l, const double* __restrict__ xsq,
+                              const double* __restrict__ lsq, int kind, double inv, int* __restrict__ bad) {
+    const long long total = rows * l;
+    for (long long e = blockIdx.x * 256LL + threadIdx.x; e < total; e += 256LL * gridDim.x) {
+        const long long r = e / l;
+        const int a = static_cast<int>(e - r * l);
+        const double dot = D[e], nx = xsq[r], nl = lsq[a];
+        double c;
+        if (kind == 1) {
+            c = -dot;
+        } else if (kind == 2) {
+            if (nx == 0.0 || nl == 0.0) {
+                atomicOr(bad, 1);
+                c = 0.0;
+            } else {
+                double cs = dot / sqrt(nx * nl);
+                cs = cs > 1.0 ? 1.0 : (cs < -1.0 ? -1.0 : cs);
+                c = sqrt(1.0 - cs);
+            }
+        } else {
+            const double sq = fmax(nx + nl - 2.0 * dot, 0.0);
+            c = kind == 0 ? sqrt(sq) : sq;
+        }
+        D[e] = exp(-c * inv);
+    }
+}
+}  // namespace
+
+void uv_gemm_exp(Ctx& ctx, const double* X, size_t rows, const double* L, size_t l, size_t d, const double* xsq,
+                 const double* lsq, int kind, double inv, double* out, int* bad) {
+    if (!rows) return;
+    cublasHandle_t h = cublas_of(ctx);
+    const double one = 1.0, zero = 0.0;
+    // out (rows x l, row-major) = X L^T: column-major out^T = L X^T
+    if (cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, static_cast<int>(l), static_cast<int>(rows), static_cast<int>(d),
+                    &one, L, static_cast<int>(d), X, static_cast<int>(d), &zero, out, static_cast<int>(l)) !=
+        CUBLAS_STATUS_SUCCESS)
+        throw Status(100, "cublasDgemm failed (point x landmark dots)");
+    const long long total = static_cast<long long>(rows) * static_cast<long long>(l);
+    uv_exp_kernel<<<static_cast<int>(std::min<long long>(ceil_div(total, 256), 16LL * ctx.num_sms)), 256, 0,
+                    ctx.stream>>>(out, static_cast<long long>(rows), static_cast<int>(l), xsq, lsq, kind, inv, bad);
+    LAUNCH_OK("U / V from fp64 GEMM");
+}
 
 cublasHandle_t cublas_of(Ctx& ctx) {
     if (!ctx.cublas) {
