@@ -322,11 +322,15 @@ __device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
     return v[0];
 }
 
-// Filtered exact pass: per warp, 32 listed points. Their fp16 rows are
-// staged in shared memory with 16-byte cp.async (one memory latency per 32
-// rows), the bound is computed lane-parallel with one transpose reduction,
-// and the survivors' rows are staged into the same buffer and folded exactly
-// as in pp_exact_kernel. dp is a multiple of 8 (16-byte row chunks).
+// Filtered exact pass: per warp, 32 listed points. Each lane loads its 4-value
+// chunks of all 32 filter rows straight into registers (32 independent
+// coalesced loads in flight per lane: the pass is memory-latency bound, ncu
+// profiles/seed_filter_r02.json), the bound is computed lane-parallel with
+// one transpose reduction, and the survivors' rows are staged 8 at a time
+// into shared memory and folded exactly as in pp_exact_kernel. The shared
+// footprint is the survivor buffer alone, so 4-warp CTAs reach the register
+// occupancy limit.
+constexpr int kSurv = 8;  // survivors staged per group
 template <typename T, typename QT, int NQ>
 __global__ void __launch_bounds__(128) pp_filter_exact_kernel(const T* __restrict__ X, const QT* __restrict__ Xh,
                                                               const float2* __restrict__ se, int d, int dp,
@@ -341,9 +345,7 @@ __global__ void __launch_bounds__(128) pp_filter_exact_kernel(const T* __restric
     float* c32 = reinterpret_cast<float*>(cs + d);  // max(dp, NQ 128) entries
     unsigned char* wb = dyn + (static_cast<size_t>(d) * 8 + (max(dp, NQ * 128) + 4) * 4 + 15) / 16 * 16;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    unsigned char* mybuf = wb + static_cast<size_t>(warp) * wbuf_bytes;
-    QT* hbuf = reinterpret_cast<QT*>(mybuf);          // 32 x dp filter values (fp16 or int8)
-    T* buf = reinterpret_cast<T*>(mybuf);             // 32 x (d + 1) survivors' rows
+    T* buf = reinterpret_cast<T*>(wb + static_cast<size_t>(warp) * wbuf_bytes);  // kSurv x (d + 1) survivors' rows
     const long long last = chosen[t];
     for (int k = threadIdx.x; k < NQ * 128; k += blockDim.x) {
         const double v = k < d ? static_cast<double>(X[last * d + k]) : 0.0;
@@ -363,10 +365,8 @@ __global__ void __launch_bounds__(128) pp_filter_exact_kernel(const T* __restric
     __syncthreads();
     const double ec = eps_c;
     const double gam = 1.0 - (dp + 4) * 1.1920928955078125e-07;  // (dp + 4) 2^-23
-    constexpr int kPer16 = 16 / static_cast<int>(sizeof(QT));    // values per 16-byte chunk
-    const int nch16 = dp / kPer16;                                // 16-byte chunks per filter row
-    // lane's 4-value chunks of the center (zero beyond dp: hbuf there is never
-    // staged, its products are multiplied out below)
+    // lane's 4-value chunks of the center (zero beyond dp: those row chunks
+    // are never loaded, their products are multiplied out below)
     float4 cq[NQ];
     bool qin[NQ];
 #pragma unroll
@@ -381,32 +381,26 @@ __global__ void __launch_bounds__(128) pp_filter_exact_kernel(const T* __restric
         const unsigned nb = cnt - b0 < 32u ? cnt - b0 : 32u;
         // rows past the batch read row 0 (harmless; their lanes are ignored)
         const uint32_t mine = lane < static_cast<int>(nb) ? list[b0 + lane] : 0u;
-        __syncwarp();
-        for (int e = lane; e < 32 * nch16; e += 32) {  // one (row, chunk) per lane and step
-            const int j = e / nch16, c = e - j * nch16;
-            const long long row = __shfl_sync(0xffffffffu, mine, j);
-            cp_async16(hbuf + j * dp + c * kPer16, Xh + row * dp + c * kPer16);
-        }
-        cp_async_commit();
         const float2 my_se = se[mine];
         const double my_d2 = dist2[mine];
-        cp_async_wait<0>();
-        __syncwarp();
         float part[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
+            const long long row = __shfl_sync(0xffffffffu, mine, j);
             const float sj = __shfl_sync(0xffffffffu, my_se.x, j);
             float acc = 0.f;
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
                 if (!qin[q]) continue;
+                const QT* src = Xh + row * dp + 4 * (lane + 32 * q);
                 float2 a, b;
                 if constexpr (sizeof(QT) == 2) {
-                    const uint2 raw = *reinterpret_cast<const uint2*>(hbuf + j * dp + 4 * (lane + 32 * q));
+                    const uint2 raw = __ldg(reinterpret_cast<const uint2*>(src));
                     a = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
                     b = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
                 } else {
-                    const char4 c4 = *reinterpret_cast<const char4*>(hbuf + j * dp + 4 * (lane + 32 * q));
+                    const int raw = __ldg(reinterpret_cast<const int*>(src));
+                    const char4 c4 = *reinterpret_cast<const char4*>(&raw);
                     a = make_float2(static_cast<float>(c4.x), static_cast<float>(c4.y));
                     b = make_float2(static_cast<float>(c4.z), static_cast<float>(c4.w));
                 }
@@ -431,29 +425,32 @@ __global__ void __launch_bounds__(128) pp_filter_exact_kernel(const T* __restric
         if (lane == 0) atomicAdd(&g_filt_surv, static_cast<unsigned long long>(ns));
 #endif
         if (!ns) continue;
-        // lane r takes the r-th survivor
+        // lane r takes the r-th survivor; groups of kSurv rows through shared memory
         const int jr = lane < ns ? static_cast<int>(__fns(sv, 0, lane + 1)) : 0;
         const uint32_t srow = __shfl_sync(0xffffffffu, mine, jr);
-        __syncwarp();
-        for (int r = 0; r < ns; ++r) {
-            const long long row = __shfl_sync(0xffffffffu, srow, r);
-            for (int k = lane; k < d; k += 32) cp_async_elem(&buf[r * (d + 1) + k], X + row * d + k);
-        }
-        cp_async_commit();
-        cp_async_wait<0>();
-        __syncwarp();
-        if (lane < ns) {
-            const T* r = buf + lane * (d + 1);
-            double acc = 0.0;
-            for (int k = 0; k < d; ++k) {
-                const double df = xsub(static_cast<double>(r[k]), cs[k]);
-                acc = xadd(acc, xmul(df, df));
+        for (int g0 = 0; g0 < ns; g0 += kSurv) {
+            const int gn = min(kSurv, ns - g0);
+            __syncwarp();
+            for (int r = 0; r < gn; ++r) {
+                const long long row = __shfl_sync(0xffffffffu, srow, g0 + r);
+                for (int k = lane; k < d; k += 32) cp_async_elem(&buf[r * (d + 1) + k], X + row * d + k);
             }
-            const double old = dist2[srow];
-            if (acc < old) {
-                dist2[srow] = acc;
-                near[srow] = static_cast<uint32_t>(t);
-                if (old < kPosInf) atomicAdd(&csum[srow / kFoldChunk], acc - old);
+            cp_async_commit();
+            cp_async_wait<0>();
+            __syncwarp();
+            if (lane >= g0 && lane < g0 + gn) {
+                const T* r = buf + (lane - g0) * (d + 1);
+                double acc = 0.0;
+                for (int k = 0; k < d; ++k) {
+                    const double df = xsub(static_cast<double>(r[k]), cs[k]);
+                    acc = xadd(acc, xmul(df, df));
+                }
+                const double old = dist2[srow];
+                if (acc < old) {
+                    dist2[srow] = acc;
+                    near[srow] = static_cast<uint32_t>(t);
+                    if (old < kPosInf) atomicAdd(&csum[srow / kFoldChunk], acc - old);
+                }
             }
         }
     }
@@ -1226,8 +1223,7 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     const bool filt = dp <= kFiltMaxQ * 128 && std::getenv("LCN_PP_NOFILTER") == nullptr;
     DevBuf<unsigned char> Xq(filt ? static_cast<size_t>(N) * dp * qsz : 1);
     DevBuf<float2> se(filt ? static_cast<size_t>(N) : 1);
-    const int wbuf_bytes = static_cast<int>(
-        (std::max(static_cast<size_t>(32) * dp * qsz, static_cast<size_t>(32) * (d + 1) * sizeof(T)) + 15) / 16 * 16);
+    const int wbuf_bytes = static_cast<int>((static_cast<size_t>(kSurv) * (d + 1) * sizeof(T) + 15) / 16 * 16);
     const int nq = (dp / 4 + 31) / 32;
     // c32 is read for NQ * 128 entries; the per-warp buffers start 16-aligned
     const size_t fx_smem = (static_cast<size_t>(d) * 8 + (std::max(dp, nq * 128) + 4) * 4 + 15) / 16 * 16 +
