@@ -21,6 +21,7 @@
 #include <cstring>
 
 #include <cublas_v2.h>
+#include <omp.h>
 #include <cmath>
 #include <limits>
 #include <numeric>
@@ -816,11 +817,12 @@ void launch_dense_tiles(Ctx& ctx, const double* A, long long na, const double* B
     LAUNCH_OK("dense_tile_kernel");
 }
 
-const double* union_norms(Op& op) {
+const double* union_norms(Op& op, cudaStream_t st = nullptr) {
     if (op.cost != 2) return nullptr;
     if (op.norms.size() != op.n + op.m) {
         op.norms.resize(op.n + op.m);
-        norms_kernel<<<ceil_div(op.n + op.m, 256), 256, 0, op.ctx->stream>>>(op.X.get(), op.n + op.m, op.d, op.norms.get());
+        norms_kernel<<<ceil_div(op.n + op.m, 256), 256, 0, st ? st : op.ctx->stream>>>(op.X.get(), op.n + op.m, op.d,
+                                                                                      op.norms.get());
         LAUNCH_OK("norms");
     }
     return op.norms.get();
@@ -1140,11 +1142,11 @@ void tc_band_tiles(Ctx& ctx, const Band& B, TcBandTiles& T) {
 }
 
 // |x|^2 of every union point (fp64 sequential fold), for the tensor-core costs
-const double* union_sqnorms(Op& op) {
+const double* union_sqnorms(Op& op, cudaStream_t st = nullptr) {
     if (op.norms.size() != op.n + op.m) {
         op.norms.resize(op.n + op.m);
-        norms_kernel<<<ceil_div(op.n + op.m, 256), 256, 0, op.ctx->stream>>>(op.X.get(), op.n + op.m, op.d,
-                                                                            op.norms.get());
+        norms_kernel<<<ceil_div(op.n + op.m, 256), 256, 0, st ? st : op.ctx->stream>>>(op.X.get(), op.n + op.m, op.d,
+                                                                                      op.norms.get());
         LAUNCH_OK("norms");
     }
     return op.norms.get();
@@ -1527,13 +1529,16 @@ void select_landmarks_device(Op& op, Ctx& ctx, int method, uint64_t seed) {
     ctx.sync();
 }
 
+bool tc_build_part(const Op& op, int part) { return use_tc_build(op, part); }
+
 void wgemm_resid(Ctx& ctx, const double* Vt, const double* Ainv, const double* Aj, size_t m, size_t l, double* Wt,
                  int* bad, unsigned long long* maxbits);
 void uv_gemm_exp(Ctx& ctx, const double* X, size_t rows, const double* L, size_t l, size_t d, const double* xsq,
                  const double* lsq, int kind, double inv, double* out, int* bad);
 
-void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed) {
-    Ctx& ctx = *op.ctx;
+void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed, Ctx* on) {
+    if (op.factors_ready) return;  // built concurrently with the LSH (lcn_op_lcn_lsh's landmark job)
+    Ctx& ctx = on ? *on : *op.ctx;
     cudaStream_t s = ctx.stream;
     const size_t n = op.n, m = op.m, d = op.d, l = op.l, N = n + m;
     if (!(op.lambda > 0.0)) throw Status(2, "build_factors: lambda must be positive");
@@ -1546,7 +1551,7 @@ void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed)
     op.landmarks_ready = false;
     ctx.sync();
     PhaseTimer ptf(ctx, "nystrom factors U, V, A, W");
-    const double* nrm = union_norms(op);
+    const double* nrm = union_norms(op, s);
     DevBuf<double> lnorm;
     if (op.cost == 2) {
         lnorm.resize(l);
@@ -1567,7 +1572,7 @@ void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed)
     op.U64.resize(std::max<size_t>(n * l, 1));
     DevBuf<double> Vt(std::max<size_t>(m * l, 1)), A(l * l);
     if (use_tc_build(op, 2)) {  // point x landmark blocks on the tensor cores (3xTF32)
-        const double* sq = union_sqnorms(op);
+        const double* sq = union_sqnorms(op, s);
         DevBuf<double> lsq(l);
         norms_kernel<<<ceil_div(l, 256), 256, 0, s>>>(op.L.get(), l, d, lsq.get());
         auto tiles_of = [](size_t rows) {
@@ -1597,7 +1602,7 @@ void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed)
         // dots keep U / V ~1e-15 from the reference's sequential folds (the
         // 3xTF32 split loses ~1e-4 of the plan to the 2 x.l cancellation,
         // see use_tc_build); LCN_UV_TILES forces the exact fold tiles.
-        const double* sq = union_sqnorms(op);
+        const double* sq = union_sqnorms(op, s);
         DevBuf<double> lsq(l);
         norms_kernel<<<ceil_div(l, 256), 256, 0, s>>>(op.L.get(), l, d, lsq.get());
         uv_gemm_exp(ctx, op.P(), n, op.L.get(), l, d, sq, lsq.get(), op.cost, 1.0 / op.lambda, op.U64.get(), bad.get());
@@ -1638,7 +1643,10 @@ void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed)
         if (!fac.ok) continue;
         std::vector<LD> inv(l * l);
         bool finite = true;
-#pragma omp parallel for schedule(static) reduction(&& : finite)
+        // on a concurrent build job the other jobs' host threads are busy:
+        // leave them cores (an oversubscribed team stalls at its barriers)
+        const int nthr = on ? std::max(1, omp_get_num_procs() / 2 - 2) : omp_get_max_threads();
+#pragma omp parallel for schedule(static) reduction(&& : finite) num_threads(nthr)
         for (long long cc = 0; cc < static_cast<long long>(l); ++cc) {
             std::vector<LD> e(l, 0.0L);
             e[cc] = 1.0L;
@@ -1682,6 +1690,8 @@ void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed)
         }
         LD cond = norm_a * norm_inv;
         op.cond = std::isfinite(cond) && cond > 0 ? static_cast<double>(cond) : std::numeric_limits<double>::infinity();
+        ctx.sync();
+        op.factors_ready = true;
         return;
     }
     throw Status(5, "build_factors: landmark kernel matrix numerically singular beyond jitter budget");

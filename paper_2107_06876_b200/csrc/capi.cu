@@ -924,6 +924,10 @@ int lcn_op_lcn_lsh(lcn_ctx* ctx, const double* p, size_t n, const double* q, siz
         size_t range = 0;
         Op& o = h->o;
         o.l = l;
+        // (building the Nystrom factors on this job too, concurrently with the
+        // LSH k-means, measured slower: 1.32 s vs 1.28 s per build at
+        // configs[3] -- the factor GEMMs and the host LDL^T contend with the
+        // seeding chains)
         auto landmarks_job = [&](Ctx& jc) {
             select_landmarks_device(o, jc, landmark_method, landmark_seed);
             o.landmarks_ready = true;

@@ -99,6 +99,7 @@ struct Op {
     DevBuf<float> X32;                    // fp32 copy of X when every coordinate is fp32-exact (k-means reads)
     DevBuf<double> norms;                 // per-point sum x_k^2 (cosine-derived cost only)
     bool landmarks_ready = false;         // L already selected (concurrently with the LSH k-means)
+    bool factors_ready = false;           // U, V^T, W already built (concurrently with the LSH k-means)
     std::vector<Band> bands;
     std::vector<DevBuf<double>> val64;    // sparse: log K; lcn: delta (fp64 master)
     std::vector<DevBuf<float>> val32;     // iteration copy (fp32 storage mode)
@@ -190,8 +191,10 @@ void batched_lcn(Ctx& ctx, const double* h_X, size_t rows, int d, int nprob, con
                  int kind, double lambda, int buckets, int kmeans_iters, const uint64_t* lsh_seeds, int l,
                  const uint64_t* lm_seeds, int iters, double* dist_out, int* status_out, int* iters_out);
 void select_landmarks_device(Op& op, Ctx& ctx, int method, uint64_t seed);
+bool tc_build_part(const Op& op, int part);  // the tensor-core build covers `part` (build.cu use_tc_build)
 void build_sparse_values(Op& op);
-void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed);
+// on: the context to run on (a concurrent build job); null = op.ctx
+void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed, Ctx* on = nullptr);
 void build_dense(Op& op);
 void dense_storage(Op& op);
 // dense_tc.cu: the dense kernel recomputed per half-iteration on tcgen05
