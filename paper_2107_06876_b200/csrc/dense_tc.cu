@@ -38,17 +38,33 @@ __device__ __forceinline__ float dense_cost(int kind, float dot, float nx, float
     return kind == 0 ? sqrtf(sq) : sq;
 }
 
-// Ring depth of the recompute kernel: the epilogue reads the accumulators
-// straight from TMEM (no staging tile), so 3 stages of 64 KB fit -- the
-// operand feed is latency-bound at 2 (profiles/dense_tc_r02.json).
-constexpr int kDS = 3;
-constexpr int kDSmem = kDS * kStage + 2 * (kM * 8 + kM * 4) + 1024 + 128;
+// Items are (row tile, pair of column tiles): one UMMA of M = 128, N = 256
+// per k-step, so a stage of 96 KB (the row tile's hi / lo k-block and both
+// column tiles') carries 2 x 128 x 256 x 32 x 3 flop -- 64 flop per byte
+// against 48 for 128-wide tiles; the operand feed, not the tensor pipe, bounds
+// this kernel (profiles/dense_tc_r02.json). The epilogue reads the
+// accumulators straight from TMEM (no staging tile).
+constexpr int kN2 = 2 * kM;                         // UMMA N
+constexpr int kDStage = kKBlock + 2 * kKBlock;      // A k-block + two B k-blocks: 96 KB
+constexpr int kDS = 2;
+constexpr int kDSmem = kDS * kDStage + 2 * (kN2 * 8 + kN2 * 4) + 1024 + 128;
+constexpr uint32_t kIdesc2 = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(kN2 >> 3) << 17) |
+                             (static_cast<uint32_t>(kM >> 4) << 24);
 
-// items: it -> (row tile it / ntb, column tile it % ntb). Epilogue thread =
-// (accumulator row = TMEM lane, half h of the 128 columns): its 64 dots come
-// from two tcgen05.ld's, the per-column log v and |y|^2 of the item from a
-// shared table; the row's (max, sum) over its 64 columns is written as
-// partial 2 ct + h.
+__device__ __forceinline__ void mma2_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(kIdesc2), "r"(acc)
+        : "memory");
+}
+
+// Epilogue thread = (accumulator row = TMEM lane, half h of the 256 columns,
+// i.e. column tile 2 cp + h): its 128 dots from four tcgen05.ld's, the
+// per-column log v and |y|^2 from a shared table; online (max, sum) written
+// as that column tile's partial.
 __global__ void __launch_bounds__(kThreads, 1) dense_lse_tc_kernel(const unsigned char* __restrict__ A,
                                                                    const unsigned char* __restrict__ B, int KB,
                                                                    int nta, int ntb, long long rows, long long cols,
@@ -61,19 +77,20 @@ __global__ void __launch_bounds__(kThreads, 1) dense_lse_tc_kernel(const unsigne
     extern __shared__ __align__(1024) unsigned char dyn_raw[];
     const uint32_t raw = smem_u32(dyn_raw);
     unsigned char* ring = dyn_raw + ((1024u - (raw & 1023u)) & 1023u);
-    double* col_lv = reinterpret_cast<double*>(ring + kDS * kStage);  // [2][kM]
-    float* col_nb = reinterpret_cast<float*>(col_lv + 2 * kM);        // [2][kM]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(col_nb + 2 * kM);
+    double* col_lv = reinterpret_cast<double*>(ring + kDS * kDStage);  // [2][kN2]
+    float* col_nb = reinterpret_cast<float*>(col_lv + 2 * kN2);        // [2][kN2]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(col_nb + 2 * kN2);
     uint64_t* full = bars;
     uint64_t* empty = bars + kDS;
     uint64_t* tfull = bars + 2 * kDS;
     uint64_t* tempty = tfull + kAcc;
     uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(tempty + kAcc);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nitems = nta * ntb;
+    const int ntp = (ntb + 1) / 2;  // column tile pairs
+    const int nitems = nta * ntp;
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
-                     "n"(kAcc * kM)
+                     "n"(kAcc * kN2)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -98,14 +115,22 @@ __global__ void __launch_bounds__(kThreads, 1) dense_lse_tc_kernel(const unsigne
         if (lane == 0) {
             uint32_t g = 0;
             for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-                const unsigned char* a = A + static_cast<size_t>(it / ntb) * tile_bytes;
-                const unsigned char* b = B + static_cast<size_t>(it % ntb) * tile_bytes;
+                const int cp = it % ntp;
+                const unsigned char* a = A + static_cast<size_t>(it / ntp) * tile_bytes;
+                const unsigned char* b0 = B + static_cast<size_t>(2 * cp) * tile_bytes;
+                // an odd last pair reads tile 0 as its second tile (masked in the epilogue)
+                const unsigned char* b1 = 2 * cp + 1 < ntb ? b0 + tile_bytes : B;
                 for (int kb = 0; kb < KB; ++kb, ++g) {
                     const uint32_t s = g % kDS;
                     if (g >= kDS) mbar_wait_spin(&empty[s], ((g / kDS) - 1) & 1);
-                    mbar_arrive_expect_tx(&full[s], kStage);
-                    bulk_g2s(ring + s * kStage, a + static_cast<size_t>(kb) * kKBlock, kKBlock, &full[s]);
-                    bulk_g2s(ring + s * kStage + kKBlock, b + static_cast<size_t>(kb) * kKBlock, kKBlock, &full[s]);
+                    unsigned char* st = ring + s * kDStage;
+                    const size_t ko = static_cast<size_t>(kb) * kKBlock;
+                    mbar_arrive_expect_tx(&full[s], kDStage);
+                    bulk_g2s(st, a + ko, kKBlock, &full[s]);                          // A hi | A lo
+                    bulk_g2s(st + kKBlock, b0 + ko, kHalf, &full[s]);                 // B0 hi
+                    bulk_g2s(st + kKBlock + kHalf, b1 + ko, kHalf, &full[s]);         // B1 hi
+                    bulk_g2s(st + 2 * kKBlock, b0 + ko + kHalf, kHalf, &full[s]);     // B0 lo
+                    bulk_g2s(st + 2 * kKBlock + kHalf, b1 + ko + kHalf, kHalf, &full[s]);  // B1 lo
                 }
             }
         }
@@ -115,20 +140,20 @@ __global__ void __launch_bounds__(kThreads, 1) dense_lse_tc_kernel(const unsigne
             const uint32_t buf = j % kAcc;
             if (j >= kAcc) mbar_wait_spin(&tempty[buf], ((j / kAcc) - 1) & 1);
             fence_after();
-            const uint32_t dt = tmem + buf * kM;
+            const uint32_t dt = tmem + buf * kN2;
             for (int kb = 0; kb < KB; ++kb, ++g) {
                 const uint32_t s = g % kDS;
                 mbar_wait_spin(&full[s], (g / kDS) & 1);
                 fence_after();
-                const uint32_t base = smem_u32(ring + s * kStage);
+                const uint32_t base = smem_u32(ring + s * kDStage);
                 const uint64_t ah = desc_sw128(base), al = desc_sw128(base + kHalf);
-                const uint64_t bh = desc_sw128(base + kKBlock), bl = desc_sw128(base + kKBlock + kHalf);
+                const uint64_t bh = desc_sw128(base + kKBlock), bl = desc_sw128(base + 2 * kKBlock);
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks) {
                     const uint64_t off = static_cast<uint64_t>(ks * 32) >> 4;
-                    mma_ss_elect(dt, ah + off, bh + off, (kb | ks) ? 1u : 0u);
-                    mma_ss_elect(dt, ah + off, bl + off, 1u);
-                    mma_ss_elect(dt, al + off, bh + off, 1u);
+                    mma2_elect(dt, ah + off, bh + off, (kb | ks) ? 1u : 0u);
+                    mma2_elect(dt, ah + off, bl + off, 1u);
+                    mma2_elect(dt, al + off, bh + off, 1u);
                 }
                 commit_elect(&empty[s]);
             }
@@ -138,46 +163,44 @@ __global__ void __launch_bounds__(kThreads, 1) dense_lse_tc_kernel(const unsigne
     } else {
         const int q = warp & 3;
         const int row = 32 * q + lane;
-        const int h = (warp - 2) >> 2;  // column half
-        const int c0 = h * kEpiCols;
+        const int h = (warp - 2) >> 2;  // column tile of the pair
         const int et = tid - 64;        // 0..255
         const float finv = static_cast<float>(inv);
         uint32_t j = 0;
         for (int it = blockIdx.x; it < nitems; it += gridDim.x, ++j) {
             const uint32_t buf = j % kAcc;
-            const int at = it / ntb, ct = it % ntb;
-            const int cb = j & 1;  // column-table buffer (the previous item may still be reading the other)
-            if (et < kM) {
-                const long long c = static_cast<long long>(ct) * kM + et;
-                col_lv[cb * kM + et] = c < cols ? lv[c] : kNegInf;
-                col_nb[cb * kM + et] = c < cols ? static_cast<float>(nb[c]) : 0.0f;
+            const int at = it / ntp, cp = it % ntp;
+            const int cb = j & 1;  // column-table buffer (the previous item may still read the other)
+            {
+                const long long c = static_cast<long long>(cp) * kN2 + et;
+                col_lv[cb * kN2 + et] = c < cols ? lv[c] : kNegInf;
+                col_nb[cb * kN2 + et] = c < cols ? static_cast<float>(nb[c]) : 0.0f;
             }
             const long long gr = static_cast<long long>(at) * kM + row;
             const float nx = gr < rows ? static_cast<float>(na[gr]) : 0.0f;
             asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");  // column table visible
             mbar_wait_spin(&tfull[buf], (j / kAcc) & 1);
             fence_after();
-            const uint32_t ta = tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * kM + c0;
-            const double* tl = col_lv + cb * kM + c0;
-            const float* tn = col_nb + cb * kM + c0;
-            // online (max, sum): one pass, nothing stored per column
+            const uint32_t ta = tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * kN2 + h * kM;
+            const double* tl = col_lv + cb * kN2 + h * kM;
+            const float* tn = col_nb + cb * kN2 + h * kM;
             double mx = kNegInf;
             float sum = 0.0f;
 #pragma unroll
-            for (int half = 0; half < 2; ++half) {
+            for (int part = 0; part < 4; ++part) {
                 uint32_t v[32];
-                ld32(ta + 32 * half, v);
+                ld32(ta + 32 * part, v);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (half == 1) {
+                if (part == 3) {
                     fence_before();
-                    mbar_arrive(&tempty[buf]);  // accumulator free for the item after next
+                    mbar_arrive(&tempty[buf]);
                 }
 #pragma unroll
                 for (int c = 0; c < 32; ++c) {
-                    const double l = tl[32 * half + c];
+                    const double l = tl[32 * part + c];
                     if (l == kNegInf) continue;
-                    const double x = l - static_cast<double>(dense_cost(kind, __uint_as_float(v[c]), nx,
-                                                                        tn[32 * half + c]) * finv);
+                    const double x =
+                        l - static_cast<double>(dense_cost(kind, __uint_as_float(v[c]), nx, tn[32 * part + c]) * finv);
                     if (x > mx) {
                         sum = sum * __expf(static_cast<float>(mx - x)) + 1.0f;
                         mx = x;
@@ -186,9 +209,10 @@ __global__ void __launch_bounds__(kThreads, 1) dense_lse_tc_kernel(const unsigne
                     }
                 }
             }
-            if (gr < rows) {
-                PM[(gr * ntb + ct) * 2 + h] = mx;
-                PS[(gr * ntb + ct) * 2 + h] = static_cast<double>(sum);
+            const int ct = 2 * cp + h;
+            if (gr < rows && ct < ntb) {
+                PM[gr * ntb + ct] = mx;
+                PS[gr * ntb + ct] = static_cast<double>(sum);
             }
         }
     }
@@ -196,7 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_lse_tc_kernel(const unsigne
     __syncthreads();
     if (warp == 1) {
         fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kAcc * kM) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kAcc * kN2) : "memory");
     }
 }
 
@@ -251,7 +275,7 @@ void dense_tc_prepare(Op& op) {
         op.X.get(), d, d, nullptr, dt.get(), KB, nullptr, op.dtc_tiles.get());
     op.dtc_norm.resize(static_cast<size_t>(n + m));
     sqnorm_kernel<<<ceil_div(n + m, 256), 256, 0, s>>>(op.X.get(), n + m, d, op.dtc_norm.get());
-    op.dtc_pm.resize(static_cast<size_t>(2 * std::max(n * op.dtc_ntb, m * op.dtc_nta)));
+    op.dtc_pm.resize(static_cast<size_t>(std::max(n * op.dtc_ntb, m * op.dtc_nta)));
     op.dtc_ps.resize(op.dtc_pm.size());
     LAUNCH_OK("dense recompute operands");
     ctx.sync();
@@ -278,12 +302,12 @@ void dense_tc_lse(Op& op, bool transposed, const double* lv, const int* done, do
     const long long rows = transposed ? m : n, cols = transposed ? n : m;
     const double* na = op.dtc_norm.get() + (transposed ? n : 0);
     const double* nb = op.dtc_norm.get() + (transposed ? 0 : n);
-    const int grid = std::min(nta * ntb, ctx.num_sms);
+    const int grid = std::min(nta * ((ntb + 1) / 2), ctx.num_sms);
     dense_lse_tc_kernel<<<grid, kThreads, kDSmem, ctx.stream>>>(transposed ? Q : P, transposed ? P : Q, KB, nta, ntb,
                                                                rows, cols, na, nb, op.cost, 1.0 / op.lambda, lv, done,
                                                                op.dtc_pm.get(), op.dtc_ps.get());
-    lse_merge_kernel<<<ceil_div(rows, 256), 256, 0, ctx.stream>>>(op.dtc_pm.get(), op.dtc_ps.get(), rows, 2 * ntb,
-                                                                  done, M, S);
+    lse_merge_kernel<<<ceil_div(rows, 256), 256, 0, ctx.stream>>>(op.dtc_pm.get(), op.dtc_ps.get(), rows, ntb, done,
+                                                                  M, S);
 }
 
 }  // namespace lcnb
