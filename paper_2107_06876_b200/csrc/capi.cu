@@ -298,7 +298,9 @@ void shard_lcn(Op& o, std::vector<DevBuf<uint32_t>>& ids, size_t range, const do
     st->m_glob = m;
     st->n_own = R.n_own;
     st->m_own = R.m_own;
-    st->nnz_glob = global_support(is, it, n, m, bands);
+    st->bands = bands;
+    st->ids_src = is;  // the support size is computed on first request (lcn_op_get_info)
+    st->ids_tgt = it;
     st->src_glob = R.src;
     st->tgt_glob = R.tgt;
     st->n_halo = R.src.size() - R.n_own;
@@ -1183,7 +1185,17 @@ int lcn_op_get_info(const lcn_op* op, lcn_op_info_t* info) {
         info->streamed = 0;
         for (const auto& I : o.iter) info->streamed += I.real[1];
     }
-    if (o.shard) info->nnz = o.shard->nnz_glob;  // stored / streamed stay this rank's
+    if (o.shard) {  // stored / streamed stay this rank's
+        ShardState& sh = *const_cast<Op&>(o).shard;
+        if (!sh.ids_src.empty()) {
+            sh.nnz_glob = global_support(sh.ids_src, sh.ids_tgt, sh.n_glob, sh.m_glob, sh.bands);
+            sh.ids_src.clear();
+            sh.ids_src.shrink_to_fit();
+            sh.ids_tgt.clear();
+            sh.ids_tgt.shrink_to_fit();
+        }
+        info->nnz = sh.nnz_glob;
+    }
     return LCN_OK;
 }
 

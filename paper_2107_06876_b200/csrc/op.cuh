@@ -70,7 +70,9 @@ struct ShardState {
     int rank = 0, world = 1;
     size_t n_glob = 0, m_glob = 0;
     uint32_t n_own = 0, m_own = 0;
-    unsigned long long nnz_glob = 0;  // support of the whole problem
+    unsigned long long nnz_glob = 0;  // support of the whole problem (lazy: ids_src / ids_tgt kept until asked)
+    std::vector<uint32_t> ids_src, ids_tgt;  // bands x n, bands x m (host), for nnz_glob
+    int bands = 0;
     std::vector<uint32_t> src_glob, tgt_glob;  // local -> global
     DevBuf<uint32_t> d_src_glob, d_tgt_glob;
     // exchange: exported local indices (slot order) and, per halo point, the

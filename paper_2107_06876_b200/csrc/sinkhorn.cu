@@ -2446,12 +2446,18 @@ struct Solver {
     void finish_shard(const DevState& h, const std::vector<double>& gq, Result& res) {
         const int fin = h.iters % 2;
         const int W = sh->world;
-        size_t F = 1;
-        for (int r = 0; r < W; ++r) F = std::max(F, 2 * sh->own_src_all[r].size() + sh->own_tgt_all[r].size());
+        // record: [distance partial | log s | P1 | log t] of the owned points
+        size_t F = 2;
+        for (int r = 0; r < W; ++r) F = std::max(F, 1 + 2 * sh->own_src_all[r].size() + sh->own_tgt_all[r].size());
         DevBuf<double> fs(F), fr(F * W);
-        CUDA_OK(cudaMemcpyAsync(fs.get(), log_s[fin].get(), n_own * 8, cudaMemcpyDeviceToDevice, s));
-        CUDA_OK(cudaMemcpyAsync(fs.get() + n_own, row_marg.get(), n_own * 8, cudaMemcpyDeviceToDevice, s));
-        CUDA_OK(cudaMemcpyAsync(fs.get() + 2 * n_own, log_t.get(), m_own * 8, cudaMemcpyDeviceToDevice, s));
+        // this rank's <log s, P1> + <log t, q> over its owned points (deterministic block partials)
+        const int DB = 64;
+        dot_partial_kernel<<<DB, 256, 0, s>>>(log_s[fin].get(), row_marg.get(), n_own, dpart.get());
+        dot_partial_kernel<<<DB, 256, 0, s>>>(log_t.get(), qv.get(), m_own, dpart.get() + DB);
+        sum_partial_kernel<<<1, 256, 0, s>>>(dpart.get(), 2 * DB, fs.get());
+        CUDA_OK(cudaMemcpyAsync(fs.get() + 1, log_s[fin].get(), n_own * 8, cudaMemcpyDeviceToDevice, s));
+        CUDA_OK(cudaMemcpyAsync(fs.get() + 1 + n_own, row_marg.get(), n_own * 8, cudaMemcpyDeviceToDevice, s));
+        CUDA_OK(cudaMemcpyAsync(fs.get() + 1 + 2 * n_own, log_t.get(), m_own * 8, cudaMemcpyDeviceToDevice, s));
         comm->allgather(fs.get(), fr.get(), F * sizeof(double), s);
         std::vector<double> hr(F * W);
         fr.download(hr.data(), F * W, s);
@@ -2460,20 +2466,23 @@ struct Solver {
         res.log_s.assign(N, 0.0);
         res.row_marg.assign(N, 0.0);
         res.log_t.assign(M, 0.0);
+        double acc = 0.0;
         for (int r = 0; r < W; ++r) {
             const std::vector<uint32_t>& os = sh->own_src_all[r];
             const std::vector<uint32_t>& ot = sh->own_tgt_all[r];
             const double* rec = hr.data() + static_cast<size_t>(r) * F;
-            for (size_t k = 0; k < os.size(); ++k) {
-                res.log_s[os[k]] = rec[k];
-                res.row_marg[os[k]] = rec[os.size() + k];
+            acc += rec[0];  // rank order: the same sum on every rank
+            const long long ns = static_cast<long long>(os.size()), nt = static_cast<long long>(ot.size());
+#pragma omp parallel for schedule(static) if (ns > 65536)
+            for (long long k = 0; k < ns; ++k) {
+                res.log_s[os[k]] = rec[1 + k];
+                res.row_marg[os[k]] = rec[1 + ns + k];
             }
-            for (size_t k = 0; k < ot.size(); ++k) res.log_t[ot[k]] = rec[2 * os.size() + k];
+#pragma omp parallel for schedule(static) if (nt > 65536)
+            for (long long k = 0; k < nt; ++k) res.log_t[ot[k]] = rec[1 + 2 * ns + k];
         }
-        // distance = lambda (<log s, P1> + <log t, q>) (sinkhorn.cpp:178-183)
-        double acc = 0.0;
-        for (size_t i = 0; i < N; ++i) acc += res.log_s[i] * res.row_marg[i];
-        for (size_t j = 0; j < M; ++j) acc += res.log_t[j] * gq[j];
+        (void)gq;
+        // distance = lambda (<log s, P1> + <log t, q>) (sinkhorn.cpp:178-183), per-rank partials
         res.distance = op.lambda * acc;
         res.n = N;
         res.m = M;
