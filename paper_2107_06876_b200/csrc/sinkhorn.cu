@@ -119,39 +119,69 @@ __global__ void __launch_bounds__(kThreads) sparse_row_band_kernel(const DevStat
         for (uint32_t c = threadIdx.x; c < cn; c += kThreads) lt[c] = log_t[bv.tgt_order[tb + c0 + c]];
         __syncthreads();
         if constexpr (sizeof(T) == 4) {
-            // fp32 storage: 4 rows per warp at a time (4 x the loads in
-            // flight), exponents in fp32 (MUFU), each row's sum widened once;
-            // the second read of the rows hits L1
+            // fp32 storage: the tile's log t as fp32 in shared memory (-inf
+            // past the bucket, so padded row ends drop out), 16-byte loads,
+            // 4 rows per warp at a time (4 x the loads in flight), exponents
+            // in fp32 (MUFU), each row's sum widened once; the second read of
+            // the rows hits L1 / L2
+            __shared__ __align__(16) float ltf[kTile];
+            const uint32_t cn4 = (cn + 3) & ~3u;
+            for (uint32_t c = threadIdx.x; c < cn4; c += kThreads)
+                ltf[c] = c < cn ? static_cast<float>(lt[c]) : -CUDART_INF_F;
+            __syncthreads();
             constexpr int kRW = 4;
             for (uint32_t r0w = warp * kRW; r0w < nb; r0w += kWarps * kRW) {
+                const float* rp[kRW];
+                bool rv[kRW];
+#pragma unroll
+                for (int k = 0; k < kRW; ++k) {
+                    rv[k] = r0w + k < nb;
+                    rp[k] = vals + off + static_cast<unsigned long long>(rv[k] ? r0w + k : r0w) * ms + c0;
+                }
+                // one read: per lane an online (max, sum) per row, merged
+                // across the warp at the end
                 float hf[kRW], af[kRW];
 #pragma unroll
                 for (int k = 0; k < kRW; ++k) {
                     hf[k] = -CUDART_INF_F;
                     af[k] = 0.0f;
                 }
-                for (uint32_t c = lane; c < cn; c += 32) {
-                    const float l = static_cast<float>(lt[c]);
+                for (uint32_t c = 4 * lane; c < cn4; c += 128) {
+                    const float4 l4 = *reinterpret_cast<const float4*>(ltf + c);
 #pragma unroll
-                    for (int k = 0; k < kRW; ++k)
-                        if (r0w + k < nb) hf[k] = fmaxf(hf[k], vals[off + (r0w + k) * ms + c0 + c] + l);
+                    for (int k = 0; k < kRW; ++k) {
+                        const float4 v = __ldg(reinterpret_cast<const float4*>(rp[k] + c));
+                        const float x0 = v.x + l4.x, x1 = v.y + l4.y, x2 = v.z + l4.z, x3 = v.w + l4.w;
+                        const float mx = fmaxf(fmaxf(x0, x1), fmaxf(x2, x3));
+                        if (mx > hf[k]) {  // new running max: rescale the sum once
+                            af[k] *= __expf(hf[k] - mx);
+                            hf[k] = mx;
+                        }
+                        if (hf[k] != -CUDART_INF_F)
+                            af[k] += (__expf(x0 - hf[k]) + __expf(x1 - hf[k])) + (__expf(x2 - hf[k]) + __expf(x3 - hf[k]));
+                    }
                 }
 #pragma unroll
-                for (int k = 0; k < kRW; ++k) hf[k] = warp_max(hf[k]);
-                for (uint32_t c = lane; c < cn; c += 32) {
-                    const float l = static_cast<float>(lt[c]);
+                for (int k = 0; k < kRW; ++k) {  // warp merge of the lanes' (max, sum)
 #pragma unroll
-                    for (int k = 0; k < kRW; ++k)
-                        if (r0w + k < nb && hf[k] != -CUDART_INF_F)
-                            af[k] += __expf(vals[off + (r0w + k) * ms + c0 + c] + l - hf[k]);
+                    for (int o = 16; o; o >>= 1) {
+                        const float ho = __shfl_xor_sync(0xffffffffu, hf[k], o);
+                        const float ao = __shfl_xor_sync(0xffffffffu, af[k], o);
+                        const float hn = fmaxf(hf[k], ho);
+                        if (hn != -CUDART_INF_F) {
+                            af[k] = af[k] * __expf(hf[k] - hn) + ao * __expf(ho - hn);
+                            hf[k] = hn;
+                        }
+                    }
                 }
-#pragma unroll
-                for (int k = 0; k < kRW; ++k) af[k] = warp_sum(af[k]);
-                if (lane < kRW && r0w + lane < nb) {
+                if (lane < kRW && rv[lane & (kRW - 1)]) {
                     float h = hf[0], a = af[0];
 #pragma unroll
                     for (int k = 1; k < kRW; ++k)
-                        if (lane == k) { h = hf[k]; a = af[k]; }
+                        if (lane == k) {
+                            h = hf[k];
+                            a = af[k];
+                        }
                     const uint32_t i = bv.src_order[sb + r0w + lane];
                     double M = Mrow[i], S = Srow[i];
                     lse_merge(M, S, h == -CUDART_INF_F ? kNegInf : static_cast<double>(h), static_cast<double>(a));
