@@ -15,7 +15,8 @@ from typing import Optional
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_build", "liblcn_b200.so")
+LIB_PATH = os.environ.get("LCN_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_build",
+                                                         "liblcn_b200.so")  # LCN_LIB_PATH: a profiling build
 
 
 # ---- error types (error.hpp:8-38) -------------------------------------------
