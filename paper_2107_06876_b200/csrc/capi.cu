@@ -305,6 +305,13 @@ void shard_lcn(Op& o, std::vector<DevBuf<uint32_t>>& ids, size_t range, const do
     st->tgt_glob = R.tgt;
     st->n_halo = R.src.size() - R.n_own;
     st->m_halo = R.tgt.size() - R.m_own;
+    // a rank with no local point on a side (more ranks than band-0 groups, or
+    // one-sided groups) gets one phantom point there, after the halo, in no
+    // shared bucket: the local operator is never empty, and the phantom is
+    // neither owned nor imported, so nothing reads its values
+    const bool ph_s = R.src.empty(), ph_t = R.tgt.empty();
+    if (ph_s) st->src_glob.push_back(0u);
+    if (ph_t) st->tgt_glob.push_back(0u);
     st->n_exp_s = R.exp_s.size();
     st->n_exp_t = R.exp_t.size();
     st->max_exp_s = P.max_exp_s;
@@ -325,8 +332,8 @@ void shard_lcn(Op& o, std::vector<DevBuf<uint32_t>>& ids, size_t range, const do
         dst.resize(std::max<size_t>(v.size(), 1));
         if (!v.empty()) dst.upload(v.data(), v.size(), s);
     };
-    up(st->d_src_glob, R.src);
-    up(st->d_tgt_glob, R.tgt);
+    up(st->d_src_glob, st->src_glob);
+    up(st->d_tgt_glob, st->tgt_glob);
     up(st->exp_s, R.exp_s);
     up(st->exp_t, R.exp_t);
     up(st->imp_s_rank, R.imp_s_rank);
@@ -334,7 +341,7 @@ void shard_lcn(Op& o, std::vector<DevBuf<uint32_t>>& ids, size_t range, const do
     up(st->imp_t_rank, R.imp_t_rank);
     up(st->imp_t_slot, R.imp_t_slot);
     // local points: sources then targets of the local union
-    const long long nl = static_cast<long long>(R.src.size()), ml = static_cast<long long>(R.tgt.size());
+    const long long nl = static_cast<long long>(st->src_glob.size()), ml = static_cast<long long>(st->tgt_glob.size());
     const int gb = static_cast<int>(std::min<long long>(ceil_div((nl + ml) * static_cast<long long>(d), 256), 8LL * ctx.num_sms)) + 1;
     DevBuf<double> X(std::max<size_t>((nl + ml) * d, 1));
     gather_points_kernel<double><<<gb, 256, 0, s>>>(o.X.get(), st->d_src_glob.get(), nl, static_cast<int>(d), 0, X.get());
@@ -358,6 +365,13 @@ void shard_lcn(Op& o, std::vector<DevBuf<uint32_t>>& ids, size_t range, const do
                                              ht, lids[b].get() + nl);
     }
     LAUNCH_OK("shard gather");
+    // phantoms: their own bucket in every later band (range + 1; band 0 has
+    // the one-sided halo buckets already)
+    for (int b = 1; b < bands; ++b) {
+        const uint32_t lone = static_cast<uint32_t>(range + 1);
+        if (ph_s) CUDA_OK(cudaMemcpyAsync(lids[b].get() + nl - 1, &lone, 4, cudaMemcpyHostToDevice, s));
+        if (ph_t) CUDA_OK(cudaMemcpyAsync(lids[b].get() + nl + ml - 1, &lone, 4, cudaMemcpyHostToDevice, s));
+    }
     ctx.sync();
     ids.clear();
     o.X = std::move(X);
