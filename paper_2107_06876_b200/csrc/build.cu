@@ -2132,7 +2132,8 @@ void finalize_storage(Op& op) {
     op.lp = (op.l + 3) & ~size_t(3);
     // compact bands (build_iter_layout) get panel arrays instead of block copies
     auto compact = [&](size_t b) {
-        return op.kind == 3 && !op.fp64 && b > 0 && op.bands[b].n_work > 0 && env_uint("LCN_PANELS", 1) != 0;
+        return (op.kind == 3 || op.kind == 1) && !op.fp64 && b > 0 && op.bands[b].n_work > 0 &&
+               env_uint("LCN_PANELS", 1) != 0;
     };
     if (!op.fp64) {
         op.val32.clear();
@@ -2173,7 +2174,8 @@ void finalize_storage(Op& op) {
             }
             LAUNCH_OK("transpose_blocks");
         }
-        if (op.kind == 3) build_iter_layout(op);
+        // the LCN band passes and the sparse operator's log-sum-exp passes (fp32)
+        if (op.kind == 3 || !op.fp64) build_iter_layout(op);
     }
     if (op.kind >= 2) {
         if (op.fp64) {

@@ -714,8 +714,34 @@ __device__ __forceinline__ int band_rows_per_stage(uint32_t ws) {
 // Split-output epilogue: partials of `count` outputs are in scratch at
 // base + piece * count; the last piece to arrive sums them in order into
 // corr[outi[c]]. Called by all consumer threads after they wrote their partials.
+// log-sum-exp partials travel as a float2 (max, sum) in one double slot
+__device__ __forceinline__ double pack_ms(float m, float s) {
+    return __longlong_as_double(static_cast<long long>(__float_as_uint(m)) |
+                                (static_cast<long long>(__float_as_uint(s)) << 32));
+}
+__device__ __forceinline__ float2 unpack_ms(double v) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+    return make_float2(__uint_as_float(static_cast<unsigned>(b)), __uint_as_float(static_cast<unsigned>(b >> 32)));
+}
+// merge (m, s) into the output's running (M, S) (lse_merge in fp64)
+__device__ __forceinline__ void lse_store(double* __restrict__ Mo, double* __restrict__ So, uint32_t i, float m, float s) {
+    if (m == -CUDART_INF_F) return;
+    double M = Mo[i], S = So[i];
+    const double mm = static_cast<double>(m);
+    if (mm > M) {
+        S = S * exp(M - mm) + static_cast<double>(s);
+        M = mm;
+    } else {
+        S += static_cast<double>(s) * exp(mm - M);
+    }
+    Mo[i] = M;
+    So[i] = S;
+}
+
+template <bool LSE>
 __device__ __forceinline__ void band_combine(BandSmem& sm, const BandWork& wk, const ItemMeta& mt, uint32_t count,
-                                             const uint32_t* outi, double* __restrict__ corr, int tid) {
+                                             const uint32_t* outi, double* __restrict__ corr, double* __restrict__ Sout,
+                                             int tid) {
     __threadfence();
     consumers_sync();
     if (tid == 0) sm.last = atomicAdd(&wk.counters[mt.split >> 8], 1u) == mt.pieces - 1;
@@ -724,9 +750,24 @@ __device__ __forceinline__ void band_combine(BandSmem& sm, const BandWork& wk, c
         __threadfence();
         const double* base = mt.part - static_cast<size_t>(mt.split & 0xffu) * count;  // piece 0
         for (uint32_t c = tid; c < count; c += kThreads) {
-            double v = 0.0;
-            for (uint32_t k = 0; k < mt.pieces; ++k) v += __ldcg(base + static_cast<size_t>(k) * count + c);
-            corr[outi[c]] = v;
+            if constexpr (LSE) {
+                float m = -CUDART_INF_F, sum = 0.0f;
+                for (uint32_t k = 0; k < mt.pieces; ++k) {
+                    const float2 ms = unpack_ms(__ldcg(base + static_cast<size_t>(k) * count + c));
+                    if (ms.x == -CUDART_INF_F) continue;
+                    if (ms.x > m) {
+                        sum = sum * __expf(m - ms.x) + ms.y;
+                        m = ms.x;
+                    } else {
+                        sum += ms.y * __expf(ms.x - m);
+                    }
+                }
+                lse_store(corr, Sout, outi[c], m, sum);
+            } else {
+                double v = 0.0;
+                for (uint32_t k = 0; k < mt.pieces; ++k) v += __ldcg(base + static_cast<size_t>(k) * count + c);
+                corr[outi[c]] = v;
+            }
         }
         if (tid == 0) wk.counters[mt.split >> 8] = 0u;
     }
@@ -735,11 +776,16 @@ __device__ __forceinline__ void band_combine(BandSmem& sm, const BandWork& wk, c
 // ROWS selects the row pass (transposed blocks). logv: the band's
 // bucket-ordered copy of the stream side's log vector (log t for the row pass,
 // log s for the column pass), written by the low-rank pass that produced it.
-template <typename T, bool ROWS>
+// LSE (the sparse operator's log-domain passes, sparse_kernel.cpp:119-155):
+// vals are log K, the stream vector enters as log v, and each output gets a
+// (max, sum exp(. - max)) merged into (corr = M, Sout = S); otherwise the
+// linear LCN correction product.
+template <typename T, bool ROWS, bool LSE = false>
 __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const DevState* __restrict__ st,
                                                                       const uint32_t* __restrict__ o_order, BandWork wk, const T* __restrict__ vals,
                                                                       const double* __restrict__ logv,
-                                                                      double* __restrict__ corr) {
+                                                                      double* __restrict__ corr,
+                                                                      double* __restrict__ Sout = nullptr) {
     if (st->done) return;
     extern __shared__ __align__(128) unsigned char dyn[];
     BandSmem& sm = *reinterpret_cast<BandSmem*>(dyn);
@@ -861,7 +907,9 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
                 for (int k = 0; k < 8; ++k) {
                     const uint32_t c = c0 + 32u * k;
                     if (c < item.ns) {
-                        if constexpr (sizeof(T) == 4)  // fp32 storage: the scalings enter fp32 products
+                        if constexpr (LSE)  // log domain: the stream value itself
+                            reinterpret_cast<float*>(sm.vec[slot])[c] = static_cast<float>(x[k]);
+                        else if constexpr (sizeof(T) == 4)  // fp32 storage: the scalings enter fp32 products
                             reinterpret_cast<float*>(sm.vec[slot])[c] = static_cast<float>(exp(x[k] - H));
                         else
                             sm.vec[slot][c] = exp(x[k] - H);
@@ -904,6 +952,8 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
         const uint32_t g = static_cast<uint32_t>(tid) / nq, q = static_cast<uint32_t>(tid) % nq;
         const bool own = g < ng;
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        float lm[4] = {-CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F};  // LSE: running max / sum
+        float ls[4] = {0.0f, 0.0f, 0.0f, 0.0f};
         const uint32_t* outi = sm.out[slot];
         for (uint32_t r0 = 0; r0 < mt.ns; r0 += R) {
             const uint32_t nr = mt.ns - r0 < static_cast<uint32_t>(R) ? mt.ns - r0 : static_cast<uint32_t>(R);
@@ -911,7 +961,48 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
             const T* blk = reinterpret_cast<const T*>(sm.ring[stage]);
             if (own) {
                 const T* p = blk + 4 * q;
-                if constexpr (sizeof(T) == 4) {
+                if constexpr (LSE) {
+                    // log domain: per output the chunk's max, then the sum of
+                    // exp(log K + log v - max) with the running sum rescaled
+                    // once per chunk (two reads of the staged chunk)
+                    const float* vf = reinterpret_cast<const float*>(sm.vec[slot]) + r0;
+                    float cm[4] = {-CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F};
+#pragma unroll 4
+                    for (uint32_t r = g; r < nr; r += ng) {
+                        const float4 x = *reinterpret_cast<const float4*>(p + r * ws);
+                        const float sr = vf[r];
+                        cm[0] = fmaxf(cm[0], x.x + sr);
+                        cm[1] = fmaxf(cm[1], x.y + sr);
+                        cm[2] = fmaxf(cm[2], x.z + sr);
+                        cm[3] = fmaxf(cm[3], x.w + sr);
+                    }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (cm[k] > lm[k]) {
+                            ls[k] *= __expf(lm[k] - cm[k]);
+                            lm[k] = cm[k];
+                        }
+                    if (lm[0] != -CUDART_INF_F || lm[1] != -CUDART_INF_F || lm[2] != -CUDART_INF_F ||
+                        lm[3] != -CUDART_INF_F) {
+                        // an output whose max is still -inf has only -inf entries:
+                        // offset 0 keeps exp(-inf - 0) = 0 instead of NaN
+                        const float o0 = lm[0] == -CUDART_INF_F ? 0.0f : lm[0];
+                        const float o1 = lm[1] == -CUDART_INF_F ? 0.0f : lm[1];
+                        const float o2 = lm[2] == -CUDART_INF_F ? 0.0f : lm[2];
+                        const float o3 = lm[3] == -CUDART_INF_F ? 0.0f : lm[3];
+                        float e0 = 0.0f, e1 = 0.0f, e2 = 0.0f, e3 = 0.0f;
+#pragma unroll 4
+                        for (uint32_t r = g; r < nr; r += ng) {
+                            const float4 x = *reinterpret_cast<const float4*>(p + r * ws);
+                            const float sr = vf[r];
+                            e0 += __expf(x.x + sr - o0);
+                            e1 += __expf(x.y + sr - o1);
+                            e2 += __expf(x.z + sr - o2);
+                            e3 += __expf(x.w + sr - o3);
+                        }
+                        ls[0] += e0; ls[1] += e1; ls[2] += e2; ls[3] += e3;
+                    }
+                } else if constexpr (sizeof(T) == 4) {
                     // fp32 products and per-chunk partials, widened once per chunk
                     const float* vf = reinterpret_cast<const float*>(sm.vec[slot]) + r0;
                     float f0 = 0.0f, f1 = 0.0f, f2 = 0.0f, f3 = 0.0f;
@@ -943,17 +1034,42 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
         // combine the groups: red[g * ws + c], one thread per output
         if (own) {
             double* o = sm.red + g * ws + 4 * q;
-            o[0] = a0; o[1] = a1; o[2] = a2; o[3] = a3;
+            if constexpr (LSE) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    // -inf entries (masked duplicates) leave the sum at exactly 0
+                    if (lm[k] == -CUDART_INF_F) ls[k] = 0.0f;
+                    o[k] = pack_ms(lm[k], ls[k]);
+                }
+            } else {
+                o[0] = a0; o[1] = a1; o[2] = a2; o[3] = a3;
+            }
         }
         consumers_sync();
         double* part = mt.part;
         for (uint32_t c = tid; c < mt.ow; c += kThreads) {
-            double v = 0.0;
-            for (uint32_t gg = 0; gg < ng; ++gg) v += sm.red[gg * ws + c];
-            if (part) part[c] = v;
-            else corr[outi[c]] = v;
+            if constexpr (LSE) {
+                float m = -CUDART_INF_F, sum = 0.0f;
+                for (uint32_t gg = 0; gg < ng; ++gg) {
+                    const float2 ms = unpack_ms(sm.red[gg * ws + c]);
+                    if (ms.x == -CUDART_INF_F) continue;
+                    if (ms.x > m) {
+                        sum = sum * __expf(m - ms.x) + ms.y;
+                        m = ms.x;
+                    } else {
+                        sum += ms.y * __expf(ms.x - m);
+                    }
+                }
+                if (part) part[c] = pack_ms(m, sum);
+                else lse_store(corr, Sout, outi[c], m, sum);
+            } else {
+                double v = 0.0;
+                for (uint32_t gg = 0; gg < ng; ++gg) v += sm.red[gg * ws + c];
+                if (part) part[c] = v;
+                else corr[outi[c]] = v;
+            }
         }
-        if (part) band_combine(sm, wk, mt, mt.ow, outi, corr, tid);
+        if (part) band_combine<LSE>(sm, wk, mt, mt.ow, outi, corr, Sout, tid);
         consumers_sync();  // red is rewritten by the next item
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.vempty[slot]);
@@ -1890,7 +2006,7 @@ struct Solver {
                 CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lowrank_pass_kernel<float, 2, 0>, kThreads + 64, smem));
         }
         G = std::max(1, occ) * ctx.num_sms;
-        if (op.kind == 3) init_band_stream();
+        if (op.kind == 3 || lse_stream()) init_band_stream();
         if (op.kind == 0) {
             const int bytes = static_cast<int>(sizeof(LseSmem));
             CUDA_OK(cudaFuncSetAttribute(dense_lse_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
@@ -1917,6 +2033,10 @@ struct Solver {
     void init_band_stream() {
         const int bytes = static_cast<int>(sizeof(BandSmem));
         CUDA_OK(cudaFuncSetAttribute(band_stream_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        CUDA_OK(cudaFuncSetAttribute(band_stream_kernel<float, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     bytes));
+        CUDA_OK(cudaFuncSetAttribute(band_stream_kernel<float, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     bytes));
         CUDA_OK(cudaFuncSetAttribute(band_stream_kernel<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
         CUDA_OK(cudaFuncSetAttribute(band_stream_kernel<double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
         CUDA_OK(cudaFuncSetAttribute(band_stream_kernel<double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
@@ -2118,6 +2238,14 @@ struct Solver {
         err_part.resize(std::max<long long>(G, ceil_div(n, 256)));
         if (op.kind <= 1) {
             Mr.resize(n); Sr.resize(n); Mc.resize(m); Sc.resize(m);
+            if (lse_stream()) {  // bucket-ordered copies of the stream vector per band
+                ltp.resize(op.bands.size());
+                lsp[0].resize(op.bands.size());
+                for (size_t b = 0; b < op.bands.size(); ++b) {
+                    ltp[b].resize(m + 16);
+                    lsp[0][b].resize(n + 16);
+                }
+            }
         } else {
             corr_s.resize(ncorr());
             corr_t.resize(ncorr());
@@ -2215,6 +2343,17 @@ struct Solver {
             return;
         }
         lse_init_kernel<<<ceil_div(n, 256), 256, 0, s>>>(st.get(), Mr.get(), Sr.get(), n);
+        if constexpr (sizeof(T) == 4)
+            if (lse_stream()) {
+                scatter_perm(lt, m, 1, 0);  // log t into every band's bucket order
+                for (size_t b = 0; b < op.bands.size(); ++b) {
+                    PassPlan& P = plans[0][b];
+                    if (P.nitems)
+                        band_stream_kernel<float, true, true><<<band_grid, kThreads + 64, sizeof(BandSmem), s>>>(
+                            st.get(), op.iter[b].so, P.work(), band_valsT<float>(b), ltp[b].get(), Mr.get(), Sr.get());
+                }
+                return;
+            }
         for (size_t b = 0; b < op.bands.size(); ++b)
             if (op.bands[b].n_work)
                 sparse_row_band_kernel<T><<<op.bands[b].n_work, kThreads, 0, s>>>(
@@ -2243,6 +2382,17 @@ struct Solver {
             return;
         }
         lse_init_kernel<<<ceil_div(m, 256), 256, 0, s>>>(st.get(), Mc.get(), Sc.get(), m);
+        if constexpr (sizeof(T) == 4)
+            if (lse_stream()) {
+                scatter_perm(ls, n, 0, 0);  // log s into every band's bucket order
+                for (size_t b = 0; b < op.bands.size(); ++b) {
+                    PassPlan& P = plans[1][b];
+                    if (P.nitems)
+                        band_stream_kernel<float, false, true><<<band_grid, kThreads + 64, sizeof(BandSmem), s>>>(
+                            st.get(), op.iter[b].to, P.work(), band_vals<float>(b), lsp[0][b].get(), Mc.get(), Sc.get());
+                }
+                return;
+            }
         for (size_t b = 0; b < op.bands.size(); ++b)
             if (op.bands[b].n_work) {
                 if (has_valsT<T>(b)) {
@@ -2325,8 +2475,12 @@ struct Solver {
             a.perm[a.nperm++] = side == 0 ? lsp[parity][b].get() : ltp[b].get();
         }
     }
+    // the sparse operator streams its log K through band_stream_kernel's
+    // log-sum-exp mode (fp32 storage, bucket-blocked support with panels)
+    bool lse_stream() const { return op.kind == 1 && !op.fp64 && !op.gcsr && op.iter.size() == op.bands.size() &&
+                                     !op.bands.empty(); }
     void scatter_perm(const double* v, long long len, int side, int parity) {
-        if (op.kind != 3) return;
+        if (op.kind != 3 && !lse_stream()) return;
         for (size_t b = 0; b < op.bands.size(); ++b)
             perm_scatter_kernel<<<ceil_div(len, 256), 256, 0, s>>>(
                 v, len, side == 0 ? op.iter[b].sp : op.iter[b].tp,
