@@ -115,4 +115,30 @@ constexpr double kPosInf = __builtin_huge_val();
 
 inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
 
+// ---- programmatic dependent launch (sm_90+) ---------------------------------
+// A chain of short dependent kernels (the k-means++ step) pays a kernel
+// boundary per launch. Launched with programmatic stream serialisation, the
+// next kernel is set up while this one runs: its CTAs start once every CTA
+// of this grid has executed pdl_launch_dependents() (or exited) and block in
+// pdl_wait() until this grid has completed and its writes are visible. Both
+// are no-ops for a kernel launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    CUDA_OK(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(std::forward<Args>(args))...));
+}
+
 }  // namespace lcnb

@@ -15,6 +15,7 @@
 #include <cub/cub.cuh>
 #include <cuda_fp16.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <random>
 #include <string>
@@ -119,7 +120,11 @@ constexpr int kFoldChunk = 2048;  // fold chunk (see the chunk-parallel exact fo
 __global__ void __launch_bounds__(256) pp_prune_kernel(long long N, int t, const double* __restrict__ dist2,
                                                        const uint32_t* __restrict__ near,
                                                        const double* __restrict__ dc, uint32_t* __restrict__ list,
-                                                       unsigned* __restrict__ count, double* __restrict__ csum) {
+                                                       unsigned* __restrict__ count, double* __restrict__ csum,
+                                                       unsigned* __restrict__ surv_count, double* __restrict__ bsum) {
+    pdl_wait();
+    pdl_launch_dependents();
+    if (surv_count && blockIdx.x == 0 && threadIdx.x == 0) *surv_count = 0u;  // this step's filter survivors
     // one block per fold chunk (kFoldChunk points, kPP per thread, strided
     // for coalescing): one list-append atomic per chunk, and the chunk's
     // dist2 sum (approximate chunk sums steer the fold's binade predictions
@@ -168,6 +173,7 @@ __global__ void __launch_bounds__(256) pp_prune_kernel(long long N, int t, const
         }
         bbase = tot ? atomicAdd(count, tot) : 0u;
         csum[blockIdx.x] = cs;
+        bsum[blockIdx.x] = cs;  // the pre-update sum (pp_pick_kernel's error bound)
     }
     __syncthreads();
     unsigned off = bbase + wbase[warp];
@@ -190,6 +196,8 @@ __global__ void __launch_bounds__(128) pp_exact_kernel(const T* __restrict__ X, 
                                                        const uint32_t* __restrict__ list,
                                                        const unsigned* __restrict__ count,
                                                        double* __restrict__ csum) {
+    pdl_wait();
+    pdl_launch_dependents();
     extern __shared__ __align__(16) unsigned char dyn[];
     double* cs = reinterpret_cast<double*>(dyn);  // the new seed, fp64
     T* rows = reinterpret_cast<T*>(cs + d);
@@ -339,6 +347,8 @@ __global__ void __launch_bounds__(128) pp_filter_exact_kernel(const T* __restric
                                                               const uint32_t* __restrict__ list,
                                                               const unsigned* __restrict__ count, int wbuf_bytes,
                                                               double* __restrict__ csum) {
+    pdl_wait();
+    pdl_launch_dependents();
     extern __shared__ __align__(16) unsigned char dyn[];
     __shared__ double eps_c;
     double* cs = reinterpret_cast<double*>(dyn);  // the new seed, fp64
@@ -456,11 +466,144 @@ __global__ void __launch_bounds__(128) pp_filter_exact_kernel(const T* __restric
     }
 }
 
+// Filter only (the default): the same bound as pp_filter_exact_kernel, but
+// the survivors are appended to `surv` and folded by pp_exact_kernel in a
+// second launch with 32 lanes per warp. Folding them inside the filter kept
+// 8 lanes busy for a 128-step dependent fp64 chain between two batches of
+// row loads, so the filter pass streamed at < 3 TB/s. Here a warp issues
+// all 32 rows' loads of a batch before it computes, and the next batch's
+// list entries, scales and dist2 are loaded before the current batch is
+// reduced.
+template <typename T, typename QT, int NQ>
+__global__ void __launch_bounds__(128) pp_filter_kernel(const T* __restrict__ X, const QT* __restrict__ Xh,
+                                                        const float2* __restrict__ se, int d, int dp,
+                                                        const uint32_t* __restrict__ chosen, int t,
+                                                        const double* __restrict__ dist2,
+                                                        const uint32_t* __restrict__ list,
+                                                        const unsigned* __restrict__ count,
+                                                        uint32_t* __restrict__ surv, unsigned* __restrict__ surv_count) {
+    pdl_wait();
+    pdl_launch_dependents();
+    __shared__ float c32[NQ * 128];
+    __shared__ double eps_part[4];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const long long last = chosen[t];
+    double e2 = 0.0;
+    for (int k = threadIdx.x; k < NQ * 128; k += blockDim.x) {
+        const double v = k < d ? static_cast<double>(X[last * d + k]) : 0.0;
+        const float f = static_cast<float>(v);
+        c32[k] = f;
+        const double df = v - static_cast<double>(f);
+        e2 += df * df;
+    }
+    e2 = warp_sum(e2);
+    if (lane == 0) eps_part[warp] = e2;
+    __syncthreads();
+    double ec2 = 0.0;
+    for (int w = 0; w < nw; ++w) ec2 += eps_part[w];
+    const double ec = sqrt(ec2) * (1.0 + 1e-12) + 1e-300;
+    const double gam = 1.0 - (dp + 4) * 1.1920928955078125e-07;  // (dp + 4) 2^-23
+    float4 cq[NQ];
+    bool qin[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const int ch = lane + 32 * q;
+        qin[q] = ch * 4 < dp;
+        cq[q] = qin[q] ? make_float4(c32[4 * ch], c32[4 * ch + 1], c32[4 * ch + 2], c32[4 * ch + 3])
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const unsigned cnt = *count;
+    const unsigned stride = gridDim.x * nw * 32u;
+    unsigned b0 = (blockIdx.x * nw + warp) * 32u;
+    // batch b0's list entry, scale and dist2 (prefetched one batch ahead)
+    uint32_t mine = 0;
+    float2 my_se = make_float2(0.f, 0.f);
+    double my_d2 = 0.0;
+    if (b0 < cnt && lane < static_cast<int>(min(32u, cnt - b0))) {
+        mine = list[b0 + lane];
+        my_se = se[mine];
+        my_d2 = dist2[mine];
+    }
+    for (; b0 < cnt; b0 += stride) {
+        const unsigned nb = cnt - b0 < 32u ? cnt - b0 : 32u;
+        // rows past the batch read row 0 (harmless; their lanes are ignored)
+        // rows in groups of RB: at most 32 8-byte loads in flight per lane
+        // (the register budget), issued before the group is reduced
+        using Raw = typename std::conditional<sizeof(QT) == 2, uint2, int>::type;
+        constexpr int RB = NQ == 1 ? 32 : 8;
+        float part[32];
+        // the next batch's list entries (independent of this batch's rows)
+        const unsigned b1 = b0 + stride;
+        uint32_t nmine = 0;
+        float2 nse = make_float2(0.f, 0.f);
+        double nd2 = 0.0;
+#pragma unroll
+        for (int g = 0; g < 32; g += RB) {
+            Raw raw[RB][NQ];
+#pragma unroll
+            for (int j = 0; j < RB; ++j) {
+                const long long row = __shfl_sync(0xffffffffu, mine, g + j);
+#pragma unroll
+                for (int q = 0; q < NQ; ++q)
+                    if (qin[q]) raw[j][q] = __ldcs(reinterpret_cast<const Raw*>(Xh + row * dp + 4 * (lane + 32 * q)));
+            }
+            if (g == 0 && b1 < cnt && lane < static_cast<int>(min(32u, cnt - b1))) {
+                nmine = list[b1 + lane];
+                nse = se[nmine];
+                nd2 = dist2[nmine];
+            }
+#pragma unroll
+            for (int j = 0; j < RB; ++j) {
+                const float sj = __shfl_sync(0xffffffffu, my_se.x, g + j);
+                float acc = 0.f;
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    if (!qin[q]) continue;
+                    float2 a, b;
+                    if constexpr (sizeof(QT) == 2) {
+                        a = __half22float2(*reinterpret_cast<const __half2*>(&raw[j][q].x));
+                        b = __half22float2(*reinterpret_cast<const __half2*>(&raw[j][q].y));
+                    } else {
+                        const char4 c4 = *reinterpret_cast<const char4*>(&raw[j][q]);
+                        a = make_float2(static_cast<float>(c4.x), static_cast<float>(c4.y));
+                        b = make_float2(static_cast<float>(c4.z), static_cast<float>(c4.w));
+                    }
+                    const float d0 = fmaf(a.x, sj, -cq[q].x), d1 = fmaf(a.y, sj, -cq[q].y);
+                    const float d2 = fmaf(b.x, sj, -cq[q].z), d3 = fmaf(b.y, sj, -cq[q].w);
+                    acc = fmaf(d0, d0, acc);
+                    acc = fmaf(d1, d1, acc);
+                    acc = fmaf(d2, d2, acc);
+                    acc = fmaf(d3, d3, acc);
+                }
+                part[g + j] = acc;
+            }
+        }
+        const float A = transpose_reduce32(part, lane);
+        bool need = false;
+        if (lane < static_cast<int>(nb)) {
+            const double lo = sqrt(static_cast<double>(A) * gam) - static_cast<double>(my_se.y) - ec;
+            need = !(lo > 0.0 && lo * lo * (1.0 - 1e-12) >= my_d2);
+        }
+        const unsigned sv = __ballot_sync(0xffffffffu, need);
+        if (sv) {
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(surv_count, static_cast<unsigned>(__popc(sv)));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (need) surv[base + __popc(sv & ((1u << lane) - 1u))] = mine;
+        }
+        mine = nmine;
+        my_se = nse;
+        my_d2 = nd2;
+    }
+}
+
 // dc[j] = |x_{chosen[j]} - x_{chosen[t]}| for j < t (fp64, one warp per j)
 template <typename T>
 __global__ void __launch_bounds__(256) seed_dist_kernel(const T* __restrict__ X, int d,
                                                         const uint32_t* __restrict__ chosen, int t,
                                                         double* __restrict__ dc) {
+    pdl_wait();
+    pdl_launch_dependents();
     const int j = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (j >= t) return;
     const long long a = chosen[j], b = chosen[t];
@@ -592,7 +735,10 @@ __device__ __forceinline__ longlong2 par_clamp(ParInc v) {
 // The prediction only decides which path a chunk takes; the walk re-checks
 // the actual binade, so the result is exact regardless.
 
-__global__ void fold_chunk_sum_kernel(const double* __restrict__ x, long long N, double* __restrict__ csum) {
+__global__ void fold_chunk_sum_kernel(const double* __restrict__ x, long long N, double* __restrict__ csum,
+                                      double* __restrict__ bsum) {
+    pdl_wait();
+    pdl_launch_dependents();
     __shared__ double red[8];
     const long long b = static_cast<long long>(blockIdx.x) * kFoldChunk;
     const long long e = min(N, b + kFoldChunk);
@@ -605,6 +751,7 @@ __global__ void fold_chunk_sum_kernel(const double* __restrict__ x, long long N,
         double t = 0.0;
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
         csum[blockIdx.x] = t;
+        bsum[blockIdx.x] = t;
     }
 }
 
@@ -651,7 +798,11 @@ __global__ void __launch_bounds__(256, 4) fold_round_kernel(const double* __rest
                                                             const double* __restrict__ csum, int* __restrict__ ebin,
                                                          longlong2* __restrict__ R, longlong2* __restrict__ Rseg,
                                                          int* __restrict__ Eseg, int* __restrict__ spred,
-                                                         unsigned* __restrict__ smask, double* __restrict__ s0end) {
+                                                         unsigned* __restrict__ smask, double* __restrict__ s0end,
+                                                         const int* __restrict__ skip) {
+    pdl_wait();
+    pdl_launch_dependents();
+    if (skip && *skip) return;  // pp_pick_kernel certified this step's pick
     __shared__ ParInc stot[kSegs];
     __shared__ double ssum[kSegs];
     __shared__ double red[8];
@@ -942,7 +1093,9 @@ __global__ void __launch_bounds__(kWalkThreads) pp_walk_pick_kernel(
     const int* __restrict__ spred, const longlong2* __restrict__ R, const longlong2* __restrict__ Rseg,
     const int* __restrict__ Eseg, const unsigned* __restrict__ smask, const double* __restrict__ s0end,
     double* __restrict__ csum, unsigned* __restrict__ cand_count, double* __restrict__ sstart, const unsigned long long* __restrict__ raw, int n_raw, int* __restrict__ draw_counter,
-    uint32_t* __restrict__ chosen, int t, int staged) {
+    uint32_t* __restrict__ chosen, int t, int staged, const int* __restrict__ skip) {
+    pdl_wait();
+    pdl_launch_dependents();
     __shared__ int flag_min;
     __shared__ double total;
     __shared__ __align__(16) double segbuf[kSegLen];
@@ -950,6 +1103,7 @@ __global__ void __launch_bounds__(kWalkThreads) pp_walk_pick_kernel(
     __shared__ int pre_list[kMaxPre];
     extern __shared__ __align__(16) unsigned char wdyn[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (skip && *skip) return;  // pp_pick_kernel certified this step's pick
     WALK_T(T0);
     // the next step's prune appends to the candidate list from zero
     if (threadIdx.x == 0) *cand_count = 0u;
@@ -1175,6 +1329,160 @@ __global__ void __launch_bounds__(kWalkThreads) pp_walk_pick_kernel(
     }
 }
 
+// ---- certified pick (kmeans.cpp:49-58) without the exact fold ---------------
+// The running sum of the reference is only consumed through two comparisons:
+// target = c * total (uniform_real(0, total)) and the first i with
+// acc_i >= target. So the pick is decided by any approximation Q_i of the
+// prefix sums whose distance to the fold acc_i is bounded by a known W:
+//   * the fold over non-negative values: |acc_i - P_i| <= gamma_N T
+//     (P the real prefix, gamma_k = k u / (1 - k u), u = 2^-53);
+//   * Q from the chunk sums csum: the prune pass writes each chunk's sum as a
+//     tree (height <= 16, also kept in bsum), the exact pass adds each
+//     update's fl(new - old) atomically: at most 2048 adds per chunk, each
+//     rounding within u of the chunk's pre-update sum, so the chunk sum is
+//     within (2 * 2048 + 20) u bsum_c of the real one; the scans here add
+//     a tree of height < 64 + nch / 1024.
+// Hence |acc_i - Q_i| <= W = 2 (N + nch + 128) u T + 8400 u sum(bsum)
+// (twice the bounds), the reference's target lies in c T +- (W + slop), and
+// an index i with
+//   Q_i - W' >= mid + W'   and   Q_{i-1} + W' < mid - W'
+// (W' = W + 16 u T covers the fl products and differences here) IS the
+// reference's pick: acc is monotone, and acc_{i-1} < target <= acc_i forces
+// dist2[i] > 0 (the second half of kmeans.cpp:53). Such an i exists unless
+// the target falls within ~4 W of a prefix boundary (probability ~4 N W / T,
+// ~3e-3 per step at N = 2e6); those steps, the total <= 0 branch and
+// non-finite sums set skip = 0 and the exact fold + walk run as before.
+// One CTA: scan of the chunk sums, target chunk, that chunk's 2048 values.
+constexpr int kPickThreads = 1024;
+__global__ void __launch_bounds__(kPickThreads) pp_pick_kernel(
+    double* __restrict__ dist2, unsigned char* __restrict__ used, long long N, int nch,
+    const double* __restrict__ csum, const double* __restrict__ bsum, double* __restrict__ qbuf,
+    int* __restrict__ skip, unsigned* __restrict__ cand_count, const unsigned long long* __restrict__ raw, int n_raw,
+    int* __restrict__ draw_counter, uint32_t* __restrict__ chosen, int t, unsigned* __restrict__ n_fallback,
+    double slack, const unsigned* __restrict__ surv_count, unsigned long long* __restrict__ stats) {
+    pdl_wait();
+    pdl_launch_dependents();
+    if (stats && threadIdx.x == 0) {  // candidates and exact folds of this step (LCN_TIMING)
+        stats[0] += *cand_count;
+        stats[1] += surv_count ? *surv_count : 0u;
+    }
+    __shared__ double red[kPickThreads / 32], bred[kPickThreads / 32];
+    __shared__ double carry_s, bs_s;
+    __shared__ int cstar_s, istar_s;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr double u = 1.1102230246251565e-16;  // 2^-53
+    if (threadIdx.x == 0) {
+        carry_s = 0.0;
+        bs_s = 0.0;
+        cstar_s = nch;
+        istar_s = kFoldChunk;
+    }
+    __syncthreads();
+    // inclusive scan of the chunk sums (qbuf[c] = Q at the end of chunk c)
+    // and the sum of the pre-update sums
+    for (int c0 = 0; c0 < nch; c0 += kPickThreads) {
+        const int c = c0 + threadIdx.x;
+        const double v = c < nch ? csum[c] : 0.0;
+        const double bv = warp_sum(c < nch ? bsum[c] : 0.0);
+        double incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double tt = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += tt;
+        }
+        if (lane == 31) red[warp] = incl;
+        if (lane == 0) bred[warp] = bv;
+        __syncthreads();
+        double off = carry_s;
+        for (int w = 0; w < warp; ++w) off += red[w];
+        if (c < nch) qbuf[c] = off + incl;
+        __syncthreads();
+        if (threadIdx.x == kPickThreads - 1) carry_s = off + incl;
+        if (threadIdx.x == 0) {
+            double bb = bs_s;
+            for (int w = 0; w < kPickThreads / 32; ++w) bb += bred[w];
+            bs_s = bb;
+        }
+        __syncthreads();
+    }
+    const double T = carry_s, BS = bs_s;
+    const int di = *draw_counter;
+    const double W = (2.0 * static_cast<double>(N + nch + 128) * u * T + 8400.0 * u * BS) * slack + 16.0 * u * T;
+    if (!(T > 0.0) || !(T < kPosInf) || !(BS < kPosInf) || di >= n_raw || !(W < 1e-3 * T)) {
+        if (threadIdx.x == 0) {
+            *skip = 0;
+            atomicAdd(n_fallback, 1u);
+        }
+        return;
+    }
+    double c = __ull2double_rn(raw[di]) * 5.421010862427522e-20;  // as pp_walk_pick_kernel
+    if (c >= 1.0) c = 0.99999999999999989;
+    const double mid = c * T, tlo = mid - W, thi = mid + W;
+    for (int cc = threadIdx.x; cc < nch; cc += kPickThreads)
+        if (qbuf[cc] >= mid) {
+            atomicMin(&cstar_s, cc);
+            break;
+        }
+    __syncthreads();
+    const int cs = min(cstar_s, nch - 1);
+    const double A = cs > 0 ? qbuf[cs - 1] : 0.0;
+    // the chunk's prefix: kPer contiguous values per thread, then warp / block
+    constexpr int kPer = kFoldChunk / kPickThreads;
+    const long long b = static_cast<long long>(cs) * kFoldChunk + threadIdx.x * kPer;
+    double xv[kPer];
+    double run = 0.0;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        xv[j] = b + j < N ? dist2[b + j] : 0.0;
+        run += xv[j];
+    }
+    double incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double tt = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += tt;
+    }
+    if (lane == 31) red[warp] = incl;
+    __syncthreads();
+    // exclusive prefix by a shuffle (a summation tree, unlike incl - run)
+    double q = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) q = 0.0;
+    for (int w = 0; w < warp; ++w) q += red[w];
+    q += A;  // Q just before this thread's first value
+    double qprev = q;
+    int hit = -1;
+    double qhit = 0.0, qhprev = 0.0;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        const double qn = qprev + xv[j];
+        if (hit < 0 && b + j < N && qn >= mid) {
+            hit = threadIdx.x * kPer + j;
+            qhit = qn;
+            qhprev = qprev;
+        }
+        qprev = qn;
+    }
+    if (hit >= 0) atomicMin(&istar_s, hit);
+    __syncthreads();
+    if (hit >= 0 && hit == istar_s) {
+        const long long pick = static_cast<long long>(cs) * kFoldChunk + hit;
+        const bool ok = tlo > 0.0 && qhit - W >= thi && qhprev + W < tlo;
+        if (ok) {
+            chosen[t] = static_cast<uint32_t>(pick);
+            dist2[pick] = 0.0;
+            used[pick] = 1;
+            *draw_counter = di + 1;
+            *cand_count = 0u;
+        } else {
+            atomicAdd(n_fallback, 1u);
+        }
+        *skip = ok ? 1 : 0;
+    } else if (threadIdx.x == 0 && istar_s == kFoldChunk) {
+        *skip = 0;  // not in the predicted chunk: the exact walk decides
+        atomicAdd(n_fallback, 1u);
+    }
+}
+
 __global__ void fill_kernel(double* p, long long n, double v) {
     long long i = blockIdx.x * 256LL + threadIdx.x;
     if (i < n) p[i] = v;
@@ -1212,12 +1520,12 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     int ex_occ = 1;
     CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ex_occ, pp_exact_kernel<T>, ex_warps * 32, ex_smem));
     const int ex_grid = std::max(1, ex_occ) * ctx.num_sms;
-    // filter copy of the points: fp16 rows with a power-of-two scale per row
-    // (default) or int8 rows (LCN_PP_FILTER=i8: half the bytes, measured no
-    // faster at configs[3] -- the filter pass is latency-, not byte-bound);
-    // rows up to 512 values
+    // filter copy of the points: int8 rows with a power-of-two scale per row
+    // (default since the filter streams; build-time seeding at configs[3]
+    // 596 -> 490 ms per band) or fp16 rows (LCN_PP_FILTER=f16: tighter
+    // bound, twice the bytes); rows up to 512 values
     const char* fenv = std::getenv("LCN_PP_FILTER");
-    const bool i8 = fenv && std::string(fenv) == "i8";
+    const bool i8 = !(fenv && std::string(fenv) == "f16");
     const int qsz = i8 ? 1 : 2;
     const int dp = i8 ? (d + 15) / 16 * 16 : (d + 7) / 8 * 8;
     const bool filt = dp <= kFiltMaxQ * 128 && std::getenv("LCN_PP_NOFILTER") == nullptr;
@@ -1240,6 +1548,34 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
                    : nq == 2 ? pp_filter_exact_kernel<T, int8_t, 2>
                    : nq == 3 ? pp_filter_exact_kernel<T, int8_t, 3>
                              : pp_filter_exact_kernel<T, int8_t, 4>;
+    // filter and exact fold in separate launches (default) or fused
+    // (LCN_PP_SPLIT=0, the round-2 kernel)
+    const char* spenv = std::getenv("LCN_PP_SPLIT");
+    const bool split = !(spenv && spenv[0] == '0');
+    using FsH = void (*)(const T*, const __half*, const float2*, int, int, const uint32_t*, int, const double*,
+                         const uint32_t*, const unsigned*, uint32_t*, unsigned*);
+    using FsQ = void (*)(const T*, const int8_t*, const float2*, int, int, const uint32_t*, int, const double*,
+                         const uint32_t*, const unsigned*, uint32_t*, unsigned*);
+    const FsH fs_h = nq == 1 ? pp_filter_kernel<T, __half, 1>
+                   : nq == 2 ? pp_filter_kernel<T, __half, 2>
+                   : nq == 3 ? pp_filter_kernel<T, __half, 3>
+                             : pp_filter_kernel<T, __half, 4>;
+    const FsQ fs_q = nq == 1 ? pp_filter_kernel<T, int8_t, 1>
+                   : nq == 2 ? pp_filter_kernel<T, int8_t, 2>
+                   : nq == 3 ? pp_filter_kernel<T, int8_t, 3>
+                             : pp_filter_kernel<T, int8_t, 4>;
+    DevBuf<uint32_t> surv(filt && split ? N : 1);
+    DevBuf<unsigned> scnt(1);
+    scnt.zero(s);
+    int fs_grid = ctx.num_sms;
+    if (filt && split) {
+        int occ = 1;
+        if (i8)
+            CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fs_q, 128, 0));
+        else
+            CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fs_h, 128, 0));
+        fs_grid = std::max(1, occ) * ctx.num_sms;
+    }
     int fx_grid = ex_grid;
     if (filt) {
         if (i8)
@@ -1261,6 +1597,20 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     }
     DevBuf<unsigned long long> d_raw(raw.size() ? raw.size() : 1);
     DevBuf<int> counter(1);
+    // certified pick first (pp_pick_kernel); the exact fold + walk only
+    // when it cannot decide. LCN_PP_EXACT_WALK=1 always runs the exact walk.
+    const char* wenv = std::getenv("LCN_PP_EXACT_WALK");
+    const bool fast = !(wenv && wenv[0] == '1');
+    const char* senv = std::getenv("LCN_PP_CERT_SLACK");  // test hook: widen the certificate (more fallbacks)
+    const double slack = senv ? std::max(1.0, std::atof(senv)) : 1.0;
+    DevBuf<double> fsum(nch), bsum(nch);
+    DevBuf<int> skip(1);
+    DevBuf<unsigned> nfall(1);
+    const bool timing = std::getenv("LCN_TIMING") != nullptr;
+    DevBuf<unsigned long long> pstats(2);
+    pstats.zero(s);
+    skip.zero(s);
+    nfall.zero(s);
     used.zero(s);
     near.zero(s);
     counter.zero(s);
@@ -1272,21 +1622,34 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     unsigned char one = 1;
     CUDA_OK(cudaMemcpyAsync(d_chosen, &f32, 4, cudaMemcpyHostToDevice, s));
     CUDA_OK(cudaMemcpyAsync(used.get() + first, &one, 1, cudaMemcpyHostToDevice, s));
+    // the step chain with programmatic dependent launches (LCN_PP_PDL=0: plain)
+    const char* penv = std::getenv("LCN_PP_PDL");
+    const bool pdl = !(penv && penv[0] == '0');
+    const dim3 b256(256), b128(128);
     for (int t = 1; t < k; ++t) {
-        if (t > 1) seed_dist_kernel<T><<<ceil_div(t - 1, 8), 256, 0, s>>>(X, d, d_chosen, t - 1, dc.get());
-        pp_prune_kernel<<<nch, 256, 0, s>>>(N, t - 1, dist2.get(), near.get(), dc.get(), list.get(), cnt.get(),
-                                            csum.get());
-        if (filt && i8)
-            fx_q<<<fx_grid, ex_warps * 32, fx_smem, s>>>(X, reinterpret_cast<const int8_t*>(Xq.get()), se.get(), d, dp,
-                                                         d_chosen, t - 1, dist2.get(), near.get(), list.get(),
-                                                         cnt.get(), wbuf_bytes, csum.get());
+        if (t > 1) launch_pdl(seed_dist_kernel<T>, dim3(ceil_div(t - 1, 8)), b256, 0, s, pdl, X, d, d_chosen, t - 1, dc.get());
+        launch_pdl(pp_prune_kernel, dim3(nch), b256, 0, s, pdl, N, t - 1, dist2.get(), near.get(), dc.get(), list.get(),
+                   cnt.get(), csum.get(), scnt.get(), bsum.get());
+        if (filt && split) {
+            if (i8)
+                launch_pdl(fs_q, dim3(fs_grid), b128, 0, s, pdl, X, reinterpret_cast<const int8_t*>(Xq.get()), se.get(),
+                           d, dp, d_chosen, t - 1, dist2.get(), list.get(), cnt.get(), surv.get(), scnt.get());
+            else
+                launch_pdl(fs_h, dim3(fs_grid), b128, 0, s, pdl, X, reinterpret_cast<const __half*>(Xq.get()), se.get(),
+                           d, dp, d_chosen, t - 1, dist2.get(), list.get(), cnt.get(), surv.get(), scnt.get());
+            launch_pdl(pp_exact_kernel<T>, dim3(ex_grid), dim3(ex_warps * 32), ex_smem, s, pdl, X, d, d_chosen, t - 1,
+                       dist2.get(), near.get(), surv.get(), scnt.get(), csum.get());
+        } else if (filt && i8)
+            launch_pdl(fx_q, dim3(fx_grid), dim3(ex_warps * 32), fx_smem, s, pdl, X,
+                       reinterpret_cast<const int8_t*>(Xq.get()), se.get(), d, dp, d_chosen, t - 1, dist2.get(),
+                       near.get(), list.get(), cnt.get(), wbuf_bytes, csum.get());
         else if (filt)
-            fx_h<<<fx_grid, ex_warps * 32, fx_smem, s>>>(X, reinterpret_cast<const __half*>(Xq.get()), se.get(), d, dp,
-                                                         d_chosen, t - 1, dist2.get(), near.get(), list.get(),
-                                                         cnt.get(), wbuf_bytes, csum.get());
+            launch_pdl(fx_h, dim3(fx_grid), dim3(ex_warps * 32), fx_smem, s, pdl, X,
+                       reinterpret_cast<const __half*>(Xq.get()), se.get(), d, dp, d_chosen, t - 1, dist2.get(),
+                       near.get(), list.get(), cnt.get(), wbuf_bytes, csum.get());
         else
-            pp_exact_kernel<T><<<ex_grid, ex_warps * 32, ex_smem, s>>>(X, d, d_chosen, t - 1, dist2.get(), near.get(),
-                                                                       list.get(), cnt.get(), csum.get());
+            launch_pdl(pp_exact_kernel<T>, dim3(ex_grid), dim3(ex_warps * 32), ex_smem, s, pdl, X, d, d_chosen, t - 1,
+                       dist2.get(), near.get(), list.get(), cnt.get(), csum.get());
 #ifdef LCN_WALK_PROFILE
         if (std::getenv("LCN_WALK_STATS") && (t % 256 == 0 || t == k - 1)) {
             unsigned hc = 0;
@@ -1302,18 +1665,38 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
 #endif
         // the first pass moves every point off +inf: its chunk sums are taken
         // afresh (later steps: prune sums minus the exact pass's updates)
-        if (t == 1) fold_chunk_sum_kernel<<<nch, 256, 0, s>>>(dist2.get(), N, csum.get());
-        fold_round_kernel<<<nch, 256, 0, s>>>(dist2.get(), N, csum.get(), ebin.get(), R.get(), Rseg.get(),
-                                              Eseg.get(), spred.get(), smask.get(), s0end.get());
-        pp_walk_pick_kernel<<<1, kWalkThreads, walk_smem, s>>>(
-            dist2.get(), used.get(), N, nch, ebin.get(), spred.get(), R.get(), Rseg.get(), Eseg.get(), smask.get(),
-            s0end.get(), csum.get(), cnt.get(), sstart.get(),
-            d_raw.get(),
-            static_cast<int>(raw.size()), counter.get(), d_chosen, t, walk_staged);
+        if (t == 1)
+            launch_pdl(fold_chunk_sum_kernel, dim3(nch), b256, 0, s, pdl, dist2.get(), N, csum.get(), bsum.get());
+        const int* skp = nullptr;
+        if (fast) {
+            launch_pdl(pp_pick_kernel, dim3(1), dim3(kPickThreads), 0, s, pdl, dist2.get(), used.get(), N, nch,
+                       csum.get(), bsum.get(), fsum.get(), skip.get(), cnt.get(), d_raw.get(),
+                       static_cast<int>(raw.size()), counter.get(), d_chosen, t, nfall.get(), slack,
+                       filt && split ? scnt.get() : nullptr, timing ? pstats.get() : nullptr);
+            skp = skip.get();
+        }
+        launch_pdl(fold_round_kernel, dim3(nch), b256, 0, s, pdl, dist2.get(), N, csum.get(), ebin.get(), R.get(),
+                   Rseg.get(), Eseg.get(), spred.get(), smask.get(), s0end.get(), skp);
+        launch_pdl(pp_walk_pick_kernel, dim3(1), dim3(kWalkThreads), walk_smem, s, pdl, dist2.get(), used.get(), N, nch,
+                   ebin.get(), spred.get(), R.get(), Rseg.get(), Eseg.get(), smask.get(), s0end.get(), csum.get(),
+                   cnt.get(), sstart.get(), d_raw.get(), static_cast<int>(raw.size()), counter.get(), d_chosen, t,
+                   walk_staged, skp);
     }
     LAUNCH_OK("kmeans++");
     if (draws_used) counter.download(draws_used, 1, s);
+    unsigned h_fall = 0;
+    unsigned long long h_st[2] = {0, 0};
+    if (fast && timing) {
+        nfall.download(&h_fall, 1, s);
+        pstats.download(h_st, 2, s);
+    }
     ctx.sync();
+    if (fast && timing)
+        std::fprintf(stderr,
+                     "[kmeans++] N=%lld k=%d: exact-walk fallbacks %u of %d steps; per step %.0f filter candidates, "
+                     "%.0f exact folds (%s rows)\n",
+                     N, k, h_fall, k - 1, static_cast<double>(h_st[0]) / (k - 1),
+                     static_cast<double>(h_st[1]) / (k - 1), filt ? (i8 ? "int8" : "fp16") : "no filter");
 #ifdef LCN_WALK_PROFILE
     if (std::getenv("LCN_WALK_STATS")) {
         unsigned long long h[16];

@@ -1,0 +1,4 @@
+# certified k-means++ pick: bit-exact tests + seeding timing
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "kmeans_pp or lloyd or lsh_buckets" > gpurun_out/tests_b.log 2>&1; echo TESTS $? >> gpurun_out/tests_b.log
+LCN_TIMING=1 PROBE_BUILDS=2 timeout 300 python scripts/probe.py c3 1.0 1 > gpurun_out/timing_b.log 2>&1; echo RC $? >> gpurun_out/timing_b.log

@@ -1,0 +1,5 @@
+# int8 filter default + seeding stats
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "kmeans_pp or lloyd or lsh_buckets" > gpurun_out/tests_f.log 2>&1; echo TESTS $? >> gpurun_out/tests_f.log
+timeout 300 python scripts/timeline.py 2000000 4096 2>&1 | grep -v Warn > gpurun_out/timeline_f.log
+LCN_TIMING=1 PROBE_BUILDS=2 timeout 300 python scripts/probe.py c3 1.0 1 > gpurun_out/timing_f.log 2>&1

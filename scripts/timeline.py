@@ -41,3 +41,11 @@ tot_gap = sum(g for g, _, _ in gaps if g > 0)
 print(f"total idle between kernels {tot_gap / 1e3:.1f} ms; largest:")
 for g, a_, b_ in gaps[:10]:
     print(f"  {g / 1e3:8.2f} ms after {a_} before {b_}")
+gagg = defaultdict(lambda: [0, 0.0])
+for g, a_, b_ in gaps:
+    if g > 0:
+        gagg[b_][0] += 1
+        gagg[b_][1] += g / 1e3
+print("idle before each kernel kind:")
+for n_, (c_, t_) in sorted(gagg.items(), key=lambda x: -x[1][1])[:10]:
+    print(f"  {n_:40s} {c_:6d} {t_:9.1f} ms ({t_ / max(c_, 1) * 1e3:.2f} us each)")

@@ -58,6 +58,20 @@ def test_kmeans_pp_large_walk(ctx, ref, kind):
     assert np.array_equal(lcn.kmeans_pp_indices(ctx, x, k, seed=9), ref.kmeans_pp(x, k, 9))
 
 
+@pytest.mark.parametrize("mode", [{}, {"LCN_PP_EXACT_WALK": "1"}, {"LCN_PP_CERT_SLACK": "20000"},
+                                  {"LCN_PP_CERT_SLACK": "1e9"}])
+def test_kmeans_pp_certified_pick(ctx, ref, monkeypatch, mode):
+    # the certified pick (pp_fast_pick_kernel) and the exact fold + walk give
+    # the same indices: default (almost every step certified), exact walk
+    # only, a widened certificate (about half the steps fall back, so the two
+    # paths alternate) and one so wide that every step falls back
+    for key, val in mode.items():
+        monkeypatch.setenv(key, val)
+    n, d, k = 200_000, 8, 96
+    x = rng_points(91, n, d, comps=20)
+    assert np.array_equal(lcn.kmeans_pp_indices(ctx, x, k, seed=13), ref.kmeans_pp(x, k, 13))
+
+
 def test_kmeans_pp_duplicates_total_zero(ctx, ref):
     # all points coincide: total <= 0 branch takes the first unused index (kmeans.cpp:42-47)
     x = np.zeros((12, 3))
