@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(128) pp_exact_kernel(const T* __restrict__ X, 
                                                        double* __restrict__ dist2, uint32_t* __restrict__ near,
                                                        const uint32_t* __restrict__ list,
                                                        const unsigned* __restrict__ count,
-                                                       double* __restrict__ csum) {
+                                                       double* __restrict__ csum, int cshift) {
     pdl_wait();
     pdl_launch_dependents();
     extern __shared__ __align__(16) unsigned char dyn[];
@@ -228,10 +228,51 @@ __global__ void __launch_bounds__(128) pp_exact_kernel(const T* __restrict__ X, 
             if (acc < old) {
                 dist2[mine] = acc;
                 near[mine] = static_cast<uint32_t>(t);
-                if (old < kPosInf) atomicAdd(&csum[mine / kFoldChunk], acc - old);
+                if (old < kPosInf) atomicAdd(&csum[mine >> cshift], acc - old);
             }
         }
         __syncwarp();
+    }
+}
+
+// Exact pass over the filter's survivors, one survivor per thread, rows read
+// straight from global memory: the row's lines are prefetched into L1 first
+// so their misses overlap, then the fold streams from L1. No shared-memory
+// staging (pp_exact_kernel's 67 KB per CTA made its launch cost ~13 us even
+// for a few thousand survivors). The center is read once per CTA.
+template <typename T>
+__global__ void __launch_bounds__(256) pp_exact_lane_kernel(const T* __restrict__ X, int d,
+                                                            const uint32_t* __restrict__ chosen, int t,
+                                                            double* __restrict__ dist2, uint32_t* __restrict__ near,
+                                                            const uint32_t* __restrict__ list,
+                                                            const unsigned* __restrict__ count,
+                                                            double* __restrict__ csum, int cshift) {
+    pdl_wait();
+    pdl_launch_dependents();
+    extern __shared__ __align__(16) unsigned char dyn[];
+    double* cs = reinterpret_cast<double*>(dyn);
+    const unsigned cnt = *count;
+    if (blockIdx.x * 256u >= cnt) return;
+    const long long last = chosen[t];
+    for (int k = threadIdx.x; k < d; k += 256) cs[k] = static_cast<double>(X[last * d + k]);
+    __syncthreads();
+    for (unsigned i = blockIdx.x * 256u + threadIdx.x; i < cnt; i += gridDim.x * 256u) {
+        const uint32_t row = list[i];
+        const T* r = X + static_cast<long long>(row) * d;
+        for (int k = 0; k < d; k += 128 / static_cast<int>(sizeof(T)))
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(r + k));
+        double acc = 0.0;
+#pragma unroll 8
+        for (int k = 0; k < d; ++k) {
+            const double df = xsub(static_cast<double>(r[k]), cs[k]);
+            acc = xadd(acc, xmul(df, df));
+        }
+        const double old = dist2[row];
+        if (acc < old) {
+            dist2[row] = acc;
+            near[row] = static_cast<uint32_t>(t);
+            if (old < kPosInf) atomicAdd(&csum[row >> cshift], acc - old);
+        }
     }
 }
 
@@ -287,7 +328,8 @@ __global__ void __launch_bounds__(256) pp_half_prep_kernel(const T* __restrict__
 // filter pass, whose rigorous bound absorbs the coarser grid.
 template <typename T>
 __global__ void __launch_bounds__(256) pp_i8_prep_kernel(const T* __restrict__ X, long long N, int d, int dp,
-                                                         int8_t* __restrict__ Xq, float2* __restrict__ se) {
+                                                         int8_t* __restrict__ Xq, float2* __restrict__ se,
+                                                         int* __restrict__ qn) {
     const long long row = blockIdx.x * 8LL + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (row >= N) return;
@@ -301,6 +343,7 @@ __global__ void __launch_bounds__(256) pp_i8_prep_kernel(const T* __restrict__ X
     frexp(m / 127.0, &e);  // m / 127 < 2^e
     const double sc = ok && m > 0.0 ? ldexp(1.0, e) : 1.0, inv = 1.0 / sc;
     double err2 = 0.0;
+    int q2 = 0;
     for (int k = lane; k < dp; k += 32) {
         const double v = k < d ? static_cast<double>(x[k]) : 0.0;
         double qv = ok ? rint(v * inv) : 0.0;
@@ -308,11 +351,15 @@ __global__ void __launch_bounds__(256) pp_i8_prep_kernel(const T* __restrict__ X
         Xq[row * dp + k] = static_cast<int8_t>(qv);
         const double df = v - qv * sc;
         err2 += df * df;
+        q2 += static_cast<int>(qv) * static_cast<int>(qv);
     }
     err2 = warp_sum(err2);
-    if (lane == 0)
+    q2 = warp_sum(q2);
+    if (lane == 0) {
         se[row] = make_float2(static_cast<float>(sc), ok ? __double2float_ru(sqrt(err2) * (1.0 + 1e-12) + 1e-300)
                                                          : kPosInf);
+        if (qn) qn[row] = q2;  // |q|^2, exact (<= 512 * 127^2)
+    }
 }
 
 // 32 values per lane -> lane l gets the warp sum of value l (31 shuffles)
@@ -597,13 +644,360 @@ __global__ void __launch_bounds__(128) pp_filter_kernel(const T* __restrict__ X,
     }
 }
 
+// Integer filter over int8 rows (the default filter). The new center is
+// quantised per step to int16 with a power-of-two scale s_c (c^ = s_c q_c,
+// eps_c >= |c - c^|), so the squared distance of the two quantised points,
+//   |x^ - c^|^2 = s_x^2 |q_x|^2 - 2 s_x s_c (q_x . q_c) + s_c^2 |q_c|^2,
+// needs only the integer dot q_x . q_c: two dp2a per lane and row (int16 x
+// int8, exact int32) instead of four int8 -> fp32 conversions and eight
+// FMAs (the conversions made the early, all-candidate steps issue-bound:
+// ncu, 50 % SM throughput at 2.4 TB/s). |q_x|^2 comes from the prep pass.
+// The three terms are exact in fp64 and the two adds err by < 2^-52 of
+// their magnitudes; then, as before, |x - c| >= |x^ - c^| - eps_x - eps_c.
+template <int NQ>
+__device__ __forceinline__ int dp2a_row(const int (&raw)[NQ], const int (&qlo)[NQ], const int (&qhi)[NQ]) {
+    int acc = 0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        acc = __dp2a_lo(qlo[q], raw[q], acc);
+        acc = __dp2a_hi(qhi[q], raw[q], acc);
+    }
+    return acc;
+}
+
+template <typename T, int NQ>
+__global__ void __launch_bounds__(128) pp_filter_i8_kernel(const T* __restrict__ X, const int8_t* __restrict__ Xq,
+                                                           const float2* __restrict__ se, const int* __restrict__ qn,
+                                                           int d, int dp, const uint32_t* __restrict__ chosen, int t,
+                                                           const double* __restrict__ dist2,
+                                                           const uint32_t* __restrict__ list,
+                                                           const unsigned* __restrict__ count,
+                                                           uint32_t* __restrict__ surv,
+                                                           unsigned* __restrict__ surv_count) {
+    pdl_wait();
+    pdl_launch_dependents();
+    __shared__ short qc[NQ * 128];
+    __shared__ double wred[4][2];
+    __shared__ double cmax_s;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const long long last = chosen[t];
+    // scale of the center: a power of two with max |c| / s_c <= 32767
+    double m = 0.0;
+    for (int k = threadIdx.x; k < d; k += blockDim.x) m = fmax(m, fabs(static_cast<double>(X[last * d + k])));
+    m = warp_max(m);
+    if (lane == 0) wred[warp][0] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double mm = 0.0;
+        for (int w = 0; w < nw; ++w) mm = fmax(mm, wred[w][0]);
+        cmax_s = mm;
+    }
+    __syncthreads();
+    const double cmax = cmax_s;
+    int e = 0;
+    frexp(cmax / 32767.0, &e);  // cmax / 32767 < 2^e
+    const bool cok = cmax < 1e30 && (cmax == 0.0 || cmax > 1e-30);
+    const double sc = cok && cmax > 0.0 ? ldexp(1.0, e) : 1.0, inv = 1.0 / sc;
+    double e2 = 0.0, n2 = 0.0;
+    for (int k = threadIdx.x; k < NQ * 128; k += blockDim.x) {
+        const double v = k < d ? static_cast<double>(X[last * d + k]) : 0.0;
+        double qv = cok ? rint(v * inv) : 0.0;
+        qv = fmin(fmax(qv, -32767.0), 32767.0);
+        qc[k] = static_cast<short>(qv);
+        const double df = v - qv * sc;
+        e2 += df * df;
+        n2 += qv * qv;  // exact: integers < 2^53
+    }
+    e2 = warp_sum(e2);
+    n2 = warp_sum(n2);
+    __syncthreads();  // wred reuse
+    if (lane == 0) {
+        wred[warp][0] = e2;
+        wred[warp][1] = n2;
+    }
+    __syncthreads();
+    double ec2 = 0.0, ncq = 0.0;
+    for (int w = 0; w < nw; ++w) {
+        ec2 += wred[w][0];
+        ncq += wred[w][1];
+    }
+    const double ec = cok ? sqrt(ec2) * (1.0 + 1e-12) + 1e-300 : kPosInf;
+    const double sc2n = sc * sc * ncq;
+    int qlo[NQ], qhi[NQ];
+    bool qin[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const int ch = lane + 32 * q;
+        qin[q] = ch * 4 < dp;
+        const int k = qin[q] ? 4 * ch : 0;
+        qlo[q] = qin[q] ? (static_cast<unsigned short>(qc[k]) | (static_cast<int>(qc[k + 1]) << 16)) : 0;
+        qhi[q] = qin[q] ? (static_cast<unsigned short>(qc[k + 2]) | (static_cast<int>(qc[k + 3]) << 16)) : 0;
+    }
+    const unsigned cnt = *count;
+    const unsigned stride = gridDim.x * nw * 32u;
+    unsigned b0 = (blockIdx.x * nw + warp) * 32u;
+    uint32_t mine = 0;
+    float2 my_se = make_float2(0.f, 0.f);
+    double my_d2 = 0.0;
+    int my_qn = 0;
+    if (b0 < cnt && lane < static_cast<int>(min(32u, cnt - b0))) {
+        mine = list[b0 + lane];
+        my_se = se[mine];
+        my_d2 = dist2[mine];
+        my_qn = qn[mine];
+    }
+    const unsigned lt = (1u << lane) - 1u;
+    for (; b0 < cnt; b0 += stride) {
+        const unsigned nb = cnt - b0 < 32u ? cnt - b0 : 32u;
+        constexpr int RB = NQ == 1 ? 32 : 16;
+        int part[32];
+        const unsigned b1 = b0 + stride;
+        uint32_t nmine = 0;
+        float2 nse = make_float2(0.f, 0.f);
+        double nd2 = 0.0;
+        int nqn = 0;
+#pragma unroll
+        for (int g = 0; g < 32; g += RB) {
+            int raw[RB][NQ];
+#pragma unroll
+            for (int j = 0; j < RB; ++j) {
+                // rows past the batch read row 0 (harmless; their lanes are ignored)
+                const long long row = __shfl_sync(0xffffffffu, mine, g + j);
+#pragma unroll
+                for (int q = 0; q < NQ; ++q)
+                    raw[j][q] = qin[q] ? __ldcs(reinterpret_cast<const int*>(Xq + row * dp + 4 * (lane + 32 * q))) : 0;
+            }
+            if (g == 0 && b1 < cnt && lane < static_cast<int>(min(32u, cnt - b1))) {
+                nmine = list[b1 + lane];
+                nse = se[nmine];
+                nd2 = dist2[nmine];
+                nqn = qn[nmine];
+            }
+#pragma unroll
+            for (int j = 0; j < RB; ++j) part[g + j] = dp2a_row<NQ>(raw[j], qlo, qhi);
+        }
+        // lane l gets the dot of row l (exact integer sums)
+#pragma unroll
+        for (int w = 16; w >= 1; w >>= 1) {
+            const bool hi = lane & w;
+#pragma unroll
+            for (int i = 0; i < w; ++i) {
+                const int send = hi ? part[i] : part[i + w];
+                const int keep = hi ? part[i + w] : part[i];
+                part[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+            }
+        }
+        bool need = false;
+        if (lane < static_cast<int>(nb)) {
+            const double sx = static_cast<double>(my_se.x);
+            const double t1 = sx * sx * static_cast<double>(my_qn);
+            const double t2 = 2.0 * sx * sc * static_cast<double>(part[0]);
+            const double a2 = (t1 - t2) + sc2n;
+            const double a2lo = a2 - 4.440892098500626e-16 * (t1 + fabs(t2) + sc2n);  // 2^-51
+            const double lo = sqrt(fmax(a2lo, 0.0)) * (1.0 - 2.220446049250313e-16) - static_cast<double>(my_se.y) - ec;
+            need = !(lo > 0.0 && lo * lo * (1.0 - 1e-12) >= my_d2);
+        }
+        const unsigned sv = __ballot_sync(0xffffffffu, need);
+        if (sv) {
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(surv_count, static_cast<unsigned>(__popc(sv)));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (need) surv[base + __popc(sv & lt)] = mine;
+        }
+        mine = nmine;
+        my_se = nse;
+        my_d2 = nd2;
+        my_qn = nqn;
+    }
+}
+
+// Prune + integer filter in one persistent pass (the default step): warps
+// walk 256-point tiles (grid-stride), test every point of the tile with the
+// triangle bound of pp_prune_kernel, compact the tile's candidates in a
+// per-warp shared list and filter them right away with the int8 rows (as
+// pp_filter_i8_kernel). The prune's global candidate list, its atomics and
+// one kernel boundary go away, and a warp's next tile is independent of
+// the others (no CTA-wide barrier in the loop). Each tile's dist2 sum (a
+// tree) goes to tsum / tbs; the exact pass adjusts tsum by its updates
+// (<= 256 per tile) and pp_pick_kernel folds the tiles into chunk sums.
+constexpr int kTile = 256;
+template <typename T, int NQ>
+__global__ void __launch_bounds__(256, NQ == 1 ? 3 : 2) pp_scan_kernel(const T* __restrict__ X, const int8_t* __restrict__ Xq,
+                                                         const float2* __restrict__ se, const int* __restrict__ qn,
+                                                         long long N, int d, int dp,
+                                                         const uint32_t* __restrict__ chosen, int t,
+                                                         const double* __restrict__ dist2,
+                                                         const uint32_t* __restrict__ near,
+                                                         const double* __restrict__ dc, double* __restrict__ tsum,
+                                                         double* __restrict__ tbs, uint32_t* __restrict__ surv,
+                                                         unsigned* __restrict__ surv_count,
+                                                         unsigned long long* __restrict__ stats) {
+    pdl_wait();
+    pdl_launch_dependents();
+    __shared__ short qc[NQ * 128];
+    __shared__ double wred[8][2];
+    __shared__ double cmax_s;
+    __shared__ uint32_t tlist[8][kTile];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long last = chosen[t];
+    // the new center, quantised to int16 (see pp_filter_i8_kernel)
+    double m = 0.0;
+    for (int k = threadIdx.x; k < d; k += 256) m = fmax(m, fabs(static_cast<double>(X[last * d + k])));
+    m = warp_max(m);
+    if (lane == 0) wred[warp][0] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double mm = 0.0;
+        for (int w = 0; w < 8; ++w) mm = fmax(mm, wred[w][0]);
+        cmax_s = mm;
+    }
+    __syncthreads();
+    const double cmax = cmax_s;
+    int e = 0;
+    frexp(cmax / 32767.0, &e);
+    const bool cok = cmax < 1e30 && (cmax == 0.0 || cmax > 1e-30);
+    const double sc = cok && cmax > 0.0 ? ldexp(1.0, e) : 1.0, inv = 1.0 / sc;
+    double e2 = 0.0, n2 = 0.0;
+    for (int k = threadIdx.x; k < NQ * 128; k += 256) {
+        const double v = k < d ? static_cast<double>(X[last * d + k]) : 0.0;
+        double qv = cok ? rint(v * inv) : 0.0;
+        qv = fmin(fmax(qv, -32767.0), 32767.0);
+        qc[k] = static_cast<short>(qv);
+        const double df = v - qv * sc;
+        e2 += df * df;
+        n2 += qv * qv;
+    }
+    e2 = warp_sum(e2);
+    n2 = warp_sum(n2);
+    __syncthreads();
+    if (lane == 0) {
+        wred[warp][0] = e2;
+        wred[warp][1] = n2;
+    }
+    __syncthreads();
+    double ec2 = 0.0, ncq = 0.0;
+    for (int w = 0; w < 8; ++w) {
+        ec2 += wred[w][0];
+        ncq += wred[w][1];
+    }
+    const double ec = cok ? sqrt(ec2) * (1.0 + 1e-12) + 1e-300 : kPosInf;
+    const double sc2n = sc * sc * ncq;
+    int qlo[NQ], qhi[NQ];
+    bool qin[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const int ch = lane + 32 * q;
+        qin[q] = ch * 4 < dp;
+        const int k = qin[q] ? 4 * ch : 0;
+        qlo[q] = qin[q] ? (static_cast<unsigned short>(qc[k]) | (static_cast<int>(qc[k + 1]) << 16)) : 0;
+        qhi[q] = qin[q] ? (static_cast<unsigned short>(qc[k + 2]) | (static_cast<int>(qc[k + 3]) << 16)) : 0;
+    }
+    uint32_t* const wl = tlist[warp];
+    const unsigned lt = (1u << lane) - 1u;
+    const long long ntile = (N + kTile - 1) / kTile;
+    unsigned long long ncand_tot = 0;
+    for (long long tile = static_cast<long long>(blockIdx.x) * 8 + warp; tile < ntile;
+         tile += static_cast<long long>(gridDim.x) * 8) {
+        // prune the tile (kmeans.cpp:38 can only fire where the triangle bound fails)
+        constexpr int kPT = kTile / 32;
+        const long long b = tile * kTile + lane;
+        double D[kPT];
+        uint32_t nr[kPT];
+#pragma unroll
+        for (int j = 0; j < kPT; ++j) {
+            const long long p = b + 32 * j;
+            D[j] = p < N ? dist2[p] : 0.0;
+            nr[j] = p < N && t > 0 ? near[p] : 0u;
+        }
+        double ts = 0.0;
+        unsigned nc = 0;
+#pragma unroll
+        for (int j = 0; j < kPT; ++j) {
+            const long long p = b + 32 * j;
+            ts += D[j];
+            bool need = p < N;
+            if (need && t > 0 && D[j] < kPosInf) {
+                const double C = dc[nr[j]];
+                if (C * (1.0 - 1e-12) >= 2.0 * sqrt(D[j]) * (1.0 + 1e-9)) need = false;
+            }
+            const unsigned mj = __ballot_sync(0xffffffffu, need);
+            if (need) wl[nc + __popc(mj & lt)] = static_cast<uint32_t>(p);
+            nc += __popc(mj);
+        }
+        ts = warp_sum(ts);
+        if (lane == 0) {
+            tsum[tile] = ts;
+            tbs[tile] = ts;
+        }
+        ncand_tot += nc;
+        __syncwarp();
+        // filter the tile's candidates, 32 rows per batch
+        for (unsigned b0 = 0; b0 < nc; b0 += 32u) {
+            const unsigned nb = nc - b0 < 32u ? nc - b0 : 32u;
+            const uint32_t mine = wl[b0 + (lane < static_cast<int>(nb) ? lane : 0)];
+            const float2 my_se = se[mine];
+            const double my_d2 = dist2[mine];
+            const int my_qn = qn[mine];
+            constexpr int RB = NQ == 1 ? 32 : 16;
+            int part[32];
+#pragma unroll
+            for (int g = 0; g < 32; g += RB) {
+                int raw[RB][NQ];
+#pragma unroll
+                for (int j = 0; j < RB; ++j) {
+                    const long long row = __shfl_sync(0xffffffffu, mine, g + j);
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q)
+                        raw[j][q] =
+                            qin[q] && (g + j) < static_cast<int>(nb)
+                                ? __ldcs(reinterpret_cast<const int*>(Xq + row * dp + 4 * (lane + 32 * q)))
+                                : 0;
+                }
+#pragma unroll
+                for (int j = 0; j < RB; ++j) part[g + j] = dp2a_row<NQ>(raw[j], qlo, qhi);
+            }
+#pragma unroll
+            for (int w = 16; w >= 1; w >>= 1) {
+                const bool hi = lane & w;
+#pragma unroll
+                for (int i = 0; i < w; ++i) {
+                    const int send = hi ? part[i] : part[i + w];
+                    const int keep = hi ? part[i + w] : part[i];
+                    part[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+                }
+            }
+            bool need = false;
+            if (lane < static_cast<int>(nb)) {
+                const double sx = static_cast<double>(my_se.x);
+                const double t1 = sx * sx * static_cast<double>(my_qn);
+                const double t2 = 2.0 * sx * sc * static_cast<double>(part[0]);
+                const double a2 = (t1 - t2) + sc2n;
+                const double a2lo = a2 - 4.440892098500626e-16 * (t1 + fabs(t2) + sc2n);  // 2^-51
+                const double lo =
+                    sqrt(fmax(a2lo, 0.0)) * (1.0 - 2.220446049250313e-16) - static_cast<double>(my_se.y) - ec;
+                need = !(lo > 0.0 && lo * lo * (1.0 - 1e-12) >= my_d2);
+            }
+            const unsigned sv = __ballot_sync(0xffffffffu, need);
+            if (sv) {
+                unsigned base = 0;
+                if (lane == 0) base = atomicAdd(surv_count, static_cast<unsigned>(__popc(sv)));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (need) surv[base + __popc(sv & lt)] = mine;
+            }
+        }
+        __syncwarp();
+    }
+    if (stats && lane == 0 && ncand_tot) atomicAdd(stats, ncand_tot);
+}
+
 // dc[j] = |x_{chosen[j]} - x_{chosen[t]}| for j < t (fp64, one warp per j)
 template <typename T>
 __global__ void __launch_bounds__(256) seed_dist_kernel(const T* __restrict__ X, int d,
                                                         const uint32_t* __restrict__ chosen, int t,
-                                                        double* __restrict__ dc) {
+                                                        double* __restrict__ dc, unsigned* __restrict__ surv_count) {
     pdl_wait();
     pdl_launch_dependents();
+    if (surv_count && blockIdx.x == 0 && threadIdx.x == 0) *surv_count = 0u;  // this step's filter survivors
     const int j = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (j >= t) return;
     const long long a = chosen[j], b = chosen[t];
@@ -736,20 +1130,32 @@ __device__ __forceinline__ longlong2 par_clamp(ParInc v) {
 // the actual binade, so the result is exact regardless.
 
 __global__ void fold_chunk_sum_kernel(const double* __restrict__ x, long long N, double* __restrict__ csum,
-                                      double* __restrict__ bsum) {
+                                      double* __restrict__ bsum, double* __restrict__ tsum,
+                                      double* __restrict__ tbs) {
     pdl_wait();
     pdl_launch_dependents();
+    // 256 threads: warp w sums tile 8 c + w (tile sums for pp_scan_kernel's
+    // bookkeeping), thread 0 the chunk
     __shared__ double red[8];
-    const long long b = static_cast<long long>(blockIdx.x) * kFoldChunk;
-    const long long e = min(N, b + kFoldChunk);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long b = static_cast<long long>(blockIdx.x) * kFoldChunk + warp * 256;
     double s = 0.0;
-    for (long long i = b + threadIdx.x; i < e; i += blockDim.x) s += x[i];
+    for (int j = 0; j < 8; ++j) {
+        const long long i = b + lane + 32 * j;
+        s += i < N ? x[i] : 0.0;
+    }
     s = warp_sum(s);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    if (lane == 0) {
+        red[warp] = s;
+        if (tsum) {
+            tsum[blockIdx.x * 8LL + warp] = s;
+            tbs[blockIdx.x * 8LL + warp] = s;
+        }
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         double t = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        for (int w = 0; w < 8; ++w) t += red[w];
         csum[blockIdx.x] = t;
         bsum[blockIdx.x] = t;
     }
@@ -1356,10 +1762,11 @@ __global__ void __launch_bounds__(kWalkThreads) pp_walk_pick_kernel(
 constexpr int kPickThreads = 1024;
 __global__ void __launch_bounds__(kPickThreads) pp_pick_kernel(
     double* __restrict__ dist2, unsigned char* __restrict__ used, long long N, int nch,
-    const double* __restrict__ csum, const double* __restrict__ bsum, double* __restrict__ qbuf,
+    double* __restrict__ csum, double* __restrict__ bsum, double* __restrict__ qbuf,
     int* __restrict__ skip, unsigned* __restrict__ cand_count, const unsigned long long* __restrict__ raw, int n_raw,
     int* __restrict__ draw_counter, uint32_t* __restrict__ chosen, int t, unsigned* __restrict__ n_fallback,
-    double slack, const unsigned* __restrict__ surv_count, unsigned long long* __restrict__ stats) {
+    double slack, const unsigned* __restrict__ surv_count, unsigned long long* __restrict__ stats, int qsmem,
+    const double* __restrict__ tsum, const double* __restrict__ tbs) {
     pdl_wait();
     pdl_launch_dependents();
     if (stats && threadIdx.x == 0) {  // candidates and exact folds of this step (LCN_TIMING)
@@ -1368,6 +1775,8 @@ __global__ void __launch_bounds__(kPickThreads) pp_pick_kernel(
     }
     __shared__ double red[kPickThreads / 32], bred[kPickThreads / 32];
     __shared__ double carry_s, bs_s;
+    extern __shared__ __align__(16) unsigned char pdyn[];
+    if (qsmem) qbuf = reinterpret_cast<double*>(pdyn);  // the chunk prefix sums stay on chip
     __shared__ int cstar_s, istar_s;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr double u = 1.1102230246251565e-16;  // 2^-53
@@ -1382,8 +1791,22 @@ __global__ void __launch_bounds__(kPickThreads) pp_pick_kernel(
     // and the sum of the pre-update sums
     for (int c0 = 0; c0 < nch; c0 += kPickThreads) {
         const int c = c0 + threadIdx.x;
-        const double v = c < nch ? csum[c] : 0.0;
-        const double bv = warp_sum(c < nch ? bsum[c] : 0.0);
+        double v = 0.0, bv = 0.0;
+        if (c < nch && tsum) {
+            // pp_scan_kernel's tiles: 8 per chunk; the chunk sums are also
+            // what the exact fold's predictions (fold_round_kernel) read
+#pragma unroll
+            for (int w = 0; w < kFoldChunk / kTile; ++w) {
+                v += tsum[static_cast<long long>(c) * (kFoldChunk / kTile) + w];
+                bv += tbs[static_cast<long long>(c) * (kFoldChunk / kTile) + w];
+            }
+            csum[c] = v;
+            bsum[c] = bv;
+        } else if (c < nch) {
+            v = csum[c];
+            bv = bsum[c];
+        }
+        bv = warp_sum(bv);
         double incl = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -1531,6 +1954,7 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     const bool filt = dp <= kFiltMaxQ * 128 && std::getenv("LCN_PP_NOFILTER") == nullptr;
     DevBuf<unsigned char> Xq(filt ? static_cast<size_t>(N) * dp * qsz : 1);
     DevBuf<float2> se(filt ? static_cast<size_t>(N) : 1);
+    DevBuf<int> qn(filt && i8 ? static_cast<size_t>(N) : 1);
     const int wbuf_bytes = static_cast<int>((static_cast<size_t>(kSurv) * (d + 1) * sizeof(T) + 15) / 16 * 16);
     const int nq = (dp / 4 + 31) / 32;
     // c32 is read for NQ * 128 entries; the per-warp buffers start 16-aligned
@@ -1564,6 +1988,46 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
                    : nq == 2 ? pp_filter_kernel<T, int8_t, 2>
                    : nq == 3 ? pp_filter_kernel<T, int8_t, 3>
                              : pp_filter_kernel<T, int8_t, 4>;
+    using FiQ = void (*)(const T*, const int8_t*, const float2*, const int*, int, int, const uint32_t*, int,
+                         const double*, const uint32_t*, const unsigned*, uint32_t*, unsigned*);
+    const FiQ fi_q = nq == 1 ? pp_filter_i8_kernel<T, 1>
+                   : nq == 2 ? pp_filter_i8_kernel<T, 2>
+                   : nq == 3 ? pp_filter_i8_kernel<T, 3>
+                             : pp_filter_i8_kernel<T, 4>;
+    int fi_grid = ctx.num_sms;
+    {
+        int occ = 1;
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fi_q, 128, 0));
+        fi_grid = std::max(1, occ) * ctx.num_sms;
+    }
+    // LCN_PP_SCAN=1: prune + int8 filter in one persistent pass (measured
+    // slower than the separate launches: 38.8 vs 12.4 + 16.8 us per step)
+    const char* scenv = std::getenv("LCN_PP_SCAN");
+    const bool scan = filt && i8 && split && scenv && scenv[0] == '1';
+    using ScQ = void (*)(const T*, const int8_t*, const float2*, const int*, long long, int, int, const uint32_t*, int,
+                         const double*, const uint32_t*, const double*, double*, double*, uint32_t*, unsigned*,
+                         unsigned long long*);
+    const ScQ sc_q = nq == 1 ? pp_scan_kernel<T, 1>
+                   : nq == 2 ? pp_scan_kernel<T, 2>
+                   : nq == 3 ? pp_scan_kernel<T, 3>
+                             : pp_scan_kernel<T, 4>;
+    int sc_grid = ctx.num_sms;
+    {
+        int occ = 1;
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sc_q, 256, 0));
+        sc_grid = std::max(1, occ) * ctx.num_sms;
+    }
+    const long long ntile = static_cast<long long>(nch) * (kFoldChunk / kTile);
+    DevBuf<double> tsum(scan ? ntile : 1), tbs(scan ? ntile : 1);
+    const size_t el_smem = static_cast<size_t>(d) * 8;
+    if (el_smem > 48 * 1024) allow_max_dyn_smem(pp_exact_lane_kernel<T>);
+    const int el_grid = 2 * ctx.num_sms;
+    // the survivors' exact pass: smem-staged rows (default) or one survivor
+    // per thread (LCN_PP_EXACT=lane); LCN_PP_EXACT_CTAS = CTAs per SM
+    const char* xenv = std::getenv("LCN_PP_EXACT");
+    const bool exact_lane = xenv && std::string(xenv) == "lane";
+    const char* xgenv = std::getenv("LCN_PP_EXACT_CTAS");
+    const int sx_grid = xgenv ? std::max(1, std::min(ex_occ, std::atoi(xgenv))) * ctx.num_sms : ex_grid;
     DevBuf<uint32_t> surv(filt && split ? N : 1);
     DevBuf<unsigned> scnt(1);
     scnt.zero(s);
@@ -1580,7 +2044,7 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     if (filt) {
         if (i8)
             pp_i8_prep_kernel<T><<<ceil_div(N, 8), 256, 0, s>>>(X, N, d, dp, reinterpret_cast<int8_t*>(Xq.get()),
-                                                               se.get());
+                                                               se.get(), qn.get());
         else
             pp_half_prep_kernel<T><<<ceil_div(N, 8), 256, 0, s>>>(X, N, d, dp, reinterpret_cast<__half*>(Xq.get()),
                                                                  se.get());
@@ -1604,6 +2068,8 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     const char* senv = std::getenv("LCN_PP_CERT_SLACK");  // test hook: widen the certificate (more fallbacks)
     const double slack = senv ? std::max(1.0, std::atof(senv)) : 1.0;
     DevBuf<double> fsum(nch), bsum(nch);
+    const size_t pk_smem = static_cast<size_t>(nch) * 8 <= 160 * 1024 ? static_cast<size_t>(nch) * 8 : 0;
+    if (pk_smem > 48 * 1024) allow_max_dyn_smem(pp_pick_kernel);
     DevBuf<int> skip(1);
     DevBuf<unsigned> nfall(1);
     const bool timing = std::getenv("LCN_TIMING") != nullptr;
@@ -1627,18 +2093,36 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     const bool pdl = !(penv && penv[0] == '0');
     const dim3 b256(256), b128(128);
     for (int t = 1; t < k; ++t) {
-        if (t > 1) launch_pdl(seed_dist_kernel<T>, dim3(ceil_div(t - 1, 8)), b256, 0, s, pdl, X, d, d_chosen, t - 1, dc.get());
-        launch_pdl(pp_prune_kernel, dim3(nch), b256, 0, s, pdl, N, t - 1, dist2.get(), near.get(), dc.get(), list.get(),
-                   cnt.get(), csum.get(), scnt.get(), bsum.get());
+        if (t > 1)
+            launch_pdl(seed_dist_kernel<T>, dim3(ceil_div(t - 1, 8)), b256, 0, s, pdl, X, d, d_chosen, t - 1, dc.get(),
+                       scnt.get());
+        double* xsums = csum.get();  // the exact pass's sum corrections: chunk or tile sums
+        int xshift = 11;
+        if (scan) {
+            launch_pdl(sc_q, dim3(sc_grid), b256, 0, s, pdl, X, reinterpret_cast<const int8_t*>(Xq.get()), se.get(),
+                       qn.get(), N, d, dp, d_chosen, t - 1, dist2.get(), near.get(), dc.get(), tsum.get(), tbs.get(),
+                       surv.get(), scnt.get(), timing ? pstats.get() : nullptr);
+            xsums = tsum.get();
+            xshift = 8;
+        } else {
+            launch_pdl(pp_prune_kernel, dim3(nch), b256, 0, s, pdl, N, t - 1, dist2.get(), near.get(), dc.get(),
+                       list.get(), cnt.get(), csum.get(), scnt.get(), bsum.get());
+        }
         if (filt && split) {
-            if (i8)
-                launch_pdl(fs_q, dim3(fs_grid), b128, 0, s, pdl, X, reinterpret_cast<const int8_t*>(Xq.get()), se.get(),
-                           d, dp, d_chosen, t - 1, dist2.get(), list.get(), cnt.get(), surv.get(), scnt.get());
+            if (scan) {
+            } else if (i8)
+                launch_pdl(fi_q, dim3(fi_grid), b128, 0, s, pdl, X, reinterpret_cast<const int8_t*>(Xq.get()), se.get(),
+                           qn.get(), d, dp, d_chosen, t - 1, dist2.get(), list.get(), cnt.get(), surv.get(),
+                           scnt.get());
             else
                 launch_pdl(fs_h, dim3(fs_grid), b128, 0, s, pdl, X, reinterpret_cast<const __half*>(Xq.get()), se.get(),
                            d, dp, d_chosen, t - 1, dist2.get(), list.get(), cnt.get(), surv.get(), scnt.get());
-            launch_pdl(pp_exact_kernel<T>, dim3(ex_grid), dim3(ex_warps * 32), ex_smem, s, pdl, X, d, d_chosen, t - 1,
-                       dist2.get(), near.get(), surv.get(), scnt.get(), csum.get());
+            if (exact_lane)
+                launch_pdl(pp_exact_lane_kernel<T>, dim3(el_grid), b256, el_smem, s, pdl, X, d, d_chosen, t - 1,
+                           dist2.get(), near.get(), surv.get(), scnt.get(), xsums, xshift);
+            else
+                launch_pdl(pp_exact_kernel<T>, dim3(sx_grid), dim3(ex_warps * 32), ex_smem, s, pdl, X, d, d_chosen,
+                           t - 1, dist2.get(), near.get(), surv.get(), scnt.get(), xsums, xshift);
         } else if (filt && i8)
             launch_pdl(fx_q, dim3(fx_grid), dim3(ex_warps * 32), fx_smem, s, pdl, X,
                        reinterpret_cast<const int8_t*>(Xq.get()), se.get(), d, dp, d_chosen, t - 1, dist2.get(),
@@ -1649,7 +2133,7 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
                        near.get(), list.get(), cnt.get(), wbuf_bytes, csum.get());
         else
             launch_pdl(pp_exact_kernel<T>, dim3(ex_grid), dim3(ex_warps * 32), ex_smem, s, pdl, X, d, d_chosen, t - 1,
-                       dist2.get(), near.get(), list.get(), cnt.get(), csum.get());
+                       dist2.get(), near.get(), list.get(), cnt.get(), csum.get(), 11);
 #ifdef LCN_WALK_PROFILE
         if (std::getenv("LCN_WALK_STATS") && (t % 256 == 0 || t == k - 1)) {
             unsigned hc = 0;
@@ -1663,16 +2147,21 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
                          100.0 * hc / N, hs);
         }
 #endif
-        // the first pass moves every point off +inf: its chunk sums are taken
-        // afresh (later steps: prune sums minus the exact pass's updates)
+        // the first pass moves every point off +inf: its chunk (and tile)
+        // sums are taken afresh (later steps: pre-update sums corrected by
+        // the exact pass's updates)
         if (t == 1)
-            launch_pdl(fold_chunk_sum_kernel, dim3(nch), b256, 0, s, pdl, dist2.get(), N, csum.get(), bsum.get());
+            launch_pdl(fold_chunk_sum_kernel, dim3(nch), b256, 0, s, pdl, dist2.get(), N, csum.get(), bsum.get(),
+                       scan ? tsum.get() : static_cast<double*>(nullptr),
+                       scan ? tbs.get() : static_cast<double*>(nullptr));
         const int* skp = nullptr;
         if (fast) {
-            launch_pdl(pp_pick_kernel, dim3(1), dim3(kPickThreads), 0, s, pdl, dist2.get(), used.get(), N, nch,
+            launch_pdl(pp_pick_kernel, dim3(1), dim3(kPickThreads), pk_smem, s, pdl, dist2.get(), used.get(), N, nch,
                        csum.get(), bsum.get(), fsum.get(), skip.get(), cnt.get(), d_raw.get(),
                        static_cast<int>(raw.size()), counter.get(), d_chosen, t, nfall.get(), slack,
-                       filt && split ? scnt.get() : nullptr, timing ? pstats.get() : nullptr);
+                       filt && split ? scnt.get() : nullptr, timing ? pstats.get() : nullptr, pk_smem ? 1 : 0,
+                       scan ? tsum.get() : static_cast<const double*>(nullptr),
+                       scan ? tbs.get() : static_cast<const double*>(nullptr));
             skp = skip.get();
         }
         launch_pdl(fold_round_kernel, dim3(nch), b256, 0, s, pdl, dist2.get(), N, csum.get(), ebin.get(), R.get(),

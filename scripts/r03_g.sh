@@ -1,0 +1,8 @@
+# fused per-chunk seeding step kernel
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "kmeans_pp or lloyd or lsh_buckets" > gpurun_out/tests_g.log 2>&1; echo TESTS $? >> gpurun_out/tests_g.log
+LCN_PP_FILTER=f16 timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "kmeans_pp" >> gpurun_out/tests_g.log 2>&1; echo TESTS_F16 $? >> gpurun_out/tests_g.log
+LCN_PP_NOFILTER=1 timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "kmeans_pp" >> gpurun_out/tests_g.log 2>&1; echo TESTS_NOFILT $? >> gpurun_out/tests_g.log
+timeout 300 python scripts/timeline.py 2000000 4096 2>&1 | grep -v Warn > gpurun_out/timeline_g.log
+LCN_PP_PDL=0 timeout 300 python scripts/timeline.py 2000000 4096 2>&1 | grep -v Warn > gpurun_out/timeline_g0.log
+LCN_TIMING=1 PROBE_BUILDS=2 timeout 300 python scripts/probe.py c3 1.0 1 > gpurun_out/timing_g.log 2>&1
