@@ -1571,6 +1571,8 @@ void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed,
     // U = k(X_p, L) (n x l), V^T = k(X_q, L) (m x l), A = k(L, L) with division.
     op.U64.resize(std::max<size_t>(n * l, 1));
     DevBuf<double> Vt(std::max<size_t>(m * l, 1)), A(l * l);
+    {
+    PhaseTimer ptuv(ctx, "  U, V point x landmark blocks");
     if (use_tc_build(op, 2)) {  // point x landmark blocks on the tensor cores (3xTF32)
         const double* sq = union_sqnorms(op, s);
         DevBuf<double> lsq(l);
@@ -1611,6 +1613,9 @@ void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed,
         exp_block(op.U64.get(), op.P(), n, nrm, op.L.get(), l, lnorm.get(), false);
         exp_block(Vt.get(), op.Q(), m, nrm ? nrm + n : nullptr, op.L.get(), l, lnorm.get(), false);
     }
+    }
+    std::optional<PhaseTimer> pta;
+    pta.emplace(ctx, "  A, max |V|, host copies");
     exp_block(A.get(), op.L.get(), l, lnorm.get(), op.L.get(), l, lnorm.get(), true);
     if (read_flag(ctx, bad)) throw Status(2, "cosine-derived cost undefined for zero vectors");
 
@@ -1625,6 +1630,7 @@ void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed,
     double vmaxd;
     std::memcpy(&vmaxd, &vbits, 8);
     const LD v_scale = std::max<LD>(static_cast<LD>(vmaxd), 1e-300L);
+    pta.reset();
     std::vector<LD> a(l * l);
     for (size_t i = 0; i < l * l; ++i) a[i] = static_cast<LD>(hA[i]);
     LD trace = 0.0L;

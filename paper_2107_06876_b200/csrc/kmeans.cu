@@ -54,15 +54,17 @@ template <typename T>
 __global__ void __launch_bounds__(256) assign_exact_kernel(const T* __restrict__ X, long long N, int d,
                                                            const double* __restrict__ Cm, int k,
                                                            uint32_t* __restrict__ out, double* __restrict__ best_out,
-                                                           const uint32_t* __restrict__ rows) {
+                                                           const uint32_t* __restrict__ rows,
+                                                           float* __restrict__ ub = nullptr,
+                                                           float* __restrict__ lb = nullptr) {
     __shared__ double As[KC][TP + 1];
     __shared__ double Bs[KC][TC + 1];
     const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
     const long long p0 = static_cast<long long>(blockIdx.x) * TP;
-    double best[4];
+    double best[4], sec[4];  // sec: second smallest fold (Lloyd's lower bound)
     int arg[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) { best[i] = kPosInf; arg[i] = 0; }
+    for (int i = 0; i < 4; ++i) { best[i] = sec[i] = kPosInf; arg[i] = 0; }
     for (int c0 = 0; c0 < k; c0 += TC) {
         double acc[4][4];
 #pragma unroll
@@ -81,19 +83,24 @@ __global__ void __launch_bounds__(256) assign_exact_kernel(const T* __restrict__
             int c = c0 + tx + 16 * j;
             if (c < k)
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    if (acc[i][j] < best[i]) { best[i] = acc[i][j]; arg[i] = c; }
+                for (int i = 0; i < 4; ++i) {
+                    if (acc[i][j] < best[i]) { sec[i] = best[i]; best[i] = acc[i][j]; arg[i] = c; }
+                    else if (acc[i][j] < sec[i]) sec[i] = acc[i][j];
+                }
         }
     }
-    // (value, index) lexicographic min over the 16 threads sharing a point.
+    // (value, index) lexicographic min over the 16 threads sharing a point;
+    // the second smallest value of the multiset alongside.
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        double b = best[i];
+        double b = best[i], s2 = sec[i];
         int a = arg[i];
 #pragma unroll
         for (int o = 8; o > 0; o >>= 1) {
             double ob = __shfl_xor_sync(0xffffffffu, b, o);
+            double os = __shfl_xor_sync(0xffffffffu, s2, o);
             int oa = __shfl_xor_sync(0xffffffffu, a, o);
+            s2 = fmin(fmin(s2, os), fmax(b, ob));
             if (ob < b || (ob == b && oa < a)) { b = ob; a = oa; }
         }
         long long p = p0 + ty + 16 * i;
@@ -101,6 +108,10 @@ __global__ void __launch_bounds__(256) assign_exact_kernel(const T* __restrict__
             const long long q = rows ? rows[p] : p;
             out[q] = static_cast<uint32_t>(a);
             if (best_out) best_out[q] = b;
+            if (ub) {  // folds are within 1e-12 (relative) of the true squares
+                ub[q] = __double2float_ru(__dsqrt_ru(b * (1.0 + 1e-12)));
+                lb[q] = __double2float_rd(__dsqrt_rd(s2 * (1.0 - 1e-12)));
+            }
         }
     }
 }
@@ -2277,7 +2288,8 @@ __global__ void farthest_partial_kernel(const T* __restrict__ X, long long N, in
 template <typename T>
 __global__ void reseed_apply_kernel(const T* __restrict__ X, int d, const double* __restrict__ pval,
                                     const long long* __restrict__ pidx, int nparts, double* __restrict__ ctr,
-                                    uint32_t* __restrict__ assign, int* __restrict__ counts, int c) {
+                                    uint32_t* __restrict__ assign, int* __restrict__ counts, int c,
+                                    float* __restrict__ lb = nullptr) {
     __shared__ long long s_arg;
     if (threadIdx.x == 0) {
         double far = -1.0;
@@ -2291,6 +2303,7 @@ __global__ void reseed_apply_kernel(const T* __restrict__ X, int d, const double
         counts[assign[arg]] -= 1;
         assign[arg] = static_cast<uint32_t>(c);
         counts[c] = 1;
+        if (lb) lb[arg] = 0.0f;  // its bound was for another assignment: re-evaluate
     }
     __syncthreads();
     const long long arg = s_arg;
@@ -2506,6 +2519,152 @@ void assign_device(Ctx& ctx, const T* X, long long N, int d, const double* C, in
     LAUNCH_OK("assign_exact_kernel");
 }
 
+// ---- Lloyd with certified distance bounds (Hamerly) ------------------------
+// After a full assignment every point carries ub >= its true distance to the
+// chosen centroid and lb <= its true distance to every other centroid
+// (assign_filter_tc / assign_exact_kernel). A Lloyd update moves centroid c
+// by delta_c, so before the next assignment ub + delta_a and
+// lb - max_{c != a} delta_c still bound the distances, and when
+//   (ub + delta_a) (1 + 1e-9) < (lb - max delta) (1 - 1e-9)
+// no other centroid can reach the assigned one: the reference's fp64 folds
+// (within 1e-12 of the true squares) keep the same strict argmin
+// (kmeans.cpp:76-82), so the point keeps its assignment with no tie possible.
+// A failing point first tightens ub to its current distance (one row read);
+// the rest are re-assigned by the tensor-core filter on a compacted list.
+__global__ void centroid_shift_kernel(const double* __restrict__ cold, const double* __restrict__ cnew, int k, int d,
+                                      double* __restrict__ delta) {
+    const int c = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (c >= k) return;
+    double s2 = 0.0;
+    for (int kk = lane; kk < d; kk += 32) {
+        const double df = cnew[static_cast<long long>(c) * d + kk] - cold[static_cast<long long>(c) * d + kk];
+        s2 += df * df;
+    }
+    s2 = warp_sum(s2);
+    if (lane == 0) delta[c] = s2 > 0.0 ? __dsqrt_ru(s2) * (1.0 + 1e-12) : 0.0;
+}
+
+// largest and second-largest shift and the argmax (one CTA)
+__global__ void __launch_bounds__(1024) shift_max_kernel(const double* __restrict__ delta, int k,
+                                                         double* __restrict__ dstat) {
+    __shared__ double m1s[32], m2s[32];
+    __shared__ int a1s[32];
+    double m1 = -1.0, m2 = -1.0;
+    int a1 = -1;
+    for (int c = threadIdx.x; c < k; c += 1024) {
+        const double v = delta[c];
+        if (v > m1) { m2 = m1; m1 = v; a1 = c; }
+        else if (v > m2) m2 = v;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const double om1 = __shfl_xor_sync(0xffffffffu, m1, o), om2 = __shfl_xor_sync(0xffffffffu, m2, o);
+        const int oa = __shfl_xor_sync(0xffffffffu, a1, o);
+        m2 = fmax(fmax(m2, om2), fmin(m1, om1));
+        if (om1 > m1) { m1 = om1; a1 = oa; }
+    }
+    if ((threadIdx.x & 31) == 0) {
+        m1s[threadIdx.x >> 5] = m1;
+        m2s[threadIdx.x >> 5] = m2;
+        a1s[threadIdx.x >> 5] = a1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double b1 = -1.0, b2 = -1.0;
+        int ba = -1;
+        for (int w = 0; w < 32; ++w) {
+            b2 = fmax(fmax(b2, m2s[w]), fmin(b1, m1s[w]));
+            if (m1s[w] > b1) { b1 = m1s[w]; ba = a1s[w]; }
+        }
+        dstat[0] = fmax(b1, 0.0);
+        dstat[1] = fmax(b2, 0.0);
+        dstat[2] = static_cast<double>(ba);
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) lloyd_bounds_kernel(const T* __restrict__ X, long long N, int d,
+                                                           const double* __restrict__ C,
+                                                           const uint32_t* __restrict__ assign,
+                                                           float* __restrict__ ub, float* __restrict__ lb,
+                                                           const double* __restrict__ delta,
+                                                           const double* __restrict__ dstat,
+                                                           uint32_t* __restrict__ list, unsigned* __restrict__ count) {
+    const int lane = threadIdx.x & 31;
+    const long long p = blockIdx.x * 256LL + threadIdx.x;
+    const double dmax = dstat[0], dmax2 = dstat[1];
+    const int amax = static_cast<int>(dstat[2]);
+    uint32_t a = 0;
+    double U = 0.0, L = 0.0;
+    bool need = false;
+    if (p < N) {
+        a = assign[p];
+        U = static_cast<double>(ub[p]) + delta[a];
+        L = static_cast<double>(lb[p]) - (static_cast<int>(a) == amax ? dmax2 : dmax);
+        need = !(U * (1.0 + 1e-9) < L * (1.0 - 1e-9));
+        if (!need) {
+            ub[p] = __double2float_ru(U);
+            lb[p] = __double2float_rd(L);
+        }
+    }
+    // tighten ub: the current distance to the assigned centroid, one
+    // coalesced row read per failing point (any summation order: within
+    // 1e-12 of the true square)
+    unsigned m = __ballot_sync(0xffffffffu, need);
+    bool still = false;
+    while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        const long long pj = __shfl_sync(0xffffffffu, p, j);
+        const uint32_t aj = __shfl_sync(0xffffffffu, a, j);
+        double s2 = 0.0;
+        for (int kk = lane; kk < d; kk += 32) {
+            const double df = static_cast<double>(X[pj * d + kk]) - C[static_cast<long long>(aj) * d + kk];
+            s2 += df * df;
+        }
+        s2 = warp_sum(s2);
+        if (lane == j) {
+            const double Ut = __dsqrt_ru(s2 * (1.0 + 1e-12));
+            if (Ut * (1.0 + 1e-9) < L * (1.0 - 1e-9)) {
+                ub[p] = __double2float_ru(Ut);
+                lb[p] = __double2float_rd(L);
+            } else {
+                still = true;
+            }
+        }
+    }
+    const unsigned sm = __ballot_sync(0xffffffffu, still);
+    if (sm) {
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(count, static_cast<unsigned>(__popc(sm)));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (still) list[base + __popc(sm & ((1u << lane) - 1u))] = static_cast<uint32_t>(p);
+    }
+}
+
+// Tensor-core assignment of the points rows[0 .. n) (all points when rows is
+// null) with bounds; ambiguous points get the exact scan (and exact bounds).
+template <typename T>
+void assign_bounded(Ctx& ctx, const T* X, long long n, int d, const double* C, int k, uint32_t* out,
+                    const uint32_t* rows, float* ub, float* lb) {
+    cudaStream_t s = ctx.stream;
+    DevBuf<uint32_t> amb(n);
+    DevBuf<unsigned> namb(1);
+    namb.zero(s);
+    if (!assign_filter_tc(ctx, reinterpret_cast<const float*>(X), n, d, C, k, out, amb.get(), namb.get(), nullptr, 0,
+                          rows, ub, lb))
+        throw Status(100, "lloyd bounds: tensor-core filter unavailable for this shape");
+    unsigned h_amb = 0;
+    namb.download(&h_amb, 1, s);
+    ctx.sync();
+    ctx.filter_ambiguous += h_amb;
+    ctx.filter_points += n;
+    if (h_amb)
+        assign_exact_kernel<T><<<ceil_div(static_cast<long long>(h_amb), TP), 256, 0, s>>>(X, h_amb, d, C, k, out,
+                                                                                            nullptr, amb.get(), ub, lb);
+    LAUNCH_OK("assign_exact_kernel (ambiguous, bounds)");
+}
+
 template <typename T>
 void lloyd_device(Ctx& ctx, const T* X, long long N, int d, int k, int iters, uint64_t seed, double* d_ctr,
                   uint32_t* d_assign) {
@@ -2549,8 +2708,42 @@ void lloyd_device(Ctx& ctx, const T* X, long long N, int d, int k, int iters, ui
     DevBuf<double> pval(fparts);
     DevBuf<long long> pidx(fparts);
     std::vector<int> h_counts(k);
+    // certified bounds (Hamerly) on the tensor-core path; LCN_LLOYD_BOUNDS=0
+    // re-assigns every point every iteration
+    const char* benv = std::getenv("LCN_LLOYD_BOUNDS");
+    const char* fsel = std::getenv("LCN_FILTER");
+    const bool bounds = std::is_same<T, float>::value && d <= 128 && N * static_cast<long long>(k) >= (1LL << 22) &&
+                        !(benv && benv[0] == '0') && !(fsel && std::string(fsel) == "fma");
+    DevBuf<float> ub(bounds ? N : 1), lb(bounds ? N : 1);
+    DevBuf<double> cold(bounds ? static_cast<size_t>(k) * d : 1), delta(bounds ? k : 1), dstat(3);
+    DevBuf<uint32_t> blist(bounds ? N : 1);
+    DevBuf<unsigned> bcnt(1);
+    long long reassigned = 0;
+    auto assign_step = [&](bool first) {
+        if (!bounds) {
+            assign_device<T>(ctx, X, N, d, d_ctr, k, d_assign);
+            return;
+        }
+        if (first) {
+            assign_bounded<T>(ctx, X, N, d, d_ctr, k, d_assign, nullptr, ub.get(), lb.get());
+            reassigned += N;
+            return;
+        }
+        bcnt.zero(s);
+        lloyd_bounds_kernel<T><<<ceil_div(N, 256), 256, 0, s>>>(X, N, d, d_ctr, d_assign, ub.get(), lb.get(),
+                                                               delta.get(), dstat.get(), blist.get(), bcnt.get());
+        LAUNCH_OK("lloyd bounds");
+        unsigned h = 0;
+        bcnt.download(&h, 1, s);
+        ctx.sync();
+        reassigned += h;
+        if (h) assign_bounded<T>(ctx, X, h, d, d_ctr, k, d_assign, blist.get(), ub.get(), lb.get());
+    };
     for (int it = 0; it < iters; ++it) {
-        assign_device<T>(ctx, X, N, d, d_ctr, k, d_assign);
+        assign_step(it == 0);
+        if (bounds)
+            CUDA_OK(cudaMemcpyAsync(cold.get(), d_ctr, static_cast<size_t>(k) * d * sizeof(double),
+                                    cudaMemcpyDeviceToDevice, s));
         counts.zero(s);
         count_kernel<<<ceil_div(N, 256), 256, 0, s>>>(d_assign, N, counts.get());
         size_t t1 = tmp.size();
@@ -2565,11 +2758,20 @@ void lloyd_device(Ctx& ctx, const T* X, long long N, int d, int k, int iters, ui
         for (int c = 0; c < k; ++c) {
             if (h_counts[c] != 0) continue;
             farthest_partial_kernel<T><<<fparts, 256, 0, s>>>(X, N, d, d_ctr, d_assign, counts.get(), pval.get(), pidx.get());
-            reseed_apply_kernel<T><<<1, 128, 0, s>>>(X, d, pval.get(), pidx.get(), fparts, d_ctr, d_assign, counts.get(), c);
+            reseed_apply_kernel<T><<<1, 128, 0, s>>>(X, d, pval.get(), pidx.get(), fparts, d_ctr, d_assign, counts.get(), c,
+                                                     bounds ? lb.get() : nullptr);
             LAUNCH_OK("reseed");
         }
+        if (bounds) {
+            centroid_shift_kernel<<<ceil_div(k, 8), 256, 0, s>>>(cold.get(), d_ctr, k, d, delta.get());
+            shift_max_kernel<<<1, 1024, 0, s>>>(delta.get(), k, dstat.get());
+            LAUNCH_OK("centroid shifts");
+        }
     }
-    assign_device<T>(ctx, X, N, d, d_ctr, k, d_assign);
+    assign_step(iters == 0);
+    if (bounds && std::getenv("LCN_TIMING"))
+        std::fprintf(stderr, "[lloyd] N=%lld k=%d: %lld of %lld point assignments re-evaluated (%.1f%%)\n", N, k,
+                     reassigned, N * (iters + 1), 100.0 * reassigned / (static_cast<double>(N) * (iters + 1)));
 }
 
 #define LCNB_INST(T)                                                                                    \

@@ -183,7 +183,8 @@ __global__ void __cluster_dims__(kTCluster, 1, 1) __launch_bounds__(kTThreads, 1
     const float* __restrict__ X, long long N, int d, const unsigned char* __restrict__ tiles,
     const float* __restrict__ ncf, int ntile, const unsigned long long* __restrict__ cmax,
     uint32_t* __restrict__ out, uint32_t* __restrict__ amb, unsigned* __restrict__ namb,
-    float* __restrict__ dbg, int hh_only) {
+    float* __restrict__ dbg, int hh_only, const uint32_t* __restrict__ rows, float* __restrict__ ub,
+    float* __restrict__ lb) {
     // all shared memory is dynamic (no static __shared__): the stage ring must
     // sit on 1024-byte swizzle-atom boundaries of the shared window
     extern __shared__ __align__(1024) unsigned char dyn_raw[];
@@ -231,7 +232,8 @@ __global__ void __cluster_dims__(kTCluster, 1, 1) __launch_bounds__(kTThreads, 1
     const uint32_t tmem = tmem_slot;
     if (eq >= 0) {
         const long long p = p0 + row;
-        const float* xr = X + p * d;
+        // rows: the points of this call are rows[0 .. N) (lloyd's bound-failing list)
+        const float* xr = X + (rows && p < N ? static_cast<long long>(rows[p]) : p) * d;
         for (int c0 = half * (kTD / 2); c0 < (half + 1) * (kTD / 2); c0 += 32) {
             uint32_t vh[32], vl[32];
 #pragma unroll
@@ -387,8 +389,21 @@ __global__ void __cluster_dims__(kTCluster, 1, 1) __launch_bounds__(kTThreads, 1
             const double E = 1.05 * ((dot_rel + 4.0 * u) * x * C + 4.0 * u * C * C + u * u * C * C) +
                              1e-12 * (x + C) * (x + C);
             const double gap = static_cast<double>(v2m) - static_cast<double>(v1m);
-            if (gap > 2.0 * E) out[p] = static_cast<uint32_t>(i1m);
-            else amb[atomicAdd(namb, 1u)] = static_cast<uint32_t>(p);
+            const long long q = rows ? static_cast<long long>(rows[p]) : p;
+            if (gap > 2.0 * E) {
+                out[q] = static_cast<uint32_t>(i1m);
+                if (ub) {
+                    // Lloyd's bounds on true distances (lloyd_device): every
+                    // fold D(x, c) lies within E of |x|^2 + v(c), the fold
+                    // within 1e-12 (relative) of the true square
+                    const double hi = (xn + static_cast<double>(v1m) + E) * (1.0 + 1e-12);
+                    const double lo = (xn + static_cast<double>(v2m) - E) * (1.0 - 1e-12);
+                    ub[q] = __double2float_ru(__dsqrt_ru(fmax(hi, 0.0)));
+                    lb[q] = __double2float_rd(__dsqrt_rd(fmax(lo, 0.0)));
+                }
+            } else {
+                amb[atomicAdd(namb, 1u)] = static_cast<uint32_t>(q);
+            }
         }
         }  // half 0
     }
@@ -406,7 +421,8 @@ __global__ void __cluster_dims__(kTCluster, 1, 1) __launch_bounds__(kTThreads, 1
 // Host side: prepare the centroid tiles and launch. Returns false when the
 // shape is not handled (d > kTD).
 bool assign_filter_tc(Ctx& ctx, const float* X, long long N, int d, const double* C, int k, uint32_t* out,
-                      uint32_t* amb, unsigned* namb, float* dbg_acc, int hh_only) {
+                      uint32_t* amb, unsigned* namb, float* dbg_acc, int hh_only, const uint32_t* rows, float* ub,
+                      float* lb) {
     if (d > kTD || d < 1) return false;
     cudaStream_t s = ctx.stream;
     const int ntile = static_cast<int>(ceil_div(k, kTN));
@@ -425,7 +441,7 @@ bool assign_filter_tc(Ctx& ctx, const float* X, long long N, int d, const double
     // grid: whole clusters (CTAs past N only help stream the centroid stages)
     const long long grid = ceil_div(ceil_div(N, kTM), kTCluster) * kTCluster;
     assign_filter_tc_kernel<<<static_cast<unsigned>(grid), kTThreads, smem, s>>>(
-        X, N, d, tiles.get(), ncf.get(), ntile, cmax.get(), out, amb, namb, dbg_acc, hh_only);
+        X, N, d, tiles.get(), ncf.get(), ntile, cmax.get(), out, amb, namb, dbg_acc, hh_only, rows, ub, lb);
     LAUNCH_OK("assign_filter_tc_kernel");
     return true;
 }

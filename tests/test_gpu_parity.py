@@ -105,6 +105,31 @@ def test_lloyd_filter_bit_exact(ctx, ref):
     assert np.array_equal(c_gpu.view(np.uint64), c_ref.view(np.uint64))
 
 
+def test_lloyd_bounds_bit_exact(ctx, ref):
+    # Lloyd with certified distance bounds (only bound-failing points are
+    # re-assigned) against the reference: N k >= 2^22 with fp32 points
+    x = rng_points(41, 60000, 32, comps=60)
+    c_gpu, a_gpu = lcn.lloyd(ctx, x, 256, 10, 41)
+    c_ref, a_ref = ref.lloyd(x, 256, 10, 41)
+    assert np.array_equal(a_gpu, a_ref)
+    assert np.array_equal(c_gpu.view(np.uint64), c_ref.view(np.uint64))
+
+
+def test_lloyd_bounds_match_full_reassignment(ctx, monkeypatch):
+    # configs[3]-like mixture at 300k points, 1024 centroids: the bounded
+    # iterations give the same assignment and centroid bits as re-assigning
+    # every point every iteration
+    r = np.random.default_rng(43)
+    means = r.standard_normal((300, 128))
+    x = (means[r.integers(0, 300, 300_000)] + 0.5 * r.standard_normal((300_000, 128))).astype(np.float32)
+    x = x.astype(np.float64)
+    c1, a1 = lcn.lloyd(ctx, x, 1024, 10, 43)
+    monkeypatch.setenv("LCN_LLOYD_BOUNDS", "0")
+    c0, a0 = lcn.lloyd(ctx, x, 1024, 10, 43)
+    assert np.array_equal(a1, a0)
+    assert np.array_equal(c1.view(np.uint64), c0.view(np.uint64))
+
+
 def test_lsh_buckets_config0(ctx, ref):
     pr = configs.config0()
     cfg = lcn.LshConfig(pr.bands, 1, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
