@@ -448,7 +448,7 @@ void cross_polytope_buckets_device(Ctx& ctx, const double* X, long long N, int d
 // jobs, together with `extra` (the landmark k-means) when given.
 void lsh_bucket_ids(Ctx& ctx, const double* d_union, const float* d_union32, size_t n, size_t m, size_t d,
                     const LshParams& cfg, std::vector<DevBuf<uint32_t>>& ids, size_t& range,
-                    const std::function<void(Ctx&)>& extra) {
+                    const std::function<void(Ctx&)>& extra, const ExtraSeeding* extra_seed) {
     const size_t N = n + m;
     const int bands = cfg.bands, rows = cfg.rows, buckets = cfg.buckets;
     if (bands < 1 || rows < 1) throw Status(2, "lsh: bands and rows_per_band must be >= 1");
@@ -467,6 +467,31 @@ void lsh_bucket_ids(Ctx& ctx, const double* d_union, const float* d_union32, siz
     // per band: an upper bound on its composite ids (hierarchical leaves can
     // exceed buckets - 1, see hier_assign_device)
     std::vector<double> band_bound(bands, 0.0);
+    // k-means scheme: every band function's k-means++ seeding (and the
+    // landmark k-means', when given) runs as one batched step chain first;
+    // the per-band jobs then run Lloyd from those seeds
+    std::vector<DevBuf<uint32_t>> inits;
+    const bool xseed = extra_seed && extra_seed->k > 0 && static_cast<size_t>(extra_seed->k) <= N && extra_seed->out;
+    if (cfg.scheme == 1 || xseed) {
+        PhaseTimer pt(ctx, "k-means++ seeding (LSH bands + landmarks, batched)");
+        std::vector<PPSeq> seqs;
+        if (cfg.scheme == 1) {
+            inits.resize(static_cast<size_t>(bands) * rows);
+            for (int b = 0; b < bands; ++b)
+                for (int fn = 0; fn < rows; ++fn) {
+                    auto& ib = inits[static_cast<size_t>(b) * rows + fn];
+                    ib.resize(buckets);
+                    seqs.push_back(
+                        lloyd_seed_seq(fn_seed(cfg.seed, b, fn), static_cast<long long>(N), buckets, ib.get()));
+                }
+        }
+        if (xseed)
+            seqs.push_back(lloyd_seed_seq(extra_seed->seed, static_cast<long long>(N), extra_seed->k, extra_seed->out));
+        if (d_union32)
+            kmeans_pp_batch<float>(ctx, d_union32, static_cast<long long>(N), static_cast<int>(d), seqs);
+        else
+            kmeans_pp_batch<double>(ctx, d_union, static_cast<long long>(N), static_cast<int>(d), seqs);
+    }
     std::vector<std::function<void(Ctx&)>> jobs;
     for (int b = 0; b < bands; ++b)
         jobs.push_back([&, b](Ctx& jc) {
@@ -509,10 +534,10 @@ void lsh_bucket_ids(Ctx& ctx, const double* d_union, const float* d_union32, siz
                                                                 cfg.branching, cfg.iters, sd, assign.get());
                     } else if (d_union32) {
                         lloyd_device<float>(jc, d_union32, NN, static_cast<int>(d), buckets, cfg.iters, sd, ctr.get(),
-                                            assign.get());
+                                            assign.get(), inits[static_cast<size_t>(b) * rows + fn].get());
                     } else {
                         lloyd_device<double>(jc, d_union, NN, static_cast<int>(d), buckets, cfg.iters, sd, ctr.get(),
-                                             assign.get());
+                                             assign.get(), inits[static_cast<size_t>(b) * rows + fn].get());
                     }
                     compose_kernel<<<ceil_div(N, 256), 256, 0, s>>>(comp.get(), assign.get(), N, radix);
                     bound = bound * static_cast<double>(radix) + static_cast<double>(leaves - 1);
@@ -1507,12 +1532,15 @@ void select_landmarks_device(Op& op, Ctx& ctx, int method, uint64_t seed) {
     op.L.resize(l * d);
     if (method == 0) {
         DevBuf<uint32_t> asg(N);
+        // seeded with the LSH bands when the build batched it (landmark_init)
+        const uint32_t* init = op.landmark_init.size() == l ? op.landmark_init.get() : nullptr;
         if (op.X32.size())
             lloyd_device<float>(ctx, op.X32.get(), N, static_cast<int>(d), static_cast<int>(l), 10, seed, op.L.get(),
-                                asg.get());
+                                asg.get(), init);
         else
             lloyd_device<double>(ctx, op.X.get(), N, static_cast<int>(d), static_cast<int>(l), 10, seed, op.L.get(),
-                                 asg.get());
+                                 asg.get(), init);
+        op.landmark_init = DevBuf<uint32_t>();  // consumed
     } else {
         std::mt19937_64 rng(seed);
         std::uniform_int_distribution<std::size_t> first(0, N - 1);

@@ -948,8 +948,13 @@ int lcn_op_lcn_lsh(lcn_ctx* ctx, const double* p, size_t n, const double* q, siz
             select_landmarks_device(o, jc, landmark_method, landmark_seed);
             o.landmarks_ready = true;
         };
+        ExtraSeeding es;
+        if (landmark_method == 0 && l >= 1 && l <= n + m) {  // k-means landmarks: seeded with the bands
+            o.landmark_init.resize(l);
+            es = ExtraSeeding{static_cast<int>(l), landmark_seed, o.landmark_init.get()};
+        }
         lsh_bucket_ids(ctx->c, o.X.get(), o.X32.size() ? o.X32.get() : nullptr, n, m, d, lsh_params(cfg), ids, range,
-                              landmarks_job);
+                              landmarks_job, &es);
         if (ctx->c.comm) shard_lcn(o, ids, range, nullptr, landmark_method, landmark_seed);
         else bands_from_union_ids(o, ids, range);
         finish_lcn(o, nullptr, l, landmark_method, landmark_seed);
@@ -1108,8 +1113,13 @@ int lcn_op_create_device(lcn_ctx* ctx, const float* d_p, size_t n, const float* 
                 select_landmarks_device(op, jc, landmark_method, landmark_seed);
                 op.landmarks_ready = true;
             };
+        ExtraSeeding es;
+        if (l && landmark_method == 0 && l <= n + m) {  // k-means landmarks: seeded with the bands
+            op.landmark_init.resize(l);
+            es = ExtraSeeding{static_cast<int>(l), landmark_seed, op.landmark_init.get()};
+        }
         lsh_bucket_ids(ctx->c, op.X.get(), op.X32.size() ? op.X32.get() : nullptr, n, m, d, lsh_params(cfg), ids, range,
-                              landmarks_job);
+                              landmarks_job, &es);
         if (ctx->c.comm && l) shard_lcn(op, ids, range, nullptr, landmark_method, landmark_seed);
         else bands_from_union_ids(op, ids, range);
         if (l) finish_lcn(op, nullptr, l, landmark_method, landmark_seed);

@@ -118,6 +118,17 @@ __global__ void __launch_bounds__(256) assign_exact_kernel(const T* __restrict__
 
 // ---- k-means++ (kmeans.cpp:23-65) ------------------------------------------
 constexpr int kFoldChunk = 2048;  // fold chunk (see the chunk-parallel exact fold below)
+// Several k-means++ sequences over the same points are seeded together (the
+// LSH bands and the landmarks of one build): every step kernel runs one grid
+// row per sequence (y = blockIdx.y), its arrays at base + y * stride, and a
+// sequence whose k is reached sits the remaining steps out.
+constexpr int kMaxSeq = 4;
+struct PPB {
+    long long sN;  // per-point arrays
+    int sC;        // per-chunk arrays
+    int sK;        // per-seed arrays (max k)
+    int k[kMaxSeq];
+};
 // dist2[i] = min(dist2[i], sqdist(x_i, x_last)), strict < as kmeans.cpp:38.
 // Pruning (exactness-preserving): near[i] is the seed whose fold gave
 // dist2[i]; with dc[j] = |x_{seed j} - x_last| (fp64, |rel err| < 1e-13), the
@@ -128,21 +139,34 @@ constexpr int kFoldChunk = 2048;  // fold chunk (see the chunk-parallel exact fo
 // Pruning pass: one thread per point; the points that can still update are
 // appended to `list` (warp-aggregated; the order is irrelevant: every point
 // is updated independently).
-__global__ void __launch_bounds__(256) pp_prune_kernel(long long N, int t, const double* __restrict__ dist2,
+constexpr int kPruneThreads = 512;
+__global__ void __launch_bounds__(kPruneThreads, 4) pp_prune_kernel(long long N, int t, const double* __restrict__ dist2,
                                                        const uint32_t* __restrict__ near,
                                                        const double* __restrict__ dc, uint32_t* __restrict__ list,
                                                        unsigned* __restrict__ count, double* __restrict__ csum,
-                                                       unsigned* __restrict__ surv_count, double* __restrict__ bsum) {
+                                                       unsigned* __restrict__ surv_count, double* __restrict__ bsum,
+                                                       PPB pb) {
     pdl_wait();
     pdl_launch_dependents();
+    const int y = blockIdx.y;
+    if (t + 1 >= pb.k[y]) return;
+    dist2 += y * pb.sN;
+    near += y * pb.sN;
+    dc += y * pb.sK;
+    list += y * pb.sN;
+    count += y;
+    csum += y * pb.sC;
+    bsum += y * pb.sC;
+    if (surv_count) surv_count += y;
     if (surv_count && blockIdx.x == 0 && threadIdx.x == 0) *surv_count = 0u;  // this step's filter survivors
     // one block per fold chunk (kFoldChunk points, kPP per thread, strided
-    // for coalescing): one list-append atomic per chunk, and the chunk's
-    // dist2 sum (approximate chunk sums steer the fold's binade predictions
-    // only; the exact pass subtracts its updates)
-    constexpr int kPP = kFoldChunk / 256;
-    __shared__ unsigned wcnt[8], wbase[8], bbase;
-    __shared__ double wsum[8];
+    // for coalescing; 512 threads x 4 points keep the registers low enough
+    // for 4 blocks per SM): one list-append atomic per chunk, and the
+    // chunk's dist2 sum (a tree; the exact pass corrects it by its updates)
+    constexpr int kPP = kFoldChunk / kPruneThreads;
+    constexpr int kW = kPruneThreads / 32;
+    __shared__ unsigned wcnt[kW], wbase[kW], bbase;
+    __shared__ double wsum[kW];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const long long base = static_cast<long long>(blockIdx.x) * kFoldChunk + threadIdx.x;
     unsigned m[kPP];
@@ -153,7 +177,7 @@ __global__ void __launch_bounds__(256) pp_prune_kernel(long long N, int t, const
     uint32_t nr[kPP];
 #pragma unroll
     for (int j = 0; j < kPP; ++j) {
-        const long long p = base + j * 256;
+        const long long p = base + j * kPruneThreads;
         D[j] = p < N ? dist2[p] : 0.0;
         nr[j] = p < N && t > 0 ? near[p] : 0u;
     }
@@ -161,10 +185,12 @@ __global__ void __launch_bounds__(256) pp_prune_kernel(long long N, int t, const
     for (int j = 0; j < kPP; ++j) C[j] = t > 0 ? dc[nr[j]] : 0.0;
 #pragma unroll
     for (int j = 0; j < kPP; ++j) {
-        const long long p = base + j * 256;
+        const long long p = base + j * kPruneThreads;
         bool need = p < N;
         bs += D[j];
-        if (need && t > 0 && D[j] < kPosInf && C[j] * (1.0 - 1e-12) >= 2.0 * sqrt(D[j]) * (1.0 + 1e-9)) need = false;
+        // squared form of dc(near) (1 - 1e-12) >= 2 sqrt(D) (1 + 1e-9), with
+        // wider margins (the fp64 products round within 2^-52)
+        if (need && t > 0 && D[j] < kPosInf && C[j] * C[j] * (1.0 - 1e-11) >= 4.0 * D[j] * (1.0 + 1e-8)) need = false;
         m[j] = __ballot_sync(0xffffffffu, need);
         wc += __popc(m[j]);
     }
@@ -177,7 +203,7 @@ __global__ void __launch_bounds__(256) pp_prune_kernel(long long N, int t, const
     if (threadIdx.x == 0) {
         unsigned tot = 0;
         double cs = 0.0;
-        for (int w = 0; w < 8; ++w) {
+        for (int w = 0; w < kW; ++w) {
             wbase[w] = tot;
             tot += wcnt[w];
             cs += wsum[w];
@@ -191,7 +217,7 @@ __global__ void __launch_bounds__(256) pp_prune_kernel(long long N, int t, const
     const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
     for (int j = 0; j < kPP; ++j) {
-        if ((m[j] >> lane) & 1) list[off + __popc(m[j] & lt)] = static_cast<uint32_t>(base + j * 256);
+        if ((m[j] >> lane) & 1) list[off + __popc(m[j] & lt)] = static_cast<uint32_t>(base + j * kPruneThreads);
         off += __popc(m[j]);
     }
 }
@@ -206,9 +232,17 @@ __global__ void __launch_bounds__(128) pp_exact_kernel(const T* __restrict__ X, 
                                                        double* __restrict__ dist2, uint32_t* __restrict__ near,
                                                        const uint32_t* __restrict__ list,
                                                        const unsigned* __restrict__ count,
-                                                       double* __restrict__ csum, int cshift) {
+                                                       double* __restrict__ csum, int cshift, PPB pb) {
     pdl_wait();
     pdl_launch_dependents();
+    const int y = blockIdx.y;
+    if (t + 1 >= pb.k[y]) return;
+    chosen += y * pb.sK;
+    dist2 += y * pb.sN;
+    near += y * pb.sN;
+    list += y * pb.sN;
+    count += y;
+    csum += y * pb.sC;
     extern __shared__ __align__(16) unsigned char dyn[];
     double* cs = reinterpret_cast<double*>(dyn);  // the new seed, fp64
     T* rows = reinterpret_cast<T*>(cs + d);
@@ -243,47 +277,6 @@ __global__ void __launch_bounds__(128) pp_exact_kernel(const T* __restrict__ X, 
             }
         }
         __syncwarp();
-    }
-}
-
-// Exact pass over the filter's survivors, one survivor per thread, rows read
-// straight from global memory: the row's lines are prefetched into L1 first
-// so their misses overlap, then the fold streams from L1. No shared-memory
-// staging (pp_exact_kernel's 67 KB per CTA made its launch cost ~13 us even
-// for a few thousand survivors). The center is read once per CTA.
-template <typename T>
-__global__ void __launch_bounds__(256) pp_exact_lane_kernel(const T* __restrict__ X, int d,
-                                                            const uint32_t* __restrict__ chosen, int t,
-                                                            double* __restrict__ dist2, uint32_t* __restrict__ near,
-                                                            const uint32_t* __restrict__ list,
-                                                            const unsigned* __restrict__ count,
-                                                            double* __restrict__ csum, int cshift) {
-    pdl_wait();
-    pdl_launch_dependents();
-    extern __shared__ __align__(16) unsigned char dyn[];
-    double* cs = reinterpret_cast<double*>(dyn);
-    const unsigned cnt = *count;
-    if (blockIdx.x * 256u >= cnt) return;
-    const long long last = chosen[t];
-    for (int k = threadIdx.x; k < d; k += 256) cs[k] = static_cast<double>(X[last * d + k]);
-    __syncthreads();
-    for (unsigned i = blockIdx.x * 256u + threadIdx.x; i < cnt; i += gridDim.x * 256u) {
-        const uint32_t row = list[i];
-        const T* r = X + static_cast<long long>(row) * d;
-        for (int k = 0; k < d; k += 128 / static_cast<int>(sizeof(T)))
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(r + k));
-        double acc = 0.0;
-#pragma unroll 8
-        for (int k = 0; k < d; ++k) {
-            const double df = xsub(static_cast<double>(r[k]), cs[k]);
-            acc = xadd(acc, xmul(df, df));
-        }
-        const double old = dist2[row];
-        if (acc < old) {
-            dist2[row] = acc;
-            near[row] = static_cast<uint32_t>(t);
-            if (old < kPosInf) atomicAdd(&csum[row >> cshift], acc - old);
-        }
     }
 }
 
@@ -388,142 +381,6 @@ __device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
     return v[0];
 }
 
-// Filtered exact pass: per warp, 32 listed points. Each lane loads its 4-value
-// chunks of all 32 filter rows straight into registers (32 independent
-// coalesced loads in flight per lane: the pass is memory-latency bound, ncu
-// profiles/seed_filter_r02.json), the bound is computed lane-parallel with
-// one transpose reduction, and the survivors' rows are staged 8 at a time
-// into shared memory and folded exactly as in pp_exact_kernel. The shared
-// footprint is the survivor buffer alone, so 4-warp CTAs reach the register
-// occupancy limit.
-constexpr int kSurv = 8;  // survivors staged per group
-template <typename T, typename QT, int NQ>
-__global__ void __launch_bounds__(128) pp_filter_exact_kernel(const T* __restrict__ X, const QT* __restrict__ Xh,
-                                                              const float2* __restrict__ se, int d, int dp,
-                                                              const uint32_t* __restrict__ chosen, int t,
-                                                              double* __restrict__ dist2, uint32_t* __restrict__ near,
-                                                              const uint32_t* __restrict__ list,
-                                                              const unsigned* __restrict__ count, int wbuf_bytes,
-                                                              double* __restrict__ csum) {
-    pdl_wait();
-    pdl_launch_dependents();
-    extern __shared__ __align__(16) unsigned char dyn[];
-    __shared__ double eps_c;
-    double* cs = reinterpret_cast<double*>(dyn);  // the new seed, fp64
-    float* c32 = reinterpret_cast<float*>(cs + d);  // max(dp, NQ 128) entries
-    unsigned char* wb = dyn + (static_cast<size_t>(d) * 8 + (max(dp, NQ * 128) + 4) * 4 + 15) / 16 * 16;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    T* buf = reinterpret_cast<T*>(wb + static_cast<size_t>(warp) * wbuf_bytes);  // kSurv x (d + 1) survivors' rows
-    const long long last = chosen[t];
-    for (int k = threadIdx.x; k < NQ * 128; k += blockDim.x) {
-        const double v = k < d ? static_cast<double>(X[last * d + k]) : 0.0;
-        if (k < d) cs[k] = v;
-        c32[k] = static_cast<float>(v);
-    }
-    __syncthreads();
-    if (warp == 0) {
-        double e2 = 0.0;
-        for (int k = lane; k < d; k += 32) {
-            const double df = cs[k] - static_cast<double>(c32[k]);
-            e2 += df * df;
-        }
-        e2 = warp_sum(e2);
-        if (lane == 0) eps_c = sqrt(e2) * (1.0 + 1e-12) + 1e-300;
-    }
-    __syncthreads();
-    const double ec = eps_c;
-    const double gam = 1.0 - (dp + 4) * 1.1920928955078125e-07;  // (dp + 4) 2^-23
-    // lane's 4-value chunks of the center (zero beyond dp: those row chunks
-    // are never loaded, their products are multiplied out below)
-    float4 cq[NQ];
-    bool qin[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-        const int ch = lane + 32 * q;
-        qin[q] = ch * 4 < dp;
-        cq[q] = qin[q] ? make_float4(c32[4 * ch], c32[4 * ch + 1], c32[4 * ch + 2], c32[4 * ch + 3])
-                       : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    const unsigned cnt = *count;
-    for (unsigned b0 = (blockIdx.x * nw + warp) * 32u; b0 < cnt; b0 += gridDim.x * nw * 32u) {
-        const unsigned nb = cnt - b0 < 32u ? cnt - b0 : 32u;
-        // rows past the batch read row 0 (harmless; their lanes are ignored)
-        const uint32_t mine = lane < static_cast<int>(nb) ? list[b0 + lane] : 0u;
-        const float2 my_se = se[mine];
-        const double my_d2 = dist2[mine];
-        float part[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            const long long row = __shfl_sync(0xffffffffu, mine, j);
-            const float sj = __shfl_sync(0xffffffffu, my_se.x, j);
-            float acc = 0.f;
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                if (!qin[q]) continue;
-                const QT* src = Xh + row * dp + 4 * (lane + 32 * q);
-                float2 a, b;
-                if constexpr (sizeof(QT) == 2) {
-                    const uint2 raw = __ldg(reinterpret_cast<const uint2*>(src));
-                    a = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
-                    b = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
-                } else {
-                    const int raw = __ldg(reinterpret_cast<const int*>(src));
-                    const char4 c4 = *reinterpret_cast<const char4*>(&raw);
-                    a = make_float2(static_cast<float>(c4.x), static_cast<float>(c4.y));
-                    b = make_float2(static_cast<float>(c4.z), static_cast<float>(c4.w));
-                }
-                const float d0 = fmaf(a.x, sj, -cq[q].x), d1 = fmaf(a.y, sj, -cq[q].y);
-                const float d2 = fmaf(b.x, sj, -cq[q].z), d3 = fmaf(b.y, sj, -cq[q].w);
-                acc = fmaf(d0, d0, acc);
-                acc = fmaf(d1, d1, acc);
-                acc = fmaf(d2, d2, acc);
-                acc = fmaf(d3, d3, acc);
-            }
-            part[j] = acc;
-        }
-        const float A = transpose_reduce32(part, lane);
-        bool need = false;
-        if (lane < static_cast<int>(nb)) {
-            const double lo = sqrt(static_cast<double>(A) * gam) - static_cast<double>(my_se.y) - ec;
-            need = !(lo > 0.0 && lo * lo * (1.0 - 1e-12) >= my_d2);
-        }
-        const unsigned sv = __ballot_sync(0xffffffffu, need);
-        const int ns = __popc(sv);
-#ifdef LCN_WALK_PROFILE
-        if (lane == 0) atomicAdd(&g_filt_surv, static_cast<unsigned long long>(ns));
-#endif
-        if (!ns) continue;
-        // lane r takes the r-th survivor; groups of kSurv rows through shared memory
-        const int jr = lane < ns ? static_cast<int>(__fns(sv, 0, lane + 1)) : 0;
-        const uint32_t srow = __shfl_sync(0xffffffffu, mine, jr);
-        for (int g0 = 0; g0 < ns; g0 += kSurv) {
-            const int gn = min(kSurv, ns - g0);
-            __syncwarp();
-            for (int r = 0; r < gn; ++r) {
-                const long long row = __shfl_sync(0xffffffffu, srow, g0 + r);
-                for (int k = lane; k < d; k += 32) cp_async_elem(&buf[r * (d + 1) + k], X + row * d + k);
-            }
-            cp_async_commit();
-            cp_async_wait<0>();
-            __syncwarp();
-            if (lane >= g0 && lane < g0 + gn) {
-                const T* r = buf + (lane - g0) * (d + 1);
-                double acc = 0.0;
-                for (int k = 0; k < d; ++k) {
-                    const double df = xsub(static_cast<double>(r[k]), cs[k]);
-                    acc = xadd(acc, xmul(df, df));
-                }
-                const double old = dist2[srow];
-                if (acc < old) {
-                    dist2[srow] = acc;
-                    near[srow] = static_cast<uint32_t>(t);
-                    if (old < kPosInf) atomicAdd(&csum[srow / kFoldChunk], acc - old);
-                }
-            }
-        }
-    }
-}
-
 // Filter only (the default): the same bound as pp_filter_exact_kernel, but
 // the survivors are appended to `surv` and folded by pp_exact_kernel in a
 // second launch with 32 lanes per warp. Folding them inside the filter kept
@@ -539,9 +396,18 @@ __global__ void __launch_bounds__(128) pp_filter_kernel(const T* __restrict__ X,
                                                         const double* __restrict__ dist2,
                                                         const uint32_t* __restrict__ list,
                                                         const unsigned* __restrict__ count,
-                                                        uint32_t* __restrict__ surv, unsigned* __restrict__ surv_count) {
+                                                        uint32_t* __restrict__ surv, unsigned* __restrict__ surv_count,
+                                                        PPB pb) {
     pdl_wait();
     pdl_launch_dependents();
+    const int y = blockIdx.y;
+    if (t + 1 >= pb.k[y]) return;
+    chosen += y * pb.sK;
+    dist2 += y * pb.sN;
+    list += y * pb.sN;
+    count += y;
+    surv += y * pb.sN;
+    surv_count += y;
     __shared__ float c32[NQ * 128];
     __shared__ double eps_part[4];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -684,9 +550,17 @@ __global__ void __launch_bounds__(128) pp_filter_i8_kernel(const T* __restrict__
                                                            const uint32_t* __restrict__ list,
                                                            const unsigned* __restrict__ count,
                                                            uint32_t* __restrict__ surv,
-                                                           unsigned* __restrict__ surv_count) {
+                                                           unsigned* __restrict__ surv_count, PPB pb) {
     pdl_wait();
     pdl_launch_dependents();
+    const int y = blockIdx.y;
+    if (t + 1 >= pb.k[y]) return;
+    chosen += y * pb.sK;
+    dist2 += y * pb.sN;
+    list += y * pb.sN;
+    count += y;
+    surv += y * pb.sN;
+    surv_count += y;
     __shared__ short qc[NQ * 128];
     __shared__ double wred[4][2];
     __shared__ double cmax_s;
@@ -822,193 +696,19 @@ __global__ void __launch_bounds__(128) pp_filter_i8_kernel(const T* __restrict__
     }
 }
 
-// Prune + integer filter in one persistent pass (the default step): warps
-// walk 256-point tiles (grid-stride), test every point of the tile with the
-// triangle bound of pp_prune_kernel, compact the tile's candidates in a
-// per-warp shared list and filter them right away with the int8 rows (as
-// pp_filter_i8_kernel). The prune's global candidate list, its atomics and
-// one kernel boundary go away, and a warp's next tile is independent of
-// the others (no CTA-wide barrier in the loop). Each tile's dist2 sum (a
-// tree) goes to tsum / tbs; the exact pass adjusts tsum by its updates
-// (<= 256 per tile) and pp_pick_kernel folds the tiles into chunk sums.
-constexpr int kTile = 256;
-template <typename T, int NQ>
-__global__ void __launch_bounds__(256, NQ == 1 ? 3 : 2) pp_scan_kernel(const T* __restrict__ X, const int8_t* __restrict__ Xq,
-                                                         const float2* __restrict__ se, const int* __restrict__ qn,
-                                                         long long N, int d, int dp,
-                                                         const uint32_t* __restrict__ chosen, int t,
-                                                         const double* __restrict__ dist2,
-                                                         const uint32_t* __restrict__ near,
-                                                         const double* __restrict__ dc, double* __restrict__ tsum,
-                                                         double* __restrict__ tbs, uint32_t* __restrict__ surv,
-                                                         unsigned* __restrict__ surv_count,
-                                                         unsigned long long* __restrict__ stats) {
-    pdl_wait();
-    pdl_launch_dependents();
-    __shared__ short qc[NQ * 128];
-    __shared__ double wred[8][2];
-    __shared__ double cmax_s;
-    __shared__ uint32_t tlist[8][kTile];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const long long last = chosen[t];
-    // the new center, quantised to int16 (see pp_filter_i8_kernel)
-    double m = 0.0;
-    for (int k = threadIdx.x; k < d; k += 256) m = fmax(m, fabs(static_cast<double>(X[last * d + k])));
-    m = warp_max(m);
-    if (lane == 0) wred[warp][0] = m;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double mm = 0.0;
-        for (int w = 0; w < 8; ++w) mm = fmax(mm, wred[w][0]);
-        cmax_s = mm;
-    }
-    __syncthreads();
-    const double cmax = cmax_s;
-    int e = 0;
-    frexp(cmax / 32767.0, &e);
-    const bool cok = cmax < 1e30 && (cmax == 0.0 || cmax > 1e-30);
-    const double sc = cok && cmax > 0.0 ? ldexp(1.0, e) : 1.0, inv = 1.0 / sc;
-    double e2 = 0.0, n2 = 0.0;
-    for (int k = threadIdx.x; k < NQ * 128; k += 256) {
-        const double v = k < d ? static_cast<double>(X[last * d + k]) : 0.0;
-        double qv = cok ? rint(v * inv) : 0.0;
-        qv = fmin(fmax(qv, -32767.0), 32767.0);
-        qc[k] = static_cast<short>(qv);
-        const double df = v - qv * sc;
-        e2 += df * df;
-        n2 += qv * qv;
-    }
-    e2 = warp_sum(e2);
-    n2 = warp_sum(n2);
-    __syncthreads();
-    if (lane == 0) {
-        wred[warp][0] = e2;
-        wred[warp][1] = n2;
-    }
-    __syncthreads();
-    double ec2 = 0.0, ncq = 0.0;
-    for (int w = 0; w < 8; ++w) {
-        ec2 += wred[w][0];
-        ncq += wred[w][1];
-    }
-    const double ec = cok ? sqrt(ec2) * (1.0 + 1e-12) + 1e-300 : kPosInf;
-    const double sc2n = sc * sc * ncq;
-    int qlo[NQ], qhi[NQ];
-    bool qin[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-        const int ch = lane + 32 * q;
-        qin[q] = ch * 4 < dp;
-        const int k = qin[q] ? 4 * ch : 0;
-        qlo[q] = qin[q] ? (static_cast<unsigned short>(qc[k]) | (static_cast<int>(qc[k + 1]) << 16)) : 0;
-        qhi[q] = qin[q] ? (static_cast<unsigned short>(qc[k + 2]) | (static_cast<int>(qc[k + 3]) << 16)) : 0;
-    }
-    uint32_t* const wl = tlist[warp];
-    const unsigned lt = (1u << lane) - 1u;
-    const long long ntile = (N + kTile - 1) / kTile;
-    unsigned long long ncand_tot = 0;
-    for (long long tile = static_cast<long long>(blockIdx.x) * 8 + warp; tile < ntile;
-         tile += static_cast<long long>(gridDim.x) * 8) {
-        // prune the tile (kmeans.cpp:38 can only fire where the triangle bound fails)
-        constexpr int kPT = kTile / 32;
-        const long long b = tile * kTile + lane;
-        double D[kPT];
-        uint32_t nr[kPT];
-#pragma unroll
-        for (int j = 0; j < kPT; ++j) {
-            const long long p = b + 32 * j;
-            D[j] = p < N ? dist2[p] : 0.0;
-            nr[j] = p < N && t > 0 ? near[p] : 0u;
-        }
-        double ts = 0.0;
-        unsigned nc = 0;
-#pragma unroll
-        for (int j = 0; j < kPT; ++j) {
-            const long long p = b + 32 * j;
-            ts += D[j];
-            bool need = p < N;
-            if (need && t > 0 && D[j] < kPosInf) {
-                const double C = dc[nr[j]];
-                if (C * (1.0 - 1e-12) >= 2.0 * sqrt(D[j]) * (1.0 + 1e-9)) need = false;
-            }
-            const unsigned mj = __ballot_sync(0xffffffffu, need);
-            if (need) wl[nc + __popc(mj & lt)] = static_cast<uint32_t>(p);
-            nc += __popc(mj);
-        }
-        ts = warp_sum(ts);
-        if (lane == 0) {
-            tsum[tile] = ts;
-            tbs[tile] = ts;
-        }
-        ncand_tot += nc;
-        __syncwarp();
-        // filter the tile's candidates, 32 rows per batch
-        for (unsigned b0 = 0; b0 < nc; b0 += 32u) {
-            const unsigned nb = nc - b0 < 32u ? nc - b0 : 32u;
-            const uint32_t mine = wl[b0 + (lane < static_cast<int>(nb) ? lane : 0)];
-            const float2 my_se = se[mine];
-            const double my_d2 = dist2[mine];
-            const int my_qn = qn[mine];
-            constexpr int RB = NQ == 1 ? 32 : 16;
-            int part[32];
-#pragma unroll
-            for (int g = 0; g < 32; g += RB) {
-                int raw[RB][NQ];
-#pragma unroll
-                for (int j = 0; j < RB; ++j) {
-                    const long long row = __shfl_sync(0xffffffffu, mine, g + j);
-#pragma unroll
-                    for (int q = 0; q < NQ; ++q)
-                        raw[j][q] =
-                            qin[q] && (g + j) < static_cast<int>(nb)
-                                ? __ldcs(reinterpret_cast<const int*>(Xq + row * dp + 4 * (lane + 32 * q)))
-                                : 0;
-                }
-#pragma unroll
-                for (int j = 0; j < RB; ++j) part[g + j] = dp2a_row<NQ>(raw[j], qlo, qhi);
-            }
-#pragma unroll
-            for (int w = 16; w >= 1; w >>= 1) {
-                const bool hi = lane & w;
-#pragma unroll
-                for (int i = 0; i < w; ++i) {
-                    const int send = hi ? part[i] : part[i + w];
-                    const int keep = hi ? part[i + w] : part[i];
-                    part[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
-                }
-            }
-            bool need = false;
-            if (lane < static_cast<int>(nb)) {
-                const double sx = static_cast<double>(my_se.x);
-                const double t1 = sx * sx * static_cast<double>(my_qn);
-                const double t2 = 2.0 * sx * sc * static_cast<double>(part[0]);
-                const double a2 = (t1 - t2) + sc2n;
-                const double a2lo = a2 - 4.440892098500626e-16 * (t1 + fabs(t2) + sc2n);  // 2^-51
-                const double lo =
-                    sqrt(fmax(a2lo, 0.0)) * (1.0 - 2.220446049250313e-16) - static_cast<double>(my_se.y) - ec;
-                need = !(lo > 0.0 && lo * lo * (1.0 - 1e-12) >= my_d2);
-            }
-            const unsigned sv = __ballot_sync(0xffffffffu, need);
-            if (sv) {
-                unsigned base = 0;
-                if (lane == 0) base = atomicAdd(surv_count, static_cast<unsigned>(__popc(sv)));
-                base = __shfl_sync(0xffffffffu, base, 0);
-                if (need) surv[base + __popc(sv & lt)] = mine;
-            }
-        }
-        __syncwarp();
-    }
-    if (stats && lane == 0 && ncand_tot) atomicAdd(stats, ncand_tot);
-}
-
 // dc[j] = |x_{chosen[j]} - x_{chosen[t]}| for j < t (fp64, one warp per j)
 template <typename T>
 __global__ void __launch_bounds__(256) seed_dist_kernel(const T* __restrict__ X, int d,
                                                         const uint32_t* __restrict__ chosen, int t,
-                                                        double* __restrict__ dc, unsigned* __restrict__ surv_count) {
+                                                        double* __restrict__ dc, unsigned* __restrict__ surv_count,
+                                                        PPB pb) {
     pdl_wait();
     pdl_launch_dependents();
-    if (surv_count && blockIdx.x == 0 && threadIdx.x == 0) *surv_count = 0u;  // this step's filter survivors
+    const int y = blockIdx.y;
+    if (t + 1 >= pb.k[y]) return;
+    chosen += y * pb.sK;
+    dc += y * pb.sK;
+    if (surv_count && blockIdx.x == 0 && threadIdx.x == 0) surv_count[y] = 0u;  // this step's filter survivors
     const int j = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (j >= t) return;
     const long long a = chosen[j], b = chosen[t];
@@ -1141,28 +841,24 @@ __device__ __forceinline__ longlong2 par_clamp(ParInc v) {
 // the actual binade, so the result is exact regardless.
 
 __global__ void fold_chunk_sum_kernel(const double* __restrict__ x, long long N, double* __restrict__ csum,
-                                      double* __restrict__ bsum, double* __restrict__ tsum,
-                                      double* __restrict__ tbs) {
+                                      double* __restrict__ bsum, int hs, PPB pb) {
     pdl_wait();
     pdl_launch_dependents();
-    // 256 threads: warp w sums tile 8 c + w (tile sums for pp_scan_kernel's
-    // bookkeeping), thread 0 the chunk
+    const int y = blockIdx.y;
+    if (hs >= pb.k[y]) return;
+    x += y * pb.sN;
+    csum += y * pb.sC;
+    bsum += y * pb.sC;
     __shared__ double red[8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const long long b = static_cast<long long>(blockIdx.x) * kFoldChunk + warp * 256;
+    const long long b0 = static_cast<long long>(blockIdx.x) * kFoldChunk + warp * 256;
     double s = 0.0;
     for (int j = 0; j < 8; ++j) {
-        const long long i = b + lane + 32 * j;
+        const long long i = b0 + lane + 32 * j;
         s += i < N ? x[i] : 0.0;
     }
     s = warp_sum(s);
-    if (lane == 0) {
-        red[warp] = s;
-        if (tsum) {
-            tsum[blockIdx.x * 8LL + warp] = s;
-            tbs[blockIdx.x * 8LL + warp] = s;
-        }
-    }
+    if (lane == 0) red[warp] = s;
     __syncthreads();
     if (threadIdx.x == 0) {
         double t = 0.0;
@@ -1216,10 +912,21 @@ __global__ void __launch_bounds__(256, 4) fold_round_kernel(const double* __rest
                                                          longlong2* __restrict__ R, longlong2* __restrict__ Rseg,
                                                          int* __restrict__ Eseg, int* __restrict__ spred,
                                                          unsigned* __restrict__ smask, double* __restrict__ s0end,
-                                                         const int* __restrict__ skip) {
+                                                         const int* __restrict__ skip, int hs, PPB pb) {
     pdl_wait();
     pdl_launch_dependents();
-    if (skip && *skip) return;  // pp_pick_kernel certified this step's pick
+    const int y = blockIdx.y;
+    if (hs >= pb.k[y]) return;
+    if (skip && skip[y]) return;  // pp_pick_kernel certified this step's pick
+    x += y * pb.sN;
+    csum += y * pb.sC;
+    ebin += y * pb.sC;
+    R += y * pb.sC;
+    Rseg += static_cast<long long>(y) * pb.sC * 2 * kSegs;
+    Eseg += static_cast<long long>(y) * pb.sC * kSegs;
+    spred += y * pb.sC;
+    smask += y * pb.sC;
+    s0end += y;
     __shared__ ParInc stot[kSegs];
     __shared__ double ssum[kSegs];
     __shared__ double red[8];
@@ -1510,9 +1217,28 @@ __global__ void __launch_bounds__(kWalkThreads) pp_walk_pick_kernel(
     const int* __restrict__ spred, const longlong2* __restrict__ R, const longlong2* __restrict__ Rseg,
     const int* __restrict__ Eseg, const unsigned* __restrict__ smask, const double* __restrict__ s0end,
     double* __restrict__ csum, unsigned* __restrict__ cand_count, double* __restrict__ sstart, const unsigned long long* __restrict__ raw, int n_raw, int* __restrict__ draw_counter,
-    uint32_t* __restrict__ chosen, int t, int staged, const int* __restrict__ skip) {
+    uint32_t* __restrict__ chosen, int t, int staged, const int* __restrict__ skip, PPB pb) {
     pdl_wait();
     pdl_launch_dependents();
+    const int y = blockIdx.y;
+    if (t >= pb.k[y]) return;
+    if (skip && skip[y]) return;  // pp_pick_kernel certified this step's pick
+    dist2 += y * pb.sN;
+    used += y * pb.sN;
+    ebin += y * pb.sC;
+    spred += y * pb.sC;
+    R += y * pb.sC;
+    Rseg += static_cast<long long>(y) * pb.sC * 2 * kSegs;
+    Eseg += static_cast<long long>(y) * pb.sC * kSegs;
+    smask += y * pb.sC;
+    s0end += y;
+    csum += y * pb.sC;
+    cand_count += y;
+    sstart += y * (pb.sC + 1);
+    raw += y * pb.sK;
+    n_raw = pb.k[y] - 1;
+    draw_counter += y;
+    chosen += y * pb.sK;
     __shared__ int flag_min;
     __shared__ double total;
     __shared__ __align__(16) double segbuf[kSegLen];
@@ -1520,7 +1246,6 @@ __global__ void __launch_bounds__(kWalkThreads) pp_walk_pick_kernel(
     __shared__ int pre_list[kMaxPre];
     extern __shared__ __align__(16) unsigned char wdyn[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (skip && *skip) return;  // pp_pick_kernel certified this step's pick
     WALK_T(T0);
     // the next step's prune appends to the candidate list from zero
     if (threadIdx.x == 0) *cand_count = 0u;
@@ -1777,9 +1502,25 @@ __global__ void __launch_bounds__(kPickThreads) pp_pick_kernel(
     int* __restrict__ skip, unsigned* __restrict__ cand_count, const unsigned long long* __restrict__ raw, int n_raw,
     int* __restrict__ draw_counter, uint32_t* __restrict__ chosen, int t, unsigned* __restrict__ n_fallback,
     double slack, const unsigned* __restrict__ surv_count, unsigned long long* __restrict__ stats, int qsmem,
-    const double* __restrict__ tsum, const double* __restrict__ tbs) {
+    PPB pb) {
     pdl_wait();
     pdl_launch_dependents();
+    const int y = blockIdx.y;
+    if (t >= pb.k[y]) return;
+    dist2 += y * pb.sN;
+    used += y * pb.sN;
+    csum += y * pb.sC;
+    bsum += y * pb.sC;
+    qbuf += y * pb.sC;
+    skip += y;
+    cand_count += y;
+    raw += y * pb.sK;
+    n_raw = pb.k[y] - 1;
+    draw_counter += y;
+    chosen += y * pb.sK;
+    n_fallback += y;
+    if (surv_count) surv_count += y;
+    if (stats) stats += 2 * y;
     if (stats && threadIdx.x == 0) {  // candidates and exact folds of this step (LCN_TIMING)
         stats[0] += *cand_count;
         stats[1] += surv_count ? *surv_count : 0u;
@@ -1802,22 +1543,8 @@ __global__ void __launch_bounds__(kPickThreads) pp_pick_kernel(
     // and the sum of the pre-update sums
     for (int c0 = 0; c0 < nch; c0 += kPickThreads) {
         const int c = c0 + threadIdx.x;
-        double v = 0.0, bv = 0.0;
-        if (c < nch && tsum) {
-            // pp_scan_kernel's tiles: 8 per chunk; the chunk sums are also
-            // what the exact fold's predictions (fold_round_kernel) read
-#pragma unroll
-            for (int w = 0; w < kFoldChunk / kTile; ++w) {
-                v += tsum[static_cast<long long>(c) * (kFoldChunk / kTile) + w];
-                bv += tbs[static_cast<long long>(c) * (kFoldChunk / kTile) + w];
-            }
-            csum[c] = v;
-            bsum[c] = bv;
-        } else if (c < nch) {
-            v = csum[c];
-            bv = bsum[c];
-        }
-        bv = warp_sum(bv);
+        const double v = c < nch ? csum[c] : 0.0;
+        const double bv = warp_sum(c < nch ? bsum[c] : 0.0);
         double incl = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -1923,16 +1650,31 @@ __global__ void fill_kernel(double* p, long long n, double v) {
 }
 
 template <typename T>
-void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t first,
-                      const std::vector<unsigned long long>& raw, uint32_t* d_chosen, int* draws_used) {
+void kmeans_pp_batch(Ctx& ctx, const T* X, long long N, int d, const std::vector<PPSeq>& seqs) {
     cudaStream_t s = ctx.stream;
+    const int S = static_cast<int>(seqs.size());
+    if (S < 1) return;
+    if (S > kMaxSeq) {  // in groups of kMaxSeq
+        for (int g = 0; g < S; g += kMaxSeq)
+            kmeans_pp_batch<T>(ctx, X, N, d,
+                               std::vector<PPSeq>(seqs.begin() + g, seqs.begin() + std::min(S, g + kMaxSeq)));
+        return;
+    }
+    int KM = 1;
+    for (const auto& q : seqs) KM = std::max(KM, q.k);
     const int nch = ceil_div(N, kFoldChunk);
-    DevBuf<double> dist2(N), csum(nch), sstart(nch + 1);
-    DevBuf<int> ebin(nch), spred(nch), Eseg(static_cast<size_t>(nch) * kSegs);
-    DevBuf<unsigned> smask(nch);
-    DevBuf<double> s0end(1);
-    DevBuf<longlong2> R(nch), Rseg(static_cast<size_t>(nch) * 2 * kSegs);
-    DevBuf<unsigned char> used(N);
+    PPB pb{};
+    pb.sN = N;
+    pb.sC = nch;
+    pb.sK = KM;
+    for (int y = 0; y < kMaxSeq; ++y) pb.k[y] = y < S ? seqs[y].k : 0;
+    const size_t SN = static_cast<size_t>(S) * N, SC = static_cast<size_t>(S) * nch, SK = static_cast<size_t>(S) * KM;
+    DevBuf<double> dist2(SN), csum(SC), bsum(SC), qbuf(SC), sstart(static_cast<size_t>(S) * (nch + 1));
+    DevBuf<int> ebin(SC), spred(SC), Eseg(SC * kSegs);
+    DevBuf<unsigned> smask(SC);
+    DevBuf<double> s0end(S);
+    DevBuf<longlong2> R(SC), Rseg(SC * 2 * kSegs);
+    DevBuf<unsigned char> used(SN);
     // walk: chunk plans + running-sum table staged in shared memory if they fit
     size_t walk_smem = static_cast<size_t>(nch) * (sizeof(longlong2) + sizeof(double) + 4 * sizeof(int)) + sizeof(double) +
                        static_cast<size_t>(kMaxPre) * (2 * kSegs * sizeof(longlong2) + kSegLen * sizeof(double) +
@@ -1942,9 +1684,9 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
         allow_max_dyn_smem(pp_walk_pick_kernel);
     else
         walk_smem = 0;
-    DevBuf<uint32_t> near(N), list(N);
-    DevBuf<unsigned> cnt(1);
-    DevBuf<double> dc(std::max(k, 1));
+    DevBuf<uint32_t> near(SN), list(SN), chosen(SK);
+    DevBuf<unsigned> cnt(S);
+    DevBuf<double> dc(SK);
     // exact-pass geometry: warps per CTA so one CTA's row buffers stay <= 96 KB
     int ex_warps = 4;
     while (ex_warps > 1 && static_cast<size_t>(ex_warps) * 32 * (d + 1) * sizeof(T) > 96 * 1024) ex_warps >>= 1;
@@ -1953,11 +1695,14 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     allow_max_dyn_smem(pp_exact_kernel<T>);
     int ex_occ = 1;
     CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ex_occ, pp_exact_kernel<T>, ex_warps * 32, ex_smem));
-    const int ex_grid = std::max(1, ex_occ) * ctx.num_sms;
-    // filter copy of the points: int8 rows with a power-of-two scale per row
-    // (default since the filter streams; build-time seeding at configs[3]
-    // 596 -> 490 ms per band) or fp16 rows (LCN_PP_FILTER=f16: tighter
-    // bound, twice the bytes); rows up to 512 values
+    // one CTA per SM and sequence: a step has a few thousand survivors (early
+    // steps loop); more CTAs only cost launch and smem reconfiguration
+    const int ex_grid = ctx.num_sms;
+    (void)ex_occ;
+    // filter copy of the points (shared by the sequences): int8 rows with a
+    // power-of-two scale per row (default: the integer filter) or fp16 rows
+    // (LCN_PP_FILTER=f16: tighter bound, twice the bytes); rows up to 512
+    // values, else (or LCN_PP_NOFILTER) every candidate is folded exactly
     const char* fenv = std::getenv("LCN_PP_FILTER");
     const bool i8 = !(fenv && std::string(fenv) == "f16");
     const int qsz = i8 ? 1 : 2;
@@ -1966,93 +1711,27 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     DevBuf<unsigned char> Xq(filt ? static_cast<size_t>(N) * dp * qsz : 1);
     DevBuf<float2> se(filt ? static_cast<size_t>(N) : 1);
     DevBuf<int> qn(filt && i8 ? static_cast<size_t>(N) : 1);
-    const int wbuf_bytes = static_cast<int>((static_cast<size_t>(kSurv) * (d + 1) * sizeof(T) + 15) / 16 * 16);
     const int nq = (dp / 4 + 31) / 32;
-    // c32 is read for NQ * 128 entries; the per-warp buffers start 16-aligned
-    const size_t fx_smem = (static_cast<size_t>(d) * 8 + (std::max(dp, nq * 128) + 4) * 4 + 15) / 16 * 16 +
-                           static_cast<size_t>(ex_warps) * wbuf_bytes;
-    using FxH = void (*)(const T*, const __half*, const float2*, int, int, const uint32_t*, int, double*, uint32_t*,
-                         const uint32_t*, const unsigned*, int, double*);
-    using FxQ = void (*)(const T*, const int8_t*, const float2*, int, int, const uint32_t*, int, double*, uint32_t*,
-                         const uint32_t*, const unsigned*, int, double*);
-    const FxH fx_h = nq == 1 ? pp_filter_exact_kernel<T, __half, 1>
-                   : nq == 2 ? pp_filter_exact_kernel<T, __half, 2>
-                   : nq == 3 ? pp_filter_exact_kernel<T, __half, 3>
-                             : pp_filter_exact_kernel<T, __half, 4>;
-    const FxQ fx_q = nq == 1 ? pp_filter_exact_kernel<T, int8_t, 1>
-                   : nq == 2 ? pp_filter_exact_kernel<T, int8_t, 2>
-                   : nq == 3 ? pp_filter_exact_kernel<T, int8_t, 3>
-                             : pp_filter_exact_kernel<T, int8_t, 4>;
-    // filter and exact fold in separate launches (default) or fused
-    // (LCN_PP_SPLIT=0, the round-2 kernel)
-    const char* spenv = std::getenv("LCN_PP_SPLIT");
-    const bool split = !(spenv && spenv[0] == '0');
     using FsH = void (*)(const T*, const __half*, const float2*, int, int, const uint32_t*, int, const double*,
-                         const uint32_t*, const unsigned*, uint32_t*, unsigned*);
-    using FsQ = void (*)(const T*, const int8_t*, const float2*, int, int, const uint32_t*, int, const double*,
-                         const uint32_t*, const unsigned*, uint32_t*, unsigned*);
+                         const uint32_t*, const unsigned*, uint32_t*, unsigned*, PPB);
     const FsH fs_h = nq == 1 ? pp_filter_kernel<T, __half, 1>
                    : nq == 2 ? pp_filter_kernel<T, __half, 2>
                    : nq == 3 ? pp_filter_kernel<T, __half, 3>
                              : pp_filter_kernel<T, __half, 4>;
-    const FsQ fs_q = nq == 1 ? pp_filter_kernel<T, int8_t, 1>
-                   : nq == 2 ? pp_filter_kernel<T, int8_t, 2>
-                   : nq == 3 ? pp_filter_kernel<T, int8_t, 3>
-                             : pp_filter_kernel<T, int8_t, 4>;
     using FiQ = void (*)(const T*, const int8_t*, const float2*, const int*, int, int, const uint32_t*, int,
-                         const double*, const uint32_t*, const unsigned*, uint32_t*, unsigned*);
+                         const double*, const uint32_t*, const unsigned*, uint32_t*, unsigned*, PPB);
     const FiQ fi_q = nq == 1 ? pp_filter_i8_kernel<T, 1>
                    : nq == 2 ? pp_filter_i8_kernel<T, 2>
                    : nq == 3 ? pp_filter_i8_kernel<T, 3>
                              : pp_filter_i8_kernel<T, 4>;
-    int fi_grid = ctx.num_sms;
-    {
-        int occ = 1;
-        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fi_q, 128, 0));
-        fi_grid = std::max(1, occ) * ctx.num_sms;
-    }
-    // LCN_PP_SCAN=1: prune + int8 filter in one persistent pass (measured
-    // slower than the separate launches: 38.8 vs 12.4 + 16.8 us per step)
-    const char* scenv = std::getenv("LCN_PP_SCAN");
-    const bool scan = filt && i8 && split && scenv && scenv[0] == '1';
-    using ScQ = void (*)(const T*, const int8_t*, const float2*, const int*, long long, int, int, const uint32_t*, int,
-                         const double*, const uint32_t*, const double*, double*, double*, uint32_t*, unsigned*,
-                         unsigned long long*);
-    const ScQ sc_q = nq == 1 ? pp_scan_kernel<T, 1>
-                   : nq == 2 ? pp_scan_kernel<T, 2>
-                   : nq == 3 ? pp_scan_kernel<T, 3>
-                             : pp_scan_kernel<T, 4>;
-    int sc_grid = ctx.num_sms;
-    {
-        int occ = 1;
-        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sc_q, 256, 0));
-        sc_grid = std::max(1, occ) * ctx.num_sms;
-    }
-    const long long ntile = static_cast<long long>(nch) * (kFoldChunk / kTile);
-    DevBuf<double> tsum(scan ? ntile : 1), tbs(scan ? ntile : 1);
-    const size_t el_smem = static_cast<size_t>(d) * 8;
-    if (el_smem > 48 * 1024) allow_max_dyn_smem(pp_exact_lane_kernel<T>);
-    const int el_grid = 2 * ctx.num_sms;
-    // the survivors' exact pass: smem-staged rows (default) or one survivor
-    // per thread (LCN_PP_EXACT=lane); LCN_PP_EXACT_CTAS = CTAs per SM
-    const char* xenv = std::getenv("LCN_PP_EXACT");
-    const bool exact_lane = xenv && std::string(xenv) == "lane";
-    const char* xgenv = std::getenv("LCN_PP_EXACT_CTAS");
-    const int sx_grid = xgenv ? std::max(1, std::min(ex_occ, std::atoi(xgenv))) * ctx.num_sms : ex_grid;
-    DevBuf<uint32_t> surv(filt && split ? N : 1);
-    DevBuf<unsigned> scnt(1);
-    scnt.zero(s);
-    int fs_grid = ctx.num_sms;
-    if (filt && split) {
+    int f_grid = ctx.num_sms;
+    if (filt) {
         int occ = 1;
         if (i8)
-            CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fs_q, 128, 0));
+            CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fi_q, 128, 0));
         else
             CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fs_h, 128, 0));
-        fs_grid = std::max(1, occ) * ctx.num_sms;
-    }
-    int fx_grid = ex_grid;
-    if (filt) {
+        f_grid = std::max(1, occ) * ctx.num_sms;
         if (i8)
             pp_i8_prep_kernel<T><<<ceil_div(N, 8), 256, 0, s>>>(X, N, d, dp, reinterpret_cast<int8_t*>(Xq.get()),
                                                                se.get(), qn.get());
@@ -2060,31 +1739,28 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
             pp_half_prep_kernel<T><<<ceil_div(N, 8), 256, 0, s>>>(X, N, d, dp, reinterpret_cast<__half*>(Xq.get()),
                                                                  se.get());
         LAUNCH_OK("kmeans++ filter copy");
-        int occ = 1;
-        if (i8) {
-            allow_max_dyn_smem(fx_q);
-            CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fx_q, ex_warps * 32, fx_smem));
-        } else {
-            allow_max_dyn_smem(fx_h);
-            CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fx_h, ex_warps * 32, fx_smem));
-        }
-        fx_grid = std::max(1, occ) * ctx.num_sms;
     }
-    DevBuf<unsigned long long> d_raw(raw.size() ? raw.size() : 1);
-    DevBuf<int> counter(1);
+    DevBuf<uint32_t> surv(filt ? SN : 1);
+    DevBuf<unsigned> scnt(S);
+    // the callers' engine draws, one row of KM per sequence
+    std::vector<unsigned long long> hraw(SK, 0ull);
+    for (int y = 0; y < S; ++y)
+        std::copy(seqs[y].raw.begin(), seqs[y].raw.begin() + std::min<size_t>(seqs[y].raw.size(), KM), hraw.begin() + y * KM);
+    DevBuf<unsigned long long> d_raw(SK);
+    d_raw.upload(hraw.data(), SK, s);
+    DevBuf<int> counter(S);
     // certified pick first (pp_pick_kernel); the exact fold + walk only
     // when it cannot decide. LCN_PP_EXACT_WALK=1 always runs the exact walk.
     const char* wenv = std::getenv("LCN_PP_EXACT_WALK");
     const bool fast = !(wenv && wenv[0] == '1');
     const char* senv = std::getenv("LCN_PP_CERT_SLACK");  // test hook: widen the certificate (more fallbacks)
     const double slack = senv ? std::max(1.0, std::atof(senv)) : 1.0;
-    DevBuf<double> fsum(nch), bsum(nch);
     const size_t pk_smem = static_cast<size_t>(nch) * 8 <= 160 * 1024 ? static_cast<size_t>(nch) * 8 : 0;
     if (pk_smem > 48 * 1024) allow_max_dyn_smem(pp_pick_kernel);
-    DevBuf<int> skip(1);
-    DevBuf<unsigned> nfall(1);
+    DevBuf<int> skip(S);
+    DevBuf<unsigned> nfall(S);
     const bool timing = std::getenv("LCN_TIMING") != nullptr;
-    DevBuf<unsigned long long> pstats(2);
+    DevBuf<unsigned long long> pstats(2 * S);
     pstats.zero(s);
     skip.zero(s);
     nfall.zero(s);
@@ -2093,110 +1769,87 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
     counter.zero(s);
     csum.zero(s);
     cnt.zero(s);
-    if (!raw.empty()) d_raw.upload(raw.data(), raw.size(), s);
-    fill_kernel<<<ceil_div(N, 256), 256, 0, s>>>(dist2.get(), N, kPosInf);
-    uint32_t f32 = static_cast<uint32_t>(first);
-    unsigned char one = 1;
-    CUDA_OK(cudaMemcpyAsync(d_chosen, &f32, 4, cudaMemcpyHostToDevice, s));
-    CUDA_OK(cudaMemcpyAsync(used.get() + first, &one, 1, cudaMemcpyHostToDevice, s));
+    scnt.zero(s);
+    fill_kernel<<<ceil_div(static_cast<long long>(SN), 256), 256, 0, s>>>(dist2.get(), static_cast<long long>(SN),
+                                                                          kPosInf);
+    {
+        std::vector<uint32_t> h0(SK, 0u);
+        for (int y = 0; y < S; ++y) h0[static_cast<size_t>(y) * KM] = static_cast<uint32_t>(seqs[y].first);
+        chosen.upload(h0.data(), SK, s);
+        const unsigned char one = 1;
+        for (int y = 0; y < S; ++y)
+            CUDA_OK(cudaMemcpyAsync(used.get() + static_cast<size_t>(y) * N + seqs[y].first, &one, 1,
+                                    cudaMemcpyHostToDevice, s));
+        ctx.sync();  // the host staging above goes out of scope
+    }
     // the step chain with programmatic dependent launches (LCN_PP_PDL=0: plain)
     const char* penv = std::getenv("LCN_PP_PDL");
     const bool pdl = !(penv && penv[0] == '0');
     const dim3 b256(256), b128(128);
-    for (int t = 1; t < k; ++t) {
+    const unsigned Sy = static_cast<unsigned>(S);
+    for (int t = 1; t < KM; ++t) {
         if (t > 1)
-            launch_pdl(seed_dist_kernel<T>, dim3(ceil_div(t - 1, 8)), b256, 0, s, pdl, X, d, d_chosen, t - 1, dc.get(),
-                       scnt.get());
-        double* xsums = csum.get();  // the exact pass's sum corrections: chunk or tile sums
-        int xshift = 11;
-        if (scan) {
-            launch_pdl(sc_q, dim3(sc_grid), b256, 0, s, pdl, X, reinterpret_cast<const int8_t*>(Xq.get()), se.get(),
-                       qn.get(), N, d, dp, d_chosen, t - 1, dist2.get(), near.get(), dc.get(), tsum.get(), tbs.get(),
-                       surv.get(), scnt.get(), timing ? pstats.get() : nullptr);
-            xsums = tsum.get();
-            xshift = 8;
+            launch_pdl(seed_dist_kernel<T>, dim3(ceil_div(t - 1, 8), Sy), b256, 0, s, pdl, X, d, chosen.get(), t - 1,
+                       dc.get(), scnt.get(), pb);
+        launch_pdl(pp_prune_kernel, dim3(nch, Sy), dim3(kPruneThreads), 0, s, pdl, N, t - 1, dist2.get(), near.get(), dc.get(),
+                   list.get(), cnt.get(), csum.get(), scnt.get(), bsum.get(), pb);
+        if (filt) {
+            if (i8)
+                launch_pdl(fi_q, dim3(f_grid, Sy), b128, 0, s, pdl, X, reinterpret_cast<const int8_t*>(Xq.get()),
+                           se.get(), qn.get(), d, dp, chosen.get(), t - 1, dist2.get(), list.get(), cnt.get(),
+                           surv.get(), scnt.get(), pb);
+            else
+                launch_pdl(fs_h, dim3(f_grid, Sy), b128, 0, s, pdl, X, reinterpret_cast<const __half*>(Xq.get()),
+                           se.get(), d, dp, chosen.get(), t - 1, dist2.get(), list.get(), cnt.get(), surv.get(),
+                           scnt.get(), pb);
+            launch_pdl(pp_exact_kernel<T>, dim3(ex_grid, Sy), dim3(ex_warps * 32), ex_smem, s, pdl, X, d, chosen.get(),
+                       t - 1, dist2.get(), near.get(), surv.get(), scnt.get(), csum.get(), 11, pb);
         } else {
-            launch_pdl(pp_prune_kernel, dim3(nch), b256, 0, s, pdl, N, t - 1, dist2.get(), near.get(), dc.get(),
-                       list.get(), cnt.get(), csum.get(), scnt.get(), bsum.get());
+            launch_pdl(pp_exact_kernel<T>, dim3(ex_grid, Sy), dim3(ex_warps * 32), ex_smem, s, pdl, X, d, chosen.get(),
+                       t - 1, dist2.get(), near.get(), list.get(), cnt.get(), csum.get(), 11, pb);
         }
-        if (filt && split) {
-            if (scan) {
-            } else if (i8)
-                launch_pdl(fi_q, dim3(fi_grid), b128, 0, s, pdl, X, reinterpret_cast<const int8_t*>(Xq.get()), se.get(),
-                           qn.get(), d, dp, d_chosen, t - 1, dist2.get(), list.get(), cnt.get(), surv.get(),
-                           scnt.get());
-            else
-                launch_pdl(fs_h, dim3(fs_grid), b128, 0, s, pdl, X, reinterpret_cast<const __half*>(Xq.get()), se.get(),
-                           d, dp, d_chosen, t - 1, dist2.get(), list.get(), cnt.get(), surv.get(), scnt.get());
-            if (exact_lane)
-                launch_pdl(pp_exact_lane_kernel<T>, dim3(el_grid), b256, el_smem, s, pdl, X, d, d_chosen, t - 1,
-                           dist2.get(), near.get(), surv.get(), scnt.get(), xsums, xshift);
-            else
-                launch_pdl(pp_exact_kernel<T>, dim3(sx_grid), dim3(ex_warps * 32), ex_smem, s, pdl, X, d, d_chosen,
-                           t - 1, dist2.get(), near.get(), surv.get(), scnt.get(), xsums, xshift);
-        } else if (filt && i8)
-            launch_pdl(fx_q, dim3(fx_grid), dim3(ex_warps * 32), fx_smem, s, pdl, X,
-                       reinterpret_cast<const int8_t*>(Xq.get()), se.get(), d, dp, d_chosen, t - 1, dist2.get(),
-                       near.get(), list.get(), cnt.get(), wbuf_bytes, csum.get());
-        else if (filt)
-            launch_pdl(fx_h, dim3(fx_grid), dim3(ex_warps * 32), fx_smem, s, pdl, X,
-                       reinterpret_cast<const __half*>(Xq.get()), se.get(), d, dp, d_chosen, t - 1, dist2.get(),
-                       near.get(), list.get(), cnt.get(), wbuf_bytes, csum.get());
-        else
-            launch_pdl(pp_exact_kernel<T>, dim3(ex_grid), dim3(ex_warps * 32), ex_smem, s, pdl, X, d, d_chosen, t - 1,
-                       dist2.get(), near.get(), list.get(), cnt.get(), csum.get(), 11);
-#ifdef LCN_WALK_PROFILE
-        if (std::getenv("LCN_WALK_STATS") && (t % 256 == 0 || t == k - 1)) {
-            unsigned hc = 0;
-            cnt.download(&hc, 1, s);
-            ctx.sync();
-            unsigned long long hs = 0;
-            CUDA_OK(cudaMemcpyFromSymbol(&hs, g_filt_surv, sizeof(hs)));
-            const unsigned long long z = 0;
-            CUDA_OK(cudaMemcpyToSymbol(g_filt_surv, &z, sizeof(z)));
-            std::fprintf(stderr, "[seed] N=%lld t=%d candidates %u (%.2f%%), exact folds since last %llu\n", N, t, hc,
-                         100.0 * hc / N, hs);
-        }
-#endif
-        // the first pass moves every point off +inf: its chunk (and tile)
-        // sums are taken afresh (later steps: pre-update sums corrected by
-        // the exact pass's updates)
+        // the first pass moves every point off +inf: its chunk sums are taken
+        // afresh (later steps: pre-update sums corrected by the exact pass)
         if (t == 1)
-            launch_pdl(fold_chunk_sum_kernel, dim3(nch), b256, 0, s, pdl, dist2.get(), N, csum.get(), bsum.get(),
-                       scan ? tsum.get() : static_cast<double*>(nullptr),
-                       scan ? tbs.get() : static_cast<double*>(nullptr));
+            launch_pdl(fold_chunk_sum_kernel, dim3(nch, Sy), b256, 0, s, pdl, dist2.get(), N, csum.get(), bsum.get(),
+                       t, pb);
         const int* skp = nullptr;
         if (fast) {
-            launch_pdl(pp_pick_kernel, dim3(1), dim3(kPickThreads), pk_smem, s, pdl, dist2.get(), used.get(), N, nch,
-                       csum.get(), bsum.get(), fsum.get(), skip.get(), cnt.get(), d_raw.get(),
-                       static_cast<int>(raw.size()), counter.get(), d_chosen, t, nfall.get(), slack,
-                       filt && split ? scnt.get() : nullptr, timing ? pstats.get() : nullptr, pk_smem ? 1 : 0,
-                       scan ? tsum.get() : static_cast<const double*>(nullptr),
-                       scan ? tbs.get() : static_cast<const double*>(nullptr));
+            launch_pdl(pp_pick_kernel, dim3(1, Sy), dim3(kPickThreads), pk_smem, s, pdl, dist2.get(), used.get(), N,
+                       nch, csum.get(), bsum.get(), qbuf.get(), skip.get(), cnt.get(), d_raw.get(), KM - 1,
+                       counter.get(), chosen.get(), t, nfall.get(), slack, filt ? scnt.get() : nullptr,
+                       timing ? pstats.get() : nullptr, pk_smem ? 1 : 0, pb);
             skp = skip.get();
         }
-        launch_pdl(fold_round_kernel, dim3(nch), b256, 0, s, pdl, dist2.get(), N, csum.get(), ebin.get(), R.get(),
-                   Rseg.get(), Eseg.get(), spred.get(), smask.get(), s0end.get(), skp);
-        launch_pdl(pp_walk_pick_kernel, dim3(1), dim3(kWalkThreads), walk_smem, s, pdl, dist2.get(), used.get(), N, nch,
-                   ebin.get(), spred.get(), R.get(), Rseg.get(), Eseg.get(), smask.get(), s0end.get(), csum.get(),
-                   cnt.get(), sstart.get(), d_raw.get(), static_cast<int>(raw.size()), counter.get(), d_chosen, t,
-                   walk_staged, skp);
+        launch_pdl(fold_round_kernel, dim3(nch, Sy), b256, 0, s, pdl, dist2.get(), N, csum.get(), ebin.get(), R.get(),
+                   Rseg.get(), Eseg.get(), spred.get(), smask.get(), s0end.get(), skp, t, pb);
+        launch_pdl(pp_walk_pick_kernel, dim3(1, Sy), dim3(kWalkThreads), walk_smem, s, pdl, dist2.get(), used.get(), N,
+                   nch, ebin.get(), spred.get(), R.get(), Rseg.get(), Eseg.get(), smask.get(), s0end.get(), csum.get(),
+                   cnt.get(), sstart.get(), d_raw.get(), KM - 1, counter.get(), chosen.get(), t, walk_staged, skp, pb);
     }
     LAUNCH_OK("kmeans++");
-    if (draws_used) counter.download(draws_used, 1, s);
-    unsigned h_fall = 0;
-    unsigned long long h_st[2] = {0, 0};
+    for (int y = 0; y < S; ++y)
+        CUDA_OK(cudaMemcpyAsync(seqs[y].d_chosen, chosen.get() + static_cast<size_t>(y) * KM,
+                                static_cast<size_t>(seqs[y].k) * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    std::vector<int> h_cnt(S, 0);
+    counter.download(h_cnt.data(), S, s);
+    std::vector<unsigned> h_fall(S, 0);
+    std::vector<unsigned long long> h_st(2 * S, 0);
     if (fast && timing) {
-        nfall.download(&h_fall, 1, s);
-        pstats.download(h_st, 2, s);
+        nfall.download(h_fall.data(), S, s);
+        pstats.download(h_st.data(), 2 * S, s);
     }
     ctx.sync();
-    if (fast && timing)
-        std::fprintf(stderr,
-                     "[kmeans++] N=%lld k=%d: exact-walk fallbacks %u of %d steps; per step %.0f filter candidates, "
-                     "%.0f exact folds (%s rows)\n",
-                     N, k, h_fall, k - 1, static_cast<double>(h_st[0]) / (k - 1),
-                     static_cast<double>(h_st[1]) / (k - 1), filt ? (i8 ? "int8" : "fp16") : "no filter");
+    for (int y = 0; y < S; ++y) {
+        if (seqs[y].draws_used) *seqs[y].draws_used = h_cnt[y];
+        const int k = seqs[y].k;
+        if (fast && timing && k > 1)
+            std::fprintf(stderr,
+                         "[kmeans++] N=%lld k=%d (sequence %d of %d): exact-walk fallbacks %u of %d steps; per step "
+                         "%.0f filter candidates, %.0f exact folds (%s rows)\n",
+                         N, k, y, S, h_fall[y], k - 1, static_cast<double>(h_st[2 * y]) / (k - 1),
+                         static_cast<double>(h_st[2 * y + 1]) / (k - 1), filt ? (i8 ? "int8" : "fp16") : "no filter");
+    }
 #ifdef LCN_WALK_PROFILE
     if (std::getenv("LCN_WALK_STATS")) {
         unsigned long long h[16];
@@ -2209,6 +1862,12 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
         CUDA_OK(cudaMemset(g_wt_ptr(), 0, sizeof(h)));
     }
 #endif
+}
+
+template <typename T>
+void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t first,
+                      const std::vector<unsigned long long>& raw, uint32_t* d_chosen, int* draws_used) {
+    kmeans_pp_batch<T>(ctx, X, N, d, {PPSeq{k, first, raw, d_chosen, draws_used}});
 }
 
 // ---- Lloyd (kmeans.cpp:87-143) ---------------------------------------------
@@ -2665,22 +2324,32 @@ void assign_bounded(Ctx& ctx, const T* X, long long n, int d, const double* C, i
     LAUNCH_OK("assign_exact_kernel (ambiguous, bounds)");
 }
 
-template <typename T>
-void lloyd_device(Ctx& ctx, const T* X, long long N, int d, int k, int iters, uint64_t seed, double* d_ctr,
-                  uint32_t* d_assign) {
-    if (N == 0) throw Status(2, "k-means on empty input");
-    if (k == 0 || k > N) throw Status(2, "k-means: more buckets than points");
-    cudaStream_t s = ctx.stream;
+PPSeq lloyd_seed_seq(uint64_t seed, long long N, int k, uint32_t* d_chosen) {
     // k-means++ init with the reference's engine and distributions (kmeans.cpp:93-94).
     std::mt19937_64 rng(seed);
     std::uniform_int_distribution<std::size_t> first(0, static_cast<std::size_t>(N - 1));
-    uint64_t f = first(rng);
-    std::vector<unsigned long long> raw(k > 1 ? k - 1 : 0);
-    for (auto& r : raw) r = rng();
-    DevBuf<uint32_t> init(k);
-    {
+    PPSeq q;
+    q.k = k;
+    q.first = first(rng);
+    q.raw.resize(k > 1 ? k - 1 : 0);
+    for (auto& r : q.raw) r = rng();
+    q.d_chosen = d_chosen;
+    q.draws_used = nullptr;
+    return q;
+}
+
+template <typename T>
+void lloyd_device(Ctx& ctx, const T* X, long long N, int d, int k, int iters, uint64_t seed, double* d_ctr,
+                  uint32_t* d_assign, const uint32_t* init_in) {
+    if (N == 0) throw Status(2, "k-means on empty input");
+    if (k == 0 || k > N) throw Status(2, "k-means: more buckets than points");
+    cudaStream_t s = ctx.stream;
+    DevBuf<uint32_t> init_buf(init_in ? 1 : k);
+    const uint32_t* init = init_in;
+    if (!init_in) {
         PhaseTimer pt(ctx, "  k-means++ seeding");
-        kmeans_pp_device<T>(ctx, X, N, d, k, f, raw, init.get(), nullptr);
+        kmeans_pp_batch<T>(ctx, X, N, d, {lloyd_seed_seq(seed, N, k, init_buf.get())});
+        init = init_buf.get();
     }
     PhaseTimer pt_lloyd(ctx, "  lloyd iterations + final assign");
     // centroids = rows of the seeds (kmeans.cpp:99-100)
@@ -2690,7 +2359,7 @@ void lloyd_device(Ctx& ctx, const T* X, long long N, int d, int k, int iters, ui
         for (int c = 0; c < k; ++c) st[c] = c;
         dummy_counts.upload(ones.data(), k, s);
         dummy_start.upload(st.data(), k, s);
-        centroid_kernel<T><<<k, 128, 0, s>>>(X, d, init.get(), dummy_start.get(), dummy_counts.get(), d_ctr);
+        centroid_kernel<T><<<k, 128, 0, s>>>(X, d, init, dummy_start.get(), dummy_counts.get(), d_ctr);
         LAUNCH_OK("centroid init");
         ctx.sync();
     }
@@ -2778,7 +2447,9 @@ void lloyd_device(Ctx& ctx, const T* X, long long N, int d, int k, int iters, ui
     template void kmeans_pp_device<T>(Ctx&, const T*, long long, int, int, uint64_t,                    \
                                       const std::vector<unsigned long long>&, uint32_t*, int*);         \
     template void assign_device<T>(Ctx&, const T*, long long, int, const double*, int, uint32_t*);      \
-    template void lloyd_device<T>(Ctx&, const T*, long long, int, int, int, uint64_t, double*, uint32_t*);
+    template void kmeans_pp_batch<T>(Ctx&, const T*, long long, int, const std::vector<PPSeq>&);          \
+    template void lloyd_device<T>(Ctx&, const T*, long long, int, int, int, uint64_t, double*, uint32_t*,  \
+                                  const uint32_t*);
 LCNB_INST(double)
 LCNB_INST(float)
 #undef LCNB_INST

@@ -101,6 +101,7 @@ struct Op {
     DevBuf<float> X32;                    // fp32 copy of X when every coordinate is fp32-exact (k-means reads)
     DevBuf<double> norms;                 // per-point sum x_k^2 (cosine-derived cost only)
     bool landmarks_ready = false;         // L already selected (concurrently with the LSH k-means)
+    DevBuf<uint32_t> landmark_init;       // landmark k-means++ indices, seeded with the LSH bands (or empty)
     bool factors_ready = false;           // U, V^T, W already built (concurrently with the LSH k-means)
     std::vector<Band> bands;
     std::vector<DevBuf<double>> val64;    // sparse: log K; lcn: delta (fp64 master)
@@ -182,9 +183,16 @@ struct LshParams {
     int bands = 1, rows = 1, buckets = 2, iters = 10, branching = 2;
     uint64_t seed = 0;
 };
+// A k-means seeded together with the LSH bands' (same points): its k and
+// engine seed, and where its k-means++ indices go (the landmark k-means).
+struct ExtraSeeding {
+    int k = 0;
+    uint64_t seed = 0;
+    uint32_t* out = nullptr;
+};
 void lsh_bucket_ids(Ctx& ctx, const double* d_union, const float* d_union32, size_t n, size_t m, size_t d,
                     const LshParams& cfg, std::vector<DevBuf<uint32_t>>& ids, size_t& range,
-                    const std::function<void(Ctx&)>& extra = {});
+                    const std::function<void(Ctx&)>& extra = {}, const ExtraSeeding* extra_seed = nullptr);
 void cross_polytope_buckets_device(Ctx& ctx, const double* X, long long N, int d, const double* h_proj, int half,
                                    uint32_t* out);
 bool nystrom_inverse_host(const double* A, int l, double rel, double* ainv, double* aj_out);
