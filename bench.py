@@ -876,6 +876,10 @@ def main():
         return 0
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    # our device pool: map 64 GB up front (the library's allocations are then
+    # carved from resident memory; see lcn_ctx_create) -- the configs[3]
+    # build + solve peaks well below that on a 180 GB B200
+    os.environ.setdefault("LCN_POOL_RESERVE_GB", "64")
     if world > 1:
         os.environ.setdefault("NCCL_DEBUG", "INFO")  # NCCL's init lines (rings, NVLS) go to stderr
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")

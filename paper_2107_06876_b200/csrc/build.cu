@@ -1579,6 +1579,8 @@ void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed,
     op.landmarks_ready = false;
     ctx.sync();
     PhaseTimer ptf(ctx, "nystrom factors U, V, A, W");
+    std::optional<PhaseTimer> pt0;
+    pt0.emplace(ctx, "  norms, U / V allocation");
     const double* nrm = union_norms(op, s);
     DevBuf<double> lnorm;
     if (op.cost == 2) {
@@ -1599,6 +1601,7 @@ void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed,
     // U = k(X_p, L) (n x l), V^T = k(X_q, L) (m x l), A = k(L, L) with division.
     op.U64.resize(std::max<size_t>(n * l, 1));
     DevBuf<double> Vt(std::max<size_t>(m * l, 1)), A(l * l);
+    pt0.reset();
     {
     PhaseTimer ptuv(ctx, "  U, V point x landmark blocks");
     if (use_tc_build(op, 2)) {  // point x landmark blocks on the tensor cores (3xTF32)
@@ -1665,8 +1668,10 @@ void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed,
     for (size_t i = 0; i < l; ++i) trace += a[i * l + i];
     const LD jitter_unit = trace / static_cast<LD>(l);
 
+    pt0.emplace(ctx, "  W allocation");
     op.Wt64.resize(std::max<size_t>(m * l, 1));
     DevBuf<double> dAinv(l * l), dAj(l * l);
+    pt0.reset();
     DevBuf<unsigned long long> rbits(1);
     for (double rel = 0.0; rel <= 1.1e-4; rel = (rel == 0.0 ? 1e-10 : rel * 10.0)) {
         std::vector<LD> aj = a;

@@ -452,6 +452,26 @@ int lcn_ctx_create(int device, int flags, lcn_ctx** out) {
         uint64_t keep = ~0ull;
         CUDA_OK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
         CUDA_OK(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking));
+        // LCN_POOL_RESERVE_GB: map that much into the pool up front (one
+        // allocation, freed at once and kept). A build's multi-GB buffers
+        // are then carved from resident memory instead of growing the pool
+        // (mapping fresh memory mid-build cost 0.1-0.25 s per configs[3]
+        // build whenever the job threads' allocation order fragmented it).
+        if (const char* rv = std::getenv("LCN_POOL_RESERVE_GB")) {
+            const double gb = std::atof(rv);
+            uint64_t have = 0;
+            CUDA_OK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &have));
+            const size_t want = gb > 0 ? static_cast<size_t>(gb * 1073741824.0) : 0;
+            if (want > have) {
+                void* p = nullptr;
+                if (cudaMallocAsync(&p, want - have, c->c.stream) == cudaSuccess) {
+                    CUDA_OK(cudaFreeAsync(p, c->c.stream));
+                } else {
+                    cudaGetLastError();  // not enough free memory: skip the reservation
+                }
+                CUDA_OK(cudaStreamSynchronize(c->c.stream));
+            }
+        }
         c->c.own_stream = c->c.stream;
         *out = c.release();
     });

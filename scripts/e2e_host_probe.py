@@ -4,6 +4,7 @@ usage: LCN_TIMING=1 python scripts/e2e_host_probe.py [reps]"""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
+os.environ.setdefault("LCN_POOL_RESERVE_GB", "64")
 import torch
 import paper_2107_06876_b200 as lcn
 from paper_2107_06876_b200 import configs
