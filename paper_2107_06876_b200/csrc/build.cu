@@ -1332,7 +1332,9 @@ struct HostLdlt {
             LD dk = f[k * l + k];
             for (size_t j = 0; j < k; ++j) dk -= f[k * l + j] * w[j];
             f[k * l + k] = dk;
-#pragma omp parallel for schedule(static) if (l - k > 256)
+            // row updates in parallel down to short columns (each entry's
+            // operation order is unchanged: bit-identical for any team)
+#pragma omp parallel for schedule(static) if ((l - k) * k > 8192)
             for (long long ii = static_cast<long long>(k) + 1; ii < static_cast<long long>(l); ++ii) {
                 const size_t i = static_cast<size_t>(ii);
                 LD v = f[i * l + k];
@@ -1678,23 +1680,49 @@ void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed,
         for (size_t i = 0; i < l; ++i) aj[i * l + i] += rel * jitter_unit;
         std::optional<PhaseTimer> pt_sub;
         pt_sub.emplace(ctx, "  host LDLT + inverse (long double)");
-        HostLdlt fac(aj, l);
-        if (!fac.ok) continue;
         std::vector<LD> inv(l * l);
-        bool finite = true;
-        // on a concurrent build job the other jobs' host threads are busy:
-        // leave them cores (an oversubscribed team stalls at its barriers)
-        const int nthr = on ? std::max(1, omp_get_num_procs() / 2 - 2) : omp_get_max_threads();
-#pragma omp parallel for schedule(static) reduction(&& : finite) num_threads(nthr)
-        for (long long cc = 0; cc < static_cast<long long>(l); ++cc) {
-            std::vector<LD> e(l, 0.0L);
-            e[cc] = 1.0L;
-            fac.solve(e.data());
-            for (size_t r = 0; r < l; ++r) {
-                inv[r * l + cc] = e[r];
-                if (!std::isfinite(e[r])) finite = false;
+        bool finite = true, fok = true;
+        auto factor = [&] {
+            HostLdlt fac(aj, l);
+            if (!fac.ok) {
+                fok = false;
+                return;
             }
+            // on a concurrent build job the other jobs' host threads are busy:
+            // leave them cores (an oversubscribed team stalls at its barriers)
+            const int nthr = on ? std::max(1, omp_get_num_procs() / 2 - 2) : omp_get_max_threads();
+            bool fin = true;
+#pragma omp parallel for schedule(static) reduction(&& : fin) num_threads(nthr)
+            for (long long cc = 0; cc < static_cast<long long>(l); ++cc) {
+                std::vector<LD> e(l, 0.0L);
+                e[cc] = 1.0L;
+                fac.solve(e.data());
+                for (size_t r = 0; r < l; ++r) {
+                    inv[r * l + cc] = e[r];
+                    if (!std::isfinite(e[r])) fin = false;
+                }
+            }
+            finite = fin;
+        };
+        if (op.during_ldlt) {
+            // the first factorisation on a host thread while this one drives
+            // device work that does not need the factors (K_sp, the CSR
+            // support): the GPU is otherwise idle during the LDL^T
+            auto work = std::move(op.during_ldlt);
+            op.during_ldlt = nullptr;
+            std::thread th(factor);
+            std::exception_ptr err;
+            try {
+                work();
+            } catch (...) {
+                err = std::current_exception();
+            }
+            th.join();
+            if (err) std::rethrow_exception(err);
+        } else {
+            factor();
         }
+        if (!fok) continue;
         pt_sub.reset();
         pt_sub.emplace(ctx, "  W = V A^-T, residual (device GEMMs)");
         if (!finite) continue;
@@ -1846,9 +1874,12 @@ void wgemm_resid(Ctx& ctx, const double* Vt, const double* Ainv, const double* A
 void build_correction(Op& op) {
     Ctx& ctx = *op.ctx;
     PhaseTimer pt(ctx, "LCN correction (incl. K_sp)");
-    // log K^sp first (same values as build_sparse), then delta.
-    build_sparse_values(op);
-    op.logk64 = std::move(op.val64);
+    // log K^sp first (same values as build_sparse; already built when the
+    // factor build overlapped it with its host LDL^T), then delta.
+    if (op.logk64.size() != op.bands.size()) {
+        build_sparse_values(op);
+        op.logk64 = std::move(op.val64);
+    }
     op.val64.clear();
     DevBuf<unsigned long long> maxbits(1);
     DevBuf<int> overflow(1);

@@ -393,7 +393,15 @@ void finish_sparse(Op& op) {
 void finish_lcn(Op& op, const double* landmarks, size_t l, int method, uint64_t seed) {
     op.l = l;
     op.kind = op.bands.empty() ? LCN_OP_NYSTROM : LCN_OP_LCN;
+    if (op.kind == LCN_OP_LCN && !op.ctx->comm)
+        op.during_ldlt = [&op] {  // overlapped with the host LDL^T
+            build_sparse_values(op);
+            op.logk64 = std::move(op.val64);
+            op.val64.clear();
+            build_csr(op);
+        };
     build_nystrom(op, landmarks, method, seed);
+    op.during_ldlt = nullptr;
     if (op.kind == LCN_OP_LCN) {
         build_correction(op);
         build_csr(op);

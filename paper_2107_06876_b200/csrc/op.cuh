@@ -110,6 +110,7 @@ struct Op {
     std::vector<DevBuf<float>> val32T;
     std::vector<DevBuf<double>> val64T;
     std::vector<DevBuf<double>> logk64;   // lcn: log K^sp at stored entries
+    std::function<void()> during_ldlt;     // device work overlapped with the host LDL^T (build_nystrom)
     // lcn: iteration layout per band; in fp32 storage the compact bands' val32
     // (column pass) and val32T (row pass) hold their panels instead of blocks
     std::vector<BandIter> iter;
