@@ -907,26 +907,12 @@ __device__ __forceinline__ void predict_binade(double a, double b, int& e_one, i
     }
 }
 
-__global__ void __launch_bounds__(256, 4) fold_round_kernel(const double* __restrict__ x, long long N,
-                                                            const double* __restrict__ csum, int* __restrict__ ebin,
-                                                         longlong2* __restrict__ R, longlong2* __restrict__ Rseg,
-                                                         int* __restrict__ Eseg, int* __restrict__ spred,
-                                                         unsigned* __restrict__ smask, double* __restrict__ s0end,
-                                                         const int* __restrict__ skip, int hs, PPB pb) {
-    pdl_wait();
-    pdl_launch_dependents();
-    const int y = blockIdx.y;
-    if (hs >= pb.k[y]) return;
-    if (skip && skip[y]) return;  // pp_pick_kernel certified this step's pick
-    x += y * pb.sN;
-    csum += y * pb.sC;
-    ebin += y * pb.sC;
-    R += y * pb.sC;
-    Rseg += static_cast<long long>(y) * pb.sC * 2 * kSegs;
-    Eseg += static_cast<long long>(y) * pb.sC * kSegs;
-    spred += y * pb.sC;
-    smask += y * pb.sC;
-    s0end += y;
+// One chunk of fold_round_kernel (cb = the chunk).
+__device__ __forceinline__ void fold_round_chunk(const int cb, const double* __restrict__ x, long long N,
+                                                 const double* __restrict__ csum, int* __restrict__ ebin,
+                                                 longlong2* __restrict__ R, longlong2* __restrict__ Rseg,
+                                                 int* __restrict__ Eseg, int* __restrict__ spred,
+                                                 unsigned* __restrict__ smask, double* __restrict__ s0end) {
     __shared__ ParInc stot[kSegs];
     __shared__ double ssum[kSegs];
     __shared__ double red[8];
@@ -936,7 +922,7 @@ __global__ void __launch_bounds__(256, 4) fold_round_kernel(const double* __rest
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane / kLanesPerSeg;
     const int si = warp * (32 / kLanesPerSeg) + g;
-    const long long b = static_cast<long long>(blockIdx.x) * kFoldChunk + threadIdx.x * kRoundPer;
+    const long long b = static_cast<long long>(cb) * kFoldChunk + threadIdx.x * kRoundPer;
     double xv[kRoundPer];
     double xsum = 0.0;
 #pragma unroll
@@ -946,13 +932,13 @@ __global__ void __launch_bounds__(256, 4) fold_round_kernel(const double* __rest
     }
     // approximate start of this chunk: the earlier chunks' approximate sums
     double a = 0.0;
-    for (int c = threadIdx.x; c < static_cast<int>(blockIdx.x); c += 256) a += csum[c];
+    for (int c = threadIdx.x; c < static_cast<int>(cb); c += 256) a += csum[c];
     a = warp_sum(a);
     if (lane == 0) red[warp] = a;
 #pragma unroll
     for (int o = 1; o < kLanesPerSeg; o <<= 1) xsum += __shfl_xor_sync(0xffffffffu, xsum, o);
     if ((lane & (kLanesPerSeg - 1)) == 0) ssum[si] = xsum;
-    if (blockIdx.x == 0)
+    if (cb == 0)
 #pragma unroll
         for (int j = 0; j < kRoundPer; ++j) c0buf[threadIdx.x * kRoundPer + j] = xv[j];
     __syncthreads();
@@ -971,15 +957,15 @@ __global__ void __launch_bounds__(256, 4) fold_round_kernel(const double* __rest
         predict_binade(a0 + (incl - v), a0 + incl, e_one, e_base);
         predict_binade(a0, a0 + __shfl_sync(0xffffffffu, incl, 31), ec_one, ec_base);
         sbase[lane] = e_base;
-        Eseg[static_cast<long long>(blockIdx.x) * kSegs + lane] = e_base;
+        Eseg[static_cast<long long>(cb) * kSegs + lane] = e_base;
         const unsigned straddle = __ballot_sync(0xffffffffu, e_one == kNoBinade);
         const unsigned one = __ballot_sync(0xffffffffu, e_one == ec_one && ec_one != kNoBinade);
         if (lane == 0) {
             all_one = one == 0xffffffffu;
             e_chunk = ec_one;
-            ebin[blockIdx.x] = ec_one;
-            spred[blockIdx.x] = straddle ? __ffs(straddle) - 1 : 0;
-            smask[blockIdx.x] = straddle;
+            ebin[cb] = ec_one;
+            spred[cb] = straddle ? __ffs(straddle) - 1 : 0;
+            smask[cb] = straddle;
         }
     }
     __syncthreads();
@@ -1017,7 +1003,7 @@ __global__ void __launch_bounds__(256, 4) fold_round_kernel(const double* __rest
     const bool sbad1 = (__ballot_sync(0xffffffffu, bad1) & gmask) != 0;
     acc0 = par_scan8(acc0, lane);
     acc1 = par_scan8(acc1, lane);
-    longlong2* seg = Rseg + static_cast<long long>(blockIdx.x) * (2 * kSegs);
+    longlong2* seg = Rseg + static_cast<long long>(cb) * (2 * kSegs);
     if ((lane & (kLanesPerSeg - 1)) == kLanesPerSeg - 1) {
         seg[si] = sbad0 ? make_longlong2(-1, -1) : par_clamp(acc0);
         seg[kSegs + si] = sbad1 ? make_longlong2(-1, -1) : par_clamp(acc1);
@@ -1031,8 +1017,8 @@ __global__ void __launch_bounds__(256, 4) fold_round_kernel(const double* __rest
         const bool ok = all_one && __ballot_sync(0xffffffffu, stot[lane].i0 < 0) == 0;
         const ParInc sl = stot[lane];
         const ParInc tot = par_scan_ns(sl.i0 < 0 ? ParInc{0, 0} : sl, lane);
-        if (lane == 31) R[blockIdx.x] = ok ? par_clamp(tot) : make_longlong2(-1, -1);
-        if (blockIdx.x == 0) {
+        if (lane == 31) R[cb] = ok ? par_clamp(tot) : make_longlong2(-1, -1);
+        if (cb == 0) {
             // chunk 0 starts the fold at 0, where the sum climbs binade after
             // binade: fold it literally here, in parallel with the other chunks
             const double2* c2 = reinterpret_cast<const double2*>(c0buf);
@@ -1049,6 +1035,34 @@ __global__ void __launch_bounds__(256, 4) fold_round_kernel(const double* __rest
         }
     }
     (void)e_chunk;
+}
+
+// Persistent over the chunks (grid-stride): a certified step (skip) costs
+// only the resident CTAs' exit, not a 977-CTA launch.
+__global__ void __launch_bounds__(256, 4) fold_round_kernel(const double* __restrict__ x, long long N,
+                                                            const double* __restrict__ csum, int* __restrict__ ebin,
+                                                         longlong2* __restrict__ R, longlong2* __restrict__ Rseg,
+                                                         int* __restrict__ Eseg, int* __restrict__ spred,
+                                                         unsigned* __restrict__ smask, double* __restrict__ s0end,
+                                                         const int* __restrict__ skip, int hs, PPB pb, int nch) {
+    pdl_wait();
+    pdl_launch_dependents();
+    const int y = blockIdx.y;
+    if (hs >= pb.k[y]) return;
+    if (skip && skip[y]) return;  // pp_pick_kernel certified this step's pick
+    x += y * pb.sN;
+    csum += y * pb.sC;
+    ebin += y * pb.sC;
+    R += y * pb.sC;
+    Rseg += static_cast<long long>(y) * pb.sC * 2 * kSegs;
+    Eseg += static_cast<long long>(y) * pb.sC * kSegs;
+    spred += y * pb.sC;
+    smask += y * pb.sC;
+    s0end += y;
+    for (int c = blockIdx.x; c < nch; c += gridDim.x) {
+        fold_round_chunk(c, x, N, csum, ebin, R, Rseg, Eseg, spred, smask, s0end);
+        __syncthreads();  // the chunk's shared tables are reused by the next
+    }
 }
 
 // ---- literal fold of one segment -------------------------------------------
@@ -1679,7 +1693,14 @@ void kmeans_pp_batch(Ctx& ctx, const T* X, long long N, int d, const std::vector
     size_t walk_smem = static_cast<size_t>(nch) * (sizeof(longlong2) + sizeof(double) + 4 * sizeof(int)) + sizeof(double) +
                        static_cast<size_t>(kMaxPre) * (2 * kSegs * sizeof(longlong2) + kSegLen * sizeof(double) +
                                                        kSegs * sizeof(int));
-    int walk_staged = walk_smem <= 200 * 1024;
+    // staged walk (its plans in 200 KB of shared memory) only on request:
+    // with the certified pick the walk runs on ~0.4 % of the steps, and a
+    // launch that needs a whole SM's shared memory just to exit costs more
+    // (LCN_PP_WALK_STAGED=1, or always without the certified pick)
+    const char* wsenv = std::getenv("LCN_PP_WALK_STAGED");
+    const char* wenv0 = std::getenv("LCN_PP_EXACT_WALK");
+    const bool want_staged = (wsenv && wsenv[0] == '1') || (wenv0 && wenv0[0] == '1');
+    int walk_staged = want_staged && walk_smem <= 200 * 1024;
     if (walk_staged)
         allow_max_dyn_smem(pp_walk_pick_kernel);
     else
@@ -1787,6 +1808,7 @@ void kmeans_pp_batch(Ctx& ctx, const T* X, long long N, int d, const std::vector
     const bool pdl = !(penv && penv[0] == '0');
     const dim3 b256(256), b128(128);
     const unsigned Sy = static_cast<unsigned>(S);
+    const int fr_grid = std::min(nch, 4 * ctx.num_sms);
     for (int t = 1; t < KM; ++t) {
         if (t > 1)
             launch_pdl(seed_dist_kernel<T>, dim3(ceil_div(t - 1, 8), Sy), b256, 0, s, pdl, X, d, chosen.get(), t - 1,
@@ -1821,8 +1843,8 @@ void kmeans_pp_batch(Ctx& ctx, const T* X, long long N, int d, const std::vector
                        timing ? pstats.get() : nullptr, pk_smem ? 1 : 0, pb);
             skp = skip.get();
         }
-        launch_pdl(fold_round_kernel, dim3(nch, Sy), b256, 0, s, pdl, dist2.get(), N, csum.get(), ebin.get(), R.get(),
-                   Rseg.get(), Eseg.get(), spred.get(), smask.get(), s0end.get(), skp, t, pb);
+        launch_pdl(fold_round_kernel, dim3(fr_grid, Sy), b256, 0, s, pdl, dist2.get(), N, csum.get(), ebin.get(),
+                   R.get(), Rseg.get(), Eseg.get(), spred.get(), smask.get(), s0end.get(), skp, t, pb, nch);
         launch_pdl(pp_walk_pick_kernel, dim3(1, Sy), dim3(kWalkThreads), walk_smem, s, pdl, dist2.get(), used.get(), N,
                    nch, ebin.get(), spred.get(), R.get(), Rseg.get(), Eseg.get(), smask.get(), s0end.get(), csum.get(),
                    cnt.get(), sstart.get(), d_raw.get(), KM - 1, counter.get(), chosen.get(), t, walk_staged, skp, pb);
