@@ -27,6 +27,7 @@
 #include <numeric>
 #include <optional>
 #include <functional>
+#include <mutex>
 #include <thread>
 #include <exception>
 #include <deque>
@@ -202,6 +203,8 @@ __global__ void narrow_kernel(uint32_t* __restrict__ out, const uint64_t* __rest
 // job, each on its own copy of the context. Their seeding walks are
 // latency-bound single-CTA kernels, so the jobs overlap well. Results do not
 // depend on the overlap (every job is deterministic on its own).
+void* cublas_pool_take(int device);
+void cublas_pool_give(int device, void* h);
 void run_jobs(Ctx& ctx, std::vector<std::function<void(Ctx&)>>& jobs) {
     if (jobs.size() == 1) {
         jobs[0](ctx);
@@ -230,7 +233,7 @@ void run_jobs(Ctx& ctx, std::vector<std::function<void(Ctx&)>>& jobs) {
         });
     for (auto& t : th) t.join();
     for (auto& c : ctxs) {
-        if (c.cublas) cublasDestroy(static_cast<cublasHandle_t>(c.cublas));
+        cublas_pool_give(c.device, c.cublas);  // back to the pool, not destroyed
         cudaStreamDestroy(c.stream);
     }
     for (auto& e : errs)
@@ -1834,12 +1837,36 @@ void uv_gemm_exp(Ctx& ctx, const double* X, size_t rows, const double* L, size_t
     LAUNCH_OK("U / V from fp64 GEMM");
 }
 
-cublasHandle_t cublas_of(Ctx& ctx) {
-    if (!ctx.cublas) {
-        cublasHandle_t h = nullptr;
-        if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) throw Status(100, "cublasCreate failed");
-        ctx.cublas = h;
+// Build jobs (run_jobs) run on copies of the context without a handle; they
+// take one from this process-wide pool and give it back when the job ends,
+// so a build does not pay cublasCreate per job (~0.1-0.2 s each on a fresh
+// box). Handles are per device; a handle serves one thread at a time.
+namespace {
+std::mutex g_cublas_mu;
+std::vector<std::pair<int, cublasHandle_t>> g_cublas_free;
+}  // namespace
+void* cublas_pool_take(int device) {
+    {
+        std::lock_guard<std::mutex> lk(g_cublas_mu);
+        for (size_t i = 0; i < g_cublas_free.size(); ++i)
+            if (g_cublas_free[i].first == device) {
+                cublasHandle_t h = g_cublas_free[i].second;
+                g_cublas_free.erase(g_cublas_free.begin() + static_cast<long>(i));
+                return h;
+            }
     }
+    cublasHandle_t h = nullptr;
+    if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) throw Status(100, "cublasCreate failed");
+    return h;
+}
+void cublas_pool_give(int device, void* h) {
+    if (!h) return;
+    std::lock_guard<std::mutex> lk(g_cublas_mu);
+    g_cublas_free.emplace_back(device, static_cast<cublasHandle_t>(h));
+}
+
+cublasHandle_t cublas_of(Ctx& ctx) {
+    if (!ctx.cublas) ctx.cublas = cublas_pool_take(ctx.device);
     cublasHandle_t h = static_cast<cublasHandle_t>(ctx.cublas);
     cublasSetStream(h, ctx.stream);
     return h;

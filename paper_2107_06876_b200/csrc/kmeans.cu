@@ -13,6 +13,7 @@
 //   * empty clusters are re-seeded in increasing cluster order to the first
 //     farthest point among clusters of size > 1 (kmeans.cpp:122-139).
 #include <cub/cub.cuh>
+#include <cublas_v2.h>
 #include <cuda_fp16.h>
 
 #include <cstdio>
@@ -2154,10 +2155,112 @@ __global__ void __launch_bounds__(256, 1) assign_filter_kernel(const float* __re
     }
 }
 
+cublasHandle_t cublas_of(Ctx& ctx);  // build.cu
+
+// fp32 filter for d > 128 (configs[1] / [2]: d = 300), where neither the
+// tensor-core filter (points in TMEM, d <= 128) nor the FMA register tiles
+// (d <= 128 in shared memory) apply: the dots x.c_f for a chunk of points
+// come from one fp32 GEMM (cuBLAS, CUBLAS_COMPUTE_32F_PEDANTIC: no TF32,
+// whatever the environment says), a warp per point then keeps the best and
+// second-best score v(c) = |c_f|^2 - 2 x.c_f and applies the same rigorous
+// gap test as assign_filter_kernel, with gamma_{d+8} for a dot summed in
+// any order (split-K included). Ambiguous points get the exact scan.
+__global__ void __launch_bounds__(256) gemm_top2_kernel(const float* __restrict__ X, long long p0, long long np,
+                                                        int d, const float* __restrict__ S, int Kp, int k,
+                                                        const float* __restrict__ ncf,
+                                                        const unsigned long long* __restrict__ cmax,
+                                                        uint32_t* __restrict__ out, uint32_t* __restrict__ amb,
+                                                        unsigned* __restrict__ namb) {
+    const int lane = threadIdx.x & 31;
+    const long long i = blockIdx.x * 8LL + (threadIdx.x >> 5);
+    if (i >= np) return;
+    const long long p = p0 + i;
+    const float* sc = S + i * Kp;
+    float v1 = kPosInf, v2 = kPosInf;
+    int i1 = 0;
+    for (int c = lane; c < k; c += 32) {
+        const float v = fmaf(-2.0f, sc[c], ncf[c]);  // one rounding of |c_f|^2 - 2 x.c_f
+        if (v < v1) { v2 = v1; v1 = v; i1 = c; }
+        else if (v < v2) v2 = v;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const float ov1 = __shfl_xor_sync(0xffffffffu, v1, o), ov2 = __shfl_xor_sync(0xffffffffu, v2, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, i1, o);
+        v2 = fminf(fminf(v2, ov2), fmaxf(v1, ov1));
+        if (ov1 < v1 || (ov1 == v1 && oi < i1)) i1 = oi;
+        v1 = fminf(v1, ov1);
+    }
+    double xn = 0.0;
+    for (int kk = lane; kk < d; kk += 32) {
+        const double xv = static_cast<double>(X[p * d + kk]);
+        xn += xv * xv;
+    }
+    xn = warp_sum(xn);
+    if (lane == 0) {
+        const double u = 5.9604644775390625e-08;  // 2^-24
+        const double g = (d + 8) * u / (1.0 - (d + 8) * u);
+        const double Cn = sqrt(__longlong_as_double(*cmax)) * (1.0 + 1e-12);
+        const double x = sqrt(xn) * (1.0 + 1e-12);
+        const double E = 1.05 * ((2.0 * g + 4.0 * u) * x * Cn + 4.0 * u * Cn * Cn + u * u * Cn * Cn) +
+                         1e-12 * (x + Cn) * (x + Cn);
+        const double gap = static_cast<double>(v2) - static_cast<double>(v1);
+        if (gap > 2.0 * E) out[p] = static_cast<uint32_t>(i1);
+        else amb[atomicAdd(namb, 1u)] = static_cast<uint32_t>(p);
+    }
+}
+
+void assign_gemm_filter(Ctx& ctx, const float* X, long long N, int d, const double* C, int k, uint32_t* out,
+                        uint32_t* amb, unsigned* namb) {
+    cudaStream_t s = ctx.stream;
+    const int Kp = static_cast<int>(ceil_div(k, 32)) * 32;
+    DevBuf<float> CfT(static_cast<size_t>(d) * Kp), ncf(Kp);
+    DevBuf<unsigned long long> cmax(1);
+    cmax.zero(s);
+    filter_prep_kernel<<<Kp, 128, 0, s>>>(C, k, d, Kp, CfT.get(), ncf.get(), cmax.get());
+    LAUNCH_OK("gemm filter prep");
+    const long long chunk = std::max<long long>(1, std::min<long long>(N, (64LL << 20) / Kp));  // 256 MB of scores
+    DevBuf<float> S(static_cast<size_t>(chunk) * Kp);
+    cublasHandle_t h = cublas_of(ctx);
+    const float one = 1.0f, zero = 0.0f;
+    for (long long p0 = 0; p0 < N; p0 += chunk) {
+        const long long np = std::min(chunk, N - p0);
+        // S (Kp x np, column-major) = CfT^T-view (Kp x d) * X_chunk^T (d x np)
+        if (cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_N, Kp, static_cast<int>(np), d, &one, CfT.get(), CUDA_R_32F, Kp,
+                         X + p0 * d, CUDA_R_32F, d, &zero, S.get(), CUDA_R_32F, Kp, CUBLAS_COMPUTE_32F_PEDANTIC,
+                         CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
+            throw Status(100, "cublasGemmEx failed (assignment filter)");
+        gemm_top2_kernel<<<static_cast<unsigned>(ceil_div(np, 8)), 256, 0, s>>>(X, p0, np, d, S.get(), Kp, k,
+                                                                                ncf.get(), cmax.get(), out, amb,
+                                                                                namb);
+        LAUNCH_OK("gemm_top2_kernel");
+    }
+}
+
 template <typename T>
 void assign_device(Ctx& ctx, const T* X, long long N, int d, const double* C, int k, uint32_t* out) {
     if (N == 0) return;
     cudaStream_t s = ctx.stream;
+    // fp32 filter for big problems with fp32 points: a GEMM + top-2 pass for
+    // d > kFD (LCN_FILTER=exact: no filter there)
+    const char* fsel0 = std::getenv("LCN_FILTER");
+    if (std::is_same<T, float>::value && d > kFD && N * static_cast<long long>(k) >= (1LL << 22) &&
+        !(fsel0 && std::string(fsel0) == "exact")) {
+        DevBuf<uint32_t> amb(N);
+        DevBuf<unsigned> namb(1);
+        namb.zero(s);
+        assign_gemm_filter(ctx, reinterpret_cast<const float*>(X), N, d, C, k, out, amb.get(), namb.get());
+        unsigned h_amb = 0;
+        namb.download(&h_amb, 1, s);
+        ctx.sync();
+        ctx.filter_ambiguous += h_amb;
+        ctx.filter_points += N;
+        if (h_amb)
+            assign_exact_kernel<T><<<ceil_div(static_cast<long long>(h_amb), TP), 256, 0, s>>>(X, h_amb, d, C, k, out,
+                                                                                                nullptr, amb.get());
+        LAUNCH_OK("assign_exact_kernel (ambiguous, gemm filter)");
+        return;
+    }
     // fp32 filter for big problems (fp32 points, d <= kFD)
     if (std::is_same<T, float>::value && d <= kFD && N * static_cast<long long>(k) >= (1LL << 22)) {
         const int Kp = static_cast<int>(ceil_div(k, kFB)) * kFB;

@@ -97,6 +97,27 @@ def test_assign_filter_bit_exact(ctx, ref, n, d, k, seed, dup):
     assert np.array_equal(lcn.assign_nearest(ctx, x, ctr), ref.assign_nearest(x, ctr))
 
 
+@pytest.mark.parametrize("dup", [False, True])
+def test_assign_gemm_filter_bit_exact(ctx, ref, dup):
+    # d > 128 with N k >= 2^22: the fp32 GEMM + top-2 filter (configs[1]'s
+    # d = 300) and its exact fallback; dup: exact ties, lowest index wins
+    n, d, k = 40000, 300, 128
+    x = rng_points(25, n, d, comps=30)
+    r = np.random.default_rng(25)
+    ctr = x[r.choice(n, k, replace=False)] + r.standard_normal((k, d)) * 0.3
+    if dup:
+        ctr[k // 2:] = ctr[:k // 2]
+    assert np.array_equal(lcn.assign_nearest(ctx, x, ctr), ref.assign_nearest(x, ctr))
+
+
+def test_lloyd_gemm_filter_bit_exact(ctx, ref):
+    x = rng_points(27, 40000, 300, comps=50)
+    c_gpu, a_gpu = lcn.lloyd(ctx, x, 128, 10, 27)
+    c_ref, a_ref = ref.lloyd(x, 128, 10, 27)
+    assert np.array_equal(a_gpu, a_ref)
+    assert np.array_equal(c_gpu.view(np.uint64), c_ref.view(np.uint64))
+
+
 def test_lloyd_filter_bit_exact(ctx, ref):
     x = rng_points(31, 30000, 64, comps=40)
     c_gpu, a_gpu = lcn.lloyd(ctx, x, 160, 10, 31)
