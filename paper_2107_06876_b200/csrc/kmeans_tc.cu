@@ -46,7 +46,10 @@ constexpr int kTD = 128;        // padded feature count (tf32 columns)
 constexpr int kTHalf = kTN * kTD * 4;   // bytes of one tile half (hi or lo): 32 KB
 constexpr int kTStage = 2 * kTHalf;     // hi + lo
 constexpr int kTStages = 3;
-constexpr int kTCluster = 4;            // CTAs sharing each centroid stage (multicast)
+#ifndef LCN_TC_CLUSTER
+#define LCN_TC_CLUSTER 4
+#endif
+constexpr int kTCluster = LCN_TC_CLUSTER;  // CTAs sharing each centroid stage (multicast)
 constexpr int kTAcc = 4;                // accumulator buffers in TMEM (columns 256..511)
 constexpr int kTSlice = kTStage / kTCluster;
 constexpr int kTEpi = 8;              // epilogue warps: two per TMEM lane quadrant
@@ -133,6 +136,21 @@ __device__ __forceinline__ void tc_mma_tf32_elect(uint32_t d_tmem, uint32_t a_tm
         "elect.sync _|e, 0xffffffff;\n\t"
         "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
         "r"(a_tmem), "l"(b_desc), "r"(kIdesc), "r"(acc)
+        : "memory");
+}
+// the three 3xTF32 products of one K step under one election:
+// x_hi.c_hi (accumulate unless first), x_hi.c_lo, x_lo.c_hi
+__device__ __forceinline__ void tc_mma3_tf32_elect(uint32_t d_tmem, uint32_t a_hi, uint32_t a_lo, uint64_t b_hi,
+                                                   uint64_t b_lo, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, q, e;\n\t"
+        "setp.ne.b32 p, %5, 0;\n\t"
+        "setp.eq.b32 q, %5, %5;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %6, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %4, %6, q;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %3, %6, q;\n\t}" ::"r"(d_tmem),
+        "r"(a_hi), "r"(a_lo), "l"(b_hi), "l"(b_lo), "r"(acc), "r"(kIdesc)
         : "memory");
 }
 __device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
@@ -293,9 +311,9 @@ __global__ void __cluster_dims__(kTCluster, 1, 1) __launch_bounds__(kTThreads, 1
 #pragma unroll
                 for (int ks = 0; ks < kTD / 8; ++ks) {
                     const uint64_t off = ((ks >> 2) * (kTN * 128) + (ks & 3) * 32) >> 4;
-                    tc_mma_tf32_elect(dt, tmem + ks * 8, dh0 + off, ks > 0 ? 1u : 0u);  // x_hi . c_hi
-                    tc_mma_tf32_elect(dt, tmem + ks * 8, dl0 + off, 1u);                // x_hi . c_lo
-                    tc_mma_tf32_elect(dt, tmem + kTD + ks * 8, dh0 + off, 1u);          // x_lo . c_hi
+                    // x_hi . c_hi, x_hi . c_lo, x_lo . c_hi
+                    tc_mma3_tf32_elect(dt, tmem + ks * 8, tmem + kTD + ks * 8, dh0 + off, dl0 + off,
+                                       ks > 0 ? 1u : 0u);
                 }
             }
             tc_commit_multicast_elect(&empty[s], cmask);  // stage consumed (in every CTA's view)
