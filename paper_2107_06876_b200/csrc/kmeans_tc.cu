@@ -41,22 +41,25 @@ namespace lcnb {
 namespace {
 
 constexpr int kTM = 128;        // points per CTA (UMMA_M, TMEM lanes)
-constexpr int kTN = 64;         // centroids per tile (UMMA_N)
+constexpr int kTN = 128;        // centroids per tile (UMMA_N)
 constexpr int kTD = 128;        // padded feature count (tf32 columns)
-constexpr int kTHalf = kTN * kTD * 4;   // bytes of one tile half (hi or lo): 32 KB
+constexpr int kTK = 64;         // features per ring stage (a tile is kTD / kTK stages)
+constexpr int kTKS = kTD / kTK;
+constexpr int kTHalf = kTN * kTK * 4;   // bytes of one stage half (hi or lo): 32 KB
 constexpr int kTStage = 2 * kTHalf;     // hi + lo
 constexpr int kTStages = 3;
 #ifndef LCN_TC_CLUSTER
 #define LCN_TC_CLUSTER 4
 #endif
 constexpr int kTCluster = LCN_TC_CLUSTER;  // CTAs sharing each centroid stage (multicast)
-constexpr int kTAcc = 4;                // accumulator buffers in TMEM (columns 256..511)
+constexpr int kTAcc = 2;                // accumulator buffers in TMEM (columns 256..511)
 constexpr int kTSlice = kTStage / kTCluster;
 constexpr int kTEpi = 8;              // epilogue warps: two per TMEM lane quadrant
 constexpr int kTThreads = 64 + 32 * kTEpi;
 
-// element (r, k) of a swizzled tile half: K-major, 128-byte swizzle atoms of
-// 8 rows x 32 tf32; K blocks of 32 features stacked (kTN rows each)
+// element (r, k) of a swizzled stage half (k < kTK): K-major, 128-byte
+// swizzle atoms of 8 rows x 32 tf32; K blocks of 32 features stacked (kTN
+// rows each)
 __host__ __device__ __forceinline__ uint32_t tile_offset(int r, int k) {
     const int kb = k >> 5, j = k & 31, chunk = j >> 2, w = j & 3;
     return static_cast<uint32_t>(kb * (kTN * 128) + r * 128 + ((chunk ^ (r & 7)) << 4) + w * 4);
@@ -74,15 +77,16 @@ __global__ void __launch_bounds__(128) tc_prep_kernel(const double* __restrict__
     __shared__ double r1[4], r2[4];
     const int c = blockIdx.x;  // centroid (padded to ntile * kTN)
     const int t = c / kTN, r = c % kTN;
-    unsigned char* hi = tiles + static_cast<size_t>(t) * kTStage;
-    unsigned char* lo = hi + kTHalf;
     double s1 = 0.0, s2 = 0.0;
     for (int kk = threadIdx.x; kk < kTD; kk += 128) {
+        // stage t * kTKS + kk / kTK holds features [kh kTK, (kh + 1) kTK) of tile t
+        unsigned char* hi = tiles + (static_cast<size_t>(t) * kTKS + kk / kTK) * kTStage;
+        unsigned char* lo = hi + kTHalf;
         const double v = (c < k && kk < d) ? C[static_cast<long long>(c) * d + kk] : 0.0;
         const float f = static_cast<float>(v);
         const float h = tf32_hi(f);
-        *reinterpret_cast<float*>(hi + tile_offset(r, kk)) = h;
-        *reinterpret_cast<float*>(lo + tile_offset(r, kk)) = f - h;  // exact
+        *reinterpret_cast<float*>(hi + tile_offset(r, kk % kTK)) = h;
+        *reinterpret_cast<float*>(lo + tile_offset(r, kk % kTK)) = f - h;  // exact
         s1 += static_cast<double>(f) * static_cast<double>(f);
         s2 += v * v;
     }
@@ -277,12 +281,12 @@ __global__ void __cluster_dims__(kTCluster, 1, 1) __launch_bounds__(kTThreads, 1
         // this CTA loads slice crank of each stage and multicasts it to the
         // cluster; its own barrier expects the whole stage (all slices)
         if (lane == 0) {
-            for (int t = 0; t < ntile; ++t) {
-                const int s = t % kTStages;
-                if (t >= kTStages) mbar_wait(&empty[s], ((t / kTStages) - 1) & 1);
+            for (int g = 0; g < ntile * kTKS; ++g) {  // stage g: tile g / kTKS, features (g % kTKS) kTK ..
+                const int s = g % kTStages;
+                if (g >= kTStages) mbar_wait(&empty[s], ((g / kTStages) - 1) & 1);
                 mbar_arrive_expect_tx(&full[s], kTStage);
                 bulk_g2s_multicast(ring + s * kTStage + crank * kTSlice,
-                                   tiles + static_cast<size_t>(t) * kTStage + crank * kTSlice, kTSlice, &full[s],
+                                   tiles + static_cast<size_t>(g) * kTStage + crank * kTSlice, kTSlice, &full[s],
                                    cmask);
             }
         }
@@ -293,31 +297,35 @@ __global__ void __cluster_dims__(kTCluster, 1, 1) __launch_bounds__(kTThreads, 1
         // descriptor plus compile-time 16-byte-unit offsets (the start
         // address field sits in the low bits and never carries inside the
         // ring).
+        int g = 0;  // ring stage counter
         for (int t = 0; t < ntile; ++t) {
-            const int s = t % kTStages, b = t % kTAcc;
-            mbar_wait(&full[s], (t / kTStages) & 1);
+            const int b = t % kTAcc;
             if (t >= kTAcc) mbar_wait(&tempty[b], ((t / kTAcc) - 1) & 1);
-            tc_fence_after();
             const uint32_t dt = tmem + 256 + b * kTN;
-            const uint64_t dh0 = umma_desc_sw128(smem_u32(ring + s * kTStage));
-            const uint64_t dl0 = dh0 + (kTHalf >> 4);
-            if (hh_only == 1) {
+            for (int kh = 0; kh < kTKS; ++kh, ++g) {
+                const int s = g % kTStages;
+                mbar_wait(&full[s], (g / kTStages) & 1);
+                tc_fence_after();
+                const uint64_t dh0 = umma_desc_sw128(smem_u32(ring + s * kTStage));
+                const uint64_t dl0 = dh0 + (kTHalf >> 4);
+                const uint32_t ah = tmem + kh * kTK, al = tmem + kTD + kh * kTK;
+                if (hh_only == 1) {
 #pragma unroll
-                for (int ks = 0; ks < kTD / 8; ++ks) {
-                    const uint64_t off = ((ks >> 2) * (kTN * 128) + (ks & 3) * 32) >> 4;
-                    tc_mma_tf32_elect(dt, tmem + ks * 8, dh0 + off, ks > 0 ? 1u : 0u);
-                }
-            } else {
+                    for (int ks = 0; ks < kTK / 8; ++ks) {
+                        const uint64_t off = ((ks >> 2) * (kTN * 128) + (ks & 3) * 32) >> 4;
+                        tc_mma_tf32_elect(dt, ah + ks * 8, dh0 + off, (kh | ks) ? 1u : 0u);
+                    }
+                } else {
 #pragma unroll
-                for (int ks = 0; ks < kTD / 8; ++ks) {
-                    const uint64_t off = ((ks >> 2) * (kTN * 128) + (ks & 3) * 32) >> 4;
-                    // x_hi . c_hi, x_hi . c_lo, x_lo . c_hi
-                    tc_mma3_tf32_elect(dt, tmem + ks * 8, tmem + kTD + ks * 8, dh0 + off, dl0 + off,
-                                       ks > 0 ? 1u : 0u);
+                    for (int ks = 0; ks < kTK / 8; ++ks) {
+                        const uint64_t off = ((ks >> 2) * (kTN * 128) + (ks & 3) * 32) >> 4;
+                        // x_hi . c_hi, x_hi . c_lo, x_lo . c_hi
+                        tc_mma3_tf32_elect(dt, ah + ks * 8, al + ks * 8, dh0 + off, dl0 + off, (kh | ks) ? 1u : 0u);
+                    }
                 }
+                tc_commit_multicast_elect(&empty[s], cmask);  // stage consumed (in every CTA's view)
             }
-            tc_commit_multicast_elect(&empty[s], cmask);  // stage consumed (in every CTA's view)
-            tc_commit_elect(&tfull[b]);                   // accumulator ready
+            tc_commit_elect(&tfull[b]);  // accumulator ready
         }
         __syncwarp();
     } else {
@@ -335,32 +343,43 @@ __global__ void __cluster_dims__(kTCluster, 1, 1) __launch_bounds__(kTThreads, 1
         for (int c = 0; c < kCh; ++c) v1[c] = v2[c] = kPosInf, i1[c] = 0;
         for (int t = 0; t < ntile; ++t) {
             const int b = t % kTAcc;
-            // |c|^2 of this half tile while the accumulator is still in flight
-            float4 nc[kHC / 4];
-            const float4* nc4 = reinterpret_cast<const float4*>(ncf + t * kTN + half * kHC);
+            const uint32_t tcol = tmem + (static_cast<uint32_t>(lane_base) << 16) + 256 + b * kTN + half * kHC;
+#pragma unroll 1
+            for (int ch = 0; ch < kHC / 32; ++ch) {
+                // |c|^2 of these 32 columns while the accumulator is in flight
+                float4 nc[8];
+                const float4* nc4 = reinterpret_cast<const float4*>(ncf + t * kTN + half * kHC + ch * 32);
 #pragma unroll
-            for (int j4 = 0; j4 < kHC / 4; ++j4) nc[j4] = __ldg(nc4 + j4);
-            mbar_wait(&tfull[b], (t / kTAcc) & 1);
-            tc_fence_after();
-            uint32_t r[kHC];
-            tc_ld32(tmem + (static_cast<uint32_t>(lane_base) << 16) + 256 + b * kTN + half * kHC, r);
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            tc_fence_before();
-            mbar_arrive(&tempty[b]);
-            if (dbg && blockIdx.x == 0 && t == 0)  // test hook: raw accumulators of tile 0
-                for (int j = 0; j < kHC; ++j) dbg[row * kTN + half * kHC + j] = __uint_as_float(r[j]);
-            const int base = t * kTN + half * kHC;
+                for (int j4 = 0; j4 < 8; ++j4) nc[j4] = __ldg(nc4 + j4);
+                if (ch == 0) {
+                    mbar_wait(&tfull[b], (t / kTAcc) & 1);
+                    tc_fence_after();
+                }
+                uint32_t r[32];
+                tc_ld32(tcol + ch * 32, r);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (ch == kHC / 32 - 1) {
+                    tc_fence_before();
+                    mbar_arrive(&tempty[b]);
+                }
+                if (dbg && blockIdx.x == 0 && t == 0)  // test hook: raw accumulators of centroids 0..63
+                    for (int j = 0; j < 32; ++j) {
+                        const int col = half * kHC + ch * 32 + j;
+                        if (col < 64) dbg[row * 64 + col] = __uint_as_float(r[j]);
+                    }
+                const int base = t * kTN + half * kHC + ch * 32;
 #pragma unroll
-            for (int j4 = 0; j4 < kHC / 4; ++j4) {
-                const float ncj[4] = {nc[j4].x, nc[j4].y, nc[j4].z, nc[j4].w};
+                for (int j4 = 0; j4 < 8; ++j4) {
+                    const float ncj[4] = {nc[j4].x, nc[j4].y, nc[j4].z, nc[j4].w};
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int j = 4 * j4 + u;
-                    const float v = fmaf(-2.0f, __uint_as_float(r[j]), ncj[u]);
-                    const bool lt1 = v < v1[u];
-                    v2[u] = fminf(v2[u], fmaxf(v1[u], v));
-                    i1[u] = lt1 ? base + j : i1[u];
-                    v1[u] = fminf(v1[u], v);
+                    for (int u = 0; u < 4; ++u) {
+                        const int j = 4 * j4 + u;
+                        const float v = fmaf(-2.0f, __uint_as_float(r[j]), ncj[u]);
+                        const bool lt1 = v < v1[u];
+                        v2[u] = fminf(v2[u], fmaxf(v1[u], v));
+                        i1[u] = lt1 ? base + j : i1[u];
+                        v1[u] = fminf(v1[u], v);
+                    }
                 }
             }
         }
@@ -444,7 +463,7 @@ bool assign_filter_tc(Ctx& ctx, const float* X, long long N, int d, const double
     if (d > kTD || d < 1) return false;
     cudaStream_t s = ctx.stream;
     const int ntile = static_cast<int>(ceil_div(k, kTN));
-    DevBuf<unsigned char> tiles(static_cast<size_t>(ntile) * kTStage);
+    DevBuf<unsigned char> tiles(static_cast<size_t>(ntile) * kTKS * kTStage);
     DevBuf<float> ncf(static_cast<size_t>(ntile) * kTN);
     DevBuf<unsigned long long> cmax(1);
     cmax.zero(s);
