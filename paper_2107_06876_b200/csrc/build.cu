@@ -451,7 +451,7 @@ void cross_polytope_buckets_device(Ctx& ctx, const double* X, long long N, int d
 // jobs, together with `extra` (the landmark k-means) when given.
 void lsh_bucket_ids(Ctx& ctx, const double* d_union, const float* d_union32, size_t n, size_t m, size_t d,
                     const LshParams& cfg, std::vector<DevBuf<uint32_t>>& ids, size_t& range,
-                    const std::function<void(Ctx&)>& extra, const ExtraSeeding* extra_seed) {
+                    const std::function<void(Ctx&)>& extra, const ExtraSeeding* extra_seed, bool early_extra) {
     const size_t N = n + m;
     const int bands = cfg.bands, rows = cfg.rows, buckets = cfg.buckets;
     if (bands < 1 || rows < 1) throw Status(2, "lsh: bands and rows_per_band must be >= 1");
@@ -473,10 +473,46 @@ void lsh_bucket_ids(Ctx& ctx, const double* d_union, const float* d_union32, siz
     // k-means scheme: every band function's k-means++ seeding (and the
     // landmark k-means', when given) runs as one batched step chain first;
     // the per-band jobs then run Lloyd from those seeds
+    // early_extra: the extra job (the landmark k-means, and the Nystrom
+    // factors when the caller adds them) starts now on its own thread and
+    // stream, concurrently with the bands' seeding chain and Lloyd jobs;
+    // its host-side LDL^T and its device work fill the seeding chain's gaps
+    struct ExtraThread {
+        std::thread th;
+        Ctx c;
+        std::exception_ptr err;
+        bool on = false;
+        ~ExtraThread() {
+            if (th.joinable()) th.join();
+            if (on) {
+                cublas_pool_give(c.device, c.cublas);
+                cudaStreamDestroy(c.stream);
+            }
+        }
+    } xt;
+    if (extra && early_extra) {
+        ctx.sync();  // inputs are ready on the caller's stream
+        xt.c = ctx;
+        xt.c.own_stream = nullptr;
+        xt.c.comm.reset();
+        xt.c.cublas = nullptr;
+        CUDA_OK(cudaStreamCreateWithFlags(&xt.c.stream, cudaStreamNonBlocking));
+        xt.on = true;
+        xt.th = std::thread([&] {
+            try {
+                CUDA_OK(cudaSetDevice(ctx.device));
+                alloc_stream() = xt.c.stream;
+                extra(xt.c);
+                CUDA_OK(cudaStreamSynchronize(xt.c.stream));
+            } catch (...) {
+                xt.err = std::current_exception();
+            }
+        });
+    }
     std::vector<DevBuf<uint32_t>> inits;
     const bool xseed = extra_seed && extra_seed->k > 0 && static_cast<size_t>(extra_seed->k) <= N && extra_seed->out;
     if (cfg.scheme == 1 || xseed) {
-        PhaseTimer pt(ctx, "k-means++ seeding (LSH bands + landmarks, batched)");
+        PhaseTimer pt(ctx, "k-means++ seeding (batched chain)");
         std::vector<PPSeq> seqs;
         if (cfg.scheme == 1) {
             inits.resize(static_cast<size_t>(bands) * rows);
@@ -553,8 +589,12 @@ void lsh_bucket_ids(Ctx& ctx, const double* d_union, const float* d_union32, siz
             jc.sync();
             ids[b] = std::move(out);
         });
-    if (extra) jobs.push_back(extra);
+    if (extra && !early_extra) jobs.push_back(extra);
     run_jobs(ctx, jobs);
+    if (xt.on) {
+        xt.th.join();
+        if (xt.err) std::rethrow_exception(xt.err);
+    }
     ctx.sync();
     for (double bb : band_bound) {
         if (bb + 1.0 > 4294967295.0) throw Status(2, "lsh: composite bucket range exceeds 2^32 on this path");

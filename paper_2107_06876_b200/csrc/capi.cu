@@ -972,17 +972,24 @@ int lcn_op_lcn_lsh(lcn_ctx* ctx, const double* p, size_t n, const double* q, siz
         // LSH k-means, measured slower: 1.32 s vs 1.28 s per build at
         // configs[3] -- the factor GEMMs and the host LDL^T contend with the
         // seeding chains)
+        // the landmark k-means and the Nystrom factors (they need no LSH
+        // ids) run on their own job from the start, beside the bands'
+        // seeding chain (LCN_EARLY_FACTORS=0: landmarks seeded with the
+        // bands in one batched chain, factors after the LSH)
+        const char* efenv = std::getenv("LCN_EARLY_FACTORS");
+        const bool early = !ctx->c.comm && !(efenv && efenv[0] == '0') && l >= 1 && l <= n + m;
         auto landmarks_job = [&](Ctx& jc) {
             select_landmarks_device(o, jc, landmark_method, landmark_seed);
             o.landmarks_ready = true;
+            if (early) build_nystrom(o, nullptr, landmark_method, landmark_seed, &jc);
         };
         ExtraSeeding es;
-        if (landmark_method == 0 && l >= 1 && l <= n + m) {  // k-means landmarks: seeded with the bands
+        if (!early && landmark_method == 0 && l >= 1 && l <= n + m) {  // k-means landmarks: seeded with the bands
             o.landmark_init.resize(l);
             es = ExtraSeeding{static_cast<int>(l), landmark_seed, o.landmark_init.get()};
         }
         lsh_bucket_ids(ctx->c, o.X.get(), o.X32.size() ? o.X32.get() : nullptr, n, m, d, lsh_params(cfg), ids, range,
-                              landmarks_job, &es);
+                              landmarks_job, &es, early);
         if (ctx->c.comm) shard_lcn(o, ids, range, nullptr, landmark_method, landmark_seed);
         else bands_from_union_ids(o, ids, range);
         finish_lcn(o, nullptr, l, landmark_method, landmark_seed);
@@ -1135,19 +1142,22 @@ int lcn_op_create_device(lcn_ctx* ctx, const float* d_p, size_t n, const float* 
         std::vector<DevBuf<uint32_t>> ids;
         size_t range = 0;
         op.l = l;
+        const char* efenv = std::getenv("LCN_EARLY_FACTORS");
+        const bool early = l && !ctx->c.comm && !(efenv && efenv[0] == '0') && l <= n + m;  // see lcn_op_lcn_lsh
         std::function<void(Ctx&)> landmarks_job;
         if (l)
             landmarks_job = [&](Ctx& jc) {
                 select_landmarks_device(op, jc, landmark_method, landmark_seed);
                 op.landmarks_ready = true;
+                if (early) build_nystrom(op, nullptr, landmark_method, landmark_seed, &jc);
             };
         ExtraSeeding es;
-        if (l && landmark_method == 0 && l <= n + m) {  // k-means landmarks: seeded with the bands
+        if (l && !early && landmark_method == 0 && l <= n + m) {  // k-means landmarks: seeded with the bands
             op.landmark_init.resize(l);
             es = ExtraSeeding{static_cast<int>(l), landmark_seed, op.landmark_init.get()};
         }
         lsh_bucket_ids(ctx->c, op.X.get(), op.X32.size() ? op.X32.get() : nullptr, n, m, d, lsh_params(cfg), ids, range,
-                              landmarks_job, &es);
+                              landmarks_job, &es, early);
         if (ctx->c.comm && l) shard_lcn(op, ids, range, nullptr, landmark_method, landmark_seed);
         else bands_from_union_ids(op, ids, range);
         if (l) finish_lcn(op, nullptr, l, landmark_method, landmark_seed);

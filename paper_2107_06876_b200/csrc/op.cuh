@@ -193,7 +193,8 @@ struct ExtraSeeding {
 };
 void lsh_bucket_ids(Ctx& ctx, const double* d_union, const float* d_union32, size_t n, size_t m, size_t d,
                     const LshParams& cfg, std::vector<DevBuf<uint32_t>>& ids, size_t& range,
-                    const std::function<void(Ctx&)>& extra = {}, const ExtraSeeding* extra_seed = nullptr);
+                    const std::function<void(Ctx&)>& extra = {}, const ExtraSeeding* extra_seed = nullptr,
+                    bool early_extra = false);
 void cross_polytope_buckets_device(Ctx& ctx, const double* X, long long N, int d, const double* h_proj, int half,
                                    uint32_t* out);
 bool nystrom_inverse_host(const double* A, int l, double rel, double* ainv, double* aj_out);
