@@ -1753,8 +1753,14 @@ void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed,
             // support): the GPU is otherwise idle during the LDL^T
             auto work = std::move(op.during_ldlt);
             op.during_ldlt = nullptr;
-            std::thread th(factor);
-            std::exception_ptr err;
+            std::exception_ptr err, ferr;
+            std::thread th([&] {
+                try {
+                    factor();
+                } catch (...) {
+                    ferr = std::current_exception();
+                }
+            });
             try {
                 work();
             } catch (...) {
@@ -1762,6 +1768,7 @@ void build_nystrom(Op& op, const double* h_landmarks, int method, uint64_t seed,
             }
             th.join();
             if (err) std::rethrow_exception(err);
+            if (ferr) std::rethrow_exception(ferr);
         } else {
             factor();
         }
