@@ -786,6 +786,8 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
                                                                       const double* __restrict__ logv,
                                                                       double* __restrict__ corr,
                                                                       double* __restrict__ Sout = nullptr) {
+    pdl_wait();  // launched with programmatic serialisation inside the LCN iteration
+    pdl_launch_dependents();
     if (st->done) return;
     extern __shared__ __align__(128) unsigned char dyn[];
     BandSmem& sm = *reinterpret_cast<BandSmem*>(dyn);
@@ -1215,6 +1217,8 @@ __device__ __forceinline__ void lds_cols(const T* p, double (&o)[CPT]) {
 
 template <typename T, int CPT, int SIDE>
 __global__ void __launch_bounds__(kThreads + 64, 2) lowrank_pass_kernel(const T* __restrict__ F, PassArgs a) {
+    pdl_wait();
+    pdl_launch_dependents();
     DevState* st = a.st;
     if (st->done) return;
     constexpr int S = PassStages<T>::kStages;
@@ -1583,6 +1587,8 @@ __global__ void __launch_bounds__(1024) lowrank_reduce_kernel(DevState* __restri
                                                               const double* __restrict__ mnp, int G, int lp,
                                                               double* __restrict__ mid, int which,
                                                               double* __restrict__ hloc) {
+    pdl_wait();
+    pdl_launch_dependents();
     if (st->done) return;
     constexpr int W = 32;  // warps
     __shared__ double sh[W], sm[W], acc_s[W][33];
@@ -1734,6 +1740,8 @@ __global__ void __launch_bounds__(256) iter_end_kernel(DevState* __restrict__ st
                                                        int G, int it, int max_iters, double tol,
                                                        double* __restrict__ trace,
                                                        const double* __restrict__ gstage) {
+    pdl_wait();
+    pdl_launch_dependents();
     if (st->done) return;
     __shared__ double red[8];
     double e = 0.0;
@@ -2287,10 +2295,11 @@ struct Solver {
     template <typename T, int SIDE>
     void pass(const PassArgs& a, long long row0 = 0) {
         const T* F = (SIDE == 0 ? U<T>() : Wt<T>()) + row0 * lp;
+        const dim3 g(G), b(kThreads + 64);
         switch (CPT) {
-            case 1: lowrank_pass_kernel<T, 1, SIDE><<<G, kThreads + 64, smem, s>>>(F, a); break;
-            case 2: lowrank_pass_kernel<T, 2, SIDE><<<G, kThreads + 64, smem, s>>>(F, a); break;
-            case 4: lowrank_pass_kernel<T, 4, SIDE><<<G, kThreads + 64, smem, s>>>(F, a); break;
+            case 1: launch_pdl(lowrank_pass_kernel<T, 1, SIDE>, g, b, smem, s, pdl(), F, a); break;
+            case 2: launch_pdl(lowrank_pass_kernel<T, 2, SIDE>, g, b, smem, s, pdl(), F, a); break;
+            case 4: launch_pdl(lowrank_pass_kernel<T, 4, SIDE>, g, b, smem, s, pdl(), F, a); break;
         }
     }
     PassArgs base_args() {
@@ -2306,8 +2315,19 @@ struct Solver {
         return a;
     }
     void reduce(double* mid, int which) {
-        lowrank_reduce_kernel<<<ceil_div(lp, 32), 1024, 0, s>>>(st.get(), part.get(), hpart.get(), mnp.get(), G, lp,
-                                                                mid, which, nullptr);
+        launch_pdl(lowrank_reduce_kernel, dim3(ceil_div(lp, 32)), dim3(1024), 0, s, pdl(), st.get(), part.get(),
+                   hpart.get(), mnp.get(), G, lp, mid, which, static_cast<double*>(nullptr));
+    }
+    // programmatic dependent launches between the iteration's kernels (each
+    // waits for its predecessor at its top; the launch itself and the CTA
+    // ramp overlap the predecessor's tail). Off while phase events are
+    // recorded between launches (ctx.profile) and with LCN_ITER_PDL=0.
+    bool pdl() const {
+        static const bool off = [] {
+            const char* e = std::getenv("LCN_ITER_PDL");
+            return e && e[0] == '0';
+        }();
+        return !ctx.profile && !off;
     }
 
     const int* done_ptr() const {
@@ -2441,9 +2461,10 @@ struct Solver {
         for (size_t b = 0; b < op.bands.size(); ++b) {
             PassPlan& P = plans[ROWS ? 0 : 1][b];
             if (P.nitems)
-                band_stream_kernel<T, ROWS><<<band_grid, kThreads + 64, sizeof(BandSmem), s>>>(
-                    st.get(), ROWS ? op.iter[b].so : op.iter[b].to, P.work(),
-                    ROWS ? band_valsT<T>(b) : band_vals<T>(b), logvp[b].get(), corr[b].get());
+                launch_pdl(band_stream_kernel<T, ROWS, false>, dim3(band_grid), dim3(kThreads + 64), sizeof(BandSmem), s,
+                           pdl(), st.get(), ROWS ? op.iter[b].so : op.iter[b].to, P.work(),
+                           ROWS ? band_valsT<T>(b) : band_vals<T>(b), logvp[b].get(), corr[b].get(),
+                           static_cast<double*>(nullptr));
         }
     }
     template <typename T>
@@ -2535,7 +2556,8 @@ struct Solver {
         set_perm(a, 0, nxt);
         pass<T, 0>(a);
         reduce(mid_s.get(), 1);
-        iter_end_kernel<<<1, 256, 0, s>>>(st.get(), err_part.get(), G, it, max_iters, tol, trace.get(), nullptr);
+        launch_pdl(iter_end_kernel, dim3(1), dim3(256), 0, s, pdl(), st.get(), err_part.get(), G, it, max_iters, tol,
+                   trace.get(), static_cast<const double*>(nullptr));
         mark(it, 4);
     }
 
