@@ -61,7 +61,7 @@ def test_kmeans_pp_large_walk(ctx, ref, kind):
 @pytest.mark.parametrize("mode", [{}, {"LCN_PP_EXACT_WALK": "1"}, {"LCN_PP_CERT_SLACK": "20000"},
                                   {"LCN_PP_CERT_SLACK": "1e9"}])
 def test_kmeans_pp_certified_pick(ctx, ref, monkeypatch, mode):
-    # the certified pick (pp_fast_pick_kernel) and the exact fold + walk give
+    # the certified pick (pp_pick_kernel) and the exact fold + walk give
     # the same indices: default (almost every step certified), exact walk
     # only, a widened certificate (about half the steps fall back, so the two
     # paths alternate) and one so wide that every step falls back
@@ -226,6 +226,34 @@ def test_lcn_small_configs(ref, scale, which, exact):
     assert rel(res.distance, rres.distance) <= REL_FP32
     assert rel(res.sp_vals, rres.sp_vals) <= REL_FP32
     assert rel(lcn.distance_lcn(res, op), rres.distance_lcn()) <= REL_FP32
+
+
+@pytest.mark.parametrize("fp64", [False, True])
+def test_build_schedules_agree(monkeypatch, fp64):
+    # the build's scheduling choices change when work runs, never what it
+    # computes: landmarks + factors on an early job (default) or after the
+    # LSH with the landmarks seeded in the bands' batched chain; the device
+    # pool mapped up front or grown on demand -> bit-identical operators
+    pr = configs.config3(0.01)
+    cfg = lcn.LshConfig(pr.bands, 1, pr.buckets, pr.kmeans_iters, pr.lsh_seed)
+    pm, qm = pr.marginals()
+    out = []
+    for env in ({}, {"LCN_EARLY_FACTORS": "0", "LCN_POOL_RESERVE_GB": "8"}):
+        for k in ("LCN_EARLY_FACTORS", "LCN_POOL_RESERVE_GB"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        c = lcn.Context(0, store_fp64=fp64)
+        op = lcn.KernelOperator.lcn_lsh(c, pr.p, pr.q, pr.cost, pr.lam_eff, cfg, pr.landmarks, lcn.LANDMARK_KMEANS,
+                                        pr.landmark_seed)
+        res = lcn.sinkhorn(op, pm, qm, lcn.SinkhornOptions(tol=0.0, max_iters=20))
+        out.append((op.factor(1), op.factor(2), op.export_csr(1), res.distance))
+    (w0, l0, (rp0, c0, d0), x0), (w1, l1, (rp1, c1, d1), x1) = out
+    assert np.array_equal(l0.view(np.uint64), l1.view(np.uint64))
+    assert np.array_equal(w0.view(np.uint64), w1.view(np.uint64))
+    assert np.array_equal(rp0, rp1) and np.array_equal(c0, c1)
+    assert np.array_equal(d0.view(np.uint64), d1.view(np.uint64))
+    assert x0 == x1
 
 
 _LARGE_REF = {}
