@@ -590,7 +590,15 @@ void lsh_bucket_ids(Ctx& ctx, const double* d_union, const float* d_union32, siz
             ids[b] = std::move(out);
         });
     if (extra && !early_extra) jobs.push_back(extra);
-    run_jobs(ctx, jobs);
+    if (ctx.comm && ctx.comm->world > 1) {
+        // sharded build: the k-means assignments are split over the ranks
+        // (lloyd_device's all-gather), so the jobs run one after the other on
+        // this context, the communicator's calls in the same order on every rank
+        for (auto& j : jobs) j(ctx);
+        ctx.sync();
+    } else {
+        run_jobs(ctx, jobs);
+    }
     if (xt.on) {
         xt.th.join();
         if (xt.err) std::rethrow_exception(xt.err);

@@ -2513,25 +2513,52 @@ void lloyd_device(Ctx& ctx, const T* X, long long N, int d, int k, int iters, ui
     DevBuf<uint32_t> blist(bounds ? N : 1);
     DevBuf<unsigned> bcnt(1);
     long long reassigned = 0;
+    // Sharded build (a communicator on the context): rank r assigns the
+    // points [r S, (r + 1) S), S = ceil(N / world), and one all-gather gives
+    // every rank the whole assignment; the centroid update, the reseeding and
+    // the shifts then run identically on every rank. Every assignment is the
+    // exact argmin, so the result is bit-identical for any world size.
+    Comm* cm = ctx.comm && ctx.comm->world > 1 ? ctx.comm.get() : nullptr;
+    const long long S = cm ? ceil_div(N, cm->world) : N;
+    const long long lo = cm ? std::min(N, static_cast<long long>(cm->rank) * S) : 0;
+    const long long Nr = cm ? std::min(N, lo + S) - lo : N;
+    DevBuf<uint32_t> gsend(cm ? S : 1), grecv(cm ? S * cm->world : 1);
+    auto gather_assign = [&] {
+        if (!cm) return;
+        CUDA_OK(cudaMemsetAsync(gsend.get(), 0, static_cast<size_t>(S) * 4, s));
+        if (Nr)
+            CUDA_OK(cudaMemcpyAsync(gsend.get(), d_assign + lo, static_cast<size_t>(Nr) * 4, cudaMemcpyDeviceToDevice,
+                                    s));
+        cm->allgather(gsend.get(), grecv.get(), static_cast<size_t>(S) * 4, s);
+        CUDA_OK(cudaMemcpyAsync(d_assign, grecv.get(), static_cast<size_t>(N) * 4, cudaMemcpyDeviceToDevice, s));
+    };
+    const T* Xr = X + lo * d;
+    uint32_t* ar = d_assign + lo;
+    float* ubr = ub.get() + (bounds ? lo : 0);
+    float* lbr = lb.get() + (bounds ? lo : 0);
     auto assign_step = [&](bool first) {
         if (!bounds) {
-            assign_device<T>(ctx, X, N, d, d_ctr, k, d_assign);
+            if (Nr) assign_device<T>(ctx, Xr, Nr, d, d_ctr, k, ar);
+            gather_assign();
             return;
         }
         if (first) {
-            assign_bounded<T>(ctx, X, N, d, d_ctr, k, d_assign, nullptr, ub.get(), lb.get());
-            reassigned += N;
+            if (Nr) assign_bounded<T>(ctx, Xr, Nr, d, d_ctr, k, ar, nullptr, ubr, lbr);
+            reassigned += Nr;
+            gather_assign();
             return;
         }
         bcnt.zero(s);
-        lloyd_bounds_kernel<T><<<ceil_div(N, 256), 256, 0, s>>>(X, N, d, d_ctr, d_assign, ub.get(), lb.get(),
-                                                               delta.get(), dstat.get(), blist.get(), bcnt.get());
+        if (Nr)
+            lloyd_bounds_kernel<T><<<ceil_div(Nr, 256), 256, 0, s>>>(Xr, Nr, d, d_ctr, ar, ubr, lbr, delta.get(),
+                                                                    dstat.get(), blist.get(), bcnt.get());
         LAUNCH_OK("lloyd bounds");
         unsigned h = 0;
         bcnt.download(&h, 1, s);
         ctx.sync();
         reassigned += h;
-        if (h) assign_bounded<T>(ctx, X, h, d, d_ctr, k, d_assign, blist.get(), ub.get(), lb.get());
+        if (h) assign_bounded<T>(ctx, Xr, h, d, d_ctr, k, ar, blist.get(), ubr, lbr);
+        gather_assign();
     };
     for (int it = 0; it < iters; ++it) {
         assign_step(it == 0);
@@ -2564,8 +2591,9 @@ void lloyd_device(Ctx& ctx, const T* X, long long N, int d, int k, int iters, ui
     }
     assign_step(iters == 0);
     if (bounds && std::getenv("LCN_TIMING"))
-        std::fprintf(stderr, "[lloyd] N=%lld k=%d: %lld of %lld point assignments re-evaluated (%.1f%%)\n", N, k,
-                     reassigned, N * (iters + 1), 100.0 * reassigned / (static_cast<double>(N) * (iters + 1)));
+        std::fprintf(stderr, "[lloyd] N=%lld k=%d%s: %lld of %lld point assignments re-evaluated (%.1f%%)\n", N, k,
+                     cm ? " (this rank's slice)" : "", reassigned, Nr * (iters + 1),
+                     100.0 * reassigned / (static_cast<double>(std::max(Nr, 1LL)) * (iters + 1)));
 }
 
 #define LCNB_INST(T)                                                                                    \

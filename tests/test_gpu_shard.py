@@ -157,3 +157,42 @@ def test_sharded_solve_with_idle_ranks(world):
     single = lcn.sinkhorn(build(c0), pm, qm, opts)
     shards = _run_ranks(world, build, True, pm, qm, opts)
     _compare(single, shards, 1e-12, 1e-9)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_lloyd_bit_identical(world):
+    """Lloyd with the assignments split over the ranks (rank r assigns
+    points [r S, (r + 1) S), one all-gather per assignment): the tensor-core
+    filter with certified bounds on each slice, the centroid update on every
+    rank -- assignment and centroid bits equal to the single-rank Lloyd."""
+    r = np.random.default_rng(61)
+    means = r.standard_normal((150, 128))
+    x = (means[r.integers(0, 150, 200_001)] + 0.5 * r.standard_normal((200_001, 128))).astype(np.float32)
+    x = x.astype(np.float64)
+    c0 = lcn.Context(0)
+    ref_c, ref_a = lcn.lloyd(c0, x, 512, 10, 61)
+    c0.close()
+    group = lcn.LoopbackGroup(world)
+    out = [None] * world
+
+    def rank(rk):
+        try:
+            c = lcn.Context(0)
+            c.set_loopback(group, rk)
+            out[rk] = lcn.lloyd(c, x, 512, 10, 61)
+            c.close()
+        except Exception as e:  # noqa: BLE001 - surfaced below
+            group.abort()
+            out[rk] = e
+
+    th = [threading.Thread(target=rank, args=(q,)) for q in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    for o in out:
+        if isinstance(o, Exception):
+            raise o
+        cc, aa = o
+        assert np.array_equal(aa, ref_a)
+        assert np.array_equal(cc.view(np.uint64), ref_c.view(np.uint64))
