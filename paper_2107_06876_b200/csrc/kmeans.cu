@@ -234,10 +234,12 @@ __global__ void __launch_bounds__(128) pp_exact_kernel(const T* __restrict__ X, 
                                                        const uint32_t* __restrict__ list,
                                                        const unsigned* __restrict__ count,
                                                        double* __restrict__ csum, int cshift, PPB pb) {
-    pdl_wait();
-    pdl_launch_dependents();
-    const int y = blockIdx.y;
-    if (t + 1 >= pb.k[y]) return;
+    const int y = blockIdx.y;  // the center load below runs before the wait (see pp_filter_i8_kernel)
+    if (t + 1 >= pb.k[y]) {
+        pdl_wait();
+        pdl_launch_dependents();
+        return;
+    }
     chosen += y * pb.sK;
     dist2 += y * pb.sN;
     near += y * pb.sN;
@@ -252,6 +254,8 @@ __global__ void __launch_bounds__(128) pp_exact_kernel(const T* __restrict__ X, 
     const long long last = chosen[t];
     for (int k = threadIdx.x; k < d; k += blockDim.x) cs[k] = static_cast<double>(X[last * d + k]);
     __syncthreads();
+    pdl_wait();  // the filter's survivor list
+    pdl_launch_dependents();
     const unsigned cnt = *count;
     for (unsigned b0 = (blockIdx.x * nw + warp) * 32u; b0 < cnt; b0 += gridDim.x * nw * 32u) {
         const unsigned nb = cnt - b0 < 32u ? cnt - b0 : 32u;
@@ -552,10 +556,15 @@ __global__ void __launch_bounds__(128) pp_filter_i8_kernel(const T* __restrict__
                                                            const unsigned* __restrict__ count,
                                                            uint32_t* __restrict__ surv,
                                                            unsigned* __restrict__ surv_count, PPB pb) {
-    pdl_wait();
-    pdl_launch_dependents();
+    // the center's quantisation needs only chosen[t] (the previous step's
+    // pick, complete before the prune kernel passed its wait) and X: it runs
+    // before this grid waits for the prune kernel
     const int y = blockIdx.y;
-    if (t + 1 >= pb.k[y]) return;
+    if (t + 1 >= pb.k[y]) {
+        pdl_wait();
+        pdl_launch_dependents();
+        return;
+    }
     chosen += y * pb.sK;
     dist2 += y * pb.sN;
     list += y * pb.sN;
@@ -619,6 +628,8 @@ __global__ void __launch_bounds__(128) pp_filter_i8_kernel(const T* __restrict__
         qlo[q] = qin[q] ? (static_cast<unsigned short>(qc[k]) | (static_cast<int>(qc[k + 1]) << 16)) : 0;
         qhi[q] = qin[q] ? (static_cast<unsigned short>(qc[k + 2]) | (static_cast<int>(qc[k + 3]) << 16)) : 0;
     }
+    pdl_wait();  // the prune kernel's candidate list
+    pdl_launch_dependents();
     const unsigned cnt = *count;
     const unsigned stride = gridDim.x * nw * 32u;
     unsigned b0 = (blockIdx.x * nw + warp) * 32u;
