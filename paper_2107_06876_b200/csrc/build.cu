@@ -2398,9 +2398,9 @@ __global__ void csr_fill_kernel(BandViews bvs, BandSet bs, long long n, const ui
 
 }  // namespace
 
-void build_csr(Op& op) {
+void build_csr(Op& op, Ctx* on) {
     if (op.csr_ready) return;
-    Ctx& ctx = *op.ctx;
+    Ctx& ctx = on ? *on : *op.ctx;
     PhaseTimer pt(ctx, "CSR support export");
     cudaStream_t s = ctx.stream;
     const long long n = op.n;

@@ -11,6 +11,7 @@
 #include <string>
 
 #include <cublas_v2.h>
+#include <thread>
 #include <nccl.h>
 
 #include "../../include/lcn_b200.h"
@@ -403,8 +404,38 @@ void finish_lcn(Op& op, const double* landmarks, size_t l, int method, uint64_t 
     build_nystrom(op, landmarks, method, seed);
     op.during_ldlt = nullptr;
     if (op.kind == LCN_OP_LCN) {
-        build_correction(op);
-        build_csr(op);
+        if (!op.csr_ready && !op.ctx->comm) {
+            // the CSR support needs only the bands: a host thread builds it on
+            // its own stream while this one runs the correction (K_sp, delta)
+            Ctx side = *op.ctx;
+            side.own_stream = nullptr;
+            side.comm.reset();
+            side.cublas = nullptr;
+            CUDA_OK(cudaStreamCreateWithFlags(&side.stream, cudaStreamNonBlocking));
+            std::exception_ptr cerr, serr;
+            std::thread th([&] {
+                try {
+                    CUDA_OK(cudaSetDevice(side.device));
+                    alloc_stream() = side.stream;
+                    build_csr(op, &side);
+                    side.sync();
+                } catch (...) {
+                    serr = std::current_exception();
+                }
+            });
+            try {
+                build_correction(op);
+            } catch (...) {
+                cerr = std::current_exception();
+            }
+            th.join();
+            cudaStreamDestroy(side.stream);
+            if (cerr) std::rethrow_exception(cerr);
+            if (serr) std::rethrow_exception(serr);
+        } else {
+            build_correction(op);
+            build_csr(op);
+        }
     }
     finalize_storage(op);
 }

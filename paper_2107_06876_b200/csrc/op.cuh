@@ -216,7 +216,7 @@ void build_dense_cost(Op& op);
 void dense_logk_from_cost(Op& op, double lambda);
 void build_correction(Op& op);
 void finalize_storage(Op& op);
-void build_csr(Op& op);
+void build_csr(Op& op, Ctx* on = nullptr);  // on: a side context (stream) to build on
 void export_csr(Op& op, int which, uint32_t* row_ptr, uint32_t* col, double* vals);
 void csr_values_device(Op& op, int which, double* d_vals);
 // staged build from host structs (the reference's stage API)
