@@ -1905,6 +1905,13 @@ void kmeans_pp_device(Ctx& ctx, const T* X, long long N, int d, int k, uint64_t 
 }
 
 // ---- Lloyd (kmeans.cpp:87-143) ---------------------------------------------
+__global__ void count_changes_kernel(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, long long N,
+                                     unsigned long long* __restrict__ changes) {
+    unsigned long long c = 0;
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < N; i += 256LL * gridDim.x) c += a[i] != b[i];
+    c = warp_sum(c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(changes, c);
+}
 __global__ void count_kernel(const uint32_t* __restrict__ assign, long long N, int* __restrict__ counts) {
     long long i = blockIdx.x * 256LL + threadIdx.x;
     if (i < N) atomicAdd(&counts[assign[i]], 1);
@@ -2571,8 +2578,35 @@ void lloyd_device(Ctx& ctx, const T* X, long long N, int d, int k, int iters, ui
         if (h) assign_bounded<T>(ctx, Xr, h, d, d_ctr, k, ar, blist.get(), ubr, lbr);
         gather_assign();
     };
+    // Fixed point: when an assignment equals the previous one and the update
+    // before it reseeded nothing, that update's centroids come back
+    // bit-identical (same members, same fold order), so every later
+    // iteration and the final assignment repeat this assignment: stop here
+    // (the reference keeps iterating to the same result). LCN_LLOYD_EARLY_EXIT=0
+    // runs every iteration.
+    const char* eenv = std::getenv("LCN_LLOYD_EARLY_EXIT");
+    const bool early_exit = !(eenv && eenv[0] == '0');
+    DevBuf<uint32_t> prev(early_exit ? N : 1);
+    DevBuf<unsigned long long> nchg(1);
+    bool reseeded_prev = true;  // iteration 0 has no previous assignment
+    int exit_it = -1;
     for (int it = 0; it < iters; ++it) {
         assign_step(it == 0);
+        if (early_exit) {
+            if (!reseeded_prev) {
+                nchg.zero(s);
+                count_changes_kernel<<<static_cast<unsigned>(std::min<long long>(ceil_div(N, 256), 4LL * ctx.num_sms)),
+                                       256, 0, s>>>(d_assign, prev.get(), N, nchg.get());
+                unsigned long long hc = 1;
+                nchg.download(&hc, 1, s);
+                ctx.sync();
+                if (hc == 0) {
+                    exit_it = it;
+                    break;
+                }
+            }
+            CUDA_OK(cudaMemcpyAsync(prev.get(), d_assign, static_cast<size_t>(N) * 4, cudaMemcpyDeviceToDevice, s));
+        }
         if (bounds)
             CUDA_OK(cudaMemcpyAsync(cold.get(), d_ctr, static_cast<size_t>(k) * d * sizeof(double),
                                     cudaMemcpyDeviceToDevice, s));
@@ -2587,8 +2621,10 @@ void lloyd_device(Ctx& ctx, const T* X, long long N, int d, int k, int iters, ui
         LAUNCH_OK("lloyd update");
         counts.download(h_counts.data(), k, s);
         ctx.sync();
+        reseeded_prev = false;
         for (int c = 0; c < k; ++c) {
             if (h_counts[c] != 0) continue;
+            reseeded_prev = true;
             farthest_partial_kernel<T><<<fparts, 256, 0, s>>>(X, N, d, d_ctr, d_assign, counts.get(), pval.get(), pidx.get());
             reseed_apply_kernel<T><<<1, 128, 0, s>>>(X, d, pval.get(), pidx.get(), fparts, d_ctr, d_assign, counts.get(), c,
                                                      bounds ? lb.get() : nullptr);
@@ -2600,7 +2636,10 @@ void lloyd_device(Ctx& ctx, const T* X, long long N, int d, int k, int iters, ui
             LAUNCH_OK("centroid shifts");
         }
     }
-    assign_step(iters == 0);
+    if (exit_it < 0) assign_step(iters == 0);
+    if (exit_it >= 0 && std::getenv("LCN_TIMING"))
+        std::fprintf(stderr, "[lloyd] N=%lld k=%d: fixed point at iteration %d of %d (the rest skipped)\n", N, k,
+                     exit_it, iters);
     if (bounds && std::getenv("LCN_TIMING"))
         std::fprintf(stderr, "[lloyd] N=%lld k=%d%s: %lld of %lld point assignments re-evaluated (%.1f%%)\n", N, k,
                      cm ? " (this rank's slice)" : "", reassigned, Nr * (iters + 1),

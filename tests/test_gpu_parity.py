@@ -598,3 +598,16 @@ def test_band_claim_order_does_not_change_results(monkeypatch):
         out.append((res.distance, res.log_s.copy()))
     assert out[0][0] == out[1][0]
     assert np.array_equal(out[0][1].view(np.uint64), out[1][1].view(np.uint64))
+
+
+@pytest.mark.parametrize("exit_", ["1", "0"])
+def test_lloyd_fixed_point_exit(ctx, ref, monkeypatch, exit_):
+    # well-separated clusters: Lloyd reaches its fixed point within a few
+    # iterations; stopping there (default) or running all 10 gives the
+    # reference's assignment and centroid bits
+    monkeypatch.setenv("LCN_LLOYD_EARLY_EXIT", exit_)
+    x = rng_points(51, 30000, 16, comps=24, spread=40.0)
+    c_gpu, a_gpu = lcn.lloyd(ctx, x, 24, 10, 51)
+    c_ref, a_ref = ref.lloyd(x, 24, 10, 51)
+    assert np.array_equal(a_gpu, a_ref)
+    assert np.array_equal(c_gpu.view(np.uint64), c_ref.view(np.uint64))
