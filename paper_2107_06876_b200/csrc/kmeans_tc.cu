@@ -43,11 +43,14 @@ namespace {
 constexpr int kTM = 128;        // points per CTA (UMMA_M, TMEM lanes)
 constexpr int kTN = 128;        // centroids per tile (UMMA_N)
 constexpr int kTD = 128;        // padded feature count (tf32 columns)
-constexpr int kTK = 64;         // features per ring stage (a tile is kTD / kTK stages)
+#ifndef LCN_TC_KSTAGE
+#define LCN_TC_KSTAGE 32
+#endif
+constexpr int kTK = LCN_TC_KSTAGE;  // features per ring stage (a tile is kTD / kTK stages)
 constexpr int kTKS = kTD / kTK;
 constexpr int kTHalf = kTN * kTK * 4;   // bytes of one stage half (hi or lo): 32 KB
 constexpr int kTStage = 2 * kTHalf;     // hi + lo
-constexpr int kTStages = 3;
+constexpr int kTStages = (3 * 64) / kTK;  // 192 KB of ring
 #ifndef LCN_TC_CLUSTER
 #define LCN_TC_CLUSTER 4
 #endif
