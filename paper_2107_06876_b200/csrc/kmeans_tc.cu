@@ -12,11 +12,13 @@
 // best centroid; every other point goes to the exact fp64 scan, so the result
 // is bit-identical to kmeans.cpp:67-85.
 //
-// CTA (320 threads, 1 per SM), clusters of 4 CTAs:
+// CTA (320 threads, 1 per SM), clusters of 2 CTAs (LCN_TC_CLUSTER; 4 measured
+// 9 % slower: the stage ring advances at the pace of the cluster's slowest CTA):
 //   warp 0  producer: 1-D bulk copies (TMA) of pre-swizzled centroid tiles
-//           (hi + lo, 64 KB per stage, 3 stages); each CTA of the cluster
-//           loads a quarter of every stage and multicasts it to all four, so
-//           L2 serves each stage once per cluster
+//           (128 centroids; a stage holds 32 features of their hi + lo
+//           halves, 32 KB, six stages); each CTA of the cluster loads its
+//           share of every stage and multicasts it to the cluster, so L2
+//           serves each stage once per cluster
 //   warp 1  owns the TMEM allocation; the converged warp runs the issue loop
 //           and one elected lane issues tcgen05.mma.kind::tf32 (A = points
 //           from TMEM, B = centroids from shared memory via UMMA descriptors
@@ -27,9 +29,9 @@
 //           half of the 64 columns of a tile); tcgen05.ld of 32 accumulators,
 //           four interleaved branch-free top-2 trackers, merged per row at
 //           the end
-// Measured (2M points x 4096 centroids, d = 128): tensor pipe ~53% active,
-// i.e. ~53% of the FP32-accurate (3xTF32) peak.
-// TMEM columns: [0,128) x_hi, [128,256) x_lo, [256,512) four 64-column D buffers.
+// Measured (2M points x 4096 centroids, d = 128): 7.96 ms, tensor pipe 73 %
+// active (64-centroid tiles with clusters of 4: 10.7 ms / 53 %).
+// TMEM columns: [0,128) x_hi, [128,256) x_lo, [256,512) two 128-column D buffers.
 #include <cstdint>
 
 #include "async.cuh"
@@ -52,7 +54,7 @@ constexpr int kTHalf = kTN * kTK * 4;   // bytes of one stage half (hi or lo): 3
 constexpr int kTStage = 2 * kTHalf;     // hi + lo
 constexpr int kTStages = (3 * 64) / kTK;  // 192 KB of ring
 #ifndef LCN_TC_CLUSTER
-#define LCN_TC_CLUSTER 4
+#define LCN_TC_CLUSTER 2
 #endif
 constexpr int kTCluster = LCN_TC_CLUSTER;  // CTAs sharing each centroid stage (multicast)
 constexpr int kTAcc = 2;                // accumulator buffers in TMEM (columns 256..511)
