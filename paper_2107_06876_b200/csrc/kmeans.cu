@@ -57,7 +57,8 @@ __global__ void __launch_bounds__(256) assign_exact_kernel(const T* __restrict__
                                                            uint32_t* __restrict__ out, double* __restrict__ best_out,
                                                            const uint32_t* __restrict__ rows,
                                                            float* __restrict__ ub = nullptr,
-                                                           float* __restrict__ lb = nullptr) {
+                                                           float* __restrict__ lb = nullptr,
+                                                           double* __restrict__ part = nullptr, int cper = 0) {
     __shared__ double As[KC][TP + 1];
     __shared__ double Bs[KC][TC + 1];
     const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
@@ -66,7 +67,11 @@ __global__ void __launch_bounds__(256) assign_exact_kernel(const T* __restrict__
     int arg[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) { best[i] = sec[i] = kPosInf; arg[i] = 0; }
-    for (int c0 = 0; c0 < k; c0 += TC) {
+    // part: this CTA scans the centroids [y cper, (y + 1) cper) only and
+    // writes (best, second, index) for assign_exact_merge_kernel
+    const int cb = part ? static_cast<int>(blockIdx.y) * cper : 0;
+    const int ce = part ? min(k, cb + cper) : k;
+    for (int c0 = cb; c0 < ce; c0 += TC) {
         double acc[4][4];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
@@ -82,7 +87,7 @@ __global__ void __launch_bounds__(256) assign_exact_kernel(const T* __restrict__
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             int c = c0 + tx + 16 * j;
-            if (c < k)
+            if (c < ce)
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     if (acc[i][j] < best[i]) { sec[i] = best[i]; best[i] = acc[i][j]; arg[i] = c; }
@@ -105,6 +110,15 @@ __global__ void __launch_bounds__(256) assign_exact_kernel(const T* __restrict__
             if (ob < b || (ob == b && oa < a)) { b = ob; a = oa; }
         }
         long long p = p0 + ty + 16 * i;
+        if (part) {
+            if (tx == 0 && p < N) {
+                double* pr = part + (static_cast<long long>(blockIdx.y) * N + p) * 3;
+                pr[0] = b;
+                pr[1] = s2;
+                pr[2] = static_cast<double>(a);
+            }
+            continue;
+        }
         if (tx == 0 && p < N) {
             const long long q = rows ? rows[p] : p;
             out[q] = static_cast<uint32_t>(a);
@@ -115,6 +129,58 @@ __global__ void __launch_bounds__(256) assign_exact_kernel(const T* __restrict__
             }
         }
     }
+}
+
+// Merge of the centroid groups of assign_exact_kernel: groups in increasing
+// centroid order, (value, index) lexicographic minimum (the lowest index on
+// ties, as the sequential scan), the second smallest value alongside.
+__global__ void assign_exact_merge_kernel(const double* __restrict__ part, int groups, long long N,
+                                          const uint32_t* __restrict__ rows, uint32_t* __restrict__ out,
+                                          double* __restrict__ best_out, float* __restrict__ ub,
+                                          float* __restrict__ lb) {
+    const long long p = blockIdx.x * 256LL + threadIdx.x;
+    if (p >= N) return;
+    double b = kPosInf, s2 = kPosInf;
+    int a = 0;
+    for (int g = 0; g < groups; ++g) {
+        const double* pr = part + (static_cast<long long>(g) * N + p) * 3;
+        const double ob = pr[0], os = pr[1];
+        const int oa = static_cast<int>(pr[2]);
+        s2 = fmin(fmin(s2, os), fmax(b, ob));
+        if (ob < b || (ob == b && oa < a)) { b = ob; a = oa; }
+    }
+    const long long q = rows ? rows[p] : p;
+    out[q] = static_cast<uint32_t>(a);
+    if (best_out) best_out[q] = b;
+    if (ub) {
+        ub[q] = __double2float_ru(__dsqrt_ru(b * (1.0 + 1e-12)));
+        lb[q] = __double2float_rd(__dsqrt_rd(s2 * (1.0 - 1e-12)));
+    }
+}
+
+// Exact scan of n listed points (rows) or of all points: point tiles x
+// centroid groups so a short ambiguous list still fills the GPU.
+template <typename T>
+void assign_exact_launch(Ctx& ctx, const T* X, long long n, int d, const double* C, int k, uint32_t* out,
+                         double* best_out, const uint32_t* rows, float* ub, float* lb) {
+    if (n <= 0) return;
+    cudaStream_t s = ctx.stream;
+    const long long ptiles = ceil_div(n, TP);
+    const int ctiles = static_cast<int>(ceil_div(k, TC));
+    const int want = static_cast<int>(std::min<long long>(ctiles, ceil_div(4LL * ctx.num_sms, ptiles)));
+    if (want <= 1) {
+        assign_exact_kernel<T><<<static_cast<unsigned>(ptiles), 256, 0, s>>>(X, n, d, C, k, out, best_out, rows, ub, lb);
+        LAUNCH_OK("assign_exact_kernel");
+        return;
+    }
+    const int cper = static_cast<int>(ceil_div(ctiles, want)) * TC;
+    const int groups = static_cast<int>(ceil_div(k, cper));
+    DevBuf<double> part(static_cast<size_t>(groups) * n * 3);
+    assign_exact_kernel<T><<<dim3(static_cast<unsigned>(ptiles), groups), 256, 0, s>>>(
+        X, n, d, C, k, out, best_out, rows, ub, lb, part.get(), cper);
+    assign_exact_merge_kernel<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, s>>>(part.get(), groups, n, rows, out,
+                                                                                     best_out, ub, lb);
+    LAUNCH_OK("assign_exact_kernel (centroid groups)");
 }
 
 // ---- k-means++ (kmeans.cpp:23-65) ------------------------------------------
@@ -2274,8 +2340,7 @@ void assign_device(Ctx& ctx, const T* X, long long N, int d, const double* C, in
         ctx.filter_ambiguous += h_amb;
         ctx.filter_points += N;
         if (h_amb)
-            assign_exact_kernel<T><<<ceil_div(static_cast<long long>(h_amb), TP), 256, 0, s>>>(X, h_amb, d, C, k, out,
-                                                                                                nullptr, amb.get());
+            assign_exact_launch<T>(ctx, X, h_amb, d, C, k, out, nullptr, amb.get(), nullptr, nullptr);
         LAUNCH_OK("assign_exact_kernel (ambiguous, gemm filter)");
         return;
     }
@@ -2312,12 +2377,11 @@ void assign_device(Ctx& ctx, const T* X, long long N, int d, const double* C, in
         ctx.filter_ambiguous += h_amb;
         ctx.filter_points += N;
         if (h_amb)
-            assign_exact_kernel<T><<<ceil_div(static_cast<long long>(h_amb), TP), 256, 0, s>>>(X, h_amb, d, C, k, out,
-                                                                                                nullptr, amb.get());
+            assign_exact_launch<T>(ctx, X, h_amb, d, C, k, out, nullptr, amb.get(), nullptr, nullptr);
         LAUNCH_OK("assign_exact_kernel (ambiguous)");
         return;
     }
-    assign_exact_kernel<T><<<ceil_div(N, TP), 256, 0, s>>>(X, N, d, C, k, out, nullptr, nullptr);
+    assign_exact_launch<T>(ctx, X, N, d, C, k, out, nullptr, nullptr, nullptr, nullptr);
     LAUNCH_OK("assign_exact_kernel");
 }
 
@@ -2462,8 +2526,7 @@ void assign_bounded(Ctx& ctx, const T* X, long long n, int d, const double* C, i
     ctx.filter_ambiguous += h_amb;
     ctx.filter_points += n;
     if (h_amb)
-        assign_exact_kernel<T><<<ceil_div(static_cast<long long>(h_amb), TP), 256, 0, s>>>(X, h_amb, d, C, k, out,
-                                                                                            nullptr, amb.get(), ub, lb);
+        assign_exact_launch<T>(ctx, X, h_amb, d, C, k, out, nullptr, amb.get(), ub, lb);
     LAUNCH_OK("assign_exact_kernel (ambiguous, bounds)");
 }
 
