@@ -2508,17 +2508,90 @@ __global__ void __launch_bounds__(256) lloyd_bounds_kernel(const T* __restrict__
     }
 }
 
+// ---- Lloyd tile skipping (Elkan / Yinyang bounds per centroid tile) ---------
+// Every full evaluation leaves, per point and tile of 128 centroids, a lower
+// bound on the true distance to all of the tile's centroids (lbt, written
+// by assign_filter_tc_kernel). After an update moving tile g's centroids by
+// at most S_g, lbt - S_g still bounds them; a tile whose bound exceeds the
+// point's upper bound ub + delta_a (its distance to its own centroid) holds
+// no centroid that could be nearer (strictly, with margins), so it need not
+// be evaluated. Points are taken in Lloyd's sorted order (grouped by
+// centroid), and a cluster of 256 of them evaluates the union of their
+// needed tiles: mostly the tiles of their own mixture component. The own
+// tile always qualifies (its bound <= the distance to the own centroid), so
+// the argmin over the evaluated tiles is the global one; ambiguous points
+// still get the exact full scan.
+__global__ void tile_shift_kernel(const double* __restrict__ delta, int k, int tn, double* __restrict__ tshift) {
+    const int g = blockIdx.x, lane = threadIdx.x;
+    double m = 0.0;
+    for (int c = g * tn + lane; c < min(k, (g + 1) * tn); c += 32) m = fmax(m, delta[c]);
+    m = warp_max(m);
+    if (lane == 0) tshift[g] = m;
+}
+
+__global__ void __launch_bounds__(256) tile_need_kernel(const uint32_t* __restrict__ order, long long N,
+                                                        const uint32_t* __restrict__ assign,
+                                                        const float* __restrict__ ub,
+                                                        const double* __restrict__ delta,
+                                                        const double* __restrict__ tshift, int ntile,
+                                                        float* __restrict__ lbt,
+                                                        unsigned long long* __restrict__ masks) {
+    __shared__ unsigned long long wm[8];
+    const long long p = blockIdx.x * 256LL + threadIdx.x;
+    unsigned long long m = 0;
+    if (p < N) {
+        const long long q = order[p];
+        const double U = (static_cast<double>(ub[q]) + delta[assign[q]]) * (1.0 + 1e-9);
+        float* L = lbt + q * ntile * 2;
+        for (int g = 0; g < ntile; ++g) {
+            const double l = static_cast<double>(fminf(L[2 * g], L[2 * g + 1])) - tshift[g];
+            const float lf = __double2float_rd(l * (1.0 - 1e-9));
+            L[2 * g] = lf;
+            L[2 * g + 1] = lf;
+            if (!(static_cast<double>(lf) > U)) m |= 1ull << g;
+        }
+    }
+    // OR over the block (the cluster's 256 points)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m |= __shfl_xor_sync(0xffffffffu, m, o);
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long all = 0;
+        for (int w = 0; w < 8; ++w) all |= wm[w];
+        masks[blockIdx.x] = all;
+    }
+}
+
+__global__ void tile_count_kernel(const unsigned long long* __restrict__ masks, int ncl, int* __restrict__ cnt) {
+    const int c = blockIdx.x * 256 + threadIdx.x;
+    if (c < ncl) cnt[c] = __popcll(masks[c]);
+}
+
+__global__ void tile_fill_kernel(const unsigned long long* __restrict__ masks, int ncl, const int* __restrict__ off,
+                                 int* __restrict__ tl) {
+    const int c = blockIdx.x * 256 + threadIdx.x;
+    if (c >= ncl) return;
+    unsigned long long m = masks[c];
+    int o = off[c];
+    while (m) {
+        tl[o++] = __ffsll(static_cast<long long>(m)) - 1;
+        m &= m - 1;
+    }
+}
+
 // Tensor-core assignment of the points rows[0 .. n) (all points when rows is
 // null) with bounds; ambiguous points get the exact scan (and exact bounds).
 template <typename T>
 void assign_bounded(Ctx& ctx, const T* X, long long n, int d, const double* C, int k, uint32_t* out,
-                    const uint32_t* rows, float* ub, float* lb) {
+                    const uint32_t* rows, float* ub, float* lb, const int* tl_off = nullptr, const int* tl = nullptr,
+                    float* lbt = nullptr) {
     cudaStream_t s = ctx.stream;
     DevBuf<uint32_t> amb(n);
     DevBuf<unsigned> namb(1);
     namb.zero(s);
     if (!assign_filter_tc(ctx, reinterpret_cast<const float*>(X), n, d, C, k, out, amb.get(), namb.get(), nullptr, 0,
-                          rows, ub, lb))
+                          rows, ub, lb, tl_off, tl, lbt))
         throw Status(100, "lloyd bounds: tensor-core filter unavailable for this shape");
     unsigned h_amb = 0;
     namb.download(&h_amb, 1, s);
@@ -2613,11 +2686,53 @@ void lloyd_device(Ctx& ctx, const T* X, long long N, int d, int k, int iters, ui
         cm->allgather(gsend.get(), grecv.get(), static_cast<size_t>(S) * 4, s);
         CUDA_OK(cudaMemcpyAsync(d_assign, grecv.get(), static_cast<size_t>(N) * 4, cudaMemcpyDeviceToDevice, s));
     };
+    // tile skipping (bounds path, one rank, 8..64 tiles of 128 centroids;
+    // LCN_LLOYD_TILES=0: every tile every time)
+    const int ntile_c = assign_tc_tile_count(k);
+    const char* tenv = std::getenv("LCN_LLOYD_TILES");
+    const bool tiles = bounds && !cm && ntile_c >= 8 && ntile_c <= 64 && !(tenv && tenv[0] == '0');
+    const int ncl = static_cast<int>(ceil_div(N, 256));
+    DevBuf<float> lbt(tiles ? static_cast<size_t>(N) * ntile_c * 2 : 1);
+    DevBuf<double> tshift(tiles ? ntile_c : 1);
+    DevBuf<unsigned long long> tmask(tiles ? ncl : 1);
+    DevBuf<int> tcnt(tiles ? ncl : 1), toff(tiles ? ncl + 1 : 1), tlst(tiles ? static_cast<size_t>(ncl) * ntile_c : 1);
+    size_t tscan = 0;
+    if (tiles) cub::DeviceScan::InclusiveSum(nullptr, tscan, tcnt.get(), toff.get() + 1, ncl, s);
+    DevBuf<unsigned char> ttmp(std::max<size_t>(tscan, 1));
+    long long tiles_eval = 0;
     const T* Xr = X + lo * d;
     uint32_t* ar = d_assign + lo;
     float* ubr = ub.get() + (bounds ? lo : 0);
     float* lbr = lb.get() + (bounds ? lo : 0);
     auto assign_step = [&](bool first) {
+        if (tiles) {
+            if (first) {
+                assign_bounded<T>(ctx, X, N, d, d_ctr, k, d_assign, nullptr, ub.get(), lb.get(), nullptr, nullptr,
+                                  lbt.get());
+                reassigned += N;
+                tiles_eval += static_cast<long long>(ncl) * ntile_c;
+                return;
+            }
+            tile_shift_kernel<<<ntile_c, 32, 0, s>>>(delta.get(), k, 128, tshift.get());
+            tile_need_kernel<<<ncl, 256, 0, s>>>(order.get(), N, d_assign, ub.get(), delta.get(), tshift.get(), ntile_c,
+                                                 lbt.get(), tmask.get());
+            tile_count_kernel<<<ceil_div(ncl, 256), 256, 0, s>>>(tmask.get(), ncl, tcnt.get());
+            CUDA_OK(cudaMemsetAsync(toff.get(), 0, sizeof(int), s));
+            size_t t1 = ttmp.size();
+            cub::DeviceScan::InclusiveSum(ttmp.get(), t1, tcnt.get(), toff.get() + 1, ncl, s);
+            tile_fill_kernel<<<ceil_div(ncl, 256), 256, 0, s>>>(tmask.get(), ncl, toff.get(), tlst.get());
+            LAUNCH_OK("lloyd tile lists");
+            if (std::getenv("LCN_TIMING")) {
+                int tot = 0;
+                CUDA_OK(cudaMemcpyAsync(&tot, toff.get() + ncl, sizeof(int), cudaMemcpyDeviceToHost, s));
+                ctx.sync();
+                tiles_eval += tot;
+            }
+            assign_bounded<T>(ctx, X, N, d, d_ctr, k, d_assign, order.get(), ub.get(), lb.get(), toff.get(),
+                              tlst.get(), lbt.get());
+            reassigned += N;
+            return;
+        }
         if (!bounds) {
             if (Nr) assign_device<T>(ctx, Xr, Nr, d, d_ctr, k, ar);
             gather_assign();
@@ -2703,6 +2818,10 @@ void lloyd_device(Ctx& ctx, const T* X, long long N, int d, int k, int iters, ui
     if (exit_it >= 0 && std::getenv("LCN_TIMING"))
         std::fprintf(stderr, "[lloyd] N=%lld k=%d: fixed point at iteration %d of %d (the rest skipped)\n", N, k,
                      exit_it, iters);
+    if (tiles && std::getenv("LCN_TIMING"))
+        std::fprintf(stderr, "[lloyd] N=%lld k=%d: tile skipping evaluated %lld of %lld cluster x tile blocks (%.1f%%)\n",
+                     N, k, tiles_eval, static_cast<long long>(ncl) * ntile_c * (iters + 1),
+                     100.0 * tiles_eval / (static_cast<double>(ncl) * ntile_c * (iters + 1)));
     if (bounds && std::getenv("LCN_TIMING"))
         std::fprintf(stderr, "[lloyd] N=%lld k=%d%s: %lld of %lld point assignments re-evaluated (%.1f%%)\n", N, k,
                      cm ? " (this rank's slice)" : "", reassigned, Nr * (iters + 1),

@@ -211,7 +211,7 @@ __global__ void __cluster_dims__(kTCluster, 1, 1) __launch_bounds__(kTThreads, 1
     const float* __restrict__ ncf, int ntile, const unsigned long long* __restrict__ cmax,
     uint32_t* __restrict__ out, uint32_t* __restrict__ amb, unsigned* __restrict__ namb,
     float* __restrict__ dbg, int hh_only, const uint32_t* __restrict__ rows, float* __restrict__ ub,
-    float* __restrict__ lb) {
+    float* __restrict__ lb, const int* __restrict__ tl_off, const int* __restrict__ tl, float* __restrict__ lbt) {
     // all shared memory is dynamic (no static __shared__): the stage ring must
     // sit on 1024-byte swizzle-atom boundaries of the shared window
     extern __shared__ __align__(1024) unsigned char dyn_raw[];
@@ -257,6 +257,16 @@ __global__ void __cluster_dims__(kTCluster, 1, 1) __launch_bounds__(kTThreads, 1
     cluster_sync_all();  // every CTA's barriers exist before any multicast lands
     tc_fence_after();
     const uint32_t tmem = tmem_slot;
+    // tile list (Lloyd's tile skipping): this cluster evaluates the centroid
+    // tiles tl[tl_off[c] .. tl_off[c + 1]) in order, both CTAs the same ones
+    // (their stages are multicast); else every tile
+    int nt = ntile;
+    const int* tlist = nullptr;
+    if (tl_off) {
+        const int cl = static_cast<int>(blockIdx.x) / kTCluster;
+        tlist = tl + tl_off[cl];
+        nt = tl_off[cl + 1] - tl_off[cl];
+    }
     if (eq >= 0) {
         const long long p = p0 + row;
         // rows: the points of this call are rows[0 .. N) (lloyd's bound-failing list)
@@ -276,6 +286,11 @@ __global__ void __cluster_dims__(kTCluster, 1, 1) __launch_bounds__(kTThreads, 1
             tc_st32(tmem + (static_cast<uint32_t>(lane_base) << 16) + kTD + c0, vl);
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        // the two halves' |x|^2 -> both (the per-tile bounds need it early)
+        double* xnx = reinterpret_cast<double*>(reinterpret_cast<float*>(tempty + kTAcc + 2) + 3 * kTM + 2) + kTM;
+        xnx[half * kTM + row] = xn;
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kTEpi) : "memory");
+        xn += xnx[(1 - half) * kTM + row];
     }
     tc_fence_before();
     __syncthreads();
@@ -286,13 +301,14 @@ __global__ void __cluster_dims__(kTCluster, 1, 1) __launch_bounds__(kTThreads, 1
         // this CTA loads slice crank of each stage and multicasts it to the
         // cluster; its own barrier expects the whole stage (all slices)
         if (lane == 0) {
-            for (int g = 0; g < ntile * kTKS; ++g) {  // stage g: tile g / kTKS, features (g % kTKS) kTK ..
+            for (int g = 0; g < nt * kTKS; ++g) {  // stage g: listed tile g / kTKS, features (g % kTKS) kTK ..
                 const int s = g % kTStages;
+                const int tile = tlist ? tlist[g / kTKS] : g / kTKS;
                 if (g >= kTStages) mbar_wait(&empty[s], ((g / kTStages) - 1) & 1);
                 mbar_arrive_expect_tx(&full[s], kTStage);
                 bulk_g2s_multicast(ring + s * kTStage + crank * kTSlice,
-                                   tiles + static_cast<size_t>(g) * kTStage + crank * kTSlice, kTSlice, &full[s],
-                                   cmask);
+                                   tiles + (static_cast<size_t>(tile) * kTKS + g % kTKS) * kTStage + crank * kTSlice,
+                                   kTSlice, &full[s], cmask);
             }
         }
     } else if (warp == 1) {
@@ -303,7 +319,7 @@ __global__ void __cluster_dims__(kTCluster, 1, 1) __launch_bounds__(kTThreads, 1
         // address field sits in the low bits and never carries inside the
         // ring).
         int g = 0;  // ring stage counter
-        for (int t = 0; t < ntile; ++t) {
+        for (int t = 0; t < nt; ++t) {
             const int b = t % kTAcc;
             if (t >= kTAcc) mbar_wait(&tempty[b], ((t / kTAcc) - 1) & 1);
             const uint32_t dt = tmem + 256 + b * kTN;
@@ -346,14 +362,25 @@ __global__ void __cluster_dims__(kTCluster, 1, 1) __launch_bounds__(kTThreads, 1
         int i1[kCh];
 #pragma unroll
         for (int c = 0; c < kCh; ++c) v1[c] = v2[c] = kPosInf, i1[c] = 0;
-        for (int t = 0; t < ntile; ++t) {
+        // per-tile bound terms: |x|^2 and the filter's error E (as below)
+        const double u24 = 5.9604644775390625e-08;  // 2^-24
+        const double Cb = sqrt(__longlong_as_double(*cmax)) * (1.0 + 1e-12);
+        const double xb2 = sqrt(xn) * (1.0 + 1e-12);
+        const double dot_rel2 = 2.0 * (3.0 * 9.5367431640625e-07 + 56.0 * 1.1920928955078125e-07);
+        const double Eb = 1.05 * ((dot_rel2 + 4.0 * u24) * xb2 * Cb + 4.0 * u24 * Cb * Cb + u24 * u24 * Cb * Cb) +
+                          1e-12 * (xb2 + Cb) * (xb2 + Cb);
+        const long long pq = p0 + row;
+        const long long qq = rows && pq < N ? static_cast<long long>(rows[pq]) : pq;
+        for (int t = 0; t < nt; ++t) {
             const int b = t % kTAcc;
+            const int tile = tlist ? tlist[t] : t;
+            float tmin = kPosInf;  // this half's minimum score in the tile
             const uint32_t tcol = tmem + (static_cast<uint32_t>(lane_base) << 16) + 256 + b * kTN + half * kHC;
 #pragma unroll 1
             for (int ch = 0; ch < kHC / 32; ++ch) {
                 // |c|^2 of these 32 columns while the accumulator is in flight
                 float4 nc[8];
-                const float4* nc4 = reinterpret_cast<const float4*>(ncf + t * kTN + half * kHC + ch * 32);
+                const float4* nc4 = reinterpret_cast<const float4*>(ncf + tile * kTN + half * kHC + ch * 32);
 #pragma unroll
                 for (int j4 = 0; j4 < 8; ++j4) nc[j4] = __ldg(nc4 + j4);
                 if (ch == 0) {
@@ -372,7 +399,7 @@ __global__ void __cluster_dims__(kTCluster, 1, 1) __launch_bounds__(kTThreads, 1
                         const int col = half * kHC + ch * 32 + j;
                         if (col < 64) dbg[row * 64 + col] = __uint_as_float(r[j]);
                     }
-                const int base = t * kTN + half * kHC + ch * 32;
+                const int base = tile * kTN + half * kHC + ch * 32;
 #pragma unroll
                 for (int j4 = 0; j4 < 8; ++j4) {
                     const float ncj[4] = {nc[j4].x, nc[j4].y, nc[j4].z, nc[j4].w};
@@ -384,8 +411,15 @@ __global__ void __cluster_dims__(kTCluster, 1, 1) __launch_bounds__(kTThreads, 1
                         v2[u] = fminf(v2[u], fmaxf(v1[u], v));
                         i1[u] = lt1 ? base + j : i1[u];
                         v1[u] = fminf(v1[u], v);
+                        tmin = fminf(tmin, v);
                     }
                 }
+            }
+            if (lbt && pq < N) {
+                // a lower bound on the true distance to every centroid of the
+                // tile (this half): D >= |x|^2 + v - E, folds within 1e-12
+                const double lo = (xn + static_cast<double>(tmin) - Eb) * (1.0 - 1e-12);
+                lbt[(qq * ntile + tile) * 2 + half] = __double2float_rd(__dsqrt_rd(fmax(lo, 0.0)));
             }
         }
         // merge the trackers: best value, lowest index among equal bests,
@@ -401,12 +435,10 @@ __global__ void __cluster_dims__(kTCluster, 1, 1) __launch_bounds__(kTThreads, 1
         // merge the two halves of each row through shared memory (named
         // barrier 1: the epilogue warps only)
         float* xb = reinterpret_cast<float*>(tempty + kTAcc + 2);  // 128 x {bv, sv, bi} + xn
-        double* xnb = reinterpret_cast<double*>(xb + 3 * kTM + 2);
         if (half == 1) {
             xb[3 * row] = bv;
             xb[3 * row + 1] = sv;
             xb[3 * row + 2] = __int_as_float(bi);
-            xnb[row] = xn;
         }
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kTEpi) : "memory");
         if (half == 0) {
@@ -416,7 +448,6 @@ __global__ void __cluster_dims__(kTCluster, 1, 1) __launch_bounds__(kTThreads, 1
             sv = fminf(fminf(sv, os), fmaxf(bv, ov));
             if (ov < bv || (ov == bv && oi < bi)) bi = oi;
             bv = fminf(bv, ov);
-            xn += xnb[row];
         }
         const float v1m = bv, v2m = sv;
         const int i1m = bi;
@@ -464,7 +495,7 @@ __global__ void __cluster_dims__(kTCluster, 1, 1) __launch_bounds__(kTThreads, 1
 // shape is not handled (d > kTD).
 bool assign_filter_tc(Ctx& ctx, const float* X, long long N, int d, const double* C, int k, uint32_t* out,
                       uint32_t* amb, unsigned* namb, float* dbg_acc, int hh_only, const uint32_t* rows, float* ub,
-                      float* lb) {
+                      float* lb, const int* tl_off, const int* tl, float* lbt) {
     if (d > kTD || d < 1) return false;
     cudaStream_t s = ctx.stream;
     const int ntile = static_cast<int>(ceil_div(k, kTN));
@@ -474,7 +505,7 @@ bool assign_filter_tc(Ctx& ctx, const float* X, long long N, int d, const double
     cmax.zero(s);
     tc_prep_kernel<<<ntile * kTN, 128, 0, s>>>(C, k, d, ntile, tiles.get(), ncf.get(), cmax.get());
     // ring + barriers (2 kTStages + 2 kTAcc) + TMEM slot + row-merge buffer
-    const int smem = kTStages * kTStage + 1024 + (2 * kTStages + 2 * kTAcc + 2) * 8 + (3 * kTM + 2) * 4 + kTM * 8 + 64;
+    const int smem = kTStages * kTStage + 1024 + (2 * kTStages + 2 * kTAcc + 2) * 8 + (3 * kTM + 2) * 4 + 3 * kTM * 8 + 64;
     static std::atomic<bool> attr[64];  // set once per device; concurrent build jobs may race here (benign, idempotent)
     if (ctx.device >= 64 || !attr[ctx.device]) {
         CUDA_OK(cudaFuncSetAttribute(assign_filter_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -483,9 +514,14 @@ bool assign_filter_tc(Ctx& ctx, const float* X, long long N, int d, const double
     // grid: whole clusters (CTAs past N only help stream the centroid stages)
     const long long grid = ceil_div(ceil_div(N, kTM), kTCluster) * kTCluster;
     assign_filter_tc_kernel<<<static_cast<unsigned>(grid), kTThreads, smem, s>>>(
-        X, N, d, tiles.get(), ncf.get(), ntile, cmax.get(), out, amb, namb, dbg_acc, hh_only, rows, ub, lb);
+        X, N, d, tiles.get(), ncf.get(), ntile, cmax.get(), out, amb, namb, dbg_acc, hh_only, rows, ub, lb, tl_off, tl,
+        lbt);
     LAUNCH_OK("assign_filter_tc_kernel");
     return true;
 }
+
+int assign_tc_tile_count(int k) { return static_cast<int>(ceil_div(k, kTN)); }
+constexpr int kTcClusterPoints = kTM * kTCluster;
+static_assert(kTcClusterPoints == 256, "lloyd's tile lists assume 256 points per cluster");
 
 }  // namespace lcnb

@@ -611,3 +611,22 @@ def test_lloyd_fixed_point_exit(ctx, ref, monkeypatch, exit_):
     c_ref, a_ref = ref.lloyd(x, 24, 10, 51)
     assert np.array_equal(a_gpu, a_ref)
     assert np.array_equal(c_gpu.view(np.uint64), c_ref.view(np.uint64))
+
+
+def test_lloyd_tile_skipping_bit_exact(ctx, ref, monkeypatch):
+    # >= 8 tiles of 128 centroids: after the first full assignment each
+    # cluster of 256 (sorted) points evaluates only the tiles its bounds do
+    # not exclude -- assignment and centroid bits equal to the reference and
+    # to evaluating every tile
+    r = np.random.default_rng(71)
+    means = r.standard_normal((200, 32)) * 3.0
+    x = (means[r.integers(0, 200, 100_000)] + 0.5 * r.standard_normal((100_000, 32))).astype(np.float32)
+    x = x.astype(np.float64)
+    c1, a1 = lcn.lloyd(ctx, x, 1024, 10, 71)
+    c_ref, a_ref = ref.lloyd(x, 1024, 10, 71)
+    assert np.array_equal(a1, a_ref)
+    assert np.array_equal(c1.view(np.uint64), c_ref.view(np.uint64))
+    monkeypatch.setenv("LCN_LLOYD_TILES", "0")
+    c0, a0 = lcn.lloyd(ctx, x, 1024, 10, 71)
+    assert np.array_equal(a0, a1)
+    assert np.array_equal(c0.view(np.uint64), c1.view(np.uint64))
