@@ -2521,12 +2521,33 @@ __global__ void __launch_bounds__(256) lloyd_bounds_kernel(const T* __restrict__
 // tile always qualifies (its bound <= the distance to the own centroid), so
 // the argmin over the evaluated tiles is the global one; ambiguous points
 // still get the exact full scan.
-__global__ void tile_shift_kernel(const double* __restrict__ delta, int k, int tn, double* __restrict__ tshift) {
+__global__ void tile_shift_kernel(const double* __restrict__ delta, int k, int tn, const uint32_t* __restrict__ perm,
+                                  double* __restrict__ tshift) {
     const int g = blockIdx.x, lane = threadIdx.x;
     double m = 0.0;
-    for (int c = g * tn + lane; c < min(k, (g + 1) * tn); c += 32) m = fmax(m, delta[c]);
+    for (int c = g * tn + lane; c < min(k, (g + 1) * tn); c += 32) m = fmax(m, delta[perm ? perm[c] : c]);
     m = warp_max(m);
     if (lane == 0) tshift[g] = m;
+}
+
+// Tile order of the centroids: each centroid's nearest among the first 32
+// (the earliest k-means++ seeds, spread over the data) is its group; a
+// stable sort by group packs nearby centroids into the same tiles.
+__global__ void tile_group_kernel(const double* __restrict__ C, int k, int d, int G, uint32_t* __restrict__ grp) {
+    const int c = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (c >= k) return;
+    double best = kPosInf;
+    int arg = 0;
+    for (int g = 0; g < G; ++g) {
+        double s2 = 0.0;
+        for (int kk = lane; kk < d; kk += 32) {
+            const double df = C[static_cast<long long>(c) * d + kk] - C[static_cast<long long>(g) * d + kk];
+            s2 += df * df;
+        }
+        s2 = warp_sum(s2);
+        if (s2 < best) { best = s2; arg = g; }
+    }
+    if (lane == 0) grp[c] = static_cast<uint32_t>(arg);
 }
 
 __global__ void __launch_bounds__(256) tile_need_kernel(const uint32_t* __restrict__ order, long long N,
@@ -2585,13 +2606,13 @@ __global__ void tile_fill_kernel(const unsigned long long* __restrict__ masks, i
 template <typename T>
 void assign_bounded(Ctx& ctx, const T* X, long long n, int d, const double* C, int k, uint32_t* out,
                     const uint32_t* rows, float* ub, float* lb, const int* tl_off = nullptr, const int* tl = nullptr,
-                    float* lbt = nullptr) {
+                    float* lbt = nullptr, const uint32_t* perm = nullptr) {
     cudaStream_t s = ctx.stream;
     DevBuf<uint32_t> amb(n);
     DevBuf<unsigned> namb(1);
     namb.zero(s);
     if (!assign_filter_tc(ctx, reinterpret_cast<const float*>(X), n, d, C, k, out, amb.get(), namb.get(), nullptr, 0,
-                          rows, ub, lb, tl_off, tl, lbt))
+                          rows, ub, lb, tl_off, tl, lbt, perm))
         throw Status(100, "lloyd bounds: tensor-core filter unavailable for this shape");
     unsigned h_amb = 0;
     namb.download(&h_amb, 1, s);
@@ -2700,6 +2721,19 @@ void lloyd_device(Ctx& ctx, const T* X, long long N, int d, int k, int iters, ui
     if (tiles) cub::DeviceScan::InclusiveSum(nullptr, tscan, tcnt.get(), toff.get() + 1, ncl, s);
     DevBuf<unsigned char> ttmp(std::max<size_t>(tscan, 1));
     long long tiles_eval = 0;
+    DevBuf<uint32_t> tperm(tiles ? k : 1);
+    if (tiles) {  // centroid tile order from the initial centroids (the seeds)
+        DevBuf<uint32_t> grp(k), grp_s(k), idx(k);
+        tile_group_kernel<<<ceil_div(k, 8), 256, 0, s>>>(d_ctr, k, d, std::min(k, 32), grp.get());
+        iota_kernel<<<ceil_div(k, 256), 256, 0, s>>>(idx.get(), k);
+        size_t ts = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, ts, grp.get(), grp_s.get(), idx.get(), tperm.get(), k, 0, 6, s);
+        DevBuf<unsigned char> tt(std::max<size_t>(ts, 1));
+        cub::DeviceRadixSort::SortPairs(tt.get(), ts, grp.get(), grp_s.get(), idx.get(), tperm.get(), k, 0, 6, s);
+        LAUNCH_OK("lloyd tile order");
+    }
+    const char* tpenv = std::getenv("LCN_LLOYD_TILE_ORDER");
+    const uint32_t* tp = tiles && !(tpenv && tpenv[0] == '0') ? tperm.get() : nullptr;
     const T* Xr = X + lo * d;
     uint32_t* ar = d_assign + lo;
     float* ubr = ub.get() + (bounds ? lo : 0);
@@ -2708,12 +2742,12 @@ void lloyd_device(Ctx& ctx, const T* X, long long N, int d, int k, int iters, ui
         if (tiles) {
             if (first) {
                 assign_bounded<T>(ctx, X, N, d, d_ctr, k, d_assign, nullptr, ub.get(), lb.get(), nullptr, nullptr,
-                                  lbt.get());
+                                  lbt.get(), tp);
                 reassigned += N;
                 tiles_eval += static_cast<long long>(ncl) * ntile_c;
                 return;
             }
-            tile_shift_kernel<<<ntile_c, 32, 0, s>>>(delta.get(), k, 128, tshift.get());
+            tile_shift_kernel<<<ntile_c, 32, 0, s>>>(delta.get(), k, 128, tp, tshift.get());
             tile_need_kernel<<<ncl, 256, 0, s>>>(order.get(), N, d_assign, ub.get(), delta.get(), tshift.get(), ntile_c,
                                                  lbt.get(), tmask.get());
             tile_count_kernel<<<ceil_div(ncl, 256), 256, 0, s>>>(tmask.get(), ncl, tcnt.get());
@@ -2729,7 +2763,7 @@ void lloyd_device(Ctx& ctx, const T* X, long long N, int d, int k, int iters, ui
                 tiles_eval += tot;
             }
             assign_bounded<T>(ctx, X, N, d, d_ctr, k, d_assign, order.get(), ub.get(), lb.get(), toff.get(),
-                              tlst.get(), lbt.get());
+                              tlst.get(), lbt.get(), tp);
             reassigned += N;
             return;
         }

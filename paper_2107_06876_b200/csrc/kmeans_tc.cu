@@ -78,16 +78,18 @@ __device__ __forceinline__ float tf32_hi(float x) {
 // +inf for padding), and max_c max(|c|^2, |c_f|^2).
 __global__ void __launch_bounds__(128) tc_prep_kernel(const double* __restrict__ C, int k, int d, int ntile,
                                                        unsigned char* __restrict__ tiles, float* __restrict__ ncf,
-                                                       unsigned long long* __restrict__ cmax) {
+                                                       unsigned long long* __restrict__ cmax,
+                                                       const uint32_t* __restrict__ perm) {
     __shared__ double r1[4], r2[4];
-    const int c = blockIdx.x;  // centroid (padded to ntile * kTN)
+    const int c = blockIdx.x;  // centroid slot (padded to ntile * kTN); perm: slot -> centroid
     const int t = c / kTN, r = c % kTN;
     double s1 = 0.0, s2 = 0.0;
     for (int kk = threadIdx.x; kk < kTD; kk += 128) {
         // stage t * kTKS + kk / kTK holds features [kh kTK, (kh + 1) kTK) of tile t
         unsigned char* hi = tiles + (static_cast<size_t>(t) * kTKS + kk / kTK) * kTStage;
         unsigned char* lo = hi + kTHalf;
-        const double v = (c < k && kk < d) ? C[static_cast<long long>(c) * d + kk] : 0.0;
+        const long long cc = perm && c < k ? static_cast<long long>(perm[c]) : c;
+        const double v = (c < k && kk < d) ? C[cc * d + kk] : 0.0;
         const float f = static_cast<float>(v);
         const float h = tf32_hi(f);
         *reinterpret_cast<float*>(hi + tile_offset(r, kk % kTK)) = h;
@@ -211,7 +213,8 @@ __global__ void __cluster_dims__(kTCluster, 1, 1) __launch_bounds__(kTThreads, 1
     const float* __restrict__ ncf, int ntile, const unsigned long long* __restrict__ cmax,
     uint32_t* __restrict__ out, uint32_t* __restrict__ amb, unsigned* __restrict__ namb,
     float* __restrict__ dbg, int hh_only, const uint32_t* __restrict__ rows, float* __restrict__ ub,
-    float* __restrict__ lb, const int* __restrict__ tl_off, const int* __restrict__ tl, float* __restrict__ lbt) {
+    float* __restrict__ lb, const int* __restrict__ tl_off, const int* __restrict__ tl, float* __restrict__ lbt,
+    const uint32_t* __restrict__ perm) {
     // all shared memory is dynamic (no static __shared__): the stage ring must
     // sit on 1024-byte swizzle-atom boundaries of the shared window
     extern __shared__ __align__(1024) unsigned char dyn_raw[];
@@ -464,7 +467,7 @@ __global__ void __cluster_dims__(kTCluster, 1, 1) __launch_bounds__(kTThreads, 1
             const double gap = static_cast<double>(v2m) - static_cast<double>(v1m);
             const long long q = rows ? static_cast<long long>(rows[p]) : p;
             if (gap > 2.0 * E) {
-                out[q] = static_cast<uint32_t>(i1m);
+                out[q] = perm ? perm[i1m] : static_cast<uint32_t>(i1m);  // slot -> centroid
                 if (ub) {
                     // Lloyd's bounds on true distances (lloyd_device): every
                     // fold D(x, c) lies within E of |x|^2 + v(c), the fold
@@ -495,7 +498,7 @@ __global__ void __cluster_dims__(kTCluster, 1, 1) __launch_bounds__(kTThreads, 1
 // shape is not handled (d > kTD).
 bool assign_filter_tc(Ctx& ctx, const float* X, long long N, int d, const double* C, int k, uint32_t* out,
                       uint32_t* amb, unsigned* namb, float* dbg_acc, int hh_only, const uint32_t* rows, float* ub,
-                      float* lb, const int* tl_off, const int* tl, float* lbt) {
+                      float* lb, const int* tl_off, const int* tl, float* lbt, const uint32_t* perm) {
     if (d > kTD || d < 1) return false;
     cudaStream_t s = ctx.stream;
     const int ntile = static_cast<int>(ceil_div(k, kTN));
@@ -503,7 +506,7 @@ bool assign_filter_tc(Ctx& ctx, const float* X, long long N, int d, const double
     DevBuf<float> ncf(static_cast<size_t>(ntile) * kTN);
     DevBuf<unsigned long long> cmax(1);
     cmax.zero(s);
-    tc_prep_kernel<<<ntile * kTN, 128, 0, s>>>(C, k, d, ntile, tiles.get(), ncf.get(), cmax.get());
+    tc_prep_kernel<<<ntile * kTN, 128, 0, s>>>(C, k, d, ntile, tiles.get(), ncf.get(), cmax.get(), perm);
     // ring + barriers (2 kTStages + 2 kTAcc) + TMEM slot + row-merge buffer
     const int smem = kTStages * kTStage + 1024 + (2 * kTStages + 2 * kTAcc + 2) * 8 + (3 * kTM + 2) * 4 + 3 * kTM * 8 + 64;
     static std::atomic<bool> attr[64];  // set once per device; concurrent build jobs may race here (benign, idempotent)
@@ -515,7 +518,7 @@ bool assign_filter_tc(Ctx& ctx, const float* X, long long N, int d, const double
     const long long grid = ceil_div(ceil_div(N, kTM), kTCluster) * kTCluster;
     assign_filter_tc_kernel<<<static_cast<unsigned>(grid), kTThreads, smem, s>>>(
         X, N, d, tiles.get(), ncf.get(), ntile, cmax.get(), out, amb, namb, dbg_acc, hh_only, rows, ub, lb, tl_off, tl,
-        lbt);
+        lbt, perm);
     LAUNCH_OK("assign_filter_tc_kernel");
     return true;
 }
