@@ -324,19 +324,24 @@ def measure_tf32_peak(dev):
         torch.backends.cuda.matmul.allow_tf32 = prev
 
 
-def distance_roofline(iv, n, m, d, bands, buckets, landmarks, iters, tf32_peak=None):
+def distance_roofline(iv, n, m, d, bands, buckets, landmarks, iters, tf32_peak=None, point_tiles=None):
     """Tensor-core roofline of the distance blocks (the tcgen05 3xTF32
-    assignment filter of the k-means in the LSH and landmark build): MMA work
-    of one build = per assign launch 2 N_pad K_pad 128 x 3 (hi.hi, hi.lo,
-    lo.hi), over the union of the launches' device intervals."""
+    assignment filter of the k-means in the LSH and landmark build) over the
+    union of the launches' device intervals. The MMA work is what the kernel
+    evaluated: the library's work counter (lcn_ctx_tc_work) of point x
+    128-centroid tile products, 2 * 128 * 128 * 3 MMA flops each (hi.hi,
+    hi.lo, lo.hi at 128 padded features). Lloyd's certified bounds and tile
+    skipping make it data dependent; `dense_equivalent` is the work of full
+    assignments of every point to every centroid."""
     N = n + m
-    npad = -(-N // 512) * 512  # whole 4-CTA clusters of 128 points
+    if d > 128 or not iv:
+        return None
     # select_landmarks runs lloyd with 10 iterations (nystrom.cpp:28-48)
     launches = [buckets] * (bands * (iters + 1)) + [landmarks] * (10 + 1)
-    if len(iv) != len(launches) or d > 128:
+    dense_mma = sum(2.0 * N * (-(-k // 128) * 128) * 128 * 3 for k in launches)
+    mma = 2.0 * 128 * 128 * 3 * point_tiles if point_tiles else None
+    if mma is None:
         return None
-    mma = sum(2.0 * npad * (-(-k // 64) * 64) * 128 * 3 for k in launches)
-    fp32 = sum(2.0 * N * k * d for k in launches)
     t = union_us(iv) * 1e-6
     nominal = 1100.0  # TF32 dense, B200_PROFILING.md
     peak = tf32_peak if tf32_peak else nominal
@@ -346,10 +351,14 @@ def distance_roofline(iv, n, m, d, bands, buckets, landmarks, iters, tf32_peak=N
     return {"bound": "tensor", "kernel": "assign_filter_tc_kernel (tcgen05.mma kind::tf32, 3xTF32)",
             "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "peak_kind": kind,
             "nominal_peak": nominal, "frac_vs_nominal": ach / nominal,
-            "fp32_accurate_achieved": fp32 / t / 1e12, "fp32_accurate_peak": peak / 3,
-            "launches": len(iv), "device_ms": t * 1e3,
-            "work": "per build: bands x (iters + 1) assigns of n+m points to the buckets + 11 to the "
-                    "landmarks; MMA flops 2 N_pad K_pad 128 x 3"}
+            "fp32_accurate_achieved": ach / 3, "fp32_accurate_peak": peak / 3,
+            "launches": len(iv), "device_ms": t * 1e3, "point_tiles": point_tiles,
+            "mma_flops": mma, "dense_equivalent_mma_flops": dense_mma,
+            "evaluated_share_of_dense": mma / dense_mma,
+            "work": "MMA flops the filter evaluated in one build (lcn_ctx_tc_work counter: point x 128-centroid "
+                    "tile products x 2*128*128*3); Lloyd's bounds and tile skipping evaluate "
+                    "evaluated_share_of_dense of the full assignments (bands x (iters + 1) of n+m points to the "
+                    "buckets + 11 to the landmarks)"}
 
 
 def batched_c4(lcn, ctx, with_cpu):
@@ -665,6 +674,7 @@ def run_ours(args, rank, world, local_rank):
     e2e = None
     dist_roof = None
     dist_iv = None
+    dist_tiles = None
     if not args.no_e2e:
         if fp64_line is None:
             del op
@@ -690,8 +700,10 @@ def run_ours(args, rank, world, local_rank):
                 # the untimed warm-up build doubles as the tensor-core trace
                 holder = []
                 try:
+                    ctx.tc_work(reset=True)
                     iv = kernel_intervals(lambda: holder.append(build2()), "assign_filter_tc_kernel")
                     dist_iv = iv  # roofline computed after the timed regions (TF32 peak GEMM)
+                    dist_tiles = ctx.tc_work(reset=True)
                 except Exception as ex:  # profiler unavailable: report none
                     print("distance roofline unavailable:", ex, file=sys.stderr)
                 op2 = holder[0] if holder else build2()
@@ -745,7 +757,7 @@ def run_ours(args, rank, world, local_rank):
         except Exception as ex:
             print("tf32 peak measurement failed:", ex, file=sys.stderr)
         if dist_iv is not None:
-            dist_roof = distance_roofline(dist_iv, n, m, d, pr.bands, pr.buckets, l, pr.kmeans_iters, tf32)
+            dist_roof = distance_roofline(dist_iv, n, m, d, pr.bands, pr.buckets, l, pr.kmeans_iters, tf32, dist_tiles)
     anchor = None
     if rank == 0 and not args.no_dense:
         try:

@@ -132,6 +132,11 @@ const char* lcn_ctx_last_error(const lcn_ctx* ctx);
 int lcn_ctx_set_stream(lcn_ctx* ctx, void* stream);
 /* Record per-phase CUDA events inside lcn_sinkhorn (see lcn_result_phase_ms). */
 int lcn_ctx_set_profile(lcn_ctx* ctx, int on);
+/* Work counter of the tensor-core assignment filter on the context's device
+ * (profiling; no reference counterpart): point x 128-centroid tile products
+ * evaluated since the last reset, one product = 2 * 128 * 128 * 3 MMA flops
+ * (3xTF32) at d <= 128. Synchronous; reset != 0 zeroes it after the read. */
+int lcn_ctx_tc_work(lcn_ctx* ctx, int reset, unsigned long long* point_tiles);
 
 /* ---- sharded solve over several GPUs ------------------ */
 /* A fresh NCCL unique id (128 bytes) on the calling rank (rank 0 makes it,

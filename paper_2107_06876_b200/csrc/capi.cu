@@ -668,6 +668,14 @@ extern "C" int lcn_debug_tc_scores(lcn_ctx* ctx, const float* points, size_t n, 
     });
 }
 
+int lcn_ctx_tc_work(lcn_ctx* ctx, int reset, unsigned long long* point_tiles) {
+    return guard(ctx, [&] {
+        if (!point_tiles) throw Status(2, "lcn_ctx_tc_work: null output");
+        CUDA_OK(cudaSetDevice(ctx->c.device));
+        *point_tiles = tc_point_tiles(reset != 0);
+    });
+}
+
 int lcn_lloyd(lcn_ctx* ctx, const double* points, size_t n, size_t d, size_t k, int iters, uint64_t seed,
               double* centroids_out, uint32_t* assign_out) {
     return guard(ctx, [&] {

@@ -208,6 +208,11 @@ __device__ __forceinline__ void tc_ld64(uint32_t taddr, uint32_t (&r)[64]) {
 
 }  // namespace
 
+// Work counter (bench.py's distance roofline): point x tile products this
+// filter evaluated, summed over launches (tile skipping and the bound-failing
+// row lists make it data dependent). One atomic per CTA.
+__device__ unsigned long long g_tc_point_tiles = 0;
+
 __global__ void __cluster_dims__(kTCluster, 1, 1) __launch_bounds__(kTThreads, 1) assign_filter_tc_kernel(
     const float* __restrict__ X, long long N, int d, const unsigned char* __restrict__ tiles,
     const float* __restrict__ ncf, int ntile, const unsigned long long* __restrict__ cmax,
@@ -270,6 +275,9 @@ __global__ void __cluster_dims__(kTCluster, 1, 1) __launch_bounds__(kTThreads, 1
         tlist = tl + tl_off[cl];
         nt = tl_off[cl + 1] - tl_off[cl];
     }
+    if (tid == 0 && p0 < N)
+        atomicAdd(&g_tc_point_tiles, static_cast<unsigned long long>(min(static_cast<long long>(kTM), N - p0)) *
+                                         static_cast<unsigned long long>(nt));
     if (eq >= 0) {
         const long long p = p0 + row;
         // rows: the points of this call are rows[0 .. N) (lloyd's bound-failing list)
@@ -521,6 +529,16 @@ bool assign_filter_tc(Ctx& ctx, const float* X, long long N, int d, const double
         lbt, perm);
     LAUNCH_OK("assign_filter_tc_kernel");
     return true;
+}
+
+unsigned long long tc_point_tiles(bool reset) {
+    unsigned long long v = 0;
+    CUDA_OK(cudaMemcpyFromSymbol(&v, g_tc_point_tiles, sizeof(v)));
+    if (reset) {
+        const unsigned long long z = 0;
+        CUDA_OK(cudaMemcpyToSymbol(g_tc_point_tiles, &z, sizeof(z)));
+    }
+    return v;
 }
 
 int assign_tc_tile_count(int k) { return static_cast<int>(ceil_div(k, kTN)); }

@@ -25,4 +25,7 @@ bool assign_filter_tc(Ctx& ctx, const float* X, long long N, int d, const double
 // that order (tiles of nearby centroids skip better); outputs stay in
 // centroid indices.
 int assign_tc_tile_count(int k);
+// the filter's work counter on the current device: point x 128-centroid tile
+// products evaluated since the last reset (synchronous read)
+unsigned long long tc_point_tiles(bool reset);
 }  // namespace lcnb

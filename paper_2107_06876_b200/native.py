@@ -124,6 +124,7 @@ def library() -> C.CDLL:
             "lcn_ctx_last_error": ([P], C.c_char_p),
             "lcn_ctx_set_stream": ([P, P], I),
             "lcn_ctx_set_profile": ([P, I], I),
+            "lcn_ctx_tc_work": ([P, I, C.POINTER(C.c_ulonglong)], I),
             "lcn_sinkhorn_device": ([P, P, P, C.POINTER(_SinkOpts), PP], I),
             "lcn_result_phase_ms": ([P, P, C.POINTER(I)], I),
             "lcn_kmeans_pp_indices": ([P, P, SZ, SZ, SZ, U64, P, SZ, P, C.POINTER(SZ)], I),
@@ -230,6 +231,13 @@ class Context:
 
     def set_profile(self, on: bool):
         self.check(self.lib.lcn_ctx_set_profile(self.h, 1 if on else 0))
+
+    def tc_work(self, reset: bool = False) -> int:
+        """Point x 128-centroid tile products the tensor-core assignment
+        filter evaluated since the last reset (lcn_ctx_tc_work)."""
+        v = C.c_ulonglong(0)
+        self.check(self.lib.lcn_ctx_tc_work(self.h, 1 if reset else 0, C.byref(v)))
+        return int(v.value)
 
     def set_comm(self, world: int, rank: int, uid: bytes):
         """Join a sharded solve (lcn_ctx_set_comm): `uid` is rank 0's

@@ -97,6 +97,25 @@ def test_assign_filter_bit_exact(ctx, ref, n, d, k, seed, dup):
     assert np.array_equal(lcn.assign_nearest(ctx, x, ctr), ref.assign_nearest(x, ctr))
 
 
+def test_tc_work_counter(ctx, ref):
+    # lcn_ctx_tc_work (bench.py's distance roofline): a full assignment
+    # evaluates every point against every 128-centroid tile; Lloyd with its
+    # bounds and tile skipping evaluates fewer than iters + 1 full ones
+    n, d, k = 40000, 128, 256
+    x = rng_points(31, n, d)
+    r = np.random.default_rng(31)
+    ctr = x[r.choice(n, k, replace=False)] + r.standard_normal((k, d)) * 0.3
+    ctx.tc_work(reset=True)
+    assert np.array_equal(lcn.assign_nearest(ctx, x, ctr), ref.assign_nearest(x, ctr))
+    assert ctx.tc_work(reset=True) == n * (k // 128)
+    n, k = 120000, 1024
+    x = rng_points(32, n, d, comps=64)
+    c_gpu, a_gpu = lcn.lloyd(ctx, x, k, 10, 32)
+    work = ctx.tc_work()
+    assert 0 < work < 11 * n * (k // 128)
+    assert ctx.tc_work(reset=True) == work and ctx.tc_work() == 0
+
+
 @pytest.mark.parametrize("dup", [False, True])
 def test_assign_gemm_filter_bit_exact(ctx, ref, dup):
     # d > 128 with N k >= 2^22: the fp32 GEMM + top-2 filter (configs[1]'s
