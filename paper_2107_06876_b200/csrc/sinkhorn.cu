@@ -440,6 +440,7 @@ __global__ void __launch_bounds__(256) dense_lse_kernel(const DevState* __restri
     }
 }
 
+constexpr float kL2E = 1.4426950408889634f;  // log2(e)
 __device__ __forceinline__ float ex2_ftz(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -507,7 +508,6 @@ __global__ void __launch_bounds__(kThreads + 32, 2) dense_lse_tma_kernel(const D
         }
         return;
     }
-    constexpr float kL2E = 1.4426950408889634f;
     const int qi = tid & 127, h = tid >> 7;  // column quad, row set
     int stage = 0;
     uint32_t phase = 0;
@@ -722,6 +722,24 @@ __device__ __forceinline__ double pack_ms(float m, float s) {
 __device__ __forceinline__ float2 unpack_ms(double v) {
     const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
     return make_float2(__uint_as_float(static_cast<unsigned>(b)), __uint_as_float(static_cast<unsigned>(b >> 32)));
+}
+// online log-sum-exp steps of the band consumers: fold entries d into the
+// running (max m, sum s of exp(. - m)). An all -inf history keeps offset 0 so
+// that exp(-inf - 0) = 0 (masked duplicates) instead of NaN.
+__device__ __forceinline__ void lse_add4(float& m, float& s, float d0, float d1, float d2, float d3) {
+    const float mn = fmaxf(fmaxf(m, fmaxf(d0, d1)), fmaxf(d2, d3));
+    const float o = mn == -CUDART_INF_F ? 0.0f : mn;
+    const float ol = o * kL2E;
+    s = fmaf(s, ex2_ftz((m - o) * kL2E),
+             (ex2_ftz(fmaf(d0, kL2E, -ol)) + ex2_ftz(fmaf(d1, kL2E, -ol))) +
+                 (ex2_ftz(fmaf(d2, kL2E, -ol)) + ex2_ftz(fmaf(d3, kL2E, -ol))));
+    m = mn;
+}
+__device__ __forceinline__ void lse_add1(float& m, float& s, float d) {
+    const float mn = fmaxf(m, d);
+    const float o = mn == -CUDART_INF_F ? 0.0f : mn;
+    s = fmaf(s, ex2_ftz((m - o) * kL2E), ex2_ftz((d - o) * kL2E));
+    m = mn;
 }
 // merge (m, s) into the output's running (M, S) (lse_merge in fp64)
 __device__ __forceinline__ void lse_store(double* __restrict__ Mo, double* __restrict__ So, uint32_t i, float m, float s) {
@@ -964,45 +982,30 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
             if (own) {
                 const T* p = blk + 4 * q;
                 if constexpr (LSE) {
-                    // log domain: per output the chunk's max, then the sum of
-                    // exp(log K + log v - max) with the running sum rescaled
-                    // once per chunk (two reads of the staged chunk)
+                    // log domain, one read of the staged chunk: blocks of four
+                    // stream rows per thread, the running (max, sum) of each
+                    // output rescaled once per block (5 exponentials per 4
+                    // entries), single rows for the remainder
                     const float* vf = reinterpret_cast<const float*>(sm.vec[slot]) + r0;
-                    float cm[4] = {-CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F};
-#pragma unroll 4
-                    for (uint32_t r = g; r < nr; r += ng) {
+                    uint32_t r = g;
+                    for (; r + 3 * ng < nr; r += 4 * ng) {
+                        const float4 x0 = *reinterpret_cast<const float4*>(p + r * ws);
+                        const float4 x1 = *reinterpret_cast<const float4*>(p + (r + ng) * ws);
+                        const float4 x2 = *reinterpret_cast<const float4*>(p + (r + 2 * ng) * ws);
+                        const float4 x3 = *reinterpret_cast<const float4*>(p + (r + 3 * ng) * ws);
+                        const float s0 = vf[r], s1 = vf[r + ng], s2 = vf[r + 2 * ng], s3 = vf[r + 3 * ng];
+                        lse_add4(lm[0], ls[0], x0.x + s0, x1.x + s1, x2.x + s2, x3.x + s3);
+                        lse_add4(lm[1], ls[1], x0.y + s0, x1.y + s1, x2.y + s2, x3.y + s3);
+                        lse_add4(lm[2], ls[2], x0.z + s0, x1.z + s1, x2.z + s2, x3.z + s3);
+                        lse_add4(lm[3], ls[3], x0.w + s0, x1.w + s1, x2.w + s2, x3.w + s3);
+                    }
+                    for (; r < nr; r += ng) {
                         const float4 x = *reinterpret_cast<const float4*>(p + r * ws);
                         const float sr = vf[r];
-                        cm[0] = fmaxf(cm[0], x.x + sr);
-                        cm[1] = fmaxf(cm[1], x.y + sr);
-                        cm[2] = fmaxf(cm[2], x.z + sr);
-                        cm[3] = fmaxf(cm[3], x.w + sr);
-                    }
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (cm[k] > lm[k]) {
-                            ls[k] *= __expf(lm[k] - cm[k]);
-                            lm[k] = cm[k];
-                        }
-                    if (lm[0] != -CUDART_INF_F || lm[1] != -CUDART_INF_F || lm[2] != -CUDART_INF_F ||
-                        lm[3] != -CUDART_INF_F) {
-                        // an output whose max is still -inf has only -inf entries:
-                        // offset 0 keeps exp(-inf - 0) = 0 instead of NaN
-                        const float o0 = lm[0] == -CUDART_INF_F ? 0.0f : lm[0];
-                        const float o1 = lm[1] == -CUDART_INF_F ? 0.0f : lm[1];
-                        const float o2 = lm[2] == -CUDART_INF_F ? 0.0f : lm[2];
-                        const float o3 = lm[3] == -CUDART_INF_F ? 0.0f : lm[3];
-                        float e0 = 0.0f, e1 = 0.0f, e2 = 0.0f, e3 = 0.0f;
-#pragma unroll 4
-                        for (uint32_t r = g; r < nr; r += ng) {
-                            const float4 x = *reinterpret_cast<const float4*>(p + r * ws);
-                            const float sr = vf[r];
-                            e0 += __expf(x.x + sr - o0);
-                            e1 += __expf(x.y + sr - o1);
-                            e2 += __expf(x.z + sr - o2);
-                            e3 += __expf(x.w + sr - o3);
-                        }
-                        ls[0] += e0; ls[1] += e1; ls[2] += e2; ls[3] += e3;
+                        lse_add1(lm[0], ls[0], x.x + sr);
+                        lse_add1(lm[1], ls[1], x.y + sr);
+                        lse_add1(lm[2], ls[2], x.z + sr);
+                        lse_add1(lm[3], ls[3], x.w + sr);
                     }
                 } else if constexpr (sizeof(T) == 4) {
                     // fp32 products and per-chunk partials, widened once per chunk
