@@ -780,7 +780,7 @@ def run_ours(args, rank, world, local_rank):
                          "roofline": {"bound": "hbm", "achieved": b_s / (ms_s * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
                                       "frac": b_s / (ms_s * 1e-3) / 1e9 / hbm,
                                       "algorithmic_bytes_per_iteration": b_s,
-                                      "kernel": "sparse_row_band_kernel (rows and the transposed blocks)"}}
+                                      "kernel": "band_stream_kernel, log-sum-exp mode (row and column band passes, single-read online consumer)"}}
             del sop, rs
         except Exception as ex:
             sparse_op = {"unavailable": str(ex)}

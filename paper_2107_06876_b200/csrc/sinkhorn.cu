@@ -803,8 +803,15 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
                                                                       const uint32_t* __restrict__ o_order, BandWork wk, const T* __restrict__ vals,
                                                                       const double* __restrict__ logv,
                                                                       double* __restrict__ corr,
-                                                                      double* __restrict__ Sout = nullptr) {
-    pdl_wait();  // launched with programmatic serialisation inside the LCN iteration
+                                                                      double* __restrict__ Sout = nullptr,
+                                                                      int late_wait = 0) {
+    // Launched with programmatic serialisation inside the LCN iteration. A
+    // later band of the same pass (late_wait) depends on nothing the band
+    // before it writes: it starts as soon as that band's CTAs have all passed
+    // their own wait (so everything earlier is complete), fills the SMs the
+    // earlier band's tail leaves idle, and waits for it only before exiting,
+    // which keeps "this grid complete" => "every earlier grid complete".
+    if (!late_wait) pdl_wait();
     pdl_launch_dependents();
     if (st->done) return;
     extern __shared__ __align__(128) unsigned char dyn[];
@@ -1085,6 +1092,7 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
         wk.ctr[0] = 0u;
         wk.ctr[1] = 0u;
     }
+    if (late_wait && tid == 0) pdl_wait();
 }
 
 // ---------------------------------------------------------------------------
@@ -2461,13 +2469,20 @@ struct Solver {
     template <typename T, bool ROWS>
     void bands(std::vector<DevBuf<double>>& logvp, std::vector<DevBuf<double>>& corr) {
         if (op.kind != 3) return;
+        // bands after the first launched one overlap its tail (late_wait);
+        // every band has its own plan, claim counters, scratch and output
+        static const bool overlap = [] {
+            const char* e = std::getenv("LCN_BAND_OVERLAP");
+            return !(e && e[0] == '0');
+        }();
+        int launched = 0;
         for (size_t b = 0; b < op.bands.size(); ++b) {
             PassPlan& P = plans[ROWS ? 0 : 1][b];
             if (P.nitems)
                 launch_pdl(band_stream_kernel<T, ROWS, false>, dim3(band_grid), dim3(kThreads + 64), sizeof(BandSmem), s,
                            pdl(), st.get(), ROWS ? op.iter[b].so : op.iter[b].to, P.work(),
                            ROWS ? band_valsT<T>(b) : band_vals<T>(b), logvp[b].get(), corr[b].get(),
-                           static_cast<double*>(nullptr));
+                           static_cast<double*>(nullptr), (pdl() && overlap && launched++ > 0) ? 1 : 0);
         }
     }
     template <typename T>
