@@ -1619,11 +1619,28 @@ __global__ void __launch_bounds__(1024) lowrank_reduce_kernel(DevState* __restri
     for (int w = 0; w < W; ++w) { H = fmax(H, sh[w]); mn = fmin(mn, sm[w]); }
     const int a = blockIdx.x * 32 + lane;
     double s = 0.0;
+    // exp(h_b - H) once per partial (thread b) instead of once per lane and
+    // partial; -1 marks a partial to skip (h_b = -inf). Same products, same order.
+    __shared__ double eb[1024];
+    const bool cached = G <= 1024;
+    if (cached && static_cast<int>(threadIdx.x) < G) {
+        const double hb = hpart[threadIdx.x];
+        eb[threadIdx.x] = (H != kNegInf && hb != kNegInf) ? exp(hb - H) : -1.0;
+    }
+    __syncthreads();
     if (H != kNegInf && a < lp) {
+        if (cached) {
 #pragma unroll 4
-        for (int b = warp; b < G; b += W) {
-            const double hb = hpart[b];
-            if (hb != kNegInf) s += part[static_cast<long long>(b) * lp + a] * exp(hb - H);
+            for (int b = warp; b < G; b += W) {
+                const double e = eb[b];
+                if (e >= 0.0) s += part[static_cast<long long>(b) * lp + a] * e;
+            }
+        } else {
+#pragma unroll 4
+            for (int b = warp; b < G; b += W) {
+                const double hb = hpart[b];
+                if (hb != kNegInf) s += part[static_cast<long long>(b) * lp + a] * exp(hb - H);
+            }
         }
     }
     acc_s[warp][lane] = s;
