@@ -2486,11 +2486,14 @@ struct Solver {
     template <typename T, bool ROWS>
     void bands(std::vector<DevBuf<double>>& logvp, std::vector<DevBuf<double>>& corr) {
         if (op.kind != 3) return;
-        // bands after the first launched one overlap its tail (late_wait);
-        // every band has its own plan, claim counters, scratch and output
+        // LCN_BAND_OVERLAP=1 (experimental, off by default): bands after the
+        // first launched one overlap its tail (late_wait); every band has its
+        // own plan, claim counters, scratch and output. Measured -2 % per
+        // iteration and bit-identical, but 2 of ~30 bench runs stalled inside
+        // a solve with it on (none of ~30 with it off), so it stays opt-in.
         static const bool overlap = [] {
             const char* e = std::getenv("LCN_BAND_OVERLAP");
-            return !(e && e[0] == '0');
+            return e && e[0] == '1';
         }();
         int launched = 0;
         for (size_t b = 0; b < op.bands.size(); ++b) {
