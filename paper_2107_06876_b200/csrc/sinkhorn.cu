@@ -811,8 +811,11 @@ __global__ void __launch_bounds__(kThreads + 64, 2) band_stream_kernel(const Dev
     // their own wait (so everything earlier is complete), fills the SMs the
     // earlier band's tail leaves idle, and waits for it only before exiting,
     // which keeps "this grid complete" => "every earlier grid complete".
+    // late_wait 2: no explicit trigger either; the dependent is launched when
+    // this grid's CTAs exit, i.e. after their late wait (wait-then-trigger
+    // order like every other kernel here).
     if (!late_wait) pdl_wait();
-    pdl_launch_dependents();
+    if (late_wait != 2) pdl_launch_dependents();
     if (st->done) return;
     extern __shared__ __align__(128) unsigned char dyn[];
     BandSmem& sm = *reinterpret_cast<BandSmem*>(dyn);
@@ -2491,9 +2494,11 @@ struct Solver {
         // own plan, claim counters, scratch and output. Measured -2 % per
         // iteration and bit-identical, but 2 of ~30 bench runs stalled inside
         // a solve with it on (none of ~30 with it off), so it stays opt-in.
-        static const bool overlap = [] {
+        // LCN_BAND_OVERLAP=2: the same, but the overlapping band triggers its
+        // dependent only by exiting (after its late wait).
+        static const int overlap = [] {
             const char* e = std::getenv("LCN_BAND_OVERLAP");
-            return e && e[0] == '1';
+            return e && (e[0] == '1' || e[0] == '2') ? e[0] - '0' : 0;
         }();
         int launched = 0;
         for (size_t b = 0; b < op.bands.size(); ++b) {
@@ -2502,7 +2507,7 @@ struct Solver {
                 launch_pdl(band_stream_kernel<T, ROWS, false>, dim3(band_grid), dim3(kThreads + 64), sizeof(BandSmem), s,
                            pdl(), st.get(), ROWS ? op.iter[b].so : op.iter[b].to, P.work(),
                            ROWS ? band_valsT<T>(b) : band_vals<T>(b), logvp[b].get(), corr[b].get(),
-                           static_cast<double*>(nullptr), (pdl() && overlap && launched++ > 0) ? 1 : 0);
+                           static_cast<double*>(nullptr), (pdl() && overlap && launched++ > 0) ? overlap : 0);
         }
     }
     template <typename T>
