@@ -2493,9 +2493,10 @@ struct Solver {
         // first launched one overlap its tail (late_wait); every band has its
         // own plan, claim counters, scratch and output. Measured -2 % per
         // iteration and bit-identical, but 2 of ~30 bench runs stalled inside
-        // a solve with it on (none of ~30 with it off), so it stays opt-in.
+        // a solve with it on (none of ~45 with it off), so it stays opt-in.
         // LCN_BAND_OVERLAP=2: the same, but the overlapping band triggers its
-        // dependent only by exiting (after its late wait).
+        // dependent only by exiting (after its late wait); 1 of 64 runs
+        // stalled with it too (profiles/band_overlap_stall_r05.txt).
         static const int overlap = [] {
             const char* e = std::getenv("LCN_BAND_OVERLAP");
             return e && (e[0] == '1' || e[0] == '2') ? e[0] - '0' : 0;
